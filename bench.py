@@ -1,0 +1,413 @@
+#!/usr/bin/env python
+"""Benchmark: vertex-target divergence evaluations/s (KL + TV), B200.
+
+Workload (BASELINE.json configs[1]): dense FP64 Poisson kernel
+of the 50:1 corridor shape, 102,104 vertices x 4,250 boundary vertices PER GPU
+(weak scaling: each rank owns one row slab of that size; the global mesh is
+N x 102,104 rows), KL and TV distance fields to a single target.  One step =
+[broadcast of the target row from its owner rank (NCCL, N>1 only)] + KL field
++ TV field over the rank's slab: 2 x rows evaluations per rank.
+
+Synthetic data (softmax rows of N(0,1) with one exact-zero column, FP64): the
+reference's real P for this shape takes ~2 min of SuperLU to build and is not
+needed for a bandwidth measurement; parity is tested on real P in tests/.
+P (3.47 GB/GPU) is far larger than L2 (126 MB), so no L2 flush is needed.
+
+JSON keys beyond the driver contract:
+  roofline      dominant kernel (dense KL) achieved GB/s from CUDA events on
+                its launch stream, algorithmic bytes rows*(8k+16)+8k per launch
+  cpu_baseline  the oracle numpy port (reference algorithm) on the host cores
+  e2e           the same metric through the public API dv_field() with the
+                field copied back to host memory every call
+
+`--impl reference` times the reference's CPU algorithm (the oracle port,
+oracle/divergence.py — the reference is pure Python and cannot travel to the
+GPU box) on a bounded sample of the same workload, on all host threads.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+WORKLOADS = {
+    # name: (rows per GPU, k, description)
+    "c2": (102_104, 4_250, "C2 corridor 50:1 dense KL+TV, single target"),
+    "c2p": (106_030, 1_234, "C2' rectangle 1.5:1 dense KL+TV, single target"),
+    "c4": (1_000_386, 4_102, "C4 holes x20 dense KL+TV, single target"),
+}
+METRIC = "vertex-target divergence evals/sec (KL, TV) at 1/2/4/8 B200; % HBM roofline"
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                    timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        loaded = [float(s[0]) for s in self.samples
+                  if s[0].replace(".", "").isdigit() and s[6].isdigit() and int(s[6]) > 0]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(loaded or sm) if sm else None,
+                "sm_max_mhz": float(self.samples[0][1]) if self.samples[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------------
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_sample_rows(k: int, rows: int, seed: int):
+    import numpy as np
+    from oracle.inputs import synthetic_kernel
+    P = synthetic_kernel(rows, k, seed)
+    P[:, 0] = 0.0
+    return P
+
+
+class CpuReference:
+    """Oracle port (reference algorithm: dv_at over row chunks == dv_field,
+    SURVEY A.1) on a bounded sample of rows of the workload shape, on all host
+    threads.  The sample is sized once so one KL+TV pass takes ~budget_s."""
+
+    def __init__(self, k: int, budget_s: float, threads: int):
+        from oracle import divergence as O
+        self.O, self.k, self.threads = O, k, threads
+        calib = cpu_sample_rows(k, 1024, seed=7)
+        t0 = time.perf_counter()
+        self._pass(calib)
+        dt = max(time.perf_counter() - t0, 1e-3)
+        self.rows = int(min(200_000, max(1024, 1024 * budget_s / dt)))
+        self.P = cpu_sample_rows(k, self.rows, seed=11)
+        self.sample = (f"KL+TV fields over {self.rows} sampled rows x k={k} "
+                       f"(target row 0), {threads} threads")
+
+    def _pass(self, P):
+        self.O.dv_field_chunked(P, "kl", 0, chunk_rows=256, threads=self.threads)
+        self.O.dv_field_chunked(P, "tv", 0, chunk_rows=256, threads=self.threads)
+
+    def step(self):
+        t0 = time.perf_counter()
+        self._pass(self.P)
+        el = time.perf_counter() - t0
+        return 2 * self.rows / el, el
+
+
+def run_reference_arm(args):
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return 0
+    n_rows, k, desc = WORKLOADS[args.workload]
+    threads = os.cpu_count() or 1
+    per_step = float(os.environ.get("PF_REF_STEP_S", "2.0"))
+    ref = CpuReference(k, per_step, threads)
+    for _ in range(args.warmup):
+        ref.step()
+    vals, els = [], []
+    for _ in range(args.steps):
+        v, el = ref.step()
+        vals.append(v)
+        els.append(el)
+    sample = ref.sample
+    value = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "evals/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * statistics.median(els), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": desc, "rows_per_gpu": n_rows, "k": k},
+        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads, "kind": "port",
+                         "sample": sample + "; oracle/divergence.py restating divergence.py:137-187"},
+        "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------
+def make_synthetic_slab(t, rows, k, ld, seed, device, chunk=8192):
+    """Softmax rows of N(0,1) with column 0 exactly zero, on the GPU (FP64)."""
+    P = t.empty((rows, ld), dtype=t.float64, device=device)
+    g = t.Generator(device=device)
+    g.manual_seed(1234 + seed)
+    for a in range(0, rows, chunk):
+        b = min(rows, a + chunk)
+        x = t.randn((b - a, k), dtype=t.float64, device=device, generator=g)
+        x[:, 0] = -float("inf")
+        P[a:b, :k] = t.softmax(x, dim=1)
+    P[:, k:] = 0.0
+    return P
+
+
+def run_native(args):
+    import numpy as np
+    import torch as t
+
+    import paper_1708_02845_b200 as pf
+    from paper_1708_02845_b200 import _device as dev
+    from paper_1708_02845_b200 import _native as nat
+
+    ws, rank, local = dist_env()
+    if args.gpus != ws and ws > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ws}")
+    t.cuda.set_device(local)
+    device = t.device("cuda", local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=device)
+
+    rows, k, desc = WORKLOADS[args.workload]
+    n_total = rows * ws
+    row0 = rank * rows
+    ld = dev.leading_dim(k)
+    P_dev = make_synthetic_slab(t, rows, k, ld, rank, device)
+    dk = dev.DeviceKernel(None, np.array([], np.int64), device=device, row0=row0, rows=rows,
+                          n=n_total, k=k, P_dev=P_dev)
+    target = n_total // 3 + 1
+    owner = target // rows
+    clamp_kl, clamp_tv = 1e-300, 1e-150
+    H = dk.negentropy(clamp_kl)
+    stream = t.cuda.current_stream(device)
+    s = stream.cuda_stream
+
+    k_pad = dev.round_up(k, 2)
+    m_pad = dev.round_up(k, 16)
+    stage = t.empty(16 * k_pad + m_pad, dtype=t.uint8, device=device)
+    tgt, logt, tmask = stage.data_ptr(), stage.data_ptr() + 8 * k_pad, stage.data_ptr() + 16 * k_pad
+    trow = t.empty(k, dtype=t.float64, device=device)
+    out_kl = t.empty(rows + 2, dtype=t.float64, device=device)
+    out_tv = t.empty(rows + 2, dtype=t.float64, device=device)
+    fk, ft = out_kl.data_ptr() + rows * 8, out_tv.data_ptr() + rows * 8
+    interior = dk.is_interior.data_ptr()
+    tau = pf.divergence.KL_GUARD_TAU
+
+    ev = [(t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)) for _ in range(2)]
+    kern_ms = {"kl": 0.0, "tv": 0.0}
+
+    def step(timed_kernels=False):
+        if ws > 1:
+            if rank == owner:
+                trow.copy_(dk.P[target - row0, :k])
+            dist.broadcast(trow, src=owner)
+            rowp = trow.data_ptr()
+        else:
+            rowp = dk.P[target - row0].data_ptr()
+        nat.call("pf_target_prep_f64", rowp, k, clamp_kl, tgt, logt, tmask, fk, s)
+        if timed_kernels:
+            ev[0][0].record(stream)
+        nat.call("pf_dense_kl_f64", dk.P.data_ptr(), dk.ld, rows, k, H.data_ptr(), tgt, logt,
+                 tmask, clamp_kl, tau, row0, target, interior, out_kl.data_ptr(), fk, s)
+        if timed_kernels:
+            ev[0][1].record(stream)
+        nat.call("pf_target_prep_f64", rowp, k, clamp_tv, tgt, 0, tmask, ft, s)
+        if timed_kernels:
+            ev[1][0].record(stream)
+        nat.call("pf_dense_tv_f64", dk.P.data_ptr(), dk.ld, rows, k, tgt, tmask, clamp_tv, row0,
+                 target, interior, out_tv.data_ptr(), ft, s)
+        if timed_kernels:
+            ev[1][1].record(stream)
+
+    def barrier():
+        t.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        t.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        v = t.tensor([x], dtype=t.float64, device=device)
+        dist.all_reduce(v, op=dist.ReduceOp.MAX)
+        return float(v.item())
+
+    for _ in range(args.warmup):
+        step()
+    # kernel-level timing pass (events around each kernel on its stream)
+    barrier()
+    for _ in range(args.steps):
+        step(timed_kernels=True)
+        stream.synchronize()
+        kern_ms["kl"] += ev[0][0].elapsed_time(ev[0][1])
+        kern_ms["tv"] += ev[1][0].elapsed_time(ev[1][1])
+    kl_ms = kern_ms["kl"] / args.steps
+    tv_ms = kern_ms["tv"] / args.steps
+
+    # whole-step timing (the reported value)
+    e0, e1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        barrier()
+    el_ms = max_over_ranks(e0.elapsed_time(e1))
+    evals = 2 * rows * ws * args.steps
+    value = evals / (el_ms / 1e3)
+    flags_kl = out_kl[rows:].view(t.int32).cpu().numpy()
+
+    # ------------------------------------------------ e2e via the public API
+    e2e = None
+    if ws == 1:
+        host = np.empty((rows, k))
+        for a in range(0, rows, 16384):
+            b = min(rows, a + 16384)
+            host[a:b] = P_dev[a:b, :k].cpu().numpy()
+        pk = pf.PoissonKernel(host, np.array([], np.int64), 0.0, 0.0)
+        dev.register(host, dk)
+        kl, tv = pf.builtin_f("kl"), pf.builtin_f("tv")
+        for _ in range(args.warmup):
+            pf.dv_field(pk, kl, target)
+            pf.dv_field(pk, tv, target)
+        barrier()
+        t0 = time.perf_counter()
+        ee0, ee1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
+        ee0.record(stream)
+        for _ in range(args.steps):
+            fkl = pf.dv_field(pk, kl, target)
+            ftv = pf.dv_field(pk, tv, target)
+        ee1.record(stream)
+        barrier()
+        wall = time.perf_counter() - t0
+        dev_ms = ee0.elapsed_time(ee1)
+        e2e_s = max(wall, dev_ms / 1e3)
+        # parity spot check of the API result against the device-only path
+        assert np.array_equal(fkl.values, out_kl[:rows].cpu().numpy())
+        assert np.array_equal(ftv.values, out_tv[:rows].cpu().numpy())
+        e2e = {"value": 2 * rows * args.steps / e2e_s, "unit": "evals/s",
+               "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 2 * (rows + 2) * 8,
+               "ms_per_step": 1e3 * e2e_s / args.steps,
+               "note": "dv_field(pk, kl|tv, t) per step: P resident in HBM (per-PoissonKernel "
+                       "device cache, as DomainContext keeps P resident); target index passed "
+                       "as a kernel argument; the n-vector field plus flags copied D2H to "
+                       "pinned host memory and returned as ScalarField"}
+        del host
+
+    # ------------------------------------------------ CPU baseline (rank 0, N=1)
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        ref = CpuReference(k, args.cpu_budget, threads)
+        v, el = ref.step()
+        cpu = {"value": v, "unit": "evals/s", "cores": threads, "kind": "port",
+               "sample": ref.sample + f" ({el:.1f} s); oracle/divergence.py restating "
+                                      "pathfield divergence.py:137-187 (numpy)"}
+
+    peak, peak_kind = peaks()
+    bytes_kl = rows * (8 * k + 16) + 8 * k
+    bytes_tv = rows * (8 * k + 8) + 8 * k
+    ach_kl = bytes_kl / (kl_ms / 1e3) / 1e9
+    ach_tv = bytes_tv / (tv_ms / 1e3) / 1e9
+    traffic = None
+    prof = ROOT / "profiles" / "ncu_summary.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get(args.workload, {}).get("dense_kl_dram_bytes")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": el_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": desc, "rows_per_gpu": rows, "k": k, "n_total": n_total,
+                   "parallelism": f"row-shard x{ws}", "target": target,
+                   "l2": "inputs larger than L2 (P slab %.2f GB/GPU vs 126 MB L2)" % (rows * ld * 8 / 1e9)},
+        "roofline": {"bound": "hbm", "achieved": ach_kl, "peak": peak, "unit": "GB/s",
+                     "frac": ach_kl / peak, "traffic": traffic, "kernel": "pf::dense_kl_kernel",
+                     "algorithmic_bytes_per_launch": bytes_kl, "avg_launch_ms": kl_ms,
+                     "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else "fallback 6.65 TB/s"},
+        "roofline_tv": {"achieved": ach_tv, "frac": ach_tv / peak, "avg_launch_ms": tv_ms,
+                        "algorithmic_bytes_per_launch": bytes_tv},
+        "kl_guarded_rows": int(flags_kl[1]),
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": 4 * args.steps,
+        "clocks": clocks.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_native(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

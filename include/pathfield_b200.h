@@ -1,0 +1,146 @@
+/*
+ * pathfield_b200.h — C ABI of the B200-native divergence-distance hot path.
+ *
+ * Drop-in boundary for the reference package `pathfield` (pure Python,
+ * /root/reference/pkg/src/pathfield).  The reference has no native code, so
+ * each entry point below replaces one numpy/scipy computation inside a
+ * reference function; the citation on each declaration names it.  The
+ * Python mirror (paper_1708_02845_b200/) keeps the reference signatures and
+ * calls these through ctypes; a maintainer of the reference would bind them
+ * the same way.
+ *
+ * Conventions
+ *   - Every pointer is a DEVICE pointer (buffers owned by the caller, e.g.
+ *     torch tensors) unless the parameter name ends in `_host`.
+ *   - Every call takes the CUDA stream to launch on (`pf_stream_t`, a
+ *     cudaStream_t passed as void*) and is asynchronous on that stream.
+ *   - Every call returns 0 on success, otherwise a PF_E_* code or a
+ *     cudaError_t value (> 0); pf_last_error() returns the message of the
+ *     most recent failure on the calling thread.  Nothing throws.
+ *   - No hidden allocation: scratch is passed in by the caller.
+ *   - Matrices are row-major with an explicit leading dimension `ld`
+ *     (elements).  Dense P rows must be 16-byte aligned: `ld` even and the
+ *     base pointer 16-byte aligned.
+ *   - Row slabs: a call may cover rows [row0, row0+rows) of the global
+ *     matrix (multi-GPU row sharding); `P`, `H`, `is_interior` and `out`
+ *     point at the slab, while `target` is a GLOBAL row index.
+ */
+#ifndef PATHFIELD_B200_H
+#define PATHFIELD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void *pf_stream_t;
+
+enum {
+  PF_OK = 0,
+  PF_E_ARG = -1,     /* invalid argument (null pointer, bad size)           */
+  PF_E_ALIGN = -2,   /* misaligned pointer or odd leading dimension         */
+  PF_E_DOMAIN = -3,  /* value outside the supported domain                  */
+  PF_E_LAUNCH = -4,  /* kernel launch failed (message in pf_last_error)     */
+  PF_E_CAPACITY = -5 /* output buffer too small (count returned separately) */
+};
+
+/* Divergence generators (divergence.py:70-104).  The dense kernels are
+ * templated over these; kl and tv are the north-star pair. */
+enum {
+  PF_DIV_KL = 0,        /* f(x) = -log x,          clamp 1e-300 (:82-83)   */
+  PF_DIV_TV = 1,        /* f(x) = |1-x|,           clamp 1e-150 (:79-81)   */
+  PF_DIV_CHI2 = 2,      /* f(x) = x^2 - 1,         clamp 1e-150 (:84-86)   */
+  PF_DIV_HELLINGER = 3, /* f(x) = (sqrt x - 1)^2,  clamp 1e-150 (:87-89)   */
+  PF_DIV_ALPHA = 4,     /* 4/(1-a^2)(1-x^((1+a)/2)), clamp 1e-300 (:90-97) */
+  PF_DIV_POWER = 5      /* |1-x|^p,                clamp 1e-150 (:98-103)  */
+};
+
+/* Flag words written by the field kernels (uint32 array `flags`, >= 4). */
+enum {
+  PF_FLAG_CLAMPED = 0,   /* != 0: clamping fired one-sidedly on an interior
+                            row — divergence.py:172-175 ("clamped")        */
+  PF_FLAG_GUARDED = 1,   /* number of rows recomputed in per-element form  */
+  PF_FLAG_NONPOS = 2,    /* reserved                                       */
+  PF_FLAG_SPARE = 3
+};
+
+int pf_version(void);
+const char *pf_last_error(void);
+/* Number of SMs of the current device (grid sizing helper). */
+int pf_sm_count(void);
+
+/* ---- K0: per-target staging ------------------------------------------
+ * From the raw target row Pt (k doubles, device) write
+ *   tgt[b]      = max(Pt[b], clamp)            (b < k; pad to k_pad = 1.0)
+ *   logt[b]     = log(max(Pt[b], clamp))       (b < k; pad 0.0)
+ *   tmask[b]    = Pt[b] < clamp                (b < k; pad 0)
+ * and zero flags[0..3].  Replaces the `ps_t = np.maximum(dense[p], clamp)`
+ * line of dv_field (divergence.py:170) and the target half of the
+ * one-sided compare (:172).  `clamp <= 0` means "no clamp" (identity).
+ * Buffers tgt/logt must hold k_pad = round_up(k, 2) doubles and tmask
+ * round_up(k, 16) bytes. */
+int pf_target_prep_f64(const double *Pt, int64_t k, double clamp, double *tgt,
+                       double *logt, uint8_t *tmask, uint32_t *flags,
+                       pf_stream_t stream);
+
+/* ---- K1: per-row negentropy -------------------------------------------
+ * H[r] = sum_{b<k} c(P[r,b]) * log c(P[r,b]),  c(x) = max(x, clamp).
+ * Target-independent; computed once per (P, clamp).  It is the Q log Q half
+ * of the reference KL sum (divergence.py:180 with f = -log, :82-83).
+ * Also writes min_out[0] = min over the slab of P (for the clamp <= 0
+ * domain check, divergence.py:162-165) if min_out != NULL (caller seeds
+ * min_out[0] with +inf). */
+int pf_row_negentropy_f64(const double *P, int64_t ld, int64_t rows, int64_t k,
+                          double clamp, double *H, double *min_out,
+                          pf_stream_t stream);
+
+/* ---- K2: dense KL field -------------------------------------------------
+ * out[r] = sum_b c(Q_rb) * (-log(c(Pt_b)/c(Q_rb)))  for global row
+ * row0 + r, evaluated as H[r] - sum_b c(Q_rb) * logt[b] with a cancellation
+ * guard: rows with |out| < tau*(|H|+|cross|) are re-evaluated in the
+ * reference's per-element form.  Then the settle rule (-1e-10,0) -> 0 and
+ * out[target-row0] = 0.  Replaces dv_field's kl evaluation
+ * (divergence.py:170-182).  flags[PF_FLAG_CLAMPED] |= one-sided clamp on a
+ * row with is_interior[r] != 0 (is_interior may be NULL = all interior). */
+int pf_dense_kl_f64(const double *P, int64_t ld, int64_t rows, int64_t k,
+                    const double *H, const double *tgt, const double *logt,
+                    const uint8_t *tmask, double clamp, double tau,
+                    int64_t row0, int64_t target, const uint8_t *is_interior,
+                    double *out, uint32_t *flags, pf_stream_t stream);
+
+/* ---- K3: dense TV field ---------------------------------------------------
+ * out[r] = sum_b |c(Q_rb) - c(Pt_b)|  (== sum c(Q)|1 - c(Pt)/c(Q)|, the
+ * reference tv evaluation divergence.py:79-81,180, within rounding), then
+ * settle and out[target-row0] = 0; clamp flag as for K2. */
+int pf_dense_tv_f64(const double *P, int64_t ld, int64_t rows, int64_t k,
+                    const double *tgt, const uint8_t *tmask, double clamp,
+                    int64_t row0, int64_t target, const uint8_t *is_interior,
+                    double *out, uint32_t *flags, pf_stream_t stream);
+
+/* ---- K2/K3 generalised: any builtin generator (divergence.py:70-104) ----
+ * out[r] = sum_b c(Q) f(c(Pt)/c(Q)) per-element (no split form), settle,
+ * target zero, clamp flag.  `kind` is PF_DIV_*, `param` the alpha or the
+ * power exponent.  swap_order != 0 evaluates sum_b c(Pt) f(c(Q)/c(Pt))
+ * (divergence.py:177-178). */
+int pf_dense_generic_f64(const double *P, int64_t ld, int64_t rows, int64_t k,
+                         const double *tgt, const uint8_t *tmask, double clamp,
+                         int kind, double param, int swap_order, int64_t row0,
+                         int64_t target, const uint8_t *is_interior,
+                         double *out, uint32_t *flags, pf_stream_t stream);
+
+/* ---- dv_at: the same arithmetic on a gathered subset of query rows ------
+ * out[i] = KL/TV/... for query row queries[i] (global index into P, whose
+ * slab starts at row0), using the per-element reference form
+ * (divergence.py:137-151); out[i] = 0 where queries[i] == target. */
+int pf_dense_at_f64(const double *P, int64_t ld, int64_t rows, int64_t k,
+                    const double *tgt, double clamp, int kind, double param,
+                    int swap_order, int64_t row0, int64_t target,
+                    const int64_t *queries, int64_t nq, double *out,
+                    pf_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PATHFIELD_B200_H */

@@ -1,0 +1,174 @@
+"""Device-resident mirrors of the reference's immutable inputs.
+
+A reference ``PoissonKernel`` is a frozen dataclass holding a read-only
+numpy ``dense`` (``solvers.py:229-252``); ``sparsify`` returns a
+``dataclasses.replace`` copy that shares the same ``dense`` array
+(``divergence.py:237-240``).  The device copy is therefore keyed on the
+identity of ``dense`` and lives as long as that array does, so the
+reference's own caching (``DomainContext._pk``, ``domain.py:43-70``) decides
+the device lifetime too.
+
+HBM layout of P (one slab per GPU; the whole matrix on one GPU):
+  rows x ld FP64, row-major, ld = round_up(k, 16) so every row starts on a
+  128-byte boundary (full-sector 128-bit streaming loads); pad columns are
+  never read.  Alongside: is_interior (uint8 per row) and the per-clamp
+  negentropy H (FP64 per row, K1), built lazily.
+"""
+
+from __future__ import annotations
+
+import threading
+import weakref
+
+import numpy as np
+
+from . import _native as nat
+from .errors import NativeError
+
+_torch = None
+
+
+def torch():
+    """Import torch lazily (it is the buffer owner, not the compute path)."""
+    global _torch
+    if _torch is None:
+        import torch as t
+        _torch = t
+    return _torch
+
+
+def require_cuda():
+    t = torch()
+    if not t.cuda.is_available():
+        raise NativeError(-101, "no CUDA device visible: the B200 path has no CPU fallback")
+    nat.load()
+    return t
+
+
+def round_up(x: int, m: int) -> int:
+    return (x + m - 1) // m * m
+
+
+def leading_dim(k: int) -> int:
+    return round_up(k, 16)
+
+
+class DeviceKernel:
+    """Row slab [row0, row0+rows) of P resident in HBM, plus per-row state."""
+
+    def __init__(self, dense: np.ndarray | None, boundary, *, device=None, row0: int = 0,
+                 rows: int | None = None, n: int | None = None, k: int | None = None,
+                 P_dev=None, chunk_rows: int = 65536):
+        t = require_cuda()
+        self.device = (t.device(device) if device is not None
+                       else t.device("cuda", t.cuda.current_device()))
+        if dense is not None:
+            n = dense.shape[0] if n is None else n
+            k = dense.shape[1]
+        if n is None or k is None:
+            raise ValueError("need `dense`, or `n` and `k` with `P_dev`")
+        self.n, self.k, self.row0 = int(n), int(k), int(row0)
+        self.rows = int(rows if rows is not None else self.n - self.row0)
+        if P_dev is not None:
+            if (P_dev.dtype != t.float64 or P_dev.device != self.device or P_dev.dim() != 2
+                    or P_dev.shape[0] != self.rows or P_dev.shape[1] < self.k
+                    or P_dev.stride(1) != 1):
+                raise ValueError("P_dev must be a row-major (rows, >=k) float64 tensor "
+                                 "on the kernel device")
+            self.ld = int(P_dev.stride(0))
+            self.P = P_dev
+        else:
+            self.ld = leading_dim(self.k)
+            self.P = t.empty((self.rows, self.ld), dtype=t.float64, device=self.device)
+            for a in range(0, self.rows, chunk_rows):
+                b = min(self.rows, a + chunk_rows)
+                src = np.ascontiguousarray(dense[self.row0 + a:self.row0 + b], dtype=np.float64)
+                self.P[a:b, :self.k].copy_(t.from_numpy(src))
+        interior = np.ones(self.n, dtype=np.uint8)
+        if boundary is not None and len(boundary):
+            interior[np.asarray(boundary, dtype=np.int64)] = 0
+        self.is_interior = t.from_numpy(interior[self.row0:self.row0 + self.rows].copy()).to(self.device)
+        self._H = {}
+        self._min = None
+        self._lock = threading.Lock()
+        self._host = weakref.ref(dense) if dense is not None else None
+
+    # -- per-row state ---------------------------------------------------
+    def owns(self, row: int) -> bool:
+        return self.row0 <= row < self.row0 + self.rows
+
+    def negentropy(self, clamp: float):
+        """H[r] = sum_b c(P) log c(P) for this slab (K1), cached per clamp."""
+        key = float(clamp)
+        with self._lock:
+            h = self._H.get(key)
+            if h is None:
+                t = torch()
+                h = t.empty(self.rows, dtype=t.float64, device=self.device)
+                mn = t.full((1,), float("inf"), dtype=t.float64, device=self.device)
+                stream = t.cuda.current_stream(self.device).cuda_stream
+                nat.call("pf_row_negentropy_f64", self.P.data_ptr(), self.ld, self.rows,
+                         self.k, key, h.data_ptr(), mn.data_ptr(), stream)
+                self._H[key] = h
+                if self._min is None:
+                    self._min = mn
+            return h
+
+    def min_value(self) -> float:
+        """min over the slab of P (divergence.py:162-165 domain check)."""
+        if self._min is None:
+            self.negentropy(1e-300)
+        return float(self._min.item())
+
+    def target_row(self, p: int, host_dense: np.ndarray | None = None):
+        """Device view of the raw target row P[p, :k].
+
+        Owned rows are read in place; rows of another slab come from the host
+        copy (single-process) — the multi-GPU path broadcasts instead
+        (parallel.py).
+        """
+        t = torch()
+        if self.owns(p):
+            return self.P[p - self.row0, :self.k]
+        if host_dense is None:
+            host_dense = self._host() if self._host is not None else None
+        if host_dense is None:
+            raise NativeError(-102, f"target row {p} is not resident on this device")
+        return t.from_numpy(np.ascontiguousarray(host_dense[p], dtype=np.float64)).to(self.device)
+
+
+_cache: dict[int, tuple[weakref.ref, DeviceKernel]] = {}
+_cache_lock = threading.Lock()
+
+
+def device_kernel(pk) -> DeviceKernel:
+    """The device mirror of ``pk.dense`` (uploaded on first use)."""
+    dense = pk.dense
+    key = id(dense)
+    with _cache_lock:
+        hit = _cache.get(key)
+        if hit is not None and hit[0]() is dense:
+            return hit[1]
+    dk = DeviceKernel(dense, getattr(pk, "boundary", None))
+    register(dense, dk)
+    return dk
+
+
+def register(dense: np.ndarray, dk: DeviceKernel) -> DeviceKernel:
+    """Bind an existing device kernel (e.g. generated on the GPU) to a host array."""
+    key = id(dense)
+
+    def _drop(_ref, key=key):
+        with _cache_lock:
+            ent = _cache.get(key)
+            if ent is not None and ent[0]() is None:
+                del _cache[key]
+
+    with _cache_lock:
+        _cache[key] = (weakref.ref(dense, _drop), dk)
+    return dk
+
+
+def evict(pk) -> None:
+    with _cache_lock:
+        _cache.pop(id(pk.dense), None)

@@ -1,0 +1,98 @@
+"""ctypes binding of libpathfield_b200.so (the C ABI in include/pathfield_b200.h).
+
+There is no CPU fallback: if the library is missing, or no CUDA device is
+visible, every device entry point raises.  ``symbols()`` lists the exported
+names so the CPU test-suite can check that the library loads and exports
+every declaration of the header without launching anything.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import re
+import threading
+from pathlib import Path
+
+from .errors import NativeError
+
+PKG = Path(__file__).resolve().parent
+LIB_PATH = PKG / "libpathfield_b200.so"
+HEADER = PKG.parent / "include" / "pathfield_b200.h"
+
+_lock = threading.Lock()
+_lib = None
+
+c_i64 = ctypes.c_int64
+c_int = ctypes.c_int
+c_dbl = ctypes.c_double
+c_vp = ctypes.c_void_p
+
+# name -> argtypes (all return int unless listed in _RESTYPES)
+_SIGS = {
+    "pf_version": [],
+    "pf_last_error": [],
+    "pf_sm_count": [],
+    "pf_target_prep_f64": [c_vp, c_i64, c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp],
+    "pf_row_negentropy_f64": [c_vp, c_i64, c_i64, c_i64, c_dbl, c_vp, c_vp, c_vp],
+    "pf_dense_kl_f64": [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_dbl, c_dbl,
+                        c_i64, c_i64, c_vp, c_vp, c_vp, c_vp],
+    "pf_dense_tv_f64": [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_dbl, c_i64, c_i64, c_vp,
+                        c_vp, c_vp, c_vp],
+    "pf_dense_generic_f64": [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_dbl, c_int, c_dbl,
+                             c_int, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp],
+    "pf_dense_at_f64": [c_vp, c_i64, c_i64, c_i64, c_vp, c_dbl, c_int, c_dbl, c_int, c_i64,
+                        c_i64, c_vp, c_i64, c_vp, c_vp],
+}
+_RESTYPES = {"pf_last_error": ctypes.c_char_p}
+
+
+def register(name: str, argtypes, restype=ctypes.c_int) -> None:
+    """Declare an additional entry point (used by later kernel modules)."""
+    _SIGS[name] = list(argtypes)
+    if restype is not ctypes.c_int:
+        _RESTYPES[name] = restype
+
+
+def load():
+    """Load the shared library once; raises if it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not LIB_PATH.exists():
+            raise NativeError(-100, f"{LIB_PATH.name} is not built; run "
+                              "`python -c 'import __graft_entry__ as g; g.build()'`")
+        lib = ctypes.CDLL(str(LIB_PATH))
+        for name, args in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = _RESTYPES.get(name, ctypes.c_int)
+        _lib = lib
+        return lib
+
+
+def header_symbols() -> list[str]:
+    """Every function declared in include/pathfield_b200.h."""
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"^\s*(?:int|const char \*)\s*(pf_\w+)\s*\(", text, re.M)))
+
+
+def symbols() -> list[str]:
+    lib = load()
+    return [s for s in header_symbols() if hasattr(lib, s)]
+
+
+def call(name: str, *args) -> None:
+    """Invoke an entry point; raise NativeError with pf_last_error() on failure."""
+    lib = load()
+    rc = getattr(lib, name)(*args)
+    if rc != 0:
+        msg = lib.pf_last_error().decode(errors="replace")
+        raise NativeError(rc, f"{name}: {msg}")
+
+
+def ptr(t) -> int:
+    """Raw device pointer of a torch tensor (None -> NULL)."""
+    return 0 if t is None else t.data_ptr()

@@ -1,0 +1,526 @@
+// dense.cu — dense divergence fields over the Poisson kernel P (K0-K3).
+//
+// Reference semantics: pathfield/divergence.py
+//   dv_field  :154-187   (dense field from target p to every vertex)
+//   dv_at     :137-151   (same arithmetic on a subset of query rows)
+//   builtin_f :70-104    (generators and their clamps)
+//
+// Design (B200, HBM-bound): one warp owns one row of P at a time and streams
+// it with 128-bit non-allocating loads; the per-target row (its clamped
+// values / logs and the "below clamp" mask) is staged ONCE per CTA into
+// shared memory with a TMA bulk copy (cp.async.bulk + mbarrier); the grid is
+// persistent (SMs x resident CTAs) and warps stride over rows, so rows near
+// the target (which trip the KL cancellation guard) spread over all SMs.
+//
+// KL is evaluated in split form  H[q] - sum_b c(Q_qb) * log c(Pt_b)  where
+// H[q] = sum_b c(Q) log c(Q) is the target-independent per-row negentropy
+// (K1, once per P): one FMA per element instead of a log.  Rows where the
+// split form cancels (|out| < tau (|H| + |cross|)) are re-evaluated in the
+// reference's per-element form c(Q) * -log(c(Pt)/c(Q)) by the same warp.
+#include <cmath>
+
+#include "pf_common.cuh"
+
+namespace pf {
+
+constexpr int kThreads = 256;
+constexpr int kWarpsPerCta = kThreads / 32;
+
+// ------------------------------------------------------------ generators --
+// term(q, p) = q * f(p / q) with the reference's f (divergence.py:79-103).
+template <int KIND>
+__device__ __forceinline__ double gen_term(double w, double x, double param) {
+  // w: weight row value (clamped), x: ratio argument (already divided).
+  if (KIND == PF_DIV_KL) return __dmul_rn(w, -log(x));
+  if (KIND == PF_DIV_TV) return __dmul_rn(w, fabs(1.0 - x));
+  if (KIND == PF_DIV_CHI2) return __dmul_rn(w, __dsub_rn(__dmul_rn(x, x), 1.0));
+  if (KIND == PF_DIV_HELLINGER) {
+    double s = sqrt(x) - 1.0;
+    return __dmul_rn(w, __dmul_rn(s, s));
+  }
+  if (KIND == PF_DIV_ALPHA) {
+    // 4/(1-a^2) * (1 - x^((1+a)/2)), divergence.py:93-97
+    double a = param;
+    double scale = 4.0 / (1.0 - a * a);
+    double expo = (1.0 + a) / 2.0;
+    return __dmul_rn(w, __dmul_rn(scale, 1.0 - pow(x, expo)));
+  }
+  // PF_DIV_POWER: |1-x|^p, divergence.py:101-103
+  double d = fabs(1.0 - x);
+  double pw = (param == 2.0) ? d * d : pow(d, param);
+  return __dmul_rn(w, pw);
+}
+
+template <int KIND>
+__device__ __forceinline__ double pair_term(double q, double p, double param, bool swap) {
+  // default order: q * f(p / q) (divergence.py:148,180);
+  // swap_order:    p * f(q / p) (divergence.py:146,178).
+  return swap ? gen_term<KIND>(p, __ddiv_rn(q, p), param)
+              : gen_term<KIND>(q, __ddiv_rn(p, q), param);
+}
+
+// ------------------------------------------------------------ K0 prep --
+__global__ void target_prep_kernel(const double *__restrict__ Pt, int64_t k, int64_t k_pad,
+                                   int64_t m_pad, double clamp, double *__restrict__ tgt,
+                                   double *__restrict__ logt, uint8_t *__restrict__ tmask,
+                                   uint32_t *__restrict__ flags) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < 4 && flags) flags[i] = 0u;
+  for (; i < m_pad; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < k) {
+      double p = Pt[i];
+      double c = fmax(p, clamp);
+      if (tgt) tgt[i] = c;
+      if (logt) logt[i] = log(c);
+      if (tmask) tmask[i] = (p < clamp) ? 1 : 0;
+    } else {
+      if (i < k_pad) {
+        if (tgt) tgt[i] = 1.0;
+        if (logt) logt[i] = 0.0;
+      }
+      if (tmask) tmask[i] = 0;
+    }
+  }
+}
+
+// ------------------------------------------------------------ K1 negentropy --
+__global__ void __launch_bounds__(kThreads) row_negentropy_kernel(
+    const double *__restrict__ P, int64_t ld, int64_t rows, int64_t k, double clamp,
+    double *__restrict__ H, double *__restrict__ min_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t npair = k >> 1;
+  double mn = INFINITY;
+  for (int64_t r = warp; r < rows; r += nwarps) {
+    const double2 *row = reinterpret_cast<const double2 *>(P + r * ld);
+    double a0 = 0.0, a1 = 0.0;
+    for (int64_t j = lane; j < npair; j += 32) {
+      double2 v = ldg_stream2(row + j);
+      mn = fmin(mn, fmin(v.x, v.y));
+      double q0 = fmax(v.x, clamp), q1 = fmax(v.y, clamp);
+      a0 += __dmul_rn(q0, log(q0));
+      a1 += __dmul_rn(q1, log(q1));
+    }
+    if ((k & 1) && lane == 0) {
+      double x = P[r * ld + k - 1];
+      mn = fmin(mn, x);
+      double q = fmax(x, clamp);
+      a0 += __dmul_rn(q, log(q));
+    }
+    double h = warp_sum(a0 + a1);
+    if (lane == 0) H[r] = h;
+  }
+  if (min_out) {
+    mn = warp_min(mn);
+    if (lane == 0 && mn < INFINITY) {
+      // atomicMin on doubles via the ordered-integer trick (values may be
+      // negative: solver noise below -1e-12 is kept, solvers.py:296-298).
+      unsigned long long *addr = reinterpret_cast<unsigned long long *>(min_out);
+      unsigned long long old = *addr, assumed;
+      do {
+        assumed = old;
+        if (__longlong_as_double(assumed) <= mn) break;
+        old = atomicCAS(addr, assumed, __double_as_longlong(mn));
+      } while (old != assumed);
+    }
+  }
+}
+
+// ------------------------------------------------------------ staging --
+struct Staged {
+  const double *vec;  // logt (KL) or tgt (TV/generic), k_pad doubles
+  const uint8_t *mask;
+};
+
+// Stage `vec` (8*k_pad bytes) and `mask` (m_pad bytes) into shared memory
+// with one TMA bulk copy each; returns shared-memory views.
+__device__ __forceinline__ Staged stage_target(unsigned char *smem, const double *vec,
+                                               const uint8_t *mask, int64_t k_pad,
+                                               int64_t m_pad) {
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
+  double *s_vec = reinterpret_cast<double *>(smem + 16);
+  uint8_t *s_mask = reinterpret_cast<uint8_t *>(s_vec + k_pad);
+  if (threadIdx.x == 0) mbar_init(bar, 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t vb = static_cast<uint32_t>(k_pad * 8), mb = static_cast<uint32_t>(m_pad);
+    mbar_expect_tx(bar, vb + mb);
+    bulk_g2s(s_vec, vec, vb, bar);
+    bulk_g2s(s_mask, mask, mb, bar);
+  }
+  mbar_wait(bar, 0);
+  return Staged{s_vec, s_mask};
+}
+
+__host__ __device__ inline size_t staged_smem_bytes(int64_t k_pad, int64_t m_pad) {
+  return 16 + static_cast<size_t>(k_pad) * 8 + static_cast<size_t>(m_pad);
+}
+
+// ------------------------------------------------------------ K2 dense KL --
+template <int U>
+__global__ void __launch_bounds__(kThreads) dense_kl_kernel(
+    const double *__restrict__ P, int64_t ld, int64_t rows, int64_t k, int64_t k_pad,
+    int64_t m_pad, const double *__restrict__ H, const double *__restrict__ tgt,
+    const double *__restrict__ logt, const uint8_t *__restrict__ tmask, double clamp,
+    double tau, int64_t row0, int64_t target, const uint8_t *__restrict__ is_interior,
+    double *__restrict__ out, uint32_t *__restrict__ flags) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const Staged st = stage_target(smem, logt, tmask, k_pad, m_pad);
+  const double2 *lt2 = reinterpret_cast<const double2 *>(st.vec);
+  const uchar2 *m2 = reinterpret_cast<const uchar2 *>(st.mask);
+
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t npair = k >> 1;
+  bool clamped_any = false;
+  uint32_t guarded = 0;
+
+  for (int64_t r = warp; r < rows; r += nwarps) {
+    const double2 *row = reinterpret_cast<const double2 *>(P + r * ld);
+    double a0 = 0.0, a1 = 0.0;
+    bool fl = false;
+    for (int64_t j0 = 0; j0 < npair; j0 += 32 * U) {
+      double2 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t j = j0 + lane + 32 * u;
+        v[u] = (j < npair) ? ldg_stream2(row + j) : make_double2(1.0, 1.0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t j = j0 + lane + 32 * u;
+        if (j < npair) {
+          const double2 lt = lt2[j];
+          const uchar2 m = m2[j];
+          a0 = fma(fmax(v[u].x, clamp), lt.x, a0);
+          a1 = fma(fmax(v[u].y, clamp), lt.y, a1);
+          fl |= ((v[u].x < clamp) != (m.x != 0)) | ((v[u].y < clamp) != (m.y != 0));
+        }
+      }
+    }
+    if ((k & 1) && lane == 0) {
+      const double x = P[r * ld + k - 1];
+      a0 = fma(fmax(x, clamp), st.vec[k - 1], a0);
+      fl |= (x < clamp) != (st.mask[k - 1] != 0);
+    }
+    const double cross = warp_sum(a0 + a1);
+    const double h = H[r];
+    double val = h - cross;
+    if (fabs(val) < tau * (fabs(h) + fabs(cross))) {
+      // Cancellation guard: reference per-element form (divergence.py:180).
+      double b0 = 0.0;
+      const double *prow = P + r * ld;
+      for (int64_t b = lane; b < k; b += 32) {
+        const double q = fmax(prow[b], clamp);
+        b0 += __dmul_rn(q, -log(__ddiv_rn(tgt[b], q)));
+      }
+      val = warp_sum(b0);
+      ++guarded;
+    }
+    val = settle(val);
+    if (row0 + r == target) val = 0.0;  // divergence.py:182
+    const bool interior = is_interior ? (is_interior[r] != 0) : true;
+    clamped_any |= interior && __any_sync(0xffffffffu, fl);
+    if (lane == 0) out[r] = val;
+  }
+  if (lane == 0) {
+    if (clamped_any) atomicOr(&flags[PF_FLAG_CLAMPED], 1u);
+    if (guarded) atomicAdd(&flags[PF_FLAG_GUARDED], guarded);
+  }
+}
+
+// ------------------------------------------------------------ K3 dense TV --
+template <int U>
+__global__ void __launch_bounds__(kThreads) dense_tv_kernel(
+    const double *__restrict__ P, int64_t ld, int64_t rows, int64_t k, int64_t k_pad,
+    int64_t m_pad, const double *__restrict__ tgt, const uint8_t *__restrict__ tmask,
+    double clamp, int64_t row0, int64_t target, const uint8_t *__restrict__ is_interior,
+    double *__restrict__ out, uint32_t *__restrict__ flags) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const Staged st = stage_target(smem, tgt, tmask, k_pad, m_pad);
+  const double2 *t2 = reinterpret_cast<const double2 *>(st.vec);
+  const uchar2 *m2 = reinterpret_cast<const uchar2 *>(st.mask);
+
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t npair = k >> 1;
+  bool clamped_any = false;
+
+  for (int64_t r = warp; r < rows; r += nwarps) {
+    const double2 *row = reinterpret_cast<const double2 *>(P + r * ld);
+    double a0 = 0.0, a1 = 0.0;
+    bool fl = false;
+    for (int64_t j0 = 0; j0 < npair; j0 += 32 * U) {
+      double2 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t j = j0 + lane + 32 * u;
+        v[u] = (j < npair) ? ldg_stream2(row + j) : make_double2(1.0, 1.0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t j = j0 + lane + 32 * u;
+        if (j < npair) {
+          const double2 t = t2[j];
+          const uchar2 m = m2[j];
+          a0 += fabs(fmax(v[u].x, clamp) - t.x);
+          a1 += fabs(fmax(v[u].y, clamp) - t.y);
+          fl |= ((v[u].x < clamp) != (m.x != 0)) | ((v[u].y < clamp) != (m.y != 0));
+        }
+      }
+    }
+    if ((k & 1) && lane == 0) {
+      const double x = P[r * ld + k - 1];
+      a0 += fabs(fmax(x, clamp) - st.vec[k - 1]);
+      fl |= (x < clamp) != (st.mask[k - 1] != 0);
+    }
+    double val = settle(warp_sum(a0 + a1));
+    if (row0 + r == target) val = 0.0;
+    const bool interior = is_interior ? (is_interior[r] != 0) : true;
+    clamped_any |= interior && __any_sync(0xffffffffu, fl);
+    if (lane == 0) out[r] = val;
+  }
+  if (lane == 0 && clamped_any) atomicOr(&flags[PF_FLAG_CLAMPED], 1u);
+}
+
+// ------------------------------------------------------ generic generator --
+template <int KIND>
+__global__ void __launch_bounds__(kThreads) dense_generic_kernel(
+    const double *__restrict__ P, int64_t ld, int64_t rows, int64_t k, int64_t k_pad,
+    int64_t m_pad, const double *__restrict__ tgt, const uint8_t *__restrict__ tmask,
+    double clamp, double param, int swap, int64_t row0, int64_t target,
+    const uint8_t *__restrict__ is_interior, double *__restrict__ out,
+    uint32_t *__restrict__ flags) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const Staged st = stage_target(smem, tgt, tmask, k_pad, m_pad);
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t npair = k >> 1;
+  const double2 *t2 = reinterpret_cast<const double2 *>(st.vec);
+  const uchar2 *m2 = reinterpret_cast<const uchar2 *>(st.mask);
+  const bool sw = swap != 0;
+  bool clamped_any = false;
+  for (int64_t r = warp; r < rows; r += nwarps) {
+    const double2 *row = reinterpret_cast<const double2 *>(P + r * ld);
+    double a0 = 0.0, a1 = 0.0;
+    bool fl = false;
+    for (int64_t j = lane; j < npair; j += 32) {
+      const double2 v = ldg_stream2(row + j);
+      const double2 t = t2[j];
+      const uchar2 m = m2[j];
+      a0 += pair_term<KIND>(fmax(v.x, clamp), t.x, param, sw);
+      a1 += pair_term<KIND>(fmax(v.y, clamp), t.y, param, sw);
+      fl |= ((v.x < clamp) != (m.x != 0)) | ((v.y < clamp) != (m.y != 0));
+    }
+    if ((k & 1) && lane == 0) {
+      const double x = P[r * ld + k - 1];
+      a0 += pair_term<KIND>(fmax(x, clamp), st.vec[k - 1], param, sw);
+      fl |= (x < clamp) != (st.mask[k - 1] != 0);
+    }
+    double val = settle(warp_sum(a0 + a1));
+    if (row0 + r == target) val = 0.0;
+    const bool interior = is_interior ? (is_interior[r] != 0) : true;
+    clamped_any |= interior && __any_sync(0xffffffffu, fl);
+    if (lane == 0) out[r] = val;
+  }
+  if (lane == 0 && clamped_any) atomicOr(&flags[PF_FLAG_CLAMPED], 1u);
+}
+
+// -------------------------------------------------------------- dv_at --
+template <int KIND>
+__global__ void __launch_bounds__(kThreads) dense_at_kernel(
+    const double *__restrict__ P, int64_t ld, int64_t rows, int64_t k,
+    const double *__restrict__ tgt, double clamp, double param, int swap, int64_t row0,
+    int64_t target, const int64_t *__restrict__ queries, int64_t nq,
+    double *__restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const bool sw = swap != 0;
+  for (int64_t i = warp; i < nq; i += nwarps) {
+    const int64_t q = queries[i];
+    const int64_t r = q - row0;
+    double acc = 0.0;
+    if (r >= 0 && r < rows) {
+      const double *prow = P + r * ld;
+      for (int64_t b = lane; b < k; b += 32)
+        acc += pair_term<KIND>(fmax(prow[b], clamp), __ldg(tgt + b), param, sw);
+    }
+    double val = settle(warp_sum(acc));
+    if (q == target) val = 0.0;  // divergence.py:150
+    if (lane == 0) out[i] = val;
+  }
+}
+
+// ------------------------------------------------------------ launch glue --
+template <typename K>
+static int launch_cfg(K kernel, size_t smem, int64_t rows, int *grid) {
+  static thread_local const void *last_kernel = nullptr;
+  static thread_local size_t last_smem = 0;
+  if (smem > 48 * 1024 && (last_kernel != (const void *)kernel || last_smem < smem)) {
+    cudaError_t e = cudaFuncSetAttribute((const void *)kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return fail(static_cast<int>(e), "smem attribute: %s",
+                                      cudaGetErrorString(e));
+    last_kernel = (const void *)kernel;
+    last_smem = smem;
+  }
+  int occ = occupancy((const void *)kernel, kThreads, smem);
+  int64_t want = (rows + kWarpsPerCta - 1) / kWarpsPerCta;
+  int64_t g = static_cast<int64_t>(sm_count()) * occ;
+  if (g > want) g = want;
+  if (g < 1) g = 1;
+  *grid = static_cast<int>(g);
+  return 0;
+}
+
+static int check_dense_args(const double *P, int64_t ld, int64_t rows, int64_t k) {
+  if (!P && rows > 0) return fail(PF_E_ARG, "P is null");
+  if (rows < 0 || k <= 0 || ld < k) return fail(PF_E_ARG, "bad shape rows=%lld k=%lld ld=%lld",
+                                                (long long)rows, (long long)k, (long long)ld);
+  if ((ld & 1) || (reinterpret_cast<uintptr_t>(P) & 15))
+    return fail(PF_E_ALIGN, "P rows must be 16-byte aligned (ld even, base aligned)");
+  return 0;
+}
+
+static constexpr size_t kMaxStagedSmem = 200 * 1024;
+
+}  // namespace pf
+
+using namespace pf;
+
+extern "C" {
+
+int pf_target_prep_f64(const double *Pt, int64_t k, double clamp, double *tgt, double *logt,
+                       uint8_t *tmask, uint32_t *flags, pf_stream_t stream) {
+  if (!Pt || k <= 0) return fail(PF_E_ARG, "target_prep: bad args");
+  const int64_t k_pad = round_up(k, 2), m_pad = round_up(k, 16);
+  const int64_t n = m_pad > k_pad ? m_pad : k_pad;
+  int blocks = static_cast<int>((n + 255) / 256);
+  if (blocks > 1024) blocks = 1024;
+  target_prep_kernel<<<blocks, 256, 0, as_stream(stream)>>>(Pt, k, k_pad, m_pad, clamp, tgt,
+                                                             logt, tmask, flags);
+  return check_launch("target_prep");
+}
+
+int pf_row_negentropy_f64(const double *P, int64_t ld, int64_t rows, int64_t k, double clamp,
+                          double *H, double *min_out, pf_stream_t stream) {
+  if (int e = check_dense_args(P, ld, rows, k)) return e;
+  if (rows == 0) return 0;
+  int grid = 0;
+  if (int e = launch_cfg(row_negentropy_kernel, 0, rows, &grid)) return e;
+  row_negentropy_kernel<<<grid, kThreads, 0, as_stream(stream)>>>(P, ld, rows, k, clamp, H,
+                                                                   min_out);
+  return check_launch("row_negentropy");
+}
+
+int pf_dense_kl_f64(const double *P, int64_t ld, int64_t rows, int64_t k, const double *H,
+                    const double *tgt, const double *logt, const uint8_t *tmask, double clamp,
+                    double tau, int64_t row0, int64_t target, const uint8_t *is_interior,
+                    double *out, uint32_t *flags, pf_stream_t stream) {
+  if (int e = check_dense_args(P, ld, rows, k)) return e;
+  if (!H || !tgt || !logt || !tmask || !out || !flags) return fail(PF_E_ARG, "dense_kl: null");
+  if (rows == 0) return 0;
+  const int64_t k_pad = round_up(k, 2), m_pad = round_up(k, 16);
+  const size_t smem = staged_smem_bytes(k_pad, m_pad);
+  if (smem > kMaxStagedSmem) return fail(PF_E_DOMAIN, "dense_kl: k=%lld too large for staging",
+                                         (long long)k);
+  auto kern = dense_kl_kernel<4>;
+  int grid = 0;
+  if (int e = launch_cfg(kern, smem, rows, &grid)) return e;
+  kern<<<grid, kThreads, smem, as_stream(stream)>>>(P, ld, rows, k, k_pad, m_pad, H, tgt, logt,
+                                                    tmask, clamp, tau, row0, target,
+                                                    is_interior, out, flags);
+  return check_launch("dense_kl");
+}
+
+int pf_dense_tv_f64(const double *P, int64_t ld, int64_t rows, int64_t k, const double *tgt,
+                    const uint8_t *tmask, double clamp, int64_t row0, int64_t target,
+                    const uint8_t *is_interior, double *out, uint32_t *flags,
+                    pf_stream_t stream) {
+  if (int e = check_dense_args(P, ld, rows, k)) return e;
+  if (!tgt || !tmask || !out || !flags) return fail(PF_E_ARG, "dense_tv: null");
+  if (rows == 0) return 0;
+  const int64_t k_pad = round_up(k, 2), m_pad = round_up(k, 16);
+  const size_t smem = staged_smem_bytes(k_pad, m_pad);
+  if (smem > kMaxStagedSmem) return fail(PF_E_DOMAIN, "dense_tv: k=%lld too large for staging",
+                                         (long long)k);
+  auto kern = dense_tv_kernel<4>;
+  int grid = 0;
+  if (int e = launch_cfg(kern, smem, rows, &grid)) return e;
+  kern<<<grid, kThreads, smem, as_stream(stream)>>>(P, ld, rows, k, k_pad, m_pad, tgt, tmask,
+                                                    clamp, row0, target, is_interior, out,
+                                                    flags);
+  return check_launch("dense_tv");
+}
+
+int pf_dense_generic_f64(const double *P, int64_t ld, int64_t rows, int64_t k,
+                         const double *tgt, const uint8_t *tmask, double clamp, int kind,
+                         double param, int swap_order, int64_t row0, int64_t target,
+                         const uint8_t *is_interior, double *out, uint32_t *flags,
+                         pf_stream_t stream) {
+  if (int e = check_dense_args(P, ld, rows, k)) return e;
+  if (!tgt || !tmask || !out || !flags) return fail(PF_E_ARG, "dense_generic: null");
+  if (rows == 0) return 0;
+  const int64_t k_pad = round_up(k, 2), m_pad = round_up(k, 16);
+  const size_t smem = staged_smem_bytes(k_pad, m_pad);
+  if (smem > kMaxStagedSmem)
+    return fail(PF_E_DOMAIN, "dense_generic: k=%lld too large for staging", (long long)k);
+  int grid = 0;
+#define PF_GEN_CASE(KIND)                                                                   \
+  case KIND: {                                                                              \
+    auto kern = dense_generic_kernel<KIND>;                                                 \
+    if (int e = launch_cfg(kern, smem, rows, &grid)) return e;                              \
+    kern<<<grid, kThreads, smem, as_stream(stream)>>>(P, ld, rows, k, k_pad, m_pad, tgt,    \
+                                                      tmask, clamp, param, swap_order,      \
+                                                      row0, target, is_interior, out, flags); \
+    break;                                                                                  \
+  }
+  switch (kind) {
+    PF_GEN_CASE(PF_DIV_KL)
+    PF_GEN_CASE(PF_DIV_TV)
+    PF_GEN_CASE(PF_DIV_CHI2)
+    PF_GEN_CASE(PF_DIV_HELLINGER)
+    PF_GEN_CASE(PF_DIV_ALPHA)
+    PF_GEN_CASE(PF_DIV_POWER)
+    default:
+      return fail(PF_E_ARG, "dense_generic: unknown kind %d", kind);
+  }
+#undef PF_GEN_CASE
+  return check_launch("dense_generic");
+}
+
+int pf_dense_at_f64(const double *P, int64_t ld, int64_t rows, int64_t k, const double *tgt,
+                    double clamp, int kind, double param, int swap_order, int64_t row0,
+                    int64_t target, const int64_t *queries, int64_t nq, double *out,
+                    pf_stream_t stream) {
+  if (!P || ld < k || k <= 0 || rows < 0) return fail(PF_E_ARG, "dense_at: bad args");
+  if (!tgt || (!queries && nq > 0) || (!out && nq > 0)) return fail(PF_E_ARG, "dense_at: null");
+  if (nq <= 0) return 0;
+  int64_t blocks64 = (nq + kWarpsPerCta - 1) / kWarpsPerCta;
+  int blocks = static_cast<int>(blocks64 > 65535 ? 65535 : blocks64);
+#define PF_AT_CASE(KIND)                                                                   \
+  case KIND:                                                                               \
+    dense_at_kernel<KIND><<<blocks, kThreads, 0, as_stream(stream)>>>(                     \
+        P, ld, rows, k, tgt, clamp, param, swap_order, row0, target, queries, nq, out);    \
+    break;
+  switch (kind) {
+    PF_AT_CASE(PF_DIV_KL)
+    PF_AT_CASE(PF_DIV_TV)
+    PF_AT_CASE(PF_DIV_CHI2)
+    PF_AT_CASE(PF_DIV_HELLINGER)
+    PF_AT_CASE(PF_DIV_ALPHA)
+    PF_AT_CASE(PF_DIV_POWER)
+    default:
+      return fail(PF_E_ARG, "dense_at: unknown kind %d", kind);
+  }
+#undef PF_AT_CASE
+  return check_launch("dense_at");
+}
+
+}  // extern "C"

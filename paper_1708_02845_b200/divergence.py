@@ -1,0 +1,274 @@
+"""f-divergence distances over Poisson-kernel rows — B200 device path.
+
+Mirror of ``pathfield/divergence.py`` (same names, signatures, argument
+meaning, return types and exceptions); every evaluation runs in the sm_100a
+kernels of ``libpathfield_b200.so``:
+
+=====================  =============================================  ==========
+function               reference                                      kernels
+=====================  =============================================  ==========
+builtin_f/FDivergence  divergence.py:42-104                           (host)
+dv_pair                divergence.py:125-134                          K0 + at
+dv_at                  divergence.py:137-151                          K0 + at
+dv_field               divergence.py:154-187                          K0 + K2/K3
+=====================  =============================================  ==========
+
+The divergence between target p and query q is
+``DV(q, p) = sum_b max(Q,c) * f(max(P,c)/max(Q,c))`` with the generator's
+clamp c (``divergence.py:12-21``).  KL uses the split form (see
+``csrc/dense.cu``) with a cancellation guard that falls back, per row, to the
+reference's per-element form; every other generator and ``swap_order`` run
+the per-element form directly.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field as dc_field
+from typing import Callable
+
+import numpy as np
+
+from . import _device as dev
+from . import _native as nat
+from .errors import DivergenceDomainError, InvalidTargetError
+from .solvers import PoissonKernel, ScalarField
+
+_CLAMP_LOG = 1e-300      # divergence.py:37
+_CLAMP_POWER = 1e-150    # divergence.py:38
+_NEG_NOISE = 1e-10       # divergence.py:39
+
+#: Split-form KL guard: rows with |KL| < tau * (|H| + |cross|) are recomputed
+#: in per-element form.  The split form's error is ~eps*(|H|+|cross|), so
+#: unguarded rows carry at most ~eps/tau ~ 1e-13 relative error.
+KL_GUARD_TAU = 1e-3
+
+# PF_DIV_* codes of include/pathfield_b200.h
+_KIND = {"kl": 0, "tv": 1, "chi2": 2, "hellinger": 3, "alpha": 4, "power-p": 5}
+
+
+@dataclass(frozen=True)
+class FDivergence:
+    """A convex generator f on the positive reals with f(1) = 0 (divergence.py:42-56)."""
+
+    name: str
+    f: Callable[[np.ndarray], np.ndarray]
+    strictly_convex: bool
+    params: dict = dc_field(default_factory=dict)
+    clamp: float = _CLAMP_LOG
+
+    def __post_init__(self):
+        val = float(self.f(np.array([1.0]))[0])
+        if abs(val) > 1e-12:
+            raise ValueError(f"f(1) must be 0, got {val} for {self.name}")
+        _spot_check_convexity(self.f, self.name)
+
+
+def _spot_check_convexity(f, name, trials=100):
+    # divergence.py:59-67 (host-side validation of a user generator)
+    rng = np.random.default_rng(12345)
+    x = rng.uniform(1e-3, 10.0, size=(trials, 3))
+    x.sort(axis=1)
+    lo, mid, hi = x[:, 0], x[:, 1], x[:, 2]
+    lam = (hi - mid) / (hi - lo)
+    interp = lam * f(lo) + (1.0 - lam) * f(hi)
+    if np.any(f(mid) > interp + 1e-9):
+        raise ValueError(f"{name} failed the sampled convexity check")
+
+
+def builtin_f(name: str, *, alpha: float | None = None,
+              power: int | None = None) -> FDivergence:
+    """Built-in generators, identical to divergence.py:70-104."""
+    if name == "tv":
+        return FDivergence("tv", lambda x: np.abs(1.0 - x), False, clamp=_CLAMP_POWER)
+    if name == "kl":
+        return FDivergence("kl", lambda x: -np.log(x), True, clamp=_CLAMP_LOG)
+    if name == "chi2":
+        return FDivergence("chi2", lambda x: x * x - 1.0, True, clamp=_CLAMP_POWER)
+    if name == "hellinger":
+        return FDivergence("hellinger", lambda x: (np.sqrt(x) - 1.0) ** 2, True,
+                           clamp=_CLAMP_POWER)
+    if name == "alpha":
+        if alpha is None or alpha in (1.0, -1.0):
+            raise ValueError("alpha divergence needs alpha != +-1")
+        a = float(alpha)
+        scale = 4.0 / (1.0 - a * a)
+        expo = (1.0 + a) / 2.0
+        return FDivergence("alpha", lambda x: scale * (1.0 - x ** expo), True,
+                           {"alpha": a}, clamp=_CLAMP_LOG)
+    if name == "power-p":
+        if power is None or int(power) < 1 or power != int(power):
+            raise ValueError("power-p needs an integer exponent p >= 1")
+        p = int(power)
+        return FDivergence("power-p", lambda x: np.abs(1.0 - x) ** p, p > 1,
+                           {"power": p}, clamp=_CLAMP_POWER)
+    raise ValueError(f"unknown divergence {name!r}")
+
+
+def _kind_param(fd) -> tuple[int, float]:
+    """Map a generator to its device functor; user generators are refused."""
+    kind = _KIND.get(fd.name)
+    if kind is None:
+        raise NotImplementedError(
+            f"generator {fd.name!r} is a host callable; the device path evaluates the "
+            "built-in generators only (divergence.py:70-104)")
+    params = getattr(fd, "params", {}) or {}
+    if fd.name == "alpha":
+        return kind, float(params["alpha"])
+    if fd.name == "power-p":
+        return kind, float(params["power"])
+    return kind, 0.0
+
+
+def _effective_clamp(dk, clamp) -> float:
+    """Kernel clamp; clamp <= 0 requires P > 0 everywhere (divergence.py:162-165)."""
+    if clamp is None or clamp <= 0.0:
+        if dk.min_value() <= 0.0:
+            raise DivergenceDomainError("zero kernel entries and clamping is disabled")
+        return 0.0
+    return float(clamp)
+
+
+class _Staging:
+    """Per-call device scratch for K0: clamped target row, its logs, mask."""
+
+    def __init__(self, t, k: int, device):
+        k_pad, m_pad = dev.round_up(k, 2), dev.round_up(k, 16)
+        self.buf = t.empty(16 * k_pad + m_pad, dtype=t.uint8, device=device)
+        base = self.buf.data_ptr()
+        self.tgt = base
+        self.logt = base + 8 * k_pad
+        self.tmask = base + 16 * k_pad
+
+
+def _field_device(pk, dk, fd, p: int, swap_order: bool, clamp: float, out_dev, flags_ptr,
+                  stream, target_row=None):
+    """Launch K0 + the field kernel for slab `dk` into `out_dev` (device)."""
+    t = dev.torch()
+    st = _Staging(t, dk.k, dk.device)
+    row = target_row if target_row is not None else dk.target_row(p)
+    nat.call("pf_target_prep_f64", row.data_ptr(), dk.k, clamp, st.tgt, st.logt, st.tmask,
+             flags_ptr, stream)
+    kind, param = _kind_param(fd)
+    if kind == 0 and not swap_order:
+        H = dk.negentropy(clamp)
+        nat.call("pf_dense_kl_f64", dk.P.data_ptr(), dk.ld, dk.rows, dk.k, H.data_ptr(),
+                 st.tgt, st.logt, st.tmask, clamp, KL_GUARD_TAU, dk.row0, p,
+                 dk.is_interior.data_ptr(), out_dev.data_ptr(), flags_ptr, stream)
+    elif kind == 1 and not swap_order:
+        nat.call("pf_dense_tv_f64", dk.P.data_ptr(), dk.ld, dk.rows, dk.k, st.tgt, st.tmask,
+                 clamp, dk.row0, p, dk.is_interior.data_ptr(), out_dev.data_ptr(),
+                 flags_ptr, stream)
+    else:
+        nat.call("pf_dense_generic_f64", dk.P.data_ptr(), dk.ld, dk.rows, dk.k, st.tgt,
+                 st.tmask, clamp, kind, param, int(bool(swap_order)), dk.row0, p,
+                 dk.is_interior.data_ptr(), out_dev.data_ptr(), flags_ptr, stream)
+    return st  # keep scratch alive until the caller synchronises
+
+
+def dv_field_device(pk: PoissonKernel, fd: FDivergence, p: int, swap_order: bool = False,
+                    clamp: float | None = None):
+    """Device-resident field: returns (values tensor (n,) on the GPU, flags tensor).
+
+    Same arithmetic as :func:`dv_field`; nothing is copied back.  Used by the
+    tracer and by ``bench.py``'s kernel-only timing.
+    """
+    if not 0 <= p < pk.n:
+        raise InvalidTargetError(f"target {p} out of range")
+    t = dev.require_cuda()
+    dk = dev.device_kernel(pk)
+    if clamp is None:
+        clamp = fd.clamp
+    c = _effective_clamp(dk, clamp)
+    buf = t.empty(dk.rows + 2, dtype=t.float64, device=dk.device)
+    flags_ptr = buf.data_ptr() + dk.rows * 8
+    stream = t.cuda.current_stream(dk.device).cuda_stream
+    st = _field_device(pk, dk, fd, p, swap_order, c, buf, flags_ptr, stream)
+    del st
+    return buf[:dk.rows], buf[dk.rows:].view(t.int32)
+
+
+def _to_host(t, dbuf, stream_obj):
+    host = t.empty(dbuf.shape, dtype=dbuf.dtype, pin_memory=True)
+    host.copy_(dbuf, non_blocking=True)
+    stream_obj.synchronize()
+    return host.numpy()
+
+
+def dv_field(pk: PoissonKernel, fd: FDivergence, p: int,
+             swap_order: bool = False, clamp: float | None = None) -> ScalarField:
+    """Divergence distance from target p to every vertex (divergence.py:154-187)."""
+    if not 0 <= p < pk.n:
+        raise InvalidTargetError(f"target {p} out of range")
+    t = dev.require_cuda()
+    dk = dev.device_kernel(pk)
+    if clamp is None:
+        clamp = fd.clamp
+    c = _effective_clamp(dk, clamp)
+    buf = t.empty(dk.rows + 2, dtype=t.float64, device=dk.device)
+    flags_ptr = buf.data_ptr() + dk.rows * 8
+    s = t.cuda.current_stream(dk.device)
+    st = _field_device(pk, dk, fd, p, swap_order, c, buf, flags_ptr, s.cuda_stream)
+    host = _to_host(t, buf, s)
+    del st
+    vals = host[:dk.rows]
+    flag_words = host[dk.rows:].view(np.uint32)
+    fired = bool(flag_words[0]) and c > 0.0
+    params = dict(getattr(fd, "params", {}) or {})
+    if swap_order:
+        params["swap_order"] = True
+    return ScalarField(vals, fd.name, p, params, 1, None, ("clamped",) if fired else ())
+
+
+def dv_at(pk: PoissonKernel, fd: FDivergence, p: int, queries,
+          swap_order: bool = False, clamp: float | None = None) -> np.ndarray:
+    """Distances from target p to a batch of query vertices (divergence.py:137-151)."""
+    t = dev.require_cuda()
+    dk = dev.device_kernel(pk)
+    if clamp is None:
+        clamp = fd.clamp
+    q = np.asarray(queries, dtype=np.int64)
+    if q.size and (q.min() < 0 or q.max() >= pk.n):
+        raise IndexError("query index out of range")
+    if not 0 <= p < pk.n:
+        raise IndexError(f"target {p} out of range")
+    # divergence.py:140-148 applies np.maximum(., clamp) directly (no domain check).
+    c = float(clamp)
+    kind, param = _kind_param(fd)
+    s = t.cuda.current_stream(dk.device)
+    st = _Staging(t, dk.k, dk.device)
+    row = dk.target_row(p)
+    nat.call("pf_target_prep_f64", row.data_ptr(), dk.k, c, st.tgt, st.logt, st.tmask, 0,
+             s.cuda_stream)
+    qd = t.from_numpy(q).to(dk.device, non_blocking=False)
+    out = t.empty(q.size, dtype=t.float64, device=dk.device)
+    nat.call("pf_dense_at_f64", dk.P.data_ptr(), dk.ld, dk.rows, dk.k, st.tgt, c, kind, param,
+             int(bool(swap_order)), dk.row0, p, qd.data_ptr(), q.size, out.data_ptr(),
+             s.cuda_stream)
+    res = _to_host(t, out, s).copy()
+    del st
+    return res
+
+
+def _settle(value: float) -> float:
+    if -_NEG_NOISE < value < 0.0:
+        return 0.0
+    return value
+
+
+def dv_pair(pk: PoissonKernel, fd: FDivergence, p: int, q: int,
+            swap_order: bool = False, clamp: float | None = None) -> float:
+    """Divergence distance between target p and query q (divergence.py:125-134)."""
+    if clamp is None:
+        clamp = fd.clamp
+    if clamp is None or clamp <= 0.0:
+        # _clamped_rows (divergence.py:107-112): validate the two rows only.
+        if np.any(pk.dense[q] <= 0.0) or np.any(pk.dense[p] <= 0.0):
+            raise DivergenceDomainError("zero kernel entry and clamping is disabled")
+    val = float(dv_at(pk, fd, p, [q], swap_order=swap_order, clamp=clamp)[0])
+    return _settle(val)
+
+
+__all__ = [
+    "FDivergence", "builtin_f", "dv_pair", "dv_at", "dv_field", "dv_field_device",
+    "KL_GUARD_TAU",
+]
