@@ -373,7 +373,7 @@ def run_native(args):
                    "parallelism": f"row-shard x{ws}", "target": target,
                    "l2": "inputs larger than L2 (P slab %.2f GB/GPU vs 126 MB L2)" % (rows * ld * 8 / 1e9)},
         "roofline": {"bound": "hbm", "achieved": ach_kl, "peak": peak, "unit": "GB/s",
-                     "frac": ach_kl / peak, "traffic": traffic, "kernel": "pf::dense_kl_kernel",
+                     "frac": ach_kl / peak, "traffic": traffic, "kernel": "pf::dense_kl_kernel (+ kl_guard_fixup scan)",
                      "algorithmic_bytes_per_launch": bytes_kl, "avg_launch_ms": kl_ms,
                      "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else "fallback 6.65 TB/s"},
         "roofline_tv": {"achieved": ach_tv, "frac": ach_tv / peak, "avg_launch_ms": tv_ms,
@@ -381,7 +381,7 @@ def run_native(args):
         "kl_guarded_rows": int(flags_kl[1]),
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": 4 * args.steps,
+        "gpu_launches": 5 * args.steps,
         "clocks": clocks.summary(),
     }
     if rank == 0:

@@ -82,7 +82,7 @@ class DeviceKernel:
             self.P = t.empty((self.rows, self.ld), dtype=t.float64, device=self.device)
             for a in range(0, self.rows, chunk_rows):
                 b = min(self.rows, a + chunk_rows)
-                src = np.ascontiguousarray(dense[self.row0 + a:self.row0 + b], dtype=np.float64)
+                src = np.array(dense[self.row0 + a:self.row0 + b], dtype=np.float64, order="C")
                 self.P[a:b, :self.k].copy_(t.from_numpy(src))
         interior = np.ones(self.n, dtype=np.uint8)
         if boundary is not None and len(boundary):
@@ -134,7 +134,7 @@ class DeviceKernel:
             host_dense = self._host() if self._host is not None else None
         if host_dense is None:
             raise NativeError(-102, f"target row {p} is not resident on this device")
-        return t.from_numpy(np.ascontiguousarray(host_dense[p], dtype=np.float64)).to(self.device)
+        return t.from_numpy(np.array(host_dense[p], dtype=np.float64)).to(self.device)
 
 
 _cache: dict[int, tuple[weakref.ref, DeviceKernel]] = {}

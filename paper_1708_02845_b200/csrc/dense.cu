@@ -157,16 +157,22 @@ __host__ __device__ inline size_t staged_smem_bytes(int64_t k_pad, int64_t m_pad
   return 16 + static_cast<size_t>(k_pad) * 8 + static_cast<size_t>(m_pad);
 }
 
+// Rows whose split-form KL cancels are marked with this NaN payload and
+// re-evaluated per-element by kl_guard_fixup_kernel.
+constexpr unsigned long long kGuardSentinel = 0x7ff8dead0000beefull;
+
 // ------------------------------------------------------------ K2 dense KL --
-template <int U>
-__global__ void __launch_bounds__(kThreads) dense_kl_kernel(
+template <int U, int MINB, bool STAGE = true>
+__global__ void __launch_bounds__(kThreads, MINB) dense_kl_kernel(
     const double *__restrict__ P, int64_t ld, int64_t rows, int64_t k, int64_t k_pad,
     int64_t m_pad, const double *__restrict__ H, const double *__restrict__ tgt,
     const double *__restrict__ logt, const uint8_t *__restrict__ tmask, double clamp,
     double tau, int64_t row0, int64_t target, const uint8_t *__restrict__ is_interior,
     double *__restrict__ out, uint32_t *__restrict__ flags) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  const Staged st = stage_target(smem, logt, tmask, k_pad, m_pad);
+  extern __shared__ __align__(128) unsigned char smem[];
+  // STAGE: target vector + mask in shared memory (one copy per CTA, TMA);
+  // otherwise read through L1 (one copy per SM, shared by all its CTAs).
+  const Staged st = STAGE ? stage_target(smem, logt, tmask, k_pad, m_pad) : Staged{logt, tmask};
   const double2 *lt2 = reinterpret_cast<const double2 *>(st.vec);
   const uchar2 *m2 = reinterpret_cast<const uchar2 *>(st.mask);
 
@@ -175,10 +181,10 @@ __global__ void __launch_bounds__(kThreads) dense_kl_kernel(
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t npair = k >> 1;
   bool clamped_any = false;
-  uint32_t guarded = 0;
 
   for (int64_t r = warp; r < rows; r += nwarps) {
     const double2 *row = reinterpret_cast<const double2 *>(P + r * ld);
+    const double h = H[r];  // issued ahead of the row stream
     double a0 = 0.0, a1 = 0.0;
     bool fl = false;
     for (int64_t j0 = 0; j0 < npair; j0 += 32 * U) {
@@ -206,40 +212,28 @@ __global__ void __launch_bounds__(kThreads) dense_kl_kernel(
       fl |= (x < clamp) != (st.mask[k - 1] != 0);
     }
     const double cross = warp_sum(a0 + a1);
-    const double h = H[r];
     double val = h - cross;
-    if (fabs(val) < tau * (fabs(h) + fabs(cross))) {
-      // Cancellation guard: reference per-element form (divergence.py:180).
-      double b0 = 0.0;
-      const double *prow = P + r * ld;
-      for (int64_t b = lane; b < k; b += 32) {
-        const double q = fmax(prow[b], clamp);
-        b0 += __dmul_rn(q, -log(__ddiv_rn(tgt[b], q)));
-      }
-      val = warp_sum(b0);
-      ++guarded;
-    }
-    val = settle(val);
-    if (row0 + r == target) val = 0.0;  // divergence.py:182
+    const bool is_t = (row0 + r == target);
+    if (!is_t && fabs(val) < tau * (fabs(h) + fabs(cross)))
+      val = __longlong_as_double(static_cast<long long>(kGuardSentinel));  // -> fixup pass
+    else
+      val = is_t ? 0.0 : settle(val);  // divergence.py:181-182
     const bool interior = is_interior ? (is_interior[r] != 0) : true;
     clamped_any |= interior && __any_sync(0xffffffffu, fl);
     if (lane == 0) out[r] = val;
   }
-  if (lane == 0) {
-    if (clamped_any) atomicOr(&flags[PF_FLAG_CLAMPED], 1u);
-    if (guarded) atomicAdd(&flags[PF_FLAG_GUARDED], guarded);
-  }
+  if (lane == 0 && clamped_any) atomicOr(&flags[PF_FLAG_CLAMPED], 1u);
 }
 
 // ------------------------------------------------------------ K3 dense TV --
-template <int U>
-__global__ void __launch_bounds__(kThreads) dense_tv_kernel(
+template <int U, int MINB, bool STAGE = true>
+__global__ void __launch_bounds__(kThreads, MINB) dense_tv_kernel(
     const double *__restrict__ P, int64_t ld, int64_t rows, int64_t k, int64_t k_pad,
     int64_t m_pad, const double *__restrict__ tgt, const uint8_t *__restrict__ tmask,
     double clamp, int64_t row0, int64_t target, const uint8_t *__restrict__ is_interior,
     double *__restrict__ out, uint32_t *__restrict__ flags) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  const Staged st = stage_target(smem, tgt, tmask, k_pad, m_pad);
+  extern __shared__ __align__(128) unsigned char smem[];
+  const Staged st = STAGE ? stage_target(smem, tgt, tmask, k_pad, m_pad) : Staged{tgt, tmask};
   const double2 *t2 = reinterpret_cast<const double2 *>(st.vec);
   const uchar2 *m2 = reinterpret_cast<const uchar2 *>(st.mask);
 
@@ -286,16 +280,58 @@ __global__ void __launch_bounds__(kThreads) dense_tv_kernel(
   if (lane == 0 && clamped_any) atomicOr(&flags[PF_FLAG_CLAMPED], 1u);
 }
 
+// KL fixup: rows the KL kernel marked with the guard sentinel are
+// re-evaluated in the reference's per-element form q * -log(p/q)
+// (divergence.py:180) by one warp each; then settle.
+__global__ void __launch_bounds__(kThreads) kl_guard_fixup_kernel(
+    const double *__restrict__ P, int64_t ld, int64_t rows, int64_t k,
+    const double *__restrict__ tgt, double clamp, double *__restrict__ out,
+    uint32_t *__restrict__ flags) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  uint32_t done = 0;
+  for (int64_t base = warp * 32; base < rows; base += nwarps * 32) {
+    const int64_t mine = base + lane;
+    const bool flag = mine < rows && static_cast<unsigned long long>(__double_as_longlong(
+                                         out[mine])) == kGuardSentinel;
+    unsigned ball = __ballot_sync(0xffffffffu, flag);
+    while (ball) {
+      const int src = __ffs(ball) - 1;
+      ball &= ball - 1;
+      const int64_t r = base + src;
+      const double *prow = P + r * ld;
+      double b[4] = {0.0, 0.0, 0.0, 0.0};
+      int64_t e = lane;
+      for (; e + 96 < k; e += 128) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double q = fmax(prow[e + 32 * u], clamp);
+          b[u] += __dmul_rn(q, -log(__ddiv_rn(tgt[e + 32 * u], q)));
+        }
+      }
+      for (; e < k; e += 32) {
+        const double q = fmax(prow[e], clamp);
+        b[0] += __dmul_rn(q, -log(__ddiv_rn(tgt[e], q)));
+      }
+      const double val = settle(warp_sum((b[0] + b[1]) + (b[2] + b[3])));
+      if (lane == 0) out[r] = val;
+      ++done;
+    }
+  }
+  if (lane == 0 && done) atomicAdd(&flags[PF_FLAG_GUARDED], done);
+}
+
 // ------------------------------------------------------ generic generator --
-template <int KIND>
+template <int KIND, bool STAGE>
 __global__ void __launch_bounds__(kThreads) dense_generic_kernel(
     const double *__restrict__ P, int64_t ld, int64_t rows, int64_t k, int64_t k_pad,
     int64_t m_pad, const double *__restrict__ tgt, const uint8_t *__restrict__ tmask,
     double clamp, double param, int swap, int64_t row0, int64_t target,
     const uint8_t *__restrict__ is_interior, double *__restrict__ out,
     uint32_t *__restrict__ flags) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  const Staged st = stage_target(smem, tgt, tmask, k_pad, m_pad);
+  extern __shared__ __align__(128) unsigned char smem[];
+  const Staged st = STAGE ? stage_target(smem, tgt, tmask, k_pad, m_pad) : Staged{tgt, tmask};
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -357,26 +393,64 @@ __global__ void __launch_bounds__(kThreads) dense_at_kernel(
 }
 
 // ------------------------------------------------------------ launch glue --
+static constexpr size_t kMaxStagedSmem = 200 * 1024;
+
 template <typename K>
-static int launch_cfg(K kernel, size_t smem, int64_t rows, int *grid) {
-  static thread_local const void *last_kernel = nullptr;
-  static thread_local size_t last_smem = 0;
-  if (smem > 48 * 1024 && (last_kernel != (const void *)kernel || last_smem < smem)) {
+static int set_smem(K kernel, size_t smem) {
+  if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute((const void *)kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
-    if (e != cudaSuccess) return fail(static_cast<int>(e), "smem attribute: %s",
-                                      cudaGetErrorString(e));
-    last_kernel = (const void *)kernel;
-    last_smem = smem;
+    if (e != cudaSuccess)
+      return fail(static_cast<int>(e), "smem attribute: %s", cudaGetErrorString(e));
   }
-  int occ = occupancy((const void *)kernel, kThreads, smem);
+  return 0;
+}
+
+template <typename K>
+static int launch_cfg(K kernel, size_t smem, int64_t rows, int *grid, int threads = kThreads) {
+  if (int e = set_smem(kernel, smem)) return e;
+  int occ = occupancy((const void *)kernel, threads, smem);
   int64_t want = (rows + kWarpsPerCta - 1) / kWarpsPerCta;
   int64_t g = static_cast<int64_t>(sm_count()) * occ;
   if (g > want) g = want;
   if (g < 1) g = 1;
   *grid = static_cast<int>(g);
   return 0;
+}
+
+// Production geometry of the dense KL/TV kernels (scripts/tune_dense.cu,
+// profiles/): 4 x 128-bit loads in flight per lane, 5 CTAs x 8 warps per SM
+// when the staged target row fits (k <~ 4,900 for 5 CTAs), else fewer.
+constexpr int kU = 4, kMinBlocks = 5;
+
+template <typename K>
+static int launch_dense(K staged, K unstaged, int64_t rows, int64_t k, cudaStream_t stream,
+                        K *chosen, int *grid, size_t *smem_out) {
+  const int64_t k_pad = round_up(k, 2), m_pad = round_up(k, 16);
+  size_t smem = staged_smem_bytes(k_pad, m_pad);
+  K kern = staged;
+  if (smem > kMaxStagedSmem) {  // very large k: target row through L1/L2 instead
+    kern = unstaged;
+    smem = 0;
+  }
+  if (int e = launch_cfg(kern, smem, rows, grid)) return e;
+  *chosen = kern;
+  *smem_out = smem;
+  (void)stream;
+  return 0;
+}
+
+static int launch_kl_fixup(const double *P, int64_t ld, int64_t rows, int64_t k,
+                           const double *tgt, double clamp, double *out, uint32_t *flags,
+                           cudaStream_t stream) {
+  int64_t want = (rows + 32 * kWarpsPerCta - 1) / (32 * kWarpsPerCta);
+  int64_t g = static_cast<int64_t>(sm_count()) * 4;
+  if (g > want) g = want;
+  if (g < 1) g = 1;
+  kl_guard_fixup_kernel<<<static_cast<int>(g), kThreads, 0, stream>>>(P, ld, rows, k, tgt, clamp,
+                                                                       out, flags);
+  return check_launch("kl_guard_fixup");
 }
 
 static int check_dense_args(const double *P, int64_t ld, int64_t rows, int64_t k) {
@@ -387,8 +461,6 @@ static int check_dense_args(const double *P, int64_t ld, int64_t rows, int64_t k
     return fail(PF_E_ALIGN, "P rows must be 16-byte aligned (ld even, base aligned)");
   return 0;
 }
-
-static constexpr size_t kMaxStagedSmem = 200 * 1024;
 
 }  // namespace pf
 
@@ -427,16 +499,18 @@ int pf_dense_kl_f64(const double *P, int64_t ld, int64_t rows, int64_t k, const 
   if (!H || !tgt || !logt || !tmask || !out || !flags) return fail(PF_E_ARG, "dense_kl: null");
   if (rows == 0) return 0;
   const int64_t k_pad = round_up(k, 2), m_pad = round_up(k, 16);
-  const size_t smem = staged_smem_bytes(k_pad, m_pad);
-  if (smem > kMaxStagedSmem) return fail(PF_E_DOMAIN, "dense_kl: k=%lld too large for staging",
-                                         (long long)k);
-  auto kern = dense_kl_kernel<4>;
+  auto kern = dense_kl_kernel<kU, kMinBlocks, true>;
   int grid = 0;
-  if (int e = launch_cfg(kern, smem, rows, &grid)) return e;
+  size_t smem = 0;
+  if (int e = launch_dense(dense_kl_kernel<kU, kMinBlocks, true>,
+                           dense_kl_kernel<kU, kMinBlocks, false>, rows, k, as_stream(stream),
+                           &kern, &grid, &smem))
+    return e;
   kern<<<grid, kThreads, smem, as_stream(stream)>>>(P, ld, rows, k, k_pad, m_pad, H, tgt, logt,
                                                     tmask, clamp, tau, row0, target,
                                                     is_interior, out, flags);
-  return check_launch("dense_kl");
+  if (int e = check_launch("dense_kl")) return e;
+  return launch_kl_fixup(P, ld, rows, k, tgt, clamp, out, flags, as_stream(stream));
 }
 
 int pf_dense_tv_f64(const double *P, int64_t ld, int64_t rows, int64_t k, const double *tgt,
@@ -447,12 +521,13 @@ int pf_dense_tv_f64(const double *P, int64_t ld, int64_t rows, int64_t k, const 
   if (!tgt || !tmask || !out || !flags) return fail(PF_E_ARG, "dense_tv: null");
   if (rows == 0) return 0;
   const int64_t k_pad = round_up(k, 2), m_pad = round_up(k, 16);
-  const size_t smem = staged_smem_bytes(k_pad, m_pad);
-  if (smem > kMaxStagedSmem) return fail(PF_E_DOMAIN, "dense_tv: k=%lld too large for staging",
-                                         (long long)k);
-  auto kern = dense_tv_kernel<4>;
+  auto kern = dense_tv_kernel<kU, kMinBlocks, true>;
   int grid = 0;
-  if (int e = launch_cfg(kern, smem, rows, &grid)) return e;
+  size_t smem = 0;
+  if (int e = launch_dense(dense_tv_kernel<kU, kMinBlocks, true>,
+                           dense_tv_kernel<kU, kMinBlocks, false>, rows, k, as_stream(stream),
+                           &kern, &grid, &smem))
+    return e;
   kern<<<grid, kThreads, smem, as_stream(stream)>>>(P, ld, rows, k, k_pad, m_pad, tgt, tmask,
                                                     clamp, row0, target, is_interior, out,
                                                     flags);
@@ -468,14 +543,15 @@ int pf_dense_generic_f64(const double *P, int64_t ld, int64_t rows, int64_t k,
   if (!tgt || !tmask || !out || !flags) return fail(PF_E_ARG, "dense_generic: null");
   if (rows == 0) return 0;
   const int64_t k_pad = round_up(k, 2), m_pad = round_up(k, 16);
-  const size_t smem = staged_smem_bytes(k_pad, m_pad);
-  if (smem > kMaxStagedSmem)
-    return fail(PF_E_DOMAIN, "dense_generic: k=%lld too large for staging", (long long)k);
   int grid = 0;
+  size_t smem = 0;
 #define PF_GEN_CASE(KIND)                                                                   \
   case KIND: {                                                                              \
-    auto kern = dense_generic_kernel<KIND>;                                                 \
-    if (int e = launch_cfg(kern, smem, rows, &grid)) return e;                              \
+    auto kern = dense_generic_kernel<KIND, true>;                                           \
+    if (int e = launch_dense(dense_generic_kernel<KIND, true>,                              \
+                             dense_generic_kernel<KIND, false>, rows, k, as_stream(stream), \
+                             &kern, &grid, &smem))                                          \
+      return e;                                                                             \
     kern<<<grid, kThreads, smem, as_stream(stream)>>>(P, ld, rows, k, k_pad, m_pad, tgt,    \
                                                       tmask, clamp, param, swap_order,      \
                                                       row0, target, is_interior, out, flags); \

@@ -98,7 +98,8 @@ def O_synth(n, k, seed):
     return synthetic_kernel(n, k, seed)
 
 
-@pytest.mark.parametrize("n,k", [(1, 1), (33, 1), (257, 3), (1000, 17), (4099, 208), (2048, 4250)])
+@pytest.mark.parametrize("n,k", [(1, 1), (33, 1), (257, 3), (1000, 17), (4099, 208), (2048, 4250),
+                                 (64, 30001)])
 def test_ragged_shapes_vs_oracle(n, k):
     dense = O_synth(n, k, seed=n + k)
     dense[:, 0] = 0.0 if k > 2 else dense[:, 0]  # exact zeros, as P has
@@ -135,3 +136,51 @@ def test_negentropy_matches_numpy():
     ok, err = rel_close(H, ref, 1e-12)
     assert ok, err
     assert dk.min_value() == c.dense.min()
+
+
+@pytest.mark.parametrize("spec", [
+    {"gen": "holes", "spacing": 0.0125},                       # n=16,176 k=838
+    {"gen": "rectangle", "length": 20.0, "width": 1.0, "spacing": 0.05},  # corridor 20:1
+])
+def test_real_kernels_vs_oracle_medium(spec):
+    """Real Poisson kernels rebuilt with the reference's preprocessing (oracle/inputs.py):
+    KL/TV fields at several targets within 1e-10 of the reference arithmetic."""
+    from oracle import inputs as I
+    mesh = I.build(spec)
+    dense, boundary = I.poisson_kernel(mesh)
+    pk = pf.PoissonKernel(dense, boundary, 0.0, 0.0)
+    src, tgt = I.default_endpoints(mesh)
+    rng = np.random.default_rng(1)
+    targets = [tgt, int(boundary[3])] + [int(x) for x in rng.choice(mesh.interior_vertices, 2)]
+    for g in ("kl", "tv"):
+        for t in targets:
+            got = pf.dv_field(pk, pf.builtin_f(g), t)
+            ref, flags = O.dv_field(dense, boundary, g, t)
+            ok, err = rel_close(got.values, ref, RTOL)
+            assert ok, (spec, g, t, err)
+            assert got.precision_flags == flags
+
+
+def test_one_vs_many_slabs_bitwise():
+    """Row sharding: a field computed slab by slab (as N GPUs would) is bitwise the
+    single-slab field, because every row is reduced by the same kernel code."""
+    import torch
+    c = case("holes_fine")
+    full = pf.dv_field(_pk(c), pf.builtin_f("kl"), c.target).values
+    tv_full = pf.dv_field(_pk(c), pf.builtin_f("tv"), c.target).values
+    parts_kl, parts_tv = [], []
+    bounds = np.linspace(0, c.n, 4).astype(int)
+    for a, b in zip(bounds[:-1], bounds[1:]):
+        dk = dev.DeviceKernel(c.dense, c.boundary, row0=int(a), rows=int(b - a))
+        for g, parts in (("kl", parts_kl), ("tv", parts_tv)):
+            fd = pf.builtin_f(g)
+            out = torch.empty(dk.rows + 2, dtype=torch.float64, device=dk.device)
+            row = torch.from_numpy(c.dense[c.target].copy()).cuda()
+            st = pf.divergence._field_device(None, dk, fd, c.target, False, fd.clamp, out,
+                                             out.data_ptr() + dk.rows * 8,
+                                             torch.cuda.current_stream().cuda_stream, target_row=row)
+            torch.cuda.synchronize()
+            parts.append(out[:dk.rows].cpu().numpy())
+            del st
+    np.testing.assert_array_equal(np.concatenate(parts_kl), full)
+    np.testing.assert_array_equal(np.concatenate(parts_tv), tv_full)
