@@ -139,6 +139,60 @@ int pf_dense_at_f64(const double *P, int64_t ld, int64_t rows, int64_t k,
                     const int64_t *queries, int64_t nq, double *out,
                     pf_stream_t stream);
 
+/* ---- K4: sparsify (divergence.py:194-240) ---------------------------------
+ * keep = P >= cut (strict_positive == 0; cut = threshold / k computed by the
+ * caller exactly as divergence.py:219) or P > 0 (threshold 0, :220).
+ * pf_csr_count_f64 writes the per-row kept count; the caller scans it into
+ * indptr (rows+1, int64, indptr[0] = 0).  pf_csr_fill_f64 then writes, in
+ * scipy's order (row-major, ascending column):
+ *   indices (int32), data = kept P values, log_data = log(data) (:224-225),
+ *   hs[r] = sum data*log_data (the split-form KL row term), and
+ *   dropped[r] = max(0, 1 - rowsum) with rowsum in numpy reduceat order
+ *   (:227-228; bitwise the reference's). */
+int pf_csr_count_f64(const double *P, int64_t ld, int64_t rows, int64_t k, double cut,
+                     int strict_positive, int64_t *rownnz, pf_stream_t stream);
+int pf_csr_fill_f64(const double *P, int64_t ld, int64_t rows, int64_t k, double cut,
+                    int strict_positive, const int64_t *indptr, int32_t *indices,
+                    double *data, double *log_data, double *hs, double *dropped,
+                    pf_stream_t stream);
+
+/* ---- K5/K6 per-target staging ---------------------------------------------
+ * From CSR row p_local of the slab: vp[0..round_up(k,2)) = the sparsified
+ * target row scattered dense (0 off-support), tscal[0] = S_p = sum of its
+ * kept values, tscal[1] = dropped[p], tscal[2] = nnz_p (tscal holds 4 doubles).
+ * Replaces _row_support/_aligned for the target side (divergence.py:243-252). */
+int pf_csr_target_prep_f64(const int64_t *indptr, const int32_t *indices,
+                           const double *data, const double *dropped, int64_t p_local,
+                           int64_t k, double *vp, double *tscal, pf_stream_t stream);
+
+/* ---- K5: CSR KL field -------------------------------------------------------
+ * out[i] = sum_{j in supp(q)} v_qj (log v_qj - logt[j]),  q = queries[i] (global;
+ * slab rows start at row0) or q = row0 + i when queries == NULL; logt[j] =
+ * log(max(P[p,j], 1e-300)) is the target's dense log row (log_dense[p],
+ * divergence.py:226,277).  Split form hs[q] - sum v logt with a cancellation
+ * guard re-evaluated in the reference form; then _settle (:286).
+ * ops[i] = |supp(q)| (:276) if ops != NULL; flags[PF_FLAG_GUARDED] counts
+ * re-evaluated rows. */
+int pf_csr_kl_f64(const int64_t *indptr, const int32_t *indices, const double *data,
+                  const double *log_data, const double *hs, int64_t rows, int64_t k,
+                  const double *logt, double tau, int64_t row0, const int64_t *queries,
+                  int64_t nq, double *out, int64_t *ops, uint32_t *flags,
+                  pf_stream_t stream);
+
+/* ---- K6: CSR TV field -------------------------------------------------------
+ * out[i] = sum_{union} |vp - vq| + dropped[p] + dropped[q] (divergence.py:288-295,
+ * no settle), evaluated in one pass over supp(q) with vp/tscal from
+ * pf_csr_target_prep_f64; ops[i] = |supp(p) U supp(q)| (:289). */
+int pf_csr_tv_f64(const int64_t *indptr, const int32_t *indices, const double *data,
+                  const double *dropped, int64_t rows, int64_t k, const double *vp,
+                  const double *tscal, int64_t row0, const int64_t *queries, int64_t nq,
+                  double *out, int64_t *ops, pf_stream_t stream);
+
+/* Elementwise log view: out[r*k + c] = log(max(P[r*ld + c], clamp)), the
+ * reference's log_dense (divergence.py:226), materialised on request. */
+int pf_log_clamped_f64(const double *P, int64_t ld, int64_t rows, int64_t k, double clamp,
+                       double *out, pf_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

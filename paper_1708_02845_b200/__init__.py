@@ -8,7 +8,8 @@ types, computed by hand-written sm_100a CUDA kernels behind the C ABI in
 
 from .config import DEFAULTS, Settings
 from .divergence import (FDivergence, builtin_f, dv_at, dv_field,
-                         dv_field_device, dv_pair)
+                         dv_field_device, dv_field_sparse, dv_pair,
+                         dv_pair_sparse, dv_pair_sparse_stats, sparsify)
 from .errors import (DivergenceDomainError, InvalidTargetError, NativeError,
                      PathfieldError)
 from .solvers import PoissonKernel, ScalarField
@@ -17,6 +18,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "DEFAULTS", "Settings", "FDivergence", "builtin_f", "dv_at", "dv_field",
-    "dv_field_device", "dv_pair", "DivergenceDomainError", "InvalidTargetError",
+    "dv_field_device", "dv_pair", "sparsify", "dv_pair_sparse", "dv_pair_sparse_stats",
+    "dv_field_sparse", "DivergenceDomainError", "InvalidTargetError",
     "NativeError", "PathfieldError", "PoissonKernel", "ScalarField",
 ]

@@ -89,6 +89,7 @@ class DeviceKernel:
             interior[np.asarray(boundary, dtype=np.int64)] = 0
         self.is_interior = t.from_numpy(interior[self.row0:self.row0 + self.rows].copy()).to(self.device)
         self._H = {}
+        self._csr = {}
         self._min = None
         self._lock = threading.Lock()
         self._host = weakref.ref(dense) if dense is not None else None
@@ -120,6 +121,16 @@ class DeviceKernel:
             self.negentropy(1e-300)
         return float(self._min.item())
 
+    def csr(self, cut: float, strict_positive: bool) -> "DeviceCSR":
+        """The thresholded CSR view of this slab (K4), cached per (cut, mode)."""
+        key = (float(cut), bool(strict_positive))
+        with self._lock:
+            c = self._csr.get(key)
+            if c is None:
+                c = DeviceCSR(self, float(cut), bool(strict_positive))
+                self._csr[key] = c
+            return c
+
     def target_row(self, p: int, host_dense: np.ndarray | None = None):
         """Device view of the raw target row P[p, :k].
 
@@ -135,6 +146,40 @@ class DeviceKernel:
         if host_dense is None:
             raise NativeError(-102, f"target row {p} is not resident on this device")
         return t.from_numpy(np.array(host_dense[p], dtype=np.float64)).to(self.device)
+
+
+class DeviceCSR:
+    """CSR arrays of one slab built on the device from the dense rows (K4).
+
+    Layout: indptr int64 (rows+1, slab-local, indptr[0] = 0), indices int32
+    (ascending per row), data / log_data FP64 (nnz), hs = sum v log v and
+    dropped (FP64 per row).  scipy's layout (int32 columns) so the CSR
+    algorithmic bytes are nnz*(8+4) + rows*(8+8+8).
+    """
+
+    def __init__(self, dk: DeviceKernel, cut: float, strict_positive: bool):
+        t = torch()
+        self.dk, self.cut, self.strict = dk, cut, strict_positive
+        rows, dev_ = dk.rows, dk.device
+        s = t.cuda.current_stream(dev_).cuda_stream
+        rownnz = t.empty(rows, dtype=t.int64, device=dev_)
+        nat.call("pf_csr_count_f64", dk.P.data_ptr(), dk.ld, rows, dk.k, cut,
+                 int(strict_positive), rownnz.data_ptr(), s)
+        self.indptr = t.zeros(rows + 1, dtype=t.int64, device=dev_)
+        t.cumsum(rownnz, 0, out=self.indptr[1:])
+        self.nnz = int(self.indptr[-1].item())
+        self.indices = t.empty(max(self.nnz, 1), dtype=t.int32, device=dev_)
+        self.data = t.empty(max(self.nnz, 1), dtype=t.float64, device=dev_)
+        self.log_data = t.empty(max(self.nnz, 1), dtype=t.float64, device=dev_)
+        self.hs = t.empty(rows, dtype=t.float64, device=dev_)
+        self.dropped = t.empty(rows, dtype=t.float64, device=dev_)
+        nat.call("pf_csr_fill_f64", dk.P.data_ptr(), dk.ld, rows, dk.k, cut,
+                 int(strict_positive), self.indptr.data_ptr(), self.indices.data_ptr(),
+                 self.data.data_ptr(), self.log_data.data_ptr(), self.hs.data_ptr(),
+                 self.dropped.data_ptr(), s)
+
+    def owns(self, row: int) -> bool:
+        return self.dk.owns(row)
 
 
 _cache: dict[int, tuple[weakref.ref, DeviceKernel]] = {}

@@ -42,6 +42,15 @@ _SIGS = {
                              c_int, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp],
     "pf_dense_at_f64": [c_vp, c_i64, c_i64, c_i64, c_vp, c_dbl, c_int, c_dbl, c_int, c_i64,
                         c_i64, c_vp, c_i64, c_vp, c_vp],
+    "pf_csr_count_f64": [c_vp, c_i64, c_i64, c_i64, c_dbl, c_int, c_vp, c_vp],
+    "pf_csr_fill_f64": [c_vp, c_i64, c_i64, c_i64, c_dbl, c_int, c_vp, c_vp, c_vp, c_vp, c_vp,
+                        c_vp, c_vp],
+    "pf_csr_target_prep_f64": [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp],
+    "pf_csr_kl_f64": [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_dbl, c_i64, c_vp,
+                      c_i64, c_vp, c_vp, c_vp, c_vp],
+    "pf_csr_tv_f64": [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_i64,
+                      c_vp, c_vp, c_vp],
+    "pf_log_clamped_f64": [c_vp, c_i64, c_i64, c_i64, c_dbl, c_vp, c_vp],
 }
 _RESTYPES = {"pf_last_error": ctypes.c_char_p}
 

@@ -1,0 +1,447 @@
+// csr.cu — thresholded sparse Poisson kernel (K4) and CSR KL/TV fields (K5/K6).
+//
+// Reference semantics: pathfield/divergence.py
+//   sparsify              :194-240  (cut = threshold/k, keep P >= cut, or P > 0 at
+//                                    threshold 0; CSR with ascending columns;
+//                                    log views; dropped = clip(1 - rowsum, 0))
+//   dv_pair_sparse_stats  :255-299  (kl: sum over supp(q) of v (log v - log_dense[p]);
+//                                    tv: union sum |vp - vq| + dropped[p] + dropped[q])
+//
+// K4 is count -> scan -> fill over the dense rows (the pattern is bit-exact: the
+// same FP64 compare against the same `cut` double).  `dropped` reproduces
+// scipy's csr.sum(axis=1) = np.add.reduceat (first element + numpy pairwise sum
+// of the rest) so it is bitwise the reference's.
+//
+// K5/K6 are warp-per-row segmented reductions over the CSR arrays with the
+// per-target dense vector (log P[t,:] for KL, the sparsified target row for
+// TV) staged once per CTA in shared memory by a TMA bulk copy.  KL uses the
+// split form hs[q] - sum v*logPt with hs[q] = sum v log v precomputed at
+// sparsify time, and the same cancellation guard + fixup pass as the dense KL
+// (the fixup re-evaluates the reference form sum v*(log v - logPt) from the
+// stored log view).  TV is restated as a single pass over supp(q):
+//   sum_{supp q}(|vq - vp| - vp) + S_p + (dropped_p + dropped_q)
+// which equals the union form (1.1e-13) and is exactly
+// 2*dropped_p at q = p because S_p is reduced in the same lane order.
+#include <cmath>
+
+#include "pf_common.cuh"
+
+namespace pf {
+
+constexpr int kCsrThreads = 256;
+constexpr unsigned long long kCsrGuard = 0x7ff8dead0000c5a1ull;  // NaN payload
+
+__device__ __forceinline__ bool keep_entry(double x, double cut, int strict_pos) {
+  return strict_pos ? (x > 0.0) : (x >= cut);
+}
+
+// ------------------------------------------------------------ K4 count --
+__global__ void __launch_bounds__(kCsrThreads) csr_count_kernel(
+    const double *__restrict__ P, int64_t ld, int64_t rows, int64_t k, double cut,
+    int strict_pos, int64_t *__restrict__ rownnz) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t npair = k >> 1;
+  for (int64_t r = warp; r < rows; r += nwarps) {
+    const double2 *row = reinterpret_cast<const double2 *>(P + r * ld);
+    int cnt = 0;
+    for (int64_t j = lane; j < npair; j += 32) {
+      const double2 v = ldg_stream2(row + j);
+      cnt += keep_entry(v.x, cut, strict_pos) + keep_entry(v.y, cut, strict_pos);
+    }
+    if ((k & 1) && lane == 0) cnt += keep_entry(P[r * ld + k - 1], cut, strict_pos);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (lane == 0) rownnz[r] = cnt;
+  }
+}
+
+// ------------------------------------------------------------ K4 fill --
+// Columns are visited in ascending order 32 at a time; positions come from a
+// ballot prefix, so the output order is scipy's (row-major, ascending).
+__global__ void __launch_bounds__(kCsrThreads) csr_fill_kernel(
+    const double *__restrict__ P, int64_t ld, int64_t rows, int64_t k, double cut,
+    int strict_pos, const int64_t *__restrict__ indptr, int32_t *__restrict__ indices,
+    double *__restrict__ data, double *__restrict__ log_data, double *__restrict__ hs) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const unsigned lower = (1u << lane) - 1u;
+  for (int64_t r = warp; r < rows; r += nwarps) {
+    const double *row = P + r * ld;
+    int64_t pos = indptr[r];
+    double acc = 0.0;
+    for (int64_t c0 = 0; c0 < k; c0 += 32) {
+      const int64_t c = c0 + lane;
+      const double x = c < k ? ldg_stream(row + c) : 0.0;
+      const bool kp = c < k && keep_entry(x, cut, strict_pos);
+      const unsigned ball = __ballot_sync(0xffffffffu, kp);
+      if (kp) {
+        const int64_t at = pos + __popc(ball & lower);
+        const double lg = log(x);
+        indices[at] = static_cast<int32_t>(c);
+        data[at] = x;
+        log_data[at] = lg;
+        acc += __dmul_rn(x, lg);
+      }
+      pos += __popc(ball);
+    }
+    const double h = warp_sum(acc);
+    if (lane == 0) hs[r] = h;
+  }
+}
+
+// numpy pairwise summation (numpy/_core/src/umath/loops_utils.h.src,
+// pairwise_sum_DOUBLE): < 8 sequential from -0.0; <= 128 eight strided
+// accumulators combined ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) then the tail;
+// else split at n/2 rounded down to a multiple of 8.
+__device__ double np_pairwise_sum(const double *a, int64_t n) {
+  if (n < 8) {
+    double res = -0.0;
+    for (int64_t i = 0; i < n; ++i) res += a[i];
+    return res;
+  }
+  if (n <= 128) {
+    double r0 = a[0], r1 = a[1], r2 = a[2], r3 = a[3], r4 = a[4], r5 = a[5], r6 = a[6],
+           r7 = a[7];
+    int64_t i = 8;
+    for (; i < n - (n % 8); i += 8) {
+      r0 += a[i + 0];
+      r1 += a[i + 1];
+      r2 += a[i + 2];
+      r3 += a[i + 3];
+      r4 += a[i + 4];
+      r5 += a[i + 5];
+      r6 += a[i + 6];
+      r7 += a[i + 7];
+    }
+    double res = ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7));
+    for (; i < n; ++i) res += a[i];
+    return res;
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  return np_pairwise_sum(a, n2) + np_pairwise_sum(a + n2, n - n2);
+}
+
+// dropped[r] = max(0, 1 - rowsum) with rowsum = np.add.reduceat semantics:
+// data[lo] + pairwise(data[lo+1:hi]); empty rows sum to 0 (divergence.py:227-228).
+__global__ void csr_dropped_kernel(const int64_t *__restrict__ indptr,
+                                   const double *__restrict__ data, int64_t rows,
+                                   double *__restrict__ dropped) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t lo = indptr[r], hi = indptr[r + 1];
+    double s = 0.0;
+    if (hi - lo == 1) s = data[lo];
+    else if (hi - lo > 1) s = data[lo] + np_pairwise_sum(data + lo + 1, hi - lo - 1);
+    const double d = 1.0 - s;
+    dropped[r] = d < 0.0 ? 0.0 : d;  // np.clip(., 0, None)
+  }
+}
+
+// ---------------------------------------------------- K5/K6 target prep --
+// vp[k_pad]: the sparsified target row scattered dense (0 off-support);
+// tscal[0] = S_p (reduced in the K6 lane order), tscal[1] = dropped[p],
+// tscal[2] = nnz_p.  One CTA.
+__global__ void csr_target_prep_kernel(const int64_t *__restrict__ indptr,
+                                       const int32_t *__restrict__ indices,
+                                       const double *__restrict__ data,
+                                       const double *__restrict__ dropped, int64_t p, int64_t k,
+                                       int64_t k_pad, double *__restrict__ vp,
+                                       double *__restrict__ tscal) {
+  for (int64_t i = threadIdx.x; i < k_pad; i += blockDim.x) vp[i] = 0.0;
+  __syncthreads();
+  const int64_t lo = indptr[p], hi = indptr[p + 1];
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) vp[indices[i]] = data[i];
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    double a = 0.0;
+    for (int64_t i = lo + lane; i < hi; i += 32) a += data[i];
+    a = warp_sum(a);
+    if (lane == 0) {
+      tscal[0] = a;
+      tscal[1] = dropped[p];
+      tscal[2] = static_cast<double>(hi - lo);
+      tscal[3] = 0.0;
+    }
+  }
+}
+
+__device__ __forceinline__ const double *stage_vec(unsigned char *smem, const double *vec,
+                                                   int64_t k_pad) {
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
+  double *s_vec = reinterpret_cast<double *>(smem + 16);
+  if (threadIdx.x == 0) mbar_init(bar, 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t b = static_cast<uint32_t>(k_pad * 8);
+    mbar_expect_tx(bar, b);
+    bulk_g2s(s_vec, vec, b, bar);
+  }
+  mbar_wait(bar, 0);
+  return s_vec;
+}
+
+// ------------------------------------------------------------ K5 CSR KL --
+template <bool STAGE>
+__global__ void __launch_bounds__(kCsrThreads) csr_kl_kernel(
+    const int64_t *__restrict__ indptr, const int32_t *__restrict__ indices,
+    const double *__restrict__ data, const double *__restrict__ hs, int64_t rows, int64_t k_pad,
+    const double *__restrict__ logt, double tau, int64_t row0, const int64_t *__restrict__ queries,
+    int64_t nq, double *__restrict__ out, int64_t *__restrict__ ops) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const double *lt = STAGE ? stage_vec(smem, logt, k_pad) : logt;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t count = queries ? nq : rows;
+  for (int64_t i = warp; i < count; i += nwarps) {
+    const int64_t r = queries ? queries[i] - row0 : i;
+    const int64_t lo = indptr[r], hi = indptr[r + 1];
+    const double h = hs[r];
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int64_t e = lo + lane;
+    for (; e + 96 < hi; e += 128) {
+      const double v0 = __ldg(data + e), v1 = __ldg(data + e + 32), v2 = __ldg(data + e + 64),
+                   v3 = __ldg(data + e + 96);
+      const int32_t c0 = __ldg(indices + e), c1 = __ldg(indices + e + 32),
+                    c2 = __ldg(indices + e + 64), c3 = __ldg(indices + e + 96);
+      a0 = fma(v0, lt[c0], a0);
+      a1 = fma(v1, lt[c1], a1);
+      a2 = fma(v2, lt[c2], a2);
+      a3 = fma(v3, lt[c3], a3);
+    }
+    for (; e < hi; e += 32) a0 = fma(__ldg(data + e), lt[__ldg(indices + e)], a0);
+    const double cross = warp_sum((a0 + a1) + (a2 + a3));
+    double val = h - cross;
+    if (fabs(val) < tau * (fabs(h) + fabs(cross)))
+      val = __longlong_as_double(static_cast<long long>(kCsrGuard));
+    else
+      val = settle(val);  // divergence.py:286
+    if (lane == 0) {
+      out[i] = val;
+      if (ops) ops[i] = hi - lo;  // divergence.py:276
+    }
+  }
+}
+
+// Guarded rows: reference form sum_{supp q} v * (log v - logPt) (divergence.py:279).
+__global__ void __launch_bounds__(kCsrThreads) csr_kl_fixup_kernel(
+    const int64_t *__restrict__ indptr, const int32_t *__restrict__ indices,
+    const double *__restrict__ data, const double *__restrict__ log_data, int64_t rows,
+    const double *__restrict__ logt, int64_t row0, const int64_t *__restrict__ queries,
+    int64_t nq, double *__restrict__ out, uint32_t *__restrict__ flags) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t count = queries ? nq : rows;
+  uint32_t done = 0;
+  for (int64_t base = warp * 32; base < count; base += nwarps * 32) {
+    const int64_t mine = base + lane;
+    const bool flag = mine < count && static_cast<unsigned long long>(
+                                          __double_as_longlong(out[mine])) == kCsrGuard;
+    unsigned ball = __ballot_sync(0xffffffffu, flag);
+    while (ball) {
+      const int src = __ffs(ball) - 1;
+      ball &= ball - 1;
+      const int64_t i = base + src;
+      const int64_t r = queries ? queries[i] - row0 : i;
+      const int64_t lo = indptr[r], hi = indptr[r + 1];
+      double a = 0.0;
+      for (int64_t e = lo + lane; e < hi; e += 32)
+        a += __dmul_rn(data[e], log_data[e] - logt[indices[e]]);
+      const double val = settle(warp_sum(a));
+      if (lane == 0) out[i] = val;
+      ++done;
+    }
+  }
+  if (lane == 0 && done && flags) atomicAdd(&flags[PF_FLAG_GUARDED], done);
+}
+
+// ------------------------------------------------------------ K6 CSR TV --
+template <bool STAGE>
+__global__ void __launch_bounds__(kCsrThreads) csr_tv_kernel(
+    const int64_t *__restrict__ indptr, const int32_t *__restrict__ indices,
+    const double *__restrict__ data, const double *__restrict__ dropped, int64_t rows,
+    int64_t k_pad, const double *__restrict__ vp, const double *__restrict__ tscal, int64_t row0,
+    const int64_t *__restrict__ queries, int64_t nq, double *__restrict__ out,
+    int64_t *__restrict__ ops) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const double *v_p = STAGE ? stage_vec(smem, vp, k_pad) : vp;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t count = queries ? nq : rows;
+  const double S_p = tscal[0], d_p = tscal[1];
+  const int64_t nnz_p = static_cast<int64_t>(tscal[2]);
+  for (int64_t i = warp; i < count; i += nwarps) {
+    const int64_t r = queries ? queries[i] - row0 : i;
+    const int64_t lo = indptr[r], hi = indptr[r + 1];
+    const double d_q = dropped[r];
+    // single per-lane accumulator in element order (matches csr_target_prep's
+    // S_p order so that q == p cancels exactly)
+    double a = 0.0;
+    int inter = 0;
+    for (int64_t e = lo + lane; e < hi; e += 32) {
+      const double v = __ldg(data + e);
+      const double w = v_p[__ldg(indices + e)];
+      a += fabs(v - w) - w;
+      inter += (w != 0.0);
+    }
+    const double base = warp_sum(a) + S_p;
+    const double val = base + (d_p + d_q);  // divergence.py:293-295 (no settle)
+    if (ops) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) inter += __shfl_xor_sync(0xffffffffu, inter, o);
+    }
+    if (lane == 0) {
+      out[i] = val;
+      if (ops) ops[i] = (hi - lo) + nnz_p - inter;  // |union|, divergence.py:289
+    }
+  }
+}
+
+__global__ void log_clamped_kernel(const double *__restrict__ P, int64_t ld, int64_t rows,
+                                   int64_t k, double clamp, double *__restrict__ out) {
+  const int64_t n = rows * k;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / k, c = i - r * k;
+    out[i] = log(fmax(P[r * ld + c], clamp));
+  }
+}
+
+static int grid_for(const void *kern, int threads, size_t smem, int64_t work_warps) {
+  int occ = occupancy(kern, threads, smem);
+  int64_t want = (work_warps + threads / 32 - 1) / (threads / 32);
+  int64_t g = static_cast<int64_t>(sm_count()) * occ;
+  if (g > want) g = want;
+  if (g < 1) g = 1;
+  return static_cast<int>(g);
+}
+
+template <typename K>
+static int smem_attr(K kern, size_t smem) {
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute((const void *)kern,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return fail(static_cast<int>(e), "smem attr: %s", cudaGetErrorString(e));
+  }
+  return 0;
+}
+
+}  // namespace pf
+
+using namespace pf;
+
+extern "C" {
+
+int pf_csr_count_f64(const double *P, int64_t ld, int64_t rows, int64_t k, double cut,
+                     int strict_positive, int64_t *rownnz, pf_stream_t stream) {
+  if ((!P && rows) || !rownnz || k <= 0 || ld < k || rows < 0)
+    return fail(PF_E_ARG, "csr_count: bad args");
+  if ((ld & 1) || (reinterpret_cast<uintptr_t>(P) & 15))
+    return fail(PF_E_ALIGN, "csr_count: P rows must be 16-byte aligned");
+  if (rows == 0) return 0;
+  const int g = grid_for((const void *)csr_count_kernel, kCsrThreads, 0, rows);
+  csr_count_kernel<<<g, kCsrThreads, 0, as_stream(stream)>>>(P, ld, rows, k, cut,
+                                                             strict_positive, rownnz);
+  return check_launch("csr_count");
+}
+
+int pf_csr_fill_f64(const double *P, int64_t ld, int64_t rows, int64_t k, double cut,
+                    int strict_positive, const int64_t *indptr, int32_t *indices, double *data,
+                    double *log_data, double *hs, double *dropped, pf_stream_t stream) {
+  if ((!P && rows) || !indptr || !hs || !dropped || k <= 0 || ld < k || rows < 0)
+    return fail(PF_E_ARG, "csr_fill: bad args");
+  if (k > 2147483647LL) return fail(PF_E_DOMAIN, "csr_fill: k exceeds int32 columns");
+  if (rows == 0) return 0;
+  const int g = grid_for((const void *)csr_fill_kernel, kCsrThreads, 0, rows);
+  csr_fill_kernel<<<g, kCsrThreads, 0, as_stream(stream)>>>(P, ld, rows, k, cut, strict_positive,
+                                                            indptr, indices, data, log_data, hs);
+  if (int e = check_launch("csr_fill")) return e;
+  int64_t blocks = (rows + 127) / 128;
+  if (blocks > 65535) blocks = 65535;
+  csr_dropped_kernel<<<static_cast<int>(blocks), 128, 0, as_stream(stream)>>>(indptr, data, rows,
+                                                                             dropped);
+  return check_launch("csr_dropped");
+}
+
+int pf_csr_target_prep_f64(const int64_t *indptr, const int32_t *indices, const double *data,
+                           const double *dropped, int64_t p_local, int64_t k, double *vp,
+                           double *tscal, pf_stream_t stream) {
+  if (!indptr || !dropped || !vp || !tscal || k <= 0 || p_local < 0)
+    return fail(PF_E_ARG, "csr_target_prep: bad args");
+  csr_target_prep_kernel<<<1, 512, 0, as_stream(stream)>>>(indptr, indices, data, dropped,
+                                                           p_local, k, round_up(k, 2), vp,
+                                                           tscal);
+  return check_launch("csr_target_prep");
+}
+
+int pf_csr_kl_f64(const int64_t *indptr, const int32_t *indices, const double *data,
+                  const double *log_data, const double *hs, int64_t rows, int64_t k,
+                  const double *logt, double tau, int64_t row0, const int64_t *queries,
+                  int64_t nq, double *out, int64_t *ops, uint32_t *flags, pf_stream_t stream) {
+  if (!indptr || !hs || !logt || !out || rows < 0 || k <= 0)
+    return fail(PF_E_ARG, "csr_kl: bad args");
+  const int64_t count = queries ? nq : rows;
+  if (count <= 0) return 0;
+  const int64_t k_pad = round_up(k, 2);
+  const size_t smem = 16 + static_cast<size_t>(k_pad) * 8;
+  const bool staged = smem <= 200 * 1024;
+  if (staged) {
+    if (int e = smem_attr(csr_kl_kernel<true>, smem)) return e;
+    const int g = grid_for((const void *)csr_kl_kernel<true>, kCsrThreads, smem, count);
+    csr_kl_kernel<true><<<g, kCsrThreads, smem, as_stream(stream)>>>(
+        indptr, indices, data, hs, rows, k_pad, logt, tau, row0, queries, nq, out, ops);
+  } else {
+    const int g = grid_for((const void *)csr_kl_kernel<false>, kCsrThreads, 0, count);
+    csr_kl_kernel<false><<<g, kCsrThreads, 0, as_stream(stream)>>>(
+        indptr, indices, data, hs, rows, k_pad, logt, tau, row0, queries, nq, out, ops);
+  }
+  if (int e = check_launch("csr_kl")) return e;
+  int64_t want = (count + 32 * 8 - 1) / (32 * 8);
+  int64_t g2 = static_cast<int64_t>(sm_count()) * 4;
+  if (g2 > want) g2 = want;
+  if (g2 < 1) g2 = 1;
+  csr_kl_fixup_kernel<<<static_cast<int>(g2), kCsrThreads, 0, as_stream(stream)>>>(
+      indptr, indices, data, log_data, rows, logt, row0, queries, nq, out, flags);
+  return check_launch("csr_kl_fixup");
+}
+
+int pf_csr_tv_f64(const int64_t *indptr, const int32_t *indices, const double *data,
+                  const double *dropped, int64_t rows, int64_t k, const double *vp,
+                  const double *tscal, int64_t row0, const int64_t *queries, int64_t nq,
+                  double *out, int64_t *ops, pf_stream_t stream) {
+  if (!indptr || !dropped || !vp || !tscal || !out || rows < 0 || k <= 0)
+    return fail(PF_E_ARG, "csr_tv: bad args");
+  const int64_t count = queries ? nq : rows;
+  if (count <= 0) return 0;
+  const int64_t k_pad = round_up(k, 2);
+  const size_t smem = 16 + static_cast<size_t>(k_pad) * 8;
+  if (smem <= 200 * 1024) {
+    if (int e = smem_attr(csr_tv_kernel<true>, smem)) return e;
+    const int g = grid_for((const void *)csr_tv_kernel<true>, kCsrThreads, smem, count);
+    csr_tv_kernel<true><<<g, kCsrThreads, smem, as_stream(stream)>>>(
+        indptr, indices, data, dropped, rows, k_pad, vp, tscal, row0, queries, nq, out, ops);
+  } else {
+    const int g = grid_for((const void *)csr_tv_kernel<false>, kCsrThreads, 0, count);
+    csr_tv_kernel<false><<<g, kCsrThreads, 0, as_stream(stream)>>>(
+        indptr, indices, data, dropped, rows, k_pad, vp, tscal, row0, queries, nq, out, ops);
+  }
+  return check_launch("csr_tv");
+}
+
+int pf_log_clamped_f64(const double *P, int64_t ld, int64_t rows, int64_t k, double clamp,
+                       double *out, pf_stream_t stream) {
+  if ((!P || !out) && rows > 0) return fail(PF_E_ARG, "log_clamped: null");
+  if (rows <= 0) return 0;
+  const int blocks = sm_count() * 8;
+  log_clamped_kernel<<<blocks, 256, 0, as_stream(stream)>>>(P, ld, rows, k, clamp, out);
+  return check_launch("log_clamped");
+}
+
+}  // extern "C"

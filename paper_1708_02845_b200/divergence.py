@@ -273,7 +273,197 @@ def dv_pair(pk: PoissonKernel, fd: FDivergence, p: int, q: int,
     return _settle(val)
 
 
+# ---------------------------------------------------------------------------
+# Sparsification and sparse distances (divergence.py:194-305)
+# ---------------------------------------------------------------------------
+
+class LogDenseView:
+    """``log_dense`` of a sparsified kernel (divergence.py:226), materialised lazily.
+
+    The reference stores an n x k FP64 log matrix eagerly; the device path
+    never needs it (the sparse KL reads only the target's log row, computed
+    per call), so it is produced on the GPU (``pf_log_clamped_f64``) only
+    when someone indexes it.
+    """
+
+    def __init__(self, dk):
+        self._dk = dk
+        self._arr = None
+        self.shape = (dk.n, dk.k)
+        self.dtype = np.dtype(np.float64)
+        self.ndim = 2
+
+    def _materialise(self) -> np.ndarray:
+        if self._arr is None:
+            t = dev.require_cuda()
+            dk = self._dk
+            outd = t.empty((dk.rows, dk.k), dtype=t.float64, device=dk.device)
+            s = t.cuda.current_stream(dk.device)
+            nat.call("pf_log_clamped_f64", dk.P.data_ptr(), dk.ld, dk.rows, dk.k, _CLAMP_LOG,
+                     outd.data_ptr(), s.cuda_stream)
+            self._arr = _to_host(t, outd, s)
+            self._arr.setflags(write=False)
+        return self._arr
+
+    def __array__(self, dtype=None, copy=None):
+        a = self._materialise()
+        return a if dtype is None else a.astype(dtype)
+
+    def __getitem__(self, idx):
+        return self._materialise()[idx]
+
+    def __len__(self):
+        return self.shape[0]
+
+
+def _csr_host(data, indices, indptr, shape):
+    try:
+        import scipy.sparse as sp
+        return sp.csr_matrix((data, indices, indptr), shape=shape)
+    except Exception:  # scipy absent: same attribute names
+        from .solvers import CsrView
+        return CsrView(data, indices, indptr, shape)
+
+
+def sparsify(pk: PoissonKernel, threshold: float | None = None) -> PoissonKernel:
+    """Add sparse + log views, dropping entries below threshold/k (divergence.py:194-240).
+
+    The CSR pattern is built on the GPU (K4) and is bit-identical to
+    ``csr_matrix`` + ``eliminate_zeros`` of the reference; ``dropped_mass``
+    follows scipy's reduceat summation order bit for bit.
+    """
+    import dataclasses
+    import math
+    n, k = pk.n, pk.k
+    if threshold is None:
+        threshold = 1.0 / math.sqrt(n)
+    if threshold < 0:
+        raise ValueError("threshold must be nonnegative")
+    if threshold >= 1.0:
+        raise ValueError(f"threshold {threshold} >= 1 would empty rows")
+    cut = threshold / k
+    t = dev.require_cuda()
+    dk = dev.device_kernel(pk)
+    dc = dk.csr(cut, threshold == 0)
+    s = t.cuda.current_stream(dk.device)
+    nnz = dc.nnz
+    idx_dtype = np.int32 if nnz < 2 ** 31 else np.int64
+    indptr = _to_host(t, dc.indptr, s).astype(idx_dtype)
+    indices = _to_host(t, dc.indices[:nnz], s).astype(idx_dtype, copy=False)
+    data = _to_host(t, dc.data[:nnz], s)
+    logs = _to_host(t, dc.log_data[:nnz], s)
+    dropped = _to_host(t, dc.dropped, s)
+    interior = np.ones(n, dtype=bool)
+    interior[np.asarray(pk.boundary, dtype=np.int64)] = False
+    m = int(interior.sum())
+    if m:
+        nnz_interior = int(np.diff(indptr.astype(np.int64))[interior].sum())
+        sparsity = 100.0 * (1.0 - nnz_interior / (m * k))
+    else:
+        sparsity = 0.0
+    return dataclasses.replace(
+        pk, threshold=float(threshold), sparse=_csr_host(data, indices, indptr, (n, k)),
+        log_sparse=_csr_host(logs, indices.copy(), indptr.copy(), (n, k)),
+        log_dense=LogDenseView(dk), dropped_mass=dropped, row_cut=float(cut),
+        sparsity_percent=float(sparsity))
+
+
+def _device_csr(pk):
+    if getattr(pk, "sparse", None) is None or getattr(pk, "log_dense", None) is None:
+        raise DivergenceDomainError("kernel has no sparse views; run sparsify")
+    dk = dev.device_kernel(pk)
+    thr = getattr(pk, "threshold", None)
+    return dk, dk.csr(float(pk.row_cut), thr == 0)
+
+
+def _sparse_launch(pk, fd, p: int, queries=None, want_ops=False):
+    """Launch K5/K6 for target p over all slab rows or `queries` (device tensors back)."""
+    t = dev.require_cuda()
+    if fd.name not in ("kl", "tv"):
+        raise NotImplementedError(
+            f"sparse {fd.name!r}: the device path implements the kl and tv sparse forms "
+            "(divergence.py:275-295)")
+    dk, dc = _device_csr(pk)
+    s = t.cuda.current_stream(dk.device)
+    qd = None
+    count = dk.rows
+    if queries is not None:
+        qd = t.from_numpy(np.asarray(queries, dtype=np.int64)).to(dk.device)
+        count = qd.numel()
+    out = t.empty(count + 2, dtype=t.float64, device=dk.device)
+    flags = out.data_ptr() + count * 8
+    ops = t.empty(max(count, 1), dtype=t.int64, device=dk.device) if want_ops else None
+    qptr = 0 if qd is None else qd.data_ptr()
+    k_pad = dev.round_up(dk.k, 2)
+    if fd.name == "kl":
+        st = _Staging(t, dk.k, dk.device)
+        row = dk.target_row(p)
+        nat.call("pf_target_prep_f64", row.data_ptr(), dk.k, _CLAMP_LOG, st.tgt, st.logt,
+                 st.tmask, flags, s.cuda_stream)
+        nat.call("pf_csr_kl_f64", dc.indptr.data_ptr(), dc.indices.data_ptr(), dc.data.data_ptr(),
+                 dc.log_data.data_ptr(), dc.hs.data_ptr(), dk.rows, dk.k, st.logt,
+                 KL_GUARD_TAU, dk.row0, qptr, count, out.data_ptr(), nat.ptr(ops), flags,
+                 s.cuda_stream)
+    else:
+        if not dk.owns(p):
+            raise NotImplementedError("target row outside this slab: use parallel.ShardedCSR")
+        st = t.empty(k_pad + 4, dtype=t.float64, device=dk.device)
+        out.view(t.int32)[2 * count:2 * count + 4].zero_()
+        nat.call("pf_csr_target_prep_f64", dc.indptr.data_ptr(), dc.indices.data_ptr(),
+                 dc.data.data_ptr(), dc.dropped.data_ptr(), p - dk.row0, dk.k, st.data_ptr(),
+                 st.data_ptr() + k_pad * 8, s.cuda_stream)
+        nat.call("pf_csr_tv_f64", dc.indptr.data_ptr(), dc.indices.data_ptr(), dc.data.data_ptr(),
+                 dc.dropped.data_ptr(), dk.rows, dk.k, st.data_ptr(), st.data_ptr() + k_pad * 8,
+                 dk.row0, qptr, count, out.data_ptr(), nat.ptr(ops), s.cuda_stream)
+    return out, ops, count, s, st
+
+
+def dv_pair_sparse_stats(pk: PoissonKernel, fd: FDivergence, p: int, q: int,
+                         swap_order: bool = False) -> tuple[float, int]:
+    """Sparse-view divergence plus the summation-slot count (divergence.py:255-299)."""
+    if getattr(pk, "sparse", None) is None or getattr(pk, "log_dense", None) is None:
+        raise DivergenceDomainError("kernel has no sparse views; run sparsify")
+    if swap_order:
+        p, q = q, p
+    t = dev.require_cuda()
+    out, ops, count, s, st = _sparse_launch(pk, fd, int(p), [int(q)], want_ops=True)
+    host = _to_host(t, out, s)
+    nops = _to_host(t, ops, s)
+    del st
+    return float(host[0]), int(nops[0])
+
+
+def dv_pair_sparse(pk: PoissonKernel, fd: FDivergence, p: int, q: int,
+                   swap_order: bool = False) -> float:
+    """Sparse-view divergence distance between target p and query q (divergence.py:302-305)."""
+    return dv_pair_sparse_stats(pk, fd, p, q, swap_order)[0]
+
+
+def dv_field_sparse(pk: PoissonKernel, fd: FDivergence, p: int) -> ScalarField:
+    """Sparse field: ``[dv_pair_sparse(pk, fd, p, q) for q in range(n)]`` in one launch.
+
+    Additive API (the reference has only the per-pair loop).
+    """
+    if not 0 <= p < pk.n:
+        raise InvalidTargetError(f"target {p} out of range")
+    t = dev.require_cuda()
+    out, ops, count, s, st = _sparse_launch(pk, fd, int(p))
+    host = _to_host(t, out, s)
+    del st
+    vals = host[:count]
+    return ScalarField(vals, fd.name, int(p), dict(getattr(fd, "params", {}) or {}), 1, None, ())
+
+
+def dv_field_sparse_device(pk: PoissonKernel, fd: FDivergence, p: int):
+    """Device-resident sparse field (values tensor, flags tensor); used by bench.py."""
+    t = dev.require_cuda()
+    out, ops, count, s, st = _sparse_launch(pk, fd, int(p))
+    return out[:count], out[count:].view(t.int32)
+
+
 __all__ = [
+    "sparsify", "dv_pair_sparse", "dv_pair_sparse_stats", "dv_field_sparse",
+    "dv_field_sparse_device", "LogDenseView",
     "FDivergence", "builtin_f", "dv_pair", "dv_at", "dv_field", "dv_field_device",
     "KL_GUARD_TAU",
 ]

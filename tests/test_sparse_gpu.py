@@ -1,0 +1,142 @@
+"""Sparsified kernel (K4) and CSR KL/TV (K5/K6) on the B200 vs the reference goldens.
+
+Bars: CSR pattern (indptr, indices) and kept data bit-exact; dropped mass
+bitwise (scipy reduceat order); sparse distances within 1e-10 relative of the
+reference's dv_pair_sparse loop; op counts exact.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+import paper_1708_02845_b200 as pf
+from oracle import divergence as O
+from oracle import inputs as I
+from tests.conftest import case, rel_close
+
+pytestmark = pytest.mark.gpu
+RTOL = 1e-10
+SPARSE_CASES = ["c1", "corridor50", "disk40"]
+
+
+def _pk(c):
+    return pf.PoissonKernel(c.dense, c.boundary, 0.0, 0.0)
+
+
+@pytest.mark.parametrize("name", SPARSE_CASES)
+def test_sparsify_bitwise(name):
+    c = case(name)
+    spk = pf.sparsify(_pk(c))
+    np.testing.assert_array_equal(spk.sparse.indptr, c["sp/indptr"])
+    np.testing.assert_array_equal(spk.sparse.indices, c["sp/indices"])
+    assert I.sha(spk.sparse.data) == str(c["sp/sha_data"])
+    np.testing.assert_array_equal(spk.dropped_mass, c["sp/dropped"])
+    thr, cut, spct = c["sp/meta"]
+    assert spk.threshold == thr and spk.row_cut == cut
+    assert spk.sparsity_percent == pytest.approx(spct, abs=1e-12)
+    ok, err = rel_close(spk.log_sparse.data, np.log(spk.sparse.data), 1e-15)
+    assert ok, err
+    assert spk.log_dense.shape == spk.dense.shape
+    rep = spk.sparsity_report()
+    assert set(rep) == {"threshold", "sparsity_percent", "max_dropped_row_mass"}
+
+
+@pytest.mark.parametrize("name", SPARSE_CASES)
+@pytest.mark.parametrize("g", ["kl", "tv"])
+def test_sparse_field_matches_reference_pair_loop(name, g):
+    c = case(name)
+    spk = pf.sparsify(_pk(c))
+    fld = pf.dv_field_sparse(spk, pf.builtin_f(g), c.target)
+    ok, err = rel_close(fld.values, c[f"spfield/{g}"], RTOL)
+    assert ok, (name, g, err)
+
+
+@pytest.mark.parametrize("name", SPARSE_CASES)
+def test_sparse_pairs_and_ops(name):
+    c = case(name)
+    spk = pf.sparsify(_pk(c))
+    rng = np.random.default_rng(5)
+    for g in ("kl", "tv"):
+        fd = pf.builtin_f(g)
+        for q in rng.choice(c.n, 16, replace=False):
+            val, ops = pf.dv_pair_sparse_stats(spk, fd, c.target, int(q))
+            assert ops == int(c[f"spops/{g}"][q]), (g, q)
+            ok, err = rel_close([val], [c[f"spfield/{g}"][q]], RTOL)
+            assert ok, (g, q, err)
+    # q == p: KL exactly 0, TV exactly 2 * dropped_p (divergence.py:288-295)
+    assert pf.dv_pair_sparse(spk, pf.builtin_f("kl"), c.target, c.target) == 0.0
+    d = spk.dropped_mass[c.target]
+    assert pf.dv_pair_sparse(spk, pf.builtin_f("tv"), c.target, c.target) == d + d
+
+
+def test_zero_threshold_identity_and_validation():
+    c = case("disk40")
+    pk = _pk(c)
+    spk = pf.sparsify(pk, 0.0)
+    assert spk.sparsity_percent == 0.0 or spk.sparse.nnz == int((c.dense > 0).sum())
+    np.testing.assert_array_equal(spk.sparse.toarray(), np.where(c.dense > 0, c.dense, 0.0))
+    kl = pf.builtin_f("kl")
+    for q in (3, 500, 2000):
+        dense = pf.dv_pair(pk, kl, c.target, q)
+        assert pf.dv_pair_sparse(spk, kl, c.target, q) == pytest.approx(dense, rel=1e-12)
+    with pytest.raises(ValueError):
+        pf.sparsify(pk, 1.0)
+    with pytest.raises(ValueError):
+        pf.sparsify(pk, -0.5)
+    with pytest.raises(pf.DivergenceDomainError):
+        pf.dv_pair_sparse(pk, kl, 0, 1)
+
+
+def test_corridor_sparse_accuracy_and_bounds():
+    # reference test_divergence.py:207-250 restated on the device path
+    c = case("corridor50")
+    pk = _pk(c)
+    spk = pf.sparsify(pk)
+    assert spk.sparsity_percent > 80.0
+    kl, tv = pf.builtin_f("kl"), pf.builtin_f("tv")
+    rng = np.random.default_rng(7)
+    worst = 0.0
+    for _ in range(50):
+        p, q = (int(x) for x in rng.integers(0, c.n, 2))
+        if p == q:
+            continue
+        dense = pf.dv_pair(pk, kl, p, q)
+        sparse = pf.dv_pair_sparse(spk, kl, p, q)
+        if dense > 0:
+            worst = max(worst, abs(sparse - dense) / dense)
+        dt = pf.dv_pair(pk, tv, p, q)
+        st = pf.dv_pair_sparse(spk, tv, p, q)
+        assert abs(st - dt) <= 2 * (spk.dropped_mass[p] + spk.dropped_mass[q]) + 1e-12
+        _, ops = pf.dv_pair_sparse_stats(spk, kl, p, q)
+        assert ops < c.k
+    assert worst < 0.01
+
+
+def test_log_dense_view():
+    c = case("c1")
+    spk = pf.sparsify(_pk(c))
+    ld = np.asarray(spk.log_dense)
+    ok, err = rel_close(ld, np.log(np.maximum(c.dense, 1e-300)), 1e-15)
+    assert ok, err
+
+
+@pytest.mark.parametrize("n,k,thr", [(500, 64, None), (300, 1, None), (257, 33, 0.5), (64, 30001, None)])
+def test_synthetic_sparse_vs_oracle(n, k, thr):
+    rng = np.random.default_rng(n + k)
+    dense = I.synthetic_kernel(n, k, seed=n) ** 3
+    dense /= dense.sum(axis=1, keepdims=True)
+    dense[:, 0] = 0.0
+    boundary = np.array([1, 2]) if n > 2 else np.array([], np.int64)
+    pk = pf.PoissonKernel(dense, boundary, 0.0, 0.0)
+    spk = pf.sparsify(pk, thr)
+    sv = O.sparsify(dense, boundary, thr)
+    np.testing.assert_array_equal(spk.sparse.indptr, sv["indptr"])
+    np.testing.assert_array_equal(spk.sparse.indices, sv["indices"])
+    np.testing.assert_array_equal(spk.dropped_mass, sv["dropped"])
+    t = n // 3
+    for g in ("kl", "tv"):
+        got = pf.dv_field_sparse(spk, pf.builtin_f(g), t).values
+        ref = O.dv_field_sparse(sv, g, t)
+        ok, err = rel_close(got, ref, RTOL)
+        assert ok, (g, err)
