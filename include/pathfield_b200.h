@@ -193,6 +193,65 @@ int pf_csr_tv_f64(const int64_t *indptr, const int32_t *indices, const double *d
 int pf_log_clamped_f64(const double *P, int64_t ld, int64_t rows, int64_t k, double clamp,
                        double *out, pf_stream_t stream);
 
+/* ---- K8: batched triangle-descent tracer (paths.py:101-307) ---------------
+ * Device-resident mesh topology (all arrays device pointers):
+ *   vertices  (n,2) FP64;  triangles (nt,3) int32 CCW exactly as stored by
+ *   TriMesh (mesh.py:57-68);  areas (nt) = TriMesh.triangle_areas;
+ *   tri_nbr (nt,3) int32: the triangle across the edge opposite each slot, -1
+ *   on the boundary (edge_adjacency, mesh.py:113-126);  vt_ptr/vt_idx: the
+ *   ascending incident triangles of each vertex (vertex_triangles);
+ *   nb_ptr/nb_idx: ascending neighbours (neighbors);
+ *   eps_prog = 1e-14 * bbox_diagonal (paths.py:143). */
+typedef struct {
+  const double *vertices;
+  const int32_t *triangles;
+  const double *areas;
+  const int32_t *tri_nbr;
+  const int64_t *vt_ptr;
+  const int32_t *vt_idx;
+  const int64_t *nb_ptr;
+  const int32_t *nb_idx;
+  int64_t n;
+  int64_t nt;
+  double eps_prog;
+} pf_mesh_t;
+
+/* Path output: location l of path p is at index p*cap + l:
+ *   kind 0 = ("vertex", i), 1 = ("edge", i, j, t); (x, y) the polyline point.
+ * count[p] = number of locations (may exceed cap: then only the first cap
+ * are written and the caller re-runs p with a larger buffer); status[p]:
+ * 0 reached, 1 stuck, 2 max-steps-exceeded (paths.py:27-29); stuck[p] the
+ * stuck vertex or -1. */
+typedef struct {
+  int8_t *kind;
+  int32_t *i;
+  int32_t *j;
+  double *t;
+  double *x;
+  double *y;
+  int64_t cap;
+  int64_t *count;
+  int32_t *status;
+  int64_t *stuck;
+} pf_paths_t;
+
+/* Trace npaths paths: path p descends field field_of[p] (fields is
+ * nfields x n FP64, row f = field f; field_of NULL = field 0) from
+ * sources[p] toward targets[field_of[p]], at most step_cap state transitions
+ * (settings.step_cap_factor * n).  Replaces triangle_descent (paths.py:292-307)
+ * for a batch of sources; FP64 rounding follows the reference bit for bit. */
+int pf_trace_batch_f64(const pf_mesh_t *mesh, const double *fields, const int64_t *targets,
+                       const int64_t *sources, const int32_t *field_of, int64_t npaths,
+                       int64_t step_cap, const pf_paths_t *out, pf_stream_t stream);
+
+/* triangle_gradient (paths.py:113-121) for a batch of triangle ids: out (ntri,2). */
+int pf_triangle_gradient_f64(const pf_mesh_t *mesh, const double *vals, const int64_t *tris,
+                             int64_t ntri, double *out, pf_stream_t stream);
+
+/* np.hypot as the tracer evaluates it (glibc non-FMA kernel), elementwise. */
+int pf_np_hypot_f64(const double *x, const double *y, int64_t n, double *out,
+                    pf_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

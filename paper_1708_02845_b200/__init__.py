@@ -10,6 +10,9 @@ from .config import DEFAULTS, Settings
 from .divergence import (FDivergence, builtin_f, dv_at, dv_field,
                          dv_field_device, dv_field_sparse, dv_pair,
                          dv_pair_sparse, dv_pair_sparse_stats, sparsify)
+from .mesh import TriMesh
+from .paths import (TracedPath, triangle_descent, triangle_descent_batch,
+                    triangle_gradient)
 from .errors import (DivergenceDomainError, InvalidTargetError, NativeError,
                      PathfieldError)
 from .solvers import PoissonKernel, ScalarField
@@ -19,6 +22,7 @@ __version__ = "0.1.0"
 __all__ = [
     "DEFAULTS", "Settings", "FDivergence", "builtin_f", "dv_at", "dv_field",
     "dv_field_device", "dv_pair", "sparsify", "dv_pair_sparse", "dv_pair_sparse_stats",
-    "dv_field_sparse", "DivergenceDomainError", "InvalidTargetError",
+    "dv_field_sparse", "TriMesh", "TracedPath", "triangle_descent", "triangle_descent_batch",
+    "triangle_gradient", "DivergenceDomainError", "InvalidTargetError",
     "NativeError", "PathfieldError", "PoissonKernel", "ScalarField",
 ]

@@ -51,15 +51,13 @@ _SIGS = {
     "pf_csr_tv_f64": [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_i64,
                       c_vp, c_vp, c_vp],
     "pf_log_clamped_f64": [c_vp, c_i64, c_i64, c_i64, c_dbl, c_vp, c_vp],
+    # struct arguments (pf_mesh_t*, pf_paths_t*) are passed as addresses
+    "pf_trace_batch_f64": [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp],
+    "pf_triangle_gradient_f64": [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp],
+    "pf_np_hypot_f64": [c_vp, c_vp, c_i64, c_vp, c_vp],
 }
 _RESTYPES = {"pf_last_error": ctypes.c_char_p}
 
-
-def register(name: str, argtypes, restype=ctypes.c_int) -> None:
-    """Declare an additional entry point (used by later kernel modules)."""
-    _SIGS[name] = list(argtypes)
-    if restype is not ctypes.c_int:
-        _RESTYPES[name] = restype
 
 
 def load():

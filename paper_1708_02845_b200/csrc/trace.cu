@@ -1,0 +1,447 @@
+// trace.cu — batched triangle-descent path tracer (K8).
+//
+// Reference: pathfield/paths.py:101-307 (triangle_gradient, _Tracer,
+// triangle_descent).  One thread advances one (source, field) path through
+// the state machine over a device-resident triangle adjacency; thousands of
+// paths run per launch.  The kernel reproduces the reference's FP64 rounding
+// exactly so that the location sequence (triangle/edge/vertex decisions) is
+// bit-identical:
+//   * this file is compiled with -fmad=false: no implicit contraction;
+//   * the only fused multiply-adds are where numpy's OpenBLAS kernels fuse
+//     (re-probed in tests): f @ G and lam @ V as
+//     fma(x2,y2, fma(x1,y1, x0*y0)), G @ d as fma(G_i0,d0, G_i1*d1), the 3-dot
+//     lam @ f as fma(l2,f2, fma(l1,f1, l0*f0));
+//   * np.hypot is glibc 2.39's non-FMA correction kernel, restated below
+//     (CUDA's hypot rounds differently);
+//   * 3-element sums are ((a+b)+c) (numpy reduce), ties break on the lowest
+//     index exactly where the reference's argmax/min/strict-< do.
+#include <cmath>
+
+#include "pf_common.cuh"
+
+namespace pf {
+
+constexpr int kTraceThreads = 128;
+
+// ---------------------------------------------------------------- hypot --
+// glibc sysdeps/ieee754/dbl-64/e_hypot.c (non-FMA kernel); SURVEY A.3.
+__device__ __forceinline__ double hypot_kernel(double ax, double ay) {
+  double h = __dsqrt_rn(__dadd_rn(__dmul_rn(ax, ax), __dmul_rn(ay, ay)));
+  double t1, t2;
+  if (h <= __dmul_rn(2.0, ay)) {
+    const double delta = __dsub_rn(h, ay);
+    t1 = __dmul_rn(ax, __dsub_rn(__dmul_rn(2.0, delta), ax));
+    t2 = __dmul_rn(__dsub_rn(delta, __dmul_rn(2.0, __dsub_rn(ax, ay))), delta);
+  } else {
+    const double delta = __dsub_rn(h, ax);
+    t1 = __dmul_rn(__dmul_rn(2.0, delta), __dsub_rn(ax, __dmul_rn(2.0, ay)));
+    t2 = __dadd_rn(__dmul_rn(__dsub_rn(__dmul_rn(4.0, delta), ay), ay), __dmul_rn(delta, delta));
+  }
+  return __dsub_rn(h, __ddiv_rn(__dadd_rn(t1, t2), __dmul_rn(2.0, h)));
+}
+
+__device__ double np_hypot(double x, double y) {
+  if (!isfinite(x) || !isfinite(y)) {
+    if (isinf(x) || isinf(y)) return INFINITY;
+    return x + y;
+  }
+  x = fabs(x);
+  y = fabs(y);
+  double ax = x < y ? y : x;
+  double ay = x < y ? x : y;
+  const double kLarge = 0x1p+511, kTiny = 0x1p-511, kEps = 0x1p-54, kScale = 0x1p-600;
+  if (ax > kLarge) {
+    if (ay <= __dmul_rn(ax, kEps)) return __dadd_rn(ax, ay);
+    return __ddiv_rn(hypot_kernel(__dmul_rn(ax, kScale), __dmul_rn(ay, kScale)), kScale);
+  }
+  if (ay < kTiny) {
+    if (ax >= __ddiv_rn(ay, kEps)) return __dadd_rn(ax, ay);
+    return __dmul_rn(hypot_kernel(__ddiv_rn(ax, kScale), __ddiv_rn(ay, kScale)), kScale);
+  }
+  if (ay <= __dmul_rn(ax, kEps)) return __dadd_rn(ax, ay);
+  return hypot_kernel(ax, ay);
+}
+
+// ----------------------------------------------------------- geometry --
+struct Tri {
+  int v[3];
+  double G[3][2];  // barycentric gradients (paths.py:105-110)
+};
+
+__device__ __forceinline__ void load_tri(const pf_mesh_t &m, int64_t ti, Tri &t) {
+  t.v[0] = m.triangles[3 * ti + 0];
+  t.v[1] = m.triangles[3 * ti + 1];
+  t.v[2] = m.triangles[3 * ti + 2];
+  const double ax = m.vertices[2 * t.v[0]], ay = m.vertices[2 * t.v[0] + 1];
+  const double bx = m.vertices[2 * t.v[1]], by = m.vertices[2 * t.v[1] + 1];
+  const double cx = m.vertices[2 * t.v[2]], cy = m.vertices[2 * t.v[2] + 1];
+  const double area2 = __dmul_rn(2.0, m.areas[ti]);
+  // _perp(v) = [-v[1], v[0]];  rows: perp(pc-pb), perp(pa-pc), perp(pb-pa); / area2
+  t.G[0][0] = __ddiv_rn(-__dsub_rn(cy, by), area2);
+  t.G[0][1] = __ddiv_rn(__dsub_rn(cx, bx), area2);
+  t.G[1][0] = __ddiv_rn(-__dsub_rn(ay, cy), area2);
+  t.G[1][1] = __ddiv_rn(__dsub_rn(ax, cx), area2);
+  t.G[2][0] = __ddiv_rn(-__dsub_rn(by, ay), area2);
+  t.G[2][1] = __ddiv_rn(__dsub_rn(bx, ax), area2);
+}
+
+// f @ G  (3,)@(3,2): fma(f2,G2j, fma(f1,G1j, f0*G0j))
+__device__ __forceinline__ void gradient(const Tri &t, const double *vals, double g[2]) {
+  const double f0 = vals[t.v[0]], f1 = vals[t.v[1]], f2 = vals[t.v[2]];
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+    g[j] = __fma_rn(f2, t.G[2][j], __fma_rn(f1, t.G[1][j], __dmul_rn(f0, t.G[0][j])));
+}
+
+// G @ d  (3,2)@(2,): fma(G_i0, d0, G_i1*d1); returns scale = max|dl| + 1e-300
+__device__ __forceinline__ double dlam_of(const Tri &t, const double d[2], double dl[3]) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i) dl[i] = __fma_rn(t.G[i][0], d[0], __dmul_rn(t.G[i][1], d[1]));
+  double mx = fabs(dl[0]);
+  if (fabs(dl[1]) > mx) mx = fabs(dl[1]);
+  if (fabs(dl[2]) > mx) mx = fabs(dl[2]);
+  return __dadd_rn(mx, 1e-300);
+}
+
+// ------------------------------------------------------------- output --
+struct Writer {
+  const pf_paths_t *o;
+  int64_t path, count;
+  double lx, ly;  // pts[-1]
+  __device__ void put(int kind, int64_t i, int64_t j, double t, double x, double y) {
+    if (count < o->cap) {
+      const int64_t at = path * o->cap + count;
+      o->kind[at] = static_cast<int8_t>(kind);
+      o->i[at] = static_cast<int32_t>(i);
+      o->j[at] = static_cast<int32_t>(j);
+      o->t[at] = t;
+      o->x[at] = x;
+      o->y[at] = y;
+    }
+    ++count;
+    lx = x;
+    ly = y;
+  }
+};
+
+// np.argmin(np.hypot(V - x)) : first minimum (paths.py:287-289)
+__device__ int64_t nearest_vertex(const pf_mesh_t &m, double x, double y) {
+  int64_t best = 0;
+  double bd = INFINITY;
+  for (int64_t v = 0; v < m.n; ++v) {
+    const double d = np_hypot(__dsub_rn(m.vertices[2 * v], x), __dsub_rn(m.vertices[2 * v + 1], y));
+    if (d < bd) {  // strict: the first minimum wins
+      bd = d;
+      best = v;
+    }
+  }
+  return best;
+}
+
+enum { ST_REACHED = 0, ST_STUCK = 1, ST_MAX = 2 };
+
+__global__ void __launch_bounds__(kTraceThreads) trace_kernel(pf_mesh_t m, const double *fields,
+                                                              const int64_t *targets,
+                                                              const int64_t *sources,
+                                                              const int32_t *field_of,
+                                                              int64_t npaths, int64_t cap,
+                                                              pf_paths_t out) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= npaths) return;
+  const int64_t fi = field_of ? field_of[p] : 0;
+  const double *vals = fields + fi * m.n;
+  const int64_t target = targets[fi];
+  const int64_t source = sources[p];
+  const double eps_prog = m.eps_prog;
+
+  Writer w{&out, p, 0, 0.0, 0.0};
+  w.put(0, source, -1, 0.0, m.vertices[2 * source], m.vertices[2 * source + 1]);
+
+  bool in_tri = false;
+  int64_t v = source, ti = -1;
+  double x0 = 0.0, x1 = 0.0, cur = 0.0;
+  int status = ST_MAX;
+  int64_t stuck = -1;
+
+  for (int64_t it = 0; it < cap; ++it) {
+    if (!in_tri) {
+      // ---------------- vertex rule (paths.py:162-196)
+      if (v == target) {
+        status = ST_REACHED;
+        break;
+      }
+      double best_norm = 0.0;
+      int64_t best = -1;
+      for (int64_t e = m.vt_ptr[v]; e < m.vt_ptr[v + 1]; ++e) {
+        const int64_t tj = m.vt_idx[e];
+        Tri t;
+        load_tri(m, tj, t);
+        double g[2];
+        gradient(t, vals, g);
+        const double norm = np_hypot(g[0], g[1]);
+        if (norm <= 0.0) continue;
+        const double d[2] = {__ddiv_rn(-g[0], norm), __ddiv_rn(-g[1], norm)};
+        const int slot = (t.v[0] == v) ? 0 : (t.v[1] == v ? 1 : 2);
+        double dl[3];
+        const double scale = dlam_of(t, d, dl);
+        const int o0 = slot == 0 ? 1 : 0, o1 = slot == 2 ? 1 : 2;
+        const double thr = __dmul_rn(1e-12, scale);
+        if (dl[o0] > thr && dl[o1] > thr) {
+          if (best < 0 || norm > best_norm) {
+            best_norm = norm;
+            best = tj;
+          }
+        }
+      }
+      if (best >= 0) {
+        in_tri = true;
+        ti = best;
+        x0 = m.vertices[2 * v];
+        x1 = m.vertices[2 * v + 1];
+        cur = vals[v];
+        continue;
+      }
+      // steepest incident edge
+      const double vx = m.vertices[2 * v], vy = m.vertices[2 * v + 1], fv = vals[v];
+      double bs = 0.0;
+      int64_t bu = -1;
+      for (int64_t e = m.nb_ptr[v]; e < m.nb_ptr[v + 1]; ++e) {
+        const int64_t u = m.nb_idx[e];
+        const double diff = __dsub_rn(fv, vals[u]);
+        const double len =
+            np_hypot(__dsub_rn(m.vertices[2 * u], vx), __dsub_rn(m.vertices[2 * u + 1], vy));
+        const double slope = __ddiv_rn(diff, len);
+        if (bu < 0 || slope > bs) {
+          bs = slope;
+          bu = u;
+        }
+      }
+      if (bu < 0 || bs <= 0.0) {
+        status = ST_STUCK;
+        stuck = v;
+        break;
+      }
+      w.put(0, bu, -1, 0.0, m.vertices[2 * bu], m.vertices[2 * bu + 1]);
+      v = bu;
+      continue;
+    }
+
+    // ---------------- triangle rule (paths.py:200-254)
+    Tri t;
+    load_tri(m, ti, t);
+    double g[2];
+    gradient(t, vals, g);
+    const double norm = np_hypot(g[0], g[1]);
+    bool slide_best = norm <= 0.0;
+    double lam[3], dl[3], s_exit = INFINITY;
+    int slot_exit = -1;
+    if (!slide_best) {
+      const double d[2] = {__ddiv_rn(-g[0], norm), __ddiv_rn(-g[1], norm)};
+      const double ax = m.vertices[2 * t.v[0]], ay = m.vertices[2 * t.v[0] + 1];
+      const double bx = m.vertices[2 * t.v[1]], by = m.vertices[2 * t.v[1] + 1];
+      const double cx = m.vertices[2 * t.v[2]], cy = m.vertices[2 * t.v[2] + 1];
+      const double area2 = __dmul_rn(2.0, m.areas[ti]);
+      // _cross2(u, w) = u0*w1 - u1*w0 (paths.py:124-134)
+      const double la = __ddiv_rn(__dsub_rn(__dmul_rn(__dsub_rn(cx, bx), __dsub_rn(x1, by)),
+                                            __dmul_rn(__dsub_rn(cy, by), __dsub_rn(x0, bx))),
+                                  area2);
+      const double lb = __ddiv_rn(__dsub_rn(__dmul_rn(__dsub_rn(ax, cx), __dsub_rn(x1, cy)),
+                                            __dmul_rn(__dsub_rn(ay, cy), __dsub_rn(x0, cx))),
+                                  area2);
+      lam[0] = la;
+      lam[1] = lb;
+      lam[2] = __dsub_rn(__dsub_rn(1.0, la), lb);
+#pragma unroll
+      for (int s = 0; s < 3; ++s) lam[s] = lam[s] < 0.0 ? 0.0 : lam[s];  // np.clip(., 0)
+      const double sum = __dadd_rn(__dadd_rn(lam[0], lam[1]), lam[2]);
+#pragma unroll
+      for (int s = 0; s < 3; ++s) lam[s] = __ddiv_rn(lam[s], sum);
+      const double scale = dlam_of(t, d, dl);
+      const double thr = __dmul_rn(-1e-14, scale);
+#pragma unroll
+      for (int s = 0; s < 3; ++s) {
+        if (dl[s] < thr && lam[s] > 0.0) {
+          const double cand = __ddiv_rn(lam[s], -dl[s]);
+          if (cand < s_exit) {
+            s_exit = cand;
+            slot_exit = s;
+          }
+        }
+      }
+      slide_best = !isfinite(s_exit);
+    }
+    if (slide_best) {
+      // _slide_to_best_vertex (paths.py:276-282): min by (value, index)
+      int64_t bw = t.v[0];
+#pragma unroll
+      for (int s = 1; s < 3; ++s) {
+        const int64_t u = t.v[s];
+        if (vals[u] < vals[bw] || (vals[u] == vals[bw] && u < bw)) bw = u;
+      }
+      if (vals[bw] >= cur) {
+        status = ST_STUCK;
+        stuck = bw;
+        break;
+      }
+      w.put(0, bw, -1, 0.0, m.vertices[2 * bw], m.vertices[2 * bw + 1]);
+      in_tri = false;
+      v = bw;
+      continue;
+    }
+    double le[3];
+#pragma unroll
+    for (int s = 0; s < 3; ++s) le[s] = __dadd_rn(lam[s], __dmul_rn(s_exit, dl[s]));
+    le[slot_exit] = 0.0;
+#pragma unroll
+    for (int s = 0; s < 3; ++s) le[s] = le[s] < 0.0 ? 0.0 : le[s];
+    const double lsum = __dadd_rn(__dadd_rn(le[0], le[1]), le[2]);
+#pragma unroll
+    for (int s = 0; s < 3; ++s) le[s] = __ddiv_rn(le[s], lsum);
+    int hi = 0;
+    if (le[1] > le[hi]) hi = 1;
+    if (le[2] > le[hi]) hi = 2;
+    if (le[hi] > 1.0 - 1e-12) {
+      // exit through a vertex
+      const int64_t wv = t.v[hi];
+      const double wx = m.vertices[2 * wv], wy = m.vertices[2 * wv + 1];
+      if (!(np_hypot(__dsub_rn(wx, w.lx), __dsub_rn(wy, w.ly)) >= eps_prog)) {
+        status = ST_STUCK;
+        stuck = nearest_vertex(m, x0, x1);
+        break;
+      }
+      w.put(0, wv, -1, 0.0, wx, wy);
+      in_tri = false;
+      v = wv;
+      continue;
+    }
+    int o0 = slot_exit == 0 ? 1 : 0, o1 = slot_exit == 2 ? 1 : 2;
+    int64_t ei = t.v[o0], ej = t.v[o1];
+    if (ei > ej) {
+      const int64_t tmp = ei;
+      ei = ej;
+      ej = tmp;
+      const int to = o0;
+      o0 = o1;
+      o1 = to;
+    }
+    const double tpar = le[o1];
+    // lam_exit @ V[tri]  (3,)@(3,2)
+    const double xe0 = __fma_rn(le[2], m.vertices[2 * t.v[2]],
+                                __fma_rn(le[1], m.vertices[2 * t.v[1]],
+                                         __dmul_rn(le[0], m.vertices[2 * t.v[0]])));
+    const double xe1 = __fma_rn(le[2], m.vertices[2 * t.v[2] + 1],
+                                __fma_rn(le[1], m.vertices[2 * t.v[1] + 1],
+                                         __dmul_rn(le[0], m.vertices[2 * t.v[0] + 1])));
+    if (!(np_hypot(__dsub_rn(xe0, w.lx), __dsub_rn(xe1, w.ly)) >= eps_prog)) {
+      status = ST_STUCK;
+      stuck = nearest_vertex(m, x0, x1);
+      break;
+    }
+    w.put(1, ei, ej, tpar, xe0, xe1);
+    // lam_exit @ vals[tri]  (3,)@(3,)
+    const double val_exit = __fma_rn(le[2], vals[t.v[2]],
+                                     __fma_rn(le[1], vals[t.v[1]], __dmul_rn(le[0], vals[t.v[0]])));
+    if (target == ei || target == ej) {
+      w.put(0, target, -1, 0.0, m.vertices[2 * target], m.vertices[2 * target + 1]);
+      status = ST_REACHED;
+      break;
+    }
+    const int64_t nt = m.tri_nbr[3 * ti + slot_exit];
+    bool enters = false;
+    if (nt >= 0) {
+      // _enters (paths.py:256-266)
+      Tri u;
+      load_tri(m, nt, u);
+      double gu[2];
+      gradient(u, vals, gu);
+      const double nu = np_hypot(gu[0], gu[1]);
+      if (nu > 0.0) {
+        const double du[2] = {__ddiv_rn(-gu[0], nu), __ddiv_rn(-gu[1], nu)};
+        int so = 0;
+        for (int s = 0; s < 3; ++s)
+          if (u.v[s] != ei && u.v[s] != ej) so = s;
+        double dlu[3];
+        const double sc = dlam_of(u, du, dlu);
+        enters = dlu[so] > __dmul_rn(1e-12, sc);
+      }
+    }
+    if (enters) {
+      ti = nt;
+      x0 = xe0;
+      x1 = xe1;
+      cur = val_exit;
+      continue;
+    }
+    // _slide_along_edge (paths.py:268-274); stuck-vertex reference point is
+    // the entry point for a boundary edge, the exit point otherwise.
+    const double rx = nt < 0 ? x0 : xe0, ry = nt < 0 ? x1 : xe1;
+    const int64_t sw = (vals[ej] < vals[ei]) ? ej : ei;
+    if (vals[sw] >= val_exit) {
+      status = ST_STUCK;
+      stuck = nearest_vertex(m, rx, ry);
+      break;
+    }
+    w.put(0, sw, -1, 0.0, m.vertices[2 * sw], m.vertices[2 * sw + 1]);
+    in_tri = false;
+    v = sw;
+  }
+  out.count[p] = w.count;
+  out.status[p] = status;
+  out.stuck[p] = stuck;
+}
+
+// triangle_gradient for a batch of triangles (paths.py:113-121)
+__global__ void tri_gradient_kernel(pf_mesh_t m, const double *vals, const int64_t *tris,
+                                    int64_t ntri, double *out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= ntri) return;
+  Tri t;
+  load_tri(m, tris[i], t);
+  double g[2];
+  gradient(t, vals, g);
+  out[2 * i] = g[0];
+  out[2 * i + 1] = g[1];
+}
+
+__global__ void hypot_kernel_batch(const double *x, const double *y, int64_t n, double *out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = np_hypot(x[i], y[i]);
+}
+
+}  // namespace pf
+
+using namespace pf;
+
+extern "C" {
+
+int pf_trace_batch_f64(const pf_mesh_t *mesh, const double *fields, const int64_t *targets,
+                       const int64_t *sources, const int32_t *field_of, int64_t npaths,
+                       int64_t step_cap, const pf_paths_t *out, pf_stream_t stream) {
+  if (!mesh || !fields || !targets || !sources || !out) return fail(PF_E_ARG, "trace: null");
+  if (npaths <= 0) return 0;
+  if (!out->count || !out->status || !out->stuck) return fail(PF_E_ARG, "trace: null outputs");
+  const int64_t blocks = (npaths + kTraceThreads - 1) / kTraceThreads;
+  trace_kernel<<<static_cast<unsigned>(blocks), kTraceThreads, 0, as_stream(stream)>>>(
+      *mesh, fields, targets, sources, field_of, npaths, step_cap, *out);
+  return check_launch("trace");
+}
+
+int pf_triangle_gradient_f64(const pf_mesh_t *mesh, const double *vals, const int64_t *tris,
+                             int64_t ntri, double *out, pf_stream_t stream) {
+  if (!mesh || !vals || !tris || !out) return fail(PF_E_ARG, "triangle_gradient: null");
+  if (ntri <= 0) return 0;
+  tri_gradient_kernel<<<static_cast<unsigned>((ntri + 127) / 128), 128, 0, as_stream(stream)>>>(
+      *mesh, vals, tris, ntri, out);
+  return check_launch("triangle_gradient");
+}
+
+int pf_np_hypot_f64(const double *x, const double *y, int64_t n, double *out,
+                    pf_stream_t stream) {
+  if (n <= 0) return 0;
+  if (!x || !y || !out) return fail(PF_E_ARG, "np_hypot: null");
+  hypot_kernel_batch<<<static_cast<unsigned>((n + 255) / 256), 256, 0, as_stream(stream)>>>(
+      x, y, n, out);
+  return check_launch("np_hypot");
+}
+
+}  // extern "C"

@@ -1,0 +1,230 @@
+"""Triangle-descent path tracing on the B200 — mirror of ``pathfield/paths.py``.
+
+* :func:`triangle_descent` (paths.py:292-307): same signature, same
+  :class:`TracedPath` (points, locations, source, target, status,
+  stuck_vertex), same statuses; runs the K8 kernel for one source.
+* :func:`triangle_descent_batch` (additive): many sources, one
+  or many fields, one launch; equal to per-source ``triangle_descent``.
+* :func:`triangle_gradient` (paths.py:113-121) on the device.
+
+The location sequence is bit-identical to the reference given the same field
+(the kernel follows numpy's rounding, see csrc/trace.cu).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _device as dev
+from . import _native as nat
+from .config import DEFAULTS, Settings
+from .errors import DegenerateGeometryError, InvalidTargetError
+from .mesh import device_mesh
+from .solvers import ScalarField
+
+STATUS_REACHED = "reached"
+STATUS_STUCK = "stuck"
+STATUS_MAX_STEPS = "max-steps-exceeded"
+_STATUS = {0: STATUS_REACHED, 1: STATUS_STUCK, 2: STATUS_MAX_STEPS}
+
+
+@dataclass(frozen=True)
+class TracedPath:
+    """A polyline of mesh-located points from source toward target (paths.py:32-55)."""
+
+    points: np.ndarray
+    locations: list
+    source: int
+    target: int
+    status: str
+    stuck_vertex: int | None = None
+
+    def __post_init__(self):
+        self.points.setflags(write=False)
+
+    @property
+    def length(self) -> float:
+        if len(self.points) < 2:
+            return 0.0
+        d = np.diff(self.points, axis=0)
+        return float(np.hypot(d[:, 0], d[:, 1]).sum())
+
+    @property
+    def reached(self) -> bool:
+        return self.status == STATUS_REACHED
+
+
+class PfPaths(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_void_p), ("i", ctypes.c_void_p), ("j", ctypes.c_void_p),
+                ("t", ctypes.c_void_p), ("x", ctypes.c_void_p), ("y", ctypes.c_void_p),
+                ("cap", ctypes.c_int64), ("count", ctypes.c_void_p),
+                ("status", ctypes.c_void_p), ("stuck", ctypes.c_void_p)]
+
+
+def _byref(s):
+    return ctypes.addressof(s)
+
+
+class PathBuffers:
+    """Device output of one tracer launch (pf_paths_t) and its host copy."""
+
+    def __init__(self, t, npaths: int, cap: int, device):
+        self.cap = cap
+        tot = max(npaths * cap, 1)
+        self.kind = t.empty(tot, dtype=t.int8, device=device)
+        self.i = t.empty(tot, dtype=t.int32, device=device)
+        self.j = t.empty(tot, dtype=t.int32, device=device)
+        self.t = t.empty(tot, dtype=t.float64, device=device)
+        self.x = t.empty(tot, dtype=t.float64, device=device)
+        self.y = t.empty(tot, dtype=t.float64, device=device)
+        self.count = t.empty(max(npaths, 1), dtype=t.int64, device=device)
+        self.status = t.empty(max(npaths, 1), dtype=t.int32, device=device)
+        self.stuck = t.empty(max(npaths, 1), dtype=t.int64, device=device)
+        self.struct = PfPaths(self.kind.data_ptr(), self.i.data_ptr(), self.j.data_ptr(),
+                              self.t.data_ptr(), self.x.data_ptr(), self.y.data_ptr(), cap,
+                              self.count.data_ptr(), self.status.data_ptr(),
+                              self.stuck.data_ptr())
+
+
+def _fields_to_device(t, fields, n, device):
+    """Stack field values (numpy or device tensors) into an (F, n) FP64 device tensor."""
+    vals = []
+    for f in fields:
+        v = f.values if hasattr(f, "values") else f
+        if hasattr(v, "is_cuda"):
+            vals.append(v.to(device=device, dtype=t.float64).reshape(-1)[:n])
+        else:
+            vals.append(t.from_numpy(np.ascontiguousarray(v, dtype=np.float64)).to(device))
+    return t.stack(vals) if len(vals) > 1 else vals[0].reshape(1, -1).contiguous()
+
+
+def trace_arrays(mesh, fields, targets, sources, field_of=None, settings: Settings = DEFAULTS,
+                 cap: int | None = None):
+    """Launch K8 and return the raw device outputs (PathBuffers), rerunning overflows.
+
+    `fields` is a list of field values (numpy or device tensors), `targets`
+    their targets, `sources` the start vertices, `field_of[p]` the field of path p.
+    """
+    t = dev.require_cuda()
+    dm = device_mesh(mesh)
+    sources = np.asarray(sources, dtype=np.int64)
+    npaths = sources.size
+    targets = np.asarray(targets, dtype=np.int64)
+    fo = None if field_of is None else np.asarray(field_of, dtype=np.int32)
+    step_cap = int(settings.step_cap_factor) * dm.n
+    F = _fields_to_device(t, fields, dm.n, dm.device)
+    src_d = t.from_numpy(sources).to(dm.device)
+    tgt_d = t.from_numpy(targets).to(dm.device)
+    fo_d = None if fo is None else t.from_numpy(fo).to(dm.device)
+    s = t.cuda.current_stream(dm.device).cuda_stream
+    if cap is None:
+        cap = int(min(step_cap + 2, max(64, 8 * int(np.sqrt(dm.n)) + 64)))
+    buf = PathBuffers(t, npaths, cap, dm.device)
+    nat.call("pf_trace_batch_f64", _byref(dm.struct), F.data_ptr(), tgt_d.data_ptr(),
+             src_d.data_ptr(), nat.ptr(fo_d), npaths, step_cap, _byref(buf.struct), s)
+    counts = buf.count.cpu().numpy()
+    over = np.flatnonzero(counts > cap)
+    extra = None
+    if over.size:
+        cap2 = int(counts[over].max())
+        sub_src = t.from_numpy(sources[over]).to(dm.device)
+        sub_fo = None if fo is None else t.from_numpy(fo[over]).to(dm.device)
+        extra = PathBuffers(t, over.size, cap2, dm.device)
+        nat.call("pf_trace_batch_f64", _byref(dm.struct), F.data_ptr(), tgt_d.data_ptr(),
+                 sub_src.data_ptr(), nat.ptr(sub_fo), over.size, step_cap,
+                 _byref(extra.struct), s)
+    return buf, counts, over, extra
+
+
+def _host_paths(buf, counts, over, extra, sources, targets, field_of):
+    kind = buf.kind.cpu().numpy()
+    ii = buf.i.cpu().numpy()
+    jj = buf.j.cpu().numpy()
+    tt = buf.t.cpu().numpy()
+    xx = buf.x.cpu().numpy()
+    yy = buf.y.cpu().numpy()
+    status = buf.status.cpu().numpy()
+    stuck = buf.stuck.cpu().numpy()
+    where = {int(p): r for r, p in enumerate(over)}
+    if extra is not None:
+        ek, ei, ej = extra.kind.cpu().numpy(), extra.i.cpu().numpy(), extra.j.cpu().numpy()
+        et, ex, ey = extra.t.cpu().numpy(), extra.x.cpu().numpy(), extra.y.cpu().numpy()
+    out = []
+    for p in range(len(sources)):
+        c = int(counts[p])
+        if p in where:
+            r = where[p]
+            a = r * extra.cap
+            K, I_, J, T_, X, Y = ek[a:a + c], ei[a:a + c], ej[a:a + c], et[a:a + c], ex[a:a + c], ey[a:a + c]
+        else:
+            a = p * buf.cap
+            K, I_, J, T_, X, Y = kind[a:a + c], ii[a:a + c], jj[a:a + c], tt[a:a + c], xx[a:a + c], yy[a:a + c]
+        locs = [("vertex", int(I_[q])) if K[q] == 0 else ("edge", int(I_[q]), int(J[q]), float(T_[q]))
+                for q in range(c)]
+        pts = np.column_stack([X, Y]).astype(np.float64, copy=True)
+        fi = 0 if field_of is None else int(field_of[p])
+        st = _STATUS[int(status[p])]
+        sv = int(stuck[p]) if st == STATUS_STUCK else None
+        out.append(TracedPath(pts, locs, int(sources[p]), int(targets[fi]), st, sv))
+    return out
+
+
+def triangle_descent_batch(mesh, fields, sources, settings: Settings = DEFAULTS,
+                           field_of=None) -> list[TracedPath]:
+    """Trace many sources in one launch; path p descends fields[field_of[p]].
+
+    ``fields`` is one ScalarField or a list of them (their ``target`` is the
+    destination); ``field_of`` defaults to field 0 for every path.  Equal to
+    ``[triangle_descent(mesh, fields[field_of[p]], sources[p]) for p]``.
+    """
+    if isinstance(fields, ScalarField) or hasattr(fields, "target"):
+        fields = [fields]
+    fields = list(fields)
+    targets = np.array([int(f.target) for f in fields], dtype=np.int64)
+    sources = np.asarray(sources, dtype=np.int64).reshape(-1)
+    fo = None if field_of is None else np.asarray(field_of, dtype=np.int64).reshape(-1)
+    ft = targets[fo] if fo is not None else np.full(sources.size, targets[0])
+    if np.any(sources == ft):
+        raise InvalidTargetError("source equals target")
+    n = len(mesh.vertices)
+    if sources.size and (sources.min() < 0 or sources.max() >= n):
+        raise InvalidTargetError("source out of range")
+    buf, counts, over, extra = trace_arrays(mesh, fields, targets, sources, fo, settings)
+    return _host_paths(buf, counts, over, extra, sources, targets, fo)
+
+
+def triangle_descent(mesh, field: ScalarField, source: int,
+                     settings: Settings = DEFAULTS) -> TracedPath:
+    """Trace the negative interpolant gradient through triangle interiors (paths.py:292-307)."""
+    if source == field.target:
+        raise InvalidTargetError("source equals target")
+    return triangle_descent_batch(mesh, [field], [int(source)], settings)[0]
+
+
+def triangle_gradient(mesh, field_values, ti: int) -> np.ndarray:
+    """Gradient of the linear interpolant on triangle ti (paths.py:113-121), on the device."""
+    if mesh.triangle_areas[ti] <= 0:
+        raise DegenerateGeometryError(f"triangle {ti} is degenerate")
+    t = dev.require_cuda()
+    dm = device_mesh(mesh)
+    vals = field_values.values if isinstance(field_values, ScalarField) else field_values
+    F = _fields_to_device(t, [vals], dm.n, dm.device)
+    tri = t.tensor([int(ti)], dtype=t.int64, device=dm.device)
+    out = t.empty(2, dtype=t.float64, device=dm.device)
+    nat.call("pf_triangle_gradient_f64", _byref(dm.struct), F.data_ptr(), tri.data_ptr(), 1,
+             out.data_ptr(), t.cuda.current_stream(dm.device).cuda_stream)
+    return out.cpu().numpy()
+
+
+def np_hypot_device(x, y) -> np.ndarray:
+    """The tracer's hypot (glibc non-FMA kernel) evaluated on the device (testing aid)."""
+    t = dev.require_cuda()
+    xd = t.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).cuda()
+    yd = t.from_numpy(np.ascontiguousarray(y, dtype=np.float64)).cuda()
+    out = t.empty_like(xd)
+    nat.call("pf_np_hypot_f64", xd.data_ptr(), yd.data_ptr(), xd.numel(), out.data_ptr(),
+             t.cuda.current_stream().cuda_stream)
+    return out.cpu().numpy()

@@ -86,7 +86,8 @@ def rel_close(a, b, rtol):
     a = np.asarray(a, dtype=np.float64)
     b = np.asarray(b, dtype=np.float64)
     same = (a == b)
-    err = np.abs(a - b)
+    with np.errstate(invalid="ignore"):
+        err = np.abs(a - b)
     ok = same | (err <= rtol * np.abs(b))
     return bool(ok.all()), (float(np.max(np.where(same, 0.0, err / np.maximum(np.abs(b), 1e-300))))
                             if a.size else 0.0)

@@ -75,3 +75,65 @@ def test_oracle_sparsify_and_sparse_pairs(name):
         got = O.dv_field_sparse(sv, g, c.target, rows)
         ok, err = rel_close(got, c[f"spfield/{g}"][list(rows)], 1e-12)
         assert ok, (g, err)
+
+
+STATUS_CODE = {"reached": 0, "stuck": 1, "max-steps-exceeded": 2}
+
+
+def encode_locs(locs):
+    kind = np.array([0 if l[0] == "vertex" else 1 for l in locs], np.int8)
+    i = np.array([l[1] for l in locs], np.int64)
+    j = np.array([l[2] if l[0] == "edge" else -1 for l in locs], np.int64)
+    t = np.array([l[3] if l[0] == "edge" else 0.0 for l in locs], np.float64)
+    return kind, i, j, t
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_oracle_tracer_matches_reference_paths(name):
+    from oracle import tracer as TR
+    c = case(name)
+    m = c.mesh
+    topo = TR.topology(m.triangles, m.n)
+    srcs = c["path_sources"]
+    for g in ("kl", "tv"):
+        vals = c[f"field/{g}/0"]
+        for pi, s in enumerate(srcs):
+            gold = c.path(g, pi)
+            res = TR.triangle_descent(m.vertices, m.triangles, m.areas, c.meta["bbox_diagonal"],
+                                      vals, c.target, int(s), topo=topo)
+            kind, i, j, t = encode_locs(res["locations"])
+            np.testing.assert_array_equal(kind, gold["kind"])
+            np.testing.assert_array_equal(i, gold["i"])
+            np.testing.assert_array_equal(j, gold["j"])
+            np.testing.assert_array_equal(t, gold["t"])
+            np.testing.assert_array_equal(res["points"], gold["points"])
+            assert STATUS_CODE[res["status"]] == int(gold["status"])
+            assert (res["stuck_vertex"] if res["stuck_vertex"] is not None else -1) == int(gold["stuck"])
+
+
+def test_topology_matches_reference_lists():
+    from oracle import tracer as TR
+    c = case("holes_fine")
+    m = c.mesh
+    vt_ptr, vt_idx, nb_ptr, nb_idx, tri_nbr = TR.topology(m.triangles, m.n)
+    # rebuild the reference's lists the way mesh.py:146-157 does
+    vt = [[] for _ in range(m.n)]
+    for ti, (a, b, cc) in enumerate(m.triangles):
+        vt[a].append(ti); vt[b].append(ti); vt[cc].append(ti)
+    for v in range(0, m.n, 7):
+        assert list(vt_idx[vt_ptr[v]:vt_ptr[v + 1]]) == sorted(vt[v])
+    edges = {}
+    for ti in range(len(m.triangles)):
+        a, b, cc = m.triangles[ti]
+        for i, j in ((a, b), (b, cc), (cc, a)):
+            edges.setdefault((min(i, j), max(i, j)), []).append(ti)
+    for ti in range(0, len(m.triangles), 5):
+        for s in range(3):
+            i, j = m.triangles[ti][(s + 1) % 3], m.triangles[ti][(s + 2) % 3]
+            other = [x for x in edges[(min(i, j), max(i, j))] if x != ti]
+            assert tri_nbr[ti, s] == (other[0] if other else -1)
+    nbr = [set() for _ in range(m.n)]
+    for (i, j) in edges:
+        nbr[i].add(j); nbr[j].add(i)
+    for v in range(0, m.n, 11):
+        assert list(nb_idx[nb_ptr[v]:nb_ptr[v + 1]]) == sorted(nbr[v])
