@@ -193,6 +193,30 @@ int pf_csr_tv_f64(const int64_t *indptr, const int32_t *indices, const double *d
 int pf_log_clamped_f64(const double *P, int64_t ld, int64_t rows, int64_t k, double clamp,
                        double *out, pf_stream_t stream);
 
+/* ---- K7: KL to a batch of T targets (T x dv_field, divergence.py:154-187) ---
+ * pf_batch_prep_f64: from the T raw target rows Pt (T x ldp) write
+ *   L[t,b] = log(max(Pt[t,b], clamp)) and Tc[t,b] = max(Pt[t,b], clamp)
+ *   (T x ldl, ldl = round_up(k,16), zero / one padded) and
+ *   tflag[t] = 1 if the below-clamp mask of Pt[t] differs from that of `ref`
+ *   (the mask shared by the interior rows, see pf_mask_uniform_f64).
+ * pf_mask_uniform_f64: nonuniform[0] |= 1 if any interior row's mask
+ *   (P < clamp) differs from ref's; with it the per-target `clamped` flag of
+ *   divergence.py:172-175 is exact: flag_t = nonuniform || tflag[t].
+ * pf_batched_kl_f64: out[q*ldo + t] = KL(q, targets[t]) for the slab rows:
+ *   H[q] - (Qc L^T)[q,t] as an FP64 GEMM with a fused epilogue (guard,
+ *   settle, zero at the target), then the guarded pairs re-evaluated in the
+ *   reference's per-element form (count added to *guarded if non-NULL). */
+int pf_batch_prep_f64(const double *Pt, int64_t ldp, int64_t T, int64_t k, int64_t ldl,
+                      double clamp, const double *ref, double *L, double *Tc, uint32_t *tflag,
+                      pf_stream_t stream);
+int pf_mask_uniform_f64(const double *P, int64_t ld, int64_t rows, int64_t k, double clamp,
+                        const uint8_t *is_interior, const double *ref, uint32_t *nonuniform,
+                        pf_stream_t stream);
+int pf_batched_kl_f64(const double *P, int64_t ld, int64_t rows, int64_t k, const double *H,
+                      const double *L, const double *Tc, int64_t ldl, int64_t T,
+                      const int64_t *targets, double clamp, double tau, int64_t row0,
+                      double *out, int64_t ldo, uint32_t *guarded, pf_stream_t stream);
+
 /* ---- K8: batched triangle-descent tracer (paths.py:101-307) ---------------
  * Device-resident mesh topology (all arrays device pointers):
  *   vertices  (n,2) FP64;  triangles (nt,3) int32 CCW exactly as stored by

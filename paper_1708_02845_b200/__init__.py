@@ -7,7 +7,7 @@ types, computed by hand-written sm_100a CUDA kernels behind the C ABI in
 """
 
 from .config import DEFAULTS, Settings
-from .divergence import (FDivergence, builtin_f, dv_at, dv_field,
+from .divergence import (FDivergence, builtin_f, dv_at, dv_field, dv_field_batch,
                          dv_field_device, dv_field_sparse, dv_pair,
                          dv_pair_sparse, dv_pair_sparse_stats, sparsify)
 from .mesh import TriMesh
@@ -20,7 +20,7 @@ from .solvers import PoissonKernel, ScalarField
 __version__ = "0.1.0"
 
 __all__ = [
-    "DEFAULTS", "Settings", "FDivergence", "builtin_f", "dv_at", "dv_field",
+    "DEFAULTS", "Settings", "FDivergence", "builtin_f", "dv_at", "dv_field", "dv_field_batch",
     "dv_field_device", "dv_pair", "sparsify", "dv_pair_sparse", "dv_pair_sparse_stats",
     "dv_field_sparse", "TriMesh", "TracedPath", "triangle_descent", "triangle_descent_batch",
     "triangle_gradient", "DivergenceDomainError", "InvalidTargetError",

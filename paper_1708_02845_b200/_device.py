@@ -90,6 +90,7 @@ class DeviceKernel:
         self.is_interior = t.from_numpy(interior[self.row0:self.row0 + self.rows].copy()).to(self.device)
         self._H = {}
         self._csr = {}
+        self._uniform = {}
         self._min = None
         self._lock = threading.Lock()
         self._host = weakref.ref(dense) if dense is not None else None
@@ -130,6 +131,32 @@ class DeviceKernel:
                 c = DeviceCSR(self, float(cut), bool(strict_positive))
                 self._csr[key] = c
             return c
+
+    def mask_nonuniform(self, clamp: float) -> tuple[bool, object]:
+        """(nonuniform, ref_row): do all interior rows share one below-clamp mask?
+
+        Cached per clamp; ref_row is the first interior row (device view) or
+        None when the slab has no interior rows.
+        """
+        key = float(clamp)
+        with self._lock:
+            hit = self._uniform.get(key)
+        if hit is not None:
+            return hit
+        t = torch()
+        interior = np.flatnonzero(self.is_interior.cpu().numpy())
+        if interior.size == 0:
+            res = (False, None)
+        else:
+            ref = self.P[int(interior[0]), :self.k]
+            flag = t.zeros(1, dtype=t.int32, device=self.device)
+            nat.call("pf_mask_uniform_f64", self.P.data_ptr(), self.ld, self.rows, self.k, key,
+                     self.is_interior.data_ptr(), ref.data_ptr(), flag.data_ptr(),
+                     t.cuda.current_stream(self.device).cuda_stream)
+            res = (bool(flag.item()), ref)
+        with self._lock:
+            self._uniform[key] = res
+        return res
 
     def target_row(self, p: int, host_dense: np.ndarray | None = None):
         """Device view of the raw target row P[p, :k].

@@ -1,0 +1,266 @@
+// batched.cu — KL to a batch of T targets as one dense contraction (K7).
+//
+// Reference semantics: T calls of pathfield/divergence.py dv_field(pk, kl, t)
+// (:154-187); the reference has no batched API.
+//
+//   KL[q, t] = H[q] - sum_b c(Q_qb) * log c(Pt_b)      (c(x) = max(x, clamp))
+//
+// i.e. C = H 1^T - Qc * L^T with Qc the clamped P (n x k) and L (T x k) the
+// clamped logs of the target rows: an FP64 GEMM n x T x k (C5: 1M x 1024 x
+// 4102 = 8.4 TFLOP) with a fused epilogue (split-form cancellation guard ->
+// sentinel, settle, KL[t, t] = 0).  tcgen05 has no FP64 kind, so the
+// contraction runs on the FP64 pipes: a register-blocked DFMA GEMM, 128x128
+// block tile, 8x8 outputs per thread, k-tiles of 16 double-buffered through
+// shared memory, the clamp applied while staging P.  Guarded pairs are
+// re-evaluated per element in the reference form by batched_kl_fixup.
+//
+// The per-target `clamped` precision flag (divergence.py:172-175) is exact
+// without an n x T x k compare: all interior rows share one below-clamp mask
+// M* (pf_mask_uniform_f64 checks it once per P), so flag_t = !uniform ||
+// mask(P[t]) != M*.
+#include <cmath>
+
+#include "pf_common.cuh"
+
+namespace pf {
+
+constexpr int kBM = 128, kBN = 128, kBK = 16, kGemmThreads = 256;
+constexpr int kApad = kBM + 1, kBpad = kBN + 1;  // k-major tiles, padded rows
+constexpr unsigned long long kBatchGuard = 0x7ff8dead0000ba7cull;
+
+// L[t, b] = log(max(Pt[t, b], clamp)), Tc[t, b] = max(Pt[t, b], clamp), zero
+// beyond k (L) / 1 (Tc) up to ldl; tflag[t] = mask(Pt[t]) != mask(ref).
+__global__ void batch_prep_kernel(const double *__restrict__ Pt, int64_t ldp, int64_t T,
+                                  int64_t k, int64_t ldl, double clamp,
+                                  const double *__restrict__ ref, double *__restrict__ L,
+                                  double *__restrict__ Tc, uint32_t *__restrict__ tflag) {
+  const int64_t t = blockIdx.x;
+  if (t >= T) return;
+  bool diff = false;
+  for (int64_t b = threadIdx.x; b < ldl; b += blockDim.x) {
+    if (b < k) {
+      const double p = Pt[t * ldp + b];
+      const double c = fmax(p, clamp);
+      L[t * ldl + b] = log(c);
+      Tc[t * ldl + b] = c;
+      if (ref) diff |= (p < clamp) != (ref[b] < clamp);
+    } else {
+      L[t * ldl + b] = 0.0;
+      Tc[t * ldl + b] = 1.0;
+    }
+  }
+  diff = __syncthreads_or(diff);
+  if (threadIdx.x == 0 && tflag) tflag[t] = diff ? 1u : 0u;
+}
+
+// nonuniform[0] |= some interior row's below-clamp mask differs from ref's.
+__global__ void mask_uniform_kernel(const double *__restrict__ P, int64_t ld, int64_t rows,
+                                    int64_t k, double clamp, const uint8_t *__restrict__ interior,
+                                    const double *__restrict__ ref, uint32_t *__restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  bool diff = false;
+  for (int64_t r = warp; r < rows; r += nwarps) {
+    if (interior && !interior[r]) continue;
+    const double *row = P + r * ld;
+    for (int64_t b = lane; b < k; b += 32) diff |= (ldg_stream(row + b) < clamp) != (ref[b] < clamp);
+  }
+  if (__any_sync(0xffffffffu, diff) && lane == 0) atomicOr(out, 1u);
+}
+
+__global__ void __launch_bounds__(kGemmThreads, 1) batched_kl_gemm_kernel(
+    const double *__restrict__ P, int64_t ld, int64_t rows, int64_t k,
+    const double *__restrict__ H, const double *__restrict__ L, int64_t ldl, int64_t T,
+    const int64_t *__restrict__ targets, double clamp, double tau, int64_t row0,
+    double *__restrict__ out, int64_t ldo) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  double *As = reinterpret_cast<double *>(smem);      // [2][kBK][kApad]
+  double *Bs = As + 2 * kBK * kApad;                   // [2][kBK][kBpad]
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * kBN;
+  const int64_t q0 = static_cast<int64_t>(blockIdx.y) * kBM;
+  const int64_t nkt = (k + kBK - 1) / kBK;
+
+  double acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+
+  double2 ra[4], rb[4];
+  auto load_tile = [&](int64_t kt) {
+    const int64_t k0 = kt * kBK;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = tid + kGemmThreads * u;  // 0..1023
+      const int row = e >> 3, kp = (e & 7) * 2;
+      const int64_t q = q0 + row, kk = k0 + kp;
+      double2 a = make_double2(0.0, 0.0);
+      if (q < rows && kk < k) {
+        a = *reinterpret_cast<const double2 *>(P + q * ld + kk);
+        a.x = fmax(a.x, clamp);
+        a.y = (kk + 1 < k) ? fmax(a.y, clamp) : 0.0;
+      }
+      ra[u] = a;
+      const int64_t t = t0 + row;
+      double2 b = make_double2(0.0, 0.0);
+      if (t < T) b = *reinterpret_cast<const double2 *>(L + t * ldl + kk);  // zero-padded
+      rb[u] = b;
+    }
+  };
+  auto store_tile = [&](int buf) {
+    double *as = As + buf * kBK * kApad, *bs = Bs + buf * kBK * kBpad;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = tid + kGemmThreads * u;
+      const int row = e >> 3, kp = (e & 7) * 2;
+      as[kp * kApad + row] = ra[u].x;
+      as[(kp + 1) * kApad + row] = ra[u].y;
+      bs[kp * kBpad + row] = rb[u].x;
+      bs[(kp + 1) * kBpad + row] = rb[u].y;
+    }
+  };
+
+  load_tile(0);
+  store_tile(0);
+  __syncthreads();
+  for (int64_t kt = 0; kt < nkt; ++kt) {
+    const int buf = kt & 1;
+    if (kt + 1 < nkt) load_tile(kt + 1);
+    const double *as = As + buf * kBK * kApad, *bs = Bs + buf * kBK * kBpad;
+#pragma unroll
+    for (int kk = 0; kk < kBK; ++kk) {
+      double a[8], b[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = as[kk * kApad + ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) b[j] = bs[kk * kBpad + tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+    if (kt + 1 < nkt) store_tile(buf ^ 1);
+    __syncthreads();
+  }
+
+  // fused epilogue: H - cross, guard, settle, zero at the target
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t q = q0 + ty + 16 * i;
+    if (q >= rows) continue;
+    const double h = H[q];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int64_t t = t0 + tx + 16 * j;
+      if (t >= T) continue;
+      const double cross = acc[i][j];
+      double val = h - cross;
+      const bool is_t = (row0 + q == targets[t]);
+      if (!is_t && fabs(val) < tau * (fabs(h) + fabs(cross)))
+        val = __longlong_as_double(static_cast<long long>(kBatchGuard));
+      else
+        val = is_t ? 0.0 : settle(val);
+      out[q * ldo + t] = val;
+    }
+  }
+}
+
+// Per-element reference form for guarded (q, t) pairs (divergence.py:180).
+__global__ void __launch_bounds__(256) batched_kl_fixup_kernel(
+    const double *__restrict__ P, int64_t ld, int64_t rows, int64_t k,
+    const double *__restrict__ Tc, int64_t ldl, int64_t T, double clamp,
+    double *__restrict__ out, int64_t ldo, uint32_t *__restrict__ count) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t total = rows * T;
+  uint32_t done = 0;
+  for (int64_t base = warp * 32; base < total; base += nwarps * 32) {
+    const int64_t mine = base + lane;
+    const int64_t mq = mine / T, mt = mine - mq * T;
+    const bool flag = mine < total && static_cast<unsigned long long>(__double_as_longlong(
+                                          out[mq * ldo + mt])) == kBatchGuard;
+    unsigned ball = __ballot_sync(0xffffffffu, flag);
+    while (ball) {
+      const int src = __ffs(ball) - 1;
+      ball &= ball - 1;
+      const int64_t e = base + src, q = e / T, t = e - q * T;
+      const double *prow = P + q * ld;
+      const double *trow = Tc + t * ldl;
+      double b[4] = {0.0, 0.0, 0.0, 0.0};
+      int64_t c = lane;
+      for (; c + 96 < k; c += 128) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double qv = fmax(prow[c + 32 * u], clamp);
+          b[u] += __dmul_rn(qv, -log(__ddiv_rn(trow[c + 32 * u], qv)));
+        }
+      }
+      for (; c < k; c += 32) {
+        const double qv = fmax(prow[c], clamp);
+        b[0] += __dmul_rn(qv, -log(__ddiv_rn(trow[c], qv)));
+      }
+      const double val = settle(warp_sum((b[0] + b[1]) + (b[2] + b[3])));
+      if (lane == 0) out[q * ldo + t] = val;
+      ++done;
+    }
+  }
+  if (lane == 0 && done && count) atomicAdd(count, done);
+}
+
+}  // namespace pf
+
+using namespace pf;
+
+extern "C" {
+
+int pf_batch_prep_f64(const double *Pt, int64_t ldp, int64_t T, int64_t k, int64_t ldl,
+                      double clamp, const double *ref, double *L, double *Tc, uint32_t *tflag,
+                      pf_stream_t stream) {
+  if (T <= 0) return 0;
+  if (!Pt || !L || !Tc || ldl < k || ldl % 16) return fail(PF_E_ARG, "batch_prep: bad args");
+  batch_prep_kernel<<<static_cast<unsigned>(T), 256, 0, as_stream(stream)>>>(
+      Pt, ldp, T, k, ldl, clamp, ref, L, Tc, tflag);
+  return check_launch("batch_prep");
+}
+
+int pf_mask_uniform_f64(const double *P, int64_t ld, int64_t rows, int64_t k, double clamp,
+                        const uint8_t *is_interior, const double *ref, uint32_t *nonuniform,
+                        pf_stream_t stream) {
+  if (rows <= 0) return 0;
+  if (!P || !ref || !nonuniform) return fail(PF_E_ARG, "mask_uniform: null");
+  mask_uniform_kernel<<<sm_count() * 8, 256, 0, as_stream(stream)>>>(P, ld, rows, k, clamp,
+                                                                      is_interior, ref,
+                                                                      nonuniform);
+  return check_launch("mask_uniform");
+}
+
+int pf_batched_kl_f64(const double *P, int64_t ld, int64_t rows, int64_t k, const double *H,
+                      const double *L, const double *Tc, int64_t ldl, int64_t T,
+                      const int64_t *targets, double clamp, double tau, int64_t row0,
+                      double *out, int64_t ldo, uint32_t *guarded, pf_stream_t stream) {
+  if (rows <= 0 || T <= 0) return 0;
+  if (!P || !H || !L || !Tc || !targets || !out) return fail(PF_E_ARG, "batched_kl: null");
+  if ((ld & 1) || (reinterpret_cast<uintptr_t>(P) & 15) || ldl % 16 || ldl < k || ldo < T)
+    return fail(PF_E_ALIGN, "batched_kl: alignment (ld even, ldl %% 16 == 0)");
+  const size_t smem = 2 * kBK * (kApad + kBpad) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(batched_kl_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    attr = true;
+  }
+  dim3 grid(static_cast<unsigned>((T + kBN - 1) / kBN), static_cast<unsigned>((rows + kBM - 1) / kBM));
+  if (grid.y > 65535) return fail(PF_E_DOMAIN, "batched_kl: too many rows per launch (%lld)",
+                                  (long long)rows);
+  batched_kl_gemm_kernel<<<grid, kGemmThreads, smem, as_stream(stream)>>>(
+      P, ld, rows, k, H, L, ldl, T, targets, clamp, tau, row0, out, ldo);
+  if (int e = check_launch("batched_kl_gemm")) return e;
+  batched_kl_fixup_kernel<<<sm_count() * 8, 256, 0, as_stream(stream)>>>(
+      P, ld, rows, k, Tc, ldl, T, clamp, out, ldo, guarded);
+  return check_launch("batched_kl_fixup");
+}
+
+}  // extern "C"

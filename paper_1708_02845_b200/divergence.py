@@ -274,6 +274,67 @@ def dv_pair(pk: PoissonKernel, fd: FDivergence, p: int, q: int,
 
 
 # ---------------------------------------------------------------------------
+# Batched targets (K7; no reference API: T x dv_field)
+# ---------------------------------------------------------------------------
+
+def dv_field_batch_device(pk: PoissonKernel, fd: FDivergence, targets, clamp=None):
+    """Fields to T targets at once on the device: (values (n, T) tensor, flags (T,) bool array).
+
+    KL (default order) runs as one FP64 GEMM with a fused epilogue (K7);
+    any other generator or ``swap_order`` is T single-target launches.
+    """
+    t = dev.require_cuda()
+    targets = np.asarray(targets, dtype=np.int64).reshape(-1)
+    if targets.size and (targets.min() < 0 or targets.max() >= pk.n):
+        raise InvalidTargetError("target out of range")
+    dk = dev.device_kernel(pk)
+    if clamp is None:
+        clamp = fd.clamp
+    c = _effective_clamp(dk, clamp)
+    T = targets.size
+    s = t.cuda.current_stream(dk.device)
+    out = t.empty((dk.rows, max(T, 1)), dtype=t.float64, device=dk.device)
+    if T == 0:
+        return out[:, :0], np.zeros(0, dtype=bool)
+    if fd.name != "kl":
+        flags = np.zeros(T, dtype=bool)
+        for j, p in enumerate(targets):
+            v, f = dv_field_device(pk, fd, int(p), clamp=clamp)
+            out[:, j] = v
+            flags[j] = bool(f[0].item()) and c > 0.0
+        return out, flags
+    if not all(dk.owns(int(p)) for p in targets):
+        raise NotImplementedError("targets outside this slab: use parallel.sharded_field_batch")
+    H = dk.negentropy(c)
+    ldl = dev.round_up(dk.k, 16)
+    tg = t.from_numpy(targets).to(dk.device)
+    Pt = dk.P.index_select(0, tg - dk.row0)
+    L = t.empty((T, ldl), dtype=t.float64, device=dk.device)
+    Tc = t.empty((T, ldl), dtype=t.float64, device=dk.device)
+    tflag = t.zeros(T + 1, dtype=t.int32, device=dk.device)
+    nonuni, ref = dk.mask_nonuniform(c) if c > 0.0 else (False, None)
+    nat.call("pf_batch_prep_f64", Pt.data_ptr(), Pt.stride(0), T, dk.k, ldl, c, nat.ptr(ref),
+             L.data_ptr(), Tc.data_ptr(), tflag.data_ptr(), s.cuda_stream)
+    nat.call("pf_batched_kl_f64", dk.P.data_ptr(), dk.ld, dk.rows, dk.k, H.data_ptr(),
+             L.data_ptr(), Tc.data_ptr(), ldl, T, tg.data_ptr(), c, KL_GUARD_TAU, dk.row0,
+             out.data_ptr(), out.stride(0), tflag.data_ptr() + 4 * T, s.cuda_stream)
+    tf = tflag.cpu().numpy()
+    flags = (nonuni | (tf[:T] != 0)) if (c > 0.0 and ref is not None) else np.zeros(T, bool)
+    return out, flags
+
+
+def dv_field_batch(pk: PoissonKernel, fd: FDivergence, targets, clamp=None):
+    """``np.column_stack([dv_field(pk, fd, t).values for t in targets])`` in one pass.
+
+    Returns the (n, T) FP64 array; the per-target ``clamped`` flags are on
+    :func:`dv_field_batch_device`.
+    """
+    t = dev.require_cuda()
+    out, flags = dv_field_batch_device(pk, fd, targets, clamp)
+    return _to_host(t, out, t.cuda.current_stream(out.device))
+
+
+# ---------------------------------------------------------------------------
 # Sparsification and sparse distances (divergence.py:194-305)
 # ---------------------------------------------------------------------------
 
@@ -462,6 +523,7 @@ def dv_field_sparse_device(pk: PoissonKernel, fd: FDivergence, p: int):
 
 
 __all__ = [
+    "dv_field_batch", "dv_field_batch_device",
     "sparsify", "dv_pair_sparse", "dv_pair_sparse_stats", "dv_field_sparse",
     "dv_field_sparse_device", "LogDenseView",
     "FDivergence", "builtin_f", "dv_pair", "dv_at", "dv_field", "dv_field_device",

@@ -184,7 +184,7 @@ class DeviceMesh:
         T = np.ascontiguousarray(mesh.triangles, dtype=np.int64)
         topo = getattr(mesh, "_topo", None) or topology(T, len(V))
         vt_ptr, vt_idx, nb_ptr, nb_idx, tri_nbr = topo
-        to = lambda a, dt: t.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(self.device)  # noqa: E731
+        to = lambda a, dt: t.from_numpy(np.array(a, dtype=dt)).to(self.device)  # noqa: E731
         self.V = to(V, np.float64)
         self.T = to(T, np.int32)
         self.A = to(np.asarray(mesh.triangle_areas), np.float64)
