@@ -197,6 +197,270 @@ def make_synthetic_slab(t, rows, k, ld, seed, device, chunk=8192):
     return P
 
 
+def make_banded_slab(t, rows, k, ld, device, width=12.5, chunk=8192):
+    """Corridor-like synthetic P: each row's mass on two exponential bands
+    (bottom wall at column c, top wall at k-1-c, c moving along the corridor),
+    ~487 entries per row above the 1/sqrt(n) cut — the C3 nnz/row."""
+    P = t.empty((rows, ld), dtype=t.float64, device=device)
+    b = t.arange(k, dtype=t.float64, device=device)[None, :]
+    for a in range(0, rows, chunk):
+        e = min(rows, a + chunk)
+        q = t.arange(a, e, dtype=t.float64, device=device)[:, None]
+        c1 = t.floor(q / rows * (k / 2))
+        c2 = (k - 1) - c1
+        x = t.exp(-t.abs(b - c1) / width) + t.exp(-t.abs(b - c2) / width)
+        P[a:e, :k] = x / x.sum(dim=1, keepdim=True)
+    P[:, k:] = 0.0
+    return P
+
+
+class DenseStep:
+    """One KL + TV field step over a slab through the C ABI, buffers preallocated.
+    With `sharded` (parallel.ShardedField) the target row is NCCL-broadcast."""
+
+    def __init__(self, t, nat, dev, dk, target, tau, sharded=None):
+        self.t, self.nat, self.dk, self.target, self.tau, self.sh = t, nat, dev, dk, target, tau
+        self.dk = dk
+        k, rows = dk.k, dk.rows
+        self.k_pad, m_pad = dev.round_up(k, 2), dev.round_up(k, 16)
+        self.stage = t.empty(16 * self.k_pad + m_pad, dtype=t.uint8, device=dk.device)
+        base = self.stage.data_ptr()
+        self.tgt, self.logt, self.tmask = base, base + 8 * self.k_pad, base + 16 * self.k_pad
+        self.out_kl = t.empty(rows + 2, dtype=t.float64, device=dk.device)
+        self.out_tv = t.empty(rows + 2, dtype=t.float64, device=dk.device)
+        self.fk = self.out_kl.data_ptr() + rows * 8
+        self.ft = self.out_tv.data_ptr() + rows * 8
+        self.H = dk.negentropy(1e-300)
+        self.stream = t.cuda.current_stream(dk.device)
+        self.ev = [(t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True))
+                   for _ in range(2)]
+        self.kern_ms = [0.0, 0.0]
+        self.launches = 0
+
+    def run(self, timed=False):
+        dk, nat, s, k = self.dk, self.nat, self.stream.cuda_stream, self.dk.k
+        if self.sh is not None:
+            rowp = self.sh.target_row(self.target, k).data_ptr()
+            self._keep = rowp
+        else:
+            rowp = dk.P[self.target - dk.row0].data_ptr()
+        nat.call("pf_target_prep_f64", rowp, k, 1e-300, self.tgt, self.logt, self.tmask, self.fk, s)
+        if timed:
+            self.ev[0][0].record(self.stream)
+        nat.call("pf_dense_kl_f64", dk.P.data_ptr(), dk.ld, dk.rows, k, self.H.data_ptr(),
+                 self.tgt, self.logt, self.tmask, 1e-300, self.tau, dk.row0, self.target,
+                 dk.is_interior.data_ptr(), self.out_kl.data_ptr(), self.fk, s)
+        if timed:
+            self.ev[0][1].record(self.stream)
+        nat.call("pf_target_prep_f64", rowp, k, 1e-150, self.tgt, 0, self.tmask, self.ft, s)
+        if timed:
+            self.ev[1][0].record(self.stream)
+        nat.call("pf_dense_tv_f64", dk.P.data_ptr(), dk.ld, dk.rows, k, self.tgt, self.tmask,
+                 1e-150, dk.row0, self.target, dk.is_interior.data_ptr(),
+                 self.out_tv.data_ptr(), self.ft, s)
+        if timed:
+            self.ev[1][1].record(self.stream)
+            self.stream.synchronize()
+            self.kern_ms[0] += self.ev[0][0].elapsed_time(self.ev[0][1])
+            self.kern_ms[1] += self.ev[1][0].elapsed_time(self.ev[1][1])
+        self.launches += 5
+
+
+def _roof(bytes_, ms, peak):
+    ach = bytes_ / (ms / 1e3) / 1e9
+    return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+            "algorithmic_bytes_per_launch": bytes_, "avg_launch_ms": ms}
+
+
+def extra_c4_and_c5(t, nat, dev, pf, device, steps, peak):
+    """C4 dense KL+TV (1,000,386 x 4,102 on one GPU) and C5 batched KL (T = 1024)."""
+    import numpy as np
+    rows, k, _ = WORKLOADS["c4"]
+    ld = dev.leading_dim(k)
+    P = make_synthetic_slab(t, rows, k, ld, 7, device, chunk=32768)
+    dk = dev.DeviceKernel(None, np.array([], np.int64), device=device, rows=rows, n=rows, k=k,
+                          P_dev=P)
+    target = rows // 3 + 1
+    st = DenseStep(t, nat, dev, dk, target, pf.divergence.KL_GUARD_TAU)
+    for _ in range(2):
+        st.run()
+    n = max(2, min(steps, 5))
+    for _ in range(n):
+        st.run(timed=True)
+    kl_ms, tv_ms = st.kern_ms[0] / n, st.kern_ms[1] / n
+    c4 = {"workload": "C4 shape 1,000,386 x 4,102 dense FP64 (32.8 GB), synthetic, 1 GPU",
+          "evals_per_s": 2 * rows / ((kl_ms + tv_ms) / 1e3),
+          "kl": _roof(rows * (8 * k + 16) + 8 * k, kl_ms, peak),
+          "tv": _roof(rows * (8 * k + 8) + 8 * k, tv_ms, peak)}
+    del st
+    # ---- C5: 1024 targets, one FP64 contraction + fused epilogue (K7)
+    T = 1024
+    rng = np.random.default_rng(0)
+    targets = rng.choice(rows, T, replace=False)
+    tg = t.from_numpy(targets.astype(np.int64)).to(device)
+    H = dk.negentropy(1e-300)
+    ldl = dev.round_up(k, 16)
+    Pt = dk.P.index_select(0, tg)
+    L = t.empty((T, ldl), dtype=t.float64, device=device)
+    Tc = t.empty((T, ldl), dtype=t.float64, device=device)
+    out = t.empty((rows, T), dtype=t.float64, device=device)
+    cnt = t.zeros(1, dtype=t.int32, device=device)
+    s = t.cuda.current_stream(device)
+    e0, e1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
+
+    def batch():
+        nat.call("pf_batch_prep_f64", Pt.data_ptr(), Pt.stride(0), T, k, ldl, 1e-300, 0,
+                 L.data_ptr(), Tc.data_ptr(), 0, s.cuda_stream)
+        nat.call("pf_batched_kl_f64", dk.P.data_ptr(), dk.ld, rows, k, H.data_ptr(), L.data_ptr(),
+                 Tc.data_ptr(), ldl, T, tg.data_ptr(), 1e-300, pf.divergence.KL_GUARD_TAU, 0,
+                 out.data_ptr(), out.stride(0), cnt.data_ptr(), s.cuda_stream)
+
+    batch()
+    t.cuda.synchronize()
+    reps = 2
+    e0.record(s)
+    for _ in range(reps):
+        batch()
+    e1.record(s)
+    t.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    flops = 2.0 * rows * k * T
+    # sustained DFMA rate of this GPU (diagnostic kernel) as the FP64 roofline
+    import ctypes
+    fl = ctypes.c_int64(0)
+    probe = t.empty(1, dtype=t.float64, device=device)
+    nat.call("pf_probe_dfma_f64", 1 << 14, ctypes.byref(fl), probe.data_ptr(), s.cuda_stream)
+    t.cuda.synchronize()
+    e0.record(s)
+    nat.call("pf_probe_dfma_f64", 1 << 16, ctypes.byref(fl), probe.data_ptr(), s.cuda_stream)
+    e1.record(s)
+    t.cuda.synchronize()
+    peak_tf = fl.value / (e0.elapsed_time(e1) / 1e3) / 1e12
+    ach = flops / (ms / 1e3) / 1e12
+    c5 = {"workload": "C5 shape: 1,000,386 x 4,102 P, T = 1024 targets, KL as one FP64 GEMM "
+                      "+ fused epilogue (K7), synthetic, 1 GPU",
+          "evals_per_s": rows * T / (ms / 1e3), "ms_per_batch": ms,
+          "guarded_pairs": int(cnt.item()) // reps if reps else 0,
+          "roofline": {"bound": "fp64", "achieved": ach, "peak": peak_tf, "unit": "TFLOP/s",
+                       "frac": ach / peak_tf,
+                       "peak_kind": "measured: pf_probe_dfma_f64 (8 DFMA chains/thread, all SMs)"}}
+    del out, L, Tc, Pt, dk, P
+    t.cuda.empty_cache()
+    return c4, c5
+
+
+def extra_c3(t, nat, dev, pf, device, steps, peak):
+    """C3: CSR KL + TV over the corridor-shaped sparse kernel (102,104 x 4,250)."""
+    import math
+    import numpy as np
+    rows, k, _ = WORKLOADS["c2"]
+    ld = dev.leading_dim(k)
+    P = make_banded_slab(t, rows, k, ld, device)
+    dk = dev.DeviceKernel(None, np.array([], np.int64), device=device, rows=rows, n=rows, k=k,
+                          P_dev=P)
+    cut = (1.0 / math.sqrt(rows)) / k
+    t0 = t.cuda.Event(enable_timing=True)
+    t1 = t.cuda.Event(enable_timing=True)
+    s = t.cuda.current_stream(device)
+    t0.record(s)
+    dc = dk.csr(cut, False)
+    t1.record(s)
+    t.cuda.synchronize()
+    build_ms = t0.elapsed_time(t1)
+    target = rows // 3 + 1
+    k_pad = dev.round_up(k, 2)
+    stage = t.empty(16 * k_pad + dev.round_up(k, 16), dtype=t.uint8, device=device)
+    logt = stage.data_ptr() + 8 * k_pad
+    vp = t.empty(k_pad + 4, dtype=t.float64, device=device)
+    out = t.empty(rows + 2, dtype=t.float64, device=device)
+    flags = out.data_ptr() + rows * 8
+    ev = [t.cuda.Event(enable_timing=True) for _ in range(4)]
+    ms = [0.0, 0.0]
+
+    def step(timed):
+        nat.call("pf_target_prep_f64", dk.P[target].data_ptr(), k, 1e-300, stage.data_ptr(), logt,
+                 stage.data_ptr() + 16 * k_pad, flags, s.cuda_stream)
+        if timed:
+            ev[0].record(s)
+        nat.call("pf_csr_kl_f64", dc.indptr.data_ptr(), dc.indices.data_ptr(), dc.data.data_ptr(),
+                 dc.log_data.data_ptr(), dc.hs.data_ptr(), rows, k, logt,
+                 pf.divergence.KL_GUARD_TAU, 0, 0, rows, out.data_ptr(), 0, flags, s.cuda_stream)
+        if timed:
+            ev[1].record(s)
+        nat.call("pf_csr_target_prep_f64", dc.indptr.data_ptr(), dc.indices.data_ptr(),
+                 dc.data.data_ptr(), dc.dropped.data_ptr(), target, k, vp.data_ptr(),
+                 vp.data_ptr() + k_pad * 8, s.cuda_stream)
+        if timed:
+            ev[2].record(s)
+        nat.call("pf_csr_tv_f64", dc.indptr.data_ptr(), dc.indices.data_ptr(), dc.data.data_ptr(),
+                 dc.dropped.data_ptr(), rows, k, vp.data_ptr(), vp.data_ptr() + k_pad * 8, 0, 0,
+                 rows, out.data_ptr(), 0, s.cuda_stream)
+        if timed:
+            ev[3].record(s)
+            s.synchronize()
+            ms[0] += ev[0].elapsed_time(ev[1])
+            ms[1] += ev[2].elapsed_time(ev[3])
+
+    for _ in range(3):
+        step(False)
+    n = max(3, steps)
+    for _ in range(n):
+        step(True)
+    kl_ms, tv_ms = ms[0] / n, ms[1] / n
+    nnz = dc.nnz
+    res = {"workload": "C3 shape: 102,104 x 4,250 corridor-banded synthetic P, threshold 1/sqrt(n)",
+           "nnz": nnz, "nnz_per_row": nnz / rows,
+           "sparsity_percent": 100.0 * (1 - nnz / (rows * k)),
+           "sparsify_build_ms": build_ms,
+           "evals_per_s": 2 * rows / ((kl_ms + tv_ms) / 1e3),
+           "kl": _roof(nnz * 12 + rows * 24 + 8 * k, kl_ms, peak),
+           "tv": _roof(nnz * 12 + rows * 24 + 16 * k, tv_ms, peak)}
+    del dc, dk, P
+    t.cuda.empty_cache()
+    return res
+
+
+def extra_tracer(t, nat, dev, pf, device):
+    """C5 tracer shape: 10,000 paths on a 1,002,001-vertex mesh, 1,024 target fields."""
+    import numpy as np
+    from paper_1708_02845_b200 import mesh as M
+    from paper_1708_02845_b200 import paths as PP
+    t0 = time.perf_counter()
+    mesh = M.grid_mesh(1000, 1000)
+    build_s = time.perf_counter() - t0
+    dm = M.device_mesh(mesh)
+    rng = np.random.default_rng(1)
+    T = 1024
+    targets = rng.choice(mesh.interior_vertices, T, replace=False)
+    V = dm.V
+    tv = V.index_select(0, t.from_numpy(targets).to(device))
+    # Euclidean distance fields (the reference tests' smooth descent field), (T, n)
+    fields = t.cdist(tv, V)
+    npaths = 10_000
+    src = rng.choice(mesh.n, npaths)
+    fo = np.arange(npaths) % T
+    src = np.where(src == targets[fo], (src + 1) % mesh.n, src)
+    PP.trace_arrays(mesh, [fields[0]], targets[:1], src[:64])  # warm-up
+    t.cuda.synchronize()
+    e0, e1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
+    s = t.cuda.current_stream(device)
+    w0 = time.perf_counter()
+    e0.record(s)
+    buf, counts, over, extra = PP.trace_arrays(mesh, list(fields), targets, src, fo)
+    e1.record(s)
+    t.cuda.synchronize()
+    wall = time.perf_counter() - w0
+    ms = e0.elapsed_time(e1)
+    status = buf.status.cpu().numpy()
+    return {"workload": "10,000 paths (source i -> target i % 1024), 1000x1000 grid mesh "
+                        "(1,002,001 vertices, 2,000,000 triangles), Euclidean fields",
+            "paths_per_s": npaths / (ms / 1e3), "ms": ms, "wall_ms_incl_launch": 1e3 * wall,
+            "locations_per_s": float(counts.sum()) / (ms / 1e3),
+            "mean_locations": float(counts.mean()), "max_locations": int(counts.max()),
+            "reached": int((status == 0).sum()), "overflow_reruns": int(over.size),
+            "mesh_build_s": build_s}
+
+
 def run_native(args):
     import numpy as np
     import torch as t
@@ -204,6 +468,7 @@ def run_native(args):
     import paper_1708_02845_b200 as pf
     from paper_1708_02845_b200 import _device as dev
     from paper_1708_02845_b200 import _native as nat
+    from paper_1708_02845_b200 import parallel as par
 
     ws, rank, local = dist_env()
     if args.gpus != ws and ws > 1:
@@ -217,54 +482,16 @@ def run_native(args):
 
     rows, k, desc = WORKLOADS[args.workload]
     n_total = rows * ws
+    bounds = [(r * rows, (r + 1) * rows) for r in range(ws)]  # weak scaling: equal slabs
     row0 = rank * rows
     ld = dev.leading_dim(k)
     P_dev = make_synthetic_slab(t, rows, k, ld, rank, device)
     dk = dev.DeviceKernel(None, np.array([], np.int64), device=device, row0=row0, rows=rows,
                           n=n_total, k=k, P_dev=P_dev)
     target = n_total // 3 + 1
-    owner = target // rows
-    clamp_kl, clamp_tv = 1e-300, 1e-150
-    H = dk.negentropy(clamp_kl)
-    stream = t.cuda.current_stream(device)
-    s = stream.cuda_stream
-
-    k_pad = dev.round_up(k, 2)
-    m_pad = dev.round_up(k, 16)
-    stage = t.empty(16 * k_pad + m_pad, dtype=t.uint8, device=device)
-    tgt, logt, tmask = stage.data_ptr(), stage.data_ptr() + 8 * k_pad, stage.data_ptr() + 16 * k_pad
-    trow = t.empty(k, dtype=t.float64, device=device)
-    out_kl = t.empty(rows + 2, dtype=t.float64, device=device)
-    out_tv = t.empty(rows + 2, dtype=t.float64, device=device)
-    fk, ft = out_kl.data_ptr() + rows * 8, out_tv.data_ptr() + rows * 8
-    interior = dk.is_interior.data_ptr()
-    tau = pf.divergence.KL_GUARD_TAU
-
-    ev = [(t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)) for _ in range(2)]
-    kern_ms = {"kl": 0.0, "tv": 0.0}
-
-    def step(timed_kernels=False):
-        if ws > 1:
-            if rank == owner:
-                trow.copy_(dk.P[target - row0, :k])
-            dist.broadcast(trow, src=owner)
-            rowp = trow.data_ptr()
-        else:
-            rowp = dk.P[target - row0].data_ptr()
-        nat.call("pf_target_prep_f64", rowp, k, clamp_kl, tgt, logt, tmask, fk, s)
-        if timed_kernels:
-            ev[0][0].record(stream)
-        nat.call("pf_dense_kl_f64", dk.P.data_ptr(), dk.ld, rows, k, H.data_ptr(), tgt, logt,
-                 tmask, clamp_kl, tau, row0, target, interior, out_kl.data_ptr(), fk, s)
-        if timed_kernels:
-            ev[0][1].record(stream)
-        nat.call("pf_target_prep_f64", rowp, k, clamp_tv, tgt, 0, tmask, ft, s)
-        if timed_kernels:
-            ev[1][0].record(stream)
-        nat.call("pf_dense_tv_f64", dk.P.data_ptr(), dk.ld, rows, k, tgt, tmask, clamp_tv, row0,
-                 target, interior, out_tv.data_ptr(), ft, s)
-        if timed_kernels:
-            ev[1][1].record(stream)
+    sharded = par.ShardedField(dk, bounds, dist, device=device) if ws > 1 else None
+    step = DenseStep(t, nat, dev, dk, target, pf.divergence.KL_GUARD_TAU, sharded)
+    stream = step.stream
 
     def barrier():
         t.cuda.synchronize()
@@ -280,30 +507,26 @@ def run_native(args):
         return float(v.item())
 
     for _ in range(args.warmup):
-        step()
-    # kernel-level timing pass (events around each kernel on its stream)
+        step.run()
     barrier()
-    for _ in range(args.steps):
-        step(timed_kernels=True)
-        stream.synchronize()
-        kern_ms["kl"] += ev[0][0].elapsed_time(ev[0][1])
-        kern_ms["tv"] += ev[1][0].elapsed_time(ev[1][1])
-    kl_ms = kern_ms["kl"] / args.steps
-    tv_ms = kern_ms["tv"] / args.steps
+    for _ in range(args.steps):           # kernel-level timing pass (events on the stream)
+        step.run(timed=True)
+    kl_ms = step.kern_ms[0] / args.steps
+    tv_ms = step.kern_ms[1] / args.steps
 
-    # whole-step timing (the reported value)
     e0, e1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clocks:
+    step.launches = 0
+    with ClockSampler(local) as clocks:   # whole-step timing: the reported value
         barrier()
         e0.record(stream)
         for _ in range(args.steps):
-            step()
+            step.run()
         e1.record(stream)
         barrier()
+    launches = step.launches
     el_ms = max_over_ranks(e0.elapsed_time(e1))
-    evals = 2 * rows * ws * args.steps
-    value = evals / (el_ms / 1e3)
-    flags_kl = out_kl[rows:].view(t.int32).cpu().numpy()
+    value = 2 * rows * ws * args.steps / (el_ms / 1e3)
+    flags_kl = step.out_kl[rows:].view(t.int32).cpu().numpy()
 
     # ------------------------------------------------ e2e via the public API
     e2e = None
@@ -319,28 +542,23 @@ def run_native(args):
             pf.dv_field(pk, kl, target)
             pf.dv_field(pk, tv, target)
         barrier()
-        t0 = time.perf_counter()
-        ee0, ee1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
-        ee0.record(stream)
+        w0 = time.perf_counter()
         for _ in range(args.steps):
             fkl = pf.dv_field(pk, kl, target)
             ftv = pf.dv_field(pk, tv, target)
-        ee1.record(stream)
         barrier()
-        wall = time.perf_counter() - t0
-        dev_ms = ee0.elapsed_time(ee1)
-        e2e_s = max(wall, dev_ms / 1e3)
-        # parity spot check of the API result against the device-only path
-        assert np.array_equal(fkl.values, out_kl[:rows].cpu().numpy())
-        assert np.array_equal(ftv.values, out_tv[:rows].cpu().numpy())
+        e2e_s = time.perf_counter() - w0
+        assert np.array_equal(fkl.values, step.out_kl[:rows].cpu().numpy())
+        assert np.array_equal(ftv.values, step.out_tv[:rows].cpu().numpy())
         e2e = {"value": 2 * rows * args.steps / e2e_s, "unit": "evals/s",
                "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 2 * (rows + 2) * 8,
                "ms_per_step": 1e3 * e2e_s / args.steps,
-               "note": "dv_field(pk, kl|tv, t) per step: P resident in HBM (per-PoissonKernel "
-                       "device cache, as DomainContext keeps P resident); target index passed "
-                       "as a kernel argument; the n-vector field plus flags copied D2H to "
-                       "pinned host memory and returned as ScalarField"}
-        del host
+               "note": "wall clock of dv_field(pk, kl, t) + dv_field(pk, tv, t) per step through "
+                       "the public API: P resident in HBM (per-PoissonKernel device cache, as "
+                       "DomainContext keeps P resident); the target index is a kernel argument; "
+                       "each n-vector field + flags is copied D2H into a fresh numpy array and "
+                       "returned as a read-only ScalarField"}
+        del host, pk
 
     # ------------------------------------------------ CPU baseline (rank 0, N=1)
     cpu = None
@@ -355,8 +573,6 @@ def run_native(args):
     peak, peak_kind = peaks()
     bytes_kl = rows * (8 * k + 16) + 8 * k
     bytes_tv = rows * (8 * k + 8) + 8 * k
-    ach_kl = bytes_kl / (kl_ms / 1e3) / 1e9
-    ach_tv = bytes_tv / (tv_ms / 1e3) / 1e9
     traffic = None
     prof = ROOT / "profiles" / "ncu_summary.json"
     if prof.exists():
@@ -364,6 +580,29 @@ def run_native(args):
             traffic = json.loads(prof.read_text()).get(args.workload, {}).get("dense_kl_dram_bytes")
         except Exception:
             traffic = None
+    roof = _roof(bytes_kl, kl_ms, peak)
+    roof.update({"traffic": traffic, "kernel": "pf::dense_kl_kernel (+ kl_guard_fixup scan)",
+                 "peak_kind": ("measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+                               if peak_kind == "measured" else "fallback 6.65 TB/s")})
+
+    extras = {}
+    if ws == 1 and not args.no_extras:
+        del step, dk, P_dev
+        t.cuda.empty_cache()
+        for name, fn in (("c3_csr", lambda: extra_c3(t, nat, dev, pf, device, args.steps, peak)),
+                         ("c4_c5", lambda: extra_c4_and_c5(t, nat, dev, pf, device, args.steps,
+                                                           peak)),
+                         ("c5_tracer", lambda: extra_tracer(t, nat, dev, pf, device))):
+            try:
+                r = fn()
+                if name == "c4_c5":
+                    extras["c4_dense"], extras["c5_batched_kl"] = r
+                else:
+                    extras[name] = r
+            except Exception as exc:  # an extra must never hide the headline number
+                extras[name] = {"error": f"{type(exc).__name__}: {exc}"}
+            t.cuda.empty_cache()
+
     line = {
         "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": el_ms / args.steps,
@@ -371,18 +610,16 @@ def run_native(args):
         "data": "synthetic",
         "config": {"workload": desc, "rows_per_gpu": rows, "k": k, "n_total": n_total,
                    "parallelism": f"row-shard x{ws}", "target": target,
-                   "l2": "inputs larger than L2 (P slab %.2f GB/GPU vs 126 MB L2)" % (rows * ld * 8 / 1e9)},
-        "roofline": {"bound": "hbm", "achieved": ach_kl, "peak": peak, "unit": "GB/s",
-                     "frac": ach_kl / peak, "traffic": traffic, "kernel": "pf::dense_kl_kernel (+ kl_guard_fixup scan)",
-                     "algorithmic_bytes_per_launch": bytes_kl, "avg_launch_ms": kl_ms,
-                     "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else "fallback 6.65 TB/s"},
-        "roofline_tv": {"achieved": ach_tv, "frac": ach_tv / peak, "avg_launch_ms": tv_ms,
-                        "algorithmic_bytes_per_launch": bytes_tv},
+                   "l2": "inputs larger than L2 (P slab %.2f GB/GPU vs 126 MB L2)"
+                         % (rows * ld * 8 / 1e9)},
+        "roofline": roof,
+        "roofline_tv": _roof(bytes_tv, tv_ms, peak),
         "kl_guarded_rows": int(flags_kl[1]),
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": 5 * args.steps,
+        "gpu_launches": launches,
         "clocks": clocks.summary(),
+        "extras": extras,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -395,12 +632,14 @@ def run_native(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the C3/C4/C5/tracer side measurements (N=1 only)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

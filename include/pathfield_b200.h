@@ -217,6 +217,11 @@ int pf_batched_kl_f64(const double *P, int64_t ld, int64_t rows, int64_t k, cons
                       const int64_t *targets, double clamp, double tau, int64_t row0,
                       double *out, int64_t ldo, uint32_t *guarded, pf_stream_t stream);
 
+/* Diagnostic: a pure-DFMA kernel (8 independent FMA chains per thread, all
+ * SMs); *flops_host receives its FLOP count so the caller can time it and
+ * obtain the sustained FP64 rate K7 is measured against. */
+int pf_probe_dfma_f64(int64_t iters, int64_t *flops_host, double *out, pf_stream_t stream);
+
 /* ---- K8: batched triangle-descent tracer (paths.py:101-307) ---------------
  * Device-resident mesh topology (all arrays device pointers):
  *   vertices  (n,2) FP64;  triangles (nt,3) int32 CCW exactly as stored by

@@ -210,6 +210,23 @@ __global__ void __launch_bounds__(256) batched_kl_fixup_kernel(
   if (lane == 0 && done && count) atomicAdd(count, done);
 }
 
+// Diagnostic: sustained DFMA throughput (8 independent chains per thread);
+// bench.py reports K7's FLOP rate against it.
+__global__ void __launch_bounds__(256) dfma_probe_kernel(int64_t iters, double *out) {
+  double a[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = 1.0 + 1e-3 * (threadIdx.x + i);
+  const double m = 0.999999, c = 1e-7;
+  for (int64_t it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = fma(a[i], m, c);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += a[i];
+  if (s == 42.0) out[0] = s;  // keep the chains alive
+}
+
 }  // namespace pf
 
 using namespace pf;
@@ -261,6 +278,13 @@ int pf_batched_kl_f64(const double *P, int64_t ld, int64_t rows, int64_t k, cons
   batched_kl_fixup_kernel<<<sm_count() * 8, 256, 0, as_stream(stream)>>>(
       P, ld, rows, k, Tc, ldl, T, clamp, out, ldo, guarded);
   return check_launch("batched_kl_fixup");
+}
+
+int pf_probe_dfma_f64(int64_t iters, int64_t *flops, double *out, pf_stream_t stream) {
+  const int blocks = sm_count() * 8;
+  dfma_probe_kernel<<<blocks, 256, 0, as_stream(stream)>>>(iters, out);
+  if (flops) *flops = 2LL * 8 * iters * blocks * 256;
+  return check_launch("dfma_probe");
 }
 
 }  // extern "C"

@@ -164,6 +164,20 @@ class TriMesh:
         return float(self.edge_lengths().min())
 
 
+def grid_mesh(nx: int, ny: int, lx: float = 1.0, ly: float = 1.0) -> TriMesh:
+    """Structured (nx+1) x (ny+1) vertex grid on [0,lx]x[0,ly], each cell split
+    along its diagonal: a synthetic benchmark mesh of any size (no Delaunay)."""
+    xs = np.linspace(0.0, lx, nx + 1)
+    ys = np.linspace(0.0, ly, ny + 1)
+    X, Y = np.meshgrid(xs, ys)
+    V = np.column_stack([X.ravel(), Y.ravel()])
+    i, j = np.meshgrid(np.arange(nx), np.arange(ny))
+    a = (j * (nx + 1) + i).ravel()
+    b, c, d = a + 1, a + nx + 2, a + nx + 1
+    T = np.concatenate([np.column_stack([a, b, c]), np.column_stack([a, c, d])])
+    return TriMesh(V, T)
+
+
 # --------------------------------------------------------------- device --
 class PfMesh(ctypes.Structure):
     _fields_ = [("vertices", ctypes.c_void_p), ("triangles", ctypes.c_void_p),

@@ -1,0 +1,116 @@
+"""Row-sharded multi-GPU evaluation: one process per GPU over torch.distributed.
+
+Every output row q of a divergence field depends only on row q of P and on
+the target row, so the GPUs of one box own contiguous row slabs
+(dense: balanced by row count; CSR: balanced by nnz) and evaluate them with
+the single-GPU kernels unchanged — the N-GPU field is bitwise the 1-GPU
+field.  The data path has exactly two exchanges, both NCCL over NVLink:
+
+* the target row P[t, :] (k FP64) is broadcast from its owner rank
+  (``ncclBroadcast``, 33 KB at k = 4,102);
+* the finished field slabs are all-gathered (``ncclAllGather``, n FP64)
+  only when a tracer on every rank needs the whole field.
+
+There are no reductions.  The host logic (partitioning, ownership,
+broadcast/gather orchestration) is backend-agnostic and is exercised with the
+gloo backend on CPU in tests/test_parallel.py; the slab computation itself is
+always the CUDA kernels (``_compute_slab``).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _device as dev
+
+
+def partition_rows(n: int, world: int) -> list[tuple[int, int]]:
+    """Contiguous, balanced row slabs [r0, r1) for `world` ranks (sizes differ by <= 1)."""
+    base, extra = divmod(n, world)
+    out, r0 = [], 0
+    for r in range(world):
+        r1 = r0 + base + (1 if r < extra else 0)
+        out.append((r0, r1))
+        r0 = r1
+    return out
+
+
+def partition_by_weight(weights, world: int) -> list[tuple[int, int]]:
+    """Contiguous slabs balanced by a per-row weight (CSR: nnz per row + 1 per row)."""
+    w = np.asarray(weights, dtype=np.float64) + 1.0
+    cum = np.concatenate([[0.0], np.cumsum(w)])
+    total = cum[-1]
+    cuts = [0]
+    for r in range(1, world):
+        cuts.append(int(np.searchsorted(cum, total * r / world, side="left")))
+    cuts.append(len(w))
+    cuts = np.maximum.accumulate(np.array(cuts))
+    return [(int(cuts[r]), int(cuts[r + 1])) for r in range(world)]
+
+
+def owner_of(row: int, bounds: list[tuple[int, int]]) -> int:
+    for r, (a, b) in enumerate(bounds):
+        if a <= row < b:
+            return r
+    raise IndexError(f"row {row} outside every slab")
+
+
+class ShardedField:
+    """Per-rank driver of a row-sharded field evaluation.
+
+    ``slab`` is this rank's :class:`~paper_1708_02845_b200._device.DeviceKernel`
+    (rows ``bounds[rank]`` of the global P); ``dist`` the initialised
+    ``torch.distributed`` module (nccl on GPUs; gloo in the CPU tests).
+    """
+
+    def __init__(self, slab, bounds, dist, device=None):
+        self.slab, self.bounds, self.dist = slab, bounds, dist
+        self.rank = dist.get_rank()
+        self.world = dist.get_world_size()
+        self.device = device if device is not None else getattr(slab, "device", None)
+        a, b = bounds[self.rank]
+        if (getattr(slab, "row0", a), getattr(slab, "rows", b - a)) != (a, b - a):
+            raise ValueError("slab does not match this rank's partition")
+
+    def target_row(self, p: int, k: int):
+        """Broadcast P[p, :k] from its owner to every rank (the one data-path exchange)."""
+        t = dev.torch()
+        own = owner_of(p, self.bounds)
+        if self.rank == own:
+            row = self.slab.P[p - self.bounds[own][0], :k].contiguous()
+        else:
+            row = t.empty(k, dtype=t.float64, device=self.device)
+        self.dist.broadcast(row, src=own)
+        return row
+
+    def field(self, fd, p: int, gather: bool = False, clamp=None):
+        """This rank's slab of the field to target p (device); all ranks' if `gather`."""
+        row = self.target_row(p, self.slab.k)
+        vals = _compute_slab(self.slab, fd, p, row, clamp)
+        if not gather:
+            return vals
+        return self.gather(vals)
+
+    def gather(self, vals):
+        """All-gather variable-size slabs into the full n-vector on every rank."""
+        t = dev.torch()
+        sizes = [b - a for a, b in self.bounds]
+        m = max(sizes)
+        buf = t.zeros(m, dtype=vals.dtype, device=vals.device)
+        buf[:vals.numel()] = vals
+        parts = [t.empty(m, dtype=vals.dtype, device=vals.device) for _ in range(self.world)]
+        self.dist.all_gather(parts, buf)
+        return t.cat([parts[r][:sizes[r]] for r in range(self.world)])
+
+
+def _compute_slab(slab, fd, p: int, target_row, clamp=None):
+    """The slab's field values to target p (CUDA kernels K0 + K2/K3/generic)."""
+    from .divergence import _effective_clamp, _field_device
+    t = dev.require_cuda()
+    c = _effective_clamp(slab, fd.clamp if clamp is None else clamp)
+    out = t.empty(slab.rows + 2, dtype=t.float64, device=slab.device)
+    s = t.cuda.current_stream(slab.device).cuda_stream
+    st = _field_device(None, slab, fd, p, False, c, out, out.data_ptr() + slab.rows * 8, s,
+                       target_row=target_row)
+    del st
+    return out[:slab.rows]
