@@ -219,8 +219,8 @@ class DenseStep:
     With `sharded` (parallel.ShardedField) the target row is NCCL-broadcast."""
 
     def __init__(self, t, nat, dev, dk, target, tau, sharded=None):
-        self.t, self.nat, self.dk, self.target, self.tau, self.sh = t, nat, dev, dk, target, tau
-        self.dk = dk
+        self.t, self.nat, self.dk = t, nat, dk
+        self.target, self.tau, self.sh = target, tau, sharded
         k, rows = dk.k, dk.rows
         self.k_pad, m_pad = dev.round_up(k, 2), dev.round_up(k, 16)
         self.stage = t.empty(16 * self.k_pad + m_pad, dtype=t.uint8, device=dk.device)
