@@ -440,13 +440,13 @@ def extra_tracer(t, nat, dev, pf, device):
     src = rng.choice(mesh.n, npaths)
     fo = np.arange(npaths) % T
     src = np.where(src == targets[fo], (src + 1) % mesh.n, src)
-    PP.trace_arrays(mesh, [fields[0]], targets[:1], src[:64])  # warm-up
+    PP.trace_arrays(mesh, fields[:1], targets[:1], src[:64])  # warm-up
     t.cuda.synchronize()
     e0, e1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
     s = t.cuda.current_stream(device)
     w0 = time.perf_counter()
     e0.record(s)
-    buf, counts, over, extra = PP.trace_arrays(mesh, list(fields), targets, src, fo)
+    buf, counts, over, extra = PP.trace_arrays(mesh, fields, targets, src, fo)
     e1.record(s)
     t.cuda.synchronize()
     wall = time.perf_counter() - w0

@@ -93,11 +93,11 @@ def _fields_to_device(t, fields, n, device):
     """Stack field values (numpy or device tensors) into an (F, n) FP64 device tensor."""
     vals = []
     for f in fields:
-        v = f.values if hasattr(f, "values") else f
-        if hasattr(v, "is_cuda"):
+        v = f if isinstance(f, t.Tensor) else (f.values if hasattr(f, "values") else f)
+        if isinstance(v, t.Tensor):
             vals.append(v.to(device=device, dtype=t.float64).reshape(-1)[:n])
         else:
-            vals.append(t.from_numpy(np.ascontiguousarray(v, dtype=np.float64)).to(device))
+            vals.append(t.from_numpy(np.array(v, dtype=np.float64)).to(device))
     return t.stack(vals) if len(vals) > 1 else vals[0].reshape(1, -1).contiguous()
 
 
@@ -115,7 +115,10 @@ def trace_arrays(mesh, fields, targets, sources, field_of=None, settings: Settin
     targets = np.asarray(targets, dtype=np.int64)
     fo = None if field_of is None else np.asarray(field_of, dtype=np.int32)
     step_cap = int(settings.step_cap_factor) * dm.n
-    F = _fields_to_device(t, fields, dm.n, dm.device)
+    if isinstance(fields, t.Tensor) and fields.dim() == 2:   # (F, n) device block
+        F = fields.to(device=dm.device, dtype=t.float64).contiguous()
+    else:
+        F = _fields_to_device(t, fields, dm.n, dm.device)
     src_d = t.from_numpy(sources).to(dm.device)
     tgt_d = t.from_numpy(targets).to(dm.device)
     fo_d = None if fo is None else t.from_numpy(fo).to(dm.device)
