@@ -11,7 +11,7 @@ the device lifetime too.
 HBM layout of P (one slab per GPU; the whole matrix on one GPU):
   rows x ld FP64, row-major, ld = round_up(k, 16) so every row starts on a
   128-byte boundary (full-sector 128-bit streaming loads); pad columns are
-  never read.  Alongside: is_interior (uint8 per row) and the per-clamp
+  zero (only the batched GEMM streams them, multiplied by zero logs).  Alongside: is_interior (uint8 per row) and the per-clamp
   negentropy H (FP64 per row, K1), built lazily.
 """
 
@@ -80,6 +80,8 @@ class DeviceKernel:
         else:
             self.ld = leading_dim(self.k)
             self.P = t.empty((self.rows, self.ld), dtype=t.float64, device=self.device)
+            if self.ld > self.k:
+                self.P[:, self.k:] = 0.0  # pad columns are zero (K7 streams whole 16-col tiles)
             for a in range(0, self.rows, chunk_rows):
                 b = min(self.rows, a + chunk_rows)
                 src = np.array(dense[self.row0 + a:self.row0 + b], dtype=np.float64, order="C")

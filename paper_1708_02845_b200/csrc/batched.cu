@@ -9,10 +9,11 @@
 // clamped logs of the target rows: an FP64 GEMM n x T x k (C5: 1M x 1024 x
 // 4102 = 8.4 TFLOP) with a fused epilogue (split-form cancellation guard ->
 // sentinel, settle, KL[t, t] = 0).  tcgen05 has no FP64 kind, so the
-// contraction runs on the FP64 pipes: a register-blocked DFMA GEMM, 128x128
-// block tile, 8x8 outputs per thread, k-tiles of 16 double-buffered through
-// shared memory, the clamp applied while staging P.  Guarded pairs are
-// re-evaluated per element in the reference form by batched_kl_fixup.
+// contraction runs on the FP64 tensor-core path, mma.sync m8n8k4 (SASS
+// DMMA), fed by a 3-stage cp.async pipeline (scripts/tune_gemm.cu records
+// the DFMA and register-prefetch variants it replaced: 20-22 TFLOP/s vs
+// 29.3).  Guarded pairs are re-evaluated per element in the reference form
+// by batched_kl_fixup.
 //
 // The per-target `clamped` precision flag (divergence.py:172-175) is exact
 // without an n x T x k compare: all interior rows share one below-clamp mask
@@ -24,8 +25,7 @@
 
 namespace pf {
 
-constexpr int kBM = 128, kBN = 128, kBK = 16, kGemmThreads = 256;
-constexpr int kApad = kBM + 1, kBpad = kBN + 1;  // k-major tiles, padded rows
+constexpr int kBK = 16, kGemmThreads = 256;
 constexpr unsigned long long kBatchGuard = 0x7ff8dead0000ba7cull;
 
 // L[t, b] = log(max(Pt[t, b], clamp)), Tc[t, b] = max(Pt[t, b], clamp), zero
@@ -69,100 +69,122 @@ __global__ void mask_uniform_kernel(const double *__restrict__ P, int64_t ld, in
   if (__any_sync(0xffffffffu, diff) && lane == 0) atomicOr(out, 1u);
 }
 
-__global__ void __launch_bounds__(kGemmThreads, 1) batched_kl_gemm_kernel(
+__device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// ---------------------------------------------------------------------------
+// DMMA v2 (production): 3-stage cp.async pipeline (no register prefetch),
+// block tile 128 (q) x 64 (t), 8 warps as 4 (m) x 2 (n) with 32 x 32 warp
+// tiles (16 FP64 accumulators pairs per thread, ~100 registers: 2 CTAs/SM),
+// tiles stored [row][k] with a 20-double stride so every fragment load is
+// bank-conflict free.  Requires P and L pad columns (up to round_up(k,16))
+// to be finite: the clamp is applied to A fragments after the shared load and
+// pad columns of L are zero.
+constexpr int kV2BM = 128, kV2BN = 64, kV2S = kBK + 4, kV2Stages = 3;
+constexpr int kV2StageA = kV2BM * kV2S, kV2StageB = kV2BN * kV2S;
+
+__device__ __forceinline__ void cp_async16(void *dst, const void *src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__global__ void __launch_bounds__(kGemmThreads, 2) batched_kl_dmma2_kernel(
     const double *__restrict__ P, int64_t ld, int64_t rows, int64_t k,
     const double *__restrict__ H, const double *__restrict__ L, int64_t ldl, int64_t T,
     const int64_t *__restrict__ targets, double clamp, double tau, int64_t row0,
     double *__restrict__ out, int64_t ldo) {
   extern __shared__ __align__(128) unsigned char smem[];
-  double *As = reinterpret_cast<double *>(smem);      // [2][kBK][kApad]
-  double *Bs = As + 2 * kBK * kApad;                   // [2][kBK][kBpad]
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * kBN;
-  const int64_t q0 = static_cast<int64_t>(blockIdx.y) * kBM;
+  double *As = reinterpret_cast<double *>(smem);           // [stages][128][20]
+  double *Bs = As + kV2Stages * kV2StageA;                   // [stages][64][20]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1;
+  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * kV2BN;
+  const int64_t q0 = static_cast<int64_t>(blockIdx.y) * kV2BM;
   const int64_t nkt = (k + kBK - 1) / kBK;
+  const int fr = lane >> 2, fc = lane & 3;
 
-  double acc[8][8];
+  auto issue = [&](int64_t kt) {
+    if (kt < nkt) {
+      const int st = static_cast<int>(kt % kV2Stages);
+      double *as = As + st * kV2StageA, *bs = Bs + st * kV2StageB;
+      const int64_t k0 = kt * kBK;
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
-#pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
-
-  double2 ra[4], rb[4];
-  auto load_tile = [&](int64_t kt) {
-    const int64_t k0 = kt * kBK;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int e = tid + kGemmThreads * u;  // 0..1023
-      const int row = e >> 3, kp = (e & 7) * 2;
-      const int64_t q = q0 + row, kk = k0 + kp;
-      double2 a = make_double2(0.0, 0.0);
-      if (q < rows && kk < k) {
-        a = *reinterpret_cast<const double2 *>(P + q * ld + kk);
-        a.x = fmax(a.x, clamp);
-        a.y = (kk + 1 < k) ? fmax(a.y, clamp) : 0.0;
+      for (int u = 0; u < 4; ++u) {  // A: 128 rows x 8 chunks of 16 B
+        const int e = tid + kGemmThreads * u, row = e >> 3, ch = e & 7;
+        const int64_t q = q0 + row;
+        const bool ok = q < rows;
+        cp_async16(as + row * kV2S + 2 * ch, P + (ok ? q : 0) * ld + k0 + 2 * ch, ok);
       }
-      ra[u] = a;
-      const int64_t t = t0 + row;
-      double2 b = make_double2(0.0, 0.0);
-      if (t < T) b = *reinterpret_cast<const double2 *>(L + t * ldl + kk);  // zero-padded
-      rb[u] = b;
-    }
-  };
-  auto store_tile = [&](int buf) {
-    double *as = As + buf * kBK * kApad, *bs = Bs + buf * kBK * kBpad;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int e = tid + kGemmThreads * u;
-      const int row = e >> 3, kp = (e & 7) * 2;
-      as[kp * kApad + row] = ra[u].x;
-      as[(kp + 1) * kApad + row] = ra[u].y;
-      bs[kp * kBpad + row] = rb[u].x;
-      bs[(kp + 1) * kBpad + row] = rb[u].y;
+      for (int u = 0; u < 2; ++u) {  // B: 64 targets x 8 chunks
+        const int e = tid + kGemmThreads * u, row = e >> 3, ch = e & 7;
+        const int64_t t = t0 + row;
+        const bool ok = t < T;
+        cp_async16(bs + row * kV2S + 2 * ch, L + (ok ? t : 0) * ldl + k0 + 2 * ch, ok);
+      }
     }
+    cp_async_commit();
   };
 
-  load_tile(0);
-  store_tile(0);
-  __syncthreads();
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < kV2Stages - 1; ++s) issue(s);
   for (int64_t kt = 0; kt < nkt; ++kt) {
-    const int buf = kt & 1;
-    if (kt + 1 < nkt) load_tile(kt + 1);
-    const double *as = As + buf * kBK * kApad, *bs = Bs + buf * kBK * kBpad;
-#pragma unroll
-    for (int kk = 0; kk < kBK; ++kk) {
-      double a[8], b[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) a[i] = as[kk * kApad + ty + 16 * i];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) b[j] = bs[kk * kBpad + tx + 16 * j];
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
-    }
-    if (kt + 1 < nkt) store_tile(buf ^ 1);
+    cp_async_wait<kV2Stages - 2>();
     __syncthreads();
-  }
-
-  // fused epilogue: H - cross, guard, settle, zero at the target
+    issue(kt + kV2Stages - 1);
+    const int st = static_cast<int>(kt % kV2Stages);
+    const double *as = As + st * kV2StageA + (wm * 32 + fr) * kV2S + fc;
+    const double *bs = Bs + st * kV2StageB + (wn * 32 + fr) * kV2S + fc;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int64_t q = q0 + ty + 16 * i;
+    for (int ks = 0; ks < kBK; ks += 4) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = fmax(as[8 * i * kV2S + ks], clamp);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = bs[8 * j * kV2S + ks];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+  }
+  cp_async_wait<0>();
+
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t q = q0 + wm * 32 + 8 * i + fr;
     if (q >= rows) continue;
     const double h = H[q];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int64_t t = t0 + tx + 16 * j;
-      if (t >= T) continue;
-      const double cross = acc[i][j];
-      double val = h - cross;
-      const bool is_t = (row0 + q == targets[t]);
-      if (!is_t && fabs(val) < tau * (fabs(h) + fabs(cross)))
-        val = __longlong_as_double(static_cast<long long>(kBatchGuard));
-      else
-        val = is_t ? 0.0 : settle(val);
-      out[q * ldo + t] = val;
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int64_t t = t0 + wn * 32 + 8 * j + 2 * fc + c;
+        if (t >= T) continue;
+        const double cross = acc[i][j][c];
+        double val = h - cross;
+        const bool is_t = (row0 + q == targets[t]);
+        if (!is_t && fabs(val) < tau * (fabs(h) + fabs(cross)))
+          val = __longlong_as_double(static_cast<long long>(kBatchGuard));
+        else
+          val = is_t ? 0.0 : settle(val);
+        out[q * ldo + t] = val;
+      }
     }
   }
 }
@@ -177,8 +199,10 @@ __global__ void __launch_bounds__(256) batched_kl_fixup_kernel(
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t total = rows * T;
   uint32_t done = 0;
-  for (int64_t base = warp * 32; base < total; base += nwarps * 32) {
-    const int64_t mine = base + lane;
+  // (q, t) entries interleaved across warps: guarded pairs cluster near each
+  // target's row, so neighbouring entries must land on different warps.
+  for (int64_t i0 = 0; warp + i0 * nwarps < total; i0 += 32) {
+    const int64_t mine = warp + (i0 + lane) * nwarps;
     const int64_t mq = mine / T, mt = mine - mq * T;
     const bool flag = mine < total && static_cast<unsigned long long>(__double_as_longlong(
                                           out[mq * ldo + mt])) == kBatchGuard;
@@ -186,7 +210,7 @@ __global__ void __launch_bounds__(256) batched_kl_fixup_kernel(
     while (ball) {
       const int src = __ffs(ball) - 1;
       ball &= ball - 1;
-      const int64_t e = base + src, q = e / T, t = e - q * T;
+      const int64_t e = warp + (i0 + src) * nwarps, q = e / T, t = e - q * T;
       const double *prow = P + q * ld;
       const double *trow = Tc + t * ldl;
       double b[4] = {0.0, 0.0, 0.0, 0.0};
@@ -262,17 +286,19 @@ int pf_batched_kl_f64(const double *P, int64_t ld, int64_t rows, int64_t k, cons
   if (!P || !H || !L || !Tc || !targets || !out) return fail(PF_E_ARG, "batched_kl: null");
   if ((ld & 1) || (reinterpret_cast<uintptr_t>(P) & 15) || ldl % 16 || ldl < k || ldo < T)
     return fail(PF_E_ALIGN, "batched_kl: alignment (ld even, ldl %% 16 == 0)");
-  const size_t smem = 2 * kBK * (kApad + kBpad) * sizeof(double);
+  const size_t smem = static_cast<size_t>(kV2Stages) * (kV2StageA + kV2StageB) * sizeof(double);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(batched_kl_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(batched_kl_dmma2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
     attr = true;
   }
-  dim3 grid(static_cast<unsigned>((T + kBN - 1) / kBN), static_cast<unsigned>((rows + kBM - 1) / kBM));
+  dim3 grid(static_cast<unsigned>((T + kV2BN - 1) / kV2BN),
+            static_cast<unsigned>((rows + kV2BM - 1) / kV2BM));
   if (grid.y > 65535) return fail(PF_E_DOMAIN, "batched_kl: too many rows per launch (%lld)",
                                   (long long)rows);
-  batched_kl_gemm_kernel<<<grid, kGemmThreads, smem, as_stream(stream)>>>(
+  if (ld % 16) return fail(PF_E_ALIGN, "batched_kl: ld must be a multiple of 16 (pad columns zero)");
+  batched_kl_dmma2_kernel<<<grid, kGemmThreads, smem, as_stream(stream)>>>(
       P, ld, rows, k, H, L, ldl, T, targets, clamp, tau, row0, out, ldo);
   if (int e = check_launch("batched_kl_gemm")) return e;
   batched_kl_fixup_kernel<<<sm_count() * 8, 256, 0, as_stream(stream)>>>(

@@ -238,21 +238,26 @@ __global__ void __launch_bounds__(kCsrThreads) csr_kl_fixup_kernel(
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t count = queries ? nq : rows;
   uint32_t done = 0;
-  for (int64_t base = warp * 32; base < count; base += nwarps * 32) {
-    const int64_t mine = base + lane;
+  // interleaved rows (see kl_guard_fixup_kernel): clustered guards spread out
+  for (int64_t i0 = 0; warp + i0 * nwarps < count; i0 += 32) {
+    const int64_t mine = warp + (i0 + lane) * nwarps;
     const bool flag = mine < count && static_cast<unsigned long long>(
                                           __double_as_longlong(out[mine])) == kCsrGuard;
     unsigned ball = __ballot_sync(0xffffffffu, flag);
     while (ball) {
       const int src = __ffs(ball) - 1;
       ball &= ball - 1;
-      const int64_t i = base + src;
+      const int64_t i = warp + (i0 + src) * nwarps;
       const int64_t r = queries ? queries[i] - row0 : i;
       const int64_t lo = indptr[r], hi = indptr[r + 1];
-      double a = 0.0;
-      for (int64_t e = lo + lane; e < hi; e += 32)
-        a += __dmul_rn(data[e], log_data[e] - logt[indices[e]]);
-      const double val = settle(warp_sum(a));
+      double a0 = 0.0, a1 = 0.0;
+      int64_t e = lo + lane;
+      for (; e + 32 < hi; e += 64) {
+        a0 += __dmul_rn(data[e], log_data[e] - logt[indices[e]]);
+        a1 += __dmul_rn(data[e + 32], log_data[e + 32] - logt[indices[e + 32]]);
+      }
+      if (e < hi) a0 += __dmul_rn(data[e], log_data[e] - logt[indices[e]]);
+      const double val = settle(warp_sum(a0 + a1));
       if (lane == 0) out[i] = val;
       ++done;
     }
@@ -403,7 +408,7 @@ int pf_csr_kl_f64(const int64_t *indptr, const int32_t *indices, const double *d
         indptr, indices, data, hs, rows, k_pad, logt, tau, row0, queries, nq, out, ops);
   }
   if (int e = check_launch("csr_kl")) return e;
-  int64_t want = (count + 32 * 8 - 1) / (32 * 8);
+  int64_t want = (count + 7) / 8;
   int64_t g2 = static_cast<int64_t>(sm_count()) * 4;
   if (g2 > want) g2 = want;
   if (g2 < 1) g2 = 1;

@@ -291,15 +291,18 @@ __global__ void __launch_bounds__(kThreads) kl_guard_fixup_kernel(
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   uint32_t done = 0;
-  for (int64_t base = warp * 32; base < rows; base += nwarps * 32) {
-    const int64_t mine = base + lane;
+  // Rows are interleaved across warps (row = warp + (32 i + lane) * nwarps):
+  // guarded rows cluster around the target, so consecutive rows must land on
+  // different warps for the recompute to spread over the GPU.
+  for (int64_t i0 = 0; warp + i0 * nwarps < rows; i0 += 32) {
+    const int64_t mine = warp + (i0 + lane) * nwarps;
     const bool flag = mine < rows && static_cast<unsigned long long>(__double_as_longlong(
                                          out[mine])) == kGuardSentinel;
     unsigned ball = __ballot_sync(0xffffffffu, flag);
     while (ball) {
       const int src = __ffs(ball) - 1;
       ball &= ball - 1;
-      const int64_t r = base + src;
+      const int64_t r = warp + (i0 + src) * nwarps;
       const double *prow = P + r * ld;
       double b[4] = {0.0, 0.0, 0.0, 0.0};
       int64_t e = lane;
@@ -444,7 +447,7 @@ static int launch_dense(K staged, K unstaged, int64_t rows, int64_t k, cudaStrea
 static int launch_kl_fixup(const double *P, int64_t ld, int64_t rows, int64_t k,
                            const double *tgt, double clamp, double *out, uint32_t *flags,
                            cudaStream_t stream) {
-  int64_t want = (rows + 32 * kWarpsPerCta - 1) / (32 * kWarpsPerCta);
+  int64_t want = (rows + kWarpsPerCta - 1) / kWarpsPerCta;
   int64_t g = static_cast<int64_t>(sm_count()) * 4;
   if (g > want) g = want;
   if (g < 1) g = 1;
