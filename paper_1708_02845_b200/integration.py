@@ -1,0 +1,106 @@
+"""Drop-in routing of the reference package ``pathfield`` to the B200 path.
+
+``install()`` rebinds the reference's hot-path functions at every binding
+site listed in SURVEY §8b (the names are imported with ``from ... import``,
+so each site is patched explicitly):
+
+    pathfield.divergence.{dv_field, dv_at, dv_pair, sparsify,
+                          dv_pair_sparse, dv_pair_sparse_stats}
+    pathfield.{dv_field, dv_pair, dv_pair_sparse, sparsify,
+               triangle_descent, triangle_gradient}          (__init__.py:4-13)
+    pathfield.domain.{dv_field, sparsify, triangle_descent}  (domain.py:17-22)
+    pathfield.bench.{dv_at, dv_field, dv_pair_sparse_stats}  (bench.py:25)
+    pathfield.paths.{triangle_descent, triangle_gradient}
+
+Results are converted to the reference's own dataclasses (``ScalarField``,
+``TracedPath``), and the reference's ``PoissonKernel`` objects are accepted
+as-is (the device cache keys on ``pk.dense``), so ``DomainContext``, the
+service and the CLI run unchanged on the GPU.  Exceptions keep the
+reference's types: ``errors.py`` re-exports ``pathfield.errors`` whenever the
+reference is importable, and argument validation precedes every launch.
+
+Call ``install()`` before importing modules that bind these names with
+``from pathfield... import`` (e.g. from a pytest plugin or a conftest), as
+the SURVEY's patch-point list notes.
+"""
+
+from __future__ import annotations
+
+import importlib
+
+from . import divergence as _div
+from . import paths as _paths
+
+_ORIGINAL: dict = {}
+
+
+def _ref_types(pathfield):
+    solvers = importlib.import_module(pathfield.__name__ + ".solvers")
+    paths = importlib.import_module(pathfield.__name__ + ".paths")
+    return solvers.ScalarField, paths.TracedPath
+
+
+def _wrap(pathfield):
+    RefField, RefPath = _ref_types(pathfield)
+
+    def to_field(f):
+        return RefField(f.values, f.kind, f.target, f.params, f.sign, f.residual,
+                        f.precision_flags)
+
+    def to_path(p):
+        return RefPath(p.points, p.locations, p.source, p.target, p.status, p.stuck_vertex)
+
+    def dv_field(pk, fd, p, swap_order=False, clamp=None):
+        return to_field(_div.dv_field(pk, fd, p, swap_order=swap_order, clamp=clamp))
+
+    def triangle_descent(mesh, field, source, settings=None):
+        from .config import DEFAULTS
+        return to_path(_paths.triangle_descent(mesh, field, source, settings or DEFAULTS))
+
+    return {
+        "dv_field": dv_field,
+        "dv_at": _div.dv_at,
+        "dv_pair": _div.dv_pair,
+        "sparsify": _div.sparsify,
+        "dv_pair_sparse": _div.dv_pair_sparse,
+        "dv_pair_sparse_stats": _div.dv_pair_sparse_stats,
+        "triangle_descent": triangle_descent,
+        "triangle_gradient": _paths.triangle_gradient,
+    }
+
+
+SITES = {
+    "divergence": ("dv_field", "dv_at", "dv_pair", "sparsify", "dv_pair_sparse",
+                   "dv_pair_sparse_stats"),
+    "": ("dv_field", "dv_pair", "dv_pair_sparse", "sparsify", "triangle_descent",
+         "triangle_gradient"),
+    "domain": ("dv_field", "sparsify", "triangle_descent"),
+    "bench": ("dv_at", "dv_field", "dv_pair_sparse_stats"),
+    "paths": ("triangle_descent", "triangle_gradient"),
+}
+
+
+def install(pathfield=None) -> dict:
+    """Patch the reference's binding sites; returns {site: [names]} patched."""
+    if pathfield is None:
+        pathfield = importlib.import_module("pathfield")
+    repl = _wrap(pathfield)
+    done = {}
+    for sub, names in SITES.items():
+        try:
+            mod = importlib.import_module(pathfield.__name__ + ("." + sub if sub else ""))
+        except Exception:  # e.g. bench needs jsonschema; skip what cannot import
+            continue
+        for name in names:
+            if hasattr(mod, name):
+                _ORIGINAL.setdefault((mod.__name__, name), getattr(mod, name))
+                setattr(mod, name, repl[name])
+                done.setdefault(mod.__name__, []).append(name)
+    return done
+
+
+def uninstall() -> None:
+    """Restore every binding ``install`` replaced."""
+    for (modname, name), fn in list(_ORIGINAL.items()):
+        setattr(importlib.import_module(modname), name, fn)
+    _ORIGINAL.clear()
