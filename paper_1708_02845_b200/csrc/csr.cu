@@ -141,6 +141,42 @@ __global__ void csr_dropped_kernel(const int64_t *__restrict__ indptr,
   }
 }
 
+// Visit the CSR segment [lo, hi) of one row across a warp with 16-byte data
+// loads (double2) and 8-byte index loads (int2): an odd head element is
+// peeled so the vector body is aligned, the body is unrolled 2x for loads in
+// flight, and an odd tail goes to lane 0.  The per-lane visiting order is a
+// fixed function of (lo, hi), which K6 relies on (csr_target_prep sums S_p
+// with this same traversal, so TV(p, p) cancels exactly).
+template <class F>
+__device__ __forceinline__ void csr_row_visit(const double *__restrict__ data,
+                                              const int32_t *__restrict__ idx, int64_t lo,
+                                              int64_t hi, int lane, F &&f) {
+  int64_t s = lo;
+  if ((s & 1) && s < hi) {
+    if (lane == 0) f(__ldg(data + s), __ldg(idx + s));
+    ++s;
+  }
+  const int64_t npairs = (hi - s) >> 1;
+  const double2 *d2 = reinterpret_cast<const double2 *>(data + s);
+  const int2 *i2 = reinterpret_cast<const int2 *>(idx + s);
+  int64_t j = lane;
+  for (; j + 32 < npairs; j += 64) {
+    const double2 va = __ldg(d2 + j), vb = __ldg(d2 + j + 32);
+    const int2 ca = __ldg(i2 + j), cb = __ldg(i2 + j + 32);
+    f(va.x, ca.x);
+    f(va.y, ca.y);
+    f(vb.x, cb.x);
+    f(vb.y, cb.y);
+  }
+  if (j < npairs) {
+    const double2 va = __ldg(d2 + j);
+    const int2 ca = __ldg(i2 + j);
+    f(va.x, ca.x);
+    f(va.y, ca.y);
+  }
+  if (((hi - s) & 1) && lane == 0) f(__ldg(data + hi - 1), __ldg(idx + hi - 1));
+}
+
 // ---------------------------------------------------- K5/K6 target prep --
 // vp[k_pad]: the sparsified target row scattered dense (0 off-support);
 // tscal[0] = S_p (reduced in the K6 lane order), tscal[1] = dropped[p],
@@ -158,7 +194,7 @@ __global__ void csr_target_prep_kernel(const int64_t *__restrict__ indptr,
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
     double a = 0.0;
-    for (int64_t i = lo + lane; i < hi; i += 32) a += data[i];
+    csr_row_visit(data, indices, lo, hi, lane, [&](double v, int32_t) { a += v; });
     a = warp_sum(a);
     if (lane == 0) {
       tscal[0] = a;
@@ -197,24 +233,22 @@ __global__ void __launch_bounds__(kCsrThreads) csr_kl_kernel(
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t count = queries ? nq : rows;
-  for (int64_t i = warp; i < count; i += nwarps) {
-    const int64_t r = queries ? queries[i] - row0 : i;
-    const int64_t lo = indptr[r], hi = indptr[r + 1];
+  int64_t i = warp;
+  int64_t r = i < count ? (queries ? queries[i] - row0 : i) : 0;
+  int64_t lo = i < count ? indptr[r] : 0, hi = i < count ? indptr[r + 1] : 0;
+  while (i < count) {
+    // prefetch the next row's extent while this row streams
+    const int64_t i2 = i + nwarps;
+    const int64_t r2 = i2 < count ? (queries ? queries[i2] - row0 : i2) : 0;
+    const int64_t lo2 = i2 < count ? indptr[r2] : 0, hi2 = i2 < count ? indptr[r2 + 1] : 0;
     const double h = hs[r];
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    int64_t e = lo + lane;
-    for (; e + 96 < hi; e += 128) {
-      const double v0 = __ldg(data + e), v1 = __ldg(data + e + 32), v2 = __ldg(data + e + 64),
-                   v3 = __ldg(data + e + 96);
-      const int32_t c0 = __ldg(indices + e), c1 = __ldg(indices + e + 32),
-                    c2 = __ldg(indices + e + 64), c3 = __ldg(indices + e + 96);
-      a0 = fma(v0, lt[c0], a0);
-      a1 = fma(v1, lt[c1], a1);
-      a2 = fma(v2, lt[c2], a2);
-      a3 = fma(v3, lt[c3], a3);
-    }
-    for (; e < hi; e += 32) a0 = fma(__ldg(data + e), lt[__ldg(indices + e)], a0);
-    const double cross = warp_sum((a0 + a1) + (a2 + a3));
+    double a0 = 0.0, a1 = 0.0;
+    bool odd = false;
+    csr_row_visit(data, indices, lo, hi, lane, [&](double v, int32_t c) {
+      if (odd) a1 = fma(v, lt[c], a1); else a0 = fma(v, lt[c], a0);
+      odd = !odd;
+    });
+    const double cross = warp_sum(a0 + a1);
     double val = h - cross;
     if (fabs(val) < tau * (fabs(h) + fabs(cross)))
       val = __longlong_as_double(static_cast<long long>(kCsrGuard));
@@ -224,6 +258,10 @@ __global__ void __launch_bounds__(kCsrThreads) csr_kl_kernel(
       out[i] = val;
       if (ops) ops[i] = hi - lo;  // divergence.py:276
     }
+    i = i2;
+    r = r2;
+    lo = lo2;
+    hi = hi2;
   }
 }
 
@@ -281,20 +319,23 @@ __global__ void __launch_bounds__(kCsrThreads) csr_tv_kernel(
   const int64_t count = queries ? nq : rows;
   const double S_p = tscal[0], d_p = tscal[1];
   const int64_t nnz_p = static_cast<int64_t>(tscal[2]);
-  for (int64_t i = warp; i < count; i += nwarps) {
-    const int64_t r = queries ? queries[i] - row0 : i;
-    const int64_t lo = indptr[r], hi = indptr[r + 1];
+  int64_t i = warp;
+  int64_t r = i < count ? (queries ? queries[i] - row0 : i) : 0;
+  int64_t lo = i < count ? indptr[r] : 0, hi = i < count ? indptr[r + 1] : 0;
+  while (i < count) {
+    const int64_t i2 = i + nwarps;
+    const int64_t r2 = i2 < count ? (queries ? queries[i2] - row0 : i2) : 0;
+    const int64_t lo2 = i2 < count ? indptr[r2] : 0, hi2 = i2 < count ? indptr[r2 + 1] : 0;
     const double d_q = dropped[r];
-    // single per-lane accumulator in element order (matches csr_target_prep's
-    // S_p order so that q == p cancels exactly)
+    // one accumulator per lane in csr_row_visit order (S_p uses the same order,
+    // so q == p cancels exactly)
     double a = 0.0;
     int inter = 0;
-    for (int64_t e = lo + lane; e < hi; e += 32) {
-      const double v = __ldg(data + e);
-      const double w = v_p[__ldg(indices + e)];
+    csr_row_visit(data, indices, lo, hi, lane, [&](double v, int32_t c) {
+      const double w = v_p[c];
       a += fabs(v - w) - w;
       inter += (w != 0.0);
-    }
+    });
     const double base = warp_sum(a) + S_p;
     const double val = base + (d_p + d_q);  // divergence.py:293-295 (no settle)
     if (ops) {
@@ -305,6 +346,10 @@ __global__ void __launch_bounds__(kCsrThreads) csr_tv_kernel(
       out[i] = val;
       if (ops) ops[i] = (hi - lo) + nnz_p - inter;  // |union|, divergence.py:289
     }
+    i = i2;
+    r = r2;
+    lo = lo2;
+    hi = hi2;
   }
 }
 
