@@ -215,3 +215,36 @@ def dv_field_sparse(sv, name, p, rows=None):
     n = sv["indptr"].size - 1
     rows = range(n) if rows is None else rows
     return np.array([dv_pair_sparse_stats(sv, name, p, int(q))[0] for q in rows])
+
+
+def _kept_row(dense, cut, strict, r):
+    row = dense[r]
+    keep = (row > 0) if strict else (row >= cut)
+    keep &= row != 0.0
+    idx = np.flatnonzero(keep)
+    vals = row[idx]
+    s = np.add.reduceat(vals, [0])[0] if vals.size else 0.0  # scipy csr.sum(axis=1) order
+    return idx, vals, max(0.0, 1.0 - s)
+
+
+def dv_pair_sparse_direct(dense, p, q, name, threshold=None):
+    """dv_pair_sparse_stats for one pair straight from the dense rows (no full CSR):
+    the same formulas as :func:`dv_pair_sparse_stats` on the rows of sparsify
+    (divergence.py:212-228, 255-295) — for inputs too large to sparsify on the host."""
+    n, k = dense.shape
+    if threshold is None:
+        threshold = 1.0 / math.sqrt(n)
+    cut = threshold / k
+    strict = threshold == 0
+    idx_p, val_p, drop_p = _kept_row(dense, cut, strict, p)
+    idx_q, val_q, drop_q = _kept_row(dense, cut, strict, q)
+    if name == "kl":
+        log_q = np.log(val_q)
+        lp = np.log(np.maximum(dense[p, idx_q], CLAMP_LOG))
+        return settle(float(val_q @ (log_q - lp))), int(idx_q.size)
+    union = np.union1d(idx_p, idx_q)
+    vp = np.zeros(union.size)
+    vp[np.searchsorted(union, idx_p)] = val_p
+    vq = np.zeros(union.size)
+    vq[np.searchsorted(union, idx_q)] = val_q
+    return float(np.abs(vp - vq).sum()) + float(drop_p + drop_q), int(union.size)

@@ -246,6 +246,60 @@ def poisson_kernel(mesh: Mesh, col_chunk: int | None = None) -> tuple[np.ndarray
     return dense, boundary
 
 
+def _solve_cols(args):
+    """Worker: factor -L_II once, solve a column range of -L_IB into shared memory."""
+    shm_name, shape, interior_size, cols, lc_ii, lc_ib = args
+    from multiprocessing import shared_memory
+    shm = shared_memory.SharedMemory(name=shm_name)
+    try:
+        out = np.ndarray(shape, dtype=np.float64, buffer=shm.buf)
+        lu = splu((-lc_ii).tocsc())
+        a, b = cols
+        for c0 in range(a, b, 64):
+            c1 = min(b, c0 + 64)
+            x = lu.solve(np.asarray(lc_ib[:, c0:c1].toarray(), dtype=float))
+            tiny = (x > -1e-12) & (x < 0.0)
+            x[tiny] = 0.0
+            out[:, c0:c1] = x
+    finally:
+        shm.close()
+    return cols
+
+
+def poisson_kernel_parallel(mesh: Mesh, workers: int = 8):
+    """poisson_kernel for large meshes: `workers` processes each factor -L_II
+    (SuperLU, as solvers.py:278-303) and solve a column range in 64-column
+    chunks into shared memory.  Column-chunked solves differ from the
+    all-columns solve by ~1e-17 absolute; there is no reference
+    P at this size to compare against, so the returned P is the shared input."""
+    from concurrent.futures import ProcessPoolExecutor
+    from multiprocessing import get_context, shared_memory
+    lc = cotan_laplacian(mesh)
+    bmask = mesh.boundary_mask()
+    boundary = np.flatnonzero(bmask)
+    interior = np.flatnonzero(~bmask)
+    n, k = mesh.n, boundary.size
+    lc_i = lc[interior]
+    lc_ii = lc_i[:, interior].tocsr()
+    lc_ib = lc_i[:, boundary].tocsc()
+    shm = shared_memory.SharedMemory(create=True, size=max(8, interior.size * k * 8))
+    try:
+        shape = (interior.size, k)
+        bounds = np.linspace(0, k, workers + 1).astype(int)
+        jobs = [(shm.name, shape, interior.size, (int(a), int(b)), lc_ii, lc_ib)
+                for a, b in zip(bounds[:-1], bounds[1:]) if b > a]
+        with ProcessPoolExecutor(len(jobs), mp_context=get_context("fork")) as ex:
+            list(ex.map(_solve_cols, jobs))
+        p_ib = np.ndarray(shape, dtype=np.float64, buffer=shm.buf)
+        dense = np.zeros((n, k))
+        dense[boundary, np.arange(k)] = 1.0
+        dense[interior] = p_ib
+    finally:
+        shm.close()
+        shm.unlink()
+    return dense, boundary
+
+
 def default_endpoints(mesh: Mesh) -> tuple[int, int]:
     """domain.py:155-165."""
     interior = mesh.interior_vertices

@@ -20,6 +20,7 @@ Prints one JSON object.
 from __future__ import annotations
 
 import json
+import os
 import sys
 import time
 from pathlib import Path
@@ -34,6 +35,9 @@ SPECS = {
     "c2p": {"gen": "rectangle", "length": 1.5, "width": 1.0, "spacing": 0.00405},
     "holes16k": {"gen": "holes", "spacing": 0.0125},
     "holes100k": {"gen": "holes", "spacing": 0.005},
+    # C4: 20 small circular obstacles, n = 1,000,386, k = 4,102
+    "c4": {"gen": "holes", "spacing": 0.0017, "size": [2.0, 1.25],
+           "holes": [[0.2 + 0.4 * i, 0.16 + 0.31 * j, 0.0034] for i in range(5) for j in range(4)]},
 }
 
 
@@ -60,7 +64,10 @@ def main(name: str):
     mesh = I.build(SPECS[name])
     res["mesh_s"] = time.perf_counter() - t0
     t0 = time.perf_counter()
-    dense, boundary = I.poisson_kernel(mesh)
+    if mesh.n > 200_000:
+        dense, boundary = I.poisson_kernel_parallel(mesh, workers=int(os.environ.get("PF_WORKERS", "8")))
+    else:
+        dense, boundary = I.poisson_kernel(mesh)
     res["poisson_kernel_s"] = time.perf_counter() - t0
     n, k = dense.shape
     res.update(n=n, k=k)
@@ -99,24 +106,56 @@ def main(name: str):
     res["kl_guard_study"] = study
 
     # sparse
-    t0 = time.perf_counter()
-    spk = pf.sparsify(pk)
-    res["sparsify_gpu_s"] = time.perf_counter() - t0
-    sv = O.sparsify(dense, boundary)
-    res["csr_pattern_bitwise"] = bool(np.array_equal(spk.sparse.indptr, sv["indptr"])
-                                      and np.array_equal(spk.sparse.indices, sv["indices"])
-                                      and np.array_equal(spk.sparse.data, sv["data"]))
-    res["dropped_bitwise"] = bool(np.array_equal(spk.dropped_mass, sv["dropped"]))
-    res["nnz"] = int(spk.sparse.nnz)
-    res["sparsity_percent"] = spk.sparsity_percent
-    rows = rng.choice(n, min(n, 4000), replace=False)
+    import math
+    thr = 1.0 / math.sqrt(n)
+    cut = thr / k
+    rows = rng.choice(n, min(n, 2000), replace=False)
+    if n <= 500_000:
+        t0 = time.perf_counter()
+        spk = pf.sparsify(pk)
+        res["sparsify_gpu_s"] = time.perf_counter() - t0
+        sv = O.sparsify(dense, boundary)
+        res["csr_pattern_bitwise"] = bool(np.array_equal(spk.sparse.indptr, sv["indptr"])
+                                          and np.array_equal(spk.sparse.indices, sv["indices"])
+                                          and np.array_equal(spk.sparse.data, sv["data"]))
+        res["dropped_bitwise"] = bool(np.array_equal(spk.dropped_mass, sv["dropped"]))
+        res["nnz"] = int(spk.sparse.nnz)
+        res["sparsity_percent"] = spk.sparsity_percent
+        ref_pair = lambda g, q: O.dv_pair_sparse_stats(sv, g, t, int(q))[0]  # noqa: E731
+    else:
+        # too large for host CSR copies (nnz ~ 2e9): check sampled rows of the device CSR
+        import dataclasses
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        dc = dk.csr(cut, False)
+        torch.cuda.synchronize()
+        res["sparsify_gpu_s"] = time.perf_counter() - t0
+        indptr = dc.indptr.cpu().numpy()
+        dropped = dc.dropped.cpu().numpy()
+        ok_pat = ok_drop = True
+        for r in rows[:500]:
+            a, b = int(indptr[r]), int(indptr[r + 1])
+            idx = dc.indices[a:b].cpu().numpy()
+            dat = dc.data[a:b].cpu().numpy()
+            ridx, rval, rdrop = O._kept_row(dense, cut, False, int(r))
+            ok_pat &= bool(np.array_equal(idx, ridx) and np.array_equal(dat, rval))
+            ok_drop &= bool(dropped[r] == rdrop)
+        res["csr_pattern_bitwise_sampled_rows"] = 500
+        res["csr_pattern_bitwise"] = ok_pat
+        res["dropped_bitwise"] = ok_drop
+        res["nnz"] = int(dc.nnz)
+        res["sparsity_percent"] = 100.0 * (1.0 - dc.nnz / (n * k))
+        spk = dataclasses.replace(pk, threshold=thr, sparse=object(),
+                                  log_dense=pf.divergence.LogDenseView(dk), row_cut=cut)
+        ref_pair = lambda g, q: O.dv_pair_sparse_direct(dense, t, int(q), g)[0]  # noqa: E731
     sp = []
     for g in ("kl", "tv"):
         fld = pf.dv_field_sparse(spk, pf.builtin_f(g), t)
-        refs = O.dv_field_sparse(sv, g, t, rows)
+        refs = np.array([ref_pair(g, q) for q in rows])
         mx, _ = relerr(fld.values[rows], refs)
         sp.append({"gen": g, "rows_checked": int(rows.size), "max_rel_err": mx})
     res["sparse"] = sp
+    del spk
 
     # tracer on the GPU field vs the oracle tracer on the same values
     m = mesh

@@ -137,3 +137,13 @@ def test_topology_matches_reference_lists():
         nbr[i].add(j); nbr[j].add(i)
     for v in range(0, m.n, 11):
         assert list(nb_idx[nb_ptr[v]:nb_ptr[v + 1]]) == sorted(nbr[v])
+
+
+def test_sparse_pair_direct_matches_reference():
+    c = case("corridor50")
+    for g in ("kl", "tv"):
+        for q in range(0, c.n, 37):
+            v, ops = O.dv_pair_sparse_direct(c.dense, c.target, q, g)
+            ok, err = rel_close([v], [c[f"spfield/{g}"][q]], 1e-14)
+            assert ok, (g, q, err)
+            assert ops == int(c[f"spops/{g}"][q])
