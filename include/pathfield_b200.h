@@ -139,6 +139,29 @@ int pf_dense_at_f64(const double *P, int64_t ld, int64_t rows, int64_t k,
                     const int64_t *queries, int64_t nq, double *out,
                     pf_stream_t stream);
 
+/* ---- FP32 storage mode (north-star tolerance 1e-5 relative) -------------
+ * pf_convert_f32: out (rows x ld32, ld32 % 4 == 0) = (float)P, pad 0.
+ * pf_row_negentropy_f32: H[r] = sum c(Q32) log c(Q32) in FP64 over FP32 rows.
+ * pf_dense_kl_f32 / pf_dense_tv_f32: the K2 / K3 fields with the query rows
+ * read from the FP32 copy (half the bytes); target row, logs, H and all
+ * accumulation FP64.  Rows whose value cannot be certified to 1e-5 against
+ * the FP32 rounding bound (|KL| < tau*(|H|+|cross|+1), |TV| < tau; tau = 1e-2)
+ * are re-evaluated from the FP64 rows P64 in the reference form (count in
+ * flags[PF_FLAG_GUARDED]).  Staging buffers as for K2/K3 (pf_target_prep_f64). */
+int pf_convert_f32(const double *P, int64_t ld, int64_t rows, int64_t k, float *out,
+                   int64_t ld32, pf_stream_t stream);
+int pf_row_negentropy_f32(const float *P, int64_t ld, int64_t rows, int64_t k, double clamp,
+                          double *H, pf_stream_t stream);
+int pf_dense_kl_f32(const float *P, int64_t ld, int64_t rows, int64_t k, const double *H,
+                    const double *tgt, const double *logt, const uint8_t *tmask, double clamp,
+                    double tau, int64_t row0, int64_t target, const uint8_t *is_interior,
+                    const double *P64, int64_t ld64, double *out, uint32_t *flags,
+                    pf_stream_t stream);
+int pf_dense_tv_f32(const float *P, int64_t ld, int64_t rows, int64_t k, const double *tgt,
+                    const uint8_t *tmask, double clamp, double tau, int64_t row0, int64_t target,
+                    const uint8_t *is_interior, const double *P64, int64_t ld64, double *out,
+                    uint32_t *flags, pf_stream_t stream);
+
 /* ---- K4: sparsify (divergence.py:194-240) ---------------------------------
  * keep = P >= cut (strict_positive == 0; cut = threshold / k computed by the
  * caller exactly as divergence.py:219) or P > 0 (threshold 0, :220).

@@ -93,6 +93,7 @@ class DeviceKernel:
         self._H = {}
         self._csr = {}
         self._uniform = {}
+        self._p32 = None
         self._min = None
         self._lock = threading.Lock()
         self._host = weakref.ref(dense) if dense is not None else None
@@ -123,6 +124,32 @@ class DeviceKernel:
         if self._min is None:
             self.negentropy(1e-300)
         return float(self._min.item())
+
+    def fp32(self):
+        """(P32, ld32): FP32 copy of the slab for the FP32 storage mode (built once)."""
+        with self._lock:
+            if self._p32 is None:
+                t = torch()
+                ld32 = round_up(self.k, 32)
+                P32 = t.empty((self.rows, ld32), dtype=t.float32, device=self.device)
+                nat.call("pf_convert_f32", self.P.data_ptr(), self.ld, self.rows, self.k,
+                         P32.data_ptr(), ld32, t.cuda.current_stream(self.device).cuda_stream)
+                self._p32 = (P32, ld32)
+            return self._p32
+
+    def negentropy32(self, clamp: float):
+        """H over the FP32 rows (FP64 accumulation), cached per clamp."""
+        key = ("f32", float(clamp))
+        P32, ld32 = self.fp32()
+        with self._lock:
+            h = self._H.get(key)
+            if h is None:
+                t = torch()
+                h = t.empty(self.rows, dtype=t.float64, device=self.device)
+                nat.call("pf_row_negentropy_f32", P32.data_ptr(), ld32, self.rows, self.k,
+                         float(clamp), h.data_ptr(), t.cuda.current_stream(self.device).cuda_stream)
+                self._H[key] = h
+            return h
 
     def csr(self, cut: float, strict_positive: bool) -> "DeviceCSR":
         """The thresholded CSR view of this slab (K4), cached per (cut, mode)."""

@@ -56,6 +56,12 @@ _SIGS = {
     "pf_batched_kl_f64": [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_dbl,
                           c_dbl, c_i64, c_vp, c_i64, c_vp, c_vp],
     "pf_probe_dfma_f64": [c_i64, ctypes.POINTER(ctypes.c_int64), c_vp, c_vp],
+    "pf_convert_f32": [c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp],
+    "pf_row_negentropy_f32": [c_vp, c_i64, c_i64, c_i64, c_dbl, c_vp, c_vp],
+    "pf_dense_kl_f32": [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_dbl, c_dbl, c_i64,
+                        c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp],
+    "pf_dense_tv_f32": [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_dbl, c_dbl, c_i64, c_i64, c_vp,
+                        c_vp, c_i64, c_vp, c_vp, c_vp],
     # struct arguments (pf_mesh_t*, pf_paths_t*) are passed as addresses
     "pf_trace_batch_f64": [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp],
     "pf_triangle_gradient_f64": [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp],

@@ -1,0 +1,275 @@
+// dense32.cu — dense KL / TV with P stored in FP32 (half the HBM bytes).
+//
+// Same fields as dense.cu (divergence.py:154-187), with the query rows read
+// from an FP32 copy of P; the target row, its logs, H and every accumulation
+// stay FP64.  The north-star tolerance for this mode is 1e-5 relative.  The
+// FP32 rounding of a row perturbs the result by at most
+//     |KL32 - KL64| <= eps32 * (|H| + |cross| + 1),   |TV32 - TV64| <= eps32,
+// (eps32 = 2^-24 relative per stored entry), so a row whose value is below
+// tau32 * (|H| + |cross| + 1) (KL) or tau32 (TV), tau32 = 1e-2, cannot be
+// certified to 1e-5 and is written as a sentinel; the fixup pass re-evaluates
+// it from the FP64 rows (reference per-element form), exactly as the FP64
+// guard does.  Unflagged rows carry <= 6e-6 relative error by that bound.
+#include <cmath>
+
+#include "pf_common.cuh"
+
+namespace pf {
+
+constexpr int kT32 = 256;
+constexpr unsigned long long kSentinel32 = 0x7ff8dead0000beefull;  // = dense.cu kGuardSentinel
+
+__device__ __forceinline__ float4 ldg_stream4f(const float4 *p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+
+__global__ void __launch_bounds__(kT32) row_negentropy32_kernel(const float *__restrict__ P,
+                                                                int64_t ld, int64_t rows,
+                                                                int64_t k, double clamp,
+                                                                double *__restrict__ H) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < rows; r += nwarps) {
+    const float *row = P + r * ld;
+    double a = 0.0;
+    for (int64_t b = lane; b < k; b += 32) {
+      const double q = fmax(static_cast<double>(row[b]), clamp);
+      a += __dmul_rn(q, log(q));
+    }
+    a = warp_sum(a);
+    if (lane == 0) H[r] = a;
+  }
+}
+
+template <bool KL>
+__device__ __forceinline__ void acc32(double q_raw, double t, uint8_t m, double clamp, double &a,
+                                      bool &fl) {
+  const double q = fmax(q_raw, clamp);
+  if (KL)
+    a = fma(q, t, a);  // t = log c(Pt)
+  else
+    a += fabs(q - t);  // t = c(Pt)
+  fl |= (q_raw < clamp) != (m != 0);
+}
+
+// KL (KL = true) or TV field over FP32 rows; vec = logt (KL) or tgt (TV), both
+// FP64, staged in shared memory with the mask by TMA.
+template <bool KL>
+__global__ void __launch_bounds__(kT32, 4) dense32_kernel(
+    const float *__restrict__ P, int64_t ld, int64_t rows, int64_t k, int64_t k_pad,
+    int64_t m_pad, const double *__restrict__ H, const double *__restrict__ vec,
+    const uint8_t *__restrict__ tmask, double clamp, double tau, int64_t row0, int64_t target,
+    const uint8_t *__restrict__ is_interior, double *__restrict__ out,
+    uint32_t *__restrict__ flags) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
+  double *s_vec = reinterpret_cast<double *>(smem + 16);
+  uint8_t *s_mask = reinterpret_cast<uint8_t *>(s_vec + k_pad);
+  if (threadIdx.x == 0) mbar_init(bar, 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t vb = static_cast<uint32_t>(k_pad * 8), mb = static_cast<uint32_t>(m_pad);
+    mbar_expect_tx(bar, vb + mb);
+    bulk_g2s(s_vec, vec, vb, bar);
+    bulk_g2s(s_mask, tmask, mb, bar);
+  }
+  mbar_wait(bar, 0);
+
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nq4 = k >> 2;  // full float4 groups
+  bool clamped_any = false;
+  for (int64_t r = warp; r < rows; r += nwarps) {
+    const float4 *row = reinterpret_cast<const float4 *>(P + r * ld);
+    const double h = KL ? H[r] : 0.0;
+    double a0 = 0.0, a1 = 0.0;
+    bool fl = false;
+    for (int64_t j0 = 0; j0 < nq4; j0 += 64) {
+      float4 v[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int64_t j = j0 + lane + 32 * u;
+        v[u] = j < nq4 ? ldg_stream4f(row + j) : make_float4(1.f, 1.f, 1.f, 1.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int64_t j = j0 + lane + 32 * u;
+        if (j < nq4) {
+          const double2 t01 = reinterpret_cast<const double2 *>(s_vec)[2 * j];
+          const double2 t23 = reinterpret_cast<const double2 *>(s_vec)[2 * j + 1];
+          const uchar4 m = reinterpret_cast<const uchar4 *>(s_mask)[j];
+          acc32<KL>(v[u].x, t01.x, m.x, clamp, a0, fl);
+          acc32<KL>(v[u].y, t01.y, m.y, clamp, a1, fl);
+          acc32<KL>(v[u].z, t23.x, m.z, clamp, a0, fl);
+          acc32<KL>(v[u].w, t23.y, m.w, clamp, a1, fl);
+        }
+      }
+    }
+    for (int64_t b = 4 * nq4 + lane; b < k; b += 32)  // ragged tail (< 4 columns)
+      acc32<KL>(static_cast<double>(P[r * ld + b]), s_vec[b], s_mask[b], clamp, a0, fl);
+    const double s = warp_sum(a0 + a1);
+    const bool is_t = (row0 + r == target);
+    double val;
+    bool guard;
+    if (KL) {
+      val = h - s;
+      guard = fabs(val) < tau * (fabs(h) + fabs(s) + 1.0);
+    } else {
+      val = s;
+      guard = fabs(val) < tau;
+    }
+    if (is_t)
+      val = 0.0;
+    else if (guard)
+      val = __longlong_as_double(static_cast<long long>(kSentinel32));
+    else
+      val = settle(val);
+    const bool interior = is_interior ? (is_interior[r] != 0) : true;
+    clamped_any |= interior && __any_sync(0xffffffffu, fl);
+    if (lane == 0) out[r] = val;
+  }
+  if (lane == 0 && clamped_any) atomicOr(&flags[PF_FLAG_CLAMPED], 1u);
+}
+
+// FP64 re-evaluation of sentinel rows from the FP64 copy of P (rows
+// interleaved across warps): KL in the reference per-element form, TV as
+// sum |c(Q) - c(Pt)|.
+template <bool KL>
+__global__ void __launch_bounds__(256) guard64_fixup_kernel(const double *__restrict__ P64,
+                                                            int64_t ld, int64_t rows, int64_t k,
+                                                            const double *__restrict__ tgt,
+                                                            double clamp,
+                                                            double *__restrict__ out,
+                                                            uint32_t *__restrict__ flags) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  uint32_t done = 0;
+  for (int64_t i0 = 0; warp + i0 * nwarps < rows; i0 += 32) {
+    const int64_t mine = warp + (i0 + lane) * nwarps;
+    const bool flag = mine < rows && static_cast<unsigned long long>(__double_as_longlong(
+                                         out[mine])) == kSentinel32;
+    unsigned ball = __ballot_sync(0xffffffffu, flag);
+    while (ball) {
+      const int src = __ffs(ball) - 1;
+      ball &= ball - 1;
+      const int64_t r = warp + (i0 + src) * nwarps;
+      const double *prow = P64 + r * ld;
+      double b[4] = {0.0, 0.0, 0.0, 0.0};
+      int64_t e = lane;
+      for (; e + 96 < k; e += 128) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double q = fmax(prow[e + 32 * u], clamp), t = tgt[e + 32 * u];
+          b[u] += KL ? __dmul_rn(q, -log(__ddiv_rn(t, q))) : fabs(q - t);
+        }
+      }
+      for (; e < k; e += 32) {
+        const double q = fmax(prow[e], clamp), t = tgt[e];
+        b[0] += KL ? __dmul_rn(q, -log(__ddiv_rn(t, q))) : fabs(q - t);
+      }
+      const double val = settle(warp_sum((b[0] + b[1]) + (b[2] + b[3])));
+      if (lane == 0) out[r] = val;
+      ++done;
+    }
+  }
+  if (lane == 0 && done) atomicAdd(&flags[PF_FLAG_GUARDED], done);
+}
+
+__global__ void convert_f32_kernel(const double *__restrict__ P, int64_t ld, int64_t rows,
+                                   int64_t k, float *__restrict__ out, int64_t ld32) {
+  const int64_t n = rows * ld32;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / ld32, c = i - r * ld32;
+    out[i] = c < k ? __double2float_rn(P[r * ld + c]) : 0.0f;
+  }
+}
+
+template <bool KL>
+static int launch32(const float *P, int64_t ld, int64_t rows, int64_t k, const double *H,
+                    const double *vec, const uint8_t *tmask, double clamp, double tau,
+                    int64_t row0, int64_t target, const uint8_t *is_interior, const double *P64,
+                    int64_t ld64, const double *tgt, double *out, uint32_t *flags,
+                    cudaStream_t stream) {
+  const int64_t k_pad = round_up(k, 4), m_pad = round_up(k, 16);
+  const size_t smem = 16 + static_cast<size_t>(k_pad) * 8 + static_cast<size_t>(m_pad);
+  if (smem > 200 * 1024) return fail(PF_E_DOMAIN, "dense32: k=%lld too large", (long long)k);
+  auto kern = dense32_kernel<KL>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return fail(static_cast<int>(e), "dense32 smem: %s", cudaGetErrorString(e));
+  }
+  const int occ = occupancy((const void *)kern, kT32, smem);
+  int64_t g = static_cast<int64_t>(sm_count()) * occ, want = (rows + 7) / 8;
+  if (g > want) g = want;
+  if (g < 1) g = 1;
+  kern<<<static_cast<int>(g), kT32, smem, stream>>>(P, ld, rows, k, k_pad, m_pad, H, vec, tmask,
+                                                    clamp, tau, row0, target, is_interior, out,
+                                                    flags);
+  if (int e = check_launch("dense32")) return e;
+  int64_t g2 = static_cast<int64_t>(sm_count()) * 4, want2 = (rows + 7) / 8;
+  if (g2 > want2) g2 = want2;
+  if (g2 < 1) g2 = 1;
+  guard64_fixup_kernel<KL><<<static_cast<int>(g2), 256, 0, stream>>>(P64, ld64, rows, k, tgt,
+                                                                      clamp, out, flags);
+  return check_launch("guard64_fixup");
+}
+
+}  // namespace pf
+
+using namespace pf;
+
+extern "C" {
+
+int pf_convert_f32(const double *P, int64_t ld, int64_t rows, int64_t k, float *out,
+                   int64_t ld32, pf_stream_t stream) {
+  if (rows <= 0) return 0;
+  if (!P || !out || ld32 < k || (ld32 & 3)) return fail(PF_E_ARG, "convert_f32: bad args");
+  convert_f32_kernel<<<sm_count() * 8, 256, 0, as_stream(stream)>>>(P, ld, rows, k, out, ld32);
+  return check_launch("convert_f32");
+}
+
+int pf_row_negentropy_f32(const float *P, int64_t ld, int64_t rows, int64_t k, double clamp,
+                          double *H, pf_stream_t stream) {
+  if (rows <= 0) return 0;
+  if (!P || !H) return fail(PF_E_ARG, "row_negentropy_f32: null");
+  row_negentropy32_kernel<<<sm_count() * 8, kT32, 0, as_stream(stream)>>>(P, ld, rows, k, clamp,
+                                                                          H);
+  return check_launch("row_negentropy_f32");
+}
+
+int pf_dense_kl_f32(const float *P, int64_t ld, int64_t rows, int64_t k, const double *H,
+                    const double *tgt, const double *logt, const uint8_t *tmask, double clamp,
+                    double tau, int64_t row0, int64_t target, const uint8_t *is_interior,
+                    const double *P64, int64_t ld64, double *out, uint32_t *flags,
+                    pf_stream_t stream) {
+  if (rows <= 0) return 0;
+  if (!P || !H || !tgt || !logt || !tmask || !P64 || !out || !flags)
+    return fail(PF_E_ARG, "dense_kl_f32: null");
+  if ((ld & 3) || (reinterpret_cast<uintptr_t>(P) & 15))
+    return fail(PF_E_ALIGN, "dense_kl_f32: FP32 rows must be 16-byte aligned");
+  return launch32<true>(P, ld, rows, k, H, logt, tmask, clamp, tau, row0, target, is_interior,
+                        P64, ld64, tgt, out, flags, as_stream(stream));
+}
+
+int pf_dense_tv_f32(const float *P, int64_t ld, int64_t rows, int64_t k, const double *tgt,
+                    const uint8_t *tmask, double clamp, double tau, int64_t row0, int64_t target,
+                    const uint8_t *is_interior, const double *P64, int64_t ld64, double *out,
+                    uint32_t *flags, pf_stream_t stream) {
+  if (rows <= 0) return 0;
+  if (!P || !tgt || !tmask || !P64 || !out || !flags) return fail(PF_E_ARG, "dense_tv_f32: null");
+  if ((ld & 3) || (reinterpret_cast<uintptr_t>(P) & 15))
+    return fail(PF_E_ALIGN, "dense_tv_f32: FP32 rows must be 16-byte aligned");
+  return launch32<false>(P, ld, rows, k, nullptr, tgt, tmask, clamp, tau, row0, target,
+                         is_interior, P64, ld64, tgt, out, flags, as_stream(stream));
+}
+
+}  // extern "C"

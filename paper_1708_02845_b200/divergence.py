@@ -274,6 +274,59 @@ def dv_pair(pk: PoissonKernel, fd: FDivergence, p: int, q: int,
 
 
 # ---------------------------------------------------------------------------
+# FP32 storage mode (north-star tolerance 1e-5 relative)
+# ---------------------------------------------------------------------------
+
+#: FP32 certification threshold (csrc/dense32.cu): rows below it are re-evaluated in FP64.
+F32_GUARD_TAU = 1e-2
+
+
+def dv_field_f32_device(pk: PoissonKernel, fd: FDivergence, p: int, clamp: float | None = None):
+    """KL / TV field with the query rows streamed from an FP32 copy of P (half the
+    HBM bytes); values within 1e-5 relative of the FP64 field (rows that the FP32
+    rounding bound cannot certify are recomputed from the FP64 rows).
+    Returns (values tensor, flags tensor) on the device."""
+    if fd.name not in ("kl", "tv"):
+        raise NotImplementedError("FP32 storage mode implements kl and tv")
+    if not 0 <= p < pk.n:
+        raise InvalidTargetError(f"target {p} out of range")
+    t = dev.require_cuda()
+    dk = dev.device_kernel(pk)
+    c = _effective_clamp(dk, fd.clamp if clamp is None else clamp)
+    P32, ld32 = dk.fp32()
+    s = t.cuda.current_stream(dk.device)
+    out = t.empty(dk.rows + 2, dtype=t.float64, device=dk.device)
+    flags = out.data_ptr() + dk.rows * 8
+    st = _Staging(t, dk.k, dk.device)
+    row = dk.target_row(p)
+    nat.call("pf_target_prep_f64", row.data_ptr(), dk.k, c, st.tgt, st.logt, st.tmask, flags,
+             s.cuda_stream)
+    if fd.name == "kl":
+        H = dk.negentropy32(c)
+        nat.call("pf_dense_kl_f32", P32.data_ptr(), ld32, dk.rows, dk.k, H.data_ptr(), st.tgt,
+                 st.logt, st.tmask, c, F32_GUARD_TAU, dk.row0, p, dk.is_interior.data_ptr(),
+                 dk.P.data_ptr(), dk.ld, out.data_ptr(), flags, s.cuda_stream)
+    else:
+        nat.call("pf_dense_tv_f32", P32.data_ptr(), ld32, dk.rows, dk.k, st.tgt, st.tmask, c,
+                 F32_GUARD_TAU, dk.row0, p, dk.is_interior.data_ptr(), dk.P.data_ptr(), dk.ld,
+                 out.data_ptr(), flags, s.cuda_stream)
+    del st
+    return out[:dk.rows], out[dk.rows:].view(t.int32)
+
+
+def dv_field_f32(pk: PoissonKernel, fd: FDivergence, p: int, clamp: float | None = None) -> ScalarField:
+    """:func:`dv_field` in the FP32 storage mode (additive API; kl and tv)."""
+    t = dev.require_cuda()
+    vals, flags = dv_field_f32_device(pk, fd, p, clamp)
+    s = t.cuda.current_stream(vals.device)
+    host = _to_host(t, t.cat([vals, flags.view(t.float64)]), s)
+    n = vals.numel()
+    fired = bool(host[n:].view(np.uint32)[0])
+    return ScalarField(host[:n], fd.name, p, dict(getattr(fd, "params", {}) or {}), 1, None,
+                       ("clamped",) if fired else ())
+
+
+# ---------------------------------------------------------------------------
 # Batched targets (K7; no reference API: T x dv_field, SURVEY §8 a9)
 # ---------------------------------------------------------------------------
 
@@ -523,7 +576,7 @@ def dv_field_sparse_device(pk: PoissonKernel, fd: FDivergence, p: int):
 
 
 __all__ = [
-    "dv_field_batch", "dv_field_batch_device",
+    "dv_field_f32", "dv_field_f32_device", "F32_GUARD_TAU", "dv_field_batch", "dv_field_batch_device",
     "sparsify", "dv_pair_sparse", "dv_pair_sparse_stats", "dv_field_sparse",
     "dv_field_sparse_device", "LogDenseView",
     "FDivergence", "builtin_f", "dv_pair", "dv_at", "dv_field", "dv_field_device",
