@@ -272,6 +272,57 @@ def _roof(bytes_, ms, peak):
             "algorithmic_bytes_per_launch": bytes_, "avg_launch_ms": ms}
 
 
+def extra_f32(t, nat, dev, pf, dk, target, steps, peak):
+    """C2 in the FP32 storage mode (query rows from an FP32 copy; 1e-5 tolerance)."""
+    rows, k = dk.rows, dk.k
+    P32, ld32 = dk.fp32()
+    H32 = dk.negentropy32(1e-300)
+    s = t.cuda.current_stream(dk.device)
+    k_pad, m_pad = dev.round_up(k, 2), dev.round_up(k, 16)
+    stage = t.empty(16 * k_pad + m_pad, dtype=t.uint8, device=dk.device)
+    tgt, logt, tmask = stage.data_ptr(), stage.data_ptr() + 8 * k_pad, stage.data_ptr() + 16 * k_pad
+    out = t.empty(rows + 2, dtype=t.float64, device=dk.device)
+    fl = out.data_ptr() + rows * 8
+    rowp = dk.P[target - dk.row0].data_ptr()
+    tau = pf.divergence.F32_GUARD_TAU
+    ev = [t.cuda.Event(enable_timing=True) for _ in range(4)]
+    ms = [0.0, 0.0]
+
+    def step(timed):
+        nat.call("pf_target_prep_f64", rowp, k, 1e-300, tgt, logt, tmask, fl, s.cuda_stream)
+        if timed:
+            ev[0].record(s)
+        nat.call("pf_dense_kl_f32", P32.data_ptr(), ld32, rows, k, H32.data_ptr(), tgt, logt, tmask,
+                 1e-300, tau, dk.row0, target, dk.is_interior.data_ptr(), dk.P.data_ptr(), dk.ld,
+                 out.data_ptr(), fl, s.cuda_stream)
+        if timed:
+            ev[1].record(s)
+        nat.call("pf_target_prep_f64", rowp, k, 1e-150, tgt, 0, tmask, fl, s.cuda_stream)
+        if timed:
+            ev[2].record(s)
+        nat.call("pf_dense_tv_f32", P32.data_ptr(), ld32, rows, k, tgt, tmask, 1e-150, tau, dk.row0,
+                 target, dk.is_interior.data_ptr(), dk.P.data_ptr(), dk.ld, out.data_ptr(), fl,
+                 s.cuda_stream)
+        if timed:
+            ev[3].record(s)
+            s.synchronize()
+            ms[0] += ev[0].elapsed_time(ev[1])
+            ms[1] += ev[2].elapsed_time(ev[3])
+
+    for _ in range(3):
+        step(False)
+    n = max(3, steps)
+    for _ in range(n):
+        step(True)
+    kl_ms, tv_ms = ms[0] / n, ms[1] / n
+    guarded = int(out[rows:].view(t.int32)[1].item())
+    return {"workload": "C2 shape in the FP32 storage mode (P streamed as FP32, FP64 logs / "
+                        "accumulation, 1e-5 relative tolerance)",
+            "evals_per_s": 2 * rows / ((kl_ms + tv_ms) / 1e3), "tv_guarded_rows_last": guarded,
+            "kl": _roof(rows * (4 * k + 16) + 8 * k, kl_ms, peak),
+            "tv": _roof(rows * (4 * k + 8) + 8 * k, tv_ms, peak)}
+
+
 def extra_c4_and_c5(t, nat, dev, pf, device, steps, peak):
     """C4 dense KL+TV (1,000,386 x 4,102 on one GPU) and C5 batched KL (T = 1024)."""
     import numpy as np
@@ -587,6 +638,10 @@ def run_native(args):
 
     extras = {}
     if ws == 1 and not args.no_extras:
+        try:
+            extras["c2_f32"] = extra_f32(t, nat, dev, pf, dk, target, args.steps, peak)
+        except Exception as exc:
+            extras["c2_f32"] = {"error": f"{type(exc).__name__}: {exc}"}
         del step, dk, P_dev
         t.cuda.empty_cache()
         for name, fn in (("c3_csr", lambda: extra_c3(t, nat, dev, pf, device, args.steps, peak)),
