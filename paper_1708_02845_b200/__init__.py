@@ -11,8 +11,8 @@ from .divergence import (FDivergence, builtin_f, dv_at, dv_field, dv_field_batch
                          dv_field_device, dv_field_sparse, dv_pair,
                          dv_pair_sparse, dv_pair_sparse_stats, sparsify)
 from .mesh import TriMesh
-from .paths import (TracedPath, triangle_descent, triangle_descent_batch,
-                    triangle_gradient)
+from .paths import (TracedPath, edge_descent, edge_descent_batch, find_local_minima,
+                    triangle_descent, triangle_descent_batch, triangle_gradient)
 from .errors import (DivergenceDomainError, InvalidTargetError, NativeError,
                      PathfieldError)
 from .solvers import PoissonKernel, ScalarField
@@ -23,6 +23,6 @@ __all__ = [
     "DEFAULTS", "Settings", "FDivergence", "builtin_f", "dv_at", "dv_field", "dv_field_batch",
     "dv_field_device", "dv_pair", "sparsify", "dv_pair_sparse", "dv_pair_sparse_stats",
     "dv_field_sparse", "TriMesh", "TracedPath", "triangle_descent", "triangle_descent_batch",
-    "triangle_gradient", "DivergenceDomainError", "InvalidTargetError",
+    "triangle_gradient", "edge_descent", "edge_descent_batch", "find_local_minima", "DivergenceDomainError", "InvalidTargetError",
     "NativeError", "PathfieldError", "PoissonKernel", "ScalarField",
 ]

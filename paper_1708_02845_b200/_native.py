@@ -65,6 +65,8 @@ _SIGS = {
     # struct arguments (pf_mesh_t*, pf_paths_t*) are passed as addresses
     "pf_trace_batch_f64": [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp],
     "pf_triangle_gradient_f64": [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp],
+    "pf_edge_descent_batch_f64": [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp],
+    "pf_local_minima_f64": [c_vp, c_vp, c_i64, c_vp, c_vp],
     "pf_np_hypot_f64": [c_vp, c_vp, c_i64, c_vp, c_vp],
 }
 _RESTYPES = {"pf_last_error": ctypes.c_char_p}

@@ -390,6 +390,63 @@ __global__ void __launch_bounds__(kTraceThreads) trace_kernel(pf_mesh_t m, const
   out.stuck[p] = stuck;
 }
 
+// edge_descent (paths.py:71-94): vertex walk to the neighbour with the largest
+// value drop (first maximum in ascending neighbour order), one thread per path.
+__global__ void __launch_bounds__(kTraceThreads) edge_trace_kernel(
+    pf_mesh_t m, const double *fields, const int64_t *targets, const int64_t *sources,
+    const int32_t *field_of, int64_t npaths, int64_t cap, pf_paths_t out) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= npaths) return;
+  const int64_t fi = field_of ? field_of[p] : 0;
+  const double *vals = fields + fi * m.n;
+  const int64_t target = targets[fi];
+  int64_t cur = sources[p];
+  Writer w{&out, p, 0, 0.0, 0.0};
+  w.put(0, cur, -1, 0.0, m.vertices[2 * cur], m.vertices[2 * cur + 1]);
+  int status = ST_MAX;
+  int64_t stuck = -1;
+  for (int64_t it = 0; it < cap; ++it) {
+    if (cur == target) {
+      status = ST_REACHED;
+      break;
+    }
+    const double fc = vals[cur];
+    int64_t best = -1;
+    double bd = 0.0;
+    for (int64_t e = m.nb_ptr[cur]; e < m.nb_ptr[cur + 1]; ++e) {
+      const int64_t u = m.nb_idx[e];
+      const double drop = __dsub_rn(fc, vals[u]);
+      if (best < 0 || drop > bd) {
+        bd = drop;
+        best = u;
+      }
+    }
+    if (best < 0 || bd <= 0.0) {
+      status = ST_STUCK;
+      stuck = cur;
+      break;
+    }
+    cur = best;
+    w.put(0, cur, -1, 0.0, m.vertices[2 * cur], m.vertices[2 * cur + 1]);
+  }
+  out.count[p] = w.count;
+  out.status[p] = status;
+  out.stuck[p] = stuck;
+}
+
+// find_local_minima (paths.py:314-324): v != target with neighbours, strictly
+// below every neighbour.
+__global__ void local_minima_kernel(pf_mesh_t m, const double *vals, int64_t target,
+                                    uint8_t *out) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < m.n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    bool mn = v != target && m.nb_ptr[v + 1] > m.nb_ptr[v];
+    const double fv = vals[v];
+    for (int64_t e = m.nb_ptr[v]; mn && e < m.nb_ptr[v + 1]; ++e) mn = fv < vals[m.nb_idx[e]];
+    out[v] = mn ? 1 : 0;
+  }
+}
+
 // triangle_gradient for a batch of triangles (paths.py:113-121)
 __global__ void tri_gradient_kernel(pf_mesh_t m, const double *vals, const int64_t *tris,
                                     int64_t ntri, double *out) {
@@ -424,6 +481,26 @@ int pf_trace_batch_f64(const pf_mesh_t *mesh, const double *fields, const int64_
   trace_kernel<<<static_cast<unsigned>(blocks), kTraceThreads, 0, as_stream(stream)>>>(
       *mesh, fields, targets, sources, field_of, npaths, step_cap, *out);
   return check_launch("trace");
+}
+
+int pf_edge_descent_batch_f64(const pf_mesh_t *mesh, const double *fields,
+                              const int64_t *targets, const int64_t *sources,
+                              const int32_t *field_of, int64_t npaths, int64_t step_cap,
+                              const pf_paths_t *out, pf_stream_t stream) {
+  if (!mesh || !fields || !targets || !sources || !out) return fail(PF_E_ARG, "edge: null");
+  if (npaths <= 0) return 0;
+  const int64_t blocks = (npaths + kTraceThreads - 1) / kTraceThreads;
+  edge_trace_kernel<<<static_cast<unsigned>(blocks), kTraceThreads, 0, as_stream(stream)>>>(
+      *mesh, fields, targets, sources, field_of, npaths, step_cap, *out);
+  return check_launch("edge_descent");
+}
+
+int pf_local_minima_f64(const pf_mesh_t *mesh, const double *vals, int64_t target, uint8_t *out,
+                        pf_stream_t stream) {
+  if (!mesh || !vals || !out) return fail(PF_E_ARG, "local_minima: null");
+  if (mesh->n <= 0) return 0;
+  local_minima_kernel<<<sm_count() * 4, 256, 0, as_stream(stream)>>>(*mesh, vals, target, out);
+  return check_launch("local_minima");
 }
 
 int pf_triangle_gradient_f64(const pf_mesh_t *mesh, const double *vals, const int64_t *tris,

@@ -41,6 +41,7 @@ def _ref_types(pathfield):
 
 
 def _wrap(pathfield):
+    from .config import DEFAULTS as DEFAULTS_
     RefField, RefPath = _ref_types(pathfield)
 
     def to_field(f):
@@ -66,6 +67,9 @@ def _wrap(pathfield):
         "dv_pair_sparse_stats": _div.dv_pair_sparse_stats,
         "triangle_descent": triangle_descent,
         "triangle_gradient": _paths.triangle_gradient,
+        "edge_descent": lambda mesh, field, source, settings=None: to_path(
+            _paths.edge_descent(mesh, field, source, settings or DEFAULTS_)),
+        "find_local_minima": _paths.find_local_minima,
     }
 
 
@@ -73,10 +77,10 @@ SITES = {
     "divergence": ("dv_field", "dv_at", "dv_pair", "sparsify", "dv_pair_sparse",
                    "dv_pair_sparse_stats"),
     "": ("dv_field", "dv_pair", "dv_pair_sparse", "sparsify", "triangle_descent",
-         "triangle_gradient"),
-    "domain": ("dv_field", "sparsify", "triangle_descent"),
+         "triangle_gradient", "edge_descent", "find_local_minima"),
+    "domain": ("dv_field", "sparsify", "triangle_descent", "edge_descent", "find_local_minima"),
     "bench": ("dv_at", "dv_field", "dv_pair_sparse_stats"),
-    "paths": ("triangle_descent", "triangle_gradient"),
+    "paths": ("triangle_descent", "triangle_gradient", "edge_descent", "find_local_minima"),
 }
 
 

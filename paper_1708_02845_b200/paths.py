@@ -102,7 +102,7 @@ def _fields_to_device(t, fields, n, device):
 
 
 def trace_arrays(mesh, fields, targets, sources, field_of=None, settings: Settings = DEFAULTS,
-                 cap: int | None = None):
+                 cap: int | None = None, entry: str = "pf_trace_batch_f64"):
     """Launch K8 and return the raw device outputs (PathBuffers), rerunning overflows.
 
     `fields` is a list of field values (numpy or device tensors), `targets`
@@ -126,7 +126,7 @@ def trace_arrays(mesh, fields, targets, sources, field_of=None, settings: Settin
     if cap is None:
         cap = int(min(step_cap + 2, max(64, 8 * int(np.sqrt(dm.n)) + 64)))
     buf = PathBuffers(t, npaths, cap, dm.device)
-    nat.call("pf_trace_batch_f64", _byref(dm.struct), F.data_ptr(), tgt_d.data_ptr(),
+    nat.call(entry, _byref(dm.struct), F.data_ptr(), tgt_d.data_ptr(),
              src_d.data_ptr(), nat.ptr(fo_d), npaths, step_cap, _byref(buf.struct), s)
     counts = buf.count.cpu().numpy()
     over = np.flatnonzero(counts > cap)
@@ -136,7 +136,7 @@ def trace_arrays(mesh, fields, targets, sources, field_of=None, settings: Settin
         sub_src = t.from_numpy(sources[over]).to(dm.device)
         sub_fo = None if fo is None else t.from_numpy(fo[over]).to(dm.device)
         extra = PathBuffers(t, over.size, cap2, dm.device)
-        nat.call("pf_trace_batch_f64", _byref(dm.struct), F.data_ptr(), tgt_d.data_ptr(),
+        nat.call(entry, _byref(dm.struct), F.data_ptr(), tgt_d.data_ptr(),
                  sub_src.data_ptr(), nat.ptr(sub_fo), over.size, step_cap,
                  _byref(extra.struct), s)
     return buf, counts, over, extra
@@ -175,14 +175,7 @@ def _host_paths(buf, counts, over, extra, sources, targets, field_of):
     return out
 
 
-def triangle_descent_batch(mesh, fields, sources, settings: Settings = DEFAULTS,
-                           field_of=None) -> list[TracedPath]:
-    """Trace many sources in one launch; path p descends fields[field_of[p]].
-
-    ``fields`` is one ScalarField or a list of them (their ``target`` is the
-    destination); ``field_of`` defaults to field 0 for every path.  Equal to
-    ``[triangle_descent(mesh, fields[field_of[p]], sources[p]) for p]``.
-    """
+def _batch(mesh, fields, sources, settings, field_of, entry):
     if isinstance(fields, ScalarField) or hasattr(fields, "target"):
         fields = [fields]
     fields = list(fields)
@@ -195,8 +188,45 @@ def triangle_descent_batch(mesh, fields, sources, settings: Settings = DEFAULTS,
     n = len(mesh.vertices)
     if sources.size and (sources.min() < 0 or sources.max() >= n):
         raise InvalidTargetError("source out of range")
-    buf, counts, over, extra = trace_arrays(mesh, fields, targets, sources, fo, settings)
+    buf, counts, over, extra = trace_arrays(mesh, fields, targets, sources, fo, settings,
+                                            entry=entry)
     return _host_paths(buf, counts, over, extra, sources, targets, fo)
+
+
+def triangle_descent_batch(mesh, fields, sources, settings: Settings = DEFAULTS,
+                           field_of=None) -> list[TracedPath]:
+    """Trace many sources in one launch; path p descends fields[field_of[p]].
+
+    ``fields`` is one ScalarField or a list of them (their ``target`` is the
+    destination); ``field_of`` defaults to field 0 for every path.  Equal to
+    ``[triangle_descent(mesh, fields[field_of[p]], sources[p]) for p]``.
+    """
+    return _batch(mesh, fields, sources, settings, field_of, "pf_trace_batch_f64")
+
+
+def edge_descent_batch(mesh, fields, sources, settings: Settings = DEFAULTS,
+                       field_of=None) -> list[TracedPath]:
+    """Vertex walks (paths.py:71-94) for many sources in one launch."""
+    return _batch(mesh, fields, sources, settings, field_of, "pf_edge_descent_batch_f64")
+
+
+def edge_descent(mesh, field: ScalarField, source: int,
+                 settings: Settings = DEFAULTS) -> TracedPath:
+    """Vertex walk choosing the neighbour with the largest value drop (paths.py:71-94)."""
+    if source == field.target:
+        raise InvalidTargetError("source equals target")
+    return edge_descent_batch(mesh, [field], [int(source)], settings)[0]
+
+
+def find_local_minima(mesh, field: ScalarField) -> list[int]:
+    """Vertices (excluding the target) strictly below every neighbour (paths.py:314-324)."""
+    t = dev.require_cuda()
+    dm = device_mesh(mesh)
+    F = _fields_to_device(t, [field], dm.n, dm.device)
+    out = t.empty(dm.n, dtype=t.uint8, device=dm.device)
+    nat.call("pf_local_minima_f64", _byref(dm.struct), F.data_ptr(), int(field.target),
+             out.data_ptr(), t.cuda.current_stream(dm.device).cuda_stream)
+    return [int(v) for v in t.nonzero(out).flatten().cpu().numpy()]
 
 
 def triangle_descent(mesh, field: ScalarField, source: int,

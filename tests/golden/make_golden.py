@@ -32,7 +32,8 @@ from pathfield.divergence import (builtin_f, dv_at, dv_field, dv_pair,  # noqa: 
                                   dv_pair_sparse_stats, sparsify)
 from pathfield.domain import default_endpoints  # noqa: E402
 from pathfield.laplacian import assemble_cotan  # noqa: E402
-from pathfield.paths import triangle_descent  # noqa: E402
+from pathfield.paths import (edge_descent, find_local_minima,  # noqa: E402
+                             triangle_descent)
 from pathfield.solvers import ScalarField, poisson_kernel  # noqa: E402
 
 from oracle import inputs as I  # noqa: E402
@@ -135,6 +136,20 @@ def main(only=None):
                 enc = encode_path(triangle_descent(mesh, fld, s))
                 for key, val in enc.items():
                     out[f"path/{gname}/{pi}/{key}"] = np.asarray(val)
+        # audits: edge walk paths and local minima, on the
+        # reference fields and on a noisy field that has spurious minima
+        noisy = dv_field(pk, builtin_f("kl"), tgt0).values.copy()
+        noisy += np.random.default_rng(5).normal(0.0, 0.02 * noisy.std(), n)
+        noisy[tgt0] = 0.0
+        out["noisy_field"] = noisy
+        for gname in ("kl", "tv", "noisy"):
+            vals = noisy if gname == "noisy" else dv_field(pk, builtin_f(gname), tgt0).values
+            fld = ScalarField(np.array(vals), "custom-f", tgt0)
+            out[f"minima/{gname}"] = np.array(find_local_minima(mesh, fld), np.int64)
+            for pi, s in enumerate(srcs[:8]):
+                enc = encode_path(edge_descent(mesh, fld, s))
+                for key, val in enc.items():
+                    out[f"epath/{gname}/{pi}/{key}"] = np.asarray(val)
         np.savez_compressed(HERE / f"{name}.npz", **out)
         print(name, n, k, "targets", targets, "paths", len(srcs))
 

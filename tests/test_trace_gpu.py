@@ -125,3 +125,22 @@ def test_device_hypot_matches_numpy_on_this_host():
     frac = float(np.mean(got == ref))
     print("device hypot == np.hypot on this host:", frac)
     assert frac == 1.0
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_edge_descent_and_local_minima_match_reference(name):
+    c = case(name)
+    mesh = _mesh(c)
+    srcs = c["path_sources"][:8]
+    for g in ("kl", "tv", "noisy"):
+        vals = c["noisy_field"] if g == "noisy" else c[f"field/{g}/0"]
+        fld = pf.ScalarField(np.array(vals), "custom-f", c.target)
+        assert pf.find_local_minima(mesh, fld) == [int(x) for x in c[f"minima/{g}"]]
+        paths = pf.edge_descent_batch(mesh, fld, srcs)
+        for pi, p in enumerate(paths):
+            pre = f"epath/{g}/{pi}/"
+            gold = {k[len(pre):]: c[k] for k in c.keys() if k.startswith(pre)}
+            _assert_same(p, gold)
+        one = pf.edge_descent(mesh, fld, int(srcs[0]))
+        _assert_same(one, {k[len(f"epath/{g}/0/"):]: c[k] for k in c.keys()
+                           if k.startswith(f"epath/{g}/0/")})
