@@ -266,6 +266,10 @@ typedef struct {
   int64_t n;
   int64_t nt;
   double eps_prog;
+  /* optional (nt,6) table of barycentric gradients, rows (G00,G01,G10,G11,
+   * G20,G21) = paths.py:105-110 bit for bit; built by pf_mesh_geometry_f64.
+   * NULL: recomputed per visit. */
+  const double *G;
 } pf_mesh_t;
 
 /* Path output: location l of path p is at index p*cap + l:
@@ -295,6 +299,9 @@ typedef struct {
 int pf_trace_batch_f64(const pf_mesh_t *mesh, const double *fields, const int64_t *targets,
                        const int64_t *sources, const int32_t *field_of, int64_t npaths,
                        int64_t step_cap, const pf_paths_t *out, pf_stream_t stream);
+
+/* Fill the (nt,6) barycentric-gradient table of pf_mesh_t.G (mesh->G ignored). */
+int pf_mesh_geometry_f64(const pf_mesh_t *mesh, double *G, pf_stream_t stream);
 
 /* triangle_gradient (paths.py:113-121) for a batch of triangle ids: out (ntri,2). */
 int pf_triangle_gradient_f64(const pf_mesh_t *mesh, const double *vals, const int64_t *tris,

@@ -68,21 +68,39 @@ struct Tri {
   double G[3][2];  // barycentric gradients (paths.py:105-110)
 };
 
+__device__ __forceinline__ void tri_G(const pf_mesh_t &m, int64_t ti, const int v[3],
+                                      double G[3][2]) {
+  const double ax = m.vertices[2 * v[0]], ay = m.vertices[2 * v[0] + 1];
+  const double bx = m.vertices[2 * v[1]], by = m.vertices[2 * v[1] + 1];
+  const double cx = m.vertices[2 * v[2]], cy = m.vertices[2 * v[2] + 1];
+  const double area2 = __dmul_rn(2.0, m.areas[ti]);
+  // _perp(v) = [-v[1], v[0]];  rows: perp(pc-pb), perp(pa-pc), perp(pb-pa); / area2
+  G[0][0] = __ddiv_rn(-__dsub_rn(cy, by), area2);
+  G[0][1] = __ddiv_rn(__dsub_rn(cx, bx), area2);
+  G[1][0] = __ddiv_rn(-__dsub_rn(ay, cy), area2);
+  G[1][1] = __ddiv_rn(__dsub_rn(ax, cx), area2);
+  G[2][0] = __ddiv_rn(-__dsub_rn(by, ay), area2);
+  G[2][1] = __ddiv_rn(__dsub_rn(bx, ax), area2);
+}
+
+// Triangle vertices + barycentric gradients: read from the per-triangle table
+// built once per mesh (pf_mesh_geometry_f64, same arithmetic) when present.
 __device__ __forceinline__ void load_tri(const pf_mesh_t &m, int64_t ti, Tri &t) {
   t.v[0] = m.triangles[3 * ti + 0];
   t.v[1] = m.triangles[3 * ti + 1];
   t.v[2] = m.triangles[3 * ti + 2];
-  const double ax = m.vertices[2 * t.v[0]], ay = m.vertices[2 * t.v[0] + 1];
-  const double bx = m.vertices[2 * t.v[1]], by = m.vertices[2 * t.v[1] + 1];
-  const double cx = m.vertices[2 * t.v[2]], cy = m.vertices[2 * t.v[2] + 1];
-  const double area2 = __dmul_rn(2.0, m.areas[ti]);
-  // _perp(v) = [-v[1], v[0]];  rows: perp(pc-pb), perp(pa-pc), perp(pb-pa); / area2
-  t.G[0][0] = __ddiv_rn(-__dsub_rn(cy, by), area2);
-  t.G[0][1] = __ddiv_rn(__dsub_rn(cx, bx), area2);
-  t.G[1][0] = __ddiv_rn(-__dsub_rn(ay, cy), area2);
-  t.G[1][1] = __ddiv_rn(__dsub_rn(ax, cx), area2);
-  t.G[2][0] = __ddiv_rn(-__dsub_rn(by, ay), area2);
-  t.G[2][1] = __ddiv_rn(__dsub_rn(bx, ax), area2);
+  if (m.G) {
+    const double2 *g = reinterpret_cast<const double2 *>(m.G + 6 * ti);
+    const double2 g0 = g[0], g1 = g[1], g2 = g[2];
+    t.G[0][0] = g0.x;
+    t.G[0][1] = g0.y;
+    t.G[1][0] = g1.x;
+    t.G[1][1] = g1.y;
+    t.G[2][0] = g2.x;
+    t.G[2][1] = g2.y;
+  } else {
+    tri_G(m, ti, t.v, t.G);
+  }
 }
 
 // f @ G  (3,)@(3,2): fma(f2,G2j, fma(f1,G1j, f0*G0j))
@@ -447,6 +465,20 @@ __global__ void local_minima_kernel(pf_mesh_t m, const double *vals, int64_t tar
   }
 }
 
+__global__ void tri_geometry_kernel(pf_mesh_t m, double *G) {
+  for (int64_t ti = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ti < m.nt;
+       ti += (int64_t)gridDim.x * blockDim.x) {
+    const int v[3] = {m.triangles[3 * ti], m.triangles[3 * ti + 1], m.triangles[3 * ti + 2]};
+    double g[3][2];
+    tri_G(m, ti, v, g);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      G[6 * ti + 2 * i] = g[i][0];
+      G[6 * ti + 2 * i + 1] = g[i][1];
+    }
+  }
+}
+
 // triangle_gradient for a batch of triangles (paths.py:113-121)
 __global__ void tri_gradient_kernel(pf_mesh_t m, const double *vals, const int64_t *tris,
                                     int64_t ntri, double *out) {
@@ -510,6 +542,15 @@ int pf_triangle_gradient_f64(const pf_mesh_t *mesh, const double *vals, const in
   tri_gradient_kernel<<<static_cast<unsigned>((ntri + 127) / 128), 128, 0, as_stream(stream)>>>(
       *mesh, vals, tris, ntri, out);
   return check_launch("triangle_gradient");
+}
+
+int pf_mesh_geometry_f64(const pf_mesh_t *mesh, double *G, pf_stream_t stream) {
+  if (!mesh || !G) return fail(PF_E_ARG, "mesh_geometry: null");
+  if (mesh->nt <= 0) return 0;
+  pf_mesh_t m = *mesh;
+  m.G = nullptr;  // compute, do not read
+  tri_geometry_kernel<<<sm_count() * 4, 256, 0, as_stream(stream)>>>(m, G);
+  return check_launch("mesh_geometry");
 }
 
 int pf_np_hypot_f64(const double *x, const double *y, int64_t n, double *out,
