@@ -289,6 +289,8 @@ typedef struct {
   int64_t *count;
   int32_t *status;
   int64_t *stuck;
+  double *qx; /* scratch (npaths): nearest-vertex query point of stuck paths */
+  double *qy;
 } pf_paths_t;
 
 /* Trace npaths paths: path p descends field field_of[p] (fields is

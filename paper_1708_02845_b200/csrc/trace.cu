@@ -142,21 +142,8 @@ struct Writer {
   }
 };
 
-// np.argmin(np.hypot(V - x)) : first minimum (paths.py:287-289)
-__device__ int64_t nearest_vertex(const pf_mesh_t &m, double x, double y) {
-  int64_t best = 0;
-  double bd = INFINITY;
-  for (int64_t v = 0; v < m.n; ++v) {
-    const double d = np_hypot(__dsub_rn(m.vertices[2 * v], x), __dsub_rn(m.vertices[2 * v + 1], y));
-    if (d < bd) {  // strict: the first minimum wins
-      bd = d;
-      best = v;
-    }
-  }
-  return best;
-}
-
 enum { ST_REACHED = 0, ST_STUCK = 1, ST_MAX = 2 };
+constexpr int64_t kNearestPending = -2;
 
 __global__ void __launch_bounds__(kTraceThreads) trace_kernel(pf_mesh_t m, const double *fields,
                                                               const int64_t *targets,
@@ -180,6 +167,7 @@ __global__ void __launch_bounds__(kTraceThreads) trace_kernel(pf_mesh_t m, const
   double x0 = 0.0, x1 = 0.0, cur = 0.0;
   int status = ST_MAX;
   int64_t stuck = -1;
+  double qx = 0.0, qy = 0.0;
 
   for (int64_t it = 0; it < cap; ++it) {
     if (!in_tri) {
@@ -324,7 +312,9 @@ __global__ void __launch_bounds__(kTraceThreads) trace_kernel(pf_mesh_t m, const
       const double wx = m.vertices[2 * wv], wy = m.vertices[2 * wv + 1];
       if (!(np_hypot(__dsub_rn(wx, w.lx), __dsub_rn(wy, w.ly)) >= eps_prog)) {
         status = ST_STUCK;
-        stuck = nearest_vertex(m, x0, x1);
+        stuck = kNearestPending;  // resolved by nearest_resolve_kernel
+        qx = x0;
+        qy = x1;
         break;
       }
       w.put(0, wv, -1, 0.0, wx, wy);
@@ -352,7 +342,9 @@ __global__ void __launch_bounds__(kTraceThreads) trace_kernel(pf_mesh_t m, const
                                          __dmul_rn(le[0], m.vertices[2 * t.v[0] + 1])));
     if (!(np_hypot(__dsub_rn(xe0, w.lx), __dsub_rn(xe1, w.ly)) >= eps_prog)) {
       status = ST_STUCK;
-      stuck = nearest_vertex(m, x0, x1);
+      stuck = kNearestPending;
+      qx = x0;
+      qy = x1;
       break;
     }
     w.put(1, ei, ej, tpar, xe0, xe1);
@@ -396,7 +388,9 @@ __global__ void __launch_bounds__(kTraceThreads) trace_kernel(pf_mesh_t m, const
     const int64_t sw = (vals[ej] < vals[ei]) ? ej : ei;
     if (vals[sw] >= val_exit) {
       status = ST_STUCK;
-      stuck = nearest_vertex(m, rx, ry);
+      stuck = kNearestPending;
+      qx = rx;
+      qy = ry;
       break;
     }
     w.put(0, sw, -1, 0.0, m.vertices[2 * sw], m.vertices[2 * sw + 1]);
@@ -406,6 +400,49 @@ __global__ void __launch_bounds__(kTraceThreads) trace_kernel(pf_mesh_t m, const
   out.count[p] = w.count;
   out.status[p] = status;
   out.stuck[p] = stuck;
+  if (stuck == kNearestPending) {
+    out.qx[p] = qx;
+    out.qy[p] = qy;
+  }
+}
+
+// A stuck path's reported vertex is the mesh vertex nearest to a point
+// (paths.py:287-289, np.argmin of np.hypot over all n vertices).  That O(n)
+// scan would serialise one thread of the tracer for milliseconds, so the
+// tracer only records the query point and this kernel resolves it with one
+// CTA per pending path: strided per-thread scans, then a (distance, index)
+// lexicographic block minimum = numpy's first minimum.
+__global__ void __launch_bounds__(256) nearest_resolve_kernel(pf_mesh_t m, int64_t npaths,
+                                                              pf_paths_t out) {
+  const int64_t p = blockIdx.x;
+  if (p >= npaths || out.stuck[p] != kNearestPending) return;
+  const double x = out.qx[p], y = out.qy[p];
+  double bd = INFINITY;
+  int64_t bv = INT64_MAX;
+  for (int64_t v = threadIdx.x; v < m.n; v += blockDim.x) {
+    const double d = np_hypot(__dsub_rn(m.vertices[2 * v], x), __dsub_rn(m.vertices[2 * v + 1], y));
+    if (d < bd) {
+      bd = d;
+      bv = v;
+    }
+  }
+  __shared__ double sd[256];
+  __shared__ int64_t sv[256];
+  sd[threadIdx.x] = bd;
+  sv[threadIdx.x] = bv;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      const double d2 = sd[threadIdx.x + o];
+      const int64_t v2 = sv[threadIdx.x + o];
+      if (d2 < sd[threadIdx.x] || (d2 == sd[threadIdx.x] && v2 < sv[threadIdx.x])) {
+        sd[threadIdx.x] = d2;
+        sv[threadIdx.x] = v2;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out.stuck[p] = sv[0] == INT64_MAX ? 0 : sv[0];
 }
 
 // edge_descent (paths.py:71-94): vertex walk to the neighbour with the largest
@@ -510,9 +547,13 @@ int pf_trace_batch_f64(const pf_mesh_t *mesh, const double *fields, const int64_
   if (npaths <= 0) return 0;
   if (!out->count || !out->status || !out->stuck) return fail(PF_E_ARG, "trace: null outputs");
   const int64_t blocks = (npaths + kTraceThreads - 1) / kTraceThreads;
+  if (!out->qx || !out->qy) return fail(PF_E_ARG, "trace: null qx/qy");
   trace_kernel<<<static_cast<unsigned>(blocks), kTraceThreads, 0, as_stream(stream)>>>(
       *mesh, fields, targets, sources, field_of, npaths, step_cap, *out);
-  return check_launch("trace");
+  if (int e = check_launch("trace")) return e;
+  nearest_resolve_kernel<<<static_cast<unsigned>(npaths), 256, 0, as_stream(stream)>>>(
+      *mesh, npaths, *out);
+  return check_launch("nearest_resolve");
 }
 
 int pf_edge_descent_batch_f64(const pf_mesh_t *mesh, const double *fields,

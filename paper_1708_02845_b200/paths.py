@@ -61,7 +61,8 @@ class PfPaths(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_void_p), ("i", ctypes.c_void_p), ("j", ctypes.c_void_p),
                 ("t", ctypes.c_void_p), ("x", ctypes.c_void_p), ("y", ctypes.c_void_p),
                 ("cap", ctypes.c_int64), ("count", ctypes.c_void_p),
-                ("status", ctypes.c_void_p), ("stuck", ctypes.c_void_p)]
+                ("status", ctypes.c_void_p), ("stuck", ctypes.c_void_p),
+                ("qx", ctypes.c_void_p), ("qy", ctypes.c_void_p)]
 
 
 def _byref(s):
@@ -83,10 +84,11 @@ class PathBuffers:
         self.count = t.empty(max(npaths, 1), dtype=t.int64, device=device)
         self.status = t.empty(max(npaths, 1), dtype=t.int32, device=device)
         self.stuck = t.empty(max(npaths, 1), dtype=t.int64, device=device)
+        self.q = t.empty((2, max(npaths, 1)), dtype=t.float64, device=device)
         self.struct = PfPaths(self.kind.data_ptr(), self.i.data_ptr(), self.j.data_ptr(),
                               self.t.data_ptr(), self.x.data_ptr(), self.y.data_ptr(), cap,
                               self.count.data_ptr(), self.status.data_ptr(),
-                              self.stuck.data_ptr())
+                              self.stuck.data_ptr(), self.q[0].data_ptr(), self.q[1].data_ptr())
 
 
 def _fields_to_device(t, fields, n, device):
