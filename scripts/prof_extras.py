@@ -17,6 +17,15 @@ which = sys.argv[1] if len(sys.argv) > 1 else "csr"
 if which == "csr":
     r = bench.extra_c3(t, nat, dev, pf, device, 3, peak)
     print({k: v for k, v in r.items()})
+elif which == "tracer":
+    print(bench.extra_tracer(t, nat, dev, pf, device))
+elif which == "f32":
+    rows, k = 102104, 4250
+    ld = dev.leading_dim(k)
+    P = bench.make_synthetic_slab(t, rows, k, ld, 0, device)
+    dk = dev.DeviceKernel(None, np.array([], np.int64), device=device, rows=rows, n=rows, k=k,
+                          P_dev=P)
+    print(bench.extra_f32(t, nat, dev, pf, dk, rows // 3 + 1, 5, peak))
 else:
     rows, k, T = 131072, 4102, 1024
     ld = dev.leading_dim(k)
