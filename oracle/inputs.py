@@ -250,6 +250,11 @@ def _solve_cols(args):
     """Worker: factor -L_II once, solve a column range of -L_IB into shared memory."""
     shm_name, shape, interior_size, cols, lc_ii, lc_ib = args
     from multiprocessing import shared_memory
+    try:  # one BLAS thread per worker: the workers are the parallelism
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(1)
+    except Exception:
+        pass
     shm = shared_memory.SharedMemory(name=shm_name)
     try:
         out = np.ndarray(shape, dtype=np.float64, buffer=shm.buf)

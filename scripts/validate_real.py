@@ -49,6 +49,16 @@ def relerr(a, b):
     return float(e.max()) if e.size else 0.0, e
 
 
+def _progress(res, msg, out_path=None):
+    res.setdefault("log", []).append([round(time.perf_counter() - _T0, 1), msg])
+    print(f"[{time.perf_counter() - _T0:8.1f}s] {msg}", file=sys.stderr, flush=True)
+    if out_path:
+        Path(out_path).write_text(json.dumps(res))
+
+
+_T0 = time.perf_counter()
+
+
 def main(name: str):
     import torch
 
@@ -60,9 +70,11 @@ def main(name: str):
     from oracle import tracer as TR
 
     res = {"case": name, "spec": SPECS[name]}
+    part = os.environ.get("PF_PARTIAL")  # partial results written after every section
     t0 = time.perf_counter()
     mesh = I.build(SPECS[name])
     res["mesh_s"] = time.perf_counter() - t0
+    _progress(res, f"mesh n={mesh.n}", part)
     t0 = time.perf_counter()
     if mesh.n > 200_000:
         dense, boundary = I.poisson_kernel_parallel(mesh, workers=int(os.environ.get("PF_WORKERS", "8")))
@@ -70,6 +82,7 @@ def main(name: str):
         dense, boundary = I.poisson_kernel(mesh)
     res["poisson_kernel_s"] = time.perf_counter() - t0
     n, k = dense.shape
+    _progress(res, f"poisson kernel {n}x{k}", part)
     res.update(n=n, k=k)
     src, tgt = I.default_endpoints(mesh)
     rng = np.random.default_rng(0)
@@ -87,6 +100,7 @@ def main(name: str):
             dense_res.append({"target": t, "gen": g, "max_rel_err": mx,
                               "flag_ok": (fld.precision_flags == ("clamped",)) == flag})
     res["dense"] = dense_res
+    _progress(res, "dense fields", part)
 
     # KL guard threshold study on the first target
     dk = dev.device_kernel(pk)
@@ -104,6 +118,7 @@ def main(name: str):
         mx, e = relerr(vals.cpu().numpy(), ref)
         study.append({"tau": tau, "guarded_rows": int(flags[1].item()), "max_rel_err": mx})
     res["kl_guard_study"] = study
+    _progress(res, "guard study", part)
 
     # sparse
     import math
@@ -156,6 +171,7 @@ def main(name: str):
         sp.append({"gen": g, "rows_checked": int(rows.size), "max_rel_err": mx})
     res["sparse"] = sp
     del spk
+    _progress(res, "sparse", part)
 
     # tracer on the GPU field vs the oracle tracer on the same values
     m = mesh
@@ -183,6 +199,7 @@ def main(name: str):
                    "reached": sum(p.status == "reached" for p in paths),
                    "locations": steps, "gpu_batch_s": gpu_s, "oracle_cpu_s": cpu_s})
     res["tracer"] = tr
+    _progress(res, "tracer", part)
     print(json.dumps(res))
 
 
