@@ -147,7 +147,12 @@ int pf_dense_at_f64(const double *P, int64_t ld, int64_t rows, int64_t k,
  * accumulation FP64.  Rows whose value cannot be certified to 1e-5 against
  * the FP32 rounding bound (|KL| < tau*(|H|+|cross|+1), |TV| < tau; tau = 1e-2)
  * are re-evaluated from the FP64 rows P64 in the reference form (count in
- * flags[PF_FLAG_GUARDED]).  Staging buffers as for K2/K3 (pf_target_prep_f64). */
+ * flags[PF_FLAG_GUARDED]).  Staging buffers as for K2/K3 (pf_target_prep_f64);
+ * tmask / is_interior are accepted for symmetry but unused: FP32 rounding
+ * flushes sub-float-range entries to 0, so the `clamped` flag must come from
+ * the FP64 rows — pf_mask_compare_f64 below plus pf_mask_uniform_f64.
+ * pf_mask_compare_f64: flag[0] |= 1 if (a[i] < clamp) != (b[i] < clamp) for
+ * some i < k. */
 int pf_convert_f32(const double *P, int64_t ld, int64_t rows, int64_t k, float *out,
                    int64_t ld32, pf_stream_t stream);
 int pf_row_negentropy_f32(const float *P, int64_t ld, int64_t rows, int64_t k, double clamp,
@@ -161,6 +166,8 @@ int pf_dense_tv_f32(const float *P, int64_t ld, int64_t rows, int64_t k, const d
                     const uint8_t *tmask, double clamp, double tau, int64_t row0, int64_t target,
                     const uint8_t *is_interior, const double *P64, int64_t ld64, double *out,
                     uint32_t *flags, pf_stream_t stream);
+int pf_mask_compare_f64(const double *a, const double *b, int64_t k, double clamp,
+                        uint32_t *flag, pf_stream_t stream);
 
 /* ---- K4: sparsify (divergence.py:194-240) ---------------------------------
  * keep = P >= cut (strict_positive == 0; cut = threshold / k computed by the

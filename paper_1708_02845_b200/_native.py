@@ -62,6 +62,7 @@ _SIGS = {
                         c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp],
     "pf_dense_tv_f32": [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_dbl, c_dbl, c_i64, c_i64, c_vp,
                         c_vp, c_i64, c_vp, c_vp, c_vp],
+    "pf_mask_compare_f64": [c_vp, c_vp, c_i64, c_dbl, c_vp, c_vp],
     # struct arguments (pf_mesh_t*, pf_paths_t*) are passed as addresses
     "pf_trace_batch_f64": [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp],
     "pf_triangle_gradient_f64": [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp],

@@ -47,72 +47,68 @@ __global__ void __launch_bounds__(kT32) row_negentropy32_kernel(const float *__r
 }
 
 template <bool KL>
-__device__ __forceinline__ void acc32(double q_raw, double t, uint8_t m, double clamp, double &a,
-                                      bool &fl) {
+__device__ __forceinline__ void acc32(double q_raw, double t, double clamp, double &a) {
   const double q = fmax(q_raw, clamp);
   if (KL)
     a = fma(q, t, a);  // t = log c(Pt)
   else
     a += fabs(q - t);  // t = c(Pt)
-  fl |= (q_raw < clamp) != (m != 0);
 }
 
 // KL (KL = true) or TV field over FP32 rows; vec = logt (KL) or tgt (TV), both
-// FP64, staged in shared memory with the mask by TMA.
+// FP64.  Each lane streams 4 x float4 per iteration (64 B in flight); the
+// FP64 target vector is staged in shared memory split into two double2
+// planes, lo[j] = (v[4j], v[4j+1]) and hi[j] = (v[4j+2], v[4j+3]), so the
+// two 16-byte shared loads per float4 are bank-conflict free.  The clamp
+// flag is not computed here: FP32 rounding flushes entries below the float
+// range to zero, so the flag comes from the FP64 rows (pf_mask_compare_f64
+// against the interior rows' shared mask, as for K7).
 template <bool KL>
 __global__ void __launch_bounds__(kT32, 4) dense32_kernel(
-    const float *__restrict__ P, int64_t ld, int64_t rows, int64_t k, int64_t k_pad,
-    int64_t m_pad, const double *__restrict__ H, const double *__restrict__ vec,
-    const uint8_t *__restrict__ tmask, double clamp, double tau, int64_t row0, int64_t target,
-    const uint8_t *__restrict__ is_interior, double *__restrict__ out,
-    uint32_t *__restrict__ flags) {
+    const float *__restrict__ P, int64_t ld, int64_t rows, int64_t k,
+    const double *__restrict__ H, const double *__restrict__ vec, double clamp, double tau,
+    int64_t row0, int64_t target, double *__restrict__ out) {
   extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
-  double *s_vec = reinterpret_cast<double *>(smem + 16);
-  uint8_t *s_mask = reinterpret_cast<uint8_t *>(s_vec + k_pad);
-  if (threadIdx.x == 0) mbar_init(bar, 1);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const uint32_t vb = static_cast<uint32_t>(k_pad * 8), mb = static_cast<uint32_t>(m_pad);
-    mbar_expect_tx(bar, vb + mb);
-    bulk_g2s(s_vec, vec, vb, bar);
-    bulk_g2s(s_mask, tmask, mb, bar);
+  const int64_t nq4 = k >> 2;  // full float4 groups
+  double2 *lo = reinterpret_cast<double2 *>(smem);
+  double2 *hi = lo + nq4;
+  double *tail = reinterpret_cast<double *>(hi + nq4);
+  for (int64_t j = threadIdx.x; j < nq4; j += blockDim.x) {
+    lo[j] = make_double2(vec[4 * j], vec[4 * j + 1]);
+    hi[j] = make_double2(vec[4 * j + 2], vec[4 * j + 3]);
   }
-  mbar_wait(bar, 0);
+  for (int64_t b = 4 * nq4 + threadIdx.x; b < k; b += blockDim.x) tail[b - 4 * nq4] = vec[b];
+  __syncthreads();
 
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t nq4 = k >> 2;  // full float4 groups
-  bool clamped_any = false;
+  constexpr int U = 4;
   for (int64_t r = warp; r < rows; r += nwarps) {
     const float4 *row = reinterpret_cast<const float4 *>(P + r * ld);
     const double h = KL ? H[r] : 0.0;
     double a0 = 0.0, a1 = 0.0;
-    bool fl = false;
-    for (int64_t j0 = 0; j0 < nq4; j0 += 64) {
-      float4 v[2];
+    for (int64_t j0 = 0; j0 < nq4; j0 += 32 * U) {
+      float4 v[U];
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < U; ++u) {
         const int64_t j = j0 + lane + 32 * u;
         v[u] = j < nq4 ? ldg_stream4f(row + j) : make_float4(1.f, 1.f, 1.f, 1.f);
       }
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < U; ++u) {
         const int64_t j = j0 + lane + 32 * u;
         if (j < nq4) {
-          const double2 t01 = reinterpret_cast<const double2 *>(s_vec)[2 * j];
-          const double2 t23 = reinterpret_cast<const double2 *>(s_vec)[2 * j + 1];
-          const uchar4 m = reinterpret_cast<const uchar4 *>(s_mask)[j];
-          acc32<KL>(v[u].x, t01.x, m.x, clamp, a0, fl);
-          acc32<KL>(v[u].y, t01.y, m.y, clamp, a1, fl);
-          acc32<KL>(v[u].z, t23.x, m.z, clamp, a0, fl);
-          acc32<KL>(v[u].w, t23.y, m.w, clamp, a1, fl);
+          const double2 t01 = lo[j], t23 = hi[j];
+          acc32<KL>(v[u].x, t01.x, clamp, a0);
+          acc32<KL>(v[u].y, t01.y, clamp, a1);
+          acc32<KL>(v[u].z, t23.x, clamp, a0);
+          acc32<KL>(v[u].w, t23.y, clamp, a1);
         }
       }
     }
     for (int64_t b = 4 * nq4 + lane; b < k; b += 32)  // ragged tail (< 4 columns)
-      acc32<KL>(static_cast<double>(P[r * ld + b]), s_vec[b], s_mask[b], clamp, a0, fl);
+      acc32<KL>(static_cast<double>(P[r * ld + b]), tail[b - 4 * nq4], clamp, a0);
     const double s = warp_sum(a0 + a1);
     const bool is_t = (row0 + r == target);
     double val;
@@ -130,11 +126,18 @@ __global__ void __launch_bounds__(kT32, 4) dense32_kernel(
       val = __longlong_as_double(static_cast<long long>(kSentinel32));
     else
       val = settle(val);
-    const bool interior = is_interior ? (is_interior[r] != 0) : true;
-    clamped_any |= interior && __any_sync(0xffffffffu, fl);
     if (lane == 0) out[r] = val;
   }
-  if (lane == 0 && clamped_any) atomicOr(&flags[PF_FLAG_CLAMPED], 1u);
+}
+
+// flag[0] |= 1 if the below-clamp masks of rows a and b differ (k entries).
+__global__ void mask_compare_kernel(const double *__restrict__ a, const double *__restrict__ b,
+                                    int64_t k, double clamp, uint32_t *__restrict__ flag) {
+  bool d = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k;
+       i += (int64_t)gridDim.x * blockDim.x)
+    d |= (a[i] < clamp) != (b[i] < clamp);
+  if (__syncthreads_or(d) && threadIdx.x == 0) atomicOr(flag, 1u);
 }
 
 // FP64 re-evaluation of sentinel rows from the FP64 copy of P (rows
@@ -194,12 +197,10 @@ __global__ void convert_f32_kernel(const double *__restrict__ P, int64_t ld, int
 
 template <bool KL>
 static int launch32(const float *P, int64_t ld, int64_t rows, int64_t k, const double *H,
-                    const double *vec, const uint8_t *tmask, double clamp, double tau,
-                    int64_t row0, int64_t target, const uint8_t *is_interior, const double *P64,
-                    int64_t ld64, const double *tgt, double *out, uint32_t *flags,
-                    cudaStream_t stream) {
-  const int64_t k_pad = round_up(k, 4), m_pad = round_up(k, 16);
-  const size_t smem = 16 + static_cast<size_t>(k_pad) * 8 + static_cast<size_t>(m_pad);
+                    const double *vec, double clamp, double tau, int64_t row0, int64_t target,
+                    const double *P64, int64_t ld64, const double *tgt, double *out,
+                    uint32_t *flags, cudaStream_t stream) {
+  const size_t smem = static_cast<size_t>(k) * 8 + 32;
   if (smem > 200 * 1024) return fail(PF_E_DOMAIN, "dense32: k=%lld too large", (long long)k);
   auto kern = dense32_kernel<KL>;
   if (smem > 48 * 1024) {
@@ -211,9 +212,8 @@ static int launch32(const float *P, int64_t ld, int64_t rows, int64_t k, const d
   int64_t g = static_cast<int64_t>(sm_count()) * occ, want = (rows + 7) / 8;
   if (g > want) g = want;
   if (g < 1) g = 1;
-  kern<<<static_cast<int>(g), kT32, smem, stream>>>(P, ld, rows, k, k_pad, m_pad, H, vec, tmask,
-                                                    clamp, tau, row0, target, is_interior, out,
-                                                    flags);
+  kern<<<static_cast<int>(g), kT32, smem, stream>>>(P, ld, rows, k, H, vec, clamp, tau, row0,
+                                                    target, out);
   if (int e = check_launch("dense32")) return e;
   int64_t g2 = static_cast<int64_t>(sm_count()) * 4, want2 = (rows + 7) / 8;
   if (g2 > want2) g2 = want2;
@@ -256,8 +256,10 @@ int pf_dense_kl_f32(const float *P, int64_t ld, int64_t rows, int64_t k, const d
     return fail(PF_E_ARG, "dense_kl_f32: null");
   if ((ld & 3) || (reinterpret_cast<uintptr_t>(P) & 15))
     return fail(PF_E_ALIGN, "dense_kl_f32: FP32 rows must be 16-byte aligned");
-  return launch32<true>(P, ld, rows, k, H, logt, tmask, clamp, tau, row0, target, is_interior,
-                        P64, ld64, tgt, out, flags, as_stream(stream));
+  (void)tmask;
+  (void)is_interior;
+  return launch32<true>(P, ld, rows, k, H, logt, clamp, tau, row0, target, P64, ld64, tgt, out,
+                        flags, as_stream(stream));
 }
 
 int pf_dense_tv_f32(const float *P, int64_t ld, int64_t rows, int64_t k, const double *tgt,
@@ -268,8 +270,20 @@ int pf_dense_tv_f32(const float *P, int64_t ld, int64_t rows, int64_t k, const d
   if (!P || !tgt || !tmask || !P64 || !out || !flags) return fail(PF_E_ARG, "dense_tv_f32: null");
   if ((ld & 3) || (reinterpret_cast<uintptr_t>(P) & 15))
     return fail(PF_E_ALIGN, "dense_tv_f32: FP32 rows must be 16-byte aligned");
-  return launch32<false>(P, ld, rows, k, nullptr, tgt, tmask, clamp, tau, row0, target,
-                         is_interior, P64, ld64, tgt, out, flags, as_stream(stream));
+  (void)tmask;
+  (void)is_interior;
+  return launch32<false>(P, ld, rows, k, nullptr, tgt, clamp, tau, row0, target, P64, ld64, tgt,
+                         out, flags, as_stream(stream));
+}
+
+int pf_mask_compare_f64(const double *a, const double *b, int64_t k, double clamp,
+                        uint32_t *flag, pf_stream_t stream) {
+  if (k <= 0) return 0;
+  if (!a || !b || !flag) return fail(PF_E_ARG, "mask_compare: null");
+  int blocks = static_cast<int>((k + 255) / 256);
+  if (blocks > 64) blocks = 64;
+  mask_compare_kernel<<<blocks, 256, 0, as_stream(stream)>>>(a, b, k, clamp, flag);
+  return check_launch("mask_compare");
 }
 
 }  // extern "C"

@@ -304,6 +304,16 @@ def dv_field_f32_device(pk: PoissonKernel, fd: FDivergence, p: int, clamp: float
         nat.call("pf_dense_tv_f32", P32.data_ptr(), ld32, dk.rows, dk.k, st.tgt, st.tmask, c,
                  F32_GUARD_TAU, dk.row0, p, dk.is_interior.data_ptr(), dk.P.data_ptr(), dk.ld,
                  out.data_ptr(), flags, s.cuda_stream)
+    # clamped flag from the FP64 rows (see pf_mask_compare_f64 in the header)
+    if c > 0.0:
+        nonuni, ref = dk.mask_nonuniform(c)
+        fw = out[dk.rows:].view(t.int32)
+        if ref is not None:
+            if nonuni:
+                fw[0] = 1
+            else:
+                nat.call("pf_mask_compare_f64", row.data_ptr(), ref.data_ptr(), dk.k, c,
+                         fw.data_ptr(), s.cuda_stream)
     del st
     return out[:dk.rows], out[dk.rows:].view(t.int32)
 
