@@ -37,11 +37,17 @@ def torch():
     return _torch
 
 
+_cuda_ok = False
+
+
 def require_cuda():
+    global _cuda_ok
     t = torch()
-    if not t.cuda.is_available():
-        raise NativeError(-101, "no CUDA device visible: the B200 path has no CPU fallback")
-    nat.load()
+    if not _cuda_ok:
+        if not t.cuda.is_available():
+            raise NativeError(-101, "no CUDA device visible: the B200 path has no CPU fallback")
+        nat.load()
+        _cuda_ok = True
     return t
 
 
@@ -92,6 +98,7 @@ class DeviceKernel:
         self.is_interior = t.from_numpy(interior[self.row0:self.row0 + self.rows].copy()).to(self.device)
         self._H = {}
         self._csr = {}
+        self._scratch = {}
         self._uniform = {}
         self._p32 = None
         self._min = None
@@ -186,6 +193,24 @@ class DeviceKernel:
         with self._lock:
             self._uniform[key] = res
         return res
+
+    def scratch(self, stream_handle: int, nbytes: int, tag: str):
+        """Per-(thread, stream, tag) device scratch reused across calls.
+
+        Safe because every user of a scratch buffer enqueues on that same
+        stream, so a later call's writes are ordered after the earlier call's
+        kernels."""
+        key = (threading.get_ident(), stream_handle, tag)
+        buf = self._scratch.get(key)
+        if buf is None or buf.numel() < nbytes:
+            t = torch()
+            buf = t.empty(nbytes, dtype=t.uint8, device=self.device)
+            self._scratch[key] = buf
+        return buf
+
+    def row_ptr(self, p: int) -> int:
+        """Device address of row p of this slab."""
+        return self.P.data_ptr() + (p - self.row0) * self.ld * 8
 
     def target_row(self, p: int, host_dense: np.ndarray | None = None):
         """Device view of the raw target row P[p, :k].

@@ -106,12 +106,17 @@ def symbols() -> list[str]:
     return [s for s in header_symbols() if hasattr(lib, s)]
 
 
+_fns: dict = {}
+
+
 def call(name: str, *args) -> None:
     """Invoke an entry point; raise NativeError with pf_last_error() on failure."""
-    lib = load()
-    rc = getattr(lib, name)(*args)
+    fn = _fns.get(name)
+    if fn is None:
+        fn = _fns[name] = getattr(load(), name)
+    rc = fn(*args)
     if rc != 0:
-        msg = lib.pf_last_error().decode(errors="replace")
+        msg = load().pf_last_error().decode(errors="replace")
         raise NativeError(rc, f"{name}: {msg}")
 
 

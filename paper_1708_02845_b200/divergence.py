@@ -129,11 +129,14 @@ def _effective_clamp(dk, clamp) -> float:
 
 
 class _Staging:
-    """Per-call device scratch for K0: clamped target row, its logs, mask."""
+    """Device scratch for K0: clamped target row, its logs, mask.
 
-    def __init__(self, t, k: int, device):
+    With `buf` given (a reused per-(thread, stream) scratch) nothing is allocated."""
+
+    def __init__(self, t, k: int, device, buf=None):
         k_pad, m_pad = dev.round_up(k, 2), dev.round_up(k, 16)
-        self.buf = t.empty(16 * k_pad + m_pad, dtype=t.uint8, device=device)
+        self.buf = buf if buf is not None else t.empty(16 * k_pad + m_pad, dtype=t.uint8,
+                                                      device=device)
         base = self.buf.data_ptr()
         self.tgt = base
         self.logt = base + 8 * k_pad
@@ -144,9 +147,16 @@ def _field_device(pk, dk, fd, p: int, swap_order: bool, clamp: float, out_dev, f
                   stream, target_row=None):
     """Launch K0 + the field kernel for slab `dk` into `out_dev` (device)."""
     t = dev.torch()
-    st = _Staging(t, dk.k, dk.device)
-    row = target_row if target_row is not None else dk.target_row(p)
-    nat.call("pf_target_prep_f64", row.data_ptr(), dk.k, clamp, st.tgt, st.logt, st.tmask,
+    k_pad, m_pad = dev.round_up(dk.k, 2), dev.round_up(dk.k, 16)
+    st = _Staging(t, dk.k, dk.device, dk.scratch(stream, 16 * k_pad + m_pad, "stage"))
+    if target_row is not None:
+        row_ptr = target_row.data_ptr()
+    elif dk.owns(p):
+        row_ptr = dk.row_ptr(p)
+    else:
+        st.row = dk.target_row(p)  # host copy of a row outside this slab; kept alive on st
+        row_ptr = st.row.data_ptr()
+    nat.call("pf_target_prep_f64", row_ptr, dk.k, clamp, st.tgt, st.logt, st.tmask,
              flags_ptr, stream)
     kind, param = _kind_param(fd)
     if kind == 0 and not swap_order:
@@ -203,9 +213,10 @@ def dv_field(pk: PoissonKernel, fd: FDivergence, p: int,
     if clamp is None:
         clamp = fd.clamp
     c = _effective_clamp(dk, clamp)
-    buf = t.empty(dk.rows + 2, dtype=t.float64, device=dk.device)
-    flags_ptr = buf.data_ptr() + dk.rows * 8
     s = t.cuda.current_stream(dk.device)
+    # the device output is internal here (copied back before returning): reuse it
+    buf = dk.scratch(s.cuda_stream, 8 * (dk.rows + 2), "out").view(t.float64)[:dk.rows + 2]
+    flags_ptr = buf.data_ptr() + dk.rows * 8
     st = _field_device(pk, dk, fd, p, swap_order, c, buf, flags_ptr, s.cuda_stream)
     host = _to_host(t, buf, s)
     del st
