@@ -491,7 +491,8 @@ def extra_tracer(t, nat, dev, pf, device):
     src = rng.choice(mesh.n, npaths)
     fo = np.arange(npaths) % T
     src = np.where(src == targets[fo], (src + 1) % mesh.n, src)
-    PP.trace_arrays(mesh, fields[:1], targets[:1], src[:64])  # warm-up
+    for _ in range(2):  # warm-up at full size (workspace + topology caches)
+        PP.trace_arrays(mesh, fields, targets, src, fo)
     t.cuda.synchronize()
     e0, e1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
     s = t.cuda.current_stream(device)

@@ -14,6 +14,7 @@ The location sequence is bit-identical to the reference given the same field
 from __future__ import annotations
 
 import ctypes
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -72,7 +73,13 @@ def _byref(s):
 class PathBuffers:
     """Device output of one tracer launch (pf_paths_t) and its host copy."""
 
+    def reshape(self, cap: int) -> None:
+        """Reuse the same storage with a different per-path capacity."""
+        self.cap = cap
+        self.struct.cap = cap
+
     def __init__(self, t, npaths: int, cap: int, device):
+        self.npaths, self.cap_total = npaths, npaths * cap
         self.cap = cap
         tot = max(npaths * cap, 1)
         self.kind = t.empty(tot, dtype=t.int8, device=device)
@@ -91,6 +98,27 @@ class PathBuffers:
                               self.stuck.data_ptr(), self.q[0].data_ptr(), self.q[1].data_ptr())
 
 
+_ws_lock = threading.Lock()
+_workspaces: dict = {}
+
+
+def _workspace(t, npaths: int, cap: int, device, slot: str) -> PathBuffers:
+    """Per-(thread, device, slot) path output buffers, grown on demand and reused:
+    a 10,000-path launch needs ~2.7 GB of location buffers, and fresh device
+    allocations of that size cost more than the trace itself."""
+    key = (threading.get_ident(), str(device), slot)
+    with _ws_lock:
+        ws = _workspaces.get(key)
+    if ws is None or ws.npaths < npaths or ws.cap_total < npaths * cap:
+        ws = PathBuffers(t, max(npaths, 1), cap, device)
+        ws.npaths, ws.cap_total = max(npaths, 1), max(npaths, 1) * cap
+        with _ws_lock:
+            _workspaces[key] = ws
+    else:
+        ws.reshape(cap)
+    return ws
+
+
 def _fields_to_device(t, fields, n, device):
     """Stack field values (numpy or device tensors) into an (F, n) FP64 device tensor."""
     vals = []
@@ -107,8 +135,10 @@ def trace_arrays(mesh, fields, targets, sources, field_of=None, settings: Settin
                  cap: int | None = None, entry: str = "pf_trace_batch_f64"):
     """Launch K8 and return the raw device outputs (PathBuffers), rerunning overflows.
 
-    `fields` is a list of field values (numpy or device tensors), `targets`
-    their targets, `sources` the start vertices, `field_of[p]` the field of path p.
+    `fields` is a list of field values (numpy or device tensors) or an (F, n)
+    device tensor, `targets` their targets, `sources` the start vertices,
+    `field_of[p]` the field of path p.  The returned buffers are a per-thread
+    workspace: valid until the next call from the same thread.
     """
     t = dev.require_cuda()
     dm = device_mesh(mesh)
@@ -127,7 +157,7 @@ def trace_arrays(mesh, fields, targets, sources, field_of=None, settings: Settin
     s = t.cuda.current_stream(dm.device).cuda_stream
     if cap is None:
         cap = int(min(step_cap + 2, max(64, 8 * int(np.sqrt(dm.n)) + 64)))
-    buf = PathBuffers(t, npaths, cap, dm.device)
+    buf = _workspace(t, npaths, cap, dm.device, "main")
     nat.call(entry, _byref(dm.struct), F.data_ptr(), tgt_d.data_ptr(),
              src_d.data_ptr(), nat.ptr(fo_d), npaths, step_cap, _byref(buf.struct), s)
     counts = buf.count.cpu().numpy()
@@ -137,7 +167,7 @@ def trace_arrays(mesh, fields, targets, sources, field_of=None, settings: Settin
         cap2 = int(counts[over].max())
         sub_src = t.from_numpy(sources[over]).to(dm.device)
         sub_fo = None if fo is None else t.from_numpy(fo[over]).to(dm.device)
-        extra = PathBuffers(t, over.size, cap2, dm.device)
+        extra = _workspace(t, over.size, cap2, dm.device, "overflow")
         nat.call(entry, _byref(dm.struct), F.data_ptr(), tgt_d.data_ptr(),
                  sub_src.data_ptr(), nat.ptr(sub_fo), over.size, step_cap,
                  _byref(extra.struct), s)
