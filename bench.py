@@ -611,6 +611,34 @@ def run_native(args):
                        "each n-vector field + flags is copied D2H into a fresh numpy array and "
                        "returned as a read-only ScalarField"}
         del host, pk
+    else:
+        # N > 1: the sharded public API (parallel.ShardedField.field: NCCL broadcast of
+        # the target row + slab kernels), each rank's field slab copied back to host
+        from paper_1708_02845_b200 import _hostpool
+        kl, tv = pf.builtin_f("kl"), pf.builtin_f("tv")
+
+        def e2e_step():
+            a = sharded.field(kl, target)
+            ha = _hostpool.to_host(t, a, stream)
+            b = sharded.field(tv, target)
+            hb = _hostpool.to_host(t, b, stream)
+            return ha, hb
+
+        for _ in range(args.warmup):
+            keep = e2e_step()
+        barrier()
+        w0 = time.perf_counter()
+        for _ in range(args.steps):
+            keep = e2e_step()
+        barrier()
+        e2e_s = max_over_ranks(time.perf_counter() - w0)
+        del keep
+        e2e = {"value": 2 * rows * ws * args.steps / e2e_s, "unit": "evals/s",
+               "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 2 * rows * 8 * ws,
+               "ms_per_step": 1e3 * e2e_s / args.steps,
+               "note": "wall clock (max over ranks) of ShardedField.field(kl|tv, t) per step: "
+                       "NCCL broadcast of the target row from its owner, the slab kernels, "
+                       "and each rank's field slab copied to host memory"}
 
     # ------------------------------------------------ CPU baseline (rank 0, N=1)
     cpu = None
