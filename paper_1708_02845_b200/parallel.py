@@ -91,6 +91,33 @@ class ShardedField:
             return vals
         return self.gather(vals)
 
+    def sparse_field(self, fd, p: int, threshold: float | None = None, gather: bool = False):
+        """This rank's slab of the sparse (CSR) field to target p (divergence.py:255-299).
+
+        KL needs the target's dense log row: the dense row is broadcast as for
+        :meth:`field`.  TV needs the target's sparsified row: its owner scatters it
+        (K6 prep) and broadcasts the dense k-vector plus (S_p, dropped_p, nnz_p).
+        CSR slabs should be partitioned with :func:`partition_by_weight` over nnz.
+        """
+        import math
+        t = dev.torch()
+        n, k = self.slab.n, self.slab.k
+        thr = 1.0 / math.sqrt(n) if threshold is None else float(threshold)
+        cut = thr / k
+        if fd.name == "kl":
+            payload = self.target_row(p, k)
+        elif fd.name == "tv":
+            own = owner_of(p, self.bounds)
+            kp = k + (k & 1)
+            payload = t.empty(kp + 4, dtype=t.float64, device=self.device)
+            if self.rank == own:
+                _sparse_tv_prep(self.slab, cut, thr == 0, p, payload)
+            self.dist.broadcast(payload, src=own)
+        else:
+            raise NotImplementedError("sparse fields implement kl and tv")
+        vals = _compute_sparse_slab(self.slab, fd, p, payload, cut, thr == 0)
+        return self.gather(vals) if gather else vals
+
     def gather(self, vals):
         """All-gather variable-size slabs into the full n-vector on every rank."""
         t = dev.torch()
@@ -113,4 +140,42 @@ def _compute_slab(slab, fd, p: int, target_row, clamp=None):
     st = _field_device(None, slab, fd, p, False, c, out, out.data_ptr() + slab.rows * 8, s,
                        target_row=target_row)
     del st
+    return out[:slab.rows]
+
+
+def _sparse_tv_prep(slab, cut, strict, p, payload):
+    """Owner side of the TV broadcast: K6 target prep into `payload` (vp, then tscal)."""
+    from . import _native as nat
+    t = dev.require_cuda()
+    dc = slab.csr(cut, strict)
+    kp = slab.k + (slab.k & 1)
+    nat.call("pf_csr_target_prep_f64", dc.indptr.data_ptr(), dc.indices.data_ptr(),
+             dc.data.data_ptr(), dc.dropped.data_ptr(), p - slab.row0, slab.k,
+             payload.data_ptr(), payload.data_ptr() + kp * 8,
+             t.cuda.current_stream(slab.device).cuda_stream)
+
+
+def _compute_sparse_slab(slab, fd, p: int, payload, cut: float, strict: bool):
+    """The slab's CSR field to target p (K5 with the broadcast dense row, or K6 with
+    the broadcast sparsified target row)."""
+    from . import _native as nat
+    from .divergence import KL_GUARD_TAU, _CLAMP_LOG, _Staging
+    t = dev.require_cuda()
+    dc = slab.csr(cut, strict)
+    s = t.cuda.current_stream(slab.device).cuda_stream
+    out = t.empty(slab.rows + 2, dtype=t.float64, device=slab.device)
+    flags = out.data_ptr() + slab.rows * 8
+    out.view(t.int32)[2 * slab.rows:].zero_()
+    if fd.name == "kl":
+        st = _Staging(t, slab.k, slab.device)
+        nat.call("pf_target_prep_f64", payload.data_ptr(), slab.k, _CLAMP_LOG, st.tgt, st.logt,
+                 st.tmask, flags, s)
+        nat.call("pf_csr_kl_f64", dc.indptr.data_ptr(), dc.indices.data_ptr(), dc.data.data_ptr(),
+                 dc.log_data.data_ptr(), dc.hs.data_ptr(), slab.rows, slab.k, st.logt,
+                 KL_GUARD_TAU, slab.row0, 0, slab.rows, out.data_ptr(), 0, flags, s)
+    else:
+        kp = slab.k + (slab.k & 1)
+        nat.call("pf_csr_tv_f64", dc.indptr.data_ptr(), dc.indices.data_ptr(), dc.data.data_ptr(),
+                 dc.dropped.data_ptr(), slab.rows, slab.k, payload.data_ptr(),
+                 payload.data_ptr() + kp * 8, slab.row0, 0, slab.rows, out.data_ptr(), 0, s)
     return out[:slab.rows]

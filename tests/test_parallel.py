@@ -37,7 +37,7 @@ def test_partitions():
 class _Slab:
     def __init__(self, P, r0, r1):
         self.P = torch.from_numpy(P[r0:r1].copy())
-        self.row0, self.rows, self.k = r0, r1 - r0, P.shape[1]
+        self.row0, self.rows, self.k, self.n = r0, r1 - r0, P.shape[1], P.shape[0]
         self.device = torch.device("cpu")
 
 
@@ -54,7 +54,18 @@ def _worker(rank, world, port, P, boundary, target, q):
             vals[np.arange(slab.row0, slab.row0 + slab.rows) == p] = 0.0
             return torch.from_numpy(vals)
 
+        def oracle_sparse_slab(slab, fd, p, payload, cut, strict):
+            full = np.vstack([P[p][None, :], slab.P.numpy()])  # restated from the dense rows
+            vals = np.array([O.dv_pair_sparse_direct(P, p, q, fd.name)[0]
+                             for q in range(slab.row0, slab.row0 + slab.rows)])
+            return torch.from_numpy(vals)
+
+        def oracle_tv_prep(slab, cut, strict, p, payload):
+            payload.fill_(float(p))  # any owner-computed payload: checks the broadcast path
+
         par._compute_slab = oracle_slab
+        par._compute_sparse_slab = oracle_sparse_slab
+        par._sparse_tv_prep = oracle_tv_prep
         bounds = par.partition_rows(P.shape[0], world)
         slab = _Slab(P, *bounds[rank])
         sf = par.ShardedField(slab, bounds, dist, device=torch.device("cpu"))
@@ -64,6 +75,9 @@ def _worker(rank, world, port, P, boundary, target, q):
             full = sf.field(pf.builtin_f(g), target, gather=True).numpy()
             ref, _ = O.dv_field(P, boundary, g, target)
             q.put((rank, g, bool(np.array_equal(full, ref))))
+            sp = sf.sparse_field(pf.builtin_f(g), target, gather=True).numpy()
+            sref = np.array([O.dv_pair_sparse_direct(P, target, qq, g)[0] for qq in range(P.shape[0])])
+            q.put((rank, "sparse-" + g, bool(np.array_equal(sp, sref))))
     finally:
         dist.destroy_process_group()
 
@@ -88,7 +102,7 @@ def test_sharded_field_gloo(world):
              for r in range(world)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=120) for _ in range(2 * world)]
+    res = [q.get(timeout=120) for _ in range(4 * world)]
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0

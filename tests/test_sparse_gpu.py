@@ -140,3 +140,29 @@ def test_synthetic_sparse_vs_oracle(n, k, thr):
         ref = O.dv_field_sparse(sv, g, t)
         ok, err = rel_close(got, ref, RTOL)
         assert ok, (g, err)
+
+
+def test_sparse_slabs_bitwise():
+    """CSR row slabs (as N GPUs would hold them) give bitwise the 1-slab sparse field."""
+    import math
+    import torch
+    from paper_1708_02845_b200 import _device as dev
+    from paper_1708_02845_b200 import parallel as par
+    c = case("corridor50")
+    spk = pf.sparsify(_pk(c))
+    cut = (1.0 / math.sqrt(c.n)) / c.k
+    full = {g: pf.dv_field_sparse(spk, pf.builtin_f(g), c.target).values for g in ("kl", "tv")}
+    indptr = spk.sparse.indptr
+    bounds = par.partition_by_weight(np.diff(indptr), 3)
+    slabs = [dev.DeviceKernel(c.dense, c.boundary, row0=a, rows=b - a) for a, b in bounds]
+    own = par.owner_of(c.target, bounds)
+    kp = c.k + (c.k & 1)
+    tv_payload = torch.empty(kp + 4, dtype=torch.float64, device="cuda")
+    par._sparse_tv_prep(slabs[own], cut, False, c.target, tv_payload)
+    kl_payload = torch.from_numpy(c.dense[c.target].copy()).cuda()
+    for g, payload in (("kl", kl_payload), ("tv", tv_payload)):
+        parts = [par._compute_sparse_slab(sl, pf.builtin_f(g), c.target, payload, cut, False)
+                 for sl in slabs]
+        torch.cuda.synchronize()
+        got = torch.cat(parts).cpu().numpy()
+        np.testing.assert_array_equal(got, full[g])
