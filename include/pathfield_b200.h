@@ -218,6 +218,19 @@ int pf_csr_tv_f64(const int64_t *indptr, const int32_t *indices, const double *d
                   const double *tscal, int64_t row0, const int64_t *queries, int64_t nq,
                   double *out, int64_t *ops, pf_stream_t stream);
 
+/* ---- K5/K6 for the other generators (divergence.py:275-299) ---------------
+ * kind PF_DIV_ALPHA: sum_{supp q} v (1 - exp(expo (logt - log v))) * scale,
+ *   settle; ops = |supp q|.  Needs logt (the target's dense log row).
+ * kind PF_DIV_CHI2 / PF_DIV_HELLINGER / PF_DIV_POWER: the union form with
+ *   weights clamped at `cut`; prow = the target's DENSE row, p_local its row in
+ *   this slab's CSR; scratch >= 2k + 4 doubles + k bytes; ops = |union|.
+ * Both settle the result. */
+int pf_csr_generic_f64(const int64_t *indptr, const int32_t *indices, const double *data,
+                       const double *log_data, int64_t rows, int64_t k, int kind, double param,
+                       double cut, const double *prow, int64_t p_local, const double *logt,
+                       double *scratch, int64_t row0, const int64_t *queries, int64_t nq,
+                       double *out, int64_t *ops, pf_stream_t stream);
+
 /* Elementwise log view: out[r*k + c] = log(max(P[r*ld + c], clamp)), the
  * reference's log_dense (divergence.py:226), materialised on request. */
 int pf_log_clamped_f64(const double *P, int64_t ld, int64_t rows, int64_t k, double clamp,

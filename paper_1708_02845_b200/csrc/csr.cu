@@ -353,6 +353,120 @@ __global__ void __launch_bounds__(kCsrThreads) csr_tv_kernel(
   }
 }
 
+// ---------------------------------------------------- other generators --
+// divergence.py:275-299 for the remaining builtins.
+//  alpha:   sum_{supp q} v (1 - exp(expo (logPt - log v))), times scale; settle.
+//  chi2 / hellinger / power-p: over supp(p) U supp(q) with weights clamped at
+//  the row cut, vq = v (or cut off-support), vp = max(P[p, j], cut):
+//      sum_{supp q} vq f(vp/vq) + sum_{supp p \ supp q} cut f(vp/cut)
+//  restated as one pass over supp(q) with g_j = cut f(vp_j/cut) [j in supp p]
+//  precomputed per target:  sum_{supp q} (vq f(vp/vq) - g_j) + C_p,
+//  C_p = sum_{supp p} g_j reduced in csr_row_visit order (so q = p is exactly 0).
+template <int KIND>
+__device__ __forceinline__ double gen_f(double x, double param) {
+  if (KIND == PF_DIV_CHI2) return __dsub_rn(__dmul_rn(x, x), 1.0);
+  if (KIND == PF_DIV_HELLINGER) {
+    const double s = sqrt(x) - 1.0;
+    return __dmul_rn(s, s);
+  }
+  const double d = fabs(1.0 - x);  // PF_DIV_POWER
+  return (param == 2.0) ? d * d : pow(d, param);
+}
+
+template <int KIND>
+__global__ void csr_generic_prep_kernel(const double *__restrict__ prow, int64_t k, double cut,
+                                        double param, const int64_t *__restrict__ indptr,
+                                        const int32_t *__restrict__ indices,
+                                        const double *__restrict__ data, int64_t p,
+                                        double *__restrict__ vpc, double *__restrict__ g,
+                                        uint8_t *__restrict__ mask, double *__restrict__ tscal) {
+  for (int64_t j = threadIdx.x; j < k; j += blockDim.x) {
+    vpc[j] = fmax(prow[j], cut);
+    g[j] = 0.0;
+    mask[j] = 0;
+  }
+  __syncthreads();
+  const int64_t lo = indptr[p], hi = indptr[p + 1];
+  for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) {
+    const int32_t j = indices[e];
+    g[j] = __dmul_rn(cut, gen_f<KIND>(__ddiv_rn(vpc[j], cut), param));
+    mask[j] = 1;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    double a = 0.0;
+    csr_row_visit(data, indices, lo, hi, lane, [&](double, int32_t c) { a += g[c]; });
+    a = warp_sum(a);
+    if (lane == 0) {
+      tscal[0] = a;
+      tscal[1] = 0.0;
+      tscal[2] = static_cast<double>(hi - lo);
+      tscal[3] = 0.0;
+    }
+  }
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kCsrThreads) csr_generic_kernel(
+    const int64_t *__restrict__ indptr, const int32_t *__restrict__ indices,
+    const double *__restrict__ data, int64_t rows, const double *__restrict__ vpc,
+    const double *__restrict__ g, const uint8_t *__restrict__ mask,
+    const double *__restrict__ tscal, double param, int64_t row0,
+    const int64_t *__restrict__ queries, int64_t nq, double *__restrict__ out,
+    int64_t *__restrict__ ops) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t count = queries ? nq : rows;
+  const double C_p = tscal[0];
+  const int64_t nnz_p = static_cast<int64_t>(tscal[2]);
+  for (int64_t i = warp; i < count; i += nwarps) {
+    const int64_t r = queries ? queries[i] - row0 : i;
+    const int64_t lo = indptr[r], hi = indptr[r + 1];
+    double a = 0.0;
+    int inter = 0;
+    csr_row_visit(data, indices, lo, hi, lane, [&](double v, int32_t c) {
+      a += __dmul_rn(v, gen_f<KIND>(__ddiv_rn(__ldg(vpc + c), v), param)) - __ldg(g + c);
+      inter += __ldg(mask + c);
+    });
+    const double val = settle(warp_sum(a) + C_p);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) inter += __shfl_xor_sync(0xffffffffu, inter, o);
+    if (lane == 0) {
+      out[i] = val;
+      if (ops) ops[i] = (hi - lo) + nnz_p - inter;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kCsrThreads) csr_alpha_kernel(
+    const int64_t *__restrict__ indptr, const int32_t *__restrict__ indices,
+    const double *__restrict__ data, const double *__restrict__ log_data, int64_t rows,
+    const double *__restrict__ logt, double alpha, int64_t row0,
+    const int64_t *__restrict__ queries, int64_t nq, double *__restrict__ out,
+    int64_t *__restrict__ ops) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t count = queries ? nq : rows;
+  const double scale = 4.0 / (1.0 - alpha * alpha), expo = (1.0 + alpha) / 2.0;
+  for (int64_t i = warp; i < count; i += nwarps) {
+    const int64_t r = queries ? queries[i] - row0 : i;
+    const int64_t lo = indptr[r], hi = indptr[r + 1];
+    double a = 0.0;
+    for (int64_t e = lo + lane; e < hi; e += 32) {
+      const double rp = exp(__dmul_rn(expo, __ldg(logt + indices[e]) - log_data[e]));
+      a += __dmul_rn(data[e], 1.0 - rp);
+    }
+    const double val = settle(__dmul_rn(scale, warp_sum(a)));
+    if (lane == 0) {
+      out[i] = val;
+      if (ops) ops[i] = hi - lo;
+    }
+  }
+}
+
 __global__ void log_clamped_kernel(const double *__restrict__ P, int64_t ld, int64_t rows,
                                    int64_t k, double clamp, double *__restrict__ out) {
   const int64_t n = rows * k;
@@ -483,6 +597,42 @@ int pf_csr_tv_f64(const int64_t *indptr, const int32_t *indices, const double *d
         indptr, indices, data, dropped, rows, k_pad, vp, tscal, row0, queries, nq, out, ops);
   }
   return check_launch("csr_tv");
+}
+
+int pf_csr_generic_f64(const int64_t *indptr, const int32_t *indices, const double *data,
+                       const double *log_data, int64_t rows, int64_t k, int kind, double param,
+                       double cut, const double *prow, int64_t p_local, const double *logt,
+                       double *scratch, int64_t row0, const int64_t *queries, int64_t nq,
+                       double *out, int64_t *ops, pf_stream_t stream) {
+  if (!indptr || !out || rows < 0 || k <= 0) return fail(PF_E_ARG, "csr_generic: bad args");
+  const int64_t count = queries ? nq : rows;
+  if (count <= 0) return 0;
+  const int g = grid_for((const void *)csr_alpha_kernel, kCsrThreads, 0, count);
+  if (kind == PF_DIV_ALPHA) {
+    if (!logt) return fail(PF_E_ARG, "csr_generic: alpha needs logt");
+    csr_alpha_kernel<<<g, kCsrThreads, 0, as_stream(stream)>>>(
+        indptr, indices, data, log_data, rows, logt, param, row0, queries, nq, out, ops);
+    return check_launch("csr_alpha");
+  }
+  if (!prow || !scratch || p_local < 0) return fail(PF_E_ARG, "csr_generic: target row");
+  double *vpc = scratch, *gg = scratch + k, *tscal = scratch + 2 * k;
+  uint8_t *mask = reinterpret_cast<uint8_t *>(scratch + 2 * k + 4);
+#define PF_CSR_GEN(KIND)                                                                      \
+  case KIND:                                                                                  \
+    csr_generic_prep_kernel<KIND><<<1, 512, 0, as_stream(stream)>>>(                          \
+        prow, k, cut, param, indptr, indices, data, p_local, vpc, gg, mask, tscal);           \
+    csr_generic_kernel<KIND><<<g, kCsrThreads, 0, as_stream(stream)>>>(                       \
+        indptr, indices, data, rows, vpc, gg, mask, tscal, param, row0, queries, nq, out, ops); \
+    break;
+  switch (kind) {
+    PF_CSR_GEN(PF_DIV_CHI2)
+    PF_CSR_GEN(PF_DIV_HELLINGER)
+    PF_CSR_GEN(PF_DIV_POWER)
+    default:
+      return fail(PF_E_ARG, "csr_generic: kind %d not supported here", kind);
+  }
+#undef PF_CSR_GEN
+  return check_launch("csr_generic");
 }
 
 int pf_log_clamped_f64(const double *P, int64_t ld, int64_t rows, int64_t k, double clamp,

@@ -506,12 +506,10 @@ def _device_csr(pk):
 
 
 def _sparse_launch(pk, fd, p: int, queries=None, want_ops=False):
-    """Launch K5/K6 for target p over all slab rows or `queries` (device tensors back)."""
+    """Launch K5/K6 (or the other-generator CSR kernels) for target p over all slab
+    rows or `queries`; returns device tensors."""
     t = dev.require_cuda()
-    if fd.name not in ("kl", "tv"):
-        raise NotImplementedError(
-            f"sparse {fd.name!r}: the device path implements the kl and tv sparse forms "
-            "(divergence.py:275-295)")
+    kind, param = _kind_param(fd)
     dk, dc = _device_csr(pk)
     s = t.cuda.current_stream(dk.device)
     qd = None
@@ -521,29 +519,44 @@ def _sparse_launch(pk, fd, p: int, queries=None, want_ops=False):
         count = qd.numel()
     out = t.empty(count + 2, dtype=t.float64, device=dk.device)
     flags = out.data_ptr() + count * 8
+    out.view(t.int32)[2 * count:2 * count + 4].zero_()
     ops = t.empty(max(count, 1), dtype=t.int64, device=dk.device) if want_ops else None
     qptr = 0 if qd is None else qd.data_ptr()
     k_pad = dev.round_up(dk.k, 2)
-    if fd.name == "kl":
+    if not dk.owns(p):
+        raise NotImplementedError("target row outside this slab: use parallel.ShardedField")
+    if fd.name in ("kl", "alpha"):
         st = _Staging(t, dk.k, dk.device)
-        row = dk.target_row(p)
-        nat.call("pf_target_prep_f64", row.data_ptr(), dk.k, _CLAMP_LOG, st.tgt, st.logt,
+        nat.call("pf_target_prep_f64", dk.row_ptr(p), dk.k, _CLAMP_LOG, st.tgt, st.logt,
                  st.tmask, flags, s.cuda_stream)
-        nat.call("pf_csr_kl_f64", dc.indptr.data_ptr(), dc.indices.data_ptr(), dc.data.data_ptr(),
-                 dc.log_data.data_ptr(), dc.hs.data_ptr(), dk.rows, dk.k, st.logt,
-                 KL_GUARD_TAU, dk.row0, qptr, count, out.data_ptr(), nat.ptr(ops), flags,
-                 s.cuda_stream)
-    else:
-        if not dk.owns(p):
-            raise NotImplementedError("target row outside this slab: use parallel.ShardedCSR")
+        if fd.name == "kl":
+            nat.call("pf_csr_kl_f64", dc.indptr.data_ptr(), dc.indices.data_ptr(),
+                     dc.data.data_ptr(), dc.log_data.data_ptr(), dc.hs.data_ptr(), dk.rows,
+                     dk.k, st.logt, KL_GUARD_TAU, dk.row0, qptr, count, out.data_ptr(),
+                     nat.ptr(ops), flags, s.cuda_stream)
+        else:
+            nat.call("pf_csr_generic_f64", dc.indptr.data_ptr(), dc.indices.data_ptr(),
+                     dc.data.data_ptr(), dc.log_data.data_ptr(), dk.rows, dk.k, kind, param,
+                     0.0, 0, -1, st.logt, 0, dk.row0, qptr, count, out.data_ptr(),
+                     nat.ptr(ops), s.cuda_stream)
+    elif fd.name == "tv":
         st = t.empty(k_pad + 4, dtype=t.float64, device=dk.device)
-        out.view(t.int32)[2 * count:2 * count + 4].zero_()
         nat.call("pf_csr_target_prep_f64", dc.indptr.data_ptr(), dc.indices.data_ptr(),
                  dc.data.data_ptr(), dc.dropped.data_ptr(), p - dk.row0, dk.k, st.data_ptr(),
                  st.data_ptr() + k_pad * 8, s.cuda_stream)
         nat.call("pf_csr_tv_f64", dc.indptr.data_ptr(), dc.indices.data_ptr(), dc.data.data_ptr(),
                  dc.dropped.data_ptr(), dk.rows, dk.k, st.data_ptr(), st.data_ptr() + k_pad * 8,
                  dk.row0, qptr, count, out.data_ptr(), nat.ptr(ops), s.cuda_stream)
+    else:
+        # chi2 / hellinger / power-p: union form, weights clamped at the row cut
+        # (divergence.py:296-299; the clamp when the cut is 0)
+        row_cut = getattr(pk, "row_cut", None)
+        cut = float(row_cut) if row_cut and row_cut > 0 else float(fd.clamp)
+        st = t.empty(2 * dk.k + 4 + (dk.k + 7) // 8, dtype=t.float64, device=dk.device)
+        nat.call("pf_csr_generic_f64", dc.indptr.data_ptr(), dc.indices.data_ptr(),
+                 dc.data.data_ptr(), dc.log_data.data_ptr(), dk.rows, dk.k, kind, param, cut,
+                 dk.row_ptr(p), p - dk.row0, 0, st.data_ptr(), dk.row0, qptr, count,
+                 out.data_ptr(), nat.ptr(ops), s.cuda_stream)
     return out, ops, count, s, st
 
 

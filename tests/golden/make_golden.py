@@ -120,9 +120,14 @@ def main(only=None):
             out["sp/sha_data"] = np.array(I.sha(spk.sparse.data))
             out["sp/dropped"] = spk.dropped_mass
             out["sp/meta"] = np.array([spk.threshold, spk.row_cut, spk.sparsity_percent])
-            for gname in ("kl", "tv"):
-                fd = builtin_f(gname)
-                vals, ops = zip(*[dv_pair_sparse_stats(spk, fd, tgt0, q) for q in range(n)])
+            sgens = [("kl", {}), ("tv", {})]
+            if name in ("corridor50", "c1"):
+                sgens += [("chi2", {}), ("hellinger", {}), ("alpha", {"alpha": 0.5}),
+                          ("power-p", {"power": 3})]
+            for gname, kw in sgens:
+                fd = builtin_f(gname, **kw)
+                with np.errstate(all="ignore"):
+                    vals, ops = zip(*[dv_pair_sparse_stats(spk, fd, tgt0, q) for q in range(n)])
                 out[f"spfield/{gname}"] = np.array(vals)
                 out[f"spops/{gname}"] = np.array(ops, np.int64)
         # traced paths on the reference's own fields

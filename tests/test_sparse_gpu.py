@@ -42,14 +42,24 @@ def test_sparsify_bitwise(name):
     assert set(rep) == {"threshold", "sparsity_percent", "max_dropped_row_mass"}
 
 
+GENS = {"kl": {}, "tv": {}, "chi2": {}, "hellinger": {}, "alpha": {"alpha": 0.5},
+        "power-p": {"power": 3}}
+
+
 @pytest.mark.parametrize("name", SPARSE_CASES)
-@pytest.mark.parametrize("g", ["kl", "tv"])
+@pytest.mark.parametrize("g", list(GENS))
 def test_sparse_field_matches_reference_pair_loop(name, g):
     c = case(name)
+    if f"spfield/{g}" not in c.keys():
+        pytest.skip("golden has kl/tv only for this case")
     spk = pf.sparsify(_pk(c))
-    fld = pf.dv_field_sparse(spk, pf.builtin_f(g), c.target)
+    fld = pf.dv_field_sparse(spk, pf.builtin_f(g, **GENS[g]), c.target)
     ok, err = rel_close(fld.values, c[f"spfield/{g}"], RTOL)
     assert ok, (name, g, err)
+    rng = np.random.default_rng(1)
+    for q in rng.choice(c.n, 8, replace=False):
+        _, ops = pf.dv_pair_sparse_stats(spk, pf.builtin_f(g, **GENS[g]), c.target, int(q))
+        assert ops == int(c[f"spops/{g}"][q]), (g, q)
 
 
 @pytest.mark.parametrize("name", SPARSE_CASES)
