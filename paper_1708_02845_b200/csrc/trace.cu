@@ -168,6 +168,9 @@ __global__ void __launch_bounds__(kTraceThreads) trace_kernel(pf_mesh_t m, const
   int status = ST_MAX;
   int64_t stuck = -1;
   double qx = 0.0, qy = 0.0;
+  bool carry = false;  // geometry of triangle `ti` already evaluated by _enters
+  Tri ct;
+  double cnorm = 0.0, cd[2] = {0.0, 0.0}, cdl[3] = {0.0, 0.0, 0.0}, cscale = 0.0;
 
   for (int64_t it = 0; it < cap; ++it) {
     if (!in_tri) {
@@ -233,16 +236,34 @@ __global__ void __launch_bounds__(kTraceThreads) trace_kernel(pf_mesh_t m, const
     }
 
     // ---------------- triangle rule (paths.py:200-254)
+    // The previous step's _enters() already evaluated this triangle's gradient,
+    // direction and dlam (the reference recomputes the identical values): reuse.
     Tri t;
-    load_tri(m, ti, t);
-    double g[2];
-    gradient(t, vals, g);
-    const double norm = np_hypot(g[0], g[1]);
+    double g[2], norm, d[2], dl[3], scale = 0.0;
+    if (carry) {
+      t = ct;
+      norm = cnorm;
+      d[0] = cd[0];
+      d[1] = cd[1];
+      dl[0] = cdl[0];
+      dl[1] = cdl[1];
+      dl[2] = cdl[2];
+      scale = cscale;
+      carry = false;
+    } else {
+      load_tri(m, ti, t);
+      gradient(t, vals, g);
+      norm = np_hypot(g[0], g[1]);
+      if (norm > 0.0) {
+        d[0] = __ddiv_rn(-g[0], norm);
+        d[1] = __ddiv_rn(-g[1], norm);
+        scale = dlam_of(t, d, dl);
+      }
+    }
     bool slide_best = norm <= 0.0;
-    double lam[3], dl[3], s_exit = INFINITY;
+    double lam[3], s_exit = INFINITY;
     int slot_exit = -1;
     if (!slide_best) {
-      const double d[2] = {__ddiv_rn(-g[0], norm), __ddiv_rn(-g[1], norm)};
       const double ax = m.vertices[2 * t.v[0]], ay = m.vertices[2 * t.v[0] + 1];
       const double bx = m.vertices[2 * t.v[1]], by = m.vertices[2 * t.v[1] + 1];
       const double cx = m.vertices[2 * t.v[2]], cy = m.vertices[2 * t.v[2] + 1];
@@ -262,7 +283,6 @@ __global__ void __launch_bounds__(kTraceThreads) trace_kernel(pf_mesh_t m, const
       const double sum = __dadd_rn(__dadd_rn(lam[0], lam[1]), lam[2]);
 #pragma unroll
       for (int s = 0; s < 3; ++s) lam[s] = __ddiv_rn(lam[s], sum);
-      const double scale = dlam_of(t, d, dl);
       const double thr = __dmul_rn(-1e-14, scale);
 #pragma unroll
       for (int s = 0; s < 3; ++s) {
@@ -359,23 +379,24 @@ __global__ void __launch_bounds__(kTraceThreads) trace_kernel(pf_mesh_t m, const
     const int64_t nt = m.tri_nbr[3 * ti + slot_exit];
     bool enters = false;
     if (nt >= 0) {
-      // _enters (paths.py:256-266)
-      Tri u;
-      load_tri(m, nt, u);
+      // _enters (paths.py:256-266); on success its geometry carries into the
+      // next step
+      load_tri(m, nt, ct);
       double gu[2];
-      gradient(u, vals, gu);
-      const double nu = np_hypot(gu[0], gu[1]);
-      if (nu > 0.0) {
-        const double du[2] = {__ddiv_rn(-gu[0], nu), __ddiv_rn(-gu[1], nu)};
+      gradient(ct, vals, gu);
+      cnorm = np_hypot(gu[0], gu[1]);
+      if (cnorm > 0.0) {
+        cd[0] = __ddiv_rn(-gu[0], cnorm);
+        cd[1] = __ddiv_rn(-gu[1], cnorm);
         int so = 0;
         for (int s = 0; s < 3; ++s)
-          if (u.v[s] != ei && u.v[s] != ej) so = s;
-        double dlu[3];
-        const double sc = dlam_of(u, du, dlu);
-        enters = dlu[so] > __dmul_rn(1e-12, sc);
+          if (ct.v[s] != ei && ct.v[s] != ej) so = s;
+        cscale = dlam_of(ct, cd, cdl);
+        enters = cdl[so] > __dmul_rn(1e-12, cscale);
       }
     }
     if (enters) {
+      carry = true;
       ti = nt;
       x0 = xe0;
       x1 = xe1;
