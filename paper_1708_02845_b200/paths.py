@@ -160,7 +160,7 @@ def trace_arrays(mesh, fields, targets, sources, field_of=None, settings: Settin
     buf = _workspace(t, npaths, cap, dm.device, "main")
     nat.call(entry, _byref(dm.struct), F.data_ptr(), tgt_d.data_ptr(),
              src_d.data_ptr(), nat.ptr(fo_d), npaths, step_cap, _byref(buf.struct), s)
-    counts = buf.count.cpu().numpy()
+    counts = buf.count[:npaths].cpu().numpy()
     over = np.flatnonzero(counts > cap)
     extra = None
     if over.size:
