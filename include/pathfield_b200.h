@@ -172,9 +172,13 @@ int pf_mask_compare_f64(const double *a, const double *b, int64_t k, double clam
 /* ---- K4: sparsify (divergence.py:194-240) ---------------------------------
  * keep = P >= cut (strict_positive == 0; cut = threshold / k computed by the
  * caller exactly as divergence.py:219) or P > 0 (threshold 0, :220).
- * pf_csr_count_f64 writes the per-row kept count; the caller scans it into
- * indptr (rows+1, int64, indptr[0] = 0).  pf_csr_fill_f64 then writes, in
- * scipy's order (row-major, ascending column):
+ * pf_csr_count_f64 writes the per-row kept count c_r; the caller scans the
+ * ROW-ALIGNED lengths c_r + (c_r & 1) into indptr (rows+1, int64, indptr[0]
+ * = 0): every row starts at an even offset, and a row with an odd count ends
+ * with one zero pad entry (data 0, log 0) that every kernel excludes — so a
+ * row's element order never depends on the row's position (a multi-GPU slab
+ * reduces each row exactly like the whole CSR).  pf_csr_fill_f64 then
+ * writes, in scipy's order (row-major, ascending column):
  *   indices (int32), data = kept P values, log_data = log(data) (:224-225),
  *   hs[r] = sum data*log_data (the split-form KL row term), and
  *   dropped[r] = max(0, 1 - rowsum) with rowsum in numpy reduceat order
@@ -223,13 +227,12 @@ int pf_csr_tv_f64(const int64_t *indptr, const int32_t *indices, const double *d
  *   settle; ops = |supp q|.  Needs logt (the target's dense log row).
  * kind PF_DIV_CHI2 / PF_DIV_HELLINGER / PF_DIV_POWER: the union form with
  *   weights clamped at `cut`; prow = the target's DENSE row, p_local its row in
- *   this slab's CSR; scratch >= 2k + 4 doubles + k bytes; ops = |union|.
- * Both settle the result. */
+ *   this slab's CSR; ops = |union|.  Both settle the result. */
 int pf_csr_generic_f64(const int64_t *indptr, const int32_t *indices, const double *data,
                        const double *log_data, int64_t rows, int64_t k, int kind, double param,
                        double cut, const double *prow, int64_t p_local, const double *logt,
-                       double *scratch, int64_t row0, const int64_t *queries, int64_t nq,
-                       double *out, int64_t *ops, pf_stream_t stream);
+                       int64_t row0, const int64_t *queries, int64_t nq, double *out,
+                       int64_t *ops, pf_stream_t stream);
 
 /* Elementwise log view: out[r*k + c] = log(max(P[r*ld + c], clamp)), the
  * reference's log_dense (divergence.py:226), materialised on request. */

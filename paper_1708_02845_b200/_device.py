@@ -232,10 +232,13 @@ class DeviceKernel:
 class DeviceCSR:
     """CSR arrays of one slab built on the device from the dense rows (K4).
 
-    Layout: indptr int64 (rows+1, slab-local, indptr[0] = 0), indices int32
-    (ascending per row), data / log_data FP64 (nnz), hs = sum v log v and
-    dropped (FP64 per row).  scipy's layout (int32 columns) so the CSR
-    algorithmic bytes are nnz*(8+4) + rows*(8+8+8).
+    Layout: indptr int64 (rows+1, slab-local) over ROW-ALIGNED rows — every
+    row starts at an even offset and a row with an odd entry count ends with
+    one zero pad entry (data 0, log 0) that the kernels exclude, so a row's
+    element order (and therefore its reduction) does not depend on where the
+    row sits; indices int32 (ascending per row), data / log_data FP64,
+    hs = sum v log v and dropped (FP64 per row), rownnz (int64, real counts).
+    The algorithmic bytes are those of scipy's layout: nnz*(8+4) + rows*24.
     """
 
     def __init__(self, dk: DeviceKernel, cut: float, strict_positive: bool):
@@ -243,15 +246,17 @@ class DeviceCSR:
         self.dk, self.cut, self.strict = dk, cut, strict_positive
         rows, dev_ = dk.rows, dk.device
         s = t.cuda.current_stream(dev_).cuda_stream
-        rownnz = t.empty(rows, dtype=t.int64, device=dev_)
+        self.rownnz = t.empty(rows, dtype=t.int64, device=dev_)
         nat.call("pf_csr_count_f64", dk.P.data_ptr(), dk.ld, rows, dk.k, cut,
-                 int(strict_positive), rownnz.data_ptr(), s)
+                 int(strict_positive), self.rownnz.data_ptr(), s)
         self.indptr = t.zeros(rows + 1, dtype=t.int64, device=dev_)
-        t.cumsum(rownnz, 0, out=self.indptr[1:])
-        self.nnz = int(self.indptr[-1].item())
-        self.indices = t.empty(max(self.nnz, 1), dtype=t.int32, device=dev_)
-        self.data = t.empty(max(self.nnz, 1), dtype=t.float64, device=dev_)
-        self.log_data = t.empty(max(self.nnz, 1), dtype=t.float64, device=dev_)
+        t.cumsum(self.rownnz + (self.rownnz & 1), 0, out=self.indptr[1:])
+        self.nnz_pad = int(self.indptr[-1].item())
+        self.nnz = int(self.rownnz.sum().item())
+        cap = max(self.nnz_pad, 1)
+        self.indices = t.empty(cap, dtype=t.int32, device=dev_)
+        self.data = t.empty(cap, dtype=t.float64, device=dev_)
+        self.log_data = t.empty(cap, dtype=t.float64, device=dev_)
         self.hs = t.empty(rows, dtype=t.float64, device=dev_)
         self.dropped = t.empty(rows, dtype=t.float64, device=dev_)
         nat.call("pf_csr_fill_f64", dk.P.data_ptr(), dk.ld, rows, dk.k, cut,
@@ -261,6 +266,22 @@ class DeviceCSR:
 
     def owns(self, row: int) -> bool:
         return self.dk.owns(row)
+
+    def real_mask(self):
+        """Boolean mask over the padded arrays selecting the real entries."""
+        t = torch()
+        keep = t.ones(max(self.nnz_pad, 1), dtype=t.bool, device=self.dk.device)
+        odd = (self.rownnz & 1).bool()
+        pads = (self.indptr[:-1] + self.rownnz)[odd]
+        keep[pads] = False
+        return keep[:self.nnz_pad]
+
+    def scipy_indptr(self):
+        """indptr of the unpadded (scipy) layout, on the device."""
+        t = torch()
+        ip = t.zeros(self.dk.rows + 1, dtype=t.int64, device=self.dk.device)
+        t.cumsum(self.rownnz, 0, out=ip[1:])
+        return ip
 
 
 _cache: dict[int, tuple[weakref.ref, DeviceKernel]] = {}

@@ -52,7 +52,7 @@ _SIGS = {
                       c_vp, c_vp, c_vp],
     "pf_log_clamped_f64": [c_vp, c_i64, c_i64, c_i64, c_dbl, c_vp, c_vp],
     "pf_csr_generic_f64": [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_int, c_dbl, c_dbl, c_vp,
-                           c_i64, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp],
+                           c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp],
     "pf_batch_prep_f64": [c_vp, c_i64, c_i64, c_i64, c_i64, c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp],
     "pf_mask_uniform_f64": [c_vp, c_i64, c_i64, c_i64, c_dbl, c_vp, c_vp, c_vp, c_vp],
     "pf_batched_kl_f64": [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_dbl,

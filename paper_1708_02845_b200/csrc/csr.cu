@@ -88,8 +88,28 @@ __global__ void __launch_bounds__(kCsrThreads) csr_fill_kernel(
       pos += __popc(ball);
     }
     const double h = warp_sum(acc);
-    if (lane == 0) hs[r] = h;
+    if (lane == 0) {
+      hs[r] = h;
+      if ((pos - indptr[r]) & 1) {  // odd row: one zero pad entry keeps the next row even
+        indices[pos] = pos > indptr[r] ? indices[pos - 1] : 0;
+        data[pos] = 0.0;
+        log_data[pos] = 0.0;
+      }
+    }
   }
+}
+
+// Row extent of the row-aligned device CSR: every row starts at an even offset
+// and a row with an odd number of entries ends with one zero pad entry (kept
+// entries are never 0), which is excluded here.  Element order inside a row is
+// therefore independent of where the row sits in the arrays, so a row slab of
+// the CSR (multi-GPU) reduces every row exactly as the whole CSR does.
+__device__ __forceinline__ void row_extent(const int64_t *__restrict__ indptr,
+                                           const double *__restrict__ data, int64_t r,
+                                           int64_t &lo, int64_t &hi) {
+  lo = indptr[r];
+  hi = indptr[r + 1];
+  if (hi > lo && data[hi - 1] == 0.0) --hi;
 }
 
 // numpy pairwise summation (numpy/_core/src/umath/loops_utils.h.src,
@@ -132,7 +152,8 @@ __global__ void csr_dropped_kernel(const int64_t *__restrict__ indptr,
                                    double *__restrict__ dropped) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows;
        r += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t lo = indptr[r], hi = indptr[r + 1];
+    int64_t lo, hi;
+    row_extent(indptr, data, r, lo, hi);
     double s = 0.0;
     if (hi - lo == 1) s = data[lo];
     else if (hi - lo > 1) s = data[lo] + np_pairwise_sum(data + lo + 1, hi - lo - 1);
@@ -189,7 +210,8 @@ __global__ void csr_target_prep_kernel(const int64_t *__restrict__ indptr,
                                        double *__restrict__ tscal) {
   for (int64_t i = threadIdx.x; i < k_pad; i += blockDim.x) vp[i] = 0.0;
   __syncthreads();
-  const int64_t lo = indptr[p], hi = indptr[p + 1];
+  int64_t lo, hi;
+  row_extent(indptr, data, p, lo, hi);
   for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) vp[indices[i]] = data[i];
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
@@ -235,12 +257,14 @@ __global__ void __launch_bounds__(kCsrThreads) csr_kl_kernel(
   const int64_t count = queries ? nq : rows;
   int64_t i = warp;
   int64_t r = i < count ? (queries ? queries[i] - row0 : i) : 0;
-  int64_t lo = i < count ? indptr[r] : 0, hi = i < count ? indptr[r + 1] : 0;
+  int64_t lo = 0, hi = 0;
+  if (i < count) row_extent(indptr, data, r, lo, hi);
   while (i < count) {
     // prefetch the next row's extent while this row streams
     const int64_t i2 = i + nwarps;
     const int64_t r2 = i2 < count ? (queries ? queries[i2] - row0 : i2) : 0;
-    const int64_t lo2 = i2 < count ? indptr[r2] : 0, hi2 = i2 < count ? indptr[r2 + 1] : 0;
+    int64_t lo2 = 0, hi2 = 0;
+    if (i2 < count) row_extent(indptr, data, r2, lo2, hi2);
     const double h = hs[r];
     double a0 = 0.0, a1 = 0.0;
     bool odd = false;
@@ -287,7 +311,8 @@ __global__ void __launch_bounds__(kCsrThreads) csr_kl_fixup_kernel(
       ball &= ball - 1;
       const int64_t i = warp + (i0 + src) * nwarps;
       const int64_t r = queries ? queries[i] - row0 : i;
-      const int64_t lo = indptr[r], hi = indptr[r + 1];
+      int64_t lo, hi;
+      row_extent(indptr, data, r, lo, hi);
       double a0 = 0.0, a1 = 0.0;
       int64_t e = lo + lane;
       for (; e + 32 < hi; e += 64) {
@@ -321,11 +346,13 @@ __global__ void __launch_bounds__(kCsrThreads) csr_tv_kernel(
   const int64_t nnz_p = static_cast<int64_t>(tscal[2]);
   int64_t i = warp;
   int64_t r = i < count ? (queries ? queries[i] - row0 : i) : 0;
-  int64_t lo = i < count ? indptr[r] : 0, hi = i < count ? indptr[r + 1] : 0;
+  int64_t lo = 0, hi = 0;
+  if (i < count) row_extent(indptr, data, r, lo, hi);
   while (i < count) {
     const int64_t i2 = i + nwarps;
     const int64_t r2 = i2 < count ? (queries ? queries[i2] - row0 : i2) : 0;
-    const int64_t lo2 = i2 < count ? indptr[r2] : 0, hi2 = i2 < count ? indptr[r2 + 1] : 0;
+    int64_t lo2 = 0, hi2 = 0;
+    if (i2 < count) row_extent(indptr, data, r2, lo2, hi2);
     const double d_q = dropped[r];
     // one accumulator per lane in csr_row_visit order (S_p uses the same order,
     // so q == p cancels exactly)
@@ -356,12 +383,11 @@ __global__ void __launch_bounds__(kCsrThreads) csr_tv_kernel(
 // ---------------------------------------------------- other generators --
 // divergence.py:275-299 for the remaining builtins.
 //  alpha:   sum_{supp q} v (1 - exp(expo (logPt - log v))), times scale; settle.
-//  chi2 / hellinger / power-p: over supp(p) U supp(q) with weights clamped at
-//  the row cut, vq = v (or cut off-support), vp = max(P[p, j], cut):
-//      sum_{supp q} vq f(vp/vq) + sum_{supp p \ supp q} cut f(vp/cut)
-//  restated as one pass over supp(q) with g_j = cut f(vp_j/cut) [j in supp p]
-//  precomputed per target:  sum_{supp q} (vq f(vp/vq) - g_j) + C_p,
-//  C_p = sum_{supp p} g_j reduced in csr_row_visit order (so q = p is exactly 0).
+//  chi2 / hellinger / power-p: the union form over supp(p) U supp(q) with
+//  weights clamped at the row cut, vp = max(P[p, j], cut), vq = v (cut
+//  off-support):  sum_{supp q} vq f(vp/vq) + sum_{supp p \ supp q} cut f(vp/cut),
+//  the second sum by binary search of each supp(p) index in the sorted supp(q)
+//  (no restated cancellation: these generators reach 1e18-scale terms).
 template <int KIND>
 __device__ __forceinline__ double gen_f(double x, double param) {
   if (KIND == PF_DIV_CHI2) return __dsub_rn(__dmul_rn(x, x), 1.0);
@@ -374,68 +400,49 @@ __device__ __forceinline__ double gen_f(double x, double param) {
 }
 
 template <int KIND>
-__global__ void csr_generic_prep_kernel(const double *__restrict__ prow, int64_t k, double cut,
-                                        double param, const int64_t *__restrict__ indptr,
-                                        const int32_t *__restrict__ indices,
-                                        const double *__restrict__ data, int64_t p,
-                                        double *__restrict__ vpc, double *__restrict__ g,
-                                        uint8_t *__restrict__ mask, double *__restrict__ tscal) {
-  for (int64_t j = threadIdx.x; j < k; j += blockDim.x) {
-    vpc[j] = fmax(prow[j], cut);
-    g[j] = 0.0;
-    mask[j] = 0;
-  }
-  __syncthreads();
-  const int64_t lo = indptr[p], hi = indptr[p + 1];
-  for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) {
-    const int32_t j = indices[e];
-    g[j] = __dmul_rn(cut, gen_f<KIND>(__ddiv_rn(vpc[j], cut), param));
-    mask[j] = 1;
-  }
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    double a = 0.0;
-    csr_row_visit(data, indices, lo, hi, lane, [&](double, int32_t c) { a += g[c]; });
-    a = warp_sum(a);
-    if (lane == 0) {
-      tscal[0] = a;
-      tscal[1] = 0.0;
-      tscal[2] = static_cast<double>(hi - lo);
-      tscal[3] = 0.0;
-    }
-  }
-}
-
-template <int KIND>
 __global__ void __launch_bounds__(kCsrThreads) csr_generic_kernel(
     const int64_t *__restrict__ indptr, const int32_t *__restrict__ indices,
-    const double *__restrict__ data, int64_t rows, const double *__restrict__ vpc,
-    const double *__restrict__ g, const uint8_t *__restrict__ mask,
-    const double *__restrict__ tscal, double param, int64_t row0,
+    const double *__restrict__ data, int64_t rows, const double *__restrict__ prow,
+    int64_t p_local, double cut, double param, int64_t row0,
     const int64_t *__restrict__ queries, int64_t nq, double *__restrict__ out,
     int64_t *__restrict__ ops) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t count = queries ? nq : rows;
-  const double C_p = tscal[0];
-  const int64_t nnz_p = static_cast<int64_t>(tscal[2]);
+  int64_t plo, phi;
+  row_extent(indptr, data, p_local, plo, phi);
   for (int64_t i = warp; i < count; i += nwarps) {
     const int64_t r = queries ? queries[i] - row0 : i;
-    const int64_t lo = indptr[r], hi = indptr[r + 1];
+    int64_t lo, hi;
+    row_extent(indptr, data, r, lo, hi);
     double a = 0.0;
+    for (int64_t e = lo + lane; e < hi; e += 32) {  // supp(q)
+      const double v = data[e];
+      const double vp = fmax(__ldg(prow + indices[e]), cut);
+      a += __dmul_rn(v, gen_f<KIND>(__ddiv_rn(vp, v), param));
+    }
     int inter = 0;
-    csr_row_visit(data, indices, lo, hi, lane, [&](double v, int32_t c) {
-      a += __dmul_rn(v, gen_f<KIND>(__ddiv_rn(__ldg(vpc + c), v), param)) - __ldg(g + c);
-      inter += __ldg(mask + c);
-    });
-    const double val = settle(warp_sum(a) + C_p);
+    for (int64_t e = plo + lane; e < phi; e += 32) {  // supp(p) \ supp(q)
+      const int32_t j = indices[e];
+      int64_t L = lo, R = hi;  // first index >= j in the sorted supp(q)
+      while (L < R) {
+        const int64_t M = (L + R) >> 1;
+        if (indices[M] < j) L = M + 1; else R = M;
+      }
+      if (L < hi && indices[L] == j) {
+        ++inter;
+      } else {
+        const double vp = fmax(__ldg(prow + j), cut);
+        a += __dmul_rn(cut, gen_f<KIND>(__ddiv_rn(vp, cut), param));
+      }
+    }
+    const double val = settle(warp_sum(a));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) inter += __shfl_xor_sync(0xffffffffu, inter, o);
     if (lane == 0) {
       out[i] = val;
-      if (ops) ops[i] = (hi - lo) + nnz_p - inter;
+      if (ops) ops[i] = (hi - lo) + (phi - plo) - inter;  // |union|, divergence.py:289
     }
   }
 }
@@ -453,7 +460,8 @@ __global__ void __launch_bounds__(kCsrThreads) csr_alpha_kernel(
   const double scale = 4.0 / (1.0 - alpha * alpha), expo = (1.0 + alpha) / 2.0;
   for (int64_t i = warp; i < count; i += nwarps) {
     const int64_t r = queries ? queries[i] - row0 : i;
-    const int64_t lo = indptr[r], hi = indptr[r + 1];
+    int64_t lo, hi;
+    row_extent(indptr, data, r, lo, hi);
     double a = 0.0;
     for (int64_t e = lo + lane; e < hi; e += 32) {
       const double rp = exp(__dmul_rn(expo, __ldg(logt + indices[e]) - log_data[e]));
@@ -602,8 +610,8 @@ int pf_csr_tv_f64(const int64_t *indptr, const int32_t *indices, const double *d
 int pf_csr_generic_f64(const int64_t *indptr, const int32_t *indices, const double *data,
                        const double *log_data, int64_t rows, int64_t k, int kind, double param,
                        double cut, const double *prow, int64_t p_local, const double *logt,
-                       double *scratch, int64_t row0, const int64_t *queries, int64_t nq,
-                       double *out, int64_t *ops, pf_stream_t stream) {
+                       int64_t row0, const int64_t *queries, int64_t nq, double *out,
+                       int64_t *ops, pf_stream_t stream) {
   if (!indptr || !out || rows < 0 || k <= 0) return fail(PF_E_ARG, "csr_generic: bad args");
   const int64_t count = queries ? nq : rows;
   if (count <= 0) return 0;
@@ -614,15 +622,11 @@ int pf_csr_generic_f64(const int64_t *indptr, const int32_t *indices, const doub
         indptr, indices, data, log_data, rows, logt, param, row0, queries, nq, out, ops);
     return check_launch("csr_alpha");
   }
-  if (!prow || !scratch || p_local < 0) return fail(PF_E_ARG, "csr_generic: target row");
-  double *vpc = scratch, *gg = scratch + k, *tscal = scratch + 2 * k;
-  uint8_t *mask = reinterpret_cast<uint8_t *>(scratch + 2 * k + 4);
-#define PF_CSR_GEN(KIND)                                                                      \
-  case KIND:                                                                                  \
-    csr_generic_prep_kernel<KIND><<<1, 512, 0, as_stream(stream)>>>(                          \
-        prow, k, cut, param, indptr, indices, data, p_local, vpc, gg, mask, tscal);           \
-    csr_generic_kernel<KIND><<<g, kCsrThreads, 0, as_stream(stream)>>>(                       \
-        indptr, indices, data, rows, vpc, gg, mask, tscal, param, row0, queries, nq, out, ops); \
+  if (!prow || p_local < 0 || p_local >= rows) return fail(PF_E_ARG, "csr_generic: target row");
+#define PF_CSR_GEN(KIND)                                                                  \
+  case KIND:                                                                              \
+    csr_generic_kernel<KIND><<<g, kCsrThreads, 0, as_stream(stream)>>>(                   \
+        indptr, indices, data, rows, prow, p_local, cut, param, row0, queries, nq, out, ops); \
     break;
   switch (kind) {
     PF_CSR_GEN(PF_DIV_CHI2)

@@ -477,10 +477,11 @@ def sparsify(pk: PoissonKernel, threshold: float | None = None) -> PoissonKernel
     s = t.cuda.current_stream(dk.device)
     nnz = dc.nnz
     idx_dtype = np.int32 if nnz < 2 ** 31 else np.int64
-    indptr = _to_host(t, dc.indptr, s).astype(idx_dtype)
-    indices = _to_host(t, dc.indices[:nnz], s).astype(idx_dtype, copy=False)
-    data = _to_host(t, dc.data[:nnz], s)
-    logs = _to_host(t, dc.log_data[:nnz], s)
+    keep = dc.real_mask()  # drop the row-alignment pads of the device layout
+    indptr = _to_host(t, dc.scipy_indptr(), s).astype(idx_dtype)
+    indices = _to_host(t, dc.indices[:dc.nnz_pad][keep], s).astype(idx_dtype, copy=False)
+    data = _to_host(t, dc.data[:dc.nnz_pad][keep], s)
+    logs = _to_host(t, dc.log_data[:dc.nnz_pad][keep], s)
     dropped = _to_host(t, dc.dropped, s)
     interior = np.ones(n, dtype=bool)
     interior[np.asarray(pk.boundary, dtype=np.int64)] = False
@@ -537,7 +538,7 @@ def _sparse_launch(pk, fd, p: int, queries=None, want_ops=False):
         else:
             nat.call("pf_csr_generic_f64", dc.indptr.data_ptr(), dc.indices.data_ptr(),
                      dc.data.data_ptr(), dc.log_data.data_ptr(), dk.rows, dk.k, kind, param,
-                     0.0, 0, -1, st.logt, 0, dk.row0, qptr, count, out.data_ptr(),
+                     0.0, 0, -1, st.logt, dk.row0, qptr, count, out.data_ptr(),
                      nat.ptr(ops), s.cuda_stream)
     elif fd.name == "tv":
         st = t.empty(k_pad + 4, dtype=t.float64, device=dk.device)
@@ -552,10 +553,10 @@ def _sparse_launch(pk, fd, p: int, queries=None, want_ops=False):
         # (divergence.py:296-299; the clamp when the cut is 0)
         row_cut = getattr(pk, "row_cut", None)
         cut = float(row_cut) if row_cut and row_cut > 0 else float(fd.clamp)
-        st = t.empty(2 * dk.k + 4 + (dk.k + 7) // 8, dtype=t.float64, device=dk.device)
+        st = None
         nat.call("pf_csr_generic_f64", dc.indptr.data_ptr(), dc.indices.data_ptr(),
                  dc.data.data_ptr(), dc.log_data.data_ptr(), dk.rows, dk.k, kind, param, cut,
-                 dk.row_ptr(p), p - dk.row0, 0, st.data_ptr(), dk.row0, qptr, count,
+                 dk.row_ptr(p), p - dk.row0, 0, dk.row0, qptr, count,
                  out.data_ptr(), nat.ptr(ops), s.cuda_stream)
     return out, ops, count, s, st
 

@@ -146,10 +146,12 @@ def main(name: str):
         torch.cuda.synchronize()
         res["sparsify_gpu_s"] = time.perf_counter() - t0
         indptr = dc.indptr.cpu().numpy()
+        rownnz = dc.rownnz.cpu().numpy()
         dropped = dc.dropped.cpu().numpy()
         ok_pat = ok_drop = True
         for r in rows[:500]:
-            a, b = int(indptr[r]), int(indptr[r + 1])
+            a = int(indptr[r])
+            b = a + int(rownnz[r])  # row-aligned device layout: exclude the pad
             idx = dc.indices[a:b].cpu().numpy()
             dat = dc.data[a:b].cpu().numpy()
             ridx, rval, rdrop = O._kept_row(dense, cut, False, int(r))
