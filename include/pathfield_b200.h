@@ -174,10 +174,11 @@ int pf_mask_compare_f64(const double *a, const double *b, int64_t k, double clam
  * caller exactly as divergence.py:219) or P > 0 (threshold 0, :220).
  * pf_csr_count_f64 writes the per-row kept count c_r; the caller scans the
  * ROW-ALIGNED lengths c_r + (c_r & 1) into indptr (rows+1, int64, indptr[0]
- * = 0): every row starts at an even offset, and a row with an odd count ends
- * with one zero pad entry (data 0, log 0) that every kernel excludes — so a
- * row's element order never depends on the row's position (a multi-GPU slab
- * reduces each row exactly like the whole CSR).  pf_csr_fill_f64 then
+ * = 0) and sets bit 0 of indptr[r+1] when c_r is odd: every row starts at an
+ * even offset (indptr[r] & ~1), and a row with an odd count ends with one zero
+ * pad entry (data 0, log 0) that every kernel excludes — so a row's element
+ * order never depends on the row's position (a multi-GPU slab reduces each
+ * row exactly like the whole CSR).  pf_csr_fill_f64 then
  * writes, in scipy's order (row-major, ascending column):
  *   indices (int32), data = kept P values, log_data = log(data) (:224-225),
  *   hs[r] = sum data*log_data (the split-form KL row term), and

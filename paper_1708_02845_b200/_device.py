@@ -233,8 +233,9 @@ class DeviceCSR:
     """CSR arrays of one slab built on the device from the dense rows (K4).
 
     Layout: indptr int64 (rows+1, slab-local) over ROW-ALIGNED rows — every
-    row starts at an even offset and a row with an odd entry count ends with
-    one zero pad entry (data 0, log 0) that the kernels exclude, so a row's
+    row starts at an even offset (bit 0 of indptr[r+1] flags a pad) and a row
+    with an odd entry count ends with one zero pad entry (data 0, log 0) that
+    the kernels exclude, so a row's
     element order (and therefore its reduction) does not depend on where the
     row sits; indices int32 (ascending per row), data / log_data FP64,
     hs = sum v log v and dropped (FP64 per row), rownnz (int64, real counts).
@@ -252,6 +253,7 @@ class DeviceCSR:
         self.indptr = t.zeros(rows + 1, dtype=t.int64, device=dev_)
         t.cumsum(self.rownnz + (self.rownnz & 1), 0, out=self.indptr[1:])
         self.nnz_pad = int(self.indptr[-1].item())
+        self.indptr[1:] |= self.rownnz & 1  # pad flag in bit 0 of the row's end offset
         self.nnz = int(self.rownnz.sum().item())
         cap = max(self.nnz_pad, 1)
         self.indices = t.empty(cap, dtype=t.int32, device=dev_)
@@ -272,7 +274,7 @@ class DeviceCSR:
         t = torch()
         keep = t.ones(max(self.nnz_pad, 1), dtype=t.bool, device=self.dk.device)
         odd = (self.rownnz & 1).bool()
-        pads = (self.indptr[:-1] + self.rownnz)[odd]
+        pads = ((self.indptr[:-1] & ~1) + self.rownnz)[odd]
         keep[pads] = False
         return keep[:self.nnz_pad]
 

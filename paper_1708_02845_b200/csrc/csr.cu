@@ -70,7 +70,8 @@ __global__ void __launch_bounds__(kCsrThreads) csr_fill_kernel(
   const unsigned lower = (1u << lane) - 1u;
   for (int64_t r = warp; r < rows; r += nwarps) {
     const double *row = P + r * ld;
-    int64_t pos = indptr[r];
+    const int64_t row_lo = indptr[r] & ~1LL;
+    int64_t pos = row_lo;
     double acc = 0.0;
     for (int64_t c0 = 0; c0 < k; c0 += 32) {
       const int64_t c = c0 + lane;
@@ -90,8 +91,8 @@ __global__ void __launch_bounds__(kCsrThreads) csr_fill_kernel(
     const double h = warp_sum(acc);
     if (lane == 0) {
       hs[r] = h;
-      if ((pos - indptr[r]) & 1) {  // odd row: one zero pad entry keeps the next row even
-        indices[pos] = pos > indptr[r] ? indices[pos - 1] : 0;
+      if ((pos - row_lo) & 1) {  // odd row: one zero pad entry keeps the next row even
+        indices[pos] = pos > row_lo ? indices[pos - 1] : 0;
         data[pos] = 0.0;
         log_data[pos] = 0.0;
       }
@@ -104,12 +105,16 @@ __global__ void __launch_bounds__(kCsrThreads) csr_fill_kernel(
 // entries are never 0), which is excluded here.  Element order inside a row is
 // therefore independent of where the row sits in the arrays, so a row slab of
 // the CSR (multi-GPU) reduces every row exactly as the whole CSR does.
+// The pad is flagged in bit 0 of the row's END offset (offsets are even), so
+// the extent needs no dependent load: lo = ip[r] & ~1, hi = (ip[r+1] & ~1) -
+// (ip[r+1] & 1).
 __device__ __forceinline__ void row_extent(const int64_t *__restrict__ indptr,
                                            const double *__restrict__ data, int64_t r,
                                            int64_t &lo, int64_t &hi) {
-  lo = indptr[r];
-  hi = indptr[r + 1];
-  if (hi > lo && data[hi - 1] == 0.0) --hi;
+  (void)data;
+  const int64_t a = indptr[r], b = indptr[r + 1];
+  lo = a & ~1LL;
+  hi = (b & ~1LL) - (b & 1);
 }
 
 // numpy pairwise summation (numpy/_core/src/umath/loops_utils.h.src,

@@ -150,7 +150,7 @@ def main(name: str):
         dropped = dc.dropped.cpu().numpy()
         ok_pat = ok_drop = True
         for r in rows[:500]:
-            a = int(indptr[r])
+            a = int(indptr[r]) & ~1
             b = a + int(rownnz[r])  # row-aligned device layout: exclude the pad
             idx = dc.indices[a:b].cpu().numpy()
             dat = dc.data[a:b].cpu().numpy()
