@@ -4,14 +4,19 @@ Mirror of ``pathfield/divergence.py`` (same names, signatures, argument
 meaning, return types and exceptions); every evaluation runs in the sm_100a
 kernels of ``libpathfield_b200.so``:
 
-=====================  =============================================  ==========
-function               reference                                      kernels
-=====================  =============================================  ==========
-builtin_f/FDivergence  divergence.py:42-104                           (host)
-dv_pair                divergence.py:125-134                          K0 + at
-dv_at                  divergence.py:137-151                          K0 + at
-dv_field               divergence.py:154-187                          K0 + K2/K3
-=====================  =============================================  ==========
+========================  ==========================================  ==================
+function                  reference                                   kernels
+========================  ==========================================  ==================
+builtin_f/FDivergence     divergence.py:42-104                        (host)
+dv_pair                   divergence.py:125-134                       K0 + dense_at
+dv_at                     divergence.py:137-151                       K0 + dense_at
+dv_field                  divergence.py:154-187                       K0 + K2/K3/generic
+sparsify                  divergence.py:194-240                       K4
+dv_pair_sparse(_stats)    divergence.py:255-305                       K5/K6/csr_generic
+dv_field_sparse           [dv_pair_sparse for q] (no reference API)   K5/K6/csr_generic
+dv_field_batch            [dv_field for t] (no reference API)         K7
+dv_field_f32              dv_field, FP32 storage (1e-5 tolerance)     dense32
+========================  ==========================================  ==================
 
 The divergence between target p and query q is
 ``DV(q, p) = sum_b max(Q,c) * f(max(P,c)/max(Q,c))`` with the generator's
@@ -605,9 +610,8 @@ def dv_field_sparse_device(pk: PoissonKernel, fd: FDivergence, p: int):
 
 
 __all__ = [
-    "dv_field_f32", "dv_field_f32_device", "F32_GUARD_TAU", "dv_field_batch", "dv_field_batch_device",
-    "sparsify", "dv_pair_sparse", "dv_pair_sparse_stats", "dv_field_sparse",
-    "dv_field_sparse_device", "LogDenseView",
     "FDivergence", "builtin_f", "dv_pair", "dv_at", "dv_field", "dv_field_device",
-    "KL_GUARD_TAU",
+    "sparsify", "dv_pair_sparse", "dv_pair_sparse_stats", "dv_field_sparse",
+    "dv_field_sparse_device", "dv_field_batch", "dv_field_batch_device", "dv_field_f32",
+    "dv_field_f32_device", "LogDenseView", "KL_GUARD_TAU", "F32_GUARD_TAU",
 ]
