@@ -202,6 +202,58 @@ def main(name: str):
                    "locations": steps, "gpu_batch_s": gpu_s, "oracle_cpu_s": cpu_s})
     res["tracer"] = tr
     _progress(res, "tracer", part)
+
+    # C5 pipeline on the real kernel: T targets as one batched KL contraction
+    # (K7), spot-checked against single-target dv_field, then many paths traced
+    # on the batched fields (source i -> target i % T) in one launch.
+    import torch as _t
+    T = int(os.environ.get("PF_BATCH_T", "1024" if n > 500_000 else "256"))
+    npaths = int(os.environ.get("PF_PATHS", "10000" if n > 500_000 else "2000"))
+    bt = rng.choice(m.interior_vertices, T, replace=False)
+    _t.cuda.synchronize()
+    t0 = time.perf_counter()
+    out, bflags = pf.divergence.dv_field_batch_device(pk, pf.builtin_f("kl"), bt)
+    _t.cuda.synchronize()
+    batch_s = time.perf_counter() - t0
+    worst = 0.0
+    for j in range(0, T, max(1, T // 8)):
+        single = pf.dv_field(pk, pf.builtin_f("kl"), int(bt[j])).values
+        mx, _ = relerr(out[:, j].cpu().numpy(), single)
+        worst = max(worst, mx)
+    fields = out.t().contiguous()  # (T, n): one field per row for the tracer
+    del out
+    srcs = rng.choice(m.interior_vertices, npaths)
+    fo = np.arange(npaths) % T
+    srcs = np.where(srcs == bt[fo], (srcs + 1) % n, srcs)
+    from paper_1708_02845_b200 import paths as PP
+    PP.trace_arrays(tm, fields, bt, srcs[:256], fo[:256])  # warm-up
+    _t.cuda.synchronize()
+    t0 = time.perf_counter()
+    buf, counts, over, extra = PP.trace_arrays(tm, fields, bt, srcs, fo)
+    _t.cuda.synchronize()
+    trace_s = time.perf_counter() - t0
+    status = buf.status[:npaths].cpu().numpy()
+    # bitwise spot check of a few batched paths against the oracle tracer
+    spot = 0
+    fh = None
+    for i in range(0, npaths, max(1, npaths // 10)):
+        if fh is None or fh[0] != fo[i]:
+            fh = (fo[i], fields[fo[i]].cpu().numpy())
+        o = TR.triangle_descent(m.vertices, m.triangles, m.areas, m.bbox_diagonal, fh[1],
+                                int(bt[fo[i]]), int(srcs[i]), topo=topo)
+        c = int(counts[i])
+        a = i * buf.cap
+        pts = np.column_stack([buf.x[a:a + c].cpu().numpy(), buf.y[a:a + c].cpu().numpy()])
+        spot += int(c == len(o["locations"]) and np.array_equal(pts, o["points"]))
+    res["c5_pipeline"] = {"T": T, "batch_kl_s": batch_s,
+                          "batch_vs_single_max_rel_err": worst,
+                          "clamped_flags": int(np.sum(bflags)),
+                          "paths": npaths, "trace_s": trace_s,
+                          "reached": int((status == 0).sum()),
+                          "stuck": int((status == 1).sum()),
+                          "mean_locations": float(counts.mean()),
+                          "spot_bitwise": f"{spot}/{len(range(0, npaths, max(1, npaths // 10)))}"}
+    _progress(res, "c5 pipeline", part)
     print(json.dumps(res))
 
 
