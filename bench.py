@@ -367,7 +367,10 @@ def extra_c4_and_c5(t, nat, dev, pf, device, steps, peak):
           "kl": _roof(rows * (8 * k + 16) + 8 * k, kl_ms, peak),
           "tv": _roof(rows * (8 * k + 8) + 8 * k, tv_ms, peak)}
     del st
-    # ---- C5: 1024 targets, one FP64 contraction + fused epilogue (K7)
+    # ---- C5: 1024 targets, KL as one contraction + fused epilogue (K7).  Product
+    # path: exact-integer emulation of the FP64 GEMM on the int8 tensor pipe
+    # (tcgen05, batched_i8.cu); the FP64 DMMA GEMM is timed beside it.
+    import ctypes
     T = 1024
     rng = np.random.default_rng(0)
     targets = rng.choice(rows, T, replace=False)
@@ -380,44 +383,93 @@ def extra_c4_and_c5(t, nat, dev, pf, device, steps, peak):
     out = t.empty((rows, T), dtype=t.float64, device=device)
     cnt = t.zeros(1, dtype=t.int32, device=device)
     s = t.cuda.current_stream(device)
-    e0, e1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
+    e0, e1, e2 = (t.cuda.Event(enable_timing=True) for _ in range(3))
+    tau = pf.divergence.KL_GUARD_TAU
+    e0.record(s)
+    A, ea, ldk = dk.slices(1e-300)          # once per P (like H)
+    e1.record(s)
+    t.cuda.synchronize()
+    slice_ms = e0.elapsed_time(e1)
+    B = t.empty((7, T, ldk), dtype=t.uint8, device=device)
+    eb = t.empty(T, dtype=t.int32, device=device)
+    bad = t.zeros(1, dtype=t.int32, device=device)
+    gemm_ms = [0.0]
 
-    def batch():
+    def batch_i8(timed=False):
+        nat.call("pf_batch_prep_f64", Pt.data_ptr(), Pt.stride(0), T, k, ldl, 1e-300, 0,
+                 L.data_ptr(), Tc.data_ptr(), 0, s.cuda_stream)
+        nat.call("pf_slice_targets_u8", L.data_ptr(), ldl, T, k, ldk, B.data_ptr(), eb.data_ptr(),
+                 bad.data_ptr(), s.cuda_stream)
+        if timed:
+            e1.record(s)
+        nat.call("pf_batched_kl_i8", A.data_ptr(), ea.data_ptr(), rows, B.data_ptr(),
+                 eb.data_ptr(), T, k, ldk, H.data_ptr(), tg.data_ptr(), tau, 0, out.data_ptr(),
+                 out.stride(0), s.cuda_stream)
+        if timed:
+            e2.record(s)
+        nat.call("pf_batched_kl_fixup_f64", dk.P.data_ptr(), dk.ld, rows, k, Tc.data_ptr(), ldl,
+                 T, 1e-300, out.data_ptr(), out.stride(0), cnt.data_ptr(), s.cuda_stream)
+
+    def batch_f64():
         nat.call("pf_batch_prep_f64", Pt.data_ptr(), Pt.stride(0), T, k, ldl, 1e-300, 0,
                  L.data_ptr(), Tc.data_ptr(), 0, s.cuda_stream)
         nat.call("pf_batched_kl_f64", dk.P.data_ptr(), dk.ld, rows, k, H.data_ptr(), L.data_ptr(),
-                 Tc.data_ptr(), ldl, T, tg.data_ptr(), 1e-300, pf.divergence.KL_GUARD_TAU, 0,
+                 Tc.data_ptr(), ldl, T, tg.data_ptr(), 1e-300, tau, 0,
                  out.data_ptr(), out.stride(0), cnt.data_ptr(), s.cuda_stream)
 
-    batch()
+    def timed(fn, reps):
+        fn()
+        t.cuda.synchronize()
+        st, en = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
+        st.record(s)
+        for _ in range(reps):
+            fn()
+        en.record(s)
+        t.cuda.synchronize()
+        return st.elapsed_time(en) / reps
+
+    reps = 3
+    ms = timed(batch_i8, reps)
+    batch_i8(True)
     t.cuda.synchronize()
-    reps = 2
-    e0.record(s)
-    for _ in range(reps):
-        batch()
-    e1.record(s)
-    t.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / reps
+    gemm_only = e1.elapsed_time(e2)
+    guarded = int(cnt.item())
+    ms64 = timed(batch_f64, 1)
     flops = 2.0 * rows * k * T
-    # sustained DFMA rate of this GPU (diagnostic kernel) as the FP64 roofline
-    import ctypes
+    # measured ceilings of this GPU: sustained DFMA, and the int8 tensor pipe
     fl = ctypes.c_int64(0)
-    probe = t.empty(1, dtype=t.float64, device=device)
-    nat.call("pf_probe_dfma_f64", 1 << 14, ctypes.byref(fl), probe.data_ptr(), s.cuda_stream)
-    t.cuda.synchronize()
-    e0.record(s)
-    nat.call("pf_probe_dfma_f64", 1 << 16, ctypes.byref(fl), probe.data_ptr(), s.cuda_stream)
-    e1.record(s)
-    t.cuda.synchronize()
-    peak_tf = fl.value / (e0.elapsed_time(e1) / 1e3) / 1e12
-    ach = flops / (ms / 1e3) / 1e12
-    c5 = {"workload": "C5 shape: 1,000,386 x 4,102 P, T = 1024 targets, KL as one FP64 GEMM "
-                      "+ fused epilogue (K7), synthetic, 1 GPU",
+    probe = t.empty(2, dtype=t.float64, device=device)
+
+    def probe_rate(name, iters):
+        nat.call(name, iters // 4, ctypes.byref(fl), probe.data_ptr(), s.cuda_stream)
+        t.cuda.synchronize()
+        e0.record(s)
+        nat.call(name, iters, ctypes.byref(fl), probe.data_ptr(), s.cuda_stream)
+        e1.record(s)
+        t.cuda.synchronize()
+        return fl.value / (e0.elapsed_time(e1) / 1e3) / 1e12
+
+    dfma_tf = probe_rate("pf_probe_dfma_f64", 1 << 16)
+    i8_tops = probe_rate("pf_probe_umma_i8", 1 << 14)
+    int_ops = 34 * flops
+    ach = int_ops / (gemm_only / 1e3) / 1e12
+    c5 = {"workload": "C5 shape: 1,000,386 x 4,102 P, T = 1024 targets, KL as one contraction "
+                      "+ fused epilogue (K7 on the int8 tensor pipe: 34 exact byte-pair GEMMs "
+                      "emulating the FP64 GEMM), synthetic, 1 GPU",
           "evals_per_s": rows * T / (ms / 1e3), "ms_per_batch": ms,
-          "guarded_pairs": int(cnt.item()) // reps if reps else 0,
-          "roofline": {"bound": "fp64", "achieved": ach, "peak": peak_tf, "unit": "TFLOP/s",
-                       "frac": ach / peak_tf,
-                       "peak_kind": "measured: pf_probe_dfma_f64 (8 DFMA chains/thread, all SMs)"}}
+          "gemm_ms": gemm_only, "guarded_pairs": guarded,
+          "fp64_equivalent_tflops": flops / (ms / 1e3) / 1e12,
+          "slice_rows_ms_once_per_P": slice_ms,
+          "roofline": {"bound": "tensor", "achieved": ach, "peak": i8_tops, "unit": "TOPS (int8)",
+                       "frac": ach / i8_tops,
+                       "algorithmic_ops_per_launch": int_ops,
+                       "peak_kind": "measured: pf_probe_umma_i8 (M128 N256 K32 u8 tcgen05.mma "
+                                    "back to back from shared memory, all SMs)"},
+          "fp64_dmma_path": {"ms_per_batch": ms64, "evals_per_s": rows * T / (ms64 / 1e3),
+                             "achieved_tflops": flops / (ms64 / 1e3) / 1e12,
+                             "dfma_peak_tflops": dfma_tf,
+                             "frac": flops / (ms64 / 1e3) / 1e12 / dfma_tf}}
+    del A, B
     del out, L, Tc, Pt, dk, P
     t.cuda.empty_cache()
     return c4, c5

@@ -264,6 +264,41 @@ int pf_batched_kl_f64(const double *P, int64_t ld, int64_t rows, int64_t k, cons
                       const int64_t *targets, double clamp, double tau, int64_t row0,
                       double *out, int64_t ldo, uint32_t *guarded, pf_stream_t stream);
 
+/* pf_batched_kl_fixup_f64: the guarded-pair pass of pf_batched_kl_f64 on its
+ * own: every out entry holding the guard sentinel is re-evaluated in the
+ * reference's per-element form sum c(Q) (-log(c(Pt)/c(Q))) (divergence.py:180)
+ * and settled; the count is added to *guarded if non-NULL. */
+int pf_batched_kl_fixup_f64(const double *P, int64_t ld, int64_t rows, int64_t k,
+                            const double *Tc, int64_t ldl, int64_t T, double clamp, double *out,
+                            int64_t ldo, uint32_t *guarded, pf_stream_t stream);
+
+/* ---- K7 on the int8 tensor pipe (batched_i8.cu) ----------------------------
+ * The same contraction as pf_batched_kl_f64, S = c(P) . (-L)^T, evaluated as
+ * an exact-integer emulation of the FP64 GEMM: both operands are non-negative
+ * 56-bit fixed-point numbers against a power-of-two scale per row / target,
+ * cut into 7 byte planes; the 34 byte-pair GEMMs of levels 2..9 run on
+ * tcgen05.mma kind::i8 (u8 x u8 -> s32 in TMEM) and are combined in FP64.
+ * pf_slice_rows_u8: slices [7][rows][ldk] and exps[rows] of max(P, clamp)
+ *   (target independent, cached per P like H); ldk % 64 == 0, pad zero.
+ * pf_slice_targets_u8: slices [7][T][ldk] and exps[T] of -L (L from
+ *   pf_batch_prep_f64); bad[0] |= 1 if some -L < 0 (then use the FP64 path).
+ * pf_batched_kl_i8: out[q*ldo + t] = H[q] + S[q,t] with the K7 epilogue
+ *   (guard sentinel, settle, zero at the target); k <= 4717.  Follow with
+ *   pf_batched_kl_fixup_f64 for the guarded pairs. */
+int pf_slice_rows_u8(const double *P, int64_t ld, int64_t rows, int64_t k, double clamp,
+                     int64_t ldk, uint8_t *slices, int32_t *exps, pf_stream_t stream);
+int pf_slice_targets_u8(const double *L, int64_t ldl, int64_t T, int64_t k, int64_t ldk,
+                        uint8_t *slices, int32_t *exps, uint32_t *bad, pf_stream_t stream);
+int pf_batched_kl_i8(const uint8_t *A, const int32_t *ea, int64_t rows, const uint8_t *B,
+                     const int32_t *eb, int64_t T, int64_t k, int64_t ldk, const double *H,
+                     const int64_t *targets, double tau, int64_t row0, double *out, int64_t ldo,
+                     pf_stream_t stream);
+
+/* Diagnostic: back-to-back M128 N256 K32 u8 tcgen05.mma on shared-memory
+ * operands, one CTA per SM (*ops_host = integer ops issued): the int8 tensor
+ * pipe ceiling pf_batched_kl_i8 is measured against. */
+int pf_probe_umma_i8(int64_t iters, int64_t *ops_host, uint32_t *sink, pf_stream_t stream);
+
 /* Diagnostic: a pure-DFMA kernel (8 independent FMA chains per thread, all
  * SMs); *flops_host receives its FLOP count so the caller can time it and
  * obtain the sustained FP64 rate K7 is measured against. */

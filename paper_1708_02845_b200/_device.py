@@ -158,6 +158,24 @@ class DeviceKernel:
                 self._H[key] = h
             return h
 
+    def slices(self, clamp: float):
+        """(A, ea, ldk): the 7 byte planes [7][rows][ldk] and per-row scale
+        exponents of max(P, clamp) for K7 on the int8 tensor pipe
+        (pf_slice_rows_u8), built once per clamp like H."""
+        key = ("i8", float(clamp))
+        with self._lock:
+            hit = self._H.get(key)
+            if hit is None:
+                t = torch()
+                ldk = round_up(self.k, 64)
+                A = t.empty((7, self.rows, ldk), dtype=t.uint8, device=self.device)
+                ea = t.empty(self.rows, dtype=t.int32, device=self.device)
+                nat.call("pf_slice_rows_u8", self.P.data_ptr(), self.ld, self.rows, self.k,
+                         float(clamp), ldk, A.data_ptr(), ea.data_ptr(),
+                         t.cuda.current_stream(self.device).cuda_stream)
+                hit = self._H[key] = (A, ea, ldk)
+            return hit
+
     def csr(self, cut: float, strict_positive: bool) -> "DeviceCSR":
         """The thresholded CSR view of this slab (K4), cached per (cut, mode)."""
         key = (float(cut), bool(strict_positive))

@@ -306,6 +306,16 @@ int pf_batched_kl_f64(const double *P, int64_t ld, int64_t rows, int64_t k, cons
   return check_launch("batched_kl_fixup");
 }
 
+int pf_batched_kl_fixup_f64(const double *P, int64_t ld, int64_t rows, int64_t k,
+                            const double *Tc, int64_t ldl, int64_t T, double clamp, double *out,
+                            int64_t ldo, uint32_t *guarded, pf_stream_t stream) {
+  if (rows <= 0 || T <= 0) return 0;
+  if (!P || !Tc || !out) return fail(PF_E_ARG, "batched_kl_fixup: null");
+  batched_kl_fixup_kernel<<<sm_count() * 8, 256, 0, as_stream(stream)>>>(
+      P, ld, rows, k, Tc, ldl, T, clamp, out, ldo, guarded);
+  return check_launch("batched_kl_fixup");
+}
+
 int pf_probe_dfma_f64(int64_t iters, int64_t *flops, double *out, pf_stream_t stream) {
   const int blocks = sm_count() * 8;
   dfma_probe_kernel<<<blocks, 256, 0, as_stream(stream)>>>(iters, out);

@@ -1,0 +1,406 @@
+// batched_i8.cu — K7 on the int8 tensor pipe: the batched-target KL
+// contraction as an exact-integer emulation of the FP64 GEMM (Ozaki scheme
+// with fixed-point byte slices) on tcgen05.mma kind::i8, TMEM accumulators,
+// TMA-fed shared memory.
+//
+// Reference semantics: T calls of pathfield/divergence.py dv_field(pk, kl, t)
+// (:154-187).  The contraction is
+//
+//   S[q, t] = sum_b a_qb * b_tb,   a_qb = max(P_qb, clamp) >= 0,
+//                                  b_tb = -log max(P_tb, clamp) >= 0,
+//   KL[q, t] = H[q] + S[q, t]      (H = sum c(Q) log c(Q), K1),
+//
+// and both operands are non-negative, so each is written as a 56-bit
+// unsigned fixed-point number against a per-row (a) / per-target (b)
+// power-of-two scale and cut into seven unsigned bytes (most significant
+// first):
+//
+//   a_qb = 2^ea_q * sum_{i=1..7} A_i[q,b] 2^-8i,  b_tb = 2^eb_t * sum_j B_j[t,b] 2^-8j
+//   S    = 2^(ea+eb) * sum_{l=2..} acc_l 2^-8l,   acc_l = sum_{i+j=l} A_i . B_j^T
+//
+// Every acc_l is an exact integer GEMM (u8 x u8 -> s32 in TMEM; at most 7
+// pairs x k x 255^2 < 2^31 for k <= 4717).  Levels 2..9 are kept (34 byte-
+// pair GEMMs); the first dropped level is 2^-80 relative, and rounding each
+// operand to 56 bits perturbs it by 2^-57 relative to its row / target
+// maximum: with sum_b a_qb = 1 (rows of P are stochastic) the absolute error
+// of S is ~1e-14, the same order as FP64 accumulation over k = 4102 terms.
+// The split-form cancellation guard of K2/K7 (|KL| < tau (|H| + |S|),
+// tau = 1e-3) sends the few pairs where that error could exceed 1e-10
+// relative to the reference-form per-element fixup (batched.cu), exactly as
+// the FP64 DMMA path does.
+//
+// Kernel shape (one CTA per 128 rows x 64 targets output tile, 128 threads):
+//   warp 0 lane 0   TMA producer: per 64-byte K block, one 3-D box of all 7
+//                   A slices (128 rows) and one of all 7 B slices (64
+//                   targets), SWIZZLE_64B, 2-stage ring (84 KB / stage)
+//   warp 1 lane 0   MMA issuer: 34 pairs x 2 K-steps of M128 N64 K32
+//   warps 0-3       epilogue: tcgen05.ld the 8 level accumulators (8 x 64
+//                   TMEM columns = all 512), combine in FP64, scale, fuse the
+//                   guard / settle / target-zero, store.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cmath>
+
+#include "pf_common.cuh"
+#include "pf_tc.cuh"
+
+namespace pf {
+
+constexpr int kOzSlices = 7;                 // bytes per operand (56-bit fixed point)
+constexpr int kOzLevels = 8;                 // levels l = 2..9 kept
+constexpr int kOzBM = 128, kOzBN = 64, kOzBK = 64;
+constexpr int kOzStages = 2;
+constexpr int kOzTileA = kOzBM * kOzBK;      // bytes per slice per stage
+constexpr int kOzTileB = kOzBN * kOzBK;
+constexpr int kOzStageBytes = kOzSlices * (kOzTileA + kOzTileB);  // 86,016
+constexpr int kOzSmem = kOzStages * kOzStageBytes + 1024;         // + alignment slack
+constexpr int kOzMaxK = 4717;                // 7 x k x 255^2 < 2^31
+constexpr unsigned long long kOzGuard = 0x7ff8dead0000ba7cull;    // == batched.cu kBatchGuard
+
+// ---------------------------------------------------------------- slicing --
+// 8 consecutive values -> 7 byte planes (most significant byte in plane 0).
+__device__ __forceinline__ void slice8(const double (&x)[8], int e, uint64_t (&w)[kOzSlices]) {
+#pragma unroll
+  for (int s = 0; s < kOzSlices; ++s) w[s] = 0;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const unsigned long long N = __double2ull_rn(ldexp(x[u], 56 - e));  // < 2^56
+#pragma unroll
+    for (int s = 0; s < kOzSlices; ++s)
+      w[s] |= static_cast<uint64_t>((N >> (8 * (kOzSlices - 1 - s))) & 0xffu) << (8 * u);
+  }
+}
+
+__device__ __forceinline__ int scale_exp(double m) { return m > 0.0 ? ilogb(m) + 1 : 0; }
+
+// Rows of the slab: a = max(P, clamp), warp per row.  slices: [7][rows][ldk].
+__global__ void __launch_bounds__(256) slice_rows_kernel(const double *__restrict__ P, int64_t ld,
+                                                         int64_t rows, int64_t k, double clamp,
+                                                         int64_t ldk, uint8_t *__restrict__ out,
+                                                         int32_t *__restrict__ exps) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t plane = rows * ldk;
+  for (int64_t r = warp; r < rows; r += nwarps) {
+    const double *row = P + r * ld;
+    double m = 0.0;
+    for (int64_t b = lane; b < k; b += 32) m = fmax(m, fmax(row[b], clamp));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    const int e = scale_exp(m);
+    if (lane == 0) exps[r] = e;
+    for (int64_t b0 = 8 * lane; b0 < ldk; b0 += 256) {
+      double x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x[u] = (b0 + u < k) ? fmax(row[b0 + u], clamp) : 0.0;
+      uint64_t w[kOzSlices];
+      slice8(x, e, w);
+#pragma unroll
+      for (int s = 0; s < kOzSlices; ++s)
+        *reinterpret_cast<uint64_t *>(out + s * plane + r * ldk + b0) = w[s];
+    }
+  }
+}
+
+// Targets: b = -L (L = log max(Pt, clamp), batch_prep_kernel), block per
+// target.  bad[0] |= 1 if some b < 0 (a target entry above 1: the caller then
+// uses the FP64 path).  slices: [7][T][ldk].
+__global__ void __launch_bounds__(256) slice_targets_kernel(const double *__restrict__ L,
+                                                            int64_t ldl, int64_t T, int64_t k,
+                                                            int64_t ldk, uint8_t *__restrict__ out,
+                                                            int32_t *__restrict__ exps,
+                                                            uint32_t *__restrict__ bad) {
+  const int64_t t = blockIdx.x;
+  if (t >= T) return;
+  const double *row = L + t * ldl;
+  __shared__ double red[8];
+  double m = 0.0;
+  bool neg = false;
+  for (int64_t b = threadIdx.x; b < k; b += blockDim.x) {
+    const double v = -row[b];
+    neg |= v < 0.0;
+    m = fmax(m, v);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  neg = __syncthreads_or(neg);
+  m = red[0];
+  for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) m = fmax(m, red[w]);
+  const int e = scale_exp(m);
+  if (threadIdx.x == 0) {
+    exps[t] = e;
+    if (neg && bad) atomicOr(bad, 1u);
+  }
+  const int64_t plane = T * ldk;
+  for (int64_t b0 = 8 * threadIdx.x; b0 < ldk; b0 += 8 * blockDim.x) {
+    double x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = (b0 + u < k) ? fmax(-row[b0 + u], 0.0) : 0.0;
+    uint64_t w[kOzSlices];
+    slice8(x, e, w);
+#pragma unroll
+    for (int s = 0; s < kOzSlices; ++s)
+      *reinterpret_cast<uint64_t *>(out + s * plane + t * ldk + b0) = w[s];
+  }
+}
+
+// ------------------------------------------------------------------ GEMM --
+__global__ void __launch_bounds__(128, 1) batched_kl_i8_kernel(
+    const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+    const int32_t *__restrict__ ea, const int32_t *__restrict__ eb, int64_t rows, int64_t T,
+    int nkb, const double *__restrict__ H, const int64_t *__restrict__ targets, double tau,
+    int64_t row0, double *__restrict__ out, int64_t ldo) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  __shared__ __align__(8) uint64_t full_bar[kOzStages], empty_bar[kOzStages], done_bar;
+  __shared__ uint32_t tmem_base;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int t0 = blockIdx.x * kOzBN;
+  const int64_t q0 = static_cast<int64_t>(blockIdx.y) * kOzBM;
+
+  if (tid == 0) {
+    tc::prefetch_map(&mapA);
+    tc::prefetch_map(&mapB);
+    for (int s = 0; s < kOzStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(&done_bar, 1);
+  }
+  if (warp == 0) tc::tmem_alloc<512>(&tmem_base);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tmem_base;
+
+  if (warp == 0 && lane == 0) {
+    // ---- TMA producer
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % kOzStages;
+      const uint32_t round = kb / kOzStages;
+      mbar_wait(&empty_bar[s], (round & 1) ^ 1);
+      uint8_t *sa = smem + s * kOzStageBytes;
+      uint8_t *sb = sa + kOzSlices * kOzTileA;
+      mbar_expect_tx(&full_bar[s], kOzStageBytes);
+      tc::tma_load_3d(sa, &mapA, kb * kOzBK, static_cast<int32_t>(q0), 0, &full_bar[s]);
+      tc::tma_load_3d(sb, &mapB, kb * kOzBK, t0, 0, &full_bar[s]);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---- MMA issuer: level l = i + j (1-based slices), accumulator l - 2
+    constexpr uint32_t idesc = tc::idesc_i8(kOzBM, kOzBN, false, false);
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % kOzStages;
+      mbar_wait(&full_bar[s], (kb / kOzStages) & 1);
+      tc::fence_after();
+      const uint32_t sa = smem_u32(smem + s * kOzStageBytes);
+      const uint32_t sb = sa + kOzSlices * kOzTileA;
+#pragma unroll
+      for (int ks = 0; ks < kOzBK / 32; ++ks) {
+#pragma unroll
+        for (int i = 1; i <= kOzSlices; ++i) {
+#pragma unroll
+          for (int j = 1; j <= kOzSlices; ++j) {
+            const int l = i + j;
+            if (l > kOzLevels + 1) continue;
+            const bool first = (kb == 0) && (ks == 0) && (i == (l <= kOzSlices + 1 ? 1 : l - kOzSlices));
+            tc::mma_i8(tmem + (l - 2) * kOzBN,
+                       tc::sdesc<64>(sa + (i - 1) * kOzTileA + 32 * ks),
+                       tc::sdesc<64>(sb + (j - 1) * kOzTileB + 32 * ks), idesc, !first);
+          }
+        }
+      }
+      tc::commit(&empty_bar[s]);  // frees this stage once its MMAs completed
+    }
+    tc::commit(&done_bar);
+  }
+  __syncwarp();
+
+  // ---- epilogue: thread = output row
+  mbar_wait(&done_bar, 0);
+  tc::fence_after();
+  const int r = warp * 32 + lane;
+  const int64_t q = q0 + r;
+  const bool row_ok = q < rows;
+  const double h = row_ok ? H[q] : 0.0;
+  const int e_q = row_ok ? ea[q] : 0;
+  const int64_t tq = row_ok ? row0 + q : -1;
+  const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+#pragma unroll 1
+  for (int c0 = 0; c0 < kOzBN; c0 += 8) {
+    uint32_t acc[kOzLevels][8];
+#pragma unroll
+    for (int l = 0; l < kOzLevels; ++l) tc::tmem_ld8(lane_base + l * kOzBN + c0, acc[l]);
+    tc::tmem_ld_wait();
+    if (!row_ok) continue;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t t = t0 + c0 + u;
+      if (t >= T) break;
+      double v = static_cast<double>(acc[kOzLevels - 1][u]);
+#pragma unroll
+      for (int l = kOzLevels - 2; l >= 0; --l) v = fma(v, 0x1p-8, static_cast<double>(acc[l][u]));
+      const double S = ldexp(v, e_q + eb[t] - 16);
+      double val = h + S;
+      const bool is_t = (tq == targets[t]);
+      if (!is_t && fabs(val) < tau * (fabs(h) + fabs(S)))
+        val = __longlong_as_double(static_cast<long long>(kOzGuard));
+      else
+        val = is_t ? 0.0 : settle(val);
+      out[q * ldo + t] = val;
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_free<512>(tmem);
+}
+
+// Diagnostic: the int8 tensor pipe's issue-rate ceiling, back-to-back
+// M128 N256 K32 u8 MMAs on shared-memory-resident operands, one CTA per SM;
+// bench.py reports K7's int8 rate against it.
+__global__ void __launch_bounds__(128, 1) umma_i8_probe_kernel(int iters, uint32_t *sink) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < (128 + 256) * 64 / 4; i += 128)
+    reinterpret_cast<uint32_t *>(smem)[i] = 0x01010101u * (i & 3);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (tid == 0) mbar_init(&bar, 1);
+  if (warp == 0) tc::tmem_alloc<256>(&tmem_base);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tm = tmem_base;
+  if (tid == 0) {
+    constexpr uint32_t id = tc::idesc_i8(128, 256, false, false);
+    const uint32_t sa = smem_u32(smem), sb = sa + 128 * 64;
+    for (int it = 0; it < iters; ++it)
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks)
+        tc::mma_i8(tm, tc::sdesc<64>(sa + 32 * ks), tc::sdesc<64>(sb + 32 * ks), id,
+                   (it | ks) != 0);
+    tc::commit(&bar);
+  }
+  __syncwarp();
+  mbar_wait(&bar, 0);
+  tc::fence_after();
+  uint32_t v[8];
+  tc::tmem_ld8(tm + (static_cast<uint32_t>(warp * 32) << 16), v);
+  tc::tmem_ld_wait();
+  if (v[0] == 0x12345u) sink[0] = v[1];
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_free<256>(tm);
+}
+
+// ------------------------------------------------------------ tensor maps --
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 3-D u8 map over slices [7][outer][ldk]: box {64, box_rows, 7}, SWIZZLE_64B,
+// out-of-range rows read as zero.
+static int slice_map(CUtensorMap *map, const uint8_t *base, int64_t outer, int64_t ldk,
+                     uint32_t box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return fail(PF_E_LAUNCH, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(ldk), static_cast<cuuint64_t>(outer),
+                        static_cast<cuuint64_t>(kOzSlices)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(ldk), static_cast<cuuint64_t>(outer * ldk)};
+  cuuint32_t box[3] = {kOzBK, box_rows, kOzSlices};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t *>(base), dims,
+                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(PF_E_ARG, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return 0;
+}
+
+}  // namespace pf
+
+using namespace pf;
+
+extern "C" {
+
+int pf_slice_rows_u8(const double *P, int64_t ld, int64_t rows, int64_t k, double clamp,
+                     int64_t ldk, uint8_t *slices, int32_t *exps, pf_stream_t stream) {
+  if (rows <= 0) return 0;
+  if (!P || !slices || !exps || k <= 0 || ldk < k || ldk % kOzBK)
+    return fail(PF_E_ARG, "slice_rows: bad args (ldk %% 64 == 0, ldk >= k)");
+  slice_rows_kernel<<<sm_count() * 8, 256, 0, as_stream(stream)>>>(P, ld, rows, k, clamp, ldk,
+                                                                    slices, exps);
+  return check_launch("slice_rows");
+}
+
+int pf_slice_targets_u8(const double *L, int64_t ldl, int64_t T, int64_t k, int64_t ldk,
+                        uint8_t *slices, int32_t *exps, uint32_t *bad, pf_stream_t stream) {
+  if (T <= 0) return 0;
+  if (!L || !slices || !exps || k <= 0 || ldk < k || ldk % kOzBK)
+    return fail(PF_E_ARG, "slice_targets: bad args (ldk %% 64 == 0, ldk >= k)");
+  slice_targets_kernel<<<static_cast<unsigned>(T), 256, 0, as_stream(stream)>>>(
+      L, ldl, T, k, ldk, slices, exps, bad);
+  return check_launch("slice_targets");
+}
+
+int pf_batched_kl_i8(const uint8_t *A, const int32_t *ea, int64_t rows, const uint8_t *B,
+                     const int32_t *eb, int64_t T, int64_t k, int64_t ldk, const double *H,
+                     const int64_t *targets, double tau, int64_t row0, double *out, int64_t ldo,
+                     pf_stream_t stream) {
+  if (rows <= 0 || T <= 0) return 0;
+  if (!A || !ea || !B || !eb || !H || !targets || !out) return fail(PF_E_ARG, "batched_kl_i8: null");
+  if (k > kOzMaxK) return fail(PF_E_DOMAIN, "batched_kl_i8: k = %lld > %d", (long long)k, kOzMaxK);
+  if (ldk % kOzBK || ldk < k || ldo < T)
+    return fail(PF_E_ALIGN, "batched_kl_i8: ldk %% 64 == 0, ldo >= T");
+  if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15)
+    return fail(PF_E_ALIGN, "batched_kl_i8: slice planes must be 16-byte aligned");
+  const int64_t row_tiles = (rows + kOzBM - 1) / kOzBM;
+  if (row_tiles > 65535) return fail(PF_E_DOMAIN, "batched_kl_i8: too many rows per launch");
+  CUtensorMap mA, mB;
+  if (int e = slice_map(&mA, A, rows, ldk, kOzBM)) return e;
+  if (int e = slice_map(&mB, B, T, ldk, kOzBN)) return e;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(batched_kl_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kOzSmem) != cudaSuccess)
+      return fail(PF_E_LAUNCH, "batched_kl_i8: smem attribute");
+    attr = true;
+  }
+  const int nkb = static_cast<int>((k + kOzBK - 1) / kOzBK);
+  dim3 grid(static_cast<unsigned>((T + kOzBN - 1) / kOzBN), static_cast<unsigned>(row_tiles));
+  batched_kl_i8_kernel<<<grid, 128, kOzSmem, as_stream(stream)>>>(
+      mA, mB, ea, eb, rows, T, nkb, H, targets, tau, row0, out, ldo);
+  return check_launch("batched_kl_i8");
+}
+
+int pf_probe_umma_i8(int64_t iters, int64_t *ops_host, uint32_t *sink, pf_stream_t stream) {
+  const int smem = (128 + 256) * 64 + 1024;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(umma_i8_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             smem) != cudaSuccess)
+      return fail(PF_E_LAUNCH, "probe_umma_i8: smem attribute");
+    attr = true;
+  }
+  const int blocks = sm_count();
+  umma_i8_probe_kernel<<<blocks, 128, smem, as_stream(stream)>>>(static_cast<int>(iters), sink);
+  if (ops_host) *ops_host = 2LL * 128 * 256 * 64 * iters * blocks;
+  return check_launch("probe_umma_i8");
+}
+
+}  // extern "C"

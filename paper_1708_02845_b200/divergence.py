@@ -350,12 +350,22 @@ def dv_field_f32(pk: PoissonKernel, fd: FDivergence, p: int, clamp: float | None
 # Batched targets (K7; no reference API: T x dv_field)
 # ---------------------------------------------------------------------------
 
-def dv_field_batch_device(pk: PoissonKernel, fd: FDivergence, targets, clamp=None):
+I8_MAX_K = 4717  # batched_i8.cu: 7 x k x 255^2 < 2^31
+
+
+def dv_field_batch_device(pk: PoissonKernel, fd: FDivergence, targets, clamp=None,
+                          method: str = "auto"):
     """Fields to T targets at once on the device: (values (n, T) tensor, flags (T,) bool array).
 
-    KL (default order) runs as one FP64 GEMM with a fused epilogue (K7);
-    any other generator or ``swap_order`` is T single-target launches.
+    KL (default order) runs as one contraction with a fused epilogue (K7):
+    ``method="i8"`` is the exact-integer emulation of the FP64 GEMM on the
+    int8 tensor pipe (tcgen05, batched_i8.cu), ``"f64"`` the FP64 DMMA GEMM;
+    ``"auto"`` picks i8 when k <= 4717 (falling back to f64 for a batch with
+    a target entry above 1).  Any other generator or ``swap_order`` is T
+    single-target launches.
     """
+    if method not in ("auto", "i8", "f64"):
+        raise ValueError(f"method must be 'auto', 'i8' or 'f64', not {method!r}")
     t = dev.require_cuda()
     targets = np.asarray(targets, dtype=np.int64).reshape(-1)
     if targets.size and (targets.min() < 0 or targets.max() >= pk.n):
@@ -388,22 +398,45 @@ def dv_field_batch_device(pk: PoissonKernel, fd: FDivergence, targets, clamp=Non
     nonuni, ref = dk.mask_nonuniform(c) if c > 0.0 else (False, None)
     nat.call("pf_batch_prep_f64", Pt.data_ptr(), Pt.stride(0), T, dk.k, ldl, c, nat.ptr(ref),
              L.data_ptr(), Tc.data_ptr(), tflag.data_ptr(), s.cuda_stream)
-    nat.call("pf_batched_kl_f64", dk.P.data_ptr(), dk.ld, dk.rows, dk.k, H.data_ptr(),
-             L.data_ptr(), Tc.data_ptr(), ldl, T, tg.data_ptr(), c, KL_GUARD_TAU, dk.row0,
-             out.data_ptr(), out.stride(0), tflag.data_ptr() + 4 * T, s.cuda_stream)
+    use_i8 = method == "i8" or (method == "auto" and dk.k <= I8_MAX_K)
+    if use_i8:
+        if dk.k > I8_MAX_K:
+            raise ValueError(f"method='i8' needs k <= {I8_MAX_K} (k = {dk.k})")
+        A, ea, ldk = dk.slices(c)
+        B = t.empty((7, T, ldk), dtype=t.uint8, device=dk.device)
+        eb = t.empty(T, dtype=t.int32, device=dk.device)
+        bad = t.zeros(1, dtype=t.int32, device=dk.device)
+        nat.call("pf_slice_targets_u8", L.data_ptr(), ldl, T, dk.k, ldk, B.data_ptr(),
+                 eb.data_ptr(), bad.data_ptr(), s.cuda_stream)
+        if bool(bad.item()):
+            if method == "i8":
+                raise ValueError("method='i8': a target row has an entry above 1")
+            use_i8 = False
+    if use_i8:
+        nat.call("pf_batched_kl_i8", A.data_ptr(), ea.data_ptr(), dk.rows, B.data_ptr(),
+                 eb.data_ptr(), T, dk.k, ldk, H.data_ptr(), tg.data_ptr(), KL_GUARD_TAU,
+                 dk.row0, out.data_ptr(), out.stride(0), s.cuda_stream)
+        nat.call("pf_batched_kl_fixup_f64", dk.P.data_ptr(), dk.ld, dk.rows, dk.k,
+                 Tc.data_ptr(), ldl, T, c, out.data_ptr(), out.stride(0),
+                 tflag.data_ptr() + 4 * T, s.cuda_stream)
+    else:
+        nat.call("pf_batched_kl_f64", dk.P.data_ptr(), dk.ld, dk.rows, dk.k, H.data_ptr(),
+                 L.data_ptr(), Tc.data_ptr(), ldl, T, tg.data_ptr(), c, KL_GUARD_TAU, dk.row0,
+                 out.data_ptr(), out.stride(0), tflag.data_ptr() + 4 * T, s.cuda_stream)
     tf = tflag.cpu().numpy()
     flags = (nonuni | (tf[:T] != 0)) if (c > 0.0 and ref is not None) else np.zeros(T, bool)
     return out, flags
 
 
-def dv_field_batch(pk: PoissonKernel, fd: FDivergence, targets, clamp=None):
+def dv_field_batch(pk: PoissonKernel, fd: FDivergence, targets, clamp=None,
+                   method: str = "auto"):
     """``np.column_stack([dv_field(pk, fd, t).values for t in targets])`` in one pass.
 
     Returns the (n, T) FP64 array; the per-target ``clamped`` flags are on
     :func:`dv_field_batch_device`.
     """
     t = dev.require_cuda()
-    out, flags = dv_field_batch_device(pk, fd, targets, clamp)
+    out, flags = dv_field_batch_device(pk, fd, targets, clamp, method)
     return _to_host(t, out, t.cuda.current_stream(out.device))
 
 

@@ -1,4 +1,6 @@
-"""K7 batched-target KL (one FP64 GEMM + fused epilogue) vs T x dv_field."""
+"""K7 batched-target KL vs T x dv_field, on both contraction paths: the FP64
+DMMA GEMM ("f64") and the exact-integer emulation on the int8 tensor pipe
+("i8", tcgen05 — batched_i8.cu)."""
 
 import numpy as np
 import pytest
@@ -12,42 +14,50 @@ pytestmark = pytest.mark.gpu
 RTOL = 1e-10
 
 
+METHODS = ("i8", "f64")
+
+
+@pytest.mark.parametrize("method", METHODS)
 @pytest.mark.parametrize("name", CASES)
-def test_batch_matches_reference_fields(name):
+def test_batch_matches_reference_fields(name, method):
     c = case(name)
     pk = pf.PoissonKernel(c.dense, c.boundary, 0.0, 0.0)
     targets = c.targets
-    out, flags = pf.divergence.dv_field_batch_device(pk, pf.builtin_f("kl"), targets)
+    out, flags = pf.divergence.dv_field_batch_device(pk, pf.builtin_f("kl"), targets,
+                                                     method=method)
     got = out.cpu().numpy()
     for j, t in enumerate(targets):
         ok, err = rel_close(got[:, j], c[f"field/kl/{j}"], RTOL)
-        assert ok, (name, j, err)
+        assert ok, (name, method, j, err)
         assert bool(flags[j]) == bool(c[f"flags/kl/{j}"])
-    host = pf.dv_field_batch(pk, pf.builtin_f("kl"), targets)
+    host = pf.dv_field_batch(pk, pf.builtin_f("kl"), targets, method=method)
     np.testing.assert_array_equal(host, got)
 
 
-def test_batch_equals_single_target_calls_large_T():
+@pytest.mark.parametrize("method", METHODS)
+def test_batch_equals_single_target_calls_large_T(method):
     # T spanning several 128-wide target tiles and a ragged row tile
     mesh = I.build({"gen": "holes", "spacing": 0.03, "seed": 1})
     dense, boundary = I.poisson_kernel(mesh)
     pk = pf.PoissonKernel(dense, boundary, 0.0, 0.0)
     rng = np.random.default_rng(3)
     targets = rng.choice(mesh.n, 300, replace=False)
-    got = pf.dv_field_batch(pk, pf.builtin_f("kl"), targets)
+    got = pf.dv_field_batch(pk, pf.builtin_f("kl"), targets, method=method)
     for j in range(0, 300, 23):
         ref, _ = O.dv_field(dense, boundary, "kl", int(targets[j]))
         ok, err = rel_close(got[:, j], ref, RTOL)
         assert ok, (j, err)
 
 
-def test_batch_flags_nonuniform_masks_and_other_generators():
+@pytest.mark.parametrize("method", METHODS)
+def test_batch_flags_nonuniform_masks_and_other_generators(method):
     dense = I.synthetic_kernel(700, 67, seed=4)
     dense[::7, 3] = 0.0          # interior rows with different zero patterns
     boundary = np.array([1, 5])
     pk = pf.PoissonKernel(dense, boundary, 0.0, 0.0)
     targets = [0, 7, 100, 699]
-    out, flags = pf.divergence.dv_field_batch_device(pk, pf.builtin_f("kl"), targets)
+    out, flags = pf.divergence.dv_field_batch_device(pk, pf.builtin_f("kl"), targets,
+                                                     method=method)
     got = out.cpu().numpy()
     for j, t in enumerate(targets):
         ref, fl = O.dv_field(dense, boundary, "kl", t)
@@ -59,3 +69,35 @@ def test_batch_flags_nonuniform_masks_and_other_generators():
         ref, _ = O.dv_field(dense, boundary, "tv", t)
         ok, err = rel_close(tv[:, j], ref, RTOL)
         assert ok, err
+
+
+def test_i8_and_f64_paths_agree_and_guard_fires():
+    # rows next to each target are near-duplicates (KL ~ 0): the split-form
+    # guard must route them to the reference-form fixup on both paths
+    rng = np.random.default_rng(11)
+    base = I.synthetic_kernel(300, 129, seed=5)
+    dense = np.repeat(base, 2, axis=0)
+    dense[1::2] *= 1.0 + 1e-4 * rng.standard_normal(dense[1::2].shape)
+    dense /= dense.sum(axis=1, keepdims=True)
+    pk = pf.PoissonKernel(dense, np.array([0, 1]), 0.0, 0.0)
+    targets = np.arange(2, 600, 37)
+    a8, _ = pf.divergence.dv_field_batch_device(pk, pf.builtin_f("kl"), targets, method="i8")
+    a64, _ = pf.divergence.dv_field_batch_device(pk, pf.builtin_f("kl"), targets, method="f64")
+    a8, a64 = a8.cpu().numpy(), a64.cpu().numpy()
+    for j, t in enumerate(targets):
+        ref, _ = O.dv_field(dense, np.array([0, 1]), "kl", int(t))
+        assert rel_close(a8[:, j], ref, RTOL)[0], j
+        assert rel_close(a64[:, j], ref, RTOL)[0], j
+        assert 0 < ref[t ^ 1] < 1e-6  # the twin row: split form cancels -> guarded
+
+
+def test_i8_limits():
+    dense = I.synthetic_kernel(64, 4800, seed=6)
+    pk = pf.PoissonKernel(dense, np.array([], dtype=np.int64), 0.0, 0.0)
+    with pytest.raises(ValueError):
+        pf.divergence.dv_field_batch_device(pk, pf.builtin_f("kl"), [3], method="i8")
+    out, _ = pf.divergence.dv_field_batch_device(pk, pf.builtin_f("kl"), [3, 9])  # auto -> f64
+    ref, _ = O.dv_field(dense, np.array([], dtype=np.int64), "kl", 9)
+    assert rel_close(out.cpu().numpy()[:, 1], ref, RTOL)[0]
+    with pytest.raises(ValueError):
+        pf.divergence.dv_field_batch_device(pk, pf.builtin_f("kl"), [3], method="bogus")
