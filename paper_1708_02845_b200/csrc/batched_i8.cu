@@ -29,14 +29,21 @@
 // relative to the reference-form per-element fixup (batched.cu), exactly as
 // the FP64 DMMA path does.
 //
-// Kernel shape (one CTA per 128 rows x 64 targets output tile, 128 threads):
-//   warp 0 lane 0   TMA producer: per 64-byte K block, one 3-D box of all 7
-//                   A slices (128 rows) and one of all 7 B slices (64
-//                   targets), SWIZZLE_64B, 2-stage ring (84 KB / stage)
-//   warp 1 lane 0   MMA issuer: 34 pairs x 2 K-steps of M128 N64 K32
-//   warps 0-3       epilogue: tcgen05.ld the 8 level accumulators (8 x 64
-//                   TMEM columns = all 512), combine in FP64, scale, fuse the
-//                   guard / settle / target-zero, store.
+// Kernel shape: one CTA per 128 rows x 128 targets output tile, 320 threads.
+// TMEM holds four N=128 s32 accumulators (all 512 columns), so each tile runs
+// two passes over K: levels 2..5 (10 pairs, slices 1..4), then levels 6..9
+// (24 pairs, slices 1..7), the first drained to FP64 registers in between.
+//   warp 0 lane 0   TMA producer: per 32-byte K block one 3-D box of the A
+//                   slices (128 rows) and one of the B slices (128 targets),
+//                   SWIZZLE_32B, 4-stage ring (<= 56 KB / stage)
+//   warp 1 lane 0   MMA issuer: M128 N128 K32 u8 x u8 -> s32
+//   warps 2-9       epilogue: each the 32 TMEM lanes of its quarter x 64
+//                   columns; tcgen05.ld, combine the levels in FP64, scale,
+//                   fuse the guard / settle / target-zero, store.
+// The int8 pipe draws the board to its 1000 W cap at this shape, so the
+// kernel is power-bound (scripts/probe_power.py); a 128 x 64 single-pass
+// variant with eight N=64 level accumulators was 7% slower (tuning record in
+// profiles/).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -49,12 +56,7 @@ namespace pf {
 
 constexpr int kOzSlices = 7;                 // bytes per operand (56-bit fixed point)
 constexpr int kOzLevels = 8;                 // levels l = 2..9 kept
-constexpr int kOzBM = 128, kOzBN = 64, kOzBK = 64;
-constexpr int kOzStages = 2;
-constexpr int kOzTileA = kOzBM * kOzBK;      // bytes per slice per stage
-constexpr int kOzTileB = kOzBN * kOzBK;
-constexpr int kOzStageBytes = kOzSlices * (kOzTileA + kOzTileB);  // 86,016
-constexpr int kOzSmem = kOzStages * kOzStageBytes + 1024;         // + alignment slack
+constexpr int kOzPad = 64;                   // ldk % 64 == 0 (slice plane row pitch)
 constexpr int kOzMaxK = 4717;                // 7 x k x 255^2 < 2^31
 constexpr unsigned long long kOzGuard = 0x7ff8dead0000ba7cull;    // == batched.cu kBatchGuard
 
@@ -148,29 +150,50 @@ __global__ void __launch_bounds__(256) slice_targets_kernel(const double *__rest
 }
 
 // ------------------------------------------------------------------ GEMM --
-__global__ void __launch_bounds__(128, 1) batched_kl_i8_kernel(
-    const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+// Two passes per 128 x 128 output tile, because TMEM holds four N=128
+// accumulators (4 x 128 columns = all 512): pass 1 = levels 2..5 (10 byte
+// pairs, slices 1..4), pass 2 = levels 6..9 (24 pairs, slices 1..7).  Between
+// them the 8 epilogue warps drain pass 1 into FP64 registers (each warp: its
+// 32 TMEM lanes x 64 columns) and release TMEM.  K blocks are 32 bytes
+// (SWIZZLE_32B rows = one MMA K step), 4-stage TMA ring of up to 56 KB.
+constexpr int kO2BN = 128, kO2BK = 32, kO2Stages = 4;
+constexpr int kO2Tile = 128 * kO2BK;                     // one slice, 4 KB (A or B)
+constexpr int kO2StageBytes = 2 * kOzSlices * kO2Tile;   // 57,344
+constexpr int kO2Smem = kO2Stages * kO2StageBytes + 1024;
+constexpr int kO2Threads = 320;                          // warp 0 TMA, 1 MMA, 2-9 epilogue
+constexpr int kO2Pass1Slices = 4;
+
+__device__ __forceinline__ int o2_first_i(int l) { return l <= kOzSlices + 1 ? 1 : l - kOzSlices; }
+
+__global__ void __launch_bounds__(kO2Threads, 1) batched_kl_i8_n128_kernel(
+    const __grid_constant__ CUtensorMap mapA7, const __grid_constant__ CUtensorMap mapA4,
+    const __grid_constant__ CUtensorMap mapB7, const __grid_constant__ CUtensorMap mapB4,
     const int32_t *__restrict__ ea, const int32_t *__restrict__ eb, int64_t rows, int64_t T,
     int nkb, const double *__restrict__ H, const int64_t *__restrict__ targets, double tau,
     int64_t row0, double *__restrict__ out, int64_t ldo) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  __shared__ __align__(8) uint64_t full_bar[kOzStages], empty_bar[kOzStages], done_bar;
+  __shared__ __align__(8) uint64_t full_bar[kO2Stages], empty_bar[kO2Stages];
+  __shared__ __align__(8) uint64_t pass_bar[2], drained_bar;
   __shared__ uint32_t tmem_base;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int t0 = blockIdx.x * kOzBN;
-  const int64_t q0 = static_cast<int64_t>(blockIdx.y) * kOzBM;
+  const int t0 = blockIdx.x * kO2BN;
+  const int64_t q0 = static_cast<int64_t>(blockIdx.y) * 128;
 
   if (tid == 0) {
-    tc::prefetch_map(&mapA);
-    tc::prefetch_map(&mapB);
-    for (int s = 0; s < kOzStages; ++s) {
+    tc::prefetch_map(&mapA7);
+    tc::prefetch_map(&mapA4);
+    tc::prefetch_map(&mapB7);
+    tc::prefetch_map(&mapB4);
+    for (int s = 0; s < kO2Stages; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
-    mbar_init(&done_bar, 1);
+    mbar_init(&pass_bar[0], 1);
+    mbar_init(&pass_bar[1], 1);
+    mbar_init(&drained_bar, 8);  // one arrival per epilogue warp
   }
   if (warp == 0) tc::tmem_alloc<512>(&tmem_base);
   tc::fence_before();
@@ -178,80 +201,122 @@ __global__ void __launch_bounds__(128, 1) batched_kl_i8_kernel(
   tc::fence_after();
   const uint32_t tmem = tmem_base;
 
-  if (warp == 0 && lane == 0) {
-    // ---- TMA producer
-    for (int kb = 0; kb < nkb; ++kb) {
-      const int s = kb % kOzStages;
-      const uint32_t round = kb / kOzStages;
-      mbar_wait(&empty_bar[s], (round & 1) ^ 1);
-      uint8_t *sa = smem + s * kOzStageBytes;
-      uint8_t *sb = sa + kOzSlices * kOzTileA;
-      mbar_expect_tx(&full_bar[s], kOzStageBytes);
-      tc::tma_load_3d(sa, &mapA, kb * kOzBK, static_cast<int32_t>(q0), 0, &full_bar[s]);
-      tc::tma_load_3d(sb, &mapB, kb * kOzBK, t0, 0, &full_bar[s]);
-    }
-  } else if (warp == 1 && lane == 0) {
-    // ---- MMA issuer: level l = i + j (1-based slices), accumulator l - 2
-    constexpr uint32_t idesc = tc::idesc_i8(kOzBM, kOzBN, false, false);
-    for (int kb = 0; kb < nkb; ++kb) {
-      const int s = kb % kOzStages;
-      mbar_wait(&full_bar[s], (kb / kOzStages) & 1);
-      tc::fence_after();
-      const uint32_t sa = smem_u32(smem + s * kOzStageBytes);
-      const uint32_t sb = sa + kOzSlices * kOzTileA;
-#pragma unroll
-      for (int ks = 0; ks < kOzBK / 32; ++ks) {
-#pragma unroll
-        for (int i = 1; i <= kOzSlices; ++i) {
-#pragma unroll
-          for (int j = 1; j <= kOzSlices; ++j) {
-            const int l = i + j;
-            if (l > kOzLevels + 1) continue;
-            const bool first = (kb == 0) && (ks == 0) && (i == (l <= kOzSlices + 1 ? 1 : l - kOzSlices));
-            tc::mma_i8(tmem + (l - 2) * kOzBN,
-                       tc::sdesc<64>(sa + (i - 1) * kOzTileA + 32 * ks),
-                       tc::sdesc<64>(sb + (j - 1) * kOzTileB + 32 * ks), idesc, !first);
-          }
-        }
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---- TMA producer: pass-1 K blocks (4 slices each), then pass-2 (7)
+      for (int it = 0; it < 2 * nkb; ++it) {
+        const int s = it % kO2Stages;
+        const uint32_t round = it / kO2Stages;
+        const bool p1 = it < nkb;
+        const int kb = p1 ? it : it - nkb;
+        mbar_wait(&empty_bar[s], (round & 1) ^ 1);
+        uint8_t *sa = smem + s * kO2StageBytes;
+        uint8_t *sb = sa + kOzSlices * kO2Tile;
+        mbar_expect_tx(&full_bar[s], (p1 ? kO2Pass1Slices : kOzSlices) * 2 * kO2Tile);
+        tc::tma_load_3d(sa, p1 ? &mapA4 : &mapA7, kb * kO2BK, static_cast<int32_t>(q0), 0,
+                        &full_bar[s]);
+        tc::tma_load_3d(sb, p1 ? &mapB4 : &mapB7, kb * kO2BK, t0, 0, &full_bar[s]);
       }
-      tc::commit(&empty_bar[s]);  // frees this stage once its MMAs completed
     }
-    tc::commit(&done_bar);
-  }
-  __syncwarp();
-
-  // ---- epilogue: thread = output row
-  mbar_wait(&done_bar, 0);
-  tc::fence_after();
-  const int r = warp * 32 + lane;
-  const int64_t q = q0 + r;
-  const bool row_ok = q < rows;
-  const double h = row_ok ? H[q] : 0.0;
-  const int e_q = row_ok ? ea[q] : 0;
-  const int64_t tq = row_ok ? row0 + q : -1;
-  const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-#pragma unroll 1
-  for (int c0 = 0; c0 < kOzBN; c0 += 8) {
-    uint32_t acc[kOzLevels][8];
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---- MMA issuer
+      constexpr uint32_t idesc = tc::idesc_i8(128, kO2BN, false, false);
+      for (int it = 0; it < 2 * nkb; ++it) {
+        const int s = it % kO2Stages;
+        const bool p1 = it < nkb;
+        const int kb = p1 ? it : it - nkb;
+        if (it == nkb) {  // pass 2 reuses the accumulators: wait for the drain
+          mbar_wait(&drained_bar, 0);
+          tc::fence_after();
+        }
+        mbar_wait(&full_bar[s], (it / kO2Stages) & 1);
+        tc::fence_after();
+        const uint32_t sa = smem_u32(smem + s * kO2StageBytes);
+        const uint32_t sb = sa + kOzSlices * kO2Tile;
+        if (p1) {
 #pragma unroll
-    for (int l = 0; l < kOzLevels; ++l) tc::tmem_ld8(lane_base + l * kOzBN + c0, acc[l]);
-    tc::tmem_ld_wait();
-    if (!row_ok) continue;
+          for (int i = 1; i <= kO2Pass1Slices; ++i)
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int64_t t = t0 + c0 + u;
-      if (t >= T) break;
-      double v = static_cast<double>(acc[kOzLevels - 1][u]);
+            for (int j = 1; j <= kO2Pass1Slices; ++j) {
+              const int l = i + j;
+              if (l > 5) continue;
+              tc::mma_i8(tmem + (l - 2) * kO2BN, tc::sdesc<32>(sa + (i - 1) * kO2Tile),
+                         tc::sdesc<32>(sb + (j - 1) * kO2Tile), idesc, !(kb == 0 && i == 1));
+            }
+        } else {
 #pragma unroll
-      for (int l = kOzLevels - 2; l >= 0; --l) v = fma(v, 0x1p-8, static_cast<double>(acc[l][u]));
-      const double S = ldexp(v, e_q + eb[t] - 16);
-      double val = h + S;
-      const bool is_t = (tq == targets[t]);
-      if (!is_t && fabs(val) < tau * (fabs(h) + fabs(S)))
-        val = __longlong_as_double(static_cast<long long>(kOzGuard));
-      else
-        val = is_t ? 0.0 : settle(val);
-      out[q * ldo + t] = val;
+          for (int i = 1; i <= kOzSlices; ++i)
+#pragma unroll
+            for (int j = 1; j <= kOzSlices; ++j) {
+              const int l = i + j;
+              if (l < 6 || l > kOzLevels + 1) continue;
+              tc::mma_i8(tmem + (l - 6) * kO2BN, tc::sdesc<32>(sa + (i - 1) * kO2Tile),
+                         tc::sdesc<32>(sb + (j - 1) * kO2Tile), idesc,
+                         !(kb == 0 && i == o2_first_i(l)));
+            }
+        }
+        tc::commit(&empty_bar[s]);
+        if (it == nkb - 1) tc::commit(&pass_bar[0]);
+      }
+      tc::commit(&pass_bar[1]);
+    }
+  } else {
+    // ---- epilogue warps 2..9: TMEM lanes 32 (warp % 4) .. +31, columns half * 64 .. +63
+    const int quarter = warp & 3, half = (warp - 2) >> 2;
+    const int r = quarter * 32 + lane;
+    const int64_t q = q0 + r;
+    const bool row_ok = q < rows;
+    const uint32_t base = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + half * 64;
+    double v1[64];
+    mbar_wait(&pass_bar[0], 0);
+    tc::fence_after();
+#pragma unroll
+    for (int c0 = 0; c0 < 64; c0 += 8) {
+      uint32_t acc[4][8];
+#pragma unroll
+      for (int l = 0; l < 4; ++l) tc::tmem_ld8(base + l * kO2BN + c0, acc[l]);
+      tc::tmem_ld_wait();
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        double v = static_cast<double>(acc[3][u]);
+#pragma unroll
+        for (int l = 2; l >= 0; --l) v = fma(v, 0x1p-8, static_cast<double>(acc[l][u]));
+        v1[c0 + u] = v;
+      }
+    }
+    tc::fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&drained_bar);
+    mbar_wait(&pass_bar[1], 0);
+    tc::fence_after();
+    const double h = row_ok ? H[q] : 0.0;
+    const int e_q = row_ok ? ea[q] : 0;
+    const int64_t tq = row_ok ? row0 + q : -1;
+#pragma unroll
+    for (int c0 = 0; c0 < 64; c0 += 8) {
+      uint32_t acc[4][8];
+#pragma unroll
+      for (int l = 0; l < 4; ++l) tc::tmem_ld8(base + l * kO2BN + c0, acc[l]);
+      tc::tmem_ld_wait();
+      if (!row_ok) continue;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int64_t t = t0 + half * 64 + c0 + u;
+        if (t >= T) continue;
+        double v = static_cast<double>(acc[3][u]);
+#pragma unroll
+        for (int l = 2; l >= 0; --l) v = fma(v, 0x1p-8, static_cast<double>(acc[l][u]));
+        v = fma(v, 0x1p-32, v1[c0 + u]);
+        const double S = ldexp(v, e_q + eb[t] - 16);
+        double val = h + S;
+        const bool is_t = (tq == targets[t]);
+        if (!is_t && fabs(val) < tau * (fabs(h) + fabs(S)))
+          val = __longlong_as_double(static_cast<long long>(kOzGuard));
+        else
+          val = is_t ? 0.0 : settle(val);
+        out[q * ldo + t] = val;
+      }
     }
   }
   tc::fence_before();
@@ -314,19 +379,22 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// 3-D u8 map over slices [7][outer][ldk]: box {64, box_rows, 7}, SWIZZLE_64B,
-// out-of-range rows read as zero.
+// 3-D u8 map over slices [7][outer][ldk]: box {box_k, box_rows, box_slices},
+// swizzle = box_k bytes, out-of-range rows read as zero.
 static int slice_map(CUtensorMap *map, const uint8_t *base, int64_t outer, int64_t ldk,
-                     uint32_t box_rows) {
+                     uint32_t box_rows, uint32_t box_k, uint32_t box_slices) {
   auto fn = encode_fn();
   if (!fn) return fail(PF_E_LAUNCH, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[3] = {static_cast<cuuint64_t>(ldk), static_cast<cuuint64_t>(outer),
                         static_cast<cuuint64_t>(kOzSlices)};
   cuuint64_t strides[2] = {static_cast<cuuint64_t>(ldk), static_cast<cuuint64_t>(outer * ldk)};
-  cuuint32_t box[3] = {kOzBK, box_rows, kOzSlices};
+  cuuint32_t box[3] = {box_k, box_rows, box_slices};
+  const CUtensorMapSwizzle sw = box_k == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : box_k == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                              : CU_TENSOR_MAP_SWIZZLE_32B;
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t *>(base), dims,
-                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(PF_E_ARG, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return 0;
@@ -341,7 +409,7 @@ extern "C" {
 int pf_slice_rows_u8(const double *P, int64_t ld, int64_t rows, int64_t k, double clamp,
                      int64_t ldk, uint8_t *slices, int32_t *exps, pf_stream_t stream) {
   if (rows <= 0) return 0;
-  if (!P || !slices || !exps || k <= 0 || ldk < k || ldk % kOzBK)
+  if (!P || !slices || !exps || k <= 0 || ldk < k || ldk % kOzPad)
     return fail(PF_E_ARG, "slice_rows: bad args (ldk %% 64 == 0, ldk >= k)");
   slice_rows_kernel<<<sm_count() * 8, 256, 0, as_stream(stream)>>>(P, ld, rows, k, clamp, ldk,
                                                                     slices, exps);
@@ -351,7 +419,7 @@ int pf_slice_rows_u8(const double *P, int64_t ld, int64_t rows, int64_t k, doubl
 int pf_slice_targets_u8(const double *L, int64_t ldl, int64_t T, int64_t k, int64_t ldk,
                         uint8_t *slices, int32_t *exps, uint32_t *bad, pf_stream_t stream) {
   if (T <= 0) return 0;
-  if (!L || !slices || !exps || k <= 0 || ldk < k || ldk % kOzBK)
+  if (!L || !slices || !exps || k <= 0 || ldk < k || ldk % kOzPad)
     return fail(PF_E_ARG, "slice_targets: bad args (ldk %% 64 == 0, ldk >= k)");
   slice_targets_kernel<<<static_cast<unsigned>(T), 256, 0, as_stream(stream)>>>(
       L, ldl, T, k, ldk, slices, exps, bad);
@@ -365,27 +433,29 @@ int pf_batched_kl_i8(const uint8_t *A, const int32_t *ea, int64_t rows, const ui
   if (rows <= 0 || T <= 0) return 0;
   if (!A || !ea || !B || !eb || !H || !targets || !out) return fail(PF_E_ARG, "batched_kl_i8: null");
   if (k > kOzMaxK) return fail(PF_E_DOMAIN, "batched_kl_i8: k = %lld > %d", (long long)k, kOzMaxK);
-  if (ldk % kOzBK || ldk < k || ldo < T)
+  if (ldk % kOzPad || ldk < k || ldo < T)
     return fail(PF_E_ALIGN, "batched_kl_i8: ldk %% 64 == 0, ldo >= T");
   if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15)
     return fail(PF_E_ALIGN, "batched_kl_i8: slice planes must be 16-byte aligned");
-  const int64_t row_tiles = (rows + kOzBM - 1) / kOzBM;
+  const int64_t row_tiles = (rows + 127) / 128;
   if (row_tiles > 65535) return fail(PF_E_DOMAIN, "batched_kl_i8: too many rows per launch");
-  CUtensorMap mA, mB;
-  if (int e = slice_map(&mA, A, rows, ldk, kOzBM)) return e;
-  if (int e = slice_map(&mB, B, T, ldk, kOzBN)) return e;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(batched_kl_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kOzSmem) != cudaSuccess)
+  CUtensorMap m[4];
+  if (int e = slice_map(&m[0], A, rows, ldk, 128, kO2BK, kOzSlices)) return e;
+  if (int e = slice_map(&m[1], A, rows, ldk, 128, kO2BK, kO2Pass1Slices)) return e;
+  if (int e = slice_map(&m[2], B, T, ldk, kO2BN, kO2BK, kOzSlices)) return e;
+  if (int e = slice_map(&m[3], B, T, ldk, kO2BN, kO2BK, kO2Pass1Slices)) return e;
+  static bool attr2 = false;
+  if (!attr2) {
+    if (cudaFuncSetAttribute(batched_kl_i8_n128_kernel,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, kO2Smem) != cudaSuccess)
       return fail(PF_E_LAUNCH, "batched_kl_i8: smem attribute");
-    attr = true;
+    attr2 = true;
   }
-  const int nkb = static_cast<int>((k + kOzBK - 1) / kOzBK);
-  dim3 grid(static_cast<unsigned>((T + kOzBN - 1) / kOzBN), static_cast<unsigned>(row_tiles));
-  batched_kl_i8_kernel<<<grid, 128, kOzSmem, as_stream(stream)>>>(
-      mA, mB, ea, eb, rows, T, nkb, H, targets, tau, row0, out, ldo);
-  return check_launch("batched_kl_i8");
+  const int nkb2 = static_cast<int>((k + kO2BK - 1) / kO2BK);
+  dim3 grid2(static_cast<unsigned>((T + kO2BN - 1) / kO2BN), static_cast<unsigned>(row_tiles));
+  batched_kl_i8_n128_kernel<<<grid2, kO2Threads, kO2Smem, as_stream(stream)>>>(
+      m[0], m[1], m[2], m[3], ea, eb, rows, T, nkb2, H, targets, tau, row0, out, ldo);
+  return check_launch("batched_kl_i8_n128");
 }
 
 int pf_probe_umma_i8(int64_t iters, int64_t *ops_host, uint32_t *sink, pf_stream_t stream) {
