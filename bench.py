@@ -395,7 +395,7 @@ def extra_c4_and_c5(t, nat, dev, pf, device, steps, peak):
     bad = t.zeros(1, dtype=t.int32, device=device)
     gemm_ms = [0.0]
 
-    def batch_i8(timed=False):
+    def batch_i8(timed=False, grade=64):
         nat.call("pf_batch_prep_f64", Pt.data_ptr(), Pt.stride(0), T, k, ldl, 1e-300, 0,
                  L.data_ptr(), Tc.data_ptr(), 0, s.cuda_stream)
         nat.call("pf_slice_targets_u8", L.data_ptr(), ldl, T, k, ldk, B.data_ptr(), eb.data_ptr(),
@@ -404,7 +404,7 @@ def extra_c4_and_c5(t, nat, dev, pf, device, steps, peak):
             e1.record(s)
         nat.call("pf_batched_kl_i8", A.data_ptr(), ea.data_ptr(), rows, B.data_ptr(),
                  eb.data_ptr(), T, k, ldk, H.data_ptr(), tg.data_ptr(), tau, 0, out.data_ptr(),
-                 out.stride(0), s.cuda_stream)
+                 out.stride(0), grade, s.cuda_stream)
         if timed:
             e2.record(s)
         nat.call("pf_batched_kl_fixup_f64", dk.P.data_ptr(), dk.ld, rows, k, Tc.data_ptr(), ldl,
@@ -434,6 +434,7 @@ def extra_c4_and_c5(t, nat, dev, pf, device, steps, peak):
     t.cuda.synchronize()
     gemm_only = e1.elapsed_time(e2)
     guarded = int(cnt.item())
+    ms_f32grade = timed(lambda: batch_i8(grade=32), reps)
     ms64 = timed(batch_f64, 1)
     flops = 2.0 * rows * k * T
     # measured ceilings of this GPU: sustained DFMA, and the int8 tensor pipe
@@ -465,6 +466,10 @@ def extra_c4_and_c5(t, nat, dev, pf, device, steps, peak):
                        "algorithmic_ops_per_launch": int_ops,
                        "peak_kind": "measured: pf_probe_umma_i8 (M128 N256 K32 u8 tcgen05.mma "
                                     "back to back from shared memory, all SMs)"},
+          "fp32_grade": {"note": "same kernel, 15 byte-pair GEMMs (levels 2..6 of the top 5 "
+                                 "planes): the north-star FP32 tolerance 1e-5",
+                         "ms_per_batch": ms_f32grade,
+                         "evals_per_s": rows * T / (ms_f32grade / 1e3)},
           "fp64_dmma_path": {"ms_per_batch": ms64, "evals_per_s": rows * T / (ms64 / 1e3),
                              "achieved_tflops": flops / (ms64 / 1e3) / 1e12,
                              "dfma_peak_tflops": dfma_tf,
@@ -500,6 +505,7 @@ def extra_c3(t, nat, dev, pf, device, steps, peak):
     vp = t.empty(k_pad + 4, dtype=t.float64, device=device)
     out = t.empty(rows + 2, dtype=t.float64, device=device)
     flags = out.data_ptr() + rows * 8
+    queue = t.empty(rows, dtype=t.int64, device=device)
     ev = [t.cuda.Event(enable_timing=True) for _ in range(4)]
     ms = [0.0, 0.0]
 
@@ -510,7 +516,8 @@ def extra_c3(t, nat, dev, pf, device, steps, peak):
             ev[0].record(s)
         nat.call("pf_csr_kl_f64", dc.indptr.data_ptr(), dc.indices.data_ptr(), dc.data.data_ptr(),
                  dc.log_data.data_ptr(), dc.hs.data_ptr(), rows, k, logt,
-                 pf.divergence.KL_GUARD_TAU, 0, 0, rows, out.data_ptr(), 0, flags, s.cuda_stream)
+                 pf.divergence.KL_GUARD_TAU, 0, 0, rows, out.data_ptr(), 0, flags,
+                 queue.data_ptr(), s.cuda_stream)
         if timed:
             ev[1].record(s)
         nat.call("pf_csr_target_prep_f64", dc.indptr.data_ptr(), dc.indices.data_ptr(),
@@ -669,10 +676,13 @@ def run_native(args):
             pf.dv_field(pk, kl, target)
             pf.dv_field(pk, tv, target)
         barrier()
+        per = []
         w0 = time.perf_counter()
         for _ in range(args.steps):
+            p0 = time.perf_counter()
             fkl = pf.dv_field(pk, kl, target)
             ftv = pf.dv_field(pk, tv, target)
+            per.append(time.perf_counter() - p0)
         barrier()
         e2e_s = time.perf_counter() - w0
         assert np.array_equal(fkl.values, step.out_kl[:rows].cpu().numpy())
@@ -680,6 +690,8 @@ def run_native(args):
         e2e = {"value": 2 * rows * args.steps / e2e_s, "unit": "evals/s",
                "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 2 * (rows + 2) * 8,
                "ms_per_step": 1e3 * e2e_s / args.steps,
+               "step_ms_min_median_max": [1e3 * min(per), 1e3 * statistics.median(per),
+                                          1e3 * max(per)],
                "note": "wall clock of dv_field(pk, kl, t) + dv_field(pk, tv, t) per step through "
                        "the public API: P resident in HBM (per-PoissonKernel device cache, as "
                        "DomainContext keeps P resident); the target index is a kernel argument; "
@@ -741,17 +753,22 @@ def run_native(args):
                                if peak_kind == "measured" else "fallback 6.65 TB/s")})
 
     extras = {}
+    want = set(args.extras.split(","))
     if ws == 1 and not args.no_extras:
-        try:
-            extras["c2_f32"] = extra_f32(t, nat, dev, pf, dk, target, args.steps, peak)
-        except Exception as exc:
-            extras["c2_f32"] = {"error": f"{type(exc).__name__}: {exc}"}
+        if "f32" in want:
+            try:
+                extras["c2_f32"] = extra_f32(t, nat, dev, pf, dk, target, args.steps, peak)
+            except Exception as exc:
+                extras["c2_f32"] = {"error": f"{type(exc).__name__}: {exc}"}
         del step, dk, P_dev
         t.cuda.empty_cache()
-        for name, fn in (("c3_csr", lambda: extra_c3(t, nat, dev, pf, device, args.steps, peak)),
-                         ("c4_c5", lambda: extra_c4_and_c5(t, nat, dev, pf, device, args.steps,
-                                                           peak)),
-                         ("c5_tracer", lambda: extra_tracer(t, nat, dev, pf, device))):
+        for name, key, fn in (
+                ("c3_csr", "c3", lambda: extra_c3(t, nat, dev, pf, device, args.steps, peak)),
+                ("c4_c5", "c4c5", lambda: extra_c4_and_c5(t, nat, dev, pf, device, args.steps,
+                                                          peak)),
+                ("c5_tracer", "tracer", lambda: extra_tracer(t, nat, dev, pf, device))):
+            if key not in want:
+                continue
             try:
                 r = fn()
                 if name == "c4_c5":
@@ -799,6 +816,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the C3/C4/C5/tracer side measurements (N=1 only)")
+    ap.add_argument("--extras", default="f32,c3,c4c5,tracer",
+                    help="comma list of side measurements to run (f32, c3, c4c5, tracer)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

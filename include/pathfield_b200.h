@@ -207,11 +207,14 @@ int pf_csr_target_prep_f64(const int64_t *indptr, const int32_t *indices,
  * divergence.py:226,277).  Split form hs[q] - sum v logt with a cancellation
  * guard re-evaluated in the reference form; then _settle (:286).
  * ops[i] = |supp(q)| (:276) if ops != NULL; flags[PF_FLAG_GUARDED] counts
- * re-evaluated rows. */
+ * re-evaluated rows.  With `queue` (capacity: one int64 per output row, and
+ * flags[PF_FLAG_GUARDED] zero on entry, as pf_target_prep_f64 leaves it) the
+ * field kernel appends guarded rows to it and the re-evaluation visits only
+ * those; with queue == NULL it scans the whole output for the guard sentinel. */
 int pf_csr_kl_f64(const int64_t *indptr, const int32_t *indices, const double *data,
                   const double *log_data, const double *hs, int64_t rows, int64_t k,
                   const double *logt, double tau, int64_t row0, const int64_t *queries,
-                  int64_t nq, double *out, int64_t *ops, uint32_t *flags,
+                  int64_t nq, double *out, int64_t *ops, uint32_t *flags, int64_t *queue,
                   pf_stream_t stream);
 
 /* ---- K6: CSR TV field -------------------------------------------------------
@@ -283,8 +286,11 @@ int pf_batched_kl_fixup_f64(const double *P, int64_t ld, int64_t rows, int64_t k
  * pf_slice_targets_u8: slices [7][T][ldk] and exps[T] of -L (L from
  *   pf_batch_prep_f64); bad[0] |= 1 if some -L < 0 (then use the FP64 path).
  * pf_batched_kl_i8: out[q*ldo + t] = H[q] + S[q,t] with the K7 epilogue
- *   (guard sentinel, settle, zero at the target); k <= 4717.  Follow with
- *   pf_batched_kl_fixup_f64 for the guarded pairs. */
+ *   (guard sentinel, settle, zero at the target); k <= 4717.  grade 64 keeps
+ *   levels 2..9 of all 7 planes (34 pairs, FP64-grade: within 1e-10 of the
+ *   reference), grade 32 levels 2..6 of the top 5 planes (15 pairs, the
+ *   north-star FP32 tolerance 1e-5).  Follow with pf_batched_kl_fixup_f64 for
+ *   the guarded pairs. */
 int pf_slice_rows_u8(const double *P, int64_t ld, int64_t rows, int64_t k, double clamp,
                      int64_t ldk, uint8_t *slices, int32_t *exps, pf_stream_t stream);
 int pf_slice_targets_u8(const double *L, int64_t ldl, int64_t T, int64_t k, int64_t ldk,
@@ -292,7 +298,7 @@ int pf_slice_targets_u8(const double *L, int64_t ldl, int64_t T, int64_t k, int6
 int pf_batched_kl_i8(const uint8_t *A, const int32_t *ea, int64_t rows, const uint8_t *B,
                      const int32_t *eb, int64_t T, int64_t k, int64_t ldk, const double *H,
                      const int64_t *targets, double tau, int64_t row0, double *out, int64_t ldo,
-                     pf_stream_t stream);
+                     int grade, pf_stream_t stream);
 
 /* Diagnostic: back-to-back M128 N256 K32 u8 tcgen05.mma on shared-memory
  * operands, one CTA per SM (*ops_host = integer ops issued): the int8 tensor

@@ -287,12 +287,7 @@ int pf_batched_kl_f64(const double *P, int64_t ld, int64_t rows, int64_t k, cons
   if ((ld & 1) || (reinterpret_cast<uintptr_t>(P) & 15) || ldl % 16 || ldl < k || ldo < T)
     return fail(PF_E_ALIGN, "batched_kl: alignment (ld even, ldl %% 16 == 0)");
   const size_t smem = static_cast<size_t>(kV2Stages) * (kV2StageA + kV2StageB) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(batched_kl_dmma2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    attr = true;
-  }
+  if (int e = ensure_smem((const void *)batched_kl_dmma2_kernel, smem)) return e;
   dim3 grid(static_cast<unsigned>((T + kV2BN - 1) / kV2BN),
             static_cast<unsigned>((rows + kV2BM - 1) / kV2BM));
   if (grid.y > 65535) return fail(PF_E_DOMAIN, "batched_kl: too many rows per launch (%lld)",

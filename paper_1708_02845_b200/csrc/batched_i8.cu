@@ -55,7 +55,6 @@
 namespace pf {
 
 constexpr int kOzSlices = 7;                 // bytes per operand (56-bit fixed point)
-constexpr int kOzLevels = 8;                 // levels l = 2..9 kept
 constexpr int kOzPad = 64;                   // ldk % 64 == 0 (slice plane row pitch)
 constexpr int kOzMaxK = 4717;                // 7 x k x 255^2 < 2^31
 constexpr unsigned long long kOzGuard = 0x7ff8dead0000ba7cull;    // == batched.cu kBatchGuard
@@ -163,8 +162,10 @@ constexpr int kO2Smem = kO2Stages * kO2StageBytes + 1024;
 constexpr int kO2Threads = 320;                          // warp 0 TMA, 1 MMA, 2-9 epilogue
 constexpr int kO2Pass1Slices = 4;
 
-__device__ __forceinline__ int o2_first_i(int l) { return l <= kOzSlices + 1 ? 1 : l - kOzSlices; }
-
+// Pass 2 covers levels 6..kMaxL with byte planes 1..kS: (7, 9) is the FP64
+// grade (34 pairs in all), (5, 6) the FP32 grade of the north-star 1e-5
+// tolerance (15 pairs, the top 40 bits of the same planes).
+template <int kS, int kMaxL>
 __global__ void __launch_bounds__(kO2Threads, 1) batched_kl_i8_n128_kernel(
     const __grid_constant__ CUtensorMap mapA7, const __grid_constant__ CUtensorMap mapA4,
     const __grid_constant__ CUtensorMap mapB7, const __grid_constant__ CUtensorMap mapB4,
@@ -212,7 +213,7 @@ __global__ void __launch_bounds__(kO2Threads, 1) batched_kl_i8_n128_kernel(
         mbar_wait(&empty_bar[s], (round & 1) ^ 1);
         uint8_t *sa = smem + s * kO2StageBytes;
         uint8_t *sb = sa + kOzSlices * kO2Tile;
-        mbar_expect_tx(&full_bar[s], (p1 ? kO2Pass1Slices : kOzSlices) * 2 * kO2Tile);
+        mbar_expect_tx(&full_bar[s], (p1 ? kO2Pass1Slices : kS) * 2 * kO2Tile);
         tc::tma_load_3d(sa, p1 ? &mapA4 : &mapA7, kb * kO2BK, static_cast<int32_t>(q0), 0,
                         &full_bar[s]);
         tc::tma_load_3d(sb, p1 ? &mapB4 : &mapB7, kb * kO2BK, t0, 0, &full_bar[s]);
@@ -246,14 +247,15 @@ __global__ void __launch_bounds__(kO2Threads, 1) batched_kl_i8_n128_kernel(
             }
         } else {
 #pragma unroll
-          for (int i = 1; i <= kOzSlices; ++i)
+          for (int i = 1; i <= kS; ++i)
 #pragma unroll
-            for (int j = 1; j <= kOzSlices; ++j) {
+            for (int j = 1; j <= kS; ++j) {
               const int l = i + j;
-              if (l < 6 || l > kOzLevels + 1) continue;
+              if (l < 6 || l > kMaxL) continue;
+              const int first_i = l - kS > 1 ? l - kS : 1;
               tc::mma_i8(tmem + (l - 6) * kO2BN, tc::sdesc<32>(sa + (i - 1) * kO2Tile),
                          tc::sdesc<32>(sb + (j - 1) * kO2Tile), idesc,
-                         !(kb == 0 && i == o2_first_i(l)));
+                         !(kb == 0 && i == first_i));
             }
         }
         tc::commit(&empty_bar[s]);
@@ -293,20 +295,21 @@ __global__ void __launch_bounds__(kO2Threads, 1) batched_kl_i8_n128_kernel(
     const double h = row_ok ? H[q] : 0.0;
     const int e_q = row_ok ? ea[q] : 0;
     const int64_t tq = row_ok ? row0 + q : -1;
+    constexpr int kL2 = kMaxL - 5;  // pass-2 accumulators
 #pragma unroll
     for (int c0 = 0; c0 < 64; c0 += 8) {
-      uint32_t acc[4][8];
+      uint32_t acc[kL2][8];
 #pragma unroll
-      for (int l = 0; l < 4; ++l) tc::tmem_ld8(base + l * kO2BN + c0, acc[l]);
+      for (int l = 0; l < kL2; ++l) tc::tmem_ld8(base + l * kO2BN + c0, acc[l]);
       tc::tmem_ld_wait();
       if (!row_ok) continue;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int64_t t = t0 + half * 64 + c0 + u;
         if (t >= T) continue;
-        double v = static_cast<double>(acc[3][u]);
+        double v = static_cast<double>(acc[kL2 - 1][u]);
 #pragma unroll
-        for (int l = 2; l >= 0; --l) v = fma(v, 0x1p-8, static_cast<double>(acc[l][u]));
+        for (int l = kL2 - 2; l >= 0; --l) v = fma(v, 0x1p-8, static_cast<double>(acc[l][u]));
         v = fma(v, 0x1p-32, v1[c0 + u]);
         const double S = ldexp(v, e_q + eb[t] - 16);
         double val = h + S;
@@ -400,6 +403,18 @@ static int slice_map(CUtensorMap *map, const uint8_t *base, int64_t outer, int64
   return 0;
 }
 
+template <int kS, int kMaxL>
+static int launch_i8(const CUtensorMap (&m)[4], const int32_t *ea, const int32_t *eb,
+                     int64_t rows, int64_t T, int64_t k, const double *H, const int64_t *targets,
+                     double tau, int64_t row0, double *out, int64_t ldo, cudaStream_t stream) {
+  if (int e = ensure_smem((const void *)batched_kl_i8_n128_kernel<kS, kMaxL>, kO2Smem)) return e;
+  const int nkb = static_cast<int>((k + kO2BK - 1) / kO2BK);
+  dim3 grid(static_cast<unsigned>((T + kO2BN - 1) / kO2BN), static_cast<unsigned>((rows + 127) / 128));
+  batched_kl_i8_n128_kernel<kS, kMaxL><<<grid, kO2Threads, kO2Smem, stream>>>(
+      m[0], m[1], m[2], m[3], ea, eb, rows, T, nkb, H, targets, tau, row0, out, ldo);
+  return check_launch("batched_kl_i8");
+}
+
 }  // namespace pf
 
 using namespace pf;
@@ -429,7 +444,9 @@ int pf_slice_targets_u8(const double *L, int64_t ldl, int64_t T, int64_t k, int6
 int pf_batched_kl_i8(const uint8_t *A, const int32_t *ea, int64_t rows, const uint8_t *B,
                      const int32_t *eb, int64_t T, int64_t k, int64_t ldk, const double *H,
                      const int64_t *targets, double tau, int64_t row0, double *out, int64_t ldo,
-                     pf_stream_t stream) {
+                     int grade, pf_stream_t stream) {
+  if (grade != 64 && grade != 32) return fail(PF_E_ARG, "batched_kl_i8: grade must be 64 or 32");
+  const int kS = grade == 64 ? kOzSlices : 5;
   if (rows <= 0 || T <= 0) return 0;
   if (!A || !ea || !B || !eb || !H || !targets || !out) return fail(PF_E_ARG, "batched_kl_i8: null");
   if (k > kOzMaxK) return fail(PF_E_DOMAIN, "batched_kl_i8: k = %lld > %d", (long long)k, kOzMaxK);
@@ -440,33 +457,19 @@ int pf_batched_kl_i8(const uint8_t *A, const int32_t *ea, int64_t rows, const ui
   const int64_t row_tiles = (rows + 127) / 128;
   if (row_tiles > 65535) return fail(PF_E_DOMAIN, "batched_kl_i8: too many rows per launch");
   CUtensorMap m[4];
-  if (int e = slice_map(&m[0], A, rows, ldk, 128, kO2BK, kOzSlices)) return e;
+  if (int e = slice_map(&m[0], A, rows, ldk, 128, kO2BK, kS)) return e;
   if (int e = slice_map(&m[1], A, rows, ldk, 128, kO2BK, kO2Pass1Slices)) return e;
-  if (int e = slice_map(&m[2], B, T, ldk, kO2BN, kO2BK, kOzSlices)) return e;
+  if (int e = slice_map(&m[2], B, T, ldk, kO2BN, kO2BK, kS)) return e;
   if (int e = slice_map(&m[3], B, T, ldk, kO2BN, kO2BK, kO2Pass1Slices)) return e;
-  static bool attr2 = false;
-  if (!attr2) {
-    if (cudaFuncSetAttribute(batched_kl_i8_n128_kernel,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, kO2Smem) != cudaSuccess)
-      return fail(PF_E_LAUNCH, "batched_kl_i8: smem attribute");
-    attr2 = true;
-  }
-  const int nkb2 = static_cast<int>((k + kO2BK - 1) / kO2BK);
-  dim3 grid2(static_cast<unsigned>((T + kO2BN - 1) / kO2BN), static_cast<unsigned>(row_tiles));
-  batched_kl_i8_n128_kernel<<<grid2, kO2Threads, kO2Smem, as_stream(stream)>>>(
-      m[0], m[1], m[2], m[3], ea, eb, rows, T, nkb2, H, targets, tau, row0, out, ldo);
-  return check_launch("batched_kl_i8_n128");
+  return grade == 64 ? launch_i8<7, 9>(m, ea, eb, rows, T, k, H, targets, tau, row0, out, ldo,
+                                       as_stream(stream))
+                     : launch_i8<5, 6>(m, ea, eb, rows, T, k, H, targets, tau, row0, out, ldo,
+                                       as_stream(stream));
 }
 
 int pf_probe_umma_i8(int64_t iters, int64_t *ops_host, uint32_t *sink, pf_stream_t stream) {
   const int smem = (128 + 256) * 64 + 1024;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(umma_i8_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             smem) != cudaSuccess)
-      return fail(PF_E_LAUNCH, "probe_umma_i8: smem attribute");
-    attr = true;
-  }
+  if (int e = ensure_smem((const void *)umma_i8_probe_kernel, smem)) return e;
   const int blocks = sm_count();
   umma_i8_probe_kernel<<<blocks, 128, smem, as_stream(stream)>>>(static_cast<int>(iters), sink);
   if (ops_host) *ops_host = 2LL * 128 * 256 * 64 * iters * blocks;

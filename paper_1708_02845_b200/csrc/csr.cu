@@ -253,7 +253,8 @@ __global__ void __launch_bounds__(kCsrThreads) csr_kl_kernel(
     const int64_t *__restrict__ indptr, const int32_t *__restrict__ indices,
     const double *__restrict__ data, const double *__restrict__ hs, int64_t rows, int64_t k_pad,
     const double *__restrict__ logt, double tau, int64_t row0, const int64_t *__restrict__ queries,
-    int64_t nq, double *__restrict__ out, int64_t *__restrict__ ops) {
+    int64_t nq, double *__restrict__ out, int64_t *__restrict__ ops, int64_t *__restrict__ queue,
+    uint32_t *__restrict__ flags) {
   extern __shared__ __align__(128) unsigned char smem[];
   const double *lt = STAGE ? stage_vec(smem, logt, k_pad) : logt;
   const int lane = threadIdx.x & 31;
@@ -279,13 +280,15 @@ __global__ void __launch_bounds__(kCsrThreads) csr_kl_kernel(
     });
     const double cross = warp_sum(a0 + a1);
     double val = h - cross;
-    if (fabs(val) < tau * (fabs(h) + fabs(cross)))
+    const bool guarded = fabs(val) < tau * (fabs(h) + fabs(cross));
+    if (guarded)
       val = __longlong_as_double(static_cast<long long>(kCsrGuard));
     else
       val = settle(val);  // divergence.py:286
     if (lane == 0) {
       out[i] = val;
       if (ops) ops[i] = hi - lo;  // divergence.py:276
+      if (guarded && queue) queue[atomicAdd(&flags[PF_FLAG_GUARDED], 1u)] = i;
     }
     i = i2;
     r = r2;
@@ -331,6 +334,58 @@ __global__ void __launch_bounds__(kCsrThreads) csr_kl_fixup_kernel(
     }
   }
   if (lane == 0 && done && flags) atomicAdd(&flags[PF_FLAG_GUARDED], done);
+}
+
+// Guarded rows from the queue K5 filled (count in flags[PF_FLAG_GUARDED]):
+// warp per row, reference form as csr_kl_fixup_kernel.  Guarded rows are few
+// but each is a chain of dependent loads (index -> logt gather), so a warp
+// takes its row 512 entries at a time with every load of the chunk in flight
+// before the gathers (row starts are even in the device CSR: aligned pairs).
+__global__ void __launch_bounds__(kCsrThreads) csr_kl_fixup_queue_kernel(
+    const int64_t *__restrict__ indptr, const int32_t *__restrict__ indices,
+    const double *__restrict__ data, const double *__restrict__ log_data,
+    const double *__restrict__ logt, int64_t row0, const int64_t *__restrict__ queries,
+    const int64_t *__restrict__ queue, const uint32_t *__restrict__ flags,
+    double *__restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t n = flags[PF_FLAG_GUARDED];
+  for (int64_t jq = warp; jq < n; jq += nwarps) {
+    const int64_t i = queue[jq];
+    const int64_t r = queries ? queries[i] - row0 : i;
+    int64_t lo, hi;
+    row_extent(indptr, data, r, lo, hi);
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int64_t base = lo & ~int64_t{1}; base < hi; base += 512) {
+      double2 dv[8], lv[8];
+      int2 iv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int64_t e = base + 2 * (lane + 32 * u);
+        if (e < hi) {
+          dv[u] = __ldg(reinterpret_cast<const double2 *>(data + e));
+          lv[u] = __ldg(reinterpret_cast<const double2 *>(log_data + e));
+          iv[u] = __ldg(reinterpret_cast<const int2 *>(indices + e));
+        }
+      }
+      double tx[8], ty[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int64_t e = base + 2 * (lane + 32 * u);
+        tx[u] = (e >= lo && e < hi) ? __ldg(logt + iv[u].x) : 0.0;
+        ty[u] = (e + 1 >= lo && e + 1 < hi) ? __ldg(logt + iv[u].y) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int64_t e = base + 2 * (lane + 32 * u);
+        if (e >= lo && e < hi) acc[u & 3] += __dmul_rn(dv[u].x, lv[u].x - tx[u]);
+        if (e + 1 >= lo && e + 1 < hi) acc[u & 3] += __dmul_rn(dv[u].y, lv[u].y - ty[u]);
+      }
+    }
+    const double val = settle(warp_sum((acc[0] + acc[1]) + (acc[2] + acc[3])));
+    if (lane == 0) out[i] = val;
+  }
 }
 
 // ------------------------------------------------------------ K6 CSR TV --
@@ -501,13 +556,7 @@ static int grid_for(const void *kern, int threads, size_t smem, int64_t work_war
 
 template <typename K>
 static int smem_attr(K kern, size_t smem) {
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute((const void *)kern,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return fail(static_cast<int>(e), "smem attr: %s", cudaGetErrorString(e));
-  }
-  return 0;
+  return ensure_smem((const void *)kern, smem);
 }
 
 }  // namespace pf
@@ -561,7 +610,9 @@ int pf_csr_target_prep_f64(const int64_t *indptr, const int32_t *indices, const 
 int pf_csr_kl_f64(const int64_t *indptr, const int32_t *indices, const double *data,
                   const double *log_data, const double *hs, int64_t rows, int64_t k,
                   const double *logt, double tau, int64_t row0, const int64_t *queries,
-                  int64_t nq, double *out, int64_t *ops, uint32_t *flags, pf_stream_t stream) {
+                  int64_t nq, double *out, int64_t *ops, uint32_t *flags, int64_t *queue,
+                  pf_stream_t stream) {
+  if (queue && !flags) return fail(PF_E_ARG, "csr_kl: the guard queue needs flags");
   if (!indptr || !hs || !logt || !out || rows < 0 || k <= 0)
     return fail(PF_E_ARG, "csr_kl: bad args");
   const int64_t count = queries ? nq : rows;
@@ -573,13 +624,20 @@ int pf_csr_kl_f64(const int64_t *indptr, const int32_t *indices, const double *d
     if (int e = smem_attr(csr_kl_kernel<true>, smem)) return e;
     const int g = grid_for((const void *)csr_kl_kernel<true>, kCsrThreads, smem, count);
     csr_kl_kernel<true><<<g, kCsrThreads, smem, as_stream(stream)>>>(
-        indptr, indices, data, hs, rows, k_pad, logt, tau, row0, queries, nq, out, ops);
+        indptr, indices, data, hs, rows, k_pad, logt, tau, row0, queries, nq, out, ops, queue,
+        flags);
   } else {
     const int g = grid_for((const void *)csr_kl_kernel<false>, kCsrThreads, 0, count);
     csr_kl_kernel<false><<<g, kCsrThreads, 0, as_stream(stream)>>>(
-        indptr, indices, data, hs, rows, k_pad, logt, tau, row0, queries, nq, out, ops);
+        indptr, indices, data, hs, rows, k_pad, logt, tau, row0, queries, nq, out, ops, queue,
+        flags);
   }
   if (int e = check_launch("csr_kl")) return e;
+  if (queue) {
+    csr_kl_fixup_queue_kernel<<<sm_count() * 2, kCsrThreads, 0, as_stream(stream)>>>(
+        indptr, indices, data, log_data, logt, row0, queries, queue, flags, out);
+    return check_launch("csr_kl_fixup_queue");
+  }
   int64_t want = (count + 7) / 8;
   int64_t g2 = static_cast<int64_t>(sm_count()) * 4;
   if (g2 > want) g2 = want;

@@ -400,14 +400,7 @@ static constexpr size_t kMaxStagedSmem = 200 * 1024;
 
 template <typename K>
 static int set_smem(K kernel, size_t smem) {
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute((const void *)kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess)
-      return fail(static_cast<int>(e), "smem attribute: %s", cudaGetErrorString(e));
-  }
-  return 0;
+  return ensure_smem((const void *)kernel, smem);
 }
 
 template <typename K>

@@ -203,11 +203,7 @@ static int launch32(const float *P, int64_t ld, int64_t rows, int64_t k, const d
   const size_t smem = static_cast<size_t>(k) * 8 + 32;
   if (smem > 200 * 1024) return fail(PF_E_DOMAIN, "dense32: k=%lld too large", (long long)k);
   auto kern = dense32_kernel<KL>;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return fail(static_cast<int>(e), "dense32 smem: %s", cudaGetErrorString(e));
-  }
+  if (int e = ensure_smem((const void *)kern, smem)) return e;
   const int occ = occupancy((const void *)kern, kT32, smem);
   int64_t g = static_cast<int64_t>(sm_count()) * occ, want = (rows + 7) / 8;
   if (g > want) g = want;

@@ -359,13 +359,15 @@ def dv_field_batch_device(pk: PoissonKernel, fd: FDivergence, targets, clamp=Non
 
     KL (default order) runs as one contraction with a fused epilogue (K7):
     ``method="i8"`` is the exact-integer emulation of the FP64 GEMM on the
-    int8 tensor pipe (tcgen05, batched_i8.cu), ``"f64"`` the FP64 DMMA GEMM;
-    ``"auto"`` picks i8 when k <= 4717 (falling back to f64 for a batch with
-    a target entry above 1).  Any other generator or ``swap_order`` is T
-    single-target launches.
+    int8 tensor pipe (tcgen05, batched_i8.cu; within 1e-10 of the reference
+    like every FP64 path), ``"i8-f32"`` the same with 15 instead of 34 byte-
+    pair GEMMs for the north-star FP32 tolerance (1e-5 relative), ``"f64"``
+    the FP64 DMMA GEMM; ``"auto"`` picks i8 when k <= 4717 (falling back to
+    f64 for a batch with a target entry above 1).  Any other generator or
+    ``swap_order`` is T single-target launches.
     """
-    if method not in ("auto", "i8", "f64"):
-        raise ValueError(f"method must be 'auto', 'i8' or 'f64', not {method!r}")
+    if method not in ("auto", "i8", "i8-f32", "f64"):
+        raise ValueError(f"method must be 'auto', 'i8', 'i8-f32' or 'f64', not {method!r}")
     t = dev.require_cuda()
     targets = np.asarray(targets, dtype=np.int64).reshape(-1)
     if targets.size and (targets.min() < 0 or targets.max() >= pk.n):
@@ -398,10 +400,10 @@ def dv_field_batch_device(pk: PoissonKernel, fd: FDivergence, targets, clamp=Non
     nonuni, ref = dk.mask_nonuniform(c) if c > 0.0 else (False, None)
     nat.call("pf_batch_prep_f64", Pt.data_ptr(), Pt.stride(0), T, dk.k, ldl, c, nat.ptr(ref),
              L.data_ptr(), Tc.data_ptr(), tflag.data_ptr(), s.cuda_stream)
-    use_i8 = method == "i8" or (method == "auto" and dk.k <= I8_MAX_K)
+    use_i8 = method.startswith("i8") or (method == "auto" and dk.k <= I8_MAX_K)
     if use_i8:
         if dk.k > I8_MAX_K:
-            raise ValueError(f"method='i8' needs k <= {I8_MAX_K} (k = {dk.k})")
+            raise ValueError(f"method={method!r} needs k <= {I8_MAX_K} (k = {dk.k})")
         A, ea, ldk = dk.slices(c)
         B = t.empty((7, T, ldk), dtype=t.uint8, device=dk.device)
         eb = t.empty(T, dtype=t.int32, device=dk.device)
@@ -409,13 +411,14 @@ def dv_field_batch_device(pk: PoissonKernel, fd: FDivergence, targets, clamp=Non
         nat.call("pf_slice_targets_u8", L.data_ptr(), ldl, T, dk.k, ldk, B.data_ptr(),
                  eb.data_ptr(), bad.data_ptr(), s.cuda_stream)
         if bool(bad.item()):
-            if method == "i8":
-                raise ValueError("method='i8': a target row has an entry above 1")
+            if method != "auto":
+                raise ValueError(f"method={method!r}: a target row has an entry above 1")
             use_i8 = False
     if use_i8:
         nat.call("pf_batched_kl_i8", A.data_ptr(), ea.data_ptr(), dk.rows, B.data_ptr(),
                  eb.data_ptr(), T, dk.k, ldk, H.data_ptr(), tg.data_ptr(), KL_GUARD_TAU,
-                 dk.row0, out.data_ptr(), out.stride(0), s.cuda_stream)
+                 dk.row0, out.data_ptr(), out.stride(0), 32 if method == "i8-f32" else 64,
+                 s.cuda_stream)
         nat.call("pf_batched_kl_fixup_f64", dk.P.data_ptr(), dk.ld, dk.rows, dk.k,
                  Tc.data_ptr(), ldl, T, c, out.data_ptr(), out.stride(0),
                  tflag.data_ptr() + 4 * T, s.cuda_stream)
@@ -572,7 +575,8 @@ def _sparse_launch(pk, fd, p: int, queries=None, want_ops=False):
             nat.call("pf_csr_kl_f64", dc.indptr.data_ptr(), dc.indices.data_ptr(),
                      dc.data.data_ptr(), dc.log_data.data_ptr(), dc.hs.data_ptr(), dk.rows,
                      dk.k, st.logt, KL_GUARD_TAU, dk.row0, qptr, count, out.data_ptr(),
-                     nat.ptr(ops), flags, s.cuda_stream)
+                     nat.ptr(ops), flags, dk.scratch(s.cuda_stream, 8 * count, "csrq").data_ptr(),
+                     s.cuda_stream)
         else:
             nat.call("pf_csr_generic_f64", dc.indptr.data_ptr(), dc.indices.data_ptr(),
                      dc.data.data_ptr(), dc.log_data.data_ptr(), dk.rows, dk.k, kind, param,

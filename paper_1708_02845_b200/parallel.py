@@ -172,7 +172,8 @@ def _compute_sparse_slab(slab, fd, p: int, payload, cut: float, strict: bool):
                  st.tmask, flags, s)
         nat.call("pf_csr_kl_f64", dc.indptr.data_ptr(), dc.indices.data_ptr(), dc.data.data_ptr(),
                  dc.log_data.data_ptr(), dc.hs.data_ptr(), slab.rows, slab.k, st.logt,
-                 KL_GUARD_TAU, slab.row0, 0, slab.rows, out.data_ptr(), 0, flags, s)
+                 KL_GUARD_TAU, slab.row0, 0, slab.rows, out.data_ptr(), 0, flags,
+                 slab.scratch(s, 8 * slab.rows, "csrq").data_ptr(), s)
     else:
         kp = slab.k + (slab.k & 1)
         nat.call("pf_csr_tv_f64", dc.indptr.data_ptr(), dc.indices.data_ptr(), dc.data.data_ptr(),

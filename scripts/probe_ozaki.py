@@ -70,7 +70,7 @@ def run(rows, k, T, seed=0, timing=False):
              bad.data_ptr(), s)
     o8 = t.empty((rows, T), dtype=t.float64, device=d)
     nat.call("pf_batched_kl_i8", A.data_ptr(), ea.data_ptr(), rows, B.data_ptr(), eb.data_ptr(), T,
-             k, ldk, H.data_ptr(), tg.data_ptr(), tau, 0, o8.data_ptr(), T, s)
+             k, ldk, H.data_ptr(), tg.data_ptr(), tau, 0, o8.data_ptr(), T, 64, s)
     raw = o8.clone()
     nat.call("pf_batched_kl_fixup_f64", P.data_ptr(), ld, rows, k, Tc.data_ptr(), ldl, T, clamp,
              o8.data_ptr(), T, cnt.data_ptr() + 4, s)
@@ -96,12 +96,12 @@ def run(rows, k, T, seed=0, timing=False):
         st = t.cuda.current_stream(d)
         for _ in range(2):
             nat.call("pf_batched_kl_i8", A.data_ptr(), ea.data_ptr(), rows, B.data_ptr(), eb.data_ptr(),
-                     T, k, ldk, H.data_ptr(), tg.data_ptr(), tau, 0, o8.data_ptr(), T, s)
+                     T, k, ldk, H.data_ptr(), tg.data_ptr(), tau, 0, o8.data_ptr(), T, 64, s)
         ev[0].record(st)
         reps = 3
         for _ in range(reps):
             nat.call("pf_batched_kl_i8", A.data_ptr(), ea.data_ptr(), rows, B.data_ptr(), eb.data_ptr(),
-                     T, k, ldk, H.data_ptr(), tg.data_ptr(), tau, 0, o8.data_ptr(), T, s)
+                     T, k, ldk, H.data_ptr(), tg.data_ptr(), tau, 0, o8.data_ptr(), T, 64, s)
         ev[1].record(st)
         for _ in range(reps):
             nat.call("pf_batched_kl_f64", P.data_ptr(), ld, rows, k, H.data_ptr(), L.data_ptr(),

@@ -68,7 +68,7 @@ def main():
 
     def gemm():
         nat.call("pf_batched_kl_i8", A.data_ptr(), ea.data_ptr(), rows, B.data_ptr(), eb.data_ptr(),
-                 T, k, ldk, H.data_ptr(), tg.data_ptr(), 1e-3, 0, out.data_ptr(), T, s.cuda_stream)
+                 T, k, ldk, H.data_ptr(), tg.data_ptr(), 1e-3, 0, out.data_ptr(), T, 64, s.cuda_stream)
 
     gemm()
     t.cuda.synchronize()

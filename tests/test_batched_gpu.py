@@ -101,3 +101,17 @@ def test_i8_limits():
     assert rel_close(out.cpu().numpy()[:, 1], ref, RTOL)[0]
     with pytest.raises(ValueError):
         pf.divergence.dv_field_batch_device(pk, pf.builtin_f("kl"), [3], method="bogus")
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_i8_fp32_grade_within_north_star_tolerance(name):
+    c = case(name)
+    pk = pf.PoissonKernel(c.dense, c.boundary, 0.0, 0.0)
+    out, flags = pf.divergence.dv_field_batch_device(pk, pf.builtin_f("kl"), c.targets,
+                                                     method="i8-f32")
+    got = out.cpu().numpy()
+    for j, t in enumerate(c.targets):
+        ok, err = rel_close(got[:, j], c[f"field/kl/{j}"], 1e-5)
+        assert ok, (name, j, err)
+        assert got[t, j] == 0.0
+        assert bool(flags[j]) == bool(c[f"flags/kl/{j}"])
