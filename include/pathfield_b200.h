@@ -367,6 +367,36 @@ int pf_trace_batch_f64(const pf_mesh_t *mesh, const double *fields, const int64_
                        const int64_t *sources, const int32_t *field_of, int64_t npaths,
                        int64_t step_cap, const pf_paths_t *out, pf_stream_t stream);
 
+/* ---- Path metric (paths.py:326-368) ----------------------------------------
+ * A polyline instance p is one side of one compared pair: points
+ * pts[2*(src_off[p] + i) + {0,1}], i < len[p].
+ * pf_polyline_arc_f64: arc[src_off[p] + i] = sequential cumsum of np.hypot
+ *   segment lengths (arc[.. + 0] = 0) and segmin[p] = the shortest positive
+ *   segment (+inf if none; the default step is min over a pair / 4).
+ * pf_polyline_resample_f64: resample_polyline (np.linspace + np.interp) into
+ *   out[2*(out_off[p] + i) + {0,1}], i < cnt[p] = out_off[p+1] - out_off[p]
+ *   points; the caller computes cnt[p] = max(2, ceil(total/step) + 1) like the
+ *   reference, 0 to copy an instance with fewer than 2 points, -1 for a
+ *   zero-length one (its first point).  total_out = out_off[ninst].
+ * pf_hausdorff_pairs_f64: best_bits[q] = bits of the larger directed squared
+ *   term between instances inst_a[q] and inst_b[q], each max_x min_y
+ *   (dx*dx) + (dy*dy) over their resampled points (scipy cKDTree's 2-D
+ *   arithmetic); the reference's path_hausdorff is its sqrt.  The search over y
+ *   visits the source segments of y's instance (pts/arc/src_off/len/cnt as
+ *   above) and measures only points next to x's projection on the segments
+ *   that can hold the minimum: the exhaustive minimum, bit for bit.
+ *   max_points >= every instance's resampled count. */
+int pf_polyline_arc_f64(const double *pts, const int64_t *src_off, const int64_t *len,
+                        int64_t ninst, double *arc, double *segmin, pf_stream_t stream);
+int pf_polyline_resample_f64(const double *pts, const int64_t *src_off, const int64_t *len,
+                             const double *arc, const int64_t *cnt, const int64_t *out_off,
+                             int64_t ninst, int64_t total_out, double *out, pf_stream_t stream);
+int pf_hausdorff_pairs_f64(const double *pts, const double *arc, const int64_t *src_off,
+                           const int64_t *len, const int64_t *cnt, const double *rp,
+                           const int64_t *out_off, const int64_t *inst_a, const int64_t *inst_b,
+                           int64_t npairs, int64_t max_points, uint64_t *best_bits,
+                           pf_stream_t stream);
+
 /* Fill the (nt,6) barycentric-gradient table of pf_mesh_t.G (mesh->G ignored). */
 int pf_mesh_geometry_f64(const pf_mesh_t *mesh, double *G, pf_stream_t stream);
 

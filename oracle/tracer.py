@@ -224,3 +224,64 @@ def triangle_descent(V, T, areas, bbox_diagonal, vals, target, source, step_cap_
         if isinstance(state, dict):
             return state
     return tr.emit(MAX_STEPS)
+
+
+# ---------------------------------------------------------------------------
+# Path metric (paths.py:326-368): resampling + symmetric Hausdorff distance
+# ---------------------------------------------------------------------------
+
+def resample_polyline(points, step: float) -> np.ndarray:
+    """paths.py:326-340 (np.hypot segments, sequential cumsum, np.linspace,
+    np.interp) — the same numpy calls, so bitwise the reference."""
+    pts = np.asarray(points, dtype=float)
+    if len(pts) < 2:
+        return pts.reshape(-1, 2)
+    d = np.diff(pts, axis=0)
+    seg = np.hypot(d[:, 0], d[:, 1])
+    arc = np.concatenate([[0.0], np.cumsum(seg)])
+    total = arc[-1]
+    if total <= 0:
+        return pts[:1]
+    cnt = max(2, int(np.ceil(total / step)) + 1)
+    s = np.linspace(0.0, total, cnt)
+    return np.column_stack([np.interp(s, arc, pts[:, 0]), np.interp(s, arc, pts[:, 1])])
+
+
+def default_step(pa, pb) -> float:
+    """paths.py:355-363: a quarter of the shortest positive segment, else 1."""
+    segs = []
+    for p in (pa, pb):
+        if len(p) > 1:
+            d = np.diff(p, axis=0)
+            s = np.hypot(d[:, 0], d[:, 1])
+            s = s[s > 0]
+            if len(s):
+                segs.append(s.min())
+    return min(segs) / 4.0 if segs else 1.0
+
+
+def directed_sq(ra, rb) -> float:
+    """max over ra of min over rb of (dx*dx) + (dy*dy): the squared distance in
+    scipy cKDTree's order for 2-D points (sqeuclidean: 0 + dx^2, then + dy^2),
+    brute force instead of the tree (the nearest distance is the same value)."""
+    best = 0.0
+    chunk = max(1, (1 << 22) // max(1, len(rb)))
+    for a in range(0, len(ra), chunk):
+        x = ra[a:a + chunk]
+        dx = x[:, None, 0] - rb[None, :, 0]
+        dy = x[:, None, 1] - rb[None, :, 1]
+        best = max(best, float(((dx * dx) + (dy * dy)).min(axis=1).max()))
+    return best
+
+
+def path_hausdorff(pa, pb, step=None) -> float:
+    """paths.py:343-368 with the cKDTree queries replaced by brute force."""
+    pa = np.asarray(pa, dtype=float)
+    pb = np.asarray(pb, dtype=float)
+    if len(pa) == 0 or len(pb) == 0:
+        raise ValueError("paths must be nonempty")
+    if step is None:
+        step = default_step(pa, pb)
+    ra = resample_polyline(pa, step)
+    rb = resample_polyline(pb, step)
+    return float(np.sqrt(max(directed_sq(ra, rb), directed_sq(rb, ra))))

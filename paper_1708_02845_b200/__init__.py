@@ -12,6 +12,7 @@ from .divergence import (FDivergence, builtin_f, dv_at, dv_field, dv_field_batch
                          dv_pair_sparse, dv_pair_sparse_stats, sparsify)
 from .mesh import TriMesh
 from .paths import (TracedPath, edge_descent, edge_descent_batch, find_local_minima,
+                    path_hausdorff, path_hausdorff_batch, resample_polyline,
                     triangle_descent, triangle_descent_batch, triangle_gradient)
 from .errors import (DivergenceDomainError, InvalidTargetError, NativeError,
                      PathfieldError)
@@ -23,6 +24,8 @@ __all__ = [
     "DEFAULTS", "Settings", "FDivergence", "builtin_f", "dv_at", "dv_field", "dv_field_batch",
     "dv_field_device", "dv_pair", "sparsify", "dv_pair_sparse", "dv_pair_sparse_stats",
     "dv_field_sparse", "TriMesh", "TracedPath", "triangle_descent", "triangle_descent_batch",
-    "triangle_gradient", "edge_descent", "edge_descent_batch", "find_local_minima", "DivergenceDomainError", "InvalidTargetError",
+    "triangle_gradient", "edge_descent", "edge_descent_batch", "find_local_minima",
+    "path_hausdorff", "path_hausdorff_batch", "resample_polyline",
+    "DivergenceDomainError", "InvalidTargetError",
     "NativeError", "PathfieldError", "PoissonKernel", "ScalarField",
 ]

@@ -555,6 +555,224 @@ __global__ void hypot_kernel_batch(const double *x, const double *y, int64_t n, 
   if (i < n) out[i] = np_hypot(x[i], y[i]);
 }
 
+
+// ---------------------------------------------------------------------------
+// Path metric (paths.py:326-368): polyline resampling + Hausdorff distance.
+// A "polyline instance" is one side of one compared pair: its points
+// (pts[src_off .. src_off + len) as (x, y)), the pair's resampling step, and
+// its slice of the resampled output.  Arithmetic follows numpy bit for bit
+// (this file is built with -fmad=false): np.hypot segments, a sequential
+// cumsum, np.linspace (i * step + 0.0, last = total), np.interp (largest j
+// with arc[j] <= s, slope form with its NaN retries), and scipy cKDTree's
+// 2-D squared distance (dx*dx) + (dy*dy).
+
+// Thread per instance: arc lengths (arc[src_off + i]) and the shortest
+// positive segment (segmin, +inf if none) for the default step.
+__global__ void polyline_arc_kernel(const double *__restrict__ pts,
+                                    const int64_t *__restrict__ src_off,
+                                    const int64_t *__restrict__ len, int64_t ninst,
+                                    double *__restrict__ arc, double *__restrict__ segmin) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= ninst) return;
+  const int64_t o = src_off[p], L = len[p];
+  double a = 0.0, mn = __longlong_as_double(0x7ff0000000000000LL);
+  if (L > 0) arc[o] = 0.0;
+  for (int64_t i = 1; i < L; ++i) {
+    const double dx = __dsub_rn(pts[2 * (o + i)], pts[2 * (o + i - 1)]);
+    const double dy = __dsub_rn(pts[2 * (o + i) + 1], pts[2 * (o + i - 1) + 1]);
+    const double sg = np_hypot(dx, dy);
+    if (sg > 0.0 && sg < mn) mn = sg;
+    a = __dadd_rn(a, sg);
+    arc[o + i] = a;
+  }
+  if (segmin) segmin[p] = mn;
+}
+
+// One thread per resampled point; instance found by binary search over the
+// output offsets.  cnt[p] == 0 marks "copy the input" (fewer than 2 points),
+// cnt[p] == -1 "first point only" (zero total length).
+__global__ void polyline_resample_kernel(const double *__restrict__ pts,
+                                         const int64_t *__restrict__ src_off,
+                                         const int64_t *__restrict__ len,
+                                         const double *__restrict__ arc,
+                                         const int64_t *__restrict__ cnt,
+                                         const int64_t *__restrict__ out_off, int64_t ninst,
+                                         double *__restrict__ out) {
+  const int64_t total_out = out_off[ninst];
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total_out;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = ninst;  // largest p with out_off[p] <= g
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (out_off[mid] <= g) lo = mid; else hi = mid;
+    }
+    const int64_t p = lo, i = g - out_off[p], o = src_off[p], L = len[p], c = cnt[p];
+    if (c <= 0) {  // input copied through (len < 2) or its first point (total <= 0)
+      out[2 * g] = pts[2 * (o + i)];
+      out[2 * g + 1] = pts[2 * (o + i) + 1];
+      continue;
+    }
+    const double total = arc[o + L - 1];
+    const int64_t div = c - 1;
+    double s;
+    if (i == c - 1) {
+      s = total;
+    } else {
+      const double step = __ddiv_rn(total, static_cast<double>(div));
+      s = step == 0.0 ? __dmul_rn(__ddiv_rn(static_cast<double>(i), static_cast<double>(div)), total)
+                      : __dmul_rn(static_cast<double>(i), step);
+      s = __dadd_rn(s, 0.0);
+    }
+    // np.interp: j = largest index with arc[j] <= s (s in [arc[0], arc[L-1]])
+    int64_t a = 0, b = L;  // arc[a] <= s < arc[b] (arc[L] = +inf)
+    while (b - a > 1) {
+      const int64_t mid = (a + b) >> 1;
+      if (arc[o + mid] <= s) a = mid; else b = mid;
+    }
+    const int64_t j = a;
+#pragma unroll
+    for (int d = 0; d < 2; ++d) {
+      const double *fp = pts + 2 * o + d;
+      double r;
+      if (j == L - 1 || arc[o + j] == s) {
+        r = fp[2 * j];
+      } else {
+        const double x0 = arc[o + j], x1 = arc[o + j + 1];
+        const double y0 = fp[2 * j], y1 = fp[2 * (j + 1)];
+        const double slope = __ddiv_rn(__dsub_rn(y1, y0), __dsub_rn(x1, x0));
+        r = __dadd_rn(__dmul_rn(slope, __dsub_rn(s, x0)), y0);
+        if (isnan(r)) {
+          r = __dadd_rn(__dmul_rn(slope, __dsub_rn(s, x1)), y1);
+          if (isnan(r) && y0 == y1) r = y0;
+        }
+      }
+      out[2 * g + d] = r;
+    }
+  }
+}
+
+// Directed squared Hausdorff term for (pair, direction) = blockIdx.y: max over
+// the resampled points x of instance X (256 per block) of min over the
+// resampled points y of instance Y of (dx*dx) + (dy*dy), folded into best[pair]
+// with an atomic max on the bits of a non-negative double (order-preserving).
+//
+// The resampled points of Y lie on Y's source polyline at uniform arc spacing
+// h = total / (cnt - 1), so instead of all |Y| points each x visits Y's source
+// segments: the squared distance to segment j is a lower bound for every
+// resampled point on it (less a rounding margin), and along the segment the
+// nearest resampled point is within two indices of x's projection.  Pass 1
+// takes the segment with the smallest bound and evaluates its window; pass 2
+// evaluates the window of every segment whose bound does not exceed that
+// minimum.  Only window points are measured, with the reference's exact
+// arithmetic, so the result is the exhaustive minimum bit for bit.
+constexpr int kHdThreads = 256, kHdTile = 512;
+
+struct HdSeg {
+  double x0, y0, ex, ey, inv_l2, a0, a1, pad;
+};
+
+__device__ __forceinline__ double seg_lower_bound(const HdSeg &g, double px, double py,
+                                                  double &tpar) {
+  double t = ((px - g.x0) * g.ex + (py - g.y0) * g.ey) * g.inv_l2;
+  t = fmin(fmax(t, 0.0), 1.0);
+  tpar = t;
+  const double qx = px - (g.x0 + t * g.ex), qy = py - (g.y0 + t * g.ey);
+  return qx * qx + qy * qy;
+}
+
+__device__ __forceinline__ double window_min(const double *__restrict__ ry, int64_t ny, double h,
+                                             double s_star, double px, double py, double best) {
+  const double fi = rint(s_star / h);
+  int64_t i0 = static_cast<int64_t>(fi) - 2, i1 = static_cast<int64_t>(fi) + 2;
+  if (i0 < 0) i0 = 0;
+  if (i1 > ny - 1) i1 = ny - 1;
+  for (int64_t i = i0; i <= i1; ++i) {
+    const double dx = __dsub_rn(px, ry[2 * i]), dy = __dsub_rn(py, ry[2 * i + 1]);
+    best = fmin(best, __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)));
+  }
+  return best;
+}
+
+__global__ void __launch_bounds__(kHdThreads) hausdorff_kernel(
+    const double *__restrict__ pts, const double *__restrict__ arc,
+    const int64_t *__restrict__ src_off, const int64_t *__restrict__ len,
+    const int64_t *__restrict__ cnt, const double *__restrict__ rp,
+    const int64_t *__restrict__ out_off, const int64_t *__restrict__ inst_a,
+    const int64_t *__restrict__ inst_b, unsigned long long *__restrict__ best_bits) {
+  __shared__ HdSeg segs[kHdTile];
+  const int64_t pair = blockIdx.y >> 1;
+  const bool rev = blockIdx.y & 1;
+  const int64_t ix = rev ? inst_b[pair] : inst_a[pair];
+  const int64_t iy = rev ? inst_a[pair] : inst_b[pair];
+  const int64_t xa = out_off[ix], nx = out_off[ix + 1] - xa;
+  const int64_t ya = out_off[iy], ny = out_off[iy + 1] - ya;
+  const int64_t x0 = static_cast<int64_t>(blockIdx.x) * kHdThreads;
+  if (x0 >= nx) return;
+  const int64_t xi = x0 + threadIdx.x;
+  const bool live = xi < nx;
+  const double px = live ? rp[2 * (xa + xi)] : 0.0, py = live ? rp[2 * (xa + xi) + 1] : 0.0;
+  const double *ry = rp + 2 * ya;
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  double best = inf;
+  const int64_t c = cnt[iy];
+  if (c <= 0) {  // Y is its input copied (< 2 points) or one point: exhaustive
+    for (int64_t i = 0; i < ny; ++i) {
+      const double dx = __dsub_rn(px, ry[2 * i]), dy = __dsub_rn(py, ry[2 * i + 1]);
+      best = fmin(best, __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)));
+    }
+  } else {
+    const int64_t so = src_off[iy], nseg = len[iy] - 1;
+    const double total = arc[so + nseg];
+    const double h = __ddiv_rn(total, static_cast<double>(c - 1));
+    // rounding margin on the bounds: the resampled points sit within a few
+    // ulps of their segment, the bound itself is a few ulps off
+    const double scale = fabs(px) + fabs(py) + 1.0;
+    double lb_min = inf, s_at_min = 0.0;
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int64_t t0 = 0; t0 < nseg; t0 += kHdTile) {
+        const int nt = static_cast<int>(nseg - t0 < kHdTile ? nseg - t0 : kHdTile);
+        __syncthreads();
+        for (int u = threadIdx.x; u < nt; u += kHdThreads) {
+          const int64_t j = so + t0 + u;
+          HdSeg g;
+          g.x0 = pts[2 * j];
+          g.y0 = pts[2 * j + 1];
+          g.ex = pts[2 * j + 2] - g.x0;
+          g.ey = pts[2 * j + 3] - g.y0;
+          const double l2 = g.ex * g.ex + g.ey * g.ey;
+          g.inv_l2 = l2 > 0.0 ? 1.0 / l2 : 0.0;
+          g.a0 = arc[j];
+          g.a1 = arc[j + 1];
+          segs[u] = g;
+        }
+        __syncthreads();
+        if (!live) continue;
+        for (int u = 0; u < nt; ++u) {
+          const HdSeg &g = segs[u];
+          double tpar;
+          const double lb = seg_lower_bound(g, px, py, tpar);
+          const double s_star = g.a0 + tpar * (g.a1 - g.a0);
+          if (pass == 0) {
+            if (lb < lb_min) {
+              lb_min = lb;
+              s_at_min = s_star;
+            }
+          } else {
+            const double d = sqrt(lb) - 1e-12 * scale;
+            if (d <= 0.0 || d * d <= best) best = window_min(ry, ny, h, s_star, px, py, best);
+          }
+        }
+      }
+      if (pass == 0 && live) best = window_min(ry, ny, h, s_at_min, px, py, best);
+    }
+  }
+  double m = live ? best : 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0)
+    atomicMax(best_bits + pair, static_cast<unsigned long long>(__double_as_longlong(m)));
+}
+
 }  // namespace pf
 
 using namespace pf;
@@ -622,6 +840,47 @@ int pf_np_hypot_f64(const double *x, const double *y, int64_t n, double *out,
   hypot_kernel_batch<<<static_cast<unsigned>((n + 255) / 256), 256, 0, as_stream(stream)>>>(
       x, y, n, out);
   return check_launch("np_hypot");
+}
+
+int pf_polyline_arc_f64(const double *pts, const int64_t *src_off, const int64_t *len,
+                        int64_t ninst, double *arc, double *segmin, pf_stream_t stream) {
+  if (ninst <= 0) return 0;
+  if (!pts || !src_off || !len || !arc) return fail(PF_E_ARG, "polyline_arc: null");
+  polyline_arc_kernel<<<static_cast<unsigned>((ninst + 127) / 128), 128, 0, as_stream(stream)>>>(
+      pts, src_off, len, ninst, arc, segmin);
+  return check_launch("polyline_arc");
+}
+
+int pf_polyline_resample_f64(const double *pts, const int64_t *src_off, const int64_t *len,
+                             const double *arc, const int64_t *cnt, const int64_t *out_off,
+                             int64_t ninst, int64_t total_out, double *out, pf_stream_t stream) {
+  if (ninst <= 0 || total_out <= 0) return 0;
+  if (!pts || !src_off || !len || !arc || !cnt || !out_off || !out)
+    return fail(PF_E_ARG, "polyline_resample: null");
+  int64_t blocks = (total_out + 255) / 256;
+  if (blocks > static_cast<int64_t>(sm_count()) * 32) blocks = static_cast<int64_t>(sm_count()) * 32;
+  polyline_resample_kernel<<<static_cast<unsigned>(blocks), 256, 0, as_stream(stream)>>>(
+      pts, src_off, len, arc, cnt, out_off, ninst, out);
+  return check_launch("polyline_resample");
+}
+
+int pf_hausdorff_pairs_f64(const double *pts, const double *arc, const int64_t *src_off,
+                           const int64_t *len, const int64_t *cnt, const double *rp,
+                           const int64_t *out_off, const int64_t *inst_a, const int64_t *inst_b,
+                           int64_t npairs, int64_t max_points, uint64_t *best_bits,
+                           pf_stream_t stream) {
+  if (npairs <= 0 || max_points <= 0) return 0;
+  if (!pts || !arc || !src_off || !len || !cnt || !rp || !out_off || !inst_a || !inst_b ||
+      !best_bits)
+    return fail(PF_E_ARG, "hausdorff_pairs: null");
+  if (2 * npairs > 65535) return fail(PF_E_DOMAIN, "hausdorff_pairs: at most 32767 pairs per call");
+  cudaMemsetAsync(best_bits, 0, npairs * sizeof(uint64_t), as_stream(stream));
+  dim3 grid(static_cast<unsigned>((max_points + kHdThreads - 1) / kHdThreads),
+            static_cast<unsigned>(2 * npairs));
+  hausdorff_kernel<<<grid, kHdThreads, 0, as_stream(stream)>>>(
+      pts, arc, src_off, len, cnt, rp, out_off, inst_a, inst_b,
+      reinterpret_cast<unsigned long long *>(best_bits));
+  return check_launch("hausdorff_pairs");
 }
 
 }  // extern "C"

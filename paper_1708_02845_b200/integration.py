@@ -10,7 +10,9 @@ so each site is patched explicitly):
                triangle_descent, triangle_gradient}          (__init__.py:4-13)
     pathfield.domain.{dv_field, sparsify, triangle_descent}  (domain.py:17-22)
     pathfield.bench.{dv_at, dv_field, dv_pair_sparse_stats}  (bench.py:25)
-    pathfield.paths.{triangle_descent, triangle_gradient}
+    pathfield.paths.{triangle_descent, triangle_gradient, edge_descent,
+                     find_local_minima, path_hausdorff, resample_polyline}
+    (domain.py also binds edge_descent, find_local_minima, path_hausdorff)
 
 Results are converted to the reference's own dataclasses (``ScalarField``,
 ``TracedPath``), and the reference's ``PoissonKernel`` objects are accepted
@@ -70,6 +72,8 @@ def _wrap(pathfield):
         "edge_descent": lambda mesh, field, source, settings=None: to_path(
             _paths.edge_descent(mesh, field, source, settings or DEFAULTS_)),
         "find_local_minima": _paths.find_local_minima,
+        "path_hausdorff": _paths.path_hausdorff,
+        "resample_polyline": _paths.resample_polyline,
     }
 
 
@@ -77,10 +81,12 @@ SITES = {
     "divergence": ("dv_field", "dv_at", "dv_pair", "sparsify", "dv_pair_sparse",
                    "dv_pair_sparse_stats"),
     "": ("dv_field", "dv_pair", "dv_pair_sparse", "sparsify", "triangle_descent",
-         "triangle_gradient", "edge_descent", "find_local_minima"),
-    "domain": ("dv_field", "sparsify", "triangle_descent", "edge_descent", "find_local_minima"),
+         "triangle_gradient", "edge_descent", "find_local_minima", "path_hausdorff"),
+    "domain": ("dv_field", "sparsify", "triangle_descent", "edge_descent", "find_local_minima",
+               "path_hausdorff"),
     "bench": ("dv_at", "dv_field", "dv_pair_sparse_stats"),
-    "paths": ("triangle_descent", "triangle_gradient", "edge_descent", "find_local_minima"),
+    "paths": ("triangle_descent", "triangle_gradient", "edge_descent", "find_local_minima",
+              "path_hausdorff", "resample_polyline"),
 }
 
 

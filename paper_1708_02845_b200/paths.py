@@ -293,3 +293,141 @@ def np_hypot_device(x, y) -> np.ndarray:
     nat.call("pf_np_hypot_f64", xd.data_ptr(), yd.data_ptr(), xd.numel(), out.data_ptr(),
              t.cuda.current_stream().cuda_stream)
     return out.cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# Path metric (paths.py:326-368)
+# ---------------------------------------------------------------------------
+
+_MAX_RESAMPLED = 1 << 31  # resampled points per call (16 B each on the device)
+
+
+def _points_of(x) -> np.ndarray:
+    """paths.py:352-353: a TracedPath's points, else the array as float."""
+    pts = x.points if hasattr(x, "points") and hasattr(x, "locations") else x
+    return np.asarray(pts, dtype=float)
+
+
+def _resample_device(sources):
+    """Upload the source polylines and run the arc-length kernel: returns the
+    device points and arcs, host offsets / lengths / totals / shortest
+    positive segments."""
+    t = dev.require_cuda()
+    device = t.device("cuda", t.cuda.current_device())
+    s = t.cuda.current_stream(device).cuda_stream
+    lens = np.array([len(p) for p in sources], dtype=np.int64)
+    offs = np.zeros(len(sources) + 1, dtype=np.int64)
+    np.cumsum(lens, out=offs[1:])
+    flat = np.concatenate([p.reshape(-1, 2) for p in sources]) if offs[-1] else np.zeros((0, 2))
+    pts = t.from_numpy(np.ascontiguousarray(flat, dtype=np.float64)).to(device)
+    src_off = t.from_numpy(offs[:-1].copy()).to(device)
+    src_len = t.from_numpy(lens).to(device)
+    arc = t.empty(max(int(offs[-1]), 1), dtype=t.float64, device=device)
+    segmin = t.empty(len(sources), dtype=t.float64, device=device)
+    nat.call("pf_polyline_arc_f64", pts.data_ptr(), src_off.data_ptr(), src_len.data_ptr(),
+             len(sources), arc.data_ptr(), segmin.data_ptr(), s)
+    arc_h = arc.cpu().numpy()
+    seg_h = segmin.cpu().numpy()
+    totals = np.array([arc_h[offs[i] + lens[i] - 1] if lens[i] else 0.0
+                       for i in range(len(sources))])
+    return t, device, s, pts, arc, offs, lens, totals, seg_h
+
+
+def _counts(lens, totals, inst_src, inst_step):
+    """Resampled point count per instance exactly as paths.py:327-339 decides it
+    (0: copied input, -1: first point only) and the number of output points."""
+    cnt = np.empty(len(inst_src), dtype=np.int64)
+    nout = np.empty(len(inst_src), dtype=np.int64)
+    for q, (si, st) in enumerate(zip(inst_src, inst_step)):
+        L, total = int(lens[si]), float(totals[si])
+        if L < 2:
+            cnt[q], nout[q] = 0, L
+        elif total <= 0:
+            cnt[q], nout[q] = -1, 1
+        else:
+            c = max(2, int(np.ceil(total / st)) + 1)
+            cnt[q], nout[q] = c, c
+    return cnt, nout
+
+
+def _launch_resample(t, device, s, pts, arc, offs, lens, inst_src, cnt, nout):
+    out_off = np.zeros(len(inst_src) + 1, dtype=np.int64)
+    np.cumsum(nout, out=out_off[1:])
+    total_out = int(out_off[-1])
+    if total_out > _MAX_RESAMPLED:
+        raise MemoryError(f"resampling needs {total_out} points (step too small)")
+    d_src = t.from_numpy(offs[np.asarray(inst_src, dtype=np.int64)].copy()).to(device)
+    d_len = t.from_numpy(lens[np.asarray(inst_src, dtype=np.int64)].copy()).to(device)
+    d_cnt = t.from_numpy(cnt).to(device)
+    d_off = t.from_numpy(out_off).to(device)
+    rp = t.empty((max(total_out, 1), 2), dtype=t.float64, device=device)
+    nat.call("pf_polyline_resample_f64", pts.data_ptr(), d_src.data_ptr(), d_len.data_ptr(),
+             arc.data_ptr(), d_cnt.data_ptr(), d_off.data_ptr(), len(inst_src), total_out,
+             rp.data_ptr(), s)
+    return rp, d_off, out_off, (d_src, d_len, d_cnt)
+
+
+def resample_polyline(points, step: float) -> np.ndarray:
+    """paths.py:326-340 on the device (bitwise the reference's numpy result)."""
+    pts = np.asarray(points, dtype=float)
+    if len(pts) < 2:
+        return pts.reshape(-1, 2)
+    t, device, s, dpts, arc, offs, lens, totals, _ = _resample_device([pts.reshape(-1, 2)])
+    cnt, nout = _counts(lens, totals, [0], [float(step)])
+    rp, _, out_off, _ = _launch_resample(t, device, s, dpts, arc, offs, lens, [0], cnt, nout)
+    return rp[:int(out_off[-1])].cpu().numpy()
+
+
+def path_hausdorff_batch(pairs, step: float | None = None) -> np.ndarray:
+    """``[path_hausdorff(a, b, step) for a, b in pairs]`` in one pass on the device.
+
+    Every pair is resampled with ``step`` (default: a quarter of the shortest
+    positive segment of the pair, paths.py:355-363) and its symmetric
+    Hausdorff distance evaluated exhaustively on the GPU — bitwise the
+    reference's cKDTree result (same squared-distance arithmetic; the nearest
+    point is the nearest point).
+    """
+    pairs = list(pairs)
+    if not pairs:
+        return np.zeros(0)
+    sources, index, inst_src = [], {}, []
+    for a, b in pairs:
+        for x in (a, b):
+            pts = _points_of(x)
+            if len(pts) == 0:
+                raise ValueError("paths must be nonempty")
+            key = id(x)
+            if key not in index:
+                index[key] = len(sources)
+                sources.append(pts.reshape(-1, 2))
+            inst_src.append(index[key])
+    t, device, s, dpts, arc, offs, lens, totals, segmin = _resample_device(sources)
+    inst_step = []
+    for q in range(len(pairs)):
+        if step is None:
+            m = min(segmin[inst_src[2 * q]], segmin[inst_src[2 * q + 1]])
+            st = float(m) / 4.0 if np.isfinite(m) else 1.0
+        else:
+            st = float(step)
+        inst_step += [st, st]
+    cnt, nout = _counts(lens, totals, inst_src, inst_step)
+    rp, d_off, _, (d_src, d_len, d_cnt) = _launch_resample(t, device, s, dpts, arc, offs, lens,
+                                                           inst_src, cnt, nout)
+    res = np.empty(len(pairs))
+    for c0 in range(0, len(pairs), 32767):
+        c1 = min(len(pairs), c0 + 32767)
+        ia = t.arange(2 * c0, 2 * c1, 2, dtype=t.int64, device=device)
+        ib = ia + 1
+        best = t.empty(c1 - c0, dtype=t.int64, device=device)
+        nat.call("pf_hausdorff_pairs_f64", dpts.data_ptr(), arc.data_ptr(), d_src.data_ptr(),
+                 d_len.data_ptr(), d_cnt.data_ptr(), rp.data_ptr(), d_off.data_ptr(),
+                 ia.data_ptr(), ib.data_ptr(), c1 - c0, int(nout[2 * c0:2 * c1].max()),
+                 best.data_ptr(), s)
+        res[c0:c1] = np.sqrt(best.cpu().numpy().view(np.float64))
+    return res
+
+
+def path_hausdorff(a, b, step: float | None = None) -> float:
+    """Symmetric Hausdorff distance between two densely resampled polylines
+    (paths.py:343-368), on the device."""
+    return float(path_hausdorff_batch([(a, b)], step)[0])

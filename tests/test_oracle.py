@@ -1,10 +1,14 @@
 """The CPU oracle is pinned to the reference's own outputs (tests/golden)."""
 
+import json
+from pathlib import Path
+
 import numpy as np
 import pytest
 
 from oracle import divergence as O
 from oracle import inputs as I
+from oracle import tracer as OT
 from tests.conftest import CASES, case, rel_close
 
 GENS = {"kl": {}, "tv": {}, "chi2": {}, "hellinger": {}, "alpha": {"alpha": 0.5},
@@ -147,3 +151,28 @@ def test_sparse_pair_direct_matches_reference():
             ok, err = rel_close([v], [c[f"spfield/{g}"][q]], 1e-14)
             assert ok, (g, q, err)
             assert ops == int(c[f"spops/{g}"][q])
+
+
+def _hd():
+    return np.load(Path(__file__).resolve().parent / "golden" / "hausdorff.npz")
+
+
+def test_oracle_path_hausdorff_pinned():
+    """oracle.tracer.path_hausdorff / resample_polyline == the reference's
+    (paths.py:326-368, cKDTree) on the committed golden vectors, bitwise."""
+    g = _hd()
+    meta = json.loads(str(g["meta"]))
+    for i in range(meta["synthetic"]):
+        st = float(g[f"syn/{i}/step"])
+        st = None if np.isnan(st) else st
+        a, b = g[f"syn/{i}/a"], g[f"syn/{i}/b"]
+        assert OT.path_hausdorff(a, b, st) == float(g[f"syn/{i}/h"]), i
+        assert np.array_equal(OT.resample_polyline(a, 0.01), g[f"syn/{i}/ra"]), i
+    for name in ("c1", "corridor50"):
+        c = case(name)
+        step = meta[name]["step"]
+        for pi in range(meta[name]["npaths"]):
+            pa, pb = c[f"path/kl/{pi}/points"], c[f"path/tv/{pi}/points"]
+            assert OT.path_hausdorff(pa, pb, step) == float(g[f"{name}/step"][pi]), (name, pi)
+        assert np.array_equal(OT.resample_polyline(c["path/kl/0/points"], step),
+                              g[f"{name}/resampled0"])
