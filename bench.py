@@ -137,6 +137,33 @@ def dist_env():
     return ws, rank, local
 
 
+def host_info() -> dict:
+    """CPU model and the numeric library versions the CPU baseline ran on."""
+    import platform
+    info = {"cpu_model": platform.processor() or "unknown", "logical_cpus": os.cpu_count()}
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                info["cpu_model"] = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    import numpy as np
+    info["numpy"] = np.__version__
+    try:
+        import scipy
+        info["scipy"] = scipy.__version__
+    except ImportError:
+        pass
+    try:
+        cfg = np.show_config(mode="dicts")
+        info["blas"] = "{} {}".format(cfg["Build Dependencies"]["blas"].get("name", "?"),
+                                      cfg["Build Dependencies"]["blas"].get("version", ""))
+    except Exception:
+        pass
+    return info
+
+
 def cpu_sample_rows(k: int, rows: int, seed: int):
     import numpy as np
     from oracle.inputs import synthetic_kernel
@@ -197,6 +224,7 @@ def run_reference_arm(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": desc, "rows_per_gpu": n_rows, "k": k},
         "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads, "kind": "port",
+                         "host": host_info(),
                          "sample": sample + "; oracle/divergence.py restating divergence.py:137-187"},
         "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -289,9 +317,13 @@ class DenseStep:
         self.launches += 5
 
 
+NORTH_STAR_HBM_GBS = 8000.0  # BASELINE.json north_star: "~8 TB/s per GPU"
+
+
 def _roof(bytes_, ms, peak):
     ach = bytes_ / (ms / 1e3) / 1e9
     return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+            "frac_of_8tbs": ach / NORTH_STAR_HBM_GBS,
             "algorithmic_bytes_per_launch": bytes_, "avg_launch_ms": ms}
 
 
@@ -735,7 +767,8 @@ def run_native(args):
         v, el = ref.step()
         cpu = {"value": v, "unit": "evals/s", "cores": threads, "kind": "port",
                "sample": ref.sample + f" ({el:.1f} s); oracle/divergence.py restating "
-                                      "pathfield divergence.py:137-187 (numpy)"}
+                                      "pathfield divergence.py:137-187 (numpy)",
+               "host": host_info()}
 
     peak, peak_kind = peaks()
     bytes_kl = rows * (8 * k + 16) + 8 * k

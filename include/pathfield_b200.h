@@ -397,6 +397,22 @@ int pf_hausdorff_pairs_f64(const double *pts, const double *arc, const int64_t *
                            int64_t npairs, int64_t max_points, uint64_t *best_bits,
                            pf_stream_t stream);
 
+/* ---- Wire formats (fileio.py:37-79, service/app.py:95-114; wire.cu) --------
+ * pf_format_lines: line i of `kind` into slots[64*i ..] (lens[i] bytes):
+ *   0 field CSV  f"{index0 + i},{v:.17g}\n"          (fileio.py:37-40)
+ *   1 path CSV   f"{x:.17g},{y:.17g}\n", vals (n,2)   (fileio.py:72-75)
+ *   2 JSON       json.dumps float (repr, NaN/Infinity) + ",\n    " but the last
+ *   3 compact    repr + "," but the last; nonfinite[0] |= 1 on NaN/inf
+ *   4 repr       float.__repr__        5 .17g   format(v, ".17g")
+ * Digits are exact (big-integer dtoa modes 2 / 0, CPython's tie rules) and the
+ * layout is CPython's format_float_short: byte-identical to the reference.
+ * pf_pack_lines: out[offs[i] ..] = the lens[i] bytes of slot i (offs = the
+ * exclusive scan of lens). */
+int pf_format_lines(const double *vals, int64_t n, int kind, int64_t index0, char *slots,
+                    int32_t *lens, uint32_t *nonfinite, pf_stream_t stream);
+int pf_pack_lines(const char *slots, const int32_t *lens, const int64_t *offs, int64_t n,
+                  char *out, pf_stream_t stream);
+
 /* Fill the (nt,6) barycentric-gradient table of pf_mesh_t.G (mesh->G ignored). */
 int pf_mesh_geometry_f64(const pf_mesh_t *mesh, double *G, pf_stream_t stream);
 

@@ -13,6 +13,8 @@ so each site is patched explicitly):
     pathfield.paths.{triangle_descent, triangle_gradient, edge_descent,
                      find_local_minima, path_hausdorff, resample_polyline}
     (domain.py also binds edge_descent, find_local_minima, path_hausdorff)
+    pathfield.fileio.{field_to_csv, field_to_json, path_to_csv}   (fileio.py:37-75)
+    pathfield.service.app.field_to_csv                            (app.py:18, 114)
 
 Results are converted to the reference's own dataclasses (``ScalarField``,
 ``TracedPath``), and the reference's ``PoissonKernel`` objects are accepted
@@ -31,6 +33,7 @@ from __future__ import annotations
 import importlib
 
 from . import divergence as _div
+from . import fileio as _fileio
 from . import paths as _paths
 
 _ORIGINAL: dict = {}
@@ -74,6 +77,9 @@ def _wrap(pathfield):
         "find_local_minima": _paths.find_local_minima,
         "path_hausdorff": _paths.path_hausdorff,
         "resample_polyline": _paths.resample_polyline,
+        "field_to_csv": _fileio.field_to_csv,
+        "field_to_json": _fileio.field_to_json,
+        "path_to_csv": _fileio.path_to_csv,
     }
 
 
@@ -87,6 +93,8 @@ SITES = {
     "bench": ("dv_at", "dv_field", "dv_pair_sparse_stats"),
     "paths": ("triangle_descent", "triangle_gradient", "edge_descent", "find_local_minima",
               "path_hausdorff", "resample_polyline"),
+    "fileio": ("field_to_csv", "field_to_json", "path_to_csv"),
+    "service.app": ("field_to_csv",),
 }
 
 

@@ -26,6 +26,13 @@ elif which == "f32":
     dk = dev.DeviceKernel(None, np.array([], np.int64), device=device, rows=rows, n=rows, k=k,
                           P_dev=P)
     print(bench.extra_f32(t, nat, dev, pf, dk, rows // 3 + 1, 5, peak))
+elif which == "hausdorff":
+    sys.path.insert(0, "tests")
+    from tests.conftest import case
+    c = case("disk40")
+    pairs = [(c[f"path/kl/{pi}/points"], c[f"path/tv/{pi}/points"]) for pi in range(24)]
+    for _ in range(2):
+        print(pf.path_hausdorff_batch(pairs)[:3])
 else:
     rows, k, T = 131072, 4102, 1024
     ld = dev.leading_dim(k)
@@ -41,10 +48,21 @@ else:
     Tc = t.empty((T, ldl), dtype=t.float64, device=device)
     out = t.empty((rows, T), dtype=t.float64, device=device)
     s = t.cuda.current_stream().cuda_stream
+    A, ea, ldk = dk.slices(1e-300)
+    B = t.empty((7, T, ldk), dtype=t.uint8, device=device)
+    eb = t.empty(T, dtype=t.int32, device=device)
     for _ in range(3):
         nat.call("pf_batch_prep_f64", Pt.data_ptr(), Pt.stride(0), T, k, ldl, 1e-300, 0,
                  L.data_ptr(), Tc.data_ptr(), 0, s)
-        nat.call("pf_batched_kl_f64", dk.P.data_ptr(), dk.ld, rows, k, H.data_ptr(), L.data_ptr(),
-                 Tc.data_ptr(), ldl, T, tg.data_ptr(), 1e-300, 1e-3, 0, out.data_ptr(), T, 0, s)
+        if which == "gemm_i8":
+            nat.call("pf_slice_targets_u8", L.data_ptr(), ldl, T, k, ldk, B.data_ptr(),
+                     eb.data_ptr(), 0, s)
+            nat.call("pf_batched_kl_i8", A.data_ptr(), ea.data_ptr(), rows, B.data_ptr(),
+                     eb.data_ptr(), T, k, ldk, H.data_ptr(), tg.data_ptr(), 1e-3, 0,
+                     out.data_ptr(), T, 64, s)
+        else:
+            nat.call("pf_batched_kl_f64", dk.P.data_ptr(), dk.ld, rows, k, H.data_ptr(),
+                     L.data_ptr(), Tc.data_ptr(), ldl, T, tg.data_ptr(), 1e-300, 1e-3, 0,
+                     out.data_ptr(), T, 0, s)
     t.cuda.synchronize()
     print("ok")

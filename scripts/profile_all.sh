@@ -1,6 +1,6 @@
 #!/bin/bash
 # ncu --set full captures of every product kernel family (run under gpurun).
-#   bash scripts/profile_all.sh <tag>
+#   bash scripts/profile_all.sh <tag> [comma list: csr,gemm,gemm_i8,tracer,f32,hausdorff]
 TAG=${1:-r1}
 mkdir -p gpurun_out
 run() {  # name, kernel regex, skip, count, args...
@@ -11,7 +11,11 @@ run() {  # name, kernel regex, skip, count, args...
       > gpurun_out/ncu_${name}_${TAG}.log 2>&1
   echo "$name rc=$?"
 }
-run csr "csr_(kl|tv)_kernel" 6 2 csr
-run gemm "batched_kl_dmma2" 1 1 gemm
-run tracer "trace_kernel" 1 1 tracer
-run f32 "dense32_kernel" 6 2 f32
+ONLY=${2:-csr,gemm,gemm_i8,tracer,f32,hausdorff}
+want() { [[ ",$ONLY," == *",$1,"* ]]; }
+want csr && run csr "csr_(kl|tv)_kernel|csr_kl_fixup_queue" 9 3 csr
+want gemm && run gemm "batched_kl_dmma2" 1 1 gemm
+want gemm_i8 && run gemm_i8 "batched_kl_i8|slice_(rows|targets)" 0 3 gemm_i8
+want tracer && run tracer "trace_kernel" 1 1 tracer
+want f32 && run f32 "dense32_kernel" 6 2 f32
+want hausdorff && run hausdorff "hausdorff_kernel|polyline" 0 3 hausdorff
