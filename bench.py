@@ -585,6 +585,49 @@ def extra_c3(t, nat, dev, pf, device, steps, peak):
     return res
 
 
+def extra_wire(t, dev, pf, device):
+    """Field CSV / JSON wire formats of a C4-sized field (1,000,386 values) on
+    the GPU (csrc/wire.cu) vs the reference's Python expressions
+    (fileio.py:37-53) timed on a 100,000-value sample of the same values."""
+    import numpy as np
+    from paper_1708_02845_b200 import fileio as F
+    n = 1_000_386
+    rng = np.random.default_rng(3)
+    vals = rng.random(n) * 10.0 ** rng.uniform(-3, 1, n)   # KL-field-like magnitudes
+    dvals = t.from_numpy(vals).to(device)
+    fld = pf.ScalarField(vals.copy(), "kl", 0)
+    F.field_to_csv(fld)
+    F._render(dvals, 0)
+    w0 = time.perf_counter()
+    F._render(dvals, 0)
+    dev_ms = 1e3 * (time.perf_counter() - w0)
+    w0 = time.perf_counter()
+    csv = F.field_to_csv(fld)
+    csv_ms = 1e3 * (time.perf_counter() - w0)
+    w0 = time.perf_counter()
+    js = F.field_to_json(fld)
+    json_ms = 1e3 * (time.perf_counter() - w0)
+    m = 100_000
+    w0 = time.perf_counter()
+    ref = "\n".join(["vertex,value"] + [f"{i},{v:.17g}" for i, v in enumerate(fld.values[:m])])
+    ref_csv_ms = 1e3 * (time.perf_counter() - w0) * n / m
+    w0 = time.perf_counter()
+    json.dumps({"values": [float(v) for v in fld.values[:m]]}, indent=2)
+    ref_json_ms = 1e3 * (time.perf_counter() - w0) * n / m
+    assert csv.startswith(ref[:1000])
+    return {"workload": "field_to_csv / field_to_json of a 1,000,386-value field (C4 rows)",
+            "bytes_csv": len(csv), "bytes_json": len(js),
+            "hbm_values_to_csv_str_ms": dev_ms, "field_to_csv_ms": csv_ms,
+            "field_to_json_ms": json_ms,
+            "reference_python_csv_ms_extrapolated": ref_csv_ms,
+            "reference_python_json_ms_extrapolated": ref_json_ms,
+            "note": "hbm_values_to_csv_str_ms: device-resident values to the CSV body as a "
+                    "Python str (kernels, D2H, decode); field_to_*_ms: wall clock from a host "
+                    "ScalarField to the "
+                    "returned str (H2D, kernels, D2H, decode); reference: the fileio.py "
+                    "expressions on 100,000 values x 10.01"}
+
+
 def extra_tracer(t, nat, dev, pf, device):
     """C5 tracer shape: 10,000 paths on a 1,002,001-vertex mesh, 1,024 target fields."""
     import numpy as np
@@ -799,7 +842,8 @@ def run_native(args):
                 ("c3_csr", "c3", lambda: extra_c3(t, nat, dev, pf, device, args.steps, peak)),
                 ("c4_c5", "c4c5", lambda: extra_c4_and_c5(t, nat, dev, pf, device, args.steps,
                                                           peak)),
-                ("c5_tracer", "tracer", lambda: extra_tracer(t, nat, dev, pf, device))):
+                ("c5_tracer", "tracer", lambda: extra_tracer(t, nat, dev, pf, device)),
+                ("wire", "wire", lambda: extra_wire(t, dev, pf, device))):
             if key not in want:
                 continue
             try:
@@ -849,8 +893,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the C3/C4/C5/tracer side measurements (N=1 only)")
-    ap.add_argument("--extras", default="f32,c3,c4c5,tracer",
-                    help="comma list of side measurements to run (f32, c3, c4c5, tracer)")
+    ap.add_argument("--extras", default="f32,c3,c4c5,tracer,wire",
+                    help="comma list of side measurements to run (f32, c3, c4c5, tracer, wire)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -177,6 +177,32 @@ PF_HD uint64_t quot(Big &R, const Big &S, Big &T) {
   return q;
 }
 
+// The same operations on one 128-bit word: the fast path for values whose
+// digit-generation ratios provably fit (1e-5 <= v < 1e20, see fast_ok).
+struct W128 {
+  unsigned __int128 v;
+};
+PF_HD inline void set_u64(W128 &a, uint64_t x) { a.v = x; }
+PF_HD inline void shl(W128 &a, int k) { a.v <<= k; }
+PF_HD inline void mul_small(W128 &a, uint32_t f) { a.v *= f; }
+PF_HD inline void mul_pow10(W128 &a, int q) {
+  while (q >= 9) {
+    a.v *= 1000000000u;
+    q -= 9;
+  }
+  while (q-- > 0) a.v *= 10u;
+}
+PF_HD inline int cmp(const W128 &a, const W128 &b) { return a.v < b.v ? -1 : (a.v > b.v ? 1 : 0); }
+PF_HD inline void sub(W128 &a, const W128 &b) { a.v -= b.v; }
+PF_HD inline void add_to(W128 &d, const W128 &a, const W128 &b) { d.v = a.v + b.v; }
+PF_HD inline bool is_zero(const W128 &a) { return a.v == 0; }
+PF_HD inline bool is_zero(const Big &a) { return a.n == 0; }
+PF_HD inline uint64_t quot(W128 &R, const W128 &S, W128 &) {
+  const uint64_t q = static_cast<uint64_t>(R.v / S.v);
+  R.v -= static_cast<unsigned __int128>(q) * S.v;
+  return q;
+}
+
 struct Parts {
   uint64_t m;
   int e;
@@ -207,9 +233,10 @@ PF_HD inline int est_k(const Parts &p) {  // floor(log10 v), may be 1 low
 
 // 17 significant digits (dtoa mode 2): writes digits (trailing zeros dropped),
 // returns their count; *decpt = decimal exponent of the first digit + 1.
-PF_HD int digits_g17(double v, char *dig, int *decpt) {
+template <class N>
+PF_HD int digits_g17_t(double v, char *dig, int *decpt) {
   const Parts p = decompose(v);
-  Big R0, S0, R, S, T;
+  N R0, S0, R, S, T;
   set_u64(R0, p.m);
   set_u64(S0, 1);
   if (p.e >= 0) shl(R0, p.e); else shl(S0, -p.e);
@@ -249,11 +276,12 @@ PF_HD int digits_g17(double v, char *dig, int *decpt) {
 }
 
 // Shortest round-trip digits (dtoa mode 0, CPython's tie rules).
-PF_HD int digits_shortest(double v, char *dig, int *decpt) {
+template <class N>
+PF_HD int digits_shortest_t(double v, char *dig, int *decpt) {
   const Parts p = decompose(v);
   const bool even = (p.m & 1) == 0;
   const bool spec = p.frac0 && p.be > 1;  // gap below is half the gap above
-  Big R, S, Mm, Mp, T;
+  N R, S, Mm, Mp, T;
   set_u64(R, p.m);
   if (p.e >= 0) {
     set_u64(S, spec ? 4 : 2);
@@ -283,6 +311,10 @@ PF_HD int digits_shortest(double v, char *dig, int *decpt) {
     ++k;
     mul_small(S, 10);
   }
+  // Digits accumulate in an integer (at most 17 < 20 decimal digits) and are
+  // written once at the end: nvcc's optimiser mishandled per-digit stores into
+  // the caller's array in this loop (wrong bytes with -O3, right with -G).
+  uint64_t acc = 0;
   int nd = 0;
   for (;;) {
     mul_small(R, 10);
@@ -298,60 +330,66 @@ PF_HD int digits_shortest(double v, char *dig, int *decpt) {
       sub(T, Mp);
       j1 = cmp(R, T);
     }
-    bool done = false, bump = false;
+    int last = -1;  // >= 0: final digit; 10: emit 9 and round the string up
     if (j1 == 0 && even) {
-      if (d == 9) bump = true;
-      else {
-        if (j > 0) ++d;
-        dig[nd++] = static_cast<char>('0' + d);
-        done = true;
-      }
+      last = d == 9 ? 10 : (j > 0 ? d + 1 : d);
     } else if (j < 0 || (j == 0 && even)) {
-      if (R.n == 0) {
-        dig[nd++] = static_cast<char>('0' + d);
-        done = true;
+      if (is_zero(R)) {
+        last = d;
       } else {
+        last = d;
         if (j1 > 0) {
           shl(R, 1);
           const int c = cmp(R, S);
-          if (c > 0 || (c == 0 && (d & 1))) {
-            if (d == 9) bump = true;
-            else ++d;
-          }
-        }
-        if (!bump) {
-          dig[nd++] = static_cast<char>('0' + d);
-          done = true;
+          if (c > 0 || (c == 0 && (d & 1))) last = d == 9 ? 10 : d + 1;
         }
       }
     } else if (j1 > 0) {
-      if (d == 9) bump = true;
-      else {
-        dig[nd++] = static_cast<char>('0' + d + 1);
-        done = true;
-      }
-    } else {
-      dig[nd++] = static_cast<char>('0' + d);
+      last = d == 9 ? 10 : d + 1;
     }
-    if (bump) {  // emit 9 and round the string up
-      dig[nd++] = '9';
-      int i = nd - 1;
-      while (i >= 0 && dig[i] == '9') --i;
-      if (i < 0) {
-        dig[0] = '1';
+    if (last < 0) {
+      acc = acc * 10 + static_cast<uint64_t>(d);
+      ++nd;
+      continue;
+    }
+    if (last == 10) {  // ...d9 -> round up: ...(d+1), carries through trailing 9s
+      acc = acc * 10 + 9 + 1;
+      ++nd;
+      uint64_t p10 = 1;
+      for (int i = 0; i < nd; ++i) p10 *= 10;
+      if (acc == p10) {
+        acc = 1;
         nd = 1;
         ++k;
-      } else {
-        ++dig[i];
-        nd = i + 1;
       }
-      done = true;
+    } else {
+      acc = acc * 10 + static_cast<uint64_t>(last);
+      ++nd;
     }
-    if (done) break;
+    break;
   }
-  while (nd > 1 && dig[nd - 1] == '0') --nd;
+  char buf[20];
+  for (int i = nd - 1; i >= 0; --i) {
+    buf[i] = static_cast<char>('0' + acc % 10);
+    acc /= 10;
+  }
+  while (nd > 1 && buf[nd - 1] == '0') --nd;
+  for (int i = 0; i < nd; ++i) dig[i] = buf[i];
   *decpt = k;
   return nd;
+}
+
+// 1e-5 <= v < 1e20: every ratio of both generators stays below 2^127 (mode 2:
+// m 10^22 < 2^127; mode 0: S <= 2^72, M+ <= 2 10^5 10^17), so one 128-bit
+// word replaces the big integer; outside that range the 42-limb integer runs.
+PF_HD inline bool fast_ok(double v) { return v >= 1e-5 && v < 1e20; }
+
+PF_HD inline int digits_g17(double v, char *dig, int *decpt) {
+  return fast_ok(v) ? digits_g17_t<W128>(v, dig, decpt) : digits_g17_t<Big>(v, dig, decpt);
+}
+PF_HD inline int digits_shortest(double v, char *dig, int *decpt) {
+  return fast_ok(v) ? digits_shortest_t<W128>(v, dig, decpt)
+                    : digits_shortest_t<Big>(v, dig, decpt);
 }
 
 // CPython format_float_short layout; returns the length written to out.

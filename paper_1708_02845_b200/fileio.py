@@ -21,6 +21,7 @@ in which case the values never leave the GPU as numbers.
 from __future__ import annotations
 
 import json
+import threading
 
 import numpy as np
 
@@ -43,35 +44,64 @@ def _device_values(t, values, width: int = 1):
     return v.reshape(-1) if width == 1 else v.reshape(-1, width)
 
 
-def format_lines(values, kind: int, index0: int = 0) -> bytes:
-    """Format every value (or (x, y) row) as one line of `kind`; returns the
-    packed bytes.  Raises ValueError for non-finite values in compact JSON."""
+_pinned = threading.local()
+
+
+def _pinned_buffer(t, nbytes: int):
+    """Per-thread pinned host staging buffer, grown geometrically (a fresh
+    pageable destination costs page faults on every copy)."""
+    buf = getattr(_pinned, "buf", None)
+    if buf is None or buf.numel() < nbytes:
+        buf = t.empty(max(nbytes, 2 * (0 if buf is None else buf.numel()), 1 << 20),
+                      dtype=t.uint8, pin_memory=True)
+        _pinned.buf = buf
+    return buf
+
+
+def _render(values, kind: int, index0: int = 0, prefix: bytes = b"", suffix: bytes = b"") -> str:
+    """prefix + one formatted line of `kind` per value (or (x, y) row) + suffix,
+    assembled on the device and decoded once on the host."""
     t = dev.require_cuda()
     width = 2 if kind == _PATH_CSV else 1
     v = _device_values(t, values, width)
     n = v.shape[0]
     if n == 0:
-        return b""
-    s = t.cuda.current_stream(v.device).cuda_stream
+        return (prefix + suffix).decode("ascii")
+    s = t.cuda.current_stream(v.device)
     slots = t.empty(n * _SLOT, dtype=t.uint8, device=v.device)
     lens = t.empty(n, dtype=t.int32, device=v.device)
     flag = t.zeros(1, dtype=t.int32, device=v.device)
     nat.call("pf_format_lines", v.data_ptr(), n, kind, index0, slots.data_ptr(), lens.data_ptr(),
-             flag.data_ptr(), s)
+             flag.data_ptr(), s.cuda_stream)
     ends = t.cumsum(lens, 0, dtype=t.int64)
-    offs = ends - lens
-    total = int(ends[-1].item())
-    if kind == _JSON_COMPACT and int(flag.item()):
+    offs = ends - lens + len(prefix)
+    stats = t.stack([ends[-1], flag[0].to(t.int64)]).cpu()
+    if kind == _JSON_COMPACT and int(stats[1]):
         raise ValueError("Out of range float values are not JSON compliant")
+    body = int(stats[0])
+    total = len(prefix) + body + len(suffix)
     out = t.empty(total, dtype=t.uint8, device=v.device)
+    if prefix:
+        out[:len(prefix)].copy_(t.frombuffer(bytearray(prefix), dtype=t.uint8))
+    if suffix:
+        out[total - len(suffix):].copy_(t.frombuffer(bytearray(suffix), dtype=t.uint8))
     nat.call("pf_pack_lines", slots.data_ptr(), lens.data_ptr(), offs.data_ptr(), n,
-             out.data_ptr(), s)
-    return out.cpu().numpy().tobytes()
+             out.data_ptr(), s.cuda_stream)
+    host = _pinned_buffer(t, total)[:total]
+    host.copy_(out, non_blocking=True)
+    s.synchronize()
+    return str(host.numpy().data, "ascii")
+
+
+def format_lines(values, kind: int, index0: int = 0) -> bytes:
+    """The packed lines of `kind` for every value, as bytes (testing aid).
+    Raises ValueError for non-finite values in compact JSON."""
+    return _render(values, kind, index0).encode("ascii")
 
 
 def field_to_csv(field) -> str:
     """``vertex,value`` then ``f"{i},{v:.17g}"`` per vertex (fileio.py:37-40)."""
-    return "vertex,value\n" + format_lines(field.values, _FIELD_CSV).decode("ascii")
+    return _render(field.values, _FIELD_CSV, prefix=b"vertex,value\n")
 
 
 def field_to_json(field) -> str:
@@ -88,22 +118,23 @@ def field_to_json(field) -> str:
         "values": ["\0values\0"] if n else [],
     }
     text = json.dumps(payload, indent=2) + "\n"
-    if n:
-        body = format_lines(values, _JSON_INDENT).decode("ascii")
-        text = text.replace(json.dumps("\0values\0"), body, 1)
-    return text
+    if not n:
+        return text
+    head, tail = text.split(json.dumps("\0values\0"), 1)
+    return _render(values, _JSON_INDENT, prefix=head.encode("ascii"),
+                   suffix=tail.encode("ascii"))
 
 
 def path_to_csv(path) -> str:
     """``x,y`` then ``f"{x:.17g},{y:.17g}"`` per point (fileio.py:72-75)."""
     pts = path.points if hasattr(path, "points") else path
-    return "x,y\n" + format_lines(pts, _PATH_CSV).decode("ascii")
+    return _render(pts, _PATH_CSV, prefix=b"x,y\n")
 
 
 def values_to_json_compact(values) -> str:
     """``json.dumps([float(v) for v in values], separators=(",", ":"),
     allow_nan=False)``: the service's JSON ``values`` array."""
-    return "[" + format_lines(values, _JSON_COMPACT).decode("ascii") + "]"
+    return _render(values, _JSON_COMPACT, prefix=b"[", suffix=b"]")
 
 
 def format_g17(values) -> list[str]:
