@@ -335,6 +335,11 @@ typedef struct {
    * G20,G21) = paths.py:105-110 bit for bit; built by pf_mesh_geometry_f64.
    * NULL: recomputed per visit. */
   const double *G;
+  /* optional (nt,16) packed records, one 128-byte line per triangle (vertex
+   * coordinates, the G row, area, vertex ids, tri_nbr; pf_mesh_pack_f64): a
+   * tracer step is then one round trip for the geometry.  NULL: the arrays
+   * above. */
+  const double *pack;
 } pf_mesh_t;
 
 /* Path output: location l of path p is at index p*cap + l:
@@ -412,6 +417,9 @@ int pf_format_lines(const double *vals, int64_t n, int kind, int64_t index0, cha
                     int32_t *lens, uint32_t *nonfinite, pf_stream_t stream);
 int pf_pack_lines(const char *slots, const int32_t *lens, const int64_t *offs, int64_t n,
                   char *out, pf_stream_t stream);
+
+/* Fill the (nt,16) packed triangle records of pf_mesh_t.pack (128-byte aligned). */
+int pf_mesh_pack_f64(const pf_mesh_t *mesh, double *pack, pf_stream_t stream);
 
 /* Fill the (nt,6) barycentric-gradient table of pf_mesh_t.G (mesh->G ignored). */
 int pf_mesh_geometry_f64(const pf_mesh_t *mesh, double *G, pf_stream_t stream);

@@ -79,6 +79,7 @@ _SIGS = {
     "pf_local_minima_f64": [c_vp, c_vp, c_i64, c_vp, c_vp],
     "pf_np_hypot_f64": [c_vp, c_vp, c_i64, c_vp, c_vp],
     "pf_mesh_geometry_f64": [c_vp, c_vp, c_vp],
+    "pf_mesh_pack_f64": [c_vp, c_vp, c_vp],
     "pf_format_lines": [c_vp, c_i64, c_int, c_i64, c_vp, c_vp, c_vp, c_vp],
     "pf_pack_lines": [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp],
     "pf_polyline_arc_f64": [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp],

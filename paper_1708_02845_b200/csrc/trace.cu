@@ -65,7 +65,11 @@ __device__ double np_hypot(double x, double y) {
 // ----------------------------------------------------------- geometry --
 struct Tri {
   int v[3];
-  double G[3][2];  // barycentric gradients (paths.py:105-110)
+  int nbr[3];       // triangle across the edge opposite each slot (-1: none)
+  double G[3][2];   // barycentric gradients (paths.py:105-110)
+  double xy[3][2];  // vertex coordinates
+  double area;
+  double f[3];      // field values at the vertices (set by gradient())
 };
 
 __device__ __forceinline__ void tri_G(const pf_mesh_t &m, int64_t ti, const int v[3],
@@ -83,12 +87,49 @@ __device__ __forceinline__ void tri_G(const pf_mesh_t &m, int64_t ti, const int 
   G[2][1] = __ddiv_rn(__dsub_rn(bx, ax), area2);
 }
 
-// Triangle vertices + barycentric gradients: read from the per-triangle table
-// built once per mesh (pf_mesh_geometry_f64, same arithmetic) when present.
+// Triangle record: with the packed per-triangle table (pf_mesh_pack_f64: one
+// 128-byte line = vertex coordinates, barycentric gradients, area, vertex ids,
+// neighbours) a visit is one round trip; otherwise the separate arrays.  Same
+// values either way (the table is built with the same arithmetic).
 __device__ __forceinline__ void load_tri(const pf_mesh_t &m, int64_t ti, Tri &t) {
+  if (m.pack) {
+    const double2 *r = reinterpret_cast<const double2 *>(m.pack + 16 * ti);
+    double2 q[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) q[u] = __ldg(r + u);
+    t.xy[0][0] = q[0].x;
+    t.xy[0][1] = q[0].y;
+    t.xy[1][0] = q[1].x;
+    t.xy[1][1] = q[1].y;
+    t.xy[2][0] = q[2].x;
+    t.xy[2][1] = q[2].y;
+    t.G[0][0] = q[3].x;
+    t.G[0][1] = q[3].y;
+    t.G[1][0] = q[4].x;
+    t.G[1][1] = q[4].y;
+    t.G[2][0] = q[5].x;
+    t.G[2][1] = q[5].y;
+    t.area = q[6].x;
+    const long long w0 = __double_as_longlong(q[6].y), w1 = __double_as_longlong(q[7].x),
+                    w2 = __double_as_longlong(q[7].y);
+    t.v[0] = static_cast<int>(w0 & 0xffffffffLL);
+    t.v[1] = static_cast<int>(w0 >> 32);
+    t.v[2] = static_cast<int>(w1 & 0xffffffffLL);
+    t.nbr[0] = static_cast<int>(w1 >> 32);
+    t.nbr[1] = static_cast<int>(w2 & 0xffffffffLL);
+    t.nbr[2] = static_cast<int>(w2 >> 32);
+    return;
+  }
   t.v[0] = m.triangles[3 * ti + 0];
   t.v[1] = m.triangles[3 * ti + 1];
   t.v[2] = m.triangles[3 * ti + 2];
+#pragma unroll
+  for (int s = 0; s < 3; ++s) {
+    t.nbr[s] = m.tri_nbr[3 * ti + s];
+    t.xy[s][0] = m.vertices[2 * t.v[s]];
+    t.xy[s][1] = m.vertices[2 * t.v[s] + 1];
+  }
+  t.area = m.areas[ti];
   if (m.G) {
     const double2 *g = reinterpret_cast<const double2 *>(m.G + 6 * ti);
     const double2 g0 = g[0], g1 = g[1], g2 = g[2];
@@ -104,8 +145,11 @@ __device__ __forceinline__ void load_tri(const pf_mesh_t &m, int64_t ti, Tri &t)
 }
 
 // f @ G  (3,)@(3,2): fma(f2,G2j, fma(f1,G1j, f0*G0j))
-__device__ __forceinline__ void gradient(const Tri &t, const double *vals, double g[2]) {
+__device__ __forceinline__ void gradient(Tri &t, const double *vals, double g[2]) {
   const double f0 = vals[t.v[0]], f1 = vals[t.v[1]], f2 = vals[t.v[2]];
+  t.f[0] = f0;
+  t.f[1] = f1;
+  t.f[2] = f2;
 #pragma unroll
   for (int j = 0; j < 2; ++j)
     g[j] = __fma_rn(f2, t.G[2][j], __fma_rn(f1, t.G[1][j], __dmul_rn(f0, t.G[0][j])));
@@ -264,10 +308,10 @@ __global__ void __launch_bounds__(kTraceThreads) trace_kernel(pf_mesh_t m, const
     double lam[3], s_exit = INFINITY;
     int slot_exit = -1;
     if (!slide_best) {
-      const double ax = m.vertices[2 * t.v[0]], ay = m.vertices[2 * t.v[0] + 1];
-      const double bx = m.vertices[2 * t.v[1]], by = m.vertices[2 * t.v[1] + 1];
-      const double cx = m.vertices[2 * t.v[2]], cy = m.vertices[2 * t.v[2] + 1];
-      const double area2 = __dmul_rn(2.0, m.areas[ti]);
+      const double ax = t.xy[0][0], ay = t.xy[0][1];
+      const double bx = t.xy[1][0], by = t.xy[1][1];
+      const double cx = t.xy[2][0], cy = t.xy[2][1];
+      const double area2 = __dmul_rn(2.0, t.area);
       // _cross2(u, w) = u0*w1 - u1*w0 (paths.py:124-134)
       const double la = __ddiv_rn(__dsub_rn(__dmul_rn(__dsub_rn(cx, bx), __dsub_rn(x1, by)),
                                             __dmul_rn(__dsub_rn(cy, by), __dsub_rn(x0, bx))),
@@ -298,18 +342,17 @@ __global__ void __launch_bounds__(kTraceThreads) trace_kernel(pf_mesh_t m, const
     }
     if (slide_best) {
       // _slide_to_best_vertex (paths.py:276-282): min by (value, index)
-      int64_t bw = t.v[0];
+      int sb = 0;
 #pragma unroll
-      for (int s = 1; s < 3; ++s) {
-        const int64_t u = t.v[s];
-        if (vals[u] < vals[bw] || (vals[u] == vals[bw] && u < bw)) bw = u;
-      }
-      if (vals[bw] >= cur) {
+      for (int s = 1; s < 3; ++s)
+        if (t.f[s] < t.f[sb] || (t.f[s] == t.f[sb] && t.v[s] < t.v[sb])) sb = s;
+      const int64_t bw = t.v[sb];
+      if (t.f[sb] >= cur) {
         status = ST_STUCK;
         stuck = bw;
         break;
       }
-      w.put(0, bw, -1, 0.0, m.vertices[2 * bw], m.vertices[2 * bw + 1]);
+      w.put(0, bw, -1, 0.0, t.xy[sb][0], t.xy[sb][1]);
       in_tri = false;
       v = bw;
       continue;
@@ -329,7 +372,7 @@ __global__ void __launch_bounds__(kTraceThreads) trace_kernel(pf_mesh_t m, const
     if (le[hi] > 1.0 - 1e-12) {
       // exit through a vertex
       const int64_t wv = t.v[hi];
-      const double wx = m.vertices[2 * wv], wy = m.vertices[2 * wv + 1];
+      const double wx = t.xy[hi][0], wy = t.xy[hi][1];
       if (!(np_hypot(__dsub_rn(wx, w.lx), __dsub_rn(wy, w.ly)) >= eps_prog)) {
         status = ST_STUCK;
         stuck = kNearestPending;  // resolved by nearest_resolve_kernel
@@ -354,12 +397,10 @@ __global__ void __launch_bounds__(kTraceThreads) trace_kernel(pf_mesh_t m, const
     }
     const double tpar = le[o1];
     // lam_exit @ V[tri]  (3,)@(3,2)
-    const double xe0 = __fma_rn(le[2], m.vertices[2 * t.v[2]],
-                                __fma_rn(le[1], m.vertices[2 * t.v[1]],
-                                         __dmul_rn(le[0], m.vertices[2 * t.v[0]])));
-    const double xe1 = __fma_rn(le[2], m.vertices[2 * t.v[2] + 1],
-                                __fma_rn(le[1], m.vertices[2 * t.v[1] + 1],
-                                         __dmul_rn(le[0], m.vertices[2 * t.v[0] + 1])));
+    const double xe0 = __fma_rn(le[2], t.xy[2][0],
+                                __fma_rn(le[1], t.xy[1][0], __dmul_rn(le[0], t.xy[0][0])));
+    const double xe1 = __fma_rn(le[2], t.xy[2][1],
+                                __fma_rn(le[1], t.xy[1][1], __dmul_rn(le[0], t.xy[0][1])));
     if (!(np_hypot(__dsub_rn(xe0, w.lx), __dsub_rn(xe1, w.ly)) >= eps_prog)) {
       status = ST_STUCK;
       stuck = kNearestPending;
@@ -369,14 +410,13 @@ __global__ void __launch_bounds__(kTraceThreads) trace_kernel(pf_mesh_t m, const
     }
     w.put(1, ei, ej, tpar, xe0, xe1);
     // lam_exit @ vals[tri]  (3,)@(3,)
-    const double val_exit = __fma_rn(le[2], vals[t.v[2]],
-                                     __fma_rn(le[1], vals[t.v[1]], __dmul_rn(le[0], vals[t.v[0]])));
+    const double val_exit = __fma_rn(le[2], t.f[2], __fma_rn(le[1], t.f[1], __dmul_rn(le[0], t.f[0])));
     if (target == ei || target == ej) {
       w.put(0, target, -1, 0.0, m.vertices[2 * target], m.vertices[2 * target + 1]);
       status = ST_REACHED;
       break;
     }
-    const int64_t nt = m.tri_nbr[3 * ti + slot_exit];
+    const int64_t nt = t.nbr[slot_exit];
     bool enters = false;
     if (nt >= 0) {
       // _enters (paths.py:256-266); on success its geometry carries into the
@@ -406,15 +446,16 @@ __global__ void __launch_bounds__(kTraceThreads) trace_kernel(pf_mesh_t m, const
     // _slide_along_edge (paths.py:268-274); stuck-vertex reference point is
     // the entry point for a boundary edge, the exit point otherwise.
     const double rx = nt < 0 ? x0 : xe0, ry = nt < 0 ? x1 : xe1;
-    const int64_t sw = (vals[ej] < vals[ei]) ? ej : ei;
-    if (vals[sw] >= val_exit) {
+    const int ssw = (t.f[o1] < t.f[o0]) ? o1 : o0;  // vals[ej] < vals[ei] ? ej : ei
+    const int64_t sw = t.v[ssw];
+    if (t.f[ssw] >= val_exit) {
       status = ST_STUCK;
       stuck = kNearestPending;
       qx = rx;
       qy = ry;
       break;
     }
-    w.put(0, sw, -1, 0.0, m.vertices[2 * sw], m.vertices[2 * sw + 1]);
+    w.put(0, sw, -1, 0.0, t.xy[ssw][0], t.xy[ssw][1]);
     in_tri = false;
     v = sw;
   }
@@ -534,6 +575,33 @@ __global__ void tri_geometry_kernel(pf_mesh_t m, double *G) {
       G[6 * ti + 2 * i] = g[i][0];
       G[6 * ti + 2 * i + 1] = g[i][1];
     }
+  }
+}
+
+// Packed per-triangle records for load_tri (16 doubles = one 128-byte line):
+// xy[3][2], G[3][2] (tri_G arithmetic), area, then int32 v0 v1 | v2 nbr0 | nbr1 nbr2.
+__global__ void tri_pack_kernel(pf_mesh_t m, double *pack) {
+  for (int64_t ti = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ti < m.nt;
+       ti += (int64_t)gridDim.x * blockDim.x) {
+    const int v[3] = {m.triangles[3 * ti], m.triangles[3 * ti + 1], m.triangles[3 * ti + 2]};
+    double g[3][2];
+    tri_G(m, ti, v, g);
+    double *r = pack + 16 * ti;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      r[2 * i] = m.vertices[2 * v[i]];
+      r[2 * i + 1] = m.vertices[2 * v[i] + 1];
+      r[6 + 2 * i] = g[i][0];
+      r[7 + 2 * i] = g[i][1];
+    }
+    r[12] = m.areas[ti];
+    auto pair = [](int lo, int hi) {
+      return __longlong_as_double(static_cast<long long>(static_cast<uint32_t>(lo)) |
+                                  (static_cast<long long>(static_cast<uint32_t>(hi)) << 32));
+    };
+    r[13] = pair(v[0], v[1]);
+    r[14] = pair(v[2], m.tri_nbr[3 * ti]);
+    r[15] = pair(m.tri_nbr[3 * ti + 1], m.tri_nbr[3 * ti + 2]);
   }
 }
 
@@ -831,6 +899,17 @@ int pf_mesh_geometry_f64(const pf_mesh_t *mesh, double *G, pf_stream_t stream) {
   m.G = nullptr;  // compute, do not read
   tri_geometry_kernel<<<sm_count() * 4, 256, 0, as_stream(stream)>>>(m, G);
   return check_launch("mesh_geometry");
+}
+
+int pf_mesh_pack_f64(const pf_mesh_t *mesh, double *pack, pf_stream_t stream) {
+  if (!mesh || !pack) return fail(PF_E_ARG, "mesh_pack: null");
+  if (mesh->nt <= 0) return 0;
+  if (reinterpret_cast<uintptr_t>(pack) & 127) return fail(PF_E_ALIGN, "mesh_pack: 128-byte alignment");
+  pf_mesh_t m = *mesh;
+  m.G = nullptr;
+  m.pack = nullptr;
+  tri_pack_kernel<<<sm_count() * 4, 256, 0, as_stream(stream)>>>(m, pack);
+  return check_launch("mesh_pack");
 }
 
 int pf_np_hypot_f64(const double *x, const double *y, int64_t n, double *out,

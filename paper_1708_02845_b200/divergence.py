@@ -389,11 +389,26 @@ def dv_field_batch_device(pk: PoissonKernel, fd: FDivergence, targets, clamp=Non
             flags[j] = bool(f[0].item()) and c > 0.0
         return out, flags
     if not all(dk.owns(int(p)) for p in targets):
-        raise NotImplementedError("targets outside this slab: use parallel.sharded_field_batch")
-    H = dk.negentropy(c)
-    ldl = dev.round_up(dk.k, 16)
+        raise NotImplementedError("targets outside this slab: use "
+                                  "parallel.ShardedField.field_batch")
     tg = t.from_numpy(targets).to(dk.device)
     Pt = dk.P.index_select(0, tg - dk.row0)
+    return _kl_batch_slab(dk, tg, Pt, c, method, out)
+
+
+def _kl_batch_slab(dk, tg, Pt, c: float, method: str, out=None):
+    """K7 over the rows of slab `dk` for the global targets `tg` (device int64)
+    whose raw rows are `Pt` (T x >=k, device): (values (rows, T), flags (T,)).
+
+    The per-target ``clamped`` flag is exact for this slab's interior rows;
+    over several slabs it is the OR of the slabs' flags."""
+    t = dev.torch()
+    s = t.cuda.current_stream(dk.device)
+    T = int(tg.numel())
+    if out is None:
+        out = t.empty((dk.rows, max(T, 1)), dtype=t.float64, device=dk.device)
+    H = dk.negentropy(c)
+    ldl = dev.round_up(dk.k, 16)
     L = t.empty((T, ldl), dtype=t.float64, device=dk.device)
     Tc = t.empty((T, ldl), dtype=t.float64, device=dk.device)
     tflag = t.zeros(T + 1, dtype=t.int32, device=dk.device)

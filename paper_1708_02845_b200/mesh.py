@@ -186,7 +186,7 @@ class PfMesh(ctypes.Structure):
                 ("vt_ptr", ctypes.c_void_p), ("vt_idx", ctypes.c_void_p),
                 ("nb_ptr", ctypes.c_void_p), ("nb_idx", ctypes.c_void_p),
                 ("n", ctypes.c_int64), ("nt", ctypes.c_int64), ("eps_prog", ctypes.c_double),
-                ("G", ctypes.c_void_p)]
+                ("G", ctypes.c_void_p), ("pack", ctypes.c_void_p)]
 
 
 class DeviceMesh:
@@ -215,13 +215,19 @@ class DeviceMesh:
         self.struct = PfMesh(self.V.data_ptr(), self.T.data_ptr(), self.A.data_ptr(),
                              self.tri_nbr.data_ptr(), self.vt_ptr.data_ptr(),
                              self.vt_idx.data_ptr(), self.nb_ptr.data_ptr(),
-                             self.nb_idx.data_ptr(), self.n, self.nt, self.eps_prog, None)
+                             self.nb_idx.data_ptr(), self.n, self.nt, self.eps_prog, None,
+                             None)
         # per-triangle barycentric gradients, computed once on the device with
         # the tracer's own arithmetic (bitwise what it would recompute per visit)
         self.G = t.empty((self.nt, 6), dtype=t.float64, device=self.device)
         nat.call("pf_mesh_geometry_f64", ctypes.addressof(self.struct), self.G.data_ptr(),
                  t.cuda.current_stream(self.device).cuda_stream)
         self.struct.G = self.G.data_ptr()
+        # packed 128-byte triangle records: one round trip per tracer step
+        self.pack = t.empty((self.nt, 16), dtype=t.float64, device=self.device)
+        nat.call("pf_mesh_pack_f64", ctypes.addressof(self.struct), self.pack.data_ptr(),
+                 t.cuda.current_stream(self.device).cuda_stream)
+        self.struct.pack = self.pack.data_ptr()
 
 
 _cache: dict[int, tuple[weakref.ref, DeviceMesh]] = {}

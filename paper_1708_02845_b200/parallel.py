@@ -11,7 +11,15 @@ field.  The data path has exactly two exchanges, both NCCL over NVLink:
 * the finished field slabs are all-gathered (``ncclAllGather``, n FP64)
   only when a tracer on every rank needs the whole field.
 
-There are no reductions.  The host logic (partitioning, ownership,
+Batched targets (K7) come in both layouts the survey
+names: :meth:`ShardedField.field_batch` keeps P row-sharded and assembles
+the T target rows with one all-reduce (each row is its owner's values plus
+zeros: exact), then every rank contracts its slab; :func:`field_batch_by_targets`
+replicates P (32.8 GB at C4 fits one B200) and partitions the targets, with
+no data-path collective at all.
+
+There are no reductions of computed values (the per-target ``clamped``
+flags are OR-ed).  The host logic (partitioning, ownership,
 broadcast/gather orchestration) is backend-agnostic and is exercised with the
 gloo backend on CPU in tests/test_parallel.py; the slab computation itself is
 always the CUDA kernels (``_compute_slab``).
@@ -118,6 +126,61 @@ class ShardedField:
         vals = _compute_sparse_slab(self.slab, fd, p, payload, cut, thr == 0)
         return self.gather(vals) if gather else vals
 
+    def target_rows(self, targets, k: int):
+        """Rows P[targets, :k] on every rank: each rank fills the rows it owns and
+        one all-reduce (sum) assembles them — exact, every other addend is 0."""
+        t = dev.torch()
+        targets = np.asarray(targets, dtype=np.int64).reshape(-1)
+        rows = t.zeros((targets.size, k), dtype=t.float64, device=self.device)
+        a, b = self.bounds[self.rank]
+        mine = np.flatnonzero((targets >= a) & (targets < b))
+        if mine.size:
+            idx = t.from_numpy(targets[mine] - a).to(self.slab.P.device)
+            rows[t.from_numpy(mine).to(rows.device)] = self.slab.P.index_select(0, idx)[:, :k].to(
+                rows.device)
+        self.dist.all_reduce(rows)
+        return rows
+
+    def field_batch(self, fd, targets, gather: bool = False, method: str = "auto",
+                    clamp=None):
+        """This rank's rows of the fields to T targets (rows x T, device) and the
+        per-target ``clamped`` flags; all ranks' rows (n x T) if `gather`.
+
+        KL runs K7 on the slab against the all-reduced target rows (SURVEY §8e
+        item 3, row-sharded variant); the result is bitwise the single-GPU one.
+        Other generators are T single-target :meth:`field` calls."""
+        t = dev.torch()
+        targets = np.asarray(targets, dtype=np.int64).reshape(-1)
+        n = self.bounds[-1][1]
+        if targets.size and (targets.min() < 0 or targets.max() >= n):
+            from .errors import InvalidTargetError
+            raise InvalidTargetError("target out of range")
+        if fd.name != "kl":
+            cols = [self.field(fd, int(p), clamp=clamp) for p in targets]
+            vals = t.stack(cols, dim=1) if cols else t.zeros((self.slab.rows, 0), dtype=t.float64)
+            flags = np.zeros(targets.size, dtype=bool)
+        else:
+            rows = self.target_rows(targets, self.slab.k)
+            vals, flags = _compute_batch_slab(self.slab, fd, targets, rows, method, clamp)
+            f = t.from_numpy(np.asarray(flags, dtype=np.int32)).to(self.device)
+            self.dist.all_reduce(f, op=self.dist.ReduceOp.MAX)
+            flags = f.cpu().numpy().astype(bool)
+        if not gather:
+            return vals, flags
+        return self.gather_rows(vals), flags
+
+    def gather_rows(self, vals):
+        """All-gather variable-size (rows x T) slabs into the (n x T) matrix."""
+        t = dev.torch()
+        T = vals.shape[1]
+        sizes = [b - a for a, b in self.bounds]
+        m = max(sizes)
+        buf = t.zeros((m, T), dtype=vals.dtype, device=vals.device)
+        buf[:vals.shape[0]] = vals
+        parts = [t.empty((m, T), dtype=vals.dtype, device=vals.device) for _ in range(self.world)]
+        self.dist.all_gather(parts, buf)
+        return t.cat([parts[r][:sizes[r]] for r in range(self.world)])
+
     def gather(self, vals):
         """All-gather variable-size slabs into the full n-vector on every rank."""
         t = dev.torch()
@@ -128,6 +191,51 @@ class ShardedField:
         parts = [t.empty(m, dtype=vals.dtype, device=vals.device) for _ in range(self.world)]
         self.dist.all_gather(parts, buf)
         return t.cat([parts[r][:sizes[r]] for r in range(self.world)])
+
+
+def field_batch_by_targets(pk, fd, targets, dist, gather: bool = False, method: str = "auto",
+                           clamp=None):
+    """Fields to T targets with the targets partitioned over the ranks and P
+    replicated on every GPU (recommended: C5's 32.8 GB P
+    fits each B200): rank r computes the n x T_r columns of its contiguous
+    target chunk with K7 — no data-path collective.  Returns (this rank's
+    columns (n x T_r, device), its flags, its target chunk), or with `gather`
+    the full (n x T) matrix and flags on every rank."""
+    t = dev.torch()
+    targets = np.asarray(targets, dtype=np.int64).reshape(-1)
+    world, rank = dist.get_world_size(), dist.get_rank()
+    chunks = partition_rows(targets.size, world)
+    a, b = chunks[rank]
+    vals, flags = _local_batch(pk, fd, targets[a:b], clamp, method)
+    if not gather:
+        return vals, flags, targets[a:b]
+    n = vals.shape[0]
+    m = max(e - s for s, e in chunks)
+    buf = t.zeros((m, n), dtype=vals.dtype, device=vals.device)
+    buf[:b - a] = vals.t()
+    parts = [t.empty((m, n), dtype=vals.dtype, device=vals.device) for _ in range(world)]
+    dist.all_gather(parts, buf)
+    fl = t.zeros(m, dtype=t.int32, device=vals.device)
+    fl[:b - a] = t.from_numpy(np.asarray(flags, dtype=np.int32)).to(vals.device)
+    fparts = [t.empty(m, dtype=t.int32, device=vals.device) for _ in range(world)]
+    dist.all_gather(fparts, fl)
+    full = t.cat([parts[r][:e - s] for r, (s, e) in enumerate(chunks)]).t()
+    fall = t.cat([fparts[r][:e - s] for r, (s, e) in enumerate(chunks)]).cpu().numpy()
+    return full, fall.astype(bool), targets
+
+
+def _local_batch(pk, fd, targets, clamp, method):
+    from .divergence import dv_field_batch_device
+    return dv_field_batch_device(pk, fd, targets, clamp=clamp, method=method)
+
+
+def _compute_batch_slab(slab, fd, targets, rows, method="auto", clamp=None):
+    """K7 on the slab for the global targets with their rows `rows` (T x k)."""
+    from .divergence import _effective_clamp, _kl_batch_slab
+    t = dev.require_cuda()
+    c = _effective_clamp(slab, fd.clamp if clamp is None else clamp)
+    tg = t.from_numpy(np.asarray(targets, dtype=np.int64)).to(slab.device)
+    return _kl_batch_slab(slab, tg, rows, c, method)
 
 
 def _compute_slab(slab, fd, p: int, target_row, clamp=None):

@@ -115,3 +115,29 @@ def test_i8_fp32_grade_within_north_star_tolerance(name):
         assert ok, (name, j, err)
         assert got[t, j] == 0.0
         assert bool(flags[j]) == bool(c[f"flags/kl/{j}"])
+
+
+@pytest.mark.parametrize("method", METHODS)
+def test_batch_slabs_bitwise_and_flags_or(method):
+    """Row-sharded K7 (parallel.ShardedField.field_batch): each slab contracted
+    against the assembled target rows, as N GPUs would, is bitwise the
+    single-GPU batch, and the OR of the slab flags is the reference's flag."""
+    import torch
+    from paper_1708_02845_b200 import _device as dev
+    from paper_1708_02845_b200 import parallel as par
+    c = case("holes_fine")
+    pk = pf.PoissonKernel(c.dense, c.boundary, 0.0, 0.0)
+    targets = np.array(c.targets)
+    full, flags = pf.divergence.dv_field_batch_device(pk, pf.builtin_f("kl"), targets,
+                                                      method=method)
+    full = full.cpu().numpy()
+    rows = torch.from_numpy(c.dense[targets].copy()).cuda()
+    parts, fl = [], np.zeros(len(targets), bool)
+    bounds = np.linspace(0, c.n, 4).astype(int)
+    for a, b in zip(bounds[:-1], bounds[1:]):
+        dk = dev.DeviceKernel(c.dense, c.boundary, row0=int(a), rows=int(b - a))
+        vals, f = par._compute_batch_slab(dk, pf.builtin_f("kl"), targets, rows, method)
+        parts.append(vals.cpu().numpy())
+        fl |= f
+    np.testing.assert_array_equal(np.concatenate(parts), full)
+    np.testing.assert_array_equal(fl, flags)

@@ -107,3 +107,74 @@ def test_sharded_field_gloo(world):
         p.join(timeout=60)
         assert p.exitcode == 0
     assert all(ok for _, _, ok in res), res
+
+
+def _batch_worker(rank, world, port, P, boundary, targets, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import divergence as O
+        import paper_1708_02845_b200 as pf
+        interior = np.ones(P.shape[0], bool)
+        interior[boundary] = False
+        c = 1e-300
+
+        def oracle_batch_slab(slab, fd, tg, rows, method="auto", clamp=None):
+            rows = rows.numpy()
+            Ps = slab.P.numpy()
+            cols, flags = [], []
+            for j, t in enumerate(tg):
+                full = np.vstack([rows[j][None, :], Ps])
+                v = O.dv_at(full, fd.name, 0, np.arange(1, slab.rows + 1))
+                v[np.arange(slab.row0, slab.row0 + slab.rows) == t] = 0.0
+                cols.append(v)
+                inter = interior[slab.row0:slab.row0 + slab.rows]
+                flags.append(bool(np.any((Ps[inter] < c) != (rows[j] < c))))
+            return torch.from_numpy(np.stack(cols, axis=1)), np.array(flags)
+
+        def oracle_local(pk, fd, tg, clamp, method):
+            res = [O.dv_field(P, boundary, fd.name, int(t)) for t in tg]
+            vals = np.stack([r[0] for r in res], axis=1) if res else np.zeros((P.shape[0], 0))
+            return torch.from_numpy(vals), np.array([bool(r[1]) for r in res], bool)
+
+        par._compute_batch_slab = oracle_batch_slab
+        par._local_batch = oracle_local
+        bounds = par.partition_rows(P.shape[0], world)
+        slab = _Slab(P, *bounds[rank])
+        sf = par.ShardedField(slab, bounds, dist, device=torch.device("cpu"))
+        rows = sf.target_rows(targets, P.shape[1]).numpy()
+        q.put((rank, "rows", bool(np.array_equal(rows, P[targets]))))
+        refs = [O.dv_field(P, boundary, "kl", int(t)) for t in targets]
+        ref = np.stack([r[0] for r in refs], axis=1)
+        rflags = np.array([bool(r[1]) for r in refs])
+        full, flags = sf.field_batch(pf.builtin_f("kl"), targets, gather=True)
+        q.put((rank, "rowsharded", bool(np.array_equal(full.numpy(), ref))
+               and bool(np.array_equal(flags, rflags))))
+        full2, flags2, _ = par.field_batch_by_targets(P, pf.builtin_f("kl"), targets, dist,
+                                                      gather=True)
+        q.put((rank, "by-targets", bool(np.array_equal(full2.numpy(), ref))
+               and bool(np.array_equal(flags2, rflags))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_field_batch_gloo(world):
+    from oracle.inputs import synthetic_kernel
+    P = synthetic_kernel(61, 11, seed=10 + world)
+    P[:, 0] = 0.0
+    P[::9, 4] = 0.0          # interior rows with different zero patterns: flags differ by target
+    boundary = np.array([3])
+    targets = np.array([0, 9, 25, 60, 44, 18, 33])   # owners on every rank, odd count
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_batch_worker, args=(r, world, port, P, boundary, targets, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(3 * world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, _, ok in res), res
