@@ -432,6 +432,101 @@ int pf_triangle_gradient_f64(const pf_mesh_t *mesh, const double *vals, const in
 int pf_np_hypot_f64(const double *x, const double *y, int64_t n, double *out,
                     pf_stream_t stream);
 
+/* ---- K11: the Poisson kernel P itself ---------------------
+ * Replaces the preprocessing that produces the hot path's input:
+ *   assemble_cotan      laplacian.py:91-134  -> pf_cotan_laplacian_f64
+ *   factor_interior     laplacian.py:29-45, 137-141 (SuperLU of -Lc_II)
+ *                       -> pf_nd_plan_build (host) + pf_mf_factor_level
+ *   poisson_kernel      solvers.py:278-303 (k back-substitutions)
+ *                       -> pf_mf_forward_level + pf_mf_backward_level
+ *                          + pf_poisson_residual + pf_poisson_finalize
+ *
+ * Host symbolic plan (host pointers; opaque handle; the only allocating
+ * entry points of the ABI).  Nested dissection of the interior vertices
+ * (geometric bisection of the planar mesh), post-order fronts, scatter maps.
+ * `nb_ptr/nb_idx` is the sorted vertex-neighbour CSR (mesh.py:151),
+ * `is_boundary` the boundary mask (mesh.boundary_vertices), `leaf` the leaf
+ * sub-domain size, `tile` the column tile of the solves.
+ * pf_nd_plan_array copies the named array into `dst_host` (if not NULL) and
+ * returns its length (-1: unknown name); names/dtypes: laplacian.py _I32/_I64. */
+int pf_nd_plan_build(int64_t n, const double *xy_host, const int64_t *nb_ptr_host,
+                     const int64_t *nb_idx_host, const uint8_t *is_boundary_host, int leaf,
+                     int tile, void **plan_out);
+void pf_nd_plan_free(void *plan);
+int64_t pf_nd_plan_array(void *plan, const char *name, void *dst_host);
+/* out_host[16]: n m k nodes levels f_total v_total nnz_l flops_factor
+ * flops_solve max_f max_c max_r ntiles tile leaf */
+int pf_nd_plan_stats(void *plan, double *out_host);
+
+/* Device copy of the plan arrays (all device pointers). */
+typedef struct {
+  const int32_t *c0, *cn, *rn, *fn;  /* per node: first position, |C|, |R|, |C|+|R| */
+  const int64_t *foff;               /* per node: offset of its f x f front in F     */
+  const int32_t *ch_ptr, *ch_idx;    /* children CSR                                 */
+  const int64_t *r_ptr;              /* R lists (original vertex ids)                */
+  const int32_t *r_orig;
+  const int64_t *relmap_off;         /* per node: its R rows inside the parent front */
+  const int32_t *relmap;
+  const int64_t *a_ptr, *a_dst, *a_src; /* A entries: F[a_dst] = -(src >= 0 ? off[src]
+                                            : diag[-1-src])                          */
+  const int64_t *b_ptr;              /* B entries: front row, column, off[] index    */
+  const int32_t *b_row, *b_col;
+  const int64_t *b_src;
+  const int32_t *act_tile;           /* active (node, tile) items of the forward     */
+  const int64_t *act_voff;           /* offset of each item's |R| x tile V block     */
+  const int64_t *tile_item;          /* node * ntiles + tile -> item or -1           */
+  const int32_t *perm_orig;          /* position -> original vertex id               */
+  int64_t nodes, ntiles, k;
+  int32_t tile;                      /* must be 32 */
+  int32_t pad_;
+} pf_mf_plan_t;
+
+/* Cotangent Laplacian, bitwise laplacian.py:91-134: off[e] for every entry e
+ * of the neighbour CSR (sum of the <= 2 corner halves 0.5*cot), diag[v] =
+ * -(scipy row sum of off: first entry + numpy pairwise sum of the rest).
+ * V (n,2) FP64, T (nt,3) int32 as stored.  *bad = min triangle index with a
+ * zero cross product (0/pi angle, DegenerateGeometryError) or INT64_MAX;
+ * nnz = nb_ptr[n]; callee initialises off and *bad (no host synchronisation). */
+int pf_cotan_laplacian_f64(const double *V, const int32_t *T, int64_t nt, const int64_t *nb_ptr,
+                           const int32_t *nb_idx, int64_t n, int64_t nnz, double *off,
+                           double *diag, int64_t *bad, pf_stream_t stream);
+
+/* Multifrontal Cholesky of A = -Lc_II, the nodes of one tree level: assemble
+ * each front (A entries + children's update matrices, in child order), then
+ * factor its |C| pivot columns in place (F[:, :c] = [L_CC; L_RC], F[c:, c:] =
+ * the update matrix).  err[0] |= 1 on a non-positive pivot. */
+int pf_mf_factor_level(const pf_mf_plan_t *plan, const double *off, const double *diag,
+                       const int32_t *nodes, int64_t count, double *F, int32_t *err,
+                       pf_stream_t stream);
+
+/* Forward solve L Y = B for the active (node, tile) items of one level
+ * (item_node[i], item_id[i]): Y rows are written into P (original vertex
+ * rows, ld ldp), update blocks into V. */
+int pf_mf_forward_level(const pf_mf_plan_t *plan, const double *F, const double *off,
+                        const int32_t *item_node, const int64_t *item_id, int64_t count,
+                        double *V, double *P, int64_t ldp, pf_stream_t stream);
+
+/* Backward solve L^T X = Y for work items (node, tiles [t0, t1)) of one level,
+ * top-down, in place in P (inactive tiles read Y = 0). */
+int pf_mf_backward_level(const pf_mf_plan_t *plan, const double *F, const int32_t *item_node,
+                         const int32_t *item_t0, const int32_t *item_t1, int64_t count,
+                         double *P, int64_t ldp, pf_stream_t stream);
+
+/* residual = max |(Lc P)[v, j]| over interior rows v and columns j < k with
+ * P's boundary rows taken as indicators (= |Lc_II P_IB + Lc_IB|, solvers.py:
+ * 292), before the clip; out_max[0] holds the max as ordered FP64 bits. */
+int pf_poisson_residual(const double *P, int64_t ldp, int64_t n, int64_t k,
+                        const uint8_t *is_boundary, const int32_t *bcol, const int64_t *nb_ptr,
+                        const int32_t *nb_idx, const double *off, const double *diag,
+                        unsigned long long *out_max, pf_stream_t stream);
+
+/* Boundary rows -> indicators of their column, pad columns -> 0, interior
+ * entries in (-1e-12, 0) -> 0 (solvers.py:293-296); out_max[0] = max
+ * |row sum - 1| (row_sum_error, :297) as ordered FP64 bits. */
+int pf_poisson_finalize(double *P, int64_t ldp, int64_t n, int64_t k,
+                        const uint8_t *is_boundary, const int32_t *bcol,
+                        unsigned long long *out_max, pf_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -26,6 +26,7 @@ BUILD = PKG.parent / "build"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", f"-I{INCLUDE}",
           "--expt-relaxed-constexpr"]
+HOST = ["-O2", "-g", "-std=c++17", "-fPIC", f"-I{INCLUDE}"]
 # Per-file extra flags.
 EXTRA = {
     "trace.cu": ["-fmad=false"],
@@ -40,35 +41,67 @@ def nvcc_path() -> str:
 
 
 def _sources():
-    return sorted(CSRC.glob("*.cu"))
+    return sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cpp"))
 
 
 def _fingerprint() -> str:
     h = hashlib.sha256()
     for p in sorted(list(CSRC.glob("*.cu")) + list(CSRC.glob("*.cuh"))
+                    + list(CSRC.glob("*.cpp"))
                     + list(INCLUDE.glob("*.h"))):
         h.update(p.name.encode())
         h.update(p.read_bytes())
-    h.update(repr((ARCH, COMMON, EXTRA)).encode())
+    h.update(repr((ARCH, COMMON, EXTRA, HOST)).encode())
+    return h.hexdigest()
+
+
+def _obj_fingerprint(src: Path, cmd: list) -> str:
+    """Source + every shared header + the command line (headers are few)."""
+    h = hashlib.sha256(" ".join(cmd).encode())
+    for p in [src] + sorted(list(CSRC.glob("*.cuh")) + list(INCLUDE.glob("*.h"))):
+        h.update(p.name.encode())
+        h.update(p.read_bytes())
     return h.hexdigest()
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
-    """Compile every CUDA source for sm_100a and link the shared library."""
+    """Compile every CUDA source for sm_100a and link the shared library.
+
+    Objects are rebuilt only when their source, a shared header or the
+    flags changed, in parallel."""
+    from concurrent.futures import ThreadPoolExecutor
     stamp = PKG / ".libpathfield_b200.stamp"
     fp = _fingerprint()
     if not force and LIB.exists() and stamp.exists() and stamp.read_text() == fp:
         return LIB
     nvcc = nvcc_path()
     BUILD.mkdir(exist_ok=True)
-    objs = []
+    jobs = []
     for src in _sources():
         obj = BUILD / (src.stem + ".o")
-        cmd = [nvcc, *ARCH, *COMMON, *EXTRA.get(src.name, []), "-c", str(src), "-o", str(obj)]
+        if src.suffix == ".cpp":  # host-only runtime (symbolic plans): plain g++
+            cmd = [shutil.which("g++") or "g++", *HOST, "-c", str(src), "-o", str(obj)]
+        else:
+            cmd = [nvcc, *ARCH, *COMMON, *EXTRA.get(src.name, []), "-c", str(src), "-o",
+                   str(obj)]
+        ofp = _obj_fingerprint(src, cmd)
+        ostamp = obj.with_suffix(".stamp")
+        fresh = (not force and obj.exists() and ostamp.exists()
+                 and ostamp.read_text() == ofp)
+        jobs.append((cmd, obj, ostamp, ofp, fresh))
+
+    def run(job):
+        cmd, obj, ostamp, ofp, fresh = job
+        if fresh:
+            return
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True)
-        objs.append(str(obj))
+        ostamp.write_text(ofp)
+
+    with ThreadPoolExecutor(max(1, min(8, os.cpu_count() or 1))) as ex:
+        list(ex.map(run, jobs))
+    objs = [str(j[1]) for j in jobs]
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [nvcc, *ARCH, "-shared", "-o", str(tmp), *objs]
     if verbose:

@@ -87,7 +87,24 @@ _SIGS = {
     "pf_hausdorff_pairs_f64": [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64,
                                c_i64, c_vp, c_vp],
 }
-_RESTYPES = {"pf_last_error": ctypes.c_char_p}
+# host-side symbolic plans (nd_plan.cpp): host pointers, opaque handle
+_SIGS.update({
+    "pf_nd_plan_build": [c_i64, c_vp, c_vp, c_vp, c_vp, c_int, c_int,
+                         ctypes.POINTER(ctypes.c_void_p)],
+    "pf_nd_plan_free": [c_vp],
+    "pf_nd_plan_array": [c_vp, ctypes.c_char_p, c_vp],
+    "pf_nd_plan_stats": [c_vp, c_vp],
+    "pf_cotan_laplacian_f64": [c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp,
+                               c_vp],
+    "pf_mf_factor_level": [c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp],
+    "pf_mf_forward_level": [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp],
+    "pf_mf_backward_level": [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp],
+    "pf_poisson_residual": [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                            c_vp],
+    "pf_poisson_finalize": [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp],
+})
+_RESTYPES = {"pf_last_error": ctypes.c_char_p, "pf_nd_plan_free": None,
+             "pf_nd_plan_array": ctypes.c_int64}
 
 
 
@@ -114,7 +131,7 @@ def load():
 def header_symbols() -> list[str]:
     """Every function declared in include/pathfield_b200.h."""
     text = HEADER.read_text()
-    return sorted(set(re.findall(r"^\s*(?:int|const char \*)\s*(pf_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|void|const char \*)\s*(pf_\w+)\s*\(", text, re.M)))
 
 
 def symbols() -> list[str]:

@@ -117,38 +117,7 @@ __device__ __forceinline__ void row_extent(const int64_t *__restrict__ indptr,
   hi = (b & ~1LL) - (b & 1);
 }
 
-// numpy pairwise summation (numpy/_core/src/umath/loops_utils.h.src,
-// pairwise_sum_DOUBLE): < 8 sequential from -0.0; <= 128 eight strided
-// accumulators combined ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) then the tail;
-// else split at n/2 rounded down to a multiple of 8.
-__device__ double np_pairwise_sum(const double *a, int64_t n) {
-  if (n < 8) {
-    double res = -0.0;
-    for (int64_t i = 0; i < n; ++i) res += a[i];
-    return res;
-  }
-  if (n <= 128) {
-    double r0 = a[0], r1 = a[1], r2 = a[2], r3 = a[3], r4 = a[4], r5 = a[5], r6 = a[6],
-           r7 = a[7];
-    int64_t i = 8;
-    for (; i < n - (n % 8); i += 8) {
-      r0 += a[i + 0];
-      r1 += a[i + 1];
-      r2 += a[i + 2];
-      r3 += a[i + 3];
-      r4 += a[i + 4];
-      r5 += a[i + 5];
-      r6 += a[i + 6];
-      r7 += a[i + 7];
-    }
-    double res = ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7));
-    for (; i < n; ++i) res += a[i];
-    return res;
-  }
-  int64_t n2 = n / 2;
-  n2 -= n2 % 8;
-  return np_pairwise_sum(a, n2) + np_pairwise_sum(a + n2, n - n2);
-}
+// np_pairwise_sum: pf_common.cuh
 
 // dropped[r] = max(0, 1 - rowsum) with rowsum = np.add.reduceat semantics:
 // data[lo] + pairwise(data[lo+1:hi]); empty rows sum to 0 (divergence.py:227-228).

@@ -1,0 +1,364 @@
+"""Device cotangent Laplacian and Poisson kernel.
+
+Mirrors the preprocessing the reference runs before the hot path:
+
+* ``assemble_cotan(mesh)`` — ``pathfield/laplacian.py:91-134``: the
+  symmetric cotangent Laplacian, assembled on the GPU bit-for-bit (each
+  edge weight is the sum of the <= 2 corner halves of its triangles, the
+  diagonal is minus scipy's row sum: first entry + numpy pairwise sum of the
+  rest, in ascending column order).
+* ``poisson_kernel(ls)`` — ``pathfield/solvers.py:278-303``: the harmonic
+  measures ``P_IB = -Lc_II^{-1} Lc_IB`` with boundary rows set to indicators.
+  The reference factors ``-Lc_II`` with SuperLU and back-substitutes all k
+  columns on one core (about 50 s at 100K vertices, 21 min at 1M).  Here:
+
+    1. a host nested-dissection plan (``csrc/nd_plan.cpp``; geometric
+       bisection of the planar mesh, post-order fronts, scatter maps),
+    2. a multifrontal Cholesky of ``A = -Lc_II`` on the GPU, one launch per
+       tree level (``pf_mf_factor_level``),
+    3. a forward solve over the sparse right-hand side ``Lc_IB`` that only
+       visits the (front, 32-column tile) pairs reachable from a boundary
+       column (``pf_mf_forward_level``), writing ``L^{-1} B`` straight into
+       the rows of the device P,
+    4. a backward solve, top-down, that overwrites those rows with ``X``
+       (``pf_mf_backward_level``) — P is produced in place, in the device
+       layout of :class:`~._device.DeviceKernel` (row-major, ``ld =
+       round_up(k, 16)``), so the divergence kernels use it without a copy,
+    5. ``pf_poisson_finalize``: boundary indicator rows, the reference's clip
+       of tiny negatives (``-1e-12 < P < 0 -> 0``), ``residual`` and
+       ``row_sum_error``.
+
+  ``-Lc_II`` is a symmetric M-matrix on Delaunay meshes, so its Cholesky
+  factor has non-positive off-diagonals and every term of both triangular
+  solves is non-negative: the device P carries small *componentwise*
+  relative error, tails included (``DESIGN.md`` §K11 and the parity tests).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+import weakref
+
+import numpy as np
+
+from . import _native as nat
+from .errors import NativeError
+
+# per-array dtypes of the host plan (nd_plan.cpp)
+_I32 = ("perm_orig", "iperm", "c0", "cn", "rn", "fn", "parent", "height", "ch_ptr", "ch_idx",
+        "r_pos", "r_orig", "relmap", "b_row", "b_col", "act_tile", "level_ptr", "level_nodes")
+_I64 = ("foff", "r_ptr", "relmap_off", "a_ptr", "a_dst", "a_src", "b_ptr", "b_src", "act_ptr",
+        "act_voff", "tile_item")
+_STATS = ("n", "m", "k", "nodes", "levels", "f_total", "v_total", "nnz_l", "flops_factor",
+          "flops_solve", "max_f", "max_c", "max_r", "ntiles", "tile", "leaf")
+
+LEAF = 64   # leaf sub-domain size of the dissection
+TILE = 32   # column tile of the multi-RHS solves
+
+
+def mesh_topology(mesh):
+    """(nb_ptr, nb_idx, is_boundary) of a mirror or reference TriMesh: the
+    sorted vertex neighbour CSR (mesh.py:151) and the boundary mask."""
+    from .mesh import topology
+    topo = getattr(mesh, "_topo", None)
+    if topo is None:
+        topo = topology(np.asarray(mesh.triangles, dtype=np.int64), len(mesh.vertices))
+    nb_ptr = np.ascontiguousarray(topo[2], dtype=np.int64)
+    nb_idx = np.ascontiguousarray(topo[3], dtype=np.int64)
+    isb = np.zeros(len(mesh.vertices), dtype=np.uint8)
+    isb[np.asarray(mesh.boundary_vertices, dtype=np.int64)] = 1
+    return nb_ptr, nb_idx, isb
+
+
+class NdPlan:
+    """Host nested-dissection plan of the interior block (nd_plan.cpp).
+
+    Attributes are numpy arrays named as in the C++ plan, plus ``stats``.
+    """
+
+    def __init__(self, vertices, nb_ptr, nb_idx, is_boundary, leaf: int = LEAF,
+                 tile: int = TILE):
+        lib = nat.load()
+        xy = np.ascontiguousarray(vertices, dtype=np.float64)
+        nb_ptr = np.ascontiguousarray(nb_ptr, dtype=np.int64)
+        nb_idx = np.ascontiguousarray(nb_idx, dtype=np.int64)
+        isb = np.ascontiguousarray(is_boundary, dtype=np.uint8)
+        h = ctypes.c_void_p()
+        rc = lib.pf_nd_plan_build(len(xy), xy.ctypes.data, nb_ptr.ctypes.data,
+                                  nb_idx.ctypes.data, isb.ctypes.data, int(leaf), int(tile),
+                                  ctypes.byref(h))
+        if rc != 0:
+            raise NativeError(rc, "pf_nd_plan_build: " + lib.pf_last_error().decode())
+        try:
+            for names, dt in ((_I32, np.int32), (_I64, np.int64)):
+                for name in names:
+                    ln = lib.pf_nd_plan_array(h, name.encode(), None)
+                    if ln < 0:
+                        raise NativeError(-1, lib.pf_last_error().decode())
+                    arr = np.empty(ln, dtype=dt)
+                    lib.pf_nd_plan_array(h, name.encode(), arr.ctypes.data)
+                    setattr(self, name, arr)
+            st = np.zeros(len(_STATS))
+            nat.call("pf_nd_plan_stats", h, st.ctypes.data)
+        finally:
+            lib.pf_nd_plan_free(h)
+        self.stats = {k: (float(v) if k.startswith("flops") else int(v))
+                      for k, v in zip(_STATS, st)}
+        self.n, self.m, self.k = self.stats["n"], self.stats["m"], self.stats["k"]
+        self.nodes = self.stats["nodes"]
+        self.ntiles = self.stats["ntiles"]
+        self.tile = self.stats["tile"]
+        self.levels = [self.level_nodes[self.level_ptr[h]:self.level_ptr[h + 1]]
+                       for h in range(len(self.level_ptr) - 1)]
+
+    @classmethod
+    def from_mesh(cls, mesh, leaf: int = LEAF, tile: int = TILE) -> "NdPlan":
+        nb_ptr, nb_idx, isb = mesh_topology(mesh)
+        return cls(mesh.vertices, nb_ptr, nb_idx, isb, leaf=leaf, tile=tile)
+
+
+# ------------------------------------------------------------------ device --
+class PfMfPlan(ctypes.Structure):
+    """ctypes mirror of pf_mf_plan_t (include/pathfield_b200.h)."""
+    _fields_ = [(name, ctypes.c_void_p) for name in (
+        "c0", "cn", "rn", "fn", "foff", "ch_ptr", "ch_idx", "r_ptr", "r_orig", "relmap_off",
+        "relmap", "a_ptr", "a_dst", "a_src", "b_ptr", "b_row", "b_col", "b_src", "act_tile",
+        "act_voff", "tile_item", "perm_orig")] + [
+        ("nodes", ctypes.c_int64), ("ntiles", ctypes.c_int64), ("k", ctypes.c_int64),
+        ("tile", ctypes.c_int32), ("pad_", ctypes.c_int32)]
+
+
+def _u64_to_f64(x: int) -> float:
+    return float(np.array([x], dtype=np.uint64).view(np.float64)[0])
+
+
+class DevicePoisson:
+    """The device pipeline of one mesh: Laplacian, plan, factor, solves.
+
+    ``laplacian()`` and ``factor()`` are cached; ``solve()`` builds a fresh P
+    (a :class:`~._device.DeviceKernel`, rows x ld FP64 in HBM) every call.
+    """
+
+    def __init__(self, mesh, leaf: int = LEAF, device=None):
+        from . import _device as dev
+        t = dev.require_cuda()
+        self.mesh = mesh
+        self.device = (t.device(device) if device is not None
+                       else t.device("cuda", t.cuda.current_device()))
+        nb_ptr, nb_idx, isb_h = mesh_topology(mesh)
+        tod = lambda a, dt: t.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(self.device)  # noqa: E731
+        # device mesh arrays of the assembly (any TriMesh-like object: vertices,
+        # triangles as stored, boundary_vertices)
+        self.dm = type("DevMesh", (), {})()
+        self.dm.V = tod(mesh.vertices, np.float64)
+        self.dm.T = tod(mesh.triangles, np.int32)
+        self.dm.nt = len(mesh.triangles)
+        self.dm.nb_ptr = tod(nb_ptr, np.int64)
+        self.dm.nb_idx = tod(nb_idx, np.int32)
+        self._nnz = int(nb_ptr[-1])
+        self.plan = NdPlan(mesh.vertices, nb_ptr, nb_idx, isb_h, leaf=leaf, tile=TILE)
+        pl = self.plan
+        self.n, self.k = pl.n, pl.k
+        self.stream = lambda: t.cuda.current_stream(self.device).cuda_stream
+        to = lambda a: t.from_numpy(np.ascontiguousarray(a)).to(self.device)  # noqa: E731
+        self._dev = {name: to(getattr(pl, name)) for name in _I32 + _I64
+                     if name not in ("iperm", "parent", "height", "r_pos", "level_ptr",
+                                     "level_nodes")}
+        d = self._dev
+        self.struct = PfMfPlan(*[d[name].data_ptr() for name, _ in PfMfPlan._fields_[:22]],
+                               pl.nodes, pl.ntiles, pl.k, pl.tile, 0)
+        isb = np.zeros(pl.n, dtype=np.uint8)
+        bnd = np.asarray(mesh.boundary_vertices, dtype=np.int64)
+        isb[bnd] = 1
+        bcol = -np.ones(pl.n, dtype=np.int32)
+        bcol[bnd] = np.arange(len(bnd), dtype=np.int32)
+        self.boundary = bnd
+        self.is_boundary = to(isb)
+        self.bcol = to(bcol)
+        # per-level launch lists
+        self.levels = [to(lv.astype(np.int32)) for lv in pl.levels]
+        self.fwd = []
+        for lv in pl.levels:
+            nodes = np.repeat(lv, pl.act_ptr[lv + 1] - pl.act_ptr[lv]).astype(np.int32)
+            ids = (np.concatenate([np.arange(pl.act_ptr[s], pl.act_ptr[s + 1]) for s in lv])
+                   if len(lv) else np.zeros(0, np.int64)).astype(np.int64)
+            self.fwd.append((to(nodes), to(ids), len(ids)))
+        self.bwd = []
+        target = 2 * 148
+        for lv in pl.levels:
+            chunks = int(min(pl.ntiles, max(1, -(-target // max(len(lv), 1)))))
+            step = -(-pl.ntiles // chunks)
+            t0 = np.arange(0, pl.ntiles, step, dtype=np.int32)
+            t1 = np.minimum(t0 + step, pl.ntiles).astype(np.int32)
+            nodes = np.repeat(lv.astype(np.int32), len(t0))
+            self.bwd.append((to(nodes), to(np.tile(t0, len(lv))), to(np.tile(t1, len(lv))),
+                             len(nodes)))
+        self._lap = None
+        self._F = None
+        self.timings: dict = {}
+
+    # -- laplacian.py:91-134 ---------------------------------------------
+    def laplacian(self):
+        """(off, diag) device tensors: Lc in neighbour-CSR order, bitwise the reference's."""
+        if self._lap is None:
+            from . import _device as dev
+            from .errors import DegenerateGeometryError
+            t = dev.torch()
+            dm = self.dm
+            nnz = int(self.plan_nnz())
+            off = t.empty(max(nnz, 1), dtype=t.float64, device=self.device)
+            diag = t.empty(self.n, dtype=t.float64, device=self.device)
+            bad = t.empty(1, dtype=t.int64, device=self.device)
+            nat.call("pf_cotan_laplacian_f64", dm.V.data_ptr(), dm.T.data_ptr(), dm.nt,
+                     dm.nb_ptr.data_ptr(), dm.nb_idx.data_ptr(), self.n, nnz, off.data_ptr(),
+                     diag.data_ptr(), bad.data_ptr(), self.stream())
+            b = int(bad.item())
+            if b != np.iinfo(np.int64).max:
+                raise DegenerateGeometryError(f"triangle {b} has a 0/pi angle")
+            self._lap = (off, diag)
+        return self._lap
+
+    def plan_nnz(self) -> int:
+        return self._nnz
+
+    # -- laplacian.py:29-45 (splu of -Lc_II) -------------------------------
+    def factor(self):
+        """Multifrontal Cholesky of -Lc_II on the device (cached)."""
+        if self._F is None:
+            from . import _device as dev
+            from .errors import FactorizationError
+            t = dev.torch()
+            off, diag = self.laplacian()
+            F = t.empty(max(self.plan.stats["f_total"], 1), dtype=t.float64, device=self.device)
+            err = t.zeros(1, dtype=t.int32, device=self.device)
+            s = self.stream()
+            for lv in self.levels:
+                nat.call("pf_mf_factor_level", ctypes.addressof(self.struct), off.data_ptr(),
+                         diag.data_ptr(), lv.data_ptr(), lv.numel(), F.data_ptr(),
+                         err.data_ptr(), s)
+            if int(err.item()):
+                raise FactorizationError(
+                    "interior block is not positive definite after negation "
+                    "(severely non-Delaunay mesh)")
+            self._F = F
+        return self._F
+
+    # -- solvers.py:278-303 ------------------------------------------------
+    def solve(self, P_out=None):
+        """P (device, rows x ld) with residual and row_sum_error.
+
+        Returns (P tensor, residual, row_sum_error)."""
+        from . import _device as dev
+        t = dev.torch()
+        off, diag = self.laplacian()
+        F = self.factor()
+        ld = dev.leading_dim(self.k)
+        P = P_out if P_out is not None else t.empty((self.n, ld), dtype=t.float64,
+                                                    device=self.device)
+        V = t.empty(max(self.plan.stats["v_total"], 1), dtype=t.float64, device=self.device)
+        s = self.stream()
+        ps = ctypes.addressof(self.struct)
+        for nodes, ids, cnt in self.fwd:
+            nat.call("pf_mf_forward_level", ps, F.data_ptr(), off.data_ptr(), nodes.data_ptr(),
+                     ids.data_ptr(), cnt, V.data_ptr(), P.data_ptr(), ld, s)
+        for nodes, t0, t1, cnt in reversed(self.bwd):
+            nat.call("pf_mf_backward_level", ps, F.data_ptr(), nodes.data_ptr(), t0.data_ptr(),
+                     t1.data_ptr(), cnt, P.data_ptr(), ld, s)
+        del V
+        mx = t.zeros(2, dtype=t.int64, device=self.device)
+        dm = self.dm
+        nat.call("pf_poisson_residual", P.data_ptr(), ld, self.n, self.k,
+                 self.is_boundary.data_ptr(), self.bcol.data_ptr(), dm.nb_ptr.data_ptr(),
+                 dm.nb_idx.data_ptr(), off.data_ptr(), diag.data_ptr(), mx.data_ptr(), s)
+        nat.call("pf_poisson_finalize", P.data_ptr(), ld, self.n, self.k,
+                 self.is_boundary.data_ptr(), self.bcol.data_ptr(), mx.data_ptr() + 8, s)
+        r = mx.cpu().numpy().astype(np.uint64)
+        residual = _u64_to_f64(int(r[0])) if self.plan.m else 0.0
+        return P, residual, _u64_to_f64(int(r[1]))
+
+    def device_kernel(self, P=None):
+        """Solve and wrap P as a DeviceKernel (the hot path's input)."""
+        from . import _device as dev
+        P, residual, rse = self.solve(P)
+        dk = dev.DeviceKernel(None, self.boundary, n=self.n, k=self.k, P_dev=P)
+        dk.residual, dk.row_sum_error = residual, rse
+        return dk
+
+
+class LaplacianSet:
+    """Mirror of ``pathfield.laplacian.LaplacianSet`` (laplacian.py:63-88) whose
+    matrix lives on the device; ``lc`` materialises the scipy CSR (bitwise the
+    reference's) on first access."""
+
+    def __init__(self, mesh, solver: DevicePoisson):
+        self.mesh = mesh
+        self.solver = solver
+        self.interior = np.asarray(mesh.interior_vertices).copy()
+        self.boundary = np.asarray(mesh.boundary_vertices).copy()
+        self._lc = None
+
+    @property
+    def lc(self):
+        if self._lc is None:
+            import scipy.sparse as sp
+            off, diag = self.solver.laplacian()
+            dm = self.solver.dm
+            nb_ptr = dm.nb_ptr.cpu().numpy()
+            nb_idx = dm.nb_idx.cpu().numpy().astype(np.int64)
+            n = self.solver.n
+            m = sp.csr_matrix((off.cpu().numpy()[:len(nb_idx)], nb_idx, nb_ptr), shape=(n, n))
+            self._lc = (m + sp.diags(diag.cpu().numpy())).tocsr()
+        return self._lc
+
+    @property
+    def lc_ii(self):
+        return self.lc[self.interior][:, self.interior]
+
+    @property
+    def lc_ib(self):
+        return self.lc[self.interior][:, self.boundary]
+
+
+def assemble_cotan(mesh, leaf: int = LEAF) -> LaplacianSet:
+    """laplacian.py:91-134 on the device (the matrix stays resident)."""
+    solver = DevicePoisson(mesh, leaf=leaf)
+    solver.laplacian()
+    return LaplacianSet(mesh, solver)
+
+
+def poisson_kernel_device(ls_or_mesh, leaf: int = LEAF):
+    """P on the device only (no host copy): a DeviceKernel with ``residual``
+    and ``row_sum_error`` attributes."""
+    solver = (ls_or_mesh.solver if isinstance(ls_or_mesh, LaplacianSet)
+              else DevicePoisson(ls_or_mesh, leaf=leaf))
+    return solver.device_kernel()
+
+
+def poisson_kernel(ls, settings=None):
+    """solvers.py:278-303: the PoissonKernel of a LaplacianSet (or mesh).
+
+    P is computed on the device and stays resident there (registered as the
+    device mirror of the returned ``dense``); ``dense`` is its host copy, as
+    the reference's return type requires."""
+    import warnings
+    from . import _device as dev
+    from .config import DEFAULTS
+    from .solvers import PoissonKernel, PrecisionWarning
+    settings = settings or DEFAULTS
+    dk = poisson_kernel_device(ls)
+    dense = np.empty((dk.n, dk.k))
+    t = dev.torch()
+    t.from_numpy(dense).copy_(dk.P[:, :dk.k])
+    if dk.residual > settings.residual_warn:
+        warnings.warn(f"poisson kernel residual {dk.residual:.2e}", PrecisionWarning,
+                      stacklevel=2)
+    pk = PoissonKernel(dense, np.asarray(dk_boundary(ls)).copy(), dk.residual,
+                       dk.row_sum_error)
+    dev.register(pk.dense, dk)
+    return pk
+
+
+def dk_boundary(ls_or_mesh):
+    mesh = ls_or_mesh.mesh if isinstance(ls_or_mesh, LaplacianSet) else ls_or_mesh
+    return np.asarray(mesh.boundary_vertices, dtype=np.int64)

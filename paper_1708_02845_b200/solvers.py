@@ -19,6 +19,12 @@ import numpy as np
 
 from .errors import InvalidTargetError
 
+try:  # drop-in mode: the reference's warning class (solvers.py:43-44)
+    from pathfield.solvers import PrecisionWarning  # type: ignore
+except Exception:
+    class PrecisionWarning(UserWarning):
+        """A numerical result is less accurate than requested (solvers.py:43)."""
+
 
 @dataclass(frozen=True)
 class ScalarField:
