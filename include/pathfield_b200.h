@@ -473,11 +473,13 @@ typedef struct {
   const int32_t *b_row, *b_col;
   const int64_t *b_src;
   const int32_t *act_tile;           /* active (node, tile) items of the forward     */
-  const int64_t *act_voff;           /* offset of each item's |R| x tile V block     */
+  const int64_t *act_voff;           /* offset of each item's f x tile block [Y_C; V] */
   const int64_t *tile_item;          /* node * ntiles + tile -> item or -1           */
   const int32_t *perm_orig;          /* position -> original vertex id               */
+  const int64_t *mt_off;             /* per node: Mt (f x round_up(c,16)) offset     */
+  const int64_t *m_off;              /* per node: M = Mt^T (c x round_up(f,16))      */
   int64_t nodes, ntiles, k;
-  int32_t tile;                      /* must be 32 */
+  int32_t tile;                      /* must be 64 */
   int32_t pad_;
 } pf_mf_plan_t;
 
@@ -499,18 +501,35 @@ int pf_mf_factor_level(const pf_mf_plan_t *plan, const double *off, const double
                        const int32_t *nodes, int64_t count, double *F, int32_t *err,
                        pf_stream_t stream);
 
-/* Forward solve L Y = B for the active (node, tile) items of one level
- * (item_node[i], item_id[i]): Y rows are written into P (original vertex
- * rows, ld ldp), update blocks into V. */
-int pf_mf_forward_level(const pf_mf_plan_t *plan, const double *F, const double *off,
-                        const int32_t *item_node, const int64_t *item_id, int64_t count,
-                        double *V, double *P, int64_t ldp, pf_stream_t stream);
+/* Explicit front inverses after the factorisation: Mt = [L_CC^{-1};
+ * -L_RC L_CC^{-1}] (f x c, row stride round_up(c,16)) for items (node, 32
+ * identity columns), then M = Mt^T (c x round_up(f,16)) for `nodes`.  Both
+ * buffers must be zero-initialised (their row pads stay 0).  Non-negative on
+ * M-matrices: the solves below are sums of non-negative products. */
+int pf_mf_inverse(const pf_mf_plan_t *plan, const double *F, const int32_t *item_node,
+                  const int32_t *item_ct, int64_t count, const int32_t *nodes, int64_t nnodes,
+                  double *Mt, double *M, pf_stream_t stream);
 
-/* Backward solve L^T X = Y for work items (node, tiles [t0, t1)) of one level,
- * top-down, in place in P (inactive tiles read Y = 0). */
-int pf_mf_backward_level(const pf_mf_plan_t *plan, const double *F, const int32_t *item_node,
-                         const int32_t *item_t0, const int32_t *item_t1, int64_t count,
-                         double *P, int64_t ldp, pf_stream_t stream);
+/* Forward solve of one level over its active (node, 64-column tile) items:
+ * assemble W = [B_C; 0] + children's V (child order) into Wb at asm_woff,
+ * then the item block O = Mt W_C + [0; W_R] = [Y_C; V] (items x 32-row
+ * blocks g_rb).  O blocks live at plan->act_voff. */
+int pf_mf_forward_level(const pf_mf_plan_t *plan, const double *Mt, const double *off,
+                        const int32_t *asm_node, const int64_t *asm_item, const int64_t *asm_woff,
+                        int64_t n_asm, const int32_t *g_node, const int64_t *g_item,
+                        const int64_t *g_woff, const int32_t *g_rb, int64_t n_gemm, double *Wb,
+                        double *O, pf_stream_t stream);
+
+/* Backward solve of one level (levels top-down): X_C = M [Y_C; X_R] for items
+ * (node, 64-row block of C, 128-column blocks [cb0, cb1)), Y_C from O (zero
+ * for tiles the forward never reached), X_R from P's rows, X_C into P (rows
+ * by original vertex id; ldp a multiple of 64).  max_f / max_ncb bound the
+ * items' front sizes and column-block counts (shared-memory sizing). */
+int pf_mf_backward_level(const pf_mf_plan_t *plan, const double *M, const double *O,
+                         const int32_t *item_node, const int32_t *item_rb,
+                         const int32_t *item_cb0, const int32_t *item_cb1, int64_t count,
+                         int32_t max_f, int32_t max_ncb, double *P, int64_t ldp,
+                         pf_stream_t stream);
 
 /* residual = max |(Lc P)[v, j]| over interior rows v and columns j < k with
  * P's boundary rows taken as indicators (= |Lc_II P_IB + Lc_IB|, solvers.py:

@@ -97,8 +97,11 @@ _SIGS.update({
     "pf_cotan_laplacian_f64": [c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp,
                                c_vp],
     "pf_mf_factor_level": [c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp],
-    "pf_mf_forward_level": [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp],
-    "pf_mf_backward_level": [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp],
+    "pf_mf_inverse": [c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp],
+    "pf_mf_forward_level": [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp,
+                            c_i64, c_vp, c_vp, c_vp],
+    "pf_mf_backward_level": [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_int, c_int,
+                             c_vp, c_i64, c_vp],
     "pf_poisson_residual": [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                             c_vp],
     "pf_poisson_finalize": [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp],

@@ -59,7 +59,7 @@ struct Plan {
   std::vector<int64_t> b_src;
   std::vector<int64_t> act_ptr;
   std::vector<int32_t> act_tile;
-  std::vector<int64_t> act_voff;  // per active (node, tile): offset of its V block
+  std::vector<int64_t> act_voff;  // per active (node, tile): offset of its f x ta block
   std::vector<int64_t> tile_item;  // node*ntiles + tile -> active item index or -1
   std::vector<int32_t> level_ptr, level_nodes;
   int64_t ntiles = 0, f_total = 0, v_total = 0, nnz_l = 0;
@@ -334,7 +334,7 @@ int build_plan(Plan &P, const double *xy, const int64_t *nb_ptr, const int64_t *
       P.act_tile[it] = act[s][i];
       P.act_voff[it] = voff;
       P.tile_item[(size_t)s * P.ntiles + act[s][i]] = it;
-      voff += (int64_t)P.rn[s] * P.ta;
+      voff += (int64_t)P.fn[s] * P.ta;  // [Y_C; V] block of the item
     }
   P.act_voff[P.act_ptr[nn]] = voff;
   P.v_total = voff;

@@ -26,7 +26,7 @@
 namespace pf {
 namespace {
 
-constexpr int kT = 32;        // column tile of the solves (plan.tile)
+constexpr int kT = 32;        // panel / identity tile of the factorisation
 constexpr int kThreads = 256;
 
 // ---------------------------------------------------------------- cotan --
@@ -216,53 +216,36 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-// ------------------------------------------------------- forward solve --
-// One CTA per active (node, tile) item: W = [B_C; 0] + sum of children's V,
-// Y_C = L_CC^{-1} W_C (into P's rows), V = W_R - L_RC Y_C.
+// ------------------------------------------------- explicit inverses --
+// Per front, Mt = [L_CC^{-1}; -L_RC L_CC^{-1}] (f x c, row stride ldc =
+// round_up(c, 2)): the forward solve of the front against the identity.  A
+// = -Lc_II is an M-matrix, so L_CC^{-1} >= 0 and -L_RC L_CC^{-1} >= 0: both
+// solves below become sums of non-negative products (no cancellation, P keeps
+// componentwise accuracy) and need no sequential triangular sweeps.
+// One CTA per (node, 32 identity columns); rows above the tile stay zero.
 __global__ void __launch_bounds__(kThreads)
-    mf_forward_kernel(pf_mf_plan_t p, const double *__restrict__ F,
-                      const double *__restrict__ off, const int32_t *__restrict__ item_node,
-                      const int64_t *__restrict__ item_id, double *V, double *P, int64_t ldp) {
+    mf_inverse_kernel(pf_mf_plan_t p, const double *__restrict__ F,
+                      const int32_t *__restrict__ item_node, const int32_t *__restrict__ item_ct,
+                      double *Mt) {
   __shared__ double D[kT][kT + 1];
   __shared__ double Y[kT][kT + 1];
   const int s = item_node[blockIdx.x];
-  const int64_t it = item_id[blockIdx.x];
-  const int f = p.fn[s], c = p.cn[s], r = p.rn[s];
+  const int f = p.fn[s], c = p.cn[s];
+  const int ldc = (c + 15) & ~15;
+  const int c0 = item_ct[blockIdx.x] * kT;
+  const int w = min(kT, c - c0);
   const double *Fs = F + p.foff[s];
-  const int tile = p.act_tile[it];
-  const int64_t j0 = (int64_t)tile * kT;
-  const int w = (int)min((int64_t)kT, p.k - j0);
-  const int32_t *Cv = p.perm_orig + p.c0[s];
-  double *Vs = V + p.act_voff[it];
+  double *W = Mt + p.mt_off[s] + c0;
   const int tid = threadIdx.x, t = tid % kT, g = tid / kT;
-  auto Wrow = [&](int i) -> double * {
-    return i < c ? P + (int64_t)Cv[i] * ldp + j0 : Vs + (int64_t)(i - c) * kT;
-  };
   for (int i = g; i < f; i += kThreads / kT)
-    if (t < w || i >= c) Wrow(i)[t] = 0.0;
+    if (t < w) W[(int64_t)i * ldc + t] = (i == c0 + t) ? 1.0 : 0.0;
   __syncthreads();
-  for (int64_t e = p.b_ptr[s] + tid; e < p.b_ptr[s + 1]; e += kThreads) {
-    const int64_t col = p.b_col[e] - j0;
-    if (col >= 0 && col < w) Wrow(p.b_row[e])[col] = off[p.b_src[e]];
-  }
-  __syncthreads();
-  for (int q = p.ch_ptr[s]; q < p.ch_ptr[s + 1]; ++q) {
-    const int ch = p.ch_idx[q];
-    const int64_t ic = p.tile_item[(int64_t)ch * p.ntiles + tile];
-    if (ic < 0) continue;
-    const int rc = p.rn[ch];
-    const double *Vc = V + p.act_voff[ic];
-    const int32_t *mp = p.relmap + p.relmap_off[ch];
-    for (int a = g; a < rc; a += kThreads / kT)
-      if (t < w) Wrow(mp[a])[t] += Vc[(int64_t)a * kT + t];
-    __syncthreads();
-  }
-  for (int jb = 0; jb < c; jb += kT) {
+  for (int jb = c0; jb < c; jb += kT) {
     const int nb = min(kT, c - jb);
     for (int idx = tid; idx < kT * kT; idx += kThreads) {
       const int i = idx / kT, j = idx % kT;
       D[i][j] = (i < nb && j <= i) ? Fs[(int64_t)(jb + i) * f + jb + j] : 0.0;
-      Y[i][j] = (i < nb && j < w) ? Wrow(jb + i)[j] : 0.0;
+      Y[i][j] = (i < nb && j < w) ? W[(int64_t)(jb + i) * ldc + j] : 0.0;
     }
     __syncthreads();
     if (tid < kT) {
@@ -274,101 +257,341 @@ __global__ void __launch_bounds__(kThreads)
     }
     __syncthreads();
     for (int i = g; i < nb; i += kThreads / kT)
-      if (t < w) Wrow(jb + i)[t] = Y[i][t];
+      if (t < w) W[(int64_t)(jb + i) * ldc + t] = Y[i][t];
     for (int i = jb + nb + g; i < f; i += kThreads / kT) {
       const double *Lr = Fs + (int64_t)i * f + jb;
       double acc = 0.0;
       for (int l = 0; l < nb; ++l) acc += Lr[l] * Y[l][t];
-      if (t < w || i >= c) Wrow(i)[t] -= acc;
+      if (t < w) W[(int64_t)i * ldc + t] -= acc;
     }
     __syncthreads();
   }
-  (void)r;
+}
+
+// M = Mt^T (c x f, row stride ldf = round_up(f, 2)), one CTA per node.
+__global__ void __launch_bounds__(kThreads)
+    mf_transpose_kernel(pf_mf_plan_t p, const int32_t *__restrict__ nodes,
+                        const double *__restrict__ Mt, double *M) {
+  __shared__ double tile[32][33];
+  const int s = nodes[blockIdx.x];
+  const int f = p.fn[s], c = p.cn[s];
+  const int ldc = (c + 15) & ~15, ldf = (f + 15) & ~15;
+  const double *A = Mt + p.mt_off[s];
+  double *B = M + p.m_off[s];
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
+  for (int l0 = 0; l0 < f; l0 += 32)
+    for (int i0 = 0; i0 < c; i0 += 32) {
+      for (int r = ty; r < 32; r += kThreads / 32)
+        tile[r][tx] = (l0 + r < f && i0 + tx < c) ? A[(int64_t)(l0 + r) * ldc + i0 + tx] : 0.0;
+      __syncthreads();
+      for (int r = ty; r < 32; r += kThreads / 32)
+        if (i0 + r < c && l0 + tx < f) B[(int64_t)(i0 + r) * ldf + l0 + tx] = tile[tx][r];
+      __syncthreads();
+    }
+}
+
+// ---------------------------------------------- gathered GEMM (DMMA) --
+// acc(32 x 64) = A (32 rows, K contiguous per row) x B (K rows of 64 columns),
+// A rows / B rows fetched through accessors (nullptr = zero row): 4 warps as
+// 2 (m) x 2 (n), warp tile 16 x 32 of m8n8k4 FP64 MMAs (SASS DMMA), 16-deep
+// K chunks through a 3-stage cp.async ring.  Column blocks are flattened into
+// the K loop, so the ring never drains between them.
+constexpr int kGT = 128, kGBM = 32, kGBN = 64, kGBK = 16, kGStages = 3;
+// row strides: every half-warp fragment load hits 16 distinct bank pairs
+constexpr int kSA = kGBK + 4, kSB = kGBN + 4;
+constexpr int kStageA = kGBM * kSA, kStageB = kGBK * kSB;
+constexpr int kGemmSmem = kGStages * (kStageA + kStageB) * 8;  // bytes of the ring
+
+// zero-initialised source of "zero rows": one 16-byte chunk per lane (a
+// single shared source address serialises cp.async across the warp)
+__device__ __align__(128) double g_zero[kGBN];
+
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// ncb column blocks x K; arow(i) / brow(cb, l) return row pointers (or
+// nullptr); epi(cb, i, t, v) consumes each finished column block.
+// As / Bs: kGStages x kStageA / kStageB doubles of shared memory.
+template <class ARow, class BRow, class Epi>
+__device__ __forceinline__ void gathered_gemm(double *As_, double *Bs_, int ma, int K, int ncb,
+                                              ARow arow, BRow brow, Epi epi) {
+  double(*As)[kStageA] = reinterpret_cast<double(*)[kStageA]>(As_);
+  double(*Bs)[kStageB] = reinterpret_cast<double(*)[kStageB]>(Bs_);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1, fr = lane >> 2, fc = lane & 3;
+  const int nkt = (K + kGBK - 1) / kGBK;
+  const int total = nkt * ncb;
+  auto issue = [&](int it) {
+    if (it < total) {
+      const int st = it % kGStages, cb = it / nkt, k0 = (it % nkt) * kGBK;
+      double *as = As[st], *bs = Bs[st];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {  // A: 32 rows x 8 chunks of 16 B
+        const int e = tid + kGT * u, r = e >> 3, ch = e & 7;
+        const double *src = r < ma ? arow(r) : nullptr;
+        const bool ok = src != nullptr && k0 + 2 * ch < K;  // row pads are zero
+        cp_async16(as + r * kSA + 2 * ch, ok ? src + k0 + 2 * ch : g_zero + 2 * ch);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {  // B: 16 rows x 32 chunks
+        const int e = tid + kGT * u, r = e >> 5, ch = e & 31;
+        const double *src = (k0 + r < K) ? brow(cb, k0 + r) : nullptr;
+        cp_async16(bs + r * kSB + 2 * ch, (src ? src : g_zero) + 2 * ch);
+      }
+    }
+    cp_commit();
+  };
+  double acc[2][4][2];
+#pragma unroll
+  for (int s = 0; s < kGStages - 1; ++s) issue(s);
+  for (int it = 0; it < total; ++it) {
+    if (it % nkt == 0) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    }
+    cp_wait<kGStages - 2>();
+    __syncthreads();
+    issue(it + kGStages - 1);
+    const int st = it % kGStages;
+    const double *as = As[st] + (wm * 16 + fr) * kSA + fc;
+    const double *bs = Bs[st] + fc * kSB + wn * 32 + fr;
+#pragma unroll
+    for (int ks = 0; ks < kGBK; ks += 4) {
+      double a[2], b[4];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) a[i] = as[8 * i * kSA + ks];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = bs[ks * kSB + 8 * j];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+    if (it % nkt == nkt - 1) {
+      const int cb = it / nkt;
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int q = 0; q < 2; ++q)
+            epi(cb, wm * 16 + 8 * i + fr, wn * 32 + 8 * j + 2 * fc + q, acc[i][j][q]);
+    }
+  }
+  cp_wait<0>();
+}
+
+// ------------------------------------------------------- forward solve --
+// Level items (node, active 64-column tile).  Assemble W = [B_C; 0] + the
+// children's V blocks (child order, one child at a time) into Wb ...
+__global__ void __launch_bounds__(kThreads)
+    mf_fwd_assemble_kernel(pf_mf_plan_t p, const double *__restrict__ off,
+                           const int32_t *__restrict__ item_node,
+                           const int64_t *__restrict__ item_id,
+                           const int64_t *__restrict__ item_woff, const double *__restrict__ O,
+                           double *Wb) {
+  const int s = item_node[blockIdx.x];
+  const int64_t it = item_id[blockIdx.x];
+  const int f = p.fn[s];
+  const int tile = p.act_tile[it];
+  const int64_t j0 = (int64_t)tile * kGBN;
+  double *W = Wb + item_woff[blockIdx.x];
+  const int tid = threadIdx.x;
+  for (int64_t e = tid; e < (int64_t)f * kGBN; e += kThreads) W[e] = 0.0;
+  __syncthreads();
+  for (int64_t e = p.b_ptr[s] + tid; e < p.b_ptr[s + 1]; e += kThreads) {
+    const int64_t col = p.b_col[e] - j0;
+    if (col >= 0 && col < kGBN) W[(int64_t)p.b_row[e] * kGBN + col] = off[p.b_src[e]];
+  }
+  __syncthreads();
+  const int t = tid % kGBN, g = tid / kGBN;
+  for (int q = p.ch_ptr[s]; q < p.ch_ptr[s + 1]; ++q) {
+    const int ch = p.ch_idx[q];
+    const int64_t ic = p.tile_item[(int64_t)ch * p.ntiles + tile];
+    if (ic < 0) continue;
+    const int rc = p.rn[ch], cc = p.cn[ch];
+    const double *Vc = O + p.act_voff[ic] + (int64_t)cc * kGBN;
+    const int32_t *mp = p.relmap + p.relmap_off[ch];
+    for (int a = g; a < rc; a += kThreads / kGBN)
+      W[(int64_t)mp[a] * kGBN + t] += Vc[(int64_t)a * kGBN + t];
+    __syncthreads();
+  }
+}
+
+// ... then O = Mt W_C + [0; W_R] (rows < c: Y_C = L_CC^{-1} W_C; rows >= c:
+// V = W_R - L_RC Y_C), items (node, tile, 32-row block of the front).
+__global__ void __launch_bounds__(kGT)
+    mf_fwd_gemm_kernel(pf_mf_plan_t p, const double *__restrict__ Mt,
+                       const int32_t *__restrict__ item_node, const int64_t *__restrict__ item_id,
+                       const int64_t *__restrict__ item_woff, const int32_t *__restrict__ item_rb,
+                       const double *__restrict__ Wb, double *O) {
+  const int s = item_node[blockIdx.x];
+  const int f = p.fn[s], c = p.cn[s];
+  const int ldc = (c + 15) & ~15;
+  const int i0 = item_rb[blockIdx.x] * kGBM;
+  const double *W = Wb + item_woff[blockIdx.x];
+  double *Ob = O + p.act_voff[item_id[blockIdx.x]];
+  const double *A = Mt + p.mt_off[s];
+  __shared__ __align__(128) double ring[kGemmSmem / 8];
+  gathered_gemm(
+      ring, ring + kGStages * kStageA, min(kGBM, f - i0), c, 1, [&](int r) { return A + (int64_t)(i0 + r) * ldc; },
+      [&](int, int l) { return W + (int64_t)l * kGBN; },
+      [&](int, int r, int t, double v) {
+        const int i = i0 + r;
+        if (i < f) Ob[(int64_t)i * kGBN + t] = v + (i >= c ? W[(int64_t)i * kGBN + t] : 0.0);
+      });
 }
 
 // ------------------------------------------------------ backward solve --
-// One CTA per (node, tiles [t0, t1)) item, levels top-down:
-//   Z = Y_C - L_RC^T X_R ;  X_C = L_CC^{-T} Z   (in place in P's C rows).
-__global__ void __launch_bounds__(kThreads)
-    mf_backward_kernel(pf_mf_plan_t p, const double *__restrict__ F,
-                       const int32_t *__restrict__ item_node, const int32_t *__restrict__ item_t0,
-                       const int32_t *__restrict__ item_t1, double *P, int64_t ldp) {
-  __shared__ double D[kT][kT + 1];
-  __shared__ double Y[kT][kT + 1];
-  constexpr int kRows = kThreads / kT;  // 8 row groups
-  constexpr int kRB = 8;                // rows per thread in the R sweep
+// Levels top-down; items (node, 32-row block of C, column blocks [cb0, cb1)):
+//   X_C = M [Y_C; X_R],  M = Mt^T = [L_CC^{-T} | -L_CC^{-T} L_RC^T]
+// Y_C from the forward blocks (zero where the tile was never reached), X_R
+// gathered from P's rows (final: ancestors ran earlier), X_C into P.
+// 64 (C rows) x 128 (columns) output tile per CTA: 8 warps as 2 (m) x 4 (n)
+// with 32 x 32 warp tiles (16 DMMAs per 4-deep k step), 16-deep K stages in a
+// 3-stage cp.async ring (81 KB: 2 CTAs = 16 warps per SM), stage counters
+// instead of divisions, and every gather offset resolved in shared memory
+// before the main loop (the issue path is branch-free selects).
+constexpr int kBM = 64, kBN = 128, kBT = 256;
+constexpr int kSB2 = kBN + 4;  // 4 mod 16: conflict-free half-warp fragment loads
+constexpr int kBStageA = kBM * kSA, kBStageB = kGBK * kSB2;
+constexpr int kBRing = kGStages * (kBStageA + kBStageB) * 8;  // bytes
+
+__global__ void __launch_bounds__(kBT, 2)
+    mf_bwd_gemm_kernel(pf_mf_plan_t p, const double *__restrict__ M,
+                       const double *__restrict__ O, const int32_t *__restrict__ item_node,
+                       const int32_t *__restrict__ item_rb, const int32_t *__restrict__ item_cb0,
+                       const int32_t *__restrict__ item_cb1, double *P, int64_t ldp) {
+  // dynamic smem: [A ring | B ring | coff[kBM] | ybase[2 * ncb] | roff[f]]
+  extern __shared__ __align__(128) double dyn[];
+  double *As = dyn, *Bs = dyn + kGStages * kBStageA;
+  int64_t *coff = reinterpret_cast<int64_t *>(dyn + kGStages * (kBStageA + kBStageB));
+  const double **ysrc = reinterpret_cast<const double **>(coff + kBM);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int s = item_node[blockIdx.x];
-  const int f = p.fn[s], c = p.cn[s], r = p.rn[s];
-  if (c == 0) return;
-  const double *Fs = F + p.foff[s];
-  const int32_t *Cv = p.perm_orig + p.c0[s];
-  const int32_t *Rv = p.r_orig + p.r_ptr[s];
-  const int tid = threadIdx.x, t = tid % kT, g = tid / kT;
-  for (int tile = item_t0[blockIdx.x]; tile < item_t1[blockIdx.x]; ++tile) {
-    const int64_t j0 = (int64_t)tile * kT;
-    const int w = (int)min((int64_t)kT, p.k - j0);
-    const bool active = p.tile_item[(int64_t)s * p.ntiles + tile] >= 0;
-    if (!active)
-      for (int i = g; i < c; i += kRows)
-        if (t < w) P[(int64_t)Cv[i] * ldp + j0 + t] = 0.0;
-    __syncthreads();
-    // Z -= L_RC^T X_R, C rows in blocks of kRows * kRB
-    for (int ib = 0; ib < c; ib += kRows * kRB) {
-      double acc[kRB] = {};
-      for (int rb = 0; rb < r; rb += kT) {
-        const int nr = min(kT, r - rb);
-        for (int idx = tid; idx < kT * kT; idx += kThreads) {
-          const int l = idx / kT, j = idx % kT;
-          Y[l][j] = (l < nr && j < w) ? P[(int64_t)Rv[rb + l] * ldp + j0 + j] : 0.0;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int u = 0; u < kRB; ++u) {
-          const int i = ib + g + kRows * u;
-          if (i < c) {
-            const double *Lc = Fs + (int64_t)(c + rb) * f + i;
-            double a = 0.0;
-            for (int l = 0; l < nr; ++l) a += Lc[(int64_t)l * f] * Y[l][t];
-            acc[u] += a;
-          }
-        }
-        __syncthreads();
-      }
-#pragma unroll
-      for (int u = 0; u < kRB; ++u) {
-        const int i = ib + g + kRows * u;
-        if (i < c && t < w) P[(int64_t)Cv[i] * ldp + j0 + t] -= acc[u];
-      }
+  const int f = p.fn[s], c = p.cn[s];
+  const int ldf = (f + 15) & ~15;
+  const int i0 = item_rb[blockIdx.x] * kBM;
+  // column blocks of 128 = pairs of 64-column plan tiles [2 cb, 2 cb + 1]
+  const int cb0 = item_cb0[blockIdx.x], ncb = item_cb1[blockIdx.x] - cb0;
+  int64_t *roff = reinterpret_cast<int64_t *>(ysrc + 2 * ncb);
+  {
+    const int32_t *Cv = p.perm_orig + p.c0[s];
+    const int32_t *Rv = p.r_orig + p.r_ptr[s];
+    const int64_t *ti = p.tile_item + (int64_t)s * p.ntiles;
+    // roff[l]: l < c -> Y row l of a 64-wide block; else the P row of X_R[l - c]
+    for (int l = tid; l < f; l += kBT)
+      roff[l] = l < c ? (int64_t)l * kGBN : (int64_t)Rv[l - c] * ldp;
+    for (int h = tid; h < 2 * ncb; h += kBT) {
+      const int64_t tile = 2 * (int64_t)cb0 + h;
+      const int64_t it = tile < p.ntiles ? ti[tile] : -1;
+      ysrc[h] = it < 0 ? nullptr : O + p.act_voff[it];
     }
-    __syncthreads();
-    // X_C = L_CC^{-T} Z, 32-row blocks from the bottom
-    for (int jb = ((c - 1) / kT) * kT; jb >= 0; jb -= kT) {
-      const int nb = min(kT, c - jb);
-      for (int idx = tid; idx < kT * kT; idx += kThreads) {
-        const int i = idx / kT, j = idx % kT;
-        D[i][j] = (i < nb && j <= i) ? Fs[(int64_t)(jb + i) * f + jb + j] : 0.0;
-        Y[i][j] = (i < nb && j < w) ? P[(int64_t)Cv[jb + i] * ldp + j0 + j] : 0.0;
+    for (int r = tid; r < kBM; r += kBT) coff[r] = i0 + r < c ? (int64_t)Cv[i0 + r] * ldp : -1;
+  }
+  __syncthreads();
+  const double *A = M + p.m_off[s] + (int64_t)i0 * ldf;
+  const int ma = min(kBM, c - i0);
+  const int nkt = (f + kGBK - 1) / kGBK;
+  // copy slots: A rows ra + 32u (chunk cha); B rows rbr + 4u (chunk chb: 64 per row)
+  const int ra = tid >> 3, cha = tid & 7, rbr = tid >> 6, chb = tid & 63;
+  const int half = chb >> 5;  // which 64-column plan tile of the block
+  int icb = 0, ikt = 0, ist = 0;  // next (column block, k stage, ring slot) to issue
+  auto issue = [&]() {
+    if (icb < ncb) {
+      const int k0 = ikt * kGBK;
+      double *as = As + ist * kBStageA, *bs = Bs + ist * kBStageB;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int r = ra + 32 * u;
+        const double *src = r < ma ? A + (int64_t)r * ldf + k0 + 2 * cha : g_zero + 2 * cha;
+        cp_async16(as + r * kSA + 2 * cha, src);
       }
-      __syncthreads();
-      if (tid < kT) {
-        for (int j = nb - 1; j >= 0; --j) {
-          double x = Y[j][t];
-          for (int l = j + 1; l < nb; ++l) x -= D[l][j] * Y[l][t];
-          Y[j][t] = x / D[j][j];
-        }
+      const double *yb = ysrc[2 * icb + half];
+      const int64_t col = (int64_t)(cb0 + icb) * kBN + 2 * chb;
+      const double *pb = P + col;
+      const bool colok = col < ldp;
+      int64_t ro[4];  // 16 rows x 64 chunks = 4 per thread
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int l = k0 + rbr + 4 * u;
+        ro[u] = l < f ? roff[l] : 0;
       }
-      __syncthreads();
-      for (int i = g; i < nb; i += kRows)
-        if (t < w) P[(int64_t)Cv[jb + i] * ldp + j0 + t] = Y[i][t];
-      for (int i = g; i < jb; i += kRows) {
-        const double *Lc = Fs + (int64_t)jb * f + i;
-        double a = 0.0;
-        for (int l = 0; l < nb; ++l) a += Lc[(int64_t)l * f] * Y[l][t];
-        if (t < w) P[(int64_t)Cv[i] * ldp + j0 + t] -= a;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int r = rbr + 4 * u, l = k0 + r;
+        const bool isy = l < c;
+        const double *base = isy ? (yb ? yb + 2 * (chb & 31) : nullptr) : (colok ? pb : nullptr);
+        const double *src = (l < f && base) ? base + ro[u] : g_zero + 2 * (chb & 31);
+        cp_async16(bs + r * kSB2 + 2 * chb, src);
       }
+      if (++ikt == nkt) {
+        ikt = 0;
+        ++icb;
+      }
+      ist = ist == kGStages - 1 ? 0 : ist + 1;
+    }
+    cp_commit();
+  };
+  const int wm = warp >> 2, wn = warp & 3, fr = lane >> 2, fc = lane & 3;
+#pragma unroll
+  for (int u = 0; u < kGStages - 1; ++u) issue();
+  int cst = 0;  // ring slot being consumed
+  const int64_t k = p.k;
+  for (int cb = 0; cb < ncb; ++cb) {
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int kt = 0; kt < nkt; ++kt) {
+      cp_wait<kGStages - 2>();
       __syncthreads();
+      issue();
+      const double *as = As + cst * kBStageA + (wm * 32 + fr) * kSA + fc;
+      const double *bs = Bs + cst * kBStageB + fc * kSB2 + wn * 32 + fr;
+#pragma unroll
+      for (int ks = 0; ks < kGBK; ks += 4) {
+        double av[4], bv[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) av[i] = as[8 * i * kSA + ks];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bv[j] = bs[ks * kSB2 + 8 * j];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], av[i], bv[j]);
+      }
+      cst = cst == kGStages - 1 ? 0 : cst + 1;
+    }
+    const int64_t colb = (int64_t)(cb0 + cb) * kBN + wn * 32 + 2 * fc;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t ro = coff[wm * 32 + 8 * i + fr];
+      if (ro < 0) continue;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t col = colb + 8 * j;
+        if (col < k)  // the pad column col+1 (k odd) is rewritten by finalize
+          *reinterpret_cast<double2 *>(P + ro + col) = make_double2(acc[i][j][0], acc[i][j][1]);
+      }
     }
   }
+  cp_wait<0>();
 }
 
 // ------------------------------------------------------- diagnostics ------
@@ -468,7 +691,7 @@ int pf_cotan_laplacian_f64(const double *V, const int32_t *T, int64_t nt, const 
 int pf_mf_factor_level(const pf_mf_plan_t *plan, const double *off, const double *diag,
                        const int32_t *nodes, int64_t count, double *F, int32_t *err,
                        pf_stream_t stream) {
-  if (!plan || !off || !diag || !nodes || !F || !err || count < 0 || plan->tile != kT)
+  if (!plan || !off || !diag || !nodes || !F || !err || count < 0)
     return fail(PF_E_ARG, "pf_mf_factor_level: bad argument");
   if (count == 0) return 0;
   mf_factor_kernel<<<(unsigned)count, kThreads, 0, as_stream(stream)>>>(*plan, off, diag, nodes,
@@ -476,27 +699,52 @@ int pf_mf_factor_level(const pf_mf_plan_t *plan, const double *off, const double
   return check_launch("pf_mf_factor_level");
 }
 
-int pf_mf_forward_level(const pf_mf_plan_t *plan, const double *F, const double *off,
-                        const int32_t *item_node, const int64_t *item_id, int64_t count,
-                        double *V, double *P, int64_t ldp, pf_stream_t stream) {
-  if (!plan || !F || !off || !item_node || !item_id || !V || !P || count < 0 ||
-      plan->tile != kT || ldp < plan->k)
+int pf_mf_inverse(const pf_mf_plan_t *plan, const double *F, const int32_t *item_node,
+                  const int32_t *item_ct, int64_t count, const int32_t *nodes, int64_t nnodes,
+                  double *Mt, double *M, pf_stream_t stream) {
+  if (!plan || !F || !item_node || !item_ct || !nodes || !Mt || !M || count < 0 || nnodes < 0 ||
+      plan->tile != kGBN)
+    return fail(PF_E_ARG, "pf_mf_inverse: bad argument");
+  cudaStream_t st = as_stream(stream);
+  if (count > 0)
+    mf_inverse_kernel<<<(unsigned)count, kThreads, 0, st>>>(*plan, F, item_node, item_ct, Mt);
+  if (nnodes > 0) mf_transpose_kernel<<<(unsigned)nnodes, kThreads, 0, st>>>(*plan, nodes, Mt, M);
+  return check_launch("pf_mf_inverse");
+}
+
+int pf_mf_forward_level(const pf_mf_plan_t *plan, const double *Mt, const double *off,
+                        const int32_t *asm_node, const int64_t *asm_item, const int64_t *asm_woff,
+                        int64_t n_asm, const int32_t *g_node, const int64_t *g_item,
+                        const int64_t *g_woff, const int32_t *g_rb, int64_t n_gemm, double *Wb,
+                        double *O, pf_stream_t stream) {
+  if (!plan || !Mt || !off || !Wb || !O || n_asm < 0 || n_gemm < 0 || plan->tile != kGBN ||
+      (n_asm && (!asm_node || !asm_item || !asm_woff)) ||
+      (n_gemm && (!g_node || !g_item || !g_woff || !g_rb)))
     return fail(PF_E_ARG, "pf_mf_forward_level: bad argument");
-  if (count == 0) return 0;
-  mf_forward_kernel<<<(unsigned)count, kThreads, 0, as_stream(stream)>>>(*plan, F, off, item_node,
-                                                                         item_id, V, P, ldp);
+  cudaStream_t st = as_stream(stream);
+  if (n_asm > 0)
+    mf_fwd_assemble_kernel<<<(unsigned)n_asm, kThreads, 0, st>>>(*plan, off, asm_node, asm_item,
+                                                                 asm_woff, O, Wb);
+  if (n_gemm > 0)
+    mf_fwd_gemm_kernel<<<(unsigned)n_gemm, kGT, 0, st>>>(*plan, Mt, g_node, g_item, g_woff, g_rb,
+                                                         Wb, O);
   return check_launch("pf_mf_forward_level");
 }
 
-int pf_mf_backward_level(const pf_mf_plan_t *plan, const double *F, const int32_t *item_node,
-                         const int32_t *item_t0, const int32_t *item_t1, int64_t count,
-                         double *P, int64_t ldp, pf_stream_t stream) {
-  if (!plan || !F || !item_node || !item_t0 || !item_t1 || !P || count < 0 ||
-      plan->tile != kT || ldp < plan->k)
-    return fail(PF_E_ARG, "pf_mf_backward_level: bad argument");
+int pf_mf_backward_level(const pf_mf_plan_t *plan, const double *M, const double *O,
+                         const int32_t *item_node, const int32_t *item_rb,
+                         const int32_t *item_cb0, const int32_t *item_cb1, int64_t count,
+                         int32_t max_f, int32_t max_ncb, double *P, int64_t ldp,
+                         pf_stream_t stream) {
+  if (!plan || !M || !O || !item_node || !item_rb || !item_cb0 || !item_cb1 || !P || count < 0 ||
+      plan->tile != kGBN || ldp < plan->k || (ldp % kGBN) != 0)
+    return fail(PF_E_ARG, "pf_mf_backward_level: bad argument (ldp must be a multiple of 64)");
   if (count == 0) return 0;
-  mf_backward_kernel<<<(unsigned)count, kThreads, 0, as_stream(stream)>>>(
-      *plan, F, item_node, item_t0, item_t1, P, ldp);
+  if (max_f < 1 || max_ncb < 1) return fail(PF_E_ARG, "pf_mf_backward_level: bad limits");
+  const size_t smem = kBRing + 8 * ((size_t)kBM + 2 * max_ncb + max_f);
+  if (int rc = ensure_smem((const void *)mf_bwd_gemm_kernel, smem)) return rc;
+  mf_bwd_gemm_kernel<<<(unsigned)count, kBT, smem, as_stream(stream)>>>(
+      *plan, M, O, item_node, item_rb, item_cb0, item_cb1, P, ldp);
   return check_launch("pf_mf_backward_level");
 }
 

@@ -54,7 +54,7 @@ _STATS = ("n", "m", "k", "nodes", "levels", "f_total", "v_total", "nnz_l", "flop
           "flops_solve", "max_f", "max_c", "max_r", "ntiles", "tile", "leaf")
 
 LEAF = 64   # leaf sub-domain size of the dissection
-TILE = 32   # column tile of the multi-RHS solves
+TILE = 64   # column tile of the multi-RHS solves (pf_mf_plan_t.tile)
 
 
 def mesh_topology(mesh):
@@ -121,10 +121,10 @@ class NdPlan:
 # ------------------------------------------------------------------ device --
 class PfMfPlan(ctypes.Structure):
     """ctypes mirror of pf_mf_plan_t (include/pathfield_b200.h)."""
-    _fields_ = [(name, ctypes.c_void_p) for name in (
-        "c0", "cn", "rn", "fn", "foff", "ch_ptr", "ch_idx", "r_ptr", "r_orig", "relmap_off",
-        "relmap", "a_ptr", "a_dst", "a_src", "b_ptr", "b_row", "b_col", "b_src", "act_tile",
-        "act_voff", "tile_item", "perm_orig")] + [
+    _PTRS = ("c0", "cn", "rn", "fn", "foff", "ch_ptr", "ch_idx", "r_ptr", "r_orig",
+             "relmap_off", "relmap", "a_ptr", "a_dst", "a_src", "b_ptr", "b_row", "b_col",
+             "b_src", "act_tile", "act_voff", "tile_item", "perm_orig", "mt_off", "m_off")
+    _fields_ = [(name, ctypes.c_void_p) for name in _PTRS] + [
         ("nodes", ctypes.c_int64), ("ntiles", ctypes.c_int64), ("k", ctypes.c_int64),
         ("tile", ctypes.c_int32), ("pad_", ctypes.c_int32)]
 
@@ -133,12 +133,23 @@ def _u64_to_f64(x: int) -> float:
     return float(np.array([x], dtype=np.uint64).view(np.float64)[0])
 
 
+def _ranges(ptr, nodes):
+    """Concatenated arange(ptr[s], ptr[s+1]) over `nodes` (and the owner of each)."""
+    lo, hi = ptr[nodes], ptr[nodes + 1]
+    cnt = hi - lo
+    owner = np.repeat(nodes, cnt)
+    idx = np.repeat(lo - np.concatenate([[0], np.cumsum(cnt)[:-1]]), cnt) + np.arange(cnt.sum())
+    return owner, idx
+
+
 class DevicePoisson:
     """The device pipeline of one mesh: Laplacian, plan, factor, solves.
 
-    ``laplacian()`` and ``factor()`` are cached; ``solve()`` builds a fresh P
-    (a :class:`~._device.DeviceKernel`, rows x ld FP64 in HBM) every call.
+    ``laplacian()`` and ``factor()`` (L, then the explicit front inverses Mt
+    and M) are cached; ``solve()`` writes a fresh P every call.
     """
+
+    GEMM_TARGET = 2 * 148  # CTAs per backward level before column blocks are split
 
     def __init__(self, mesh, leaf: int = LEAF, device=None):
         from . import _device as dev
@@ -157,16 +168,18 @@ class DevicePoisson:
         self.dm.nb_ptr = tod(nb_ptr, np.int64)
         self.dm.nb_idx = tod(nb_idx, np.int32)
         self._nnz = int(nb_ptr[-1])
-        self.plan = NdPlan(mesh.vertices, nb_ptr, nb_idx, isb_h, leaf=leaf, tile=TILE)
-        pl = self.plan
+        self.plan = pl = NdPlan(mesh.vertices, nb_ptr, nb_idx, isb_h, leaf=leaf, tile=TILE)
         self.n, self.k = pl.n, pl.k
         self.stream = lambda: t.cuda.current_stream(self.device).cuda_stream
-        to = lambda a: t.from_numpy(np.ascontiguousarray(a)).to(self.device)  # noqa: E731
-        self._dev = {name: to(getattr(pl, name)) for name in _I32 + _I64
-                     if name not in ("iperm", "parent", "height", "r_pos", "level_ptr",
-                                     "level_nodes")}
-        d = self._dev
-        self.struct = PfMfPlan(*[d[name].data_ptr() for name, _ in PfMfPlan._fields_[:22]],
+        c, f = pl.cn.astype(np.int64), pl.fn.astype(np.int64)
+        ldc, ldf = (c + 15) // 16 * 16, (f + 15) // 16 * 16  # 128-byte rows
+        mt_sz, m_sz = f * ldc, c * ldf
+        self.mt_off = np.concatenate([[0], np.cumsum(mt_sz)]).astype(np.int64)
+        self.m_off = np.concatenate([[0], np.cumsum(m_sz)]).astype(np.int64)
+        arrays = {name: getattr(pl, name) for name in PfMfPlan._PTRS if hasattr(pl, name)}
+        arrays["mt_off"], arrays["m_off"] = self.mt_off, self.m_off
+        self._dev = {name: tod(a, a.dtype) for name, a in arrays.items()}
+        self.struct = PfMfPlan(*[self._dev[name].data_ptr() for name in PfMfPlan._PTRS],
                                pl.nodes, pl.ntiles, pl.k, pl.tile, 0)
         isb = np.zeros(pl.n, dtype=np.uint8)
         bnd = np.asarray(mesh.boundary_vertices, dtype=np.int64)
@@ -174,29 +187,52 @@ class DevicePoisson:
         bcol = -np.ones(pl.n, dtype=np.int32)
         bcol[bnd] = np.arange(len(bnd), dtype=np.int32)
         self.boundary = bnd
-        self.is_boundary = to(isb)
-        self.bcol = to(bcol)
-        # per-level launch lists
-        self.levels = [to(lv.astype(np.int32)) for lv in pl.levels]
-        self.fwd = []
+        self.is_boundary = tod(isb, np.uint8)
+        self.bcol = tod(bcol, np.int32)
+        # ---- launch lists ------------------------------------------------
+        self.levels = [tod(lv, np.int32) for lv in pl.levels]
+        all_nodes = np.arange(pl.nodes, dtype=np.int64)
+        ct = (c + 31) // 32
+        inv_node = np.repeat(all_nodes, ct)
+        inv_ct = np.arange(ct.sum()) - np.repeat(np.concatenate([[0], np.cumsum(ct)[:-1]]), ct)
+        self.inv = (tod(inv_node, np.int32), tod(inv_ct, np.int32), len(inv_node),
+                    tod(all_nodes, np.int32))
+        self.fwd, wmax = [], 1
         for lv in pl.levels:
-            nodes = np.repeat(lv, pl.act_ptr[lv + 1] - pl.act_ptr[lv]).astype(np.int32)
-            ids = (np.concatenate([np.arange(pl.act_ptr[s], pl.act_ptr[s + 1]) for s in lv])
-                   if len(lv) else np.zeros(0, np.int64)).astype(np.int64)
-            self.fwd.append((to(nodes), to(ids), len(ids)))
+            lv = lv.astype(np.int64)
+            node, item = _ranges(pl.act_ptr, lv)
+            fi = f[node]
+            woff = np.concatenate([[0], np.cumsum(fi * TILE)[:-1]]).astype(np.int64)
+            wmax = max(wmax, int((fi * TILE).sum()))
+            rb = (fi + 31) // 32
+            g_node = np.repeat(node, rb)
+            g_item = np.repeat(item, rb)
+            g_woff = np.repeat(woff, rb)
+            g_rb = np.arange(rb.sum()) - np.repeat(np.concatenate([[0], np.cumsum(rb)[:-1]]), rb)
+            self.fwd.append((tod(node, np.int32), tod(item, np.int64), tod(woff, np.int64),
+                             len(node), tod(g_node, np.int32), tod(g_item, np.int64),
+                             tod(g_woff, np.int64), tod(g_rb, np.int32), len(g_node)))
+        self.w_total = wmax
         self.bwd = []
-        target = 2 * 148
+        nblk = (pl.ntiles + 1) // 2  # 128-column blocks (pairs of plan tiles)
         for lv in pl.levels:
-            chunks = int(min(pl.ntiles, max(1, -(-target // max(len(lv), 1)))))
-            step = -(-pl.ntiles // chunks)
-            t0 = np.arange(0, pl.ntiles, step, dtype=np.int32)
-            t1 = np.minimum(t0 + step, pl.ntiles).astype(np.int32)
-            nodes = np.repeat(lv.astype(np.int32), len(t0))
-            self.bwd.append((to(nodes), to(np.tile(t0, len(lv))), to(np.tile(t1, len(lv))),
-                             len(nodes)))
+            lv = lv.astype(np.int64)
+            lv = lv[c[lv] > 0]
+            rb = (c[lv] + 63) // 64  # 64-row blocks of C (mf_bwd_gemm_kernel)
+            blocks = int(rb.sum())
+            chunks = int(min(nblk, max(1, -(-self.GEMM_TARGET // max(blocks, 1)))))
+            step = -(-nblk // chunks)
+            cb0 = np.arange(0, nblk, step, dtype=np.int64)
+            cb1 = np.minimum(cb0 + step, nblk)
+            nodes = np.repeat(lv, rb)
+            rbi = np.arange(blocks) - np.repeat(np.concatenate([[0], np.cumsum(rb)[:-1]]), rb)
+            nn = len(nodes)
+            self.bwd.append((tod(np.repeat(nodes, len(cb0)), np.int32),
+                             tod(np.repeat(rbi, len(cb0)), np.int32),
+                             tod(np.tile(cb0, nn), np.int32), tod(np.tile(cb1, nn), np.int32),
+                             nn * len(cb0), int(f[lv].max()) if len(lv) else 1, int(step)))
         self._lap = None
         self._F = None
-        self.timings: dict = {}
 
     # -- laplacian.py:91-134 ---------------------------------------------
     def laplacian(self):
@@ -224,7 +260,8 @@ class DevicePoisson:
 
     # -- laplacian.py:29-45 (splu of -Lc_II) -------------------------------
     def factor(self):
-        """Multifrontal Cholesky of -Lc_II on the device (cached)."""
+        """Multifrontal Cholesky of -Lc_II and the explicit front inverses
+        (Mt, M) on the device (cached).  Returns (Mt, M)."""
         if self._F is None:
             from . import _device as dev
             from .errors import FactorizationError
@@ -237,35 +274,45 @@ class DevicePoisson:
                 nat.call("pf_mf_factor_level", ctypes.addressof(self.struct), off.data_ptr(),
                          diag.data_ptr(), lv.data_ptr(), lv.numel(), F.data_ptr(),
                          err.data_ptr(), s)
+            Mt = t.zeros(max(int(self.mt_off[-1]), 1), dtype=t.float64, device=self.device)
+            M = t.zeros(max(int(self.m_off[-1]), 1), dtype=t.float64, device=self.device)
+            inode, ict, icnt, nodes = self.inv
+            nat.call("pf_mf_inverse", ctypes.addressof(self.struct), F.data_ptr(),
+                     inode.data_ptr(), ict.data_ptr(), icnt, nodes.data_ptr(), nodes.numel(),
+                     Mt.data_ptr(), M.data_ptr(), s)
             if int(err.item()):
                 raise FactorizationError(
                     "interior block is not positive definite after negation "
                     "(severely non-Delaunay mesh)")
-            self._F = F
+            del F
+            self._F = (Mt, M)
         return self._F
 
     # -- solvers.py:278-303 ------------------------------------------------
     def solve(self, P_out=None):
-        """P (device, rows x ld) with residual and row_sum_error.
-
-        Returns (P tensor, residual, row_sum_error)."""
+        """P (device, n x round_up(k, 64) FP64, pads zero) with the reference's
+        diagnostics.  Returns (P, residual, row_sum_error)."""
         from . import _device as dev
         t = dev.torch()
         off, diag = self.laplacian()
-        F = self.factor()
-        ld = dev.leading_dim(self.k)
+        Mt, M = self.factor()
+        ld = round_up_cols(self.k)
         P = P_out if P_out is not None else t.empty((self.n, ld), dtype=t.float64,
                                                     device=self.device)
-        V = t.empty(max(self.plan.stats["v_total"], 1), dtype=t.float64, device=self.device)
+        if P.stride(0) != ld:
+            raise ValueError("P_out must be (n, round_up(k, 64)) row-major")
+        O = t.empty(max(self.plan.stats["v_total"], 1), dtype=t.float64, device=self.device)
+        Wb = t.empty(self.w_total, dtype=t.float64, device=self.device)
         s = self.stream()
         ps = ctypes.addressof(self.struct)
-        for nodes, ids, cnt in self.fwd:
-            nat.call("pf_mf_forward_level", ps, F.data_ptr(), off.data_ptr(), nodes.data_ptr(),
-                     ids.data_ptr(), cnt, V.data_ptr(), P.data_ptr(), ld, s)
-        for nodes, t0, t1, cnt in reversed(self.bwd):
-            nat.call("pf_mf_backward_level", ps, F.data_ptr(), nodes.data_ptr(), t0.data_ptr(),
-                     t1.data_ptr(), cnt, P.data_ptr(), ld, s)
-        del V
+        for (an, ai, aw, acnt, gn, gi, gw, grb, gcnt) in self.fwd:
+            nat.call("pf_mf_forward_level", ps, Mt.data_ptr(), off.data_ptr(), an.data_ptr(),
+                     ai.data_ptr(), aw.data_ptr(), acnt, gn.data_ptr(), gi.data_ptr(),
+                     gw.data_ptr(), grb.data_ptr(), gcnt, Wb.data_ptr(), O.data_ptr(), s)
+        for nodes, rb, cb0, cb1, cnt, maxf, ncb in reversed(self.bwd):
+            nat.call("pf_mf_backward_level", ps, M.data_ptr(), O.data_ptr(), nodes.data_ptr(),
+                     rb.data_ptr(), cb0.data_ptr(), cb1.data_ptr(), cnt, maxf, ncb,
+                     P.data_ptr(), ld, s)
         mx = t.zeros(2, dtype=t.int64, device=self.device)
         dm = self.dm
         nat.call("pf_poisson_residual", P.data_ptr(), ld, self.n, self.k,
@@ -273,6 +320,7 @@ class DevicePoisson:
                  dm.nb_idx.data_ptr(), off.data_ptr(), diag.data_ptr(), mx.data_ptr(), s)
         nat.call("pf_poisson_finalize", P.data_ptr(), ld, self.n, self.k,
                  self.is_boundary.data_ptr(), self.bcol.data_ptr(), mx.data_ptr() + 8, s)
+        del O, Wb
         r = mx.cpu().numpy().astype(np.uint64)
         residual = _u64_to_f64(int(r[0])) if self.plan.m else 0.0
         return P, residual, _u64_to_f64(int(r[1]))
@@ -284,6 +332,11 @@ class DevicePoisson:
         dk = dev.DeviceKernel(None, self.boundary, n=self.n, k=self.k, P_dev=P)
         dk.residual, dk.row_sum_error = residual, rse
         return dk
+
+
+def round_up_cols(k: int) -> int:
+    """Row stride of a device-built P: 64-column tiles never cross a row end."""
+    return (k + 63) // 64 * 64
 
 
 class LaplacianSet:

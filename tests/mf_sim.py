@@ -53,7 +53,8 @@ def factor(plan, off, diag):
 
 
 def solve(plan, F, off, k, ld=None):
-    """Forward (tile-sparse, V blocks per active item) + backward into P rows."""
+    """Forward (tile-sparse, one f x tile [Y_C; V] block per active item) +
+    backward into P rows."""
     n, T = plan.n, plan.tile
     P = np.zeros((n, k))
     V = np.zeros(plan.stats["v_total"])
@@ -76,15 +77,16 @@ def solve(plan, F, off, k, ld=None):
                     ic = plan.tile_item[ch * plan.ntiles + t]
                     if ic < 0:
                         continue
-                    rc = int(plan.rn[ch])
-                    Vc = V[plan.act_voff[ic]:plan.act_voff[ic] + rc * T].reshape(rc, T)
+                    rc, fc, cc = int(plan.rn[ch]), int(plan.fn[ch]), int(plan.cn[ch])
+                    Vc = V[plan.act_voff[ic]:plan.act_voff[ic] + fc * T].reshape(fc, T)[cc:]
                     mp = plan.relmap[plan.relmap_off[ch]:plan.relmap_off[ch] + rc]
                     W[mp] += Vc
                 Y = np.linalg.solve(np.tril(Fs[:c, :c]), W[:c]) if c else W[:0]
                 W[c:] -= Fs[c:, :c] @ Y
                 P[Crows, j0:j1] = Y[:, :j1 - j0]
                 touched[Crows, t] = True
-                V[plan.act_voff[it]:plan.act_voff[it] + r * T] = W[c:].ravel()
+                W[:c] = Y
+                V[plan.act_voff[it]:plan.act_voff[it] + f * T] = W.ravel()  # [Y_C; V]
     for level in reversed(plan.levels):
         for s in level:
             f, c, r = int(plan.fn[s]), int(plan.cn[s]), int(plan.rn[s])
