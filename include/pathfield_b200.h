@@ -496,10 +496,13 @@ int pf_cotan_laplacian_f64(const double *V, const int32_t *T, int64_t nt, const 
 /* Multifrontal Cholesky of A = -Lc_II, the nodes of one tree level: assemble
  * each front (A entries + children's update matrices, in child order), then
  * factor its |C| pivot columns in place (F[:, :c] = [L_CC; L_RC], F[c:, c:] =
- * the update matrix).  err[0] |= 1 on a non-positive pivot. */
+ * the update matrix).  err[0] |= 1 on a non-positive pivot.  split = 0: one
+ * CTA per front; split = 1 (few large fronts): assembly, pivot block, panel
+ * TRSM and trailing update are each spread over CTAs (max_f / max_c bound the
+ * level's fronts). */
 int pf_mf_factor_level(const pf_mf_plan_t *plan, const double *off, const double *diag,
-                       const int32_t *nodes, int64_t count, double *F, int32_t *err,
-                       pf_stream_t stream);
+                       const int32_t *nodes, int64_t count, int32_t max_f, int32_t max_c,
+                       int split, double *F, int32_t *err, pf_stream_t stream);
 
 /* Explicit front inverses after the factorisation: Mt = [L_CC^{-1};
  * -L_RC L_CC^{-1}] (f x c, row stride round_up(c,16)) for items (node, 32

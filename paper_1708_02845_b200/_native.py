@@ -96,7 +96,7 @@ _SIGS.update({
     "pf_nd_plan_stats": [c_vp, c_vp],
     "pf_cotan_laplacian_f64": [c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp,
                                c_vp],
-    "pf_mf_factor_level": [c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp],
+    "pf_mf_factor_level": [c_vp, c_vp, c_vp, c_vp, c_i64, c_int, c_int, c_int, c_vp, c_vp, c_vp],
     "pf_mf_inverse": [c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp],
     "pf_mf_forward_level": [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp,
                             c_i64, c_vp, c_vp, c_vp],

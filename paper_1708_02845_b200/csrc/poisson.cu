@@ -19,6 +19,7 @@
 // factor and of the right-hand sides in shared memory; a CTA owns a front
 // (and a range of column tiles), so no two CTAs ever write the same P entry
 // and every sum has a fixed order: results are deterministic run to run.
+#include <algorithm>
 #include <cfloat>
 
 #include "pf_common.cuh"
@@ -92,8 +93,152 @@ __global__ void laplacian_diag_kernel(const int64_t *__restrict__ nb_ptr,
 }
 
 // ------------------------------------------------------- factorisation --
-// One CTA per front of the level.
-__global__ void __launch_bounds__(kThreads)
+// Building blocks shared by the one-CTA-per-front kernel (many small fronts)
+// and the split kernels (few large fronts: every step spread over CTAs).
+
+// Zero rows [r0, r1) of the front, scatter the A entries of those rows, then
+// add each child's update matrix (child order) into those rows.  The row
+// range makes the assembly of one front splittable across CTAs while every
+// entry still receives its contributions in a fixed order.
+__device__ __forceinline__ void front_assemble_rows(const pf_mf_plan_t &p, int s,
+                                                    const double *__restrict__ off,
+                                                    const double *__restrict__ diag, double *F,
+                                                    int r0, int r1) {
+  const int f = p.fn[s];
+  double *Fs = F + p.foff[s];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int64_t i = (int64_t)r0 * f + tid; i < (int64_t)r1 * f; i += nt) Fs[i] = 0.0;
+  __syncthreads();
+  for (int64_t e = p.a_ptr[s] + tid; e < p.a_ptr[s + 1]; e += nt) {
+    const int64_t d = p.a_dst[e] - p.foff[s];
+    const int row = (int)(d / f);
+    if (row < r0 || row >= r1) continue;
+    const int64_t src = p.a_src[e];
+    Fs[d] = src >= 0 ? -off[src] : -diag[-1 - src];
+  }
+  __syncthreads();
+  for (int q = p.ch_ptr[s]; q < p.ch_ptr[s + 1]; ++q) {
+    const int ch = p.ch_idx[q];
+    const int fc = p.fn[ch], cc = p.cn[ch], rc = p.rn[ch];
+    const double *U = F + p.foff[ch] + (int64_t)cc * fc + cc;
+    const int32_t *mp = p.relmap + p.relmap_off[ch];
+    for (int a = tid / 32; a < rc; a += nt / 32) {
+      const int ra = mp[a];
+      if (ra < r0 || ra >= r1) continue;
+      const int64_t dst = (int64_t)ra * f;
+      for (int b = tid % 32; b <= a; b += 32) Fs[dst + mp[b]] += U[(int64_t)a * fc + b];
+    }
+    __syncthreads();
+  }
+}
+
+// Load the pb x pb pivot block at p0 into D (identity-padded to kT) and, if
+// `factor`, Cholesky-factor it with one warp and write it back.
+__device__ __forceinline__ void panel_diag(double *Fs, int f, int p0, int pb,
+                                           double (*D)[kT + 1], int32_t *err, bool factor) {
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < kT * kT; idx += blockDim.x) {
+    const int i = idx / kT, j = idx % kT;
+    double v;
+    if (i < pb && j <= i) v = Fs[(int64_t)(p0 + i) * f + p0 + j];
+    else v = (i == j) ? 1.0 : 0.0;  // identity padding: the unrolled TRSM divides by it
+    D[i][j] = v;
+  }
+  __syncthreads();
+  if (!factor) return;
+  if (tid < 32) {
+    const int lane = tid;
+    for (int j = 0; j < pb; ++j) {
+      const double djj = D[j][j];
+      if (!(djj > 0.0)) atomicOr(err, 1);
+      const double d = sqrt(djj);
+      __syncwarp();
+      if (lane == j) D[j][j] = d;
+      if (lane > j && lane < pb) D[lane][j] /= d;
+      __syncwarp();
+      if (lane > j && lane < pb) {
+        const double lij = D[lane][j];
+        for (int l = j + 1; l <= lane; ++l) D[lane][l] -= lij * D[l][j];
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  for (int idx = tid; idx < pb * pb; idx += blockDim.x) {
+    const int i = idx / pb, j = idx % pb;
+    if (j <= i) Fs[(int64_t)(p0 + i) * f + p0 + j] = D[i][j];
+  }
+}
+
+// Panel rows i = i_begin, i_begin + i_step, ... < f (one warp per row, lane j
+// holding column j): x D^T = F[i, p0:p0+pb], right-looking over the pivots.
+__device__ __forceinline__ void panel_trsm_rows(double *Fs, int f, int p0, int pb,
+                                                const double (*D)[kT + 1], int i_begin,
+                                                int i_step) {
+  const int lane = threadIdx.x & 31;
+  for (int i = i_begin; i < f; i += i_step) {
+    double *row = Fs + (int64_t)i * f + p0;
+    double v = lane < pb ? row[lane] : 0.0;
+    for (int j = 0; j < pb; ++j) {
+      const double xj = __shfl_sync(0xffffffffu, v, j) / D[j][j];
+      if (lane == j) v = xj;
+      else if (lane > j) v -= xj * D[lane][j];
+    }
+    if (lane < pb) row[lane] = v;
+  }
+}
+
+// Trailing-update tile (ti, tl), tl <= ti, of 64 x 64 at q0 = p0 + pb:
+// F[i][l] -= sum_j L[i][p0+j] L[l][p0+j] (lower triangle only).
+__device__ __forceinline__ void panel_syrk_tile(double *Fs, int f, int p0, int pb, int ti,
+                                                int tl, double (*Ai)[kT + 1],
+                                                double (*Al)[kT + 1]) {
+  const int tid = threadIdx.x;
+  const int q0 = p0 + pb;
+  const int gi0 = q0 + ti * 64, gl0 = q0 + tl * 64;
+  for (int idx = tid; idx < 64 * kT; idx += blockDim.x) {
+    const int r = idx / kT, j = idx % kT;
+    Ai[r][j] = (gi0 + r < f && j < pb) ? Fs[(int64_t)(gi0 + r) * f + p0 + j] : 0.0;
+    Al[r][j] = (gl0 + r < f && j < pb) ? Fs[(int64_t)(gl0 + r) * f + p0 + j] : 0.0;
+  }
+  __syncthreads();
+  const int ri = tid / 16, ci = tid % 16;
+  double acc[4][4] = {};
+  for (int j = 0; j < pb; ++j) {
+    double a[4], b[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      a[u] = Ai[ri + 16 * u][j];
+      b[u] = Al[ci + 16 * u][j];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int w = 0; w < 4; ++w) acc[u][w] += a[u] * b[w];
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int gi = gi0 + ri + 16 * u;
+    if (gi >= f) continue;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const int gl = gl0 + ci + 16 * w;
+      if (gl <= gi) Fs[(int64_t)gi * f + gl] -= acc[u][w];
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void tri_pair(int pr, int &ti, int &tl) {
+  int t = (int)((sqrt(8.0 * pr + 1.0) - 1.0) * 0.5);
+  while ((t + 1) * (t + 2) / 2 <= pr) ++t;
+  while (t * (t + 1) / 2 > pr) --t;
+  ti = t;
+  tl = pr - t * (t + 1) / 2;
+}
+
+// One CTA per front of the level (many small fronts).
+__global__ void __launch_bounds__(kThreads, 2)
     mf_factor_kernel(pf_mf_plan_t p, const double *__restrict__ off,
                      const double *__restrict__ diag, const int32_t *__restrict__ nodes,
                      double *F, int32_t *err) {
@@ -103,116 +248,70 @@ __global__ void __launch_bounds__(kThreads)
   const int s = nodes[blockIdx.x];
   const int f = p.fn[s], c = p.cn[s];
   double *Fs = F + p.foff[s];
-  const int tid = threadIdx.x;
-  const int64_t ff = (int64_t)f * f;
-  for (int64_t i = tid; i < ff; i += kThreads) Fs[i] = 0.0;
-  __syncthreads();
-  for (int64_t e = p.a_ptr[s] + tid; e < p.a_ptr[s + 1]; e += kThreads) {
-    const int64_t src = p.a_src[e];
-    F[p.a_dst[e]] = src >= 0 ? -off[src] : -diag[-1 - src];
-  }
-  __syncthreads();
-  // extend-add of the children's update matrices, one child at a time
-  for (int q = p.ch_ptr[s]; q < p.ch_ptr[s + 1]; ++q) {
-    const int ch = p.ch_idx[q];
-    const int fc = p.fn[ch], cc = p.cn[ch], rc = p.rn[ch];
-    const double *U = F + p.foff[ch] + (int64_t)cc * fc + cc;
-    const int32_t *mp = p.relmap + p.relmap_off[ch];
-    for (int a = tid / 32; a < rc; a += kThreads / 32) {
-      const int64_t dst = (int64_t)mp[a] * f;
-      for (int b = tid % 32; b <= a; b += 32) Fs[dst + mp[b]] += U[(int64_t)a * fc + b];
-    }
-    __syncthreads();
-  }
-  // partial Cholesky of the first c columns, 32-wide panels
+  front_assemble_rows(p, s, off, diag, F, 0, f);
   for (int p0 = 0; p0 < c; p0 += kT) {
     const int pb = min(kT, c - p0);
-    for (int idx = tid; idx < kT * kT; idx += kThreads) {
-      const int i = idx / kT, j = idx % kT;
-      double v;
-      if (i < pb && j <= i) v = Fs[(int64_t)(p0 + i) * f + p0 + j];
-      else v = (i == j) ? 1.0 : 0.0;  // identity padding: the unrolled TRSM divides by it
-      D[i][j] = v;
-    }
+    panel_diag(Fs, f, p0, pb, D, err, true);
+    panel_trsm_rows(Fs, f, p0, pb, D, p0 + pb + threadIdx.x / 32, kThreads / 32);
     __syncthreads();
-    if (tid < 32) {
-      const int lane = tid;
-      for (int j = 0; j < pb; ++j) {
-        const double djj = D[j][j];
-        if (!(djj > 0.0)) atomicOr(err, 1);
-        const double d = sqrt(djj);
-        __syncwarp();
-        if (lane == j) D[j][j] = d;
-        if (lane > j && lane < pb) D[lane][j] /= d;
-        __syncwarp();
-        if (lane > j && lane < pb) {
-          const double lij = D[lane][j];
-          for (int l = j + 1; l <= lane; ++l) D[lane][l] -= lij * D[l][j];
-        }
-        __syncwarp();
-      }
-    }
-    __syncthreads();
-    for (int idx = tid; idx < pb * pb; idx += kThreads) {
-      const int i = idx / pb, j = idx % pb;
-      if (j <= i) Fs[(int64_t)(p0 + i) * f + p0 + j] = D[i][j];
-    }
-    // panel rows below the pivot block: x D^T = row
-    for (int i = p0 + pb + tid; i < f; i += kThreads) {
-      double *row = Fs + (int64_t)i * f + p0;
-      double x[kT];
-#pragma unroll
-      for (int j = 0; j < kT; ++j) {
-        double v = j < pb ? row[j] : 0.0;
-#pragma unroll
-        for (int l = 0; l < j; ++l) v -= x[l] * D[j][l];
-        x[j] = v / D[j][j];
-      }
-#pragma unroll
-      for (int j = 0; j < kT; ++j)
-        if (j < pb) row[j] = x[j];
-    }
-    __syncthreads();
-    // trailing update F[q0:, q0:] -= L[q0:, p0:p0+pb] L[q0:, p0:p0+pb]^T (lower)
-    const int q0 = p0 + pb, nr = f - q0;
-    const int nb = (nr + 63) / 64;
-    const int ri = tid / 16, ci = tid % 16;
+    const int nb = (f - p0 - pb + 63) / 64;
     for (int pr = 0; pr < nb * (nb + 1) / 2; ++pr) {
-      int ti = 0;
-      while ((ti + 1) * (ti + 2) / 2 <= pr) ++ti;
-      const int tl = pr - ti * (ti + 1) / 2;
-      const int gi0 = q0 + ti * 64, gl0 = q0 + tl * 64;
-      for (int idx = tid; idx < 64 * kT; idx += kThreads) {
-        const int r = idx / kT, j = idx % kT;
-        Ai[r][j] = (gi0 + r < f && j < pb) ? Fs[(int64_t)(gi0 + r) * f + p0 + j] : 0.0;
-        Al[r][j] = (gl0 + r < f && j < pb) ? Fs[(int64_t)(gl0 + r) * f + p0 + j] : 0.0;
-      }
-      __syncthreads();
-      double acc[4][4] = {};
-      for (int j = 0; j < pb; ++j) {
-        double a[4], b[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          a[u] = Ai[ri + 16 * u][j];
-          b[u] = Al[ci + 16 * u][j];
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-          for (int w = 0; w < 4; ++w) acc[u][w] += a[u] * b[w];
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int gi = gi0 + ri + 16 * u;
-        if (gi >= f) continue;
-#pragma unroll
-        for (int w = 0; w < 4; ++w) {
-          const int gl = gl0 + ci + 16 * w;
-          if (gl <= gi) Fs[(int64_t)gi * f + gl] -= acc[u][w];
-        }
-      }
-      __syncthreads();
+      int ti, tl;
+      tri_pair(pr, ti, tl);
+      panel_syrk_tile(Fs, f, p0, pb, ti, tl, Ai, Al);
     }
+  }
+}
+
+// Split path (few large fronts): grid (fronts, parts) per step.
+__global__ void __launch_bounds__(kThreads)
+    mf_assemble_split_kernel(pf_mf_plan_t p, const double *__restrict__ off,
+                             const double *__restrict__ diag, const int32_t *__restrict__ nodes,
+                             double *F) {
+  const int s = nodes[blockIdx.x];
+  const int f = p.fn[s];
+  const int per = (f + gridDim.y - 1) / gridDim.y;
+  const int r0 = min(f, (int)blockIdx.y * per), r1 = min(f, r0 + per);
+  if (r0 >= r1) return;
+  front_assemble_rows(p, s, off, diag, F, r0, r1);
+}
+
+__global__ void __launch_bounds__(kThreads)
+    mf_panel_diag_kernel(pf_mf_plan_t p, const int32_t *__restrict__ nodes, int p0, double *F,
+                         int32_t *err) {
+  __shared__ double D[kT][kT + 1];
+  const int s = nodes[blockIdx.x];
+  const int c = p.cn[s];
+  if (p0 >= c) return;
+  panel_diag(F + p.foff[s], p.fn[s], p0, min(kT, c - p0), D, err, true);
+}
+
+__global__ void __launch_bounds__(kThreads, 2)
+    mf_panel_trsm_kernel(pf_mf_plan_t p, const int32_t *__restrict__ nodes, int p0, double *F) {
+  __shared__ double D[kT][kT + 1];
+  const int s = nodes[blockIdx.x];
+  const int c = p.cn[s], f = p.fn[s];
+  if (p0 >= c) return;
+  const int pb = min(kT, c - p0);
+  double *Fs = F + p.foff[s];
+  panel_diag(Fs, f, p0, pb, D, nullptr, false);
+  panel_trsm_rows(Fs, f, p0, pb, D, p0 + pb + blockIdx.y * (kThreads / 32) + threadIdx.x / 32,
+                  gridDim.y * (kThreads / 32));
+}
+
+__global__ void __launch_bounds__(kThreads)
+    mf_panel_syrk_kernel(pf_mf_plan_t p, const int32_t *__restrict__ nodes, int p0, double *F) {
+  __shared__ double Ai[64][kT + 1];
+  __shared__ double Al[64][kT + 1];
+  const int s = nodes[blockIdx.x];
+  const int c = p.cn[s], f = p.fn[s];
+  if (p0 >= c) return;
+  const int pb = min(kT, c - p0);
+  const int nb = (f - p0 - pb + 63) / 64;
+  for (int pr = blockIdx.y; pr < nb * (nb + 1) / 2; pr += gridDim.y) {
+    int ti, tl;
+    tri_pair(pr, ti, tl);
+    panel_syrk_tile(F + p.foff[s], f, p0, pb, ti, tl, Ai, Al);
   }
 }
 
@@ -476,7 +575,7 @@ __global__ void __launch_bounds__(kBT, 2)
                        const double *__restrict__ O, const int32_t *__restrict__ item_node,
                        const int32_t *__restrict__ item_rb, const int32_t *__restrict__ item_cb0,
                        const int32_t *__restrict__ item_cb1, double *P, int64_t ldp) {
-  // dynamic smem: [A ring | B ring | coff[kBM] | ybase[2 * ncb] | roff[f]]
+  // dynamic smem: [A ring | B ring | coff[kBM] | ysrc[2 ncb] | kt0[ncb] | roff[f]]
   extern __shared__ __align__(128) double dyn[];
   double *As = dyn, *Bs = dyn + kGStages * kBStageA;
   int64_t *coff = reinterpret_cast<int64_t *>(dyn + kGStages * (kBStageA + kBStageB));
@@ -488,7 +587,10 @@ __global__ void __launch_bounds__(kBT, 2)
   const int i0 = item_rb[blockIdx.x] * kBM;
   // column blocks of 128 = pairs of 64-column plan tiles [2 cb, 2 cb + 1]
   const int cb0 = item_cb0[blockIdx.x], ncb = item_cb1[blockIdx.x] - cb0;
-  int64_t *roff = reinterpret_cast<int64_t *>(ysrc + 2 * ncb);
+  // first K stage per column block: a block no boundary column reached in the
+  // forward has Y_C = 0, so its K range starts at the X_R rows
+  int64_t *kt0 = reinterpret_cast<int64_t *>(ysrc + 2 * ncb);
+  int64_t *roff = kt0 + ncb;
   {
     const int32_t *Cv = p.perm_orig + p.c0[s];
     const int32_t *Rv = p.r_orig + p.r_ptr[s];
@@ -504,13 +606,20 @@ __global__ void __launch_bounds__(kBT, 2)
     for (int r = tid; r < kBM; r += kBT) coff[r] = i0 + r < c ? (int64_t)Cv[i0 + r] * ldp : -1;
   }
   __syncthreads();
+  for (int cb = tid; cb < ncb; cb += kBT)
+    kt0[cb] = (ysrc[2 * cb] || ysrc[2 * cb + 1]) ? 0 : c / kGBK;
+  __syncthreads();
   const double *A = M + p.m_off[s] + (int64_t)i0 * ldf;
   const int ma = min(kBM, c - i0);
   const int nkt = (f + kGBK - 1) / kGBK;
   // copy slots: A rows ra + 32u (chunk cha); B rows rbr + 4u (chunk chb: 64 per row)
   const int ra = tid >> 3, cha = tid & 7, rbr = tid >> 6, chb = tid & 63;
   const int half = chb >> 5;  // which 64-column plan tile of the block
-  int icb = 0, ikt = 0, ist = 0;  // next (column block, k stage, ring slot) to issue
+  int icb = 0, ikt = (int)kt0[0], ist = 0;  // next (column block, k stage, ring slot)
+  while (icb < ncb && ikt >= nkt) {
+    ++icb;
+    ikt = icb < ncb ? (int)kt0[icb] : 0;
+  }
   auto issue = [&]() {
     if (icb < ncb) {
       const int k0 = ikt * kGBK;
@@ -539,9 +648,11 @@ __global__ void __launch_bounds__(kBT, 2)
         const double *src = (l < f && base) ? base + ro[u] : g_zero + 2 * (chb & 31);
         cp_async16(bs + r * kSB2 + 2 * chb, src);
       }
-      if (++ikt == nkt) {
-        ikt = 0;
-        ++icb;
+      if (++ikt >= nkt) {
+        do {
+          ++icb;
+          ikt = icb < ncb ? (int)kt0[icb] : 0;
+        } while (icb < ncb && ikt >= nkt);
       }
       ist = ist == kGStages - 1 ? 0 : ist + 1;
     }
@@ -558,7 +669,7 @@ __global__ void __launch_bounds__(kBT, 2)
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    for (int kt = 0; kt < nkt; ++kt) {
+    for (int kt = (int)kt0[cb]; kt < nkt; ++kt) {
       cp_wait<kGStages - 2>();
       __syncthreads();
       issue();
@@ -601,29 +712,63 @@ __device__ __forceinline__ void atomic_max_nonneg(unsigned long long *p, double 
 }
 
 // Warp per interior row: max_j |diag[v] P[v,j] + sum_e off[e] P[u_e, j]|,
-// boundary neighbours contributing off[e] to column bcol[u].
-__global__ void residual_kernel(const double *__restrict__ P, int64_t ldp, int64_t n, int64_t k,
-                                const uint8_t *__restrict__ isb, const int32_t *__restrict__ bcol,
-                                const int64_t *__restrict__ nb_ptr,
-                                const int32_t *__restrict__ nb_idx,
-                                const double *__restrict__ off, const double *__restrict__ diag,
-                                unsigned long long *out) {
-  const int lane = threadIdx.x % 32;
+// boundary neighbours contributing off[e] to column bcol[u].  The row's
+// neighbour list is staged once per row in shared memory; columns go in
+// 16-byte pairs (ldp is a multiple of 64, so every pair is in the row).
+__global__ void __launch_bounds__(256)
+    residual_kernel(const double *__restrict__ P, int64_t ldp, int64_t n, int64_t k,
+                    const uint8_t *__restrict__ isb, const int32_t *__restrict__ bcol,
+                    const int64_t *__restrict__ nb_ptr, const int32_t *__restrict__ nb_idx,
+                    const double *__restrict__ off, const double *__restrict__ diag,
+                    unsigned long long *out) {
+  constexpr int kMaxDeg = 32;
+  __shared__ int64_t nrow[8][kMaxDeg];  // P offset of an interior neighbour, or -1-bcol
+  __shared__ double nw[8][kMaxDeg];
+  const int lane = threadIdx.x % 32, w = threadIdx.x / 32;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
   double mx = 0.0;
-  for (int64_t v = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32; v < n;
-       v += warps) {
+  for (int64_t v = blockIdx.x * (int64_t)(blockDim.x / 32) + w; v < n; v += warps) {
     if (isb[v]) continue;
-    const int64_t e0 = nb_ptr[v], e1 = nb_ptr[v + 1];
-    const double dv = diag[v];
-    for (int64_t j = lane; j < k; j += 32) {
-      double acc = dv * P[v * ldp + j];
-      for (int64_t e = e0; e < e1; ++e) {
-        const int32_t u = nb_idx[e];
-        const double x = isb[u] ? (bcol[u] == j ? 1.0 : 0.0) : P[(int64_t)u * ldp + j];
-        acc += off[e] * x;
+    const int64_t e0 = nb_ptr[v];
+    const int deg = (int)(nb_ptr[v + 1] - e0);
+    if (deg > kMaxDeg) {  // exact per-column evaluation for a (rare) high-valence row
+      for (int64_t j = lane; j < k; j += 32) {
+        double acc = diag[v] * P[v * ldp + j];
+        for (int64_t e = e0; e < e0 + deg; ++e) {
+          const int32_t u = nb_idx[e];
+          const double x = isb[u] ? (bcol[u] == j ? 1.0 : 0.0) : P[(int64_t)u * ldp + j];
+          acc += off[e] * x;
+        }
+        mx = fmax(mx, fabs(acc));
       }
-      mx = fmax(mx, fabs(acc));
+      continue;
+    }
+    __syncwarp();
+    if (lane < deg) {
+      const int32_t u = nb_idx[e0 + lane];
+      nrow[w][lane] = isb[u] ? -1 - (int64_t)bcol[u] : (int64_t)u * ldp;
+      nw[w][lane] = off[e0 + lane];
+    }
+    __syncwarp();
+    const double dv = diag[v];
+    for (int64_t j = 2 * lane; j < k; j += 64) {
+      const double2 pv = *reinterpret_cast<const double2 *>(P + v * ldp + j);
+      double a0 = dv * pv.x, a1 = dv * pv.y;
+      for (int e = 0; e < deg; ++e) {
+        const int64_t ro = nrow[w][e];
+        const double we = nw[w][e];
+        if (ro >= 0) {
+          const double2 x = *reinterpret_cast<const double2 *>(P + ro + j);
+          a0 += we * x.x;
+          a1 += we * x.y;
+        } else {
+          const int64_t b = -1 - ro;
+          if (b == j) a0 += we;
+          if (b == j + 1) a1 += we;
+        }
+      }
+      mx = fmax(mx, fabs(a0));
+      if (j + 1 < k) mx = fmax(mx, fabs(a1));
     }
   }
   mx = warp_max(mx);
@@ -689,13 +834,32 @@ int pf_cotan_laplacian_f64(const double *V, const int32_t *T, int64_t nt, const 
 }
 
 int pf_mf_factor_level(const pf_mf_plan_t *plan, const double *off, const double *diag,
-                       const int32_t *nodes, int64_t count, double *F, int32_t *err,
-                       pf_stream_t stream) {
-  if (!plan || !off || !diag || !nodes || !F || !err || count < 0)
+                       const int32_t *nodes, int64_t count, int32_t max_f, int32_t max_c,
+                       int split, double *F, int32_t *err, pf_stream_t stream) {
+  if (!plan || !off || !diag || !nodes || !F || !err || count < 0 || max_f < 0 || max_c < 0)
     return fail(PF_E_ARG, "pf_mf_factor_level: bad argument");
   if (count == 0) return 0;
-  mf_factor_kernel<<<(unsigned)count, kThreads, 0, as_stream(stream)>>>(*plan, off, diag, nodes,
-                                                                        F, err);
+  cudaStream_t st = as_stream(stream);
+  if (!split) {
+    mf_factor_kernel<<<(unsigned)count, kThreads, 0, st>>>(*plan, off, diag, nodes, F, err);
+    return check_launch("pf_mf_factor_level");
+  }
+  // few large fronts: spread every step of each front over ~2 waves of CTAs
+  const int target = 2 * sm_count();
+  const int per = (int)std::max<int64_t>(1, (target + count - 1) / count);
+  mf_assemble_split_kernel<<<dim3((unsigned)count, (unsigned)std::min(per, std::max(1, max_f / 16))),
+                             kThreads, 0, st>>>(*plan, off, diag, nodes, F);
+  for (int p0 = 0; p0 < max_c; p0 += kT) {
+    mf_panel_diag_kernel<<<(unsigned)count, kThreads, 0, st>>>(*plan, nodes, p0, F, err);
+    const int rows = max_f - p0;
+    const int ty = std::max(1, std::min(per, (rows + kThreads / 32 - 1) / (kThreads / 32)));
+    mf_panel_trsm_kernel<<<dim3((unsigned)count, (unsigned)ty), kThreads, 0, st>>>(*plan, nodes,
+                                                                                  p0, F);
+    const int nb = (rows - 1 + 63) / 64;
+    const int pairs = std::max(1, nb * (nb + 1) / 2);
+    mf_panel_syrk_kernel<<<dim3((unsigned)count, (unsigned)std::min(pairs, std::max(per, 1))),
+                           kThreads, 0, st>>>(*plan, nodes, p0, F);
+  }
   return check_launch("pf_mf_factor_level");
 }
 
@@ -741,7 +905,7 @@ int pf_mf_backward_level(const pf_mf_plan_t *plan, const double *M, const double
     return fail(PF_E_ARG, "pf_mf_backward_level: bad argument (ldp must be a multiple of 64)");
   if (count == 0) return 0;
   if (max_f < 1 || max_ncb < 1) return fail(PF_E_ARG, "pf_mf_backward_level: bad limits");
-  const size_t smem = kBRing + 8 * ((size_t)kBM + 2 * max_ncb + max_f);
+  const size_t smem = kBRing + 8 * ((size_t)kBM + 3 * max_ncb + max_f);
   if (int rc = ensure_smem((const void *)mf_bwd_gemm_kernel, smem)) return rc;
   mf_bwd_gemm_kernel<<<(unsigned)count, kBT, smem, as_stream(stream)>>>(
       *plan, M, O, item_node, item_rb, item_cb0, item_cb1, P, ldp);
@@ -753,8 +917,8 @@ int pf_poisson_residual(const double *P, int64_t ldp, int64_t n, int64_t k,
                         const int32_t *nb_idx, const double *off, const double *diag,
                         unsigned long long *out_max, pf_stream_t stream) {
   if (!P || !is_boundary || !bcol || !nb_ptr || !nb_idx || !off || !diag || !out_max ||
-      n < 0 || k < 0 || ldp < k)
-    return fail(PF_E_ARG, "pf_poisson_residual: bad argument");
+      n < 0 || k < 0 || ldp < k || (ldp & 1) || (reinterpret_cast<uintptr_t>(P) & 15))
+    return fail(PF_E_ARG, "pf_poisson_residual: bad argument (ldp even, P 16-byte aligned)");
   if (n == 0) return 0;
   residual_kernel<<<grid_for(n, 8), 256, 0, as_stream(stream)>>>(
       P, ldp, n, k, is_boundary, bcol, nb_ptr, nb_idx, off, diag, out_max);

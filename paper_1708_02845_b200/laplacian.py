@@ -150,6 +150,7 @@ class DevicePoisson:
     """
 
     GEMM_TARGET = 2 * 148  # CTAs per backward level before column blocks are split
+    SPLIT_BELOW = 148      # levels with fewer fronts factor each front over many CTAs
 
     def __init__(self, mesh, leaf: int = LEAF, device=None):
         from . import _device as dev
@@ -191,6 +192,10 @@ class DevicePoisson:
         self.bcol = tod(bcol, np.int32)
         # ---- launch lists ------------------------------------------------
         self.levels = [tod(lv, np.int32) for lv in pl.levels]
+        # (max f, max c, split) per level: few fronts -> every step over many CTAs
+        self.level_shape = [(int(f[lv].max()) if len(lv) else 0,
+                             int(c[lv].max()) if len(lv) else 0,
+                             int(len(lv) < self.SPLIT_BELOW)) for lv in pl.levels]
         all_nodes = np.arange(pl.nodes, dtype=np.int64)
         ct = (c + 31) // 32
         inv_node = np.repeat(all_nodes, ct)
@@ -270,10 +275,10 @@ class DevicePoisson:
             F = t.empty(max(self.plan.stats["f_total"], 1), dtype=t.float64, device=self.device)
             err = t.zeros(1, dtype=t.int32, device=self.device)
             s = self.stream()
-            for lv in self.levels:
+            for lv, (mf, mc, split) in zip(self.levels, self.level_shape):
                 nat.call("pf_mf_factor_level", ctypes.addressof(self.struct), off.data_ptr(),
-                         diag.data_ptr(), lv.data_ptr(), lv.numel(), F.data_ptr(),
-                         err.data_ptr(), s)
+                         diag.data_ptr(), lv.data_ptr(), lv.numel(), mf, mc, split,
+                         F.data_ptr(), err.data_ptr(), s)
             Mt = t.zeros(max(int(self.mt_off[-1]), 1), dtype=t.float64, device=self.device)
             M = t.zeros(max(int(self.m_off[-1]), 1), dtype=t.float64, device=self.device)
             inode, ict, icnt, nodes = self.inv
