@@ -628,6 +628,96 @@ def extra_wire(t, dev, pf, device):
                     "expressions on 100,000 values x 10.01"}
 
 
+def extra_poisson(t, nat, dev, device, dfma_peak=None):
+    """the Poisson kernel P itself on the device (cotan Laplacian,
+    nested-dissection multifrontal Cholesky, multi-RHS solves) at C2 and C4,
+    beside the reference algorithm (SuperLU factor + column solves,
+    oracle/inputs.poisson_kernel_parallel on all host cores) at C2."""
+    import numpy as np
+    from oracle import inputs as I
+    import paper_1708_02845_b200.laplacian as L
+    specs = {"c2": {"gen": "rectangle", "length": 50.0, "width": 1.0, "spacing": 0.024},
+             "c4": {"gen": "holes", "spacing": 0.0017, "size": [2.0, 1.25],
+                    "holes": [[0.2 + 0.4 * i, 0.16 + 0.31 * j, 0.0034]
+                              for i in range(5) for j in range(4)]}}
+    if dfma_peak is None:  # measured sustained DFMA rate of this GPU (pf_probe_dfma_f64)
+        import ctypes
+        fl = ctypes.c_int64(0)
+        probe = t.empty(2, dtype=t.float64, device=device)
+        s = t.cuda.current_stream(device)
+        nat.call("pf_probe_dfma_f64", 1 << 14, ctypes.byref(fl), probe.data_ptr(), s.cuda_stream)
+        t.cuda.synchronize()
+        p0, p1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
+        p0.record(s)
+        nat.call("pf_probe_dfma_f64", 1 << 16, ctypes.byref(fl), probe.data_ptr(), s.cuda_stream)
+        p1.record(s)
+        t.cuda.synchronize()
+        dfma_peak = fl.value / (p0.elapsed_time(p1) / 1e3) / 1e12
+    out = {"dfma_peak_tflops": dfma_peak}
+    for name, spec in specs.items():
+        t0 = time.perf_counter()
+        mesh = I.build(spec)
+        mesh_s = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        dp = L.DevicePoisson(mesh)
+        setup_s = time.perf_counter() - t0
+        ev = lambda: t.cuda.Event(enable_timing=True)  # noqa: E731
+        P, reps = None, []
+        for rep in range(3):
+            dp._lap, dp._F = None, None
+            t.cuda.synchronize()
+            e0, e1 = ev(), ev()
+            phases = {}
+            e0.record()
+            dp.laplacian()
+            dp.factor()
+            P, residual, rse = dp.solve(P, events=phases)
+            e1.record()
+            t.cuda.synchronize()
+            if rep:
+                reps.append((e0.elapsed_time(e1), phases["fwd0"].elapsed_time(phases["bwd0"]),
+                             phases["bwd0"].elapsed_time(phases["bwd1"]),
+                             e0.elapsed_time(phases["fwd0"])))
+        tot, fwd, bwd, fac = (float(np.median([r[i] for r in reps])) for i in range(4))
+        fl = dp.solve_flops()
+        st = dp.plan.stats
+        res = {"workload": f"{name}: {dp.n:,} vertices x {dp.k:,} boundary columns "
+                           f"({dp.n * dp.k * 8 / 1e9:.2f} GB FP64 P, device-resident)",
+               "total_ms": tot, "laplacian_factor_inverse_ms": fac, "forward_ms": fwd,
+               "backward_ms": bwd, "residual": residual, "row_sum_error": rse,
+               "fronts": st["nodes"], "levels": st["levels"], "max_front": st["max_f"],
+               "host_plan_and_upload_s": setup_s, "mesh_build_s": mesh_s,
+               "backward_roofline": {
+                   "bound": "fp64", "unit": "TFLOP/s",
+                   "achieved": fl["backward"] / (bwd * 1e-3) / 1e12,
+                   "issued": fl["backward_issued"] / (bwd * 1e-3) / 1e12,
+                   "peak": dfma_peak, "frac": (fl["backward"] / (bwd * 1e-3) / 1e12 / dfma_peak
+                                               if dfma_peak else None),
+                   "algorithmic_flops": fl["backward"],
+                   "kernel": "pf::mf_bwd_gemm_kernel (DMMA m8n8k4, gathered rows)"}}
+        if name == "c2":
+            t0 = time.perf_counter()
+            ref, _ = I.poisson_kernel_parallel(mesh, workers=os.cpu_count() or 8)
+            cpu_s = time.perf_counter() - t0
+            idx = np.random.default_rng(0).choice(np.asarray(mesh.interior_vertices), 2000,
+                                                  replace=False)
+            x = P[t.from_numpy(idx).to(P.device), :dp.k].cpu().numpy()
+            y = ref[idx]
+            big = y > 1e-290
+            res["cpu_baseline"] = {"value_s": cpu_s, "cores": os.cpu_count(), "kind": "port",
+                                   "sample": "SuperLU factor of -Lc_II + solves of all k "
+                                             "columns in 64-column chunks, one process per "
+                                             "core (oracle/inputs.poisson_kernel_parallel)"}
+            res["speedup_vs_cpu"] = cpu_s / (tot * 1e-3)
+            res["max_rel_vs_superlu_2000_rows"] = float(
+                (np.abs(x[big] - y[big]) / y[big]).max())
+            del ref
+        out[name] = res
+        del P, dp
+        t.cuda.empty_cache()
+    return out
+
+
 def extra_tracer(t, nat, dev, pf, device):
     """C5 tracer shape: 10,000 paths on a 1,002,001-vertex mesh, 1,024 target fields."""
     import numpy as np
@@ -843,6 +933,10 @@ def run_native(args):
                 ("c4_c5", "c4c5", lambda: extra_c4_and_c5(t, nat, dev, pf, device, args.steps,
                                                           peak)),
                 ("c5_tracer", "tracer", lambda: extra_tracer(t, nat, dev, pf, device)),
+                ("poisson", "poisson", lambda: extra_poisson(
+                    t, nat, dev, device,
+                    ((extras.get("c5_batched_kl") or {}).get("fp64_dmma_path") or {}).get(
+                        "dfma_peak_tflops"))),
                 ("wire", "wire", lambda: extra_wire(t, dev, pf, device))):
             if key not in want:
                 continue
@@ -893,8 +987,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the C3/C4/C5/tracer side measurements (N=1 only)")
-    ap.add_argument("--extras", default="f32,c3,c4c5,tracer,wire",
-                    help="comma list of side measurements to run (f32, c3, c4c5, tracer, wire)")
+    ap.add_argument("--extras", default="f32,c3,c4c5,tracer,wire,poisson",
+                    help="comma list of side measurements to run "
+                         "(f32, c3, c4c5, tracer, wire, poisson)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

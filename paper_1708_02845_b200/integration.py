@@ -15,6 +15,8 @@ so each site is patched explicitly):
     (domain.py also binds edge_descent, find_local_minima, path_hausdorff)
     pathfield.fileio.{field_to_csv, field_to_json, path_to_csv}   (fileio.py:37-75)
     pathfield.service.app.field_to_csv                            (app.py:18, 114)
+    pathfield.{solvers, domain, bench, ""}.poisson_kernel         (solvers.py:278-303;
+        DomainContext.kernel, domain.py:54-61, builds P on the GPU and keeps it resident)
 
 Results are converted to the reference's own dataclasses (``ScalarField``,
 ``TracedPath``), and the reference's ``PoissonKernel`` objects are accepted
@@ -59,6 +61,12 @@ def _wrap(pathfield):
     def dv_field(pk, fd, p, swap_order=False, clamp=None):
         return to_field(_div.dv_field(pk, fd, p, swap_order=swap_order, clamp=clamp))
 
+    solvers = importlib.import_module(pathfield.__name__ + ".solvers")
+
+    def poisson_kernel(ls, settings=None):
+        from . import laplacian as _lap
+        return _lap.poisson_kernel(ls, settings, kernel_type=solvers.PoissonKernel)
+
     def triangle_descent(mesh, field, source, settings=None):
         from .config import DEFAULTS
         return to_path(_paths.triangle_descent(mesh, field, source, settings or DEFAULTS))
@@ -80,6 +88,7 @@ def _wrap(pathfield):
         "field_to_csv": _fileio.field_to_csv,
         "field_to_json": _fileio.field_to_json,
         "path_to_csv": _fileio.path_to_csv,
+        "poisson_kernel": poisson_kernel,
     }
 
 
@@ -87,10 +96,12 @@ SITES = {
     "divergence": ("dv_field", "dv_at", "dv_pair", "sparsify", "dv_pair_sparse",
                    "dv_pair_sparse_stats"),
     "": ("dv_field", "dv_pair", "dv_pair_sparse", "sparsify", "triangle_descent",
-         "triangle_gradient", "edge_descent", "find_local_minima", "path_hausdorff"),
+         "triangle_gradient", "edge_descent", "find_local_minima", "path_hausdorff",
+         "poisson_kernel"),
     "domain": ("dv_field", "sparsify", "triangle_descent", "edge_descent", "find_local_minima",
-               "path_hausdorff"),
-    "bench": ("dv_at", "dv_field", "dv_pair_sparse_stats"),
+               "path_hausdorff", "poisson_kernel"),
+    "bench": ("dv_at", "dv_field", "dv_pair_sparse_stats", "poisson_kernel"),
+    "solvers": ("poisson_kernel",),
     "paths": ("triangle_descent", "triangle_gradient", "edge_descent", "find_local_minima",
               "path_hausdorff", "resample_polyline"),
     "fileio": ("field_to_csv", "field_to_json", "path_to_csv"),

@@ -294,11 +294,15 @@ class DevicePoisson:
         return self._F
 
     # -- solvers.py:278-303 ------------------------------------------------
-    def solve(self, P_out=None):
+    def solve(self, P_out=None, events: dict | None = None):
         """P (device, n x round_up(k, 64) FP64, pads zero) with the reference's
-        diagnostics.  Returns (P, residual, row_sum_error)."""
+        diagnostics.  Returns (P, residual, row_sum_error).  `events`, if given,
+        receives CUDA events bracketing the forward / backward / diagnostics
+        phases on the launch stream."""
         from . import _device as dev
         t = dev.torch()
+        mark = (lambda name: events.setdefault(name, t.cuda.Event(enable_timing=True)).record(
+            t.cuda.current_stream(self.device))) if events is not None else (lambda name: None)
         off, diag = self.laplacian()
         Mt, M = self.factor()
         ld = round_up_cols(self.k)
@@ -310,14 +314,17 @@ class DevicePoisson:
         Wb = t.empty(self.w_total, dtype=t.float64, device=self.device)
         s = self.stream()
         ps = ctypes.addressof(self.struct)
+        mark("fwd0")
         for (an, ai, aw, acnt, gn, gi, gw, grb, gcnt) in self.fwd:
             nat.call("pf_mf_forward_level", ps, Mt.data_ptr(), off.data_ptr(), an.data_ptr(),
                      ai.data_ptr(), aw.data_ptr(), acnt, gn.data_ptr(), gi.data_ptr(),
                      gw.data_ptr(), grb.data_ptr(), gcnt, Wb.data_ptr(), O.data_ptr(), s)
+        mark("bwd0")
         for nodes, rb, cb0, cb1, cnt, maxf, ncb in reversed(self.bwd):
             nat.call("pf_mf_backward_level", ps, M.data_ptr(), O.data_ptr(), nodes.data_ptr(),
                      rb.data_ptr(), cb0.data_ptr(), cb1.data_ptr(), cnt, maxf, ncb,
                      P.data_ptr(), ld, s)
+        mark("bwd1")
         mx = t.zeros(2, dtype=t.int64, device=self.device)
         dm = self.dm
         nat.call("pf_poisson_residual", P.data_ptr(), ld, self.n, self.k,
@@ -325,10 +332,38 @@ class DevicePoisson:
                  dm.nb_idx.data_ptr(), off.data_ptr(), diag.data_ptr(), mx.data_ptr(), s)
         nat.call("pf_poisson_finalize", P.data_ptr(), ld, self.n, self.k,
                  self.is_boundary.data_ptr(), self.bcol.data_ptr(), mx.data_ptr() + 8, s)
+        mark("end")
         del O, Wb
         r = mx.cpu().numpy().astype(np.uint64)
         residual = _u64_to_f64(int(r[0])) if self.plan.m else 0.0
         return P, residual, _u64_to_f64(int(r[1]))
+
+    def solve_flops(self) -> dict:
+        """Algorithmic FP64 work of the solves (SURVEY §8d convention): the
+        triangular-solve count sum_s (c^2 + 2 c r) per column for each of the
+        backward (all k columns) and the forward (its active 64-column tiles),
+        plus what the backward GEMM issues (2 c f per column, less the
+        skipped zero Y rows of unreached tiles)."""
+        pl = self.plan
+        c = pl.cn.astype(np.float64)
+        r = pl.rn.astype(np.float64)
+        f = pl.fn.astype(np.float64)
+        per_col = c * c + 2 * c * r
+        k = float(self.k)
+        act = np.diff(pl.act_ptr).astype(np.float64)
+        issued = 0.0
+        nblk = (pl.ntiles + 1) // 2
+        ti = pl.tile_item.reshape(pl.nodes, pl.ntiles)
+        if pl.ntiles % 2:
+            ti = np.concatenate([ti, -np.ones((pl.nodes, 1), np.int64)], axis=1)
+        blk_active = (ti.reshape(pl.nodes, nblk, 2) >= 0).any(axis=2)
+        width = np.minimum(128.0, k - 128.0 * np.arange(nblk))
+        kskip = np.floor(c / 16) * 16
+        keff = np.where(blk_active, f[:, None], (f - kskip)[:, None])
+        issued = float((2.0 * c[:, None] * keff * width[None, :]).sum())
+        return {"backward": float(per_col.sum() * k),
+                "forward": float((per_col * act).sum() * TILE),
+                "backward_issued": issued}
 
     def device_kernel(self, P=None):
         """Solve and wrap P as a DeviceKernel (the hot path's input)."""
@@ -393,26 +428,78 @@ def poisson_kernel_device(ls_or_mesh, leaf: int = LEAF):
     return solver.device_kernel()
 
 
-def poisson_kernel(ls, settings=None):
-    """solvers.py:278-303: the PoissonKernel of a LaplacianSet (or mesh).
+def dense_to_host(P, n: int, k: int, chunk_rows: int = 16384, threads: int = 8) -> np.ndarray:
+    """Host (n, k) copy of a device P (row stride >= k): row chunks are copied
+    D2H into two alternating pinned buffers while a thread pool scatters the
+    previous chunk into the numpy result (a direct pageable copy of a strided
+    33 GB matrix runs at a fraction of the PCIe rate)."""
+    from concurrent.futures import ThreadPoolExecutor
+    from . import _device as dev
+    t = dev.torch()
+    out = np.empty((n, k))
+    if n == 0:
+        return out
+    ld = P.stride(0)
+    rows = max(1, min(chunk_rows, n))
+    bufs = [t.empty((rows, ld), dtype=t.float64, pin_memory=True) for _ in range(2)]
+    evs = [t.cuda.Event() for _ in range(2)]
+    stream = t.cuda.Stream(P.device)
+    stream.wait_stream(t.cuda.current_stream(P.device))
+    pool = ThreadPoolExecutor(threads)
+
+    def scatter(buf, a, b):
+        src = buf.numpy()
+        step = -(-(b - a) // threads)
+        futs = [pool.submit(np.copyto, out[a + i:min(b, a + i + step)],
+                            src[i:min(b - a, i + step), :k]) for i in range(0, b - a, step)]
+        for fu in futs:
+            fu.result()
+
+    pending = None
+    try:
+        for ci, a in enumerate(range(0, n, rows)):
+            b = min(n, a + rows)
+            j = ci & 1
+            with t.cuda.stream(stream):
+                bufs[j][:b - a].copy_(P[a:b], non_blocking=True)
+                evs[j].record(stream)
+            if pending is not None:
+                pj, pa, pb = pending
+                evs[pj].synchronize()
+                scatter(bufs[pj], pa, pb)
+            pending = (j, a, b)
+        pj, pa, pb = pending
+        evs[pj].synchronize()
+        scatter(bufs[pj], pa, pb)
+    finally:
+        pool.shutdown()
+    return out
+
+
+def poisson_kernel(ls, settings=None, kernel_type=None):
+    """solvers.py:278-303: the PoissonKernel of a LaplacianSet (this package's
+    or the reference's: only ``.mesh`` is read) or of a mesh.
 
     P is computed on the device and stays resident there (registered as the
-    device mirror of the returned ``dense``); ``dense`` is its host copy, as
-    the reference's return type requires."""
+    device mirror of the returned ``dense``, so the hot path never re-uploads
+    it); ``dense`` is its host copy, as the reference's return type requires.
+    ``kernel_type`` builds the reference's own PoissonKernel class in drop-in
+    mode (integration.py)."""
     import warnings
     from . import _device as dev
     from .config import DEFAULTS
     from .solvers import PoissonKernel, PrecisionWarning
     settings = settings or DEFAULTS
-    dk = poisson_kernel_device(ls)
-    dense = np.empty((dk.n, dk.k))
-    t = dev.torch()
-    t.from_numpy(dense).copy_(dk.P[:, :dk.k])
+    mesh = getattr(ls, "mesh", ls)
+    solver = ls.solver if isinstance(ls, LaplacianSet) else DevicePoisson(mesh)
+    dk = solver.device_kernel()
+    dense = dense_to_host(dk.P, dk.n, dk.k)
     if dk.residual > settings.residual_warn:
         warnings.warn(f"poisson kernel residual {dk.residual:.2e}", PrecisionWarning,
                       stacklevel=2)
-    pk = PoissonKernel(dense, np.asarray(dk_boundary(ls)).copy(), dk.residual,
-                       dk.row_sum_error)
+    cls = kernel_type or PoissonKernel
+    pk = cls(dense, np.asarray(mesh.boundary_vertices, dtype=np.int64).copy(), dk.residual,
+             dk.row_sum_error)
     dev.register(pk.dense, dk)
     return pk
 

@@ -26,6 +26,16 @@ assert D.dv_field.__module__.startswith("paper_1708_02845_b200"), D.dv_field
 assert Dom.dv_field is D.dv_field is pathfield.dv_field
 assert Pth.triangle_descent is Dom.triangle_descent is pathfield.triangle_descent
 assert Dom.sparsify is pf.sparsify
+import pathfield.solvers as Sol
+assert Sol.poisson_kernel is Dom.poisson_kernel is pathfield.poisson_kernel      # GPU P build
+assert Sol.poisson_kernel.__module__.startswith("paper_1708_02845_b200")
+from pathfield.mesh import generate_disk_mesh
+from pathfield.laplacian import assemble_cotan
+try:
+    Dom.DomainContext(generate_disk_mesh(4)).kernel   # DomainContext.kernel -> device build
+    raise SystemExit("silent fallback (poisson_kernel)")
+except PathfieldError as e:
+    assert "CUDA" in str(e) or "built" in str(e), e
 dense = np.array([[0.5, 0.5, 0.0], [0.2, 0.3, 0.5], [0.0, 0.0, 1.0]])
 pk = pathfield.solvers.PoissonKernel(dense, np.array([2]), 0.0, 0.0)
 try:
@@ -40,6 +50,7 @@ except PathfieldError as e:
     assert "CUDA" in str(e) or "built" in str(e), e
 integration.uninstall()
 assert D.dv_field.__module__ == "pathfield.divergence"
+assert Sol.poisson_kernel.__module__ == "pathfield.solvers"
 print("OK", sorted(done))
 '''
 
