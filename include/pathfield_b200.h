@@ -524,15 +524,16 @@ int pf_mf_forward_level(const pf_mf_plan_t *plan, const double *Mt, const double
                         double *O, pf_stream_t stream);
 
 /* Backward solve of one level (levels top-down): X_C = M [Y_C; X_R] for items
- * (node, 64-row block of C, 128-column blocks [cb0, cb1)), Y_C from O (zero
- * for tiles the forward never reached), X_R from P's rows, X_C into P (rows
- * by original vertex id; ldp a multiple of 64).  max_f / max_ncb bound the
- * items' front sizes and column-block counts (shared-memory sizing). */
+ * (node, nb_rows-row block of C, 128-column blocks [cb0, cb1)), Y_C from O
+ * (zero for tiles the forward never reached), X_R from P's rows, X_C into P
+ * (rows by original vertex id; ldp a multiple of 64).  nb_rows in {8, 16, 32,
+ * 64}; max_f / max_ncb bound the items' front sizes and column-block counts
+ * (shared-memory sizing). */
 int pf_mf_backward_level(const pf_mf_plan_t *plan, const double *M, const double *O,
                          const int32_t *item_node, const int32_t *item_rb,
                          const int32_t *item_cb0, const int32_t *item_cb1, int64_t count,
-                         int32_t max_f, int32_t max_ncb, double *P, int64_t ldp,
-                         pf_stream_t stream);
+                         int32_t max_f, int32_t max_ncb, int32_t nb_rows, double *P,
+                         int64_t ldp, pf_stream_t stream);
 
 /* residual = max |(Lc P)[v, j]| over interior rows v and columns j < k with
  * P's boundary rows taken as indicators (= |Lc_II P_IB + Lc_IB|, solvers.py:

@@ -101,7 +101,7 @@ _SIGS.update({
     "pf_mf_forward_level": [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp,
                             c_i64, c_vp, c_vp, c_vp],
     "pf_mf_backward_level": [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_int, c_int,
-                             c_vp, c_i64, c_vp],
+                             c_int, c_vp, c_i64, c_vp],
     "pf_poisson_residual": [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                             c_vp],
     "pf_poisson_finalize": [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp],

@@ -560,35 +560,43 @@ __global__ void __launch_bounds__(kGT)
 //   X_C = M [Y_C; X_R],  M = Mt^T = [L_CC^{-T} | -L_CC^{-T} L_RC^T]
 // Y_C from the forward blocks (zero where the tile was never reached), X_R
 // gathered from P's rows (final: ancestors ran earlier), X_C into P.
-// 64 (C rows) x 128 (columns) output tile per CTA: 8 warps as 2 (m) x 4 (n)
-// with 32 x 32 warp tiles (16 DMMAs per 4-deep k step), 16-deep K stages in a
-// 3-stage cp.async ring (81 KB: 2 CTAs = 16 warps per SM), stage counters
-// instead of divisions, and every gather offset resolved in shared memory
-// before the main loop (the issue path is branch-free selects).
-constexpr int kBM = 64, kBN = 128, kBT = 256;
+// Output tile per CTA: 128 P columns (M dimension of the MMA) x NB rows of C
+// (N dimension, NB in {8, 16, 32, 64} chosen per level from its separator
+// sizes, so a 12-vertex separator pads to 16, not 64):
+//   X_C^T (cols x NB) = Z^T (cols x f) . M^T (f x NB),  Z = [Y_C; X_R].
+// 8 warps, each 16 columns x NB (2 x NB/8 m8n8k4 DMMAs per 4-deep k step);
+// Z rows (128 contiguous doubles, gathered from P or the forward's Y blocks)
+// and M rows stream through a 3-stage cp.async ring of 16-deep K stages;
+// stage counters instead of divisions; every gather offset is resolved in
+// shared memory before the main loop (branch-free selects in the issue
+// path); column blocks whose tiles the forward never reached skip the zero
+// Y rows of K.
+constexpr int kBN = 128, kBT = 256;
 constexpr int kSB2 = kBN + 4;  // 4 mod 16: conflict-free half-warp fragment loads
-constexpr int kBStageA = kBM * kSA, kBStageB = kGBK * kSB2;
-constexpr int kBRing = kGStages * (kBStageA + kBStageB) * 8;  // bytes
+constexpr int kZStage = kGBK * kSB2;
+template <int NB>
+constexpr int m_stage() { return NB * kSA; }
+template <int NB>
+constexpr int bwd_ring_bytes() { return kGStages * (kZStage + m_stage<NB>()) * 8; }
 
+template <int NB>
 __global__ void __launch_bounds__(kBT, 2)
     mf_bwd_gemm_kernel(pf_mf_plan_t p, const double *__restrict__ M,
                        const double *__restrict__ O, const int32_t *__restrict__ item_node,
                        const int32_t *__restrict__ item_rb, const int32_t *__restrict__ item_cb0,
                        const int32_t *__restrict__ item_cb1, double *P, int64_t ldp) {
-  // dynamic smem: [A ring | B ring | coff[kBM] | ysrc[2 ncb] | kt0[ncb] | roff[f]]
+  constexpr int kMS = m_stage<NB>();
+  // dynamic smem: [Z ring | M ring | coff[NB] | ysrc[2 ncb] | kt0[ncb] | roff[f]]
   extern __shared__ __align__(128) double dyn[];
-  double *As = dyn, *Bs = dyn + kGStages * kBStageA;
-  int64_t *coff = reinterpret_cast<int64_t *>(dyn + kGStages * (kBStageA + kBStageB));
-  const double **ysrc = reinterpret_cast<const double **>(coff + kBM);
+  double *Zs = dyn, *Ms = dyn + kGStages * kZStage;
+  int64_t *coff = reinterpret_cast<int64_t *>(dyn + kGStages * (kZStage + kMS));
+  const double **ysrc = reinterpret_cast<const double **>(coff + NB);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int s = item_node[blockIdx.x];
   const int f = p.fn[s], c = p.cn[s];
   const int ldf = (f + 15) & ~15;
-  const int i0 = item_rb[blockIdx.x] * kBM;
-  // column blocks of 128 = pairs of 64-column plan tiles [2 cb, 2 cb + 1]
+  const int i0 = item_rb[blockIdx.x] * NB;
   const int cb0 = item_cb0[blockIdx.x], ncb = item_cb1[blockIdx.x] - cb0;
-  // first K stage per column block: a block no boundary column reached in the
-  // forward has Y_C = 0, so its K range starts at the X_R rows
   int64_t *kt0 = reinterpret_cast<int64_t *>(ysrc + 2 * ncb);
   int64_t *roff = kt0 + ncb;
   {
@@ -603,18 +611,18 @@ __global__ void __launch_bounds__(kBT, 2)
       const int64_t it = tile < p.ntiles ? ti[tile] : -1;
       ysrc[h] = it < 0 ? nullptr : O + p.act_voff[it];
     }
-    for (int r = tid; r < kBM; r += kBT) coff[r] = i0 + r < c ? (int64_t)Cv[i0 + r] * ldp : -1;
+    for (int r = tid; r < NB; r += kBT) coff[r] = i0 + r < c ? (int64_t)Cv[i0 + r] * ldp : -1;
   }
   __syncthreads();
   for (int cb = tid; cb < ncb; cb += kBT)
     kt0[cb] = (ysrc[2 * cb] || ysrc[2 * cb + 1]) ? 0 : c / kGBK;
   __syncthreads();
   const double *A = M + p.m_off[s] + (int64_t)i0 * ldf;
-  const int ma = min(kBM, c - i0);
+  const int ma = min(NB, c - i0);
   const int nkt = (f + kGBK - 1) / kGBK;
-  // copy slots: A rows ra + 32u (chunk cha); B rows rbr + 4u (chunk chb: 64 per row)
-  const int ra = tid >> 3, cha = tid & 7, rbr = tid >> 6, chb = tid & 63;
-  const int half = chb >> 5;  // which 64-column plan tile of the block
+  // copy slots: Z rows zr + 4u (chunk zch of 64 per row); M row mr (chunk mch)
+  const int zr = tid >> 6, zch = tid & 63, half = zch >> 5;
+  const int mr = tid >> 3, mch = tid & 7;
   int icb = 0, ikt = (int)kt0[0], ist = 0;  // next (column block, k stage, ring slot)
   while (icb < ncb && ikt >= nkt) {
     ++icb;
@@ -623,30 +631,27 @@ __global__ void __launch_bounds__(kBT, 2)
   auto issue = [&]() {
     if (icb < ncb) {
       const int k0 = ikt * kGBK;
-      double *as = As + ist * kBStageA, *bs = Bs + ist * kBStageB;
+      double *zs = Zs + ist * kZStage, *ms = Ms + ist * kMS;
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int r = ra + 32 * u;
-        const double *src = r < ma ? A + (int64_t)r * ldf + k0 + 2 * cha : g_zero + 2 * cha;
-        cp_async16(as + r * kSA + 2 * cha, src);
+      for (int r = mr; r < NB; r += kBT / 8) {  // NB rows x 8 chunks
+        const double *src = r < ma ? A + (int64_t)r * ldf + k0 + 2 * mch : g_zero + 2 * mch;
+        cp_async16(ms + r * kSA + 2 * mch, src);
       }
       const double *yb = ysrc[2 * icb + half];
-      const int64_t col = (int64_t)(cb0 + icb) * kBN + 2 * chb;
-      const double *pb = P + col;
-      const bool colok = col < ldp;
+      const int64_t col = (int64_t)(cb0 + icb) * kBN + 2 * zch;
+      const double *pb = col < ldp ? P + col : nullptr;
       int64_t ro[4];  // 16 rows x 64 chunks = 4 per thread
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const int l = k0 + rbr + 4 * u;
+        const int l = k0 + zr + 4 * u;
         ro[u] = l < f ? roff[l] : 0;
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const int r = rbr + 4 * u, l = k0 + r;
-        const bool isy = l < c;
-        const double *base = isy ? (yb ? yb + 2 * (chb & 31) : nullptr) : (colok ? pb : nullptr);
-        const double *src = (l < f && base) ? base + ro[u] : g_zero + 2 * (chb & 31);
-        cp_async16(bs + r * kSB2 + 2 * chb, src);
+        const int r = zr + 4 * u, l = k0 + r;
+        const double *base = l < c ? (yb ? yb + 2 * (zch & 31) : nullptr) : pb;
+        const double *src = (l < f && base) ? base + ro[u] : g_zero + 2 * (zch & 31);
+        cp_async16(zs + r * kSB2 + 2 * zch, src);
       }
       if (++ikt >= nkt) {
         do {
@@ -658,49 +663,51 @@ __global__ void __launch_bounds__(kBT, 2)
     }
     cp_commit();
   };
-  const int wm = warp >> 2, wn = warp & 3, fr = lane >> 2, fc = lane & 3;
+  const int fr = lane >> 2, fc = lane & 3;
+  constexpr int NJ = NB / 8;
 #pragma unroll
   for (int u = 0; u < kGStages - 1; ++u) issue();
   int cst = 0;  // ring slot being consumed
   const int64_t k = p.k;
   for (int cb = 0; cb < ncb; ++cb) {
-    double acc[4][4][2];
+    double acc[2][NJ][2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 2; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     for (int kt = (int)kt0[cb]; kt < nkt; ++kt) {
       cp_wait<kGStages - 2>();
       __syncthreads();
       issue();
-      const double *as = As + cst * kBStageA + (wm * 32 + fr) * kSA + fc;
-      const double *bs = Bs + cst * kBStageB + fc * kSB2 + wn * 32 + fr;
+      const double *zs = Zs + cst * kZStage + fc * kSB2 + warp * 16 + fr;
+      const double *ms = Ms + cst * kMS + fr * kSA + fc;
 #pragma unroll
       for (int ks = 0; ks < kGBK; ks += 4) {
-        double av[4], bv[4];
+        double av[2], bv[NJ];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) av[i] = as[8 * i * kSA + ks];
+        for (int i = 0; i < 2; ++i) av[i] = zs[ks * kSB2 + 8 * i];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) bv[j] = bs[ks * kSB2 + 8 * j];
+        for (int j = 0; j < NJ; ++j) bv[j] = ms[8 * j * kSA + ks];
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < 2; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], av[i], bv[j]);
+          for (int j = 0; j < NJ; ++j) dmma884(acc[i][j][0], acc[i][j][1], av[i], bv[j]);
       }
       cst = cst == kGStages - 1 ? 0 : cst + 1;
     }
-    const int64_t colb = (int64_t)(cb0 + cb) * kBN + wn * 32 + 2 * fc;
+    const int64_t colb = (int64_t)(cb0 + cb) * kBN + warp * 16 + fr;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int64_t ro = coff[wm * 32 + 8 * i + fr];
-      if (ro < 0) continue;
+    for (int j = 0; j < NJ; ++j)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int64_t col = colb + 8 * j;
-        if (col < k)  // the pad column col+1 (k odd) is rewritten by finalize
-          *reinterpret_cast<double2 *>(P + ro + col) = make_double2(acc[i][j][0], acc[i][j][1]);
+      for (int q = 0; q < 2; ++q) {
+        const int64_t ro = coff[8 * j + 2 * fc + q];
+        if (ro < 0) continue;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int64_t col = colb + 8 * i;
+          if (col < k) P[ro + col] = acc[i][j][q];
+        }
       }
-    }
   }
   cp_wait<0>();
 }
@@ -898,17 +905,30 @@ int pf_mf_forward_level(const pf_mf_plan_t *plan, const double *Mt, const double
 int pf_mf_backward_level(const pf_mf_plan_t *plan, const double *M, const double *O,
                          const int32_t *item_node, const int32_t *item_rb,
                          const int32_t *item_cb0, const int32_t *item_cb1, int64_t count,
-                         int32_t max_f, int32_t max_ncb, double *P, int64_t ldp,
-                         pf_stream_t stream) {
+                         int32_t max_f, int32_t max_ncb, int32_t nb_rows, double *P,
+                         int64_t ldp, pf_stream_t stream) {
   if (!plan || !M || !O || !item_node || !item_rb || !item_cb0 || !item_cb1 || !P || count < 0 ||
       plan->tile != kGBN || ldp < plan->k || (ldp % kGBN) != 0)
     return fail(PF_E_ARG, "pf_mf_backward_level: bad argument (ldp must be a multiple of 64)");
   if (count == 0) return 0;
   if (max_f < 1 || max_ncb < 1) return fail(PF_E_ARG, "pf_mf_backward_level: bad limits");
-  const size_t smem = kBRing + 8 * ((size_t)kBM + 3 * max_ncb + max_f);
-  if (int rc = ensure_smem((const void *)mf_bwd_gemm_kernel, smem)) return rc;
-  mf_bwd_gemm_kernel<<<(unsigned)count, kBT, smem, as_stream(stream)>>>(
-      *plan, M, O, item_node, item_rb, item_cb0, item_cb1, P, ldp);
+  cudaStream_t st = as_stream(stream);
+  auto launch = [&](auto kern, int nb, size_t ring) -> int {
+    const size_t smem = ring + 8 * ((size_t)nb + 3 * max_ncb + max_f);
+    if (int rc = ensure_smem((const void *)kern, smem)) return rc;
+    kern<<<(unsigned)count, kBT, smem, st>>>(*plan, M, O, item_node, item_rb, item_cb0,
+                                             item_cb1, P, ldp);
+    return 0;
+  };
+  int rc;
+  switch (nb_rows) {
+    case 8: rc = launch(mf_bwd_gemm_kernel<8>, 8, bwd_ring_bytes<8>()); break;
+    case 16: rc = launch(mf_bwd_gemm_kernel<16>, 16, bwd_ring_bytes<16>()); break;
+    case 32: rc = launch(mf_bwd_gemm_kernel<32>, 32, bwd_ring_bytes<32>()); break;
+    case 64: rc = launch(mf_bwd_gemm_kernel<64>, 64, bwd_ring_bytes<64>()); break;
+    default: return fail(PF_E_ARG, "pf_mf_backward_level: nb_rows must be 8, 16, 32 or 64");
+  }
+  if (rc) return rc;
   return check_launch("pf_mf_backward_level");
 }
 

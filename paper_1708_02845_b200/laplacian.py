@@ -223,7 +223,11 @@ class DevicePoisson:
         for lv in pl.levels:
             lv = lv.astype(np.int64)
             lv = lv[c[lv] > 0]
-            rb = (c[lv] + 63) // 64  # 64-row blocks of C (mf_bwd_gemm_kernel)
+            # C-row block of the level: the smallest of 8/16/32/64 covering most
+            # of its separators (the 90th percentile), larger ones in blocks
+            cq = int(np.percentile(c[lv], 90)) if len(lv) else 1
+            nbr = next(x for x in (8, 16, 32, 64) if x >= min(cq, 64))
+            rb = (c[lv] + nbr - 1) // nbr
             blocks = int(rb.sum())
             chunks = int(min(nblk, max(1, -(-self.GEMM_TARGET // max(blocks, 1)))))
             step = -(-nblk // chunks)
@@ -235,7 +239,8 @@ class DevicePoisson:
             self.bwd.append((tod(np.repeat(nodes, len(cb0)), np.int32),
                              tod(np.repeat(rbi, len(cb0)), np.int32),
                              tod(np.tile(cb0, nn), np.int32), tod(np.tile(cb1, nn), np.int32),
-                             nn * len(cb0), int(f[lv].max()) if len(lv) else 1, int(step)))
+                             nn * len(cb0), int(f[lv].max()) if len(lv) else 1, int(step),
+                             nbr))
         self._lap = None
         self._F = None
 
@@ -320,9 +325,9 @@ class DevicePoisson:
                      ai.data_ptr(), aw.data_ptr(), acnt, gn.data_ptr(), gi.data_ptr(),
                      gw.data_ptr(), grb.data_ptr(), gcnt, Wb.data_ptr(), O.data_ptr(), s)
         mark("bwd0")
-        for nodes, rb, cb0, cb1, cnt, maxf, ncb in reversed(self.bwd):
+        for nodes, rb, cb0, cb1, cnt, maxf, ncb, nbr in reversed(self.bwd):
             nat.call("pf_mf_backward_level", ps, M.data_ptr(), O.data_ptr(), nodes.data_ptr(),
-                     rb.data_ptr(), cb0.data_ptr(), cb1.data_ptr(), cnt, maxf, ncb,
+                     rb.data_ptr(), cb0.data_ptr(), cb1.data_ptr(), cnt, maxf, ncb, nbr,
                      P.data_ptr(), ld, s)
         mark("bwd1")
         mx = t.zeros(2, dtype=t.int64, device=self.device)
