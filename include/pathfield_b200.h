@@ -454,6 +454,11 @@ int pf_nd_plan_build(int64_t n, const double *xy_host, const int64_t *nb_ptr_hos
                      int tile, void **plan_out);
 void pf_nd_plan_free(void *plan);
 int64_t pf_nd_plan_array(void *plan, const char *name, void *dst_host);
+/* Host: the sorted vertex-neighbour CSR of a triangle mesh (mesh.py:151
+ * `neighbors`), tri_host (nt,3) int64; nb_idx_host capacity 6*nt; *nnz_out
+ * receives the entry count. */
+int pf_vertex_neighbors(int64_t n, int64_t nt, const int64_t *tri_host, int64_t *nb_ptr_host,
+                        int64_t *nb_idx_host, int64_t *nnz_out);
 /* out_host[16]: n m k nodes levels f_total v_total nnz_l flops_factor
  * flops_solve max_f max_c max_r ntiles tile leaf */
 int pf_nd_plan_stats(void *plan, double *out_host);

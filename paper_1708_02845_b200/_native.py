@@ -94,6 +94,7 @@ _SIGS.update({
     "pf_nd_plan_free": [c_vp],
     "pf_nd_plan_array": [c_vp, ctypes.c_char_p, c_vp],
     "pf_nd_plan_stats": [c_vp, c_vp],
+    "pf_vertex_neighbors": [c_i64, c_i64, c_vp, c_vp, c_vp, ctypes.POINTER(ctypes.c_int64)],
     "pf_cotan_laplacian_f64": [c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp,
                                c_vp],
     "pf_mf_factor_level": [c_vp, c_vp, c_vp, c_vp, c_i64, c_int, c_int, c_int, c_vp, c_vp, c_vp],

@@ -415,6 +415,55 @@ int64_t pf_nd_plan_array(void *plan, const char *name, void *dst_host) {
   return -1;
 }
 
+// Sorted vertex-neighbour CSR of a triangle mesh (mesh.py:151 `neighbors`):
+// counting sort of the 6 directed edge entries per triangle by source vertex,
+// then a per-vertex sort + unique.  nb_idx_host needs capacity 6 * nt; the
+// number of entries is returned in *nnz_out.
+int pf_vertex_neighbors(int64_t n, int64_t nt, const int64_t *tri_host, int64_t *nb_ptr_host,
+                        int64_t *nb_idx_host, int64_t *nnz_out) {
+  if (n < 0 || nt < 0 || (nt && !tri_host) || !nb_ptr_host || (nt && !nb_idx_host) ||
+      !nnz_out) {
+    pf::set_error("pf_vertex_neighbors: bad argument");
+    return PF_E_ARG;
+  }
+  try {
+    std::vector<int64_t> cnt(n + 1, 0);
+    for (int64_t t = 0; t < 3 * nt; ++t) {
+      const int64_t v = tri_host[t];
+      if (v < 0 || v >= n) {
+        pf::set_error("pf_vertex_neighbors: vertex index out of range");
+        return PF_E_DOMAIN;
+      }
+      cnt[v + 1] += 2;
+    }
+    for (int64_t v = 0; v < n; ++v) cnt[v + 1] += cnt[v];
+    std::vector<int64_t> cand(cnt[n]);
+    std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1);
+    for (int64_t t = 0; t < nt; ++t) {
+      const int64_t *T = tri_host + 3 * t;
+      for (int a = 0; a < 3; ++a) {
+        const int64_t v = T[a];
+        cand[fill[v]++] = T[(a + 1) % 3];
+        cand[fill[v]++] = T[(a + 2) % 3];
+      }
+    }
+    int64_t out = 0;
+    nb_ptr_host[0] = 0;
+    for (int64_t v = 0; v < n; ++v) {
+      auto b = cand.begin() + cnt[v], e = cand.begin() + cnt[v + 1];
+      std::sort(b, e);
+      e = std::unique(b, e);
+      for (auto it = b; it != e; ++it) nb_idx_host[out++] = *it;
+      nb_ptr_host[v + 1] = out;
+    }
+    *nnz_out = out;
+  } catch (const std::bad_alloc &) {
+    pf::set_error("pf_vertex_neighbors: out of host memory");
+    return PF_E_CAPACITY;
+  }
+  return PF_OK;
+}
+
 int pf_nd_plan_stats(void *plan, double *out_host) {
   if (!plan || !out_host) {
     pf::set_error("pf_nd_plan_stats: bad argument");

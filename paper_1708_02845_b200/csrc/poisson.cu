@@ -718,10 +718,14 @@ __device__ __forceinline__ void atomic_max_nonneg(unsigned long long *p, double 
   atomicMax(p, (unsigned long long)__double_as_longlong(v));
 }
 
-// Warp per interior row: max_j |diag[v] P[v,j] + sum_e off[e] P[u_e, j]|,
-// boundary neighbours contributing off[e] to column bcol[u].  The row's
-// neighbour list is staged once per row in shared memory; columns go in
-// 16-byte pairs (ldp is a multiple of 64, so every pair is in the row).
+// max_j |diag[v] P[v,j] + sum_e off[e] P[u_e, j]| over interior rows v, with
+// boundary neighbours contributing off[e] to column bcol[u].  Grid: x = row
+// groups (a warp per row), y = 512-column chunks; CTAs run chunk-major, so the
+// chunks of a row's mesh neighbours (v +- 1, v +- one mesh row) are read
+// while still in L2 and P streams from DRAM about once.  The row's neighbour
+// list is staged in shared memory; columns go in 16-byte pairs.
+constexpr int kResCols = 512;
+
 __global__ void __launch_bounds__(256)
     residual_kernel(const double *__restrict__ P, int64_t ldp, int64_t n, int64_t k,
                     const uint8_t *__restrict__ isb, const int32_t *__restrict__ bcol,
@@ -732,6 +736,7 @@ __global__ void __launch_bounds__(256)
   __shared__ int64_t nrow[8][kMaxDeg];  // P offset of an interior neighbour, or -1-bcol
   __shared__ double nw[8][kMaxDeg];
   const int lane = threadIdx.x % 32, w = threadIdx.x / 32;
+  const int64_t j0 = (int64_t)blockIdx.y * kResCols, j1 = min(k, j0 + kResCols);
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
   double mx = 0.0;
   for (int64_t v = blockIdx.x * (int64_t)(blockDim.x / 32) + w; v < n; v += warps) {
@@ -739,7 +744,7 @@ __global__ void __launch_bounds__(256)
     const int64_t e0 = nb_ptr[v];
     const int deg = (int)(nb_ptr[v + 1] - e0);
     if (deg > kMaxDeg) {  // exact per-column evaluation for a (rare) high-valence row
-      for (int64_t j = lane; j < k; j += 32) {
+      for (int64_t j = j0 + lane; j < j1; j += 32) {
         double acc = diag[v] * P[v * ldp + j];
         for (int64_t e = e0; e < e0 + deg; ++e) {
           const int32_t u = nb_idx[e];
@@ -758,7 +763,7 @@ __global__ void __launch_bounds__(256)
     }
     __syncwarp();
     const double dv = diag[v];
-    for (int64_t j = 2 * lane; j < k; j += 64) {
+    for (int64_t j = j0 + 2 * lane; j < j1; j += 64) {
       const double2 pv = *reinterpret_cast<const double2 *>(P + v * ldp + j);
       double a0 = dv * pv.x, a1 = dv * pv.y;
       for (int e = 0; e < deg; ++e) {
@@ -940,7 +945,9 @@ int pf_poisson_residual(const double *P, int64_t ldp, int64_t n, int64_t k,
       n < 0 || k < 0 || ldp < k || (ldp & 1) || (reinterpret_cast<uintptr_t>(P) & 15))
     return fail(PF_E_ARG, "pf_poisson_residual: bad argument (ldp even, P 16-byte aligned)");
   if (n == 0) return 0;
-  residual_kernel<<<grid_for(n, 8), 256, 0, as_stream(stream)>>>(
+  const unsigned chunks = (unsigned)((k + kResCols - 1) / kResCols);
+  const unsigned rows = (unsigned)std::min<int64_t>((n + 7) / 8, (int64_t)sm_count() * 8);
+  residual_kernel<<<dim3(rows, std::max(1u, chunks)), 256, 0, as_stream(stream)>>>(
       P, ldp, n, k, is_boundary, bcol, nb_ptr, nb_idx, off, diag, out_max);
   return check_launch("pf_poisson_residual");
 }

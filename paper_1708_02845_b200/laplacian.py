@@ -57,15 +57,27 @@ LEAF = 64   # leaf sub-domain size of the dissection
 TILE = 64   # column tile of the multi-RHS solves (pf_mf_plan_t.tile)
 
 
+def vertex_neighbors(triangles, n: int):
+    """Sorted vertex-neighbour CSR (nb_ptr, nb_idx) of a triangle list
+    (mesh.py:151), built by the C++ runtime (pf_vertex_neighbors)."""
+    tri = np.ascontiguousarray(triangles, dtype=np.int64)
+    nb_ptr = np.empty(n + 1, dtype=np.int64)
+    nb_idx = np.empty(max(6 * len(tri), 1), dtype=np.int64)
+    nnz = ctypes.c_int64(0)
+    nat.call("pf_vertex_neighbors", n, len(tri), tri.ctypes.data, nb_ptr.ctypes.data,
+             nb_idx.ctypes.data, ctypes.byref(nnz))
+    return nb_ptr, nb_idx[:nnz.value].copy()
+
+
 def mesh_topology(mesh):
     """(nb_ptr, nb_idx, is_boundary) of a mirror or reference TriMesh: the
     sorted vertex neighbour CSR (mesh.py:151) and the boundary mask."""
-    from .mesh import topology
     topo = getattr(mesh, "_topo", None)
     if topo is None:
-        topo = topology(np.asarray(mesh.triangles, dtype=np.int64), len(mesh.vertices))
-    nb_ptr = np.ascontiguousarray(topo[2], dtype=np.int64)
-    nb_idx = np.ascontiguousarray(topo[3], dtype=np.int64)
+        nb_ptr, nb_idx = vertex_neighbors(mesh.triangles, len(mesh.vertices))
+    else:
+        nb_ptr = np.ascontiguousarray(topo[2], dtype=np.int64)
+        nb_idx = np.ascontiguousarray(topo[3], dtype=np.int64)
     isb = np.zeros(len(mesh.vertices), dtype=np.uint8)
     isb[np.asarray(mesh.boundary_vertices, dtype=np.int64)] = 1
     return nb_ptr, nb_idx, isb
@@ -433,11 +445,28 @@ def poisson_kernel_device(ls_or_mesh, leaf: int = LEAF):
     return solver.device_kernel()
 
 
-def dense_to_host(P, n: int, k: int, chunk_rows: int = 16384, threads: int = 8) -> np.ndarray:
-    """Host (n, k) copy of a device P (row stride >= k): row chunks are copied
-    D2H into two alternating pinned buffers while a thread pool scatters the
-    previous chunk into the numpy result (a direct pageable copy of a strided
-    33 GB matrix runs at a fraction of the PCIe rate)."""
+_STAGING: dict = {}
+
+
+def _staging(t, rows: int, ld: int):
+    """Two persistent pinned staging buffers per (rows, ld) (a fresh pinned
+    allocation costs ~0.3 ms per MB)."""
+    key = (rows, ld)
+    bufs = _STAGING.get(key)
+    if bufs is None:
+        bufs = _STAGING[key] = [t.empty((rows, ld), dtype=t.float64, pin_memory=True)
+                                for _ in range(2)]
+    return bufs
+
+
+def dense_to_host(P, n: int, k: int, chunk_bytes: int = 64 << 20,
+                  threads: int | None = None) -> np.ndarray:
+    """Host (n, k) copy of a device P (row stride >= k): ~64 MB row chunks are
+    copied D2H into two alternating pinned buffers while a thread pool
+    scatters the previous chunk into the numpy result (first-touching its
+    pages in parallel; a direct pageable copy of a strided 33 GB matrix runs
+    at a fraction of the PCIe rate)."""
+    import os
     from concurrent.futures import ThreadPoolExecutor
     from . import _device as dev
     t = dev.torch()
@@ -445,11 +474,12 @@ def dense_to_host(P, n: int, k: int, chunk_rows: int = 16384, threads: int = 8) 
     if n == 0:
         return out
     ld = P.stride(0)
-    rows = max(1, min(chunk_rows, n))
-    bufs = [t.empty((rows, ld), dtype=t.float64, pin_memory=True) for _ in range(2)]
+    rows = max(1, min(n, chunk_bytes // (8 * ld)))
+    bufs = _staging(t, rows, ld)
     evs = [t.cuda.Event() for _ in range(2)]
     stream = t.cuda.Stream(P.device)
     stream.wait_stream(t.cuda.current_stream(P.device))
+    threads = threads or max(1, min(16, os.cpu_count() or 1))
     pool = ThreadPoolExecutor(threads)
 
     def scatter(buf, a, b):
