@@ -564,34 +564,41 @@ __global__ void __launch_bounds__(kGT)
 // (N dimension, NB in {8, 16, 32, 64} chosen per level from its separator
 // sizes, so a 12-vertex separator pads to 16, not 64):
 //   X_C^T (cols x NB) = Z^T (cols x f) . M^T (f x NB),  Z = [Y_C; X_R].
-// 8 warps, each 16 columns x NB (2 x NB/8 m8n8k4 DMMAs per 4-deep k step);
-// Z rows (128 contiguous doubles, gathered from P or the forward's Y blocks)
-// and M rows stream through a 3-stage cp.async ring of 16-deep K stages;
-// stage counters instead of divisions; every gather offset is resolved in
-// shared memory before the main loop (branch-free selects in the issue
-// path); column blocks whose tiles the forward never reached skip the zero
-// Y rows of K.
-constexpr int kBN = 128, kBT = 256;
+// Warp-specialised: one producer warp streams 16-deep K stages with TMA bulk
+// copies (cp.async.bulk, one per gathered Z row of 128 doubles and per M row
+// of 16) into a 3-stage ring guarded by full/empty mbarriers; 8 consumer
+// warps each own 16 columns x NB (2 x NB/8 m8n8k4 DMMAs per 4-deep k step).
+// Gather offsets are resolved in shared memory before the loop; column blocks
+// whose tiles the forward never reached skip the zero Y rows of K.
+constexpr int kBN = 128, kBT = 256, kBW = kBT / 32;  // consumer threads / warps
 constexpr int kSB2 = kBN + 4;  // 4 mod 16: conflict-free half-warp fragment loads
 constexpr int kZStage = kGBK * kSB2;
 template <int NB>
 constexpr int m_stage() { return NB * kSA; }
 template <int NB>
-constexpr int bwd_ring_bytes() { return kGStages * (kZStage + m_stage<NB>()) * 8; }
+constexpr int bwd_ring_bytes() {
+  return kGStages * (kZStage + m_stage<NB>()) * 8 + 2 * kGStages * 8;  // + mbarriers
+}
+__device__ __align__(128) double g_zero_row[kBN];  // zero source of 1 KB bulk copies
 
 template <int NB>
-__global__ void __launch_bounds__(kBT, 2)
+__global__ void __launch_bounds__(kBT + 32, 2)
     mf_bwd_gemm_kernel(pf_mf_plan_t p, const double *__restrict__ M,
                        const double *__restrict__ O, const int32_t *__restrict__ item_node,
                        const int32_t *__restrict__ item_rb, const int32_t *__restrict__ item_cb0,
                        const int32_t *__restrict__ item_cb1, double *P, int64_t ldp) {
   constexpr int kMS = m_stage<NB>();
-  // dynamic smem: [Z ring | M ring | coff[NB] | ysrc[2 ncb] | kt0[ncb] | roff[f]]
+  constexpr uint32_t kStageBytes = (kGBK * kBN + NB * kGBK) * 8;
+  // dynamic smem: [Z ring | M ring | full[S] | empty[S] | coff[NB] | ysrc[2 ncb] |
+  //                kt0[ncb] | roff[f]]
   extern __shared__ __align__(128) double dyn[];
   double *Zs = dyn, *Ms = dyn + kGStages * kZStage;
-  int64_t *coff = reinterpret_cast<int64_t *>(dyn + kGStages * (kZStage + kMS));
+  uint64_t *full = reinterpret_cast<uint64_t *>(Ms + kGStages * kMS);
+  uint64_t *empty = full + kGStages;
+  int64_t *coff = reinterpret_cast<int64_t *>(empty + kGStages);
   const double **ysrc = reinterpret_cast<const double **>(coff + NB);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nthr = kBT + 32;
   const int s = item_node[blockIdx.x];
   const int f = p.fn[s], c = p.cn[s];
   const int ldf = (f + 15) & ~15;
@@ -604,83 +611,78 @@ __global__ void __launch_bounds__(kBT, 2)
     const int32_t *Rv = p.r_orig + p.r_ptr[s];
     const int64_t *ti = p.tile_item + (int64_t)s * p.ntiles;
     // roff[l]: l < c -> Y row l of a 64-wide block; else the P row of X_R[l - c]
-    for (int l = tid; l < f; l += kBT)
+    for (int l = tid; l < f; l += nthr)
       roff[l] = l < c ? (int64_t)l * kGBN : (int64_t)Rv[l - c] * ldp;
-    for (int h = tid; h < 2 * ncb; h += kBT) {
+    for (int h = tid; h < 2 * ncb; h += nthr) {
       const int64_t tile = 2 * (int64_t)cb0 + h;
       const int64_t it = tile < p.ntiles ? ti[tile] : -1;
       ysrc[h] = it < 0 ? nullptr : O + p.act_voff[it];
     }
-    for (int r = tid; r < NB; r += kBT) coff[r] = i0 + r < c ? (int64_t)Cv[i0 + r] * ldp : -1;
+    for (int r = tid; r < NB; r += nthr) coff[r] = i0 + r < c ? (int64_t)Cv[i0 + r] * ldp : -1;
+    if (tid == 0)
+      for (int q = 0; q < kGStages; ++q) {
+        mbar_init(&full[q], 1);
+        mbar_init(&empty[q], kBW);
+      }
   }
   __syncthreads();
-  for (int cb = tid; cb < ncb; cb += kBT)
+  for (int cb = tid; cb < ncb; cb += nthr)
     kt0[cb] = (ysrc[2 * cb] || ysrc[2 * cb + 1]) ? 0 : c / kGBK;
   __syncthreads();
-  const double *A = M + p.m_off[s] + (int64_t)i0 * ldf;
-  const int ma = min(NB, c - i0);
   const int nkt = (f + kGBK - 1) / kGBK;
-  // copy slots: Z rows zr + 4u (chunk zch of 64 per row); M row mr (chunk mch)
-  const int zr = tid >> 6, zch = tid & 63, half = zch >> 5;
-  const int mr = tid >> 3, mch = tid & 7;
-  int icb = 0, ikt = (int)kt0[0], ist = 0;  // next (column block, k stage, ring slot)
-  while (icb < ncb && ikt >= nkt) {
-    ++icb;
-    ikt = icb < ncb ? (int)kt0[icb] : 0;
-  }
-  auto issue = [&]() {
-    if (icb < ncb) {
-      const int k0 = ikt * kGBK;
-      double *zs = Zs + ist * kZStage, *ms = Ms + ist * kMS;
-#pragma unroll
-      for (int r = mr; r < NB; r += kBT / 8) {  // NB rows x 8 chunks
-        const double *src = r < ma ? A + (int64_t)r * ldf + k0 + 2 * mch : g_zero + 2 * mch;
-        cp_async16(ms + r * kSA + 2 * mch, src);
+  if (warp == kBW) {  // ------------------------------------------- producer
+    const double *A = M + p.m_off[s] + (int64_t)i0 * ldf;
+    const int ma = min(NB, c - i0);
+    int it = 0;
+    for (int cb = 0; cb < ncb; ++cb) {
+      const int64_t col = (int64_t)(cb0 + cb) * kBN;
+      const bool whole = col + kBN <= ldp;  // else the upper half lies past the row end
+      const double *yb0 = ysrc[2 * cb], *yb1 = ysrc[2 * cb + 1];
+      for (int kt = (int)kt0[cb]; kt < nkt; ++kt, ++it) {
+        const int st = it % kGStages;
+        mbar_wait(&empty[st], ((it / kGStages) & 1) ^ 1);
+        if (lane == 0) mbar_expect_tx(&full[st], kStageBytes);
+        __syncwarp();
+        const int k0 = kt * kGBK;
+        if (lane < kGBK) {
+          const int l = k0 + lane;
+          double *dst = Zs + st * kZStage + lane * kSB2;
+          if (l >= f) {
+            bulk_g2s(dst, g_zero_row, kBN * 8, &full[st]);
+          } else if (l < c) {
+            bulk_g2s(dst, yb0 ? yb0 + roff[l] : g_zero_row, kGBN * 8, &full[st]);
+            bulk_g2s(dst + kGBN, yb1 ? yb1 + roff[l] : g_zero_row, kGBN * 8, &full[st]);
+          } else if (whole) {
+            bulk_g2s(dst, P + roff[l] + col, kBN * 8, &full[st]);
+          } else {
+            bulk_g2s(dst, P + roff[l] + col, kGBN * 8, &full[st]);
+            bulk_g2s(dst + kGBN, g_zero_row, kGBN * 8, &full[st]);
+          }
+        }
+        for (int r = lane; r < NB; r += 32) {
+          const double *src = r < ma ? A + (int64_t)r * ldf + k0 : g_zero_row;
+          bulk_g2s(Ms + st * kMS + r * kSA, src, kGBK * 8, &full[st]);
+        }
       }
-      const double *yb = ysrc[2 * icb + half];
-      const int64_t col = (int64_t)(cb0 + icb) * kBN + 2 * zch;
-      const double *pb = col < ldp ? P + col : nullptr;
-      int64_t ro[4];  // 16 rows x 64 chunks = 4 per thread
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int l = k0 + zr + 4 * u;
-        ro[u] = l < f ? roff[l] : 0;
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int r = zr + 4 * u, l = k0 + r;
-        const double *base = l < c ? (yb ? yb + 2 * (zch & 31) : nullptr) : pb;
-        const double *src = (l < f && base) ? base + ro[u] : g_zero + 2 * (zch & 31);
-        cp_async16(zs + r * kSB2 + 2 * zch, src);
-      }
-      if (++ikt >= nkt) {
-        do {
-          ++icb;
-          ikt = icb < ncb ? (int)kt0[icb] : 0;
-        } while (icb < ncb && ikt >= nkt);
-      }
-      ist = ist == kGStages - 1 ? 0 : ist + 1;
     }
-    cp_commit();
-  };
+    return;
+  }
+  // ------------------------------------------------------------ consumers
   const int fr = lane >> 2, fc = lane & 3;
   constexpr int NJ = NB / 8;
-#pragma unroll
-  for (int u = 0; u < kGStages - 1; ++u) issue();
-  int cst = 0;  // ring slot being consumed
   const int64_t k = p.k;
+  int it = 0;
   for (int cb = 0; cb < ncb; ++cb) {
     double acc[2][NJ][2];
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll
       for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    for (int kt = (int)kt0[cb]; kt < nkt; ++kt) {
-      cp_wait<kGStages - 2>();
-      __syncthreads();
-      issue();
-      const double *zs = Zs + cst * kZStage + fc * kSB2 + warp * 16 + fr;
-      const double *ms = Ms + cst * kMS + fr * kSA + fc;
+    for (int kt = (int)kt0[cb]; kt < nkt; ++kt, ++it) {
+      const int st = it % kGStages;
+      mbar_wait(&full[st], (it / kGStages) & 1);
+      const double *zs = Zs + st * kZStage + fc * kSB2 + warp * 16 + fr;
+      const double *ms = Ms + st * kMS + fr * kSA + fc;
 #pragma unroll
       for (int ks = 0; ks < kGBK; ks += 4) {
         double av[2], bv[NJ];
@@ -693,7 +695,8 @@ __global__ void __launch_bounds__(kBT, 2)
 #pragma unroll
           for (int j = 0; j < NJ; ++j) dmma884(acc[i][j][0], acc[i][j][1], av[i], bv[j]);
       }
-      cst = cst == kGStages - 1 ? 0 : cst + 1;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
     }
     const int64_t colb = (int64_t)(cb0 + cb) * kBN + warp * 16 + fr;
 #pragma unroll
@@ -709,7 +712,6 @@ __global__ void __launch_bounds__(kBT, 2)
         }
       }
   }
-  cp_wait<0>();
 }
 
 // ------------------------------------------------------- diagnostics ------
@@ -921,8 +923,8 @@ int pf_mf_backward_level(const pf_mf_plan_t *plan, const double *M, const double
   auto launch = [&](auto kern, int nb, size_t ring) -> int {
     const size_t smem = ring + 8 * ((size_t)nb + 3 * max_ncb + max_f);
     if (int rc = ensure_smem((const void *)kern, smem)) return rc;
-    kern<<<(unsigned)count, kBT, smem, st>>>(*plan, M, O, item_node, item_rb, item_cb0,
-                                             item_cb1, P, ldp);
+    kern<<<(unsigned)count, kBT + 32, smem, st>>>(*plan, M, O, item_node, item_rb, item_cb0,
+                                                  item_cb1, P, ldp);
     return 0;
   };
   int rc;
