@@ -540,13 +540,21 @@ int pf_mf_backward_level(const pf_mf_plan_t *plan, const double *M, const double
                          int32_t max_f, int32_t max_ncb, int32_t nb_rows, double *P,
                          int64_t ldp, pf_stream_t stream);
 
-/* residual = max |(Lc P)[v, j]| over interior rows v and columns j < k with
- * P's boundary rows taken as indicators (= |Lc_II P_IB + Lc_IB|, solvers.py:
- * 292), before the clip; out_max[0] holds the max as ordered FP64 bits. */
-int pf_poisson_residual(const double *P, int64_t ldp, int64_t n, int64_t k,
-                        const uint8_t *is_boundary, const int32_t *bcol, const int64_t *nb_ptr,
-                        const int32_t *nb_idx, const double *off, const double *diag,
-                        unsigned long long *out_max, pf_stream_t stream);
+/* Gather table of the residual: nrow[e] = nb_idx[e] * ldp for an interior
+ * neighbour entry, -1 - bcol[u] for a boundary one (built once per mesh). */
+int pf_poisson_residual_table(const int32_t *nb_idx, int64_t nnz, const uint8_t *is_boundary,
+                              const int32_t *bcol, int64_t ldp, int64_t *nrow,
+                              pf_stream_t stream);
+
+/* residual = max |(Lc P)[v, j]| over the interior rows v = order[0..count)
+ * and columns j < k with P's boundary rows taken as indicators (= |Lc_II P_IB
+ * + Lc_IB|, solvers.py:292), before the clip; out_max[0] holds the max as
+ * ordered FP64 bits.  `order` is best the plan's perm_orig (spatially compact
+ * row groups share their neighbours' rows in cache). */
+int pf_poisson_residual(const double *P, int64_t ldp, int64_t k, const int32_t *order,
+                        int64_t count, const int64_t *nb_ptr, const int64_t *nrow,
+                        const double *off, const double *diag, unsigned long long *out_max,
+                        pf_stream_t stream);
 
 /* Boundary rows -> indicators of their column, pad columns -> 0, interior
  * entries in (-1e-12, 0) -> 0 (solvers.py:293-296); out_max[0] = max

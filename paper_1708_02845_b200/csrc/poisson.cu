@@ -720,66 +720,83 @@ __device__ __forceinline__ void atomic_max_nonneg(unsigned long long *p, double 
   atomicMax(p, (unsigned long long)__double_as_longlong(v));
 }
 
-// max_j |diag[v] P[v,j] + sum_e off[e] P[u_e, j]| over interior rows v, with
-// boundary neighbours contributing off[e] to column bcol[u].  Grid: x = row
-// groups (a warp per row), y = 512-column chunks; CTAs run chunk-major, so the
-// chunks of a row's mesh neighbours (v +- 1, v +- one mesh row) are read
-// while still in L2 and P streams from DRAM about once.  The row's neighbour
-// list is staged in shared memory; columns go in 16-byte pairs.
+// max_j |diag[v] P[v,j] + sum_e off[e] P[u_e, j]| over the interior rows v =
+// order[i] (the nested-dissection order: consecutive rows are spatially
+// compact leaf patches, so the rows their neighbours read are shared by the
+// warps of the same CTA and stay in L1/L2), with nrow[e] the precomputed P
+// offset of neighbour entry e (or -1 - its boundary column, contributing
+// off[e] to that column).  Grid: x = row groups (a warp per row), y =
+// 512-column chunks; columns go in 16-byte pairs.
 constexpr int kResCols = 512;
 
 __global__ void __launch_bounds__(256)
-    residual_kernel(const double *__restrict__ P, int64_t ldp, int64_t n, int64_t k,
-                    const uint8_t *__restrict__ isb, const int32_t *__restrict__ bcol,
-                    const int64_t *__restrict__ nb_ptr, const int32_t *__restrict__ nb_idx,
+    residual_kernel(const double *__restrict__ P, int64_t ldp, int64_t k,
+                    const int32_t *__restrict__ order, int64_t count,
+                    const int64_t *__restrict__ nb_ptr, const int64_t *__restrict__ nrow,
                     const double *__restrict__ off, const double *__restrict__ diag,
                     unsigned long long *out) {
-  constexpr int kMaxDeg = 32;
-  __shared__ int64_t nrow[8][kMaxDeg];  // P offset of an interior neighbour, or -1-bcol
-  __shared__ double nw[8][kMaxDeg];
+  // Neighbour rows are gathered in unrolled groups of 8 (all loads in flight
+  // before the FMAs; missing slots point at row v with weight 0); boundary
+  // neighbours add their weight to one column each, in a separate short list.
+  constexpr int kG = 8, kMaxDeg = 32;
+  __shared__ int64_t srow[8][kMaxDeg];
+  __shared__ double sw[8][kMaxDeg];
+  __shared__ int64_t bcl[8][kMaxDeg];
+  __shared__ double bw[8][kMaxDeg];
   const int lane = threadIdx.x % 32, w = threadIdx.x / 32;
   const int64_t j0 = (int64_t)blockIdx.y * kResCols, j1 = min(k, j0 + kResCols);
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
   double mx = 0.0;
-  for (int64_t v = blockIdx.x * (int64_t)(blockDim.x / 32) + w; v < n; v += warps) {
-    if (isb[v]) continue;
+  for (int64_t i = blockIdx.x * (int64_t)(blockDim.x / 32) + w; i < count; i += warps) {
+    const int64_t v = order[i];
     const int64_t e0 = nb_ptr[v];
     const int deg = (int)(nb_ptr[v + 1] - e0);
+    const double dv = diag[v];
     if (deg > kMaxDeg) {  // exact per-column evaluation for a (rare) high-valence row
       for (int64_t j = j0 + lane; j < j1; j += 32) {
-        double acc = diag[v] * P[v * ldp + j];
+        double acc = dv * P[v * ldp + j];
         for (int64_t e = e0; e < e0 + deg; ++e) {
-          const int32_t u = nb_idx[e];
-          const double x = isb[u] ? (bcol[u] == j ? 1.0 : 0.0) : P[(int64_t)u * ldp + j];
-          acc += off[e] * x;
+          const int64_t ro = nrow[e];
+          acc += off[e] * (ro >= 0 ? P[ro + j] : (-1 - ro == j ? 1.0 : 0.0));
         }
         mx = fmax(mx, fabs(acc));
       }
       continue;
     }
     __syncwarp();
-    if (lane < deg) {
-      const int32_t u = nb_idx[e0 + lane];
-      nrow[w][lane] = isb[u] ? -1 - (int64_t)bcol[u] : (int64_t)u * ldp;
-      nw[w][lane] = off[e0 + lane];
+    const int64_t me = lane < deg ? nrow[e0 + lane] : 0;
+    const double mw = lane < deg ? off[e0 + lane] : 0.0;
+    const bool inner = lane < deg && me >= 0;
+    const unsigned bmask = __ballot_sync(0xffffffffu, lane < deg && me < 0);
+    const int nbnd = __popc(bmask);
+    srow[w][lane] = inner ? me : v * ldp;  // all 32 slots: padding reads row v, weight 0
+    sw[w][lane] = inner ? mw : 0.0;
+    if (lane < deg && me < 0) {
+      const int slot = __popc(bmask & ((1u << lane) - 1));
+      bcl[w][slot] = -1 - me;
+      bw[w][slot] = mw;
     }
     __syncwarp();
-    const double dv = diag[v];
+    const int ngroups = (deg + kG - 1) / kG;
     for (int64_t j = j0 + 2 * lane; j < j1; j += 64) {
       const double2 pv = *reinterpret_cast<const double2 *>(P + v * ldp + j);
       double a0 = dv * pv.x, a1 = dv * pv.y;
-      for (int e = 0; e < deg; ++e) {
-        const int64_t ro = nrow[w][e];
-        const double we = nw[w][e];
-        if (ro >= 0) {
-          const double2 x = *reinterpret_cast<const double2 *>(P + ro + j);
-          a0 += we * x.x;
-          a1 += we * x.y;
-        } else {
-          const int64_t b = -1 - ro;
-          if (b == j) a0 += we;
-          if (b == j + 1) a1 += we;
+      for (int g = 0; g < ngroups; ++g) {
+        double2 x[kG];
+#pragma unroll
+        for (int u = 0; u < kG; ++u)
+          x[u] = *reinterpret_cast<const double2 *>(P + srow[w][g * kG + u] + j);
+#pragma unroll
+        for (int u = 0; u < kG; ++u) {
+          const double we = sw[w][g * kG + u];
+          a0 += we * x[u].x;
+          a1 += we * x[u].y;
         }
+      }
+      for (int q = 0; q < nbnd; ++q) {
+        const int64_t b = bcl[w][q];
+        if (b == j) a0 += bw[w][q];
+        if (b == j + 1) a1 += bw[w][q];
       }
       mx = fmax(mx, fabs(a0));
       if (j + 1 < k) mx = fmax(mx, fabs(a1));
@@ -787,6 +804,19 @@ __global__ void __launch_bounds__(256)
   }
   mx = warp_max(mx);
   if (lane == 0) atomic_max_nonneg(out, mx);
+}
+
+// nrow[e] = nb_idx[e] * ldp for an interior neighbour, -1 - bcol for a
+// boundary one (the residual's gather table, built once per mesh).
+__global__ void residual_table_kernel(const int32_t *__restrict__ nb_idx, int64_t nnz,
+                                      const uint8_t *__restrict__ isb,
+                                      const int32_t *__restrict__ bcol, int64_t ldp,
+                                      int64_t *__restrict__ nrow) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t u = nb_idx[e];
+    nrow[e] = isb[u] ? -1 - (int64_t)bcol[u] : (int64_t)u * ldp;
+  }
 }
 
 __global__ void finalize_kernel(double *P, int64_t ldp, int64_t n, int64_t k,
@@ -939,18 +969,29 @@ int pf_mf_backward_level(const pf_mf_plan_t *plan, const double *M, const double
   return check_launch("pf_mf_backward_level");
 }
 
-int pf_poisson_residual(const double *P, int64_t ldp, int64_t n, int64_t k,
-                        const uint8_t *is_boundary, const int32_t *bcol, const int64_t *nb_ptr,
-                        const int32_t *nb_idx, const double *off, const double *diag,
-                        unsigned long long *out_max, pf_stream_t stream) {
-  if (!P || !is_boundary || !bcol || !nb_ptr || !nb_idx || !off || !diag || !out_max ||
-      n < 0 || k < 0 || ldp < k || (ldp & 1) || (reinterpret_cast<uintptr_t>(P) & 15))
+int pf_poisson_residual_table(const int32_t *nb_idx, int64_t nnz, const uint8_t *is_boundary,
+                              const int32_t *bcol, int64_t ldp, int64_t *nrow,
+                              pf_stream_t stream) {
+  if ((nnz && (!nb_idx || !nrow)) || !is_boundary || !bcol || nnz < 0 || ldp < 1)
+    return fail(PF_E_ARG, "pf_poisson_residual_table: bad argument");
+  if (nnz == 0) return 0;
+  residual_table_kernel<<<grid_for(nnz, 256), 256, 0, as_stream(stream)>>>(
+      nb_idx, nnz, is_boundary, bcol, ldp, nrow);
+  return check_launch("pf_poisson_residual_table");
+}
+
+int pf_poisson_residual(const double *P, int64_t ldp, int64_t k, const int32_t *order,
+                        int64_t count, const int64_t *nb_ptr, const int64_t *nrow,
+                        const double *off, const double *diag, unsigned long long *out_max,
+                        pf_stream_t stream) {
+  if (!P || !order || !nb_ptr || !nrow || !off || !diag || !out_max || k < 0 || count < 0 ||
+      ldp < k || (ldp & 1) || (reinterpret_cast<uintptr_t>(P) & 15))
     return fail(PF_E_ARG, "pf_poisson_residual: bad argument (ldp even, P 16-byte aligned)");
-  if (n == 0) return 0;
+  if (count == 0) return 0;
   const unsigned chunks = (unsigned)((k + kResCols - 1) / kResCols);
-  const unsigned rows = (unsigned)std::min<int64_t>((n + 7) / 8, (int64_t)sm_count() * 8);
+  const unsigned rows = (unsigned)std::min<int64_t>((count + 7) / 8, (int64_t)sm_count() * 8);
   residual_kernel<<<dim3(rows, std::max(1u, chunks)), 256, 0, as_stream(stream)>>>(
-      P, ldp, n, k, is_boundary, bcol, nb_ptr, nb_idx, off, diag, out_max);
+      P, ldp, k, order, count, nb_ptr, nrow, off, diag, out_max);
   return check_launch("pf_poisson_residual");
 }
 

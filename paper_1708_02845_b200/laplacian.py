@@ -161,7 +161,7 @@ class DevicePoisson:
     and M) are cached; ``solve()`` writes a fresh P every call.
     """
 
-    GEMM_TARGET = 2 * 148  # CTAs per backward level before column blocks are split
+    GEMM_TARGET = 8 * 148  # CTAs per backward level before column blocks are split
     SPLIT_BELOW = 148      # levels with fewer fronts factor each front over many CTAs
 
     def __init__(self, mesh, leaf: int = LEAF, device=None):
@@ -344,9 +344,10 @@ class DevicePoisson:
         mark("bwd1")
         mx = t.zeros(2, dtype=t.int64, device=self.device)
         dm = self.dm
-        nat.call("pf_poisson_residual", P.data_ptr(), ld, self.n, self.k,
-                 self.is_boundary.data_ptr(), self.bcol.data_ptr(), dm.nb_ptr.data_ptr(),
-                 dm.nb_idx.data_ptr(), off.data_ptr(), diag.data_ptr(), mx.data_ptr(), s)
+        nrow = self._residual_table(ld)
+        nat.call("pf_poisson_residual", P.data_ptr(), ld, self.k,
+                 self._dev["perm_orig"].data_ptr(), self.plan.m, dm.nb_ptr.data_ptr(),
+                 nrow.data_ptr(), off.data_ptr(), diag.data_ptr(), mx.data_ptr(), s)
         nat.call("pf_poisson_finalize", P.data_ptr(), ld, self.n, self.k,
                  self.is_boundary.data_ptr(), self.bcol.data_ptr(), mx.data_ptr() + 8, s)
         mark("end")
@@ -354,6 +355,20 @@ class DevicePoisson:
         r = mx.cpu().numpy().astype(np.uint64)
         residual = _u64_to_f64(int(r[0])) if self.plan.m else 0.0
         return P, residual, _u64_to_f64(int(r[1]))
+
+    def _residual_table(self, ld: int):
+        """Per neighbour entry: the P offset of an interior neighbour's row or
+        -1 - the boundary column (pf_poisson_residual_table), cached per ld."""
+        hit = getattr(self, "_rtab", None)
+        if hit is None or hit[0] != ld:
+            from . import _device as dev
+            t = dev.torch()
+            nrow = t.empty(max(self._nnz, 1), dtype=t.int64, device=self.device)
+            nat.call("pf_poisson_residual_table", self.dm.nb_idx.data_ptr(), self._nnz,
+                     self.is_boundary.data_ptr(), self.bcol.data_ptr(), ld, nrow.data_ptr(),
+                     self.stream())
+            hit = self._rtab = (ld, nrow)
+        return hit[1]
 
     def solve_flops(self) -> dict:
         """Algorithmic FP64 work of the solves (SURVEY §8d convention): the
