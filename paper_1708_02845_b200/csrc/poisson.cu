@@ -135,7 +135,8 @@ __device__ __forceinline__ void front_assemble_rows(const pf_mf_plan_t &p, int s
 // Load the pb x pb pivot block at p0 into D (identity-padded to kT) and, if
 // `factor`, Cholesky-factor it with one warp and write it back.
 __device__ __forceinline__ void panel_diag(double *Fs, int f, int p0, int pb,
-                                           double (*D)[kT + 1], int32_t *err, bool factor) {
+                                           double (*D)[kT + 1], int32_t *err, bool factor,
+                                           bool write = true) {
   const int tid = threadIdx.x;
   for (int idx = tid; idx < kT * kT; idx += blockDim.x) {
     const int i = idx / kT, j = idx % kT;
@@ -164,6 +165,7 @@ __device__ __forceinline__ void panel_diag(double *Fs, int f, int p0, int pb,
     }
   }
   __syncthreads();
+  if (!write) return;
   for (int idx = tid; idx < pb * pb; idx += blockDim.x) {
     const int i = idx / pb, j = idx % pb;
     if (j <= i) Fs[(int64_t)(p0 + i) * f + p0 + j] = D[i][j];
@@ -276,25 +278,18 @@ __global__ void __launch_bounds__(kThreads)
   front_assemble_rows(p, s, off, diag, F, r0, r1);
 }
 
-__global__ void __launch_bounds__(kThreads)
-    mf_panel_diag_kernel(pf_mf_plan_t p, const int32_t *__restrict__ nodes, int p0, double *F,
-                         int32_t *err) {
-  __shared__ double D[kT][kT + 1];
-  const int s = nodes[blockIdx.x];
-  const int c = p.cn[s];
-  if (p0 >= c) return;
-  panel_diag(F + p.foff[s], p.fn[s], p0, min(kT, c - p0), D, err, true);
-}
-
 __global__ void __launch_bounds__(kThreads, 2)
-    mf_panel_trsm_kernel(pf_mf_plan_t p, const int32_t *__restrict__ nodes, int p0, double *F) {
+    mf_panel_trsm_kernel(pf_mf_plan_t p, const int32_t *__restrict__ nodes, int p0, double *F,
+                         int32_t *err) {
   __shared__ double D[kT][kT + 1];
   const int s = nodes[blockIdx.x];
   const int c = p.cn[s], f = p.fn[s];
   if (p0 >= c) return;
   const int pb = min(kT, c - p0);
   double *Fs = F + p.foff[s];
-  panel_diag(Fs, f, p0, pb, D, nullptr, false);
+  // every CTA factors the 32 x 32 pivot block itself (cheaper than a launch);
+  // the first writes it back
+  panel_diag(Fs, f, p0, pb, D, err, true, blockIdx.y == 0);
   panel_trsm_rows(Fs, f, p0, pb, D, p0 + pb + blockIdx.y * (kThreads / 32) + threadIdx.x / 32,
                   gridDim.y * (kThreads / 32));
 }
@@ -670,6 +665,7 @@ __global__ void __launch_bounds__(kBT + 32, 2)
   // ------------------------------------------------------------ consumers
   const int fr = lane >> 2, fc = lane & 3;
   constexpr int NJ = NB / 8;
+  const int njv = (min(NB, c - i0) + 7) >> 3;  // n-tiles holding real C rows (uniform)
   const int64_t k = p.k;
   int it = 0;
   for (int cb = 0; cb < ncb; ++cb) {
@@ -691,9 +687,11 @@ __global__ void __launch_bounds__(kBT + 32, 2)
 #pragma unroll
         for (int j = 0; j < NJ; ++j) bv[j] = ms[8 * j * kSA + ks];
 #pragma unroll
-        for (int i = 0; i < 2; ++i)
+        for (int j = 0; j < NJ; ++j)
+          if (j < njv) {
 #pragma unroll
-          for (int j = 0; j < NJ; ++j) dmma884(acc[i][j][0], acc[i][j][1], av[i], bv[j]);
+            for (int i = 0; i < 2; ++i) dmma884(acc[i][j][0], acc[i][j][1], av[i], bv[j]);
+          }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
@@ -894,11 +892,10 @@ int pf_mf_factor_level(const pf_mf_plan_t *plan, const double *off, const double
   mf_assemble_split_kernel<<<dim3((unsigned)count, (unsigned)std::min(per, std::max(1, max_f / 16))),
                              kThreads, 0, st>>>(*plan, off, diag, nodes, F);
   for (int p0 = 0; p0 < max_c; p0 += kT) {
-    mf_panel_diag_kernel<<<(unsigned)count, kThreads, 0, st>>>(*plan, nodes, p0, F, err);
     const int rows = max_f - p0;
     const int ty = std::max(1, std::min(per, (rows + kThreads / 32 - 1) / (kThreads / 32)));
     mf_panel_trsm_kernel<<<dim3((unsigned)count, (unsigned)ty), kThreads, 0, st>>>(*plan, nodes,
-                                                                                  p0, F);
+                                                                                  p0, F, err);
     const int nb = (rows - 1 + 63) / 64;
     const int pairs = std::max(1, nb * (nb + 1) / 2);
     mf_panel_syrk_kernel<<<dim3((unsigned)count, (unsigned)std::min(pairs, std::max(per, 1))),

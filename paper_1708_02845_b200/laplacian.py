@@ -255,6 +255,7 @@ class DevicePoisson:
                              nbr))
         self._lap = None
         self._F = None
+        self._bufs = None
 
     # -- laplacian.py:91-134 ---------------------------------------------
     def laplacian(self):
@@ -289,15 +290,19 @@ class DevicePoisson:
             from .errors import FactorizationError
             t = dev.torch()
             off, diag = self.laplacian()
-            F = t.empty(max(self.plan.stats["f_total"], 1), dtype=t.float64, device=self.device)
+            if self._bufs is None:  # kept across refactorisations (pads of Mt / M stay 0)
+                self._bufs = (
+                    t.empty(max(self.plan.stats["f_total"], 1), dtype=t.float64,
+                            device=self.device),
+                    t.zeros(max(int(self.mt_off[-1]), 1), dtype=t.float64, device=self.device),
+                    t.zeros(max(int(self.m_off[-1]), 1), dtype=t.float64, device=self.device))
+            F, Mt, M = self._bufs
             err = t.zeros(1, dtype=t.int32, device=self.device)
             s = self.stream()
             for lv, (mf, mc, split) in zip(self.levels, self.level_shape):
                 nat.call("pf_mf_factor_level", ctypes.addressof(self.struct), off.data_ptr(),
                          diag.data_ptr(), lv.data_ptr(), lv.numel(), mf, mc, split,
                          F.data_ptr(), err.data_ptr(), s)
-            Mt = t.zeros(max(int(self.mt_off[-1]), 1), dtype=t.float64, device=self.device)
-            M = t.zeros(max(int(self.m_off[-1]), 1), dtype=t.float64, device=self.device)
             inode, ict, icnt, nodes = self.inv
             nat.call("pf_mf_inverse", ctypes.addressof(self.struct), F.data_ptr(),
                      inode.data_ptr(), ict.data_ptr(), icnt, nodes.data_ptr(), nodes.numel(),
@@ -306,7 +311,6 @@ class DevicePoisson:
                 raise FactorizationError(
                     "interior block is not positive definite after negation "
                     "(severely non-Delaunay mesh)")
-            del F
             self._F = (Mt, M)
         return self._F
 
