@@ -200,6 +200,107 @@ class CpuReference:
         return 2 * self.rows / el, el
 
 
+# ---- bounded CPU baselines of the side workloads (SURVEY §8d "CPU timing
+# beside it"): the oracle restatement of the reference algorithm on all host
+# cores (fork workers: the reference's per-pair / per-path loops are Python).
+_CPU_STATE: dict = {}
+
+
+def _cpu_pool_run(fn, items, procs):
+    """Run fn over items in `procs` forked workers; returns (results, seconds)."""
+    import multiprocessing as mp
+    t0 = time.perf_counter()
+    if procs <= 1:
+        res = [fn(x) for x in items]
+    else:
+        with mp.get_context("fork").Pool(procs) as pool:
+            res = pool.map(fn, items, chunksize=max(1, len(items) // (4 * procs)))
+    return res, time.perf_counter() - t0
+
+
+def _csr_pairs(chunk):
+    from oracle import divergence as O
+    sv, name, p = _CPU_STATE["csr"]
+    return [O.dv_pair_sparse_stats(sv, name, p, int(q))[0] for q in chunk]
+
+
+def cpu_baseline_csr(rows_full: int, k: int, n_sample: int = 4096, pairs: int = 8192):
+    """dv_pair_sparse_stats loop (divergence.py:255-305, restated in
+    oracle/divergence.py) over `pairs` sampled query rows of a C3-shaped
+    banded P (same generator, `n_sample` rows), all host cores."""
+    import math
+    import numpy as np
+    from oracle import divergence as O
+    b = np.arange(k, dtype=np.float64)[None, :]
+    q = np.linspace(0, rows_full - 1, n_sample)[:, None]
+    c1 = np.floor(q / rows_full * (k / 2))
+    x = np.exp(-np.abs(b - c1) / 12.5) + np.exp(-np.abs(b - ((k - 1) - c1)) / 12.5)
+    P = x / x.sum(axis=1, keepdims=True)
+    sv = O.sparsify(P, np.array([], np.int64), threshold=1.0 / math.sqrt(rows_full))
+    procs = os.cpu_count() or 1
+    rng = np.random.default_rng(5)
+    qs = rng.integers(0, n_sample, pairs)
+    out = {}
+    for name in ("kl", "tv"):
+        _CPU_STATE["csr"] = (sv, name, n_sample // 3)
+        chunks = [qs[i:i + 64] for i in range(0, pairs, 64)]
+        _, sec = _cpu_pool_run(_csr_pairs, chunks, procs)
+        out[name] = pairs / sec
+    return {"value": 2.0 / (1.0 / out["kl"] + 1.0 / out["tv"]), "unit": "evals/s",
+            "kl_evals_per_s": out["kl"], "tv_evals_per_s": out["tv"], "cores": procs,
+            "kind": "port",
+            "sample": f"dv_pair_sparse_stats loop (the reference's only sparse field) over "
+                      f"{pairs} sampled query rows of a {n_sample} x {k} C3-banded P "
+                      f"sparsified at 1/sqrt({rows_full}), {procs} processes"}
+
+
+def cpu_baseline_batched(k: int, targets: int = 4, rows: int = 8192):
+    """T x dv_field (the reference has no batched API): dv_at over row chunks
+    for `targets` targets over a `rows`-row synthetic sample, all threads;
+    evals/s extrapolates linearly to T = 1024."""
+    import numpy as np
+    from oracle import divergence as O
+    P = cpu_sample_rows(k, rows, seed=13)
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    for t in range(targets):
+        O.dv_field_chunked(P, "kl", 1 + t, chunk_rows=256, threads=threads)
+    sec = time.perf_counter() - t0
+    return {"value": rows * targets / sec, "unit": "evals/s", "cores": threads, "kind": "port",
+            "sample": f"KL fields (dv_at row chunks == dv_field) for {targets} targets over "
+                      f"{rows} sampled rows x k={k}, {threads} threads; the reference "
+                      "evaluates T targets as T fields, so evals/s carries to T = 1024"}
+
+
+def _trace_one(i):
+    from oracle import tracer as OT
+    V, T, areas, diag, topo, fields, jobs = _CPU_STATE["trace"]
+    src, tgt, fi = jobs[i]
+    r = OT.triangle_descent(V, T, areas, diag, fields[fi], int(tgt), int(src), topo=topo)
+    return len(r["locations"]) if "locations" in r else 0
+
+
+def cpu_baseline_tracer(mesh, V_dev_fields, targets, src, fo, paths: int = 200):
+    """triangle_descent (paths.py:292-307, oracle/tracer.py) for `paths`
+    sampled (source, target) pairs of the C5 tracer workload, all cores."""
+    import numpy as np
+    from oracle import tracer as OT
+    pick = np.flatnonzero(fo < 32)[:paths]
+    used = np.unique(fo[pick])
+    fields = {int(f): V_dev_fields[int(f)].cpu().numpy() for f in used}
+    V = np.asarray(mesh.vertices)
+    T = np.asarray(mesh.triangles)
+    topo = OT.topology(T, len(V))
+    _CPU_STATE["trace"] = (V, T, np.asarray(mesh.triangle_areas), float(mesh.bbox_diagonal),
+                           topo, fields, [(src[i], targets[fo[i]], int(fo[i])) for i in pick])
+    procs = os.cpu_count() or 1
+    locs, sec = _cpu_pool_run(_trace_one, list(range(len(pick))), procs)
+    return {"value": len(pick) / sec, "unit": "paths/s", "cores": procs, "kind": "port",
+            "locations_per_s": float(sum(locs)) / sec,
+            "sample": f"{len(pick)} of the 10,000 paths (targets 0-31), oracle/tracer.py "
+                      f"restating paths.py:137-307, {procs} processes"}
+
+
 def run_reference_arm(args):
     ws, rank, local = dist_env()
     if rank != 0:
@@ -506,6 +607,11 @@ def extra_c4_and_c5(t, nat, dev, pf, device, steps, peak):
                              "achieved_tflops": flops / (ms64 / 1e3) / 1e12,
                              "dfma_peak_tflops": dfma_tf,
                              "frac": flops / (ms64 / 1e3) / 1e12 / dfma_tf}}
+    if not NO_CPU:
+        try:
+            c5["cpu_baseline"] = cpu_baseline_batched(k)
+        except Exception as exc:
+            c5["cpu_baseline"] = {"error": f"{type(exc).__name__}: {exc}"}
     del A, B
     del out, L, Tc, Pt, dk, P
     t.cuda.empty_cache()
@@ -582,6 +688,11 @@ def extra_c3(t, nat, dev, pf, device, steps, peak):
            "tv": _roof(nnz * 12 + rows * 24 + 16 * k, tv_ms, peak)}
     del dc, dk, P
     t.cuda.empty_cache()
+    if not NO_CPU:
+        try:
+            res["cpu_baseline"] = cpu_baseline_csr(rows, k)
+        except Exception as exc:
+            res["cpu_baseline"] = {"error": f"{type(exc).__name__}: {exc}"}
     return res
 
 
@@ -764,7 +875,14 @@ def extra_tracer(t, nat, dev, pf, device):
     wall = time.perf_counter() - w0
     ms = e0.elapsed_time(e1)
     status = buf.status.cpu().numpy()
-    return {"workload": "10,000 paths (source i -> target i % 1024), 1000x1000 grid mesh "
+    cpu = None
+    if not NO_CPU:
+        try:
+            cpu = cpu_baseline_tracer(mesh, fields, targets, src, fo)
+        except Exception as exc:
+            cpu = {"error": f"{type(exc).__name__}: {exc}"}
+    return {"cpu_baseline": cpu,
+            "workload": "10,000 paths (source i -> target i % 1024), 1000x1000 grid mesh "
                         "(1,002,001 vertices, 2,000,000 triangles), Euclidean fields",
             "paths_per_s": npaths / (ms / 1e3), "ms": ms, "wall_ms_incl_launch": 1e3 * wall,
             "locations_per_s": float(counts.sum()) / (ms / 1e3),
@@ -989,7 +1107,11 @@ def run_native(args):
     return 0
 
 
+NO_CPU = False
+
+
 def main():
+    global NO_CPU
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
@@ -1004,6 +1126,7 @@ def main():
                     help="comma list of side measurements to run "
                          "(f32, c3, c4c5, tracer, wire, poisson)")
     args = ap.parse_args()
+    NO_CPU = bool(args.no_cpu)
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
