@@ -226,6 +226,22 @@ int pf_csr_tv_f64(const int64_t *indptr, const int32_t *indices, const double *d
                   const double *tscal, int64_t row0, const int64_t *queries, int64_t nq,
                   double *out, int64_t *ops, pf_stream_t stream);
 
+/* ---- K5/K6 over 16-bit column indices (k <= 65,536) -------------------------
+ * The same fields with the device CSR's columns narrowed to uint16
+ * (pf_csr_narrow_u16, once per CSR): 10 instead of 12 streamed bytes per
+ * entry (the algorithmic figure stays scipy's int32 layout). */
+int pf_csr_narrow_u16(const int32_t *indices, int64_t n, uint16_t *indices16,
+                      pf_stream_t stream);
+int pf_csr_kl_u16_f64(const int64_t *indptr, const uint16_t *indices16, const double *data,
+                      const double *log_data, const double *hs, int64_t rows, int64_t k,
+                      const double *logt, double tau, int64_t row0, const int64_t *queries,
+                      int64_t nq, double *out, int64_t *ops, uint32_t *flags, int64_t *queue,
+                      pf_stream_t stream);
+int pf_csr_tv_u16_f64(const int64_t *indptr, const uint16_t *indices16, const double *data,
+                      const double *dropped, int64_t rows, int64_t k, const double *vp,
+                      const double *tscal, int64_t row0, const int64_t *queries, int64_t nq,
+                      double *out, int64_t *ops, pf_stream_t stream);
+
 /* ---- K5/K6 for the other generators (divergence.py:275-299) ---------------
  * kind PF_DIV_ALPHA: sum_{supp q} v (1 - exp(expo (logt - log v))) * scale,
  *   settle; ops = |supp q|.  Needs logt (the target's dense log row).

@@ -24,6 +24,8 @@
 // 2*dropped_p at q = p because S_p is reduced in the same lane order.
 #include <cmath>
 
+#include <algorithm>
+
 #include "pf_common.cuh"
 
 namespace pf {
@@ -142,34 +144,52 @@ __global__ void csr_dropped_kernel(const int64_t *__restrict__ indptr,
 // flight, and an odd tail goes to lane 0.  The per-lane visiting order is a
 // fixed function of (lo, hi), which K6 relies on (csr_target_prep sums S_p
 // with this same traversal, so TV(p, p) cancels exactly).
-template <class F>
+// Index pairs: int32 columns load as int2 (8 B), 16-bit columns (k < 65,536,
+// the B200 layout of pf_csr_narrow_u16) as ushort2 (4 B): 10 instead of 12
+// streamed bytes per entry.
+__device__ __forceinline__ int2 idx_pair(const int32_t *__restrict__ idx, int64_t s, int64_t j) {
+  return __ldg(reinterpret_cast<const int2 *>(idx + s) + j);
+}
+__device__ __forceinline__ int2 idx_pair(const uint16_t *__restrict__ idx, int64_t s, int64_t j) {
+  const ushort2 u = __ldg(reinterpret_cast<const ushort2 *>(idx + s) + j);
+  return make_int2(u.x, u.y);
+}
+
+template <class Idx, class F>
 __device__ __forceinline__ void csr_row_visit(const double *__restrict__ data,
-                                              const int32_t *__restrict__ idx, int64_t lo,
+                                              const Idx *__restrict__ idx, int64_t lo,
                                               int64_t hi, int lane, F &&f) {
   int64_t s = lo;
   if ((s & 1) && s < hi) {
-    if (lane == 0) f(__ldg(data + s), __ldg(idx + s));
+    if (lane == 0) f(__ldg(data + s), (int32_t)__ldg(idx + s));
     ++s;
   }
   const int64_t npairs = (hi - s) >> 1;
   const double2 *d2 = reinterpret_cast<const double2 *>(data + s);
-  const int2 *i2 = reinterpret_cast<const int2 *>(idx + s);
   int64_t j = lane;
-  for (; j + 32 < npairs; j += 64) {
-    const double2 va = __ldg(d2 + j), vb = __ldg(d2 + j + 32);
-    const int2 ca = __ldg(i2 + j), cb = __ldg(i2 + j + 32);
-    f(va.x, ca.x);
-    f(va.y, ca.y);
-    f(vb.x, cb.x);
-    f(vb.y, cb.y);
+  // 4 pairs per lane in flight (the kernels are latency-bound: ~32 resident
+  // warps per SM need ~2.5 KB each in flight to cover DRAM latency at 7 TB/s)
+  for (; j + 96 < npairs; j += 128) {
+    double2 v[4];
+    int2 cidx[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      v[u] = __ldg(d2 + j + 32 * u);
+      cidx[u] = idx_pair(idx, s, j + 32 * u);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      f(v[u].x, cidx[u].x);
+      f(v[u].y, cidx[u].y);
+    }
   }
-  if (j < npairs) {
+  for (; j < npairs; j += 32) {
     const double2 va = __ldg(d2 + j);
-    const int2 ca = __ldg(i2 + j);
+    const int2 ca = idx_pair(idx, s, j);
     f(va.x, ca.x);
     f(va.y, ca.y);
   }
-  if (((hi - s) & 1) && lane == 0) f(__ldg(data + hi - 1), __ldg(idx + hi - 1));
+  if (((hi - s) & 1) && lane == 0) f(__ldg(data + hi - 1), (int32_t)__ldg(idx + hi - 1));
 }
 
 // ---------------------------------------------------- K5/K6 target prep --
@@ -217,9 +237,9 @@ __device__ __forceinline__ const double *stage_vec(unsigned char *smem, const do
 }
 
 // ------------------------------------------------------------ K5 CSR KL --
-template <bool STAGE>
+template <bool STAGE, class Idx>
 __global__ void __launch_bounds__(kCsrThreads) csr_kl_kernel(
-    const int64_t *__restrict__ indptr, const int32_t *__restrict__ indices,
+    const int64_t *__restrict__ indptr, const Idx *__restrict__ indices,
     const double *__restrict__ data, const double *__restrict__ hs, int64_t rows, int64_t k_pad,
     const double *__restrict__ logt, double tau, int64_t row0, const int64_t *__restrict__ queries,
     int64_t nq, double *__restrict__ out, int64_t *__restrict__ ops, int64_t *__restrict__ queue,
@@ -267,8 +287,9 @@ __global__ void __launch_bounds__(kCsrThreads) csr_kl_kernel(
 }
 
 // Guarded rows: reference form sum_{supp q} v * (log v - logPt) (divergence.py:279).
+template <class Idx>
 __global__ void __launch_bounds__(kCsrThreads) csr_kl_fixup_kernel(
-    const int64_t *__restrict__ indptr, const int32_t *__restrict__ indices,
+    const int64_t *__restrict__ indptr, const Idx *__restrict__ indices,
     const double *__restrict__ data, const double *__restrict__ log_data, int64_t rows,
     const double *__restrict__ logt, int64_t row0, const int64_t *__restrict__ queries,
     int64_t nq, double *__restrict__ out, uint32_t *__restrict__ flags) {
@@ -310,8 +331,9 @@ __global__ void __launch_bounds__(kCsrThreads) csr_kl_fixup_kernel(
 // but each is a chain of dependent loads (index -> logt gather), so a warp
 // takes its row 512 entries at a time with every load of the chunk in flight
 // before the gathers (row starts are even in the device CSR: aligned pairs).
+template <class Idx>
 __global__ void __launch_bounds__(kCsrThreads) csr_kl_fixup_queue_kernel(
-    const int64_t *__restrict__ indptr, const int32_t *__restrict__ indices,
+    const int64_t *__restrict__ indptr, const Idx *__restrict__ indices,
     const double *__restrict__ data, const double *__restrict__ log_data,
     const double *__restrict__ logt, int64_t row0, const int64_t *__restrict__ queries,
     const int64_t *__restrict__ queue, const uint32_t *__restrict__ flags,
@@ -335,7 +357,7 @@ __global__ void __launch_bounds__(kCsrThreads) csr_kl_fixup_queue_kernel(
         if (e < hi) {
           dv[u] = __ldg(reinterpret_cast<const double2 *>(data + e));
           lv[u] = __ldg(reinterpret_cast<const double2 *>(log_data + e));
-          iv[u] = __ldg(reinterpret_cast<const int2 *>(indices + e));
+          iv[u] = idx_pair(indices, e, 0);
         }
       }
       double tx[8], ty[8];
@@ -358,9 +380,9 @@ __global__ void __launch_bounds__(kCsrThreads) csr_kl_fixup_queue_kernel(
 }
 
 // ------------------------------------------------------------ K6 CSR TV --
-template <bool STAGE>
+template <bool STAGE, class Idx>
 __global__ void __launch_bounds__(kCsrThreads) csr_tv_kernel(
-    const int64_t *__restrict__ indptr, const int32_t *__restrict__ indices,
+    const int64_t *__restrict__ indptr, const Idx *__restrict__ indices,
     const double *__restrict__ data, const double *__restrict__ dropped, int64_t rows,
     int64_t k_pad, const double *__restrict__ vp, const double *__restrict__ tscal, int64_t row0,
     const int64_t *__restrict__ queries, int64_t nq, double *__restrict__ out,
@@ -528,6 +550,78 @@ static int smem_attr(K kern, size_t smem) {
   return ensure_smem((const void *)kern, smem);
 }
 
+template <class Idx>
+int csr_kl_launch(const int64_t *indptr, const Idx *indices, const double *data,
+                  const double *log_data, const double *hs, int64_t rows, int64_t k,
+                  const double *logt, double tau, int64_t row0, const int64_t *queries,
+                  int64_t nq, double *out, int64_t *ops, uint32_t *flags, int64_t *queue,
+                  pf_stream_t stream) {
+  if (queue && !flags) return fail(PF_E_ARG, "csr_kl: the guard queue needs flags");
+  if (!indptr || !indices || !hs || !logt || !out || rows < 0 || k <= 0)
+    return fail(PF_E_ARG, "csr_kl: bad args");
+  const int64_t count = queries ? nq : rows;
+  if (count <= 0) return 0;
+  const int64_t k_pad = round_up(k, 2);
+  const size_t smem = 16 + static_cast<size_t>(k_pad) * 8;
+  const bool staged = smem <= 200 * 1024;
+  if (staged) {
+    if (int e = smem_attr(csr_kl_kernel<true, Idx>, smem)) return e;
+    const int g = grid_for((const void *)csr_kl_kernel<true, Idx>, kCsrThreads, smem, count);
+    csr_kl_kernel<true, Idx><<<g, kCsrThreads, smem, as_stream(stream)>>>(
+        indptr, indices, data, hs, rows, k_pad, logt, tau, row0, queries, nq, out, ops, queue,
+        flags);
+  } else {
+    const int g = grid_for((const void *)csr_kl_kernel<false, Idx>, kCsrThreads, 0, count);
+    csr_kl_kernel<false, Idx><<<g, kCsrThreads, 0, as_stream(stream)>>>(
+        indptr, indices, data, hs, rows, k_pad, logt, tau, row0, queries, nq, out, ops, queue,
+        flags);
+  }
+  if (int e = check_launch("csr_kl")) return e;
+  if (queue) {
+    csr_kl_fixup_queue_kernel<Idx><<<sm_count() * 2, kCsrThreads, 0, as_stream(stream)>>>(
+        indptr, indices, data, log_data, logt, row0, queries, queue, flags, out);
+    return check_launch("csr_kl_fixup_queue");
+  }
+  int64_t want = (count + 7) / 8;
+  int64_t g2 = static_cast<int64_t>(sm_count()) * 4;
+  if (g2 > want) g2 = want;
+  if (g2 < 1) g2 = 1;
+  csr_kl_fixup_kernel<Idx><<<static_cast<int>(g2), kCsrThreads, 0, as_stream(stream)>>>(
+      indptr, indices, data, log_data, rows, logt, row0, queries, nq, out, flags);
+  return check_launch("csr_kl_fixup");
+}
+
+template <class Idx>
+int csr_tv_launch(const int64_t *indptr, const Idx *indices, const double *data,
+                  const double *dropped, int64_t rows, int64_t k, const double *vp,
+                  const double *tscal, int64_t row0, const int64_t *queries, int64_t nq,
+                  double *out, int64_t *ops, pf_stream_t stream) {
+  if (!indptr || !indices || !dropped || !vp || !tscal || !out || rows < 0 || k <= 0)
+    return fail(PF_E_ARG, "csr_tv: bad args");
+  const int64_t count = queries ? nq : rows;
+  if (count <= 0) return 0;
+  const int64_t k_pad = round_up(k, 2);
+  const size_t smem = 16 + static_cast<size_t>(k_pad) * 8;
+  if (smem <= 200 * 1024) {
+    if (int e = smem_attr(csr_tv_kernel<true, Idx>, smem)) return e;
+    const int g = grid_for((const void *)csr_tv_kernel<true, Idx>, kCsrThreads, smem, count);
+    csr_tv_kernel<true, Idx><<<g, kCsrThreads, smem, as_stream(stream)>>>(
+        indptr, indices, data, dropped, rows, k_pad, vp, tscal, row0, queries, nq, out, ops);
+  } else {
+    const int g = grid_for((const void *)csr_tv_kernel<false, Idx>, kCsrThreads, 0, count);
+    csr_tv_kernel<false, Idx><<<g, kCsrThreads, 0, as_stream(stream)>>>(
+        indptr, indices, data, dropped, rows, k_pad, vp, tscal, row0, queries, nq, out, ops);
+  }
+  return check_launch("csr_tv");
+}
+
+__global__ void narrow_u16_kernel(const int32_t *__restrict__ in, int64_t n,
+                                  uint16_t *__restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = static_cast<uint16_t>(in[i]);
+}
+
 }  // namespace pf
 
 using namespace pf;
@@ -576,67 +670,49 @@ int pf_csr_target_prep_f64(const int64_t *indptr, const int32_t *indices, const 
   return check_launch("csr_target_prep");
 }
 
+
 int pf_csr_kl_f64(const int64_t *indptr, const int32_t *indices, const double *data,
                   const double *log_data, const double *hs, int64_t rows, int64_t k,
                   const double *logt, double tau, int64_t row0, const int64_t *queries,
                   int64_t nq, double *out, int64_t *ops, uint32_t *flags, int64_t *queue,
                   pf_stream_t stream) {
-  if (queue && !flags) return fail(PF_E_ARG, "csr_kl: the guard queue needs flags");
-  if (!indptr || !hs || !logt || !out || rows < 0 || k <= 0)
-    return fail(PF_E_ARG, "csr_kl: bad args");
-  const int64_t count = queries ? nq : rows;
-  if (count <= 0) return 0;
-  const int64_t k_pad = round_up(k, 2);
-  const size_t smem = 16 + static_cast<size_t>(k_pad) * 8;
-  const bool staged = smem <= 200 * 1024;
-  if (staged) {
-    if (int e = smem_attr(csr_kl_kernel<true>, smem)) return e;
-    const int g = grid_for((const void *)csr_kl_kernel<true>, kCsrThreads, smem, count);
-    csr_kl_kernel<true><<<g, kCsrThreads, smem, as_stream(stream)>>>(
-        indptr, indices, data, hs, rows, k_pad, logt, tau, row0, queries, nq, out, ops, queue,
-        flags);
-  } else {
-    const int g = grid_for((const void *)csr_kl_kernel<false>, kCsrThreads, 0, count);
-    csr_kl_kernel<false><<<g, kCsrThreads, 0, as_stream(stream)>>>(
-        indptr, indices, data, hs, rows, k_pad, logt, tau, row0, queries, nq, out, ops, queue,
-        flags);
-  }
-  if (int e = check_launch("csr_kl")) return e;
-  if (queue) {
-    csr_kl_fixup_queue_kernel<<<sm_count() * 2, kCsrThreads, 0, as_stream(stream)>>>(
-        indptr, indices, data, log_data, logt, row0, queries, queue, flags, out);
-    return check_launch("csr_kl_fixup_queue");
-  }
-  int64_t want = (count + 7) / 8;
-  int64_t g2 = static_cast<int64_t>(sm_count()) * 4;
-  if (g2 > want) g2 = want;
-  if (g2 < 1) g2 = 1;
-  csr_kl_fixup_kernel<<<static_cast<int>(g2), kCsrThreads, 0, as_stream(stream)>>>(
-      indptr, indices, data, log_data, rows, logt, row0, queries, nq, out, flags);
-  return check_launch("csr_kl_fixup");
+  return csr_kl_launch(indptr, indices, data, log_data, hs, rows, k, logt, tau, row0, queries,
+                       nq, out, ops, flags, queue, stream);
+}
+
+int pf_csr_kl_u16_f64(const int64_t *indptr, const uint16_t *indices16, const double *data,
+                      const double *log_data, const double *hs, int64_t rows, int64_t k,
+                      const double *logt, double tau, int64_t row0, const int64_t *queries,
+                      int64_t nq, double *out, int64_t *ops, uint32_t *flags, int64_t *queue,
+                      pf_stream_t stream) {
+  if (k > 65536) return fail(PF_E_DOMAIN, "csr_kl_u16: k must be <= 65536");
+  return csr_kl_launch(indptr, indices16, data, log_data, hs, rows, k, logt, tau, row0,
+                       queries, nq, out, ops, flags, queue, stream);
 }
 
 int pf_csr_tv_f64(const int64_t *indptr, const int32_t *indices, const double *data,
                   const double *dropped, int64_t rows, int64_t k, const double *vp,
                   const double *tscal, int64_t row0, const int64_t *queries, int64_t nq,
                   double *out, int64_t *ops, pf_stream_t stream) {
-  if (!indptr || !dropped || !vp || !tscal || !out || rows < 0 || k <= 0)
-    return fail(PF_E_ARG, "csr_tv: bad args");
-  const int64_t count = queries ? nq : rows;
-  if (count <= 0) return 0;
-  const int64_t k_pad = round_up(k, 2);
-  const size_t smem = 16 + static_cast<size_t>(k_pad) * 8;
-  if (smem <= 200 * 1024) {
-    if (int e = smem_attr(csr_tv_kernel<true>, smem)) return e;
-    const int g = grid_for((const void *)csr_tv_kernel<true>, kCsrThreads, smem, count);
-    csr_tv_kernel<true><<<g, kCsrThreads, smem, as_stream(stream)>>>(
-        indptr, indices, data, dropped, rows, k_pad, vp, tscal, row0, queries, nq, out, ops);
-  } else {
-    const int g = grid_for((const void *)csr_tv_kernel<false>, kCsrThreads, 0, count);
-    csr_tv_kernel<false><<<g, kCsrThreads, 0, as_stream(stream)>>>(
-        indptr, indices, data, dropped, rows, k_pad, vp, tscal, row0, queries, nq, out, ops);
-  }
-  return check_launch("csr_tv");
+  return csr_tv_launch(indptr, indices, data, dropped, rows, k, vp, tscal, row0, queries, nq,
+                       out, ops, stream);
+}
+
+int pf_csr_tv_u16_f64(const int64_t *indptr, const uint16_t *indices16, const double *data,
+                      const double *dropped, int64_t rows, int64_t k, const double *vp,
+                      const double *tscal, int64_t row0, const int64_t *queries, int64_t nq,
+                      double *out, int64_t *ops, pf_stream_t stream) {
+  if (k > 65536) return fail(PF_E_DOMAIN, "csr_tv_u16: k must be <= 65536");
+  return csr_tv_launch(indptr, indices16, data, dropped, rows, k, vp, tscal, row0, queries, nq,
+                       out, ops, stream);
+}
+
+int pf_csr_narrow_u16(const int32_t *indices, int64_t n, uint16_t *indices16,
+                      pf_stream_t stream) {
+  if (n < 0 || (n && (!indices || !indices16))) return fail(PF_E_ARG, "csr_narrow_u16: bad args");
+  if (n == 0) return 0;
+  narrow_u16_kernel<<<static_cast<int>(std::min<int64_t>((n + 255) / 256, sm_count() * 32)), 256, 0, as_stream(stream)>>>(indices, n, indices16);
+  return check_launch("csr_narrow_u16");
 }
 
 int pf_csr_generic_f64(const int64_t *indptr, const int32_t *indices, const double *data,

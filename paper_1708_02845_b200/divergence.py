@@ -587,7 +587,8 @@ def _sparse_launch(pk, fd, p: int, queries=None, want_ops=False):
         nat.call("pf_target_prep_f64", dk.row_ptr(p), dk.k, _CLAMP_LOG, st.tgt, st.logt,
                  st.tmask, flags, s.cuda_stream)
         if fd.name == "kl":
-            nat.call("pf_csr_kl_f64", dc.indptr.data_ptr(), dc.indices.data_ptr(),
+            entry, idx = dc.field_entry("kl")
+            nat.call(entry, dc.indptr.data_ptr(), idx,
                      dc.data.data_ptr(), dc.log_data.data_ptr(), dc.hs.data_ptr(), dk.rows,
                      dk.k, st.logt, KL_GUARD_TAU, dk.row0, qptr, count, out.data_ptr(),
                      nat.ptr(ops), flags, dk.scratch(s.cuda_stream, 8 * count, "csrq").data_ptr(),
@@ -602,7 +603,8 @@ def _sparse_launch(pk, fd, p: int, queries=None, want_ops=False):
         nat.call("pf_csr_target_prep_f64", dc.indptr.data_ptr(), dc.indices.data_ptr(),
                  dc.data.data_ptr(), dc.dropped.data_ptr(), p - dk.row0, dk.k, st.data_ptr(),
                  st.data_ptr() + k_pad * 8, s.cuda_stream)
-        nat.call("pf_csr_tv_f64", dc.indptr.data_ptr(), dc.indices.data_ptr(), dc.data.data_ptr(),
+        entry, idx = dc.field_entry("tv")
+        nat.call(entry, dc.indptr.data_ptr(), idx, dc.data.data_ptr(),
                  dc.dropped.data_ptr(), dk.rows, dk.k, st.data_ptr(), st.data_ptr() + k_pad * 8,
                  dk.row0, qptr, count, out.data_ptr(), nat.ptr(ops), s.cuda_stream)
     else:

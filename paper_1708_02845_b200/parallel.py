@@ -278,13 +278,15 @@ def _compute_sparse_slab(slab, fd, p: int, payload, cut: float, strict: bool):
         st = _Staging(t, slab.k, slab.device)
         nat.call("pf_target_prep_f64", payload.data_ptr(), slab.k, _CLAMP_LOG, st.tgt, st.logt,
                  st.tmask, flags, s)
-        nat.call("pf_csr_kl_f64", dc.indptr.data_ptr(), dc.indices.data_ptr(), dc.data.data_ptr(),
+        entry, idx = dc.field_entry("kl")
+        nat.call(entry, dc.indptr.data_ptr(), idx, dc.data.data_ptr(),
                  dc.log_data.data_ptr(), dc.hs.data_ptr(), slab.rows, slab.k, st.logt,
                  KL_GUARD_TAU, slab.row0, 0, slab.rows, out.data_ptr(), 0, flags,
                  slab.scratch(s, 8 * slab.rows, "csrq").data_ptr(), s)
     else:
         kp = slab.k + (slab.k & 1)
-        nat.call("pf_csr_tv_f64", dc.indptr.data_ptr(), dc.indices.data_ptr(), dc.data.data_ptr(),
+        entry, idx = dc.field_entry("tv")
+        nat.call(entry, dc.indptr.data_ptr(), idx, dc.data.data_ptr(),
                  dc.dropped.data_ptr(), slab.rows, slab.k, payload.data_ptr(),
                  payload.data_ptr() + kp * 8, slab.row0, 0, slab.rows, out.data_ptr(), 0, s)
     return out[:slab.rows]

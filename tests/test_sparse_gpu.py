@@ -176,3 +176,29 @@ def test_sparse_slabs_bitwise():
         torch.cuda.synchronize()
         got = torch.cat(parts).cpu().numpy()
         np.testing.assert_array_equal(got, full[g])
+
+
+@pytest.mark.parametrize("name", SPARSE_CASES)
+def test_u16_columns_bitwise_equal_int32(name):
+    """The 16-bit-column field kernels (pf_csr_{kl,tv}_u16_f64) return exactly the
+    int32-column results: same entries, same visiting order."""
+    from paper_1708_02845_b200 import _device as dev
+    from paper_1708_02845_b200 import divergence as D
+    c = case(name)
+    spk = pf.sparsify(_pk(c))
+    dk, dc = D._device_csr(spk)
+    assert dc.indices16 is not None
+    np.testing.assert_array_equal(dc.indices16.cpu().numpy().astype(np.int64) & 0xffff,
+                                  dc.indices.cpu().numpy().astype(np.int64))
+    t = dev.torch()
+    target = int(c.target)
+    for g in ("kl", "tv"):
+        a = pf.dv_field_sparse(spk, pf.builtin_f(g), target).values.copy()
+        saved = dc.indices16
+        try:
+            dc.indices16 = None  # force the int32 entry points
+            b = pf.dv_field_sparse(spk, pf.builtin_f(g), target).values.copy()
+        finally:
+            dc.indices16 = saved
+        assert np.array_equal(a.view(np.int64), b.view(np.int64)), g
+    del t
