@@ -574,10 +574,13 @@ int pf_poisson_residual(const double *P, int64_t ldp, int64_t k, const int32_t *
 
 /* Boundary rows -> indicators of their column, pad columns -> 0, interior
  * entries in (-1e-12, 0) -> 0 (solvers.py:293-296); out_max[0] = max
- * |row sum - 1| (row_sum_error, :297) as ordered FP64 bits. */
+ * |row sum - 1| (row_sum_error, :297) as ordered FP64 bits.  Fused K1: if H
+ * != NULL, H[r] = sum_b c(P) log c(P) with c = max(., clamp), bitwise what
+ * pf_row_negentropy_f64 returns, and min_out[0] (seeded +inf by the caller) =
+ * min over P[:, :k]. */
 int pf_poisson_finalize(double *P, int64_t ldp, int64_t n, int64_t k,
-                        const uint8_t *is_boundary, const int32_t *bcol,
-                        unsigned long long *out_max, pf_stream_t stream);
+                        const uint8_t *is_boundary, const int32_t *bcol, double clamp, double *H,
+                        double *min_out, unsigned long long *out_max, pf_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -817,34 +817,76 @@ __global__ void residual_table_kernel(const int32_t *__restrict__ nb_idx, int64_
   }
 }
 
+// Boundary rows -> indicators, pad columns -> 0, the reference's clip of
+// (-1e-12, 0) on interior entries, max |row sum - 1|, and (fused K1) the
+// per-row negentropy H[r] = sum_b c(P) log c(P), c = max(., clamp) with
+// pf_row_negentropy_f64's exact lane order (pairs per lane, x / y
+// accumulators, odd tail on lane 0), plus min(P) over columns < k — so the
+// first KL field on a freshly built P does not stream it once more for K1.
 __global__ void finalize_kernel(double *P, int64_t ldp, int64_t n, int64_t k,
                                 const uint8_t *__restrict__ isb, const int32_t *__restrict__ bcol,
+                                double clamp, double *__restrict__ H, double *min_out,
                                 unsigned long long *out) {
   const int lane = threadIdx.x % 32;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
-  double mx = 0.0;
+  const int64_t npair = k >> 1;
+  double mx = 0.0, mn = INFINITY;
   for (int64_t v = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32; v < n;
        v += warps) {
     double *row = P + v * ldp;
-    if (isb[v]) {
+    const bool bnd = isb[v];
+    if (bnd) {
       const int32_t b = bcol[v];
       for (int64_t j = lane; j < ldp; j += 32) row[j] = (j == b) ? 1.0 : 0.0;
-      continue;  // rows sum to exactly 1
+      __syncwarp();
     }
-    double s = 0.0;
-    for (int64_t j = lane; j < k; j += 32) {
-      double x = row[j];
-      if (x > -1e-12 && x < 0.0) {  // solvers.py:293-295
-        x = 0.0;
-        row[j] = 0.0;
+    double s0 = 0.0, s1 = 0.0, a0 = 0.0, a1 = 0.0;
+    for (int64_t j = lane; j < npair; j += 32) {
+      double2 x = reinterpret_cast<double2 *>(row)[j];
+      if (!bnd) {
+        const bool cx = x.x > -1e-12 && x.x < 0.0, cy = x.y > -1e-12 && x.y < 0.0;
+        if (cx) x.x = 0.0;  // solvers.py:293-295
+        if (cy) x.y = 0.0;
+        if (cx || cy) reinterpret_cast<double2 *>(row)[j] = x;
       }
-      s += x;
+      s0 += x.x;
+      s1 += x.y;
+      mn = fmin(mn, fmin(x.x, x.y));
+      const double q0 = fmax(x.x, clamp), q1 = fmax(x.y, clamp);
+      a0 += __dmul_rn(q0, log(q0));
+      a1 += __dmul_rn(q1, log(q1));
     }
-    for (int64_t j = k + lane; j < ldp; j += 32) row[j] = 0.0;
-    s = warp_sum(s);
-    mx = fmax(mx, fabs(s - 1.0));
+    if ((k & 1) && lane == 0) {
+      double x = row[k - 1];
+      if (!bnd && x > -1e-12 && x < 0.0) {
+        x = 0.0;
+        row[k - 1] = 0.0;
+      }
+      s0 += x;
+      mn = fmin(mn, x);
+      const double q = fmax(x, clamp);
+      a0 += __dmul_rn(q, log(q));
+    }
+    if (!bnd)
+      for (int64_t j = k + lane; j < ldp; j += 32) row[j] = 0.0;
+    const double h = warp_sum(a0 + a1);
+    if (H && lane == 0) H[v] = h;
+    const double sum = warp_sum(s0 + s1);
+    if (!bnd) mx = fmax(mx, fabs(sum - 1.0));  // boundary rows sum to exactly 1
   }
   if (lane == 0) atomic_max_nonneg(out, mx);
+  if (min_out) {
+    mn = warp_min(mn);
+    if (lane == 0 && mn < INFINITY) {  // ordered-integer atomic min (values may be < 0)
+      unsigned long long *addr = reinterpret_cast<unsigned long long *>(min_out);
+      unsigned long long old = *addr, assumed;
+      do {
+        assumed = old;
+        if (__longlong_as_double(assumed) <= mn) break;
+        old = atomicCAS(addr, assumed, __double_as_longlong(mn));
+      } while (old != assumed);
+    }
+  }
 }
 
 int grid_for(int64_t work, int per_block) {
@@ -993,13 +1035,14 @@ int pf_poisson_residual(const double *P, int64_t ldp, int64_t k, const int32_t *
 }
 
 int pf_poisson_finalize(double *P, int64_t ldp, int64_t n, int64_t k,
-                        const uint8_t *is_boundary, const int32_t *bcol,
-                        unsigned long long *out_max, pf_stream_t stream) {
-  if (!P || !is_boundary || !bcol || !out_max || n < 0 || k < 0 || ldp < k)
+                        const uint8_t *is_boundary, const int32_t *bcol, double clamp, double *H,
+                        double *min_out, unsigned long long *out_max, pf_stream_t stream) {
+  if (!P || !is_boundary || !bcol || !out_max || n < 0 || k < 0 || ldp < k || (ldp & 1) ||
+      (reinterpret_cast<uintptr_t>(P) & 15))
     return fail(PF_E_ARG, "pf_poisson_finalize: bad argument");
   if (n == 0) return 0;
   finalize_kernel<<<grid_for(n, 8), 256, 0, as_stream(stream)>>>(P, ldp, n, k, is_boundary, bcol,
-                                                                  out_max);
+                                                                  clamp, H, min_out, out_max);
   return check_launch("pf_poisson_finalize");
 }
 

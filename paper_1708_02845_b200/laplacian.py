@@ -54,6 +54,7 @@ _STATS = ("n", "m", "k", "nodes", "levels", "f_total", "v_total", "nnz_l", "flop
           "flops_solve", "max_f", "max_c", "max_r", "ntiles", "tile", "leaf")
 
 LEAF = 64   # leaf sub-domain size of the dissection
+KL_CLAMP = 1e-300  # divergence.py:82-83 (the H the fused K1 precomputes)
 TILE = 64   # column tile of the multi-RHS solves (pf_mf_plan_t.tile)
 
 
@@ -352,8 +353,14 @@ class DevicePoisson:
         nat.call("pf_poisson_residual", P.data_ptr(), ld, self.k,
                  self._dev["perm_orig"].data_ptr(), self.plan.m, dm.nb_ptr.data_ptr(),
                  nrow.data_ptr(), off.data_ptr(), diag.data_ptr(), mx.data_ptr(), s)
+        # fused K1: the KL negentropy per row (clamp 1e-300) and min(P), so the
+        # first field on this P does not stream it again
+        H = t.empty(self.n, dtype=t.float64, device=self.device)
+        mn = t.full((1,), float("inf"), dtype=t.float64, device=self.device)
         nat.call("pf_poisson_finalize", P.data_ptr(), ld, self.n, self.k,
-                 self.is_boundary.data_ptr(), self.bcol.data_ptr(), mx.data_ptr() + 8, s)
+                 self.is_boundary.data_ptr(), self.bcol.data_ptr(), KL_CLAMP, H.data_ptr(),
+                 mn.data_ptr(), mx.data_ptr() + 8, s)
+        self.last_H, self.last_min = H, mn
         mark("end")
         del O, Wb
         r = mx.cpu().numpy().astype(np.uint64)
@@ -407,6 +414,8 @@ class DevicePoisson:
         P, residual, rse = self.solve(P)
         dk = dev.DeviceKernel(None, self.boundary, n=self.n, k=self.k, P_dev=P)
         dk.residual, dk.row_sum_error = residual, rse
+        dk._H[KL_CLAMP] = self.last_H     # K1, fused into the build's finalize pass
+        dk._min = self.last_min
         return dk
 
 

@@ -177,3 +177,24 @@ def test_poisson_kernel_host_copy_and_device_registration():
     np.testing.assert_array_equal(dk.P[:, :c.k].cpu().numpy(), pk.dense)
     assert not pk.dense.flags.writeable
     np.testing.assert_array_equal(pk.boundary, c.boundary)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["c1", "holes_fine"])
+def test_fused_negentropy_bitwise_k1(name):
+    """The build's finalize pass precomputes K1 (H for the KL clamp, min P):
+    bitwise what pf_row_negentropy_f64 returns on the finished P."""
+    from paper_1708_02845_b200 import _device as dev
+    from paper_1708_02845_b200 import _native as nat
+    from paper_1708_02845_b200.laplacian import KL_CLAMP, DevicePoisson
+    t = dev.torch()
+    c = case(name)
+    dk = DevicePoisson(c.mesh).device_kernel()
+    fused = dk._H[KL_CLAMP].clone()
+    fused_min = float(dk._min.item())
+    H = t.empty_like(fused)
+    mn = t.full((1,), float("inf"), dtype=t.float64, device=fused.device)
+    nat.call("pf_row_negentropy_f64", dk.P.data_ptr(), dk.ld, dk.rows, dk.k, KL_CLAMP,
+             H.data_ptr(), mn.data_ptr(), t.cuda.current_stream().cuda_stream)
+    assert bool((H.view(t.int64) == fused.view(t.int64)).all())
+    assert float(mn.item()) == fused_min
