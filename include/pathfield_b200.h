@@ -499,6 +499,8 @@ typedef struct {
   const int32_t *perm_orig;          /* position -> original vertex id               */
   const int64_t *mt_off;             /* per node: Mt (f x round_up(c,16)) offset     */
   const int64_t *m_off;              /* per node: M = Mt^T (c x round_up(f,16))      */
+  const int64_t *rowoff;             /* NULL: vertex v's output row at v * ldp; else
+                                        the row-slab build's per-vertex offsets   */
   int64_t nodes, ntiles, k;
   int32_t tile;                      /* must be 64 */
   int32_t pad_;
@@ -559,8 +561,8 @@ int pf_mf_backward_level(const pf_mf_plan_t *plan, const double *M, const double
 /* Gather table of the residual: nrow[e] = nb_idx[e] * ldp for an interior
  * neighbour entry, -1 - bcol[u] for a boundary one (built once per mesh). */
 int pf_poisson_residual_table(const int32_t *nb_idx, int64_t nnz, const uint8_t *is_boundary,
-                              const int32_t *bcol, int64_t ldp, int64_t *nrow,
-                              pf_stream_t stream);
+                              const int32_t *bcol, int64_t ldp, const int64_t *rowoff,
+                              int64_t *nrow, pf_stream_t stream);
 
 /* residual = max |(Lc P)[v, j]| over the interior rows v = order[0..count)
  * and columns j < k with P's boundary rows taken as indicators (= |Lc_II P_IB
@@ -568,9 +570,9 @@ int pf_poisson_residual_table(const int32_t *nb_idx, int64_t nnz, const uint8_t 
  * ordered FP64 bits.  `order` is best the plan's perm_orig (spatially compact
  * row groups share their neighbours' rows in cache). */
 int pf_poisson_residual(const double *P, int64_t ldp, int64_t k, const int32_t *order,
-                        int64_t count, const int64_t *nb_ptr, const int64_t *nrow,
-                        const double *off, const double *diag, unsigned long long *out_max,
-                        pf_stream_t stream);
+                        int64_t count, const int64_t *rowoff, const int64_t *nb_ptr,
+                        const int64_t *nrow, const double *off, const double *diag,
+                        unsigned long long *out_max, pf_stream_t stream);
 
 /* Boundary rows -> indicators of their column, pad columns -> 0, interior
  * entries in (-1e-12, 0) -> 0 (solvers.py:293-296); out_max[0] = max
@@ -578,7 +580,7 @@ int pf_poisson_residual(const double *P, int64_t ldp, int64_t k, const int32_t *
  * != NULL, H[r] = sum_b c(P) log c(P) with c = max(., clamp), bitwise what
  * pf_row_negentropy_f64 returns, and min_out[0] (seeded +inf by the caller) =
  * min over P[:, :k]. */
-int pf_poisson_finalize(double *P, int64_t ldp, int64_t n, int64_t k,
+int pf_poisson_finalize(double *P, int64_t ldp, int64_t row0, int64_t n, int64_t k,
                         const uint8_t *is_boundary, const int32_t *bcol, double clamp, double *H,
                         double *min_out, unsigned long long *out_max, pf_stream_t stream);
 

@@ -108,10 +108,11 @@ _SIGS.update({
                             c_i64, c_vp, c_vp, c_vp],
     "pf_mf_backward_level": [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_int, c_int,
                              c_int, c_vp, c_i64, c_vp],
-    "pf_poisson_residual_table": [c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp],
-    "pf_poisson_residual": [c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
-    "pf_poisson_finalize": [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_dbl, c_vp, c_vp, c_vp,
+    "pf_poisson_residual_table": [c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp],
+    "pf_poisson_residual": [c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                             c_vp],
+    "pf_poisson_finalize": [c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_dbl, c_vp, c_vp,
+                            c_vp, c_vp],
 })
 _RESTYPES = {"pf_last_error": ctypes.c_char_p, "pf_nd_plan_free": None,
              "pf_nd_plan_array": ctypes.c_int64}

@@ -28,6 +28,13 @@ namespace pf {
 namespace {
 
 constexpr int kT = 32;        // panel / identity tile of the factorisation
+
+// Offset of vertex v's row in the output: v * ldp for the whole P, or the
+// row-slab build's table (slab rows first, then the scratch rows of the other
+// fronts the slab depends on).
+__device__ __forceinline__ int64_t row_off(const pf_mf_plan_t &p, int64_t v, int64_t ldp) {
+  return p.rowoff ? p.rowoff[v] : v * ldp;
+}
 constexpr int kThreads = 256;
 
 // ---------------------------------------------------------------- cotan --
@@ -607,13 +614,13 @@ __global__ void __launch_bounds__(kBT + 32, 2)
     const int64_t *ti = p.tile_item + (int64_t)s * p.ntiles;
     // roff[l]: l < c -> Y row l of a 64-wide block; else the P row of X_R[l - c]
     for (int l = tid; l < f; l += nthr)
-      roff[l] = l < c ? (int64_t)l * kGBN : (int64_t)Rv[l - c] * ldp;
+      roff[l] = l < c ? (int64_t)l * kGBN : row_off(p, Rv[l - c], ldp);
     for (int h = tid; h < 2 * ncb; h += nthr) {
       const int64_t tile = 2 * (int64_t)cb0 + h;
       const int64_t it = tile < p.ntiles ? ti[tile] : -1;
       ysrc[h] = it < 0 ? nullptr : O + p.act_voff[it];
     }
-    for (int r = tid; r < NB; r += nthr) coff[r] = i0 + r < c ? (int64_t)Cv[i0 + r] * ldp : -1;
+    for (int r = tid; r < NB; r += nthr) coff[r] = i0 + r < c ? row_off(p, Cv[i0 + r], ldp) : -1;
     if (tid == 0)
       for (int q = 0; q < kGStages; ++q) {
         mbar_init(&full[q], 1);
@@ -730,6 +737,7 @@ constexpr int kResCols = 512;
 __global__ void __launch_bounds__(256)
     residual_kernel(const double *__restrict__ P, int64_t ldp, int64_t k,
                     const int32_t *__restrict__ order, int64_t count,
+                    const int64_t *__restrict__ rowoff,
                     const int64_t *__restrict__ nb_ptr, const int64_t *__restrict__ nrow,
                     const double *__restrict__ off, const double *__restrict__ diag,
                     unsigned long long *out) {
@@ -747,12 +755,13 @@ __global__ void __launch_bounds__(256)
   double mx = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)(blockDim.x / 32) + w; i < count; i += warps) {
     const int64_t v = order[i];
+    const int64_t vo = rowoff ? rowoff[v] : v * ldp;  // this row's offset in P
     const int64_t e0 = nb_ptr[v];
     const int deg = (int)(nb_ptr[v + 1] - e0);
     const double dv = diag[v];
     if (deg > kMaxDeg) {  // exact per-column evaluation for a (rare) high-valence row
       for (int64_t j = j0 + lane; j < j1; j += 32) {
-        double acc = dv * P[v * ldp + j];
+        double acc = dv * P[vo + j];
         for (int64_t e = e0; e < e0 + deg; ++e) {
           const int64_t ro = nrow[e];
           acc += off[e] * (ro >= 0 ? P[ro + j] : (-1 - ro == j ? 1.0 : 0.0));
@@ -767,7 +776,7 @@ __global__ void __launch_bounds__(256)
     const bool inner = lane < deg && me >= 0;
     const unsigned bmask = __ballot_sync(0xffffffffu, lane < deg && me < 0);
     const int nbnd = __popc(bmask);
-    srow[w][lane] = inner ? me : v * ldp;  // all 32 slots: padding reads row v, weight 0
+    srow[w][lane] = inner ? me : vo;  // all 32 slots: padding reads row v, weight 0
     sw[w][lane] = inner ? mw : 0.0;
     if (lane < deg && me < 0) {
       const int slot = __popc(bmask & ((1u << lane) - 1));
@@ -777,7 +786,7 @@ __global__ void __launch_bounds__(256)
     __syncwarp();
     const int ngroups = (deg + kG - 1) / kG;
     for (int64_t j = j0 + 2 * lane; j < j1; j += 64) {
-      const double2 pv = *reinterpret_cast<const double2 *>(P + v * ldp + j);
+      const double2 pv = *reinterpret_cast<const double2 *>(P + vo + j);
       double a0 = dv * pv.x, a1 = dv * pv.y;
       for (int g = 0; g < ngroups; ++g) {
         double2 x[kG];
@@ -809,11 +818,12 @@ __global__ void __launch_bounds__(256)
 __global__ void residual_table_kernel(const int32_t *__restrict__ nb_idx, int64_t nnz,
                                       const uint8_t *__restrict__ isb,
                                       const int32_t *__restrict__ bcol, int64_t ldp,
+                                      const int64_t *__restrict__ rowoff,
                                       int64_t *__restrict__ nrow) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int32_t u = nb_idx[e];
-    nrow[e] = isb[u] ? -1 - (int64_t)bcol[u] : (int64_t)u * ldp;
+    nrow[e] = isb[u] ? -1 - (int64_t)bcol[u] : (rowoff ? rowoff[u] : (int64_t)u * ldp);
   }
 }
 
@@ -823,7 +833,7 @@ __global__ void residual_table_kernel(const int32_t *__restrict__ nb_idx, int64_
 // pf_row_negentropy_f64's exact lane order (pairs per lane, x / y
 // accumulators, odd tail on lane 0), plus min(P) over columns < k — so the
 // first KL field on a freshly built P does not stream it once more for K1.
-__global__ void finalize_kernel(double *P, int64_t ldp, int64_t n, int64_t k,
+__global__ void finalize_kernel(double *P, int64_t ldp, int64_t row0, int64_t n, int64_t k,
                                 const uint8_t *__restrict__ isb, const int32_t *__restrict__ bcol,
                                 double clamp, double *__restrict__ H, double *min_out,
                                 unsigned long long *out) {
@@ -833,10 +843,10 @@ __global__ void finalize_kernel(double *P, int64_t ldp, int64_t n, int64_t k,
   double mx = 0.0, mn = INFINITY;
   for (int64_t v = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32; v < n;
        v += warps) {
-    double *row = P + v * ldp;
-    const bool bnd = isb[v];
+    double *row = P + v * ldp;  // slab-local row v = global row row0 + v
+    const bool bnd = isb[row0 + v];
     if (bnd) {
-      const int32_t b = bcol[v];
+      const int32_t b = bcol[row0 + v];
       for (int64_t j = lane; j < ldp; j += 32) row[j] = (j == b) ? 1.0 : 0.0;
       __syncwarp();
     }
@@ -1009,20 +1019,21 @@ int pf_mf_backward_level(const pf_mf_plan_t *plan, const double *M, const double
 }
 
 int pf_poisson_residual_table(const int32_t *nb_idx, int64_t nnz, const uint8_t *is_boundary,
-                              const int32_t *bcol, int64_t ldp, int64_t *nrow,
-                              pf_stream_t stream) {
+                              const int32_t *bcol, int64_t ldp, const int64_t *rowoff,
+                              int64_t *nrow, pf_stream_t stream) {
   if ((nnz && (!nb_idx || !nrow)) || !is_boundary || !bcol || nnz < 0 || ldp < 1)
     return fail(PF_E_ARG, "pf_poisson_residual_table: bad argument");
   if (nnz == 0) return 0;
   residual_table_kernel<<<grid_for(nnz, 256), 256, 0, as_stream(stream)>>>(
-      nb_idx, nnz, is_boundary, bcol, ldp, nrow);
+      nb_idx, nnz, is_boundary, bcol, ldp, rowoff, nrow);
   return check_launch("pf_poisson_residual_table");
 }
 
 int pf_poisson_residual(const double *P, int64_t ldp, int64_t k, const int32_t *order,
-                        int64_t count, const int64_t *nb_ptr, const int64_t *nrow,
-                        const double *off, const double *diag, unsigned long long *out_max,
-                        pf_stream_t stream) {
+                        int64_t count, const int64_t *rowoff, const int64_t *nb_ptr,
+                        const int64_t *nrow, const double *off, const double *diag,
+                        unsigned long long *out_max, pf_stream_t stream) {
+  if (count == 0) return 0;  // a row slab with no interior rows
   if (!P || !order || !nb_ptr || !nrow || !off || !diag || !out_max || k < 0 || count < 0 ||
       ldp < k || (ldp & 1) || (reinterpret_cast<uintptr_t>(P) & 15))
     return fail(PF_E_ARG, "pf_poisson_residual: bad argument (ldp even, P 16-byte aligned)");
@@ -1030,19 +1041,19 @@ int pf_poisson_residual(const double *P, int64_t ldp, int64_t k, const int32_t *
   const unsigned chunks = (unsigned)((k + kResCols - 1) / kResCols);
   const unsigned rows = (unsigned)std::min<int64_t>((count + 7) / 8, (int64_t)sm_count() * 8);
   residual_kernel<<<dim3(rows, std::max(1u, chunks)), 256, 0, as_stream(stream)>>>(
-      P, ldp, k, order, count, nb_ptr, nrow, off, diag, out_max);
+      P, ldp, k, order, count, rowoff, nb_ptr, nrow, off, diag, out_max);
   return check_launch("pf_poisson_residual");
 }
 
-int pf_poisson_finalize(double *P, int64_t ldp, int64_t n, int64_t k,
+int pf_poisson_finalize(double *P, int64_t ldp, int64_t row0, int64_t n, int64_t k,
                         const uint8_t *is_boundary, const int32_t *bcol, double clamp, double *H,
                         double *min_out, unsigned long long *out_max, pf_stream_t stream) {
   if (!P || !is_boundary || !bcol || !out_max || n < 0 || k < 0 || ldp < k || (ldp & 1) ||
       (reinterpret_cast<uintptr_t>(P) & 15))
     return fail(PF_E_ARG, "pf_poisson_finalize: bad argument");
   if (n == 0) return 0;
-  finalize_kernel<<<grid_for(n, 8), 256, 0, as_stream(stream)>>>(P, ldp, n, k, is_boundary, bcol,
-                                                                  clamp, H, min_out, out_max);
+  finalize_kernel<<<grid_for(n, 8), 256, 0, as_stream(stream)>>>(
+      P, ldp, row0, n, k, is_boundary, bcol, clamp, H, min_out, out_max);
   return check_launch("pf_poisson_finalize");
 }
 

@@ -136,7 +136,8 @@ class PfMfPlan(ctypes.Structure):
     """ctypes mirror of pf_mf_plan_t (include/pathfield_b200.h)."""
     _PTRS = ("c0", "cn", "rn", "fn", "foff", "ch_ptr", "ch_idx", "r_ptr", "r_orig",
              "relmap_off", "relmap", "a_ptr", "a_dst", "a_src", "b_ptr", "b_row", "b_col",
-             "b_src", "act_tile", "act_voff", "tile_item", "perm_orig", "mt_off", "m_off")
+             "b_src", "act_tile", "act_voff", "tile_item", "perm_orig", "mt_off", "m_off",
+             "rowoff")
     _fields_ = [(name, ctypes.c_void_p) for name in _PTRS] + [
         ("nodes", ctypes.c_int64), ("ntiles", ctypes.c_int64), ("k", ctypes.c_int64),
         ("tile", ctypes.c_int32), ("pad_", ctypes.c_int32)]
@@ -193,7 +194,8 @@ class DevicePoisson:
         arrays = {name: getattr(pl, name) for name in PfMfPlan._PTRS if hasattr(pl, name)}
         arrays["mt_off"], arrays["m_off"] = self.mt_off, self.m_off
         self._dev = {name: tod(a, a.dtype) for name, a in arrays.items()}
-        self.struct = PfMfPlan(*[self._dev[name].data_ptr() for name in PfMfPlan._PTRS],
+        self.struct = PfMfPlan(*[self._dev[name].data_ptr() if name in self._dev else None
+                                 for name in PfMfPlan._PTRS],
                                pl.nodes, pl.ntiles, pl.k, pl.tile, 0)
         isb = np.zeros(pl.n, dtype=np.uint8)
         bnd = np.asarray(mesh.boundary_vertices, dtype=np.int64)
@@ -231,11 +233,27 @@ class DevicePoisson:
                              len(node), tod(g_node, np.int32), tod(g_item, np.int64),
                              tod(g_woff, np.int64), tod(g_rb, np.int32), len(g_node)))
         self.w_total = wmax
-        self.bwd = []
+        self._tod, self._c, self._f = tod, c, f
+        self.bwd = self._bwd_lists(None)
+        # host copies for the row-slab build (pf_mf_plan_t.rowoff)
+        self._nb_host = (nb_ptr, nb_idx)
+        self._isb_host = isb
+        self._slabs: dict = {}
+        self._lap = None
+        self._F = None
+        self._bufs = None
+
+    def _bwd_lists(self, need):
+        """Per-level backward launch lists (node, C-row block, column-block
+        range), optionally restricted to the fronts in the boolean mask `need`."""
+        pl, c, f, tod = self.plan, self._c, self._f, self._tod
+        out = []
         nblk = (pl.ntiles + 1) // 2  # 128-column blocks (pairs of plan tiles)
         for lv in pl.levels:
             lv = lv.astype(np.int64)
             lv = lv[c[lv] > 0]
+            if need is not None:
+                lv = lv[need[lv]]
             # C-row block of the level: the smallest of 8/16/32/64 covering most
             # of its separators (the 90th percentile), larger ones in blocks
             cq = int(np.percentile(c[lv], 90)) if len(lv) else 1
@@ -247,16 +265,66 @@ class DevicePoisson:
             cb0 = np.arange(0, nblk, step, dtype=np.int64)
             cb1 = np.minimum(cb0 + step, nblk)
             nodes = np.repeat(lv, rb)
-            rbi = np.arange(blocks) - np.repeat(np.concatenate([[0], np.cumsum(rb)[:-1]]), rb)
+            rbi = np.arange(blocks) - np.repeat(np.cumsum(rb) - rb, rb)
             nn = len(nodes)
-            self.bwd.append((tod(np.repeat(nodes, len(cb0)), np.int32),
-                             tod(np.repeat(rbi, len(cb0)), np.int32),
-                             tod(np.tile(cb0, nn), np.int32), tod(np.tile(cb1, nn), np.int32),
-                             nn * len(cb0), int(f[lv].max()) if len(lv) else 1, int(step),
-                             nbr))
-        self._lap = None
-        self._F = None
-        self._bufs = None
+            out.append((tod(np.repeat(nodes, len(cb0)), np.int32),
+                        tod(np.repeat(rbi, len(cb0)), np.int32),
+                        tod(np.tile(cb0, nn), np.int32), tod(np.tile(cb1, nn), np.int32),
+                        nn * len(cb0), int(f[lv].max()) if len(lv) else 1, int(step), nbr))
+        return out
+
+    def slab_plan(self, row0: int, rows: int) -> dict:
+        """What a rank owning rows [row0, row0 + rows) of P computes (§8e /
+        §8f-1: P row slabs written straight into each GPU's shard): the
+        backward of every front holding a slab row, a row of the slab's 1-ring
+        (the residual reads it) or an ancestor's row (X_R of a descendant);
+        per-vertex output offsets — slab rows first, the other needed rows in
+        scratch rows after them — and the slab's interior rows in
+        nested-dissection order (the residual's walk)."""
+        key = (int(row0), int(rows))
+        hit = self._slabs.get(key)
+        if hit is not None:
+            return hit
+        pl, tod = self.plan, self._tod
+        n, ld = self.n, round_up_cols(self.k)
+        isb = self._isb_host.astype(bool)
+        nb_ptr, nb_idx = self._nb_host
+        pos_of = -np.ones(n, dtype=np.int64)
+        pos_of[pl.perm_orig] = np.arange(pl.m)
+        node_of_pos = np.repeat(np.arange(pl.nodes), pl.cn)
+        slab = np.arange(row0, row0 + rows)
+        slab_int = slab[~isb[slab]]
+        lo, hi = nb_ptr[slab_int], nb_ptr[slab_int + 1]
+        ring = nb_idx[np.repeat(lo, hi - lo) + (np.arange((hi - lo).sum())
+                                               - np.repeat(np.cumsum(hi - lo) - (hi - lo), hi - lo))]
+        verts = np.unique(np.concatenate([slab_int, ring]))
+        verts = verts[~isb[verts]]
+        need = np.zeros(pl.nodes, dtype=bool)
+        cur = np.unique(node_of_pos[pos_of[verts]])
+        while cur.size:
+            cur = cur[~need[cur]]
+            need[cur] = True
+            cur = np.unique(pl.parent[cur])
+            cur = cur[cur >= 0]
+        # rows of every needed front: slab rows at their slab offset, the rest in scratch
+        need_pos = np.flatnonzero(need[node_of_pos])
+        need_v = pl.perm_orig[need_pos].astype(np.int64)
+        rowoff = np.full(n, -1, dtype=np.int64)
+        in_slab = (need_v >= row0) & (need_v < row0 + rows)
+        rowoff[need_v[in_slab]] = (need_v[in_slab] - row0) * ld
+        extra = need_v[~in_slab]
+        rowoff[extra] = (rows + np.arange(extra.size)) * ld
+        in_slab_pos = (pl.perm_orig >= row0) & (pl.perm_orig < row0 + rows)
+        hit = {"need": need, "rowoff": tod(rowoff, np.int64), "scratch_rows": int(extra.size),
+               "order": tod(pl.perm_orig[in_slab_pos], np.int32),
+               "count": int(in_slab_pos.sum()), "bwd": self._bwd_lists(need),
+               "fronts": int(need.sum())}
+        st = PfMfPlan()
+        ctypes.pointer(st)[0] = self.struct
+        st.rowoff = hit["rowoff"].data_ptr()
+        hit["struct"] = st
+        self._slabs[key] = hit
+        return hit
 
     # -- laplacian.py:91-134 ---------------------------------------------
     def laplacian(self):
@@ -316,11 +384,14 @@ class DevicePoisson:
         return self._F
 
     # -- solvers.py:278-303 ------------------------------------------------
-    def solve(self, P_out=None, events: dict | None = None):
+    def solve(self, P_out=None, events: dict | None = None, slab=None):
         """P (device, n x round_up(k, 64) FP64, pads zero) with the reference's
         diagnostics.  Returns (P, residual, row_sum_error).  `events`, if given,
         receives CUDA events bracketing the forward / backward / diagnostics
-        phases on the launch stream."""
+        phases on the launch stream.  `slab = (row0, rows)` builds only rows
+        [row0, row0 + rows) (the rank's shard; bitwise the same rows as the
+        whole build): the returned P is (rows, ld) and the diagnostics cover
+        the slab (the max over ranks is the whole P's)."""
         from . import _device as dev
         t = dev.torch()
         mark = (lambda name: events.setdefault(name, t.cuda.Event(enable_timing=True)).record(
@@ -328,58 +399,75 @@ class DevicePoisson:
         off, diag = self.laplacian()
         Mt, M = self.factor()
         ld = round_up_cols(self.k)
-        P = P_out if P_out is not None else t.empty((self.n, ld), dtype=t.float64,
-                                                    device=self.device)
-        if P.stride(0) != ld:
-            raise ValueError("P_out must be (n, round_up(k, 64)) row-major")
+        if slab is None:
+            row0, rows, extra = 0, self.n, 0
+            st, bwd, rowoff = self.struct, self.bwd, None
+            order, count = self._dev["perm_orig"], self.plan.m
+        else:
+            row0, rows = int(slab[0]), int(slab[1])
+            sp = self.slab_plan(row0, rows)
+            st, bwd, rowoff = sp["struct"], sp["bwd"], sp["rowoff"]
+            order, count, extra = sp["order"], sp["count"], sp["scratch_rows"]
+        want = rows + extra
+        if P_out is not None and (P_out.stride(0) != ld or P_out.shape[0] < want):
+            raise ValueError(f"P_out must be ({want}, {ld}) row-major")
+        Pbuf = P_out if P_out is not None else t.empty((want, ld), dtype=t.float64,
+                                                       device=self.device)
         O = t.empty(max(self.plan.stats["v_total"], 1), dtype=t.float64, device=self.device)
         Wb = t.empty(self.w_total, dtype=t.float64, device=self.device)
         s = self.stream()
-        ps = ctypes.addressof(self.struct)
+        ps = ctypes.addressof(st)
         mark("fwd0")
         for (an, ai, aw, acnt, gn, gi, gw, grb, gcnt) in self.fwd:
             nat.call("pf_mf_forward_level", ps, Mt.data_ptr(), off.data_ptr(), an.data_ptr(),
                      ai.data_ptr(), aw.data_ptr(), acnt, gn.data_ptr(), gi.data_ptr(),
                      gw.data_ptr(), grb.data_ptr(), gcnt, Wb.data_ptr(), O.data_ptr(), s)
         mark("bwd0")
-        for nodes, rb, cb0, cb1, cnt, maxf, ncb, nbr in reversed(self.bwd):
+        for nodes, rb, cb0, cb1, cnt, maxf, ncb, nbr in reversed(bwd):
+            if cnt == 0:  # a slab build may need no front of a level
+                continue
             nat.call("pf_mf_backward_level", ps, M.data_ptr(), O.data_ptr(), nodes.data_ptr(),
                      rb.data_ptr(), cb0.data_ptr(), cb1.data_ptr(), cnt, maxf, ncb, nbr,
-                     P.data_ptr(), ld, s)
+                     Pbuf.data_ptr(), ld, s)
         mark("bwd1")
         mx = t.zeros(2, dtype=t.int64, device=self.device)
         dm = self.dm
-        nrow = self._residual_table(ld)
-        nat.call("pf_poisson_residual", P.data_ptr(), ld, self.k,
-                 self._dev["perm_orig"].data_ptr(), self.plan.m, dm.nb_ptr.data_ptr(),
-                 nrow.data_ptr(), off.data_ptr(), diag.data_ptr(), mx.data_ptr(), s)
+        nrow = self._residual_table(ld, rowoff)
+        nat.call("pf_poisson_residual", Pbuf.data_ptr(), ld, self.k, order.data_ptr(), count,
+                 nat.ptr(rowoff), dm.nb_ptr.data_ptr(), nrow.data_ptr(), off.data_ptr(),
+                 diag.data_ptr(), mx.data_ptr(), s)
         # fused K1: the KL negentropy per row (clamp 1e-300) and min(P), so the
         # first field on this P does not stream it again
-        H = t.empty(self.n, dtype=t.float64, device=self.device)
+        H = t.empty(rows, dtype=t.float64, device=self.device)
         mn = t.full((1,), float("inf"), dtype=t.float64, device=self.device)
-        nat.call("pf_poisson_finalize", P.data_ptr(), ld, self.n, self.k,
+        nat.call("pf_poisson_finalize", Pbuf.data_ptr(), ld, row0, rows, self.k,
                  self.is_boundary.data_ptr(), self.bcol.data_ptr(), KL_CLAMP, H.data_ptr(),
                  mn.data_ptr(), mx.data_ptr() + 8, s)
         self.last_H, self.last_min = H, mn
         mark("end")
         del O, Wb
         r = mx.cpu().numpy().astype(np.uint64)
-        residual = _u64_to_f64(int(r[0])) if self.plan.m else 0.0
-        return P, residual, _u64_to_f64(int(r[1]))
+        residual = _u64_to_f64(int(r[0])) if count else 0.0
+        return Pbuf[:rows], residual, _u64_to_f64(int(r[1]))
 
-    def _residual_table(self, ld: int):
-        """Per neighbour entry: the P offset of an interior neighbour's row or
-        -1 - the boundary column (pf_poisson_residual_table), cached per ld."""
-        hit = getattr(self, "_rtab", None)
-        if hit is None or hit[0] != ld:
+    def _residual_table(self, ld: int, rowoff=None):
+        """Per neighbour entry: the output offset of an interior neighbour's row
+        or -1 - the boundary column (pf_poisson_residual_table), cached per
+        (ld, row-offset table)."""
+        key = (ld, None if rowoff is None else rowoff.data_ptr())
+        tabs = getattr(self, "_rtabs", None)
+        if tabs is None:
+            tabs = self._rtabs = {}
+        hit = tabs.get(key)
+        if hit is None:
             from . import _device as dev
             t = dev.torch()
-            nrow = t.empty(max(self._nnz, 1), dtype=t.int64, device=self.device)
+            hit = t.empty(max(self._nnz, 1), dtype=t.int64, device=self.device)
             nat.call("pf_poisson_residual_table", self.dm.nb_idx.data_ptr(), self._nnz,
-                     self.is_boundary.data_ptr(), self.bcol.data_ptr(), ld, nrow.data_ptr(),
-                     self.stream())
-            hit = self._rtab = (ld, nrow)
-        return hit[1]
+                     self.is_boundary.data_ptr(), self.bcol.data_ptr(), ld, nat.ptr(rowoff),
+                     hit.data_ptr(), self.stream())
+            tabs[key] = hit
+        return hit
 
     def solve_flops(self) -> dict:
         """Algorithmic FP64 work of the solves (SURVEY §8d convention): the
@@ -408,11 +496,14 @@ class DevicePoisson:
                 "forward": float((per_col * act).sum() * TILE),
                 "backward_issued": issued}
 
-    def device_kernel(self, P=None):
-        """Solve and wrap P as a DeviceKernel (the hot path's input)."""
+    def device_kernel(self, P=None, slab=None):
+        """Solve and wrap P (or the row slab (row0, rows)) as a DeviceKernel
+        (the hot path's input; a slab is a parallel.ShardedField shard)."""
         from . import _device as dev
-        P, residual, rse = self.solve(P)
-        dk = dev.DeviceKernel(None, self.boundary, n=self.n, k=self.k, P_dev=P)
+        P, residual, rse = self.solve(P, slab=slab)
+        row0 = 0 if slab is None else int(slab[0])
+        dk = dev.DeviceKernel(None, self.boundary, n=self.n, k=self.k, P_dev=P, row0=row0,
+                              rows=P.shape[0])
         dk.residual, dk.row_sum_error = residual, rse
         dk._H[KL_CLAMP] = self.last_H     # K1, fused into the build's finalize pass
         dk._min = self.last_min

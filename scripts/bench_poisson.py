@@ -40,6 +40,8 @@ def main():
     ap.add_argument("--leaf", type=int, default=None)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--workers", type=int, default=os.cpu_count() or 8)
+    ap.add_argument("--slabs", type=int, default=0,
+                    help="also time the row-slab builds of N ranks (one after another)")
     args = ap.parse_args()
     import torch
     from oracle import inputs as I
@@ -81,6 +83,29 @@ def main():
     out["P_bytes"] = n * k * 8
     out["write_gbs"] = n * k * 8 / (np.median([r["solve_ms"] for r in reps]) * 1e-3) / 1e9
     print(json.dumps(out), flush=True)
+    if args.slabs:
+        from paper_1708_02845_b200.parallel import partition_rows
+        sl = []
+        for a, b in partition_rows(dp.n, args.slabs):
+            dp.slab_plan(a, b - a)  # host plan outside the timing
+            times = []
+            for rep in range(3):
+                ev0, ev1 = ev(), ev()
+                torch.cuda.synchronize()
+                ev0.record()
+                Ps, r_, s_ = dp.solve(slab=(a, b - a))
+                ev1.record()
+                torch.cuda.synchronize()
+                times.append(ev0.elapsed_time(ev1))
+                del Ps
+            spl = dp.slab_plan(a, b - a)
+            sl.append({"rows": [a, b], "solve_ms": float(np.median(times)),
+                       "fronts": spl["fronts"], "scratch_rows": spl["scratch_rows"]})
+        fac = float(np.median([r["factor_ms"] + r["laplacian_ms"] for r in reps]))
+        print(json.dumps({"slabs": args.slabs, "factor_ms_replicated": fac,
+                          "max_slab_solve_ms": max(x["solve_ms"] for x in sl),
+                          "per_rank_total_ms": fac + max(x["solve_ms"] for x in sl),
+                          "per_slab": sl}), flush=True)
     if args.validate:
         t0 = time.perf_counter()
         ref, bnd = I.poisson_kernel_parallel(mesh, workers=args.workers)

@@ -198,3 +198,33 @@ def test_fused_negentropy_bitwise_k1(name):
              H.data_ptr(), mn.data_ptr(), t.cuda.current_stream().cuda_stream)
     assert bool((H.view(t.int64) == fused.view(t.int64)).all())
     assert float(mn.item()) == fused_min
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["c1", "corridor50", "holes_fine"])
+@pytest.mark.parametrize("parts", [3, 8])
+def test_row_slab_builds_bitwise(name, parts):
+    """§8e / §8f-1: each rank builds only its row slab of P (the backward of the
+    fronts its rows, their 1-ring and their ancestors need): the slabs are
+    bitwise the rows of the whole build, and the per-slab diagnostics' max is
+    the whole build's."""
+    from paper_1708_02845_b200.laplacian import KL_CLAMP, DevicePoisson
+    c = case(name)
+    dp = DevicePoisson(c.mesh)
+    full, res, rse = dp.solve()
+    full = full.cpu().numpy()
+    H_full = dp.last_H.cpu().numpy()
+    bounds = np.linspace(0, dp.n, parts + 1).astype(int)
+    res_max = rse_max = 0.0
+    fronts = []
+    for a, b in zip(bounds[:-1], bounds[1:]):
+        dk = dp.device_kernel(slab=(int(a), int(b - a)))
+        P = dk.P.cpu().numpy()
+        assert dk.row0 == a and dk.rows == b - a
+        assert np.array_equal(P.view(np.int64), full[a:b].view(np.int64))
+        assert np.array_equal(dk._H[KL_CLAMP].cpu().numpy().view(np.int64),
+                              H_full[a:b].view(np.int64))
+        res_max, rse_max = max(res_max, dk.residual), max(rse_max, dk.row_sum_error)
+        fronts.append(dp.slab_plan(int(a), int(b - a))["fronts"])
+    assert res_max == res and rse_max == rse
+    assert min(fronts) < dp.plan.nodes  # some rank skips part of the backward
