@@ -228,3 +228,32 @@ def test_row_slab_builds_bitwise(name, parts):
         fronts.append(dp.slab_plan(int(a), int(b - a))["fronts"])
     assert res_max == res and rse_max == rse
     assert min(fronts) < dp.plan.nodes  # some rank skips part of the backward
+
+
+@pytest.mark.gpu
+def test_sharded_field_from_mesh_world1():
+    """ShardedField.from_mesh over a 1-rank NCCL group: the whole P, bitwise the
+    single-GPU build, and a field through the sharded API equal to dv_field."""
+    import os
+    import torch.distributed as dist
+    import paper_1708_02845_b200 as pf
+    from paper_1708_02845_b200.laplacian import DevicePoisson
+    from paper_1708_02845_b200.parallel import ShardedField
+    c = case("holes_fine")
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29517")
+    own = not dist.is_initialized()
+    if own:
+        dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        sf = ShardedField.from_mesh(c.mesh, dist)
+        full, res, rse = DevicePoisson(c.mesh).solve()
+        assert bool((sf.slab.P == full).all())
+        assert sf.slab.residual == res and sf.slab.row_sum_error == rse
+        t0 = int(c.targets[0])
+        got = sf.field(pf.builtin_f("kl"), t0).cpu().numpy()
+        ok, err = rel_close(got, c["field/kl/0"], 1e-10)
+        assert ok, err
+    finally:
+        if own:
+            dist.destroy_process_group()
