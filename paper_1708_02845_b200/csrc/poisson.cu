@@ -959,8 +959,9 @@ int pf_mf_factor_level(const pf_mf_plan_t *plan, const double *off, const double
 int pf_mf_inverse(const pf_mf_plan_t *plan, const double *F, const int32_t *item_node,
                   const int32_t *item_ct, int64_t count, const int32_t *nodes, int64_t nnodes,
                   double *Mt, double *M, pf_stream_t stream) {
-  if (!plan || !F || !item_node || !item_ct || !nodes || !Mt || !M || count < 0 || nnodes < 0 ||
-      plan->tile != kGBN)
+  if (count == 0 && nnodes == 0) return 0;  // no interior vertices: nothing to invert
+  if (!plan || !F || (count && (!item_node || !item_ct)) || (nnodes && !nodes) || !Mt || !M ||
+      count < 0 || nnodes < 0 || plan->tile != kGBN)
     return fail(PF_E_ARG, "pf_mf_inverse: bad argument");
   cudaStream_t st = as_stream(stream);
   if (count > 0)

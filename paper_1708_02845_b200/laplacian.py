@@ -152,7 +152,7 @@ def _ranges(ptr, nodes):
     lo, hi = ptr[nodes], ptr[nodes + 1]
     cnt = hi - lo
     owner = np.repeat(nodes, cnt)
-    idx = np.repeat(lo - np.concatenate([[0], np.cumsum(cnt)[:-1]]), cnt) + np.arange(cnt.sum())
+    idx = np.repeat(lo - (np.cumsum(cnt) - cnt), cnt) + np.arange(cnt.sum())
     return owner, idx
 
 
@@ -173,7 +173,7 @@ class DevicePoisson:
         self.device = (t.device(device) if device is not None
                        else t.device("cuda", t.cuda.current_device()))
         nb_ptr, nb_idx, isb_h = mesh_topology(mesh)
-        tod = lambda a, dt: t.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(self.device)  # noqa: E731
+        tod = lambda a, dt: t.from_numpy(np.array(a, dtype=dt)).to(self.device)  # noqa: E731
         # device mesh arrays of the assembly (any TriMesh-like object: vertices,
         # triangles as stored, boundary_vertices)
         self.dm = type("DevMesh", (), {})()
@@ -214,7 +214,7 @@ class DevicePoisson:
         all_nodes = np.arange(pl.nodes, dtype=np.int64)
         ct = (c + 31) // 32
         inv_node = np.repeat(all_nodes, ct)
-        inv_ct = np.arange(ct.sum()) - np.repeat(np.concatenate([[0], np.cumsum(ct)[:-1]]), ct)
+        inv_ct = np.arange(ct.sum()) - np.repeat(np.cumsum(ct) - ct, ct)
         self.inv = (tod(inv_node, np.int32), tod(inv_ct, np.int32), len(inv_node),
                     tod(all_nodes, np.int32))
         self.fwd, wmax = [], 1
@@ -222,13 +222,13 @@ class DevicePoisson:
             lv = lv.astype(np.int64)
             node, item = _ranges(pl.act_ptr, lv)
             fi = f[node]
-            woff = np.concatenate([[0], np.cumsum(fi * TILE)[:-1]]).astype(np.int64)
+            woff = (np.cumsum(fi * TILE) - fi * TILE).astype(np.int64)
             wmax = max(wmax, int((fi * TILE).sum()))
             rb = (fi + 31) // 32
             g_node = np.repeat(node, rb)
             g_item = np.repeat(item, rb)
             g_woff = np.repeat(woff, rb)
-            g_rb = np.arange(rb.sum()) - np.repeat(np.concatenate([[0], np.cumsum(rb)[:-1]]), rb)
+            g_rb = np.arange(rb.sum()) - np.repeat(np.cumsum(rb) - rb, rb)
             self.fwd.append((tod(node, np.int32), tod(item, np.int64), tod(woff, np.int64),
                              len(node), tod(g_node, np.int32), tod(g_item, np.int64),
                              tod(g_woff, np.int64), tod(g_rb, np.int32), len(g_node)))

@@ -257,3 +257,40 @@ def test_sharded_field_from_mesh_world1():
     finally:
         if own:
             dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_no_interior_vertices_gives_indicator_rows():
+    """solvers.py:287-291: with an empty interior the reference skips the solve and
+    P is the boundary indicator matrix, residual 0."""
+    import paper_1708_02845_b200 as pf
+    import paper_1708_02845_b200.laplacian as L
+    V = np.array([[0.0, 0.0], [1.0, 0.0], [1.0, 1.0], [0.0, 1.0]])
+    T = np.array([[0, 1, 2], [0, 2, 3]])
+    mesh = pf.TriMesh(V, T)
+    assert mesh.m == 0
+    pk = L.poisson_kernel(mesh)
+    np.testing.assert_array_equal(pk.dense, np.eye(4))
+    assert pk.residual == 0.0 and pk.row_sum_error == 0.0
+
+
+@pytest.mark.gpu
+def test_degenerate_triangle_raises():
+    """laplacian.py:110-113: a 0/pi angle (zero cross product) raises
+    DegenerateGeometryError, as the reference does."""
+    from paper_1708_02845_b200.errors import DegenerateGeometryError
+    from paper_1708_02845_b200.laplacian import DevicePoisson
+    c = case("disk8")
+    V = np.array(c.mesh.vertices, dtype=np.float64)
+    T = np.array(c.mesh.triangles)
+    # collapse one triangle's vertex onto the midpoint of its opposite edge
+    a, b, cc = T[0]
+    V2 = V.copy()
+    V2[cc] = 0.5 * (V[a] + V[b])
+
+    class M:
+        vertices, triangles = V2, T
+        boundary_vertices = c.mesh.boundary_vertices
+        interior_vertices = c.mesh.interior_vertices
+    with pytest.raises(DegenerateGeometryError):
+        DevicePoisson(M()).laplacian()
