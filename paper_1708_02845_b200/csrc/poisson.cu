@@ -861,10 +861,12 @@ __global__ void finalize_kernel(double *P, int64_t ldp, int64_t row0, int64_t n,
       }
       s0 += x.x;
       s1 += x.y;
-      mn = fmin(mn, fmin(x.x, x.y));
-      const double q0 = fmax(x.x, clamp), q1 = fmax(x.y, clamp);
-      a0 += __dmul_rn(q0, log(q0));
-      a1 += __dmul_rn(q1, log(q1));
+      if (H) {  // fused K1 (FP64 log per entry: only when the caller wants H)
+        mn = fmin(mn, fmin(x.x, x.y));
+        const double q0 = fmax(x.x, clamp), q1 = fmax(x.y, clamp);
+        a0 += __dmul_rn(q0, log(q0));
+        a1 += __dmul_rn(q1, log(q1));
+      }
     }
     if ((k & 1) && lane == 0) {
       double x = row[k - 1];
@@ -873,19 +875,23 @@ __global__ void finalize_kernel(double *P, int64_t ldp, int64_t row0, int64_t n,
         row[k - 1] = 0.0;
       }
       s0 += x;
-      mn = fmin(mn, x);
-      const double q = fmax(x, clamp);
-      a0 += __dmul_rn(q, log(q));
+      if (H) {
+        mn = fmin(mn, x);
+        const double q = fmax(x, clamp);
+        a0 += __dmul_rn(q, log(q));
+      }
     }
     if (!bnd)
       for (int64_t j = k + lane; j < ldp; j += 32) row[j] = 0.0;
-    const double h = warp_sum(a0 + a1);
-    if (H && lane == 0) H[v] = h;
+    if (H) {
+      const double h = warp_sum(a0 + a1);
+      if (lane == 0) H[v] = h;
+    }
     const double sum = warp_sum(s0 + s1);
     if (!bnd) mx = fmax(mx, fabs(sum - 1.0));  // boundary rows sum to exactly 1
   }
   if (lane == 0) atomic_max_nonneg(out, mx);
-  if (min_out) {
+  if (H && min_out) {
     mn = warp_min(mn);
     if (lane == 0 && mn < INFINITY) {  // ordered-integer atomic min (values may be < 0)
       unsigned long long *addr = reinterpret_cast<unsigned long long *>(min_out);

@@ -215,8 +215,14 @@ class DevicePoisson:
         ct = (c + 31) // 32
         inv_node = np.repeat(all_nodes, ct)
         inv_ct = np.arange(ct.sum()) - np.repeat(np.cumsum(ct) - ct, ct)
+        # longest items first (an item sweeps rows 32*ct .. f of its front): the
+        # top separators' CTAs would otherwise start last and form the tail
+        work = (f[inv_node] - 32 * inv_ct) * (c[inv_node] - 32 * inv_ct)
+        o = np.argsort(-work, kind="stable")
+        inv_node, inv_ct = inv_node[o], inv_ct[o]
+        big_first = all_nodes[np.argsort(-(c * f), kind="stable")]
         self.inv = (tod(inv_node, np.int32), tod(inv_ct, np.int32), len(inv_node),
-                    tod(all_nodes, np.int32))
+                    tod(big_first, np.int32))
         self.fwd, wmax = [], 1
         for lv in pl.levels:
             lv = lv.astype(np.int64)
@@ -384,14 +390,17 @@ class DevicePoisson:
         return self._F
 
     # -- solvers.py:278-303 ------------------------------------------------
-    def solve(self, P_out=None, events: dict | None = None, slab=None):
+    def solve(self, P_out=None, events: dict | None = None, slab=None, fuse_h: bool = False):
         """P (device, n x round_up(k, 64) FP64, pads zero) with the reference's
         diagnostics.  Returns (P, residual, row_sum_error).  `events`, if given,
         receives CUDA events bracketing the forward / backward / diagnostics
         phases on the launch stream.  `slab = (row0, rows)` builds only rows
         [row0, row0 + rows) (the rank's shard; bitwise the same rows as the
         whole build): the returned P is (rows, ld) and the diagnostics cover
-        the slab (the max over ranks is the whole P's)."""
+        the slab (the max over ranks is the whole P's).  `fuse_h` also
+        computes the KL negentropy H and min P in the finalize pass (K1: one
+        FP64 log per entry, worth it only when a KL field follows —
+        device_kernel() sets it)."""
         from . import _device as dev
         t = dev.torch()
         mark = (lambda name: events.setdefault(name, t.cuda.Event(enable_timing=True)).record(
@@ -438,11 +447,11 @@ class DevicePoisson:
                  diag.data_ptr(), mx.data_ptr(), s)
         # fused K1: the KL negentropy per row (clamp 1e-300) and min(P), so the
         # first field on this P does not stream it again
-        H = t.empty(rows, dtype=t.float64, device=self.device)
-        mn = t.full((1,), float("inf"), dtype=t.float64, device=self.device)
+        H = t.empty(rows, dtype=t.float64, device=self.device) if fuse_h else None
+        mn = t.full((1,), float("inf"), dtype=t.float64, device=self.device) if fuse_h else None
         nat.call("pf_poisson_finalize", Pbuf.data_ptr(), ld, row0, rows, self.k,
-                 self.is_boundary.data_ptr(), self.bcol.data_ptr(), KL_CLAMP, H.data_ptr(),
-                 mn.data_ptr(), mx.data_ptr() + 8, s)
+                 self.is_boundary.data_ptr(), self.bcol.data_ptr(), KL_CLAMP, nat.ptr(H),
+                 nat.ptr(mn), mx.data_ptr() + 8, s)
         self.last_H, self.last_min = H, mn
         mark("end")
         del O, Wb
@@ -500,7 +509,7 @@ class DevicePoisson:
         """Solve and wrap P (or the row slab (row0, rows)) as a DeviceKernel
         (the hot path's input; a slab is a parallel.ShardedField shard)."""
         from . import _device as dev
-        P, residual, rse = self.solve(P, slab=slab)
+        P, residual, rse = self.solve(P, slab=slab, fuse_h=True)
         row0 = 0 if slab is None else int(slab[0])
         dk = dev.DeviceKernel(None, self.boundary, n=self.n, k=self.k, P_dev=P, row0=row0,
                               rows=P.shape[0])

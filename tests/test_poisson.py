@@ -211,7 +211,7 @@ def test_row_slab_builds_bitwise(name, parts):
     from paper_1708_02845_b200.laplacian import KL_CLAMP, DevicePoisson
     c = case(name)
     dp = DevicePoisson(c.mesh)
-    full, res, rse = dp.solve()
+    full, res, rse = dp.solve(fuse_h=True)
     full = full.cpu().numpy()
     H_full = dp.last_H.cpu().numpy()
     bounds = np.linspace(0, dp.n, parts + 1).astype(int)
