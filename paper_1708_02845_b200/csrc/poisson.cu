@@ -734,7 +734,8 @@ __device__ __forceinline__ void atomic_max_nonneg(unsigned long long *p, double 
 // 512-column chunks; columns go in 16-byte pairs.
 constexpr int kResCols = 512;
 
-__global__ void __launch_bounds__(256)
+template <int WARPS>
+__global__ void __launch_bounds__(WARPS * 32)
     residual_kernel(const double *__restrict__ P, int64_t ldp, int64_t k,
                     const int32_t *__restrict__ order, int64_t count,
                     const int64_t *__restrict__ rowoff,
@@ -745,10 +746,10 @@ __global__ void __launch_bounds__(256)
   // before the FMAs; missing slots point at row v with weight 0); boundary
   // neighbours add their weight to one column each, in a separate short list.
   constexpr int kG = 8, kMaxDeg = 32;
-  __shared__ int64_t srow[8][kMaxDeg];
-  __shared__ double sw[8][kMaxDeg];
-  __shared__ int64_t bcl[8][kMaxDeg];
-  __shared__ double bw[8][kMaxDeg];
+  __shared__ int64_t srow[WARPS][kMaxDeg];
+  __shared__ double sw[WARPS][kMaxDeg];
+  __shared__ int64_t bcl[WARPS][kMaxDeg];
+  __shared__ double bw[WARPS][kMaxDeg];
   const int lane = threadIdx.x % 32, w = threadIdx.x / 32;
   const int64_t j0 = (int64_t)blockIdx.y * kResCols, j1 = min(k, j0 + kResCols);
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
@@ -1045,9 +1046,12 @@ int pf_poisson_residual(const double *P, int64_t ldp, int64_t k, const int32_t *
       ldp < k || (ldp & 1) || (reinterpret_cast<uintptr_t>(P) & 15))
     return fail(PF_E_ARG, "pf_poisson_residual: bad argument (ldp even, P 16-byte aligned)");
   if (count == 0) return 0;
+  // (32-warp CTAs over consecutive nested-dissection rows measured slower: 19.1
+  // vs 17.7 ms at C4 — the kernel is bound by L2 traffic, ~9 reads per entry)
+  constexpr int kW = 8;
   const unsigned chunks = (unsigned)((k + kResCols - 1) / kResCols);
-  const unsigned rows = (unsigned)std::min<int64_t>((count + 7) / 8, (int64_t)sm_count() * 8);
-  residual_kernel<<<dim3(rows, std::max(1u, chunks)), 256, 0, as_stream(stream)>>>(
+  const unsigned rows = (unsigned)std::min<int64_t>((count + kW - 1) / kW, (int64_t)sm_count() * 8);
+  residual_kernel<kW><<<dim3(rows, std::max(1u, chunks)), kW * 32, 0, as_stream(stream)>>>(
       P, ldp, k, order, count, rowoff, nb_ptr, nrow, off, diag, out_max);
   return check_launch("pf_poisson_residual");
 }
