@@ -99,6 +99,13 @@ __global__ void laplacian_diag_kernel(const int64_t *__restrict__ nb_ptr,
   }
 }
 
+// FP64 tensor-core MMA (SASS DMMA): D(8x8) += A(8x4, row) B(4x8, col).
+__device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
 // ------------------------------------------------------- factorisation --
 // Building blocks shared by the one-CTA-per-front kernel (many small fronts)
 // and the split kernels (few large fronts: every step spread over CTAs).
@@ -198,10 +205,14 @@ __device__ __forceinline__ void panel_trsm_rows(double *Fs, int f, int p0, int p
 }
 
 // Trailing-update tile (ti, tl), tl <= ti, of 64 x 64 at q0 = p0 + pb:
-// F[i][l] -= sum_j L[i][p0+j] L[l][p0+j] (lower triangle only).
+// F[i][l] -= sum_j L[i][p0+j] L[l][p0+j] (lower triangle only), on the FP64
+// tensor pipe: 8 warps as 4 (i) x 2 (l), 16 x 32 warp tiles of m8n8k4 DMMAs
+// over the (<= 32)-deep panel; A = the tile's panel rows, B = the other
+// tile's panel rows transposed.  Row stride kSY = 36 (4 mod 16): conflict-free
+// half-warp fragment loads.
+constexpr int kSY = kT + 4;
 __device__ __forceinline__ void panel_syrk_tile(double *Fs, int f, int p0, int pb, int ti,
-                                                int tl, double (*Ai)[kT + 1],
-                                                double (*Al)[kT + 1]) {
+                                                int tl, double (*Ai)[kSY], double (*Al)[kSY]) {
   const int tid = threadIdx.x;
   const int q0 = p0 + pb;
   const int gi0 = q0 + ti * 64, gl0 = q0 + tl * 64;
@@ -211,29 +222,31 @@ __device__ __forceinline__ void panel_syrk_tile(double *Fs, int f, int p0, int p
     Al[r][j] = (gl0 + r < f && j < pb) ? Fs[(int64_t)(gl0 + r) * f + p0 + j] : 0.0;
   }
   __syncthreads();
-  const int ri = tid / 16, ci = tid % 16;
-  double acc[4][4] = {};
-  for (int j = 0; j < pb; ++j) {
-    double a[4], b[4];
+  const int lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1, fr = lane >> 2, fc = lane & 3;
+  double acc[2][4][2] = {};
+  for (int ks = 0; ks < pb; ks += 4) {
+    double a[2], b[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      a[u] = Ai[ri + 16 * u][j];
-      b[u] = Al[ci + 16 * u][j];
-    }
+    for (int u = 0; u < 2; ++u) a[u] = Ai[wm * 16 + 8 * u + fr][ks + fc];
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int w = 0; w < 4; ++w) b[w] = Al[wn * 32 + 8 * w + fr][ks + fc];
 #pragma unroll
-      for (int w = 0; w < 4; ++w) acc[u][w] += a[u] * b[w];
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int w = 0; w < 4; ++w) dmma884(acc[u][w][0], acc[u][w][1], a[u], b[w]);
   }
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int gi = gi0 + ri + 16 * u;
+  for (int u = 0; u < 2; ++u) {
+    const int gi = gi0 + wm * 16 + 8 * u + fr;
     if (gi >= f) continue;
 #pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const int gl = gl0 + ci + 16 * w;
-      if (gl <= gi) Fs[(int64_t)gi * f + gl] -= acc[u][w];
-    }
+    for (int w = 0; w < 4; ++w)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int gl = gl0 + wn * 32 + 8 * w + 2 * fc + q;
+        if (gl <= gi) Fs[(int64_t)gi * f + gl] -= acc[u][w][q];
+      }
   }
   __syncthreads();
 }
@@ -247,13 +260,13 @@ __device__ __forceinline__ void tri_pair(int pr, int &ti, int &tl) {
 }
 
 // One CTA per front of the level (many small fronts).
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, 4)
     mf_factor_kernel(pf_mf_plan_t p, const double *__restrict__ off,
                      const double *__restrict__ diag, const int32_t *__restrict__ nodes,
                      double *F, int32_t *err) {
   __shared__ double D[kT][kT + 1];
-  __shared__ double Ai[64][kT + 1];
-  __shared__ double Al[64][kT + 1];
+  __shared__ double Ai[64][kSY];
+  __shared__ double Al[64][kSY];
   const int s = nodes[blockIdx.x];
   const int f = p.fn[s], c = p.cn[s];
   double *Fs = F + p.foff[s];
@@ -285,7 +298,7 @@ __global__ void __launch_bounds__(kThreads)
   front_assemble_rows(p, s, off, diag, F, r0, r1);
 }
 
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, 4)
     mf_panel_trsm_kernel(pf_mf_plan_t p, const int32_t *__restrict__ nodes, int p0, double *F,
                          int32_t *err) {
   __shared__ double D[kT][kT + 1];
@@ -303,8 +316,8 @@ __global__ void __launch_bounds__(kThreads, 2)
 
 __global__ void __launch_bounds__(kThreads)
     mf_panel_syrk_kernel(pf_mf_plan_t p, const int32_t *__restrict__ nodes, int p0, double *F) {
-  __shared__ double Ai[64][kT + 1];
-  __shared__ double Al[64][kT + 1];
+  __shared__ double Ai[64][kSY];
+  __shared__ double Al[64][kSY];
   const int s = nodes[blockIdx.x];
   const int c = p.cn[s], f = p.fn[s];
   if (p0 >= c) return;
@@ -415,11 +428,6 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-__device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-               : "+d"(d0), "+d"(d1)
-               : "d"(a), "d"(b));
 }
 
 // ncb column blocks x K; arow(i) / brow(cb, l) return row pointers (or
