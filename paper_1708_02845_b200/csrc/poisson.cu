@@ -343,6 +343,8 @@ __global__ void __launch_bounds__(kThreads)
                       double *Mt) {
   __shared__ double D[kT][kT + 1];
   __shared__ double Y[kT][kT + 1];
+  __shared__ double Ls[64][kSY];   // stride 4 mod 16: conflict-free DMMA fragments
+  __shared__ double Yb[kT][kSY];
   const int s = item_node[blockIdx.x];
   const int f = p.fn[s], c = p.cn[s];
   const int ldc = (c + 15) & ~15;
@@ -372,13 +374,46 @@ __global__ void __launch_bounds__(kThreads)
     __syncthreads();
     for (int i = g; i < nb; i += kThreads / kT)
       if (t < w) W[(int64_t)(jb + i) * ldc + t] = Y[i][t];
-    for (int i = jb + nb + g; i < f; i += kThreads / kT) {
-      const double *Lr = Fs + (int64_t)i * f + jb;
-      double acc = 0.0;
-      for (int l = 0; l < nb; ++l) acc += Lr[l] * Y[l][t];
-      if (t < w) W[(int64_t)i * ldc + t] -= acc;
+    // rows below the block: W[i] -= L[i, jb:jb+nb] Y, 64 rows at a time on the
+    // FP64 tensor pipe (8 warps as 4 (rows) x 2 (columns), 16 x 16 warp tiles)
+    for (int i0 = jb + nb; i0 < f; i0 += 64) {
+      for (int idx = tid; idx < 64 * kT; idx += kThreads) {
+        const int r = idx / kT, j = idx % kT;
+        Ls[r][j] = (i0 + r < f && j < nb) ? Fs[(int64_t)(i0 + r) * f + jb + j] : 0.0;
+      }
+      for (int idx = tid; idx < kT * kT; idx += kThreads) {
+        const int l = idx / kT, j = idx % kT;
+        Yb[l][j] = Y[l][j];
+      }
+      __syncthreads();
+      const int lane = tid & 31, warp = tid >> 5;
+      const int wm = warp >> 1, wn = warp & 1, fr = lane >> 2, fc = lane & 3;
+      double acc[2][2][2] = {};
+      for (int ks = 0; ks < nb; ks += 4) {
+        double a[2], b[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) a[u] = Ls[wm * 16 + 8 * u + fr][ks + fc];
+#pragma unroll
+        for (int v = 0; v < 2; ++v) b[v] = Yb[ks + fc][wn * 16 + 8 * v + fr];
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int v = 0; v < 2; ++v) dmma884(acc[u][v][0], acc[u][v][1], a[u], b[v]);
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int i = i0 + wm * 16 + 8 * u + fr;
+        if (i >= f) continue;
+#pragma unroll
+        for (int v = 0; v < 2; ++v)
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int col = wn * 16 + 8 * v + 2 * fc + q;
+            if (col < w) W[(int64_t)i * ldc + col] -= acc[u][v][q];
+          }
+      }
+      __syncthreads();
     }
-    __syncthreads();
   }
 }
 
