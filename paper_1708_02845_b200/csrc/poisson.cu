@@ -186,21 +186,68 @@ __device__ __forceinline__ void panel_diag(double *Fs, int f, int p0, int pb,
   }
 }
 
-// Panel rows i = i_begin, i_begin + i_step, ... < f (one warp per row, lane j
-// holding column j): x D^T = F[i, p0:p0+pb], right-looking over the pivots.
-__device__ __forceinline__ void panel_trsm_rows(double *Fs, int f, int p0, int pb,
-                                                const double (*D)[kT + 1], int i_begin,
-                                                int i_step) {
-  const int lane = threadIdx.x & 31;
-  for (int i = i_begin; i < f; i += i_step) {
-    double *row = Fs + (int64_t)i * f + p0;
-    double v = lane < pb ? row[lane] : 0.0;
-    for (int j = 0; j < pb; ++j) {
-      const double xj = __shfl_sync(0xffffffffu, v, j) / D[j][j];
-      if (lane == j) v = xj;
-      else if (lane > j) v -= xj * D[lane][j];
+// Panel rows below the pivot block on the FP64 tensor pipe: with the pivot
+// block D factored in shared memory, Dinv = D^{-1} (lower, >= 0 on
+// M-matrices: no cancellation) is formed by warp 0 (lane j = column j), then
+// X = F[rows, p0:p0+pb] Dinv^T for 64-row chunks chunk0, chunk0 + cstep, ...
+// (8 warps as 4 (rows) x 2 (columns), 16 x 16 warp tiles of m8n8k4 DMMAs).
+constexpr int kSY = kT + 4;  // row stride 4 mod 16: conflict-free half-warp fragments
+__device__ __forceinline__ void panel_trsm_dmma(double *Fs, int f, int p0, int pb,
+                                                const double (*D)[kT + 1],
+                                                double (*Dinv)[kSY], double (*Xs)[kSY],
+                                                int chunk0, int cstep) {
+  const int tid = threadIdx.x;
+  if (tid < 32) {
+    const int j = tid;
+    for (int i = 0; i < kT; ++i) {
+      double v;
+      if (i < j) v = 0.0;
+      else if (i == j) v = 1.0 / D[j][j];
+      else {
+        double acc = 0.0;
+        for (int l = j; l < i; ++l) acc += D[i][l] * Dinv[l][j];
+        v = -acc / D[i][i];
+      }
+      Dinv[i][j] = v;
     }
-    if (lane < pb) row[lane] = v;
+  }
+  __syncthreads();
+  const int lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1, fr = lane >> 2, fc = lane & 3;
+  const int r0 = p0 + pb;
+  for (int ch = chunk0; r0 + ch * 64 < f; ch += cstep) {
+    const int i0 = r0 + ch * 64;
+    for (int idx = tid; idx < 64 * kT; idx += blockDim.x) {
+      const int r = idx / kT, j = idx % kT;
+      Xs[r][j] = (i0 + r < f && j < pb) ? Fs[(int64_t)(i0 + r) * f + p0 + j] : 0.0;
+    }
+    __syncthreads();
+    double acc[2][2][2] = {};
+#pragma unroll
+    for (int ks = 0; ks < kT; ks += 4) {
+      double a[2], b[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) a[u] = Xs[wm * 16 + 8 * u + fr][ks + fc];
+#pragma unroll
+      for (int v = 0; v < 2; ++v) b[v] = Dinv[wn * 16 + 8 * v + fr][ks + fc];
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) dmma884(acc[u][v][0], acc[u][v][1], a[u], b[v]);
+    }
+    __syncthreads();  // every warp has read Xs before the next chunk overwrites it
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int i = i0 + wm * 16 + 8 * u + fr;
+      if (i >= f) continue;
+#pragma unroll
+      for (int v = 0; v < 2; ++v)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int col = wn * 16 + 8 * v + 2 * fc + q;
+          if (col < pb) Fs[(int64_t)i * f + p0 + col] = acc[u][v][q];
+        }
+    }
   }
 }
 
@@ -210,7 +257,6 @@ __device__ __forceinline__ void panel_trsm_rows(double *Fs, int f, int p0, int p
 // over the (<= 32)-deep panel; A = the tile's panel rows, B = the other
 // tile's panel rows transposed.  Row stride kSY = 36 (4 mod 16): conflict-free
 // half-warp fragment loads.
-constexpr int kSY = kT + 4;
 __device__ __forceinline__ void panel_syrk_tile(double *Fs, int f, int p0, int pb, int ti,
                                                 int tl, double (*Ai)[kSY], double (*Al)[kSY]) {
   const int tid = threadIdx.x;
@@ -274,7 +320,7 @@ __global__ void __launch_bounds__(kThreads, 4)
   for (int p0 = 0; p0 < c; p0 += kT) {
     const int pb = min(kT, c - p0);
     panel_diag(Fs, f, p0, pb, D, err, true);
-    panel_trsm_rows(Fs, f, p0, pb, D, p0 + pb + threadIdx.x / 32, kThreads / 32);
+    panel_trsm_dmma(Fs, f, p0, pb, D, Ai, Al, 0, 1);
     __syncthreads();
     const int nb = (f - p0 - pb + 63) / 64;
     for (int pr = 0; pr < nb * (nb + 1) / 2; ++pr) {
@@ -302,6 +348,8 @@ __global__ void __launch_bounds__(kThreads, 4)
     mf_panel_trsm_kernel(pf_mf_plan_t p, const int32_t *__restrict__ nodes, int p0, double *F,
                          int32_t *err) {
   __shared__ double D[kT][kT + 1];
+  __shared__ double Dinv[kT][kSY];
+  __shared__ double Xs[64][kSY];
   const int s = nodes[blockIdx.x];
   const int c = p.cn[s], f = p.fn[s];
   if (p0 >= c) return;
@@ -310,8 +358,7 @@ __global__ void __launch_bounds__(kThreads, 4)
   // every CTA factors the 32 x 32 pivot block itself (cheaper than a launch);
   // the first writes it back
   panel_diag(Fs, f, p0, pb, D, err, true, blockIdx.y == 0);
-  panel_trsm_rows(Fs, f, p0, pb, D, p0 + pb + blockIdx.y * (kThreads / 32) + threadIdx.x / 32,
-                  gridDim.y * (kThreads / 32));
+  panel_trsm_dmma(Fs, f, p0, pb, D, Dinv, Xs, blockIdx.y, gridDim.y);
 }
 
 __global__ void __launch_bounds__(kThreads)
@@ -995,7 +1042,7 @@ int pf_mf_factor_level(const pf_mf_plan_t *plan, const double *off, const double
                              kThreads, 0, st>>>(*plan, off, diag, nodes, F);
   for (int p0 = 0; p0 < max_c; p0 += kT) {
     const int rows = max_f - p0;
-    const int ty = std::max(1, std::min(per, (rows + kThreads / 32 - 1) / (kThreads / 32)));
+    const int ty = std::max(1, std::min(per, (rows + 63) / 64));  // 64-row DMMA chunks
     mf_panel_trsm_kernel<<<dim3((unsigned)count, (unsigned)ty), kThreads, 0, st>>>(*plan, nodes,
                                                                                   p0, F, err);
     const int nb = (rows - 1 + 63) / 64;
