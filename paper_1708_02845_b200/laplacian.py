@@ -84,6 +84,42 @@ def mesh_topology(mesh):
     return nb_ptr, nb_idx, isb
 
 
+def slab_needs(plan, nb_ptr, nb_idx, is_boundary, row0: int, rows: int, ld: int):
+    """Host half of a row-slab build (DevicePoisson.slab_plan): which fronts the
+    backward must run for rows [row0, row0 + rows) — those holding a slab row,
+    a row of the slab's 1-ring (the residual reads it) or an ancestor's row —
+    and the per-vertex output offsets (slab rows at (v - row0) * ld, the other
+    needed rows in scratch rows after the slab, -1 elsewhere).
+    Returns (need mask over fronts, rowoff (n,), number of scratch rows)."""
+    pl = plan
+    n = pl.n
+    isb = np.asarray(is_boundary).astype(bool)
+    pos_of = -np.ones(n, dtype=np.int64)
+    pos_of[pl.perm_orig] = np.arange(pl.m)
+    node_of_pos = np.repeat(np.arange(pl.nodes), pl.cn)
+    slab = np.arange(row0, row0 + rows)
+    slab_int = slab[~isb[slab]]
+    lo, hi = nb_ptr[slab_int], nb_ptr[slab_int + 1]
+    cnt = hi - lo
+    ring = nb_idx[np.repeat(lo - (np.cumsum(cnt) - cnt), cnt) + np.arange(cnt.sum())]
+    verts = np.unique(np.concatenate([slab_int, ring]))
+    verts = verts[~isb[verts]]
+    need = np.zeros(pl.nodes, dtype=bool)
+    cur = np.unique(node_of_pos[pos_of[verts]])
+    while cur.size:
+        cur = cur[~need[cur]]
+        need[cur] = True
+        cur = np.unique(pl.parent[cur])
+        cur = cur[cur >= 0]
+    need_v = pl.perm_orig[np.flatnonzero(need[node_of_pos])].astype(np.int64)
+    rowoff = np.full(n, -1, dtype=np.int64)
+    in_slab = (need_v >= row0) & (need_v < row0 + rows)
+    rowoff[need_v[in_slab]] = (need_v[in_slab] - row0) * ld
+    extra = need_v[~in_slab]
+    rowoff[extra] = (rows + np.arange(extra.size)) * ld
+    return need, rowoff, int(extra.size)
+
+
 class NdPlan:
     """Host nested-dissection plan of the interior block (nd_plan.cpp).
 
@@ -292,36 +328,11 @@ class DevicePoisson:
         if hit is not None:
             return hit
         pl, tod = self.plan, self._tod
-        n, ld = self.n, round_up_cols(self.k)
-        isb = self._isb_host.astype(bool)
+        ld = round_up_cols(self.k)
         nb_ptr, nb_idx = self._nb_host
-        pos_of = -np.ones(n, dtype=np.int64)
-        pos_of[pl.perm_orig] = np.arange(pl.m)
-        node_of_pos = np.repeat(np.arange(pl.nodes), pl.cn)
-        slab = np.arange(row0, row0 + rows)
-        slab_int = slab[~isb[slab]]
-        lo, hi = nb_ptr[slab_int], nb_ptr[slab_int + 1]
-        ring = nb_idx[np.repeat(lo, hi - lo) + (np.arange((hi - lo).sum())
-                                               - np.repeat(np.cumsum(hi - lo) - (hi - lo), hi - lo))]
-        verts = np.unique(np.concatenate([slab_int, ring]))
-        verts = verts[~isb[verts]]
-        need = np.zeros(pl.nodes, dtype=bool)
-        cur = np.unique(node_of_pos[pos_of[verts]])
-        while cur.size:
-            cur = cur[~need[cur]]
-            need[cur] = True
-            cur = np.unique(pl.parent[cur])
-            cur = cur[cur >= 0]
-        # rows of every needed front: slab rows at their slab offset, the rest in scratch
-        need_pos = np.flatnonzero(need[node_of_pos])
-        need_v = pl.perm_orig[need_pos].astype(np.int64)
-        rowoff = np.full(n, -1, dtype=np.int64)
-        in_slab = (need_v >= row0) & (need_v < row0 + rows)
-        rowoff[need_v[in_slab]] = (need_v[in_slab] - row0) * ld
-        extra = need_v[~in_slab]
-        rowoff[extra] = (rows + np.arange(extra.size)) * ld
+        need, rowoff, extra = slab_needs(pl, nb_ptr, nb_idx, self._isb_host, row0, rows, ld)
         in_slab_pos = (pl.perm_orig >= row0) & (pl.perm_orig < row0 + rows)
-        hit = {"need": need, "rowoff": tod(rowoff, np.int64), "scratch_rows": int(extra.size),
+        hit = {"need": need, "rowoff": tod(rowoff, np.int64), "scratch_rows": int(extra),
                "order": tod(pl.perm_orig[in_slab_pos], np.int32),
                "count": int(in_slab_pos.sum()), "bwd": self._bwd_lists(need),
                "fronts": int(need.sum())}

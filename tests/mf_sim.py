@@ -52,9 +52,11 @@ def factor(plan, off, diag):
     return F
 
 
-def solve(plan, F, off, k, ld=None):
+def solve(plan, F, off, k, ld=None, need=None):
     """Forward (tile-sparse, one f x tile [Y_C; V] block per active item) +
-    backward into P rows."""
+    backward into P rows.  `need` (bool per front) restricts the backward to
+    those fronts, as a row-slab build does: the rows of the other fronts stay
+    NaN, so a slab that read one of them shows it."""
     n, T = plan.n, plan.tile
     P = np.zeros((n, k))
     V = np.zeros(plan.stats["v_total"])
@@ -87,10 +89,13 @@ def solve(plan, F, off, k, ld=None):
                 touched[Crows, t] = True
                 W[:c] = Y
                 V[plan.act_voff[it]:plan.act_voff[it] + f * T] = W.ravel()  # [Y_C; V]
+    if need is not None:  # forget what the slab's backward does not compute
+        for s in np.flatnonzero(~need):
+            P[plan.perm_orig[plan.c0[s]:plan.c0[s] + plan.cn[s]]] = np.nan
     for level in reversed(plan.levels):
         for s in level:
             f, c, r = int(plan.fn[s]), int(plan.cn[s]), int(plan.rn[s])
-            if not c:
+            if not c or (need is not None and not need[s]):
                 continue
             Fs = F[plan.foff[s]:plan.foff[s] + f * f].reshape(f, f)
             Crows = plan.perm_orig[plan.c0[s]:plan.c0[s] + c]

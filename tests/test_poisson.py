@@ -85,6 +85,37 @@ def test_plan_tiles_cover_rhs():
     assert len(root_tiles) <= plan.ntiles
 
 
+@pytest.mark.parametrize("name", ["c1", "holes_fine"])
+@pytest.mark.parametrize("parts", [3, 8])
+def test_slab_needs_cover_the_slab(name, parts):
+    """laplacian.slab_needs: a backward over only the needed fronts (numpy
+    simulation; unneeded rows NaN) reproduces the slab rows and their 1-ring
+    exactly; the row offsets put slab rows first and scratch rows after."""
+    from paper_1708_02845_b200.laplacian import NdPlan, mesh_topology, slab_needs
+    c = case(name)
+    m = c.mesh
+    nb_ptr, nb_idx, isb = mesh_topology(m)
+    plan = NdPlan(m.vertices, nb_ptr, nb_idx, isb, leaf=16)
+    off, diag = mf_sim.laplacian_parts(I.cotan_laplacian(m), nb_ptr, nb_idx)
+    F = mf_sim.factor(plan, off, diag)
+    full = mf_sim.solve(plan, F, off, plan.k)
+    bounds = np.linspace(0, plan.n, parts + 1).astype(int)
+    for a, b in zip(bounds[:-1], bounds[1:]):
+        need, rowoff, extra = slab_needs(plan, nb_ptr, nb_idx, isb, int(a), int(b - a), 7)
+        got = mf_sim.solve(plan, F, off, plan.k, need=need)
+        rows = np.arange(a, b)
+        inner = rows[isb[rows] == 0]
+        lo, hi = nb_ptr[inner], nb_ptr[inner + 1]
+        ring = np.unique(np.concatenate([nb_idx[x:y] for x, y in zip(lo, hi)] + [inner]))
+        ring = ring[isb[ring] == 0]
+        assert np.array_equal(got[ring], full[ring])            # no NaN: every row computed
+        assert np.array_equal(rowoff[inner], (inner - a) * 7)   # slab rows first
+        assert np.all(rowoff[ring] >= 0)
+        scratch = rowoff[(rowoff >= 0) & ((np.arange(plan.n) < a) | (np.arange(plan.n) >= b))]
+        assert scratch.size == extra and np.array_equal(np.sort(scratch) // 7,
+                                                        (b - a) + np.arange(extra))
+
+
 def test_plan_rejects_bad_arguments():
     from paper_1708_02845_b200 import _native as nat
     from paper_1708_02845_b200.errors import NativeError
