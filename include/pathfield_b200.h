@@ -529,8 +529,9 @@ int pf_mf_factor_level(const pf_mf_plan_t *plan, const double *off, const double
 
 /* Explicit front inverses after the factorisation: Mt = [L_CC^{-1};
  * -L_RC L_CC^{-1}] (f x c, row stride round_up(c,16)) for items (node, 32
- * identity columns), then M = Mt^T (c x round_up(f,16)) for `nodes`.  Both
- * buffers must be zero-initialised (their row pads stay 0).  Non-negative on
+ * identity columns), then, if M != NULL, M = Mt^T (c x round_up(f,16)) for
+ * `nodes` (the solves read Mt only).  Buffers must be zero-initialised (their
+ * row pads stay 0).  Non-negative on
  * M-matrices: the solves below are sums of non-negative products. */
 int pf_mf_inverse(const pf_mf_plan_t *plan, const double *F, const int32_t *item_node,
                   const int32_t *item_ct, int64_t count, const int32_t *nodes, int64_t nnodes,
@@ -546,13 +547,13 @@ int pf_mf_forward_level(const pf_mf_plan_t *plan, const double *Mt, const double
                         const int64_t *g_woff, const int32_t *g_rb, int64_t n_gemm, double *Wb,
                         double *O, pf_stream_t stream);
 
-/* Backward solve of one level (levels top-down): X_C = M [Y_C; X_R] for items
+/* Backward solve of one level (levels top-down): X_C = Mt^T [Y_C; X_R] for items
  * (node, nb_rows-row block of C, 128-column blocks [cb0, cb1)), Y_C from O
  * (zero for tiles the forward never reached), X_R from P's rows, X_C into P
  * (rows by original vertex id; ldp a multiple of 64).  nb_rows in {8, 16, 32,
  * 64}; max_f / max_ncb bound the items' front sizes and column-block counts
  * (shared-memory sizing). */
-int pf_mf_backward_level(const pf_mf_plan_t *plan, const double *M, const double *O,
+int pf_mf_backward_level(const pf_mf_plan_t *plan, const double *Mt, const double *O,
                          const int32_t *item_node, const int32_t *item_rb,
                          const int32_t *item_cb0, const int32_t *item_cb1, int64_t count,
                          int32_t max_f, int32_t max_ncb, int32_t nb_rows, double *P,

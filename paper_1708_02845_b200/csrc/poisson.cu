@@ -666,7 +666,7 @@ constexpr int kBN = 128, kBT = 256, kBW = kBT / 32;  // consumer threads / warps
 constexpr int kSB2 = kBN + 4;  // 4 mod 16: conflict-free half-warp fragment loads
 constexpr int kZStage = kGBK * kSB2;
 template <int NB>
-constexpr int m_stage() { return NB * kSA; }
+constexpr int m_stage() { return kGBK * (NB + 4); }  // 16 k-rows of Mt, NB + 4 stride
 template <int NB>
 constexpr int bwd_ring_bytes() {
   return kGStages * (kZStage + m_stage<NB>()) * 8 + 2 * kGStages * 8;  // + mbarriers
@@ -693,7 +693,6 @@ __global__ void __launch_bounds__(kBT + 32, 2)
   const int nthr = kBT + 32;
   const int s = item_node[blockIdx.x];
   const int f = p.fn[s], c = p.cn[s];
-  const int ldf = (f + 15) & ~15;
   const int i0 = item_rb[blockIdx.x] * NB;
   const int cb0 = item_cb0[blockIdx.x], ncb = item_cb1[blockIdx.x] - cb0;
   int64_t *kt0 = reinterpret_cast<int64_t *>(ysrc + 2 * ncb);
@@ -723,8 +722,12 @@ __global__ void __launch_bounds__(kBT + 32, 2)
   __syncthreads();
   const int nkt = (f + kGBK - 1) / kGBK;
   if (warp == kBW) {  // ------------------------------------------- producer
-    const double *A = M + p.m_off[s] + (int64_t)i0 * ldf;
-    const int ma = min(NB, c - i0);
+    // B operand straight from Mt (f x ldc): a K stage is 16 rows of Mt, each
+    // the NB contiguous entries of this C-row block — the k-major layout the
+    // DMMA B fragment wants (no transpose, one bulk copy per k-row)
+    const int ldc = (c + 15) & ~15;
+    const double *A = M + p.mt_off[s] + i0;
+    const int mb = min(NB, ldc - i0);  // real columns in this row (pads are zero)
     int it = 0;
     for (int cb = 0; cb < ncb; ++cb) {
       const int64_t col = (int64_t)(cb0 + cb) * kBN;
@@ -751,9 +754,15 @@ __global__ void __launch_bounds__(kBT + 32, 2)
             bulk_g2s(dst + kGBN, g_zero_row, kGBN * 8, &full[st]);
           }
         }
-        for (int r = lane; r < NB; r += 32) {
-          const double *src = r < ma ? A + (int64_t)r * ldf + k0 : g_zero_row;
-          bulk_g2s(Ms + st * kMS + r * kSA, src, kGBK * 8, &full[st]);
+        if (lane < kGBK) {
+          const int l = k0 + lane;
+          double *dst = Ms + st * kMS + lane * (NB + 4);
+          if (l < f) {
+            bulk_g2s(dst, A + (int64_t)l * ldc, mb * 8, &full[st]);
+            if (mb < NB) bulk_g2s(dst + mb, g_zero_row, (NB - mb) * 8, &full[st]);
+          } else {
+            bulk_g2s(dst, g_zero_row, NB * 8, &full[st]);
+          }
         }
       }
     }
@@ -775,14 +784,14 @@ __global__ void __launch_bounds__(kBT + 32, 2)
       const int st = it % kGStages;
       mbar_wait(&full[st], (it / kGStages) & 1);
       const double *zs = Zs + st * kZStage + fc * kSB2 + warp * 16 + fr;
-      const double *ms = Ms + st * kMS + fr * kSA + fc;
+      const double *ms = Ms + st * kMS + fc * (NB + 4) + fr;
 #pragma unroll
       for (int ks = 0; ks < kGBK; ks += 4) {
         double av[2], bv[NJ];
 #pragma unroll
         for (int i = 0; i < 2; ++i) av[i] = zs[ks * kSB2 + 8 * i];
 #pragma unroll
-        for (int j = 0; j < NJ; ++j) bv[j] = ms[8 * j * kSA + ks];
+        for (int j = 0; j < NJ; ++j) bv[j] = ms[ks * (NB + 4) + 8 * j];
 #pragma unroll
         for (int j = 0; j < NJ; ++j)
           if (j < njv) {
@@ -1057,13 +1066,14 @@ int pf_mf_inverse(const pf_mf_plan_t *plan, const double *F, const int32_t *item
                   const int32_t *item_ct, int64_t count, const int32_t *nodes, int64_t nnodes,
                   double *Mt, double *M, pf_stream_t stream) {
   if (count == 0 && nnodes == 0) return 0;  // no interior vertices: nothing to invert
-  if (!plan || !F || (count && (!item_node || !item_ct)) || (nnodes && !nodes) || !Mt || !M ||
+  if (!plan || !F || (count && (!item_node || !item_ct)) || (nnodes && M && !nodes) || !Mt ||
       count < 0 || nnodes < 0 || plan->tile != kGBN)
     return fail(PF_E_ARG, "pf_mf_inverse: bad argument");
   cudaStream_t st = as_stream(stream);
   if (count > 0)
     mf_inverse_kernel<<<(unsigned)count, kThreads, 0, st>>>(*plan, F, item_node, item_ct, Mt);
-  if (nnodes > 0) mf_transpose_kernel<<<(unsigned)nnodes, kThreads, 0, st>>>(*plan, nodes, Mt, M);
+  if (nnodes > 0 && M)  // M = Mt^T only on request (the solves read Mt)
+    mf_transpose_kernel<<<(unsigned)nnodes, kThreads, 0, st>>>(*plan, nodes, Mt, M);
   return check_launch("pf_mf_inverse");
 }
 

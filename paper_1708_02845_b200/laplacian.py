@@ -369,20 +369,19 @@ class DevicePoisson:
 
     # -- laplacian.py:29-45 (splu of -Lc_II) -------------------------------
     def factor(self):
-        """Multifrontal Cholesky of -Lc_II and the explicit front inverses
-        (Mt, M) on the device (cached).  Returns (Mt, M)."""
+        """Multifrontal Cholesky of -Lc_II and the explicit front inverses Mt
+        on the device (cached).  Returns Mt."""
         if self._F is None:
             from . import _device as dev
             from .errors import FactorizationError
             t = dev.torch()
             off, diag = self.laplacian()
-            if self._bufs is None:  # kept across refactorisations (pads of Mt / M stay 0)
+            if self._bufs is None:  # kept across refactorisations (pads of Mt stay 0)
                 self._bufs = (
                     t.empty(max(self.plan.stats["f_total"], 1), dtype=t.float64,
                             device=self.device),
-                    t.zeros(max(int(self.mt_off[-1]), 1), dtype=t.float64, device=self.device),
-                    t.zeros(max(int(self.m_off[-1]), 1), dtype=t.float64, device=self.device))
-            F, Mt, M = self._bufs
+                    t.zeros(max(int(self.mt_off[-1]), 1), dtype=t.float64, device=self.device))
+            F, Mt = self._bufs
             err = t.zeros(1, dtype=t.int32, device=self.device)
             s = self.stream()
             for lv, (mf, mc, split) in zip(self.levels, self.level_shape):
@@ -392,12 +391,12 @@ class DevicePoisson:
             inode, ict, icnt, nodes = self.inv
             nat.call("pf_mf_inverse", ctypes.addressof(self.struct), F.data_ptr(),
                      inode.data_ptr(), ict.data_ptr(), icnt, nodes.data_ptr(), nodes.numel(),
-                     Mt.data_ptr(), M.data_ptr(), s)
+                     Mt.data_ptr(), None, s)  # the solves read Mt (no transpose)
             if int(err.item()):
                 raise FactorizationError(
                     "interior block is not positive definite after negation "
                     "(severely non-Delaunay mesh)")
-            self._F = (Mt, M)
+            self._F = Mt
         return self._F
 
     # -- solvers.py:278-303 ------------------------------------------------
@@ -417,7 +416,7 @@ class DevicePoisson:
         mark = (lambda name: events.setdefault(name, t.cuda.Event(enable_timing=True)).record(
             t.cuda.current_stream(self.device))) if events is not None else (lambda name: None)
         off, diag = self.laplacian()
-        Mt, M = self.factor()
+        Mt = self.factor()
         ld = round_up_cols(self.k)
         if slab is None:
             row0, rows, extra = 0, self.n, 0
@@ -446,7 +445,7 @@ class DevicePoisson:
         for nodes, rb, cb0, cb1, cnt, maxf, ncb, nbr in reversed(bwd):
             if cnt == 0:  # a slab build may need no front of a level
                 continue
-            nat.call("pf_mf_backward_level", ps, M.data_ptr(), O.data_ptr(), nodes.data_ptr(),
+            nat.call("pf_mf_backward_level", ps, Mt.data_ptr(), O.data_ptr(), nodes.data_ptr(),
                      rb.data_ptr(), cb0.data_ptr(), cb1.data_ptr(), cnt, maxf, ncb, nbr,
                      Pbuf.data_ptr(), ld, s)
         mark("bwd1")
