@@ -162,18 +162,31 @@ __device__ __forceinline__ void panel_diag(double *Fs, int f, int p0, int pb,
   __syncthreads();
   if (!factor) return;
   if (tid < 32) {
+    // right-looking, lane i owns row i; the trailing update of step j goes
+    // in batches of 8 whose loads all issue before their stores (a plain
+    // loop serialises each load behind the previous possibly-aliasing store)
     const int lane = tid;
     for (int j = 0; j < pb; ++j) {
       const double djj = D[j][j];
-      if (!(djj > 0.0)) atomicOr(err, 1);
+      if (lane == 0 && !(djj > 0.0)) atomicOr(err, 1);
       const double d = sqrt(djj);
       __syncwarp();
       if (lane == j) D[j][j] = d;
       if (lane > j && lane < pb) D[lane][j] /= d;
       __syncwarp();
-      if (lane > j && lane < pb) {
-        const double lij = D[lane][j];
-        for (int l = j + 1; l <= lane; ++l) D[lane][l] -= lij * D[l][j];
+      const double lij = D[lane][j];
+      const bool mine = lane > j && lane < pb;
+      for (int l0 = j + 1; l0 <= lane; l0 += 8) {
+        double cj[8], rv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int l = min(l0 + u, kT - 1);
+          cj[u] = D[l][j];
+          rv[u] = D[lane][l];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (mine && l0 + u <= lane) D[lane][l0 + u] = rv[u] - lij * cj[u];
       }
       __syncwarp();
     }
@@ -198,17 +211,28 @@ __device__ __forceinline__ void panel_trsm_dmma(double *Fs, int f, int p0, int p
                                                 int chunk0, int cstep) {
   const int tid = threadIdx.x;
   if (tid < 32) {
+    // lane j solves L x = e_j right-looking in its Dinv column: once x_i is
+    // final, x_k -= L[k][i] x_i (k > i) are independent FMAs, issued in
+    // batches of 8 loads before 8 stores.  x_k accumulates -(sum_l L[k][l]
+    // x_l) in the left-looking order, so x_k / L[k][k] is bitwise the
+    // left-looking -acc / L[k][k].
     const int j = tid;
+    for (int i = 0; i < kT; ++i) Dinv[i][j] = (i == j) ? 1.0 : 0.0;
     for (int i = 0; i < kT; ++i) {
-      double v;
-      if (i < j) v = 0.0;
-      else if (i == j) v = 1.0 / D[j][j];
-      else {
-        double acc = 0.0;
-        for (int l = j; l < i; ++l) acc += D[i][l] * Dinv[l][j];
-        v = -acc / D[i][i];
+      const double xi = Dinv[i][j] / D[i][i];
+      Dinv[i][j] = xi;
+      for (int k0 = i + 1; k0 < kT; k0 += 8) {
+        double dv[8], xv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int k = min(k0 + u, kT - 1);
+          dv[u] = D[k][i];
+          xv[u] = Dinv[k][j];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (k0 + u < kT) Dinv[k0 + u][j] = xv[u] - dv[u] * xi;
       }
-      Dinv[i][j] = v;
     }
   }
   __syncthreads();
@@ -355,26 +379,44 @@ __global__ void __launch_bounds__(kThreads, 4)
   if (p0 >= c) return;
   const int pb = min(kT, c - p0);
   double *Fs = F + p.foff[s];
-  // every CTA factors the 32 x 32 pivot block itself (cheaper than a launch);
-  // the first writes it back
-  panel_diag(Fs, f, p0, pb, D, err, true, blockIdx.y == 0);
+  // the pivot block was factored by the previous launch (mf_panel_diag_kernel
+  // for the first panel, the SYRK CTA owning tile (0, 0) after that): a CTA
+  // of this grid factoring and writing it back would race the others' reads
+  panel_diag(Fs, f, p0, pb, D, err, false);
   panel_trsm_dmma(Fs, f, p0, pb, D, Dinv, Xs, blockIdx.y, gridDim.y);
 }
 
+// First pivot block of each front on the split path (one warp per front).
+__global__ void __launch_bounds__(32)
+    mf_panel_diag_kernel(pf_mf_plan_t p, const int32_t *__restrict__ nodes, double *F,
+                         int32_t *err) {
+  __shared__ double D[kT][kT + 1];
+  const int s = nodes[blockIdx.x];
+  const int c = p.cn[s], f = p.fn[s];
+  if (c <= 0) return;
+  panel_diag(F + p.foff[s], f, 0, min(kT, c), D, err, true);
+}
+
 __global__ void __launch_bounds__(kThreads)
-    mf_panel_syrk_kernel(pf_mf_plan_t p, const int32_t *__restrict__ nodes, int p0, double *F) {
+    mf_panel_syrk_kernel(pf_mf_plan_t p, const int32_t *__restrict__ nodes, int p0, double *F,
+                         int32_t *err) {
   __shared__ double Ai[64][kSY];
   __shared__ double Al[64][kSY];
+  __shared__ double D[kT][kT + 1];
   const int s = nodes[blockIdx.x];
   const int c = p.cn[s], f = p.fn[s];
   if (p0 >= c) return;
   const int pb = min(kT, c - p0);
   const int nb = (f - p0 - pb + 63) / 64;
+  double *Fs = F + p.foff[s];
   for (int pr = blockIdx.y; pr < nb * (nb + 1) / 2; pr += gridDim.y) {
     int ti, tl;
     tri_pair(pr, ti, tl);
-    panel_syrk_tile(F + p.foff[s], f, p0, pb, ti, tl, Ai, Al);
+    panel_syrk_tile(Fs, f, p0, pb, ti, tl, Ai, Al);
   }
+  // tile (0, 0), updated by this CTA alone, holds the next pivot block
+  const int q0 = p0 + pb;
+  if (blockIdx.y == 0 && q0 < c) panel_diag(Fs, f, q0, min(kT, c - q0), D, err, true);
 }
 
 // ------------------------------------------------- explicit inverses --
@@ -1045,10 +1087,11 @@ int pf_mf_factor_level(const pf_mf_plan_t *plan, const double *off, const double
     return check_launch("pf_mf_factor_level");
   }
   // few large fronts: spread every step of each front over ~2 waves of CTAs
-  const int target = 2 * sm_count();
+  const int target = 8 * sm_count();
   const int per = (int)std::max<int64_t>(1, (target + count - 1) / count);
   mf_assemble_split_kernel<<<dim3((unsigned)count, (unsigned)std::min(per, std::max(1, max_f / 16))),
                              kThreads, 0, st>>>(*plan, off, diag, nodes, F);
+  mf_panel_diag_kernel<<<(unsigned)count, 32, 0, st>>>(*plan, nodes, F, err);
   for (int p0 = 0; p0 < max_c; p0 += kT) {
     const int rows = max_f - p0;
     const int ty = std::max(1, std::min(per, (rows + 63) / 64));  // 64-row DMMA chunks
@@ -1057,7 +1100,7 @@ int pf_mf_factor_level(const pf_mf_plan_t *plan, const double *off, const double
     const int nb = (rows - 1 + 63) / 64;
     const int pairs = std::max(1, nb * (nb + 1) / 2);
     mf_panel_syrk_kernel<<<dim3((unsigned)count, (unsigned)std::min(pairs, std::max(per, 1))),
-                           kThreads, 0, st>>>(*plan, nodes, p0, F);
+                           kThreads, 0, st>>>(*plan, nodes, p0, F, err);
   }
   return check_launch("pf_mf_factor_level");
 }
