@@ -569,7 +569,8 @@ int pf_poisson_residual_table(const int32_t *nb_idx, int64_t nnz, const uint8_t 
  * and columns j < k with P's boundary rows taken as indicators (= |Lc_II P_IB
  * + Lc_IB|, solvers.py:292), before the clip; out_max[0] holds the max as
  * ordered FP64 bits.  `order` is best the plan's perm_orig (spatially compact
- * row groups share their neighbours' rows in cache). */
+ * row groups share their neighbours' rows in cache).  Every row offset (rowoff,
+ * nrow) is a multiple of ldp and names one of fewer than 2^31 rows. */
 int pf_poisson_residual(const double *P, int64_t ldp, int64_t k, const int32_t *order,
                         int64_t count, const int64_t *rowoff, const int64_t *nb_ptr,
                         const int64_t *nrow, const double *off, const double *diag,

@@ -876,7 +876,7 @@ __device__ __forceinline__ void atomic_max_nonneg(unsigned long long *p, double 
 constexpr int kResCols = 512;
 
 template <int WARPS>
-__global__ void __launch_bounds__(WARPS * 32)
+__global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32))
     residual_kernel(const double *__restrict__ P, int64_t ldp, int64_t k,
                     const int32_t *__restrict__ order, int64_t count,
                     const int64_t *__restrict__ rowoff,
@@ -926,6 +926,40 @@ __global__ void __launch_bounds__(WARPS * 32)
       bw[w][slot] = mw;
     }
     __syncwarp();
+    if (deg <= kG) {
+      // the common valence: the 8 slots live in registers for the whole
+      // column chunk (re-reading them from shared memory per step cost a
+      // third of the L1 data-pipe wavefronts), fetched once by shuffle
+      int32_t ro[kG];  // row indices (every P row offset is a multiple of ldp)
+      double wr[kG];
+      const int32_t mr = (int32_t)((inner ? me : vo) / ldp);
+#pragma unroll
+      for (int u = 0; u < kG; ++u) {
+        ro[u] = __shfl_sync(0xffffffffu, mr, u);
+        wr[u] = __shfl_sync(0xffffffffu, inner ? mw : 0.0, u);
+      }
+      for (int64_t j = j0 + 2 * lane; j < j1; j += 64) {
+        const double2 pv = *reinterpret_cast<const double2 *>(P + vo + j);
+        double2 x[kG];
+#pragma unroll
+        for (int u = 0; u < kG; ++u)
+          x[u] = *reinterpret_cast<const double2 *>(P + (int64_t)ro[u] * ldp + j);
+        double a0 = dv * pv.x, a1 = dv * pv.y;
+#pragma unroll
+        for (int u = 0; u < kG; ++u) {
+          a0 += wr[u] * x[u].x;
+          a1 += wr[u] * x[u].y;
+        }
+        for (int q = 0; q < nbnd; ++q) {
+          const int64_t b = bcl[w][q];
+          if (b == j) a0 += bw[w][q];
+          if (b == j + 1) a1 += bw[w][q];
+        }
+        mx = fmax(mx, fabs(a0));
+        if (j + 1 < k) mx = fmax(mx, fabs(a1));
+      }
+      continue;
+    }
     const int ngroups = (deg + kG - 1) / kG;
     for (int64_t j = j0 + 2 * lane; j < j1; j += 64) {
       const double2 pv = *reinterpret_cast<const double2 *>(P + vo + j);
