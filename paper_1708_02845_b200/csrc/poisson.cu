@@ -169,10 +169,11 @@ __device__ __forceinline__ void panel_diag(double *Fs, int f, int p0, int pb,
     for (int j = 0; j < pb; ++j) {
       const double djj = D[j][j];
       if (lane == 0 && !(djj > 0.0)) atomicOr(err, 1);
-      const double d = sqrt(djj);
+      const double rd = rsqrt(djj);  // one MUFU-seeded chain; d and the column
+      const double d = djj * rd;      // scale both follow from it in parallel
       __syncwarp();
       if (lane == j) D[j][j] = d;
-      if (lane > j && lane < pb) D[lane][j] /= d;
+      if (lane > j && lane < pb) D[lane][j] *= rd;
       __syncwarp();
       const double lij = D[lane][j];
       const bool mine = lane > j && lane < pb;
@@ -213,13 +214,13 @@ __device__ __forceinline__ void panel_trsm_dmma(double *Fs, int f, int p0, int p
   if (tid < 32) {
     // lane j solves L x = e_j right-looking in its Dinv column: once x_i is
     // final, x_k -= L[k][i] x_i (k > i) are independent FMAs, issued in
-    // batches of 8 loads before 8 stores.  x_k accumulates -(sum_l L[k][l]
-    // x_l) in the left-looking order, so x_k / L[k][k] is bitwise the
-    // left-looking -acc / L[k][k].
+    // batches of 8 loads before 8 stores; x_i = x_i * (1 / L[i][i]) keeps
+    // the divisions off the dependent chain (entries stay non-negative).
     const int j = tid;
+    const double rdj = 1.0 / D[j][j];  // all 32 reciprocals at once, off the chain
     for (int i = 0; i < kT; ++i) Dinv[i][j] = (i == j) ? 1.0 : 0.0;
     for (int i = 0; i < kT; ++i) {
-      const double xi = Dinv[i][j] / D[i][i];
+      const double xi = Dinv[i][j] * __shfl_sync(0xffffffffu, rdj, i);
       Dinv[i][j] = xi;
       for (int k0 = i + 1; k0 < kT; k0 += 8) {
         double dv[8], xv[8];
