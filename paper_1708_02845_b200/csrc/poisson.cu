@@ -760,8 +760,11 @@ __global__ void __launch_bounds__(kBT + 32, 2)
       }
   }
   __syncthreads();
+  // Mt's top block L_CC^{-1} is lower triangular: rows l < i0 are zero in
+  // this CTA's columns, so K starts at i0's tile (or past Y_C when the
+  // forward never reached these columns)
   for (int cb = tid; cb < ncb; cb += nthr)
-    kt0[cb] = (ysrc[2 * cb] || ysrc[2 * cb + 1]) ? 0 : c / kGBK;
+    kt0[cb] = (ysrc[2 * cb] || ysrc[2 * cb + 1]) ? i0 / kGBK : c / kGBK;
   __syncthreads();
   const int nkt = (f + kGBK - 1) / kGBK;
   if (warp == kBW) {  // ------------------------------------------- producer
@@ -828,6 +831,7 @@ __global__ void __launch_bounds__(kBT + 32, 2)
       mbar_wait(&full[st], (it / kGStages) & 1);
       const double *zs = Zs + st * kZStage + fc * kSB2 + warp * 16 + fr;
       const double *ms = Ms + st * kMS + fc * (NB + 4) + fr;
+      const int k0 = kt * kGBK;
 #pragma unroll
       for (int ks = 0; ks < kGBK; ks += 4) {
         double av[2], bv[NJ];
@@ -835,9 +839,12 @@ __global__ void __launch_bounds__(kBT + 32, 2)
         for (int i = 0; i < 2; ++i) av[i] = zs[ks * kSB2 + 8 * i];
 #pragma unroll
         for (int j = 0; j < NJ; ++j) bv[j] = ms[ks * (NB + 4) + 8 * j];
+        // n-tile j is all zero in L_CC^{-1} while its first column i0 + 8j
+        // exceeds the step's last row (exact zeros: skipping is bitwise free)
+        const int lmax = k0 + ks + 3 < c ? k0 + ks + 3 - i0 : NB;
 #pragma unroll
         for (int j = 0; j < NJ; ++j)
-          if (j < njv) {
+          if (j < njv && 8 * j <= lmax) {
 #pragma unroll
             for (int i = 0; i < 2; ++i) dmma884(acc[i][j][0], acc[i][j][1], av[i], bv[j]);
           }
