@@ -586,6 +586,25 @@ int pf_poisson_finalize(double *P, int64_t ldp, int64_t row0, int64_t n, int64_t
                         const uint8_t *is_boundary, const int32_t *bcol, double clamp, double *H,
                         double *min_out, unsigned long long *out_max, pf_stream_t stream);
 
+/* Finalize without a second pass over P (bare builds, no fused K1): the
+ * residual pass also writes, per interior row r (P row index, rowoff / ldp)
+ * and 512-column chunk c, row_part[r * ceil(k / PF_RESIDUAL_COLS) + c] = the
+ * chunk's sum of the row's entries, and sets out_max[2] = 1 if any such entry
+ * is negative (out_max: 3 words; [0] the residual as above).  Then
+ * pf_poisson_finalize_rows writes the boundary indicator rows, zero pads and
+ * out_max[0] = max |row sum - 1| over interior rows (sums over the chunks in
+ * order).  When out_max[2] is set the clip of solvers.py:293-296 may apply:
+ * run pf_poisson_finalize instead (it clips and re-sums). */
+#define PF_RESIDUAL_COLS 512
+int pf_poisson_residual_rows(const double *P, int64_t ldp, int64_t k, const int32_t *order,
+                             int64_t count, const int64_t *rowoff, const int64_t *nb_ptr,
+                             const int64_t *nrow, const double *off, const double *diag,
+                             double *row_part, unsigned long long *out_max, pf_stream_t stream);
+int pf_poisson_finalize_rows(double *P, int64_t ldp, int64_t row0, int64_t n, int64_t k,
+                             const uint8_t *is_boundary, const int32_t *bcol,
+                             const double *row_part, unsigned long long *out_max,
+                             pf_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -113,6 +113,10 @@ _SIGS.update({
                             c_vp],
     "pf_poisson_finalize": [c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_dbl, c_vp, c_vp,
                             c_vp, c_vp],
+    "pf_poisson_residual_rows": [c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                 c_vp, c_vp, c_vp],
+    "pf_poisson_finalize_rows": [c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp,
+                                 c_vp],
 })
 _RESTYPES = {"pf_last_error": ctypes.c_char_p, "pf_nd_plan_free": None,
              "pf_nd_plan_array": ctypes.c_int64}

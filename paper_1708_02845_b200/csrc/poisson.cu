@@ -883,6 +883,21 @@ __device__ __forceinline__ void atomic_max_nonneg(unsigned long long *p, double 
 // 512-column chunks; columns go in 16-byte pairs.
 constexpr int kResCols = 512;
 
+// Per (row, column chunk): the warp's partial row sum (lane partials, then
+// the butterfly sum: deterministic) into row_part[row * chunks + chunk], and
+// the negative-entry flag into out[2].
+__device__ __forceinline__ void residual_row_done(double *row_part, int64_t row,
+                                                  unsigned chunks, double rs, bool neg,
+                                                  unsigned long long *out) {
+  if (!row_part) return;
+  rs = warp_sum(rs);
+  const bool any = __any_sync(0xffffffffu, neg);
+  if ((threadIdx.x & 31) == 0) {
+    row_part[row * chunks + blockIdx.y] = rs;
+    if (any) atomicOr(out + 2, 1ull);
+  }
+}
+
 template <int WARPS>
 __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32))
     residual_kernel(const double *__restrict__ P, int64_t ldp, int64_t k,
@@ -890,7 +905,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32))
                     const int64_t *__restrict__ rowoff,
                     const int64_t *__restrict__ nb_ptr, const int64_t *__restrict__ nrow,
                     const double *__restrict__ off, const double *__restrict__ diag,
-                    unsigned long long *out) {
+                    double *__restrict__ row_part, unsigned long long *out) {
   // Neighbour rows are gathered in unrolled groups of 8 (all loads in flight
   // before the FMAs; missing slots point at row v with weight 0); boundary
   // neighbours add their weight to one column each, in a separate short list.
@@ -909,15 +924,23 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32))
     const int64_t e0 = nb_ptr[v];
     const int deg = (int)(nb_ptr[v + 1] - e0);
     const double dv = diag[v];
+    // optional finalize work on the row's own entries (already loaded): the
+    // chunk's partial row sum and whether any entry is negative (the clip)
+    double rs = 0.0;
+    bool neg = false;
     if (deg > kMaxDeg) {  // exact per-column evaluation for a (rare) high-valence row
       for (int64_t j = j0 + lane; j < j1; j += 32) {
-        double acc = dv * P[vo + j];
+        const double pj = P[vo + j];
+        rs += pj;
+        neg |= pj < 0.0;
+        double acc = dv * pj;
         for (int64_t e = e0; e < e0 + deg; ++e) {
           const int64_t ro = nrow[e];
           acc += off[e] * (ro >= 0 ? P[ro + j] : (-1 - ro == j ? 1.0 : 0.0));
         }
         mx = fmax(mx, fabs(acc));
       }
+      residual_row_done(row_part, vo / ldp, gridDim.y, rs, neg, out);
       continue;
     }
     __syncwarp();
@@ -963,9 +986,15 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32))
           if (b == j) a0 += bw[w][q];
           if (b == j + 1) a1 += bw[w][q];
         }
+        // row-sum work after the loads are in flight (the odd tail's partner
+        // is a pad column)
+        const bool two = j + 1 < k;
+        rs += two ? pv.x + pv.y : pv.x;
+        neg |= pv.x < 0.0 || (two && pv.y < 0.0);
         mx = fmax(mx, fabs(a0));
-        if (j + 1 < k) mx = fmax(mx, fabs(a1));
+        if (two) mx = fmax(mx, fabs(a1));
       }
+      residual_row_done(row_part, vo / ldp, gridDim.y, rs, neg, out);
       continue;
     }
     const int ngroups = (deg + kG - 1) / kG;
@@ -989,9 +1018,13 @@ __global__ void __launch_bounds__(WARPS * 32, 1024 / (WARPS * 32))
         if (b == j) a0 += bw[w][q];
         if (b == j + 1) a1 += bw[w][q];
       }
+      const bool two = j + 1 < k;
+      rs += two ? pv.x + pv.y : pv.x;
+      neg |= pv.x < 0.0 || (two && pv.y < 0.0);
       mx = fmax(mx, fabs(a0));
-      if (j + 1 < k) mx = fmax(mx, fabs(a1));
+      if (two) mx = fmax(mx, fabs(a1));
     }
+    residual_row_done(row_part, vo / ldp, gridDim.y, rs, neg, out);
   }
   mx = warp_max(mx);
   if (lane == 0) atomic_max_nonneg(out, mx);
@@ -1087,6 +1120,38 @@ __global__ void finalize_kernel(double *P, int64_t ldp, int64_t row0, int64_t n,
       } while (old != assumed);
     }
   }
+}
+
+// Finalize without a second pass over P (after residual_kernel filled
+// row_part): boundary rows -> indicators, pad columns -> 0, max |row sum - 1|
+// with each interior row's sum taken over its chunk partials in chunk order.
+// (The clip of (-1e-12, 0) cannot apply: the caller runs finalize_kernel when
+// the residual pass flagged a negative entry.)
+__global__ void finalize_rows_kernel(double *P, int64_t ldp, int64_t row0, int64_t n, int64_t k,
+                                     const uint8_t *__restrict__ isb,
+                                     const int32_t *__restrict__ bcol,
+                                     const double *__restrict__ row_part, int chunks,
+                                     unsigned long long *out) {
+  const int lane = threadIdx.x % 32;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
+  double mx = 0.0;
+  for (int64_t v = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32; v < n;
+       v += warps) {
+    double *row = P + v * ldp;
+    if (isb[row0 + v]) {
+      const int32_t b = bcol[row0 + v];
+      for (int64_t j = lane; j < ldp; j += 32) row[j] = (j == b) ? 1.0 : 0.0;
+      continue;  // sums to exactly 1
+    }
+    for (int64_t j = k + lane; j < ldp; j += 32) row[j] = 0.0;
+    if (lane == 0) {
+      double sum = 0.0;
+      for (int c = 0; c < chunks; ++c) sum += row_part[v * chunks + c];
+      mx = fmax(mx, fabs(sum - 1.0));
+    }
+  }
+  mx = warp_max(mx);
+  if (lane == 0) atomic_max_nonneg(out, mx);
 }
 
 int grid_for(int64_t work, int per_block) {
@@ -1222,23 +1287,54 @@ int pf_poisson_residual_table(const int32_t *nb_idx, int64_t nnz, const uint8_t 
   return check_launch("pf_poisson_residual_table");
 }
 
-int pf_poisson_residual(const double *P, int64_t ldp, int64_t k, const int32_t *order,
-                        int64_t count, const int64_t *rowoff, const int64_t *nb_ptr,
-                        const int64_t *nrow, const double *off, const double *diag,
-                        unsigned long long *out_max, pf_stream_t stream) {
+static int residual_launch(const char *what, const double *P, int64_t ldp, int64_t k,
+                           const int32_t *order, int64_t count, const int64_t *rowoff,
+                           const int64_t *nb_ptr, const int64_t *nrow, const double *off,
+                           const double *diag, double *row_part, unsigned long long *out_max,
+                           pf_stream_t stream) {
   if (count == 0) return 0;  // a row slab with no interior rows
   if (!P || !order || !nb_ptr || !nrow || !off || !diag || !out_max || k < 0 || count < 0 ||
       ldp < k || (ldp & 1) || (reinterpret_cast<uintptr_t>(P) & 15))
-    return fail(PF_E_ARG, "pf_poisson_residual: bad argument (ldp even, P 16-byte aligned)");
-  if (count == 0) return 0;
+    return fail(PF_E_ARG, "%s: bad argument (ldp even, P 16-byte aligned)", what);
   // (32-warp CTAs over consecutive nested-dissection rows measured slower: 19.1
   // vs 17.7 ms at C4 — the kernel is bound by L2 traffic, ~9 reads per entry)
   constexpr int kW = 8;
   const unsigned chunks = (unsigned)((k + kResCols - 1) / kResCols);
   const unsigned rows = (unsigned)std::min<int64_t>((count + kW - 1) / kW, (int64_t)sm_count() * 8);
   residual_kernel<kW><<<dim3(rows, std::max(1u, chunks)), kW * 32, 0, as_stream(stream)>>>(
-      P, ldp, k, order, count, rowoff, nb_ptr, nrow, off, diag, out_max);
-  return check_launch("pf_poisson_residual");
+      P, ldp, k, order, count, rowoff, nb_ptr, nrow, off, diag, row_part, out_max);
+  return check_launch(what);
+}
+
+int pf_poisson_residual(const double *P, int64_t ldp, int64_t k, const int32_t *order,
+                        int64_t count, const int64_t *rowoff, const int64_t *nb_ptr,
+                        const int64_t *nrow, const double *off, const double *diag,
+                        unsigned long long *out_max, pf_stream_t stream) {
+  return residual_launch("pf_poisson_residual", P, ldp, k, order, count, rowoff, nb_ptr, nrow,
+                         off, diag, nullptr, out_max, stream);
+}
+
+int pf_poisson_residual_rows(const double *P, int64_t ldp, int64_t k, const int32_t *order,
+                             int64_t count, const int64_t *rowoff, const int64_t *nb_ptr,
+                             const int64_t *nrow, const double *off, const double *diag,
+                             double *row_part, unsigned long long *out_max, pf_stream_t stream) {
+  if (!row_part && count > 0) return fail(PF_E_ARG, "pf_poisson_residual_rows: row_part is NULL");
+  return residual_launch("pf_poisson_residual_rows", P, ldp, k, order, count, rowoff, nb_ptr,
+                         nrow, off, diag, row_part, out_max, stream);
+}
+
+int pf_poisson_finalize_rows(double *P, int64_t ldp, int64_t row0, int64_t n, int64_t k,
+                             const uint8_t *is_boundary, const int32_t *bcol,
+                             const double *row_part, unsigned long long *out_max,
+                             pf_stream_t stream) {
+  if (!P || !is_boundary || !bcol || !out_max || (n > 0 && !row_part) || n < 0 || k < 0 ||
+      row0 < 0 || ldp < k)
+    return fail(PF_E_ARG, "pf_poisson_finalize_rows: bad argument");
+  if (n == 0) return 0;
+  const int chunks = (int)((k + kResCols - 1) / kResCols);
+  finalize_rows_kernel<<<grid_for(n * 32, 256), 256, 0, as_stream(stream)>>>(
+      P, ldp, row0, n, k, is_boundary, bcol, row_part, std::max(1, chunks), out_max);
+  return check_launch("pf_poisson_finalize_rows");
 }
 
 int pf_poisson_finalize(double *P, int64_t ldp, int64_t row0, int64_t n, int64_t k,

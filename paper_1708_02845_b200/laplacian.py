@@ -24,9 +24,12 @@ Mirrors the preprocessing the reference runs before the hot path:
        (``pf_mf_backward_level``) — P is produced in place, in the device
        layout of :class:`~._device.DeviceKernel` (row-major, ``ld =
        round_up(k, 16)``), so the divergence kernels use it without a copy,
-    5. ``pf_poisson_finalize``: boundary indicator rows, the reference's clip
-       of tiny negatives (``-1e-12 < P < 0 -> 0``), ``residual`` and
-       ``row_sum_error``.
+    5. ``pf_poisson_residual_rows`` + ``pf_poisson_finalize_rows``:
+       ``residual`` and, on the same read of each row, the chunk row sums;
+       then boundary indicator rows, zero pads and ``row_sum_error`` — or,
+       when K1 is fused or a negative entry makes the reference's clip of
+       tiny negatives (``-1e-12 < P < 0 -> 0``) possible,
+       ``pf_poisson_finalize``'s full pass.
 
   ``-Lc_II`` is a symmetric M-matrix on Delaunay meshes, so its Cholesky
   factor has non-positive off-diagonals and every term of both triangular
@@ -56,6 +59,7 @@ _STATS = ("n", "m", "k", "nodes", "levels", "f_total", "v_total", "nnz_l", "flop
 LEAF = 64   # leaf sub-domain size of the dissection
 KL_CLAMP = 1e-300  # divergence.py:82-83 (the H the fused K1 precomputes)
 TILE = 64   # column tile of the multi-RHS solves (pf_mf_plan_t.tile)
+RESIDUAL_COLS = 512  # PF_RESIDUAL_COLS: column chunk of the residual pass
 
 
 def vertex_neighbors(triangles, n: int):
@@ -449,23 +453,34 @@ class DevicePoisson:
                      rb.data_ptr(), cb0.data_ptr(), cb1.data_ptr(), cnt, maxf, ncb, nbr,
                      Pbuf.data_ptr(), ld, s)
         mark("bwd1")
-        mx = t.zeros(2, dtype=t.int64, device=self.device)
+        mx = t.zeros(4, dtype=t.int64, device=self.device)  # residual, row sums, neg flag
         dm = self.dm
         nrow = self._residual_table(ld, rowoff)
-        nat.call("pf_poisson_residual", Pbuf.data_ptr(), ld, self.k, order.data_ptr(), count,
-                 nat.ptr(rowoff), dm.nb_ptr.data_ptr(), nrow.data_ptr(), off.data_ptr(),
-                 diag.data_ptr(), mx.data_ptr(), s)
         # fused K1: the KL negentropy per row (clamp 1e-300) and min(P), so the
         # first field on this P does not stream it again
         H = t.empty(rows, dtype=t.float64, device=self.device) if fuse_h else None
         mn = t.full((1,), float("inf"), dtype=t.float64, device=self.device) if fuse_h else None
-        nat.call("pf_poisson_finalize", Pbuf.data_ptr(), ld, row0, rows, self.k,
-                 self.is_boundary.data_ptr(), self.bcol.data_ptr(), KL_CLAMP, nat.ptr(H),
-                 nat.ptr(mn), mx.data_ptr() + 8, s)
+        resargs = (Pbuf.data_ptr(), ld, self.k, order.data_ptr(), count, nat.ptr(rowoff),
+                   dm.nb_ptr.data_ptr(), nrow.data_ptr(), off.data_ptr(), diag.data_ptr())
+        finargs = (Pbuf.data_ptr(), ld, row0, rows, self.k, self.is_boundary.data_ptr(),
+                   self.bcol.data_ptr())
+        if fuse_h:  # the K1 pass reads every entry anyway: it also finalizes
+            nat.call("pf_poisson_residual", *resargs, mx.data_ptr(), s)
+            nat.call("pf_poisson_finalize", *finargs, KL_CLAMP, nat.ptr(H), nat.ptr(mn),
+                     mx.data_ptr() + 8, s)
+        else:  # row sums ride on the residual's read of each row: no second pass
+            part = t.empty(max(rows * (-(-self.k // RESIDUAL_COLS)), 1), dtype=t.float64,
+                           device=self.device)
+            nat.call("pf_poisson_residual_rows", *resargs, part.data_ptr(), mx.data_ptr(), s)
+            nat.call("pf_poisson_finalize_rows", *finargs, part.data_ptr(), mx.data_ptr() + 8, s)
         self.last_H, self.last_min = H, mn
         mark("end")
         del O, Wb
         r = mx.cpu().numpy().astype(np.uint64)
+        if r[2]:  # a negative entry: the reference's clip may apply (full finalize)
+            mx[1] = 0
+            nat.call("pf_poisson_finalize", *finargs, KL_CLAMP, None, None, mx.data_ptr() + 8, s)
+            r = mx.cpu().numpy().astype(np.uint64)
         residual = _u64_to_f64(int(r[0])) if count else 0.0
         return Pbuf[:rows], residual, _u64_to_f64(int(r[1]))
 

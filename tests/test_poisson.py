@@ -262,6 +262,34 @@ def test_row_slab_builds_bitwise(name, parts):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("name", ["c1", "holes_fine"])
+def test_row_sums_ride_on_the_residual_pass(name):
+    """A bare solve() takes row_sum_error from the residual pass's chunk sums
+    (no second read of P): bitwise the same P as the fused-K1 build, the same
+    residual, a row_sum_error within summation-order noise of the full
+    finalize's, and per-slab maxima equal to the whole build's."""
+    from paper_1708_02845_b200.laplacian import DevicePoisson
+    c = case(name)
+    dp = DevicePoisson(c.mesh)
+    Pf, res_f, rse_f = dp.solve(fuse_h=True)
+    Pf = Pf.cpu().numpy()
+    P, res, rse = dp.solve()
+    assert np.array_equal(P.cpu().numpy().view(np.int64), Pf.view(np.int64))
+    assert res == res_f and abs(rse - rse_f) < 1e-14 and rse < 1e-12
+    bounds = np.linspace(0, dp.n, 4).astype(int)
+    got = [dp.solve(slab=(int(a), int(b - a)))[1:] for a, b in zip(bounds[:-1], bounds[1:])]
+    assert max(g[0] for g in got) == res and max(g[1] for g in got) == rse
+
+
+def test_residual_chunk_matches_header():
+    import re
+    from paper_1708_02845_b200.laplacian import RESIDUAL_COLS
+    from tests.conftest import ROOT
+    hdr = (ROOT / "include" / "pathfield_b200.h").read_text()
+    assert int(re.search(r"#define PF_RESIDUAL_COLS (\d+)", hdr).group(1)) == RESIDUAL_COLS
+
+
+@pytest.mark.gpu
 def test_sharded_field_from_mesh_world1():
     """ShardedField.from_mesh over a 1-rank NCCL group: the whole P, bitwise the
     single-GPU build, and a field through the sharded API equal to dv_field."""
