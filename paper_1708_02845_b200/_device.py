@@ -64,7 +64,7 @@ class DeviceKernel:
 
     def __init__(self, dense: np.ndarray | None, boundary, *, device=None, row0: int = 0,
                  rows: int | None = None, n: int | None = None, k: int | None = None,
-                 P_dev=None, chunk_rows: int = 65536):
+                 P_dev=None):
         t = require_cuda()
         self.device = (t.device(device) if device is not None
                        else t.device("cuda", t.cuda.current_device()))
@@ -88,10 +88,8 @@ class DeviceKernel:
             self.P = t.empty((self.rows, self.ld), dtype=t.float64, device=self.device)
             if self.ld > self.k:
                 self.P[:, self.k:] = 0.0  # pad columns are zero (K7 streams whole 16-col tiles)
-            for a in range(0, self.rows, chunk_rows):
-                b = min(self.rows, a + chunk_rows)
-                src = np.array(dense[self.row0 + a:self.row0 + b], dtype=np.float64, order="C")
-                self.P[a:b, :self.k].copy_(t.from_numpy(src))
+            from ._hostpool import upload_rows
+            upload_rows(t, self.P, dense, self.row0)
         interior = np.ones(self.n, dtype=np.uint8)
         if boundary is not None and len(boundary):
             interior[np.asarray(boundary, dtype=np.int64)] = 0

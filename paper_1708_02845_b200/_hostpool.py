@@ -43,3 +43,59 @@ def to_host(t, dbuf, stream) -> np.ndarray:
     arr = host.numpy()
     weakref.finalize(arr, _give_back, key, host)
     return arr
+
+
+# -- host -> device row upload ------------------------------------------------
+_UPLOAD_CHUNK_BYTES = 64 << 20
+_UPLOAD_BUFFERS = 3
+_upload_pool = None
+
+
+def _threads():
+    global _upload_pool
+    if _upload_pool is None:
+        import os
+        from concurrent.futures import ThreadPoolExecutor
+        _upload_pool = ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1),
+                                          thread_name_prefix="pf-upload")
+    return _upload_pool
+
+
+def upload_rows(t, dst, src: np.ndarray, row0: int = 0) -> None:
+    """``dst[:, :k] = src[row0:row0+rows]`` for a (rows, >=k) device tensor.
+
+    The reference's P is a pageable numpy array (``solvers.py:251-252``).  A plain
+    ``copy_`` from pageable memory runs at the driver's bounce-buffer rate; here the
+    rows go through ``_UPLOAD_BUFFERS`` pinned staging buffers instead: host threads
+    fill buffer i+1 (``np.copyto`` releases the GIL) while the DMA of buffer i runs
+    on a side stream, and a buffer is refilled only after its copy's event.
+    """
+    rows, k = int(dst.shape[0]), int(src.shape[1])
+    if rows == 0:
+        return
+    chunk = max(1, _UPLOAD_CHUNK_BYTES // (8 * k))
+    nbuf = min(_UPLOAD_BUFFERS, -(-rows // chunk))
+    bufs = [t.empty((chunk, k), dtype=t.float64, pin_memory=True) for _ in range(nbuf)]
+    views = [b.numpy() for b in bufs]
+    done = [None] * nbuf
+    stream = t.cuda.Stream(device=dst.device)
+    pool = _threads()
+    nthr = pool._max_workers
+    with t.cuda.stream(stream):
+        for i, a in enumerate(range(0, rows, chunk)):
+            b = min(rows, a + chunk)
+            j = i % nbuf
+            if done[j] is not None:
+                done[j].synchronize()
+            hv = views[j]
+            step = -(-(b - a) // nthr)
+            futs = [pool.submit(np.copyto, hv[s:min(b - a, s + step)],
+                                src[row0 + a + s:row0 + min(b, a + s + step)])
+                    for s in range(0, b - a, step)]
+            for f in futs:
+                f.result()
+            dst[a:b, :k].copy_(bufs[j][:b - a], non_blocking=True)
+            ev = t.cuda.Event()
+            ev.record(stream)
+            done[j] = ev
+    stream.synchronize()

@@ -184,3 +184,26 @@ def test_one_vs_many_slabs_bitwise():
             del st
     np.testing.assert_array_equal(np.concatenate(parts_kl), full)
     np.testing.assert_array_equal(np.concatenate(parts_tv), tv_full)
+
+
+@pytest.mark.parametrize("rows,k,row0", [(1, 7, 0), (5000, 4250, 0), (3000, 33, 1234),
+                                         (70000, 130, 17)])
+def test_staged_upload_bitwise(rows, k, row0):
+    """_hostpool.upload_rows: pinned staging with several chunks and buffer reuse, padded
+    leading dimension, a row offset, a non-float64 source (cast as np.array did)."""
+    import torch as t
+    from paper_1708_02845_b200 import _hostpool
+    rng = np.random.default_rng(rows + k)
+    host = rng.random((row0 + rows, k))
+    old = _hostpool._UPLOAD_CHUNK_BYTES
+    _hostpool._UPLOAD_CHUNK_BYTES = 1 << 20     # force many chunks through 3 buffers
+    try:
+        for src in (host, host.astype(np.float32)):
+            ld = dev.leading_dim(k)
+            P = t.full((rows, ld), -1.0, dtype=t.float64, device="cuda")
+            _hostpool.upload_rows(t, P, src, row0)
+            got = P.cpu().numpy()
+            assert np.array_equal(got[:, :k], src[row0:].astype(np.float64))
+            assert (got[:, k:] == -1.0).all()
+    finally:
+        _hostpool._UPLOAD_CHUNK_BYTES = old
