@@ -207,10 +207,12 @@ int pf_csr_target_prep_f64(const int64_t *indptr, const int32_t *indices,
  * divergence.py:226,277).  Split form hs[q] - sum v logt with a cancellation
  * guard re-evaluated in the reference form; then _settle (:286).
  * ops[i] = |supp(q)| (:276) if ops != NULL; flags[PF_FLAG_GUARDED] counts
- * re-evaluated rows.  With `queue` (capacity: one int64 per output row, and
- * flags[PF_FLAG_GUARDED] zero on entry, as pf_target_prep_f64 leaves it) the
- * field kernel appends guarded rows to it and the re-evaluation visits only
- * those; with queue == NULL it scans the whole output for the guard sentinel. */
+ * re-evaluated rows.  With `queue` non-NULL (flags[PF_FLAG_GUARDED] zero on
+ * entry, as pf_target_prep_f64 leaves it) the field kernel re-evaluates a guarded
+ * row in place, with the target logs already in shared memory (one launch; the
+ * buffer itself is no longer written and may be any non-NULL pointer); with
+ * queue == NULL a second pass scans the output for the guard sentinel.  Both
+ * re-evaluate in the same order, so the results are identical. */
 int pf_csr_kl_f64(const int64_t *indptr, const int32_t *indices, const double *data,
                   const double *log_data, const double *hs, int64_t rows, int64_t k,
                   const double *logt, double tau, int64_t row0, const int64_t *queries,

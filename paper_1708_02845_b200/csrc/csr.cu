@@ -240,9 +240,10 @@ __device__ __forceinline__ const double *stage_vec(unsigned char *smem, const do
 template <bool STAGE, class Idx>
 __global__ void __launch_bounds__(kCsrThreads) csr_kl_kernel(
     const int64_t *__restrict__ indptr, const Idx *__restrict__ indices,
-    const double *__restrict__ data, const double *__restrict__ hs, int64_t rows, int64_t k_pad,
+    const double *__restrict__ data, const double *__restrict__ log_data,
+    const double *__restrict__ hs, int64_t rows, int64_t k_pad,
     const double *__restrict__ logt, double tau, int64_t row0, const int64_t *__restrict__ queries,
-    int64_t nq, double *__restrict__ out, int64_t *__restrict__ ops, int64_t *__restrict__ queue,
+    int64_t nq, double *__restrict__ out, int64_t *__restrict__ ops, bool fix_inline,
     uint32_t *__restrict__ flags) {
   extern __shared__ __align__(128) unsigned char smem[];
   const double *lt = STAGE ? stage_vec(smem, logt, k_pad) : logt;
@@ -269,15 +270,29 @@ __global__ void __launch_bounds__(kCsrThreads) csr_kl_kernel(
     });
     const double cross = warp_sum(a0 + a1);
     double val = h - cross;
-    const bool guarded = fabs(val) < tau * (fabs(h) + fabs(cross));
-    if (guarded)
+    const bool guarded = fabs(val) < tau * (fabs(h) + fabs(cross));  // warp-uniform
+    if (guarded && fix_inline) {
+      // reference form sum v * (log v - logPt) (divergence.py:279) right here, the
+      // target logs already in shared memory: the order of csr_kl_fixup_kernel, so
+      // the field and the dv_at / pair paths agree bitwise on guarded rows
+      double b0 = 0.0, b1 = 0.0;
+      int64_t e = lo + lane;
+      for (; e + 32 < hi; e += 64) {
+        b0 += __dmul_rn(__ldg(data + e), __ldg(log_data + e) - lt[__ldg(indices + e)]);
+        b1 += __dmul_rn(__ldg(data + e + 32),
+                        __ldg(log_data + e + 32) - lt[__ldg(indices + e + 32)]);
+      }
+      if (e < hi) b0 += __dmul_rn(__ldg(data + e), __ldg(log_data + e) - lt[__ldg(indices + e)]);
+      val = settle(warp_sum(b0 + b1));
+    } else if (guarded) {
       val = __longlong_as_double(static_cast<long long>(kCsrGuard));
-    else
+    } else {
       val = settle(val);  // divergence.py:286
+    }
     if (lane == 0) {
       out[i] = val;
       if (ops) ops[i] = hi - lo;  // divergence.py:276
-      if (guarded && queue) queue[atomicAdd(&flags[PF_FLAG_GUARDED], 1u)] = i;
+      if (guarded && fix_inline) atomicAdd(&flags[PF_FLAG_GUARDED], 1u);
     }
     i = i2;
     r = r2;
@@ -324,59 +339,6 @@ __global__ void __launch_bounds__(kCsrThreads) csr_kl_fixup_kernel(
     }
   }
   if (lane == 0 && done && flags) atomicAdd(&flags[PF_FLAG_GUARDED], done);
-}
-
-// Guarded rows from the queue K5 filled (count in flags[PF_FLAG_GUARDED]):
-// warp per row, reference form as csr_kl_fixup_kernel.  Guarded rows are few
-// but each is a chain of dependent loads (index -> logt gather), so a warp
-// takes its row 512 entries at a time with every load of the chunk in flight
-// before the gathers (row starts are even in the device CSR: aligned pairs).
-template <class Idx>
-__global__ void __launch_bounds__(kCsrThreads) csr_kl_fixup_queue_kernel(
-    const int64_t *__restrict__ indptr, const Idx *__restrict__ indices,
-    const double *__restrict__ data, const double *__restrict__ log_data,
-    const double *__restrict__ logt, int64_t row0, const int64_t *__restrict__ queries,
-    const int64_t *__restrict__ queue, const uint32_t *__restrict__ flags,
-    double *__restrict__ out) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t n = flags[PF_FLAG_GUARDED];
-  for (int64_t jq = warp; jq < n; jq += nwarps) {
-    const int64_t i = queue[jq];
-    const int64_t r = queries ? queries[i] - row0 : i;
-    int64_t lo, hi;
-    row_extent(indptr, data, r, lo, hi);
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int64_t base = lo & ~int64_t{1}; base < hi; base += 512) {
-      double2 dv[8], lv[8];
-      int2 iv[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int64_t e = base + 2 * (lane + 32 * u);
-        if (e < hi) {
-          dv[u] = __ldg(reinterpret_cast<const double2 *>(data + e));
-          lv[u] = __ldg(reinterpret_cast<const double2 *>(log_data + e));
-          iv[u] = idx_pair(indices, e, 0);
-        }
-      }
-      double tx[8], ty[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int64_t e = base + 2 * (lane + 32 * u);
-        tx[u] = (e >= lo && e < hi) ? __ldg(logt + iv[u].x) : 0.0;
-        ty[u] = (e + 1 >= lo && e + 1 < hi) ? __ldg(logt + iv[u].y) : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int64_t e = base + 2 * (lane + 32 * u);
-        if (e >= lo && e < hi) acc[u & 3] += __dmul_rn(dv[u].x, lv[u].x - tx[u]);
-        if (e + 1 >= lo && e + 1 < hi) acc[u & 3] += __dmul_rn(dv[u].y, lv[u].y - ty[u]);
-      }
-    }
-    const double val = settle(warp_sum((acc[0] + acc[1]) + (acc[2] + acc[3])));
-    if (lane == 0) out[i] = val;
-  }
 }
 
 // ------------------------------------------------------------ K6 CSR TV --
@@ -556,7 +518,8 @@ int csr_kl_launch(const int64_t *indptr, const Idx *indices, const double *data,
                   const double *logt, double tau, int64_t row0, const int64_t *queries,
                   int64_t nq, double *out, int64_t *ops, uint32_t *flags, int64_t *queue,
                   pf_stream_t stream) {
-  if (queue && !flags) return fail(PF_E_ARG, "csr_kl: the guard queue needs flags");
+  if (queue && (!flags || !log_data))
+    return fail(PF_E_ARG, "csr_kl: in-place guard re-evaluation needs flags and log_data");
   if (!indptr || !indices || !hs || !logt || !out || rows < 0 || k <= 0)
     return fail(PF_E_ARG, "csr_kl: bad args");
   const int64_t count = queries ? nq : rows;
@@ -568,20 +531,16 @@ int csr_kl_launch(const int64_t *indptr, const Idx *indices, const double *data,
     if (int e = smem_attr(csr_kl_kernel<true, Idx>, smem)) return e;
     const int g = grid_for((const void *)csr_kl_kernel<true, Idx>, kCsrThreads, smem, count);
     csr_kl_kernel<true, Idx><<<g, kCsrThreads, smem, as_stream(stream)>>>(
-        indptr, indices, data, hs, rows, k_pad, logt, tau, row0, queries, nq, out, ops, queue,
-        flags);
+        indptr, indices, data, log_data, hs, rows, k_pad, logt, tau, row0, queries, nq, out,
+        ops, queue != nullptr, flags);
   } else {
     const int g = grid_for((const void *)csr_kl_kernel<false, Idx>, kCsrThreads, 0, count);
     csr_kl_kernel<false, Idx><<<g, kCsrThreads, 0, as_stream(stream)>>>(
-        indptr, indices, data, hs, rows, k_pad, logt, tau, row0, queries, nq, out, ops, queue,
-        flags);
+        indptr, indices, data, log_data, hs, rows, k_pad, logt, tau, row0, queries, nq, out,
+        ops, queue != nullptr, flags);
   }
   if (int e = check_launch("csr_kl")) return e;
-  if (queue) {
-    csr_kl_fixup_queue_kernel<Idx><<<sm_count() * 2, kCsrThreads, 0, as_stream(stream)>>>(
-        indptr, indices, data, log_data, logt, row0, queries, queue, flags, out);
-    return check_launch("csr_kl_fixup_queue");
-  }
+  if (queue) return 0;  // guarded rows were fixed inline
   int64_t want = (count + 7) / 8;
   int64_t g2 = static_cast<int64_t>(sm_count()) * 4;
   if (g2 > want) g2 = want;

@@ -303,7 +303,7 @@ def _compute_sparse_slab(slab, fd, p: int, payload, cut: float, strict: bool):
         nat.call(entry, dc.indptr.data_ptr(), idx, dc.data.data_ptr(),
                  dc.log_data.data_ptr(), dc.hs.data_ptr(), slab.rows, slab.k, st.logt,
                  KL_GUARD_TAU, slab.row0, 0, slab.rows, out.data_ptr(), 0, flags,
-                 slab.scratch(s, 8 * slab.rows, "csrq").data_ptr(), s)
+                 slab.scratch(s, 8, "csrq").data_ptr(), s)
     else:
         kp = slab.k + (slab.k & 1)
         entry, idx = dc.field_entry("tv")

@@ -202,3 +202,34 @@ def test_u16_columns_bitwise_equal_int32(name):
             dc.indices16 = saved
         assert np.array_equal(a.view(np.int64), b.view(np.int64)), g
     del t
+
+
+def test_csr_kl_guard_in_place():
+    """Rows that nearly repeat the target's make hs[q] - sum v logPt cancel; K5 must
+    re-evaluate them (in place, in the field kernel) in the reference form: values
+    within 1e-10 of the oracle, the guard counter equal to the rows that fired, and the
+    field path equal bitwise to the query path (dv_at-style launch, same order)."""
+    import torch as t
+    from paper_1708_02845_b200 import divergence as D
+    n, k, p = 2048, 512, 100
+    dense = I.synthetic_kernel(n, k, seed=3)
+    # near-duplicates far enough apart that one-ulp differences between the device's
+    # and numpy's log stay below 1e-10 of the distance (KL >= ~1e-6)
+    for j, eps in enumerate([0.0, 1e-2, -1e-2, 3e-2, 5e-2, 1e-1, -1e-1, 0.3]):
+        row = dense[p].copy()
+        row[3::7] *= (1.0 + eps)
+        dense[200 + j] = row / row.sum()
+    pk = pf.PoissonKernel(dense, np.array([], np.int64), 0.0, 0.0)
+    spk = pf.sparsify(pk)
+    thr = 1.0 / math.sqrt(n)
+    vals, flags = D.dv_field_sparse_device(spk, pf.builtin_f("kl"), p)
+    field = vals.cpu().numpy()
+    guarded = int(flags[1].item())
+    assert guarded >= 4
+    rows = np.r_[np.arange(190, 215), [0, 1, n - 1]]
+    ref = np.array([O.dv_pair_sparse_direct(dense, p, int(q), "kl", threshold=thr)[0]
+                    for q in rows])
+    ok, err = rel_close(field[rows], ref, RTOL)
+    assert ok, err
+    for q in rows:
+        assert pf.dv_pair_sparse(spk, pf.builtin_f("kl"), p, int(q)) == field[q]
