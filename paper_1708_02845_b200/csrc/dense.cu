@@ -157,9 +157,27 @@ __host__ __device__ inline size_t staged_smem_bytes(int64_t k_pad, int64_t m_pad
   return 16 + static_cast<size_t>(k_pad) * 8 + static_cast<size_t>(m_pad);
 }
 
-// Rows whose split-form KL cancels are marked with this NaN payload and
-// re-evaluated per-element by kl_guard_fixup_kernel.
-constexpr unsigned long long kGuardSentinel = 0x7ff8dead0000beefull;
+// The reference's per-element KL form of one row, q * -log(p/q) summed
+// (divergence.py:180), one warp, then settle: used for guarded rows, by the
+// field kernel in place (one warp, warp-uniform branch; no second pass).
+__device__ __forceinline__ double kl_reference_row(const double *__restrict__ prow, int64_t k,
+                                                   const double *__restrict__ tgt, double clamp,
+                                                   int lane) {
+  double b[4] = {0.0, 0.0, 0.0, 0.0};
+  int64_t e = lane;
+  for (; e + 96 < k; e += 128) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double q = fmax(prow[e + 32 * u], clamp);
+      b[u] += __dmul_rn(q, -log(__ddiv_rn(tgt[e + 32 * u], q)));
+    }
+  }
+  for (; e < k; e += 32) {
+    const double q = fmax(prow[e], clamp);
+    b[0] += __dmul_rn(q, -log(__ddiv_rn(tgt[e], q)));
+  }
+  return settle(warp_sum((b[0] + b[1]) + (b[2] + b[3])));
+}
 
 // ------------------------------------------------------------ K2 dense KL --
 template <int U, int MINB, bool STAGE = true>
@@ -214,10 +232,13 @@ __global__ void __launch_bounds__(kThreads, MINB) dense_kl_kernel(
     const double cross = warp_sum(a0 + a1);
     double val = h - cross;
     const bool is_t = (row0 + r == target);
-    if (!is_t && fabs(val) < tau * (fabs(h) + fabs(cross)))
-      val = __longlong_as_double(static_cast<long long>(kGuardSentinel));  // -> fixup pass
-    else
+    const bool guarded = !is_t && fabs(val) < tau * (fabs(h) + fabs(cross));  // warp-uniform
+    if (guarded) {
+      val = kl_reference_row(P + r * ld, k, tgt, clamp, lane);  // in place, no second pass
+      if (lane == 0) atomicAdd(&flags[PF_FLAG_GUARDED], 1u);
+    } else {
       val = is_t ? 0.0 : settle(val);  // divergence.py:181-182
+    }
     const bool interior = is_interior ? (is_interior[r] != 0) : true;
     clamped_any |= interior && __any_sync(0xffffffffu, fl);
     if (lane == 0) out[r] = val;
@@ -278,51 +299,6 @@ __global__ void __launch_bounds__(kThreads, MINB) dense_tv_kernel(
     if (lane == 0) out[r] = val;
   }
   if (lane == 0 && clamped_any) atomicOr(&flags[PF_FLAG_CLAMPED], 1u);
-}
-
-// KL fixup: rows the KL kernel marked with the guard sentinel are
-// re-evaluated in the reference's per-element form q * -log(p/q)
-// (divergence.py:180) by one warp each; then settle.
-__global__ void __launch_bounds__(kThreads) kl_guard_fixup_kernel(
-    const double *__restrict__ P, int64_t ld, int64_t rows, int64_t k,
-    const double *__restrict__ tgt, double clamp, double *__restrict__ out,
-    uint32_t *__restrict__ flags) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  uint32_t done = 0;
-  // Rows are interleaved across warps (row = warp + (32 i + lane) * nwarps):
-  // guarded rows cluster around the target, so consecutive rows must land on
-  // different warps for the recompute to spread over the GPU.
-  for (int64_t i0 = 0; warp + i0 * nwarps < rows; i0 += 32) {
-    const int64_t mine = warp + (i0 + lane) * nwarps;
-    const bool flag = mine < rows && static_cast<unsigned long long>(__double_as_longlong(
-                                         out[mine])) == kGuardSentinel;
-    unsigned ball = __ballot_sync(0xffffffffu, flag);
-    while (ball) {
-      const int src = __ffs(ball) - 1;
-      ball &= ball - 1;
-      const int64_t r = warp + (i0 + src) * nwarps;
-      const double *prow = P + r * ld;
-      double b[4] = {0.0, 0.0, 0.0, 0.0};
-      int64_t e = lane;
-      for (; e + 96 < k; e += 128) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const double q = fmax(prow[e + 32 * u], clamp);
-          b[u] += __dmul_rn(q, -log(__ddiv_rn(tgt[e + 32 * u], q)));
-        }
-      }
-      for (; e < k; e += 32) {
-        const double q = fmax(prow[e], clamp);
-        b[0] += __dmul_rn(q, -log(__ddiv_rn(tgt[e], q)));
-      }
-      const double val = settle(warp_sum((b[0] + b[1]) + (b[2] + b[3])));
-      if (lane == 0) out[r] = val;
-      ++done;
-    }
-  }
-  if (lane == 0 && done) atomicAdd(&flags[PF_FLAG_GUARDED], done);
 }
 
 // ------------------------------------------------------ generic generator --
@@ -437,18 +413,6 @@ static int launch_dense(K staged, K unstaged, int64_t rows, int64_t k, cudaStrea
   return 0;
 }
 
-static int launch_kl_fixup(const double *P, int64_t ld, int64_t rows, int64_t k,
-                           const double *tgt, double clamp, double *out, uint32_t *flags,
-                           cudaStream_t stream) {
-  int64_t want = (rows + kWarpsPerCta - 1) / kWarpsPerCta;
-  int64_t g = static_cast<int64_t>(sm_count()) * 4;
-  if (g > want) g = want;
-  if (g < 1) g = 1;
-  kl_guard_fixup_kernel<<<static_cast<int>(g), kThreads, 0, stream>>>(P, ld, rows, k, tgt, clamp,
-                                                                       out, flags);
-  return check_launch("kl_guard_fixup");
-}
-
 static int check_dense_args(const double *P, int64_t ld, int64_t rows, int64_t k) {
   if (!P && rows > 0) return fail(PF_E_ARG, "P is null");
   if (rows < 0 || k <= 0 || ld < k) return fail(PF_E_ARG, "bad shape rows=%lld k=%lld ld=%lld",
@@ -505,8 +469,7 @@ int pf_dense_kl_f64(const double *P, int64_t ld, int64_t rows, int64_t k, const 
   kern<<<grid, kThreads, smem, as_stream(stream)>>>(P, ld, rows, k, k_pad, m_pad, H, tgt, logt,
                                                     tmask, clamp, tau, row0, target,
                                                     is_interior, out, flags);
-  if (int e = check_launch("dense_kl")) return e;
-  return launch_kl_fixup(P, ld, rows, k, tgt, clamp, out, flags, as_stream(stream));
+  return check_launch("dense_kl");  // guarded rows were re-evaluated in place
 }
 
 int pf_dense_tv_f64(const double *P, int64_t ld, int64_t rows, int64_t k, const double *tgt,

@@ -17,7 +17,7 @@
 namespace pf {
 
 constexpr int kT32 = 256;
-constexpr unsigned long long kSentinel32 = 0x7ff8dead0000beefull;  // = dense.cu kGuardSentinel
+constexpr unsigned long long kSentinel32 = 0x7ff8dead0000beefull;
 
 __device__ __forceinline__ float4 ldg_stream4f(const float4 *p) {
   float4 v;
