@@ -20,13 +20,17 @@
 // Nothing here is numeric: values stay on the device (poisson.cu) and are
 // addressed by their index in the mesh's neighbour CSR.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <future>
+#include <memory>
 #include <new>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/pathfield_b200.h"
@@ -101,12 +105,25 @@ struct Builder {
     return id;
   }
 
-  // Nested dissection of S (interior-local ids); returns the node id.
-  int32_t build(std::vector<int32_t> &S) {
+  // Nested dissection of S (interior-local ids), in two phases.  partition()
+  // splits S recursively into a tree of (C, children) and is where the time
+  // goes (a median split and a separator scan per level); below the top
+  // kParDepth levels' splits the two halves run on separate threads (they touch
+  // disjoint vertices; `side` is written per vertex).  number() then walks the
+  // tree in post-order and assigns node ids and permutation positions exactly
+  // as the sequential recursion did, so the plan is independent of threading.
+  struct Part {
+    std::vector<int32_t> C;
+    std::vector<std::unique_ptr<Part>> ch;
+  };
+  static constexpr int kParDepth = 4;  // up to 16 concurrent subtrees
+
+  std::unique_ptr<Part> partition(std::vector<int32_t> &S, int depth) {
+    auto node = std::make_unique<Part>();
     if ((int64_t)S.size() <= P.leaf) {
       // leaf: order by the wider axis for locality of the dense front
-      std::vector<int32_t> C(S);
-      return new_node(std::move(C), {});
+      node->C = S;
+      return node;
     }
     double lo[2] = {1e300, 1e300}, hi[2] = {-1e300, -1e300};
     for (int32_t v : S)
@@ -143,20 +160,65 @@ struct Builder {
       if (side[v] < 2) part[side[v]].push_back(v);
     for (int32_t v : S) side[v] = -1;
     std::vector<int32_t>().swap(S);
-    std::vector<int32_t> children;
-    for (int h = 0; h < 2; ++h)
-      if (!part[h].empty()) children.push_back(build(part[h]));
-    std::vector<int32_t> C(std::move(sep[pick]));
+    if (depth < kParDepth && !part[0].empty() && !part[1].empty()) {
+      auto left = std::async(std::launch::async,
+                             [this, &part, depth] { return partition(part[0], depth + 1); });
+      auto right = partition(part[1], depth + 1);
+      node->ch.push_back(left.get());
+      node->ch.push_back(std::move(right));
+    } else {
+      for (int h = 0; h < 2; ++h)
+        if (!part[h].empty()) node->ch.push_back(partition(part[h], depth + 1));
+    }
+    std::vector<int32_t> &C = node->C;
+    C = std::move(sep[pick]);
     std::sort(C.begin(), C.end(), [&](int32_t a, int32_t b) {
       const double ca = coord(a, 1 - axis), cb = coord(b, 1 - axis);
       return ca < cb || (ca == cb && a < b);
     });
-    return new_node(std::move(C), std::move(children));
+    return node;
+  }
+
+  int32_t number(Part &t) {
+    std::vector<int32_t> children;
+    for (auto &c : t.ch) children.push_back(number(*c));
+    t.ch.clear();
+    return new_node(std::move(t.C), std::move(children));
+  }
+
+  int32_t build(std::vector<int32_t> &S) {
+    auto root = partition(S, 0);
+    return number(*root);
   }
 };
 
 int64_t lower_pos(const std::vector<int32_t> &v, int64_t lo, int64_t hi, int32_t x) {
   return std::lower_bound(v.begin() + lo, v.begin() + hi, x) - v.begin();
+}
+
+// f(i) for i in [0, n) on up to 16 host threads, dynamically chunked (fronts
+// vary in size); sequential for small n.  f must only write what index i owns.
+template <class F>
+void parallel_for(int64_t n, F &&f) {
+  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  if (n < 2048 || hw == 1) {
+    for (int64_t i = 0; i < n; ++i) f(i);
+    return;
+  }
+  constexpr int64_t kChunk = 64;
+  std::atomic<int64_t> next{0};
+  auto work = [&] {
+    for (;;) {
+      const int64_t a = next.fetch_add(kChunk);
+      if (a >= n) return;
+      const int64_t b = std::min(n, a + kChunk);
+      for (int64_t i = a; i < b; ++i) f(i);
+    }
+  };
+  std::vector<std::thread> pool;
+  for (unsigned t = 1; t < hw; ++t) pool.emplace_back(work);
+  work();
+  for (auto &th : pool) th.join();
 }
 
 int build_plan(Plan &P, const double *xy, const int64_t *nb_ptr, const int64_t *nb_idx,
@@ -201,32 +263,37 @@ int build_plan(Plan &P, const double *xy, const int64_t *nb_ptr, const int64_t *
   // R sets (perm positions > c1), bottom-up (post-order ids)
   P.r_ptr.assign(nn + 1, 0);
   P.rn.assign(nn, 0);
-  std::vector<int32_t> mark(m, -1), tmp;
+  // R[s] = the sorted positions >= c1 coupled to C (mesh neighbours) or to the
+  // children's R; fronts of one height are independent, so each height is one
+  // parallel pass (children always have a smaller height)
   std::vector<std::vector<int32_t>> R(nn);
-  for (int32_t s = 0; s < nn; ++s) {
-    const int32_t c1 = P.c0[s] + P.cn[s];
-    tmp.clear();
-    for (int32_t v : B.node_C[s]) {
-      const int32_t o = interior[v];
-      for (int64_t e = nb_ptr[o]; e < nb_ptr[o + 1]; ++e) {
-        const int32_t u = ilocal[nb_idx[e]];
-        if (u < 0) continue;
-        const int32_t p = P.iperm[u];
-        if (p >= c1 && mark[p] != s) {
-          mark[p] = s;
-          tmp.push_back(p);
+  int32_t hmax_r = 0;
+  for (int32_t s = 0; s < nn; ++s) hmax_r = std::max(hmax_r, P.height[s]);
+  std::vector<std::vector<int32_t>> by_h(hmax_r + 1);
+  for (int32_t s = 0; s < nn; ++s) by_h[P.height[s]].push_back(s);
+  for (int32_t h = 0; h <= hmax_r; ++h) {
+    const std::vector<int32_t> &nodes = by_h[h];
+    parallel_for((int64_t)nodes.size(), [&](int64_t i) {
+      const int32_t s = nodes[i];
+      const int32_t c1 = P.c0[s] + P.cn[s];
+      std::vector<int32_t> tmp;
+      for (int32_t v : B.node_C[s]) {
+        const int32_t o = interior[v];
+        for (int64_t e = nb_ptr[o]; e < nb_ptr[o + 1]; ++e) {
+          const int32_t u = ilocal[nb_idx[e]];
+          if (u < 0) continue;
+          const int32_t p = P.iperm[u];
+          if (p >= c1) tmp.push_back(p);
         }
       }
-    }
-    for (int32_t i = P.ch_ptr[s]; i < P.ch_ptr[s + 1]; ++i)
-      for (int32_t p : R[P.ch_idx[i]])
-        if (p >= c1 && mark[p] != s) {
-          mark[p] = s;
-          tmp.push_back(p);
-        }
-    std::sort(tmp.begin(), tmp.end());
-    R[s] = tmp;
-    P.rn[s] = (int32_t)tmp.size();
+      for (int32_t j = P.ch_ptr[s]; j < P.ch_ptr[s + 1]; ++j)
+        for (int32_t p : R[P.ch_idx[j]])
+          if (p >= c1) tmp.push_back(p);
+      std::sort(tmp.begin(), tmp.end());
+      tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+      P.rn[s] = (int32_t)tmp.size();
+      R[s] = std::move(tmp);
+    });
   }
   for (int32_t s = 0; s < nn; ++s) P.r_ptr[s + 1] = P.r_ptr[s] + P.rn[s];
   P.r_pos.resize(P.r_ptr[nn]);
@@ -264,50 +331,86 @@ int build_plan(Plan &P, const double *xy, const int64_t *nb_ptr, const int64_t *
   P.relmap_off.assign(nn + 1, 0);
   for (int32_t s = 0; s < nn; ++s) P.relmap_off[s + 1] = P.relmap_off[s] + P.rn[s];
   P.relmap.resize(P.relmap_off[nn]);
-  for (int32_t s = 0; s < nn; ++s) {
+  std::atomic<int32_t> bad_rel{-1};
+  parallel_for(nn, [&](int64_t si) {
+    const int32_t s = (int32_t)si;
     const int32_t par = P.parent[s];
     for (int32_t i = 0; i < P.rn[s]; ++i) {
       const int64_t l = par >= 0 ? local(par, P.r_pos[P.r_ptr[s] + i]) : -1;
       if (l < 0) {
-        pf::set_error("nd plan: update row of node %d not in its parent front", s);
-        return PF_E_DOMAIN;
+        bad_rel.store(s);
+        return;
       }
       P.relmap[P.relmap_off[s] + i] = (int32_t)l;
     }
+  });
+  if (bad_rel.load() >= 0) {
+    pf::set_error("nd plan: update row of node %d not in its parent front", (int)bad_rel.load());
+    return PF_E_DOMAIN;
   }
-  // A entries (lower triangle of each front's C columns) and B entries
+  // A entries (lower triangle of each front's C columns) and B entries: counted,
+  // then filled per front in parallel (each front owns its slice; same order as
+  // a sequential pass)
   P.a_ptr.assign(nn + 1, 0);
   P.b_ptr.assign(nn + 1, 0);
-  for (int32_t s = 0; s < nn; ++s) {
+  std::atomic<int32_t> bad_vertex{-1};
+  auto front_entries = [&](int32_t s, bool fill) {
     const int64_t f = P.fn[s];
     const int32_t c0 = P.c0[s];
+    int64_t ia = fill ? P.a_ptr[s] : 0, ib = fill ? P.b_ptr[s] : 0;
     for (int32_t j = 0; j < P.cn[s]; ++j) {
       const int32_t p = c0 + j;
       const int32_t o = P.perm_orig[p];
-      P.a_dst.push_back(P.foff[s] + (int64_t)j * f + j);
-      P.a_src.push_back(-1 - (int64_t)o);  // diagonal of vertex o
+      if (fill) {
+        P.a_dst[ia] = P.foff[s] + (int64_t)j * f + j;
+        P.a_src[ia] = -1 - (int64_t)o;  // diagonal of vertex o
+      }
+      ++ia;
       for (int64_t e = nb_ptr[o]; e < nb_ptr[o + 1]; ++e) {
         const int64_t u = nb_idx[e];
         const int32_t ul = ilocal[u];
         if (ul < 0) {
-          P.b_row.push_back(j);
-          P.b_col.push_back(bcol[u]);
-          P.b_src.push_back(e);
+          if (fill) {
+            P.b_row[ib] = j;
+            P.b_col[ib] = bcol[u];
+            P.b_src[ib] = e;
+          }
+          ++ib;
           continue;
         }
         const int32_t pu = P.iperm[ul];
         if (pu <= p) continue;  // upper triangle / already eliminated
-        const int64_t i = local(s, pu);
-        if (i < 0) {
-          pf::set_error("nd plan: coupling of vertex %d not in its front", (int)o);
-          return PF_E_DOMAIN;
+        if (fill) {
+          const int64_t i = local(s, pu);
+          if (i < 0) {
+            bad_vertex.store(o);
+            return;
+          }
+          P.a_dst[ia] = P.foff[s] + i * f + j;
+          P.a_src[ia] = e;
         }
-        P.a_dst.push_back(P.foff[s] + i * f + j);
-        P.a_src.push_back(e);
+        ++ia;
       }
     }
-    P.a_ptr[s + 1] = (int64_t)P.a_dst.size();
-    P.b_ptr[s + 1] = (int64_t)P.b_row.size();
+    if (!fill) {
+      P.a_ptr[s + 1] = ia;
+      P.b_ptr[s + 1] = ib;
+    }
+  };
+  parallel_for(nn, [&](int64_t s) { front_entries((int32_t)s, false); });
+  for (int32_t s = 0; s < nn; ++s) {
+    P.a_ptr[s + 1] += P.a_ptr[s];
+    P.b_ptr[s + 1] += P.b_ptr[s];
+  }
+  P.a_dst.resize(P.a_ptr[nn]);
+  P.a_src.resize(P.a_ptr[nn]);
+  P.b_row.resize(P.b_ptr[nn]);
+  P.b_col.resize(P.b_ptr[nn]);
+  P.b_src.resize(P.b_ptr[nn]);
+  parallel_for(nn, [&](int64_t s) { front_entries((int32_t)s, true); });
+  if (bad_vertex.load() >= 0) {
+    pf::set_error("nd plan: coupling of vertex %d not in its front", (int)bad_vertex.load());
+    return PF_E_DOMAIN;
   }
   // active 32-column tiles of the forward solve (bottom-up union)
   P.ntiles = (k + P.ta - 1) / P.ta;

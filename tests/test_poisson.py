@@ -353,3 +353,27 @@ def test_degenerate_triangle_raises():
         interior_vertices = c.mesh.interior_vertices
     with pytest.raises(DegenerateGeometryError):
         DevicePoisson(M()).laplacian()
+
+
+def test_threaded_plan_is_the_sequential_plan():
+    """nd_plan.cpp partitions subtrees and fills the per-front scatter lists on host
+    threads; the plan must not depend on that.  The digest was taken from the
+    single-threaded implementation on the same mesh (90,601 vertices, 3,501 fronts:
+    large enough for every parallel pass to engage), and two builds must agree."""
+    import hashlib
+    from paper_1708_02845_b200 import mesh as M
+    from paper_1708_02845_b200 import laplacian as L
+    mesh = M.grid_mesh(300, 300)
+    digests = []
+    for _ in range(2):
+        pl = L.NdPlan.from_mesh(mesh)
+        h = hashlib.sha256()
+        for name in sorted(vars(pl)):
+            v = getattr(pl, name)
+            if isinstance(v, np.ndarray):
+                h.update(name.encode())
+                h.update(np.ascontiguousarray(v).tobytes())
+        digests.append(h.hexdigest())
+    assert pl.nodes == 3501
+    assert digests[0] == digests[1] == \
+        "bcb050007ab4bc93fb62a58ae04eef7ea2f0a0cf4d90d8b14b714637413705d1"
