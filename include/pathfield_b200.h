@@ -99,7 +99,8 @@ int pf_row_negentropy_f64(const double *P, int64_t ld, int64_t rows, int64_t k,
  * out[r] = sum_b c(Q_rb) * (-log(c(Pt_b)/c(Q_rb)))  for global row
  * row0 + r, evaluated as H[r] - sum_b c(Q_rb) * logt[b] with a cancellation
  * guard: rows with |out| < tau*(|H|+|cross|) are re-evaluated in the
- * reference's per-element form.  Then the settle rule (-1e-10,0) -> 0 and
+ * reference's per-element form, in place by the same launch (counted in
+ * flags[PF_FLAG_GUARDED]).  Then the settle rule (-1e-10,0) -> 0 and
  * out[target-row0] = 0.  Replaces dv_field's kl evaluation
  * (divergence.py:170-182).  flags[PF_FLAG_CLAMPED] |= one-sided clamp on a
  * row with is_interior[r] != 0 (is_interior may be NULL = all interior). */
