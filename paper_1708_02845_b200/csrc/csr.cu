@@ -236,6 +236,34 @@ __device__ __forceinline__ const double *stage_vec(unsigned char *smem, const do
   return s_vec;
 }
 
+// Reference form of one guarded CSR KL row, sum v * (log v - logPt)
+// (divergence.py:279), one warp: every load of 4 elements per lane issued
+// before the dependent logPt gathers, four accumulators, then settle.  Used in
+// place by the field kernel and by the scan fixup (same order, same bits).
+template <class Idx>
+__device__ __forceinline__ double csr_kl_reference_row(const double *__restrict__ data,
+                                                       const double *__restrict__ log_data,
+                                                       const Idx *__restrict__ indices,
+                                                       const double *__restrict__ lt,
+                                                       int64_t lo, int64_t hi, int lane) {
+  double b[4] = {0.0, 0.0, 0.0, 0.0};
+  int64_t e = lo + lane;
+  for (; e + 96 < hi; e += 128) {
+    double d[4], l[4];
+    int c[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      d[u] = __ldg(data + e + 32 * u);
+      l[u] = __ldg(log_data + e + 32 * u);
+      c[u] = static_cast<int>(__ldg(indices + e + 32 * u));
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) b[u] += __dmul_rn(d[u], l[u] - lt[c[u]]);
+  }
+  for (; e < hi; e += 32) b[0] += __dmul_rn(__ldg(data + e), __ldg(log_data + e) - lt[__ldg(indices + e)]);
+  return settle(warp_sum((b[0] + b[1]) + (b[2] + b[3])));
+}
+
 // ------------------------------------------------------------ K5 CSR KL --
 template <bool STAGE, class Idx>
 __global__ void __launch_bounds__(kCsrThreads) csr_kl_kernel(
@@ -272,18 +300,8 @@ __global__ void __launch_bounds__(kCsrThreads) csr_kl_kernel(
     double val = h - cross;
     const bool guarded = fabs(val) < tau * (fabs(h) + fabs(cross));  // warp-uniform
     if (guarded && fix_inline) {
-      // reference form sum v * (log v - logPt) (divergence.py:279) right here, the
-      // target logs already in shared memory: the order of csr_kl_fixup_kernel, so
-      // the field and the dv_at / pair paths agree bitwise on guarded rows
-      double b0 = 0.0, b1 = 0.0;
-      int64_t e = lo + lane;
-      for (; e + 32 < hi; e += 64) {
-        b0 += __dmul_rn(__ldg(data + e), __ldg(log_data + e) - lt[__ldg(indices + e)]);
-        b1 += __dmul_rn(__ldg(data + e + 32),
-                        __ldg(log_data + e + 32) - lt[__ldg(indices + e + 32)]);
-      }
-      if (e < hi) b0 += __dmul_rn(__ldg(data + e), __ldg(log_data + e) - lt[__ldg(indices + e)]);
-      val = settle(warp_sum(b0 + b1));
+      // reference form right here, the target logs already in shared memory
+      val = csr_kl_reference_row(data, log_data, indices, lt, lo, hi, lane);
     } else if (guarded) {
       val = __longlong_as_double(static_cast<long long>(kCsrGuard));
     } else {
@@ -313,7 +331,7 @@ __global__ void __launch_bounds__(kCsrThreads) csr_kl_fixup_kernel(
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t count = queries ? nq : rows;
   uint32_t done = 0;
-  // interleaved rows (see kl_guard_fixup_kernel): clustered guards spread out
+  // interleaved rows: guarded rows cluster around the target, spread them out
   for (int64_t i0 = 0; warp + i0 * nwarps < count; i0 += 32) {
     const int64_t mine = warp + (i0 + lane) * nwarps;
     const bool flag = mine < count && static_cast<unsigned long long>(
@@ -326,14 +344,7 @@ __global__ void __launch_bounds__(kCsrThreads) csr_kl_fixup_kernel(
       const int64_t r = queries ? queries[i] - row0 : i;
       int64_t lo, hi;
       row_extent(indptr, data, r, lo, hi);
-      double a0 = 0.0, a1 = 0.0;
-      int64_t e = lo + lane;
-      for (; e + 32 < hi; e += 64) {
-        a0 += __dmul_rn(data[e], log_data[e] - logt[indices[e]]);
-        a1 += __dmul_rn(data[e + 32], log_data[e + 32] - logt[indices[e + 32]]);
-      }
-      if (e < hi) a0 += __dmul_rn(data[e], log_data[e] - logt[indices[e]]);
-      const double val = settle(warp_sum(a0 + a1));
+      const double val = csr_kl_reference_row(data, log_data, indices, logt, lo, hi, lane);
       if (lane == 0) out[i] = val;
       ++done;
     }
