@@ -17,7 +17,6 @@
 namespace pf {
 
 constexpr int kT32 = 256;
-constexpr unsigned long long kSentinel32 = 0x7ff8dead0000beefull;
 
 __device__ __forceinline__ float4 ldg_stream4f(const float4 *p) {
   float4 v;
@@ -63,11 +62,34 @@ __device__ __forceinline__ void acc32(double q_raw, double t, double clamp, doub
 // flag is not computed here: FP32 rounding flushes entries below the float
 // range to zero, so the flag comes from the FP64 rows (pf_mask_compare_f64
 // against the interior rows' shared mask, as for K7).
+// FP64 re-evaluation of one guarded row from the FP64 copy of P, one warp: KL in
+// the reference per-element form, TV as sum |c(Q) - c(Pt)|; then settle.
+template <bool KL>
+__device__ __forceinline__ double guard64_row(const double *__restrict__ prow, int64_t k,
+                                              const double *__restrict__ tgt, double clamp,
+                                              int lane) {
+  double b[4] = {0.0, 0.0, 0.0, 0.0};
+  int64_t e = lane;
+  for (; e + 96 < k; e += 128) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double q = fmax(prow[e + 32 * u], clamp), t = tgt[e + 32 * u];
+      b[u] += KL ? __dmul_rn(q, -log(__ddiv_rn(t, q))) : fabs(q - t);
+    }
+  }
+  for (; e < k; e += 32) {
+    const double q = fmax(prow[e], clamp), t = tgt[e];
+    b[0] += KL ? __dmul_rn(q, -log(__ddiv_rn(t, q))) : fabs(q - t);
+  }
+  return settle(warp_sum((b[0] + b[1]) + (b[2] + b[3])));
+}
+
 template <bool KL>
 __global__ void __launch_bounds__(kT32, 4) dense32_kernel(
     const float *__restrict__ P, int64_t ld, int64_t rows, int64_t k,
     const double *__restrict__ H, const double *__restrict__ vec, double clamp, double tau,
-    int64_t row0, int64_t target, double *__restrict__ out) {
+    int64_t row0, int64_t target, const double *__restrict__ P64, int64_t ld64,
+    const double *__restrict__ tgt, double *__restrict__ out, uint32_t *__restrict__ flags) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int64_t nq4 = k >> 2;  // full float4 groups
   double2 *lo = reinterpret_cast<double2 *>(smem);
@@ -120,12 +142,14 @@ __global__ void __launch_bounds__(kT32, 4) dense32_kernel(
       val = s;
       guard = fabs(val) < tau;
     }
-    if (is_t)
+    if (is_t) {
       val = 0.0;
-    else if (guard)
-      val = __longlong_as_double(static_cast<long long>(kSentinel32));
-    else
+    } else if (guard) {  // warp-uniform: re-evaluated in FP64 in place
+      val = guard64_row<KL>(P64 + r * ld64, k, tgt, clamp, lane);
+      if (lane == 0) atomicAdd(&flags[PF_FLAG_GUARDED], 1u);
+    } else {
       val = settle(val);
+    }
     if (lane == 0) out[r] = val;
   }
 }
@@ -138,51 +162,6 @@ __global__ void mask_compare_kernel(const double *__restrict__ a, const double *
        i += (int64_t)gridDim.x * blockDim.x)
     d |= (a[i] < clamp) != (b[i] < clamp);
   if (__syncthreads_or(d) && threadIdx.x == 0) atomicOr(flag, 1u);
-}
-
-// FP64 re-evaluation of sentinel rows from the FP64 copy of P (rows
-// interleaved across warps): KL in the reference per-element form, TV as
-// sum |c(Q) - c(Pt)|.
-template <bool KL>
-__global__ void __launch_bounds__(256) guard64_fixup_kernel(const double *__restrict__ P64,
-                                                            int64_t ld, int64_t rows, int64_t k,
-                                                            const double *__restrict__ tgt,
-                                                            double clamp,
-                                                            double *__restrict__ out,
-                                                            uint32_t *__restrict__ flags) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  uint32_t done = 0;
-  for (int64_t i0 = 0; warp + i0 * nwarps < rows; i0 += 32) {
-    const int64_t mine = warp + (i0 + lane) * nwarps;
-    const bool flag = mine < rows && static_cast<unsigned long long>(__double_as_longlong(
-                                         out[mine])) == kSentinel32;
-    unsigned ball = __ballot_sync(0xffffffffu, flag);
-    while (ball) {
-      const int src = __ffs(ball) - 1;
-      ball &= ball - 1;
-      const int64_t r = warp + (i0 + src) * nwarps;
-      const double *prow = P64 + r * ld;
-      double b[4] = {0.0, 0.0, 0.0, 0.0};
-      int64_t e = lane;
-      for (; e + 96 < k; e += 128) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const double q = fmax(prow[e + 32 * u], clamp), t = tgt[e + 32 * u];
-          b[u] += KL ? __dmul_rn(q, -log(__ddiv_rn(t, q))) : fabs(q - t);
-        }
-      }
-      for (; e < k; e += 32) {
-        const double q = fmax(prow[e], clamp), t = tgt[e];
-        b[0] += KL ? __dmul_rn(q, -log(__ddiv_rn(t, q))) : fabs(q - t);
-      }
-      const double val = settle(warp_sum((b[0] + b[1]) + (b[2] + b[3])));
-      if (lane == 0) out[r] = val;
-      ++done;
-    }
-  }
-  if (lane == 0 && done) atomicAdd(&flags[PF_FLAG_GUARDED], done);
 }
 
 __global__ void convert_f32_kernel(const double *__restrict__ P, int64_t ld, int64_t rows,
@@ -208,15 +187,10 @@ static int launch32(const float *P, int64_t ld, int64_t rows, int64_t k, const d
   int64_t g = static_cast<int64_t>(sm_count()) * occ, want = (rows + 7) / 8;
   if (g > want) g = want;
   if (g < 1) g = 1;
+  if (!P64 || !tgt || !flags) return fail(PF_E_ARG, "dense32: the FP64 guard needs P64, tgt, flags");
   kern<<<static_cast<int>(g), kT32, smem, stream>>>(P, ld, rows, k, H, vec, clamp, tau, row0,
-                                                    target, out);
-  if (int e = check_launch("dense32")) return e;
-  int64_t g2 = static_cast<int64_t>(sm_count()) * 4, want2 = (rows + 7) / 8;
-  if (g2 > want2) g2 = want2;
-  if (g2 < 1) g2 = 1;
-  guard64_fixup_kernel<KL><<<static_cast<int>(g2), 256, 0, stream>>>(P64, ld64, rows, k, tgt,
-                                                                      clamp, out, flags);
-  return check_launch("guard64_fixup");
+                                                    target, P64, ld64, tgt, out, flags);
+  return check_launch("dense32");  // guarded rows were re-evaluated in place
 }
 
 }  // namespace pf
