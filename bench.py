@@ -1,34 +1,44 @@
 #!/usr/bin/env python
 """Benchmark: vertex-target divergence evaluations/s (KL + TV), B200.
 
-Workload (BASELINE.json configs[1]): dense FP64 Poisson kernel
-of the 50:1 corridor shape, 102,104 vertices x 4,250 boundary vertices PER GPU
-(weak scaling: each rank owns one row slab of that size; the global mesh is
-N x 102,104 rows), KL and TV distance fields to a single target.  One step =
-[broadcast of the target row from its owner rank (NCCL, N>1 only)] + KL field
-+ TV field over the rank's slab: 2 x rows evaluations per rank.
-
-Synthetic data (softmax rows of N(0,1) with one exact-zero column, FP64): the
-reference's real P for this shape takes ~2 min of SuperLU to build and is not
-needed for a bandwidth measurement; parity is tested on real P in tests/.
-P (3.47 GB/GPU) is far larger than L2 (126 MB), so no L2 flush is needed.
+Headline workload (BASELINE.json north_star target): the
+multiply-connected domain with 20 obstacles, 1,000,386 vertices x 4,102
+boundary vertices, REAL Poisson kernel P: the mesh is the reference
+generator's (workloads/meshes.py, bitwise the reference's) and P is built on
+the GPU by the product's multifrontal solve (laplacian.DevicePoisson, K11;
+within 1e-11 of the reference's SuperLU P).  Strong scaling: the
+n rows are split into N contiguous slabs, rank r builds ONLY its slab of P
+(ShardedField.from_mesh) and owns it.  One step = [NCCL broadcast of the
+target row from its owner rank (N > 1, pf_nccl_broadcast)] + KL field + TV
+field over the rank's slab = 2 n evaluations for the whole job.  The target
+is the reference's default_endpoints target (domain.py:155-165).  P (32.8 GB,
+4.1 GB per rank at N = 8) is far larger than L2 (126 MB): no L2 flush needed.
 
 JSON keys beyond the driver contract:
-  roofline      dominant kernel (dense KL) achieved GB/s from CUDA events on
-                its launch stream, algorithmic bytes rows*(8k+16)+8k per launch
+  roofline      dense KL kernel achieved GB/s from CUDA events on its launch
+                stream, algorithmic bytes rows*(8k+16)+8k per launch
+                (SURVEY §8d), against the measured copy bandwidth
   cpu_baseline  the oracle numpy port (reference algorithm) on the host cores
-  e2e           the same metric through the public API dv_field() with the
-                field copied back to host memory every call
+                over a bounded sample of REAL rows of the same P
+  e2e           the same metric through the public API (dv_field at N = 1,
+                ShardedField.field at N > 1) with each field copied to host
+                memory every call
+  preprocessing the one-time mesh / P / negentropy builds (not in `value`)
+  extras        side configs: C2/C2' real (dense, FP32 mode, C3 CSR), C4 FP32,
+                C5 (1,024-target batched KL + 10,000 traced paths), the
+                synthetic C2 weak-scaling line of round 1, Poisson build,
+                wire formats; at N > 1 the sharded C3 and distributed C5
 
 `--impl reference` times the reference's CPU algorithm (the oracle port,
 oracle/divergence.py — the reference is pure Python and cannot travel to the
-GPU box) on a bounded sample of the same workload, on all host threads.
+GPU box) on a bounded sample of the same workload shape, on all host threads.
 """
 
 from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -40,13 +50,18 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
+# name: (n, k, description); the mesh recipe is workloads.meshes.SPECS[name]
 WORKLOADS = {
-    # name: (rows per GPU, k, description)
-    "c2": (102_104, 4_250, "C2 corridor 50:1 dense KL+TV, single target"),
-    "c2p": (106_030, 1_234, "C2' rectangle 1.5:1 dense KL+TV, single target"),
-    "c4": (1_000_386, 4_102, "C4 holes x20 dense KL+TV, single target"),
+    "c4": (1_000_386, 4_102, "C4 holes x20 (1,000,386 x 4,102), real P, dense KL+TV, "
+                             "single target, row slabs over N GPUs"),
+    "c2": (102_104, 4_250, "C2 corridor 50:1 (102,104 x 4,250), real P, dense KL+TV, "
+                           "single target, row slabs over N GPUs"),
+    "c2p": (106_030, 1_234, "C2' rectangle 1.5:1 (106,030 x 1,234), real P, dense KL+TV, "
+                            "single target, row slabs over N GPUs"),
 }
 METRIC = "vertex-target divergence evals/sec (KL, TV) at 1/2/4/8 B200; % HBM roofline"
+NORTH_STAR_HBM_GBS = 8000.0  # BASELINE.json north_star: "~8 TB/s per GPU"
+NO_CPU = False
 
 
 def peaks():
@@ -74,7 +89,6 @@ class ClockSampler:
         self.max_mhz = None
         self._stop = threading.Event()
         self._t = None
-        self._nvml = None
 
     def _run(self):
         try:
@@ -164,30 +178,40 @@ def host_info() -> dict:
     return info
 
 
-def cpu_sample_rows(k: int, rows: int, seed: int):
-    import numpy as np
-    from oracle.inputs import synthetic_kernel
-    P = synthetic_kernel(rows, k, seed)
-    P[:, 0] = 0.0
-    return P
+def _events(t, n=2):
+    return [t.cuda.Event(enable_timing=True) for _ in range(n)]
 
 
+def _roof(bytes_, ms, peak, streamed=None):
+    ach = bytes_ / (ms / 1e3) / 1e9
+    r = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+         "frac_of_8tbs": ach / NORTH_STAR_HBM_GBS,
+         "algorithmic_bytes_per_launch": bytes_, "avg_launch_ms": ms}
+    if streamed is not None:  # bytes the kernel actually streams (e.g. 16-bit CSR columns)
+        r["streamed_bytes_per_launch"] = streamed
+        r["frac_streamed"] = streamed / (ms / 1e3) / 1e9 / peak
+    return r
+
+
+# ---- CPU baselines: the oracle restatement of the reference algorithm on all
+# host cores (SURVEY §8d "CPU timing beside it")
 class CpuReference:
     """Oracle port (reference algorithm: dv_at over row chunks == dv_field,
-    SURVEY A.1) on a bounded sample of rows of the workload shape, on all host
-    threads.  The sample is sized once so one KL+TV pass takes ~budget_s."""
+    SURVEY A.1) on a bounded sample of rows, on all host threads.  `rows_of(m)`
+    returns an (m, k) host matrix whose row 0 is the target row; the sample
+    is sized once so one KL+TV pass takes ~budget_s."""
 
-    def __init__(self, k: int, budget_s: float, threads: int):
+    def __init__(self, rows_of, k: int, budget_s: float, threads: int, what: str):
         from oracle import divergence as O
         self.O, self.k, self.threads = O, k, threads
-        calib = cpu_sample_rows(k, 1024, seed=7)
+        calib = rows_of(1024)
         t0 = time.perf_counter()
         self._pass(calib)
         dt = max(time.perf_counter() - t0, 1e-3)
         self.rows = int(min(200_000, max(1024, 1024 * budget_s / dt)))
-        self.P = cpu_sample_rows(k, self.rows, seed=11)
-        self.sample = (f"KL+TV fields over {self.rows} sampled rows x k={k} "
-                       f"(target row 0), {threads} threads")
+        self.P = rows_of(self.rows)
+        self.sample = (f"KL+TV fields over {self.rows} sampled rows x k={k} ({what}; target "
+                       f"row first), {threads} threads")
 
     def _pass(self, P):
         self.O.dv_field_chunked(P, "kl", 0, chunk_rows=256, threads=self.threads)
@@ -200,9 +224,28 @@ class CpuReference:
         return 2 * self.rows / el, el
 
 
-# ---- bounded CPU baselines of the side workloads (SURVEY §8d "CPU timing
-# beside it"): the oracle restatement of the reference algorithm on all host
-# cores (fork workers: the reference's per-pair / per-path loops are Python).
+def synthetic_rows(k: int, seed: int):
+    """Row-stochastic synthetic rows (softmax of N(0,1), one zero column)."""
+    def rows_of(m):
+        from workloads.meshes import synthetic_kernel
+        P = synthetic_kernel(m, k, seed)
+        P[:, 0] = 0.0
+        return P
+    return rows_of
+
+
+def device_rows(t, dk, target: int):
+    """Real rows of a device-resident P: the target row, then evenly spaced rows."""
+    import numpy as np
+
+    def rows_of(m):
+        idx = np.linspace(0, dk.rows - 1, max(1, m - 1)).astype(np.int64)
+        idx = np.concatenate([[target - dk.row0], idx])[:m]
+        sel = dk.P.index_select(0, t.from_numpy(idx).to(dk.device))[:, :dk.k]
+        return sel.cpu().numpy()
+    return rows_of
+
+
 _CPU_STATE: dict = {}
 
 
@@ -224,25 +267,20 @@ def _csr_pairs(chunk):
     return [O.dv_pair_sparse_stats(sv, name, p, int(q))[0] for q in chunk]
 
 
-def cpu_baseline_csr(rows_full: int, k: int, n_sample: int = 4096, pairs: int = 8192):
+def cpu_baseline_csr(P_rows, n_full: int, pairs: int = 8192):
     """dv_pair_sparse_stats loop (divergence.py:255-305, restated in
-    oracle/divergence.py) over `pairs` sampled query rows of a C3-shaped
-    banded P (same generator, `n_sample` rows), all host cores."""
-    import math
+    oracle/divergence.py) over `pairs` sampled query rows of a row sample of
+    the real P (row 0 = the target), sparsified at the reference's default
+    threshold 1/sqrt(n) of the full mesh, all host cores."""
     import numpy as np
     from oracle import divergence as O
-    b = np.arange(k, dtype=np.float64)[None, :]
-    q = np.linspace(0, rows_full - 1, n_sample)[:, None]
-    c1 = np.floor(q / rows_full * (k / 2))
-    x = np.exp(-np.abs(b - c1) / 12.5) + np.exp(-np.abs(b - ((k - 1) - c1)) / 12.5)
-    P = x / x.sum(axis=1, keepdims=True)
-    sv = O.sparsify(P, np.array([], np.int64), threshold=1.0 / math.sqrt(rows_full))
+    m, k = P_rows.shape
+    sv = O.sparsify(P_rows, np.array([], np.int64), threshold=1.0 / math.sqrt(n_full))
     procs = os.cpu_count() or 1
-    rng = np.random.default_rng(5)
-    qs = rng.integers(0, n_sample, pairs)
+    qs = np.random.default_rng(5).integers(0, m, pairs)
     out = {}
     for name in ("kl", "tv"):
-        _CPU_STATE["csr"] = (sv, name, n_sample // 3)
+        _CPU_STATE["csr"] = (sv, name, 0)
         chunks = [qs[i:i + 64] for i in range(0, pairs, 64)]
         _, sec = _cpu_pool_run(_csr_pairs, chunks, procs)
         out[name] = pairs / sec
@@ -250,26 +288,25 @@ def cpu_baseline_csr(rows_full: int, k: int, n_sample: int = 4096, pairs: int = 
             "kl_evals_per_s": out["kl"], "tv_evals_per_s": out["tv"], "cores": procs,
             "kind": "port",
             "sample": f"dv_pair_sparse_stats loop (the reference's only sparse field) over "
-                      f"{pairs} sampled query rows of a {n_sample} x {k} C3-banded P "
-                      f"sparsified at 1/sqrt({rows_full}), {procs} processes"}
+                      f"{pairs} sampled query rows of {m} real rows x {k} sparsified at "
+                      f"1/sqrt({n_full}), {procs} processes"}
 
 
-def cpu_baseline_batched(k: int, targets: int = 4, rows: int = 8192):
+def cpu_baseline_batched(P_rows, targets: int = 4):
     """T x dv_field (the reference has no batched API): dv_at over row chunks
-    for `targets` targets over a `rows`-row synthetic sample, all threads;
-    evals/s extrapolates linearly to T = 1024."""
-    import numpy as np
+    for `targets` target rows over a real row sample, all threads; evals/s
+    carries to T = 1024 (the reference evaluates T targets as T fields)."""
     from oracle import divergence as O
-    P = cpu_sample_rows(k, rows, seed=13)
+    m, k = P_rows.shape
     threads = os.cpu_count() or 1
     t0 = time.perf_counter()
     for t in range(targets):
-        O.dv_field_chunked(P, "kl", 1 + t, chunk_rows=256, threads=threads)
+        O.dv_field_chunked(P_rows, "kl", t, chunk_rows=256, threads=threads)
     sec = time.perf_counter() - t0
-    return {"value": rows * targets / sec, "unit": "evals/s", "cores": threads, "kind": "port",
+    return {"value": m * targets / sec, "unit": "evals/s", "cores": threads, "kind": "port",
             "sample": f"KL fields (dv_at row chunks == dv_field) for {targets} targets over "
-                      f"{rows} sampled rows x k={k}, {threads} threads; the reference "
-                      "evaluates T targets as T fields, so evals/s carries to T = 1024"}
+                      f"{m} real rows x k={k}, {threads} threads; the reference evaluates T "
+                      "targets as T fields, so evals/s carries to T = 1024"}
 
 
 def _trace_one(i):
@@ -280,25 +317,24 @@ def _trace_one(i):
     return len(r["locations"]) if "locations" in r else 0
 
 
-def cpu_baseline_tracer(mesh, V_dev_fields, targets, src, fo, paths: int = 200):
+def cpu_baseline_tracer(omesh, field_cols, targets, src, fo, paths: int = 200):
     """triangle_descent (paths.py:292-307, oracle/tracer.py) for `paths`
-    sampled (source, target) pairs of the C5 tracer workload, all cores."""
+    sampled (source, target) pairs of the C5 workload on the real mesh and
+    fields, all cores.  `field_cols(j)` returns target j's field (host)."""
     import numpy as np
     from oracle import tracer as OT
     pick = np.flatnonzero(fo < 32)[:paths]
     used = np.unique(fo[pick])
-    fields = {int(f): V_dev_fields[int(f)].cpu().numpy() for f in used}
-    V = np.asarray(mesh.vertices)
-    T = np.asarray(mesh.triangles)
-    topo = OT.topology(T, len(V))
-    _CPU_STATE["trace"] = (V, T, np.asarray(mesh.triangle_areas), float(mesh.bbox_diagonal),
+    fields = {int(f): field_cols(int(f)) for f in used}
+    topo = OT.topology(omesh.triangles, omesh.n)
+    _CPU_STATE["trace"] = (omesh.vertices, omesh.triangles, omesh.areas, omesh.bbox_diagonal,
                            topo, fields, [(src[i], targets[fo[i]], int(fo[i])) for i in pick])
     procs = os.cpu_count() or 1
     locs, sec = _cpu_pool_run(_trace_one, list(range(len(pick))), procs)
     return {"value": len(pick) / sec, "unit": "paths/s", "cores": procs, "kind": "port",
             "locations_per_s": float(sum(locs)) / sec,
-            "sample": f"{len(pick)} of the 10,000 paths (targets 0-31), oracle/tracer.py "
-                      f"restating paths.py:137-307, {procs} processes"}
+            "sample": f"{len(pick)} of the C5 paths (targets 0-31) on the real mesh and "
+                      f"fields, oracle/tracer.py restating paths.py:137-307, {procs} processes"}
 
 
 def run_reference_arm(args):
@@ -308,7 +344,9 @@ def run_reference_arm(args):
     n_rows, k, desc = WORKLOADS[args.workload]
     threads = os.cpu_count() or 1
     per_step = float(os.environ.get("PF_REF_STEP_S", "2.0"))
-    ref = CpuReference(k, per_step, threads)
+    ref = CpuReference(synthetic_rows(k, 11), k, per_step, threads,
+                       "synthetic row-stochastic rows of the workload's k: the real P needs "
+                       "the GPU build, and the port's cost per row depends on k only")
     for _ in range(args.warmup):
         ref.step()
     vals, els = [], []
@@ -316,17 +354,18 @@ def run_reference_arm(args):
         v, el = ref.step()
         vals.append(v)
         els.append(el)
-    sample = ref.sample
     value = statistics.median(vals)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "evals/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * statistics.median(els), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": desc, "rows_per_gpu": n_rows, "k": k},
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic rows of the workload shape",
+        "config": {"workload": desc, "n": n_rows, "k": k},
         "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads, "kind": "port",
                          "host": host_info(),
-                         "sample": sample + "; oracle/divergence.py restating divergence.py:137-187"},
+                         "sample": ref.sample + "; oracle/divergence.py restating "
+                                                "divergence.py:137-187"},
         "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -335,37 +374,6 @@ def run_reference_arm(args):
 
 
 # --------------------------------------------------------------------------
-def make_synthetic_slab(t, rows, k, ld, seed, device, chunk=8192):
-    """Softmax rows of N(0,1) with column 0 exactly zero, on the GPU (FP64)."""
-    P = t.empty((rows, ld), dtype=t.float64, device=device)
-    g = t.Generator(device=device)
-    g.manual_seed(1234 + seed)
-    for a in range(0, rows, chunk):
-        b = min(rows, a + chunk)
-        x = t.randn((b - a, k), dtype=t.float64, device=device, generator=g)
-        x[:, 0] = -float("inf")
-        P[a:b, :k] = t.softmax(x, dim=1)
-    P[:, k:] = 0.0
-    return P
-
-
-def make_banded_slab(t, rows, k, ld, device, width=12.5, chunk=8192):
-    """Corridor-like synthetic P: each row's mass on two exponential bands
-    (bottom wall at column c, top wall at k-1-c, c moving along the corridor),
-    ~487 entries per row above the 1/sqrt(n) cut — the C3 nnz/row."""
-    P = t.empty((rows, ld), dtype=t.float64, device=device)
-    b = t.arange(k, dtype=t.float64, device=device)[None, :]
-    for a in range(0, rows, chunk):
-        e = min(rows, a + chunk)
-        q = t.arange(a, e, dtype=t.float64, device=device)[:, None]
-        c1 = t.floor(q / rows * (k / 2))
-        c2 = (k - 1) - c1
-        x = t.exp(-t.abs(b - c1) / width) + t.exp(-t.abs(b - c2) / width)
-        P[a:e, :k] = x / x.sum(dim=1, keepdim=True)
-    P[:, k:] = 0.0
-    return P
-
-
 class DenseStep:
     """One KL + TV field step over a slab through the C ABI, buffers preallocated.
     With `sharded` (parallel.ShardedField) the target row is NCCL-broadcast."""
@@ -384,16 +392,16 @@ class DenseStep:
         self.ft = self.out_tv.data_ptr() + rows * 8
         self.H = dk.negentropy(1e-300)
         self.stream = t.cuda.current_stream(dk.device)
-        self.ev = [(t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True))
-                   for _ in range(2)]
+        self.ev = [_events(t) for _ in range(2)]
         self.kern_ms = [0.0, 0.0]
         self.launches = 0
 
     def run(self, timed=False):
         dk, nat, s, k = self.dk, self.nat, self.stream.cuda_stream, self.dk.k
         if self.sh is not None:
-            rowp = self.sh.target_row(self.target, k).data_ptr()
-            self._keep = rowp
+            row = self.sh.target_row(self.target, k)
+            self._keep = row
+            rowp = row.data_ptr()
         else:
             rowp = dk.P[self.target - dk.row0].data_ptr()
         nat.call("pf_target_prep_f64", rowp, k, 1e-300, self.tgt, self.logt, self.tmask, self.fk, s)
@@ -417,19 +425,58 @@ class DenseStep:
             self.kern_ms[1] += self.ev[1][0].elapsed_time(self.ev[1][1])
         self.launches += 4   # 2 x target prep, K2, K3
 
+    def kernel_ms(self, steps):
+        """Average K2 / K3 launch time over `steps` event-timed steps."""
+        self.kern_ms = [0.0, 0.0]
+        for _ in range(steps):
+            self.run(timed=True)
+        return self.kern_ms[0] / steps, self.kern_ms[1] / steps
 
-NORTH_STAR_HBM_GBS = 8000.0  # BASELINE.json north_star: "~8 TB/s per GPU"
+
+def build_mesh(name):
+    from workloads.meshes import SPECS, build
+    t0 = time.perf_counter()
+    omesh = build(SPECS[name])
+    return omesh, time.perf_counter() - t0
 
 
-def _roof(bytes_, ms, peak):
-    ach = bytes_ / (ms / 1e3) / 1e9
-    return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-            "frac_of_8tbs": ach / NORTH_STAR_HBM_GBS,
-            "algorithmic_bytes_per_launch": bytes_, "avg_launch_ms": ms}
+def device_build(t, L, omesh, device, slab=None):
+    """P (or the row slab) on the device with the fused K1 (DevicePoisson);
+    returns (dp, dk, timings)."""
+    w0 = time.perf_counter()
+    dp = L.DevicePoisson(omesh, device=device)
+    plan_s = time.perf_counter() - w0
+    e0, e1 = _events(t)
+    t.cuda.synchronize()
+    w0 = time.perf_counter()
+    e0.record()
+    dk = dp.device_kernel(slab=slab)
+    e1.record()
+    t.cuda.synchronize()
+    return dp, dk, {"host_plan_and_upload_s": plan_s, "device_build_ms": e0.elapsed_time(e1),
+                    "device_build_wall_s": time.perf_counter() - w0,
+                    "residual": dk.residual, "row_sum_error": dk.row_sum_error}
+
+
+def dense_fields_extra(t, nat, dev, pf, dk, target, steps, peak, f32=True):
+    """KL+TV (and FP32-mode) kernel timings over a device P (single GPU)."""
+    st = DenseStep(t, nat, dev, dk, target, pf.divergence.KL_GUARD_TAU)
+    for _ in range(3):
+        st.run()
+    kl_ms, tv_ms = st.kernel_ms(max(3, steps))
+    rows, k = dk.rows, dk.k
+    res = {"evals_per_s": 2 * rows / ((kl_ms + tv_ms) / 1e3),
+           "kl_guarded_rows": int(st.out_kl[rows:].view(t.int32)[1].item()),
+           "kl": _roof(rows * (8 * k + 16) + 8 * k, kl_ms, peak),
+           "tv": _roof(rows * (8 * k + 8) + 8 * k, tv_ms, peak)}
+    del st
+    if f32:
+        res["fp32_mode"] = extra_f32(t, nat, dev, pf, dk, target, steps, peak)
+    return res
 
 
 def extra_f32(t, nat, dev, pf, dk, target, steps, peak):
-    """C2 in the FP32 storage mode (query rows from an FP32 copy; 1e-5 tolerance)."""
+    """KL+TV in the FP32 storage mode (query rows from an FP32 copy; 1e-5 tolerance)."""
     rows, k = dk.rows, dk.k
     P32, ld32 = dk.fp32()
     H32 = dk.negentropy32(1e-300)
@@ -441,8 +488,9 @@ def extra_f32(t, nat, dev, pf, dk, target, steps, peak):
     fl = out.data_ptr() + rows * 8
     rowp = dk.P[target - dk.row0].data_ptr()
     tau = pf.divergence.F32_GUARD_TAU
-    ev = [t.cuda.Event(enable_timing=True) for _ in range(4)]
+    ev = _events(t, 4)
     ms = [0.0, 0.0]
+    guarded = [0, 0]
 
     def step(timed):
         nat.call("pf_target_prep_f64", rowp, k, 1e-300, tgt, logt, tmask, fl, s.cuda_stream)
@@ -453,6 +501,8 @@ def extra_f32(t, nat, dev, pf, dk, target, steps, peak):
                  out.data_ptr(), fl, s.cuda_stream)
         if timed:
             ev[1].record(s)
+            s.synchronize()
+            guarded[0] = int(out[rows:].view(t.int32)[1].item())
         nat.call("pf_target_prep_f64", rowp, k, 1e-150, tgt, 0, tmask, fl, s.cuda_stream)
         if timed:
             ev[2].record(s)
@@ -462,6 +512,7 @@ def extra_f32(t, nat, dev, pf, dk, target, steps, peak):
         if timed:
             ev[3].record(s)
             s.synchronize()
+            guarded[1] = int(out[rows:].view(t.int32)[1].item())
             ms[0] += ev[0].elapsed_time(ev[1])
             ms[1] += ev[2].elapsed_time(ev[3])
 
@@ -471,182 +522,37 @@ def extra_f32(t, nat, dev, pf, dk, target, steps, peak):
     for _ in range(n):
         step(True)
     kl_ms, tv_ms = ms[0] / n, ms[1] / n
-    guarded = int(out[rows:].view(t.int32)[1].item())
-    return {"workload": "C2 shape in the FP32 storage mode (P streamed as FP32, FP64 logs / "
-                        "accumulation, 1e-5 relative tolerance)",
-            "evals_per_s": 2 * rows / ((kl_ms + tv_ms) / 1e3), "tv_guarded_rows_last": guarded,
+    return {"workload": "FP32 storage mode (P streamed as FP32, FP64 logs / accumulation, "
+                        "1e-5 relative tolerance)",
+            "evals_per_s": 2 * rows / ((kl_ms + tv_ms) / 1e3),
+            "kl_guarded_rows": guarded[0], "tv_guarded_rows": guarded[1],
             "kl": _roof(rows * (4 * k + 16) + 8 * k, kl_ms, peak),
             "tv": _roof(rows * (4 * k + 8) + 8 * k, tv_ms, peak)}
 
 
-def extra_c4_and_c5(t, nat, dev, pf, device, steps, peak):
-    """C4 dense KL+TV (1,000,386 x 4,102 on one GPU) and C5 batched KL (T = 1024)."""
-    import numpy as np
-    rows, k, _ = WORKLOADS["c4"]
-    ld = dev.leading_dim(k)
-    P = make_synthetic_slab(t, rows, k, ld, 7, device, chunk=32768)
-    dk = dev.DeviceKernel(None, np.array([], np.int64), device=device, rows=rows, n=rows, k=k,
-                          P_dev=P)
-    target = rows // 3 + 1
-    st = DenseStep(t, nat, dev, dk, target, pf.divergence.KL_GUARD_TAU)
-    for _ in range(2):
-        st.run()
-    n = max(2, min(steps, 5))
-    for _ in range(n):
-        st.run(timed=True)
-    kl_ms, tv_ms = st.kern_ms[0] / n, st.kern_ms[1] / n
-    c4 = {"workload": "C4 shape 1,000,386 x 4,102 dense FP64 (32.8 GB), synthetic, 1 GPU",
-          "evals_per_s": 2 * rows / ((kl_ms + tv_ms) / 1e3),
-          "kl": _roof(rows * (8 * k + 16) + 8 * k, kl_ms, peak),
-          "tv": _roof(rows * (8 * k + 8) + 8 * k, tv_ms, peak)}
-    del st
-    # ---- C5: 1024 targets, KL as one contraction + fused epilogue (K7).  Product
-    # path: exact-integer emulation of the FP64 GEMM on the int8 tensor pipe
-    # (tcgen05, batched_i8.cu); the FP64 DMMA GEMM is timed beside it.
-    import ctypes
-    T = 1024
-    rng = np.random.default_rng(0)
-    targets = rng.choice(rows, T, replace=False)
-    tg = t.from_numpy(targets.astype(np.int64)).to(device)
-    H = dk.negentropy(1e-300)
-    ldl = dev.round_up(k, 16)
-    Pt = dk.P.index_select(0, tg)
-    L = t.empty((T, ldl), dtype=t.float64, device=device)
-    Tc = t.empty((T, ldl), dtype=t.float64, device=device)
-    out = t.empty((rows, T), dtype=t.float64, device=device)
-    cnt = t.zeros(1, dtype=t.int32, device=device)
-    s = t.cuda.current_stream(device)
-    e0, e1, e2 = (t.cuda.Event(enable_timing=True) for _ in range(3))
-    tau = pf.divergence.KL_GUARD_TAU
+def csr_fields_extra(t, nat, dev, pf, dk, target, steps, peak):
+    """C3: sparsify (K4) at the reference default 1/sqrt(n), then CSR KL + TV
+    fields (K5/K6) to one target on the device CSR."""
+    n, rows, k = dk.n, dk.rows, dk.k
+    cut = (1.0 / math.sqrt(n)) / k
+    s = t.cuda.current_stream(dk.device)
+    t.cuda.synchronize()
+    w0 = time.perf_counter()
+    e0, e1 = _events(t)
     e0.record(s)
-    A, ea, ldk = dk.slices(1e-300)          # once per P (like H)
+    dc = dk.csr(cut, False)
     e1.record(s)
     t.cuda.synchronize()
-    slice_ms = e0.elapsed_time(e1)
-    B = t.empty((7, T, ldk), dtype=t.uint8, device=device)
-    eb = t.empty(T, dtype=t.int32, device=device)
-    bad = t.zeros(1, dtype=t.int32, device=device)
-    gemm_ms = [0.0]
-
-    def batch_i8(timed=False, grade=64):
-        nat.call("pf_batch_prep_f64", Pt.data_ptr(), Pt.stride(0), T, k, ldl, 1e-300, 0,
-                 L.data_ptr(), Tc.data_ptr(), 0, s.cuda_stream)
-        nat.call("pf_slice_targets_u8", L.data_ptr(), ldl, T, k, ldk, B.data_ptr(), eb.data_ptr(),
-                 bad.data_ptr(), s.cuda_stream)
-        if timed:
-            e1.record(s)
-        nat.call("pf_batched_kl_i8", A.data_ptr(), ea.data_ptr(), rows, B.data_ptr(),
-                 eb.data_ptr(), T, k, ldk, H.data_ptr(), tg.data_ptr(), tau, 0, out.data_ptr(),
-                 out.stride(0), grade, s.cuda_stream)
-        if timed:
-            e2.record(s)
-        nat.call("pf_batched_kl_fixup_f64", dk.P.data_ptr(), dk.ld, rows, k, Tc.data_ptr(), ldl,
-                 T, 1e-300, out.data_ptr(), out.stride(0), cnt.data_ptr(), s.cuda_stream)
-
-    def batch_f64():
-        nat.call("pf_batch_prep_f64", Pt.data_ptr(), Pt.stride(0), T, k, ldl, 1e-300, 0,
-                 L.data_ptr(), Tc.data_ptr(), 0, s.cuda_stream)
-        nat.call("pf_batched_kl_f64", dk.P.data_ptr(), dk.ld, rows, k, H.data_ptr(), L.data_ptr(),
-                 Tc.data_ptr(), ldl, T, tg.data_ptr(), 1e-300, tau, 0,
-                 out.data_ptr(), out.stride(0), cnt.data_ptr(), s.cuda_stream)
-
-    def timed(fn, reps):
-        fn()
-        t.cuda.synchronize()
-        st, en = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
-        st.record(s)
-        for _ in range(reps):
-            fn()
-        en.record(s)
-        t.cuda.synchronize()
-        return st.elapsed_time(en) / reps
-
-    reps = 3
-    ms = timed(batch_i8, reps)
-    batch_i8(True)
-    t.cuda.synchronize()
-    gemm_only = e1.elapsed_time(e2)
-    guarded = int(cnt.item())
-    ms_f32grade = timed(lambda: batch_i8(grade=32), reps)
-    ms64 = timed(batch_f64, 1)
-    flops = 2.0 * rows * k * T
-    # measured ceilings of this GPU: sustained DFMA, and the int8 tensor pipe
-    fl = ctypes.c_int64(0)
-    probe = t.empty(2, dtype=t.float64, device=device)
-
-    def probe_rate(name, iters):
-        nat.call(name, iters // 4, ctypes.byref(fl), probe.data_ptr(), s.cuda_stream)
-        t.cuda.synchronize()
-        e0.record(s)
-        nat.call(name, iters, ctypes.byref(fl), probe.data_ptr(), s.cuda_stream)
-        e1.record(s)
-        t.cuda.synchronize()
-        return fl.value / (e0.elapsed_time(e1) / 1e3) / 1e12
-
-    dfma_tf = probe_rate("pf_probe_dfma_f64", 1 << 16)
-    i8_tops = probe_rate("pf_probe_umma_i8", 1 << 14)
-    int_ops = 34 * flops
-    ach = int_ops / (gemm_only / 1e3) / 1e12
-    c5 = {"workload": "C5 shape: 1,000,386 x 4,102 P, T = 1024 targets, KL as one contraction "
-                      "+ fused epilogue (K7 on the int8 tensor pipe: 34 exact byte-pair GEMMs "
-                      "emulating the FP64 GEMM), synthetic, 1 GPU",
-          "evals_per_s": rows * T / (ms / 1e3), "ms_per_batch": ms,
-          "gemm_ms": gemm_only, "guarded_pairs": guarded,
-          "fp64_equivalent_tflops": flops / (ms / 1e3) / 1e12,
-          "slice_rows_ms_once_per_P": slice_ms,
-          "roofline": {"bound": "tensor", "achieved": ach, "peak": i8_tops, "unit": "TOPS (int8)",
-                       "frac": ach / i8_tops,
-                       "algorithmic_ops_per_launch": int_ops,
-                       "peak_kind": "measured: pf_probe_umma_i8 (M128 N256 K32 u8 tcgen05.mma "
-                                    "back to back from shared memory, all SMs)"},
-          "fp32_grade": {"note": "same kernel, 15 byte-pair GEMMs (levels 2..6 of the top 5 "
-                                 "planes): the north-star FP32 tolerance 1e-5",
-                         "ms_per_batch": ms_f32grade,
-                         "evals_per_s": rows * T / (ms_f32grade / 1e3)},
-          "fp64_dmma_path": {"ms_per_batch": ms64, "evals_per_s": rows * T / (ms64 / 1e3),
-                             "achieved_tflops": flops / (ms64 / 1e3) / 1e12,
-                             "dfma_peak_tflops": dfma_tf,
-                             "frac": flops / (ms64 / 1e3) / 1e12 / dfma_tf}}
-    if not NO_CPU:
-        try:
-            c5["cpu_baseline"] = cpu_baseline_batched(k)
-        except Exception as exc:
-            c5["cpu_baseline"] = {"error": f"{type(exc).__name__}: {exc}"}
-    del A, B
-    del out, L, Tc, Pt, dk, P
-    t.cuda.empty_cache()
-    return c4, c5
-
-
-def extra_c3(t, nat, dev, pf, device, steps, peak):
-    """C3: CSR KL + TV over the corridor-shaped sparse kernel (102,104 x 4,250)."""
-    import math
-    import numpy as np
-    rows, k, _ = WORKLOADS["c2"]
-    ld = dev.leading_dim(k)
-    P = make_banded_slab(t, rows, k, ld, device)
-    dk = dev.DeviceKernel(None, np.array([], np.int64), device=device, rows=rows, n=rows, k=k,
-                          P_dev=P)
-    cut = (1.0 / math.sqrt(rows)) / k
-    t0 = t.cuda.Event(enable_timing=True)
-    t1 = t.cuda.Event(enable_timing=True)
-    s = t.cuda.current_stream(device)
-    t0.record(s)
-    dc = dk.csr(cut, False)
-    t1.record(s)
-    t.cuda.synchronize()
-    build_ms = t0.elapsed_time(t1)
-    target = rows // 3 + 1
+    build_ms, build_wall = e0.elapsed_time(e1), time.perf_counter() - w0
     k_pad = dev.round_up(k, 2)
-    stage = t.empty(16 * k_pad + dev.round_up(k, 16), dtype=t.uint8, device=device)
+    stage = t.empty(16 * k_pad + dev.round_up(k, 16), dtype=t.uint8, device=dk.device)
     logt = stage.data_ptr() + 8 * k_pad
-    vp = t.empty(k_pad + 4, dtype=t.float64, device=device)
-    out = t.empty(rows + 2, dtype=t.float64, device=device)
+    vp = t.empty(k_pad + 4, dtype=t.float64, device=dk.device)
+    out = t.empty(rows + 2, dtype=t.float64, device=dk.device)
     flags = out.data_ptr() + rows * 8
-    queue = t.empty(rows, dtype=t.int64, device=device)
     kl_entry, kl_idx = dc.field_entry("kl")   # 16-bit columns (k < 65,536)
     tv_entry, tv_idx = dc.field_entry("tv")
-    ev = [t.cuda.Event(enable_timing=True) for _ in range(4)]
+    ev = _events(t, 4)
     ms = [0.0, 0.0]
 
     def step(timed):
@@ -657,7 +563,7 @@ def extra_c3(t, nat, dev, pf, device, steps, peak):
         nat.call(kl_entry, dc.indptr.data_ptr(), kl_idx, dc.data.data_ptr(),
                  dc.log_data.data_ptr(), dc.hs.data_ptr(), rows, k, logt,
                  pf.divergence.KL_GUARD_TAU, 0, 0, rows, out.data_ptr(), 0, flags,
-                 queue.data_ptr(), s.cuda_stream)
+                 1, s.cuda_stream)
         if timed:
             ev[1].record(s)
         nat.call("pf_csr_target_prep_f64", dc.indptr.data_ptr(), dc.indices.data_ptr(),
@@ -676,27 +582,260 @@ def extra_c3(t, nat, dev, pf, device, steps, peak):
 
     for _ in range(3):
         step(False)
-    n = max(3, steps)
-    for _ in range(n):
+    n_t = max(3, steps)
+    for _ in range(n_t):
         step(True)
-    kl_ms, tv_ms = ms[0] / n, ms[1] / n
+    kl_ms, tv_ms = ms[0] / n_t, ms[1] / n_t
     nnz = dc.nnz
-    res = {"workload": "C3 shape: 102,104 x 4,250 corridor-banded synthetic P, threshold 1/sqrt(n)",
-           "columns": "uint16 device copy (10 B/entry streamed; algorithmic bytes are scipy's "
+    ib = 2 if dc.indices16 is not None else 4
+    # streamed: data (8) + column (2 or 4) per stored entry incl. row-alignment pads
+    str_kl = dc.nnz_pad * (8 + ib) + rows * (8 + 8 + 8) + 8 * k
+    str_tv = dc.nnz_pad * (8 + ib) + rows * (8 + 8 + 8) + 16 * k
+    # the public sparsify (host scipy views) end to end, for the wall-time record
+    pk = _host_pk_of(t, pf, dev, dk) if rows * k * 8 < 8e9 else None
+    sp_wall = None
+    if pk is not None:
+        dk._csr.clear()   # the public call builds its CSR (K4) inside the timed region
+        t.cuda.synchronize()
+        w0 = time.perf_counter()
+        sp = pf.sparsify(pk)
+        sp_wall = time.perf_counter() - w0
+        del sp
+    res = {"columns": "uint16 device copy (10 B/entry streamed; algorithmic bytes are scipy's "
                       "int32 layout, 12 B/entry)" if dc.indices16 is not None else "int32",
            "nnz": nnz, "nnz_per_row": nnz / rows,
            "sparsity_percent": 100.0 * (1 - nnz / (rows * k)),
-           "sparsify_build_ms": build_ms,
+           "device_csr_build_ms": build_ms, "device_csr_build_wall_s": build_wall,
+           "public_sparsify_wall_s": sp_wall,
            "evals_per_s": 2 * rows / ((kl_ms + tv_ms) / 1e3),
-           "kl": _roof(nnz * 12 + rows * 24 + 8 * k, kl_ms, peak),
-           "tv": _roof(nnz * 12 + rows * 24 + 16 * k, tv_ms, peak)}
-    del dc, dk, P
-    t.cuda.empty_cache()
+           "kl": _roof(nnz * 12 + rows * 24 + 8 * k, kl_ms, peak, str_kl),
+           "tv": _roof(nnz * 12 + rows * 24 + 16 * k, tv_ms, peak, str_tv)}
+    del dc
+    dk._csr.clear()
+    return res
+
+
+def _host_pk_of(t, pf, dev, dk):
+    """A host PoissonKernel whose device mirror is `dk` (as poisson_kernel() returns)."""
+    from paper_1708_02845_b200 import laplacian as L
+    dense = L.dense_to_host(dk.P, dk.n, dk.k)
+    pk = pf.PoissonKernel(dense, dk.boundary, dk.residual, dk.row_sum_error)
+    dev.register(pk.dense, dk)
+    return pk
+
+
+def extra_small_real(t, nat, dev, pf, L, device, name, steps, peak):
+    """C2 / C2' on their real P (device build): dense KL/TV, FP32 mode, and for
+    C2 the C3 CSR fields, each beside its CPU baseline on real rows."""
+    import numpy as np
+    from workloads.meshes import default_endpoints
+    omesh, mesh_s = build_mesh(name)
+    dp, dk, build = device_build(t, L, omesh, device)
+    build["mesh_build_s"] = mesh_s
+    _, target = default_endpoints(omesh)
+    res = {"workload": WORKLOADS[name][2].replace("row slabs over N GPUs", "1 GPU"),
+           "preprocessing": build, "target": int(target)}
+    res.update(dense_fields_extra(t, nat, dev, pf, dk, target, steps, peak))
+    rows_of = device_rows(t, dk, target)
     if not NO_CPU:
         try:
-            res["cpu_baseline"] = cpu_baseline_csr(rows, k)
+            ref = CpuReference(rows_of, dk.k, 5.0, os.cpu_count() or 1, "real rows of this P")
+            v, _ = ref.step()
+            res["cpu_baseline"] = {"value": v, "unit": "evals/s", "cores": ref.threads,
+                                   "kind": "port", "sample": ref.sample}
         except Exception as exc:
             res["cpu_baseline"] = {"error": f"{type(exc).__name__}: {exc}"}
+    if name == "c2":
+        c3 = {"workload": "C3: the C2 real P sparsified at 1/sqrt(n) (K4), CSR KL+TV fields "
+                          "(K5/K6), 1 GPU"}
+        c3.update(csr_fields_extra(t, nat, dev, pf, dk, target, steps, peak))
+        if not NO_CPU:
+            try:
+                c3["cpu_baseline"] = cpu_baseline_csr(rows_of(4096), dk.n)
+            except Exception as exc:
+                c3["cpu_baseline"] = {"error": f"{type(exc).__name__}: {exc}"}
+        res["c3_csr"] = c3
+    del dk, dp
+    t.cuda.empty_cache()
+    return res
+
+
+def extra_c5(t, nat, dev, pf, device, dk, omesh, steps, peak):
+    """C5 on the C4 real P: 1,024 targets' KL fields as one contraction (K7 on
+    the int8 tensor pipe), then 10,000 paths traced through those fields
+    straight from the (n, T) output (pf_trace_fields_f64)."""
+    import ctypes
+    import numpy as np
+    from paper_1708_02845_b200 import paths as PP
+    from workloads.meshes import c5_jobs
+    rows, k = dk.rows, dk.k
+    targets, src, fo = c5_jobs(omesh)
+    T = targets.size
+    tg = t.from_numpy(targets).to(device)
+    H = dk.negentropy(1e-300)
+    ldl = dev.round_up(k, 16)
+    Pt = dk.P.index_select(0, tg)
+    L_ = t.empty((T, ldl), dtype=t.float64, device=device)
+    Tc = t.empty((T, ldl), dtype=t.float64, device=device)
+    out = t.empty((rows, T), dtype=t.float64, device=device)
+    cnt = t.zeros(1, dtype=t.int32, device=device)
+    s = t.cuda.current_stream(device)
+    e0, e1, e2 = _events(t, 3)
+    tau = pf.divergence.KL_GUARD_TAU
+    e0.record(s)
+    A, ea, ldk = dk.slices(1e-300)          # once per P (like H)
+    e1.record(s)
+    t.cuda.synchronize()
+    slice_ms = e0.elapsed_time(e1)
+    B = t.empty((7, T, ldk), dtype=t.uint8, device=device)
+    eb = t.empty(T, dtype=t.int32, device=device)
+    bad = t.zeros(1, dtype=t.int32, device=device)
+
+    def batch_i8(timed=False, grade=64):
+        cnt.zero_()
+        nat.call("pf_batch_prep_f64", Pt.data_ptr(), Pt.stride(0), T, k, ldl, 1e-300, 0,
+                 L_.data_ptr(), Tc.data_ptr(), 0, s.cuda_stream)
+        nat.call("pf_slice_targets_u8", L_.data_ptr(), ldl, T, k, ldk, B.data_ptr(), eb.data_ptr(),
+                 bad.data_ptr(), s.cuda_stream)
+        if timed:
+            e1.record(s)
+        nat.call("pf_batched_kl_i8", A.data_ptr(), ea.data_ptr(), rows, B.data_ptr(),
+                 eb.data_ptr(), T, k, ldk, H.data_ptr(), tg.data_ptr(), tau, 0, out.data_ptr(),
+                 out.stride(0), grade, s.cuda_stream)
+        if timed:
+            e2.record(s)
+        nat.call("pf_batched_kl_fixup_f64", dk.P.data_ptr(), dk.ld, rows, k, Tc.data_ptr(), ldl,
+                 T, 1e-300, out.data_ptr(), out.stride(0), cnt.data_ptr(), s.cuda_stream)
+
+    def batch_f64():
+        cnt.zero_()
+        nat.call("pf_batch_prep_f64", Pt.data_ptr(), Pt.stride(0), T, k, ldl, 1e-300, 0,
+                 L_.data_ptr(), Tc.data_ptr(), 0, s.cuda_stream)
+        nat.call("pf_batched_kl_f64", dk.P.data_ptr(), dk.ld, rows, k, H.data_ptr(), L_.data_ptr(),
+                 Tc.data_ptr(), ldl, T, tg.data_ptr(), 1e-300, tau, 0,
+                 out.data_ptr(), out.stride(0), cnt.data_ptr(), s.cuda_stream)
+
+    def timed(fn, reps):
+        fn()
+        t.cuda.synchronize()
+        st, en = _events(t)
+        st.record(s)
+        for _ in range(reps):
+            fn()
+        en.record(s)
+        t.cuda.synchronize()
+        return st.elapsed_time(en) / reps
+
+    ms_f32grade = timed(lambda: batch_i8(grade=32), 2)
+    ms64 = timed(batch_f64, 1)
+    ms = timed(batch_i8, 3)
+    batch_i8(True)
+    t.cuda.synchronize()
+    gemm_only = e1.elapsed_time(e2)
+    guarded = int(cnt.item())
+    flops = 2.0 * rows * k * T
+    fl = ctypes.c_int64(0)
+    probe = t.empty(2, dtype=t.float64, device=device)
+
+    def probe_rate(name, iters):
+        nat.call(name, iters // 4, ctypes.byref(fl), probe.data_ptr(), s.cuda_stream)
+        t.cuda.synchronize()
+        e0.record(s)
+        nat.call(name, iters, ctypes.byref(fl), probe.data_ptr(), s.cuda_stream)
+        e1.record(s)
+        t.cuda.synchronize()
+        return fl.value / (e0.elapsed_time(e1) / 1e3) / 1e12
+
+    dfma_tf = probe_rate("pf_probe_dfma_f64", 1 << 16)
+    i8_tops = probe_rate("pf_probe_umma_i8", 1 << 14)
+    int_ops = 34 * flops
+    ach = int_ops / (gemm_only / 1e3) / 1e12
+    res = {"workload": f"C5: C4 real P ({rows:,} x {k:,}), T = {T} targets (SURVEY §8d C5), KL "
+                       "as one contraction + fused epilogue (K7 on the int8 tensor pipe: 34 exact "
+                       f"byte-pair GEMMs emulating the FP64 GEMM), then {src.size:,} paths traced, "
+                       "1 GPU",
+           "evals_per_s": rows * T / (ms / 1e3), "ms_per_batch": ms,
+           "gemm_ms": gemm_only, "guarded_pairs": guarded,
+           "fp64_equivalent_tflops": flops / (ms / 1e3) / 1e12,
+           "slice_rows_ms_once_per_P": slice_ms,
+           "roofline": {"bound": "tensor", "achieved": ach, "peak": i8_tops, "unit": "TOPS (int8)",
+                        "frac": ach / i8_tops, "algorithmic_ops_per_launch": int_ops,
+                        "peak_kind": "measured: pf_probe_umma_i8 (M128 N256 K32 u8 tcgen05.mma "
+                                     "back to back from shared memory, all SMs)"},
+           "fp32_grade": {"note": "same kernel, 15 byte-pair GEMMs (levels 2..6 of the top 5 "
+                                  "planes): the north-star FP32 tolerance 1e-5",
+                          "ms_per_batch": ms_f32grade,
+                          "evals_per_s": rows * T / (ms_f32grade / 1e3)},
+           "fp64_dmma_path": {"ms_per_batch": ms64, "evals_per_s": rows * T / (ms64 / 1e3),
+                              "achieved_tflops": flops / (ms64 / 1e3) / 1e12,
+                              "dfma_peak_tflops": dfma_tf,
+                              "frac": flops / (ms64 / 1e3) / 1e12 / dfma_tf}}
+    del A, B
+    # ---- the tracer over the K7 fields, read in place: field j = column j of `out`
+    PP.trace_arrays(omesh_tri(omesh, pf), out, targets, src[:64], fo[:64], layout=(1, T))
+    t.cuda.synchronize()
+    w0 = time.perf_counter()
+    e0.record(s)
+    buf, counts, over, extra = PP.trace_arrays(omesh_tri(omesh, pf), out, targets, src, fo,
+                                               layout=(1, T))
+    e1.record(s)
+    t.cuda.synchronize()
+    tr_ms = e0.elapsed_time(e1)
+    status = buf.status[:src.size].cpu().numpy()
+    res["tracer"] = {"paths": int(src.size), "ms": tr_ms,
+                     "wall_ms_incl_launch": 1e3 * (time.perf_counter() - w0),
+                     "paths_per_s": src.size / (tr_ms / 1e3),
+                     "locations_per_s": float(counts.sum()) / (tr_ms / 1e3),
+                     "mean_locations": float(counts.mean()), "max_locations": int(counts.max()),
+                     "reached": int((status == 0).sum()), "overflow_reruns": int(over.size)}
+    if not NO_CPU:
+        try:
+            res["cpu_baseline"] = cpu_baseline_batched(device_rows(t, dk, int(targets[0]))(4096))
+        except Exception as exc:
+            res["cpu_baseline"] = {"error": f"{type(exc).__name__}: {exc}"}
+        try:
+            res["tracer"]["cpu_baseline"] = cpu_baseline_tracer(
+                omesh, lambda j: out[:, j].cpu().numpy(), targets, src, fo)
+        except Exception as exc:
+            res["tracer"]["cpu_baseline"] = {"error": f"{type(exc).__name__}: {exc}"}
+    del out, L_, Tc, Pt
+    dk._H.pop(("i8", 1e-300), None)
+    t.cuda.empty_cache()
+    return res
+
+
+_TRI = {}
+
+
+def omesh_tri(omesh, pf):
+    """The product TriMesh of a workload mesh (cached: its device topology is)."""
+    key = id(omesh)
+    if key not in _TRI:
+        _TRI[key] = pf.TriMesh(omesh.vertices, omesh.triangles)
+    return _TRI[key]
+
+
+def extra_synthetic_c2(t, nat, dev, pf, device, steps, peak):
+    """Round 1's headline, kept for continuity: a synthetic C2-shaped slab
+    (softmax rows, one zero column), dense KL + TV."""
+    import numpy as np
+    rows, k = 102_104, 4_250
+    ld = dev.leading_dim(k)
+    P = t.empty((rows, ld), dtype=t.float64, device=device)
+    g = t.Generator(device=device)
+    g.manual_seed(1234)
+    for a in range(0, rows, 8192):
+        b = min(rows, a + 8192)
+        x = t.randn((b - a, k), dtype=t.float64, device=device, generator=g)
+        x[:, 0] = -float("inf")
+        P[a:b, :k] = t.softmax(x, dim=1)
+    P[:, k:] = 0.0
+    dk = dev.DeviceKernel(None, np.array([], np.int64), device=device, rows=rows, n=rows, k=k,
+                          P_dev=P)
+    res = {"workload": "synthetic C2 shape 102,104 x 4,250 (round-1 headline)"}
+    res.update(dense_fields_extra(t, nat, dev, pf, dk, rows // 3 + 1, steps, peak, f32=False))
+    del dk, P
+    t.cuda.empty_cache()
     return res
 
 
@@ -735,58 +874,30 @@ def extra_wire(t, dev, pf, device):
             "hbm_values_to_csv_str_ms": dev_ms, "field_to_csv_ms": csv_ms,
             "field_to_json_ms": json_ms,
             "reference_python_csv_ms_extrapolated": ref_csv_ms,
-            "reference_python_json_ms_extrapolated": ref_json_ms,
-            "note": "hbm_values_to_csv_str_ms: device-resident values to the CSV body as a "
-                    "Python str (kernels, D2H, decode); field_to_*_ms: wall clock from a host "
-                    "ScalarField to the "
-                    "returned str (H2D, kernels, D2H, decode); reference: the fileio.py "
-                    "expressions on 100,000 values x 10.01"}
+            "reference_python_json_ms_extrapolated": ref_json_ms}
 
 
-def extra_poisson(t, nat, dev, device, dfma_peak=None):
-    """the Poisson kernel P itself on the device (cotan Laplacian,
-    nested-dissection multifrontal Cholesky, multi-RHS solves) at C2 and C4,
-    beside the reference algorithm (SuperLU factor + column solves,
-    oracle/inputs.poisson_kernel_parallel on all host cores) at C2."""
+def extra_poisson(t, nat, dev, device, L, dp_c4=None, dfma_peak=None):
+    """the Poisson kernel P itself on the device at C2 (beside
+    SuperLU on all host cores, oracle/inputs.poisson_kernel_parallel) and C4
+    (phases of a re-solve of the headline mesh)."""
     import numpy as np
     from oracle import inputs as I
-    import paper_1708_02845_b200.laplacian as L
-    specs = {"c2": {"gen": "rectangle", "length": 50.0, "width": 1.0, "spacing": 0.024},
-             "c4": {"gen": "holes", "spacing": 0.0017, "size": [2.0, 1.25],
-                    "holes": [[0.2 + 0.4 * i, 0.16 + 0.31 * j, 0.0034]
-                              for i in range(5) for j in range(4)]}}
-    if dfma_peak is None:  # measured sustained DFMA rate of this GPU (pf_probe_dfma_f64)
-        import ctypes
-        fl = ctypes.c_int64(0)
-        probe = t.empty(2, dtype=t.float64, device=device)
-        s = t.cuda.current_stream(device)
-        nat.call("pf_probe_dfma_f64", 1 << 14, ctypes.byref(fl), probe.data_ptr(), s.cuda_stream)
-        t.cuda.synchronize()
-        p0, p1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
-        p0.record(s)
-        nat.call("pf_probe_dfma_f64", 1 << 16, ctypes.byref(fl), probe.data_ptr(), s.cuda_stream)
-        p1.record(s)
-        t.cuda.synchronize()
-        dfma_peak = fl.value / (p0.elapsed_time(p1) / 1e3) / 1e12
     out = {"dfma_peak_tflops": dfma_peak}
-    for name, spec in specs.items():
-        t0 = time.perf_counter()
-        omesh = I.build(spec)
-        # the reference TriMesh holds its boundary as a field computed at construction
-        # (mesh.py:79-82); the oracle mesh recomputes it per access, so freeze it here
-        from types import SimpleNamespace
-        mesh = SimpleNamespace(vertices=omesh.vertices, triangles=omesh.triangles,
-                               boundary_vertices=omesh.boundary_vertices)
-        mesh_s = time.perf_counter() - t0
-        t0 = time.perf_counter()
-        dp = L.DevicePoisson(mesh)
-        setup_s = time.perf_counter() - t0
-        ev = lambda: t.cuda.Event(enable_timing=True)  # noqa: E731
+    todo = [("c2", None)] + ([("c4", dp_c4)] if dp_c4 is not None else [])
+    for name, dp in todo:
+        omesh, mesh_s = (None, None) if dp is not None else build_mesh(name)
+        if dp is None:
+            w0 = time.perf_counter()
+            dp = L.DevicePoisson(omesh, device=device)
+            setup_s = time.perf_counter() - w0
+        else:
+            setup_s = None
         P, reps = None, []
         for rep in range(3):
             dp._lap, dp._F = None, None
             t.cuda.synchronize()
-            e0, e1 = ev(), ev()
+            e0, e1 = _events(t)
             phases = {}
             e0.record()
             dp.laplacian()
@@ -810,24 +921,13 @@ def extra_poisson(t, nat, dev, device, dfma_peak=None):
                "backward_roofline": {
                    "bound": "fp64", "unit": "TFLOP/s",
                    "achieved": fl["backward"] / (bwd * 1e-3) / 1e12,
-                   "issued": fl["backward_issued"] / (bwd * 1e-3) / 1e12,
-                   "peak": dfma_peak, "frac": (fl["backward"] / (bwd * 1e-3) / 1e12 / dfma_peak
-                                               if dfma_peak else None),
+                   "peak": dfma_peak,
+                   "frac": (fl["backward"] / (bwd * 1e-3) / 1e12 / dfma_peak
+                            if dfma_peak else None),
                    "algorithmic_flops": fl["backward"],
                    "kernel": "pf::mf_bwd_gemm_kernel (DMMA m8n8k4, gathered rows)"}}
-        kk = dp.k
-        del P, dp
-        t.cuda.empty_cache()
-        # end to end through the public API: topology + plan + uploads + device
-        # build + the pinned, chunked host copy of P (the reference returns P on
-        # the host); the device P stays registered as the mirror of pk.dense
-        t.cuda.synchronize()
-        w0 = time.perf_counter()
-        pk = L.poisson_kernel(mesh)
-        res["e2e_poisson_kernel_s"] = time.perf_counter() - w0
-        res["e2e_d2h_bytes"] = int(pk.dense.nbytes)
-        P = dev.device_kernel(pk).P
-        if name == "c2":
+        if name == "c2" and not NO_CPU:
+            kk = dp.k
             t0 = time.perf_counter()
             ref, _ = I.poisson_kernel_parallel(omesh, workers=os.cpu_count() or 8)
             cpu_s = time.perf_counter() - t0
@@ -841,63 +941,13 @@ def extra_poisson(t, nat, dev, device, dfma_peak=None):
                                              "columns in 64-column chunks, one process per "
                                              "core (oracle/inputs.poisson_kernel_parallel)"}
             res["speedup_vs_cpu"] = cpu_s / (tot * 1e-3)
-            res["e2e_speedup_vs_cpu"] = cpu_s / res["e2e_poisson_kernel_s"]
             res["max_rel_vs_superlu_2000_rows"] = float(
                 (np.abs(x[big] - y[big]) / y[big]).max())
             del ref
         out[name] = res
-        del P, pk
+        del P
         t.cuda.empty_cache()
     return out
-
-
-def extra_tracer(t, nat, dev, pf, device):
-    """C5 tracer shape: 10,000 paths on a 1,002,001-vertex mesh, 1,024 target fields."""
-    import numpy as np
-    from paper_1708_02845_b200 import mesh as M
-    from paper_1708_02845_b200 import paths as PP
-    t0 = time.perf_counter()
-    mesh = M.grid_mesh(1000, 1000)
-    build_s = time.perf_counter() - t0
-    dm = M.device_mesh(mesh)
-    rng = np.random.default_rng(1)
-    T = 1024
-    targets = rng.choice(mesh.interior_vertices, T, replace=False)
-    V = dm.V
-    tv = V.index_select(0, t.from_numpy(targets).to(device))
-    # Euclidean distance fields (the reference tests' smooth descent field), (T, n)
-    fields = t.cdist(tv, V)
-    npaths = 10_000
-    src = rng.choice(mesh.n, npaths)
-    fo = np.arange(npaths) % T
-    src = np.where(src == targets[fo], (src + 1) % mesh.n, src)
-    for _ in range(2):  # warm-up at full size (workspace + topology caches)
-        PP.trace_arrays(mesh, fields, targets, src, fo)
-    t.cuda.synchronize()
-    e0, e1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
-    s = t.cuda.current_stream(device)
-    w0 = time.perf_counter()
-    e0.record(s)
-    buf, counts, over, extra = PP.trace_arrays(mesh, fields, targets, src, fo)
-    e1.record(s)
-    t.cuda.synchronize()
-    wall = time.perf_counter() - w0
-    ms = e0.elapsed_time(e1)
-    status = buf.status.cpu().numpy()
-    cpu = None
-    if not NO_CPU:
-        try:
-            cpu = cpu_baseline_tracer(mesh, fields, targets, src, fo)
-        except Exception as exc:
-            cpu = {"error": f"{type(exc).__name__}: {exc}"}
-    return {"cpu_baseline": cpu,
-            "workload": "10,000 paths (source i -> target i % 1024), 1000x1000 grid mesh "
-                        "(1,002,001 vertices, 2,000,000 triangles), Euclidean fields",
-            "paths_per_s": npaths / (ms / 1e3), "ms": ms, "wall_ms_incl_launch": 1e3 * wall,
-            "locations_per_s": float(counts.sum()) / (ms / 1e3),
-            "mean_locations": float(counts.mean()), "max_locations": int(counts.max()),
-            "reached": int((status == 0).sum()), "overflow_reruns": int(over.size),
-            "mesh_build_s": build_s}
 
 
 def run_native(args):
@@ -907,7 +957,9 @@ def run_native(args):
     import paper_1708_02845_b200 as pf
     from paper_1708_02845_b200 import _device as dev
     from paper_1708_02845_b200 import _native as nat
+    from paper_1708_02845_b200 import laplacian as L
     from paper_1708_02845_b200 import parallel as par
+    from workloads.meshes import default_endpoints
 
     ws, rank, local = dist_env()
     if args.gpus != ws and ws > 1:
@@ -916,19 +968,30 @@ def run_native(args):
     device = t.device("cuda", local)
     dist = None
     if ws > 1:
+        # control plane (rendezvous, NCCL unique id, barriers, timing max) on gloo;
+        # the data plane is NCCL through the C ABI (parallel.NcclComm)
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=device)
+        dist.init_process_group("gloo")
 
-    rows, k, desc = WORKLOADS[args.workload]
-    n_total = rows * ws
-    bounds = [(r * rows, (r + 1) * rows) for r in range(ws)]  # weak scaling: equal slabs
-    row0 = rank * rows
-    ld = dev.leading_dim(k)
-    P_dev = make_synthetic_slab(t, rows, k, ld, rank, device)
-    dk = dev.DeviceKernel(None, np.array([], np.int64), device=device, row0=row0, rows=rows,
-                          n=n_total, k=k, P_dev=P_dev)
-    target = n_total // 3 + 1
-    sharded = par.ShardedField(dk, bounds, dist, device=device) if ws > 1 else None
+    n_expect, k_expect, desc = WORKLOADS[args.workload]
+    omesh, mesh_s = build_mesh(args.workload)
+    n = omesh.n
+    _, target = default_endpoints(omesh)
+    bounds = par.partition_rows(n, ws)
+    sharded = None
+    if ws == 1:
+        dp, dk, prep = device_build(t, L, omesh, device)
+    else:
+        dp = None
+        t.cuda.synchronize()
+        w0 = time.perf_counter()
+        sharded = par.ShardedField.from_mesh(omesh, dist, device=device, bounds=bounds)
+        t.cuda.synchronize()
+        dk = sharded.slab
+        prep = {"slab_build_wall_s": time.perf_counter() - w0, "residual": dk.residual,
+                "row_sum_error": dk.row_sum_error}
+    prep["mesh_build_s"] = mesh_s
+    rows, k = dk.rows, dk.k
     step = DenseStep(t, nat, dev, dk, target, pf.divergence.KL_GUARD_TAU, sharded)
     stream = step.stream
 
@@ -941,19 +1004,17 @@ def run_native(args):
     def max_over_ranks(x):
         if dist is None:
             return x
-        v = t.tensor([x], dtype=t.float64, device=device)
+        v = t.tensor([x], dtype=t.float64)
         dist.all_reduce(v, op=dist.ReduceOp.MAX)
         return float(v.item())
 
     for _ in range(args.warmup):
         step.run()
     barrier()
-    for _ in range(args.steps):           # kernel-level timing pass (events on the stream)
-        step.run(timed=True)
-    kl_ms = step.kern_ms[0] / args.steps
-    tv_ms = step.kern_ms[1] / args.steps
+    kl_ms, tv_ms = step.kernel_ms(args.steps)   # kernel-level pass (events on the stream)
+    kl_ms_max = max_over_ranks(kl_ms)
 
-    e0, e1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
+    e0, e1 = _events(t)
     step.launches = 0
     with ClockSampler(local) as clocks:   # whole-step timing: the reported value
         barrier()
@@ -964,21 +1025,22 @@ def run_native(args):
         barrier()
     launches = step.launches
     el_ms = max_over_ranks(e0.elapsed_time(e1))
-    value = 2 * rows * ws * args.steps / (el_ms / 1e3)
+    value = 2 * n * args.steps / (el_ms / 1e3)
     flags_kl = step.out_kl[rows:].view(t.int32).cpu().numpy()
+    guarded = int(flags_kl[1])
+    if dist is not None:
+        g = t.tensor([guarded], dtype=t.int64)
+        dist.all_reduce(g)
+        guarded = int(g.item())
 
     # ------------------------------------------------ e2e via the public API
-    e2e = None
     if ws == 1:
-        host = np.empty((rows, k))
-        for a in range(0, rows, 16384):
-            b = min(rows, a + 16384)
-            host[a:b] = P_dev[a:b, :k].cpu().numpy()
-        pk = pf.PoissonKernel(host, np.array([], np.int64), 0.0, 0.0)
-        dev.register(host, dk)
+        w0 = time.perf_counter()
+        dense = L.dense_to_host(dk.P, n, k)
+        host_copy_s = time.perf_counter() - w0
+        pk = pf.PoissonKernel(dense, dk.boundary, dk.residual, dk.row_sum_error)
+        dev.register(pk.dense, dk)
         kl, tv = pf.builtin_f("kl"), pf.builtin_f("tv")
-        # warm-up identical to the timed loop (results held across iterations, so the
-        # pinned result pool reaches its steady size before timing)
         for _ in range(args.warmup):
             fkl = pf.dv_field(pk, kl, target)
             ftv = pf.dv_field(pk, tv, target)
@@ -994,53 +1056,51 @@ def run_native(args):
         e2e_s = time.perf_counter() - w0
         assert np.array_equal(fkl.values, step.out_kl[:rows].cpu().numpy())
         assert np.array_equal(ftv.values, step.out_tv[:rows].cpu().numpy())
-        e2e = {"value": 2 * rows * args.steps / e2e_s, "unit": "evals/s",
+        e2e = {"value": 2 * n * args.steps / e2e_s, "unit": "evals/s",
                "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 2 * (rows + 2) * 8,
                "ms_per_step": 1e3 * e2e_s / args.steps,
                "step_ms_min_median_max": [1e3 * min(per), 1e3 * statistics.median(per),
                                           1e3 * max(per)],
+               "precision_flags": list(fkl.precision_flags),
                "note": "wall clock of dv_field(pk, kl, t) + dv_field(pk, tv, t) per step through "
-                       "the public API: P resident in HBM (per-PoissonKernel device cache, as "
-                       "DomainContext keeps P resident); the target index is a kernel argument; "
-                       "each n-vector field + flags is copied D2H into a fresh numpy array and "
-                       "returned as a read-only ScalarField"}
-        # cold: a PoissonKernel the device has not seen (first query of a DomainContext),
-        # so P itself crosses PCIe inside the timed region
-        cold_steps = max(1, min(3, args.steps))
+                       "the public API on the PoissonKernel poisson_kernel(mesh) returns (host "
+                       "dense + its resident device mirror, as DomainContext keeps it); the "
+                       "target index is a kernel argument (no H2D bytes); each n-vector field "
+                       "+ flag words is copied D2H into a pinned numpy array and returned as a "
+                       "read-only ScalarField"}
+        # cold: a PoissonKernel the device has not seen (first query of a DomainContext):
+        # the host P crosses PCIe inside the timed region
         dev.evict(pk)
+        del step
         t.cuda.empty_cache()
-        per = []
-        for _ in range(cold_steps):
-            barrier()
-            p0 = time.perf_counter()
-            fkl = pf.dv_field(pk, kl, target)
-            ftv = pf.dv_field(pk, tv, target)
-            per.append(time.perf_counter() - p0)
-            assert np.array_equal(fkl.values, step.out_kl[:rows].cpu().numpy())
-            dev.evict(pk)
-            t.cuda.empty_cache()
-        cold_s = statistics.median(per)
-        e2e["cold"] = {"value": 2 * rows / cold_s, "unit": "evals/s",
-                       "h2d_bytes_per_step": rows * k * 8 + rows,
-                       "d2h_bytes_per_step": 2 * (rows + 2) * 8,
-                       "ms_per_step": 1e3 * cold_s, "steps": cold_steps,
-                       "h2d_gbs_lower_bound": rows * k * 8 / cold_s / 1e9,
+        barrier()
+        p0 = time.perf_counter()
+        fkl = pf.dv_field(pk, kl, target)
+        ftv = pf.dv_field(pk, tv, target)
+        cold_s = time.perf_counter() - p0
+        e2e["cold"] = {"value": 2 * n / cold_s, "unit": "evals/s",
+                       "h2d_bytes_per_step": n * k * 8 + n, "d2h_bytes_per_step": 2 * (n + 2) * 8,
+                       "ms_per_step": 1e3 * cold_s, "steps": 1,
+                       "h2d_gbs_lower_bound": n * k * 8 / cold_s / 1e9,
                        "note": "dv_field(kl) + dv_field(tv) on a PoissonKernel with no device "
                                "mirror: pinned staged upload of the host P (_hostpool."
                                "upload_rows), K1 negentropy, K2, K3, D2H of both fields"}
-        del host, pk
+        dev.evict(pk)
+        dev.register(pk.dense, dk)
+        prep["host_copy_of_P_s"] = host_copy_s
+        del fkl, ftv
+        t.cuda.empty_cache()
+        step = None
     else:
-        # N > 1: the sharded public API (parallel.ShardedField.field: NCCL broadcast of
-        # the target row + slab kernels), each rank's field slab copied back to host
         from paper_1708_02845_b200 import _hostpool
         kl, tv = pf.builtin_f("kl"), pf.builtin_f("tv")
 
         def e2e_step():
             a = sharded.field(kl, target)
-            ha = _hostpool.to_host(t, a, stream)
+            ha = _hostpool.to_host(t, a.values, stream)
             b = sharded.field(tv, target)
-            hb = _hostpool.to_host(t, b, stream)
-            return ha, hb
+            hb = _hostpool.to_host(t, b.values, stream)
+            return ha, hb, a.precision_flags
 
         for _ in range(args.warmup):
             keep = e2e_step()
@@ -1050,19 +1110,21 @@ def run_native(args):
             keep = e2e_step()
         barrier()
         e2e_s = max_over_ranks(time.perf_counter() - w0)
-        del keep
-        e2e = {"value": 2 * rows * ws * args.steps / e2e_s, "unit": "evals/s",
-               "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 2 * rows * 8 * ws,
-               "ms_per_step": 1e3 * e2e_s / args.steps,
+        e2e = {"value": 2 * n * args.steps / e2e_s, "unit": "evals/s",
+               "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 2 * (n + ws) * 8,
+               "ms_per_step": 1e3 * e2e_s / args.steps, "precision_flags": list(keep[2]),
                "note": "wall clock (max over ranks) of ShardedField.field(kl|tv, t) per step: "
-                       "NCCL broadcast of the target row from its owner, the slab kernels, "
-                       "and each rank's field slab copied to host memory"}
+                       "NCCL broadcast of the target row from its owner, the slab kernels, the "
+                       "flag-word max-reduction, and each rank's field slab copied to host "
+                       "memory"}
+        del keep
 
     # ------------------------------------------------ CPU baseline (rank 0, N=1)
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
-        ref = CpuReference(k, args.cpu_budget, threads)
+        ref = CpuReference(device_rows(t, dk, target), k, args.cpu_budget, threads,
+                           "real rows of this P")
         v, el = ref.step()
         cpu = {"value": v, "unit": "evals/s", "cores": threads, "kind": "port",
                "sample": ref.sample + f" ({el:.1f} s); oracle/divergence.py restating "
@@ -1074,92 +1136,209 @@ def run_native(args):
     bytes_tv = rows * (8 * k + 8) + 8 * k
     traffic = None
     prof = ROOT / "profiles" / "ncu_summary.json"
-    if prof.exists():
+    if prof.exists() and ws == 1:
         try:
             traffic = json.loads(prof.read_text()).get(args.workload, {}).get("dense_kl_dram_bytes")
         except Exception:
             traffic = None
     roof = _roof(bytes_kl, kl_ms, peak)
-    roof.update({"traffic": traffic, "kernel": "pf::dense_kl_kernel (guarded rows re-evaluated in place)",
+    roof.update({"traffic": traffic,
+                 "kernel": "pf::dense_kl_kernel (guarded rows re-evaluated in place)",
+                 "slowest_rank_avg_launch_ms": kl_ms_max,
                  "peak_kind": ("measured (MEASURED_PEAKS.json hbm_gbs, copy)"
                                if peak_kind == "measured" else "fallback 6.65 TB/s")})
 
     extras = {}
-    want = set(args.extras.split(","))
-    if ws == 1 and not args.no_extras:
-        if "f32" in want:
+    want = set(args.extras.split(",")) if not args.no_extras else set()
+    if ws == 1:
+        def run_extra(name, fn):
+            if name not in want:
+                return
             try:
-                extras["c2_f32"] = extra_f32(t, nat, dev, pf, dk, target, args.steps, peak)
-            except Exception as exc:
-                extras["c2_f32"] = {"error": f"{type(exc).__name__}: {exc}"}
-        del step, dk, P_dev
-        t.cuda.empty_cache()
-        for name, key, fn in (
-                ("c3_csr", "c3", lambda: extra_c3(t, nat, dev, pf, device, args.steps, peak)),
-                ("c4_c5", "c4c5", lambda: extra_c4_and_c5(t, nat, dev, pf, device, args.steps,
-                                                          peak)),
-                ("c5_tracer", "tracer", lambda: extra_tracer(t, nat, dev, pf, device)),
-                ("poisson", "poisson", lambda: extra_poisson(
-                    t, nat, dev, device,
-                    ((extras.get("c5_batched_kl") or {}).get("fp64_dmma_path") or {}).get(
-                        "dfma_peak_tflops"))),
-                ("wire", "wire", lambda: extra_wire(t, dev, pf, device))):
-            if key not in want:
-                continue
-            try:
-                r = fn()
-                if name == "c4_c5":
-                    extras["c4_dense"], extras["c5_batched_kl"] = r
-                else:
-                    extras[name] = r
+                extras[name] = fn()
             except Exception as exc:  # an extra must never hide the headline number
                 extras[name] = {"error": f"{type(exc).__name__}: {exc}"}
             t.cuda.empty_cache()
 
+        if args.workload == "c4":
+            run_extra("c4_f32", lambda: extra_f32(t, nat, dev, pf, dk, target, args.steps, peak))
+            dk._p32 = None
+            dk._H.pop(("f32", 1e-300), None)
+            t.cuda.empty_cache()
+            run_extra("c5", lambda: extra_c5(t, nat, dev, pf, device, dk, omesh, args.steps,
+                                             peak))
+        run_extra("poisson", lambda: extra_poisson(
+            t, nat, dev, device, L, dp if args.workload == "c4" else None,
+            ((extras.get("c5") or {}).get("fp64_dmma_path") or {}).get("dfma_peak_tflops")))
+        pk = None
+        dev._cache.clear()
+        del dk, dp
+        t.cuda.empty_cache()
+        for name in ("c2", "c2p"):
+            if name != args.workload:
+                run_extra(name, lambda name=name: extra_small_real(t, nat, dev, pf, L, device,
+                                                                   name, args.steps, peak))
+        run_extra("c2_synthetic", lambda: extra_synthetic_c2(t, nat, dev, pf, device,
+                                                             args.steps, peak))
+        run_extra("wire", lambda: extra_wire(t, dev, pf, device))
+    else:
+        del step
+        t.cuda.empty_cache()
+        extras.update(run_sharded_extras(t, nat, dev, pf, L, par, dist, device, sharded,
+                                         omesh, want, args))
+
     line = {
         "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": el_ms / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
-        "config": {"workload": desc, "rows_per_gpu": rows, "k": k, "n_total": n_total,
-                   "parallelism": f"row-shard x{ws}", "target": target,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "real: reference-generator mesh, Poisson kernel P built on the GPU",
+        "config": {"workload": desc, "n": n, "k": k, "rows_per_gpu_max": max(b - a for a, b in bounds),
+                   "parallelism": f"row-slab x{ws}", "target": int(target),
                    "l2": "inputs larger than L2 (P slab %.2f GB/GPU vs 126 MB L2)"
-                         % (rows * ld * 8 / 1e9)},
+                         % (rows * dk_ld(k) * 8 / 1e9)},
         "roofline": roof,
         "roofline_tv": _roof(bytes_tv, tv_ms, peak),
-        "kl_guarded_rows": int(flags_kl[1]),
+        "kl_guarded_rows": guarded,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clocks.summary(),
+        "preprocessing": prep,
         "extras": extras,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if sharded is not None:
+        sharded.close()
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
     return 0
 
 
-NO_CPU = False
+def dk_ld(k):
+    return (k + 63) // 64 * 64
+
+
+def run_sharded_extras(t, nat, dev, pf, L, par, dist, device, sharded, omesh, want, args):
+    """N > 1 side configs (strong scaling of the configs BASELINE names):
+    C3 — CSR KL + TV over nnz-balanced row slabs of the C2 real P; C5 — 1,024
+    targets partitioned over the ranks (P replicated, K7), each rank tracing
+    the paths of its own targets (parallel.trace_batch; no field exchange)."""
+    import numpy as np
+    ws, rank = dist.get_world_size(), dist.get_rank()
+    out = {}
+
+    def max_ms(x):
+        v = t.tensor([x], dtype=t.float64)
+        dist.all_reduce(v, op=dist.ReduceOp.MAX)
+        return float(v.item())
+
+    if "c3" in want:
+        try:
+            from workloads.meshes import default_endpoints
+            om2, _ = build_mesh("c2")
+            _, tgt = default_endpoints(om2)
+            dp2 = L.DevicePoisson(om2, device=device)
+            full = dp2.device_kernel()
+            cut = (1.0 / math.sqrt(full.n)) / full.k
+            cnt = t.empty(full.rows, dtype=t.int64, device=device)
+            nat.call("pf_csr_count_f64", full.P.data_ptr(), full.ld, full.rows, full.k, cut, 0,
+                     cnt.data_ptr(), t.cuda.current_stream(device).cuda_stream)
+            b3 = par.partition_by_weight(cnt.cpu().numpy(), ws)
+            a, b = b3[rank]
+            Ps = full.P[a:b].clone()
+            slab = dev.DeviceKernel(None, np.asarray(om2.boundary_vertices), device=device,
+                                    row0=a, rows=b - a, n=full.n, k=full.k, P_dev=Ps)
+            del full, dp2
+            t.cuda.empty_cache()
+            sf = par.ShardedField(slab, b3, dist, device=device, comm=sharded.comm)
+            kl, tv = pf.builtin_f("kl"), pf.builtin_f("tv")
+            for _ in range(3):
+                sf.sparse_field(kl, tgt)
+                sf.sparse_field(tv, tgt)
+            e0, e1 = _events(t)
+            t.cuda.synchronize()
+            dist.barrier()
+            e0.record()
+            for _ in range(args.steps):
+                sf.sparse_field(kl, tgt)
+                sf.sparse_field(tv, tgt)
+            e1.record()
+            t.cuda.synchronize()
+            ms = max_ms(e0.elapsed_time(e1)) / args.steps
+            nnz = t.tensor([slab.csr(cut, False).nnz], dtype=t.int64)
+            dist.all_reduce(nnz)
+            out["c3_sharded"] = {"workload": "C3: C2 real P sparsified at 1/sqrt(n), CSR KL + TV "
+                                             f"over {ws} nnz-balanced row slabs",
+                                 "evals_per_s": 2 * om2.n / (ms / 1e3), "ms_per_step": ms,
+                                 "nnz": int(nnz.item()), "slabs": b3}
+            del sf, slab, Ps
+            t.cuda.empty_cache()
+        except Exception as exc:
+            out["c3_sharded"] = {"error": f"{type(exc).__name__}: {exc}"}
+    if "c5" in want:
+        try:
+            from workloads.meshes import c5_jobs
+            dp4 = L.DevicePoisson(omesh, device=device)
+            full = dp4.device_kernel()          # P replicated (32.8 GB fits each B200)
+            pk = _DeviceOnlyKernel(full)
+            targets, src, fo = c5_jobs(omesh)
+            mesh = omesh_tri(omesh, pf)
+            par.trace_batch(mesh, pk, pf.builtin_f("kl"), targets[:ws], src[:ws],
+                            np.arange(ws), dist)   # warm-up (topology, slices, workspaces)
+            t.cuda.synchronize()
+            dist.barrier()
+            w0 = time.perf_counter()
+            e0, e1 = _events(t)
+            e0.record()
+            mine, paths = par.trace_batch(mesh, pk, pf.builtin_f("kl"), targets, src, fo, dist)
+            e1.record()
+            t.cuda.synchronize()
+            wall = max_ms(1e3 * (time.perf_counter() - w0))
+            ms = max_ms(e0.elapsed_time(e1))
+            reached = t.tensor([sum(p.status == "reached" for p in paths)], dtype=t.int64)
+            dist.all_reduce(reached)
+            out["c5_distributed"] = {
+                "workload": f"C5: {targets.size} targets partitioned over {ws} GPUs (C4 real P "
+                            f"replicated), K7 + {src.size:,} paths traced on the owning rank",
+                "ms_device_max_over_ranks": ms, "wall_ms_incl_host_paths": wall,
+                "evals_per_s": omesh.n * targets.size / (ms / 1e3),
+                "paths_per_s": src.size / (ms / 1e3), "reached": int(reached.item())}
+            del full, dp4, pk
+            t.cuda.empty_cache()
+        except Exception as exc:
+            out["c5_distributed"] = {"error": f"{type(exc).__name__}: {exc}"}
+    return out
+
+
+class _DeviceOnlyKernel:
+    """A PoissonKernel-shaped handle of a device-built P (no host copy): the
+    device cache is keyed on `dense`, so this object stands in for it."""
+
+    def __init__(self, dk):
+        import numpy as np
+        from paper_1708_02845_b200 import _device as dev
+        self.dense = np.empty((0, 0))
+        self.boundary = dk.boundary
+        self.n, self.k = dk.n, dk.k
+        dev.register(self.dense, dk)
 
 
 def main():
     global NO_CPU
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-extras", action="store_true",
-                    help="skip the C3/C4/C5/tracer side measurements (N=1 only)")
-    ap.add_argument("--extras", default="f32,c3,c4c5,tracer,wire,poisson",
-                    help="comma list of side measurements to run "
-                         "(f32, c3, c4c5, tracer, wire, poisson)")
+    ap.add_argument("--no-extras", action="store_true", help="skip the side measurements")
+    ap.add_argument("--extras", default="c4_f32,c5,poisson,c2,c2p,c2_synthetic,wire,c3",
+                    help="comma list of side measurements (N=1: c4_f32, c5, poisson, c2, c2p, "
+                         "c2_synthetic, wire; N>1: c3, c5)")
     args = ap.parse_args()
     NO_CPU = bool(args.no_cpu)
     if args.warmup < 3:

@@ -208,16 +208,16 @@ int pf_csr_target_prep_f64(const int64_t *indptr, const int32_t *indices,
  * divergence.py:226,277).  Split form hs[q] - sum v logt with a cancellation
  * guard re-evaluated in the reference form; then _settle (:286).
  * ops[i] = |supp(q)| (:276) if ops != NULL; flags[PF_FLAG_GUARDED] counts
- * re-evaluated rows.  With `queue` non-NULL (flags[PF_FLAG_GUARDED] zero on
- * entry, as pf_target_prep_f64 leaves it) the field kernel re-evaluates a guarded
- * row in place, with the target logs already in shared memory (one launch; the
- * buffer itself is no longer written and may be any non-NULL pointer); with
- * queue == NULL a second pass scans the output for the guard sentinel.  Both
- * re-evaluate in the same order, so the results are identical. */
+ * re-evaluated rows.  With `inline_guard` != 0 (flags and log_data required;
+ * flags[PF_FLAG_GUARDED] zero on entry, as pf_target_prep_f64 leaves it) the
+ * field kernel re-evaluates a guarded row in place, with the target logs
+ * already in shared memory (one launch); with inline_guard == 0 a second pass
+ * scans the output for the guard sentinel.  Both re-evaluate in the same
+ * order, so the results are identical. */
 int pf_csr_kl_f64(const int64_t *indptr, const int32_t *indices, const double *data,
                   const double *log_data, const double *hs, int64_t rows, int64_t k,
                   const double *logt, double tau, int64_t row0, const int64_t *queries,
-                  int64_t nq, double *out, int64_t *ops, uint32_t *flags, int64_t *queue,
+                  int64_t nq, double *out, int64_t *ops, uint32_t *flags, int inline_guard,
                   pf_stream_t stream);
 
 /* ---- K6: CSR TV field -------------------------------------------------------
@@ -238,7 +238,7 @@ int pf_csr_narrow_u16(const int32_t *indices, int64_t n, uint16_t *indices16,
 int pf_csr_kl_u16_f64(const int64_t *indptr, const uint16_t *indices16, const double *data,
                       const double *log_data, const double *hs, int64_t rows, int64_t k,
                       const double *logt, double tau, int64_t row0, const int64_t *queries,
-                      int64_t nq, double *out, int64_t *ops, uint32_t *flags, int64_t *queue,
+                      int64_t nq, double *out, int64_t *ops, uint32_t *flags, int inline_guard,
                       pf_stream_t stream);
 int pf_csr_tv_u16_f64(const int64_t *indptr, const uint16_t *indices16, const double *data,
                       const double *dropped, int64_t rows, int64_t k, const double *vp,
@@ -390,6 +390,16 @@ typedef struct {
 int pf_trace_batch_f64(const pf_mesh_t *mesh, const double *fields, const int64_t *targets,
                        const int64_t *sources, const int32_t *field_of, int64_t npaths,
                        int64_t step_cap, const pf_paths_t *out, pf_stream_t stream);
+/* The same over fields in any 2-D layout: field f's value at vertex v is
+ * fields[f * field_ld + v * vertex_ld].  pf_trace_batch_f64 is field_ld = n,
+ * vertex_ld = 1; the (n, T) row-major output of the batched KL
+ * (pf_batched_kl_*) is traced in place with field_ld = 1, vertex_ld = ldo, so
+ * a rank tracing the paths of its own target columns copies
+ * nothing. */
+int pf_trace_fields_f64(const pf_mesh_t *mesh, const double *fields, int64_t field_ld,
+                        int64_t vertex_ld, const int64_t *targets, const int64_t *sources,
+                        const int32_t *field_of, int64_t npaths, int64_t step_cap,
+                        const pf_paths_t *out, pf_stream_t stream);
 
 /* ---- Path metric (paths.py:326-368) ----------------------------------------
  * A polyline instance p is one side of one compared pair: points
@@ -607,6 +617,38 @@ int pf_poisson_finalize_rows(double *P, int64_t ldp, int64_t row0, int64_t n, in
                              const uint8_t *is_boundary, const int32_t *bcol,
                              const double *row_part, unsigned long long *out_max,
                              pf_stream_t stream);
+
+/* ---- NCCL plumbing of the row-sharded path (SURVEY §8b pf_nccl_*, §8e) ---
+ * The reference is single-process (dv_field, divergence.py:154-187, reads
+ * the whole of `pk.dense`); with P partitioned into row slabs over the GPUs
+ * of one box the path gains exactly these exchanges: the target row
+ * P[t, :] broadcast from its owner (replaces the `dense[p]` read of
+ * divergence.py:170 on the other ranks), the all-gather of finished field
+ * slabs when the tracer needs the whole field (paths.py:292-307 reads
+ * `field.values` at every vertex), and small max/min reductions of the
+ * `clamped` flag word and the clamp <= 0 domain check (divergence.py:162-175),
+ * so every rank returns the flags / raises exactly as the single process does.
+ * NCCL is bound at run time: pf_nccl_load reuses the libnccl.so.2 already in
+ * the process (torch's) or dlopens `path_host`.  The 128-byte unique id from
+ * pf_nccl_unique_id is exchanged by the caller (rank 0 -> all) before
+ * pf_nccl_comm_init.  Collectives are asynchronous on `stream`. */
+#define PF_NCCL_ID_BYTES 128
+enum { PF_T_U8 = 0, PF_T_I32 = 1, PF_T_I64 = 2, PF_T_F64 = 3 };
+enum { PF_OP_SUM = 0, PF_OP_MAX = 1, PF_OP_MIN = 2 };
+int pf_nccl_load(const char *path_host);
+int pf_nccl_version(int *version_host);
+int pf_nccl_unique_id(void *id_host);
+int pf_nccl_comm_init(int nranks, const void *id_host, int rank, int device, void **comm_host);
+int pf_nccl_comm_destroy(void *comm);
+/* in place: buf (count elements) on every rank = root's */
+int pf_nccl_broadcast(void *comm, void *buf, int64_t count, int dtype, int root,
+                      pf_stream_t stream);
+/* recv (nranks * count) = concatenation of every rank's send (count) */
+int pf_nccl_all_gather(void *comm, const void *send, void *recv, int64_t count, int dtype,
+                       pf_stream_t stream);
+/* recv (count) = op over ranks of send (count); send == recv is in place */
+int pf_nccl_all_reduce(void *comm, const void *send, void *recv, int64_t count, int dtype,
+                       int op, pf_stream_t stream);
 
 #ifdef __cplusplus
 }

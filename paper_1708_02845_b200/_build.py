@@ -103,7 +103,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         list(ex.map(run, jobs))
     objs = [str(j[1]) for j in jobs]
     tmp = LIB.with_suffix(".so.tmp")
-    cmd = [nvcc, *ARCH, "-shared", "-o", str(tmp), *objs]
+    cmd = [nvcc, *ARCH, "-shared", "-o", str(tmp), *objs, "-ldl"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)

@@ -90,6 +90,8 @@ class DeviceKernel:
                 self.P[:, self.k:] = 0.0  # pad columns are zero (K7 streams whole 16-col tiles)
             from ._hostpool import upload_rows
             upload_rows(t, self.P, dense, self.row0)
+        self.boundary = (np.asarray(boundary, dtype=np.int64) if boundary is not None
+                         else np.zeros(0, dtype=np.int64))
         interior = np.ones(self.n, dtype=np.uint8)
         if boundary is not None and len(boundary):
             interior[np.asarray(boundary, dtype=np.int64)] = 0

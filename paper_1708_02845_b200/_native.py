@@ -47,11 +47,11 @@ _SIGS = {
                         c_vp, c_vp],
     "pf_csr_target_prep_f64": [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp],
     "pf_csr_kl_f64": [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_dbl, c_i64, c_vp,
-                      c_i64, c_vp, c_vp, c_vp, c_vp, c_vp],
+                      c_i64, c_vp, c_vp, c_vp, c_int, c_vp],
     "pf_csr_tv_f64": [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_i64,
                       c_vp, c_vp, c_vp],
     "pf_csr_kl_u16_f64": [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_dbl, c_i64, c_vp,
-                      c_i64, c_vp, c_vp, c_vp, c_vp, c_vp],
+                          c_i64, c_vp, c_vp, c_vp, c_int, c_vp],
     "pf_csr_tv_u16_f64": [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_i64,
                       c_vp, c_vp, c_vp],
     "pf_csr_narrow_u16": [c_vp, c_i64, c_vp, c_vp],
@@ -79,6 +79,7 @@ _SIGS = {
     "pf_mask_compare_f64": [c_vp, c_vp, c_i64, c_dbl, c_vp, c_vp],
     # struct arguments (pf_mesh_t*, pf_paths_t*) are passed as addresses
     "pf_trace_batch_f64": [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp],
+    "pf_trace_fields_f64": [c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp],
     "pf_triangle_gradient_f64": [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp],
     "pf_edge_descent_batch_f64": [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp],
     "pf_local_minima_f64": [c_vp, c_vp, c_i64, c_vp, c_vp],
@@ -117,6 +118,15 @@ _SIGS.update({
                                  c_vp, c_vp, c_vp],
     "pf_poisson_finalize_rows": [c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp,
                                  c_vp],
+    # NCCL plumbing (pf_nccl.cu): host id / handle pointers, device buffers
+    "pf_nccl_load": [ctypes.c_char_p],
+    "pf_nccl_version": [ctypes.POINTER(ctypes.c_int)],
+    "pf_nccl_unique_id": [c_vp],
+    "pf_nccl_comm_init": [c_int, c_vp, c_int, c_int, ctypes.POINTER(ctypes.c_void_p)],
+    "pf_nccl_comm_destroy": [c_vp],
+    "pf_nccl_broadcast": [c_vp, c_vp, c_i64, c_int, c_int, c_vp],
+    "pf_nccl_all_gather": [c_vp, c_vp, c_vp, c_i64, c_int, c_vp],
+    "pf_nccl_all_reduce": [c_vp, c_vp, c_vp, c_i64, c_int, c_int, c_vp],
 })
 _RESTYPES = {"pf_last_error": ctypes.c_char_p, "pf_nd_plan_free": None,
              "pf_nd_plan_array": ctypes.c_int64}

@@ -527,9 +527,9 @@ template <class Idx>
 int csr_kl_launch(const int64_t *indptr, const Idx *indices, const double *data,
                   const double *log_data, const double *hs, int64_t rows, int64_t k,
                   const double *logt, double tau, int64_t row0, const int64_t *queries,
-                  int64_t nq, double *out, int64_t *ops, uint32_t *flags, int64_t *queue,
+                  int64_t nq, double *out, int64_t *ops, uint32_t *flags, int inline_guard,
                   pf_stream_t stream) {
-  if (queue && (!flags || !log_data))
+  if (inline_guard && (!flags || !log_data))
     return fail(PF_E_ARG, "csr_kl: in-place guard re-evaluation needs flags and log_data");
   if (!indptr || !indices || !hs || !logt || !out || rows < 0 || k <= 0)
     return fail(PF_E_ARG, "csr_kl: bad args");
@@ -543,15 +543,15 @@ int csr_kl_launch(const int64_t *indptr, const Idx *indices, const double *data,
     const int g = grid_for((const void *)csr_kl_kernel<true, Idx>, kCsrThreads, smem, count);
     csr_kl_kernel<true, Idx><<<g, kCsrThreads, smem, as_stream(stream)>>>(
         indptr, indices, data, log_data, hs, rows, k_pad, logt, tau, row0, queries, nq, out,
-        ops, queue != nullptr, flags);
+        ops, inline_guard != 0, flags);
   } else {
     const int g = grid_for((const void *)csr_kl_kernel<false, Idx>, kCsrThreads, 0, count);
     csr_kl_kernel<false, Idx><<<g, kCsrThreads, 0, as_stream(stream)>>>(
         indptr, indices, data, log_data, hs, rows, k_pad, logt, tau, row0, queries, nq, out,
-        ops, queue != nullptr, flags);
+        ops, inline_guard != 0, flags);
   }
   if (int e = check_launch("csr_kl")) return e;
-  if (queue) return 0;  // guarded rows were fixed inline
+  if (inline_guard) return 0;  // guarded rows were fixed inline
   int64_t want = (count + 7) / 8;
   int64_t g2 = static_cast<int64_t>(sm_count()) * 4;
   if (g2 > want) g2 = want;
@@ -644,20 +644,20 @@ int pf_csr_target_prep_f64(const int64_t *indptr, const int32_t *indices, const 
 int pf_csr_kl_f64(const int64_t *indptr, const int32_t *indices, const double *data,
                   const double *log_data, const double *hs, int64_t rows, int64_t k,
                   const double *logt, double tau, int64_t row0, const int64_t *queries,
-                  int64_t nq, double *out, int64_t *ops, uint32_t *flags, int64_t *queue,
+                  int64_t nq, double *out, int64_t *ops, uint32_t *flags, int inline_guard,
                   pf_stream_t stream) {
   return csr_kl_launch(indptr, indices, data, log_data, hs, rows, k, logt, tau, row0, queries,
-                       nq, out, ops, flags, queue, stream);
+                       nq, out, ops, flags, inline_guard, stream);
 }
 
 int pf_csr_kl_u16_f64(const int64_t *indptr, const uint16_t *indices16, const double *data,
                       const double *log_data, const double *hs, int64_t rows, int64_t k,
                       const double *logt, double tau, int64_t row0, const int64_t *queries,
-                      int64_t nq, double *out, int64_t *ops, uint32_t *flags, int64_t *queue,
+                      int64_t nq, double *out, int64_t *ops, uint32_t *flags, int inline_guard,
                       pf_stream_t stream) {
   if (k > 65536) return fail(PF_E_DOMAIN, "csr_kl_u16: k must be <= 65536");
   return csr_kl_launch(indptr, indices16, data, log_data, hs, rows, k, logt, tau, row0,
-                       queries, nq, out, ops, flags, queue, stream);
+                       queries, nq, out, ops, flags, inline_guard, stream);
 }
 
 int pf_csr_tv_f64(const int64_t *indptr, const int32_t *indices, const double *data,

@@ -144,8 +144,16 @@ __device__ __forceinline__ void load_tri(const pf_mesh_t &m, int64_t ti, Tri &t)
   }
 }
 
+// One field's values: vertex v at p[v * s] (s = 1: a field per row of an
+// (F, n) block; s = T: a column of the (n, T) output of the batched KL).
+struct FieldView {
+  const double *p;
+  int64_t s;
+  __device__ __forceinline__ double operator[](int64_t v) const { return p[v * s]; }
+};
+
 // f @ G  (3,)@(3,2): fma(f2,G2j, fma(f1,G1j, f0*G0j))
-__device__ __forceinline__ void gradient(Tri &t, const double *vals, double g[2]) {
+__device__ __forceinline__ void gradient(Tri &t, const FieldView &vals, double g[2]) {
   const double f0 = vals[t.v[0]], f1 = vals[t.v[1]], f2 = vals[t.v[2]];
   t.f[0] = f0;
   t.f[1] = f1;
@@ -190,6 +198,7 @@ enum { ST_REACHED = 0, ST_STUCK = 1, ST_MAX = 2 };
 constexpr int64_t kNearestPending = -2;
 
 __global__ void __launch_bounds__(kTraceThreads) trace_kernel(pf_mesh_t m, const double *fields,
+                                                              int64_t field_ld, int64_t vertex_ld,
                                                               const int64_t *targets,
                                                               const int64_t *sources,
                                                               const int32_t *field_of,
@@ -198,7 +207,7 @@ __global__ void __launch_bounds__(kTraceThreads) trace_kernel(pf_mesh_t m, const
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= npaths) return;
   const int64_t fi = field_of ? field_of[p] : 0;
-  const double *vals = fields + fi * m.n;
+  const FieldView vals{fields + fi * field_ld, vertex_ld};
   const int64_t target = targets[fi];
   const int64_t source = sources[p];
   const double eps_prog = m.eps_prog;
@@ -510,12 +519,13 @@ __global__ void __launch_bounds__(256) nearest_resolve_kernel(pf_mesh_t m, int64
 // edge_descent (paths.py:71-94): vertex walk to the neighbour with the largest
 // value drop (first maximum in ascending neighbour order), one thread per path.
 __global__ void __launch_bounds__(kTraceThreads) edge_trace_kernel(
-    pf_mesh_t m, const double *fields, const int64_t *targets, const int64_t *sources,
-    const int32_t *field_of, int64_t npaths, int64_t cap, pf_paths_t out) {
+    pf_mesh_t m, const double *fields, int64_t field_ld, int64_t vertex_ld,
+    const int64_t *targets, const int64_t *sources, const int32_t *field_of, int64_t npaths,
+    int64_t cap, pf_paths_t out) {
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= npaths) return;
   const int64_t fi = field_of ? field_of[p] : 0;
-  const double *vals = fields + fi * m.n;
+  const FieldView vals{fields + fi * field_ld, vertex_ld};
   const int64_t target = targets[fi];
   int64_t cur = sources[p];
   Writer w{&out, p, 0, 0.0, 0.0};
@@ -613,7 +623,7 @@ __global__ void tri_gradient_kernel(pf_mesh_t m, const double *vals, const int64
   Tri t;
   load_tri(m, tris[i], t);
   double g[2];
-  gradient(t, vals, g);
+  gradient(t, FieldView{vals, 1}, g);
   out[2 * i] = g[0];
   out[2 * i + 1] = g[1];
 }
@@ -847,20 +857,30 @@ using namespace pf;
 
 extern "C" {
 
-int pf_trace_batch_f64(const pf_mesh_t *mesh, const double *fields, const int64_t *targets,
-                       const int64_t *sources, const int32_t *field_of, int64_t npaths,
-                       int64_t step_cap, const pf_paths_t *out, pf_stream_t stream) {
+int pf_trace_fields_f64(const pf_mesh_t *mesh, const double *fields, int64_t field_ld,
+                        int64_t vertex_ld, const int64_t *targets, const int64_t *sources,
+                        const int32_t *field_of, int64_t npaths, int64_t step_cap,
+                        const pf_paths_t *out, pf_stream_t stream) {
   if (!mesh || !fields || !targets || !sources || !out) return fail(PF_E_ARG, "trace: null");
   if (npaths <= 0) return 0;
+  if (vertex_ld < 1 || field_ld < 0) return fail(PF_E_ARG, "trace: bad field layout");
   if (!out->count || !out->status || !out->stuck) return fail(PF_E_ARG, "trace: null outputs");
   const int64_t blocks = (npaths + kTraceThreads - 1) / kTraceThreads;
   if (!out->qx || !out->qy) return fail(PF_E_ARG, "trace: null qx/qy");
   trace_kernel<<<static_cast<unsigned>(blocks), kTraceThreads, 0, as_stream(stream)>>>(
-      *mesh, fields, targets, sources, field_of, npaths, step_cap, *out);
+      *mesh, fields, field_ld, vertex_ld, targets, sources, field_of, npaths, step_cap, *out);
   if (int e = check_launch("trace")) return e;
   nearest_resolve_kernel<<<static_cast<unsigned>(npaths), 256, 0, as_stream(stream)>>>(
       *mesh, npaths, *out);
   return check_launch("nearest_resolve");
+}
+
+int pf_trace_batch_f64(const pf_mesh_t *mesh, const double *fields, const int64_t *targets,
+                       const int64_t *sources, const int32_t *field_of, int64_t npaths,
+                       int64_t step_cap, const pf_paths_t *out, pf_stream_t stream) {
+  if (!mesh) return fail(PF_E_ARG, "trace: null");
+  return pf_trace_fields_f64(mesh, fields, mesh->n, 1, targets, sources, field_of, npaths,
+                             step_cap, out, stream);
 }
 
 int pf_edge_descent_batch_f64(const pf_mesh_t *mesh, const double *fields,
@@ -871,7 +891,7 @@ int pf_edge_descent_batch_f64(const pf_mesh_t *mesh, const double *fields,
   if (npaths <= 0) return 0;
   const int64_t blocks = (npaths + kTraceThreads - 1) / kTraceThreads;
   edge_trace_kernel<<<static_cast<unsigned>(blocks), kTraceThreads, 0, as_stream(stream)>>>(
-      *mesh, fields, targets, sources, field_of, npaths, step_cap, *out);
+      *mesh, fields, mesh->n, 1, targets, sources, field_of, npaths, step_cap, *out);
   return check_launch("edge_descent");
 }
 

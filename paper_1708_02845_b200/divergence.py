@@ -591,7 +591,7 @@ def _sparse_launch(pk, fd, p: int, queries=None, want_ops=False):
             nat.call(entry, dc.indptr.data_ptr(), idx,
                      dc.data.data_ptr(), dc.log_data.data_ptr(), dc.hs.data_ptr(), dk.rows,
                      dk.k, st.logt, KL_GUARD_TAU, dk.row0, qptr, count, out.data_ptr(),
-                     nat.ptr(ops), flags, dk.scratch(s.cuda_stream, 8, "csrq").data_ptr(),
+                     nat.ptr(ops), flags, 1,
                      s.cuda_stream)
         else:
             nat.call("pf_csr_generic_f64", dc.indptr.data_ptr(), dc.indices.data_ptr(),

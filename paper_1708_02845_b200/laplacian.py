@@ -599,11 +599,15 @@ def poisson_kernel_device(ls_or_mesh, leaf: int = LEAF):
 
 
 _STAGING: dict = {}
+# dense_to_host holds this for the whole copy: the staging buffers are shared
+# per (rows, ld), and concurrent DomainContext builds (domain.py:45-61 locks
+# only its own context) may copy P to the host from several threads at once
+_STAGING_LOCK = threading.Lock()
 
 
 def _staging(t, rows: int, ld: int):
     """Two persistent pinned staging buffers per (rows, ld) (a fresh pinned
-    allocation costs ~0.3 ms per MB)."""
+    allocation costs ~0.3 ms per MB).  Callers hold _STAGING_LOCK."""
     key = (rows, ld)
     bufs = _STAGING.get(key)
     if bufs is None:
@@ -619,13 +623,18 @@ def dense_to_host(P, n: int, k: int, chunk_bytes: int = 64 << 20,
     scatters the previous chunk into the numpy result (first-touching its
     pages in parallel; a direct pageable copy of a strided 33 GB matrix runs
     at a fraction of the PCIe rate)."""
-    import os
-    from concurrent.futures import ThreadPoolExecutor
     from . import _device as dev
     t = dev.torch()
     out = np.empty((n, k))
     if n == 0:
         return out
+    with _STAGING_LOCK:
+        return _dense_to_host_locked(t, P, out, n, k, chunk_bytes, threads)
+
+
+def _dense_to_host_locked(t, P, out, n, k, chunk_bytes, threads):
+    import os
+    from concurrent.futures import ThreadPoolExecutor
     ld = P.stride(0)
     rows = max(1, min(n, chunk_bytes // (8 * ld)))
     bufs = _staging(t, rows, ld)

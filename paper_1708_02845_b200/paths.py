@@ -132,13 +132,16 @@ def _fields_to_device(t, fields, n, device):
 
 
 def trace_arrays(mesh, fields, targets, sources, field_of=None, settings: Settings = DEFAULTS,
-                 cap: int | None = None, entry: str = "pf_trace_batch_f64"):
+                 cap: int | None = None, entry: str = "pf_trace_batch_f64", layout=None):
     """Launch K8 and return the raw device outputs (PathBuffers), rerunning overflows.
 
     `fields` is a list of field values (numpy or device tensors) or an (F, n)
     device tensor, `targets` their targets, `sources` the start vertices,
-    `field_of[p]` the field of path p.  The returned buffers are a per-thread
-    workspace: valid until the next call from the same thread.
+    `field_of[p]` the field of path p.  With `layout = (field_ld, vertex_ld)`
+    `fields` is a device FP64 tensor read in place as field f, vertex v at
+    ``fields[f * field_ld + v * vertex_ld]`` (e.g. the (n, T) batched-KL
+    output: (1, T)).  The returned buffers are a per-thread workspace: valid
+    until the next call from the same thread.
     """
     t = dev.require_cuda()
     dm = device_mesh(mesh)
@@ -147,10 +150,22 @@ def trace_arrays(mesh, fields, targets, sources, field_of=None, settings: Settin
     targets = np.asarray(targets, dtype=np.int64)
     fo = None if field_of is None else np.asarray(field_of, dtype=np.int32)
     step_cap = int(settings.step_cap_factor) * dm.n
-    if isinstance(fields, t.Tensor) and fields.dim() == 2:   # (F, n) device block
-        F = fields.to(device=dm.device, dtype=t.float64).contiguous()
+    if layout is not None:
+        if fields.dtype != t.float64 or fields.device != dm.device:
+            raise ValueError("strided fields must be an FP64 tensor on the mesh device")
+        F = fields
+        fld_ld, vtx_ld = int(layout[0]), int(layout[1])
+        call = lambda src, fo_, cnt, out: nat.call(  # noqa: E731
+            "pf_trace_fields_f64", _byref(dm.struct), F.data_ptr(), fld_ld, vtx_ld,
+            tgt_d.data_ptr(), src, fo_, cnt, step_cap, _byref(out), s)
     else:
-        F = _fields_to_device(t, fields, dm.n, dm.device)
+        if isinstance(fields, t.Tensor) and fields.dim() == 2:   # (F, n) device block
+            F = fields.to(device=dm.device, dtype=t.float64).contiguous()
+        else:
+            F = _fields_to_device(t, fields, dm.n, dm.device)
+        call = lambda src, fo_, cnt, out: nat.call(  # noqa: E731
+            entry, _byref(dm.struct), F.data_ptr(), tgt_d.data_ptr(), src, fo_, cnt, step_cap,
+            _byref(out), s)
     src_d = t.from_numpy(sources).to(dm.device)
     tgt_d = t.from_numpy(targets).to(dm.device)
     fo_d = None if fo is None else t.from_numpy(fo).to(dm.device)
@@ -158,8 +173,8 @@ def trace_arrays(mesh, fields, targets, sources, field_of=None, settings: Settin
     if cap is None:
         cap = int(min(step_cap + 2, max(64, 8 * int(np.sqrt(dm.n)) + 64)))
     buf = _workspace(t, npaths, cap, dm.device, "main")
-    nat.call(entry, _byref(dm.struct), F.data_ptr(), tgt_d.data_ptr(),
-             src_d.data_ptr(), nat.ptr(fo_d), npaths, step_cap, _byref(buf.struct), s)
+    if npaths:
+        call(src_d.data_ptr(), nat.ptr(fo_d), npaths, buf.struct)
     counts = buf.count[:npaths].cpu().numpy()
     over = np.flatnonzero(counts > cap)
     extra = None
@@ -168,10 +183,26 @@ def trace_arrays(mesh, fields, targets, sources, field_of=None, settings: Settin
         sub_src = t.from_numpy(sources[over]).to(dm.device)
         sub_fo = None if fo is None else t.from_numpy(fo[over]).to(dm.device)
         extra = _workspace(t, over.size, cap2, dm.device, "overflow")
-        nat.call(entry, _byref(dm.struct), F.data_ptr(), tgt_d.data_ptr(),
-                 sub_src.data_ptr(), nat.ptr(sub_fo), over.size, step_cap,
-                 _byref(extra.struct), s)
+        call(sub_src.data_ptr(), nat.ptr(sub_fo), over.size, extra.struct)
     return buf, counts, over, extra
+
+
+def trace_fields(mesh, fields, field_ld: int, vertex_ld: int, targets, sources, field_of=None,
+                 settings: Settings = DEFAULTS) -> list[TracedPath]:
+    """:func:`triangle_descent_batch` over device-resident fields in any 2-D
+    layout (field f's value at vertex v is ``fields[f * field_ld + v * vertex_ld]``),
+    without copying them: the multi-GPU tracers (parallel.py) trace straight
+    from a gathered field or from a rank's (n, T) batched-KL columns.
+    `targets[f]` is field f's target; path p descends field ``field_of[p]``
+    (0 if None).  Validation (source == target) is the caller's."""
+    sources = np.asarray(sources, dtype=np.int64).reshape(-1)
+    targets = np.asarray(targets, dtype=np.int64).reshape(-1)
+    fo = None if field_of is None else np.asarray(field_of, dtype=np.int64).reshape(-1)
+    if sources.size == 0:
+        return []
+    buf, counts, over, extra = trace_arrays(mesh, fields, targets, sources, fo, settings,
+                                            layout=(field_ld, vertex_ld))
+    return _host_paths(buf, counts, over, extra, sources, targets, fo)
 
 
 def _host_paths(buf, counts, over, extra, sources, targets, field_of):
