@@ -1,0 +1,21 @@
+"""pytest plugin: run the reference package's own test-suite on the B200 path.
+
+    python -m pytest -p paper_1708_02845_b200.pytest_plugin <pathfield tests>
+
+The reference binds its hot-path functions with ``from ... import`` at
+module import (SURVEY §8b patch points), so the bindings must be replaced
+before any test module or conftest imports them: this module calls
+:func:`integration.install` when pytest imports it (``-p`` plugins load
+before the initial conftests).  Every routed call then runs the sm_100a
+kernels; there is no CPU fallback, so a missing library or device fails the
+suite loudly.
+"""
+
+from . import integration as _integration
+
+PATCHED = _integration.install()
+
+
+def pytest_report_header(config):
+    sites = sum(len(v) for v in PATCHED.values())
+    return f"pathfield routed to the B200 path: {sites} bindings in {len(PATCHED)} modules"
