@@ -99,8 +99,8 @@ int pf_row_negentropy_f64(const double *P, int64_t ld, int64_t rows, int64_t k,
  * out[r] = sum_b c(Q_rb) * (-log(c(Pt_b)/c(Q_rb)))  for global row
  * row0 + r, evaluated as H[r] - sum_b c(Q_rb) * logt[b] with a cancellation
  * guard: rows with |out| < tau*(|H|+|cross|) are re-evaluated in the
- * reference's per-element form, in place by the same launch (counted in
- * flags[PF_FLAG_GUARDED]).  Then the settle rule (-1e-10,0) -> 0 and
+ * reference's per-element form by the same launch (counted in
+ * flags[PF_FLAG_GUARDED]; `ws` below).  Then the settle rule (-1e-10,0) -> 0 and
  * out[target-row0] = 0.  Replaces dv_field's kl evaluation
  * (divergence.py:170-182).  flags[PF_FLAG_CLAMPED] |= one-sided clamp on a
  * row with is_interior[r] != 0 (is_interior may be NULL = all interior). */
@@ -108,7 +108,18 @@ int pf_dense_kl_f64(const double *P, int64_t ld, int64_t rows, int64_t k,
                     const double *H, const double *tgt, const double *logt,
                     const uint8_t *tmask, double clamp, double tau,
                     int64_t row0, int64_t target, const uint8_t *is_interior,
-                    double *out, uint32_t *flags, pf_stream_t stream);
+                    double *out, uint32_t *flags, void *ws, int64_t ws_bytes,
+                    pf_stream_t stream);
+/* Workspace of the guarded rows (pf_dense_kl_f64, pf_dense_kl_f32): a
+ * guarded row is split into 512-element chunks queued grid-wide, so its
+ * per-element re-evaluation spreads over every warp and overlaps the stream
+ * instead of lengthening one warp; the summation order depends on k only, so
+ * the values are bitwise independent of the queue.  `ws` (16-byte aligned,
+ * ZERO-FILLED when allocated; each launch leaves it zeroed) holds
+ * pf_guard_ws_bytes(k, rows_cap) bytes for rows_cap queued rows; rows beyond
+ * the capacity, or every guarded row when ws is NULL, are evaluated by the warp
+ * that found them, with the same result. */
+int64_t pf_guard_ws_bytes(int64_t k, int64_t rows_cap);
 
 /* ---- K3: dense TV field ---------------------------------------------------
  * out[r] = sum_b |c(Q_rb) - c(Pt_b)|  (== sum c(Q)|1 - c(Pt)/c(Q)|, the
@@ -147,8 +158,11 @@ int pf_dense_at_f64(const double *P, int64_t ld, int64_t rows, int64_t k,
  * read from the FP32 copy (half the bytes); target row, logs, H and all
  * accumulation FP64.  Rows whose value cannot be certified to 1e-5 against
  * the FP32 rounding bound (|KL| < tau*(|H|+|cross|+1), |TV| < tau; tau = 1e-2)
- * are re-evaluated from the FP64 rows P64 in the reference form (count in
- * flags[PF_FLAG_GUARDED]).  Staging buffers as for K2/K3 (pf_target_prep_f64);
+ * are re-evaluated from the FP64 rows P64 (count in flags[PF_FLAG_GUARDED]):
+ * TV exactly; KL in the FP64 split form H64[r] - sum c(Q64) logt when H64
+ * (pf_row_negentropy_f64 of P64) is given, falling back to the reference form
+ * only where that cancels too (|KL| < tau64*(|H64|+|cross64|), the K2 guard),
+ * or directly in the reference form when H64 is NULL.  Staging buffers as for K2/K3 (pf_target_prep_f64);
  * tmask / is_interior are accepted for symmetry but unused: FP32 rounding
  * flushes sub-float-range entries to 0, so the `clamped` flag must come from
  * the FP64 rows — pf_mask_compare_f64 below plus pf_mask_uniform_f64.
@@ -161,7 +175,8 @@ int pf_row_negentropy_f32(const float *P, int64_t ld, int64_t rows, int64_t k, d
 int pf_dense_kl_f32(const float *P, int64_t ld, int64_t rows, int64_t k, const double *H,
                     const double *tgt, const double *logt, const uint8_t *tmask, double clamp,
                     double tau, int64_t row0, int64_t target, const uint8_t *is_interior,
-                    const double *P64, int64_t ld64, double *out, uint32_t *flags,
+                    const double *P64, int64_t ld64, const double *H64, double tau64,
+                    double *out, uint32_t *flags, void *ws, int64_t ws_bytes,
                     pf_stream_t stream);
 int pf_dense_tv_f32(const float *P, int64_t ld, int64_t rows, int64_t k, const double *tgt,
                     const uint8_t *tmask, double clamp, double tau, int64_t row0, int64_t target,
@@ -617,6 +632,37 @@ int pf_poisson_finalize_rows(double *P, int64_t ldp, int64_t row0, int64_t n, in
                              const uint8_t *is_boundary, const int32_t *bcol,
                              const double *row_part, unsigned long long *out_max,
                              pf_stream_t stream);
+
+/* ---- User-defined generators (divergence.py:42-56: FDivergence(name, f)) --
+ * The reference evaluates any numpy generator f as q * f(p / q) per element
+ * in dv_field / dv_at / dv_pair (:137-187).  The Python side traces f into a
+ * scalar CUDA expression of `x` (arithmetic, comparisons, ternaries and CUDA
+ * math functions only; _userf.py); pf_user_compile compiles it with NVRTC
+ * (loaded at run time: `nvrtc_path_host` or libnvrtc.so.12) for sm_100a into
+ * the two kernels below and, if `load`, loads them on the current device.
+ * pf_dense_user_f64 is pf_dense_generic_f64 with f = the expression (same
+ * settle, target zero, clamp flag, swap_order); pf_dense_user_at_f64 is
+ * pf_dense_at_f64 likewise; pf_csr_user_f64 below pf_csr_generic_f64 likewise.
+ * pf_user_cubin_size reports the cubin size (a
+ * compile-only check needs no device). */
+int pf_user_compile(const char *expr_host, const char *nvrtc_path_host, int load,
+                    void **handle_host);
+int pf_user_cubin_size(void *handle, int64_t *bytes_host);
+int pf_user_free(void *handle);
+int pf_dense_user_f64(void *handle, const double *P, int64_t ld, int64_t rows, int64_t k,
+                      const double *tgt, const uint8_t *tmask, double clamp, int swap_order,
+                      int64_t row0, int64_t target, const uint8_t *is_interior, double *out,
+                      uint32_t *flags, pf_stream_t stream);
+int pf_dense_user_at_f64(void *handle, const double *P, int64_t ld, int64_t rows, int64_t k,
+                         const double *tgt, double clamp, int swap_order, int64_t row0,
+                         int64_t target, const int64_t *queries, int64_t nq, double *out,
+                         pf_stream_t stream);
+/* pf_csr_generic_f64's union form (divergence.py:296-299) with f = the user
+ * expression: prow is the target's raw dense row, cut the row cut. */
+int pf_csr_user_f64(void *handle, const int64_t *indptr, const int32_t *indices,
+                    const double *data, int64_t rows, const double *prow, int64_t p_local,
+                    double cut, int64_t row0, const int64_t *queries, int64_t nq, double *out,
+                    int64_t *ops, pf_stream_t stream);
 
 /* ---- NCCL plumbing of the row-sharded path (SURVEY §8b pf_nccl_*, §8e) ---
  * The reference is single-process (dv_field, divergence.py:154-187, reads

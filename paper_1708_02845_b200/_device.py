@@ -90,11 +90,21 @@ class DeviceKernel:
                 self.P[:, self.k:] = 0.0  # pad columns are zero (K7 streams whole 16-col tiles)
             from ._hostpool import upload_rows
             upload_rows(t, self.P, dense, self.row0)
-        self.boundary = (np.asarray(boundary, dtype=np.int64) if boundary is not None
-                         else np.zeros(0, dtype=np.int64))
+        self.boundary = (np.asarray(boundary, dtype=np.int64).reshape(-1)
+                         if boundary is not None else np.zeros(0, dtype=np.int64))
         interior = np.ones(self.n, dtype=np.uint8)
-        if boundary is not None and len(boundary):
-            interior[np.asarray(boundary, dtype=np.int64)] = 0
+        # The reference accepts any `boundary` array and only indexes with it in
+        # dv_field's interior mask (divergence.py:173-174); keep out-of-range
+        # entries here and let dv_field raise numpy's IndexError (dv_pair /
+        # dv_at never read it).
+        ok = (self.boundary >= -self.n) & (self.boundary < self.n)
+        self.boundary_error = None
+        if not ok.all():
+            bad = int(self.boundary[~ok][0])
+            self.boundary_error = (f"index {bad} is out of bounds for axis 0 with size "
+                                   f"{self.n}")
+        if self.boundary.size:
+            interior[self.boundary[ok]] = 0
         self.is_interior = t.from_numpy(interior[self.row0:self.row0 + self.rows].copy()).to(self.device)
         self._H = {}
         self._csr = {}
@@ -225,6 +235,21 @@ class DeviceKernel:
             buf = t.empty(nbytes, dtype=t.uint8, device=self.device)
             self._scratch[key] = buf
         return buf
+
+    GUARD_ROWS = 16384   # guarded rows queued grid-wide per launch (pf_guard_ws_bytes)
+
+    def guard_ws(self, stream_handle: int):
+        """(pointer, bytes) of the zero-filled guarded-row workspace of the KL
+        field kernels, one per (thread, stream) — the kernels reset its header
+        per launch and leave the rest zeroed."""
+        key = (threading.get_ident(), stream_handle, "guard")
+        buf = self._scratch.get(key)
+        if buf is None:
+            t = torch()
+            nbytes = int(nat.load().pf_guard_ws_bytes(self.k, min(self.rows, self.GUARD_ROWS)))
+            buf = t.zeros(nbytes, dtype=t.uint8, device=self.device)
+            self._scratch[key] = buf
+        return buf.data_ptr(), buf.numel()
 
     def row_ptr(self, p: int) -> int:
         """Device address of row p of this slab."""

@@ -16,7 +16,8 @@
 // H[q] = sum_b c(Q) log c(Q) is the target-independent per-row negentropy
 // (K1, once per P): one FMA per element instead of a log.  Rows where the
 // split form cancels (|out| < tau (|H| + |cross|)) are re-evaluated in the
-// reference's per-element form c(Q) * -log(c(Pt)/c(Q)) by the same warp.
+// reference's per-element form c(Q) * -log(c(Pt)/c(Q)), chunked over every
+// warp of the grid through a work queue (pf_common.cuh, "guarded KL rows").
 #include <cmath>
 
 #include "pf_common.cuh"
@@ -157,28 +158,6 @@ __host__ __device__ inline size_t staged_smem_bytes(int64_t k_pad, int64_t m_pad
   return 16 + static_cast<size_t>(k_pad) * 8 + static_cast<size_t>(m_pad);
 }
 
-// The reference's per-element KL form of one row, q * -log(p/q) summed
-// (divergence.py:180), one warp, then settle: used for guarded rows, by the
-// field kernel in place (one warp, warp-uniform branch; no second pass).
-__device__ __forceinline__ double kl_reference_row(const double *__restrict__ prow, int64_t k,
-                                                   const double *__restrict__ tgt, double clamp,
-                                                   int lane) {
-  double b[4] = {0.0, 0.0, 0.0, 0.0};
-  int64_t e = lane;
-  for (; e + 96 < k; e += 128) {
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const double q = fmax(prow[e + 32 * u], clamp);
-      b[u] += __dmul_rn(q, -log(__ddiv_rn(tgt[e + 32 * u], q)));
-    }
-  }
-  for (; e < k; e += 32) {
-    const double q = fmax(prow[e], clamp);
-    b[0] += __dmul_rn(q, -log(__ddiv_rn(tgt[e], q)));
-  }
-  return settle(warp_sum((b[0] + b[1]) + (b[2] + b[3])));
-}
-
 // ------------------------------------------------------------ K2 dense KL --
 template <int U, int MINB, bool STAGE = true>
 __global__ void __launch_bounds__(kThreads, MINB) dense_kl_kernel(
@@ -186,8 +165,10 @@ __global__ void __launch_bounds__(kThreads, MINB) dense_kl_kernel(
     int64_t m_pad, const double *__restrict__ H, const double *__restrict__ tgt,
     const double *__restrict__ logt, const uint8_t *__restrict__ tmask, double clamp,
     double tau, int64_t row0, int64_t target, const uint8_t *__restrict__ is_interior,
-    double *__restrict__ out, uint32_t *__restrict__ flags) {
+    double *__restrict__ out, uint32_t *__restrict__ flags, void *guard_ws,
+    int64_t guard_ws_bytes) {
   extern __shared__ __align__(128) unsigned char smem[];
+  const GuardView gq = guard_view(guard_ws, guard_ws_bytes, k);  // grid-wide guarded rows
   // STAGE: target vector + mask in shared memory (one copy per CTA, TMA);
   // otherwise read through L1 (one copy per SM, shared by all its CTAs).
   const Staged st = STAGE ? stage_target(smem, logt, tmask, k_pad, m_pad) : Staged{logt, tmask};
@@ -233,17 +214,25 @@ __global__ void __launch_bounds__(kThreads, MINB) dense_kl_kernel(
     double val = h - cross;
     const bool is_t = (row0 + r == target);
     const bool guarded = !is_t && fabs(val) < tau * (fabs(h) + fabs(cross));  // warp-uniform
-    if (guarded) {
-      val = kl_reference_row(P + r * ld, k, tgt, clamp, lane);  // in place, no second pass
-      if (lane == 0) atomicAdd(&flags[PF_FLAG_GUARDED], 1u);
-    } else {
-      val = is_t ? 0.0 : settle(val);  // divergence.py:181-182
-    }
     const bool interior = is_interior ? (is_interior[r] != 0) : true;
     clamped_any |= interior && __any_sync(0xffffffffu, fl);
-    if (lane == 0) out[r] = val;
+    if (guarded) {
+      if (!guard_push(gq, r, lane)) {  // no room: evaluated here, same value
+        val = kl_reference_row_chunked(P + r * ld, k, tgt, clamp, lane);
+        if (lane == 0) {
+          out[r] = val;
+          atomicAdd(&flags[PF_FLAG_GUARDED], 1u);
+        }
+      }
+    } else {
+      val = is_t ? 0.0 : settle(val);  // divergence.py:181-182
+      if (lane == 0) out[r] = val;
+    }
+    guard_work(gq, P, ld, k, tgt, clamp, out, flags, true, lane);  // one pending chunk, if any
   }
   if (lane == 0 && clamped_any) atomicOr(&flags[PF_FLAG_CLAMPED], 1u);
+  while (guard_work(gq, P, ld, k, tgt, clamp, out, flags, true, lane)) {
+  }
 }
 
 // ------------------------------------------------------------ K3 dense TV --
@@ -451,12 +440,19 @@ int pf_row_negentropy_f64(const double *P, int64_t ld, int64_t rows, int64_t k, 
   return check_launch("row_negentropy");
 }
 
+int64_t pf_guard_ws_bytes(int64_t k, int64_t rows_cap) {
+  return 64 + rows_cap * (16 + 8 * guard_chunks(k > 0 ? k : 1));
+}
+
 int pf_dense_kl_f64(const double *P, int64_t ld, int64_t rows, int64_t k, const double *H,
                     const double *tgt, const double *logt, const uint8_t *tmask, double clamp,
                     double tau, int64_t row0, int64_t target, const uint8_t *is_interior,
-                    double *out, uint32_t *flags, pf_stream_t stream) {
+                    double *out, uint32_t *flags, void *ws, int64_t ws_bytes,
+                    pf_stream_t stream) {
   if (int e = check_dense_args(P, ld, rows, k)) return e;
   if (!H || !tgt || !logt || !tmask || !out || !flags) return fail(PF_E_ARG, "dense_kl: null");
+  if (ws && (ws_bytes < 64 || (reinterpret_cast<uintptr_t>(ws) & 15)))
+    return fail(PF_E_ARG, "dense_kl: workspace must be >= 64 bytes, 16-byte aligned");
   if (rows == 0) return 0;
   const int64_t k_pad = round_up(k, 2), m_pad = round_up(k, 16);
   auto kern = dense_kl_kernel<kU, kMinBlocks, true>;
@@ -466,10 +462,14 @@ int pf_dense_kl_f64(const double *P, int64_t ld, int64_t rows, int64_t k, const 
                            dense_kl_kernel<kU, kMinBlocks, false>, rows, k, as_stream(stream),
                            &kern, &grid, &smem))
     return e;
+  if (ws) {  // the work-queue header is per launch
+    const cudaError_t e = cudaMemsetAsync(ws, 0, 64, as_stream(stream));
+    if (e != cudaSuccess) return fail(static_cast<int>(e), "dense_kl: ws reset");
+  }
   kern<<<grid, kThreads, smem, as_stream(stream)>>>(P, ld, rows, k, k_pad, m_pad, H, tgt, logt,
                                                     tmask, clamp, tau, row0, target,
-                                                    is_interior, out, flags);
-  return check_launch("dense_kl");  // guarded rows were re-evaluated in place
+                                                    is_interior, out, flags, ws, ws ? ws_bytes : 0);
+  return check_launch("dense_kl");  // guarded rows were re-evaluated in the same launch
 }
 
 int pf_dense_tv_f64(const double *P, int64_t ld, int64_t rows, int64_t k, const double *tgt,

@@ -7,9 +7,13 @@
 //     |KL32 - KL64| <= eps32 * (|H| + |cross| + 1),   |TV32 - TV64| <= eps32,
 // (eps32 = 2^-24 relative per stored entry), so a row whose value is below
 // tau32 * (|H| + |cross| + 1) (KL) or tau32 (TV), tau32 = 1e-2, cannot be
-// certified to 1e-5 and is written as a sentinel; the fixup pass re-evaluates
-// it from the FP64 rows (reference per-element form), exactly as the FP64
-// guard does.  Unflagged rows carry <= 6e-6 relative error by that bound.
+// certified to 1e-5 and is re-evaluated from the FP64 rows in place by the
+// warp that found it: TV exactly (sum |c(Q) - c(Pt)|, one streaming pass); KL
+// in the FP64 split form H64 - sum c(Q) log c(Pt) (one streaming FMA pass,
+// ~1e-13 relative), and only if THAT cancels too (the FP64 guard, tau64) in
+// the reference's per-element form, evaluated by the whole CTA after its
+// loop exactly as the FP64 kernel does (pf_common.cuh GuardQueue).  Unflagged
+// rows carry <= 6e-6 relative error by the bound above.
 #include <cmath>
 
 #include "pf_common.cuh"
@@ -84,13 +88,34 @@ __device__ __forceinline__ double guard64_row(const double *__restrict__ prow, i
   return settle(warp_sum((b[0] + b[1]) + (b[2] + b[3])));
 }
 
+// FP64 split-form KL cross term sum_b c(Q_b) log c(Pt_b) of one FP64 row, one
+// warp, logs from the staged lo / hi planes (and the ragged tail).
+__device__ __forceinline__ double cross64_row(const double *__restrict__ prow, int64_t k,
+                                              const double2 *lo, const double2 *hi,
+                                              const double *tail, double clamp, int lane) {
+  const int64_t nq4 = k >> 2;
+  const double2 *row2 = reinterpret_cast<const double2 *>(prow);
+  double a0 = 0.0, a1 = 0.0;
+  for (int64_t i = lane; i < 2 * nq4; i += 32) {
+    const double2 v = ldg_stream2(row2 + i);
+    const double2 t = (i & 1) ? hi[i >> 1] : lo[i >> 1];
+    a0 = fma(fmax(v.x, clamp), t.x, a0);
+    a1 = fma(fmax(v.y, clamp), t.y, a1);
+  }
+  for (int64_t b = 4 * nq4 + lane; b < k; b += 32) a0 = fma(fmax(prow[b], clamp), tail[b - 4 * nq4], a0);
+  return warp_sum(a0 + a1);
+}
+
 template <bool KL>
 __global__ void __launch_bounds__(kT32, 4) dense32_kernel(
     const float *__restrict__ P, int64_t ld, int64_t rows, int64_t k,
     const double *__restrict__ H, const double *__restrict__ vec, double clamp, double tau,
     int64_t row0, int64_t target, const double *__restrict__ P64, int64_t ld64,
-    const double *__restrict__ tgt, double *__restrict__ out, uint32_t *__restrict__ flags) {
+    const double *__restrict__ H64, double tau64, const double *__restrict__ tgt,
+    double *__restrict__ out, uint32_t *__restrict__ flags, void *guard_ws,
+    int64_t guard_ws_bytes) {
   extern __shared__ __align__(128) unsigned char smem[];
+  const GuardView gq = guard_view(KL ? guard_ws : nullptr, guard_ws_bytes, k);
   const int64_t nq4 = k >> 2;  // full float4 groups
   double2 *lo = reinterpret_cast<double2 *>(smem);
   double2 *hi = lo + nq4;
@@ -145,13 +170,32 @@ __global__ void __launch_bounds__(kT32, 4) dense32_kernel(
     if (is_t) {
       val = 0.0;
     } else if (guard) {  // warp-uniform: re-evaluated in FP64 in place
-      val = guard64_row<KL>(P64 + r * ld64, k, tgt, clamp, lane);
       if (lane == 0) atomicAdd(&flags[PF_FLAG_GUARDED], 1u);
+      if (KL && H64) {
+        const double h64 = H64[r];
+        const double c64 = cross64_row(P64 + r * ld64, k, lo, hi, tail, clamp, lane);
+        val = h64 - c64;
+        if (fabs(val) < tau64 * (fabs(h64) + fabs(c64))) {  // the FP64 guard
+          if (guard_push(gq, r, lane)) {
+            guard_work(gq, P64, ld64, k, tgt, clamp, out, flags, false, lane);
+            continue;
+          }
+          val = kl_reference_row_chunked(P64 + r * ld64, k, tgt, clamp, lane);
+        } else {
+          val = settle(val);
+        }
+      } else {
+        val = guard64_row<KL>(P64 + r * ld64, k, tgt, clamp, lane);
+      }
     } else {
       val = settle(val);
     }
     if (lane == 0) out[r] = val;
+    if (KL) guard_work(gq, P64, ld64, k, tgt, clamp, out, flags, false, lane);
   }
+  if (KL)
+    while (guard_work(gq, P64, ld64, k, tgt, clamp, out, flags, false, lane)) {
+    }
 }
 
 // flag[0] |= 1 if the below-clamp masks of rows a and b differ (k entries).
@@ -177,8 +221,9 @@ __global__ void convert_f32_kernel(const double *__restrict__ P, int64_t ld, int
 template <bool KL>
 static int launch32(const float *P, int64_t ld, int64_t rows, int64_t k, const double *H,
                     const double *vec, double clamp, double tau, int64_t row0, int64_t target,
-                    const double *P64, int64_t ld64, const double *tgt, double *out,
-                    uint32_t *flags, cudaStream_t stream) {
+                    const double *P64, int64_t ld64, const double *H64, double tau64,
+                    const double *tgt, double *out, uint32_t *flags, void *ws, int64_t ws_bytes,
+                    cudaStream_t stream) {
   const size_t smem = static_cast<size_t>(k) * 8 + 32;
   if (smem > 200 * 1024) return fail(PF_E_DOMAIN, "dense32: k=%lld too large", (long long)k);
   auto kern = dense32_kernel<KL>;
@@ -188,8 +233,17 @@ static int launch32(const float *P, int64_t ld, int64_t rows, int64_t k, const d
   if (g > want) g = want;
   if (g < 1) g = 1;
   if (!P64 || !tgt || !flags) return fail(PF_E_ARG, "dense32: the FP64 guard needs P64, tgt, flags");
+  if ((ld64 & 1) || (reinterpret_cast<uintptr_t>(P64) & 15))
+    return fail(PF_E_ALIGN, "dense32: FP64 rows must be 16-byte aligned");
+  if (ws) {
+    if (ws_bytes < 64 || (reinterpret_cast<uintptr_t>(ws) & 15))
+      return fail(PF_E_ARG, "dense32: workspace must be >= 64 bytes, 16-byte aligned");
+    const cudaError_t e = cudaMemsetAsync(ws, 0, 64, stream);
+    if (e != cudaSuccess) return fail(static_cast<int>(e), "dense32: ws reset");
+  }
   kern<<<static_cast<int>(g), kT32, smem, stream>>>(P, ld, rows, k, H, vec, clamp, tau, row0,
-                                                    target, P64, ld64, tgt, out, flags);
+                                                    target, P64, ld64, H64, tau64, tgt, out,
+                                                    flags, ws, ws ? ws_bytes : 0);
   return check_launch("dense32");  // guarded rows were re-evaluated in place
 }
 
@@ -219,7 +273,8 @@ int pf_row_negentropy_f32(const float *P, int64_t ld, int64_t rows, int64_t k, d
 int pf_dense_kl_f32(const float *P, int64_t ld, int64_t rows, int64_t k, const double *H,
                     const double *tgt, const double *logt, const uint8_t *tmask, double clamp,
                     double tau, int64_t row0, int64_t target, const uint8_t *is_interior,
-                    const double *P64, int64_t ld64, double *out, uint32_t *flags,
+                    const double *P64, int64_t ld64, const double *H64, double tau64,
+                    double *out, uint32_t *flags, void *ws, int64_t ws_bytes,
                     pf_stream_t stream) {
   if (rows <= 0) return 0;
   if (!P || !H || !tgt || !logt || !tmask || !P64 || !out || !flags)
@@ -228,8 +283,8 @@ int pf_dense_kl_f32(const float *P, int64_t ld, int64_t rows, int64_t k, const d
     return fail(PF_E_ALIGN, "dense_kl_f32: FP32 rows must be 16-byte aligned");
   (void)tmask;
   (void)is_interior;
-  return launch32<true>(P, ld, rows, k, H, logt, clamp, tau, row0, target, P64, ld64, tgt, out,
-                        flags, as_stream(stream));
+  return launch32<true>(P, ld, rows, k, H, logt, clamp, tau, row0, target, P64, ld64, H64, tau64,
+                        tgt, out, flags, ws, ws_bytes, as_stream(stream));
 }
 
 int pf_dense_tv_f32(const float *P, int64_t ld, int64_t rows, int64_t k, const double *tgt,
@@ -242,8 +297,8 @@ int pf_dense_tv_f32(const float *P, int64_t ld, int64_t rows, int64_t k, const d
     return fail(PF_E_ALIGN, "dense_tv_f32: FP32 rows must be 16-byte aligned");
   (void)tmask;
   (void)is_interior;
-  return launch32<false>(P, ld, rows, k, nullptr, tgt, clamp, tau, row0, target, P64, ld64, tgt,
-                         out, flags, as_stream(stream));
+  return launch32<false>(P, ld, rows, k, nullptr, tgt, clamp, tau, row0, target, P64, ld64,
+                         nullptr, 0.0, tgt, out, flags, nullptr, 0, as_stream(stream));
 }
 
 int pf_mask_compare_f64(const double *a, const double *b, int64_t k, double clamp,

@@ -35,6 +35,7 @@ import numpy as np
 
 from . import _device as dev
 from . import _native as nat
+from . import _userf
 from .errors import DivergenceDomainError, InvalidTargetError
 from .solvers import PoissonKernel, ScalarField
 
@@ -110,18 +111,20 @@ def builtin_f(name: str, *, alpha: float | None = None,
 
 
 def _kind_param(fd) -> tuple[int, float]:
-    """Map a generator to its device functor; user generators are refused."""
-    kind = _KIND.get(fd.name)
-    if kind is None:
+    """The built-in device functor of a generator; NotImplementedError for a
+    user generator on a path that only has built-in kernels (the dense field
+    and dv_at paths compile user generators instead, _userf.py)."""
+    r = _userf.resolve(fd)
+    if r[0] != "builtin":
         raise NotImplementedError(
-            f"generator {fd.name!r} is a host callable; the device path evaluates the "
-            "built-in generators only (divergence.py:70-104)")
-    params = getattr(fd, "params", {}) or {}
-    if fd.name == "alpha":
-        return kind, float(params["alpha"])
-    if fd.name == "power-p":
-        return kind, float(params["power"])
-    return kind, 0.0
+            f"generator {fd.name!r} is user-defined; this path evaluates the built-in "
+            "generators only (divergence.py:70-104); dv_field / dv_at / dv_pair compile it")
+    return r[1], r[2]
+
+
+def _is_builtin(fd, name: str) -> bool:
+    """fd is the built-in generator `name` (by expression, not by name alone)."""
+    return getattr(fd, "name", None) == name and _userf.builtin_kind(fd) == _KIND[name]
 
 
 def _effective_clamp(dk, clamp) -> float:
@@ -163,12 +166,19 @@ def _field_device(pk, dk, fd, p: int, swap_order: bool, clamp: float, out_dev, f
         row_ptr = st.row.data_ptr()
     nat.call("pf_target_prep_f64", row_ptr, dk.k, clamp, st.tgt, st.logt, st.tmask,
              flags_ptr, stream)
-    kind, param = _kind_param(fd)
+    gen = _userf.resolve(fd)
+    if gen[0] == "user":   # NVRTC-compiled generator (csrc/pf_jit.cu)
+        nat.call("pf_dense_user_f64", gen[1].handle, dk.P.data_ptr(), dk.ld, dk.rows, dk.k,
+                 st.tgt, st.tmask, clamp, int(bool(swap_order)), dk.row0, p,
+                 dk.is_interior.data_ptr(), out_dev.data_ptr(), flags_ptr, stream)
+        return st
+    kind, param = gen[1], gen[2]
     if kind == 0 and not swap_order:
         H = dk.negentropy(clamp)
+        ws, wsb = dk.guard_ws(stream)
         nat.call("pf_dense_kl_f64", dk.P.data_ptr(), dk.ld, dk.rows, dk.k, H.data_ptr(),
                  st.tgt, st.logt, st.tmask, clamp, KL_GUARD_TAU, dk.row0, p,
-                 dk.is_interior.data_ptr(), out_dev.data_ptr(), flags_ptr, stream)
+                 dk.is_interior.data_ptr(), out_dev.data_ptr(), flags_ptr, ws, wsb, stream)
     elif kind == 1 and not swap_order:
         nat.call("pf_dense_tv_f64", dk.P.data_ptr(), dk.ld, dk.rows, dk.k, st.tgt, st.tmask,
                  clamp, dk.row0, p, dk.is_interior.data_ptr(), out_dev.data_ptr(),
@@ -218,6 +228,8 @@ def dv_field(pk: PoissonKernel, fd: FDivergence, p: int,
     if clamp is None:
         clamp = fd.clamp
     c = _effective_clamp(dk, clamp)
+    if c > 0.0 and dk.boundary_error:   # divergence.py:173-174 indexes with pk.boundary
+        raise IndexError(dk.boundary_error)
     s = t.cuda.current_stream(dk.device)
     # the device output is internal here (copied back before returning): reuse it
     buf = dk.scratch(s.cuda_stream, 8 * (dk.rows + 2), "out").view(t.float64)[:dk.rows + 2]
@@ -248,7 +260,7 @@ def dv_at(pk: PoissonKernel, fd: FDivergence, p: int, queries,
         raise IndexError(f"target {p} out of range")
     # divergence.py:140-148 applies np.maximum(., clamp) directly (no domain check).
     c = float(clamp)
-    kind, param = _kind_param(fd)
+    gen = _userf.resolve(fd)
     s = t.cuda.current_stream(dk.device)
     st = _Staging(t, dk.k, dk.device)
     row = dk.target_row(p)
@@ -256,9 +268,14 @@ def dv_at(pk: PoissonKernel, fd: FDivergence, p: int, queries,
              s.cuda_stream)
     qd = t.from_numpy(q).to(dk.device, non_blocking=False)
     out = t.empty(q.size, dtype=t.float64, device=dk.device)
-    nat.call("pf_dense_at_f64", dk.P.data_ptr(), dk.ld, dk.rows, dk.k, st.tgt, c, kind, param,
-             int(bool(swap_order)), dk.row0, p, qd.data_ptr(), q.size, out.data_ptr(),
-             s.cuda_stream)
+    if gen[0] == "user":
+        nat.call("pf_dense_user_at_f64", gen[1].handle, dk.P.data_ptr(), dk.ld, dk.rows, dk.k,
+                 st.tgt, c, int(bool(swap_order)), dk.row0, p, qd.data_ptr(), q.size,
+                 out.data_ptr(), s.cuda_stream)
+    else:
+        nat.call("pf_dense_at_f64", dk.P.data_ptr(), dk.ld, dk.rows, dk.k, st.tgt, c, gen[1],
+                 gen[2], int(bool(swap_order)), dk.row0, p, qd.data_ptr(), q.size,
+                 out.data_ptr(), s.cuda_stream)
     res = _to_host(t, out, s).copy()
     del st
     return res
@@ -296,7 +313,7 @@ def dv_field_f32_device(pk: PoissonKernel, fd: FDivergence, p: int, clamp: float
     HBM bytes); values within 1e-5 relative of the FP64 field (rows that the FP32
     rounding bound cannot certify are recomputed from the FP64 rows).
     Returns (values tensor, flags tensor) on the device."""
-    if fd.name not in ("kl", "tv"):
+    if not (_is_builtin(fd, "kl") or _is_builtin(fd, "tv")):
         raise NotImplementedError("FP32 storage mode implements kl and tv")
     if not 0 <= p < pk.n:
         raise InvalidTargetError(f"target {p} out of range")
@@ -311,11 +328,14 @@ def dv_field_f32_device(pk: PoissonKernel, fd: FDivergence, p: int, clamp: float
     row = dk.target_row(p)
     nat.call("pf_target_prep_f64", row.data_ptr(), dk.k, c, st.tgt, st.logt, st.tmask, flags,
              s.cuda_stream)
-    if fd.name == "kl":
+    if _is_builtin(fd, "kl"):
         H = dk.negentropy32(c)
+        H64 = dk.negentropy(c)   # FP64 split form for the guarded rows
+        ws, wsb = dk.guard_ws(s.cuda_stream)
         nat.call("pf_dense_kl_f32", P32.data_ptr(), ld32, dk.rows, dk.k, H.data_ptr(), st.tgt,
                  st.logt, st.tmask, c, F32_GUARD_TAU, dk.row0, p, dk.is_interior.data_ptr(),
-                 dk.P.data_ptr(), dk.ld, out.data_ptr(), flags, s.cuda_stream)
+                 dk.P.data_ptr(), dk.ld, H64.data_ptr(), KL_GUARD_TAU, out.data_ptr(), flags,
+                 ws, wsb, s.cuda_stream)
     else:
         nat.call("pf_dense_tv_f32", P32.data_ptr(), ld32, dk.rows, dk.k, st.tgt, st.tmask, c,
                  F32_GUARD_TAU, dk.row0, p, dk.is_interior.data_ptr(), dk.P.data_ptr(), dk.ld,
@@ -381,7 +401,7 @@ def dv_field_batch_device(pk: PoissonKernel, fd: FDivergence, targets, clamp=Non
     out = t.empty((dk.rows, max(T, 1)), dtype=t.float64, device=dk.device)
     if T == 0:
         return out[:, :0], np.zeros(0, dtype=bool)
-    if fd.name != "kl":
+    if not _is_builtin(fd, "kl"):
         flags = np.zeros(T, dtype=bool)
         for j, p in enumerate(targets):
             v, f = dv_field_device(pk, fd, int(p), clamp=clamp)
@@ -566,7 +586,17 @@ def _sparse_launch(pk, fd, p: int, queries=None, want_ops=False):
     """Launch K5/K6 (or the other-generator CSR kernels) for target p over all slab
     rows or `queries`; returns device tensors."""
     t = dev.require_cuda()
-    kind, param = _kind_param(fd)
+    # divergence.py:273-299 dispatches the sparse pair by NAME: kl / alpha over
+    # supp(q) with the dense log row, tv over the union plus dropped mass, and
+    # every other generator through fd.f over the union with the cut clamp
+    name = fd.name
+    if name == "alpha":
+        kind, param = _KIND["alpha"], float(fd.params["alpha"])
+    elif name in ("kl", "tv"):
+        kind, param = _KIND[name], 0.0
+    else:
+        gen = _userf.resolve(fd)
+        kind, param = (gen[1], gen[2]) if gen[0] == "builtin" else (-1, 0.0)
     dk, dc = _device_csr(pk)
     s = t.cuda.current_stream(dk.device)
     qd = None
@@ -582,11 +612,11 @@ def _sparse_launch(pk, fd, p: int, queries=None, want_ops=False):
     k_pad = dev.round_up(dk.k, 2)
     if not dk.owns(p):
         raise NotImplementedError("target row outside this slab: use parallel.ShardedField")
-    if fd.name in ("kl", "alpha"):
+    if name in ("kl", "alpha"):
         st = _Staging(t, dk.k, dk.device)
         nat.call("pf_target_prep_f64", dk.row_ptr(p), dk.k, _CLAMP_LOG, st.tgt, st.logt,
                  st.tmask, flags, s.cuda_stream)
-        if fd.name == "kl":
+        if name == "kl":
             entry, idx = dc.field_entry("kl")
             nat.call(entry, dc.indptr.data_ptr(), idx,
                      dc.data.data_ptr(), dc.log_data.data_ptr(), dc.hs.data_ptr(), dk.rows,
@@ -598,7 +628,7 @@ def _sparse_launch(pk, fd, p: int, queries=None, want_ops=False):
                      dc.data.data_ptr(), dc.log_data.data_ptr(), dk.rows, dk.k, kind, param,
                      0.0, 0, -1, st.logt, dk.row0, qptr, count, out.data_ptr(),
                      nat.ptr(ops), s.cuda_stream)
-    elif fd.name == "tv":
+    elif name == "tv":
         st = t.empty(k_pad + 4, dtype=t.float64, device=dk.device)
         nat.call("pf_csr_target_prep_f64", dc.indptr.data_ptr(), dc.indices.data_ptr(),
                  dc.data.data_ptr(), dc.dropped.data_ptr(), p - dk.row0, dk.k, st.data_ptr(),
@@ -613,10 +643,16 @@ def _sparse_launch(pk, fd, p: int, queries=None, want_ops=False):
         row_cut = getattr(pk, "row_cut", None)
         cut = float(row_cut) if row_cut and row_cut > 0 else float(fd.clamp)
         st = None
-        nat.call("pf_csr_generic_f64", dc.indptr.data_ptr(), dc.indices.data_ptr(),
-                 dc.data.data_ptr(), dc.log_data.data_ptr(), dk.rows, dk.k, kind, param, cut,
-                 dk.row_ptr(p), p - dk.row0, 0, dk.row0, qptr, count,
-                 out.data_ptr(), nat.ptr(ops), s.cuda_stream)
+        if kind < 0:   # a user generator: the NVRTC-compiled union kernel
+            nat.call("pf_csr_user_f64", gen[1].handle, dc.indptr.data_ptr(),
+                     dc.indices.data_ptr(), dc.data.data_ptr(), dk.rows, dk.row_ptr(p),
+                     p - dk.row0, cut, dk.row0, qptr, count, out.data_ptr(), nat.ptr(ops),
+                     s.cuda_stream)
+        else:
+            nat.call("pf_csr_generic_f64", dc.indptr.data_ptr(), dc.indices.data_ptr(),
+                     dc.data.data_ptr(), dc.log_data.data_ptr(), dk.rows, dk.k, kind, param,
+                     cut, dk.row_ptr(p), p - dk.row0, 0, dk.row0, qptr, count,
+                     out.data_ptr(), nat.ptr(ops), s.cuda_stream)
     return out, ops, count, s, st
 
 

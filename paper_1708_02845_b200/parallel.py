@@ -329,9 +329,10 @@ class ShardedField:
         if thr >= 1.0:
             raise ValueError(f"threshold {thr} >= 1 would empty rows")
         cut = thr / k
-        if fd.name == "kl":
+        from .divergence import _is_builtin
+        if _is_builtin(fd, "kl"):
             payload = self.target_row(p, k)
-        elif fd.name == "tv":
+        elif _is_builtin(fd, "tv"):
             own = owner_of(p, self.bounds)
             kp = k + (k & 1)
             payload = t.empty(kp + 4, dtype=t.float64, device=self.device)
@@ -373,7 +374,8 @@ class ShardedField:
         if targets.size and (targets.min() < 0 or targets.max() >= self.n):
             raise InvalidTargetError("target out of range")
         c = self._clamp(fd.clamp if clamp is None else clamp)
-        if fd.name != "kl":
+        from .divergence import _is_builtin
+        if not _is_builtin(fd, "kl"):
             res = [self.field(fd, int(p), clamp=clamp) for p in targets]
             vals = (t.stack([r.values for r in res], dim=1) if res
                     else t.zeros((self.slab.rows, 0), dtype=t.float64, device=self.device))

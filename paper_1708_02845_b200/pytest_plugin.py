@@ -16,6 +16,14 @@ from . import integration as _integration
 PATCHED = _integration.install()
 
 
-def pytest_report_header(config):
+def _banner() -> str:
     sites = sum(len(v) for v in PATCHED.values())
     return f"pathfield routed to the B200 path: {sites} bindings in {len(PATCHED)} modules"
+
+
+def pytest_report_header(config):
+    return _banner()
+
+
+def pytest_terminal_summary(terminalreporter, exitstatus, config):
+    terminalreporter.write_line(_banner())

@@ -310,7 +310,7 @@ def test_sharded_field_from_mesh_world1():
         assert bool((sf.slab.P == full).all())
         assert sf.slab.residual == res and sf.slab.row_sum_error == rse
         t0 = int(c.targets[0])
-        got = sf.field(pf.builtin_f("kl"), t0).cpu().numpy()
+        got = sf.field(pf.builtin_f("kl"), t0).values.cpu().numpy()
         ok, err = rel_close(got, c["field/kl/0"], 1e-10)
         assert ok, err
     finally:
