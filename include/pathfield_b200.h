@@ -248,6 +248,12 @@ int pf_csr_tv_f64(const int64_t *indptr, const int32_t *indices, const double *d
  * The same fields with the device CSR's columns narrowed to uint16
  * (pf_csr_narrow_u16, once per CSR): 10 instead of 12 streamed bytes per
  * entry (the algorithmic figure stays scipy's int32 layout). */
+/* The row-aligned device CSR in scipy's layout (what sparsify returns,
+ * divergence.py:221-226): entries of row r move to sp_indptr[r] (the exclusive
+ * prefix of the real row counts), pads dropped; o_data / o_log may be NULL. */
+int pf_csr_unpad(const int64_t *indptr, const int64_t *sp_indptr, int64_t rows,
+                 const int32_t *indices, const double *data, const double *log_data,
+                 int32_t *o_indices, double *o_data, double *o_log, pf_stream_t stream);
 int pf_csr_narrow_u16(const int32_t *indices, int64_t n, uint16_t *indices16,
                       pf_stream_t stream);
 int pf_csr_kl_u16_f64(const int64_t *indptr, const uint16_t *indices16, const double *data,

@@ -227,13 +227,15 @@ class DeviceKernel:
 
         Safe because every user of a scratch buffer enqueues on that same
         stream, so a later call's writes are ordered after the earlier call's
-        kernels."""
+        kernels; threads never share one."""
         key = (threading.get_ident(), stream_handle, tag)
-        buf = self._scratch.get(key)
+        with self._lock:
+            buf = self._scratch.get(key)
         if buf is None or buf.numel() < nbytes:
             t = torch()
             buf = t.empty(nbytes, dtype=t.uint8, device=self.device)
-            self._scratch[key] = buf
+            with self._lock:
+                self._scratch[key] = buf
         return buf
 
     GUARD_ROWS = 16384   # guarded rows queued grid-wide per launch (pf_guard_ws_bytes)
@@ -243,12 +245,14 @@ class DeviceKernel:
         field kernels, one per (thread, stream) — the kernels reset its header
         per launch and leave the rest zeroed."""
         key = (threading.get_ident(), stream_handle, "guard")
-        buf = self._scratch.get(key)
+        with self._lock:
+            buf = self._scratch.get(key)
         if buf is None:
             t = torch()
             nbytes = int(nat.load().pf_guard_ws_bytes(self.k, min(self.rows, self.GUARD_ROWS)))
             buf = t.zeros(nbytes, dtype=t.uint8, device=self.device)
-            self._scratch[key] = buf
+            with self._lock:
+                self._scratch[key] = buf
         return buf.data_ptr(), buf.numel()
 
     def row_ptr(self, p: int) -> int:
@@ -290,29 +294,38 @@ class DeviceCSR:
         self.dk, self.cut, self.strict = dk, cut, strict_positive
         rows, dev_ = dk.rows, dk.device
         s = t.cuda.current_stream(dev_).cuda_stream
-        self.rownnz = t.empty(rows, dtype=t.int64, device=dev_)
+        # per-row arrays in one allocation: rownnz, indptr (rows + 1), hs, dropped
+        rowbuf = t.empty(4 * rows + 1, dtype=t.int64, device=dev_)
+        self.rownnz = rowbuf[:rows]
         nat.call("pf_csr_count_f64", dk.P.data_ptr(), dk.ld, rows, dk.k, cut,
                  int(strict_positive), self.rownnz.data_ptr(), s)
-        self.indptr = t.zeros(rows + 1, dtype=t.int64, device=dev_)
+        self.indptr = rowbuf[rows:2 * rows + 1]
+        self.indptr[:1].zero_()
         t.cumsum(self.rownnz + (self.rownnz & 1), 0, out=self.indptr[1:])
-        self.nnz_pad = int(self.indptr[-1].item())
+        # the padded and the real totals in ONE host round trip
+        tot = t.stack([self.indptr[-1], self.rownnz.sum()]).cpu().tolist()
+        self.nnz_pad, self.nnz = int(tot[0]), int(tot[1])
         self.indptr[1:] |= self.rownnz & 1  # pad flag in bit 0 of the row's end offset
-        self.nnz = int(self.rownnz.sum().item())
+        self.hs = rowbuf[2 * rows + 1:3 * rows + 1].view(t.float64)
+        self.dropped = rowbuf[3 * rows + 1:].view(t.float64)
+        # entry arrays in one allocation: data, log_data (FP64), indices (i32),
+        # and the 16-bit column copy the K5/K6 field kernels stream (k <= 65,536:
+        # 10 instead of 12 bytes per entry)
         cap = max(self.nnz_pad, 1)
-        self.indices = t.empty(cap, dtype=t.int32, device=dev_)
-        self.data = t.empty(cap, dtype=t.float64, device=dev_)
-        self.log_data = t.empty(cap, dtype=t.float64, device=dev_)
-        self.hs = t.empty(rows, dtype=t.float64, device=dev_)
-        self.dropped = t.empty(rows, dtype=t.float64, device=dev_)
+        narrow = dk.k <= 65536
+        cap8 = (cap + 7) // 8 * 8
+        ent = t.empty(cap8 * (8 + 8 + 4 + (2 if narrow else 0)), dtype=t.uint8, device=dev_)
+        self._entries = ent
+        self.data = ent[:8 * cap8].view(t.float64)[:cap]
+        self.log_data = ent[8 * cap8:16 * cap8].view(t.float64)[:cap]
+        self.indices = ent[16 * cap8:20 * cap8].view(t.int32)[:cap]
         nat.call("pf_csr_fill_f64", dk.P.data_ptr(), dk.ld, rows, dk.k, cut,
                  int(strict_positive), self.indptr.data_ptr(), self.indices.data_ptr(),
                  self.data.data_ptr(), self.log_data.data_ptr(), self.hs.data_ptr(),
                  self.dropped.data_ptr(), s)
-        # 16-bit copy of the columns for the K5/K6 field kernels (k <= 65,536):
-        # 10 instead of 12 streamed bytes per entry
         self.indices16 = None
-        if dk.k <= 65536:
-            self.indices16 = t.empty(cap, dtype=t.int16, device=dev_)
+        if narrow:
+            self.indices16 = ent[20 * cap8:22 * cap8].view(t.int16)[:cap]
             nat.call("pf_csr_narrow_u16", self.indices.data_ptr(), self.nnz_pad,
                      self.indices16.data_ptr(), s)
 
@@ -325,6 +338,24 @@ class DeviceCSR:
 
     def owns(self, row: int) -> bool:
         return self.dk.owns(row)
+
+    def scipy_arrays(self, with_data: bool = True, with_log: bool = True):
+        """(indptr, indices, data, log_data) in scipy's unpadded layout, on the
+        device (pf_csr_unpad: one pass, no host round trip)."""
+        t = torch()
+        dev_ = self.dk.device
+        ip = self.scipy_indptr()
+        n = max(self.nnz, 1)
+        idx = t.empty(n, dtype=t.int32, device=dev_)
+        dat = t.empty(n, dtype=t.float64, device=dev_) if with_data else None
+        lg = t.empty(n, dtype=t.float64, device=dev_) if with_log else None
+        nat.call("pf_csr_unpad", self.indptr.data_ptr(), ip.data_ptr(), self.dk.rows,
+                 self.indices.data_ptr(), self.data.data_ptr(), self.log_data.data_ptr(),
+                 idx.data_ptr(), nat.ptr(dat), nat.ptr(lg),
+                 t.cuda.current_stream(dev_).cuda_stream)
+        m = self.nnz
+        return ip, idx[:m], (dat[:m] if dat is not None else None), (
+            lg[:m] if lg is not None else None)
 
     def real_mask(self):
         """Boolean mask over the padded arrays selecting the real entries."""
@@ -345,19 +376,72 @@ class DeviceCSR:
 
 _cache: dict[int, tuple[weakref.ref, DeviceKernel]] = {}
 _cache_lock = threading.Lock()
+_building: dict[int, threading.Lock] = {}   # per-array creation locks
+
+
+def _lookup(dense):
+    with _cache_lock:
+        hit = _cache.get(id(dense))
+        if hit is not None and hit[0]() is dense:
+            return hit[1]
+    return None
 
 
 def device_kernel(pk) -> DeviceKernel:
-    """The device mirror of ``pk.dense`` (uploaded on first use)."""
+    """The device mirror of ``pk.dense`` (uploaded on first use).
+
+    Reentrant (FastAPI serves dv_field from a thread pool, SURVEY §8b
+    "Threading"): concurrent first calls on the same kernel build ONE mirror —
+    the others wait on that array's creation lock — while calls on other
+    kernels proceed."""
     dense = pk.dense
-    key = id(dense)
+    dk = _lookup(dense)
+    if dk is not None:
+        return dk
     with _cache_lock:
-        hit = _cache.get(key)
-        if hit is not None and hit[0]() is dense:
-            return hit[1]
-    dk = DeviceKernel(dense, getattr(pk, "boundary", None))
-    register(dense, dk)
+        lk = _building.setdefault(id(dense), threading.Lock())
+    with lk:
+        dk = _lookup(dense)
+        if dk is None:
+            dk = DeviceKernel(dense, getattr(pk, "boundary", None))
+            register(dense, dk)
+    with _cache_lock:
+        if _building.get(id(dense)) is lk:
+            del _building[id(dense)]
     return dk
+
+
+# ---- device mirrors of returned fields ------------------------------------
+# dv_field copies the field to the host (the reference returns numpy); a
+# tracer call that follows on the same ScalarField (DomainContext.trace,
+# domain.py:86-96) reads this device copy instead of uploading the values
+# again.  Bounded: the most recent fields only.
+_FIELD_KEEP = 8
+_fields: dict[int, tuple] = {}
+_fields_order: list[int] = []
+
+
+def register_field(values, dev_values) -> None:
+    key = id(values)
+
+    def _drop(_ref, key=key):
+        with _cache_lock:
+            _fields.pop(key, None)
+
+    with _cache_lock:
+        _fields[key] = (weakref.ref(values, _drop), dev_values)
+        _fields_order.append(key)
+        while len(_fields_order) > _FIELD_KEEP:
+            _fields.pop(_fields_order.pop(0), None)
+
+
+def field_mirror(values):
+    """The device copy of a field's host values, if it is still registered."""
+    with _cache_lock:
+        hit = _fields.get(id(values))
+    if hit is not None and hit[0]() is values:
+        return hit[1]
+    return None
 
 
 def register(dense: np.ndarray, dk: DeviceKernel) -> DeviceKernel:

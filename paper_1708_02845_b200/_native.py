@@ -56,6 +56,7 @@ _SIGS = {
     "pf_csr_tv_u16_f64": [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_i64,
                       c_vp, c_vp, c_vp],
     "pf_csr_narrow_u16": [c_vp, c_i64, c_vp, c_vp],
+    "pf_csr_unpad": [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
     "pf_log_clamped_f64": [c_vp, c_i64, c_i64, c_i64, c_dbl, c_vp, c_vp],
     "pf_csr_generic_f64": [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_int, c_dbl, c_dbl, c_vp,
                            c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp],

@@ -585,6 +585,28 @@ int csr_tv_launch(const int64_t *indptr, const Idx *indices, const double *data,
   return check_launch("csr_tv");
 }
 
+// Row-aligned device CSR -> scipy's layout (no pads): warp per row copies its
+// entries to the row's scipy offset (the exclusive prefix of the real counts).
+__global__ void __launch_bounds__(kCsrThreads) csr_unpad_kernel(
+    const int64_t *__restrict__ indptr, const int64_t *__restrict__ sp_indptr, int64_t rows,
+    const int32_t *__restrict__ indices, const double *__restrict__ data,
+    const double *__restrict__ log_data, int32_t *__restrict__ o_indices,
+    double *__restrict__ o_data, double *__restrict__ o_log) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < rows; r += nwarps) {
+    int64_t lo, hi;
+    row_extent(indptr, data, r, lo, hi);
+    const int64_t d = sp_indptr[r] - lo;
+    for (int64_t e = lo + lane; e < hi; e += 32) {
+      o_indices[e + d] = indices[e];
+      if (o_data) o_data[e + d] = data[e];
+      if (o_log) o_log[e + d] = log_data[e];
+    }
+  }
+}
+
 __global__ void narrow_u16_kernel(const int32_t *__restrict__ in, int64_t n,
                                   uint16_t *__restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -675,6 +697,20 @@ int pf_csr_tv_u16_f64(const int64_t *indptr, const uint16_t *indices16, const do
   if (k > 65536) return fail(PF_E_DOMAIN, "csr_tv_u16: k must be <= 65536");
   return csr_tv_launch(indptr, indices16, data, dropped, rows, k, vp, tscal, row0, queries, nq,
                        out, ops, stream);
+}
+
+int pf_csr_unpad(const int64_t *indptr, const int64_t *sp_indptr, int64_t rows,
+                 const int32_t *indices, const double *data, const double *log_data,
+                 int32_t *o_indices, double *o_data, double *o_log, pf_stream_t stream) {
+  if (rows < 0 || (rows && (!indptr || !sp_indptr || !indices || !data || !o_indices)))
+    return fail(PF_E_ARG, "csr_unpad: bad args");
+  if (o_log && !log_data) return fail(PF_E_ARG, "csr_unpad: o_log needs log_data");
+  if (rows == 0) return 0;
+  const int g = grid_for((const void *)csr_unpad_kernel, kCsrThreads, 0, rows);
+  csr_unpad_kernel<<<g, kCsrThreads, 0, as_stream(stream)>>>(indptr, sp_indptr, rows, indices,
+                                                             data, log_data, o_indices, o_data,
+                                                             o_log);
+  return check_launch("csr_unpad");
 }
 
 int pf_csr_narrow_u16(const int32_t *indices, int64_t n, uint16_t *indices16,

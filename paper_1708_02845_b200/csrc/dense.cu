@@ -166,9 +166,10 @@ __global__ void __launch_bounds__(kThreads, MINB) dense_kl_kernel(
     const double *__restrict__ logt, const uint8_t *__restrict__ tmask, double clamp,
     double tau, int64_t row0, int64_t target, const uint8_t *__restrict__ is_interior,
     double *__restrict__ out, uint32_t *__restrict__ flags, void *guard_ws,
-    int64_t guard_ws_bytes) {
+    int64_t guard_ws_bytes, int64_t guard_mail) {
   extern __shared__ __align__(128) unsigned char smem[];
-  const GuardView gq = guard_view(guard_ws, guard_ws_bytes, k);  // grid-wide guarded rows
+  const GuardView gq = guard_view(guard_ws, guard_ws_bytes, k, guard_mail);  // guarded rows
+  unsigned int mail_head = 0;
   // STAGE: target vector + mask in shared memory (one copy per CTA, TMA);
   // otherwise read through L1 (one copy per SM, shared by all its CTAs).
   const Staged st = STAGE ? stage_target(smem, logt, tmask, k_pad, m_pad) : Staged{logt, tmask};
@@ -217,8 +218,8 @@ __global__ void __launch_bounds__(kThreads, MINB) dense_kl_kernel(
     const bool interior = is_interior ? (is_interior[r] != 0) : true;
     clamped_any |= interior && __any_sync(0xffffffffu, fl);
     if (guarded) {
-      if (!guard_push(gq, r, lane)) {  // no room: evaluated here, same value
-        val = kl_reference_row_chunked(P + r * ld, k, tgt, clamp, lane);
+      if (!guard_push(gq, r, P, ld, k, tgt, clamp, out, flags, true, lane)) {
+        val = kl_reference_row_chunked(P + r * ld, k, tgt, clamp, lane);  // same value
         if (lane == 0) {
           out[r] = val;
           atomicAdd(&flags[PF_FLAG_GUARDED], 1u);
@@ -228,11 +229,10 @@ __global__ void __launch_bounds__(kThreads, MINB) dense_kl_kernel(
       val = is_t ? 0.0 : settle(val);  // divergence.py:181-182
       if (lane == 0) out[r] = val;
     }
-    guard_work(gq, P, ld, k, tgt, clamp, out, flags, true, lane);  // one pending chunk, if any
+    guard_poll(gq, mail_head, false, P, ld, k, tgt, clamp, out, flags, true, lane);
   }
   if (lane == 0 && clamped_any) atomicOr(&flags[PF_FLAG_CLAMPED], 1u);
-  while (guard_work(gq, P, ld, k, tgt, clamp, out, flags, true, lane)) {
-  }
+  guard_poll(gq, mail_head, true, P, ld, k, tgt, clamp, out, flags, true, lane);
 }
 
 // ------------------------------------------------------------ K3 dense TV --
@@ -441,7 +441,7 @@ int pf_row_negentropy_f64(const double *P, int64_t ld, int64_t rows, int64_t k, 
 }
 
 int64_t pf_guard_ws_bytes(int64_t k, int64_t rows_cap) {
-  return 64 + rows_cap * (16 + 8 * guard_chunks(k > 0 ? k : 1));
+  return guard_fixed_bytes(guard_mailboxes()) + rows_cap * (16 + 8 * guard_chunks(k > 0 ? k : 1));
 }
 
 int pf_dense_kl_f64(const double *P, int64_t ld, int64_t rows, int64_t k, const double *H,
@@ -462,13 +462,15 @@ int pf_dense_kl_f64(const double *P, int64_t ld, int64_t rows, int64_t k, const 
                            dense_kl_kernel<kU, kMinBlocks, false>, rows, k, as_stream(stream),
                            &kern, &grid, &smem))
     return e;
-  if (ws) {  // the work-queue header is per launch
-    const cudaError_t e = cudaMemsetAsync(ws, 0, 64, as_stream(stream));
+  const int64_t mail = guard_mailboxes();
+  if (ws) {  // header + mailbox tail words are per launch
+    const cudaError_t e = cudaMemsetAsync(ws, 0, 64 + 4 * mail, as_stream(stream));
     if (e != cudaSuccess) return fail(static_cast<int>(e), "dense_kl: ws reset");
   }
   kern<<<grid, kThreads, smem, as_stream(stream)>>>(P, ld, rows, k, k_pad, m_pad, H, tgt, logt,
                                                     tmask, clamp, tau, row0, target,
-                                                    is_interior, out, flags, ws, ws ? ws_bytes : 0);
+                                                    is_interior, out, flags, ws,
+                                                    ws ? ws_bytes : 0, mail);
   return check_launch("dense_kl");  // guarded rows were re-evaluated in the same launch
 }
 

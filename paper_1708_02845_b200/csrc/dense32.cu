@@ -113,9 +113,10 @@ __global__ void __launch_bounds__(kT32, 4) dense32_kernel(
     int64_t row0, int64_t target, const double *__restrict__ P64, int64_t ld64,
     const double *__restrict__ H64, double tau64, const double *__restrict__ tgt,
     double *__restrict__ out, uint32_t *__restrict__ flags, void *guard_ws,
-    int64_t guard_ws_bytes) {
+    int64_t guard_ws_bytes, int64_t guard_mail) {
   extern __shared__ __align__(128) unsigned char smem[];
-  const GuardView gq = guard_view(KL ? guard_ws : nullptr, guard_ws_bytes, k);
+  const GuardView gq = guard_view(KL ? guard_ws : nullptr, guard_ws_bytes, k, guard_mail);
+  unsigned int mail_head = 0;
   const int64_t nq4 = k >> 2;  // full float4 groups
   double2 *lo = reinterpret_cast<double2 *>(smem);
   double2 *hi = lo + nq4;
@@ -176,8 +177,8 @@ __global__ void __launch_bounds__(kT32, 4) dense32_kernel(
         const double c64 = cross64_row(P64 + r * ld64, k, lo, hi, tail, clamp, lane);
         val = h64 - c64;
         if (fabs(val) < tau64 * (fabs(h64) + fabs(c64))) {  // the FP64 guard
-          if (guard_push(gq, r, lane)) {
-            guard_work(gq, P64, ld64, k, tgt, clamp, out, flags, false, lane);
+          if (guard_push(gq, r, P64, ld64, k, tgt, clamp, out, flags, false, lane)) {
+            guard_poll(gq, mail_head, false, P64, ld64, k, tgt, clamp, out, flags, false, lane);
             continue;
           }
           val = kl_reference_row_chunked(P64 + r * ld64, k, tgt, clamp, lane);
@@ -191,11 +192,9 @@ __global__ void __launch_bounds__(kT32, 4) dense32_kernel(
       val = settle(val);
     }
     if (lane == 0) out[r] = val;
-    if (KL) guard_work(gq, P64, ld64, k, tgt, clamp, out, flags, false, lane);
+    if (KL) guard_poll(gq, mail_head, false, P64, ld64, k, tgt, clamp, out, flags, false, lane);
   }
-  if (KL)
-    while (guard_work(gq, P64, ld64, k, tgt, clamp, out, flags, false, lane)) {
-    }
+  if (KL) guard_poll(gq, mail_head, true, P64, ld64, k, tgt, clamp, out, flags, false, lane);
 }
 
 // flag[0] |= 1 if the below-clamp masks of rows a and b differ (k entries).
@@ -238,12 +237,13 @@ static int launch32(const float *P, int64_t ld, int64_t rows, int64_t k, const d
   if (ws) {
     if (ws_bytes < 64 || (reinterpret_cast<uintptr_t>(ws) & 15))
       return fail(PF_E_ARG, "dense32: workspace must be >= 64 bytes, 16-byte aligned");
-    const cudaError_t e = cudaMemsetAsync(ws, 0, 64, stream);
+    const cudaError_t e = cudaMemsetAsync(ws, 0, 64 + 4 * guard_mailboxes(), stream);
     if (e != cudaSuccess) return fail(static_cast<int>(e), "dense32: ws reset");
   }
   kern<<<static_cast<int>(g), kT32, smem, stream>>>(P, ld, rows, k, H, vec, clamp, tau, row0,
                                                     target, P64, ld64, H64, tau64, tgt, out,
-                                                    flags, ws, ws ? ws_bytes : 0);
+                                                    flags, ws, ws ? ws_bytes : 0,
+                                                    guard_mailboxes());
   return check_launch("dense32");  // guarded rows were re-evaluated in place
 }
 

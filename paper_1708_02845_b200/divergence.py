@@ -231,13 +231,14 @@ def dv_field(pk: PoissonKernel, fd: FDivergence, p: int,
     if c > 0.0 and dk.boundary_error:   # divergence.py:173-174 indexes with pk.boundary
         raise IndexError(dk.boundary_error)
     s = t.cuda.current_stream(dk.device)
-    # the device output is internal here (copied back before returning): reuse it
-    buf = dk.scratch(s.cuda_stream, 8 * (dk.rows + 2), "out").view(t.float64)[:dk.rows + 2]
+    buf = t.empty(dk.rows + 2, dtype=t.float64, device=dk.device)
     flags_ptr = buf.data_ptr() + dk.rows * 8
     st = _field_device(pk, dk, fd, p, swap_order, c, buf, flags_ptr, s.cuda_stream)
     host = _to_host(t, buf, s)
     del st
     vals = host[:dk.rows]
+    # a tracer call on this field (DomainContext.trace) reads the device copy
+    dev.register_field(vals, buf[:dk.rows])
     flag_words = host[dk.rows:].view(np.uint32)
     fired = bool(flag_words[0]) and c > 0.0
     params = dict(getattr(fd, "params", {}) or {})
@@ -553,12 +554,15 @@ def sparsify(pk: PoissonKernel, threshold: float | None = None) -> PoissonKernel
     s = t.cuda.current_stream(dk.device)
     nnz = dc.nnz
     idx_dtype = np.int32 if nnz < 2 ** 31 else np.int64
-    keep = dc.real_mask()  # drop the row-alignment pads of the device layout
-    indptr = _to_host(t, dc.scipy_indptr(), s).astype(idx_dtype)
-    indices = _to_host(t, dc.indices[:dc.nnz_pad][keep], s).astype(idx_dtype, copy=False)
-    data = _to_host(t, dc.data[:dc.nnz_pad][keep], s)
-    logs = _to_host(t, dc.log_data[:dc.nnz_pad][keep], s)
-    dropped = _to_host(t, dc.dropped, s)
+    # scipy's layout (row-alignment pads dropped) on the device, then bulk
+    # downloads through pinned staging (_hostpool.download)
+    from ._hostpool import download
+    ip_d, idx_d, dat_d, log_d = dc.scipy_arrays()
+    indptr = download(t, ip_d).astype(idx_dtype)
+    indices = download(t, idx_d).astype(idx_dtype, copy=False)
+    data = download(t, dat_d)
+    logs = download(t, log_d)
+    dropped = _to_host(t, dc.dropped, s).copy()
     interior = np.ones(n, dtype=bool)
     interior[np.asarray(pk.boundary, dtype=np.int64)] = False
     m = int(interior.sum())
@@ -567,9 +571,10 @@ def sparsify(pk: PoissonKernel, threshold: float | None = None) -> PoissonKernel
         sparsity = 100.0 * (1.0 - nnz_interior / (m * k))
     else:
         sparsity = 0.0
+    # the reference's log view shares the pattern arrays (divergence.py:224-225)
     return dataclasses.replace(
         pk, threshold=float(threshold), sparse=_csr_host(data, indices, indptr, (n, k)),
-        log_sparse=_csr_host(logs, indices.copy(), indptr.copy(), (n, k)),
+        log_sparse=_csr_host(logs, indices, indptr, (n, k)),
         log_dense=LogDenseView(dk), dropped_mass=dropped, row_cut=float(cut),
         sparsity_percent=float(sparsity))
 

@@ -124,6 +124,10 @@ def _fields_to_device(t, fields, n, device):
     vals = []
     for f in fields:
         v = f if isinstance(f, t.Tensor) else (f.values if hasattr(f, "values") else f)
+        if isinstance(v, np.ndarray):   # a field dv_field returned: its device copy
+            mirror = dev.field_mirror(v)
+            if mirror is not None and mirror.device == device and mirror.numel() >= n:
+                v = mirror
         if isinstance(v, t.Tensor):
             vals.append(v.to(device=device, dtype=t.float64).reshape(-1)[:n])
         else:
