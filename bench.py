@@ -392,7 +392,6 @@ class DenseStep:
         self.ft = self.out_tv.data_ptr() + rows * 8
         self.H = dk.negentropy(1e-300)
         self.stream = t.cuda.current_stream(dk.device)
-        self.ws = dk.guard_ws(self.stream.cuda_stream)
         self.ev = [_events(t) for _ in range(2)]
         self.kern_ms = [0.0, 0.0]
         self.launches = 0
@@ -410,7 +409,7 @@ class DenseStep:
             self.ev[0][0].record(self.stream)
         nat.call("pf_dense_kl_f64", dk.P.data_ptr(), dk.ld, dk.rows, k, self.H.data_ptr(),
                  self.tgt, self.logt, self.tmask, 1e-300, self.tau, dk.row0, self.target,
-                 dk.is_interior.data_ptr(), self.out_kl.data_ptr(), self.fk, *self.ws, s)
+                 dk.is_interior.data_ptr(), self.out_kl.data_ptr(), self.fk, s)
         if timed:
             self.ev[0][1].record(self.stream)
         nat.call("pf_target_prep_f64", rowp, k, 1e-150, self.tgt, 0, self.tmask, self.ft, s)
@@ -483,7 +482,6 @@ def extra_f32(t, nat, dev, pf, dk, target, steps, peak):
     H32 = dk.negentropy32(1e-300)
     H64 = dk.negentropy(1e-300)
     s = t.cuda.current_stream(dk.device)
-    ws = dk.guard_ws(s.cuda_stream)
     k_pad, m_pad = dev.round_up(k, 2), dev.round_up(k, 16)
     stage = t.empty(16 * k_pad + m_pad, dtype=t.uint8, device=dk.device)
     tgt, logt, tmask = stage.data_ptr(), stage.data_ptr() + 8 * k_pad, stage.data_ptr() + 16 * k_pad
@@ -501,8 +499,7 @@ def extra_f32(t, nat, dev, pf, dk, target, steps, peak):
             ev[0].record(s)
         nat.call("pf_dense_kl_f32", P32.data_ptr(), ld32, rows, k, H32.data_ptr(), tgt, logt, tmask,
                  1e-300, tau, dk.row0, target, dk.is_interior.data_ptr(), dk.P.data_ptr(), dk.ld,
-                 H64.data_ptr(), pf.divergence.KL_GUARD_TAU, out.data_ptr(), fl, *ws,
-                 s.cuda_stream)
+                 H64.data_ptr(), pf.divergence.KL_GUARD_TAU, out.data_ptr(), fl, s.cuda_stream)
         if timed:
             ev[1].record(s)
             s.synchronize()

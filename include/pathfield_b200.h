@@ -99,8 +99,9 @@ int pf_row_negentropy_f64(const double *P, int64_t ld, int64_t rows, int64_t k,
  * out[r] = sum_b c(Q_rb) * (-log(c(Pt_b)/c(Q_rb)))  for global row
  * row0 + r, evaluated as H[r] - sum_b c(Q_rb) * logt[b] with a cancellation
  * guard: rows with |out| < tau*(|H|+|cross|) are re-evaluated in the
- * reference's per-element form by the same launch (counted in
- * flags[PF_FLAG_GUARDED]; `ws` below).  Then the settle rule (-1e-10,0) -> 0 and
+ * reference's per-element form by the same launch — in 512-element chunks
+ * shared by the warps of the CTA that found them, summed in an order fixed by
+ * k alone (counted in flags[PF_FLAG_GUARDED]).  Then the settle rule (-1e-10,0) -> 0 and
  * out[target-row0] = 0.  Replaces dv_field's kl evaluation
  * (divergence.py:170-182).  flags[PF_FLAG_CLAMPED] |= one-sided clamp on a
  * row with is_interior[r] != 0 (is_interior may be NULL = all interior). */
@@ -108,18 +109,7 @@ int pf_dense_kl_f64(const double *P, int64_t ld, int64_t rows, int64_t k,
                     const double *H, const double *tgt, const double *logt,
                     const uint8_t *tmask, double clamp, double tau,
                     int64_t row0, int64_t target, const uint8_t *is_interior,
-                    double *out, uint32_t *flags, void *ws, int64_t ws_bytes,
-                    pf_stream_t stream);
-/* Workspace of the guarded rows (pf_dense_kl_f64, pf_dense_kl_f32): a
- * guarded row is split into 512-element chunks queued grid-wide, so its
- * per-element re-evaluation spreads over every warp and overlaps the stream
- * instead of lengthening one warp; the summation order depends on k only, so
- * the values are bitwise independent of the queue.  `ws` (16-byte aligned,
- * ZERO-FILLED when allocated; each launch leaves it zeroed) holds
- * pf_guard_ws_bytes(k, rows_cap) bytes for rows_cap queued rows; rows beyond
- * the capacity, or every guarded row when ws is NULL, are evaluated by the warp
- * that found them, with the same result. */
-int64_t pf_guard_ws_bytes(int64_t k, int64_t rows_cap);
+                    double *out, uint32_t *flags, pf_stream_t stream);
 
 /* ---- K3: dense TV field ---------------------------------------------------
  * out[r] = sum_b |c(Q_rb) - c(Pt_b)|  (== sum c(Q)|1 - c(Pt)/c(Q)|, the
@@ -176,8 +166,7 @@ int pf_dense_kl_f32(const float *P, int64_t ld, int64_t rows, int64_t k, const d
                     const double *tgt, const double *logt, const uint8_t *tmask, double clamp,
                     double tau, int64_t row0, int64_t target, const uint8_t *is_interior,
                     const double *P64, int64_t ld64, const double *H64, double tau64,
-                    double *out, uint32_t *flags, void *ws, int64_t ws_bytes,
-                    pf_stream_t stream);
+                    double *out, uint32_t *flags, pf_stream_t stream);
 int pf_dense_tv_f32(const float *P, int64_t ld, int64_t rows, int64_t k, const double *tgt,
                     const uint8_t *tmask, double clamp, double tau, int64_t row0, int64_t target,
                     const uint8_t *is_interior, const double *P64, int64_t ld64, double *out,

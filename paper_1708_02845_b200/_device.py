@@ -238,23 +238,6 @@ class DeviceKernel:
                 self._scratch[key] = buf
         return buf
 
-    GUARD_ROWS = 16384   # guarded rows queued grid-wide per launch (pf_guard_ws_bytes)
-
-    def guard_ws(self, stream_handle: int):
-        """(pointer, bytes) of the zero-filled guarded-row workspace of the KL
-        field kernels, one per (thread, stream) — the kernels reset its header
-        per launch and leave the rest zeroed."""
-        key = (threading.get_ident(), stream_handle, "guard")
-        with self._lock:
-            buf = self._scratch.get(key)
-        if buf is None:
-            t = torch()
-            nbytes = int(nat.load().pf_guard_ws_bytes(self.k, min(self.rows, self.GUARD_ROWS)))
-            buf = t.zeros(nbytes, dtype=t.uint8, device=self.device)
-            with self._lock:
-                self._scratch[key] = buf
-        return buf.data_ptr(), buf.numel()
-
     def row_ptr(self, p: int) -> int:
         """Device address of row p of this slab."""
         return self.P.data_ptr() + (p - self.row0) * self.ld * 8

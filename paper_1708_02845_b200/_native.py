@@ -35,8 +35,7 @@ _SIGS = {
     "pf_target_prep_f64": [c_vp, c_i64, c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp],
     "pf_row_negentropy_f64": [c_vp, c_i64, c_i64, c_i64, c_dbl, c_vp, c_vp, c_vp],
     "pf_dense_kl_f64": [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_dbl, c_dbl,
-                        c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp],
-    "pf_guard_ws_bytes": [c_i64, c_i64],
+                        c_i64, c_i64, c_vp, c_vp, c_vp, c_vp],
     "pf_dense_tv_f64": [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_dbl, c_i64, c_i64, c_vp,
                         c_vp, c_vp, c_vp],
     "pf_dense_generic_f64": [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_dbl, c_int, c_dbl,
@@ -75,7 +74,7 @@ _SIGS = {
     "pf_convert_f32": [c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp],
     "pf_row_negentropy_f32": [c_vp, c_i64, c_i64, c_i64, c_dbl, c_vp, c_vp],
     "pf_dense_kl_f32": [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_dbl, c_dbl, c_i64,
-                        c_i64, c_vp, c_vp, c_i64, c_vp, c_dbl, c_vp, c_vp, c_vp, c_i64, c_vp],
+                        c_i64, c_vp, c_vp, c_i64, c_vp, c_dbl, c_vp, c_vp, c_vp],
     "pf_dense_tv_f32": [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_dbl, c_dbl, c_i64, c_i64, c_vp,
                         c_vp, c_i64, c_vp, c_vp, c_vp],
     "pf_mask_compare_f64": [c_vp, c_vp, c_i64, c_dbl, c_vp, c_vp],
@@ -141,7 +140,7 @@ _SIGS.update({
     "pf_nccl_all_reduce": [c_vp, c_vp, c_vp, c_i64, c_int, c_int, c_vp],
 })
 _RESTYPES = {"pf_last_error": ctypes.c_char_p, "pf_nd_plan_free": None,
-             "pf_nd_plan_array": ctypes.c_int64, "pf_guard_ws_bytes": ctypes.c_int64}
+             "pf_nd_plan_array": ctypes.c_int64}
 
 
 

@@ -16,8 +16,8 @@
 // H[q] = sum_b c(Q) log c(Q) is the target-independent per-row negentropy
 // (K1, once per P): one FMA per element instead of a log.  Rows where the
 // split form cancels (|out| < tau (|H| + |cross|)) are re-evaluated in the
-// reference's per-element form c(Q) * -log(c(Pt)/c(Q)), chunked over every
-// warp of the grid through a work queue (pf_common.cuh, "guarded KL rows").
+// reference's per-element form c(Q) * -log(c(Pt)/c(Q)), chunk-wise by the
+// warps of the CTA that found them (pf_common.cuh, "guarded KL rows").
 #include <cmath>
 
 #include "pf_common.cuh"
@@ -159,17 +159,17 @@ __host__ __device__ inline size_t staged_smem_bytes(int64_t k_pad, int64_t m_pad
 }
 
 // ------------------------------------------------------------ K2 dense KL --
-template <int U, int MINB, bool STAGE = true>
+template <int U, int MINB, bool STAGE = true, bool GUARD = true>
 __global__ void __launch_bounds__(kThreads, MINB) dense_kl_kernel(
     const double *__restrict__ P, int64_t ld, int64_t rows, int64_t k, int64_t k_pad,
     int64_t m_pad, const double *__restrict__ H, const double *__restrict__ tgt,
     const double *__restrict__ logt, const uint8_t *__restrict__ tmask, double clamp,
     double tau, int64_t row0, int64_t target, const uint8_t *__restrict__ is_interior,
-    double *__restrict__ out, uint32_t *__restrict__ flags, void *guard_ws,
-    int64_t guard_ws_bytes, int64_t guard_mail) {
+    double *__restrict__ out, uint32_t *__restrict__ flags, int64_t warp_mul) {
   extern __shared__ __align__(128) unsigned char smem[];
-  const GuardView gq = guard_view(guard_ws, guard_ws_bytes, k, guard_mail);  // guarded rows
-  unsigned int mail_head = 0;
+  __shared__ GuardRows gq;  // guarded rows, evaluated by the CTA after the loop
+  if (GUARD) guard_init(gq);
+  if (!STAGE) __syncthreads();
   // STAGE: target vector + mask in shared memory (one copy per CTA, TMA);
   // otherwise read through L1 (one copy per SM, shared by all its CTAs).
   const Staged st = STAGE ? stage_target(smem, logt, tmask, k_pad, m_pad) : Staged{logt, tmask};
@@ -182,7 +182,11 @@ __global__ void __launch_bounds__(kThreads, MINB) dense_kl_kernel(
   const int64_t npair = k >> 1;
   bool clamped_any = false;
 
-  for (int64_t r = warp; r < rows; r += nwarps) {
+  // guarded rows cluster in runs of consecutive rows: inside each block of
+  // nwarps rows the rows are dealt to warps in a scattered order
+  // (guard_warp_mul; the identity without the guard)
+  const int64_t first = GUARD ? (warp * warp_mul) % nwarps : warp;
+  for (int64_t r = first; r < rows; r += nwarps) {
     const double2 *row = reinterpret_cast<const double2 *>(P + r * ld);
     const double h = H[r];  // issued ahead of the row stream
     double a0 = 0.0, a1 = 0.0;
@@ -214,25 +218,21 @@ __global__ void __launch_bounds__(kThreads, MINB) dense_kl_kernel(
     const double cross = warp_sum(a0 + a1);
     double val = h - cross;
     const bool is_t = (row0 + r == target);
-    const bool guarded = !is_t && fabs(val) < tau * (fabs(h) + fabs(cross));  // warp-uniform
+    const bool guarded = GUARD && !is_t && fabs(val) < tau * (fabs(h) + fabs(cross));
     const bool interior = is_interior ? (is_interior[r] != 0) : true;
     clamped_any |= interior && __any_sync(0xffffffffu, fl);
-    if (guarded) {
-      if (!guard_push(gq, r, P, ld, k, tgt, clamp, out, flags, true, lane)) {
-        val = kl_reference_row_chunked(P + r * ld, k, tgt, clamp, lane);  // same value
-        if (lane == 0) {
-          out[r] = val;
-          atomicAdd(&flags[PF_FLAG_GUARDED], 1u);
-        }
-      }
-    } else {
-      val = is_t ? 0.0 : settle(val);  // divergence.py:181-182
-      if (lane == 0) out[r] = val;
+    if (guarded) {  // warp-uniform: evaluated by the CTA after the loop
+      guard_note(gq, r, out, lane);
+    } else if (lane == 0) {
+      out[r] = is_t ? 0.0 : settle(val);  // divergence.py:181-182
     }
-    guard_poll(gq, mail_head, false, P, ld, k, tgt, clamp, out, flags, true, lane);
   }
   if (lane == 0 && clamped_any) atomicOr(&flags[PF_FLAG_CLAMPED], 1u);
-  guard_poll(gq, mail_head, true, P, ld, k, tgt, clamp, out, flags, true, lane);
+  // the chunk partials reuse the staged target vector (or the unstaged
+  // variant's small dynamic buffer): no thread reads it after the loop
+  if (GUARD)
+    guard_drain(gq, reinterpret_cast<double *>(smem + 16), P, ld, rows, k, tgt, clamp, out,
+                flags, true, first, nwarps);
 }
 
 // ------------------------------------------------------------ K3 dense TV --
@@ -393,8 +393,9 @@ static int launch_dense(K staged, K unstaged, int64_t rows, int64_t k, cudaStrea
   K kern = staged;
   if (smem > kMaxStagedSmem) {  // very large k: target row through L1/L2 instead
     kern = unstaged;
-    smem = 0;
+    smem = 16 + kGuardPartBytes;  // the guarded-row drain's partials only
   }
+  if (smem < 16 + kGuardPartBytes) smem = 16 + kGuardPartBytes;
   if (int e = launch_cfg(kern, smem, rows, grid)) return e;
   *chosen = kern;
   *smem_out = smem;
@@ -440,37 +441,33 @@ int pf_row_negentropy_f64(const double *P, int64_t ld, int64_t rows, int64_t k, 
   return check_launch("row_negentropy");
 }
 
-int64_t pf_guard_ws_bytes(int64_t k, int64_t rows_cap) {
-  return guard_fixed_bytes(guard_mailboxes()) + rows_cap * (16 + 8 * guard_chunks(k > 0 ? k : 1));
-}
-
 int pf_dense_kl_f64(const double *P, int64_t ld, int64_t rows, int64_t k, const double *H,
                     const double *tgt, const double *logt, const uint8_t *tmask, double clamp,
                     double tau, int64_t row0, int64_t target, const uint8_t *is_interior,
-                    double *out, uint32_t *flags, void *ws, int64_t ws_bytes,
-                    pf_stream_t stream) {
+                    double *out, uint32_t *flags, pf_stream_t stream) {
   if (int e = check_dense_args(P, ld, rows, k)) return e;
   if (!H || !tgt || !logt || !tmask || !out || !flags) return fail(PF_E_ARG, "dense_kl: null");
-  if (ws && (ws_bytes < 64 || (reinterpret_cast<uintptr_t>(ws) & 15)))
-    return fail(PF_E_ARG, "dense_kl: workspace must be >= 64 bytes, 16-byte aligned");
   if (rows == 0) return 0;
   const int64_t k_pad = round_up(k, 2), m_pad = round_up(k, 16);
   auto kern = dense_kl_kernel<kU, kMinBlocks, true>;
   int grid = 0;
   size_t smem = 0;
-  if (int e = launch_dense(dense_kl_kernel<kU, kMinBlocks, true>,
-                           dense_kl_kernel<kU, kMinBlocks, false>, rows, k, as_stream(stream),
-                           &kern, &grid, &smem))
-    return e;
-  const int64_t mail = guard_mailboxes();
-  if (ws) {  // header + mailbox tail words are per launch
-    const cudaError_t e = cudaMemsetAsync(ws, 0, 64 + 4 * mail, as_stream(stream));
-    if (e != cudaSuccess) return fail(static_cast<int>(e), "dense_kl: ws reset");
+  if (tau > 0.0) {
+    if (int e = launch_dense(dense_kl_kernel<kU, kMinBlocks, true>,
+                             dense_kl_kernel<kU, kMinBlocks, false>, rows, k,
+                             as_stream(stream), &kern, &grid, &smem))
+      return e;
+  } else {  // no cancellation guard: the split form for every row
+    if (int e = launch_dense(dense_kl_kernel<kU, kMinBlocks, true, false>,
+                             dense_kl_kernel<kU, kMinBlocks, false, false>, rows, k,
+                             as_stream(stream), &kern, &grid, &smem))
+      return e;
   }
   kern<<<grid, kThreads, smem, as_stream(stream)>>>(P, ld, rows, k, k_pad, m_pad, H, tgt, logt,
                                                     tmask, clamp, tau, row0, target,
-                                                    is_interior, out, flags, ws,
-                                                    ws ? ws_bytes : 0, mail);
+                                                    is_interior, out, flags,
+                                                    guard_warp_mul(static_cast<int64_t>(grid) *
+                                                                   kWarpsPerCta));
   return check_launch("dense_kl");  // guarded rows were re-evaluated in the same launch
 }
 

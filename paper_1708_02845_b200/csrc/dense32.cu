@@ -90,7 +90,7 @@ __device__ __forceinline__ double guard64_row(const double *__restrict__ prow, i
 
 // FP64 split-form KL cross term sum_b c(Q_b) log c(Pt_b) of one FP64 row, one
 // warp, logs from the staged lo / hi planes (and the ragged tail).
-__device__ __forceinline__ double cross64_row(const double *__restrict__ prow, int64_t k,
+static __device__ __noinline__ double cross64_row(const double *__restrict__ prow, int64_t k,
                                               const double2 *lo, const double2 *hi,
                                               const double *tail, double clamp, int lane) {
   const int64_t nq4 = k >> 2;
@@ -112,11 +112,10 @@ __global__ void __launch_bounds__(kT32, 4) dense32_kernel(
     const double *__restrict__ H, const double *__restrict__ vec, double clamp, double tau,
     int64_t row0, int64_t target, const double *__restrict__ P64, int64_t ld64,
     const double *__restrict__ H64, double tau64, const double *__restrict__ tgt,
-    double *__restrict__ out, uint32_t *__restrict__ flags, void *guard_ws,
-    int64_t guard_ws_bytes, int64_t guard_mail) {
+    double *__restrict__ out, uint32_t *__restrict__ flags, int64_t warp_mul) {
   extern __shared__ __align__(128) unsigned char smem[];
-  const GuardView gq = guard_view(KL ? guard_ws : nullptr, guard_ws_bytes, k, guard_mail);
-  unsigned int mail_head = 0;
+  __shared__ GuardRows gq;
+  guard_init(gq);
   const int64_t nq4 = k >> 2;  // full float4 groups
   double2 *lo = reinterpret_cast<double2 *>(smem);
   double2 *hi = lo + nq4;
@@ -132,7 +131,8 @@ __global__ void __launch_bounds__(kT32, 4) dense32_kernel(
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   constexpr int U = 4;
-  for (int64_t r = warp; r < rows; r += nwarps) {
+  const int64_t first = (warp * warp_mul) % nwarps;  // scattered rows (pf_common.cuh)
+  for (int64_t r = first; r < rows; r += nwarps) {
     const float4 *row = reinterpret_cast<const float4 *>(P + r * ld);
     const double h = KL ? H[r] : 0.0;
     double a0 = 0.0, a1 = 0.0;
@@ -177,11 +177,8 @@ __global__ void __launch_bounds__(kT32, 4) dense32_kernel(
         const double c64 = cross64_row(P64 + r * ld64, k, lo, hi, tail, clamp, lane);
         val = h64 - c64;
         if (fabs(val) < tau64 * (fabs(h64) + fabs(c64))) {  // the FP64 guard
-          if (guard_push(gq, r, P64, ld64, k, tgt, clamp, out, flags, false, lane)) {
-            guard_poll(gq, mail_head, false, P64, ld64, k, tgt, clamp, out, flags, false, lane);
-            continue;
-          }
-          val = kl_reference_row_chunked(P64 + r * ld64, k, tgt, clamp, lane);
+          guard_note(gq, r, out, lane);  // the reference form, by the CTA after the loop
+          continue;
         } else {
           val = settle(val);
         }
@@ -192,9 +189,10 @@ __global__ void __launch_bounds__(kT32, 4) dense32_kernel(
       val = settle(val);
     }
     if (lane == 0) out[r] = val;
-    if (KL) guard_poll(gq, mail_head, false, P64, ld64, k, tgt, clamp, out, flags, false, lane);
   }
-  if (KL) guard_poll(gq, mail_head, true, P64, ld64, k, tgt, clamp, out, flags, false, lane);
+  if (KL)  // partials reuse the staged lo / hi planes (dead after the loop)
+    guard_drain(gq, reinterpret_cast<double *>(smem), P64, ld64, rows, k, tgt, clamp, out, flags,
+                false, first, nwarps);
 }
 
 // flag[0] |= 1 if the below-clamp masks of rows a and b differ (k entries).
@@ -221,9 +219,9 @@ template <bool KL>
 static int launch32(const float *P, int64_t ld, int64_t rows, int64_t k, const double *H,
                     const double *vec, double clamp, double tau, int64_t row0, int64_t target,
                     const double *P64, int64_t ld64, const double *H64, double tau64,
-                    const double *tgt, double *out, uint32_t *flags, void *ws, int64_t ws_bytes,
-                    cudaStream_t stream) {
-  const size_t smem = static_cast<size_t>(k) * 8 + 32;
+                    const double *tgt, double *out, uint32_t *flags, cudaStream_t stream) {
+  size_t smem = static_cast<size_t>(k) * 8 + 32;
+  if (smem < kGuardPartBytes) smem = kGuardPartBytes;
   if (smem > 200 * 1024) return fail(PF_E_DOMAIN, "dense32: k=%lld too large", (long long)k);
   auto kern = dense32_kernel<KL>;
   if (int e = ensure_smem((const void *)kern, smem)) return e;
@@ -234,16 +232,9 @@ static int launch32(const float *P, int64_t ld, int64_t rows, int64_t k, const d
   if (!P64 || !tgt || !flags) return fail(PF_E_ARG, "dense32: the FP64 guard needs P64, tgt, flags");
   if ((ld64 & 1) || (reinterpret_cast<uintptr_t>(P64) & 15))
     return fail(PF_E_ALIGN, "dense32: FP64 rows must be 16-byte aligned");
-  if (ws) {
-    if (ws_bytes < 64 || (reinterpret_cast<uintptr_t>(ws) & 15))
-      return fail(PF_E_ARG, "dense32: workspace must be >= 64 bytes, 16-byte aligned");
-    const cudaError_t e = cudaMemsetAsync(ws, 0, 64 + 4 * guard_mailboxes(), stream);
-    if (e != cudaSuccess) return fail(static_cast<int>(e), "dense32: ws reset");
-  }
   kern<<<static_cast<int>(g), kT32, smem, stream>>>(P, ld, rows, k, H, vec, clamp, tau, row0,
                                                     target, P64, ld64, H64, tau64, tgt, out,
-                                                    flags, ws, ws ? ws_bytes : 0,
-                                                    guard_mailboxes());
+                                                    flags, guard_warp_mul(g * (kT32 / 32)));
   return check_launch("dense32");  // guarded rows were re-evaluated in place
 }
 
@@ -274,8 +265,7 @@ int pf_dense_kl_f32(const float *P, int64_t ld, int64_t rows, int64_t k, const d
                     const double *tgt, const double *logt, const uint8_t *tmask, double clamp,
                     double tau, int64_t row0, int64_t target, const uint8_t *is_interior,
                     const double *P64, int64_t ld64, const double *H64, double tau64,
-                    double *out, uint32_t *flags, void *ws, int64_t ws_bytes,
-                    pf_stream_t stream) {
+                    double *out, uint32_t *flags, pf_stream_t stream) {
   if (rows <= 0) return 0;
   if (!P || !H || !tgt || !logt || !tmask || !P64 || !out || !flags)
     return fail(PF_E_ARG, "dense_kl_f32: null");
@@ -284,7 +274,7 @@ int pf_dense_kl_f32(const float *P, int64_t ld, int64_t rows, int64_t k, const d
   (void)tmask;
   (void)is_interior;
   return launch32<true>(P, ld, rows, k, H, logt, clamp, tau, row0, target, P64, ld64, H64, tau64,
-                        tgt, out, flags, ws, ws_bytes, as_stream(stream));
+                        tgt, out, flags, as_stream(stream));
 }
 
 int pf_dense_tv_f32(const float *P, int64_t ld, int64_t rows, int64_t k, const double *tgt,
@@ -298,7 +288,7 @@ int pf_dense_tv_f32(const float *P, int64_t ld, int64_t rows, int64_t k, const d
   (void)tmask;
   (void)is_interior;
   return launch32<false>(P, ld, rows, k, nullptr, tgt, clamp, tau, row0, target, P64, ld64,
-                         nullptr, 0.0, tgt, out, flags, nullptr, 0, as_stream(stream));
+                         nullptr, 0.0, tgt, out, flags, as_stream(stream));
 }
 
 int pf_mask_compare_f64(const double *a, const double *b, int64_t k, double clamp,

@@ -175,10 +175,9 @@ def _field_device(pk, dk, fd, p: int, swap_order: bool, clamp: float, out_dev, f
     kind, param = gen[1], gen[2]
     if kind == 0 and not swap_order:
         H = dk.negentropy(clamp)
-        ws, wsb = dk.guard_ws(stream)
         nat.call("pf_dense_kl_f64", dk.P.data_ptr(), dk.ld, dk.rows, dk.k, H.data_ptr(),
                  st.tgt, st.logt, st.tmask, clamp, KL_GUARD_TAU, dk.row0, p,
-                 dk.is_interior.data_ptr(), out_dev.data_ptr(), flags_ptr, ws, wsb, stream)
+                 dk.is_interior.data_ptr(), out_dev.data_ptr(), flags_ptr, stream)
     elif kind == 1 and not swap_order:
         nat.call("pf_dense_tv_f64", dk.P.data_ptr(), dk.ld, dk.rows, dk.k, st.tgt, st.tmask,
                  clamp, dk.row0, p, dk.is_interior.data_ptr(), out_dev.data_ptr(),
@@ -332,11 +331,10 @@ def dv_field_f32_device(pk: PoissonKernel, fd: FDivergence, p: int, clamp: float
     if _is_builtin(fd, "kl"):
         H = dk.negentropy32(c)
         H64 = dk.negentropy(c)   # FP64 split form for the guarded rows
-        ws, wsb = dk.guard_ws(s.cuda_stream)
         nat.call("pf_dense_kl_f32", P32.data_ptr(), ld32, dk.rows, dk.k, H.data_ptr(), st.tgt,
                  st.logt, st.tmask, c, F32_GUARD_TAU, dk.row0, p, dk.is_interior.data_ptr(),
                  dk.P.data_ptr(), dk.ld, H64.data_ptr(), KL_GUARD_TAU, out.data_ptr(), flags,
-                 ws, wsb, s.cuda_stream)
+                 s.cuda_stream)
     else:
         nat.call("pf_dense_tv_f32", P32.data_ptr(), ld32, dk.rows, dk.k, st.tgt, st.tmask, c,
                  F32_GUARD_TAU, dk.row0, p, dk.is_interior.data_ptr(), dk.P.data_ptr(), dk.ld,

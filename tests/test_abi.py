@@ -27,7 +27,7 @@ def test_version_and_error_string():
 def test_argument_errors_without_launch():
     # validation failures return an error code, not a launch
     lib = nat.load()
-    rc = lib.pf_dense_kl_f64(0, 4, 10, 4, 0, 0, 0, 0, 1e-300, 1e-3, 0, 0, 0, 0, 0, 0, 0, 0)
+    rc = lib.pf_dense_kl_f64(0, 4, 10, 4, 0, 0, 0, 0, 1e-300, 1e-3, 0, 0, 0, 0, 0, 0)
     assert rc != 0
     assert b"null" in lib.pf_last_error()
     rc = lib.pf_row_negentropy_f64(8, 3, 10, 3, 1e-300, 16, 0, 0)  # odd ld
