@@ -692,7 +692,7 @@ def extra_c5(t, nat, dev, pf, device, dk, omesh, steps, peak):
     eb = t.empty(T, dtype=t.int32, device=device)
     bad = t.zeros(1, dtype=t.int32, device=device)
 
-    def batch_i8(timed=False, grade=64):
+    def batch_i8(timed=False, grade=64, pair=1):
         cnt.zero_()
         nat.call("pf_batch_prep_f64", Pt.data_ptr(), Pt.stride(0), T, k, ldl, 1e-300, 0,
                  L_.data_ptr(), Tc.data_ptr(), 0, s.cuda_stream)
@@ -702,7 +702,7 @@ def extra_c5(t, nat, dev, pf, device, dk, omesh, steps, peak):
             e1.record(s)
         nat.call("pf_batched_kl_i8", A.data_ptr(), ea.data_ptr(), rows, B.data_ptr(),
                  eb.data_ptr(), T, k, ldk, H.data_ptr(), tg.data_ptr(), tau, 0, out.data_ptr(),
-                 out.stride(0), grade, s.cuda_stream)
+                 out.stride(0), grade, pair, s.cuda_stream)
         if timed:
             e2.record(s)
         nat.call("pf_batched_kl_fixup_f64", dk.P.data_ptr(), dk.ld, rows, k, Tc.data_ptr(), ldl,
@@ -733,6 +733,9 @@ def extra_c5(t, nat, dev, pf, device, dk, omesh, steps, peak):
     batch_i8(True)
     t.cuda.synchronize()
     gemm_only = e1.elapsed_time(e2)
+    batch_i8(True, pair=0)                  # the single-CTA kernel beside it
+    t.cuda.synchronize()
+    gemm_single = e1.elapsed_time(e2)
     guarded = int(cnt.item())
     flops = 2.0 * rows * k * T
     fl = ctypes.c_int64(0)
@@ -756,13 +759,15 @@ def extra_c5(t, nat, dev, pf, device, dk, omesh, steps, peak):
                        f"byte-pair GEMMs emulating the FP64 GEMM), then {src.size:,} paths traced, "
                        "1 GPU",
            "evals_per_s": rows * T / (ms / 1e3), "ms_per_batch": ms,
-           "gemm_ms": gemm_only, "guarded_pairs": guarded,
+           "gemm_ms": gemm_only, "gemm_ms_single_cta_kernel": gemm_single,
+           "guarded_pairs": guarded,
            "fp64_equivalent_tflops": flops / (ms / 1e3) / 1e12,
            "slice_rows_ms_once_per_P": slice_ms,
            "roofline": {"bound": "tensor", "achieved": ach, "peak": i8_tops, "unit": "TOPS (int8)",
                         "frac": ach / i8_tops, "algorithmic_ops_per_launch": int_ops,
                         "peak_kind": "measured: pf_probe_umma_i8 (M128 N256 K32 u8 tcgen05.mma "
-                                     "back to back from shared memory, all SMs)"},
+                                     "back to back from shared memory, all SMs)",
+                        "kernel": "pf::batched_kl_i8_pair_kernel<7,9> (tcgen05 cta_group::2)"},
            "fp32_grade": {"note": "same kernel, 15 byte-pair GEMMs (levels 2..6 of the top 5 "
                                   "planes): the north-star FP32 tolerance 1e-5",
                           "ms_per_batch": ms_f32grade,

@@ -318,7 +318,10 @@ int pf_batched_kl_fixup_f64(const double *P, int64_t ld, int64_t rows, int64_t k
  *   (guard sentinel, settle, zero at the target); k <= 4717.  grade 64 keeps
  *   levels 2..9 of all 7 planes (34 pairs, FP64-grade: within 1e-10 of the
  *   reference), grade 32 levels 2..6 of the top 5 planes (15 pairs, the
- *   north-star FP32 tolerance 1e-5).  Follow with pf_batched_kl_fixup_f64 for
+ *   north-star FP32 tolerance 1e-5).  cta_pair != 0 runs the CTA-pair kernel
+ *   (tcgen05 cta_group::2, M256 tiles over two SMs: half the shared-memory
+ *   operand traffic per SM), bitwise the same outputs as cta_pair == 0.
+ *   Follow with pf_batched_kl_fixup_f64 for
  *   the guarded pairs. */
 int pf_slice_rows_u8(const double *P, int64_t ld, int64_t rows, int64_t k, double clamp,
                      int64_t ldk, uint8_t *slices, int32_t *exps, pf_stream_t stream);
@@ -327,7 +330,7 @@ int pf_slice_targets_u8(const double *L, int64_t ldl, int64_t T, int64_t k, int6
 int pf_batched_kl_i8(const uint8_t *A, const int32_t *ea, int64_t rows, const uint8_t *B,
                      const int32_t *eb, int64_t T, int64_t k, int64_t ldk, const double *H,
                      const int64_t *targets, double tau, int64_t row0, double *out, int64_t ldo,
-                     int grade, pf_stream_t stream);
+                     int grade, int cta_pair, pf_stream_t stream);
 
 /* Diagnostic: back-to-back M128 N256 K32 u8 tcgen05.mma on shared-memory
  * operands, one CTA per SM (*ops_host = integer ops issued): the int8 tensor

@@ -327,6 +327,195 @@ __global__ void __launch_bounds__(kO2Threads, 1) batched_kl_i8_n128_kernel(
   if (warp == 0) tc::tmem_free<512>(tmem);
 }
 
+// ---------------------------------------------------------- GEMM, CTA pair --
+// The same two-pass level schedule on a CTA pair (cta_group::2, cluster of 2
+// CTAs on two row tiles): the leader issues M256 N128 K32 MMAs whose A rows
+// 0-127 come from its own shared memory and 128-255 from the peer's, and whose
+// B (the 128 targets) is split 64 / 64 between the two; each CTA's TMEM gets
+// its own 128 rows.  Per SM and MMA the tensor pipe reads 4 KB of A + 2 KB of
+// B from shared memory instead of 4 + 4 KB, and TMA writes 6 instead of 8 KB
+// per slice: the 1-CTA kernel is shared-memory bound (UMMA operand reads +
+// TMA writes ~151 B/clk against ~128).  5-stage ring of 42 KB per CTA.  The
+// arithmetic is the same exact integers, so the outputs are bitwise the
+// 1-CTA kernel's.
+constexpr int kP2BN = 128, kP2HalfN = 64, kP2Stages = 5;
+constexpr int kP2TileA = 128 * kO2BK;                         // 4 KB per slice
+constexpr int kP2TileB = kP2HalfN * kO2BK;                    // 2 KB per slice
+constexpr int kP2StageBytes = kOzSlices * (kP2TileA + kP2TileB);  // 43,008
+constexpr int kP2Smem = kP2Stages * kP2StageBytes + 1024;
+
+template <int kS, int kMaxL>
+__global__ void __launch_bounds__(kO2Threads, 1)
+    batched_kl_i8_pair_kernel(const __grid_constant__ CUtensorMap mapA7,
+                              const __grid_constant__ CUtensorMap mapA4,
+                              const __grid_constant__ CUtensorMap mapB7,
+                              const __grid_constant__ CUtensorMap mapB4,
+                              const int32_t *__restrict__ ea, const int32_t *__restrict__ eb,
+                              int64_t rows, int64_t T, int nkb, const double *__restrict__ H,
+                              const int64_t *__restrict__ targets, double tau, int64_t row0,
+                              double *__restrict__ out, int64_t ldo) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  __shared__ __align__(8) uint64_t full_bar[kP2Stages], empty_bar[kP2Stages];
+  __shared__ __align__(8) uint64_t pass_bar[2], drained_bar;
+  __shared__ uint32_t tmem_base;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // cluster (2, 1, 1): x = 2 x target tile + pair rank (the 2-CTA MMA pairs
+  // adjacent x ranks), y = row-tile pair; the target tiles of one row pair are
+  // consecutive CTAs, so its A tiles stream from HBM once and hit L2 after
+  const uint32_t rank = tc::cluster_rank();   // 0 = leader (issues the MMAs)
+  const int t0 = (blockIdx.x >> 1) * kP2BN;
+  const int64_t q0 = (static_cast<int64_t>(blockIdx.y) * 2 + rank) * 128;   // this CTA's rows
+
+  if (tid == 0) {
+    tc::prefetch_map(&mapA7);
+    tc::prefetch_map(&mapA4);
+    tc::prefetch_map(&mapB7);
+    tc::prefetch_map(&mapB4);
+    for (int s = 0; s < kP2Stages; ++s) {
+      mbar_init(&full_bar[s], 1);    // the leader's producer arrives (both CTAs' bytes)
+      mbar_init(&empty_bar[s], 1);   // one multicast MMA commit
+    }
+    mbar_init(&pass_bar[0], 1);
+    mbar_init(&pass_bar[1], 1);
+    mbar_init(&drained_bar, 16);     // every epilogue warp of both CTAs
+  }
+  if (warp == 0) tc::tmem_alloc_pair<512>(&tmem_base);
+  tc::fence_before();
+  tc::cluster_sync();               // barriers of both CTAs initialised, TMEM allocated
+  tc::fence_after();
+  const uint32_t tmem = tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---- TMA producer (both CTAs): own 128 A rows, own half of the targets
+      const int32_t tb = t0 + static_cast<int32_t>(rank) * kP2HalfN;
+      for (int it = 0; it < 2 * nkb; ++it) {
+        const int s = it % kP2Stages;
+        const uint32_t round = it / kP2Stages;
+        const bool p1 = it < nkb;
+        const int kb = p1 ? it : it - nkb;
+        const int ns = p1 ? kO2Pass1Slices : kS;
+        mbar_wait(&empty_bar[s], (round & 1) ^ 1);
+        uint8_t *sa = smem + s * kP2StageBytes;
+        uint8_t *sb = sa + kOzSlices * kP2TileA;
+        if (rank == 0) mbar_expect_tx(&full_bar[s], 2 * ns * (kP2TileA + kP2TileB));
+        const uint32_t lb = tc::mapa(&full_bar[s], 0);
+        tc::tma_load_3d_pair(sa, p1 ? &mapA4 : &mapA7, kb * kO2BK, static_cast<int32_t>(q0), 0, lb);
+        tc::tma_load_3d_pair(sb, p1 ? &mapB4 : &mapB7, kb * kO2BK, tb, 0, lb);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // ---- MMA issuer (leader only): M256 N128 K32
+      constexpr uint32_t idesc = tc::idesc_i8(256, kP2BN, false, false);
+      for (int it = 0; it < 2 * nkb; ++it) {
+        const int s = it % kP2Stages;
+        const bool p1 = it < nkb;
+        const int kb = p1 ? it : it - nkb;
+        if (it == nkb) {  // pass 2 reuses the accumulators: wait for both drains
+          mbar_wait(&drained_bar, 0);
+          tc::fence_after();
+        }
+        mbar_wait(&full_bar[s], (it / kP2Stages) & 1);
+        tc::fence_after();
+        const uint32_t sa = smem_u32(smem + s * kP2StageBytes);
+        const uint32_t sb = sa + kOzSlices * kP2TileA;
+        if (p1) {
+#pragma unroll
+          for (int i = 1; i <= kO2Pass1Slices; ++i)
+#pragma unroll
+            for (int j = 1; j <= kO2Pass1Slices; ++j) {
+              const int l = i + j;
+              if (l > 5) continue;
+              tc::mma_i8_pair(tmem + (l - 2) * kP2BN, tc::sdesc<32>(sa + (i - 1) * kP2TileA),
+                              tc::sdesc<32>(sb + (j - 1) * kP2TileB), idesc,
+                              !(kb == 0 && i == 1));
+            }
+        } else {
+#pragma unroll
+          for (int i = 1; i <= kS; ++i)
+#pragma unroll
+            for (int j = 1; j <= kS; ++j) {
+              const int l = i + j;
+              if (l < 6 || l > kMaxL) continue;
+              const int first_i = l - kS > 1 ? l - kS : 1;
+              tc::mma_i8_pair(tmem + (l - 6) * kP2BN, tc::sdesc<32>(sa + (i - 1) * kP2TileA),
+                              tc::sdesc<32>(sb + (j - 1) * kP2TileB), idesc,
+                              !(kb == 0 && i == first_i));
+            }
+        }
+        tc::commit_pair(&empty_bar[s]);
+        if (it == nkb - 1) tc::commit_pair(&pass_bar[0]);
+      }
+      tc::commit_pair(&pass_bar[1]);
+    }
+  } else {
+    // ---- epilogue warps 2..9 (both CTAs, own TMEM = own 128 rows x 128 targets)
+    const int quarter = warp & 3, half = (warp - 2) >> 2;
+    const int r = quarter * 32 + lane;
+    const int64_t q = q0 + r;
+    const bool row_ok = q < rows;
+    const uint32_t base = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + half * 64;
+    double v1[64];
+    mbar_wait(&pass_bar[0], 0);
+    tc::fence_after();
+#pragma unroll
+    for (int c0 = 0; c0 < 64; c0 += 8) {
+      uint32_t acc[4][8];
+#pragma unroll
+      for (int l = 0; l < 4; ++l) tc::tmem_ld8(base + l * kP2BN + c0, acc[l]);
+      tc::tmem_ld_wait();
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        double v = static_cast<double>(acc[3][u]);
+#pragma unroll
+        for (int l = 2; l >= 0; --l) v = fma(v, 0x1p-8, static_cast<double>(acc[l][u]));
+        v1[c0 + u] = v;
+      }
+    }
+    tc::fence_before();
+    __syncwarp();
+    if (lane == 0) tc::mbar_arrive_cluster(tc::mapa(&drained_bar, 0));
+    mbar_wait(&pass_bar[1], 0);
+    tc::fence_after();
+    const double h = row_ok ? H[q] : 0.0;
+    const int e_q = row_ok ? ea[q] : 0;
+    const int64_t tq = row_ok ? row0 + q : -1;
+    constexpr int kL2 = kMaxL - 5;
+#pragma unroll
+    for (int c0 = 0; c0 < 64; c0 += 8) {
+      uint32_t acc[kL2][8];
+#pragma unroll
+      for (int l = 0; l < kL2; ++l) tc::tmem_ld8(base + l * kP2BN + c0, acc[l]);
+      tc::tmem_ld_wait();
+      if (!row_ok) continue;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int64_t t = t0 + half * 64 + c0 + u;
+        if (t >= T) continue;
+        double v = static_cast<double>(acc[kL2 - 1][u]);
+#pragma unroll
+        for (int l = kL2 - 2; l >= 0; --l) v = fma(v, 0x1p-8, static_cast<double>(acc[l][u]));
+        v = fma(v, 0x1p-32, v1[c0 + u]);
+        const double S = ldexp(v, e_q + eb[t] - 16);
+        double val = h + S;
+        const bool is_t = (tq == targets[t]);
+        if (!is_t && fabs(val) < tau * (fabs(h) + fabs(S)))
+          val = __longlong_as_double(static_cast<long long>(kOzGuard));
+        else
+          val = is_t ? 0.0 : settle(val);
+        out[q * ldo + t] = val;
+      }
+    }
+  }
+  tc::fence_before();
+  tc::cluster_sync();   // both CTAs done with TMEM and with each other's barriers
+  if (warp == 0) tc::tmem_free_pair<512>(tmem);
+}
+
 // Diagnostic: the int8 tensor pipe's issue-rate ceiling, back-to-back
 // M128 N256 K32 u8 MMAs on shared-memory-resident operands, one CTA per SM;
 // bench.py reports K7's int8 rate against it.
@@ -406,10 +595,40 @@ static int slice_map(CUtensorMap *map, const uint8_t *base, int64_t outer, int64
 template <int kS, int kMaxL>
 static int launch_i8(const CUtensorMap (&m)[4], const int32_t *ea, const int32_t *eb,
                      int64_t rows, int64_t T, int64_t k, const double *H, const int64_t *targets,
-                     double tau, int64_t row0, double *out, int64_t ldo, cudaStream_t stream) {
-  if (int e = ensure_smem((const void *)batched_kl_i8_n128_kernel<kS, kMaxL>, kO2Smem)) return e;
+                     double tau, int64_t row0, double *out, int64_t ldo, bool pair,
+                     cudaStream_t stream) {
   const int nkb = static_cast<int>((k + kO2BK - 1) / kO2BK);
-  dim3 grid(static_cast<unsigned>((T + kO2BN - 1) / kO2BN), static_cast<unsigned>((rows + 127) / 128));
+  const unsigned tiles = static_cast<unsigned>((rows + 127) / 128);
+  if (pair) {  // a pair's second CTA may hold only out-of-range rows
+    auto kern = batched_kl_i8_pair_kernel<kS, kMaxL>;
+    if (int e = ensure_smem((const void *)kern, kP2Smem)) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * static_cast<unsigned>((T + kP2BN - 1) / kP2BN), (tiles + 1) / 2, 1);
+    cfg.blockDim = dim3(kO2Threads, 1, 1);
+    cfg.dynamicSmemBytes = kP2Smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int clusters = 0;
+    const cudaError_t oe = cudaOccupancyMaxActiveClusters(&clusters, (const void *)kern, &cfg);
+    if (oe != cudaSuccess || clusters == 0) {
+      cudaGetLastError();
+      return fail(PF_E_LAUNCH, "batched_kl_i8_pair: no CTA pair fits an SM pair (%s, %d)",
+                  cudaGetErrorString(oe), clusters);
+    }
+    const cudaError_t le = cudaLaunchKernelEx(&cfg, kern, m[0], m[1], m[2], m[3], ea, eb, rows, T,
+                                              nkb, H, targets, tau, row0, out, ldo);
+    if (le != cudaSuccess)
+      return fail(static_cast<int>(le), "batched_kl_i8_pair: %s", cudaGetErrorString(le));
+    return check_launch("batched_kl_i8_pair");
+  }
+  if (int e = ensure_smem((const void *)batched_kl_i8_n128_kernel<kS, kMaxL>, kO2Smem)) return e;
+  dim3 grid(static_cast<unsigned>((T + kO2BN - 1) / kO2BN), tiles);
   batched_kl_i8_n128_kernel<kS, kMaxL><<<grid, kO2Threads, kO2Smem, stream>>>(
       m[0], m[1], m[2], m[3], ea, eb, rows, T, nkb, H, targets, tau, row0, out, ldo);
   return check_launch("batched_kl_i8");
@@ -444,7 +663,7 @@ int pf_slice_targets_u8(const double *L, int64_t ldl, int64_t T, int64_t k, int6
 int pf_batched_kl_i8(const uint8_t *A, const int32_t *ea, int64_t rows, const uint8_t *B,
                      const int32_t *eb, int64_t T, int64_t k, int64_t ldk, const double *H,
                      const int64_t *targets, double tau, int64_t row0, double *out, int64_t ldo,
-                     int grade, pf_stream_t stream) {
+                     int grade, int cta_pair, pf_stream_t stream) {
   if (grade != 64 && grade != 32) return fail(PF_E_ARG, "batched_kl_i8: grade must be 64 or 32");
   const int kS = grade == 64 ? kOzSlices : 5;
   if (rows <= 0 || T <= 0) return 0;
@@ -456,15 +675,17 @@ int pf_batched_kl_i8(const uint8_t *A, const int32_t *ea, int64_t rows, const ui
     return fail(PF_E_ALIGN, "batched_kl_i8: slice planes must be 16-byte aligned");
   const int64_t row_tiles = (rows + 127) / 128;
   if (row_tiles > 65535) return fail(PF_E_DOMAIN, "batched_kl_i8: too many rows per launch");
+  const bool pair = cta_pair != 0;
+  const uint32_t bn = pair ? kP2HalfN : kO2BN;   // each CTA of a pair loads half the targets
   CUtensorMap m[4];
   if (int e = slice_map(&m[0], A, rows, ldk, 128, kO2BK, kS)) return e;
   if (int e = slice_map(&m[1], A, rows, ldk, 128, kO2BK, kO2Pass1Slices)) return e;
-  if (int e = slice_map(&m[2], B, T, ldk, kO2BN, kO2BK, kS)) return e;
-  if (int e = slice_map(&m[3], B, T, ldk, kO2BN, kO2BK, kO2Pass1Slices)) return e;
+  if (int e = slice_map(&m[2], B, T, ldk, bn, kO2BK, kS)) return e;
+  if (int e = slice_map(&m[3], B, T, ldk, bn, kO2BK, kO2Pass1Slices)) return e;
   return grade == 64 ? launch_i8<7, 9>(m, ea, eb, rows, T, k, H, targets, tau, row0, out, ldo,
-                                       as_stream(stream))
+                                       pair, as_stream(stream))
                      : launch_i8<5, 6>(m, ea, eb, rows, T, k, H, targets, tau, row0, out, ldo,
-                                       as_stream(stream));
+                                       pair, as_stream(stream));
 }
 
 int pf_probe_umma_i8(int64_t iters, int64_t *ops_host, uint32_t *sink, pf_stream_t stream) {

@@ -370,6 +370,8 @@ def dv_field_f32(pk: PoissonKernel, fd: FDivergence, p: int, clamp: float | None
 # ---------------------------------------------------------------------------
 
 I8_MAX_K = 4717  # batched_i8.cu: 7 x k x 255^2 < 2^31
+#: K7 on a CTA pair (tcgen05 cta_group::2): bitwise the single-CTA kernel's output
+I8_CTA_PAIR = True
 
 
 def dv_field_batch_device(pk: PoissonKernel, fd: FDivergence, targets, clamp=None,
@@ -452,7 +454,7 @@ def _kl_batch_slab(dk, tg, Pt, c: float, method: str, out=None):
         nat.call("pf_batched_kl_i8", A.data_ptr(), ea.data_ptr(), dk.rows, B.data_ptr(),
                  eb.data_ptr(), T, dk.k, ldk, H.data_ptr(), tg.data_ptr(), KL_GUARD_TAU,
                  dk.row0, out.data_ptr(), out.stride(0), 32 if method == "i8-f32" else 64,
-                 s.cuda_stream)
+                 int(I8_CTA_PAIR), s.cuda_stream)
         nat.call("pf_batched_kl_fixup_f64", dk.P.data_ptr(), dk.ld, dk.rows, dk.k,
                  Tc.data_ptr(), ldl, T, c, out.data_ptr(), out.stride(0),
                  tflag.data_ptr() + 4 * T, s.cuda_stream)

@@ -141,3 +141,32 @@ def test_batch_slabs_bitwise_and_flags_or(method):
         fl |= f
     np.testing.assert_array_equal(np.concatenate(parts), full)
     np.testing.assert_array_equal(fl, flags)
+
+
+@pytest.mark.parametrize("rows,k,T", [(300, 200, 50), (129, 64, 64), (2047, 1234, 256)])
+def test_i8_cta_pair_kernel_bitwise_equals_single_cta(rows, k, T):
+    """K7 on a CTA pair (tcgen05 cta_group::2, M256 over two SMs) computes the same
+    exact integer levels as the single-CTA kernel: the outputs are bitwise equal,
+    including odd row-tile counts (a pair's second CTA past the last row) and
+    ragged target tiles."""
+    import torch
+    from paper_1708_02845_b200 import _device as dev
+    from paper_1708_02845_b200 import divergence as D
+    rng = np.random.default_rng(rows)
+    P = rng.random((rows, k)) ** 4
+    P[:, 0] = 0.0
+    P /= P.sum(axis=1, keepdims=True)
+    pk = pf.PoissonKernel(P, np.array([1]), 0.0, 0.0)
+    targets = rng.choice(rows, T, replace=False)
+    old = D.I8_CTA_PAIR
+    try:
+        D.I8_CTA_PAIR = False
+        a, fa = D.dv_field_batch_device(pk, pf.builtin_f("kl"), targets, method="i8")
+        a = a.clone()
+        D.I8_CTA_PAIR = True
+        b, fb = D.dv_field_batch_device(pk, pf.builtin_f("kl"), targets, method="i8")
+    finally:
+        D.I8_CTA_PAIR = old
+    torch.cuda.synchronize()
+    assert torch.equal(a.view(torch.int64), b.view(torch.int64))
+    assert np.array_equal(fa, fb)

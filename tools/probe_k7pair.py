@@ -1,0 +1,72 @@
+"""K7 on the int8 tensor pipe: the CTA-pair kernel (cta_group::2) vs the
+single-CTA kernel — bitwise equal outputs on ragged shapes, then GEMM time."""
+import ctypes, json, sys, time
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import numpy as np
+import torch as t
+import paper_1708_02845_b200 as pf
+from paper_1708_02845_b200 import _device as dev, _native as nat
+
+
+def setup(rows, k, T, seed=0):
+    g = t.Generator(device="cuda:0"); g.manual_seed(seed)
+    ld = dev.round_up(k, 16)
+    P = t.softmax(t.randn((rows, k), dtype=t.float64, device="cuda:0", generator=g), dim=1)
+    Pp = t.zeros((rows, ld), dtype=t.float64, device="cuda:0"); Pp[:, :k] = P
+    dk = dev.DeviceKernel(None, np.array([], np.int64), device=t.device("cuda", 0), rows=rows, n=rows, k=k, P_dev=Pp)
+    tg = t.from_numpy(np.random.default_rng(seed).choice(rows, T, replace=False).astype(np.int64)).cuda()
+    H = dk.negentropy(1e-300)
+    A, ea, ldk = dk.slices(1e-300)
+    ldl = dev.round_up(k, 16)
+    Pt = dk.P.index_select(0, tg)
+    L = t.empty((T, ldl), dtype=t.float64, device="cuda:0"); Tc = t.empty_like(L)
+    s = t.cuda.current_stream().cuda_stream
+    nat.call("pf_batch_prep_f64", Pt.data_ptr(), Pt.stride(0), T, k, ldl, 1e-300, 0, L.data_ptr(), Tc.data_ptr(), 0, s)
+    B = t.empty((7, T, ldk), dtype=t.uint8, device="cuda:0"); eb = t.empty(T, dtype=t.int32, device="cuda:0")
+    bad = t.zeros(1, dtype=t.int32, device="cuda:0")
+    nat.call("pf_slice_targets_u8", L.data_ptr(), ldl, T, k, ldk, B.data_ptr(), eb.data_ptr(), bad.data_ptr(), s)
+    return dict(dk=dk, tg=tg, H=H, A=A, ea=ea, ldk=ldk, B=B, eb=eb, rows=rows, k=k, T=T)
+
+
+def run(c, pair, grade=64):
+    out = t.full((c["rows"], c["T"]), -7.0, dtype=t.float64, device="cuda:0")
+    s = t.cuda.current_stream().cuda_stream
+    nat.call("pf_batched_kl_i8", c["A"].data_ptr(), c["ea"].data_ptr(), c["rows"], c["B"].data_ptr(),
+             c["eb"].data_ptr(), c["T"], c["k"], c["ldk"], c["H"].data_ptr(), c["tg"].data_ptr(), 1e-3, 0,
+             out.data_ptr(), out.stride(0), grade, pair, s)
+    t.cuda.synchronize()
+    return out
+
+
+res = {}
+for rows, k, T in [(300, 200, 50), (1000, 300, 130), (129, 64, 64), (2047, 1234, 256), (5000, 4102, 1024)]:
+    c = setup(rows, k, T)
+    for grade in (64, 32):
+        a = run(c, 0, grade).cpu().numpy()
+        b = run(c, 1, grade).cpu().numpy()
+        same = (a.view(np.int64) == b.view(np.int64))
+        res[f"{rows}x{k}xT{T} g{grade}"] = {"bitwise": bool(same.all()), "mismatch": int((~same).sum()),
+                                          "untouched": int((b == -7.0).sum())}
+    del c
+print(json.dumps(res, indent=1), flush=True)
+if not all(v["bitwise"] and v["untouched"] == 0 for v in res.values()):
+    sys.exit(1)
+# timing at a C5-like slab
+c = setup(262144, 4102, 1024, seed=3)
+tm = {}
+for pair in (0, 1):
+    run(c, pair)
+    e0, e1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
+    ms = []
+    for _ in range(3):
+        out = t.empty((c["rows"], c["T"]), dtype=t.float64, device="cuda:0")
+        s = t.cuda.current_stream().cuda_stream
+        e0.record()
+        nat.call("pf_batched_kl_i8", c["A"].data_ptr(), c["ea"].data_ptr(), c["rows"], c["B"].data_ptr(),
+                 c["eb"].data_ptr(), c["T"], c["k"], c["ldk"], c["H"].data_ptr(), c["tg"].data_ptr(), 1e-3, 0,
+                 out.data_ptr(), out.stride(0), 64, pair, s)
+        e1.record(); t.cuda.synchronize(); ms.append(e0.elapsed_time(e1))
+    ops = 34 * 2.0 * c["rows"] * c["k"] * c["T"]
+    tm[f"pair={pair}"] = {"ms": min(ms), "int8_tops": ops / (min(ms) / 1e3) / 1e12}
+print(json.dumps(tm, indent=1))
