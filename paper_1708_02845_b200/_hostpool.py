@@ -2,7 +2,7 @@
 
 A field returned by the public API is an ``n``-vector the caller owns.
 Copying it into a fresh pageable array costs page faults on every call, and a
-fresh pinned allocation costs ~0.8 ms (measured, scripts/micro_d2h.py).  This
+fresh pinned allocation costs ~0.8 ms (measured, tools/micro_d2h.py).  This
 pool hands out pinned buffers whose numpy view *is* the returned array: the
 device-to-host copy is a straight DMA into already-mapped memory, and the
 buffer goes back to the pool when the last numpy view of it is garbage

@@ -10,7 +10,7 @@
 // 4102 = 8.4 TFLOP) with a fused epilogue (split-form cancellation guard ->
 // sentinel, settle, KL[t, t] = 0).  tcgen05 has no FP64 kind, so the
 // contraction runs on the FP64 tensor-core path, mma.sync m8n8k4 (SASS
-// DMMA), fed by a 3-stage cp.async pipeline (scripts/tune_gemm.cu records
+// DMMA), fed by a 3-stage cp.async pipeline (tools/tune_gemm.cu records
 // the DFMA and register-prefetch variants it replaced: 20-22 TFLOP/s vs
 // 29.3).  Guarded pairs are re-evaluated per element in the reference form
 // by batched_kl_fixup.

@@ -41,7 +41,7 @@
 //                   columns; tcgen05.ld, combine the levels in FP64, scale,
 //                   fuse the guard / settle / target-zero, store.
 // The int8 pipe draws the board to its 1000 W cap at this shape, so the
-// kernel is power-bound (scripts/probe_power.py); a 128 x 64 single-pass
+// kernel is power-bound (tools/probe_power.py); a 128 x 64 single-pass
 // variant with eight N=64 level accumulators was 7% slower (tuning record in
 // profiles/).
 #include <cuda.h>

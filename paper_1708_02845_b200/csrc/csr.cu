@@ -31,6 +31,7 @@
 namespace pf {
 
 constexpr int kCsrThreads = 256;
+constexpr int kCsrMinBlocks = 4;
 constexpr unsigned long long kCsrGuard = 0x7ff8dead0000c5a1ull;  // NaN payload
 
 __device__ __forceinline__ bool keep_entry(double x, double cut, int strict_pos) {
@@ -264,9 +265,50 @@ __device__ __forceinline__ double csr_kl_reference_row(const double *__restrict_
   return settle(warp_sum((b[0] + b[1]) + (b[2] + b[3])));
 }
 
+// Guarded rows of the field kernel: the loop only notes them (a shared-memory
+// append, past kCsrGuardQ per CTA a sentinel in `out`); after the loop the
+// CTA's warps evaluate them in the reference form — out of line, so the
+// streaming loop keeps its registers (pf_common.cuh, "guarded KL rows").
+constexpr int kCsrGuardQ = 64;
+struct CsrGuard {
+  int n;
+  int64_t out_index[kCsrGuardQ];
+};
+
+template <class Idx>
+static __device__ __noinline__ void csr_guard_drain(
+    CsrGuard &g, const int64_t *__restrict__ indptr, const Idx *__restrict__ indices,
+    const double *__restrict__ data, const double *__restrict__ log_data,
+    const double *__restrict__ lt, int64_t row0, const int64_t *__restrict__ queries,
+    int64_t count, double *__restrict__ out, uint32_t *__restrict__ flags, int64_t first,
+    int64_t step) {
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wc = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int total = g.n, n = total < kCsrGuardQ ? total : kCsrGuardQ;
+  for (int j = wc; j < n; j += nw) {
+    const int64_t i = g.out_index[j];
+    const int64_t r = queries ? queries[i] - row0 : i;
+    int64_t lo, hi;
+    row_extent(indptr, data, r, lo, hi);
+    const double v = csr_kl_reference_row(data, log_data, indices, lt, lo, hi, lane);
+    if (lane == 0) out[i] = v;
+  }
+  if (threadIdx.x == 0 && total) atomicAdd(&flags[PF_FLAG_GUARDED], static_cast<uint32_t>(total));
+  if (total > kCsrGuardQ) {  // the rest: sentinels among this warp's own rows
+    for (int64_t i = first; i < count; i += step) {
+      if (__double_as_longlong(out[i]) != static_cast<long long>(kCsrGuard)) continue;
+      const int64_t r = queries ? queries[i] - row0 : i;
+      int64_t lo, hi;
+      row_extent(indptr, data, r, lo, hi);
+      const double v = csr_kl_reference_row(data, log_data, indices, lt, lo, hi, lane);
+      if (lane == 0) out[i] = v;
+    }
+  }
+}
+
 // ------------------------------------------------------------ K5 CSR KL --
-template <bool STAGE, class Idx>
-__global__ void __launch_bounds__(kCsrThreads) csr_kl_kernel(
+template <bool STAGE, class Idx, int MINB = kCsrMinBlocks>
+__global__ void __launch_bounds__(kCsrThreads, MINB) csr_kl_kernel(
     const int64_t *__restrict__ indptr, const Idx *__restrict__ indices,
     const double *__restrict__ data, const double *__restrict__ log_data,
     const double *__restrict__ hs, int64_t rows, int64_t k_pad,
@@ -274,6 +316,9 @@ __global__ void __launch_bounds__(kCsrThreads) csr_kl_kernel(
     int64_t nq, double *__restrict__ out, int64_t *__restrict__ ops, bool fix_inline,
     uint32_t *__restrict__ flags) {
   extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ CsrGuard gq;
+  if (threadIdx.x == 0) gq.n = 0;
+  if (!STAGE) __syncthreads();
   const double *lt = STAGE ? stage_vec(smem, logt, k_pad) : logt;
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -299,24 +344,28 @@ __global__ void __launch_bounds__(kCsrThreads) csr_kl_kernel(
     const double cross = warp_sum(a0 + a1);
     double val = h - cross;
     const bool guarded = fabs(val) < tau * (fabs(h) + fabs(cross));  // warp-uniform
-    if (guarded && fix_inline) {
-      // reference form right here, the target logs already in shared memory
-      val = csr_kl_reference_row(data, log_data, indices, lt, lo, hi, lane);
-    } else if (guarded) {
-      val = __longlong_as_double(static_cast<long long>(kCsrGuard));
-    } else {
-      val = settle(val);  // divergence.py:286
-    }
     if (lane == 0) {
-      out[i] = val;
+      if (guarded) {
+        // the reference form after the loop (fix_inline) or by the fixup scan
+        int slot = kCsrGuardQ;
+        if (fix_inline) slot = atomicAdd(&gq.n, 1);
+        if (slot < kCsrGuardQ)
+          gq.out_index[slot] = i;
+        else
+          out[i] = __longlong_as_double(static_cast<long long>(kCsrGuard));
+      } else {
+        out[i] = settle(val);  // divergence.py:286
+      }
       if (ops) ops[i] = hi - lo;  // divergence.py:276
-      if (guarded && fix_inline) atomicAdd(&flags[PF_FLAG_GUARDED], 1u);
     }
     i = i2;
     r = r2;
     lo = lo2;
     hi = hi2;
   }
+  if (fix_inline)
+    csr_guard_drain(gq, indptr, indices, data, log_data, lt, row0, queries, count, out, flags,
+                    warp, nwarps);
 }
 
 // Guarded rows: reference form sum_{supp q} v * (log v - logPt) (divergence.py:279).
@@ -353,8 +402,8 @@ __global__ void __launch_bounds__(kCsrThreads) csr_kl_fixup_kernel(
 }
 
 // ------------------------------------------------------------ K6 CSR TV --
-template <bool STAGE, class Idx>
-__global__ void __launch_bounds__(kCsrThreads) csr_tv_kernel(
+template <bool STAGE, class Idx, int MINB = kCsrMinBlocks>
+__global__ void __launch_bounds__(kCsrThreads, MINB) csr_tv_kernel(
     const int64_t *__restrict__ indptr, const Idx *__restrict__ indices,
     const double *__restrict__ data, const double *__restrict__ dropped, int64_t rows,
     int64_t k_pad, const double *__restrict__ vp, const double *__restrict__ tscal, int64_t row0,
@@ -539,11 +588,16 @@ int csr_kl_launch(const int64_t *indptr, const Idx *indices, const double *data,
   const size_t smem = 16 + static_cast<size_t>(k_pad) * 8;
   const bool staged = smem <= 200 * 1024;
   if (staged) {
-    if (int e = smem_attr(csr_kl_kernel<true, Idx>, smem)) return e;
-    const int g = grid_for((const void *)csr_kl_kernel<true, Idx>, kCsrThreads, smem, count);
-    csr_kl_kernel<true, Idx><<<g, kCsrThreads, smem, as_stream(stream)>>>(
-        indptr, indices, data, log_data, hs, rows, k_pad, logt, tau, row0, queries, nq, out,
-        ops, inline_guard != 0, flags);
+    auto go = [&](auto kern) -> int {
+      if (int e = smem_attr(kern, smem)) return e;
+      const int g = grid_for((const void *)kern, kCsrThreads, smem, count);
+      kern<<<g, kCsrThreads, smem, as_stream(stream)>>>(
+          indptr, indices, data, log_data, hs, rows, k_pad, logt, tau, row0, queries, nq, out,
+          ops, inline_guard != 0, flags);
+      return 0;
+    };
+    // 4 CTAs x 8 warps per SM, <= 64 registers (5 or 6 CTAs spill: measured 2x slower)
+    if (int e = go(csr_kl_kernel<true, Idx, kCsrMinBlocks>)) return e;
   } else {
     const int g = grid_for((const void *)csr_kl_kernel<false, Idx>, kCsrThreads, 0, count);
     csr_kl_kernel<false, Idx><<<g, kCsrThreads, 0, as_stream(stream)>>>(
@@ -573,10 +627,15 @@ int csr_tv_launch(const int64_t *indptr, const Idx *indices, const double *data,
   const int64_t k_pad = round_up(k, 2);
   const size_t smem = 16 + static_cast<size_t>(k_pad) * 8;
   if (smem <= 200 * 1024) {
-    if (int e = smem_attr(csr_tv_kernel<true, Idx>, smem)) return e;
-    const int g = grid_for((const void *)csr_tv_kernel<true, Idx>, kCsrThreads, smem, count);
-    csr_tv_kernel<true, Idx><<<g, kCsrThreads, smem, as_stream(stream)>>>(
-        indptr, indices, data, dropped, rows, k_pad, vp, tscal, row0, queries, nq, out, ops);
+    auto go = [&](auto kern) -> int {
+      if (int e = smem_attr(kern, smem)) return e;
+      const int g = grid_for((const void *)kern, kCsrThreads, smem, count);
+      kern<<<g, kCsrThreads, smem, as_stream(stream)>>>(
+          indptr, indices, data, dropped, rows, k_pad, vp, tscal, row0, queries, nq, out, ops);
+      return 0;
+    };
+    // 4 CTAs x 8 warps per SM, <= 64 registers (5 or 6 CTAs spill: measured 2x slower)
+    if (int e = go(csr_tv_kernel<true, Idx, kCsrMinBlocks>)) return e;
   } else {
     const int g = grid_for((const void *)csr_tv_kernel<false, Idx>, kCsrThreads, 0, count);
     csr_tv_kernel<false, Idx><<<g, kCsrThreads, 0, as_stream(stream)>>>(

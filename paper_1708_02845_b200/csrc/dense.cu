@@ -380,7 +380,7 @@ static int launch_cfg(K kernel, size_t smem, int64_t rows, int *grid, int thread
   return 0;
 }
 
-// Production geometry of the dense KL/TV kernels (scripts/tune_dense.cu,
+// Production geometry of the dense KL/TV kernels (tools/tune_dense.cu,
 // profiles/): 4 x 128-bit loads in flight per lane, 5 CTAs x 8 warps per SM
 // when the staged target row fits (k <~ 4,900 for 5 CTAs), else fewer.
 constexpr int kU = 4, kMinBlocks = 5;

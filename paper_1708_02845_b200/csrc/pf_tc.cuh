@@ -3,7 +3,7 @@
 // tcgen05.commit / tcgen05.ld, and TMA tensor loads (cp.async.bulk.tensor)
 // completing on mbarriers.  Used by batched_i8.cu (K7 on the int8 tensor
 // pipe).  The descriptor encodings were validated bit-for-bit against a host
-// GEMM by scripts/tune_umma.cu on the B200.
+// GEMM by tools/tune_umma.cu on the B200.
 #pragma once
 
 #include <cuda.h>

@@ -16,7 +16,7 @@
 //          broken exactly as CPython's _Py_dg_dtoa;
 // and the layout is CPython's format_float_short ('g': exponent when decpt
 // <= -4 or > 17; 'r': <= -4 or > 16, ".0" on integers, exponent "e+XX").
-// scripts/proto_wire.py is the same algorithm in Python integers, checked
+// tools/proto_wire.py is the same algorithm in Python integers, checked
 // against CPython on ~400K values; tests/test_wire_gpu.py checks this port.
 //
 // Lines are formatted into fixed 64-byte slots with their lengths, then

@@ -1,5 +1,5 @@
 // wire_core.cuh — exact double -> text digit generation shared by the device
-// formatter (wire.cu) and its host build (scripts/wire_host_check.py): a
+// formatter (wire.cu) and its host build (tools/wire_host_check.py): a
 // fixed-capacity big integer, dtoa modes 2 (17 digits) and 0 (shortest
 // round trip, CPython's tie rules), and CPython's format_float_short layout.
 #pragma once

@@ -1,6 +1,6 @@
 """The reference's own test-suite as the drop-in regression on the B200.
 
-`scripts/install_reference.sh` installs the unmodified reference package into
+`tools/install_reference.sh` installs the unmodified reference package into
 baseline/_ref (git-ignored, shipped with the snapshot) with its 224 tests
 beside it.  This test runs that suite in a subprocess with
 ``-p paper_1708_02845_b200.pytest_plugin``, which routes every hot-path
@@ -30,7 +30,7 @@ EXPECTED_DIFFERENT: dict = {}
 
 
 @pytest.mark.skipif(not (REF / "pathfield").is_dir() or not (SUITE / "tests").is_dir(),
-                    reason="reference not installed (scripts/install_reference.sh)")
+                    reason="reference not installed (tools/install_reference.sh)")
 def test_reference_suite_through_install():
     env = dict(os.environ)
     env["PYTHONPATH"] = os.pathsep.join([str(REF), str(ROOT)])

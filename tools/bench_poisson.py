@@ -1,6 +1,6 @@
 """Time (and optionally validate) the device Poisson kernel at full size.
 
-    python scripts/bench_poisson.py c2 [--validate] [--leaf 64] [--reps 3]
+    python tools/bench_poisson.py c2 [--validate] [--leaf 64] [--reps 3]
 
 Phases: host plan (nd_plan.cpp), device Laplacian, multifrontal factor,
 forward + backward solves and finalize (CUDA events on the launch stream).

@@ -1,6 +1,6 @@
 """Summarise ncu reports into profiles/ (run in the build container).
 
-    python scripts/ncu_summarize.py <tag> gpurun_out/prof_*_<tag>.ncu-rep ...
+    python tools/ncu_summarize.py <tag> gpurun_out/prof_*_<tag>.ncu-rep ...
 """
 import csv
 import json

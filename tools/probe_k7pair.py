@@ -39,8 +39,9 @@ def run(c, pair, grade=64):
     return out
 
 
+ONCE = "--once" in sys.argv
 res = {}
-for rows, k, T in [(300, 200, 50), (1000, 300, 130), (129, 64, 64), (2047, 1234, 256), (5000, 4102, 1024)]:
+for rows, k, T in [] if ONCE else [(300, 200, 50), (1000, 300, 130), (129, 64, 64), (2047, 1234, 256), (5000, 4102, 1024)]:
     c = setup(rows, k, T)
     for grade in (64, 32):
         a = run(c, 0, grade).cpu().numpy()
@@ -52,6 +53,11 @@ for rows, k, T in [(300, 200, 50), (1000, 300, 130), (129, 64, 64), (2047, 1234,
 print(json.dumps(res, indent=1), flush=True)
 if not all(v["bitwise"] and v["untouched"] == 0 for v in res.values()):
     sys.exit(1)
+if ONCE:   # one launch of each kernel for ncu
+    c = setup(262144, 4102, 1024, seed=3)
+    run(c, 1)
+    run(c, 0)
+    sys.exit(0)
 # timing at a C5-like slab
 c = setup(262144, 4102, 1024, seed=3)
 tm = {}

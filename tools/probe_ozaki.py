@@ -1,7 +1,7 @@
 """GPU probe for K7 on the int8 tensor pipe (batched_i8.cu): accuracy against
 the FP64 DMMA path and a torch FP64 GEMM, then timing at the C5 shape.
 
-python scripts/probe_ozaki.py [--big]
+python tools/probe_ozaki.py [--big]
 """
 import sys
 import time

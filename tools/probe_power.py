@@ -1,7 +1,7 @@
 """Sustained-load clocks/power probe: K7 i8 GEMM at C5 shape and the int8 UMMA
 ceiling probe, each run back to back for ~2 s with NVML sampled every 5 ms.
 
-python scripts/probe_power.py
+python tools/probe_power.py
 """
 import ctypes
 import statistics

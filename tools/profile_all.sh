@@ -1,13 +1,13 @@
 #!/bin/bash
 # ncu --set full captures of every product kernel family (run under gpurun).
-#   bash scripts/profile_all.sh <tag> [comma list: csr,gemm,gemm_i8,tracer,f32,hausdorff]
+#   bash tools/profile_all.sh <tag> [comma list: csr,gemm,gemm_i8,tracer,f32,hausdorff]
 TAG=${1:-r1}
 mkdir -p gpurun_out
 run() {  # name, kernel regex, skip, count, args...
   local name=$1 re=$2 skip=$3 cnt=$4; shift 4
-  python scripts/prof_extras.py "$@" > gpurun_out/pa_${name}_${TAG}.log 2>&1 && \
+  python tools/prof_extras.py "$@" > gpurun_out/pa_${name}_${TAG}.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:"$re" -s $skip -c $cnt \
-      -o gpurun_out/prof_${name}_${TAG} python scripts/prof_extras.py "$@" \
+      -o gpurun_out/prof_${name}_${TAG} python tools/prof_extras.py "$@" \
       > gpurun_out/ncu_${name}_${TAG}.log 2>&1
   echo "$name rc=$?"
 }

@@ -1,6 +1,6 @@
 #!/bin/bash
 # Profiling recipe (run under gpurun from the repo root):
-#   bash scripts/profile_round.sh <tag> [bench args...]
+#   bash tools/profile_round.sh <tag> [bench args...]
 # 1) plain bench run, 2) ncu launch list of the same command,
 # 3) ncu --set full of the dense KL/TV kernels (same command again).
 TAG=${1:-r1}; shift

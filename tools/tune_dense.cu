@@ -1,6 +1,6 @@
 // Standalone tuner for the dense field kernels (not part of the product).
 // Build: nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -I include \
-//        scripts/tune_dense.cu -o build/tune_dense
+//        tools/tune_dense.cu -o build/tune_dense
 // Times KL/TV template variants and a pure streaming-read ceiling on
 // synthetic P of the C2 shape (rows x k FP64, ld = round_up(k,16)).
 #include <cstdio>

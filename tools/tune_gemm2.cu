@@ -1,5 +1,5 @@
 // Tile-shape sweep for the K7 DMMA GEMM (not part of the product).
-// nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -Iinclude scripts/tune_gemm2.cu
+// nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -Iinclude tools/tune_gemm2.cu
 #include <cstdio>
 #include <cstdlib>
 #include <vector>

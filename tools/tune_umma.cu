@@ -4,7 +4,7 @@
 //     TMEM read back with tcgen05.ld) against a host GEMM;
 //  2) issue-rate throughput of back-to-back M=128 MMAs at N = 64/128/256 with
 //     operands resident in shared memory (no global traffic), all SMs.
-// nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a scripts/tune_umma.cu -o /tmp/tu
+// nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a tools/tune_umma.cu -o /tmp/tu
 #include <cstdio>
 #include <cstdlib>
 #include <cstdint>

@@ -1,6 +1,6 @@
 """Full-size parity on REAL Poisson kernels (run on the GPU box; minutes of CPU).
 
-    python scripts/validate_real.py c2 > gpurun_out/validate_c2.json
+    python tools/validate_real.py c2 > gpurun_out/validate_c2.json
 
 Builds the config mesh with the reference's generators (oracle/inputs.py,
 bitwise the reference's, see tests/test_oracle.py), the Poisson kernel with

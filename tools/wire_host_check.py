@@ -1,7 +1,7 @@
 """Host build of csrc/wire_core.cuh (the exact digit generators the device
 formatter runs) checked against CPython: f"{v:.17g}" and repr(v).
 
-python scripts/wire_host_check.py [n_random]
+python tools/wire_host_check.py [n_random]
 """
 import ctypes
 import subprocess
@@ -12,7 +12,7 @@ from pathlib import Path
 import numpy as np
 
 ROOT = Path(__file__).resolve().parents[1]
-sys.path.insert(0, str(ROOT / "scripts"))
+sys.path.insert(0, str(ROOT / "tools"))
 import proto_wire as P  # noqa: E402
 
 SRC = r'''
