@@ -973,10 +973,19 @@ def run_native(args):
     t.cuda.set_device(local)
     device = t.device("cuda", local)
     dist = None
-    if ws > 1:
+    single = ws == 1 and not args.sharded   # --sharded: the N-rank path on one rank
+    if not single:
         # control plane (rendezvous, NCCL unique id, barriers, timing max) on gloo;
         # the data plane is NCCL through the C ABI (parallel.NcclComm)
         import torch.distributed as dist
+        if ws == 1:
+            import socket
+            with socket.socket() as so:
+                so.bind(("127.0.0.1", 0))
+                os.environ.setdefault("MASTER_PORT", str(so.getsockname()[1]))
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("gloo")
 
     n_expect, k_expect, desc = WORKLOADS[args.workload]
@@ -985,7 +994,7 @@ def run_native(args):
     _, target = default_endpoints(omesh)
     bounds = par.partition_rows(n, ws)
     sharded = None
-    if ws == 1:
+    if single:
         dp, dk, prep = device_build(t, L, omesh, device)
     else:
         dp = None
@@ -1040,7 +1049,7 @@ def run_native(args):
         guarded = int(g.item())
 
     # ------------------------------------------------ e2e via the public API
-    if ws == 1:
+    if single:
         w0 = time.perf_counter()
         dense = L.dense_to_host(dk.P, n, k)
         host_copy_s = time.perf_counter() - w0
@@ -1127,7 +1136,7 @@ def run_native(args):
 
     # ------------------------------------------------ CPU baseline (rank 0, N=1)
     cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu:
+    if rank == 0 and single and not args.no_cpu:
         threads = os.cpu_count() or 1
         ref = CpuReference(device_rows(t, dk, target), k, args.cpu_budget, threads,
                            "real rows of this P")
@@ -1142,7 +1151,7 @@ def run_native(args):
     bytes_tv = rows * (8 * k + 8) + 8 * k
     traffic = None
     prof = ROOT / "profiles" / "ncu_summary.json"
-    if prof.exists() and ws == 1:
+    if prof.exists() and single:
         try:
             traffic = json.loads(prof.read_text()).get(args.workload, {}).get("dense_kl_dram_bytes")
         except Exception:
@@ -1156,7 +1165,7 @@ def run_native(args):
 
     extras = {}
     want = set(args.extras.split(",")) if not args.no_extras else set()
-    if ws == 1:
+    if single:
         def run_extra(name, fn):
             if name not in want:
                 return
@@ -1199,7 +1208,8 @@ def run_native(args):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "real: reference-generator mesh, Poisson kernel P built on the GPU",
         "config": {"workload": desc, "n": n, "k": k, "rows_per_gpu_max": max(b - a for a, b in bounds),
-                   "parallelism": f"row-slab x{ws}", "target": int(target),
+                   "parallelism": f"row-slab x{ws}" + ("" if single else " (sharded path)"),
+                   "target": int(target),
                    "l2": "inputs larger than L2 (P slab %.2f GB/GPU vs 126 MB L2)"
                          % (rows * dk_ld(k) * 8 / 1e9)},
         "roofline": roof,
@@ -1342,6 +1352,9 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the side measurements")
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the N-rank path (slab build, NCCL collectives, sharded extras) "
+                         "even at one rank")
     ap.add_argument("--extras", default="c4_f32,c5,poisson,c2,c2p,c2_synthetic,wire,c3",
                     help="comma list of side measurements (N=1: c4_f32, c5, poisson, c2, c2p, "
                          "c2_synthetic, wire; N>1: c3, c5)")
