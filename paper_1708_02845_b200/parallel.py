@@ -486,7 +486,8 @@ def field_batch_by_targets(pk, fd, targets, dist, gather: bool = False, method: 
 
 
 def trace_batch(mesh, pk, fd, targets, sources, field_of, dist, settings=None,
-                method: str = "auto", clamp=None, gather_paths: bool = False):
+                method: str = "auto", clamp=None, gather_paths: bool = False,
+                status_only: bool = False):
     """C5 on N GPUs (SURVEY §8e item 3, §8 a9 + a10): fields to T targets with
     the targets partitioned over the ranks (:func:`field_batch_by_targets`,
     P replicated) and each path p traced on the rank that owns its target
@@ -495,7 +496,9 @@ def trace_batch(mesh, pk, fd, targets, sources, field_of, dist, settings=None,
 
     Every path equals ``triangle_descent(mesh, dv_field(pk, fd, targets[field_of[p]]),
     sources[p])``.  Returns ``(path_indices, paths)`` for this rank, or with
-    `gather_paths` the list of every path in input order on every rank."""
+    `gather_paths` the list of every path in input order on every rank; with
+    `status_only`, ``(path_indices, status codes, location counts)`` without
+    building the host path objects (what a throughput measurement needs)."""
     from .config import DEFAULTS
     settings = settings or DEFAULTS
     targets = np.asarray(targets, dtype=np.int64).reshape(-1)
@@ -514,6 +517,11 @@ def trace_batch(mesh, pk, fd, targets, sources, field_of, dist, settings=None,
                                                   clamp=clamp)
     mine = np.flatnonzero((field_of >= a) & (field_of < b))
     ldo = int(vals.stride(0)) if vals.dim() == 2 else 1
+    if status_only:
+        from .paths import trace_fields_status
+        st, cnt = trace_fields_status(mesh, vals, 1, ldo, mine_t, sources[mine],
+                                      field_of[mine] - a, settings)
+        return mine, st, cnt
     paths = _trace_local(mesh, vals, 1, ldo, mine_t, sources[mine], field_of[mine] - a, settings)
     if not gather_paths:
         return mine, paths

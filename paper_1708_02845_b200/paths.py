@@ -191,6 +191,21 @@ def trace_arrays(mesh, fields, targets, sources, field_of=None, settings: Settin
     return buf, counts, over, extra
 
 
+def trace_fields_status(mesh, fields, field_ld: int, vertex_ld: int, targets, sources,
+                        field_of=None, settings: Settings = DEFAULTS):
+    """:func:`trace_fields` without building the host TracedPath objects:
+    returns (status codes (0 reached, 1 stuck, 2 max steps), location counts)
+    as numpy arrays — the per-path result summary a batched caller needs."""
+    sources = np.asarray(sources, dtype=np.int64).reshape(-1)
+    targets = np.asarray(targets, dtype=np.int64).reshape(-1)
+    fo = None if field_of is None else np.asarray(field_of, dtype=np.int64).reshape(-1)
+    if sources.size == 0:
+        return np.zeros(0, np.int32), np.zeros(0, np.int64)
+    buf, counts, over, extra = trace_arrays(mesh, fields, targets, sources, fo, settings,
+                                            layout=(field_ld, vertex_ld))
+    return buf.status[:sources.size].cpu().numpy().astype(np.int32), counts
+
+
 def trace_fields(mesh, fields, field_ld: int, vertex_ld: int, targets, sources, field_of=None,
                  settings: Settings = DEFAULTS) -> list[TracedPath]:
     """:func:`triangle_descent_batch` over device-resident fields in any 2-D
