@@ -40,8 +40,9 @@ def run(c, pair, grade=64):
 
 
 ONCE = "--once" in sys.argv
+SCAN = "--scan" in sys.argv
 res = {}
-for rows, k, T in [] if ONCE else [(300, 200, 50), (1000, 300, 130), (129, 64, 64), (2047, 1234, 256), (5000, 4102, 1024)]:
+for rows, k, T in [] if (ONCE or SCAN) else [(300, 200, 50), (1000, 300, 130), (129, 64, 64), (2047, 1234, 256), (5000, 4102, 1024)]:
     c = setup(rows, k, T)
     for grade in (64, 32):
         a = run(c, 0, grade).cpu().numpy()
@@ -53,6 +54,28 @@ for rows, k, T in [] if ONCE else [(300, 200, 50), (1000, 300, 130), (129, 64, 6
 print(json.dumps(res, indent=1), flush=True)
 if not all(v["bitwise"] and v["untouched"] == 0 for v in res.values()):
     sys.exit(1)
+if SCAN:   # time per unit of work against T (A reuse across target tiles)
+    out = {}
+    for T in (128, 256, 512, 1024):
+        c = setup(131072, 4102, T, seed=5)
+        for pair in (0, 1):
+            run(c, pair)
+            e0, e1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
+            o = t.empty((c["rows"], c["T"]), dtype=t.float64, device="cuda:0")
+            ms = []
+            for _ in range(3):
+                e0.record()
+                nat.call("pf_batched_kl_i8", c["A"].data_ptr(), c["ea"].data_ptr(), c["rows"],
+                         c["B"].data_ptr(), c["eb"].data_ptr(), c["T"], c["k"], c["ldk"],
+                         c["H"].data_ptr(), c["tg"].data_ptr(), 1e-3, 0, o.data_ptr(), o.stride(0),
+                         64, pair, t.cuda.current_stream().cuda_stream)
+                e1.record(); t.cuda.synchronize(); ms.append(e0.elapsed_time(e1))
+            ops = 34 * 2.0 * c["rows"] * c["k"] * c["T"]
+            out[f"T={T} pair={pair}"] = {"ms": min(ms), "int8_tops": ops / (min(ms) / 1e3) / 1e12}
+        del c
+        t.cuda.empty_cache()
+    print(json.dumps(out, indent=1))
+    sys.exit(0)
 if ONCE:   # one launch of each kernel for ncu
     c = setup(262144, 4102, 1024, seed=3)
     run(c, 1)
