@@ -199,27 +199,47 @@ class CpuReference:
     """Oracle port (reference algorithm: dv_at over row chunks == dv_field,
     SURVEY A.1) on a bounded sample of rows, on all host threads.  `rows_of(m)`
     returns an (m, k) host matrix whose row 0 is the target row; the sample
-    is sized once so one KL+TV pass takes ~budget_s."""
+    is sized once so one KL+TV pass takes ~budget_s.  `on_matrix` instead
+    evaluates rows of a full host P in place (evenly spaced rows, or all of
+    them when the budget allows: then the sample IS the whole field)."""
 
-    def __init__(self, rows_of, k: int, budget_s: float, threads: int, what: str):
+    def __init__(self, rows_of, k: int, budget_s: float, threads: int, what: str,
+                 matrix=None, target: int = 0):
+        import numpy as np
         from oracle import divergence as O
         self.O, self.k, self.threads = O, k, threads
+        if matrix is not None:
+            n = matrix.shape[0]
+            self.P, self.target = matrix, int(target)
+            probe = np.linspace(0, n - 1, 2048).astype(np.int64)
+            t0 = time.perf_counter()
+            self._pass(self.P, probe)
+            dt = max(time.perf_counter() - t0, 1e-3)
+            m = int(min(n, max(2048, 2048 * budget_s / dt)))
+            self.idx = np.arange(n, dtype=np.int64) if m >= n else \
+                np.linspace(0, n - 1, m).astype(np.int64)
+            self.rows = int(self.idx.size)
+            self.sample = (f"KL+TV fields over {self.rows:,} of {n:,} rows x k={k} ({what}; "
+                           f"evaluated in place in the host P), {threads} threads")
+            return
+        self.target, self.idx = 0, None
         calib = rows_of(1024)
         t0 = time.perf_counter()
-        self._pass(calib)
+        self._pass(calib, None)
         dt = max(time.perf_counter() - t0, 1e-3)
         self.rows = int(min(200_000, max(1024, 1024 * budget_s / dt)))
         self.P = rows_of(self.rows)
         self.sample = (f"KL+TV fields over {self.rows} sampled rows x k={k} ({what}; target "
                        f"row first), {threads} threads")
 
-    def _pass(self, P):
-        self.O.dv_field_chunked(P, "kl", 0, chunk_rows=256, threads=self.threads)
-        self.O.dv_field_chunked(P, "tv", 0, chunk_rows=256, threads=self.threads)
+    def _pass(self, P, idx):
+        tgt = self.target if idx is not None else 0
+        self.O.dv_field_chunked(P, "kl", tgt, rows=idx, chunk_rows=256, threads=self.threads)
+        self.O.dv_field_chunked(P, "tv", tgt, rows=idx, chunk_rows=256, threads=self.threads)
 
     def step(self):
         t0 = time.perf_counter()
-        self._pass(self.P)
+        self._pass(self.P, self.idx)
         el = time.perf_counter() - t0
         return 2 * self.rows / el, el
 
@@ -1168,8 +1188,8 @@ def run_native(args):
     cpu = None
     if rank == 0 and single and not args.no_cpu:
         threads = os.cpu_count() or 1
-        ref = CpuReference(device_rows(t, dk, target), k, args.cpu_budget, threads,
-                           "real rows of this P")
+        ref = CpuReference(None, k, args.cpu_budget, threads, "real rows of this P",
+                           matrix=pk.dense, target=target)
         v, el = ref.step()
         cpu = {"value": v, "unit": "evals/s", "cores": threads, "kind": "port",
                "sample": ref.sample + f" ({el:.1f} s); oracle/divergence.py restating "
