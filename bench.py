@@ -125,7 +125,11 @@ class ClockSampler:
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
-        time.sleep(0.02)
+        # the timed region starts only once the sampler is producing samples
+        # (NVML initialisation can take longer than a short timed region)
+        t0 = time.perf_counter()
+        while not self.samples and time.perf_counter() - t0 < 10.0:
+            time.sleep(0.005)
         return self
 
     def __exit__(self, *a):
