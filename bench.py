@@ -777,30 +777,32 @@ def extra_c5(t, nat, dev, pf, device, dk, omesh, steps, peak):
     fl = ctypes.c_int64(0)
     probe = t.empty(2, dtype=t.float64, device=device)
 
-    def probe_rate(name, iters):
-        nat.call(name, iters // 4, ctypes.byref(fl), probe.data_ptr(), s.cuda_stream)
+    def probe_rate(name, iters, *mode):
+        nat.call(name, iters // 4, *mode, ctypes.byref(fl), probe.data_ptr(), s.cuda_stream)
         t.cuda.synchronize()
         e0.record(s)
-        nat.call(name, iters, ctypes.byref(fl), probe.data_ptr(), s.cuda_stream)
+        nat.call(name, iters, *mode, ctypes.byref(fl), probe.data_ptr(), s.cuda_stream)
         e1.record(s)
         t.cuda.synchronize()
         return fl.value / (e0.elapsed_time(e1) / 1e3) / 1e12
 
-    def probe_sustained(name, iters, reps=8):
+    def probe_sustained(name, iters, *mode, reps=8):
         """The probe back to back for ~0.3 s (the board at its power cap, as
         during a C5 batch); rate over the last half of the launches."""
         for _ in range(reps // 2):
-            nat.call(name, iters, ctypes.byref(fl), probe.data_ptr(), s.cuda_stream)
+            nat.call(name, iters, *mode, ctypes.byref(fl), probe.data_ptr(), s.cuda_stream)
         e0.record(s)
         for _ in range(reps - reps // 2):
-            nat.call(name, iters, ctypes.byref(fl), probe.data_ptr(), s.cuda_stream)
+            nat.call(name, iters, *mode, ctypes.byref(fl), probe.data_ptr(), s.cuda_stream)
         e1.record(s)
         t.cuda.synchronize()
         return fl.value * (reps - reps // 2) / (e0.elapsed_time(e1) / 1e3) / 1e12
 
     dfma_tf = probe_rate("pf_probe_dfma_f64", 1 << 16)
-    i8_tops = probe_rate("pf_probe_umma_i8", 1 << 14)
-    i8_tops_sustained = probe_sustained("pf_probe_umma_i8", 1 << 14)
+    i8_tops = probe_rate("pf_probe_umma_i8", 1 << 14, 1)
+    i8_tops_sustained = probe_sustained("pf_probe_umma_i8", 1 << 14, 1)
+    i8_tops_pattern = probe_rate("pf_probe_umma_i8", 1 << 14, 0)
+    i8_tops_pattern_sustained = probe_sustained("pf_probe_umma_i8", 1 << 14, 0)
     int_ops = 34 * flops
     ach = int_ops / (gemm_only / 1e3) / 1e12
     res = {"workload": f"C5: C4 real P ({rows:,} x {k:,}), T = {T} targets (SURVEY §8d C5), KL "
@@ -815,12 +817,20 @@ def extra_c5(t, nat, dev, pf, device, dk, omesh, steps, peak):
            "roofline": {"bound": "tensor", "achieved": ach, "peak": i8_tops_sustained,
                         "unit": "TOPS (int8)", "frac": ach / i8_tops_sustained,
                         "frac_of_burst_probe": ach / i8_tops, "burst_peak": i8_tops,
+                        "pattern_operand_probe": {
+                            "burst": i8_tops_pattern, "sustained": i8_tops_pattern_sustained,
+                            "frac_of_sustained": ach / i8_tops_pattern_sustained,
+                            "note": "the round-1 probe (operand bytes 0..3): the tensor pipe "
+                                    "draws less power on it and holds a higher clock"},
                         "algorithmic_ops_per_launch": int_ops,
                         "peak_kind": "measured: pf_probe_umma_i8 (M128 N256 K32 u8 tcgen05.mma "
-                                     "back to back from shared memory, all SMs), sustained "
-                                     "(~0.3 s back to back, under the 1 kW power cap, as the "
-                                     "~0.1 s C5 GEMM runs); burst_peak is one ~36 ms launch",
-                        "kernel": "pf::batched_kl_i8_pair_kernel<7,9> (tcgen05 cta_group::2)"},
+                                     "back to back from shared memory, all SMs, random operand "
+                                     "bytes as K7's slice planes and as MEASURED_PEAKS' bf16 "
+                                     "matmul), sustained (~0.3 s back to back, under the 1 kW "
+                                     "power cap, as the ~0.1 s C5 GEMM runs); burst_peak is "
+                                     "one launch",
+                        "kernel": "pf::batched_kl_i8_pp_kernel<7,9> (persistent tcgen05 "
+                                  "cta_group::2 pair, epilogue off the MMA critical path)"},
            "fp32_grade": {"note": "same kernel, 15 byte-pair GEMMs (levels 2..6 of the top 5 "
                                   "planes): the north-star FP32 tolerance 1e-5",
                           "ms_per_batch": ms_f32grade,

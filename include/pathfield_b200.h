@@ -334,8 +334,13 @@ int pf_batched_kl_i8(const uint8_t *A, const int32_t *ea, int64_t rows, const ui
 
 /* Diagnostic: back-to-back M128 N256 K32 u8 tcgen05.mma on shared-memory
  * operands, one CTA per SM (*ops_host = integer ops issued): the int8 tensor
- * pipe ceiling pf_batched_kl_i8 is measured against. */
-int pf_probe_umma_i8(int64_t iters, int64_t *ops_host, uint32_t *sink, pf_stream_t stream);
+ * pipe ceiling pf_batched_kl_i8 is measured against.  random_operands != 0
+ * fills the operands with hashed random bytes (K7's slice planes are random
+ * bytes, and the tensor pipe's power draw -- hence the clock it holds under
+ * the board's power cap -- depends on the operand bits; MEASURED_PEAKS'
+ * bf16 figure is likewise taken on random matrices), 0 with a 0..3 pattern. */
+int pf_probe_umma_i8(int64_t iters, int random_operands, int64_t *ops_host, uint32_t *sink,
+                     pf_stream_t stream);
 
 /* Diagnostic: a pure-DFMA kernel (8 independent FMA chains per thread, all
  * SMs); *flops_host receives its FLOP count so the caller can time it and

@@ -148,6 +148,13 @@ __global__ void __launch_bounds__(256) slice_targets_kernel(const double *__rest
   }
 }
 
+// v * 2^e with one rounding == ldexp(v, e) whenever 2^e is a normal double
+__device__ __forceinline__ double pow2_scale(double v, int e) {
+  return (e >= -1022 && e <= 1023)
+             ? v * __longlong_as_double(static_cast<long long>(e + 1023) << 52)
+             : ldexp(v, e);
+}
+
 // ------------------------------------------------------------------ GEMM --
 // Two passes per 128 x 128 output tile, because TMEM holds four N=128
 // accumulators (4 x 128 columns = all 512): pass 1 = levels 2..5 (10 byte
@@ -221,45 +228,46 @@ __global__ void __launch_bounds__(kO2Threads, 1) batched_kl_i8_n128_kernel(
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      // ---- MMA issuer
+      // ---- MMA issuer; each pass its own loop (a conditional commit inside
+      // a shared loop compiles to a predicated UTCBAR that stalls every stage)
       constexpr uint32_t idesc = tc::idesc_i8(128, kO2BN, false, false);
-      for (int it = 0; it < 2 * nkb; ++it) {
-        const int s = it % kO2Stages;
-        const bool p1 = it < nkb;
-        const int kb = p1 ? it : it - nkb;
-        if (it == nkb) {  // pass 2 reuses the accumulators: wait for the drain
-          mbar_wait(&drained_bar, 0);
-          tc::fence_after();
-        }
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % kO2Stages;
+        mbar_wait(&full_bar[s], (kb / kO2Stages) & 1);
+        tc::fence_after();
+        const uint32_t sa = smem_u32(smem + s * kO2StageBytes);
+        const uint32_t sb = sa + kOzSlices * kO2Tile;
+#pragma unroll
+        for (int i = 1; i <= kO2Pass1Slices; ++i)
+#pragma unroll
+          for (int j = 1; j <= kO2Pass1Slices; ++j) {
+            const int l = i + j;
+            if (l > 5) continue;
+            tc::mma_i8(tmem + (l - 2) * kO2BN, tc::sdesc<32>(sa + (i - 1) * kO2Tile),
+                       tc::sdesc<32>(sb + (j - 1) * kO2Tile), idesc, !(kb == 0 && i == 1));
+          }
+        tc::commit(&empty_bar[s]);
+      }
+      tc::commit(&pass_bar[0]);
+      mbar_wait(&drained_bar, 0);   // pass 2 reuses the accumulators
+      tc::fence_after();
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int it = nkb + kb, s = it % kO2Stages;
         mbar_wait(&full_bar[s], (it / kO2Stages) & 1);
         tc::fence_after();
         const uint32_t sa = smem_u32(smem + s * kO2StageBytes);
         const uint32_t sb = sa + kOzSlices * kO2Tile;
-        if (p1) {
 #pragma unroll
-          for (int i = 1; i <= kO2Pass1Slices; ++i)
+        for (int i = 1; i <= kS; ++i)
 #pragma unroll
-            for (int j = 1; j <= kO2Pass1Slices; ++j) {
-              const int l = i + j;
-              if (l > 5) continue;
-              tc::mma_i8(tmem + (l - 2) * kO2BN, tc::sdesc<32>(sa + (i - 1) * kO2Tile),
-                         tc::sdesc<32>(sb + (j - 1) * kO2Tile), idesc, !(kb == 0 && i == 1));
-            }
-        } else {
-#pragma unroll
-          for (int i = 1; i <= kS; ++i)
-#pragma unroll
-            for (int j = 1; j <= kS; ++j) {
-              const int l = i + j;
-              if (l < 6 || l > kMaxL) continue;
-              const int first_i = l - kS > 1 ? l - kS : 1;
-              tc::mma_i8(tmem + (l - 6) * kO2BN, tc::sdesc<32>(sa + (i - 1) * kO2Tile),
-                         tc::sdesc<32>(sb + (j - 1) * kO2Tile), idesc,
-                         !(kb == 0 && i == first_i));
-            }
-        }
+          for (int j = 1; j <= kS; ++j) {
+            const int l = i + j;
+            if (l < 6 || l > kMaxL) continue;
+            const int first_i = l - kS > 1 ? l - kS : 1;
+            tc::mma_i8(tmem + (l - 6) * kO2BN, tc::sdesc<32>(sa + (i - 1) * kO2Tile),
+                       tc::sdesc<32>(sb + (j - 1) * kO2Tile), idesc, !(kb == 0 && i == first_i));
+          }
         tc::commit(&empty_bar[s]);
-        if (it == nkb - 1) tc::commit(&pass_bar[0]);
       }
       tc::commit(&pass_bar[1]);
     }
@@ -311,7 +319,7 @@ __global__ void __launch_bounds__(kO2Threads, 1) batched_kl_i8_n128_kernel(
 #pragma unroll
         for (int l = kL2 - 2; l >= 0; --l) v = fma(v, 0x1p-8, static_cast<double>(acc[l][u]));
         v = fma(v, 0x1p-32, v1[c0 + u]);
-        const double S = ldexp(v, e_q + eb[t] - 16);
+        const double S = pow2_scale(v, e_q + eb[t] - 16);
         double val = h + S;
         const bool is_t = (tq == targets[t]);
         if (!is_t && fabs(val) < tau * (fabs(h) + fabs(S)))
@@ -325,6 +333,18 @@ __global__ void __launch_bounds__(kO2Threads, 1) batched_kl_i8_n128_kernel(
   tc::fence_before();
   __syncthreads();
   if (warp == 0) tc::tmem_free<512>(tmem);
+}
+
+// PF_K7_DIAG bit 2: per-CTA %globaltimer stamps into out[cta * 8 + i]
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ uint32_t smid() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
 }
 
 // ---------------------------------------------------------- GEMM, CTA pair --
@@ -344,7 +364,18 @@ constexpr int kP2TileB = kP2HalfN * kO2BK;                    // 2 KB per slice
 constexpr int kP2StageBytes = kOzSlices * (kP2TileA + kP2TileB);  // 43,008
 constexpr int kP2Smem = kP2Stages * kP2StageBytes + 1024;
 
-template <int kS, int kMaxL>
+//
+// kQuad: two such pairs in one cluster of 4 on the same row-tile pair and
+// adjacent target tiles share every A tile by TMA multicast: each CTA loads
+// one 64-row half of its row tile (one box per slice, the UMMA layout needs
+// the halves interleaved within each slice plane) and multicasts it to the
+// CTA of the other pair holding the same rows, so A crosses L2 -> SM once
+// per two pairs.  Each slot's empty barrier then waits for both pairs' MMAs.
+//
+// kDiag (timing diagnostics only, PF_K7_DIAG, wrong outputs): bit 0 = no TMA
+// loads (the MMAs run on stale shared memory), bit 1 = no epilogue arithmetic
+// or stores (accumulators drained and dropped).
+template <int kS, int kMaxL, bool kQuad, int kDiag = 0>
 __global__ void __launch_bounds__(kO2Threads, 1)
     batched_kl_i8_pair_kernel(const __grid_constant__ CUtensorMap mapA7,
                               const __grid_constant__ CUtensorMap mapA4,
@@ -362,11 +393,17 @@ __global__ void __launch_bounds__(kO2Threads, 1)
   __shared__ uint32_t tmem_base;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  double *stamp = (kDiag & 4) ? out + (static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x) * 8
+                              : nullptr;
+  if ((kDiag & 4) && tid == 0) stamp[0] = static_cast<double>(gtimer());
   // cluster (2, 1, 1): x = 2 x target tile + pair rank (the 2-CTA MMA pairs
   // adjacent x ranks), y = row-tile pair; the target tiles of one row pair are
   // consecutive CTAs, so its A tiles stream from HBM once and hit L2 after
-  const uint32_t rank = tc::cluster_rank();   // 0 = leader (issues the MMAs)
-  const int t0 = (blockIdx.x >> 1) * kP2BN;
+  const uint32_t crank = tc::cluster_rank();
+  const uint32_t rank = crank & 1;           // 0 = pair leader (issues the MMAs)
+  const uint32_t pairi = crank >> 1;         // kQuad: which pair of the cluster
+  const uint32_t leader = crank & 2;         // cluster rank of this pair's leader
+  const int t0 = kQuad ? ((blockIdx.x >> 2) * 2 + pairi) * kP2BN : (blockIdx.x >> 1) * kP2BN;
   const int64_t q0 = (static_cast<int64_t>(blockIdx.y) * 2 + rank) * 128;   // this CTA's rows
 
   if (tid == 0) {
@@ -376,7 +413,7 @@ __global__ void __launch_bounds__(kO2Threads, 1)
     tc::prefetch_map(&mapB4);
     for (int s = 0; s < kP2Stages; ++s) {
       mbar_init(&full_bar[s], 1);    // the leader's producer arrives (both CTAs' bytes)
-      mbar_init(&empty_bar[s], 1);   // one multicast MMA commit
+      mbar_init(&empty_bar[s], kQuad ? 2 : 1);   // one multicast commit per pair
     }
     mbar_init(&pass_bar[0], 1);
     mbar_init(&pass_bar[1], 1);
@@ -385,6 +422,7 @@ __global__ void __launch_bounds__(kO2Threads, 1)
   if (warp == 0) tc::tmem_alloc_pair<512>(&tmem_base);
   tc::fence_before();
   tc::cluster_sync();               // barriers of both CTAs initialised, TMEM allocated
+  if ((kDiag & 4) && tid == 0) stamp[1] = static_cast<double>(gtimer());
   tc::fence_after();
   const uint32_t tmem = tmem_base;
 
@@ -401,56 +439,85 @@ __global__ void __launch_bounds__(kO2Threads, 1)
         mbar_wait(&empty_bar[s], (round & 1) ^ 1);
         uint8_t *sa = smem + s * kP2StageBytes;
         uint8_t *sb = sa + kOzSlices * kP2TileA;
+        if constexpr ((kDiag & 1) != 0) {
+          if (rank == 0) mbar_arrive(&full_bar[s]);
+          continue;
+        }
         if (rank == 0) mbar_expect_tx(&full_bar[s], 2 * ns * (kP2TileA + kP2TileB));
-        const uint32_t lb = tc::mapa(&full_bar[s], 0);
-        tc::tma_load_3d_pair(sa, p1 ? &mapA4 : &mapA7, kb * kO2BK, static_cast<int32_t>(q0), 0, lb);
+        const uint32_t lb = tc::mapa(&full_bar[s], leader);
+        if constexpr (kQuad) {   // mapA7 = 64-row, 1-slice boxes
+          const uint16_t mc = static_cast<uint16_t>(5u << rank);   // {rank, rank + 2}
+          for (int sl = 0; sl < ns; ++sl)
+            tc::tma_load_3d_pair_mc(sa + sl * kP2TileA + pairi * (64 * kO2BK), &mapA7, kb * kO2BK,
+                                    static_cast<int32_t>(q0 + pairi * 64), sl, &full_bar[s], mc);
+        } else {
+          tc::tma_load_3d_pair(sa, p1 ? &mapA4 : &mapA7, kb * kO2BK, static_cast<int32_t>(q0), 0,
+                               lb);
+        }
         tc::tma_load_3d_pair(sb, p1 ? &mapB4 : &mapB7, kb * kO2BK, tb, 0, lb);
       }
     }
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
-      // ---- MMA issuer (leader only): M256 N128 K32
+      // ---- MMA issuer (leader only): M256 N128 K32.  The two passes are
+      // separate loops: a conditional tcgen05.commit inside one loop compiles
+      // to a predicated UTCBAR that stalls the issue every stage even when
+      // its predicate is off (pass 1 ran at 94 instead of 64 clk per MMA).
       constexpr uint32_t idesc = tc::idesc_i8(256, kP2BN, false, false);
-      for (int it = 0; it < 2 * nkb; ++it) {
+      const uint16_t own = static_cast<uint16_t>(3u << leader);
+      constexpr uint16_t ring = kQuad ? 0xF : 3;
+      auto wait_stage = [&](int it) -> uint32_t {
         const int s = it % kP2Stages;
-        const bool p1 = it < nkb;
-        const int kb = p1 ? it : it - nkb;
-        if (it == nkb) {  // pass 2 reuses the accumulators: wait for both drains
-          mbar_wait(&drained_bar, 0);
-          tc::fence_after();
+        uint64_t tw0 = 0;
+        if constexpr ((kDiag & 8) != 0) tw0 = clock64();
+        if constexpr ((kDiag & 16) == 0) mbar_wait(&full_bar[s], (it / kP2Stages) & 1);
+        if constexpr ((kDiag & 8) != 0) {
+          if (blockIdx.x == 0 && blockIdx.y == 0) {
+            double *tl = out + static_cast<int64_t>(gridDim.x) * gridDim.y * 8;
+            tl[2 * it] = static_cast<double>(tw0);
+            tl[2 * it + 1] = static_cast<double>(clock64());
+          }
         }
-        mbar_wait(&full_bar[s], (it / kP2Stages) & 1);
         tc::fence_after();
-        const uint32_t sa = smem_u32(smem + s * kP2StageBytes);
+        return smem_u32(smem + s * kP2StageBytes);
+      };
+      for (int kb = 0; kb < nkb; ++kb) {
+        const uint32_t sa = wait_stage(kb);
         const uint32_t sb = sa + kOzSlices * kP2TileA;
-        if (p1) {
 #pragma unroll
-          for (int i = 1; i <= kO2Pass1Slices; ++i)
+        for (int i = 1; i <= kO2Pass1Slices; ++i)
 #pragma unroll
-            for (int j = 1; j <= kO2Pass1Slices; ++j) {
-              const int l = i + j;
-              if (l > 5) continue;
-              tc::mma_i8_pair(tmem + (l - 2) * kP2BN, tc::sdesc<32>(sa + (i - 1) * kP2TileA),
-                              tc::sdesc<32>(sb + (j - 1) * kP2TileB), idesc,
-                              !(kb == 0 && i == 1));
-            }
-        } else {
-#pragma unroll
-          for (int i = 1; i <= kS; ++i)
-#pragma unroll
-            for (int j = 1; j <= kS; ++j) {
-              const int l = i + j;
-              if (l < 6 || l > kMaxL) continue;
-              const int first_i = l - kS > 1 ? l - kS : 1;
-              tc::mma_i8_pair(tmem + (l - 6) * kP2BN, tc::sdesc<32>(sa + (i - 1) * kP2TileA),
-                              tc::sdesc<32>(sb + (j - 1) * kP2TileB), idesc,
-                              !(kb == 0 && i == first_i));
-            }
-        }
-        tc::commit_pair(&empty_bar[s]);
-        if (it == nkb - 1) tc::commit_pair(&pass_bar[0]);
+          for (int j = 1; j <= kO2Pass1Slices; ++j) {
+            const int l = i + j;
+            if (l > 5) continue;
+            tc::mma_i8_pair(tmem + (l - 2) * kP2BN, tc::sdesc<32>(sa + (i - 1) * kP2TileA),
+                            tc::sdesc<32>(sb + (j - 1) * kP2TileB), idesc, !(kb == 0 && i == 1));
+          }
+        tc::commit_pair_mask(&empty_bar[kb % kP2Stages], ring);
       }
-      tc::commit_pair(&pass_bar[1]);
+      tc::commit_pair_mask(&pass_bar[0], own);
+      // pass 2 reuses the accumulators: wait for both CTAs' drains
+      if (kDiag & 4) stamp[2] = static_cast<double>(gtimer());
+      mbar_wait(&drained_bar, 0);
+      if (kDiag & 4) stamp[3] = static_cast<double>(gtimer());
+      tc::fence_after();
+      for (int kb = 0; kb < nkb; ++kb) {
+        const uint32_t sa = wait_stage(nkb + kb);
+        const uint32_t sb = sa + kOzSlices * kP2TileA;
+#pragma unroll
+        for (int i = 1; i <= kS; ++i)
+#pragma unroll
+          for (int j = 1; j <= kS; ++j) {
+            const int l = i + j;
+            if (l < 6 || l > kMaxL) continue;
+            const int first_i = l - kS > 1 ? l - kS : 1;
+            tc::mma_i8_pair(tmem + (l - 6) * kP2BN, tc::sdesc<32>(sa + (i - 1) * kP2TileA),
+                            tc::sdesc<32>(sb + (j - 1) * kP2TileB), idesc,
+                            !(kb == 0 && i == first_i));
+          }
+        tc::commit_pair_mask(&empty_bar[(nkb + kb) % kP2Stages], ring);
+      }
+      tc::commit_pair_mask(&pass_bar[1], own);
     }
   } else {
     // ---- epilogue warps 2..9 (both CTAs, own TMEM = own 128 rows x 128 targets)
@@ -478,8 +545,9 @@ __global__ void __launch_bounds__(kO2Threads, 1)
     }
     tc::fence_before();
     __syncwarp();
-    if (lane == 0) tc::mbar_arrive_cluster(tc::mapa(&drained_bar, 0));
+    if (lane == 0) tc::mbar_arrive_cluster(tc::mapa(&drained_bar, leader));
     mbar_wait(&pass_bar[1], 0);
+    if ((kDiag & 4) && tid == 64) stamp[4] = static_cast<double>(gtimer());
     tc::fence_after();
     const double h = row_ok ? H[q] : 0.0;
     const int e_q = row_ok ? ea[q] : 0;
@@ -491,7 +559,7 @@ __global__ void __launch_bounds__(kO2Threads, 1)
 #pragma unroll
       for (int l = 0; l < kL2; ++l) tc::tmem_ld8(base + l * kP2BN + c0, acc[l]);
       tc::tmem_ld_wait();
-      if (!row_ok) continue;
+      if (!row_ok || (kDiag & 2) != 0) continue;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int64_t t = t0 + half * 64 + c0 + u;
@@ -500,7 +568,7 @@ __global__ void __launch_bounds__(kO2Threads, 1)
 #pragma unroll
         for (int l = kL2 - 2; l >= 0; --l) v = fma(v, 0x1p-8, static_cast<double>(acc[l][u]));
         v = fma(v, 0x1p-32, v1[c0 + u]);
-        const double S = ldexp(v, e_q + eb[t] - 16);
+        const double S = pow2_scale(v, e_q + eb[t] - 16);
         double val = h + S;
         const bool is_t = (tq == targets[t]);
         if (!is_t && fabs(val) < tau * (fabs(h) + fabs(S)))
@@ -508,6 +576,231 @@ __global__ void __launch_bounds__(kO2Threads, 1)
         else
           val = is_t ? 0.0 : settle(val);
         out[q * ldo + t] = val;
+      }
+    }
+  }
+  if ((kDiag & 4) && tid == 64) stamp[5] = static_cast<double>(gtimer());
+  tc::fence_before();
+  tc::cluster_sync();   // both CTAs done with TMEM and with each other's barriers
+  if ((kDiag & 4) && tid == 0) {
+    stamp[6] = static_cast<double>(gtimer());
+    stamp[7] = static_cast<double>(smid());
+  }
+  if (warp == 0) tc::tmem_free_pair<512>(tmem);
+}
+
+// ------------------------------------------------ GEMM, persistent CTA pair --
+// The CTA-pair kernel made persistent (one cluster per SM pair, tiles
+// strided over the clusters; consecutive clusters share a row pair so its A
+// planes are read from HBM once and from L2 after) with the epilogue taken
+// off the tensor pipe's critical path: the epilogue warps fold the pass-2
+// accumulators into the FP64 pass-1 partials in registers, release TMEM to
+// the MMA thread (free_bar), and only then apply the scale / guard / settle
+// and store -- while the next tile's pass-1 MMAs run.  Same integers, same
+// FP64 operation order: bitwise the 1-CTA kernel's outputs.
+template <int kS, int kMaxL, int kDiag = 0>
+__global__ void __launch_bounds__(kO2Threads, 1)
+    batched_kl_i8_pp_kernel(const __grid_constant__ CUtensorMap mapA7,
+                            const __grid_constant__ CUtensorMap mapA4,
+                            const __grid_constant__ CUtensorMap mapB7,
+                            const __grid_constant__ CUtensorMap mapB4,
+                            const int32_t *__restrict__ ea, const int32_t *__restrict__ eb,
+                            int64_t rows, int64_t T, int nkb, const double *__restrict__ H,
+                            const int64_t *__restrict__ targets, double tau, int64_t row0,
+                            double *__restrict__ out, int64_t ldo, int t_tiles, int ntiles) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  __shared__ __align__(8) uint64_t full_bar[kP2Stages], empty_bar[kP2Stages];
+  __shared__ __align__(8) uint64_t pass_bar[2], drained_bar, free_bar;
+  __shared__ uint32_t tmem_base;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = tc::cluster_rank();   // 0 = leader (issues the MMAs)
+  const int cid = static_cast<int>(blockIdx.x >> 1), ncl = static_cast<int>(gridDim.x >> 1);
+
+  if (tid == 0) {
+    tc::prefetch_map(&mapA7);
+    tc::prefetch_map(&mapA4);
+    tc::prefetch_map(&mapB7);
+    tc::prefetch_map(&mapB4);
+    for (int s = 0; s < kP2Stages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(&pass_bar[0], 1);
+    mbar_init(&pass_bar[1], 1);
+    mbar_init(&drained_bar, 16);     // every epilogue warp of both CTAs, per tile
+    mbar_init(&free_bar, 16);
+  }
+  if (warp == 0) tc::tmem_alloc_pair<512>(&tmem_base);
+  tc::fence_before();
+  tc::cluster_sync();
+  tc::fence_after();
+  const uint32_t tmem = tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---- TMA producer (both CTAs): own 128 A rows, own half of the targets
+      int it = 0;
+      for (int w = cid; w < ntiles; w += ncl) {
+        const int64_t q0 = (static_cast<int64_t>(w / t_tiles) * 2 + rank) * 128;
+        const int32_t tb = (w % t_tiles) * kP2BN + static_cast<int32_t>(rank) * kP2HalfN;
+        for (int pass = 0; pass < 2; ++pass) {
+          const int ns = pass == 0 ? kO2Pass1Slices : kS;
+          const CUtensorMap *ma = pass == 0 ? &mapA4 : &mapA7;
+          const CUtensorMap *mb = pass == 0 ? &mapB4 : &mapB7;
+          for (int kb = 0; kb < nkb; ++kb, ++it) {
+            const int s = it % kP2Stages;
+            mbar_wait(&empty_bar[s], ((it / kP2Stages) & 1) ^ 1);
+            if constexpr ((kDiag & 1) != 0) {
+              if (rank == 0) mbar_arrive(&full_bar[s]);
+              continue;
+            }
+            uint8_t *sa = smem + s * kP2StageBytes;
+            uint8_t *sb = sa + kOzSlices * kP2TileA;
+            if (rank == 0) mbar_expect_tx(&full_bar[s], 2 * ns * (kP2TileA + kP2TileB));
+            const uint32_t lb = tc::mapa(&full_bar[s], 0);
+            tc::tma_load_3d_pair(sa, ma, kb * kO2BK, static_cast<int32_t>(q0), 0, lb);
+            tc::tma_load_3d_pair(sb, mb, kb * kO2BK, tb, 0, lb);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // ---- MMA issuer (leader only): M256 N128 K32; each pass its own loop
+      // (a conditional commit inside a shared loop costs a stall per stage)
+      constexpr uint32_t idesc = tc::idesc_i8(256, kP2BN, false, false);
+      int it = 0, k = 0;
+      for (int w = cid; w < ntiles; w += ncl, ++k) {
+        if (k > 0) {   // the previous tile's pass-2 accumulators drained
+          mbar_wait(&free_bar, (k - 1) & 1);
+          tc::fence_after();
+        }
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % kP2Stages;
+          mbar_wait(&full_bar[s], (it / kP2Stages) & 1);
+          tc::fence_after();
+          const uint32_t sa = smem_u32(smem + s * kP2StageBytes);
+          const uint32_t sb = sa + kOzSlices * kP2TileA;
+#pragma unroll
+          for (int i = 1; i <= kO2Pass1Slices; ++i)
+#pragma unroll
+            for (int j = 1; j <= kO2Pass1Slices; ++j) {
+              const int l = i + j;
+              if (l > 5) continue;
+              tc::mma_i8_pair(tmem + (l - 2) * kP2BN, tc::sdesc<32>(sa + (i - 1) * kP2TileA),
+                              tc::sdesc<32>(sb + (j - 1) * kP2TileB), idesc,
+                              !(kb == 0 && i == 1));
+            }
+          tc::commit_pair(&empty_bar[s]);
+        }
+        tc::commit_pair(&pass_bar[0]);
+        mbar_wait(&drained_bar, k & 1);   // pass 2 reuses the accumulators
+        tc::fence_after();
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % kP2Stages;
+          mbar_wait(&full_bar[s], (it / kP2Stages) & 1);
+          tc::fence_after();
+          const uint32_t sa = smem_u32(smem + s * kP2StageBytes);
+          const uint32_t sb = sa + kOzSlices * kP2TileA;
+#pragma unroll
+          for (int i = 1; i <= kS; ++i)
+#pragma unroll
+            for (int j = 1; j <= kS; ++j) {
+              const int l = i + j;
+              if (l < 6 || l > kMaxL) continue;
+              const int first_i = l - kS > 1 ? l - kS : 1;
+              tc::mma_i8_pair(tmem + (l - 6) * kP2BN, tc::sdesc<32>(sa + (i - 1) * kP2TileA),
+                              tc::sdesc<32>(sb + (j - 1) * kP2TileB), idesc,
+                              !(kb == 0 && i == first_i));
+            }
+          tc::commit_pair(&empty_bar[s]);
+        }
+        tc::commit_pair(&pass_bar[1]);
+      }
+    }
+  } else {
+    // ---- epilogue warps 2..9 (both CTAs, own TMEM = own 128 rows x 128 targets)
+    const int quarter = warp & 3, half = (warp - 2) >> 2;
+    const int r = quarter * 32 + lane;
+    const uint32_t base = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + half * 64;
+    const uint32_t drained_leader = tc::mapa(&drained_bar, 0);
+    const uint32_t free_leader = tc::mapa(&free_bar, 0);
+    constexpr int kL2 = kMaxL - 5;
+    const bool pairs_ok = (ldo % 2 == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+    int k = 0;
+    for (int w = cid; w < ntiles; w += ncl, ++k) {
+      const int64_t q = (static_cast<int64_t>(w / t_tiles) * 2 + rank) * 128 + r;
+      const int64_t tc0 = static_cast<int64_t>(w % t_tiles) * kP2BN + half * 64;
+      double v[64];
+      mbar_wait(&pass_bar[0], k & 1);
+      tc::fence_after();
+#pragma unroll
+      for (int c0 = 0; c0 < 64; c0 += 8) {
+        uint32_t acc[4][8];
+#pragma unroll
+        for (int l = 0; l < 4; ++l) tc::tmem_ld8(base + l * kP2BN + c0, acc[l]);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          double x = static_cast<double>(acc[3][u]);
+#pragma unroll
+          for (int l = 2; l >= 0; --l) x = fma(x, 0x1p-8, static_cast<double>(acc[l][u]));
+          v[c0 + u] = x;
+        }
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive_cluster(drained_leader);
+      mbar_wait(&pass_bar[1], k & 1);
+      tc::fence_after();
+#pragma unroll
+      for (int c0 = 0; c0 < 64; c0 += 8) {
+        uint32_t acc[kL2][8];
+#pragma unroll
+        for (int l = 0; l < kL2; ++l) tc::tmem_ld8(base + l * kP2BN + c0, acc[l]);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          double x = static_cast<double>(acc[kL2 - 1][u]);
+#pragma unroll
+          for (int l = kL2 - 2; l >= 0; --l) x = fma(x, 0x1p-8, static_cast<double>(acc[l][u]));
+          v[c0 + u] = fma(x, 0x1p-32, v[c0 + u]);
+        }
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive_cluster(free_leader);   // TMEM free for the next tile
+      if ((kDiag & 2) != 0 || q >= rows) continue;
+      const double h = H[q];
+      const int e_q = ea[q] - 16;
+      const int64_t tq = row0 + q;
+      double *orow = out + q * ldo + tc0;
+      const bool full = pairs_ok && tc0 + 64 <= T;
+#pragma unroll
+      for (int c = 0; c < 64; c += 2) {
+        double o[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int64_t t = tc0 + c + u;
+          const bool in = t < T;
+          const double S = pow2_scale(v[c + u], e_q + (in ? eb[t] : 0));
+          double val = h + S;
+          const bool is_t = in && (tq == targets[t]);
+          if (!is_t && fabs(val) < tau * (fabs(h) + fabs(S)))
+            val = __longlong_as_double(static_cast<long long>(kOzGuard));
+          else
+            val = is_t ? 0.0 : settle(val);
+          o[u] = val;
+        }
+        if (full) {
+          *reinterpret_cast<double2 *>(orow + c) = make_double2(o[0], o[1]);
+        } else {
+          if (tc0 + c < T) orow[c] = o[0];
+          if (tc0 + c + 1 < T) orow[c + 1] = o[1];
+        }
       }
     }
   }
@@ -519,15 +812,21 @@ __global__ void __launch_bounds__(kO2Threads, 1)
 // Diagnostic: the int8 tensor pipe's issue-rate ceiling, back-to-back
 // M128 N256 K32 u8 MMAs on shared-memory-resident operands, one CTA per SM;
 // bench.py reports K7's int8 rate against it.
-__global__ void __launch_bounds__(128, 1) umma_i8_probe_kernel(int iters, uint32_t *sink) {
+__global__ void __launch_bounds__(128, 1) umma_i8_probe_kernel(int iters, int random,
+                                                              uint32_t *sink) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   __shared__ __align__(8) uint64_t bar;
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5;
-  for (int i = tid; i < (128 + 256) * 64 / 4; i += 128)
-    reinterpret_cast<uint32_t *>(smem)[i] = 0x01010101u * (i & 3);
+  for (int i = tid; i < (128 + 256) * 64 / 4; i += 128) {
+    uint32_t h = static_cast<uint32_t>(i + 4099 * blockIdx.x) * 2654435761u;   // random bytes
+    h ^= h >> 15;
+    h *= 2246822519u;
+    h ^= h >> 13;
+    reinterpret_cast<uint32_t *>(smem)[i] = random ? h : 0x01010101u * (i & 3);
+  }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (tid == 0) mbar_init(&bar, 1);
   if (warp == 0) tc::tmem_alloc<256>(&tmem_base);
@@ -595,34 +894,66 @@ static int slice_map(CUtensorMap *map, const uint8_t *base, int64_t outer, int64
 template <int kS, int kMaxL>
 static int launch_i8(const CUtensorMap (&m)[4], const int32_t *ea, const int32_t *eb,
                      int64_t rows, int64_t T, int64_t k, const double *H, const int64_t *targets,
-                     double tau, int64_t row0, double *out, int64_t ldo, bool pair,
+                     double tau, int64_t row0, double *out, int64_t ldo, int pair,
                      cudaStream_t stream) {
   const int nkb = static_cast<int>((k + kO2BK - 1) / kO2BK);
   const unsigned tiles = static_cast<unsigned>((rows + 127) / 128);
   if (pair) {  // a pair's second CTA may hold only out-of-range rows
-    auto kern = batched_kl_i8_pair_kernel<kS, kMaxL>;
-    if (int e = ensure_smem((const void *)kern, kP2Smem)) return e;
+    // 1: persistent pair (the product path), 2: two pairs sharing A by TMA
+    // multicast, 3: one tile per pair (kept for A/B measurements)
+    const bool quad = pair == 2, persistent = pair == 1;
+    static const int diag = [] {
+      const char *e = getenv("PF_K7_DIAG");
+      return e ? atoi(e) : 0;
+    }();
+    using Kern = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, const int32_t *,
+                          const int32_t *, int64_t, int64_t, int, const double *, const int64_t *,
+                          double, int64_t, double *, int64_t);
+    using KernP = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, const int32_t *,
+                           const int32_t *, int64_t, int64_t, int, const double *,
+                           const int64_t *, double, int64_t, double *, int64_t, int, int);
+    Kern kern = quad ? batched_kl_i8_pair_kernel<kS, kMaxL, true>
+                     : batched_kl_i8_pair_kernel<kS, kMaxL, false>;
+    KernP kernp = diag == 1   ? batched_kl_i8_pp_kernel<kS, kMaxL, 1>
+                  : diag == 2 ? batched_kl_i8_pp_kernel<kS, kMaxL, 2>
+                  : diag == 3 ? batched_kl_i8_pp_kernel<kS, kMaxL, 3>
+                              : batched_kl_i8_pp_kernel<kS, kMaxL, 0>;
+    const void *kfn = persistent ? (const void *)kernp : (const void *)kern;
+    if (int e = ensure_smem(kfn, kP2Smem)) return e;
+    const unsigned ttiles = static_cast<unsigned>((T + kP2BN - 1) / kP2BN);
+    const unsigned row_pairs = (tiles + 1) / 2;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2 * static_cast<unsigned>((T + kP2BN - 1) / kP2BN), (tiles + 1) / 2, 1);
+    cfg.gridDim = dim3(quad ? 4 * ((ttiles + 1) / 2) : 2 * ttiles, row_pairs, 1);
     cfg.blockDim = dim3(kO2Threads, 1, 1);
     cfg.dynamicSmemBytes = kP2Smem;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.x = quad ? 4 : 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int clusters = 0;
-    const cudaError_t oe = cudaOccupancyMaxActiveClusters(&clusters, (const void *)kern, &cfg);
+    const cudaError_t oe = cudaOccupancyMaxActiveClusters(&clusters, kfn, &cfg);
     if (oe != cudaSuccess || clusters == 0) {
       cudaGetLastError();
       return fail(PF_E_LAUNCH, "batched_kl_i8_pair: no CTA pair fits an SM pair (%s, %d)",
                   cudaGetErrorString(oe), clusters);
     }
-    const cudaError_t le = cudaLaunchKernelEx(&cfg, kern, m[0], m[1], m[2], m[3], ea, eb, rows, T,
-                                              nkb, H, targets, tau, row0, out, ldo);
+    cudaError_t le;
+    if (persistent) {
+      const long long ntiles = static_cast<long long>(row_pairs) * ttiles;
+      if (ntiles > INT32_MAX) return fail(PF_E_DOMAIN, "batched_kl_i8_pair: too many tiles");
+      const unsigned ncl = static_cast<unsigned>(ntiles < clusters ? ntiles : clusters);
+      cfg.gridDim = dim3(2 * ncl, 1, 1);
+      le = cudaLaunchKernelEx(&cfg, kernp, m[0], m[1], m[2], m[3], ea, eb, rows, T, nkb, H,
+                              targets, tau, row0, out, ldo, static_cast<int>(ttiles),
+                              static_cast<int>(ntiles));
+    } else {
+      le = cudaLaunchKernelEx(&cfg, kern, m[0], m[1], m[2], m[3], ea, eb, rows, T, nkb, H, targets,
+                              tau, row0, out, ldo);
+    }
     if (le != cudaSuccess)
       return fail(static_cast<int>(le), "batched_kl_i8_pair: %s", cudaGetErrorString(le));
     return check_launch("batched_kl_i8_pair");
@@ -675,10 +1006,16 @@ int pf_batched_kl_i8(const uint8_t *A, const int32_t *ea, int64_t rows, const ui
     return fail(PF_E_ALIGN, "batched_kl_i8: slice planes must be 16-byte aligned");
   const int64_t row_tiles = (rows + 127) / 128;
   if (row_tiles > 65535) return fail(PF_E_DOMAIN, "batched_kl_i8: too many rows per launch");
-  const bool pair = cta_pair != 0;
+  if (cta_pair < 0 || cta_pair > 3)
+    return fail(PF_E_ARG, "batched_kl_i8: cta_pair must be 0 .. 3");
+  const int pair = cta_pair;
   const uint32_t bn = pair ? kP2HalfN : kO2BN;   // each CTA of a pair loads half the targets
   CUtensorMap m[4];
-  if (int e = slice_map(&m[0], A, rows, ldk, 128, kO2BK, kS)) return e;
+  if (pair == 2) {   // multicast halves: 64-row boxes, one slice each
+    if (int e = slice_map(&m[0], A, rows, ldk, 64, kO2BK, 1)) return e;
+  } else if (int e = slice_map(&m[0], A, rows, ldk, 128, kO2BK, kS)) {
+    return e;
+  }
   if (int e = slice_map(&m[1], A, rows, ldk, 128, kO2BK, kO2Pass1Slices)) return e;
   if (int e = slice_map(&m[2], B, T, ldk, bn, kO2BK, kS)) return e;
   if (int e = slice_map(&m[3], B, T, ldk, bn, kO2BK, kO2Pass1Slices)) return e;
@@ -688,11 +1025,13 @@ int pf_batched_kl_i8(const uint8_t *A, const int32_t *ea, int64_t rows, const ui
                                        pair, as_stream(stream));
 }
 
-int pf_probe_umma_i8(int64_t iters, int64_t *ops_host, uint32_t *sink, pf_stream_t stream) {
+int pf_probe_umma_i8(int64_t iters, int random_operands, int64_t *ops_host, uint32_t *sink,
+                     pf_stream_t stream) {
   const int smem = (128 + 256) * 64 + 1024;
   if (int e = ensure_smem((const void *)umma_i8_probe_kernel, smem)) return e;
   const int blocks = sm_count();
-  umma_i8_probe_kernel<<<blocks, 128, smem, as_stream(stream)>>>(static_cast<int>(iters), sink);
+  umma_i8_probe_kernel<<<blocks, 128, smem, as_stream(stream)>>>(static_cast<int>(iters),
+                                                                  random_operands, sink);
   if (ops_host) *ops_host = 2LL * 128 * 256 * 64 * iters * blocks;
   return check_launch("probe_umma_i8");
 }

@@ -41,15 +41,18 @@ def run(c, pair, grade=64):
 
 ONCE = "--once" in sys.argv
 SCAN = "--scan" in sys.argv
+PAIRS = (1, 2, 3) if "--quad" in sys.argv else (1, 3)
 res = {}
 for rows, k, T in [] if (ONCE or SCAN) else [(300, 200, 50), (1000, 300, 130), (129, 64, 64), (2047, 1234, 256), (5000, 4102, 1024)]:
     c = setup(rows, k, T)
     for grade in (64, 32):
         a = run(c, 0, grade).cpu().numpy()
-        b = run(c, 1, grade).cpu().numpy()
-        same = (a.view(np.int64) == b.view(np.int64))
-        res[f"{rows}x{k}xT{T} g{grade}"] = {"bitwise": bool(same.all()), "mismatch": int((~same).sum()),
-                                          "untouched": int((b == -7.0).sum())}
+        for pair in PAIRS:
+            b = run(c, pair, grade).cpu().numpy()
+            same = (a.view(np.int64) == b.view(np.int64))
+            res[f"{rows}x{k}xT{T} g{grade} pair{pair}"] = {
+                "bitwise": bool(same.all()), "mismatch": int((~same).sum()),
+                "untouched": int((b == -7.0).sum())}
     del c
 print(json.dumps(res, indent=1), flush=True)
 if not all(v["bitwise"] and v["untouched"] == 0 for v in res.values()):
@@ -58,7 +61,7 @@ if SCAN:   # time per unit of work against T (A reuse across target tiles)
     out = {}
     for T in (128, 256, 512, 1024):
         c = setup(131072, 4102, T, seed=5)
-        for pair in (0, 1):
+        for pair in (0,) + PAIRS:
             run(c, pair)
             e0, e1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
             o = t.empty((c["rows"], c["T"]), dtype=t.float64, device="cuda:0")
@@ -84,7 +87,7 @@ if ONCE:   # one launch of each kernel for ncu
 # timing at a C5-like slab
 c = setup(262144, 4102, 1024, seed=3)
 tm = {}
-for pair in (0, 1):
+for pair in (0,) + PAIRS:
     run(c, pair)
     e0, e1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
     ms = []

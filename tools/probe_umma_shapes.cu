@@ -1,0 +1,339 @@
+// Standalone probe (not part of the product): where does K7's int8 MMA rate
+// go?  Back-to-back tcgen05.mma kind::i8 over shared-memory-resident slice
+// planes laid out exactly as K7 stages them (SWIZZLE_32B K-major, 7 A and 7 B
+// planes, levels 2..9 rotating over the TMEM accumulators), 1-CTA or CTA
+// pair, N = 128 or 256, optionally with a concurrent bulk-copy stream into a
+// scratch ring at K7's bytes-per-MMA ratio (the TMA writes that share the
+// SM's shared-memory bandwidth with the UMMA operand reads).
+// nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -I include \
+//      tools/probe_umma_shapes.cu -o tools/probe_umma_shapes.bin -lcuda
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "../paper_1708_02845_b200/csrc/pf_tc.cuh"
+
+using namespace pf;
+
+#define CK(x)                                                                       \
+  do {                                                                              \
+    cudaError_t e_ = (x);                                                           \
+    if (e_ != cudaSuccess) {                                                        \
+      printf("CUDA %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, __LINE__);     \
+      exit(1);                                                                      \
+    }                                                                               \
+  } while (0)
+
+constexpr int kSlices = 7, kRing = 4, kChunk = 16384;
+
+__device__ __forceinline__ bool mbar_try(uint64_t *bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+
+// kPair: cta_group::2 (M256, B split 50/50); kN: MMA N; kSW: swizzle bytes =
+// K bytes per slice row (32: K7's layout; 128: 4 K-steps per slice pair)
+template <bool kPair, int kN, int kSW>
+__global__ void __launch_bounds__(384, 1)
+    shape_kernel(int iters, int tma_bytes_per_iter, const uint8_t *gsrc, int64_t gsrc_bytes,
+                 uint32_t *sink, unsigned long long *cycles, int mode, int fill, int spin, int stride, int off) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  constexpr int kNloc = kPair ? kN / 2 : kN;
+  constexpr int kS = kSW == 32 ? kSlices : 3;          // SW128 planes are 4x larger
+  constexpr int kTileA = 128 * kSW, kTileB = kNloc * kSW;
+  constexpr int kAcc = 512 / kN;                        // accumulators that fit TMEM
+  uint8_t *sa = smem, *sb = smem + kS * kTileA, *scratch = sb + kS * kTileB;
+  __shared__ __align__(8) uint64_t done_bar, ring_bar[kRing], junk_bar, spin_bar;
+  __shared__ __align__(8) uint64_t full_bar[5], empty_bar[5];
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const uint32_t rank = kPair ? tc::cluster_rank() : 0;
+  const int init_bytes = mode >= 5 ? 5 * 43008 + 4096 : kS * (kTileA + kTileB);
+  for (int i = tid; i < init_bytes / 4; i += 128) {
+    uint32_t h = static_cast<uint32_t>(i) * 2654435761u + rank * 97u;
+    h ^= h >> 15;
+    h *= 2246822519u;
+    h ^= h >> 13;
+    reinterpret_cast<uint32_t *>(smem)[i] = fill ? h : 0x01010101u * ((i * 7 + rank) & 3);
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (tid == 0) {
+    mbar_init(&done_bar, 1);
+    mbar_init(&junk_bar, 1 << 20);
+    mbar_init(&spin_bar, 1);
+    for (int q = 0; q < 5; ++q) {
+      mbar_init(&full_bar[q], 1);
+      mbar_init(&empty_bar[q], 1);
+    }
+    for (int s = 0; s < kRing; ++s) mbar_init(&ring_bar[s], 1);
+  }
+  if (warp == 0) {
+    if constexpr (kPair) tc::tmem_alloc_pair<512>(&tmem_base);
+    else tc::tmem_alloc<512>(&tmem_base);
+  }
+  tc::fence_before();
+  if constexpr (kPair) tc::cluster_sync();
+  else __syncthreads();
+  tc::fence_after();
+  const uint32_t tm = tmem_base;
+  const unsigned long long c0 = clock64();
+  if (warp == 0 && tid == 0 && rank == 0) {
+    constexpr uint32_t id = tc::idesc_i8(kPair ? 256 : 128, kN, false, false);
+    const uint32_t a0 = smem_u32(sa), b0 = smem_u32(sb);
+    if (mode >= 5 && mode != 6 && kSW == 32 && kN == 128) {   // pass 1 over a rotating 5-stage ring
+      for (int it = 0; it < iters * 34 / 10; ++it) {
+        if (mode == 7) mbar_wait(&full_bar[it % 5], (it / 5) & 1);
+        const uint32_t sa = a0 + off + (it % 5) * stride, sbb = sa + 7 * kTileA;
+#pragma unroll
+        for (int i = 1; i <= 4; ++i)
+#pragma unroll
+          for (int j = 1; j <= 4; ++j) {
+            if (i + j > 5) continue;
+            const uint32_t d = tm + (i + j - 2) * kN;
+            const uint64_t da = tc::sdesc<kSW>(sa + (i - 1) * kTileA);
+            const uint64_t db = tc::sdesc<kSW>(sbb + (j - 1) * kTileB);
+            if constexpr (kPair) tc::mma_i8_pair(d, da, db, id, true);
+            else tc::mma_i8(d, da, db, id, true);
+          }
+        if (mode >= 7) {
+          if constexpr (kPair) tc::commit_pair(&empty_bar[it % 5]);
+          else tc::commit(&empty_bar[it % 5]);
+        } else {
+          if constexpr (kPair) tc::commit_pair(&junk_bar);
+          else tc::commit(&junk_bar);
+        }
+      }
+    } else if (mode == 6 && kSW == 32 && kN == 128) {   // pass 2 over the ring
+      for (int it = 0; it < iters * 34 / 24; ++it) {
+        const uint32_t sa = a0 + (it % 5) * 43008, sbb = sa + 7 * kTileA;
+#pragma unroll
+        for (int i = 1; i <= 7; ++i)
+#pragma unroll
+          for (int j = 1; j <= 7; ++j) {
+            if (i + j < 6 || i + j > 9) continue;
+            const uint32_t d = tm + (i + j - 6) * kN;
+            const uint64_t da = tc::sdesc<kSW>(sa + (i - 1) * kTileA);
+            const uint64_t db = tc::sdesc<kSW>(sbb + (j - 1) * kTileB);
+            if constexpr (kPair) tc::mma_i8_pair(d, da, db, id, true);
+            else tc::mma_i8(d, da, db, id, true);
+          }
+        if constexpr (kPair) tc::commit_pair(&junk_bar);
+        else tc::commit(&junk_bar);
+      }
+    } else if (mode >= 1 && kSW == 32) {
+      // mode 1: every MMA into one accumulator (a dependent chain);
+      // mode 2: K7 pass 1 (levels 2..5 of slices 1..4, acc l - 2), i-major,
+      //         in bursts of 10 (34 per "iteration" for the op count);
+      // mode 3: mode 2 + a tcgen05.commit after every 10 MMAs;
+      // mode 4: K7 pass 1 reordered: L5 L4 L5 L3 L5 L4 L2 L5 L3 L4, + commits
+      constexpr int ord[10][2] = {{1, 4}, {1, 3}, {2, 3}, {1, 2}, {3, 2},
+                                  {2, 2}, {1, 1}, {4, 1}, {2, 1}, {3, 1}};
+      constexpr int nat[10][2] = {{1, 1}, {1, 2}, {1, 3}, {1, 4}, {2, 1},
+                                  {2, 2}, {2, 3}, {3, 1}, {3, 2}, {4, 1}};
+      int cnt = 0;
+      for (int it = 0; it < iters * 34 / 10; ++it) {
+#pragma unroll
+        for (int q = 0; q < 10; ++q) {
+          const int i = mode == 4 ? ord[q][0] : nat[q][0];
+          const int j = mode == 4 ? ord[q][1] : nat[q][1];
+          const uint32_t d = mode == 1 ? tm : tm + (i + j - 2) * kN;
+          const uint64_t da = tc::sdesc<kSW>(a0 + (i - 1) * kTileA);
+          const uint64_t db = tc::sdesc<kSW>(b0 + (j - 1) * kTileB);
+          if constexpr (kPair) tc::mma_i8_pair(d, da, db, id, true);
+          else tc::mma_i8(d, da, db, id, true);
+          ++cnt;
+        }
+        if (mode >= 3) {
+          if constexpr (kPair) tc::commit_pair(&junk_bar);
+          else tc::commit(&junk_bar);
+        }
+      }
+      if (cnt == -1) sink[1] = 0;
+    } else
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int i = 1; i <= kS; ++i)
+#pragma unroll
+        for (int j = 1; j <= kS; ++j) {
+          const int l = i + j;
+          if (kSW == 32 && l > 9) continue;
+#pragma unroll
+          for (int ks = 0; ks < kSW / 32; ++ks) {
+            const uint32_t d = tm + (l % kAcc) * kN;
+            const uint64_t da = tc::sdesc<kSW>(a0 + (i - 1) * kTileA + ks * 32);
+            const uint64_t db = tc::sdesc<kSW>(b0 + (j - 1) * kTileB + ks * 32);
+            if constexpr (kPair) tc::mma_i8_pair(d, da, db, id, true);
+            else tc::mma_i8(d, da, db, id, true);
+          }
+        }
+    }
+    if constexpr (kPair) tc::commit_pair(&done_bar);
+    else tc::commit(&done_bar);
+  } else if (warp == 1 && tid == 32 && mode >= 7) {
+    // K7's ring handshake without loads: wait the slot's MMA commit, arrive
+    for (int it = 0; it < iters * 34 / 10; ++it) {
+      const int q = it % 5;
+      mbar_wait(&empty_bar[q], ((it / 5) & 1) ^ 1);
+      if (rank == 0) mbar_arrive(&full_bar[q]);
+    }
+  } else if (warp == 1 && tid == 32 && tma_bytes_per_iter > 0) {
+    // bulk-copy stream into the scratch ring, kRing chunks in flight
+    const int64_t total = static_cast<int64_t>(iters) * tma_bytes_per_iter;
+    const int64_t nchunks = total / kChunk;
+    const int64_t span = gsrc_bytes / kChunk;
+    const int64_t base = (blockIdx.x * 977) % span;
+    for (int64_t c = 0; c < nchunks; ++c) {
+      const int s = static_cast<int>(c % kRing);
+      if (c >= kRing) mbar_wait(&ring_bar[s], ((c / kRing) - 1) & 1);
+      mbar_expect_tx(&ring_bar[s], kChunk);
+      bulk_g2s(scratch + s * kChunk, gsrc + ((base + c) % span) * kChunk, kChunk, &ring_bar[s]);
+    }
+    for (int64_t c = nchunks > kRing ? nchunks - kRing : 0; c < nchunks; ++c)
+      mbar_wait(&ring_bar[c % kRing], (c / kRing) & 1);
+    cycles[2 * blockIdx.x + 1] = clock64() - c0;
+  }
+  if (warp >= 4) {   // idle warps polling an mbarrier (spin 1) or backing off (spin 2)
+    if (spin == 1) {
+      mbar_wait(&spin_bar, 0);
+    } else {
+      while (!mbar_try(&spin_bar, 0)) __nanosleep(256);
+    }
+  }
+  if (warp == 0) {
+    __syncwarp();
+    mbar_wait(&done_bar, 0);
+    tc::fence_after();
+    if (tid == 0) cycles[2 * blockIdx.x] = clock64() - c0;
+    if (tid == 0) mbar_arrive(&spin_bar);
+    uint32_t v[8];
+    tc::tmem_ld8(tm, v);
+    tc::tmem_ld_wait();
+    if (v[0] == 0x12345u) sink[0] = v[1];
+  }
+  tc::fence_before();
+  if constexpr (kPair) tc::cluster_sync();
+  else __syncthreads();
+  if (warp == 0) {
+    if constexpr (kPair) tc::tmem_free_pair<512>(tm);
+    else tc::tmem_free<512>(tm);
+  }
+}
+
+template <bool kPair, int kN, int kSW>
+void run(const char *name, int tma_per_iter, const uint8_t *gsrc, int64_t gbytes, uint32_t *sink,
+         unsigned long long *cyc, int mode = 0, int fill = 0, int spin = 0, int stride = 43008,
+         int off = 0) {
+  constexpr int kNloc = kPair ? kN / 2 : kN;
+  constexpr int kS = kSW == 32 ? kSlices : 3;
+  int smem = kS * (128 * kSW + kNloc * kSW) + kRing * kChunk + 1024;
+  if (mode >= 5) smem = 5 * 43008 + 1024 + 4096;
+  auto kern = shape_kernel<kPair, kN, kSW>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  int mmas = 0;
+  for (int i = 1; i <= kS; ++i)
+    for (int j = 1; j <= kS; ++j)
+      if (!(kSW == 32 && i + j > 9)) mmas += kSW / 32;
+  if (mode) mmas = 34;
+  const int iters = kSW == 32 ? 3000 : 3000 * 34 / mmas;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(148, 1, 1);
+  cfg.blockDim = dim3(spin ? 384 : 128, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kPair ? 2 : 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  float best = 1e30f;
+  for (int rep = 0; rep < 4; ++rep) {
+    CK(cudaEventRecord(e0));
+    CK(cudaLaunchKernelEx(&cfg, kern, iters, tma_per_iter, gsrc, gbytes, sink, cyc, mode, fill, spin, stride, off));
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    float ms;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    if (rep && ms < best) best = ms;
+  }
+  std::vector<unsigned long long> h(2 * 148);
+  CK(cudaMemcpy(h.data(), cyc, h.size() * 8, cudaMemcpyDeviceToHost));
+  double mma_c = 0, tma_c = 0;
+  for (int b = 0; b < 148; ++b) {
+    if (!kPair || b % 2 == 0) mma_c = mma_c > h[2 * b] ? mma_c : h[2 * b];
+    tma_c = tma_c > h[2 * b + 1] ? tma_c : h[2 * b + 1];
+  }
+  const double ctas_mma = kPair ? 74.0 : 148.0;
+  const double ops = 2.0 * (kPair ? 256 : 128) * kN * 32 * double(mmas) * iters * ctas_mma;
+  const double per_sm_mma_clk = mma_c / (double(mmas) * iters);
+  printf("{\"variant\": \"%s\", \"tma_bytes_per_34mma\": %d, \"ms\": %.4f, \"int8_tops\": %.1f, "
+         "\"clk_per_mma\": %.2f, \"ideal_clk_per_mma\": %d, \"tma_B_per_clk_per_sm\": %.2f}\n",
+         name, tma_per_iter * 34 / mmas, best, ops / (best * 1e-3) / 1e12, per_sm_mma_clk,
+         (kPair ? 256 : 128) * kN * 32 / (kPair ? 2 : 1) / 8192,
+         tma_c > 0 ? double(tma_per_iter) * iters / tma_c : 0.0);
+}
+
+int main() {
+  uint8_t *gsrc;
+  const int64_t gbytes = 64ll << 20;
+  CK(cudaMalloc(&gsrc, gbytes));
+  CK(cudaMemset(gsrc, 1, gbytes));
+  uint32_t *sink;
+  unsigned long long *cyc;
+  CK(cudaMalloc(&sink, 64));
+  CK(cudaMalloc(&cyc, 2 * 148 * 8));
+  CK(cudaMemset(cyc, 0, 2 * 148 * 8));
+  // K7 per CTA per 34 MMAs: 1-CTA 11 slices x 8 KB = 88 KB, pair 11 x 6 KB = 66 KB
+  for (int off = 0; off < 4096; off += 1024)
+    for (int stride = 43008; stride <= 45056; stride += 2048) {
+      char nm[96];
+      snprintf(nm, sizeof nm, "pair mode 5 stage stride %d base offset %d", stride, off);
+      run<true, 128, 32>(nm, 0, gsrc, gbytes, sink, cyc, 5, 0, 0, stride, off);
+    }
+  return 0;
+  for (int m = 2; m <= 8; ++m) {
+    if (m == 3 || m == 4 || m == 6) continue;
+    char nm[64];
+    snprintf(nm, sizeof nm, "pair M256 N128 SW32 mode %d", m);
+    run<true, 128, 32>(nm, 0, gsrc, gbytes, sink, cyc, m, 0, 0);
+    run<true, 128, 32>(nm, 0, gsrc, gbytes, sink, cyc, m, 0, 0);
+  }
+  return 0;
+  for (int f = 0; f < 2; ++f)
+    for (int m = 2; m <= 6; m += (m == 2 ? 3 : 1)) {
+      char nm[64];
+      snprintf(nm, sizeof nm, "pair M256 N128 SW32 mode %d fill %d", m, f);
+      run<true, 128, 32>(nm, 0, gsrc, gbytes, sink, cyc, m, f);
+      snprintf(nm, sizeof nm, "1cta M128 N128 SW32 mode %d fill %d", m, f);
+      if (m != 5 && m != 6) run<false, 128, 32>(nm, 0, gsrc, gbytes, sink, cyc, m, f);
+    }
+  for (int m = 1; m <= 0; ++m) {
+    char nm[64];
+    snprintf(nm, sizeof nm, "pair M256 N128 SW32 mode %d", m);
+    run<true, 128, 32>(nm, 0, gsrc, gbytes, sink, cyc, m);
+    snprintf(nm, sizeof nm, "1cta M128 N128 SW32 mode %d", m);
+    run<false, 128, 32>(nm, 0, gsrc, gbytes, sink, cyc, m);
+  }
+  for (int t = 0; t < 2; ++t) {
+    run<false, 256, 128>("1cta M128 N256 SW128 (probe shape)", 0, gsrc, gbytes, sink, cyc);
+    run<false, 128, 32>("1cta M128 N128 SW32 (K7)", t ? 88 * 1024 : 0, gsrc, gbytes, sink, cyc);
+    run<true, 128, 32>("pair M256 N128 SW32 (K7 pair)", t ? 66 * 1024 : 0, gsrc, gbytes, sink, cyc);
+    run<false, 256, 32>("1cta M128 N256 SW32", t ? 88 * 1024 : 0, gsrc, gbytes, sink, cyc);
+    run<true, 256, 32>("pair M256 N256 SW32", t ? 88 * 1024 : 0, gsrc, gbytes, sink, cyc);
+    run<true, 128, 128>("pair M256 N128 SW128", t ? 66 * 1024 : 0, gsrc, gbytes, sink, cyc);
+    run<false, 128, 128>("1cta M128 N128 SW128", t ? 88 * 1024 : 0, gsrc, gbytes, sink, cyc);
+  }
+  CK(cudaDeviceSynchronize());
+  return 0;
+}
