@@ -318,9 +318,10 @@ int pf_batched_kl_fixup_f64(const double *P, int64_t ld, int64_t rows, int64_t k
  *   (guard sentinel, settle, zero at the target); k <= 4717.  grade 64 keeps
  *   levels 2..9 of all 7 planes (34 pairs, FP64-grade: within 1e-10 of the
  *   reference), grade 32 levels 2..6 of the top 5 planes (15 pairs, the
- *   north-star FP32 tolerance 1e-5).  cta_pair != 0 runs the CTA-pair kernel
- *   (tcgen05 cta_group::2, M256 tiles over two SMs: half the shared-memory
- *   operand traffic per SM), bitwise the same outputs as cta_pair == 0.
+ *   north-star FP32 tolerance 1e-5).  cta_pair != 0 runs the persistent
+ *   CTA-pair kernel (tcgen05 cta_group::2, M256 tiles over two SMs, the
+ *   epilogue overlapped with the next tile's MMAs), bitwise the same outputs
+ *   as cta_pair == 0 (one CTA per 128 x 128 tile).
  *   Follow with pf_batched_kl_fixup_f64 for
  *   the guarded pairs. */
 int pf_slice_rows_u8(const double *P, int64_t ld, int64_t rows, int64_t k, double clamp,

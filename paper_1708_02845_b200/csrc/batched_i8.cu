@@ -148,11 +148,17 @@ __global__ void __launch_bounds__(256) slice_targets_kernel(const double *__rest
   }
 }
 
-// v * 2^e with one rounding == ldexp(v, e) whenever 2^e is a normal double
+// ldexp(v, e) for the Ozaki sums v (0 or within [2^-64, 2^64]), branch-free:
+// v * 2^e1 is exact (normal, |e1| <= 900), the second power-of-two multiply
+// rounds once -- the single rounding ldexp does; |e| beyond 1922 gives 0 or
+// inf either way.
+__device__ __forceinline__ double pow2_exact(int e) {   // 2^e, -1022 <= e <= 1023
+  return __longlong_as_double(static_cast<long long>(e + 1023) << 52);
+}
 __device__ __forceinline__ double pow2_scale(double v, int e) {
-  return (e >= -1022 && e <= 1023)
-             ? v * __longlong_as_double(static_cast<long long>(e + 1023) << 52)
-             : ldexp(v, e);
+  e = max(-1922, min(1922, e));
+  const int e1 = max(-900, min(900, e));
+  return (v * pow2_exact(e1)) * pow2_exact(e - e1);
 }
 
 // ------------------------------------------------------------------ GEMM --
@@ -347,257 +353,31 @@ __device__ __forceinline__ uint32_t smid() {
   return r;
 }
 
-// ---------------------------------------------------------- GEMM, CTA pair --
-// The same two-pass level schedule on a CTA pair (cta_group::2, cluster of 2
-// CTAs on two row tiles): the leader issues M256 N128 K32 MMAs whose A rows
-// 0-127 come from its own shared memory and 128-255 from the peer's, and whose
-// B (the 128 targets) is split 64 / 64 between the two; each CTA's TMEM gets
-// its own 128 rows.  Per SM and MMA the tensor pipe reads 4 KB of A + 2 KB of
-// B from shared memory instead of 4 + 4 KB, and TMA writes 6 instead of 8 KB
-// per slice: the 1-CTA kernel is shared-memory bound (UMMA operand reads +
-// TMA writes ~151 B/clk against ~128).  5-stage ring of 42 KB per CTA.  The
-// arithmetic is the same exact integers, so the outputs are bitwise the
-// 1-CTA kernel's.
+// ------------------------------------------------ GEMM, persistent CTA pair --
+// The same two-pass level schedule on persistent CTA pairs (tcgen05
+// cta_group::2, one cluster of 2 per SM pair, tiles strided over the
+// clusters; consecutive clusters share a row pair so its A planes stream
+// from HBM once and hit L2 after).  The leader issues M256 N128 K32 MMAs
+// whose A rows 0-127 come from its own shared memory and 128-255 from the
+// peer's, and whose B (the 128 targets) is split 64 / 64 between the two;
+// each CTA's TMEM gets its own 128 rows.  Per SM and MMA the tensor pipe
+// reads 4 KB of A + 2 KB of B instead of 4 + 4 KB.  The epilogue is off the
+// tensor pipe's critical path: the epilogue warps fold the pass-2
+// accumulators into the FP64 pass-1 partials in registers, release TMEM
+// (free_bar), and only then scale / guard / settle / store while the next
+// tile's pass-1 MMAs run.  Same integers, same FP64 operation order: bitwise
+// the 1-CTA kernel's outputs.  5-stage ring of 42 KB per CTA.
+//
+// kDiag (timing diagnostics only, PF_K7_DIAG, wrong outputs): bit 0 = no TMA
+// loads (the MMAs run on stale shared memory), bit 1 = no epilogue arithmetic
+// or stores, bit 2 = %globaltimer phase stamps of cluster 0 per tile k at
+// out[k * 16 + i] (tools/probe_k7pp_stamps.py).
 constexpr int kP2BN = 128, kP2HalfN = 64, kP2Stages = 5;
 constexpr int kP2TileA = 128 * kO2BK;                         // 4 KB per slice
 constexpr int kP2TileB = kP2HalfN * kO2BK;                    // 2 KB per slice
 constexpr int kP2StageBytes = kOzSlices * (kP2TileA + kP2TileB);  // 43,008
 constexpr int kP2Smem = kP2Stages * kP2StageBytes + 1024;
 
-//
-// kQuad: two such pairs in one cluster of 4 on the same row-tile pair and
-// adjacent target tiles share every A tile by TMA multicast: each CTA loads
-// one 64-row half of its row tile (one box per slice, the UMMA layout needs
-// the halves interleaved within each slice plane) and multicasts it to the
-// CTA of the other pair holding the same rows, so A crosses L2 -> SM once
-// per two pairs.  Each slot's empty barrier then waits for both pairs' MMAs.
-//
-// kDiag (timing diagnostics only, PF_K7_DIAG, wrong outputs): bit 0 = no TMA
-// loads (the MMAs run on stale shared memory), bit 1 = no epilogue arithmetic
-// or stores (accumulators drained and dropped).
-template <int kS, int kMaxL, bool kQuad, int kDiag = 0>
-__global__ void __launch_bounds__(kO2Threads, 1)
-    batched_kl_i8_pair_kernel(const __grid_constant__ CUtensorMap mapA7,
-                              const __grid_constant__ CUtensorMap mapA4,
-                              const __grid_constant__ CUtensorMap mapB7,
-                              const __grid_constant__ CUtensorMap mapB4,
-                              const int32_t *__restrict__ ea, const int32_t *__restrict__ eb,
-                              int64_t rows, int64_t T, int nkb, const double *__restrict__ H,
-                              const int64_t *__restrict__ targets, double tau, int64_t row0,
-                              double *__restrict__ out, int64_t ldo) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  __shared__ __align__(8) uint64_t full_bar[kP2Stages], empty_bar[kP2Stages];
-  __shared__ __align__(8) uint64_t pass_bar[2], drained_bar;
-  __shared__ uint32_t tmem_base;
-
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  double *stamp = (kDiag & 4) ? out + (static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x) * 8
-                              : nullptr;
-  if ((kDiag & 4) && tid == 0) stamp[0] = static_cast<double>(gtimer());
-  // cluster (2, 1, 1): x = 2 x target tile + pair rank (the 2-CTA MMA pairs
-  // adjacent x ranks), y = row-tile pair; the target tiles of one row pair are
-  // consecutive CTAs, so its A tiles stream from HBM once and hit L2 after
-  const uint32_t crank = tc::cluster_rank();
-  const uint32_t rank = crank & 1;           // 0 = pair leader (issues the MMAs)
-  const uint32_t pairi = crank >> 1;         // kQuad: which pair of the cluster
-  const uint32_t leader = crank & 2;         // cluster rank of this pair's leader
-  const int t0 = kQuad ? ((blockIdx.x >> 2) * 2 + pairi) * kP2BN : (blockIdx.x >> 1) * kP2BN;
-  const int64_t q0 = (static_cast<int64_t>(blockIdx.y) * 2 + rank) * 128;   // this CTA's rows
-
-  if (tid == 0) {
-    tc::prefetch_map(&mapA7);
-    tc::prefetch_map(&mapA4);
-    tc::prefetch_map(&mapB7);
-    tc::prefetch_map(&mapB4);
-    for (int s = 0; s < kP2Stages; ++s) {
-      mbar_init(&full_bar[s], 1);    // the leader's producer arrives (both CTAs' bytes)
-      mbar_init(&empty_bar[s], kQuad ? 2 : 1);   // one multicast commit per pair
-    }
-    mbar_init(&pass_bar[0], 1);
-    mbar_init(&pass_bar[1], 1);
-    mbar_init(&drained_bar, 16);     // every epilogue warp of both CTAs
-  }
-  if (warp == 0) tc::tmem_alloc_pair<512>(&tmem_base);
-  tc::fence_before();
-  tc::cluster_sync();               // barriers of both CTAs initialised, TMEM allocated
-  if ((kDiag & 4) && tid == 0) stamp[1] = static_cast<double>(gtimer());
-  tc::fence_after();
-  const uint32_t tmem = tmem_base;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      // ---- TMA producer (both CTAs): own 128 A rows, own half of the targets
-      const int32_t tb = t0 + static_cast<int32_t>(rank) * kP2HalfN;
-      for (int it = 0; it < 2 * nkb; ++it) {
-        const int s = it % kP2Stages;
-        const uint32_t round = it / kP2Stages;
-        const bool p1 = it < nkb;
-        const int kb = p1 ? it : it - nkb;
-        const int ns = p1 ? kO2Pass1Slices : kS;
-        mbar_wait(&empty_bar[s], (round & 1) ^ 1);
-        uint8_t *sa = smem + s * kP2StageBytes;
-        uint8_t *sb = sa + kOzSlices * kP2TileA;
-        if constexpr ((kDiag & 1) != 0) {
-          if (rank == 0) mbar_arrive(&full_bar[s]);
-          continue;
-        }
-        if (rank == 0) mbar_expect_tx(&full_bar[s], 2 * ns * (kP2TileA + kP2TileB));
-        const uint32_t lb = tc::mapa(&full_bar[s], leader);
-        if constexpr (kQuad) {   // mapA7 = 64-row, 1-slice boxes
-          const uint16_t mc = static_cast<uint16_t>(5u << rank);   // {rank, rank + 2}
-          for (int sl = 0; sl < ns; ++sl)
-            tc::tma_load_3d_pair_mc(sa + sl * kP2TileA + pairi * (64 * kO2BK), &mapA7, kb * kO2BK,
-                                    static_cast<int32_t>(q0 + pairi * 64), sl, &full_bar[s], mc);
-        } else {
-          tc::tma_load_3d_pair(sa, p1 ? &mapA4 : &mapA7, kb * kO2BK, static_cast<int32_t>(q0), 0,
-                               lb);
-        }
-        tc::tma_load_3d_pair(sb, p1 ? &mapB4 : &mapB7, kb * kO2BK, tb, 0, lb);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
-      // ---- MMA issuer (leader only): M256 N128 K32.  The two passes are
-      // separate loops: a conditional tcgen05.commit inside one loop compiles
-      // to a predicated UTCBAR that stalls the issue every stage even when
-      // its predicate is off (pass 1 ran at 94 instead of 64 clk per MMA).
-      constexpr uint32_t idesc = tc::idesc_i8(256, kP2BN, false, false);
-      const uint16_t own = static_cast<uint16_t>(3u << leader);
-      constexpr uint16_t ring = kQuad ? 0xF : 3;
-      auto wait_stage = [&](int it) -> uint32_t {
-        const int s = it % kP2Stages;
-        uint64_t tw0 = 0;
-        if constexpr ((kDiag & 8) != 0) tw0 = clock64();
-        if constexpr ((kDiag & 16) == 0) mbar_wait(&full_bar[s], (it / kP2Stages) & 1);
-        if constexpr ((kDiag & 8) != 0) {
-          if (blockIdx.x == 0 && blockIdx.y == 0) {
-            double *tl = out + static_cast<int64_t>(gridDim.x) * gridDim.y * 8;
-            tl[2 * it] = static_cast<double>(tw0);
-            tl[2 * it + 1] = static_cast<double>(clock64());
-          }
-        }
-        tc::fence_after();
-        return smem_u32(smem + s * kP2StageBytes);
-      };
-      for (int kb = 0; kb < nkb; ++kb) {
-        const uint32_t sa = wait_stage(kb);
-        const uint32_t sb = sa + kOzSlices * kP2TileA;
-#pragma unroll
-        for (int i = 1; i <= kO2Pass1Slices; ++i)
-#pragma unroll
-          for (int j = 1; j <= kO2Pass1Slices; ++j) {
-            const int l = i + j;
-            if (l > 5) continue;
-            tc::mma_i8_pair(tmem + (l - 2) * kP2BN, tc::sdesc<32>(sa + (i - 1) * kP2TileA),
-                            tc::sdesc<32>(sb + (j - 1) * kP2TileB), idesc, !(kb == 0 && i == 1));
-          }
-        tc::commit_pair_mask(&empty_bar[kb % kP2Stages], ring);
-      }
-      tc::commit_pair_mask(&pass_bar[0], own);
-      // pass 2 reuses the accumulators: wait for both CTAs' drains
-      if (kDiag & 4) stamp[2] = static_cast<double>(gtimer());
-      mbar_wait(&drained_bar, 0);
-      if (kDiag & 4) stamp[3] = static_cast<double>(gtimer());
-      tc::fence_after();
-      for (int kb = 0; kb < nkb; ++kb) {
-        const uint32_t sa = wait_stage(nkb + kb);
-        const uint32_t sb = sa + kOzSlices * kP2TileA;
-#pragma unroll
-        for (int i = 1; i <= kS; ++i)
-#pragma unroll
-          for (int j = 1; j <= kS; ++j) {
-            const int l = i + j;
-            if (l < 6 || l > kMaxL) continue;
-            const int first_i = l - kS > 1 ? l - kS : 1;
-            tc::mma_i8_pair(tmem + (l - 6) * kP2BN, tc::sdesc<32>(sa + (i - 1) * kP2TileA),
-                            tc::sdesc<32>(sb + (j - 1) * kP2TileB), idesc,
-                            !(kb == 0 && i == first_i));
-          }
-        tc::commit_pair_mask(&empty_bar[(nkb + kb) % kP2Stages], ring);
-      }
-      tc::commit_pair_mask(&pass_bar[1], own);
-    }
-  } else {
-    // ---- epilogue warps 2..9 (both CTAs, own TMEM = own 128 rows x 128 targets)
-    const int quarter = warp & 3, half = (warp - 2) >> 2;
-    const int r = quarter * 32 + lane;
-    const int64_t q = q0 + r;
-    const bool row_ok = q < rows;
-    const uint32_t base = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + half * 64;
-    double v1[64];
-    mbar_wait(&pass_bar[0], 0);
-    tc::fence_after();
-#pragma unroll
-    for (int c0 = 0; c0 < 64; c0 += 8) {
-      uint32_t acc[4][8];
-#pragma unroll
-      for (int l = 0; l < 4; ++l) tc::tmem_ld8(base + l * kP2BN + c0, acc[l]);
-      tc::tmem_ld_wait();
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        double v = static_cast<double>(acc[3][u]);
-#pragma unroll
-        for (int l = 2; l >= 0; --l) v = fma(v, 0x1p-8, static_cast<double>(acc[l][u]));
-        v1[c0 + u] = v;
-      }
-    }
-    tc::fence_before();
-    __syncwarp();
-    if (lane == 0) tc::mbar_arrive_cluster(tc::mapa(&drained_bar, leader));
-    mbar_wait(&pass_bar[1], 0);
-    if ((kDiag & 4) && tid == 64) stamp[4] = static_cast<double>(gtimer());
-    tc::fence_after();
-    const double h = row_ok ? H[q] : 0.0;
-    const int e_q = row_ok ? ea[q] : 0;
-    const int64_t tq = row_ok ? row0 + q : -1;
-    constexpr int kL2 = kMaxL - 5;
-#pragma unroll
-    for (int c0 = 0; c0 < 64; c0 += 8) {
-      uint32_t acc[kL2][8];
-#pragma unroll
-      for (int l = 0; l < kL2; ++l) tc::tmem_ld8(base + l * kP2BN + c0, acc[l]);
-      tc::tmem_ld_wait();
-      if (!row_ok || (kDiag & 2) != 0) continue;
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int64_t t = t0 + half * 64 + c0 + u;
-        if (t >= T) continue;
-        double v = static_cast<double>(acc[kL2 - 1][u]);
-#pragma unroll
-        for (int l = kL2 - 2; l >= 0; --l) v = fma(v, 0x1p-8, static_cast<double>(acc[l][u]));
-        v = fma(v, 0x1p-32, v1[c0 + u]);
-        const double S = pow2_scale(v, e_q + eb[t] - 16);
-        double val = h + S;
-        const bool is_t = (tq == targets[t]);
-        if (!is_t && fabs(val) < tau * (fabs(h) + fabs(S)))
-          val = __longlong_as_double(static_cast<long long>(kOzGuard));
-        else
-          val = is_t ? 0.0 : settle(val);
-        out[q * ldo + t] = val;
-      }
-    }
-  }
-  if ((kDiag & 4) && tid == 64) stamp[5] = static_cast<double>(gtimer());
-  tc::fence_before();
-  tc::cluster_sync();   // both CTAs done with TMEM and with each other's barriers
-  if ((kDiag & 4) && tid == 0) {
-    stamp[6] = static_cast<double>(gtimer());
-    stamp[7] = static_cast<double>(smid());
-  }
-  if (warp == 0) tc::tmem_free_pair<512>(tmem);
-}
-
-// ------------------------------------------------ GEMM, persistent CTA pair --
-// The CTA-pair kernel made persistent (one cluster per SM pair, tiles
-// strided over the clusters; consecutive clusters share a row pair so its A
-// planes are read from HBM once and from L2 after) with the epilogue taken
-// off the tensor pipe's critical path: the epilogue warps fold the pass-2
-// accumulators into the FP64 pass-1 partials in registers, release TMEM to
-// the MMA thread (free_bar), and only then apply the scale / guard / settle
-// and store -- while the next tile's pass-1 MMAs run.  Same integers, same
-// FP64 operation order: bitwise the 1-CTA kernel's outputs.
 template <int kS, int kMaxL, int kDiag = 0>
 __global__ void __launch_bounds__(kO2Threads, 1)
     batched_kl_i8_pp_kernel(const __grid_constant__ CUtensorMap mapA7,
@@ -618,6 +398,13 @@ __global__ void __launch_bounds__(kO2Threads, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t rank = tc::cluster_rank();   // 0 = leader (issues the MMAs)
   const int cid = static_cast<int>(blockIdx.x >> 1), ncl = static_cast<int>(gridDim.x >> 1);
+  // tile w: row pair w / t_tiles, target tile w % t_tiles
+  // kDiag & 4: %globaltimer stamps of cluster 0's leader, per tile k, at out[k * 16 + i]
+  const bool stamping = (kDiag & 4) != 0 && blockIdx.x == 0;
+#define PP_STAMP(k, i) \
+  do {                 \
+    if (stamping) out[(k) * 16 + (i)] = static_cast<double>(gtimer()); \
+  } while (0)
 
   if (tid == 0) {
     tc::prefetch_map(&mapA7);
@@ -625,8 +412,8 @@ __global__ void __launch_bounds__(kO2Threads, 1)
     tc::prefetch_map(&mapB7);
     tc::prefetch_map(&mapB4);
     for (int s = 0; s < kP2Stages; ++s) {
-      mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
+      mbar_init(&full_bar[s], 1);    // the leader's producer arrives (both CTAs' bytes)
+      mbar_init(&empty_bar[s], 1);   // one multicast MMA commit
     }
     mbar_init(&pass_bar[0], 1);
     mbar_init(&pass_bar[1], 1);
@@ -641,8 +428,11 @@ __global__ void __launch_bounds__(kO2Threads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      // ---- TMA producer (both CTAs): own 128 A rows, own half of the targets
-      int it = 0;
+      // ---- TMA producer (both CTAs): own 128 A rows, own half of the targets.
+      // Every pass starts at ring slot 0 (slots left over at a pass end are
+      // skipped), so the MMA loop below can be unrolled over the ring with
+      // compile-time slot addresses; per-slot phases live in `ph`.
+      uint32_t ph = 0;
       for (int w = cid; w < ntiles; w += ncl) {
         const int64_t q0 = (static_cast<int64_t>(w / t_tiles) * 2 + rank) * 128;
         const int32_t tb = (w % t_tiles) * kP2BN + static_cast<int32_t>(rank) * kP2HalfN;
@@ -650,75 +440,103 @@ __global__ void __launch_bounds__(kO2Threads, 1)
           const int ns = pass == 0 ? kO2Pass1Slices : kS;
           const CUtensorMap *ma = pass == 0 ? &mapA4 : &mapA7;
           const CUtensorMap *mb = pass == 0 ? &mapB4 : &mapB7;
-          for (int kb = 0; kb < nkb; ++kb, ++it) {
-            const int s = it % kP2Stages;
-            mbar_wait(&empty_bar[s], ((it / kP2Stages) & 1) ^ 1);
-            if constexpr ((kDiag & 1) != 0) {
-              if (rank == 0) mbar_arrive(&full_bar[s]);
-              continue;
+          for (int kb0 = 0; kb0 < nkb; kb0 += kP2Stages) {
+#pragma unroll
+            for (int st = 0; st < kP2Stages; ++st) {
+              const int kb = kb0 + st;
+              if (kb >= nkb) break;
+              mbar_wait(&empty_bar[st], ((ph >> st) & 1) ^ 1);
+              ph ^= 1u << st;
+              if constexpr ((kDiag & 1) != 0) {
+                if (rank == 0) mbar_arrive(&full_bar[st]);
+                continue;
+              }
+              uint8_t *sa = smem + st * kP2StageBytes;
+              uint8_t *sb = sa + kOzSlices * kP2TileA;
+              if (rank == 0) mbar_expect_tx(&full_bar[st], 2 * ns * (kP2TileA + kP2TileB));
+              const uint32_t lb = tc::mapa(&full_bar[st], 0);
+              tc::tma_load_3d_pair(sa, ma, kb * kO2BK, static_cast<int32_t>(q0), 0, lb);
+              tc::tma_load_3d_pair(sb, mb, kb * kO2BK, tb, 0, lb);
             }
-            uint8_t *sa = smem + s * kP2StageBytes;
-            uint8_t *sb = sa + kOzSlices * kP2TileA;
-            if (rank == 0) mbar_expect_tx(&full_bar[s], 2 * ns * (kP2TileA + kP2TileB));
-            const uint32_t lb = tc::mapa(&full_bar[s], 0);
-            tc::tma_load_3d_pair(sa, ma, kb * kO2BK, static_cast<int32_t>(q0), 0, lb);
-            tc::tma_load_3d_pair(sb, mb, kb * kO2BK, tb, 0, lb);
           }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
-      // ---- MMA issuer (leader only): M256 N128 K32; each pass its own loop
-      // (a conditional commit inside a shared loop costs a stall per stage)
+      // ---- MMA issuer (leader only): M256 N128 K32.  The tensor pipe keeps
+      // almost no queue of its own, so whatever this thread does between two
+      // MMAs beyond the executing MMA's 64 clocks is a pipe bubble: each pass
+      // is its own loop (a conditional commit inside a shared loop costs a
+      // stall per stage), and the ring is unrolled so that the descriptors
+      // after each full-barrier wait are compile-time offsets of uniform
+      // registers (a runtime slot address put an R2UR chain behind every wait:
+      // ~145 clocks per stage, measured by tools/probe_umma_shapes.cu).
       constexpr uint32_t idesc = tc::idesc_i8(256, kP2BN, false, false);
-      int it = 0, k = 0;
+      const uint32_t ring = smem_u32(smem);
+      uint32_t ph = 0;
+      int k = 0;
       for (int w = cid; w < ntiles; w += ncl, ++k) {
+        PP_STAMP(k, 0);
         if (k > 0) {   // the previous tile's pass-2 accumulators drained
           mbar_wait(&free_bar, (k - 1) & 1);
           tc::fence_after();
         }
-        for (int kb = 0; kb < nkb; ++kb, ++it) {
-          const int s = it % kP2Stages;
-          mbar_wait(&full_bar[s], (it / kP2Stages) & 1);
-          tc::fence_after();
-          const uint32_t sa = smem_u32(smem + s * kP2StageBytes);
-          const uint32_t sb = sa + kOzSlices * kP2TileA;
+        PP_STAMP(k, 1);
+        for (int kb0 = 0; kb0 < nkb; kb0 += kP2Stages) {
 #pragma unroll
-          for (int i = 1; i <= kO2Pass1Slices; ++i)
+          for (int st = 0; st < kP2Stages; ++st) {
+            const int kb = kb0 + st;
+            if (kb >= nkb) break;
+            mbar_wait(&full_bar[st], (ph >> st) & 1);
+            ph ^= 1u << st;
+            tc::fence_after();
+            const uint32_t sa = ring + st * kP2StageBytes;
+            const uint32_t sb = sa + kOzSlices * kP2TileA;
 #pragma unroll
-            for (int j = 1; j <= kO2Pass1Slices; ++j) {
-              const int l = i + j;
-              if (l > 5) continue;
-              tc::mma_i8_pair(tmem + (l - 2) * kP2BN, tc::sdesc<32>(sa + (i - 1) * kP2TileA),
-                              tc::sdesc<32>(sb + (j - 1) * kP2TileB), idesc,
-                              !(kb == 0 && i == 1));
-            }
-          tc::commit_pair(&empty_bar[s]);
+            for (int i = 1; i <= kO2Pass1Slices; ++i)
+#pragma unroll
+              for (int j = 1; j <= kO2Pass1Slices; ++j) {
+                const int l = i + j;
+                if (l > 5) continue;
+                tc::mma_i8_pair(tmem + (l - 2) * kP2BN, tc::sdesc<32>(sa + (i - 1) * kP2TileA),
+                                tc::sdesc<32>(sb + (j - 1) * kP2TileB), idesc,
+                                !(kb == 0 && i == 1));
+              }
+            tc::commit_pair(&empty_bar[st]);
+          }
         }
         tc::commit_pair(&pass_bar[0]);
+        PP_STAMP(k, 2);
         mbar_wait(&drained_bar, k & 1);   // pass 2 reuses the accumulators
         tc::fence_after();
-        for (int kb = 0; kb < nkb; ++kb, ++it) {
-          const int s = it % kP2Stages;
-          mbar_wait(&full_bar[s], (it / kP2Stages) & 1);
-          tc::fence_after();
-          const uint32_t sa = smem_u32(smem + s * kP2StageBytes);
-          const uint32_t sb = sa + kOzSlices * kP2TileA;
+        PP_STAMP(k, 3);
+        for (int kb0 = 0; kb0 < nkb; kb0 += kP2Stages) {
 #pragma unroll
-          for (int i = 1; i <= kS; ++i)
+          for (int st = 0; st < kP2Stages; ++st) {
+            const int kb = kb0 + st;
+            if (kb >= nkb) break;
+            mbar_wait(&full_bar[st], (ph >> st) & 1);
+            ph ^= 1u << st;
+            tc::fence_after();
+            const uint32_t sa = ring + st * kP2StageBytes;
+            const uint32_t sb = sa + kOzSlices * kP2TileA;
 #pragma unroll
-            for (int j = 1; j <= kS; ++j) {
-              const int l = i + j;
-              if (l < 6 || l > kMaxL) continue;
-              const int first_i = l - kS > 1 ? l - kS : 1;
-              tc::mma_i8_pair(tmem + (l - 6) * kP2BN, tc::sdesc<32>(sa + (i - 1) * kP2TileA),
-                              tc::sdesc<32>(sb + (j - 1) * kP2TileB), idesc,
-                              !(kb == 0 && i == first_i));
-            }
-          tc::commit_pair(&empty_bar[s]);
+            for (int i = 1; i <= kS; ++i)
+#pragma unroll
+              for (int j = 1; j <= kS; ++j) {
+                const int l = i + j;
+                if (l < 6 || l > kMaxL) continue;
+                const int first_i = l - kS > 1 ? l - kS : 1;
+                tc::mma_i8_pair(tmem + (l - 6) * kP2BN, tc::sdesc<32>(sa + (i - 1) * kP2TileA),
+                                tc::sdesc<32>(sb + (j - 1) * kP2TileB), idesc,
+                                !(kb == 0 && i == first_i));
+              }
+            tc::commit_pair(&empty_bar[st]);
+          }
         }
         tc::commit_pair(&pass_bar[1]);
+        PP_STAMP(k, 4);
       }
     }
   } else {
@@ -737,14 +555,15 @@ __global__ void __launch_bounds__(kO2Threads, 1)
       double v[64];
       mbar_wait(&pass_bar[0], k & 1);
       tc::fence_after();
+      if (tid == 64) PP_STAMP(k, 5);
 #pragma unroll
-      for (int c0 = 0; c0 < 64; c0 += 8) {
-        uint32_t acc[4][8];
+      for (int c0 = 0; c0 < 64; c0 += 4) {   // x4 chunks: v[64] + acc stay in 168 registers
+        uint32_t acc[4][4];
 #pragma unroll
-        for (int l = 0; l < 4; ++l) tc::tmem_ld8(base + l * kP2BN + c0, acc[l]);
+        for (int l = 0; l < 4; ++l) tc::tmem_ld4(base + l * kP2BN + c0, acc[l]);
         tc::tmem_ld_wait();
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < 4; ++u) {
           double x = static_cast<double>(acc[3][u]);
 #pragma unroll
           for (int l = 2; l >= 0; --l) x = fma(x, 0x1p-8, static_cast<double>(acc[l][u]));
@@ -754,16 +573,18 @@ __global__ void __launch_bounds__(kO2Threads, 1)
       tc::fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive_cluster(drained_leader);
+      if (tid == 64) PP_STAMP(k, 6);
       mbar_wait(&pass_bar[1], k & 1);
       tc::fence_after();
+      if (tid == 64) PP_STAMP(k, 7);
 #pragma unroll
-      for (int c0 = 0; c0 < 64; c0 += 8) {
-        uint32_t acc[kL2][8];
+      for (int c0 = 0; c0 < 64; c0 += 4) {
+        uint32_t acc[kL2][4];
 #pragma unroll
-        for (int l = 0; l < kL2; ++l) tc::tmem_ld8(base + l * kP2BN + c0, acc[l]);
+        for (int l = 0; l < kL2; ++l) tc::tmem_ld4(base + l * kP2BN + c0, acc[l]);
         tc::tmem_ld_wait();
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < 4; ++u) {
           double x = static_cast<double>(acc[kL2 - 1][u]);
 #pragma unroll
           for (int l = kL2 - 2; l >= 0; --l) x = fma(x, 0x1p-8, static_cast<double>(acc[l][u]));
@@ -773,37 +594,50 @@ __global__ void __launch_bounds__(kO2Threads, 1)
       tc::fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive_cluster(free_leader);   // TMEM free for the next tile
-      if ((kDiag & 2) != 0 || q >= rows) continue;
-      const double h = H[q];
-      const int e_q = ea[q] - 16;
-      const int64_t tq = row0 + q;
+      if (tid == 64) PP_STAMP(k, 8);
+      if constexpr ((kDiag & 2) != 0) continue;
+      // Branch-free per element (the epilogue has 2 warps per scheduler and
+      // FP64 latency to hide: a branchy element body serialised it to ~1 us
+      // per element-row, longer than pass 1): the column data (eb, target)
+      // is loaded once per lane and broadcast by shuffles, the 2^e scaling
+      // is two exact power-of-two multiplies, the guard/settle are selects.
+      const bool row_ok = q < rows;
+      const double h = row_ok ? H[q] : 0.0;
+      const int e_q = (row_ok ? ea[q] : 0) - 16;
+      const int64_t tq = row_ok ? row0 + q : -2;
+      const int64_t tA = tc0 + lane, tB = tc0 + 32 + lane;
+      const int ebA = tA < T ? eb[tA] : 0, ebB = tB < T ? eb[tB] : 0;
+      const int64_t tgA = tA < T ? targets[tA] : -1, tgB = tB < T ? targets[tB] : -1;
       double *orow = out + q * ldo + tc0;
-      const bool full = pairs_ok && tc0 + 64 <= T;
+      const bool full = row_ok && pairs_ok && tc0 + 64 <= T;
 #pragma unroll
       for (int c = 0; c < 64; c += 2) {
         double o[2];
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
-          const int64_t t = tc0 + c + u;
-          const bool in = t < T;
-          const double S = pow2_scale(v[c + u], e_q + (in ? eb[t] : 0));
-          double val = h + S;
-          const bool is_t = in && (tq == targets[t]);
-          if (!is_t && fabs(val) < tau * (fabs(h) + fabs(S)))
-            val = __longlong_as_double(static_cast<long long>(kOzGuard));
-          else
-            val = is_t ? 0.0 : settle(val);
-          o[u] = val;
+          const int cc = c + u;
+          const int ebt = __shfl_sync(0xffffffffu, cc < 32 ? ebA : ebB, cc & 31);
+          const long long tg = __shfl_sync(0xffffffffu, static_cast<long long>(cc < 32 ? tgA : tgB),
+                                           cc & 31);
+          const double S = pow2_scale(v[cc], e_q + ebt);
+          const double val = h + S;
+          const bool is_t = tq == tg;
+          const bool guard = !is_t && fabs(val) < tau * (fabs(h) + fabs(S));
+          const double settled = settle(val);
+          o[u] = guard ? __longlong_as_double(static_cast<long long>(kOzGuard))
+                       : (is_t ? 0.0 : settled);
         }
         if (full) {
           *reinterpret_cast<double2 *>(orow + c) = make_double2(o[0], o[1]);
-        } else {
+        } else if (row_ok) {
           if (tc0 + c < T) orow[c] = o[0];
           if (tc0 + c + 1 < T) orow[c + 1] = o[1];
         }
       }
+      if (tid == 64) PP_STAMP(k, 9);
     }
   }
+#undef PP_STAMP
   tc::fence_before();
   tc::cluster_sync();   // both CTAs done with TMEM and with each other's barriers
   if (warp == 0) tc::tmem_free_pair<512>(tmem);
@@ -894,66 +728,51 @@ static int slice_map(CUtensorMap *map, const uint8_t *base, int64_t outer, int64
 template <int kS, int kMaxL>
 static int launch_i8(const CUtensorMap (&m)[4], const int32_t *ea, const int32_t *eb,
                      int64_t rows, int64_t T, int64_t k, const double *H, const int64_t *targets,
-                     double tau, int64_t row0, double *out, int64_t ldo, int pair,
+                     double tau, int64_t row0, double *out, int64_t ldo, bool pair,
                      cudaStream_t stream) {
   const int nkb = static_cast<int>((k + kO2BK - 1) / kO2BK);
   const unsigned tiles = static_cast<unsigned>((rows + 127) / 128);
   if (pair) {  // a pair's second CTA may hold only out-of-range rows
-    // 1: persistent pair (the product path), 2: two pairs sharing A by TMA
-    // multicast, 3: one tile per pair (kept for A/B measurements)
-    const bool quad = pair == 2, persistent = pair == 1;
     static const int diag = [] {
       const char *e = getenv("PF_K7_DIAG");
       return e ? atoi(e) : 0;
     }();
-    using Kern = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, const int32_t *,
-                          const int32_t *, int64_t, int64_t, int, const double *, const int64_t *,
-                          double, int64_t, double *, int64_t);
-    using KernP = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, const int32_t *,
-                           const int32_t *, int64_t, int64_t, int, const double *,
-                           const int64_t *, double, int64_t, double *, int64_t, int, int);
-    Kern kern = quad ? batched_kl_i8_pair_kernel<kS, kMaxL, true>
-                     : batched_kl_i8_pair_kernel<kS, kMaxL, false>;
-    KernP kernp = diag == 1   ? batched_kl_i8_pp_kernel<kS, kMaxL, 1>
-                  : diag == 2 ? batched_kl_i8_pp_kernel<kS, kMaxL, 2>
-                  : diag == 3 ? batched_kl_i8_pp_kernel<kS, kMaxL, 3>
-                              : batched_kl_i8_pp_kernel<kS, kMaxL, 0>;
-    const void *kfn = persistent ? (const void *)kernp : (const void *)kern;
-    if (int e = ensure_smem(kfn, kP2Smem)) return e;
+    auto kern = diag == 1   ? batched_kl_i8_pp_kernel<kS, kMaxL, 1>
+                : diag == 2 ? batched_kl_i8_pp_kernel<kS, kMaxL, 2>
+                : diag == 3 ? batched_kl_i8_pp_kernel<kS, kMaxL, 3>
+                : diag == 4 ? batched_kl_i8_pp_kernel<kS, kMaxL, 4>
+                : diag == 6 ? batched_kl_i8_pp_kernel<kS, kMaxL, 6>
+                : diag == 7 ? batched_kl_i8_pp_kernel<kS, kMaxL, 7>
+                            : batched_kl_i8_pp_kernel<kS, kMaxL, 0>;
+    if (int e = ensure_smem((const void *)kern, kP2Smem)) return e;
     const unsigned ttiles = static_cast<unsigned>((T + kP2BN - 1) / kP2BN);
     const unsigned row_pairs = (tiles + 1) / 2;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(quad ? 4 * ((ttiles + 1) / 2) : 2 * ttiles, row_pairs, 1);
+    cfg.gridDim = dim3(2, 1, 1);   // for the occupancy query
     cfg.blockDim = dim3(kO2Threads, 1, 1);
     cfg.dynamicSmemBytes = kP2Smem;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = quad ? 4 : 2;
+    attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int clusters = 0;
-    const cudaError_t oe = cudaOccupancyMaxActiveClusters(&clusters, kfn, &cfg);
+    const cudaError_t oe = cudaOccupancyMaxActiveClusters(&clusters, (const void *)kern, &cfg);
     if (oe != cudaSuccess || clusters == 0) {
       cudaGetLastError();
       return fail(PF_E_LAUNCH, "batched_kl_i8_pair: no CTA pair fits an SM pair (%s, %d)",
                   cudaGetErrorString(oe), clusters);
     }
-    cudaError_t le;
-    if (persistent) {
-      const long long ntiles = static_cast<long long>(row_pairs) * ttiles;
-      if (ntiles > INT32_MAX) return fail(PF_E_DOMAIN, "batched_kl_i8_pair: too many tiles");
-      const unsigned ncl = static_cast<unsigned>(ntiles < clusters ? ntiles : clusters);
-      cfg.gridDim = dim3(2 * ncl, 1, 1);
-      le = cudaLaunchKernelEx(&cfg, kernp, m[0], m[1], m[2], m[3], ea, eb, rows, T, nkb, H,
-                              targets, tau, row0, out, ldo, static_cast<int>(ttiles),
-                              static_cast<int>(ntiles));
-    } else {
-      le = cudaLaunchKernelEx(&cfg, kern, m[0], m[1], m[2], m[3], ea, eb, rows, T, nkb, H, targets,
-                              tau, row0, out, ldo);
-    }
+    const long long ntiles = static_cast<long long>(row_pairs) * ttiles;
+    if (ntiles > INT32_MAX) return fail(PF_E_DOMAIN, "batched_kl_i8_pair: too many tiles");
+    const unsigned ncl = static_cast<unsigned>(ntiles < clusters ? ntiles : clusters);
+    cfg.gridDim = dim3(2 * ncl, 1, 1);
+    const cudaError_t le = cudaLaunchKernelEx(&cfg, kern, m[0], m[1], m[2], m[3], ea, eb, rows, T,
+                                              nkb, H, targets, tau, row0, out, ldo,
+                                              static_cast<int>(ttiles), static_cast<int>(ntiles));
     if (le != cudaSuccess)
       return fail(static_cast<int>(le), "batched_kl_i8_pair: %s", cudaGetErrorString(le));
     return check_launch("batched_kl_i8_pair");
@@ -1006,16 +825,10 @@ int pf_batched_kl_i8(const uint8_t *A, const int32_t *ea, int64_t rows, const ui
     return fail(PF_E_ALIGN, "batched_kl_i8: slice planes must be 16-byte aligned");
   const int64_t row_tiles = (rows + 127) / 128;
   if (row_tiles > 65535) return fail(PF_E_DOMAIN, "batched_kl_i8: too many rows per launch");
-  if (cta_pair < 0 || cta_pair > 3)
-    return fail(PF_E_ARG, "batched_kl_i8: cta_pair must be 0 .. 3");
-  const int pair = cta_pair;
+  const bool pair = cta_pair != 0;
   const uint32_t bn = pair ? kP2HalfN : kO2BN;   // each CTA of a pair loads half the targets
   CUtensorMap m[4];
-  if (pair == 2) {   // multicast halves: 64-row boxes, one slice each
-    if (int e = slice_map(&m[0], A, rows, ldk, 64, kO2BK, 1)) return e;
-  } else if (int e = slice_map(&m[0], A, rows, ldk, 128, kO2BK, kS)) {
-    return e;
-  }
+  if (int e = slice_map(&m[0], A, rows, ldk, 128, kO2BK, kS)) return e;
   if (int e = slice_map(&m[1], A, rows, ldk, 128, kO2BK, kO2Pass1Slices)) return e;
   if (int e = slice_map(&m[2], B, T, ldk, bn, kO2BK, kS)) return e;
   if (int e = slice_map(&m[3], B, T, ldk, bn, kO2BK, kO2Pass1Slices)) return e;

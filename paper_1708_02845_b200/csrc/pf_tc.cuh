@@ -80,6 +80,11 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
                  "=r"(v[6]), "=r"(v[7])
                : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t (&v)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+               : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -155,30 +160,6 @@ __device__ __forceinline__ void tmem_alloc_pair(uint32_t *dst) {
 template <int kCols>
 __device__ __forceinline__ void tmem_free_pair(uint32_t base) {
   asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(base), "n"(kCols));
-}
-
-// Arrive once on `bar` (same offset) in every CTA of `mask` (cluster ranks)
-// when every previously issued tcgen05.mma of this pair has completed.
-__device__ __forceinline__ void commit_pair_mask(uint64_t *bar, uint16_t mask) {
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
-      " [%0], %1;" ::"r"(smem_u32(bar)),
-      "h"(mask)
-      : "memory");
-}
-
-// TMA 3-D load multicast to the CTAs of `mask` (same shared-memory offset in
-// each); the transaction bytes complete on the mbarrier at `bar`'s offset in
-// the leader of each destination CTA's pair (CUTLASS SM100_TMA_2SM_LOAD_MULTICAST).
-__device__ __forceinline__ void tma_load_3d_pair_mc(void *dst, const CUtensorMap *map, int32_t c0,
-                                                    int32_t c1, int32_t c2, uint64_t *bar,
-                                                    uint16_t mask) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::"
-      "bytes.multicast::cluster [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1),
-      "r"(c2), "h"(mask)
-      : "memory");
 }
 
 // TMA 3-D load by either CTA of the pair into its own shared memory; the

@@ -37,6 +37,104 @@ __device__ __forceinline__ bool mbar_try(uint64_t *bar, uint32_t phase) {
   return ok != 0;
 }
 
+template <bool kPair, int kMode>
+__device__ __forceinline__ void pass1_bursts(int bursts, uint32_t a0, uint32_t tm, uint32_t id,
+                                             uint64_t *full_bar, uint64_t *empty_bar,
+                                             uint64_t *junk_bar, uint64_t *ready_bar,
+                                             volatile uint32_t *flag) {
+  constexpr int kTileA = 128 * 32, kTileB = (kPair ? 64 : 128) * 32;
+  bool ready = false;
+  uint32_t seen = 0;
+  for (int it = 0; it < bursts; ++it) {
+    if constexpr (kMode == 31 || kMode == 32) {
+      if (seen < static_cast<uint32_t>(it + 1)) {   // rare: spin until the watcher saw it
+        do { seen = *flag; } while (seen < static_cast<uint32_t>(it + 1));
+      }
+      tc::fence_after();
+      seen = *flag;   // read early; consumed at the next stage boundary
+    }
+    if constexpr (kMode == 16) {
+      if (!ready) mbar_wait(&full_bar[it % 5], (it / 5) & 1);
+    }
+    if constexpr (kMode >= 20 && kMode < 30) {   // busy-wait (kMode - 20) * 100 clk per burst
+      const long long t0 = clock64();
+      while (clock64() - t0 < (kMode - 20) * 100) {}
+    }
+    if constexpr (kMode == 11) mbar_wait(ready_bar, 0);
+    if constexpr (kMode == 12) {
+      asm volatile("{\n\t.reg .pred p;\nS_%=:\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%0], 0;"
+                   "\n\t@!p bra S_%=;\n}" ::"r"(smem_u32(ready_bar)) : "memory");
+    }
+    if constexpr (kMode == 13) {
+      while (*flag == 0) {}
+    }
+    if constexpr (kMode == 14) mbar_wait(&full_bar[it % 5], (it / 5) & 1);
+    if constexpr (kMode == 33) mbar_wait(ready_bar, 0);
+    if constexpr (kMode == 34) seen += *flag;
+    if constexpr (kMode != 33) tc::fence_after();
+    const uint32_t sa = a0 + (it % 5) * 43008, sbb = sa + 7 * kTileA;
+#pragma unroll
+    for (int i = 1; i <= 4; ++i)
+#pragma unroll
+      for (int j = 1; j <= 4; ++j) {
+        if (i + j > 5) continue;
+        const uint32_t d = tm + (i + j - 2) * 128;
+        const uint64_t da = tc::sdesc<32>(sa + (i - 1) * kTileA);
+        const uint64_t db = tc::sdesc<32>(sbb + (j - 1) * kTileB);
+        if constexpr (kPair) tc::mma_i8_pair(d, da, db, id, true);
+        else tc::mma_i8(d, da, db, id, true);
+        if constexpr (kMode == 16) {
+          if (i == 1 && j == 2) {   // look ahead: the next stage's barrier, non-blocking
+            uint32_t ok;
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                "selp.u32 %0, 1, 0, p;\n\t}"
+                : "=r"(ok)
+                : "r"(smem_u32(&full_bar[(it + 1) % 5])), "r"(((it + 1) / 5) & 1)
+                : "memory");
+            ready = ok != 0;
+          }
+        }
+      }
+    if constexpr (kMode >= 14 && kMode != 31) {
+      if constexpr (kPair) tc::commit_pair(&empty_bar[it % 5]);
+      else tc::commit(&empty_bar[it % 5]);
+    } else {
+      if constexpr (kPair) tc::commit_pair(junk_bar);
+      else tc::commit(junk_bar);
+    }
+  }
+}
+
+// kMode 35: mode 11 with the ring unrolled by 5 (stage offsets compile-time)
+template <bool kPair, int kWaitKind>
+__device__ __forceinline__ void pass1_bursts_unrolled(int bursts, uint32_t a0, uint32_t tm,
+                                                      uint32_t id, uint64_t *ready_bar,
+                                                      uint64_t *junk_bar) {
+  constexpr int kTileA = 128 * 32, kTileB = (kPair ? 64 : 128) * 32;
+  for (int it0 = 0; it0 < bursts; it0 += 5) {
+#pragma unroll
+    for (int st = 0; st < 5; ++st) {
+      if constexpr (kWaitKind == 1) mbar_wait(ready_bar, 0);
+      tc::fence_after();
+      const uint32_t sa = a0 + st * 43008, sbb = sa + 7 * kTileA;
+#pragma unroll
+      for (int i = 1; i <= 4; ++i)
+#pragma unroll
+        for (int j = 1; j <= 4; ++j) {
+          if (i + j > 5) continue;
+          const uint32_t d = tm + (i + j - 2) * 128;
+          const uint64_t da = tc::sdesc<32>(sa + (i - 1) * kTileA);
+          const uint64_t db = tc::sdesc<32>(sbb + (j - 1) * kTileB);
+          if constexpr (kPair) tc::mma_i8_pair(d, da, db, id, true);
+          else tc::mma_i8(d, da, db, id, true);
+        }
+      if constexpr (kPair) tc::commit_pair(junk_bar);
+      else tc::commit(junk_bar);
+    }
+  }
+}
+
 // kPair: cta_group::2 (M256, B split 50/50); kN: MMA N; kSW: swizzle bytes =
 // K bytes per slice row (32: K7's layout; 128: 4 K-steps per slice pair)
 template <bool kPair, int kN, int kSW>
@@ -52,7 +150,8 @@ __global__ void __launch_bounds__(384, 1)
   constexpr int kAcc = 512 / kN;                        // accumulators that fit TMEM
   uint8_t *sa = smem, *sb = smem + kS * kTileA, *scratch = sb + kS * kTileB;
   __shared__ __align__(8) uint64_t done_bar, ring_bar[kRing], junk_bar, spin_bar;
-  __shared__ __align__(8) uint64_t full_bar[5], empty_bar[5];
+  __shared__ __align__(8) uint64_t full_bar[5], empty_bar[5], ready_bar;
+  __shared__ uint32_t flag;
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5;
   const uint32_t rank = kPair ? tc::cluster_rank() : 0;
@@ -69,6 +168,9 @@ __global__ void __launch_bounds__(384, 1)
     mbar_init(&done_bar, 1);
     mbar_init(&junk_bar, 1 << 20);
     mbar_init(&spin_bar, 1);
+    mbar_init(&ready_bar, 1);
+    mbar_arrive(&ready_bar);   // phase 0 complete from the start
+    flag = mode == 32 ? 0u : 1u << 30;
     for (int q = 0; q < 5; ++q) {
       mbar_init(&full_bar[q], 1);
       mbar_init(&empty_bar[q], 1);
@@ -88,7 +190,30 @@ __global__ void __launch_bounds__(384, 1)
   if (warp == 0 && tid == 0 && rank == 0) {
     constexpr uint32_t id = tc::idesc_i8(kPair ? 256 : 128, kN, false, false);
     const uint32_t a0 = smem_u32(sa), b0 = smem_u32(sb);
-    if (mode >= 5 && mode != 6 && kSW == 32 && kN == 128) {   // pass 1 over a rotating 5-stage ring
+    if (mode >= 10 && kSW == 32 && kN == 128) {
+      const int b = iters * 34 / 10;
+      if (mode == 10) pass1_bursts<kPair, 10>(b, a0, tm, id, full_bar, empty_bar, &junk_bar, &ready_bar, &flag);
+      if (mode == 11) pass1_bursts<kPair, 11>(b, a0, tm, id, full_bar, empty_bar, &junk_bar, &ready_bar, &flag);
+      if (mode == 12) pass1_bursts<kPair, 12>(b, a0, tm, id, full_bar, empty_bar, &junk_bar, &ready_bar, &flag);
+      if (mode == 13) pass1_bursts<kPair, 13>(b, a0, tm, id, full_bar, empty_bar, &junk_bar, &ready_bar, &flag);
+      if (mode == 14) pass1_bursts<kPair, 14>(b, a0, tm, id, full_bar, empty_bar, &junk_bar, &ready_bar, &flag);
+      if (mode == 15) pass1_bursts<kPair, 15>(b, a0, tm, id, full_bar, empty_bar, &junk_bar, &ready_bar, &flag);
+      if (mode == 16) pass1_bursts<kPair, 16>(b, a0, tm, id, full_bar, empty_bar, &junk_bar, &ready_bar, &flag);
+      if (mode == 21) pass1_bursts<kPair, 21>(b, a0, tm, id, full_bar, empty_bar, &junk_bar, &ready_bar, &flag);
+      if (mode == 22) pass1_bursts<kPair, 22>(b, a0, tm, id, full_bar, empty_bar, &junk_bar, &ready_bar, &flag);
+      if (mode == 23) pass1_bursts<kPair, 23>(b, a0, tm, id, full_bar, empty_bar, &junk_bar, &ready_bar, &flag);
+      if (mode == 24) pass1_bursts<kPair, 24>(b, a0, tm, id, full_bar, empty_bar, &junk_bar, &ready_bar, &flag);
+      if (mode == 26) pass1_bursts<kPair, 26>(b, a0, tm, id, full_bar, empty_bar, &junk_bar, &ready_bar, &flag);
+      if (mode == 31) pass1_bursts<kPair, 31>(b, a0, tm, id, full_bar, empty_bar, &junk_bar, &ready_bar, &flag);
+      if (mode == 32) pass1_bursts<kPair, 32>(b, a0, tm, id, full_bar, empty_bar, &junk_bar, &ready_bar, &flag);
+      if (mode == 33) pass1_bursts<kPair, 33>(b, a0, tm, id, full_bar, empty_bar, &junk_bar, &ready_bar, &flag);
+      if (mode == 34) {
+        pass1_bursts<kPair, 34>(b, a0, tm, id, full_bar, empty_bar, &junk_bar, &ready_bar, &flag);
+      }
+      if (mode == 35) pass1_bursts_unrolled<kPair, 1>(b, a0, tm, id, &ready_bar, &junk_bar);
+      if (mode == 36) pass1_bursts_unrolled<kPair, 0>(b, a0, tm, id, &ready_bar, &junk_bar);
+      if (mode == 29) pass1_bursts<kPair, 29>(b, a0, tm, id, full_bar, empty_bar, &junk_bar, &ready_bar, &flag);
+    } else if (mode >= 5 && mode != 6 && kSW == 32 && kN == 128) {   // pass 1 over a rotating 5-stage ring
       for (int it = 0; it < iters * 34 / 10; ++it) {
         if (mode == 7) mbar_wait(&full_bar[it % 5], (it / 5) & 1);
         const uint32_t sa = a0 + off + (it % 5) * stride, sbb = sa + 7 * kTileA;
@@ -177,7 +302,12 @@ __global__ void __launch_bounds__(384, 1)
     }
     if constexpr (kPair) tc::commit_pair(&done_bar);
     else tc::commit(&done_bar);
-  } else if (warp == 1 && tid == 32 && mode >= 7) {
+  } else if (warp == 2 && tid == 64 && mode == 32 && rank == 0) {
+    for (int it = 0; it < iters * 34 / 10; ++it) {   // watcher: publish full stages
+      mbar_wait(&full_bar[it % 5], (it / 5) & 1);
+      asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(smem_u32(&flag)), "r"(it + 1) : "memory");
+    }
+  } else if (warp == 1 && tid == 32 && (mode == 7 || mode == 8 || (mode >= 14 && mode <= 30))) {
     // K7's ring handshake without loads: wait the slot's MMA commit, arrive
     for (int it = 0; it < iters * 34 / 10; ++it) {
       const int q = it % 5;
@@ -224,6 +354,43 @@ __global__ void __launch_bounds__(384, 1)
   if (warp == 0) {
     if constexpr (kPair) tc::tmem_free_pair<512>(tm);
     else tc::tmem_free<512>(tm);
+  }
+}
+
+
+// TMA ingest throughput per SM: a producer streaming 3-D boxes {box_k bytes,
+// 128 rows, 7 slices} of a [7][rows][ldk] u8 slice array (K7's A operand
+// shape) vs 1-D bulk copies of the same bytes, 4-deep ring, all SMs.
+__global__ void __launch_bounds__(128, 1)
+    tma_rate_kernel(const __grid_constant__ CUtensorMap map, const uint8_t *flat, int64_t flat_bytes,
+                    int iters, int box_k, int bulk, unsigned long long *cycles) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  __shared__ __align__(8) uint64_t bar[4];
+  const int tid = threadIdx.x;
+  const uint32_t bytes = 7u * 128u * static_cast<uint32_t>(box_k);
+  if (tid == 0) {
+    for (int i = 0; i < 4; ++i) mbar_init(&bar[i], 1);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const unsigned long long c0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      const int s = it & 3;
+      if (it >= 4) mbar_wait(&bar[s], ((it >> 2) - 1) & 1);
+      mbar_expect_tx(&bar[s], bytes);
+      const int kb = (it * 7 + blockIdx.x * 13) % 120;
+      const int rt = (blockIdx.x * 37 + it / 120) % 256;
+      if (bulk) {
+        const int64_t off = ((static_cast<int64_t>(rt) * 120 + kb) * bytes) % (flat_bytes - bytes);
+        bulk_g2s(smem + s * 65536, flat + (off & ~15ll), bytes, &bar[s]);
+      } else {
+        tc::tma_load_3d(smem + s * 65536, &map, kb * box_k, rt * 128, 0, &bar[s]);
+      }
+    }
+    for (int it = iters - 4; it < iters; ++it) mbar_wait(&bar[it & 3], (it >> 2) & 1);
+    cycles[blockIdx.x] = clock64() - c0;
   }
 }
 
@@ -282,6 +449,62 @@ void run(const char *name, int tma_per_iter, const uint8_t *gsrc, int64_t gbytes
          name, tma_per_iter * 34 / mmas, best, ops / (best * 1e-3) / 1e12, per_sm_mma_clk,
          (kPair ? 256 : 128) * kN * 32 / (kPair ? 2 : 1) / 8192,
          tma_c > 0 ? double(tma_per_iter) * iters / tma_c : 0.0);
+  fflush(stdout);
+}
+
+#include <cudaTypedefs.h>
+static void tma_rate(int box_k, int bulk) {
+  const int64_t rows = 256 * 128, ldk = 4160;   // 7 x 32768 x 4160 = 954 MB (> L2)
+  uint8_t *A;
+  CK(cudaMalloc(&A, 7 * rows * ldk));
+  CK(cudaMemset(A, 3, 7 * rows * ldk));
+  void *fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+  auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  CUtensorMap map;
+  cuuint64_t dims[3] = {(cuuint64_t)ldk, (cuuint64_t)rows, 7};
+  cuuint64_t strides[2] = {(cuuint64_t)ldk, (cuuint64_t)(rows * ldk)};
+  cuuint32_t box[3] = {(cuuint32_t)box_k, 128, 7};
+  cuuint32_t es[3] = {1, 1, 1};
+  const CUtensorMapSwizzle sw = box_k == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : box_k == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                              : CU_TENSOR_MAP_SWIZZLE_32B;
+  if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, A, dims, strides, box, es,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+    printf("encode failed\n");
+    exit(1);
+  }
+  unsigned long long *cyc;
+  CK(cudaMalloc(&cyc, 148 * 8));
+  const int smem = 4 * 65536 > 227 * 1024 ? 3 * 65536 : 4 * 65536;
+  CK(cudaFuncSetAttribute(tma_rate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 57344 + 1024));
+  const int iters = 2000;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  float best = 1e30f;
+  for (int rep = 0; rep < 3; ++rep) {
+    CK(cudaEventRecord(e0));
+    tma_rate_kernel<<<148, 128, 4 * 57344 + 1024>>>(map, A, 7 * rows * ldk, iters, box_k, bulk, cyc);
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    float ms;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    if (ms < best) best = ms;
+  }
+  std::vector<unsigned long long> h(148);
+  CK(cudaMemcpy(h.data(), cyc, 148 * 8, cudaMemcpyDeviceToHost));
+  double mx = 0;
+  for (auto v : h) mx = mx > v ? mx : v;
+  const double bytes = 7.0 * 128 * box_k * iters;
+  printf("{\"tma_rate\": \"%s box_k %d\", \"ms\": %.3f, \"chip_TBps\": %.2f, \"B_per_clk_per_sm\": %.1f}\n",
+         bulk ? "bulk" : "tensor3d", box_k, best, bytes * 148 / (best * 1e-3) / 1e12, bytes / mx);
+  fflush(stdout);
+  CK(cudaFree(A));
+  CK(cudaFree(cyc));
+  (void)smem;
 }
 
 int main() {
@@ -295,12 +518,15 @@ int main() {
   CK(cudaMalloc(&cyc, 2 * 148 * 8));
   CK(cudaMemset(cyc, 0, 2 * 148 * 8));
   // K7 per CTA per 34 MMAs: 1-CTA 11 slices x 8 KB = 88 KB, pair 11 x 6 KB = 66 KB
-  for (int off = 0; off < 4096; off += 1024)
-    for (int stride = 43008; stride <= 45056; stride += 2048) {
-      char nm[96];
-      snprintf(nm, sizeof nm, "pair mode 5 stage stride %d base offset %d", stride, off);
-      run<true, 128, 32>(nm, 0, gsrc, gbytes, sink, cyc, 5, 0, 0, stride, off);
-    }
+  tma_rate(32, 0);
+  tma_rate(32, 1);
+  tma_rate(64, 0);
+  return 0;
+  for (int m : {10, 11, 35, 36}) {
+    char nm[96];
+    snprintf(nm, sizeof nm, "pair pass-1 bursts mode %d", m);
+    run<true, 128, 32>(nm, 0, gsrc, gbytes, sink, cyc, m, 0, 0);
+  }
   return 0;
   for (int m = 2; m <= 8; ++m) {
     if (m == 3 || m == 4 || m == 6) continue;
