@@ -158,6 +158,25 @@ __host__ __device__ inline size_t staged_smem_bytes(int64_t k_pad, int64_t m_pad
   return 16 + static_cast<size_t>(k_pad) * 8 + static_cast<size_t>(m_pad);
 }
 
+// One pair of row entries against the staged target (KL: logs, TV: values)
+// and its below-clamp mask.  max(x, clamp) as a select on the same compare
+// the clamp flag needs (fmax's NaN handling cost ~6 ALU instructions per
+// entry; P holds no NaNs, and for non-NaN inputs the values are identical).
+__device__ __forceinline__ void kl_pair(double2 v, double2 lt, uchar2 m, double clamp, double &a0,
+                                        double &a1, bool &fl) {
+  const bool bx = v.x < clamp, by = v.y < clamp;
+  a0 = fma(bx ? clamp : v.x, lt.x, a0);
+  a1 = fma(by ? clamp : v.y, lt.y, a1);
+  fl |= (bx != (m.x != 0)) | (by != (m.y != 0));
+}
+__device__ __forceinline__ void tv_pair(double2 v, double2 t, uchar2 m, double clamp, double &a0,
+                                        double &a1, bool &fl) {
+  const bool bx = v.x < clamp, by = v.y < clamp;
+  a0 += fabs((bx ? clamp : v.x) - t.x);
+  a1 += fabs((by ? clamp : v.y) - t.y);
+  fl |= (bx != (m.x != 0)) | (by != (m.y != 0));
+}
+
 // ------------------------------------------------------------ K2 dense KL --
 template <int U, int MINB, bool STAGE = true, bool GUARD = true>
 __global__ void __launch_bounds__(kThreads, MINB) dense_kl_kernel(
@@ -180,6 +199,7 @@ __global__ void __launch_bounds__(kThreads, MINB) dense_kl_kernel(
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t npair = k >> 1;
+  const int np = static_cast<int>(npair), nfull = np / (32 * U) * (32 * U);
   bool clamped_any = false;
 
   // guarded rows cluster in runs of consecutive rows: inside each block of
@@ -191,25 +211,18 @@ __global__ void __launch_bounds__(kThreads, MINB) dense_kl_kernel(
     const double h = H[r];  // issued ahead of the row stream
     double a0 = 0.0, a1 = 0.0;
     bool fl = false;
-    for (int64_t j0 = 0; j0 < npair; j0 += 32 * U) {
+    for (int j0 = lane; j0 < nfull; j0 += 32 * U) {   // full chunks: no bounds checks
       double2 v[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t j = j0 + lane + 32 * u;
-        v[u] = (j < npair) ? ldg_stream2(row + j) : make_double2(1.0, 1.0);
-      }
+      for (int u = 0; u < U; ++u) v[u] = ldg_stream2(row + j0 + 32 * u);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int64_t j = j0 + lane + 32 * u;
-        if (j < npair) {
-          const double2 lt = lt2[j];
-          const uchar2 m = m2[j];
-          a0 = fma(fmax(v[u].x, clamp), lt.x, a0);
-          a1 = fma(fmax(v[u].y, clamp), lt.y, a1);
-          fl |= ((v[u].x < clamp) != (m.x != 0)) | ((v[u].y < clamp) != (m.y != 0));
-        }
+        const double2 lt = lt2[j0 + 32 * u];
+        const uchar2 m = m2[j0 + 32 * u];
+        kl_pair(v[u], lt, m, clamp, a0, a1, fl);
       }
     }
+    for (int j = nfull + lane; j < np; j += 32) kl_pair(ldg_stream2(row + j), lt2[j], m2[j], clamp, a0, a1, fl);
     if ((k & 1) && lane == 0) {
       const double x = P[r * ld + k - 1];
       a0 = fma(fmax(x, clamp), st.vec[k - 1], a0);
@@ -251,31 +264,25 @@ __global__ void __launch_bounds__(kThreads, MINB) dense_tv_kernel(
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t npair = k >> 1;
+  const int np = static_cast<int>(npair), nfull = np / (32 * U) * (32 * U);
   bool clamped_any = false;
 
   for (int64_t r = warp; r < rows; r += nwarps) {
     const double2 *row = reinterpret_cast<const double2 *>(P + r * ld);
     double a0 = 0.0, a1 = 0.0;
     bool fl = false;
-    for (int64_t j0 = 0; j0 < npair; j0 += 32 * U) {
+    for (int j0 = lane; j0 < nfull; j0 += 32 * U) {   // full chunks: no bounds checks
       double2 v[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t j = j0 + lane + 32 * u;
-        v[u] = (j < npair) ? ldg_stream2(row + j) : make_double2(1.0, 1.0);
-      }
+      for (int u = 0; u < U; ++u) v[u] = ldg_stream2(row + j0 + 32 * u);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int64_t j = j0 + lane + 32 * u;
-        if (j < npair) {
-          const double2 t = t2[j];
-          const uchar2 m = m2[j];
-          a0 += fabs(fmax(v[u].x, clamp) - t.x);
-          a1 += fabs(fmax(v[u].y, clamp) - t.y);
-          fl |= ((v[u].x < clamp) != (m.x != 0)) | ((v[u].y < clamp) != (m.y != 0));
-        }
+        const double2 t = t2[j0 + 32 * u];
+        const uchar2 m = m2[j0 + 32 * u];
+        tv_pair(v[u], t, m, clamp, a0, a1, fl);
       }
     }
+    for (int j = nfull + lane; j < np; j += 32) tv_pair(ldg_stream2(row + j), t2[j], m2[j], clamp, a0, a1, fl);
     if ((k & 1) && lane == 0) {
       const double x = P[r * ld + k - 1];
       a0 += fabs(fmax(x, clamp) - st.vec[k - 1]);

@@ -14,6 +14,7 @@
 // the reference's per-element form, evaluated by the whole CTA after its
 // loop exactly as the FP64 kernel does (pf_common.cuh GuardQueue).  Unflagged
 // rows carry <= 6e-6 relative error by the bound above.
+#include <cfloat>
 #include <cmath>
 
 #include "pf_common.cuh"
@@ -49,9 +50,16 @@ __global__ void __launch_bounds__(kT32) row_negentropy32_kernel(const float *__r
   }
 }
 
-template <bool KL>
-__device__ __forceinline__ void acc32(double q_raw, double t, double clamp, double &a) {
-  const double q = fmax(q_raw, clamp);
+// One element: q = max(stored FP32 entry, clamp) in FP32 (clamp rounded to FP32
+// -- below FLT_MIN it is 0 and the max is skipped: P >= 0), widened to FP64.
+// The FP32 clamp moves a clamped term by at most eps32 relative (the same
+// order as the FP32 storage of P, inside the guard bound below), or by the
+// clamp itself (< FLT_MIN, i.e. < 1.2e-38 absolute per entry).  fmax in FP64
+// compiled to ~6 ALU instructions of NaN handling per element and left the
+// kernel ALU-bound (ncu: ALU pipe ~80% at speed, DRAM 84%).
+template <bool KL, bool CLAMP>
+__device__ __forceinline__ void acc32(float q_raw, double t, float clamp32, double &a) {
+  const double q = static_cast<double>(CLAMP ? fmaxf(q_raw, clamp32) : q_raw);
   if (KL)
     a = fma(q, t, a);  // t = log c(Pt)
   else
@@ -106,11 +114,11 @@ static __device__ __noinline__ double cross64_row(const double *__restrict__ pro
   return warp_sum(a0 + a1);
 }
 
-template <bool KL>
+template <bool KL, bool CLAMP>
 __global__ void __launch_bounds__(kT32, 4) dense32_kernel(
     const float *__restrict__ P, int64_t ld, int64_t rows, int64_t k,
-    const double *__restrict__ H, const double *__restrict__ vec, double clamp, double tau,
-    int64_t row0, int64_t target, const double *__restrict__ P64, int64_t ld64,
+    const double *__restrict__ H, const double *__restrict__ vec, double clamp, float clamp32,
+    double tau, int64_t row0, int64_t target, const double *__restrict__ P64, int64_t ld64,
     const double *__restrict__ H64, double tau64, const double *__restrict__ tgt,
     double *__restrict__ out, uint32_t *__restrict__ flags, int64_t warp_mul) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -131,32 +139,36 @@ __global__ void __launch_bounds__(kT32, 4) dense32_kernel(
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   constexpr int U = 4;
+  const int nq = static_cast<int>(nq4);                    // < 2^31 (k <= 25,600)
+  const int nfull = nq / (32 * U) * (32 * U);               // chunks with every lane in range
   const int64_t first = (warp * warp_mul) % nwarps;  // scattered rows (pf_common.cuh)
   for (int64_t r = first; r < rows; r += nwarps) {
     const float4 *row = reinterpret_cast<const float4 *>(P + r * ld);
     const double h = KL ? H[r] : 0.0;
     double a0 = 0.0, a1 = 0.0;
-    for (int64_t j0 = 0; j0 < nq4; j0 += 32 * U) {
+    for (int j0 = lane; j0 < nfull; j0 += 32 * U) {   // no bounds checks in the hot loop
       float4 v[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t j = j0 + lane + 32 * u;
-        v[u] = j < nq4 ? ldg_stream4f(row + j) : make_float4(1.f, 1.f, 1.f, 1.f);
-      }
+      for (int u = 0; u < U; ++u) v[u] = ldg_stream4f(row + j0 + 32 * u);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int64_t j = j0 + lane + 32 * u;
-        if (j < nq4) {
-          const double2 t01 = lo[j], t23 = hi[j];
-          acc32<KL>(v[u].x, t01.x, clamp, a0);
-          acc32<KL>(v[u].y, t01.y, clamp, a1);
-          acc32<KL>(v[u].z, t23.x, clamp, a0);
-          acc32<KL>(v[u].w, t23.y, clamp, a1);
-        }
+        const double2 t01 = lo[j0 + 32 * u], t23 = hi[j0 + 32 * u];
+        acc32<KL, CLAMP>(v[u].x, t01.x, clamp32, a0);
+        acc32<KL, CLAMP>(v[u].y, t01.y, clamp32, a1);
+        acc32<KL, CLAMP>(v[u].z, t23.x, clamp32, a0);
+        acc32<KL, CLAMP>(v[u].w, t23.y, clamp32, a1);
       }
     }
+    for (int j = nfull + lane; j < nq; j += 32) {   // the ragged chunk
+      const float4 v = ldg_stream4f(row + j);
+      const double2 t01 = lo[j], t23 = hi[j];
+      acc32<KL, CLAMP>(v.x, t01.x, clamp32, a0);
+      acc32<KL, CLAMP>(v.y, t01.y, clamp32, a1);
+      acc32<KL, CLAMP>(v.z, t23.x, clamp32, a0);
+      acc32<KL, CLAMP>(v.w, t23.y, clamp32, a1);
+    }
     for (int64_t b = 4 * nq4 + lane; b < k; b += 32)  // ragged tail (< 4 columns)
-      acc32<KL>(static_cast<double>(P[r * ld + b]), tail[b - 4 * nq4], clamp, a0);
+      acc32<KL, CLAMP>(P[r * ld + b], tail[b - 4 * nq4], clamp32, a0);
     const double s = warp_sum(a0 + a1);
     const bool is_t = (row0 + r == target);
     double val;
@@ -223,7 +235,9 @@ static int launch32(const float *P, int64_t ld, int64_t rows, int64_t k, const d
   size_t smem = static_cast<size_t>(k) * 8 + 32;
   if (smem < kGuardPartBytes) smem = kGuardPartBytes;
   if (smem > 200 * 1024) return fail(PF_E_DOMAIN, "dense32: k=%lld too large", (long long)k);
-  auto kern = dense32_kernel<KL>;
+  // the clamp in FP32, rounded to nearest; flushed to 0 (no max) below FLT_MIN
+  const float clamp32 = clamp >= static_cast<double>(FLT_MIN) ? static_cast<float>(clamp) : 0.0f;
+  auto kern = clamp32 > 0.0f ? dense32_kernel<KL, true> : dense32_kernel<KL, false>;
   if (int e = ensure_smem((const void *)kern, smem)) return e;
   const int occ = occupancy((const void *)kern, kT32, smem);
   int64_t g = static_cast<int64_t>(sm_count()) * occ, want = (rows + 7) / 8;
@@ -232,8 +246,8 @@ static int launch32(const float *P, int64_t ld, int64_t rows, int64_t k, const d
   if (!P64 || !tgt || !flags) return fail(PF_E_ARG, "dense32: the FP64 guard needs P64, tgt, flags");
   if ((ld64 & 1) || (reinterpret_cast<uintptr_t>(P64) & 15))
     return fail(PF_E_ALIGN, "dense32: FP64 rows must be 16-byte aligned");
-  kern<<<static_cast<int>(g), kT32, smem, stream>>>(P, ld, rows, k, H, vec, clamp, tau, row0,
-                                                    target, P64, ld64, H64, tau64, tgt, out,
+  kern<<<static_cast<int>(g), kT32, smem, stream>>>(P, ld, rows, k, H, vec, clamp, clamp32, tau,
+                                                    row0, target, P64, ld64, H64, tau64, tgt, out,
                                                     flags, guard_warp_mul(g * (kT32 / 32)));
   return check_launch("dense32");  // guarded rows were re-evaluated in place
 }

@@ -246,6 +246,9 @@ def dv_field(pk: PoissonKernel, fd: FDivergence, p: int,
     return ScalarField(vals, fd.name, p, params, 1, None, ("clamped",) if fired else ())
 
 
+from ._hostpool import upload_small  # noqa: E402
+
+
 def dv_at(pk: PoissonKernel, fd: FDivergence, p: int, queries,
           swap_order: bool = False, clamp: float | None = None) -> np.ndarray:
     """Distances from target p to a batch of query vertices (divergence.py:137-151)."""
@@ -262,11 +265,15 @@ def dv_at(pk: PoissonKernel, fd: FDivergence, p: int, queries,
     c = float(clamp)
     gen = _userf.resolve(fd)
     s = t.cuda.current_stream(dk.device)
-    st = _Staging(t, dk.k, dk.device)
+    k_pad, m_pad = dev.round_up(dk.k, 2), dev.round_up(dk.k, 16)
+    st = _Staging(t, dk.k, dk.device, dk.scratch(s.cuda_stream, 16 * k_pad + m_pad, "stage"))
     row = dk.target_row(p)
     nat.call("pf_target_prep_f64", row.data_ptr(), dk.k, c, st.tgt, st.logt, st.tmask, 0,
              s.cuda_stream)
-    qd = t.from_numpy(q).to(dk.device, non_blocking=False)
+    # queries through a pooled pinned buffer (async), scratch-resident on the device
+    qd = dk.scratch(s.cuda_stream, max(8 * q.size, 8), "at_q").view(t.int64)
+    if q.size:
+        upload_small(t, q, qd, s)
     out = t.empty(q.size, dtype=t.float64, device=dk.device)
     if gen[0] == "user":
         nat.call("pf_dense_user_at_f64", gen[1].handle, dk.P.data_ptr(), dk.ld, dk.rows, dk.k,
@@ -277,7 +284,7 @@ def dv_at(pk: PoissonKernel, fd: FDivergence, p: int, queries,
                  gen[2], int(bool(swap_order)), dk.row0, p, qd.data_ptr(), q.size,
                  out.data_ptr(), s.cuda_stream)
     res = _to_host(t, out, s).copy()
-    del st
+    del st, row
     return res
 
 
