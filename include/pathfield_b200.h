@@ -303,6 +303,13 @@ int pf_batched_kl_f64(const double *P, int64_t ld, int64_t rows, int64_t k, cons
 int pf_batched_kl_fixup_f64(const double *P, int64_t ld, int64_t rows, int64_t k,
                             const double *Tc, int64_t ldl, int64_t T, double clamp, double *out,
                             int64_t ldo, uint32_t *guarded, pf_stream_t stream);
+/* The same over the guarded-pair list pf_batched_kl_i8_listed recorded
+ * (guard_list[0] = count, then q * T + t): no scan of the output; a list
+ * that overflowed guard_cap falls back to the scan.  Same values. */
+int pf_batched_kl_fixup_list_f64(const double *P, int64_t ld, int64_t rows, int64_t k,
+                                 const double *Tc, int64_t ldl, int64_t T, double clamp,
+                                 double *out, int64_t ldo, uint32_t *guarded,
+                                 const int64_t *guard_list, int64_t guard_cap, pf_stream_t stream);
 
 /* ---- K7 on the int8 tensor pipe (batched_i8.cu) ----------------------------
  * The same contraction as pf_batched_kl_f64, S = c(P) . (-L)^T, evaluated as
@@ -332,6 +339,14 @@ int pf_batched_kl_i8(const uint8_t *A, const int32_t *ea, int64_t rows, const ui
                      const int32_t *eb, int64_t T, int64_t k, int64_t ldk, const double *H,
                      const int64_t *targets, double tau, int64_t row0, double *out, int64_t ldo,
                      int grade, int cta_pair, pf_stream_t stream);
+/* pf_batched_kl_i8 that also appends every guarded pair to guard_list
+ * (int64[1 + guard_cap]; guard_list[0] is the count and must be zero before
+ * the call): then follow with pf_batched_kl_fixup_list_f64. */
+int pf_batched_kl_i8_listed(const uint8_t *A, const int32_t *ea, int64_t rows, const uint8_t *B,
+                            const int32_t *eb, int64_t T, int64_t k, int64_t ldk, const double *H,
+                            const int64_t *targets, double tau, int64_t row0, double *out,
+                            int64_t ldo, int grade, int cta_pair, int64_t *guard_list,
+                            int64_t guard_cap, pf_stream_t stream);
 
 /* Diagnostic: back-to-back M128 N256 K32 u8 tcgen05.mma on shared-memory
  * operands, one CTA per SM (*ops_host = integer ops issued): the int8 tensor

@@ -65,10 +65,14 @@ _SIGS = {
                           c_dbl, c_i64, c_vp, c_i64, c_vp, c_vp],
     "pf_batched_kl_fixup_f64": [c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_i64, c_dbl, c_vp,
                                 c_i64, c_vp, c_vp],
+    "pf_batched_kl_fixup_list_f64": [c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_i64, c_dbl,
+                                     c_vp, c_i64, c_vp, c_vp, c_i64, c_vp],
     "pf_slice_rows_u8": [c_vp, c_i64, c_i64, c_i64, c_dbl, c_i64, c_vp, c_vp, c_vp],
     "pf_slice_targets_u8": [c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp],
     "pf_batched_kl_i8": [c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_dbl,
                          c_i64, c_vp, c_i64, c_int, c_int, c_vp],
+    "pf_batched_kl_i8_listed": [c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp,
+                                c_dbl, c_i64, c_vp, c_i64, c_int, c_int, c_vp, c_i64, c_vp],
     "pf_probe_umma_i8": [c_i64, c_int, ctypes.POINTER(ctypes.c_int64), c_vp, c_vp],
     "pf_probe_dfma_f64": [c_i64, ctypes.POINTER(ctypes.c_int64), c_vp, c_vp],
     "pf_convert_f32": [c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp],

@@ -234,6 +234,85 @@ __global__ void __launch_bounds__(256) batched_kl_fixup_kernel(
   if (lane == 0 && done && count) atomicAdd(count, done);
 }
 
+// The same per-element reference form over a list of guarded pairs recorded
+// by the K7 epilogue (guard_list[0] = count, then q * T + t entries): no scan
+// of the rows x T output for sentinels (an 8 GB strided read at C5), and two
+// iterations of loads in flight per lane (the fixup was latency-bound: ncu
+// long-scoreboard on the row loads).  The per-lane order of the terms is the
+// scan kernel's, so both give the same values.  A list that overflowed
+// (count > cap) falls back to the scan.
+__device__ __forceinline__ double fixup_pair(const double *__restrict__ prow,
+                                             const double *__restrict__ trow, int64_t k,
+                                             double clamp, int lane) {
+  double b[4] = {0.0, 0.0, 0.0, 0.0};
+  int64_t c = lane;
+  for (; c + 224 < k; c += 256) {   // two 128-element steps, 8 loads in flight
+    double pv[8], tv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      pv[u] = ldg_stream(prow + c + 32 * u);
+      tv[u] = __ldg(trow + c + 32 * u);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const double qv = fmax(pv[u], clamp);
+      b[u & 3] += __dmul_rn(qv, -log(__ddiv_rn(tv[u], qv)));
+    }
+  }
+  for (; c + 96 < k; c += 128) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double qv = fmax(prow[c + 32 * u], clamp);
+      b[u] += __dmul_rn(qv, -log(__ddiv_rn(trow[c + 32 * u], qv)));
+    }
+  }
+  for (; c < k; c += 32) {
+    const double qv = fmax(prow[c], clamp);
+    b[0] += __dmul_rn(qv, -log(__ddiv_rn(trow[c], qv)));
+  }
+  return settle(warp_sum((b[0] + b[1]) + (b[2] + b[3])));
+}
+
+__global__ void __launch_bounds__(256) batched_kl_fixup_list_kernel(
+    const double *__restrict__ P, int64_t ld, int64_t rows, int64_t k,
+    const double *__restrict__ Tc, int64_t ldl, int64_t T, double clamp,
+    double *__restrict__ out, int64_t ldo, uint32_t *__restrict__ count,
+    const int64_t *__restrict__ guard_list, int64_t cap) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t n = guard_list[0];
+  if (n > cap) {   // overflowed: the scan kernel's loop
+    uint32_t done = 0;
+    const int64_t total = rows * T;
+    for (int64_t i0 = 0; warp + i0 * nwarps < total; i0 += 32) {
+      const int64_t mine = warp + (i0 + lane) * nwarps;
+      const int64_t mq = mine / T, mt = mine - mq * T;
+      const bool flag = mine < total && static_cast<unsigned long long>(__double_as_longlong(
+                                            out[mq * ldo + mt])) == kBatchGuard;
+      unsigned ball = __ballot_sync(0xffffffffu, flag);
+      while (ball) {
+        const int src = __ffs(ball) - 1;
+        ball &= ball - 1;
+        const int64_t e = warp + (i0 + src) * nwarps, q = e / T, t = e - q * T;
+        const double val = fixup_pair(P + q * ld, Tc + t * ldl, k, clamp, lane);
+        if (lane == 0) out[q * ldo + t] = val;
+        ++done;
+      }
+    }
+    if (lane == 0 && done && count) atomicAdd(count, done);
+    return;
+  }
+  uint32_t done = 0;
+  for (int64_t i = warp; i < n; i += nwarps) {
+    const int64_t e = guard_list[1 + i], q = e / T, t = e - q * T;
+    const double val = fixup_pair(P + q * ld, Tc + t * ldl, k, clamp, lane);
+    if (lane == 0) out[q * ldo + t] = val;
+    ++done;
+  }
+  if (lane == 0 && done && count) atomicAdd(count, done);
+}
+
 // Diagnostic: sustained DFMA throughput (8 independent chains per thread);
 // bench.py reports K7's FLOP rate against it.
 __global__ void __launch_bounds__(256) dfma_probe_kernel(int64_t iters, double *out) {
@@ -309,6 +388,17 @@ int pf_batched_kl_fixup_f64(const double *P, int64_t ld, int64_t rows, int64_t k
   batched_kl_fixup_kernel<<<sm_count() * 8, 256, 0, as_stream(stream)>>>(
       P, ld, rows, k, Tc, ldl, T, clamp, out, ldo, guarded);
   return check_launch("batched_kl_fixup");
+}
+
+int pf_batched_kl_fixup_list_f64(const double *P, int64_t ld, int64_t rows, int64_t k,
+                                 const double *Tc, int64_t ldl, int64_t T, double clamp,
+                                 double *out, int64_t ldo, uint32_t *guarded,
+                                 const int64_t *guard_list, int64_t guard_cap, pf_stream_t stream) {
+  if (rows <= 0 || T <= 0) return 0;
+  if (!P || !Tc || !out || !guard_list) return fail(PF_E_ARG, "batched_kl_fixup_list: null");
+  batched_kl_fixup_list_kernel<<<sm_count() * 8, 256, 0, as_stream(stream)>>>(
+      P, ld, rows, k, Tc, ldl, T, clamp, out, ldo, guarded, guard_list, guard_cap);
+  return check_launch("batched_kl_fixup_list");
 }
 
 int pf_probe_dfma_f64(int64_t iters, int64_t *flops, double *out, pf_stream_t stream) {

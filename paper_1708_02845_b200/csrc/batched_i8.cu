@@ -161,6 +161,24 @@ __device__ __forceinline__ double pow2_scale(double v, int e) {
   return (v * pow2_exact(e1)) * pow2_exact(e - e1);
 }
 
+// Append the guarded (q, t) pairs of one thread's columns to the fixup list
+// (list[0] = count, then q * T + t; entries past cap are dropped and the
+// fixup falls back to scanning the output for sentinels).
+__device__ __forceinline__ void push_guards(int64_t *list, int64_t cap, uint64_t mask, int64_t q,
+                                            int64_t t0, int64_t T) {
+  if (list == nullptr || mask == 0) return;
+  const int n = __popcll(mask);
+  const int64_t base = static_cast<int64_t>(
+      atomicAdd(reinterpret_cast<unsigned long long *>(list), static_cast<unsigned long long>(n)));
+  int j = 0;
+  while (mask) {
+    const int c = __ffsll(static_cast<long long>(mask)) - 1;
+    mask &= mask - 1;
+    if (base + j < cap) list[1 + base + j] = q * T + t0 + c;
+    ++j;
+  }
+}
+
 // ------------------------------------------------------------------ GEMM --
 // Two passes per 128 x 128 output tile, because TMEM holds four N=128
 // accumulators (4 x 128 columns = all 512): pass 1 = levels 2..5 (10 byte
@@ -184,7 +202,7 @@ __global__ void __launch_bounds__(kO2Threads, 1) batched_kl_i8_n128_kernel(
     const __grid_constant__ CUtensorMap mapB7, const __grid_constant__ CUtensorMap mapB4,
     const int32_t *__restrict__ ea, const int32_t *__restrict__ eb, int64_t rows, int64_t T,
     int nkb, const double *__restrict__ H, const int64_t *__restrict__ targets, double tau,
-    int64_t row0, double *__restrict__ out, int64_t ldo) {
+    int64_t row0, double *__restrict__ out, int64_t ldo, int64_t *guard_list, int64_t guard_cap) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -310,6 +328,7 @@ __global__ void __launch_bounds__(kO2Threads, 1) batched_kl_i8_n128_kernel(
     const int e_q = row_ok ? ea[q] : 0;
     const int64_t tq = row_ok ? row0 + q : -1;
     constexpr int kL2 = kMaxL - 5;  // pass-2 accumulators
+    uint64_t gmask = 0;
 #pragma unroll
     for (int c0 = 0; c0 < 64; c0 += 8) {
       uint32_t acc[kL2][8];
@@ -328,13 +347,16 @@ __global__ void __launch_bounds__(kO2Threads, 1) batched_kl_i8_n128_kernel(
         const double S = pow2_scale(v, e_q + eb[t] - 16);
         double val = h + S;
         const bool is_t = (tq == targets[t]);
-        if (!is_t && fabs(val) < tau * (fabs(h) + fabs(S)))
+        if (!is_t && fabs(val) < tau * (fabs(h) + fabs(S))) {
           val = __longlong_as_double(static_cast<long long>(kOzGuard));
-        else
+          gmask |= 1ull << (c0 + u);
+        } else {
           val = is_t ? 0.0 : settle(val);
+        }
         out[q * ldo + t] = val;
       }
     }
+    push_guards(guard_list, guard_cap, gmask, q, t0 + half * 64, T);
   }
   tc::fence_before();
   __syncthreads();
@@ -387,7 +409,8 @@ __global__ void __launch_bounds__(kO2Threads, 1)
                             const int32_t *__restrict__ ea, const int32_t *__restrict__ eb,
                             int64_t rows, int64_t T, int nkb, const double *__restrict__ H,
                             const int64_t *__restrict__ targets, double tau, int64_t row0,
-                            double *__restrict__ out, int64_t ldo, int t_tiles, int ntiles) {
+                            double *__restrict__ out, int64_t ldo, int t_tiles, int ntiles,
+                            int64_t *guard_list, int64_t guard_cap) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -610,6 +633,7 @@ __global__ void __launch_bounds__(kO2Threads, 1)
       const int64_t tgA = tA < T ? targets[tA] : -1, tgB = tB < T ? targets[tB] : -1;
       double *orow = out + q * ldo + tc0;
       const bool full = row_ok && pairs_ok && tc0 + 64 <= T;
+      uint64_t gmask = 0;
 #pragma unroll
       for (int c = 0; c < 64; c += 2) {
         double o[2];
@@ -626,6 +650,7 @@ __global__ void __launch_bounds__(kO2Threads, 1)
           const double settled = settle(val);
           o[u] = guard ? __longlong_as_double(static_cast<long long>(kOzGuard))
                        : (is_t ? 0.0 : settled);
+          gmask |= static_cast<uint64_t>(guard && tc0 + cc < T) << cc;
         }
         if (full) {
           *reinterpret_cast<double2 *>(orow + c) = make_double2(o[0], o[1]);
@@ -634,6 +659,7 @@ __global__ void __launch_bounds__(kO2Threads, 1)
           if (tc0 + c + 1 < T) orow[c + 1] = o[1];
         }
       }
+      if (row_ok) push_guards(guard_list, guard_cap, gmask, q, tc0, T);
       if (tid == 64) PP_STAMP(k, 9);
     }
   }
@@ -729,7 +755,7 @@ template <int kS, int kMaxL>
 static int launch_i8(const CUtensorMap (&m)[4], const int32_t *ea, const int32_t *eb,
                      int64_t rows, int64_t T, int64_t k, const double *H, const int64_t *targets,
                      double tau, int64_t row0, double *out, int64_t ldo, bool pair,
-                     cudaStream_t stream) {
+                     int64_t *glist, int64_t gcap, cudaStream_t stream) {
   const int nkb = static_cast<int>((k + kO2BK - 1) / kO2BK);
   const unsigned tiles = static_cast<unsigned>((rows + 127) / 128);
   if (pair) {  // a pair's second CTA may hold only out-of-range rows
@@ -772,7 +798,8 @@ static int launch_i8(const CUtensorMap (&m)[4], const int32_t *ea, const int32_t
     cfg.gridDim = dim3(2 * ncl, 1, 1);
     const cudaError_t le = cudaLaunchKernelEx(&cfg, kern, m[0], m[1], m[2], m[3], ea, eb, rows, T,
                                               nkb, H, targets, tau, row0, out, ldo,
-                                              static_cast<int>(ttiles), static_cast<int>(ntiles));
+                                              static_cast<int>(ttiles), static_cast<int>(ntiles),
+                                              glist, gcap);
     if (le != cudaSuccess)
       return fail(static_cast<int>(le), "batched_kl_i8_pair: %s", cudaGetErrorString(le));
     return check_launch("batched_kl_i8_pair");
@@ -780,7 +807,7 @@ static int launch_i8(const CUtensorMap (&m)[4], const int32_t *ea, const int32_t
   if (int e = ensure_smem((const void *)batched_kl_i8_n128_kernel<kS, kMaxL>, kO2Smem)) return e;
   dim3 grid(static_cast<unsigned>((T + kO2BN - 1) / kO2BN), tiles);
   batched_kl_i8_n128_kernel<kS, kMaxL><<<grid, kO2Threads, kO2Smem, stream>>>(
-      m[0], m[1], m[2], m[3], ea, eb, rows, T, nkb, H, targets, tau, row0, out, ldo);
+      m[0], m[1], m[2], m[3], ea, eb, rows, T, nkb, H, targets, tau, row0, out, ldo, glist, gcap);
   return check_launch("batched_kl_i8");
 }
 
@@ -814,6 +841,15 @@ int pf_batched_kl_i8(const uint8_t *A, const int32_t *ea, int64_t rows, const ui
                      const int32_t *eb, int64_t T, int64_t k, int64_t ldk, const double *H,
                      const int64_t *targets, double tau, int64_t row0, double *out, int64_t ldo,
                      int grade, int cta_pair, pf_stream_t stream) {
+  return pf_batched_kl_i8_listed(A, ea, rows, B, eb, T, k, ldk, H, targets, tau, row0, out, ldo,
+                                 grade, cta_pair, nullptr, 0, stream);
+}
+
+int pf_batched_kl_i8_listed(const uint8_t *A, const int32_t *ea, int64_t rows, const uint8_t *B,
+                            const int32_t *eb, int64_t T, int64_t k, int64_t ldk, const double *H,
+                            const int64_t *targets, double tau, int64_t row0, double *out,
+                            int64_t ldo, int grade, int cta_pair, int64_t *guard_list,
+                            int64_t guard_cap, pf_stream_t stream) {
   if (grade != 64 && grade != 32) return fail(PF_E_ARG, "batched_kl_i8: grade must be 64 or 32");
   const int kS = grade == 64 ? kOzSlices : 5;
   if (rows <= 0 || T <= 0) return 0;
@@ -833,9 +869,9 @@ int pf_batched_kl_i8(const uint8_t *A, const int32_t *ea, int64_t rows, const ui
   if (int e = slice_map(&m[2], B, T, ldk, bn, kO2BK, kS)) return e;
   if (int e = slice_map(&m[3], B, T, ldk, bn, kO2BK, kO2Pass1Slices)) return e;
   return grade == 64 ? launch_i8<7, 9>(m, ea, eb, rows, T, k, H, targets, tau, row0, out, ldo,
-                                       pair, as_stream(stream))
+                                       pair, guard_list, guard_cap, as_stream(stream))
                      : launch_i8<5, 6>(m, ea, eb, rows, T, k, H, targets, tau, row0, out, ldo,
-                                       pair, as_stream(stream));
+                                       pair, guard_list, guard_cap, as_stream(stream));
 }
 
 int pf_probe_umma_i8(int64_t iters, int random_operands, int64_t *ops_host, uint32_t *sink,

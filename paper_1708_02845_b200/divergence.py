@@ -381,6 +381,11 @@ I8_MAX_K = 4717  # batched_i8.cu: 7 x k x 255^2 < 2^31
 I8_CTA_PAIR = True
 
 
+def guard_list_cap(rows: int, T: int) -> int:
+    """Entries of the K7 guarded-pair list (a fuller list falls back to the scan)."""
+    return int(min(rows * T, max(1 << 20, rows * T // 128)))
+
+
 def dv_field_batch_device(pk: PoissonKernel, fd: FDivergence, targets, clamp=None,
                           method: str = "auto"):
     """Fields to T targets at once on the device: (values (n, T) tensor, flags (T,) bool array).
@@ -458,13 +463,17 @@ def _kl_batch_slab(dk, tg, Pt, c: float, method: str, out=None):
                 raise ValueError(f"method={method!r}: a target row has an entry above 1")
             use_i8 = False
     if use_i8:
-        nat.call("pf_batched_kl_i8", A.data_ptr(), ea.data_ptr(), dk.rows, B.data_ptr(),
+        # the epilogue lists its guarded pairs; the fixup walks the list
+        cap = guard_list_cap(dk.rows, T)
+        glist = dk.scratch(s.cuda_stream, 8 * (cap + 1), "k7_guards").view(t.int64)
+        glist[:1].zero_()
+        nat.call("pf_batched_kl_i8_listed", A.data_ptr(), ea.data_ptr(), dk.rows, B.data_ptr(),
                  eb.data_ptr(), T, dk.k, ldk, H.data_ptr(), tg.data_ptr(), KL_GUARD_TAU,
                  dk.row0, out.data_ptr(), out.stride(0), 32 if method == "i8-f32" else 64,
-                 int(I8_CTA_PAIR), s.cuda_stream)
-        nat.call("pf_batched_kl_fixup_f64", dk.P.data_ptr(), dk.ld, dk.rows, dk.k,
+                 int(I8_CTA_PAIR), glist.data_ptr(), cap, s.cuda_stream)
+        nat.call("pf_batched_kl_fixup_list_f64", dk.P.data_ptr(), dk.ld, dk.rows, dk.k,
                  Tc.data_ptr(), ldl, T, c, out.data_ptr(), out.stride(0),
-                 tflag.data_ptr() + 4 * T, s.cuda_stream)
+                 tflag.data_ptr() + 4 * T, glist.data_ptr(), cap, s.cuda_stream)
     else:
         nat.call("pf_batched_kl_f64", dk.P.data_ptr(), dk.ld, dk.rows, dk.k, H.data_ptr(),
                  L.data_ptr(), Tc.data_ptr(), ldl, T, tg.data_ptr(), c, KL_GUARD_TAU, dk.row0,

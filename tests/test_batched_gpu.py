@@ -170,3 +170,58 @@ def test_i8_cta_pair_kernel_bitwise_equals_single_cta(rows, k, T):
     torch.cuda.synchronize()
     assert torch.equal(a.view(torch.int64), b.view(torch.int64))
     assert np.array_equal(fa, fb)
+
+
+def test_guard_list_fixup_matches_scan_fixup_and_overflow():
+    """The K7 epilogue's guarded-pair list + list fixup give the scan fixup's
+    values bitwise, with a list that holds every pair and with one that
+    overflows (falls back to the scan)."""
+    import torch
+    from paper_1708_02845_b200 import _device as dev, _native as nat
+    from paper_1708_02845_b200 import divergence as D
+    mesh = I.build({"gen": "holes", "spacing": 0.03, "seed": 1})
+    dense, boundary = I.poisson_kernel(mesh)
+    pk = pf.PoissonKernel(dense, boundary, 0.0, 0.0)
+    dk = dev.device_kernel(pk)
+    rng = np.random.default_rng(5)
+    T = 200
+    tg = torch.from_numpy(rng.choice(mesh.n, T, replace=False).astype(np.int64)).cuda()
+    s = torch.cuda.current_stream().cuda_stream
+    k, rows = dk.k, dk.rows
+    ldl = dev.round_up(k, 16)
+    Pt = dk.P.index_select(0, tg)
+    L = torch.empty((T, ldl), dtype=torch.float64, device="cuda")
+    Tc = torch.empty_like(L)
+    nat.call("pf_batch_prep_f64", Pt.data_ptr(), Pt.stride(0), T, k, ldl, 1e-300, 0,
+             L.data_ptr(), Tc.data_ptr(), 0, s)
+    A, ea, ldk = dk.slices(1e-300)
+    B = torch.empty((7, T, ldk), dtype=torch.uint8, device="cuda")
+    eb = torch.empty(T, dtype=torch.int32, device="cuda")
+    bad = torch.zeros(1, dtype=torch.int32, device="cuda")
+    nat.call("pf_slice_targets_u8", L.data_ptr(), ldl, T, k, ldk, B.data_ptr(), eb.data_ptr(),
+             bad.data_ptr(), s)
+    H = dk.negentropy(1e-300)
+    res = {}
+    for mode, cap in (("scan", 0), ("list", rows * T), ("overflow", 3)):
+        out = torch.empty((rows, T), dtype=torch.float64, device="cuda")
+        cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
+        glist = torch.zeros(max(cap, 1) + 1, dtype=torch.int64, device="cuda")
+        nat.call("pf_batched_kl_i8_listed", A.data_ptr(), ea.data_ptr(), rows, B.data_ptr(),
+                 eb.data_ptr(), T, k, ldk, H.data_ptr(), tg.data_ptr(), D.KL_GUARD_TAU, 0,
+                 out.data_ptr(), out.stride(0), 64, 1, glist.data_ptr() if cap else None,
+                 cap, s)
+        if mode == "scan":
+            nat.call("pf_batched_kl_fixup_f64", dk.P.data_ptr(), dk.ld, rows, k, Tc.data_ptr(),
+                     ldl, T, 1e-300, out.data_ptr(), out.stride(0), cnt.data_ptr(), s)
+        else:
+            nat.call("pf_batched_kl_fixup_list_f64", dk.P.data_ptr(), dk.ld, rows, k,
+                     Tc.data_ptr(), ldl, T, 1e-300, out.data_ptr(), out.stride(0), cnt.data_ptr(),
+                     glist.data_ptr(), cap, s)
+        torch.cuda.synchronize()
+        res[mode] = (out.cpu(), int(cnt.item()), int(glist[0].item()))
+    n_scan = res["scan"][1]
+    assert n_scan > 0                                   # the case has guarded pairs
+    assert res["list"][2] == n_scan and res["list"][1] == n_scan
+    assert res["overflow"][2] == n_scan > 3 and res["overflow"][1] == n_scan
+    for mode in ("list", "overflow"):
+        assert torch.equal(res[mode][0].view(torch.int64), res["scan"][0].view(torch.int64)), mode
