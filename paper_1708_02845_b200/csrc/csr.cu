@@ -32,6 +32,7 @@ namespace pf {
 
 constexpr int kCsrThreads = 256;
 constexpr int kCsrMinBlocks = 4;
+constexpr int kCsrU = 4;   // entry pairs per lane in flight
 constexpr unsigned long long kCsrGuard = 0x7ff8dead0000c5a1ull;  // NaN payload
 
 __device__ __forceinline__ bool keep_entry(double x, double cut, int strict_pos) {
@@ -167,28 +168,30 @@ __device__ __forceinline__ void csr_row_visit(const double *__restrict__ data,
   }
   const int64_t npairs = (hi - s) >> 1;
   const double2 *d2 = reinterpret_cast<const double2 *>(data + s);
-  int64_t j = lane;
-  // 4 pairs per lane in flight (the kernels are latency-bound: ~32 resident
-  // warps per SM need ~2.5 KB each in flight to cover DRAM latency at 7 TB/s)
-  for (; j + 96 < npairs; j += 128) {
-    double2 v[4];
-    int2 cidx[4];
+  // Up to 8 pairs per lane per block (a ~490-entry row is one block: one
+  // memory round trip per row instead of ~3).  Pairs past the row's end load a
+  // clamped in-row address and visit (0, column 0): +0 to a KL accumulator, and
+  // an even number of visits leaves the lane's alternation unchanged; TV masks
+  // them itself (a zero value).  The per-lane order of the real pairs is
+  // lane, lane + 32, ... as before.
+  if (npairs > 0) {
+    for (int64_t j0 = 0; j0 < npairs; j0 += 32 * kCsrU) {
+      double2 v[kCsrU];
+      int2 cidx[kCsrU];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      v[u] = __ldg(d2 + j + 32 * u);
-      cidx[u] = idx_pair(idx, s, j + 32 * u);
-    }
+      for (int u = 0; u < kCsrU; ++u) {
+        const int64_t j = j0 + lane + 32 * u;
+        const int64_t jc = j < npairs ? j : npairs - 1;
+        v[u] = __ldg(d2 + jc);
+        cidx[u] = idx_pair(idx, s, jc);
+      }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      f(v[u].x, cidx[u].x);
-      f(v[u].y, cidx[u].y);
+      for (int u = 0; u < kCsrU; ++u) {
+        const bool in = j0 + lane + 32 * u < npairs;
+        f(in ? v[u].x : 0.0, in ? cidx[u].x : 0);
+        f(in ? v[u].y : 0.0, in ? cidx[u].y : 0);
+      }
     }
-  }
-  for (; j < npairs; j += 32) {
-    const double2 va = __ldg(d2 + j);
-    const int2 ca = idx_pair(idx, s, j);
-    f(va.x, ca.x);
-    f(va.y, ca.y);
   }
   if (((hi - s) & 1) && lane == 0) f(__ldg(data + hi - 1), (int32_t)__ldg(idx + hi - 1));
 }
@@ -319,11 +322,11 @@ __global__ void __launch_bounds__(kCsrThreads, MINB) csr_kl_kernel(
   __shared__ CsrGuard gq;
   if (threadIdx.x == 0) gq.n = 0;
   if (!STAGE) __syncthreads();
-  const double *lt = STAGE ? stage_vec(smem, logt, k_pad) : logt;
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t count = queries ? nq : rows;
+  const double *lt = STAGE ? stage_vec(smem, logt, k_pad) : logt;
   int64_t i = warp;
   int64_t r = i < count ? (queries ? queries[i] - row0 : i) : 0;
   int64_t lo = 0, hi = 0;
@@ -410,11 +413,11 @@ __global__ void __launch_bounds__(kCsrThreads, MINB) csr_tv_kernel(
     const int64_t *__restrict__ queries, int64_t nq, double *__restrict__ out,
     int64_t *__restrict__ ops) {
   extern __shared__ __align__(128) unsigned char smem[];
-  const double *v_p = STAGE ? stage_vec(smem, vp, k_pad) : vp;
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t count = queries ? nq : rows;
+  const double *v_p = STAGE ? stage_vec(smem, vp, k_pad) : vp;
   const double S_p = tscal[0], d_p = tscal[1];
   const int64_t nnz_p = static_cast<int64_t>(tscal[2]);
   int64_t i = warp;
@@ -434,7 +437,7 @@ __global__ void __launch_bounds__(kCsrThreads, MINB) csr_tv_kernel(
     csr_row_visit(data, indices, lo, hi, lane, [&](double v, int32_t c) {
       const double w = v_p[c];
       a += fabs(v - w) - w;
-      inter += (w != 0.0);
+      inter += (w != 0.0) && (v != 0.0);   // v == 0: a masked visit (stored entries are > 0)
     });
     const double base = warp_sum(a) + S_p;
     const double val = base + (d_p + d_q);  // divergence.py:293-295 (no settle)
