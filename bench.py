@@ -551,8 +551,13 @@ def extra_f32(t, nat, dev, pf, dk, target, steps, peak):
                         "1e-5 relative tolerance)",
             "evals_per_s": 2 * rows / ((kl_ms + tv_ms) / 1e3),
             "kl_guarded_rows": guarded[0], "tv_guarded_rows": guarded[1],
-            "kl": _roof(rows * (4 * k + 16) + 8 * k, kl_ms, peak),
-            "tv": _roof(rows * (4 * k + 8) + 8 * k, tv_ms, peak)}
+            "kl": dict(_roof(rows * (4 * k + 16) + 8 * k, kl_ms, peak),
+                       # the FP32-guarded rows are re-read as FP64 rows (8k B each)
+                       frac_incl_guard_reads=(rows * (4 * k + 16) + 8 * k + guarded[0] * 8 * k)
+                       / (kl_ms / 1e3) / 1e9 / peak),
+            "tv": dict(_roof(rows * (4 * k + 8) + 8 * k, tv_ms, peak),
+                       frac_incl_guard_reads=(rows * (4 * k + 8) + 8 * k + guarded[1] * 8 * k)
+                       / (tv_ms / 1e3) / 1e9 / peak)}
 
 
 def csr_fields_extra(t, nat, dev, pf, dk, target, steps, peak):
