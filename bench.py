@@ -1032,6 +1032,20 @@ def extra_poisson(t, nat, dev, device, L, dp_c4=None, dfma_peak=None):
     return out
 
 
+EXTRAS_DEADLINE_S = 900
+_emit_lock = __import__("threading").Lock()
+_emitted = []
+
+
+def emit(line):
+    """Print the one JSON line (at most once: the N > 1 watchdog may race the normal path)."""
+    with _emit_lock:
+        if _emitted:
+            return
+        _emitted.append(True)
+        print(json.dumps(line), flush=True)
+
+
 def run_native(args):
     import numpy as np
     import torch as t
@@ -1239,6 +1253,27 @@ def run_native(args):
                  "peak_kind": ("measured (MEASURED_PEAKS.json hbm_gbs, copy)"
                                if peak_kind == "measured" else "fallback 6.65 TB/s")})
 
+    def headline():
+        return {
+        "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": el_ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "real: reference-generator mesh, Poisson kernel P built on the GPU",
+        "config": {"workload": desc, "n": n, "k": k, "rows_per_gpu_max": max(b - a for a, b in bounds),
+                   "parallelism": f"row-slab x{ws}" + ("" if single else " (sharded path)"),
+                   "target": int(target),
+                   "l2": "inputs larger than L2 (P slab %.2f GB/GPU vs 126 MB L2)"
+                         % (rows * dk_ld(k) * 8 / 1e9)},
+        "roofline": roof,
+        "roofline_tv": _roof(bytes_tv, tv_ms, peak),
+        "kl_guarded_rows": guarded,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+        "preprocessing": prep,
+    }
+
     extras = {}
     want = set(args.extras.split(",")) if not args.no_extras else set()
     if single:
@@ -1275,31 +1310,28 @@ def run_native(args):
     else:
         del step
         t.cuda.empty_cache()
-        extras.update(run_sharded_extras(t, nat, dev, pf, L, par, dist, device, sharded,
-                                         omesh, want, args))
+        # A rank that fails inside an extra while the others sit in a collective would
+        # hang the job before the headline line is printed: past EXTRAS_DEADLINE_S the
+        # watchdog prints the line with the extras finished so far and ends every rank.
+        partial = {}
 
-    line = {
-        "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": ws,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": el_ms / args.steps,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "real: reference-generator mesh, Poisson kernel P built on the GPU",
-        "config": {"workload": desc, "n": n, "k": k, "rows_per_gpu_max": max(b - a for a, b in bounds),
-                   "parallelism": f"row-slab x{ws}" + ("" if single else " (sharded path)"),
-                   "target": int(target),
-                   "l2": "inputs larger than L2 (P slab %.2f GB/GPU vs 126 MB L2)"
-                         % (rows * dk_ld(k) * 8 / 1e9)},
-        "roofline": roof,
-        "roofline_tv": _roof(bytes_tv, tv_ms, peak),
-        "kl_guarded_rows": guarded,
-        "cpu_baseline": cpu,
-        "e2e": e2e,
-        "gpu_launches": launches,
-        "clocks": clocks.summary(),
-        "preprocessing": prep,
-        "extras": extras,
-    }
+        def expire():
+            if rank == 0:
+                emit(dict(headline(), extras=dict(partial, timeout=(
+                    f"N>1 extras unfinished after {EXTRAS_DEADLINE_S} s"))))
+            os._exit(0)
+
+        import threading
+        dog = threading.Timer(EXTRAS_DEADLINE_S, expire)
+        dog.daemon = True
+        dog.start()
+        extras.update(run_sharded_extras(t, nat, dev, pf, L, par, dist, device, sharded,
+                                         omesh, want, args, partial))
+        dog.cancel()
+
+    line = dict(headline(), extras=extras)
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     if sharded is not None:
         sharded.close()
     if dist is not None:
@@ -1312,14 +1344,15 @@ def dk_ld(k):
     return (k + 63) // 64 * 64
 
 
-def run_sharded_extras(t, nat, dev, pf, L, par, dist, device, sharded, omesh, want, args):
+def run_sharded_extras(t, nat, dev, pf, L, par, dist, device, sharded, omesh, want, args,
+                       out=None):
     """N > 1 side configs (strong scaling of the configs BASELINE names):
     C3 — CSR KL + TV over nnz-balanced row slabs of the C2 real P; C5 — 1,024
     targets partitioned over the ranks (P replicated, K7), each rank tracing
     the paths of its own targets (parallel.trace_batch; no field exchange)."""
     import numpy as np
     ws, rank = dist.get_world_size(), dist.get_rank()
-    out = {}
+    out = {} if out is None else out   # filled as each extra finishes (the watchdog reads it)
 
     def max_ms(x):
         v = t.tensor([x], dtype=t.float64)
