@@ -363,6 +363,11 @@ int pf_probe_umma_i8(int64_t iters, int random_operands, int64_t *ops_host, uint
  * obtain the sustained FP64 rate K7 is measured against. */
 int pf_probe_dfma_f64(int64_t iters, int64_t *flops_host, double *out, pf_stream_t stream);
 
+/* Diagnostic: stream n doubles of buf (16-byte aligned) with the field
+ * kernels' loads and nothing else: the pure-read HBM ceiling the dense
+ * streams are reported against beside the copy peak. */
+int pf_probe_hbm_read(const double *buf, int64_t n, double *sink, pf_stream_t stream);
+
 /* ---- K8: batched triangle-descent tracer (paths.py:101-307) ---------------
  * Device-resident mesh topology (all arrays device pointers):
  *   vertices  (n,2) FP64;  triangles (nt,3) int32 CCW exactly as stored by

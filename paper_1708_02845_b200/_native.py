@@ -75,6 +75,7 @@ _SIGS = {
                                 c_dbl, c_i64, c_vp, c_i64, c_int, c_int, c_vp, c_i64, c_vp],
     "pf_probe_umma_i8": [c_i64, c_int, ctypes.POINTER(ctypes.c_int64), c_vp, c_vp],
     "pf_probe_dfma_f64": [c_i64, ctypes.POINTER(ctypes.c_int64), c_vp, c_vp],
+    "pf_probe_hbm_read": [c_vp, c_i64, c_vp, c_vp],
     "pf_convert_f32": [c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp],
     "pf_row_negentropy_f32": [c_vp, c_i64, c_i64, c_i64, c_dbl, c_vp, c_vp],
     "pf_dense_kl_f32": [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_dbl, c_dbl, c_i64,

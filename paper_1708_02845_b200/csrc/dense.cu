@@ -388,9 +388,12 @@ static int launch_cfg(K kernel, size_t smem, int64_t rows, int *grid, int thread
 }
 
 // Production geometry of the dense KL/TV kernels (tools/tune_dense.cu,
-// profiles/): 4 x 128-bit loads in flight per lane, 5 CTAs x 8 warps per SM
+// profiles/): 6 x 128-bit loads in flight per lane, 5 CTAs x 8 warps per SM
 // when the staged target row fits (k <~ 4,900 for 5 CTAs), else fewer.
-constexpr int kU = 4, kMinBlocks = 5;
+// Re-tuned once the loop stopped being ALU-bound: on real C4, (U, CTAs/SM) =
+// (6, 5) streams KL / TV at 0.955 / 0.98 of the pure-read ceiling, (4, 5)
+// 0.94 / 0.95, (8, 4) 0.96 / 0.93, (6, 4) 0.946 / 0.961, (8, 3) 0.948 / 0.970.
+constexpr int kU = 6, kMinBlocks = 5;
 
 template <typename K>
 static int launch_dense(K staged, K unstaged, int64_t rows, int64_t k, cudaStream_t stream,
@@ -419,6 +422,30 @@ static int check_dense_args(const double *P, int64_t ld, int64_t rows, int64_t k
   return 0;
 }
 
+
+// Diagnostic: the pure-read HBM ceiling — a persistent grid streaming a
+// buffer with the field kernels' 16-byte non-allocating loads and nothing
+// else (4 CTAs x 8 warps per SM, 4 loads in flight per lane); bench.py
+// reports the dense streams against it beside the copy peak.
+__global__ void __launch_bounds__(256) hbm_read_probe_kernel(const double2 *__restrict__ a,
+                                                             int64_t n2, double *out) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+  double s = 0.0;
+  int64_t i = tid;
+  for (; i + 3 * nt < n2; i += 4 * nt) {
+    double2 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = ldg_stream2(a + i + u * nt);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) s += v[u].x + v[u].y;
+  }
+  for (; i < n2; i += nt) {
+    const double2 v = ldg_stream2(a + i);
+    s += v.x + v.y;
+  }
+  if (s == 1.2345) out[0] = s;   // keeps the loads
+}
 }  // namespace pf
 
 using namespace pf;
@@ -562,6 +589,15 @@ int pf_dense_at_f64(const double *P, int64_t ld, int64_t rows, int64_t k, const 
   }
 #undef PF_AT_CASE
   return check_launch("dense_at");
+}
+
+int pf_probe_hbm_read(const double *buf, int64_t n, double *sink, pf_stream_t stream) {
+  if (n <= 0) return 0;
+  if (!buf || !sink || (reinterpret_cast<uintptr_t>(buf) & 15))
+    return fail(PF_E_ARG, "probe_hbm_read: 16-byte aligned buffer and a sink");
+  hbm_read_probe_kernel<<<sm_count() * 4, 256, 0, as_stream(stream)>>>(
+      reinterpret_cast<const double2 *>(buf), n / 2, sink);
+  return check_launch("probe_hbm_read");
 }
 
 }  // extern "C"
