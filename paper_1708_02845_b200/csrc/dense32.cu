@@ -114,8 +114,8 @@ static __device__ __noinline__ double cross64_row(const double *__restrict__ pro
   return warp_sum(a0 + a1);
 }
 
-template <bool KL, bool CLAMP>
-__global__ void __launch_bounds__(kT32, 4) dense32_kernel(
+template <bool KL, bool CLAMP, int U = 4, int MINB = 4>
+__global__ void __launch_bounds__(kT32, MINB) dense32_kernel(
     const float *__restrict__ P, int64_t ld, int64_t rows, int64_t k,
     const double *__restrict__ H, const double *__restrict__ vec, double clamp, float clamp32,
     double tau, int64_t row0, int64_t target, const double *__restrict__ P64, int64_t ld64,
@@ -138,7 +138,6 @@ __global__ void __launch_bounds__(kT32, 4) dense32_kernel(
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  constexpr int U = 4;
   const int nq = static_cast<int>(nq4);                    // < 2^31 (k <= 25,600)
   const int nfull = nq / (32 * U) * (32 * U);               // chunks with every lane in range
   const int64_t first = (warp * warp_mul) % nwarps;  // scattered rows (pf_common.cuh)
@@ -237,7 +236,10 @@ static int launch32(const float *P, int64_t ld, int64_t rows, int64_t k, const d
   if (smem > 200 * 1024) return fail(PF_E_DOMAIN, "dense32: k=%lld too large", (long long)k);
   // the clamp in FP32, rounded to nearest; flushed to 0 (no max) below FLT_MIN
   const float clamp32 = clamp >= static_cast<double>(FLT_MIN) ? static_cast<float>(clamp) : 0.0f;
-  auto kern = clamp32 > 0.0f ? dense32_kernel<KL, true> : dense32_kernel<KL, false>;
+  // 8 float4 per lane in flight, 3 CTAs x 8 warps per SM: re-tuned once the loop
+  // stopped being ALU-bound (synthetic C4: (U, CTAs) = (8, 3) 6.96 / 6.96 TB/s
+  // KL / TV, (4, 4) 6.86 / 6.87, (6, 4) 6.89 / 6.98, (6, 5) 6.81 / 6.93)
+  auto kern = clamp32 > 0.0f ? dense32_kernel<KL, true, 8, 3> : dense32_kernel<KL, false, 8, 3>;
   if (int e = ensure_smem((const void *)kern, smem)) return e;
   const int occ = occupancy((const void *)kern, kT32, smem);
   int64_t g = static_cast<int64_t>(sm_count()) * occ, want = (rows + 7) / 8;
