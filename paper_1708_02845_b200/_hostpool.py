@@ -45,6 +45,23 @@ def to_host(t, dbuf, stream) -> np.ndarray:
     return arr
 
 
+_tls = threading.local()
+
+
+def pinned_view(t, arr: np.ndarray) -> int:
+    """Copy a small host array into this thread's pinned scratch and return its
+    address, which kernels read in place (pinned memory is mapped into the
+    device's address space under UVA: no copy operation, no event).  Valid
+    until this thread's next call; callers synchronize before returning."""
+    need = max(int(arr.nbytes), 64)
+    buf = getattr(_tls, "pinned", None)
+    if buf is None or buf.numel() < need:
+        buf = t.empty(max(need, 1 << 16), dtype=t.uint8, pin_memory=True)
+        _tls.pinned = buf
+    buf.numpy()[: arr.nbytes] = np.ascontiguousarray(arr).view(np.uint8).reshape(-1)
+    return buf.data_ptr()
+
+
 def upload_small(t, arr: np.ndarray, dbuf, stream) -> None:
     """Host array -> device tensor `dbuf` (same byte size) through a pooled
     pinned buffer: an async DMA on `stream` instead of a pageable, synchronous

@@ -246,7 +246,7 @@ def dv_field(pk: PoissonKernel, fd: FDivergence, p: int,
     return ScalarField(vals, fd.name, p, params, 1, None, ("clamped",) if fired else ())
 
 
-from ._hostpool import upload_small  # noqa: E402
+from ._hostpool import pinned_view  # noqa: E402
 
 
 def dv_at(pk: PoissonKernel, fd: FDivergence, p: int, queries,
@@ -270,22 +270,24 @@ def dv_at(pk: PoissonKernel, fd: FDivergence, p: int, queries,
     row = dk.target_row(p)
     nat.call("pf_target_prep_f64", row.data_ptr(), dk.k, c, st.tgt, st.logt, st.tmask, 0,
              s.cuda_stream)
-    # queries through a pooled pinned buffer (async), scratch-resident on the device
-    qd = dk.scratch(s.cuda_stream, max(8 * q.size, 8), "at_q").view(t.int64)
-    if q.size:
-        upload_small(t, q, qd, s)
+    # up to 64K queries are read by the kernel in place from this thread's pinned
+    # scratch (mapped under UVA): no H2D copy operation on the critical path;
+    # more go up in one copy
+    if q.size <= 1 << 16:
+        qptr = pinned_view(t, q)
+    else:
+        qd = t.from_numpy(q).to(dk.device)
+        qptr = qd.data_ptr()
     out = t.empty(q.size, dtype=t.float64, device=dk.device)
     if gen[0] == "user":
         nat.call("pf_dense_user_at_f64", gen[1].handle, dk.P.data_ptr(), dk.ld, dk.rows, dk.k,
-                 st.tgt, c, int(bool(swap_order)), dk.row0, p, qd.data_ptr(), q.size,
+                 st.tgt, c, int(bool(swap_order)), dk.row0, p, qptr, q.size,
                  out.data_ptr(), s.cuda_stream)
     else:
         nat.call("pf_dense_at_f64", dk.P.data_ptr(), dk.ld, dk.rows, dk.k, st.tgt, c, gen[1],
-                 gen[2], int(bool(swap_order)), dk.row0, p, qd.data_ptr(), q.size,
+                 gen[2], int(bool(swap_order)), dk.row0, p, qptr, q.size,
                  out.data_ptr(), s.cuda_stream)
-    res = _to_host(t, out, s).copy()
-    del st, row
-    return res
+    return _to_host(t, out, s)   # synchronizes the stream: the pinned queries are free
 
 
 def _settle(value: float) -> float:
