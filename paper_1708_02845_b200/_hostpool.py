@@ -62,33 +62,6 @@ def pinned_view(t, arr: np.ndarray) -> int:
     return buf.data_ptr()
 
 
-def upload_small(t, arr: np.ndarray, dbuf, stream) -> None:
-    """Host array -> device tensor `dbuf` (same byte size) through a pooled
-    pinned buffer: an async DMA on `stream` instead of a pageable, synchronous
-    copy.  The pinned buffer returns to the pool once the stream reaches it."""
-    key = (int(arr.nbytes), "upload")
-    with _lock:
-        lst = _free.get(key)
-        host = lst.pop() if lst else None
-    if host is None:
-        host = t.empty(int(arr.nbytes), dtype=t.uint8, pin_memory=True)
-    host.numpy()[:] = np.ascontiguousarray(arr).view(np.uint8).reshape(-1)
-    dbuf.view(t.uint8).reshape(-1)[: arr.nbytes].copy_(host, non_blocking=True)
-    ev = t.cuda.Event()
-    ev.record(stream)
-    with _lock:
-        _pending.append((ev, key, host))
-        done, keep = [], []
-        for e in _pending:
-            (done if e[0].query() else keep).append(e)
-        _pending[:] = keep
-    for _, k, h in done:
-        _give_back(k, h)
-
-
-_pending: list = []   # (event, pool key, pinned buffer) of uploads in flight
-
-
 # -- host -> device row upload ------------------------------------------------
 _UPLOAD_CHUNK_BYTES = 64 << 20
 _UPLOAD_BUFFERS = 3
