@@ -189,6 +189,47 @@ __global__ void __launch_bounds__(kGemmThreads, 2) batched_kl_dmma2_kernel(
   }
 }
 
+template <bool FAST>
+__device__ __forceinline__ double fixup_pair_t(const double *__restrict__ prow,
+                                             const double *__restrict__ trow, int64_t k,
+                                             double clamp, int lane) {
+  double b[4] = {0.0, 0.0, 0.0, 0.0};
+  int64_t c = lane;
+  for (; c + 224 < k; c += 256) {   // two 128-element steps, 8 loads in flight
+    double pv[8], tv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      pv[u] = ldg_stream(prow + c + 32 * u);
+      tv[u] = __ldg(trow + c + 32 * u);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const double qv = fmax(pv[u], clamp);
+      b[u & 3] += kl_term<FAST>(qv, tv[u]);
+    }
+  }
+  for (; c + 96 < k; c += 128) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double qv = fmax(prow[c + 32 * u], clamp);
+      b[u] += kl_term<FAST>(qv, trow[c + 32 * u]);
+    }
+  }
+  for (; c < k; c += 32) {
+    const double qv = fmax(prow[c], clamp);
+    b[0] += kl_term<FAST>(qv, trow[c]);
+  }
+  return settle(warp_sum((b[0] + b[1]) + (b[2] + b[3])));
+}
+
+// clamp >= kFastTermMin: the branch-free terms (pf_common.cuh kl_term)
+__device__ __forceinline__ double fixup_pair(const double *__restrict__ prow,
+                                             const double *__restrict__ trow, int64_t k,
+                                             double clamp, int lane) {
+  return clamp >= kFastTermMin ? fixup_pair_t<true>(prow, trow, k, clamp, lane)
+                               : fixup_pair_t<false>(prow, trow, k, clamp, lane);
+}
+
 // Per-element reference form for guarded (q, t) pairs (divergence.py:180).
 __global__ void __launch_bounds__(256) batched_kl_fixup_kernel(
     const double *__restrict__ P, int64_t ld, int64_t rows, int64_t k,
@@ -211,22 +252,7 @@ __global__ void __launch_bounds__(256) batched_kl_fixup_kernel(
       const int src = __ffs(ball) - 1;
       ball &= ball - 1;
       const int64_t e = warp + (i0 + src) * nwarps, q = e / T, t = e - q * T;
-      const double *prow = P + q * ld;
-      const double *trow = Tc + t * ldl;
-      double b[4] = {0.0, 0.0, 0.0, 0.0};
-      int64_t c = lane;
-      for (; c + 96 < k; c += 128) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const double qv = fmax(prow[c + 32 * u], clamp);
-          b[u] += __dmul_rn(qv, -log(__ddiv_rn(trow[c + 32 * u], qv)));
-        }
-      }
-      for (; c < k; c += 32) {
-        const double qv = fmax(prow[c], clamp);
-        b[0] += __dmul_rn(qv, -log(__ddiv_rn(trow[c], qv)));
-      }
-      const double val = settle(warp_sum((b[0] + b[1]) + (b[2] + b[3])));
+      const double val = fixup_pair(P + q * ld, Tc + t * ldl, k, clamp, lane);
       if (lane == 0) out[q * ldo + t] = val;
       ++done;
     }
@@ -241,47 +267,16 @@ __global__ void __launch_bounds__(256) batched_kl_fixup_kernel(
 // long-scoreboard on the row loads).  The per-lane order of the terms is the
 // scan kernel's, so both give the same values.  A list that overflowed
 // (count > cap) falls back to the scan.
-__device__ __forceinline__ double fixup_pair(const double *__restrict__ prow,
-                                             const double *__restrict__ trow, int64_t k,
-                                             double clamp, int lane) {
-  double b[4] = {0.0, 0.0, 0.0, 0.0};
-  int64_t c = lane;
-  for (; c + 224 < k; c += 256) {   // two 128-element steps, 8 loads in flight
-    double pv[8], tv[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      pv[u] = ldg_stream(prow + c + 32 * u);
-      tv[u] = __ldg(trow + c + 32 * u);
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const double qv = fmax(pv[u], clamp);
-      b[u & 3] += __dmul_rn(qv, -log(__ddiv_rn(tv[u], qv)));
-    }
-  }
-  for (; c + 96 < k; c += 128) {
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const double qv = fmax(prow[c + 32 * u], clamp);
-      b[u] += __dmul_rn(qv, -log(__ddiv_rn(trow[c + 32 * u], qv)));
-    }
-  }
-  for (; c < k; c += 32) {
-    const double qv = fmax(prow[c], clamp);
-    b[0] += __dmul_rn(qv, -log(__ddiv_rn(trow[c], qv)));
-  }
-  return settle(warp_sum((b[0] + b[1]) + (b[2] + b[3])));
-}
-
 __global__ void __launch_bounds__(256) batched_kl_fixup_list_kernel(
     const double *__restrict__ P, int64_t ld, int64_t rows, int64_t k,
     const double *__restrict__ Tc, int64_t ldl, int64_t T, double clamp,
     double *__restrict__ out, int64_t ldo, uint32_t *__restrict__ count,
-    const int64_t *__restrict__ guard_list, int64_t cap) {
+    const int64_t *__restrict__ guard_list, int64_t cap, int scan_only) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t n = guard_list[0];
+  if (n <= cap && scan_only) return;   // the staged kernel walks the list
   if (n > cap) {   // overflowed: the scan kernel's loop
     uint32_t done = 0;
     const int64_t total = rows * T;
@@ -304,11 +299,117 @@ __global__ void __launch_bounds__(256) batched_kl_fixup_list_kernel(
     return;
   }
   uint32_t done = 0;
+  const uint32_t row_bytes = static_cast<uint32_t>((k * 8 + 15) & ~15ll);
+  auto prefetch_row = [&](int64_t j) {   // the P row of list entry j into L2
+    if (lane == 0 && j < n) {
+      const int64_t qj = guard_list[1 + j] / T;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(P + qj * ld),
+                   "r"(row_bytes)
+                   : "memory");
+    }
+  };
+  prefetch_row(warp);
   for (int64_t i = warp; i < n; i += nwarps) {
     const int64_t e = guard_list[1 + i], q = e / T, t = e - q * T;
+    prefetch_row(i + nwarps);   // the next pair's row streams in while this one reduces
     const double val = fixup_pair(P + q * ld, Tc + t * ldl, k, clamp, lane);
     if (lane == 0) out[q * ldo + t] = val;
     ++done;
+  }
+  if (lane == 0 && done && count) atomicAdd(count, done);
+}
+
+// The list fixup with the rows staged through shared memory: each warp
+// streams its pairs' P and target rows in 256-element chunks (both 2 KB)
+// through a two-slot ring with cp.async.bulk, one chunk ahead of the chunk it
+// reduces -- the register-loaded version left the FP64 pipe at ~50% on
+// long-scoreboard stalls with 8 loads per lane in flight.  The terms are the
+// branch-free ones (clamp >= kFastTermMin) and each lane adds them to the same
+// four accumulators in the same order as fixup_pair_t: bitwise its values.
+constexpr int kFxChunk = 256;                    // elements per chunk
+constexpr int kFxWarps = 16;                     // 512 threads, one CTA per SM
+constexpr int kFxSlots = 2;                      // chunks per warp in the ring (3: no faster)
+constexpr int kFxSlotBytes = 2 * kFxChunk * 8;   // P + target chunk
+constexpr int kFxSmem = kFxWarps * kFxSlots * kFxSlotBytes;   // 128 KB
+
+__global__ void __launch_bounds__(kFxWarps * 32, 1) batched_kl_fixup_staged_kernel(
+    const double *__restrict__ P, int64_t ld, int64_t k, const double *__restrict__ Tc,
+    int64_t ldl, int64_t T, double clamp, double *__restrict__ out, int64_t ldo,
+    uint32_t *__restrict__ count, const int64_t *__restrict__ guard_list, int64_t cap) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bar[kFxWarps][kFxSlots];
+  const int lane = threadIdx.x & 31, wc = threadIdx.x >> 5;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t n = guard_list[0];
+  if (n > cap) return;   // overflowed: the scan (batched_kl_fixup_list_kernel) did it
+  double *ring = reinterpret_cast<double *>(smem + wc * kFxSlots * kFxSlotBytes);
+  if (lane == 0)
+    for (int st = 0; st < kFxSlots; ++st) mbar_init(&bar[wc][st], 1);
+  __syncwarp();
+  const int64_t nch = (k + kFxChunk - 1) / kFxChunk;
+  // the chunk stream: (pair i, chunk c) for i = warp, warp + nwarps, ...
+  int64_t ii = warp, ic = 0;            // issue side
+  auto issue = [&](int st) {
+    if (lane == 0 && ii < n) {
+      const int64_t e = guard_list[1 + ii], q = e / T, t = e - q * T;
+      const int64_t base = ic * kFxChunk;
+      const int64_t len = k - base < kFxChunk ? k - base : kFxChunk;
+      const uint32_t bytes = static_cast<uint32_t>((len * 8 + 15) & ~15ll);
+      double *dst = ring + st * 2 * kFxChunk;
+      mbar_expect_tx(&bar[wc][st], 2 * bytes);
+      bulk_g2s(dst, P + q * ld + base, bytes, &bar[wc][st]);
+      bulk_g2s(dst + kFxChunk, Tc + t * ldl + base, bytes, &bar[wc][st]);
+    }
+    if (ii < n && ++ic == nch) {
+      ic = 0;
+      ii += nwarps;
+    }
+  };
+#pragma unroll
+  for (int st = 0; st < kFxSlots - 1; ++st) issue(st);
+  uint32_t done = 0;
+  double b[4] = {0.0, 0.0, 0.0, 0.0};
+  int64_t ci = warp, cc = 0;            // reduce side
+  for (int64_t s = 0; ci < n; ++s) {
+    issue(static_cast<int>((s + kFxSlots - 1) % kFxSlots));   // the slot freed by chunk s - 1
+    const int st = static_cast<int>(s % kFxSlots);
+    mbar_wait(&bar[wc][st], static_cast<uint32_t>((s / kFxSlots) & 1));
+    const double *pc = ring + st * 2 * kFxChunk, *tcn = pc + kFxChunk;
+    const int64_t base = cc * kFxChunk;
+    if (base + kFxChunk <= k) {   // every 128-element block full for every lane: straight-line
+      double tm[kFxChunk / 32];
+#pragma unroll
+      for (int u = 0; u < kFxChunk / 32; ++u)
+        tm[u] = kl_term<true>(fmax(pc[lane + 32 * u], clamp), tcn[lane + 32 * u]);
+#pragma unroll
+      for (int u = 0; u < kFxChunk / 32; ++u) b[u & 3] += tm[u];
+    } else
+#pragma unroll
+    for (int u = 0; u < kFxChunk / 32; ++u) {
+      const int64_t e = base + lane + 32 * u;   // this lane's elements, in order
+      if (e < k) {
+        // fixup_pair_t's accumulator: u & 3 inside a full 128-element block, else 0
+        const int64_t blk = base + 128 * (u >> 2);
+        const int acc = (blk + lane + 96 < k) ? (u & 3) : 0;
+        const double term = kl_term<true>(fmax(pc[lane + 32 * u], clamp), tcn[lane + 32 * u]);
+        if (acc == 0) b[0] += term;
+        else if (acc == 1) b[1] += term;
+        else if (acc == 2) b[2] += term;
+        else b[3] += term;
+      }
+    }
+    __syncwarp();   // every lane is done with this slot before it is refilled
+    if (++cc == nch) {
+      const double val = settle(warp_sum((b[0] + b[1]) + (b[2] + b[3])));
+      const int64_t e = guard_list[1 + ci];
+      const int64_t q = e / T, t = e - q * T;
+      if (lane == 0) out[q * ldo + t] = val;
+      ++done;
+      b[0] = b[1] = b[2] = b[3] = 0.0;
+      cc = 0;
+      ci += nwarps;
+    }
   }
   if (lane == 0 && done && count) atomicAdd(count, done);
 }
@@ -396,8 +497,19 @@ int pf_batched_kl_fixup_list_f64(const double *P, int64_t ld, int64_t rows, int6
                                  const int64_t *guard_list, int64_t guard_cap, pf_stream_t stream) {
   if (rows <= 0 || T <= 0) return 0;
   if (!P || !Tc || !out || !guard_list) return fail(PF_E_ARG, "batched_kl_fixup_list: null");
+  if (clamp >= kFastTermMin && (ld & 1) == 0 && (ldl & 1) == 0 &&
+      (reinterpret_cast<uintptr_t>(P) & 15) == 0 && (reinterpret_cast<uintptr_t>(Tc) & 15) == 0) {
+    // the staged version; a list that overflowed is the scan kernel's job
+    if (int e = ensure_smem((const void *)batched_kl_fixup_staged_kernel, kFxSmem)) return e;
+    batched_kl_fixup_list_kernel<<<sm_count() * 8, 256, 0, as_stream(stream)>>>(
+        P, ld, rows, k, Tc, ldl, T, clamp, out, ldo, guarded, guard_list, guard_cap, 1);
+    if (int e = check_launch("batched_kl_fixup_list")) return e;
+    batched_kl_fixup_staged_kernel<<<sm_count(), kFxWarps * 32, kFxSmem, as_stream(stream)>>>(
+        P, ld, k, Tc, ldl, T, clamp, out, ldo, guarded, guard_list, guard_cap);
+    return check_launch("batched_kl_fixup_staged");
+  }
   batched_kl_fixup_list_kernel<<<sm_count() * 8, 256, 0, as_stream(stream)>>>(
-      P, ld, rows, k, Tc, ldl, T, clamp, out, ldo, guarded, guard_list, guard_cap);
+      P, ld, rows, k, Tc, ldl, T, clamp, out, ldo, guarded, guard_list, guard_cap, 0);
   return check_launch("batched_kl_fixup_list");
 }
 
