@@ -347,6 +347,24 @@ int pf_batched_kl_i8_listed(const uint8_t *A, const int32_t *ea, int64_t rows, c
                             const int64_t *targets, double tau, int64_t row0, double *out,
                             int64_t ldo, int grade, int cta_pair, int64_t *guard_list,
                             int64_t guard_cap, pf_stream_t stream);
+/* The tiled operand layout the CTA-pair kernel streams best: byte plane s,
+ * tile u, 32-byte K block kb is one contiguous run of R x 32 bytes (R = 128
+ * rows for A, 64 targets for B) holding the SWIZZLE_32B shared-memory image,
+ * so a TMA box is 256-byte rows (1.6x the L2 ingest rate of the row-major
+ * box, 4x from HBM).  Each operand takes pf_i8_tiled_bytes(n, k) bytes (rows
+ * / targets padded to 128 with zeros, K to 32), 16-byte aligned.
+ * pf_batched_kl_i8_tiled: pf_batched_kl_i8_listed with cta_pair = 1 on the
+ * tiled operands (guard_list may be NULL); bitwise the same outputs. */
+int64_t pf_i8_tiled_bytes(int64_t n, int64_t k);
+int pf_slice_rows_u8_tiled(const double *P, int64_t ld, int64_t rows, int64_t k, double clamp,
+                           uint8_t *tiles, int32_t *exps, pf_stream_t stream);
+int pf_slice_targets_u8_tiled(const double *L, int64_t ldl, int64_t T, int64_t k, uint8_t *tiles,
+                              int32_t *exps, uint32_t *bad, pf_stream_t stream);
+int pf_batched_kl_i8_tiled(const uint8_t *A, const int32_t *ea, int64_t rows, const uint8_t *B,
+                           const int32_t *eb, int64_t T, int64_t k, const double *H,
+                           const int64_t *targets, double tau, int64_t row0, double *out,
+                           int64_t ldo, int grade, int64_t *guard_list, int64_t guard_cap,
+                           pf_stream_t stream);
 
 /* Diagnostic: back-to-back M128 N256 K32 u8 tcgen05.mma on shared-memory
  * operands, one CTA per SM (*ops_host = integer ops issued): the int8 tensor

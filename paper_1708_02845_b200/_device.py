@@ -51,6 +51,11 @@ def require_cuda():
     return t
 
 
+def i8_tiled_bytes(n: int, k: int) -> int:
+    """Bytes of one K7 operand in the tiled layout (== pf_i8_tiled_bytes)."""
+    return 0 if n <= 0 or k <= 0 else 7 * round_up(n, 128) * round_up(k, 32)
+
+
 def round_up(x: int, m: int) -> int:
     return (x + m - 1) // m * m
 
@@ -184,6 +189,22 @@ class DeviceKernel:
                          float(clamp), ldk, A.data_ptr(), ea.data_ptr(),
                          t.cuda.current_stream(self.device).cuda_stream)
                 hit = self._H[key] = (A, ea, ldk)
+            return hit
+
+    def slices_tiled(self, clamp: float):
+        """(A, ea): the same byte planes in the tiled layout the CTA-pair
+        kernel streams (pf_slice_rows_u8_tiled; pf_i8_tiled_bytes bytes)."""
+        key = ("i8t", float(clamp))
+        with self._lock:
+            hit = self._H.get(key)
+            if hit is None:
+                t = torch()
+                A = t.empty(i8_tiled_bytes(self.rows, self.k), dtype=t.uint8, device=self.device)
+                ea = t.empty(self.rows, dtype=t.int32, device=self.device)
+                nat.call("pf_slice_rows_u8_tiled", self.P.data_ptr(), self.ld, self.rows, self.k,
+                         float(clamp), A.data_ptr(), ea.data_ptr(),
+                         t.cuda.current_stream(self.device).cuda_stream)
+                hit = self._H[key] = (A, ea)
             return hit
 
     def csr(self, cut: float, strict_positive: bool) -> "DeviceCSR":

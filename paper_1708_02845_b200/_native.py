@@ -73,6 +73,11 @@ _SIGS = {
                          c_i64, c_vp, c_i64, c_int, c_int, c_vp],
     "pf_batched_kl_i8_listed": [c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp,
                                 c_dbl, c_i64, c_vp, c_i64, c_int, c_int, c_vp, c_i64, c_vp],
+    "pf_i8_tiled_bytes": [c_i64, c_i64],
+    "pf_slice_rows_u8_tiled": [c_vp, c_i64, c_i64, c_i64, c_dbl, c_vp, c_vp, c_vp],
+    "pf_slice_targets_u8_tiled": [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp],
+    "pf_batched_kl_i8_tiled": [c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_dbl,
+                               c_i64, c_vp, c_i64, c_int, c_vp, c_i64, c_vp],
     "pf_probe_umma_i8": [c_i64, c_int, ctypes.POINTER(ctypes.c_int64), c_vp, c_vp],
     "pf_probe_dfma_f64": [c_i64, ctypes.POINTER(ctypes.c_int64), c_vp, c_vp],
     "pf_probe_hbm_read": [c_vp, c_i64, c_vp, c_vp],
@@ -145,7 +150,7 @@ _SIGS.update({
     "pf_nccl_all_reduce": [c_vp, c_vp, c_vp, c_i64, c_int, c_int, c_vp],
 })
 _RESTYPES = {"pf_last_error": ctypes.c_char_p, "pf_nd_plan_free": None,
-             "pf_nd_plan_array": ctypes.c_int64}
+             "pf_nd_plan_array": ctypes.c_int64, "pf_i8_tiled_bytes": ctypes.c_int64}
 
 
 

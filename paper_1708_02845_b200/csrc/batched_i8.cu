@@ -75,32 +75,57 @@ __device__ __forceinline__ void slice8(const double (&x)[8], int e, uint64_t (&w
 
 __device__ __forceinline__ int scale_exp(double m) { return m > 0.0 ? ilogb(m) + 1 : 0; }
 
-// Rows of the slab: a = max(P, clamp), warp per row.  slices: [7][rows][ldk].
+// Two layouts of the byte planes.  Row-major: [7][rows][ldk].  Tiled (the
+// CTA-pair kernel's): [7][rows / R][nkb][R x 32 B], each R-row x 32-byte K
+// block stored as the exact SWIZZLE_32B shared-memory image the MMA reads
+// (16-byte chunk c of row r at r * 32 + (c ^ (r >> 2 & 1)) * 16), so one
+// stage of one slice is one contiguous 4 KB (R = 128) or 2 KB (R = 64) run
+// and the TMA box is {256 B, R / 8, slices} with 256-byte rows instead of R
+// 32-byte rows: 53 B/clk/SM from L2 and the full HBM rate, against 32 and 6
+// for the row-major box (tools/probe_umma_shapes.cu tma_rate).
+struct SliceLayout {
+  int64_t ldk;    // row-major pitch (0: tiled)
+  int tile_rows;  // tiled: R
+  int nkb;        // tiled: 32-byte K blocks per row
+  __device__ __forceinline__ int64_t at(int64_t r, int64_t b0) const {   // b0 % 8 == 0
+    if (ldk) return r * ldk + b0;
+    return ((r / tile_rows) * nkb + (b0 >> 5)) * (tile_rows * 32) + (r % tile_rows) * 32 +
+           ((((b0 >> 4) & 1) ^ ((r >> 2) & 1)) << 4) + (b0 & 15);
+  }
+  __device__ __forceinline__ int64_t kspan() const { return ldk ? ldk : int64_t(nkb) * 32; }
+};
+
+// Rows of the slab: a = max(P, clamp), warp per row; rows in [rows, rows_pad)
+// are written as zeros (tiled padding).
 __global__ void __launch_bounds__(256) slice_rows_kernel(const double *__restrict__ P, int64_t ld,
-                                                         int64_t rows, int64_t k, double clamp,
-                                                         int64_t ldk, uint8_t *__restrict__ out,
+                                                         int64_t rows, int64_t rows_pad, int64_t k,
+                                                         double clamp, SliceLayout lay,
+                                                         int64_t plane, uint8_t *__restrict__ out,
                                                          int32_t *__restrict__ exps) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t plane = rows * ldk;
-  for (int64_t r = warp; r < rows; r += nwarps) {
-    const double *row = P + r * ld;
+  const int64_t span = lay.kspan();
+  for (int64_t r = warp; r < rows_pad; r += nwarps) {
+    const bool live = r < rows;
+    const double *row = P + (live ? r : 0) * ld;
     double m = 0.0;
-    for (int64_t b = lane; b < k; b += 32) m = fmax(m, fmax(row[b], clamp));
+    if (live) {
+      for (int64_t b = lane; b < k; b += 32) m = fmax(m, fmax(row[b], clamp));
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+      for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    }
     const int e = scale_exp(m);
-    if (lane == 0) exps[r] = e;
-    for (int64_t b0 = 8 * lane; b0 < ldk; b0 += 256) {
+    if (live && lane == 0) exps[r] = e;
+    for (int64_t b0 = 8 * lane; b0 < span; b0 += 256) {
       double x[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) x[u] = (b0 + u < k) ? fmax(row[b0 + u], clamp) : 0.0;
+      for (int u = 0; u < 8; ++u) x[u] = (live && b0 + u < k) ? fmax(row[b0 + u], clamp) : 0.0;
       uint64_t w[kOzSlices];
       slice8(x, e, w);
+      const int64_t o = lay.at(r, b0);
 #pragma unroll
-      for (int s = 0; s < kOzSlices; ++s)
-        *reinterpret_cast<uint64_t *>(out + s * plane + r * ldk + b0) = w[s];
+      for (int s = 0; s < kOzSlices; ++s) *reinterpret_cast<uint64_t *>(out + s * plane + o) = w[s];
     }
   }
 }
@@ -108,18 +133,20 @@ __global__ void __launch_bounds__(256) slice_rows_kernel(const double *__restric
 // Targets: b = -L (L = log max(Pt, clamp), batch_prep_kernel), block per
 // target.  bad[0] |= 1 if some b < 0 (a target entry above 1: the caller then
 // uses the FP64 path).  slices: [7][T][ldk].
+// Blocks t in [T, gridDim.x) write the zero padding of the tiled layout.
 __global__ void __launch_bounds__(256) slice_targets_kernel(const double *__restrict__ L,
                                                             int64_t ldl, int64_t T, int64_t k,
-                                                            int64_t ldk, uint8_t *__restrict__ out,
+                                                            SliceLayout lay, int64_t plane,
+                                                            uint8_t *__restrict__ out,
                                                             int32_t *__restrict__ exps,
                                                             uint32_t *__restrict__ bad) {
   const int64_t t = blockIdx.x;
-  if (t >= T) return;
-  const double *row = L + t * ldl;
+  const bool live = t < T;
+  const double *row = L + (live ? t : 0) * ldl;
   __shared__ double red[8];
   double m = 0.0;
   bool neg = false;
-  for (int64_t b = threadIdx.x; b < k; b += blockDim.x) {
+  for (int64_t b = threadIdx.x; live && b < k; b += blockDim.x) {
     const double v = -row[b];
     neg |= v < 0.0;
     m = fmax(m, v);
@@ -131,20 +158,20 @@ __global__ void __launch_bounds__(256) slice_targets_kernel(const double *__rest
   m = red[0];
   for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) m = fmax(m, red[w]);
   const int e = scale_exp(m);
-  if (threadIdx.x == 0) {
+  if (live && threadIdx.x == 0) {
     exps[t] = e;
     if (neg && bad) atomicOr(bad, 1u);
   }
-  const int64_t plane = T * ldk;
-  for (int64_t b0 = 8 * threadIdx.x; b0 < ldk; b0 += 8 * blockDim.x) {
+  const int64_t span = lay.kspan();
+  for (int64_t b0 = 8 * threadIdx.x; b0 < span; b0 += 8 * blockDim.x) {
     double x[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) x[u] = (b0 + u < k) ? fmax(-row[b0 + u], 0.0) : 0.0;
+    for (int u = 0; u < 8; ++u) x[u] = (live && b0 + u < k) ? fmax(-row[b0 + u], 0.0) : 0.0;
     uint64_t w[kOzSlices];
     slice8(x, e, w);
+    const int64_t o = lay.at(t, b0);
 #pragma unroll
-    for (int s = 0; s < kOzSlices; ++s)
-      *reinterpret_cast<uint64_t *>(out + s * plane + t * ldk + b0) = w[s];
+    for (int s = 0; s < kOzSlices; ++s) *reinterpret_cast<uint64_t *>(out + s * plane + o) = w[s];
   }
 }
 
@@ -393,14 +420,19 @@ __device__ __forceinline__ uint32_t smid() {
 // kDiag (timing diagnostics only, PF_K7_DIAG, wrong outputs): bit 0 = no TMA
 // loads (the MMAs run on stale shared memory), bit 1 = no epilogue arithmetic
 // or stores, bit 2 = %globaltimer phase stamps of cluster 0 per tile k at
-// out[k * 16 + i] (tools/probe_k7pp_stamps.py).
+// out[k * 16 + i] (tools/probe_k7pp_stamps.py), bit 3 = per-stage timeline of
+// cluster 0's leader in SM clocks (%globaltimer ticks too coarsely for
+// stage-sized gaps): load issue at out[65536 + 2 s], full-barrier pass at
+// out[65536 + 2 s + 1] (tools/probe_k7stages.py).  kTiled: operands in the
+// tiled layout (SliceLayout), the default; the row-major form stays for the
+// pf_batched_kl_i8 ABI.
 constexpr int kP2BN = 128, kP2HalfN = 64, kP2Stages = 5;
 constexpr int kP2TileA = 128 * kO2BK;                         // 4 KB per slice
 constexpr int kP2TileB = kP2HalfN * kO2BK;                    // 2 KB per slice
 constexpr int kP2StageBytes = kOzSlices * (kP2TileA + kP2TileB);  // 43,008
 constexpr int kP2Smem = kP2Stages * kP2StageBytes + 1024;
 
-template <int kS, int kMaxL, int kDiag = 0>
+template <int kS, int kMaxL, int kDiag = 0, bool kTiled = false>
 __global__ void __launch_bounds__(kO2Threads, 1)
     batched_kl_i8_pp_kernel(const __grid_constant__ CUtensorMap mapA7,
                             const __grid_constant__ CUtensorMap mapA4,
@@ -456,6 +488,7 @@ __global__ void __launch_bounds__(kO2Threads, 1)
       // skipped), so the MMA loop below can be unrolled over the ring with
       // compile-time slot addresses; per-slot phases live in `ph`.
       uint32_t ph = 0;
+      int gstage = 0;
       for (int w = cid; w < ntiles; w += ncl) {
         const int64_t q0 = (static_cast<int64_t>(w / t_tiles) * 2 + rank) * 128;
         const int32_t tb = (w % t_tiles) * kP2BN + static_cast<int32_t>(rank) * kP2HalfN;
@@ -470,6 +503,11 @@ __global__ void __launch_bounds__(kO2Threads, 1)
               if (kb >= nkb) break;
               mbar_wait(&empty_bar[st], ((ph >> st) & 1) ^ 1);
               ph ^= 1u << st;
+              if constexpr ((kDiag & 8) != 0) {   // stage timeline of cluster 0's leader
+                if (blockIdx.x == 0 && gstage < 4096)
+                  out[65536 + 2 * gstage] = static_cast<double>(clock64());
+                ++gstage;
+              }
               if constexpr ((kDiag & 1) != 0) {
                 if (rank == 0) mbar_arrive(&full_bar[st]);
                 continue;
@@ -478,8 +516,14 @@ __global__ void __launch_bounds__(kO2Threads, 1)
               uint8_t *sb = sa + kOzSlices * kP2TileA;
               if (rank == 0) mbar_expect_tx(&full_bar[st], 2 * ns * (kP2TileA + kP2TileB));
               const uint32_t lb = tc::mapa(&full_bar[st], 0);
-              tc::tma_load_3d_pair(sa, ma, kb * kO2BK, static_cast<int32_t>(q0), 0, lb);
-              tc::tma_load_3d_pair(sb, mb, kb * kO2BK, tb, 0, lb);
+              if constexpr (kTiled) {   // 256-byte box rows: 16 per A tile, 8 per B tile
+                tc::tma_load_3d_pair(sa, ma, 0, static_cast<int32_t>((q0 / 128 * nkb + kb) * 16),
+                                     0, lb);
+                tc::tma_load_3d_pair(sb, mb, 0, (tb / kP2HalfN * nkb + kb) * 8, 0, lb);
+              } else {
+                tc::tma_load_3d_pair(sa, ma, kb * kO2BK, static_cast<int32_t>(q0), 0, lb);
+                tc::tma_load_3d_pair(sb, mb, kb * kO2BK, tb, 0, lb);
+              }
             }
           }
         }
@@ -498,7 +542,7 @@ __global__ void __launch_bounds__(kO2Threads, 1)
       constexpr uint32_t idesc = tc::idesc_i8(256, kP2BN, false, false);
       const uint32_t ring = smem_u32(smem);
       uint32_t ph = 0;
-      int k = 0;
+      int k = 0, mstage = 0;
       for (int w = cid; w < ntiles; w += ncl, ++k) {
         PP_STAMP(k, 0);
         if (k > 0) {   // the previous tile's pass-2 accumulators drained
@@ -513,6 +557,11 @@ __global__ void __launch_bounds__(kO2Threads, 1)
             if (kb >= nkb) break;
             mbar_wait(&full_bar[st], (ph >> st) & 1);
             ph ^= 1u << st;
+            if constexpr ((kDiag & 8) != 0) {
+              if (blockIdx.x == 0 && mstage < 4096)
+                out[65536 + 2 * mstage + 1] = static_cast<double>(clock64());
+              ++mstage;
+            }
             tc::fence_after();
             const uint32_t sa = ring + st * kP2StageBytes;
             const uint32_t sb = sa + kOzSlices * kP2TileA;
@@ -541,6 +590,11 @@ __global__ void __launch_bounds__(kO2Threads, 1)
             if (kb >= nkb) break;
             mbar_wait(&full_bar[st], (ph >> st) & 1);
             ph ^= 1u << st;
+            if constexpr ((kDiag & 8) != 0) {
+              if (blockIdx.x == 0 && mstage < 4096)
+                out[65536 + 2 * mstage + 1] = static_cast<double>(clock64());
+              ++mstage;
+            }
             tc::fence_after();
             const uint32_t sa = ring + st * kP2StageBytes;
             const uint32_t sb = sa + kOzSlices * kP2TileA;
@@ -751,7 +805,34 @@ static int slice_map(CUtensorMap *map, const uint8_t *base, int64_t outer, int64
   return 0;
 }
 
-template <int kS, int kMaxL>
+// 3-D u8 map over a tiled layout [7][units][256 B]: box {256, box_units,
+// box_slices}, no swizzle (the bytes already are the swizzled image).
+static int tiled_map(CUtensorMap *map, const uint8_t *base, int64_t units, uint32_t box_units,
+                     uint32_t box_slices) {
+  auto fn = encode_fn();
+  if (!fn) return fail(PF_E_LAUNCH, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {256, static_cast<cuuint64_t>(units), static_cast<cuuint64_t>(kOzSlices)};
+  cuuint64_t strides[2] = {256, static_cast<cuuint64_t>(units * 256)};
+  cuuint32_t box[3] = {256, box_units, box_slices};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t *>(base), dims,
+                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(PF_E_ARG, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return 0;
+}
+
+template <int kS, int kMaxL, bool kTiled>
+static auto pp_kernel(int diag) {
+  return diag == 1    ? batched_kl_i8_pp_kernel<kS, kMaxL, 1, kTiled>
+         : diag == 2  ? batched_kl_i8_pp_kernel<kS, kMaxL, 2, kTiled>
+         : diag == 3  ? batched_kl_i8_pp_kernel<kS, kMaxL, 3, kTiled>
+         : diag == 4  ? batched_kl_i8_pp_kernel<kS, kMaxL, 4, kTiled>
+         : diag == 10 ? batched_kl_i8_pp_kernel<kS, kMaxL, 10, kTiled>
+                      : batched_kl_i8_pp_kernel<kS, kMaxL, 0, kTiled>;
+}
+
+template <int kS, int kMaxL, bool kTiled = false>
 static int launch_i8(const CUtensorMap (&m)[4], const int32_t *ea, const int32_t *eb,
                      int64_t rows, int64_t T, int64_t k, const double *H, const int64_t *targets,
                      double tau, int64_t row0, double *out, int64_t ldo, bool pair,
@@ -763,13 +844,7 @@ static int launch_i8(const CUtensorMap (&m)[4], const int32_t *ea, const int32_t
       const char *e = getenv("PF_K7_DIAG");
       return e ? atoi(e) : 0;
     }();
-    auto kern = diag == 1   ? batched_kl_i8_pp_kernel<kS, kMaxL, 1>
-                : diag == 2 ? batched_kl_i8_pp_kernel<kS, kMaxL, 2>
-                : diag == 3 ? batched_kl_i8_pp_kernel<kS, kMaxL, 3>
-                : diag == 4 ? batched_kl_i8_pp_kernel<kS, kMaxL, 4>
-                : diag == 6 ? batched_kl_i8_pp_kernel<kS, kMaxL, 6>
-                : diag == 7 ? batched_kl_i8_pp_kernel<kS, kMaxL, 7>
-                            : batched_kl_i8_pp_kernel<kS, kMaxL, 0>;
+    auto kern = pp_kernel<kS, kMaxL, kTiled>(diag);
     if (int e = ensure_smem((const void *)kern, kP2Smem)) return e;
     const unsigned ttiles = static_cast<unsigned>((T + kP2BN - 1) / kP2BN);
     const unsigned row_pairs = (tiles + 1) / 2;
@@ -822,9 +897,29 @@ int pf_slice_rows_u8(const double *P, int64_t ld, int64_t rows, int64_t k, doubl
   if (rows <= 0) return 0;
   if (!P || !slices || !exps || k <= 0 || ldk < k || ldk % kOzPad)
     return fail(PF_E_ARG, "slice_rows: bad args (ldk %% 64 == 0, ldk >= k)");
-  slice_rows_kernel<<<sm_count() * 8, 256, 0, as_stream(stream)>>>(P, ld, rows, k, clamp, ldk,
-                                                                    slices, exps);
+  slice_rows_kernel<<<sm_count() * 8, 256, 0, as_stream(stream)>>>(
+      P, ld, rows, rows, k, clamp, SliceLayout{ldk, 0, 0}, rows * ldk, slices, exps);
   return check_launch("slice_rows");
+}
+
+int64_t pf_i8_tiled_bytes(int64_t n, int64_t k) {
+  if (n <= 0 || k <= 0) return 0;
+  return int64_t(kOzSlices) * ((n + 127) / 128 * 128) * ((k + kO2BK - 1) / kO2BK * kO2BK);
+}
+
+int pf_slice_rows_u8_tiled(const double *P, int64_t ld, int64_t rows, int64_t k, double clamp,
+                           uint8_t *tiles, int32_t *exps, pf_stream_t stream) {
+  if (rows <= 0) return 0;
+  if (!P || !tiles || !exps || k <= 0 || ld < k)
+    return fail(PF_E_ARG, "slice_rows_tiled: bad args");
+  if (reinterpret_cast<uintptr_t>(tiles) & 15)
+    return fail(PF_E_ALIGN, "slice_rows_tiled: tiles must be 16-byte aligned");
+  const int nkb = static_cast<int>((k + kO2BK - 1) / kO2BK);
+  const int64_t rows_pad = (rows + 127) / 128 * 128;
+  slice_rows_kernel<<<sm_count() * 8, 256, 0, as_stream(stream)>>>(
+      P, ld, rows, rows_pad, k, clamp, SliceLayout{0, 128, nkb}, pf_i8_tiled_bytes(rows, k) / 7,
+      tiles, exps);
+  return check_launch("slice_rows_tiled");
 }
 
 int pf_slice_targets_u8(const double *L, int64_t ldl, int64_t T, int64_t k, int64_t ldk,
@@ -833,8 +928,22 @@ int pf_slice_targets_u8(const double *L, int64_t ldl, int64_t T, int64_t k, int6
   if (!L || !slices || !exps || k <= 0 || ldk < k || ldk % kOzPad)
     return fail(PF_E_ARG, "slice_targets: bad args (ldk %% 64 == 0, ldk >= k)");
   slice_targets_kernel<<<static_cast<unsigned>(T), 256, 0, as_stream(stream)>>>(
-      L, ldl, T, k, ldk, slices, exps, bad);
+      L, ldl, T, k, SliceLayout{ldk, 0, 0}, T * ldk, slices, exps, bad);
   return check_launch("slice_targets");
+}
+
+int pf_slice_targets_u8_tiled(const double *L, int64_t ldl, int64_t T, int64_t k, uint8_t *tiles,
+                              int32_t *exps, uint32_t *bad, pf_stream_t stream) {
+  if (T <= 0) return 0;
+  if (!L || !tiles || !exps || k <= 0 || ldl < k)
+    return fail(PF_E_ARG, "slice_targets_tiled: bad args");
+  if (reinterpret_cast<uintptr_t>(tiles) & 15)
+    return fail(PF_E_ALIGN, "slice_targets_tiled: tiles must be 16-byte aligned");
+  const int nkb = static_cast<int>((k + kO2BK - 1) / kO2BK);
+  const int64_t T_pad = (T + 127) / 128 * 128;
+  slice_targets_kernel<<<static_cast<unsigned>(T_pad), 256, 0, as_stream(stream)>>>(
+      L, ldl, T, k, SliceLayout{0, kP2HalfN, nkb}, pf_i8_tiled_bytes(T, k) / 7, tiles, exps, bad);
+  return check_launch("slice_targets_tiled");
 }
 
 int pf_batched_kl_i8(const uint8_t *A, const int32_t *ea, int64_t rows, const uint8_t *B,
@@ -872,6 +981,35 @@ int pf_batched_kl_i8_listed(const uint8_t *A, const int32_t *ea, int64_t rows, c
                                        pair, guard_list, guard_cap, as_stream(stream))
                      : launch_i8<5, 6>(m, ea, eb, rows, T, k, H, targets, tau, row0, out, ldo,
                                        pair, guard_list, guard_cap, as_stream(stream));
+}
+
+int pf_batched_kl_i8_tiled(const uint8_t *A, const int32_t *ea, int64_t rows, const uint8_t *B,
+                           const int32_t *eb, int64_t T, int64_t k, const double *H,
+                           const int64_t *targets, double tau, int64_t row0, double *out,
+                           int64_t ldo, int grade, int64_t *guard_list, int64_t guard_cap,
+                           pf_stream_t stream) {
+  if (grade != 64 && grade != 32) return fail(PF_E_ARG, "batched_kl_i8: grade must be 64 or 32");
+  const int kS = grade == 64 ? kOzSlices : 5;
+  if (rows <= 0 || T <= 0) return 0;
+  if (!A || !ea || !B || !eb || !H || !targets || !out) return fail(PF_E_ARG, "batched_kl_i8: null");
+  if (k > kOzMaxK) return fail(PF_E_DOMAIN, "batched_kl_i8: k = %lld > %d", (long long)k, kOzMaxK);
+  if (ldo < T) return fail(PF_E_ALIGN, "batched_kl_i8: ldo >= T");
+  if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15)
+    return fail(PF_E_ALIGN, "batched_kl_i8: tiles must be 16-byte aligned");
+  const int64_t row_tiles = (rows + 127) / 128;
+  if (row_tiles > 65535) return fail(PF_E_DOMAIN, "batched_kl_i8: too many rows per launch");
+  const int64_t ua = pf_i8_tiled_bytes(rows, k) / 7 / 256, ub = pf_i8_tiled_bytes(T, k) / 7 / 256;
+  if (ua > INT32_MAX || ub > INT32_MAX) return fail(PF_E_DOMAIN, "batched_kl_i8: operand too large");
+  CUtensorMap m[4];
+  if (int e = tiled_map(&m[0], A, ua, kP2TileA / 256, kS)) return e;
+  if (int e = tiled_map(&m[1], A, ua, kP2TileA / 256, kO2Pass1Slices)) return e;
+  if (int e = tiled_map(&m[2], B, ub, kP2TileB / 256, kS)) return e;
+  if (int e = tiled_map(&m[3], B, ub, kP2TileB / 256, kO2Pass1Slices)) return e;
+  return grade == 64
+             ? launch_i8<7, 9, true>(m, ea, eb, rows, T, k, H, targets, tau, row0, out, ldo, true,
+                                     guard_list, guard_cap, as_stream(stream))
+             : launch_i8<5, 6, true>(m, ea, eb, rows, T, k, H, targets, tau, row0, out, ldo, true,
+                                     guard_list, guard_cap, as_stream(stream));
 }
 
 int pf_probe_umma_i8(int64_t iters, int random_operands, int64_t *ops_host, uint32_t *sink,

@@ -454,12 +454,19 @@ def _kl_batch_slab(dk, tg, Pt, c: float, method: str, out=None):
     if use_i8:
         if dk.k > I8_MAX_K:
             raise ValueError(f"method={method!r} needs k <= {I8_MAX_K} (k = {dk.k})")
-        A, ea, ldk = dk.slices(c)
-        B = t.empty((7, T, ldk), dtype=t.uint8, device=dk.device)
+        tiled = bool(I8_CTA_PAIR)
         eb = t.empty(T, dtype=t.int32, device=dk.device)
         bad = t.zeros(1, dtype=t.int32, device=dk.device)
-        nat.call("pf_slice_targets_u8", L.data_ptr(), ldl, T, dk.k, ldk, B.data_ptr(),
-                 eb.data_ptr(), bad.data_ptr(), s.cuda_stream)
+        if tiled:   # the CTA-pair kernel streams the tiled layout
+            A, ea = dk.slices_tiled(c)
+            B = t.empty(dev.i8_tiled_bytes(T, dk.k), dtype=t.uint8, device=dk.device)
+            nat.call("pf_slice_targets_u8_tiled", L.data_ptr(), ldl, T, dk.k, B.data_ptr(),
+                     eb.data_ptr(), bad.data_ptr(), s.cuda_stream)
+        else:
+            A, ea, ldk = dk.slices(c)
+            B = t.empty((7, T, ldk), dtype=t.uint8, device=dk.device)
+            nat.call("pf_slice_targets_u8", L.data_ptr(), ldl, T, dk.k, ldk, B.data_ptr(),
+                     eb.data_ptr(), bad.data_ptr(), s.cuda_stream)
         if bool(bad.item()):
             if method != "auto":
                 raise ValueError(f"method={method!r}: a target row has an entry above 1")
@@ -469,10 +476,16 @@ def _kl_batch_slab(dk, tg, Pt, c: float, method: str, out=None):
         cap = guard_list_cap(dk.rows, T)
         glist = dk.scratch(s.cuda_stream, 8 * (cap + 1), "k7_guards").view(t.int64)
         glist[:1].zero_()
-        nat.call("pf_batched_kl_i8_listed", A.data_ptr(), ea.data_ptr(), dk.rows, B.data_ptr(),
-                 eb.data_ptr(), T, dk.k, ldk, H.data_ptr(), tg.data_ptr(), KL_GUARD_TAU,
-                 dk.row0, out.data_ptr(), out.stride(0), 32 if method == "i8-f32" else 64,
-                 int(I8_CTA_PAIR), glist.data_ptr(), cap, s.cuda_stream)
+        grade = 32 if method == "i8-f32" else 64
+        if tiled:
+            nat.call("pf_batched_kl_i8_tiled", A.data_ptr(), ea.data_ptr(), dk.rows, B.data_ptr(),
+                     eb.data_ptr(), T, dk.k, H.data_ptr(), tg.data_ptr(), KL_GUARD_TAU, dk.row0,
+                     out.data_ptr(), out.stride(0), grade, glist.data_ptr(), cap, s.cuda_stream)
+        else:
+            nat.call("pf_batched_kl_i8_listed", A.data_ptr(), ea.data_ptr(), dk.rows,
+                     B.data_ptr(), eb.data_ptr(), T, dk.k, ldk, H.data_ptr(), tg.data_ptr(),
+                     KL_GUARD_TAU, dk.row0, out.data_ptr(), out.stride(0), grade, 0,
+                     glist.data_ptr(), cap, s.cuda_stream)
         nat.call("pf_batched_kl_fixup_list_f64", dk.P.data_ptr(), dk.ld, dk.rows, dk.k,
                  Tc.data_ptr(), ldl, T, c, out.data_ptr(), out.stride(0),
                  tflag.data_ptr() + 4 * T, glist.data_ptr(), cap, s.cuda_stream)

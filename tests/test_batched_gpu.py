@@ -225,3 +225,55 @@ def test_guard_list_fixup_matches_scan_fixup_and_overflow():
     assert res["overflow"][2] == n_scan > 3 and res["overflow"][1] == n_scan
     for mode in ("list", "overflow"):
         assert torch.equal(res[mode][0].view(torch.int64), res["scan"][0].view(torch.int64)), mode
+
+
+@pytest.mark.parametrize("rows,k,T", [(129, 64, 64), (300, 200, 50), (1000, 1234, 130)])
+def test_tiled_slices_are_the_swizzled_row_major_planes(rows, k, T):
+    """pf_slice_rows_u8_tiled / pf_slice_targets_u8_tiled write the same bytes
+    as the row-major slicing, permuted into R x 32-byte SWIZZLE_32B tiles
+    (chunk c of row r at r * 32 + (c ^ (r >> 2 & 1)) * 16), zero padded."""
+    import torch
+    from paper_1708_02845_b200 import _device as dev
+    from paper_1708_02845_b200 import _native as nat
+    rng = np.random.default_rng(rows + k)
+    P = rng.random((rows, k)) ** 3
+    P /= P.sum(axis=1, keepdims=True)
+    Pd = torch.from_numpy(P).cuda()
+    s = torch.cuda.current_stream().cuda_stream
+    ldk = dev.round_up(k, 64)
+
+    def untile(buf, n, R):
+        nkb = (k + 31) // 32
+        npad = (n + 127) // 128 * 128
+        tiles = buf.reshape(7, npad // R, nkb, R, 2, 16)
+        r = np.arange(R)
+        swz = (r >> 2) & 1
+        un = np.empty_like(tiles)
+        for c in (0, 1):   # smem chunk c holds logical chunk c ^ swz
+            un[:, :, :, r, c ^ swz, :] = tiles[:, :, :, r, c, :]
+        return un.transpose(0, 1, 3, 2, 4, 5).reshape(7, npad, nkb * 32)
+
+    for what, n, R in (("rows", rows, 128), ("targets", T, 64)):
+        src = Pd if what == "rows" else torch.log(Pd[:n].clamp_min(1e-300))
+        plain = torch.zeros((7, n, ldk), dtype=torch.uint8, device="cuda")
+        tiled = torch.full((dev.i8_tiled_bytes(n, k),), 0xAB, dtype=torch.uint8, device="cuda")
+        e1 = torch.empty(n, dtype=torch.int32, device="cuda")
+        e2 = torch.empty_like(e1)
+        if what == "rows":
+            nat.call("pf_slice_rows_u8", src.data_ptr(), k, n, k, 1e-300, ldk, plain.data_ptr(),
+                     e1.data_ptr(), s)
+            nat.call("pf_slice_rows_u8_tiled", src.data_ptr(), k, n, k, 1e-300, tiled.data_ptr(),
+                     e2.data_ptr(), s)
+        else:
+            L = src.contiguous()
+            nat.call("pf_slice_targets_u8", L.data_ptr(), k, n, k, ldk, plain.data_ptr(),
+                     e1.data_ptr(), 0, s)
+            nat.call("pf_slice_targets_u8_tiled", L.data_ptr(), k, n, k, tiled.data_ptr(),
+                     e2.data_ptr(), 0, s)
+        torch.cuda.synchronize()
+        assert torch.equal(e1, e2)
+        un = untile(tiled.cpu().numpy(), n, R)
+        kk = (k + 31) // 32 * 32
+        want = np.zeros_like(un)
+        want[:, :n, :min(kk, ldk)] = plain.cpu().numpy()[:, :, :kk]
+        np.testing.assert_array_equal(un, want, err_msg=what)

@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(384, 1)
 // shape) vs 1-D bulk copies of the same bytes, 4-deep ring, all SMs.
 __global__ void __launch_bounds__(128, 1)
     tma_rate_kernel(const __grid_constant__ CUtensorMap map, const uint8_t *flat, int64_t flat_bytes,
-                    int iters, int box_k, int bulk, unsigned long long *cycles) {
+                    int iters, int box_k, int bulk, unsigned long long *cycles, int rtiles) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -381,8 +381,13 @@ __global__ void __launch_bounds__(128, 1)
       if (it >= 4) mbar_wait(&bar[s], ((it >> 2) - 1) & 1);
       mbar_expect_tx(&bar[s], bytes);
       const int kb = (it * 7 + blockIdx.x * 13) % 120;
-      const int rt = (blockIdx.x * 37 + it / 120) % 256;
-      if (bulk) {
+      const int rt = (blockIdx.x * 37 + it / 120) % rtiles;
+      if (bulk >= 2) {   // pre-tiled operand: 3-D box {256 or 128 B, rows of it, 7}
+        const int br = bulk == 2 ? 16 : 32;
+        const int64_t units = flat_bytes / 7 / (bulk == 2 ? 256 : 128);
+        const int64_t u = ((static_cast<int64_t>(rt) * 120 + kb) * br) % (units - br);
+        tc::tma_load_3d(smem + s * 65536, &map, 0, static_cast<int32_t>(u), 0, &bar[s]);
+      } else if (bulk) {
         const int64_t off = ((static_cast<int64_t>(rt) * 120 + kb) * bytes) % (flat_bytes - bytes);
         bulk_g2s(smem + s * 65536, flat + (off & ~15ll), bytes, &bar[s]);
       } else {
@@ -453,8 +458,8 @@ void run(const char *name, int tma_per_iter, const uint8_t *gsrc, int64_t gbytes
 }
 
 #include <cudaTypedefs.h>
-static void tma_rate(int box_k, int bulk) {
-  const int64_t rows = 256 * 128, ldk = 4160;   // 7 x 32768 x 4160 = 954 MB (> L2)
+static void tma_rate(int box_k, int bulk, int64_t rows = 256 * 128) {
+  const int64_t ldk = 4160;   // 7 x rows x 4160 (rows 32768: 954 MB > L2; 2048: 60 MB, L2-resident)
   uint8_t *A;
   CK(cudaMalloc(&A, 7 * rows * ldk));
   CK(cudaMemset(A, 3, 7 * rows * ldk));
@@ -467,9 +472,18 @@ static void tma_rate(int box_k, int bulk) {
   cuuint64_t strides[2] = {(cuuint64_t)ldk, (cuuint64_t)(rows * ldk)};
   cuuint32_t box[3] = {(cuuint32_t)box_k, 128, 7};
   cuuint32_t es[3] = {1, 1, 1};
-  const CUtensorMapSwizzle sw = box_k == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
-                                : box_k == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
-                                              : CU_TENSOR_MAP_SWIZZLE_32B;
+  CUtensorMapSwizzle sw = box_k == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                          : box_k == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                        : CU_TENSOR_MAP_SWIZZLE_32B;
+  if (bulk >= 2) {   // the same bytes viewed as [7][rows * ldk / W][W], W = 256 or 128
+    const int64_t W = bulk == 2 ? 256 : 128;
+    dims[0] = W;
+    dims[1] = rows * ldk / W;
+    strides[0] = W;
+    box[0] = (cuuint32_t)W;
+    box[1] = bulk == 2 ? 16 : 32;
+    sw = CU_TENSOR_MAP_SWIZZLE_NONE;
+  }
   if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, A, dims, strides, box, es,
           CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
@@ -487,7 +501,8 @@ static void tma_rate(int box_k, int bulk) {
   float best = 1e30f;
   for (int rep = 0; rep < 3; ++rep) {
     CK(cudaEventRecord(e0));
-    tma_rate_kernel<<<148, 128, 4 * 57344 + 1024>>>(map, A, 7 * rows * ldk, iters, box_k, bulk, cyc);
+    tma_rate_kernel<<<148, 128, 4 * 57344 + 1024>>>(map, A, 7 * rows * ldk, iters, box_k, bulk, cyc,
+                                                   static_cast<int>(rows / 128));
     CK(cudaEventRecord(e1));
     CK(cudaEventSynchronize(e1));
     float ms;
@@ -499,8 +514,8 @@ static void tma_rate(int box_k, int bulk) {
   double mx = 0;
   for (auto v : h) mx = mx > v ? mx : v;
   const double bytes = 7.0 * 128 * box_k * iters;
-  printf("{\"tma_rate\": \"%s box_k %d\", \"ms\": %.3f, \"chip_TBps\": %.2f, \"B_per_clk_per_sm\": %.1f}\n",
-         bulk ? "bulk" : "tensor3d", box_k, best, bytes * 148 / (best * 1e-3) / 1e12, bytes / mx);
+  printf("{\"tma_rate\": \"%s box_k %d rows %lld\", \"ms\": %.3f, \"chip_TBps\": %.2f, \"B_per_clk_per_sm\": %.1f}\n",
+         bulk == 3 ? "tiled128" : bulk == 2 ? "tiled256" : bulk ? "bulk" : "tensor3d", box_k, (long long)rows, best, bytes * 148 / (best * 1e-3) / 1e12, bytes / mx);
   fflush(stdout);
   CK(cudaFree(A));
   CK(cudaFree(cyc));
@@ -518,9 +533,8 @@ int main() {
   CK(cudaMalloc(&cyc, 2 * 148 * 8));
   CK(cudaMemset(cyc, 0, 2 * 148 * 8));
   // K7 per CTA per 34 MMAs: 1-CTA 11 slices x 8 KB = 88 KB, pair 11 x 6 KB = 66 KB
-  tma_rate(32, 0);
-  tma_rate(32, 1);
-  tma_rate(64, 0);
+  for (int64_t rows : {2048, 256 * 128})
+    for (int mode : {0, 1, 2, 3}) tma_rate(32, mode, rows);
   return 0;
   for (int m : {10, 11, 35, 36}) {
     char nm[96];
