@@ -48,6 +48,7 @@
 #include <cudaTypedefs.h>
 
 #include <cmath>
+#include <type_traits>
 
 #include "pf_common.cuh"
 #include "pf_tc.cuh"
@@ -160,7 +161,10 @@ __global__ void __launch_bounds__(256) slice_targets_kernel(const double *__rest
   const int e = scale_exp(m);
   if (live && threadIdx.x == 0) {
     exps[t] = e;
-    if (neg && bad) atomicOr(bad, 1u);
+    // the pair kernel's epilogue packs eb + 64 into a byte (-L is 0 or
+    // >= 2^-53, so eb >= -52 for any P <= 1; a target above that range is
+    // a target row with an entry above 1 anyway)
+    if ((neg || e < -64 || e > 191) && bad) atomicOr(bad, 1u);
   }
   const int64_t span = lay.kspan();
   for (int64_t b0 = 8 * threadIdx.x; b0 < span; b0 += 8 * blockDim.x) {
@@ -186,6 +190,60 @@ __device__ __forceinline__ double pow2_scale(double v, int e) {
   e = max(-1922, min(1922, e));
   const int e1 = max(-900, min(900, e));
   return (v * pow2_exact(e1)) * pow2_exact(e - e1);
+}
+
+// The epilogue value of one (row, target) from S = v 2^e >= 0: the split
+// form h + S, or the guard sentinel when |h + S| < tau (|h| + S) (evaluated
+// as fma(tau, S, tau |h|) -- two FP64 instructions per element in all: FP64
+// issue is starved while the int8 MMAs run, ~5x slower than with the tensor
+// pipe idle, measured by the stage stamps), settled, or 0 at the target.
+// settle and the guard compare are integer compares of the bit patterns
+// (same results as the FP64 forms for every input: the operands are finite
+// and the magnitude bits of doubles order like the values).
+__device__ __forceinline__ double k7_value(double S, double h, double tau, double tau_h, bool is_t,
+                                           bool &guard) {
+  const double val = h + S;
+  const double thr = fma(tau, S, tau_h);
+  // magnitude bits from the 32-bit halves (a 64-bit mask of the sign bit
+  // would be folded back into an FP64 |x|)
+  const int hi = __double2hiint(val);
+  const unsigned lo = static_cast<unsigned>(__double2loint(val));
+  const long long mag = (static_cast<long long>(hi & 0x7fffffff) << 32) | lo;
+  guard = !is_t && mag < __double_as_longlong(thr);
+  const bool noise = hi < 0 && mag != 0 && mag < __double_as_longlong(kNegNoise);   // settle()
+  return guard ? __longlong_as_double(static_cast<long long>(kOzGuard))
+               : ((is_t || noise) ? 0.0 : val);
+}
+
+// RNE((a0 2^24 + a1 2^16 + a2 2^8 + a3) 2^-24) for the s32 (non-negative)
+// level accumulators of one pass: the same value as the FP64 chain
+// x = a3; x = fma(x, 2^-8, a_l) for l = 2, 1, 0 (whose first two steps are
+// exact, so it rounds once), from one 64-bit integer sum split into two
+// exactly representable halves: 3 FP64 adds instead of 4 s32->f64
+// conversions (4x slower than an add) and 3 FMAs.
+__device__ __forceinline__ double levels4_f64(uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3) {
+  const unsigned long long X = static_cast<unsigned long long>(a3) +
+                               (static_cast<unsigned long long>(a2) << 8) +
+                               (static_cast<unsigned long long>(a1) << 16) +
+                               (static_cast<unsigned long long>(a0) << 24);   // < 2^56
+  const double dh = __hiloint2double(0x43B00000, static_cast<int>(X >> 32)) - 0x1p60;   // Xh 2^8
+  const double dl = __hiloint2double(0x41B00000, static_cast<int>(static_cast<uint32_t>(X))) -
+                    0x1p28;   // Xl 2^-24
+  return dh + dl;
+}
+__device__ __forceinline__ double u32_f64(uint32_t a) {   // exact
+  return __hiloint2double(0x43300000, static_cast<int>(a)) - 0x1p52;
+}
+
+// v 2^e for v = 0 or within [2^-64, 2^64] and e within [-958, 959]: the
+// exponent field moves, exactly (the result is normal).
+__device__ __forceinline__ double pow2_scale_normal(double v, int e) {
+  const long long b = __double_as_longlong(v);
+  const int hi = static_cast<int>(b >> 32);
+  return hi == 0 ? 0.0 : __hiloint2double(hi + (e << 20), static_cast<int>(b));
+}
+__device__ __forceinline__ double k7_scale(double v, int e) {   // == pow2_scale
+  return (e >= -958 && e <= 959) ? pow2_scale_normal(v, e) : pow2_scale(v, e);
 }
 
 // Append the guarded (q, t) pairs of one thread's columns to the fixup list
@@ -371,15 +429,10 @@ __global__ void __launch_bounds__(kO2Threads, 1) batched_kl_i8_n128_kernel(
 #pragma unroll
         for (int l = kL2 - 2; l >= 0; --l) v = fma(v, 0x1p-8, static_cast<double>(acc[l][u]));
         v = fma(v, 0x1p-32, v1[c0 + u]);
-        const double S = pow2_scale(v, e_q + eb[t] - 16);
-        double val = h + S;
-        const bool is_t = (tq == targets[t]);
-        if (!is_t && fabs(val) < tau * (fabs(h) + fabs(S))) {
-          val = __longlong_as_double(static_cast<long long>(kOzGuard));
-          gmask |= 1ull << (c0 + u);
-        } else {
-          val = is_t ? 0.0 : settle(val);
-        }
+        const double S = k7_scale(v, e_q + eb[t] - 16);
+        bool guard;
+        const double val = k7_value(S, h, tau, tau * fabs(h), tq == targets[t], guard);
+        if (guard) gmask |= 1ull << (c0 + u);
         out[q * ldo + t] = val;
       }
     }
@@ -419,7 +472,7 @@ __device__ __forceinline__ uint32_t smid() {
 //
 // kDiag (timing diagnostics only, PF_K7_DIAG, wrong outputs): bit 0 = no TMA
 // loads (the MMAs run on stale shared memory), bit 1 = no epilogue arithmetic
-// or stores, bit 2 = %globaltimer phase stamps of cluster 0 per tile k at
+// or stores, bit 2 = SM-clock phase stamps of cluster 0 per tile k at
 // out[k * 16 + i] (tools/probe_k7pp_stamps.py), bit 3 = per-stage timeline of
 // cluster 0's leader in SM clocks (%globaltimer ticks too coarsely for
 // stage-sized gaps): load issue at out[65536 + 2 s], full-barrier pass at
@@ -454,11 +507,11 @@ __global__ void __launch_bounds__(kO2Threads, 1)
   const uint32_t rank = tc::cluster_rank();   // 0 = leader (issues the MMAs)
   const int cid = static_cast<int>(blockIdx.x >> 1), ncl = static_cast<int>(gridDim.x >> 1);
   // tile w: row pair w / t_tiles, target tile w % t_tiles
-  // kDiag & 4: %globaltimer stamps of cluster 0's leader, per tile k, at out[k * 16 + i]
+  // kDiag & 4: SM-clock stamps of cluster 0's leader, per tile k, at out[k * 16 + i]
   const bool stamping = (kDiag & 4) != 0 && blockIdx.x == 0;
 #define PP_STAMP(k, i) \
   do {                 \
-    if (stamping) out[(k) * 16 + (i)] = static_cast<double>(gtimer()); \
+    if (stamping) out[(k) * 16 + (i)] = static_cast<double>(clock64()); \
   } while (0)
 
   if (tid == 0) {
@@ -571,6 +624,7 @@ __global__ void __launch_bounds__(kO2Threads, 1)
               for (int j = 1; j <= kO2Pass1Slices; ++j) {
                 const int l = i + j;
                 if (l > 5) continue;
+                if constexpr ((kDiag & 32) != 0) continue;   // no MMAs (commits only)
                 tc::mma_i8_pair(tmem + (l - 2) * kP2BN, tc::sdesc<32>(sa + (i - 1) * kP2TileA),
                                 tc::sdesc<32>(sb + (j - 1) * kP2TileB), idesc,
                                 !(kb == 0 && i == 1));
@@ -604,6 +658,7 @@ __global__ void __launch_bounds__(kO2Threads, 1)
               for (int j = 1; j <= kS; ++j) {
                 const int l = i + j;
                 if (l < 6 || l > kMaxL) continue;
+                if constexpr ((kDiag & 32) != 0) continue;
                 const int first_i = l - kS > 1 ? l - kS : 1;
                 tc::mma_i8_pair(tmem + (l - 6) * kP2BN, tc::sdesc<32>(sa + (i - 1) * kP2TileA),
                                 tc::sdesc<32>(sb + (j - 1) * kP2TileB), idesc,
@@ -640,12 +695,7 @@ __global__ void __launch_bounds__(kO2Threads, 1)
         for (int l = 0; l < 4; ++l) tc::tmem_ld4(base + l * kP2BN + c0, acc[l]);
         tc::tmem_ld_wait();
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          double x = static_cast<double>(acc[3][u]);
-#pragma unroll
-          for (int l = 2; l >= 0; --l) x = fma(x, 0x1p-8, static_cast<double>(acc[l][u]));
-          v[c0 + u] = x;
-        }
+        for (int u = 0; u < 4; ++u) v[c0 + u] = levels4_f64(acc[0][u], acc[1][u], acc[2][u], acc[3][u]);
       }
       tc::fence_before();
       __syncwarp();
@@ -662,9 +712,9 @@ __global__ void __launch_bounds__(kO2Threads, 1)
         tc::tmem_ld_wait();
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          double x = static_cast<double>(acc[kL2 - 1][u]);
-#pragma unroll
-          for (int l = kL2 - 2; l >= 0; --l) x = fma(x, 0x1p-8, static_cast<double>(acc[l][u]));
+          static_assert(kL2 == 4 || kL2 == 1, "pass-2 level count");
+          const double x = kL2 == 4 ? levels4_f64(acc[0][u], acc[1][u], acc[2][u], acc[kL2 - 1][u])
+                                    : u32_f64(acc[0][u]);
           v[c0 + u] = fma(x, 0x1p-32, v[c0 + u]);
         }
       }
@@ -673,46 +723,114 @@ __global__ void __launch_bounds__(kO2Threads, 1)
       if (lane == 0) tc::mbar_arrive_cluster(free_leader);   // TMEM free for the next tile
       if (tid == 64) PP_STAMP(k, 8);
       if constexpr ((kDiag & 2) != 0) continue;
-      // Branch-free per element (the epilogue has 2 warps per scheduler and
-      // FP64 latency to hide: a branchy element body serialised it to ~1 us
-      // per element-row, longer than pass 1): the column data (eb, target)
-      // is loaded once per lane and broadcast by shuffles, the 2^e scaling
-      // is two exact power-of-two multiplies, the guard/settle are selects.
+      // Per element ~20 ALU / FP64 instructions and no shared-memory or
+      // shuffle traffic: the tensor core's operand reads plus the TMA writes
+      // take ~95% of the SM's shared-memory bandwidth while the MMAs run, so
+      // every LDS / SHFL in this loop waits behind them (a per-element column
+      // broadcast through either cost ~1.5K clocks per element-column and made
+      // the epilogue longer than the next tile's pass 1).  Per tile instead:
+      //  * the 64 column exponents eb are loaded once (16 x 16-byte loads) and
+      //    packed as bytes eb + 64 into 16 registers;
+      //  * the columns whose target row is this lane's row form a 64-bit mask
+      //    built from ballots over the owner-lane bits (at most one row per
+      //    column);
+      //  * the scale 2^(ea + eb - 16) is three power-of-two multiplies:
+      //    v * 2^eb and then * 2^max(e_q, -900) are exact (v is 0 or within
+      //    [2^-64, 2^64], eb within [-52, 12]: -L is 0 or >= 2^-53; the
+      //    slicing flags anything outside [-64, 191] as bad), the last
+      //    multiply rounds once -- the single rounding of ldexp.
+      auto pack4 = [](int a, int b, int c, int d) -> uint32_t {
+        return (static_cast<uint32_t>(a + 64) & 255u) | ((static_cast<uint32_t>(b + 64) & 255u) << 8) |
+               ((static_cast<uint32_t>(c + 64) & 255u) << 16) | (static_cast<uint32_t>(d + 64) << 24);
+      };
+      const bool eb_vec = tc0 + 64 <= T && (reinterpret_cast<uintptr_t>(eb) & 15) == 0;
+      // 8 packed registers of 32 column exponents (the loop runs in two
+      // halves so that v[64] + these fit the 168-register budget of 10 warps)
+      auto load_eb = [&](int c0, uint32_t (&ebp)[8]) {
+        if (eb_vec) {
+          const int4 *ev = reinterpret_cast<const int4 *>(eb + tc0 + c0);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int4 e4 = __ldg(ev + j);
+            ebp[j] = pack4(e4.x, e4.y, e4.z, e4.w);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            int e4[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int64_t tt = tc0 + c0 + 4 * j + u;
+              e4[u] = tt < T ? eb[tt] : 0;
+            }
+            ebp[j] = pack4(e4[0], e4[1], e4[2], e4[3]);
+          }
+        }
+      };
+      const long long qw = row0 + q - lane;   // global row of this warp's lane 0
+      const int64_t tA = tc0 + lane, tB = tc0 + 32 + lane;
+      const long long oA = tA < T ? targets[tA] - qw : -1, oB = tB < T ? targets[tB] - qw : -1;
+      uint32_t tmA = __ballot_sync(0xffffffffu, oA >= 0 && oA < 32);
+      uint32_t tmB = __ballot_sync(0xffffffffu, oB >= 0 && oB < 32);
+#pragma unroll
+      for (int b = 0; b < 5; ++b) {
+        const uint32_t bA = __ballot_sync(0xffffffffu, (oA >> b) & 1);
+        const uint32_t bB = __ballot_sync(0xffffffffu, (oB >> b) & 1);
+        tmA &= ((lane >> b) & 1) ? bA : ~bA;
+        tmB &= ((lane >> b) & 1) ? bB : ~bB;
+      }
       const bool row_ok = q < rows;
       const double h = row_ok ? H[q] : 0.0;
-      const int e_q = (row_ok ? ea[q] : 0) - 16;
-      const int64_t tq = row_ok ? row0 + q : -2;
-      const int64_t tA = tc0 + lane, tB = tc0 + 32 + lane;
-      const int ebA = tA < T ? eb[tA] : 0, ebB = tB < T ? eb[tB] : 0;
-      const int64_t tgA = tA < T ? targets[tA] : -1, tgB = tB < T ? targets[tB] : -1;
+      const double tau_h = tau * fabs(h);
+      const int e_q = (row_ok ? ea[q] : 0) - 16;   // S = v 2^(e_q + eb), eb + 64 in a byte
+      // every element of the row scales by moving the exponent field
+      const bool fast = __all_sync(0xffffffffu, e_q - 64 >= -958 && e_q + 191 <= 959);
       double *orow = out + q * ldo + tc0;
       const bool full = row_ok && pairs_ok && tc0 + 64 <= T;
-      uint64_t gmask = 0;
+      uint32_t gm[2] = {0u, 0u};
+      // two copies of the loop: the exponent-field scale (every row of the
+      // warp in range, the rule) and pow2_scale
+      auto columns = [&](auto fast_c) {
+        constexpr bool kFast = decltype(fast_c)::value;
 #pragma unroll
-      for (int c = 0; c < 64; c += 2) {
-        double o[2];
+        for (int hh = 0; hh < 2; ++hh) {
+          uint32_t ebp[8];
+          load_eb(32 * hh, ebp);
+          const uint32_t tm = hh ? tmB : tmA;
+          auto element = [&](int cl) -> double {   // column 32 hh + cl
+            const int cc = 32 * hh + cl;
+            const int e = e_q - 64 + static_cast<int>((ebp[cl >> 2] >> (8 * (cl & 3))) & 255u);
+            const double S = kFast ? pow2_scale_normal(v[cc], e) : pow2_scale(v[cc], e);
+            bool guard;
+            const double o = k7_value(S, h, tau, tau_h, (tm >> cl) & 1, guard);
+            gm[hh] |= static_cast<uint32_t>(guard) << cl;
+            return o;
+          };
+          if constexpr ((kDiag & 16) != 0) {   // the element math without the stores
+            double x = 0.0;
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int cc = c + u;
-          const int ebt = __shfl_sync(0xffffffffu, cc < 32 ? ebA : ebB, cc & 31);
-          const long long tg = __shfl_sync(0xffffffffu, static_cast<long long>(cc < 32 ? tgA : tgB),
-                                           cc & 31);
-          const double S = pow2_scale(v[cc], e_q + ebt);
-          const double val = h + S;
-          const bool is_t = tq == tg;
-          const bool guard = !is_t && fabs(val) < tau * (fabs(h) + fabs(S));
-          const double settled = settle(val);
-          o[u] = guard ? __longlong_as_double(static_cast<long long>(kOzGuard))
-                       : (is_t ? 0.0 : settled);
-          gmask |= static_cast<uint64_t>(guard && tc0 + cc < T) << cc;
+            for (int c = 0; c < 32; ++c) x += element(c);
+            if (x == 1.2345) orow[0] = x;
+            continue;
+          }
+#pragma unroll
+          for (int c = 0; c < 32; c += 2) {
+            const double o0 = element(c), o1 = element(c + 1);
+            const int cc = 32 * hh + c;
+            if (full) {
+              *reinterpret_cast<double2 *>(orow + cc) = make_double2(o0, o1);
+            } else if (row_ok) {
+              if (tc0 + cc < T) orow[cc] = o0;
+              if (tc0 + cc + 1 < T) orow[cc + 1] = o1;
+            }
+          }
         }
-        if (full) {
-          *reinterpret_cast<double2 *>(orow + c) = make_double2(o[0], o[1]);
-        } else if (row_ok) {
-          if (tc0 + c < T) orow[c] = o[0];
-          if (tc0 + c + 1 < T) orow[c + 1] = o[1];
-        }
-      }
+      };
+      if (fast)
+        columns(std::true_type{});
+      else
+        columns(std::false_type{});
+      const uint64_t gmask = gm[0] | (static_cast<uint64_t>(gm[1]) << 32);
       if (row_ok) push_guards(guard_list, guard_cap, gmask, q, tc0, T);
       if (tid == 64) PP_STAMP(k, 9);
     }
@@ -829,6 +947,8 @@ static auto pp_kernel(int diag) {
          : diag == 3  ? batched_kl_i8_pp_kernel<kS, kMaxL, 3, kTiled>
          : diag == 4  ? batched_kl_i8_pp_kernel<kS, kMaxL, 4, kTiled>
          : diag == 10 ? batched_kl_i8_pp_kernel<kS, kMaxL, 10, kTiled>
+         : diag == 20 ? batched_kl_i8_pp_kernel<kS, kMaxL, 20, kTiled>
+         : diag == 36 ? batched_kl_i8_pp_kernel<kS, kMaxL, 36, kTiled>
                       : batched_kl_i8_pp_kernel<kS, kMaxL, 0, kTiled>;
 }
 
