@@ -727,26 +727,44 @@ def extra_c5(t, nat, dev, pf, device, dk, omesh, steps, peak):
     gcap = pf.divergence.guard_list_cap(rows, T)
     glist = t.empty(gcap + 1, dtype=t.int64, device=device)
     e0.record(s)
-    A, ea, ldk = dk.slices(1e-300)          # once per P (like H)
+    At, eat = dk.slices_tiled(1e-300)       # once per P (like H); the product's layout
     e1.record(s)
     t.cuda.synchronize()
     slice_ms = e0.elapsed_time(e1)
-    B = t.empty((7, T, ldk), dtype=t.uint8, device=device)
+    Bt = t.empty(dev.i8_tiled_bytes(T, k), dtype=t.uint8, device=device)
     eb = t.empty(T, dtype=t.int32, device=device)
     bad = t.zeros(1, dtype=t.int32, device=device)
+    rowmajor = {}
 
     def batch_i8(timed=False, grade=64, pair=1):
+        # pair=1: the product path (dv_field_batch_device): CTA-pair kernel on the
+        # tiled planes; pair=0: the single-CTA kernel on row-major planes, beside it
         cnt.zero_()
         nat.call("pf_batch_prep_f64", Pt.data_ptr(), Pt.stride(0), T, k, ldl, 1e-300, 0,
                  L_.data_ptr(), Tc.data_ptr(), 0, s.cuda_stream)
-        nat.call("pf_slice_targets_u8", L_.data_ptr(), ldl, T, k, ldk, B.data_ptr(), eb.data_ptr(),
-                 bad.data_ptr(), s.cuda_stream)
+        if pair:
+            nat.call("pf_slice_targets_u8_tiled", L_.data_ptr(), ldl, T, k, Bt.data_ptr(),
+                     eb.data_ptr(), bad.data_ptr(), s.cuda_stream)
+        else:
+            if not rowmajor:
+                A, ea, ldk = dk.slices(1e-300)
+                rowmajor.update(A=A, ea=ea, ldk=ldk,
+                                B=t.empty((7, T, ldk), dtype=t.uint8, device=device))
+            rm = rowmajor
+            nat.call("pf_slice_targets_u8", L_.data_ptr(), ldl, T, k, rm["ldk"], rm["B"].data_ptr(),
+                     eb.data_ptr(), bad.data_ptr(), s.cuda_stream)
         if timed:
             e1.record(s)
         glist[:1].zero_()
-        nat.call("pf_batched_kl_i8_listed", A.data_ptr(), ea.data_ptr(), rows, B.data_ptr(),
-                 eb.data_ptr(), T, k, ldk, H.data_ptr(), tg.data_ptr(), tau, 0, out.data_ptr(),
-                 out.stride(0), grade, pair, glist.data_ptr(), gcap, s.cuda_stream)
+        if pair:
+            nat.call("pf_batched_kl_i8_tiled", At.data_ptr(), eat.data_ptr(), rows, Bt.data_ptr(),
+                     eb.data_ptr(), T, k, H.data_ptr(), tg.data_ptr(), tau, 0, out.data_ptr(),
+                     out.stride(0), grade, glist.data_ptr(), gcap, s.cuda_stream)
+        else:
+            nat.call("pf_batched_kl_i8_listed", rm["A"].data_ptr(), rm["ea"].data_ptr(), rows,
+                     rm["B"].data_ptr(), eb.data_ptr(), T, k, rm["ldk"], H.data_ptr(),
+                     tg.data_ptr(), tau, 0, out.data_ptr(), out.stride(0), grade, 0,
+                     glist.data_ptr(), gcap, s.cuda_stream)
         if timed:
             e2.record(s)
         nat.call("pf_batched_kl_fixup_list_f64", dk.P.data_ptr(), dk.ld, rows, k, Tc.data_ptr(),
@@ -784,6 +802,8 @@ def extra_c5(t, nat, dev, pf, device, dk, omesh, steps, peak):
     batch_i8(True, pair=0)                  # the single-CTA kernel beside it
     t.cuda.synchronize()
     gemm_single = e1.elapsed_time(e2)
+    rowmajor.clear()
+    dk._H.pop(("i8", 1e-300), None)         # the row-major planes only served that comparison
     guarded = int(cnt.item())
     flops = 2.0 * rows * k * T
     fl = ctypes.c_int64(0)
@@ -841,8 +861,9 @@ def extra_c5(t, nat, dev, pf, device, dk, omesh, steps, peak):
                                      "matmul), sustained (~0.3 s back to back, under the 1 kW "
                                      "power cap, as the ~0.1 s C5 GEMM runs); burst_peak is "
                                      "one launch",
-                        "kernel": "pf::batched_kl_i8_pp_kernel<7,9> (persistent tcgen05 "
-                                  "cta_group::2 pair, epilogue off the MMA critical path)"},
+                        "kernel": "pf::batched_kl_i8_pp_kernel<7,9,0,tiled> (persistent tcgen05 "
+                                  "cta_group::2 pair on the tiled planes, epilogue off the MMA "
+                                  "critical path)"},
            "fp32_grade": {"note": "same kernel, 15 byte-pair GEMMs (levels 2..6 of the top 5 "
                                   "planes): the north-star FP32 tolerance 1e-5",
                           "ms_per_batch": ms_f32grade,
@@ -851,7 +872,7 @@ def extra_c5(t, nat, dev, pf, device, dk, omesh, steps, peak):
                               "achieved_tflops": flops / (ms64 / 1e3) / 1e12,
                               "dfma_peak_tflops": dfma_tf,
                               "frac": flops / (ms64 / 1e3) / 1e12 / dfma_tf}}
-    del A, B
+    del At, Bt
     # ---- the tracer over the K7 fields, read in place: field j = column j of `out`
     for _ in range(2):   # warm-up at full size: the 2.7 GB path workspace is allocated here
         PP.trace_arrays(omesh_tri(omesh, pf), out, targets, src, fo, layout=(1, T))
