@@ -40,7 +40,7 @@ __global__ void batch_prep_kernel(const double *__restrict__ Pt, int64_t ldp, in
   for (int64_t b = threadIdx.x; b < ldl; b += blockDim.x) {
     if (b < k) {
       const double p = Pt[t * ldp + b];
-      const double c = fmax(p, clamp);
+      const double c = clamp_lo(p, clamp);
       L[t * ldl + b] = log(c);
       Tc[t * ldl + b] = c;
       if (ref) diff |= (p < clamp) != (ref[b] < clamp);
@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(kGemmThreads, 2) batched_kl_dmma2_kernel(
     for (int ks = 0; ks < kBK; ks += 4) {
       double a[4], b[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = fmax(as[8 * i * kV2S + ks], clamp);
+      for (int i = 0; i < 4; ++i) a[i] = clamp_lo(as[8 * i * kV2S + ks], clamp);
 #pragma unroll
       for (int j = 0; j < 4; ++j) b[j] = bs[8 * j * kV2S + ks];
 #pragma unroll
@@ -204,19 +204,19 @@ __device__ __forceinline__ double fixup_pair_t(const double *__restrict__ prow,
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const double qv = fmax(pv[u], clamp);
+      const double qv = clamp_lo(pv[u], clamp);
       b[u & 3] += kl_term<FAST>(qv, tv[u]);
     }
   }
   for (; c + 96 < k; c += 128) {
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const double qv = fmax(prow[c + 32 * u], clamp);
+      const double qv = clamp_lo(prow[c + 32 * u], clamp);
       b[u] += kl_term<FAST>(qv, trow[c + 32 * u]);
     }
   }
   for (; c < k; c += 32) {
-    const double qv = fmax(prow[c], clamp);
+    const double qv = clamp_lo(prow[c], clamp);
     b[0] += kl_term<FAST>(qv, trow[c]);
   }
   return settle(warp_sum((b[0] + b[1]) + (b[2] + b[3])));
@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(kFxWarps * 32, 1) batched_kl_fixup_staged_kern
       double tm[kFxChunk / 32];
 #pragma unroll
       for (int u = 0; u < kFxChunk / 32; ++u)
-        tm[u] = kl_term<true>(fmax(pc[lane + 32 * u], clamp), tcn[lane + 32 * u]);
+        tm[u] = kl_term<true>(clamp_lo(pc[lane + 32 * u], clamp), tcn[lane + 32 * u]);
 #pragma unroll
       for (int u = 0; u < kFxChunk / 32; ++u) b[u & 3] += tm[u];
     } else
@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(kFxWarps * 32, 1) batched_kl_fixup_staged_kern
         // fixup_pair_t's accumulator: u & 3 inside a full 128-element block, else 0
         const int64_t blk = base + 128 * (u >> 2);
         const int acc = (blk + lane + 96 < k) ? (u & 3) : 0;
-        const double term = kl_term<true>(fmax(pc[lane + 32 * u], clamp), tcn[lane + 32 * u]);
+        const double term = kl_term<true>(clamp_lo(pc[lane + 32 * u], clamp), tcn[lane + 32 * u]);
         if (acc == 0) b[0] += term;
         else if (acc == 1) b[1] += term;
         else if (acc == 2) b[2] += term;
