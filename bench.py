@@ -503,7 +503,6 @@ def extra_f32(t, nat, dev, pf, dk, target, steps, peak):
     """KL+TV in the FP32 storage mode (query rows from an FP32 copy; 1e-5 tolerance)."""
     rows, k = dk.rows, dk.k
     P32, ld32 = dk.fp32()
-    H32 = dk.negentropy32(1e-300)
     H64 = dk.negentropy(1e-300)
     s = t.cuda.current_stream(dk.device)
     k_pad, m_pad = dev.round_up(k, 2), dev.round_up(k, 16)
@@ -521,7 +520,7 @@ def extra_f32(t, nat, dev, pf, dk, target, steps, peak):
         nat.call("pf_target_prep_f64", rowp, k, 1e-300, tgt, logt, tmask, fl, s.cuda_stream)
         if timed:
             ev[0].record(s)
-        nat.call("pf_dense_kl_f32", P32.data_ptr(), ld32, rows, k, H32.data_ptr(), tgt, logt, tmask,
+        nat.call("pf_dense_kl_f32", P32.data_ptr(), ld32, rows, k, H64.data_ptr(), tgt, logt, tmask,
                  1e-300, tau, dk.row0, target, dk.is_interior.data_ptr(), dk.P.data_ptr(), dk.ld,
                  H64.data_ptr(), pf.divergence.KL_GUARD_TAU, out.data_ptr(), fl, s.cuda_stream)
         if timed:

@@ -146,8 +146,10 @@ int pf_dense_at_f64(const double *P, int64_t ld, int64_t rows, int64_t k,
  * pf_row_negentropy_f32: H[r] = sum c(Q32) log c(Q32) in FP64 over FP32 rows.
  * pf_dense_kl_f32 / pf_dense_tv_f32: the K2 / K3 fields with the query rows
  * read from the FP32 copy (half the bytes); target row, logs, H and all
- * accumulation FP64.  Rows whose value cannot be certified to 1e-5 against
- * the FP32 rounding bound (|KL| < tau*(|H|+|cross|+1), |TV| < tau; tau = 1e-2)
+ * accumulation FP64, H the FP64 negentropy of the FP64 rows
+ * (pf_row_negentropy_f64 of P64; the FP32 rounding then only perturbs the
+ * cross term, by at most 2^-24 |cross|).  Rows whose value cannot be
+ * certified to 1e-5 against that bound (|KL| < tau*|cross|, |TV| < tau; tau = 1e-2)
  * are re-evaluated from the FP64 rows P64 (count in flags[PF_FLAG_GUARDED]):
  * TV exactly; KL in the FP64 split form H64[r] - sum c(Q64) logt when H64
  * (pf_row_negentropy_f64 of P64) is given, falling back to the reference form

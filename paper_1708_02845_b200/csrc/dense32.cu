@@ -2,12 +2,15 @@
 //
 // Same fields as dense.cu (divergence.py:154-187), with the query rows read
 // from an FP32 copy of P; the target row, its logs, H and every accumulation
-// stay FP64.  The north-star tolerance for this mode is 1e-5 relative.  The
-// FP32 rounding of a row perturbs the result by at most
-//     |KL32 - KL64| <= eps32 * (|H| + |cross| + 1),   |TV32 - TV64| <= eps32,
-// (eps32 = 2^-24 relative per stored entry), so a row whose value is below
-// tau32 * (|H| + |cross| + 1) (KL) or tau32 (TV), tau32 = 1e-2, cannot be
-// certified to 1e-5 and is re-evaluated from the FP64 rows in place by the
+// stay FP64.  The north-star tolerance for this mode is 1e-5 relative.  H is
+// the FP64 negentropy of the FP64 rows, so the FP32 rounding only touches the
+// cross term, each c(Q) by at most eps32 = 2^-24 relative, and with every
+// log c(Pt) <= 0
+//     |KL32 - KL64| <= eps32 * sum c(Q) |log c(Pt)| = eps32 * |cross|,
+//     |TV32 - TV64| <= eps32 * (sum c(Q) + sum c(Pt)) ~ 2 eps32,
+// so a row whose value is below tau32 * |cross| (KL) or tau32 (TV), tau32 =
+// 1e-2, cannot be certified to 1e-5 and is re-evaluated from the FP64 rows in
+// place by the
 // warp that found it: TV exactly (sum |c(Q) - c(Pt)|, one streaming pass); KL
 // in the FP64 split form H64 - sum c(Q) log c(Pt) (one streaming FMA pass,
 // ~1e-13 relative), and only if THAT cancels too (the FP64 guard, tau64) in
@@ -174,7 +177,7 @@ __global__ void __launch_bounds__(kT32, MINB) dense32_kernel(
     bool guard;
     if (KL) {
       val = h - s;
-      guard = fabs(val) < tau * (fabs(h) + fabs(s) + 1.0);
+      guard = fabs(val) < tau * fabs(s);
     } else {
       val = s;
       guard = fabs(val) < tau;

@@ -338,9 +338,8 @@ def dv_field_f32_device(pk: PoissonKernel, fd: FDivergence, p: int, clamp: float
     nat.call("pf_target_prep_f64", row.data_ptr(), dk.k, c, st.tgt, st.logt, st.tmask, flags,
              s.cuda_stream)
     if _is_builtin(fd, "kl"):
-        H = dk.negentropy32(c)
-        H64 = dk.negentropy(c)   # FP64 split form for the guarded rows
-        nat.call("pf_dense_kl_f32", P32.data_ptr(), ld32, dk.rows, dk.k, H.data_ptr(), st.tgt,
+        H64 = dk.negentropy(c)   # H of the FP64 rows: the FP32 rounding only touches the cross term
+        nat.call("pf_dense_kl_f32", P32.data_ptr(), ld32, dk.rows, dk.k, H64.data_ptr(), st.tgt,
                  st.logt, st.tmask, c, F32_GUARD_TAU, dk.row0, p, dk.is_interior.data_ptr(),
                  dk.P.data_ptr(), dk.ld, H64.data_ptr(), KL_GUARD_TAU, out.data_ptr(), flags,
                  s.cuda_stream)

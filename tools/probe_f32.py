@@ -32,7 +32,7 @@ res = {}
 for name in ("kl", "tv"):
     def run():
         if name == "kl":
-            nat.call("pf_dense_kl_f32", P32.data_ptr(), ld32, rows, k, H.data_ptr(), tgt.data_ptr(),
+            nat.call("pf_dense_kl_f32", P32.data_ptr(), ld32, rows, k, H64.data_ptr(), tgt.data_ptr(),
                      logt.data_ptr(), tmask.data_ptr(), 1e-300, 1e-2, 0, target, inter.data_ptr(),
                      P.data_ptr(), ld, H64.data_ptr(), 1e-3, out.data_ptr(), flags.data_ptr(), s)
         else:
