@@ -161,13 +161,37 @@ __global__ void __launch_bounds__(kT32, MINB) dense32_kernel(
         acc32<KL, CLAMP>(v[u].w, t23.y, clamp32, a1);
       }
     }
-    for (int j = nfull + lane; j < nq; j += 32) {   // the ragged chunk
-      const float4 v = ldg_stream4f(row + j);
-      const double2 t01 = lo[j], t23 = hi[j];
-      acc32<KL, CLAMP>(v.x, t01.x, clamp32, a0);
-      acc32<KL, CLAMP>(v.y, t01.y, clamp32, a1);
-      acc32<KL, CLAMP>(v.z, t23.x, clamp32, a0);
-      acc32<KL, CLAMP>(v.w, t23.y, clamp32, a1);
+    if (nq - nfull > 32) {
+      // a ragged chunk of several float4 per lane (short rows: C2' has k =
+      // 1,310, 71 of its 327 float4 past the full chunk): all its loads in
+      // flight at once (in-row clamped addresses), then the in-range ones
+      // accumulated in the same per-lane order as the loop below
+      float4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int j = nfull + lane + 32 * u;
+        v[u] = ldg_stream4f(row + (j < nq ? j : nq - 1));
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int j = nfull + lane + 32 * u;
+        if (j < nq) {
+          const double2 t01 = lo[j], t23 = hi[j];
+          acc32<KL, CLAMP>(v[u].x, t01.x, clamp32, a0);
+          acc32<KL, CLAMP>(v[u].y, t01.y, clamp32, a1);
+          acc32<KL, CLAMP>(v[u].z, t23.x, clamp32, a0);
+          acc32<KL, CLAMP>(v[u].w, t23.y, clamp32, a1);
+        }
+      }
+    } else {
+      for (int j = nfull + lane; j < nq; j += 32) {   // the ragged chunk
+        const float4 v = ldg_stream4f(row + j);
+        const double2 t01 = lo[j], t23 = hi[j];
+        acc32<KL, CLAMP>(v.x, t01.x, clamp32, a0);
+        acc32<KL, CLAMP>(v.y, t01.y, clamp32, a1);
+        acc32<KL, CLAMP>(v.z, t23.x, clamp32, a0);
+        acc32<KL, CLAMP>(v.w, t23.y, clamp32, a1);
+      }
     }
     for (int64_t b = 4 * nq4 + lane; b < k; b += 32)  // ragged tail (< 4 columns)
       acc32<KL, CLAMP>(P[r * ld + b], tail[b - 4 * nq4], clamp32, a0);
