@@ -144,6 +144,15 @@ __device__ __forceinline__ void load_tri(const pf_mesh_t &m, int64_t ti, Tri &t)
   }
 }
 
+// Speculative prefetch into L1 of the packed records the walk may visit next
+// (a triangle's neighbours, a vertex's incident triangles): each visit then
+// starts from L1 instead of a DRAM round trip.  Loads only -- the walk's
+// arithmetic and order are untouched (bitwise the same paths).
+__device__ __forceinline__ void prefetch_rec(const pf_mesh_t &m, int64_t ti) {
+  if (m.pack && ti >= 0)
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(m.pack + 16 * ti));
+}
+
 // One field's values: vertex v at p[v * s] (s = 1: a field per row of an
 // (F, n) block; s = T: a column of the (n, T) output of the batched KL).
 struct FieldView {
@@ -234,7 +243,9 @@ __global__ void __launch_bounds__(kTraceThreads) trace_kernel(pf_mesh_t m, const
       }
       double best_norm = 0.0;
       int64_t best = -1;
-      for (int64_t e = m.vt_ptr[v]; e < m.vt_ptr[v + 1]; ++e) {
+      const int64_t e0 = m.vt_ptr[v], e1 = m.vt_ptr[v + 1];
+      for (int64_t e = e0; e < e1; ++e) prefetch_rec(m, m.vt_idx[e]);
+      for (int64_t e = e0; e < e1; ++e) {
         const int64_t tj = m.vt_idx[e];
         Tri t;
         load_tri(m, tj, t);
@@ -445,6 +456,10 @@ __global__ void __launch_bounds__(kTraceThreads) trace_kernel(pf_mesh_t m, const
       }
     }
     if (enters) {
+      // the triangle after this one is one of nt's other neighbours
+#pragma unroll
+      for (int s = 0; s < 3; ++s)
+        if (ct.nbr[s] != ti) prefetch_rec(m, ct.nbr[s]);
       carry = true;
       ti = nt;
       x0 = xe0;
