@@ -143,7 +143,8 @@ def test_batch_slabs_bitwise_and_flags_or(method):
     np.testing.assert_array_equal(fl, flags)
 
 
-@pytest.mark.parametrize("rows,k,T", [(300, 200, 50), (129, 64, 64), (2047, 1234, 256)])
+@pytest.mark.parametrize("rows,k,T", [(300, 200, 50), (129, 64, 64), (2047, 1234, 256),
+                                      (2, 5, 1), (127, 31, 3), (385, 33, 65), (640, 97, 200)])
 def test_i8_cta_pair_kernel_bitwise_equals_single_cta(rows, k, T):
     """K7 on a CTA pair (tcgen05 cta_group::2, M256 over two SMs) computes the same
     exact integer levels as the single-CTA kernel: the outputs are bitwise equal,
