@@ -723,22 +723,19 @@ __global__ void __launch_bounds__(kO2Threads, 1)
       if (lane == 0) tc::mbar_arrive_cluster(free_leader);   // TMEM free for the next tile
       if (tid == 64) PP_STAMP(k, 8);
       if constexpr ((kDiag & 2) != 0) continue;
-      // Per element ~20 ALU / FP64 instructions and no shared-memory or
-      // shuffle traffic: the tensor core's operand reads plus the TMA writes
-      // take ~95% of the SM's shared-memory bandwidth while the MMAs run, so
-      // every LDS / SHFL in this loop waits behind them (a per-element column
-      // broadcast through either cost ~1.5K clocks per element-column and made
-      // the epilogue longer than the next tile's pass 1).  Per tile instead:
-      //  * the 64 column exponents eb are loaded once (16 x 16-byte loads) and
-      //    packed as bytes eb + 64 into 16 registers;
-      //  * the columns whose target row is this lane's row form a 64-bit mask
-      //    built from ballots over the owner-lane bits (at most one row per
-      //    column);
-      //  * the scale 2^(ea + eb - 16) is three power-of-two multiplies:
-      //    v * 2^eb and then * 2^max(e_q, -900) are exact (v is 0 or within
-      //    [2^-64, 2^64], eb within [-52, 12]: -L is 0 or >= 2^-53; the
-      //    slicing flags anything outside [-64, 191] as bad), the last
-      //    multiply rounds once -- the single rounding of ldexp.
+      // The element loop runs while the next tile's pass-1 MMAs do, and FP64
+      // instructions issue ~5x slower then (PF_K7_DIAG=36 runs the loop without
+      // MMAs: 21K against 103K clocks per tile), so it keeps two FP64
+      // instructions per element (h + S and fma(tau, S, tau |h|), k7_value) and
+      // no per-element shared-memory or shuffle traffic.  Per tile:
+      //  * the 64 column exponents eb are loaded with 16-byte loads and packed
+      //    as bytes eb + 64, 32 columns (8 registers) per half of the loop;
+      //  * the columns whose target is this lane's row form a mask built from
+      //    ballots over the owner-lane bits (at most one row per column);
+      //  * S = v 2^(ea + eb - 16) moves the exponent field (exact: v is 0 or
+      //    within [2^-64, 2^64], eb within [-52, 12] -- -L is 0 or >= 2^-53,
+      //    and the slicing flags anything outside [-64, 191] as bad), rows
+      //    whose exponents could leave the normal range take pow2_scale.
       auto pack4 = [](int a, int b, int c, int d) -> uint32_t {
         return (static_cast<uint32_t>(a + 64) & 255u) | ((static_cast<uint32_t>(b + 64) & 255u) << 8) |
                ((static_cast<uint32_t>(c + 64) & 255u) << 16) | (static_cast<uint32_t>(d + 64) << 24);
