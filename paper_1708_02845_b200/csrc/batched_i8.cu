@@ -476,8 +476,10 @@ __device__ __forceinline__ uint32_t smid() {
 // out[k * 16 + i] (tools/probe_k7pp_stamps.py), bit 3 = per-stage timeline of
 // cluster 0's leader in SM clocks (%globaltimer ticks too coarsely for
 // stage-sized gaps): load issue at out[65536 + 2 s], full-barrier pass at
-// out[65536 + 2 s + 1] (tools/probe_k7stages.py).  kTiled: operands in the
-// tiled layout (SliceLayout), the default; the row-major form stays for the
+// out[65536 + 2 s + 1] (tools/probe_k7stages.py), bit 4 = the element loop
+// without its stores, bit 5 = no MMAs (commits only; with bit 2: how fast the
+// epilogue runs when the tensor pipe is idle).  kTiled: operands in the tiled
+// layout (SliceLayout), the default; the row-major form stays for the
 // pf_batched_kl_i8 ABI.
 constexpr int kP2BN = 128, kP2HalfN = 64, kP2Stages = 5;
 constexpr int kP2TileA = 128 * kO2BK;                         // 4 KB per slice
