@@ -627,9 +627,16 @@ __global__ void __launch_bounds__(kO2Threads, 1)
                 const int l = i + j;
                 if (l > 5) continue;
                 if constexpr ((kDiag & 32) != 0) continue;   // no MMAs (commits only)
-                tc::mma_i8_pair(tmem + (l - 2) * kP2BN, tc::sdesc<32>(sa + (i - 1) * kP2TileA),
-                                tc::sdesc<32>(sb + (j - 1) * kP2TileB), idesc,
-                                !(kb == 0 && i == 1));
+                // A_i serves j = 1 .. 5 - i back to back: read it once (collector)
+                const int jl = 5 - i;
+                const int coll = jl == 1 ? 0 : (j == 1 ? 1 : (j == jl ? 3 : 2));
+                const uint64_t ad = tc::sdesc<32>(sa + (i - 1) * kP2TileA);
+                const uint64_t bd = tc::sdesc<32>(sb + (j - 1) * kP2TileB);
+                const bool acc = !(kb == 0 && i == 1);
+                if (coll == 1) tc::mma_i8_pair_c<1>(tmem + (l - 2) * kP2BN, ad, bd, idesc, acc);
+                else if (coll == 2) tc::mma_i8_pair_c<2>(tmem + (l - 2) * kP2BN, ad, bd, idesc, acc);
+                else if (coll == 3) tc::mma_i8_pair_c<3>(tmem + (l - 2) * kP2BN, ad, bd, idesc, acc);
+                else tc::mma_i8_pair(tmem + (l - 2) * kP2BN, ad, bd, idesc, acc);
               }
             tc::commit_pair(&empty_bar[st]);
           }
@@ -662,9 +669,15 @@ __global__ void __launch_bounds__(kO2Threads, 1)
                 if (l < 6 || l > kMaxL) continue;
                 if constexpr ((kDiag & 32) != 0) continue;
                 const int first_i = l - kS > 1 ? l - kS : 1;
-                tc::mma_i8_pair(tmem + (l - 6) * kP2BN, tc::sdesc<32>(sa + (i - 1) * kP2TileA),
-                                tc::sdesc<32>(sb + (j - 1) * kP2TileB), idesc,
-                                !(kb == 0 && i == first_i));
+                const int jf = 6 - i > 1 ? 6 - i : 1, jl = kMaxL - i < kS ? kMaxL - i : kS;
+                const int coll = jl == jf ? 0 : (j == jf ? 1 : (j == jl ? 3 : 2));
+                const uint64_t ad = tc::sdesc<32>(sa + (i - 1) * kP2TileA);
+                const uint64_t bd = tc::sdesc<32>(sb + (j - 1) * kP2TileB);
+                const bool acc = !(kb == 0 && i == first_i);
+                if (coll == 1) tc::mma_i8_pair_c<1>(tmem + (l - 6) * kP2BN, ad, bd, idesc, acc);
+                else if (coll == 2) tc::mma_i8_pair_c<2>(tmem + (l - 6) * kP2BN, ad, bd, idesc, acc);
+                else if (coll == 3) tc::mma_i8_pair_c<3>(tmem + (l - 6) * kP2BN, ad, bd, idesc, acc);
+                else tc::mma_i8_pair(tmem + (l - 6) * kP2BN, ad, bd, idesc, acc);
               }
             tc::commit_pair(&empty_bar[st]);
           }

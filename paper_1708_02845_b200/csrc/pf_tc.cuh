@@ -140,6 +140,31 @@ __device__ __forceinline__ void mma_i8_pair(uint32_t d_tmem, uint64_t a, uint64_
       "l"(a), "l"(b), "r"(idesc), "r"(static_cast<uint32_t>(accumulate)));
 }
 
+// The same with a collector-buffer usage for A (kColl: 0 = default/discard,
+// 1 = fill, 2 = use, 3 = lastuse): consecutive MMAs on the same A operand
+// read it from shared memory once.
+template <int kColl>
+__device__ __forceinline__ void mma_i8_pair_c(uint32_t d_tmem, uint64_t a, uint64_t b,
+                                              uint32_t idesc, bool accumulate) {
+  if constexpr (kColl == 1)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::i8.collector::a::fill [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(static_cast<uint32_t>(accumulate)));
+  else if constexpr (kColl == 2)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::i8.collector::a::use [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(static_cast<uint32_t>(accumulate)));
+  else if constexpr (kColl == 3)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::i8.collector::a::lastuse [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(static_cast<uint32_t>(accumulate)));
+  else
+    mma_i8_pair(d_tmem, a, b, idesc, accumulate);
+}
+
 // Arrive once on `bar` (same offset) in both CTAs of the pair when every
 // previously issued tcgen05.mma of the pair has completed.
 __device__ __forceinline__ void commit_pair(uint64_t *bar) {
