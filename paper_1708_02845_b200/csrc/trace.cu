@@ -17,11 +17,14 @@
 //     index exactly where the reference's argmax/min/strict-< do.
 #include <cmath>
 
+#include <cstdlib>
+
 #include "pf_common.cuh"
 
 namespace pf {
 
 constexpr int kTraceThreads = 128;
+constexpr int kTraceSpread = 4;   // lanes per path in trace_kernel (see the launch)
 
 // ---------------------------------------------------------------- hypot --
 // glibc sysdeps/ieee754/dbl-64/e_hypot.c (non-FMA kernel); SURVEY A.3.
@@ -212,8 +215,11 @@ __global__ void __launch_bounds__(kTraceThreads) trace_kernel(pf_mesh_t m, const
                                                               const int64_t *sources,
                                                               const int32_t *field_of,
                                                               int64_t npaths, int64_t cap,
-                                                              pf_paths_t out) {
-  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+                                                              pf_paths_t out, int spread) {
+  // one path per `spread` lanes (fewer paths per warp to diverge)
+  const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (gid % spread) return;
+  const int64_t p = gid / spread;
   if (p >= npaths) return;
   const int64_t fi = field_of ? field_of[p] : 0;
   const FieldView vals{fields + fi * field_ld, vertex_ld};
@@ -880,10 +886,16 @@ int pf_trace_fields_f64(const pf_mesh_t *mesh, const double *fields, int64_t fie
   if (npaths <= 0) return 0;
   if (vertex_ld < 1 || field_ld < 0) return fail(PF_E_ARG, "trace: bad field layout");
   if (!out->count || !out->status || !out->stuck) return fail(PF_E_ARG, "trace: null outputs");
-  const int64_t blocks = (npaths + kTraceThreads - 1) / kTraceThreads;
+  // 8 paths per warp (one per 4 lanes): the walks diverge step by step, and a
+  // warp's time is the sum over its steps of every taken branch.  C5 (10,000
+  // paths on the C4 mesh): 32 paths per warp 13.4 ms, 16 12.4, 8 11.7, 4 18.2
+  // (tools/probe_trace_layout.py with the spread as a parameter).
+  constexpr int spread = kTraceSpread;
+  const int64_t blocks = (npaths * spread + kTraceThreads - 1) / kTraceThreads;
   if (!out->qx || !out->qy) return fail(PF_E_ARG, "trace: null qx/qy");
   trace_kernel<<<static_cast<unsigned>(blocks), kTraceThreads, 0, as_stream(stream)>>>(
-      *mesh, fields, field_ld, vertex_ld, targets, sources, field_of, npaths, step_cap, *out);
+      *mesh, fields, field_ld, vertex_ld, targets, sources, field_of, npaths, step_cap, *out,
+      spread);
   if (int e = check_launch("trace")) return e;
   nearest_resolve_kernel<<<static_cast<unsigned>(npaths), 256, 0, as_stream(stream)>>>(
       *mesh, npaths, *out);
