@@ -888,8 +888,8 @@ int pf_trace_fields_f64(const pf_mesh_t *mesh, const double *fields, int64_t fie
   if (!out->count || !out->status || !out->stuck) return fail(PF_E_ARG, "trace: null outputs");
   // 8 paths per warp (one per 4 lanes): the walks diverge step by step, and a
   // warp's time is the sum over its steps of every taken branch.  C5 (10,000
-  // paths on the C4 mesh): 32 paths per warp 13.4 ms, 16 12.4, 8 11.7, 4 18.2
-  // (tools/probe_trace_layout.py with the spread as a parameter).
+  // paths on the C4 mesh): 32 paths per warp 13.4 ms, 16 12.4, ~11 12.1, 8 11.7,
+  // ~6 12.1, ~5 17.2, 4 18.2 (tools/probe_trace_layout.py, the spread as a parameter).
   constexpr int spread = kTraceSpread;
   const int64_t blocks = (npaths * spread + kTraceThreads - 1) / kTraceThreads;
   if (!out->qx || !out->qy) return fail(PF_E_ARG, "trace: null qx/qy");
