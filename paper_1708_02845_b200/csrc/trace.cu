@@ -156,6 +156,17 @@ __device__ __forceinline__ void prefetch_rec(const pf_mesh_t &m, int64_t ti) {
     asm volatile("prefetch.global.L1 [%0];" ::"l"(m.pack + 16 * ti));
 }
 
+// a[i] for a 3-element array and a runtime i, as selects: a dynamic index
+// would put the array in local memory, an L1 round trip inside the walk's
+// serial chain (same values either way)
+template <class T>
+__device__ __forceinline__ T sel3(int i, const T (&a)[3]) {
+  return i == 0 ? a[0] : (i == 1 ? a[1] : a[2]);
+}
+__device__ __forceinline__ double sel3xy(int i, const double (&xy)[3][2], int c) {
+  return i == 0 ? xy[0][c] : (i == 1 ? xy[1][c] : xy[2][c]);
+}
+
 // One field's values: vertex v at p[v * s] (s = 1: a field per row of an
 // (F, n) block; s = T: a column of the (n, T) output of the batched KL).
 struct FieldView {
@@ -265,7 +276,7 @@ __global__ void __launch_bounds__(kTraceThreads) trace_kernel(pf_mesh_t m, const
         const double scale = dlam_of(t, d, dl);
         const int o0 = slot == 0 ? 1 : 0, o1 = slot == 2 ? 1 : 2;
         const double thr = __dmul_rn(1e-12, scale);
-        if (dl[o0] > thr && dl[o1] > thr) {
+        if (sel3(o0, dl) > thr && sel3(o1, dl) > thr) {
           if (best < 0 || norm > best_norm) {
             best_norm = norm;
             best = tj;
@@ -371,14 +382,14 @@ __global__ void __launch_bounds__(kTraceThreads) trace_kernel(pf_mesh_t m, const
       int sb = 0;
 #pragma unroll
       for (int s = 1; s < 3; ++s)
-        if (t.f[s] < t.f[sb] || (t.f[s] == t.f[sb] && t.v[s] < t.v[sb])) sb = s;
-      const int64_t bw = t.v[sb];
-      if (t.f[sb] >= cur) {
+        if (t.f[s] < sel3(sb, t.f) || (t.f[s] == sel3(sb, t.f) && t.v[s] < sel3(sb, t.v))) sb = s;
+      const int64_t bw = sel3(sb, t.v);
+      if (sel3(sb, t.f) >= cur) {
         status = ST_STUCK;
         stuck = bw;
         break;
       }
-      w.put(0, bw, -1, 0.0, t.xy[sb][0], t.xy[sb][1]);
+      w.put(0, bw, -1, 0.0, sel3xy(sb, t.xy, 0), sel3xy(sb, t.xy, 1));
       in_tri = false;
       v = bw;
       continue;
@@ -386,19 +397,28 @@ __global__ void __launch_bounds__(kTraceThreads) trace_kernel(pf_mesh_t m, const
     double le[3];
 #pragma unroll
     for (int s = 0; s < 3; ++s) le[s] = __dadd_rn(lam[s], __dmul_rn(s_exit, dl[s]));
-    le[slot_exit] = 0.0;
+#pragma unroll
+    for (int s = 0; s < 3; ++s)
+      if (s == slot_exit) le[s] = 0.0;
 #pragma unroll
     for (int s = 0; s < 3; ++s) le[s] = le[s] < 0.0 ? 0.0 : le[s];
     const double lsum = __dadd_rn(__dadd_rn(le[0], le[1]), le[2]);
 #pragma unroll
     for (int s = 0; s < 3; ++s) le[s] = __ddiv_rn(le[s], lsum);
     int hi = 0;
-    if (le[1] > le[hi]) hi = 1;
-    if (le[2] > le[hi]) hi = 2;
-    if (le[hi] > 1.0 - 1e-12) {
+    double lhi = le[0];
+    if (le[1] > lhi) {
+      hi = 1;
+      lhi = le[1];
+    }
+    if (le[2] > lhi) {
+      hi = 2;
+      lhi = le[2];
+    }
+    if (lhi > 1.0 - 1e-12) {
       // exit through a vertex
-      const int64_t wv = t.v[hi];
-      const double wx = t.xy[hi][0], wy = t.xy[hi][1];
+      const int64_t wv = sel3(hi, t.v);
+      const double wx = sel3xy(hi, t.xy, 0), wy = sel3xy(hi, t.xy, 1);
       if (!(np_hypot(__dsub_rn(wx, w.lx), __dsub_rn(wy, w.ly)) >= eps_prog)) {
         status = ST_STUCK;
         stuck = kNearestPending;  // resolved by nearest_resolve_kernel
@@ -412,7 +432,7 @@ __global__ void __launch_bounds__(kTraceThreads) trace_kernel(pf_mesh_t m, const
       continue;
     }
     int o0 = slot_exit == 0 ? 1 : 0, o1 = slot_exit == 2 ? 1 : 2;
-    int64_t ei = t.v[o0], ej = t.v[o1];
+    int64_t ei = sel3(o0, t.v), ej = sel3(o1, t.v);
     if (ei > ej) {
       const int64_t tmp = ei;
       ei = ej;
@@ -421,7 +441,7 @@ __global__ void __launch_bounds__(kTraceThreads) trace_kernel(pf_mesh_t m, const
       o0 = o1;
       o1 = to;
     }
-    const double tpar = le[o1];
+    const double tpar = sel3(o1, le);
     // lam_exit @ V[tri]  (3,)@(3,2)
     const double xe0 = __fma_rn(le[2], t.xy[2][0],
                                 __fma_rn(le[1], t.xy[1][0], __dmul_rn(le[0], t.xy[0][0])));
@@ -442,7 +462,7 @@ __global__ void __launch_bounds__(kTraceThreads) trace_kernel(pf_mesh_t m, const
       status = ST_REACHED;
       break;
     }
-    const int64_t nt = t.nbr[slot_exit];
+    const int64_t nt = sel3(slot_exit, t.nbr);
     bool enters = false;
     if (nt >= 0) {
       // _enters (paths.py:256-266); on success its geometry carries into the
@@ -458,7 +478,7 @@ __global__ void __launch_bounds__(kTraceThreads) trace_kernel(pf_mesh_t m, const
         for (int s = 0; s < 3; ++s)
           if (ct.v[s] != ei && ct.v[s] != ej) so = s;
         cscale = dlam_of(ct, cd, cdl);
-        enters = cdl[so] > __dmul_rn(1e-12, cscale);
+        enters = sel3(so, cdl) > __dmul_rn(1e-12, cscale);
       }
     }
     if (enters) {
@@ -476,16 +496,16 @@ __global__ void __launch_bounds__(kTraceThreads) trace_kernel(pf_mesh_t m, const
     // _slide_along_edge (paths.py:268-274); stuck-vertex reference point is
     // the entry point for a boundary edge, the exit point otherwise.
     const double rx = nt < 0 ? x0 : xe0, ry = nt < 0 ? x1 : xe1;
-    const int ssw = (t.f[o1] < t.f[o0]) ? o1 : o0;  // vals[ej] < vals[ei] ? ej : ei
-    const int64_t sw = t.v[ssw];
-    if (t.f[ssw] >= val_exit) {
+    const int ssw = (sel3(o1, t.f) < sel3(o0, t.f)) ? o1 : o0;  // vals[ej] < vals[ei] ? ej : ei
+    const int64_t sw = sel3(ssw, t.v);
+    if (sel3(ssw, t.f) >= val_exit) {
       status = ST_STUCK;
       stuck = kNearestPending;
       qx = rx;
       qy = ry;
       break;
     }
-    w.put(0, sw, -1, 0.0, t.xy[ssw][0], t.xy[ssw][1]);
+    w.put(0, sw, -1, 0.0, sel3xy(ssw, t.xy, 0), sel3xy(ssw, t.xy, 1));
     in_tri = false;
     v = sw;
   }
